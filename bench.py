@@ -1,0 +1,357 @@
+"""Benchmark: batched SuCo k-NN queries/sec on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+
+One step = one pass of the hot path over one batch: all Q queries of the
+config (10,000 at cfg2) through centroid distances -> Dynamic Activation ->
+SC counting -> top-m select -> exact re-rank -> top-k, with the dataset,
+index and queries resident in HBM (`value`), and again end to end through the
+C-ABI with pinned host buffers (`e2e`: H2D queries + D2H ids/distances inside
+the timed region). Timing: CUDA events on the stream the library launches on,
+W untimed warm-up steps, an L2 flush (256 MiB write, outside the events)
+between timed steps, max over ranks. Multi-GPU: N independent replicas (the
+sharded protocol is not wired into bench yet), scaling "weak".
+
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref/libsuco_ref.so, built from /root/reference sources) on this
+host's cores for the same config/metric: each step = a bounded sample of the
+queries through run_suco_batch-style knn_query (suco_cli.cpp:95-114).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import bench_data  # noqa: E402
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def run_reference_arm(args, cfg):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle.oracle import ref, ref_available
+    if not ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libsuco_ref.so not built"}))
+        return
+    R = ref()
+    base, queries = bench_data.generate(cfg)
+    threads = R.hardware_threads()
+    t0 = time.time()
+    idx = R.build_index(base, cfg.num_subspaces, cfg.k_half, cfg.iterations, 42, 0, 0)
+    build_s = time.time() - t0
+    sample = args.ref_sample
+    rng = np.random.default_rng(7)
+    times = []
+    for step in range(args.warmup + args.steps):
+        sel = np.sort(rng.choice(len(queries), size=min(sample, len(queries)), replace=False))
+        _, _, wall = idx.knn_query_batch(base, queries[sel], cfg.alpha, cfg.beta, cfg.k, threads=0)
+        if step >= args.warmup:
+            times.append(wall)
+    qps = sample * len(times) / sum(times)
+    line = {
+        "impl": "reference", "metric": "batched queries/sec at k=10 (oracle-exact IDs)", "value": qps,
+        "unit": "queries/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * sum(times) / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Gaussian mixture, bench_data.py)",
+        "config": {"workload": cfg.describe(), "queries_per_step": sample, "build_s": build_s},
+        "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": threads, "kind": "reference",
+                         "sample": f"{sample} random queries of {cfg.name} per step, run_suco_batch-style "
+                                   f"parallel_chunks over {threads} threads; index build {build_s:.1f} s"},
+        "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg2", choices=sorted(bench_data.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--index-source", default="gpu", choices=["gpu", "reference"],
+                    help="gpu: suco_gpu_build_index (timed); reference: load the reference CPU build's bytes")
+    ap.add_argument("--ref-sample", type=int, default=256, help="queries per step in the reference arm")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline query time (rank 0)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-only", action="store_true", help="no L2 flush/e2e/cpu legs (for ncu)")
+    args = ap.parse_args()
+    cfg = bench_data.CONFIGS[args.config]
+
+    if args.impl == "reference":
+        run_reference_arm(args, cfg)
+        return
+
+    import torch
+    import paper_2411_14754_b200 as suco
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    t0 = time.time()
+    base, queries = bench_data.generate(cfg)
+    log(f"[rank {rank}] data {cfg.describe()} generated in {time.time() - t0:.1f}s")
+    params = suco.IndexParams(cfg.num_subspaces, cfg.k_half, cfg.iterations, 42, suco.SubspaceMode.Contiguous)
+    cp = suco.CollisionParams(cfg.alpha, cfg.beta, cfg.k)
+    nq, d, k = len(queries), cfg.d, cfg.k
+
+    ref_idx = None
+    ref_build_s = None
+    build_s = None
+    if args.index_source == "reference":
+        from oracle.oracle import ref
+        R = ref()
+        t0 = time.time()
+        ref_idx = R.build_index(base, cfg.num_subspaces, cfg.k_half, cfg.iterations, 42, 0, 0)
+        ref_build_s = time.time() - t0
+        idx = suco.load_index(ref_idx.serialize(), base, device=local)
+    else:
+        torch.cuda.synchronize()
+        t0 = time.time()
+        idx = suco.build_index(base, params, device=local)
+        torch.cuda.synchronize()
+        build_s = time.time() - t0
+    log(f"[rank {rank}] index ready (gpu build {build_s}, reference build {ref_build_s})")
+
+    stream = torch.cuda.Stream()
+    idx.set_stream(stream.cuda_stream)
+    dq = torch.from_numpy(queries).cuda()
+    dids = torch.empty((nq, k), dtype=torch.int32, device="cuda")
+    dd = torch.empty((nq, k), dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def step():
+        idx.knn_query_batch_device(dq.data_ptr(), nq, d, cp, dids.data_ptr(), dd.data_ptr(), stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        step()
+    stream.synchronize()
+
+    idx.set_profiling(True)
+    step_ms, stage_ms = [], np.zeros(3)
+    stats = None
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            if not args.profile_only:
+                with torch.cuda.stream(stream):
+                    flush.fill_(1)
+            if ws > 1:
+                torch.distributed.barrier()
+            stream.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            ms, cum, sq, m = idx.stage_times()
+            stage_ms += ms
+            stats = (cum, sq, m)
+    idx.set_profiling(False)
+    total_ms = sum(step_ms)
+    if ws > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = ws * nq * args.steps / (total_ms / 1000.0)
+    gpu_ids = dids.cpu().numpy().view(np.uint32).copy()
+    gpu_d = dd.cpu().numpy().copy()
+
+    # end to end through the C-ABI host entry: pinned host queries in, ids/distances out
+    e2e = None
+    if not args.profile_only:
+        hq = torch.from_numpy(queries).pin_memory()
+        hi = torch.empty((nq, k), dtype=torch.int32).pin_memory()
+        hd = torch.empty((nq, k), dtype=torch.float64).pin_memory()
+        import ctypes as C
+        from paper_2411_14754_b200 import _capi
+        cpc = cp._c()
+
+        def host_step():
+            rc = _capi.knn_query_batch(idx.handle, C.cast(hq.data_ptr(), _capi.f32p), nq, d, C.byref(cpc),
+                                       C.cast(hi.data_ptr(), _capi.u32p), C.cast(hd.data_ptr(), _capi.f64p))
+            if rc:
+                raise RuntimeError(_capi.last_error().decode())
+
+        host_step()
+        e2e_ms = []
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(1)
+            stream.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            host_step()
+            e1.record(stream)
+            e1.synchronize()
+            e2e_ms.append(e0.elapsed_time(e1))
+        tot = sum(e2e_ms)
+        if ws > 1:
+            t = torch.tensor([tot], dtype=torch.float64, device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            tot = float(t.item())
+        e2e = {"value": ws * nq * args.steps / (tot / 1000.0), "unit": "queries/s",
+               "h2d_bytes_per_step": nq * d * 4, "d2h_bytes_per_step": nq * k * (4 + 8),
+               "ms_per_step": tot / args.steps}
+        assert np.array_equal(hi.numpy().view(np.uint32), gpu_ids) and np.array_equal(hd.numpy(), gpu_d)
+
+    # roofline of the dominant kernel (SURVEY §8(d) algorithmic bytes)
+    peak, peak_src = measured_peaks()
+    cum, sq, m = stats
+    stage_avg = stage_ms / args.steps
+    bytes_select = 4.0 * cum                      # u32 inverted-list ids streamed (query.cpp:235-239)
+    bytes_rerank = 4.0 * d * m * sq + 4.0 * d * sq  # candidate rows + query (query.cpp:177-182)
+    names = ["traverse", "select", "rerank"]
+    per_kernel = {}
+    for i, (nm, b) in enumerate(zip(names, [None, bytes_select, bytes_rerank])):
+        per_kernel[nm] = {"ms": stage_avg[i], "algorithmic_bytes": b,
+                          "achieved_gbs": (b / (stage_avg[i] / 1000.0) / 1e9) if b else None}
+    dom = int(np.argmax(stage_avg))
+    dom_name = names[dom]
+    dom_bytes = [bytes_select, bytes_select, bytes_rerank][dom] if dom else bytes_select
+    achieved = dom_bytes / (stage_avg[dom] / 1000.0) / 1e9
+    path_bytes = bytes_select + bytes_rerank
+    roofline = {"bound": "hbm", "kernel": dom_name if dom else "traverse (bytes of select shown)",
+                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                "peak_source": peak_src,
+                "query_path": {"bytes_per_step": path_bytes, "achieved": path_bytes / (total_ms / ws / args.steps / 1e3) / 1e9,
+                               "frac": path_bytes / (total_ms / ws / args.steps / 1e3) / 1e9 / peak},
+                "per_kernel": per_kernel}
+
+    # CPU baseline (rank 0, N = 1): the reference itself on a bounded sample of the same queries
+    cpu = None
+    parity = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.profile_only:
+        try:
+            from oracle.oracle import ref, ref_available
+            if ref_available():
+                R = ref()
+                if ref_idx is None:
+                    t0 = time.time()
+                    ref_idx = R.build_index(base, cfg.num_subspaces, cfg.k_half, cfg.iterations, 42, 0, 0)
+                    ref_build_s = time.time() - t0
+                threads = R.hardware_threads()
+                probe = min(nq, 200)
+                _, _, w = ref_idx.knn_query_batch(base, queries[:probe], cfg.alpha, cfg.beta, k, threads=0)
+                sample = int(min(nq, max(probe, args.cpu_seconds * probe / max(w, 1e-6))))
+                sel = np.arange(sample)
+                ri, rd, wall = ref_idx.knn_query_batch(base, queries[sel], cfg.alpha, cfg.beta, k, threads=0)
+                cpu = {"value": sample / wall, "unit": "queries/s", "cores": threads, "kind": "reference",
+                       "sample": f"first {sample} of {nq} {cfg.name} queries through the reference knn_query "
+                                 f"(run_suco_batch parallel_chunks, {threads} threads); reference build_index "
+                                 f"{ref_build_s:.1f} s", "build_s": ref_build_s}
+                parity = {"checked_queries": sample, "ids_equal": bool(np.array_equal(ri, gpu_ids[sel])),
+                          "dists_equal": bool(np.array_equal(rd, gpu_d[sel]))}
+                if args.index_source == "gpu":
+                    parity["index_bytes_equal"] = idx.serialize() == ref_idx.serialize()
+        except Exception as e:  # the baseline must not mask the GPU number
+            cpu = {"error": repr(e)}
+
+    launches_per_step = 3 + (1 if k > 32 else 0)
+    line = {
+        "metric": "batched queries/sec at k=10 (oracle-exact IDs)", "value": value, "unit": "queries/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded Gaussian mixture, bench_data.py; stands in for SIFT1M-shape corpus)",
+        "config": {"workload": cfg.describe(), "queries_per_step": nq, "index_build_s": build_s,
+                   "index_source": args.index_source, "l2": "256 MiB flush write between timed steps",
+                   "parallelism": f"replicas x{ws}"},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "parity": parity,
+        "gpu_launches": launches_per_step * args.steps, "clocks": clocks.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

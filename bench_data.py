@@ -1,0 +1,80 @@
+"""Seeded synthetic inputs for the five BASELINE.json configs (benchmark input prep only).
+
+The reference measures on real corpora that are not in this container
+(SIFT/GIST/Deep); per SURVEY §8(d) seeded Gaussian mixtures
+with each config's shape, value range and spread stand in for them. This is
+NOT the reference generator (that one is a single mt19937_64 stream, too slow
+for 10^7-10^8 points); it is a chunked numpy PCG64 mixture with the same
+recipe: component means U[lo, hi]^d, isotropic sigma, optional u8
+quantisation (round + clip to 0..255) or L2 normalisation, n + Q points drawn
+from one mixture, Q of them held out (seeded, without replacement) as
+queries, base and queries both in ascending original-id order (io.cpp:212-252).
+Both the GPU path and the reference CPU path consume the same arrays.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Tuple
+
+import numpy as np
+
+
+@dataclass(frozen=True)
+class Config:
+    name: str
+    n: int
+    d: int
+    clusters: int
+    lo: float
+    hi: float
+    sigma: float
+    quantize: bool
+    normalize: bool
+    queries: int
+    num_subspaces: int
+    k_half: int
+    alpha: float
+    beta: float
+    k: int
+    seed: int
+    iterations: int = 10
+    train_sample: float = 1.0  # cfg5: k-means trained on a 1% sample
+
+    def describe(self) -> str:
+        kind = "u8-valued" if self.quantize else ("unit-norm" if self.normalize else "float32")
+        return (f"{self.name}: n={self.n:,} d={self.d} {kind} {self.clusters}-component mixture, "
+                f"{self.queries:,} queries, N_s={self.num_subspaces}, {self.k_half}x{self.k_half} centroids, "
+                f"alpha={self.alpha} beta={self.beta} k={self.k}")
+
+
+CONFIGS = {
+    "cfg1": Config("cfg1", 100_000, 128, 100, 0.0, 100.0, 10.0, False, False, 1_000, 8, 50, 0.05, 0.005, 10, 1001),
+    "cfg2": Config("cfg2", 1_000_000, 128, 1000, 20.0, 140.0, 18.0, True, False, 10_000, 8, 50, 0.05, 0.005, 10, 1002),
+    "cfg3": Config("cfg3", 1_000_000, 960, 1000, 0.0, 1.0, 0.05, False, False, 1_000, 16, 50, 0.05, 0.01, 10, 1003),
+    "cfg4": Config("cfg4", 10_000_000, 96, 10_000, -1.0, 1.0, 0.2, False, True, 10_000, 8, 64, 0.03, 0.005, 10, 1004),
+    "cfg5": Config("cfg5", 100_000_000, 128, 100_000, 20.0, 140.0, 18.0, True, False, 10_000, 8, 100, 0.02, 0.002,
+                   10, 1005, train_sample=0.01),
+}
+
+
+def generate(cfg: Config, n: int | None = None, queries: int | None = None,
+             chunk: int = 1 << 17) -> Tuple[np.ndarray, np.ndarray]:
+    """(base n x d float32, queries Q x d float32) for `cfg` (optionally resized for tests)."""
+    n = cfg.n if n is None else n
+    nq = cfg.queries if queries is None else queries
+    total = n + nq
+    rng = np.random.default_rng(cfg.seed)
+    centers = rng.uniform(cfg.lo, cfg.hi, size=(cfg.clusters, cfg.d))
+    labels = rng.integers(0, cfg.clusters, size=total)
+    out = np.empty((total, cfg.d), np.float32)
+    for lo in range(0, total, chunk):
+        hi = min(total, lo + chunk)
+        v = centers[labels[lo:hi]] + cfg.sigma * rng.standard_normal((hi - lo, cfg.d))
+        if cfg.quantize:
+            np.clip(np.rint(v, out=v), 0.0, 255.0, out=v)
+        if cfg.normalize:
+            v /= np.sqrt(np.einsum("ij,ij->i", v, v))[:, None]
+        out[lo:hi] = v
+    held = np.zeros(total, bool)
+    held[rng.choice(total, size=nq, replace=False)] = True
+    return np.ascontiguousarray(out[~held]), np.ascontiguousarray(out[held])

@@ -1,0 +1,175 @@
+/*
+ * suco_b200.h — the drop-in C-ABI boundary of the B200-native SuCo hot path.
+ *
+ * Plain C, plain pointers and sizes, no exceptions and no torch types. Every
+ * entry point names the reference interface (/root/reference/proj) it
+ * replaces; INTEGRATION.md shows the binding a maintainer adds on the
+ * reference side. The C++ mirror of the reference API (typed exceptions,
+ * suco::gpu namespace) is include/suco_b200.hpp; the Python mirror is the
+ * paper_2411_14754_b200 package. All compute runs on the GPU: there is no
+ * CPU fallback — without a usable CUDA device every compute call returns
+ * SUCO_ERR_INTERNAL with a message.
+ *
+ * Status codes mirror the reference's exception taxonomy (error.hpp:9-37)
+ * and the CLI exit codes (suco_cli.cpp:693-707):
+ */
+#ifndef SUCO_B200_H
+#define SUCO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SUCO_OK 0
+#define SUCO_ERR_INTERNAL 1      /* suco::Error / CUDA / NCCL failure          */
+#define SUCO_ERR_CONFIG 2        /* suco::ConfigError                          */
+#define SUCO_ERR_FORMAT 3        /* suco::FormatError / CorruptIndexError      */
+#define SUCO_ERR_INCOMPATIBLE 4  /* suco::IncompatibilityError                 */
+#define SUCO_ERR_CONTRACT 5      /* suco::ContractError                        */
+
+/* IndexParams (index.hpp:53-61). mode: 0 Contiguous, 1 Shuffled (subspace.hpp:13-16). */
+typedef struct suco_index_params {
+    uint32_t num_subspaces; /* default 8  */
+    uint32_t k_half;        /* default 50 */
+    uint32_t iterations;    /* default 10 */
+    uint32_t mode;          /* default 0  */
+    uint64_t seed;          /* default 42 */
+} suco_index_params;
+
+/* CollisionParams (sc_linear.hpp:22-31). */
+typedef struct suco_collision_params {
+    double alpha; /* default 0.05  */
+    double beta;  /* default 0.005 */
+    uint32_t k;   /* default 50    */
+} suco_collision_params;
+
+/* Opaque device-resident index: layout, centroids, IMI and the dataset rows
+ * (the reference index holds no dataset, index.hpp:63-66; the GPU index must
+ * own device copies of the rows it re-ranks). Immutable after build/load;
+ * concurrent queries need distinct streams (see suco_gpu_set_stream). */
+typedef struct suco_gpu_index suco_gpu_index;
+
+/* Message of the last failing call on this thread. */
+const char* suco_last_error(void);
+
+/* Number of visible CUDA devices (0 on a CPU-only host). */
+int suco_gpu_device_count(int* count);
+
+/* ---------------------------------------------------------------- params
+ * collision_count (sc_linear.hpp:36, sc_linear.cpp:39-42),
+ * candidate_count (sc_linear.hpp:40, sc_linear.cpp:44-47),
+ * CollisionParams::validate (sc_linear.hpp:30, sc_linear.cpp:26-37). Host
+ * arithmetic, bit-identical to the reference's snapping rule. */
+uint64_t suco_collision_count(double alpha, uint64_t n);
+uint64_t suco_candidate_count(double beta, uint64_t n, uint64_t k);
+int suco_validate_collision_params(const suco_collision_params* p, uint64_t n);
+
+/* ----------------------------------------------------------------- build
+ * build_index (index.hpp:85, index.cpp:98-145) on `device`. Checks the
+ * Dataset invariants (core.cpp:8-21 -> CONTRACT) then the reference's order:
+ * k_half/iterations/n<k_half -> CONFIG, n > 2^32-1 -> CONTRACT, layout ->
+ * CONFIG. Output is identical to the reference's build for the same input. */
+int suco_gpu_build_index(const float* data, uint64_t n, uint32_t d, const suco_index_params* params,
+                         int device, suco_gpu_index** out);
+
+/* deserialize_index (index.hpp:107, index.cpp:191-293) + check_compatible
+ * (index.hpp:108, index.cpp:295-305): uploads a serialized `.suco` index and
+ * the dataset it was built from. Corrupt bytes -> FORMAT naming the section;
+ * (n, d) mismatch -> INCOMPATIBLE. */
+int suco_gpu_load_index(const unsigned char* bytes, uint64_t len, const float* data, uint64_t n, uint32_t d,
+                        int device, suco_gpu_index** out);
+
+/* serialize_index (index.hpp:99, index.cpp:147-170): byte-identical to the
+ * reference's serialization of the same index. Two-call protocol: with
+ * buf == NULL only *len is written. */
+int suco_gpu_serialize_index(const suco_gpu_index* index, unsigned char* buf, uint64_t cap, uint64_t* len);
+
+/* Host copies of one subspace's codebook (SubspaceCodebook, index.hpp:44-50):
+ * centroids_first k_half x h1, centroids_second k_half x h2, IMI offsets
+ * (k_half^2 + 1, u64) and ids (n, u32). Any pointer may be NULL. */
+int suco_gpu_index_subspace(const suco_gpu_index* index, uint32_t subspace, float* centroids_first,
+                            float* centroids_second, uint64_t* imi_offsets, uint32_t* imi_ids);
+
+/* n, d, params and the per-subspace layout (SubspaceLayout, subspace.hpp:27-50):
+ * dims (d entries, concatenated in subspace order), sizes (N_s), half_split (N_s).
+ * Layout pointers may be NULL. */
+int suco_gpu_index_info(const suco_gpu_index* index, uint64_t* n, uint32_t* d, suco_index_params* params,
+                        uint32_t* dims, uint32_t* sizes, uint32_t* half_split);
+
+void suco_gpu_free_index(suco_gpu_index* index);
+
+/* ----------------------------------------------------------------- query
+ * knn_query (query.hpp:93-96, query.cpp:199-262) over a batch of queries, the
+ * way run_suco_batch (suco_cli.cpp:95-114) drives it: results[q] =
+ * knn_query(index, dataset, queries[q], params). Check order per the
+ * reference: query length != d -> CONTRACT, params -> CONFIG. Outputs are
+ * nq x k: ids ascending by (distance, id), distances = sqrt of the fp64
+ * squared distance, bit-identical to the reference. Host buffers. */
+int suco_gpu_knn_query_batch(suco_gpu_index* index, const float* queries, uint64_t nq, uint32_t qlen,
+                             const suco_collision_params* params, uint32_t* ids, double* dists);
+
+/* Same, with device-resident queries/outputs, enqueued on `stream`
+ * (cudaStream_t; NULL = the index's stream). Returns once enqueued. */
+int suco_gpu_knn_query_batch_device(suco_gpu_index* index, const float* d_queries, uint64_t nq, uint32_t qlen,
+                                    const suco_collision_params* params, uint32_t* d_ids, double* d_dists,
+                                    void* stream);
+
+/* Stream used by later calls on this index (cudaStream_t; NULL restores the
+ * index's own stream). */
+int suco_gpu_set_stream(suco_gpu_index* index, void* stream);
+int suco_gpu_synchronize(suco_gpu_index* index);
+
+/* Stage profiling: when enabled, every query call records CUDA events around
+ * each kernel on the launching stream; suco_gpu_stage_times then returns the
+ * summed device milliseconds of the last call per stage (0 traverse, 1 select,
+ * 2 rerank) and the algorithmic work counters of that call: stats[0] = sum
+ * over queries and subspaces of the retrieved ids (the final cumulative of
+ * every traversal, query.cpp:105-106), stats[1] = queries, stats[2] = m. */
+int suco_gpu_set_profiling(suco_gpu_index* index, int enabled);
+int suco_gpu_stage_times(suco_gpu_index* index, double* ms /*3*/, uint64_t* stats /*3*/);
+
+/* Per-query intermediates of knn_query for parity checks: SC-scores (n u32,
+ * query.cpp:235-239), the top-m candidate set sorted ascending (m u32,
+ * query.cpp:242-260), per-subspace retrieved-cell counts and final cumulative
+ * (query.cpp:229-233). scores / cells / cumulative may be NULL. */
+int suco_gpu_query_intermediates(suco_gpu_index* index, const float* query, uint32_t qlen,
+                                 const suco_collision_params* params, uint32_t* scores, uint32_t* cands,
+                                 uint64_t* m, uint32_t* cells_per_subspace, uint64_t* cumulative);
+
+/* ------------------------------------------------ stage-level entry points
+ * Each runs the device kernel of one stage on host inputs (parity tests of
+ * the reference's free functions). */
+
+/* centroid_distances (query.hpp:27-28, query.cpp:42-64). */
+int suco_gpu_centroid_distances(const float* half_query, uint32_t dim, const float* centroids, uint32_t k_half,
+                                double* dists, uint32_t* order);
+
+/* dynamic_activation (query.hpp:57-58, query.cpp:66-121) over an IMI given
+ * by its CSR offsets (k_half^2 + 1). Writes up to `cap` cells (c1, c2,
+ * cumulative, sum_dist) in retrieval order; *count = cells retrieved. */
+int suco_gpu_dynamic_activation(double alpha, uint64_t n, const double* dists1, const uint32_t* order1,
+                                const double* dists2, const uint32_t* order2, uint32_t k_half,
+                                const uint64_t* imi_offsets, uint32_t* c1, uint32_t* c2, uint64_t* cumulative,
+                                double* sum_dist, uint64_t cap, uint64_t* count);
+
+/* rerank (query.hpp:83-84, query.cpp:159-197). */
+int suco_gpu_rerank(const float* data, uint64_t n, uint32_t d, const float* query, uint32_t qlen,
+                    const uint32_t* candidates, uint64_t m, uint32_t k, uint32_t* ids, double* dists);
+
+/* kmeans (kmeans.hpp:46-48, kmeans.cpp:118-194): centroids k x dim,
+ * assignments n, repaired cluster ids (<= k * iterations entries). */
+int suco_gpu_kmeans(const float* points, uint64_t n, uint32_t dim, uint32_t k, uint32_t iterations,
+                    uint64_t seed, int device, float* centroids, uint32_t* assignments, uint32_t* repaired,
+                    uint32_t* num_repaired);
+
+/* build_imi (index.hpp:38-39, index.cpp:69-96). */
+int suco_gpu_build_imi(const uint32_t* first, const uint32_t* second, uint64_t n, uint32_t k_half,
+                       uint64_t* offsets, uint32_t* ids);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SUCO_B200_H */

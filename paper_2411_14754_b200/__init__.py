@@ -1,0 +1,400 @@
+"""SuCo on B200: the reference's index-build and batched-query API, on sm_100a kernels.
+
+Python mirror of the reference library's public interface (/root/reference/proj/include/suco):
+same names, argument meaning, defaults and error taxonomy, so tests written
+against the reference read the same here. Everything below calls the C-ABI of
+libsuco_b200.so (include/suco_b200.h); numpy arrays are only host buffers.
+
+    suco.IndexParams        index.hpp:53-61         suco.build_index      index.hpp:85
+    suco.CollisionParams    sc_linear.hpp:22-31     suco.knn_query        query.hpp:93-96
+    suco.collision_count    sc_linear.hpp:36        suco.rerank           query.hpp:83-84
+    suco.candidate_count    sc_linear.hpp:40        suco.centroid_distances query.hpp:27-28
+    suco.kmeans             kmeans.hpp:46-48        suco.dynamic_activation query.hpp:57-58
+    suco.build_imi          index.hpp:38-39         suco.load_index / GpuIndex.serialize  index.hpp:99-108
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass
+from typing import List, NamedTuple, Optional, Tuple
+
+import numpy as np
+
+from . import _capi as _c
+
+__all__ = [
+    "Error", "ContractError", "ConfigError", "FormatError", "CorruptIndexError", "IncompatibilityError",
+    "SubspaceMode", "IndexParams", "CollisionParams", "Dataset", "Neighbor", "RetrievedCell", "GpuIndex",
+    "collision_count", "candidate_count", "build_index", "load_index", "knn_query", "centroid_distances",
+    "dynamic_activation", "rerank", "kmeans", "build_imi", "device_count",
+]
+
+
+# ------------------------------------------------------------------ errors (error.hpp:9-37)
+class Error(RuntimeError):
+    pass
+
+
+class ContractError(Error):
+    pass
+
+
+class ConfigError(Error):
+    pass
+
+
+class FormatError(Error):
+    pass
+
+
+class CorruptIndexError(FormatError):
+    pass
+
+
+class IncompatibilityError(Error):
+    pass
+
+
+_CODES = {1: Error, 2: ConfigError, 3: CorruptIndexError, 4: IncompatibilityError, 5: ContractError}
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise _CODES.get(rc, Error)(_c.last_error().decode(errors="replace"))
+
+
+def _p(a: np.ndarray, t):
+    return a.ctypes.data_as(t)
+
+
+def _f32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def device_count() -> int:
+    n = C.c_int(0)
+    _check(_c.device_count(C.byref(n)))
+    return n.value
+
+
+# ------------------------------------------------------------------ params
+class SubspaceMode(enum.IntEnum):
+    Contiguous = 0
+    Shuffled = 1
+
+
+@dataclass
+class IndexParams:
+    num_subspaces: int = 8
+    k_half: int = 50
+    iterations: int = 10
+    seed: int = 42
+    mode: SubspaceMode = SubspaceMode.Contiguous
+
+    def _c(self) -> _c.IndexParamsC:
+        return _c.IndexParamsC(self.num_subspaces, self.k_half, self.iterations, int(self.mode), self.seed)
+
+
+@dataclass
+class CollisionParams:
+    alpha: float = 0.05
+    beta: float = 0.005
+    k: int = 50
+
+    def _c(self) -> _c.CollisionParamsC:
+        return _c.CollisionParamsC(float(self.alpha), float(self.beta), int(self.k))
+
+    def validate(self, n: int) -> None:
+        """sc_linear.cpp:26-37 — ConfigError unless 0<alpha<=1, 0<beta<=1, 1<=k<=n."""
+        cp = self._c()
+        _check(_c.validate_collision_params(C.byref(cp), n))
+
+
+def collision_count(alpha: float, n: int) -> int:
+    """max(1, floor(alpha*n)) with 1e-6 snapping (sc_linear.cpp:39-42)."""
+    return int(_c.collision_count(alpha, n))
+
+
+def candidate_count(beta: float, n: int, k: int) -> int:
+    """max(k, ceil(beta*n)) with 1e-6 snapping (sc_linear.cpp:44-47)."""
+    return int(_c.candidate_count(beta, n, k))
+
+
+class Dataset:
+    """Row-major n x d float32 matrix (core.hpp:17-37); validated on upload."""
+
+    def __init__(self, values):
+        v = _f32(values)
+        if v.ndim != 2:
+            raise ContractError("dataset must be a 2-D n x d matrix")
+        self.values = v
+
+    @property
+    def n(self) -> int:
+        return self.values.shape[0]
+
+    @property
+    def d(self) -> int:
+        return self.values.shape[1]
+
+    def size(self) -> int:
+        return self.n
+
+    def dim(self) -> int:
+        return self.d
+
+    def row(self, i: int) -> np.ndarray:
+        return self.values[i]
+
+
+def _values(ds) -> np.ndarray:
+    return ds.values if isinstance(ds, Dataset) else _f32(ds)
+
+
+class Neighbor(NamedTuple):
+    id: int
+    distance: float
+
+
+class RetrievedCell(NamedTuple):
+    c1: int
+    c2: int
+    cumulative: int
+    sum_dist: float
+
+
+# ------------------------------------------------------------------ index
+class GpuIndex:
+    """Device-resident SucoIndex (index.hpp:67-74) plus the dataset rows it re-ranks."""
+
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _c.free_index(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self):
+        n = C.c_uint64()
+        d = C.c_uint32()
+        p = _c.IndexParamsC()
+        _check(_c.index_info(self._h, C.byref(n), C.byref(d), C.byref(p), None, None, None))
+        return n.value, d.value, IndexParams(p.num_subspaces, p.k_half, p.iterations, p.seed, SubspaceMode(p.mode))
+
+    @property
+    def n(self) -> int:
+        return self.info()[0]
+
+    @property
+    def d(self) -> int:
+        return self.info()[1]
+
+    @property
+    def params(self) -> IndexParams:
+        return self.info()[2]
+
+    def layout(self):
+        n, d, p = self.info()
+        dims = np.empty(d, np.uint32)
+        sizes = np.empty(p.num_subspaces, np.uint32)
+        split = np.empty(p.num_subspaces, np.uint32)
+        _check(_c.index_info(self._h, None, None, None, _p(dims, _c.u32p), _p(sizes, _c.u32p), _p(split, _c.u32p)))
+        return dims, sizes, split
+
+    def subspace(self, s: int):
+        """(centroids_first, centroids_second, imi_offsets, imi_ids) of subspace s."""
+        n, d, p = self.info()
+        _, sizes, split = self.layout()
+        h1, h2 = int(split[s]), int(sizes[s] - split[s])
+        c1 = np.empty((p.k_half, h1), np.float32)
+        c2 = np.empty((p.k_half, h2), np.float32)
+        off = np.empty(p.k_half * p.k_half + 1, np.uint64)
+        ids = np.empty(n, np.uint32)
+        _check(_c.index_subspace(self._h, s, _p(c1, _c.f32p), _p(c2, _c.f32p), _p(off, _c.u64p), _p(ids, _c.u32p)))
+        return c1, c2, off, ids
+
+    def serialize(self) -> bytes:
+        """serialize_index (index.cpp:147-170): byte-identical to the reference."""
+        ln = C.c_uint64()
+        _check(_c.serialize_index(self._h, None, 0, C.byref(ln)))
+        buf = np.empty(ln.value, np.uint8)
+        _check(_c.serialize_index(self._h, _p(buf, _c.u8p), ln.value, C.byref(ln)))
+        return buf.tobytes()
+
+    def save(self, path: str) -> None:
+        with open(path, "wb") as f:
+            f.write(self.serialize())
+
+    def knn_query_batch(self, queries, params: CollisionParams) -> Tuple[np.ndarray, np.ndarray]:
+        """Batched knn_query (run_suco_batch, suco_cli.cpp:95-114): (ids nq x k, distances nq x k)."""
+        q = _f32(queries)
+        if q.ndim == 1:
+            q = q[None, :]
+        nq, qlen = q.shape
+        k = int(params.k)
+        ids = np.zeros((nq, max(k, 1)), np.uint32)
+        dists = np.zeros((nq, max(k, 1)), np.float64)
+        cp = params._c()
+        _check(_c.knn_query_batch(self._h, _p(q, _c.f32p), nq, qlen, C.byref(cp), _p(ids, _c.u32p),
+                                  _p(dists, _c.f64p)))
+        return ids[:, :k], dists[:, :k]
+
+    def knn_query_batch_device(self, d_queries: int, nq: int, qlen: int, params: CollisionParams, d_ids: int,
+                               d_dists: int, stream: Optional[int] = None) -> None:
+        """Device-resident variant: raw device pointers (e.g. torch tensor .data_ptr())."""
+        cp = params._c()
+        _check(_c.knn_query_batch_device(self._h, C.c_void_p(d_queries), nq, qlen, C.byref(cp), C.c_void_p(d_ids),
+                                         C.c_void_p(d_dists), C.c_void_p(stream or 0)))
+
+    def set_stream(self, stream: Optional[int]) -> None:
+        _check(_c.set_stream(self._h, C.c_void_p(stream or 0)))
+
+    def synchronize(self) -> None:
+        _check(_c.synchronize(self._h))
+
+    def set_profiling(self, enabled: bool) -> None:
+        _check(_c.set_profiling(self._h, int(bool(enabled))))
+
+    def stage_times(self):
+        """(ms per stage [traverse, select, rerank], retrieved ids summed over queries x subspaces, nq, m)
+        of the last query call; needs set_profiling(True) before that call."""
+        ms = np.zeros(3, np.float64)
+        st = np.zeros(3, np.uint64)
+        _check(_c.stage_times(self._h, _p(ms, _c.f64p), _p(st, _c.u64p)))
+        return ms, int(st[0]), int(st[1]), int(st[2])
+
+    def query_intermediates(self, query, params: CollisionParams):
+        """(scores n, candidates ascending, cells per subspace, cumulative per subspace) of one query."""
+        q = _f32(query).ravel()
+        n, d, p = self.info()
+        scores = np.empty(n, np.uint32)
+        cands = np.empty(n, np.uint32)
+        m = C.c_uint64()
+        cps = np.empty(p.num_subspaces, np.uint32)
+        cum = np.empty(p.num_subspaces, np.uint64)
+        cp = params._c()
+        _check(_c.query_intermediates(self._h, _p(q, _c.f32p), q.size, C.byref(cp), _p(scores, _c.u32p),
+                                      _p(cands, _c.u32p), C.byref(m), _p(cps, _c.u32p), _p(cum, _c.u64p)))
+        return scores, cands[: m.value].copy(), cps, cum
+
+
+def build_index(dataset, params: IndexParams = IndexParams(), device: int = 0) -> GpuIndex:
+    """build_index (index.hpp:85, index.cpp:98-145) on the GPU."""
+    v = _values(dataset)
+    if v.ndim != 2:
+        raise ContractError("dataset must be a 2-D n x d matrix")
+    h = C.c_void_p()
+    ip = params._c()
+    _check(_c.build_index(_p(v, _c.f32p), v.shape[0], v.shape[1], C.byref(ip), device, C.byref(h)))
+    return GpuIndex(h)
+
+
+def load_index(blob: bytes, dataset, device: int = 0) -> GpuIndex:
+    """deserialize_index (index.cpp:191-293) + check_compatible (index.cpp:295-305), uploaded to the GPU."""
+    if isinstance(blob, str):
+        with open(blob, "rb") as f:
+            blob = f.read()
+    v = _values(dataset)
+    buf = np.frombuffer(blob, np.uint8)
+    h = C.c_void_p()
+    _check(_c.load_index(_p(buf, _c.u8p), len(blob), _p(v, _c.f32p), v.shape[0], v.shape[1], device, C.byref(h)))
+    return GpuIndex(h)
+
+
+def knn_query(index: GpuIndex, dataset, query, params: CollisionParams) -> List[Neighbor]:
+    """knn_query (query.hpp:93-96) for one query; the index owns the dataset rows on the device,
+    `dataset` is checked for compatibility (index.cpp:295-305) like the reference."""
+    v = _values(dataset)
+    n, d, _ = index.info()
+    if v.shape[0] != n:
+        raise IncompatibilityError(f"index was built from n = {n} points but dataset has n = {v.shape[0]}")
+    if v.shape[1] != d:
+        raise IncompatibilityError(f"index was built for d = {d} but dataset has d = {v.shape[1]}")
+    ids, dists = index.knn_query_batch(_f32(query).reshape(1, -1), params)
+    return [Neighbor(int(i), float(x)) for i, x in zip(ids[0], dists[0])]
+
+
+def centroid_distances(half_query, centroids, k_half: int):
+    """query.cpp:42-64: (dists true-Euclidean fp64, order by (dist, id))."""
+    q = _f32(half_query).ravel()
+    c = _f32(centroids).ravel()
+    if k_half >= 1 and q.size and c.size != k_half * q.size:
+        raise ContractError("centroid matrix does not match k_half x half dim")
+    dists = np.empty(max(k_half, 1), np.float64)
+    order = np.empty(max(k_half, 1), np.uint32)
+    _check(_c.centroid_distances(_p(q, _c.f32p), q.size, _p(c, _c.f32p), k_half, _p(dists, _c.f64p),
+                                 _p(order, _c.u32p)))
+    return dists[:k_half], order[:k_half]
+
+
+def dynamic_activation(alpha: float, n: int, cd1, cd2, imi_offsets) -> List[RetrievedCell]:
+    """query.cpp:66-121 over the IMI given by its CSR offsets; cd = (dists, order)."""
+    d1, o1 = (np.ascontiguousarray(cd1[0], np.float64), np.ascontiguousarray(cd1[1], np.uint32))
+    d2, o2 = (np.ascontiguousarray(cd2[0], np.float64), np.ascontiguousarray(cd2[1], np.uint32))
+    off = np.ascontiguousarray(imi_offsets, np.uint64)
+    k = int(round((off.size - 1) ** 0.5))
+    if k * k + 1 != off.size:
+        raise ContractError("imi offsets must hold k_half^2 + 1 entries")
+    if d1.size != k or o1.size != k or d2.size != k or o2.size != k:
+        raise ContractError("centroid distance arrays do not match the imi's k_half")
+    cap = k * k
+    c1 = np.empty(cap, np.uint32)
+    c2 = np.empty(cap, np.uint32)
+    cum = np.empty(cap, np.uint64)
+    sums = np.empty(cap, np.float64)
+    cnt = C.c_uint64()
+    _check(_c.dynamic_activation(alpha, n, _p(d1, _c.f64p), _p(o1, _c.u32p), _p(d2, _c.f64p), _p(o2, _c.u32p), k,
+                                 _p(off, _c.u64p), _p(c1, _c.u32p), _p(c2, _c.u32p), _p(cum, _c.u64p),
+                                 _p(sums, _c.f64p), cap, C.byref(cnt)))
+    return [RetrievedCell(int(c1[i]), int(c2[i]), int(cum[i]), float(sums[i])) for i in range(cnt.value)]
+
+
+def rerank(dataset, query, candidates, k: int) -> List[Neighbor]:
+    """query.cpp:159-197: exact top-k of the candidates by (distance, id)."""
+    v = _values(dataset)
+    q = _f32(query).ravel()
+    cands = np.ascontiguousarray(candidates, np.uint32)
+    ids = np.empty(max(k, 1), np.uint32)
+    dists = np.empty(max(k, 1), np.float64)
+    _check(_c.rerank(_p(v, _c.f32p), v.shape[0], v.shape[1], _p(q, _c.f32p), q.size, _p(cands, _c.u32p), cands.size,
+                     k, _p(ids, _c.u32p), _p(dists, _c.f64p)))
+    return [Neighbor(int(i), float(x)) for i, x in zip(ids[:k], dists[:k])]
+
+
+def kmeans(points, k: int, iterations: int, seed: int, device: int = 0):
+    """kmeans (kmeans.cpp:118-194): dict(centroids k x dim, assignments n, repaired)."""
+    pts = _f32(points)
+    if pts.ndim == 1:
+        pts = pts[:, None]
+    n, dim = pts.shape
+    cent = np.empty((max(k, 1), dim), np.float32)
+    assign = np.empty(n, np.uint32)
+    rep = np.empty(max(k * max(iterations, 1), 1), np.uint32)
+    nrep = C.c_uint32()
+    _check(_c.kmeans(_p(pts, _c.f32p), n, dim, k, iterations, seed, device, _p(cent, _c.f32p), _p(assign, _c.u32p),
+                     _p(rep, _c.u32p), C.byref(nrep)))
+    return dict(centroids=cent[:k], assignments=assign, repaired=rep[: nrep.value].copy())
+
+
+def build_imi(first, second, k_half: int):
+    """build_imi (index.cpp:69-96): (offsets k_half^2+1 u64, ids n u32)."""
+    a = np.ascontiguousarray(first, np.uint32)
+    b = np.ascontiguousarray(second, np.uint32)
+    if a.size != b.size:
+        raise ContractError(f"assignment arrays differ in length: {a.size} vs {b.size}")
+    off = np.empty(max(k_half, 1) ** 2 + 1, np.uint64)
+    ids = np.empty(a.size, np.uint32)
+    _check(_c.build_imi(_p(a, _c.u32p), _p(b, _c.u32p), a.size, k_half, _p(off, _c.u64p), _p(ids, _c.u32p)))
+    return off, ids

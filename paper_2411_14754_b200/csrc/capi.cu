@@ -1,0 +1,814 @@
+// C-ABI implementation (include/suco_b200.h): validation in the reference's
+// order, index upload/build, and the query pipeline
+//   traverse (warp per query x subspace) -> select (cluster per query)
+//   -> rerank (CTA per query)
+// enqueued on the index's stream, tiled over the query batch so the
+// per-query scratch (retrieved cells, candidates) stays bounded.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/suco_b200.h"
+#include "build.h"
+#include "index_format.h"
+#include "kernels.h"
+
+using namespace suco_gpu;
+
+namespace {
+
+thread_local std::string g_err;
+
+#define CUDA_TRY(x)                                                                                     \
+    do {                                                                                                \
+        const cudaError_t e_ = (x);                                                                     \
+        if (e_ != cudaSuccess) raise(SUCO_ERR_INTERNAL, std::string("CUDA error '") +                 \
+                                                            cudaGetErrorString(e_) + "' in " #x);       \
+    } while (0)
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+    try {
+        fn();
+        return SUCO_OK;
+    } catch (const Status& s) {
+        g_err = s.msg;
+        return s.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "out of host memory";
+        return SUCO_ERR_INTERNAL;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return SUCO_ERR_INTERNAL;
+    }
+}
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t cap = 0;
+    void reserve(size_t count) {
+        if (count <= cap && p) return;
+        release();
+        CUDA_TRY(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+        cap = count;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    ~DevBuf() { release(); }
+};
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        int count = 0;
+        if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+            cudaGetLastError();
+            raise(SUCO_ERR_INTERNAL, "no CUDA device available: the SuCo B200 path has no CPU fallback");
+        }
+        if (dev < 0 || dev >= count) raise(SUCO_ERR_INTERNAL, "CUDA device " + std::to_string(dev) + " does not exist");
+        CUDA_TRY(cudaGetDevice(&prev));
+        if (prev != dev) CUDA_TRY(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+int cluster_size_from_env() {
+    const char* v = std::getenv("SUCO_CLUSTER");
+    if (!v) return 8;
+    const int c = std::atoi(v);
+    return (c == 1 || c == 2 || c == 4 || c == 8 || c == 16) ? c : 8;
+}
+
+}  // namespace
+
+struct suco_gpu_index {
+    int device = 0;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    HostIndex host;  // layout, params, centroids (IMI lives on the device)
+    uint32_t K = 0, hmax = 0;
+    DevBuf<float> data;
+    DevBuf<uint32_t> dims;
+    DevBuf<SubDesc> sub;
+    DevBuf<float> cent;
+    DevBuf<uint32_t> cell_off;   // ns x (K+1)
+    DevBuf<uint32_t> cell_size;  // ns x K
+    DevBuf<uint32_t> ids;        // ns x n
+    DevBuf<uint32_t> slab_off;   // ns x K x (nslabs+1)
+    SelectConfig sel{};
+    // query scratch
+    DevBuf<float> q;
+    DevBuf<uint32_t> cells, ncells, cands, out_ids, all_id;
+    DevBuf<double> out_d, all_d;
+    // stage profiling (suco_gpu_set_profiling)
+    bool profile = false;
+    std::vector<cudaEvent_t> events;  // 4 per tile: before traverse/select/rerank, after rerank
+    uint32_t tiles = 0;
+    DevBuf<unsigned long long> stat_cum;
+    uint64_t last_nq = 0, last_m = 0;
+
+    ~suco_gpu_index() {
+        for (cudaEvent_t e : events) cudaEventDestroy(e);
+        if (own) cudaStreamDestroy(own);
+    }
+};
+
+namespace {
+
+void check_dataset(const float* data, uint64_t n, uint32_t d) {
+    if (n < 1 || d < 1) raise(SUCO_ERR_CONTRACT, "dataset requires n >= 1 and d >= 1");
+    if (!data) raise(SUCO_ERR_CONTRACT, "dataset buffer is null");
+}
+
+// Dataset finiteness (core.cpp:15-19), checked on the device after upload.
+void check_finite_device(const float* d_data, uint64_t count, cudaStream_t st) {
+    unsigned long long* flag = nullptr;
+    CUDA_TRY(cudaMalloc(&flag, sizeof(unsigned long long)));
+    const unsigned long long init = ~0ull;
+    unsigned long long got = 0;
+    cudaError_t e = cudaMemcpyAsync(flag, &init, sizeof init, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = launch_check_finite(d_data, count, reinterpret_cast<int*>(flag), st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&got, flag, sizeof got, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(flag);
+    CUDA_TRY(e);
+    if (got != ~0ull) raise(SUCO_ERR_CONTRACT, "dataset component " + std::to_string(got) + " is not finite");
+}
+
+void create_stream(suco_gpu_index* x) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&x->own, cudaStreamNonBlocking));
+    x->stream = x->own;
+}
+
+void upload_data(suco_gpu_index* x, const float* data, uint64_t n, uint32_t d) {
+    x->data.reserve(n * d);
+    CUDA_TRY(cudaMemcpyAsync(x->data.p, data, n * d * sizeof(float), cudaMemcpyHostToDevice, x->stream));
+    check_finite_device(x->data.p, n * d, x->stream);
+}
+
+// Layout + centroid tables on the device, from x->host.
+void upload_codebooks(suco_gpu_index* x) {
+    const HostIndex& h = x->host;
+    const uint32_t ns = h.layout.ns;
+    std::vector<SubDesc> sd(ns);
+    std::vector<float> cent;
+    uint32_t pos = 0;
+    x->hmax = 0;
+    for (uint32_t s = 0; s < ns; ++s) {
+        SubDesc& d = sd[s];
+        d.h1 = h.layout.h1(s);
+        d.h2 = h.layout.h2(s);
+        d.dims1 = pos;
+        d.dims2 = pos + d.h1;
+        pos += h.layout.sizes[s];
+        d.cent1 = cent.size();
+        cent.insert(cent.end(), h.cent1[s].begin(), h.cent1[s].end());
+        d.cent2 = cent.size();
+        cent.insert(cent.end(), h.cent2[s].begin(), h.cent2[s].end());
+        x->hmax = std::max({x->hmax, d.h1, d.h2});
+    }
+    x->dims.reserve(h.layout.dims.size());
+    CUDA_TRY(cudaMemcpyAsync(x->dims.p, h.layout.dims.data(), h.layout.dims.size() * 4, cudaMemcpyHostToDevice, x->stream));
+    x->sub.reserve(ns);
+    CUDA_TRY(cudaMemcpyAsync(x->sub.p, sd.data(), ns * sizeof(SubDesc), cudaMemcpyHostToDevice, x->stream));
+    x->cent.reserve(cent.size());
+    CUDA_TRY(cudaMemcpyAsync(x->cent.p, cent.data(), cent.size() * 4, cudaMemcpyHostToDevice, x->stream));
+    CUDA_TRY(cudaStreamSynchronize(x->stream));
+}
+
+// Cell sizes and slab offsets from the device-resident CSR.
+void finalize_device(suco_gpu_index* x) {
+    const uint32_t ns = x->host.layout.ns;
+    x->K = x->host.p.k_half * x->host.p.k_half;
+    x->cell_size.reserve(uint64_t(ns) * x->K);
+    CUDA_TRY(launch_cell_sizes(x->cell_off.p, ns, x->K, x->cell_size.p, x->stream));
+    x->sel = plan_select(x->host.n, ns, cluster_size_from_env());
+    x->slab_off.reserve(uint64_t(ns) * x->K * (x->sel.nslabs + 1));
+    CUDA_TRY(launch_slab_offsets(x->cell_off.p, x->ids.p, x->host.n, ns, x->K, x->sel.CH, x->sel.nslabs, x->slab_off.p,
+                                 x->stream));
+    CUDA_TRY(cudaStreamSynchronize(x->stream));
+}
+
+void upload_imi(suco_gpu_index* x) {
+    HostIndex& h = x->host;
+    const uint32_t ns = h.layout.ns;
+    const uint64_t K = uint64_t(h.p.k_half) * h.p.k_half;
+    x->cell_off.reserve(ns * (K + 1));
+    x->ids.reserve(ns * h.n);
+    std::vector<uint32_t> off32(K + 1);
+    for (uint32_t s = 0; s < ns; ++s) {
+        for (uint64_t c = 0; c <= K; ++c) off32[c] = static_cast<uint32_t>(h.offsets[s][c]);
+        CUDA_TRY(cudaMemcpy(x->cell_off.p + s * (K + 1), off32.data(), (K + 1) * 4, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(x->ids.p + s * h.n, h.ids[s].data(), h.n * 4, cudaMemcpyHostToDevice));
+    }
+    // the IMI's home is the device; host copies are re-read on demand
+    h.offsets.clear();
+    h.ids.clear();
+    h.offsets.shrink_to_fit();
+    h.ids.shrink_to_fit();
+}
+
+void download_imi(const suco_gpu_index* x, uint32_t s, uint64_t* offsets, uint32_t* ids) {
+    const uint64_t K = x->K, n = x->host.n;
+    if (offsets) {
+        std::vector<uint32_t> off32(K + 1);
+        CUDA_TRY(cudaMemcpy(off32.data(), x->cell_off.p + s * (K + 1), (K + 1) * 4, cudaMemcpyDeviceToHost));
+        for (uint64_t c = 0; c <= K; ++c) offsets[c] = off32[c];
+    }
+    if (ids) CUDA_TRY(cudaMemcpy(ids, x->ids.p + s * n, n * 4, cudaMemcpyDeviceToHost));
+}
+
+// ---------------------------------------------------------------- params
+double snapped_product(double ratio, uint64_t n) {  // sc_linear.cpp:18-22
+    const double product = ratio * static_cast<double>(n);
+    const double nearest = std::round(product);
+    return std::abs(product - nearest) <= 1e-6 ? nearest : product;
+}
+
+void validate_params(const suco_collision_params* p, uint64_t n) {  // sc_linear.cpp:26-37
+    if (!p) raise(SUCO_ERR_CONTRACT, "collision params are null");
+    if (!(p->alpha > 0.0) || p->alpha > 1.0) raise(SUCO_ERR_CONFIG, "alpha must be in (0, 1], got " + std::to_string(p->alpha));
+    if (!(p->beta > 0.0) || p->beta > 1.0) raise(SUCO_ERR_CONFIG, "beta must be in (0, 1], got " + std::to_string(p->beta));
+    if (p->k < 1 || p->k > n) {
+        raise(SUCO_ERR_CONFIG, "k must be in [1, n]; got k = " + std::to_string(p->k) + " with n = " + std::to_string(n));
+    }
+}
+
+// -------------------------------------------------------------- pipeline
+struct Dbg {
+    uint8_t* scores = nullptr;  // n
+    double* sums = nullptr;     // ns x K
+    uint64_t* cum = nullptr;    // ns x K
+};
+
+uint64_t tile_size(const suco_gpu_index* x, uint64_t nq, uint64_t m, uint32_t k) {
+    const uint64_t ns = x->host.layout.ns;
+    const uint64_t per = ns * x->K * 4 + ns * 4 + m * 4 + (k > 32 ? m * 12 : 0) + uint64_t(x->host.d) * 4 + k * 12;
+    const uint64_t budget = 4ull << 30;
+    return std::max<uint64_t>(1, std::min<uint64_t>(nq, budget / per));
+}
+
+// Runs the three stages for nt device-resident queries.
+void run_tile(suco_gpu_index* x, const float* d_q, uint64_t nt, uint64_t target, uint64_t m, uint32_t k,
+              uint32_t* d_ids, double* d_dists, cudaStream_t st, const Dbg* dbg) {
+    const HostIndex& h = x->host;
+    const uint32_t ns = h.layout.ns;
+    cudaEvent_t* ev = nullptr;
+    if (x->profile && !dbg) {
+        while (x->events.size() < 4ull * (x->tiles + 1)) {
+            cudaEvent_t e;
+            CUDA_TRY(cudaEventCreate(&e));
+            x->events.push_back(e);
+        }
+        ev = x->events.data() + 4ull * x->tiles;
+        ++x->tiles;
+    }
+    x->cells.reserve(nt * ns * x->K);
+    x->ncells.reserve(nt * ns);
+    x->cands.reserve(nt * m);
+    TraverseArgs ta{};
+    ta.queries = d_q;
+    ta.d = h.d;
+    ta.nq = nt;
+    ta.dims = x->dims.p;
+    ta.sub = x->sub.p;
+    ta.cent = x->cent.p;
+    ta.cell_size = x->cell_size.p;
+    ta.ns = ns;
+    ta.k_half = h.p.k_half;
+    ta.K = x->K;
+    ta.hmax = x->hmax;
+    ta.target = target;
+    ta.cells = x->cells.p;
+    ta.ncells = x->ncells.p;
+    ta.dbg_sum = dbg ? dbg->sums : nullptr;
+    ta.dbg_cum = dbg ? dbg->cum : nullptr;
+    ta.stat_cum = ev ? x->stat_cum.p : nullptr;
+    if (ev) CUDA_TRY(cudaEventRecord(ev[0], st));
+    CUDA_TRY(launch_traverse(ta, st));
+    if (ev) CUDA_TRY(cudaEventRecord(ev[1], st));
+
+    SelectArgs sa{};
+    sa.ids = x->ids.p;
+    sa.slab_off = x->slab_off.p;
+    sa.cells = x->cells.p;
+    sa.ncells = x->ncells.p;
+    sa.cells_cap = x->K;
+    sa.n = h.n;
+    sa.ns = ns;
+    sa.K = x->K;
+    sa.nslabs = x->sel.nslabs;
+    sa.CH = x->sel.CH;
+    sa.rounds = x->sel.rounds;
+    sa.CS = x->sel.CS;
+    sa.m = m;
+    sa.cands = x->cands.p;
+    sa.scores_dbg = dbg ? dbg->scores : nullptr;
+    CUDA_TRY(launch_select(sa, x->sel, nt, st));
+    if (ev) CUDA_TRY(cudaEventRecord(ev[2], st));
+
+    RerankArgs ra{};
+    ra.data = x->data.p;
+    ra.n = h.n;
+    ra.d = h.d;
+    ra.queries = d_q;
+    ra.cands = x->cands.p;
+    ra.m = m;
+    ra.k = k;
+    ra.out_ids = d_ids;
+    ra.out_dists = d_dists;
+    if (k > 32) {
+        x->all_d.reserve(nt * m);
+        x->all_id.reserve(nt * m);
+        ra.all_d = x->all_d.p;
+        ra.all_id = x->all_id.p;
+    }
+    CUDA_TRY(launch_rerank(ra, nt, st));
+    if (ev) CUDA_TRY(cudaEventRecord(ev[3], st));
+}
+
+// Resets the per-call profiling state (events + work counters).
+void begin_call(suco_gpu_index* x, uint64_t nq, uint64_t m, cudaStream_t st) {
+    x->tiles = 0;
+    x->last_nq = nq;
+    x->last_m = m;
+    if (x->profile) {
+        x->stat_cum.reserve(1);
+        CUDA_TRY(cudaMemsetAsync(x->stat_cum.p, 0, sizeof(unsigned long long), st));
+    }
+}
+
+void check_query_args(const suco_gpu_index* x, uint32_t qlen, const suco_collision_params* p) {
+    if (!x) raise(SUCO_ERR_CONTRACT, "index is null");
+    if (qlen != x->host.d) {  // query.cpp:203-206
+        raise(SUCO_ERR_CONTRACT, "query length " + std::to_string(qlen) + " does not match dataset d = " +
+                                     std::to_string(x->host.d));
+    }
+    validate_params(p, x->host.n);  // query.cpp:208
+    if (x->host.layout.ns > 255) raise(SUCO_ERR_CONFIG, "the GPU path keeps u8 collision counters: N_s must be <= 255");
+}
+
+suco_gpu_index* new_index(int device) {
+    auto* x = new suco_gpu_index();
+    x->device = device;
+    return x;
+}
+
+}  // namespace
+
+// ======================================================================= C ABI
+extern "C" {
+
+const char* suco_last_error(void) { return g_err.c_str(); }
+
+int suco_gpu_device_count(int* count) {
+    return guarded([&] {
+        int c = 0;
+        if (cudaGetDeviceCount(&c) != cudaSuccess) {
+            cudaGetLastError();
+            c = 0;
+        }
+        *count = c;
+    });
+}
+
+uint64_t suco_collision_count(double alpha, uint64_t n) {  // sc_linear.cpp:39-42
+    const uint64_t c = static_cast<uint64_t>(std::floor(snapped_product(alpha, n)));
+    return std::max<uint64_t>(1, c);
+}
+
+uint64_t suco_candidate_count(double beta, uint64_t n, uint64_t k) {  // sc_linear.cpp:44-47
+    const uint64_t c = static_cast<uint64_t>(std::ceil(snapped_product(beta, n)));
+    return std::max(k, c);
+}
+
+int suco_validate_collision_params(const suco_collision_params* p, uint64_t n) {
+    return guarded([&] { validate_params(p, n); });
+}
+
+int suco_gpu_load_index(const unsigned char* bytes, uint64_t len, const float* data, uint64_t n, uint32_t d, int device,
+                        suco_gpu_index** out) {
+    return guarded([&] {
+        if (!out) raise(SUCO_ERR_CONTRACT, "output handle pointer is null");
+        *out = nullptr;
+        HostIndex h = parse_index(bytes, len);  // FORMAT first (load_index), as suco_cli.cpp:243
+        check_dataset(data, n, d);              // then the dataset (CONTRACT)
+        if (h.n != n) {                         // index.cpp:295-305
+            raise(SUCO_ERR_INCOMPATIBLE, "index was built from n = " + std::to_string(h.n) +
+                                             " points but dataset has n = " + std::to_string(n));
+        }
+        if (h.d != d) {
+            raise(SUCO_ERR_INCOMPATIBLE, "index was built for d = " + std::to_string(h.d) +
+                                             " but dataset has d = " + std::to_string(d));
+        }
+        DeviceGuard g(device);
+        suco_gpu_index* x = new_index(device);
+        try {
+            create_stream(x);
+            x->host = std::move(h);
+            upload_data(x, data, n, d);
+            upload_codebooks(x);
+            upload_imi(x);
+            finalize_device(x);
+        } catch (...) {
+            delete x;
+            throw;
+        }
+        *out = x;
+    });
+}
+
+int suco_gpu_build_index(const float* data, uint64_t n, uint32_t d, const suco_index_params* params, int device,
+                         suco_gpu_index** out) {
+    return guarded([&] {
+        if (!out) raise(SUCO_ERR_CONTRACT, "output handle pointer is null");
+        *out = nullptr;
+        if (!params) raise(SUCO_ERR_CONTRACT, "index params are null");
+        check_dataset(data, n, d);
+        DeviceGuard g(device);
+        suco_gpu_index* x = new_index(device);
+        try {
+            create_stream(x);
+            upload_data(x, data, n, d);  // finiteness (core.cpp:15-19) before any parameter check
+            // index.cpp:100-108
+            if (params->k_half < 1) raise(SUCO_ERR_CONFIG, "k_half must be >= 1");
+            if (params->iterations < 1) raise(SUCO_ERR_CONFIG, "iterations must be >= 1");
+            if (n < params->k_half) {
+                raise(SUCO_ERR_CONFIG, "dataset has n = " + std::to_string(n) + " points, fewer than k_half = " +
+                                           std::to_string(params->k_half));
+            }
+            if (n > 0xFFFFFFFFull) raise(SUCO_ERR_CONTRACT, "dataset exceeds 32-bit point-id capacity");
+            x->host.layout = sample_subspaces(d, params->num_subspaces, params->mode, params->seed);
+            x->host.n = n;
+            x->host.d = d;
+            x->host.p = *params;
+            const uint64_t K = uint64_t(params->k_half) * params->k_half;
+            x->cell_off.reserve(uint64_t(params->num_subspaces) * (K + 1));
+            x->ids.reserve(uint64_t(params->num_subspaces) * n);
+            BuildOutputs bo{x->cell_off.p, x->ids.p, &x->host.cent1, &x->host.cent2};
+            build_index_device(x->data.p, n, d, x->host.layout, *params, bo, x->stream);
+            upload_codebooks(x);
+            finalize_device(x);
+        } catch (...) {
+            delete x;
+            throw;
+        }
+        *out = x;
+    });
+}
+
+int suco_gpu_serialize_index(const suco_gpu_index* x, unsigned char* buf, uint64_t cap, uint64_t* len) {
+    return guarded([&] {
+        if (!x || !len) raise(SUCO_ERR_CONTRACT, "null argument");
+        DeviceGuard g(x->device);
+        HostIndex h;
+        h.n = x->host.n;
+        h.d = x->host.d;
+        h.p = x->host.p;
+        h.layout = x->host.layout;
+        h.cent1 = x->host.cent1;
+        h.cent2 = x->host.cent2;
+        const uint32_t ns = h.layout.ns;
+        h.offsets.resize(ns);
+        h.ids.resize(ns);
+        for (uint32_t s = 0; s < ns; ++s) {
+            h.offsets[s].resize(x->K + 1);
+            h.ids[s].resize(h.n);
+            download_imi(x, s, h.offsets[s].data(), h.ids[s].data());
+        }
+        const std::vector<unsigned char> bytes = serialize(h);
+        *len = bytes.size();
+        if (buf) {
+            if (cap < bytes.size()) raise(SUCO_ERR_CONTRACT, "serialize: buffer too small");
+            std::memcpy(buf, bytes.data(), bytes.size());
+        }
+    });
+}
+
+int suco_gpu_index_subspace(const suco_gpu_index* x, uint32_t s, float* c1, float* c2, uint64_t* offsets, uint32_t* ids) {
+    return guarded([&] {
+        if (!x) raise(SUCO_ERR_CONTRACT, "index is null");
+        if (s >= x->host.layout.ns) raise(SUCO_ERR_CONTRACT, "subspace index out of range");
+        if (c1) std::memcpy(c1, x->host.cent1[s].data(), x->host.cent1[s].size() * 4);
+        if (c2) std::memcpy(c2, x->host.cent2[s].data(), x->host.cent2[s].size() * 4);
+        if (offsets || ids) {
+            DeviceGuard g(x->device);
+            download_imi(x, s, offsets, ids);
+        }
+    });
+}
+
+int suco_gpu_index_info(const suco_gpu_index* x, uint64_t* n, uint32_t* d, suco_index_params* params, uint32_t* dims,
+                        uint32_t* sizes, uint32_t* split) {
+    return guarded([&] {
+        if (!x) raise(SUCO_ERR_CONTRACT, "index is null");
+        if (n) *n = x->host.n;
+        if (d) *d = x->host.d;
+        if (params) *params = x->host.p;
+        const HostLayout& L = x->host.layout;
+        if (dims) std::memcpy(dims, L.dims.data(), L.dims.size() * 4);
+        if (sizes) std::memcpy(sizes, L.sizes.data(), L.ns * 4);
+        if (split) std::memcpy(split, L.split.data(), L.ns * 4);
+    });
+}
+
+void suco_gpu_free_index(suco_gpu_index* x) {
+    if (!x) return;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(x->device);
+    delete x;
+    if (prev >= 0) cudaSetDevice(prev);
+}
+
+int suco_gpu_set_stream(suco_gpu_index* x, void* stream) {
+    return guarded([&] {
+        if (!x) raise(SUCO_ERR_CONTRACT, "index is null");
+        x->stream = stream ? static_cast<cudaStream_t>(stream) : x->own;
+    });
+}
+
+int suco_gpu_set_profiling(suco_gpu_index* x, int enabled) {
+    return guarded([&] {
+        if (!x) raise(SUCO_ERR_CONTRACT, "index is null");
+        DeviceGuard g(x->device);
+        x->profile = enabled != 0;
+        if (x->profile) x->stat_cum.reserve(1);
+    });
+}
+
+int suco_gpu_stage_times(suco_gpu_index* x, double* ms, uint64_t* stats) {
+    return guarded([&] {
+        if (!x) raise(SUCO_ERR_CONTRACT, "index is null");
+        if (!x->profile) raise(SUCO_ERR_CONTRACT, "profiling is not enabled on this index");
+        DeviceGuard g(x->device);
+        double acc[3] = {0, 0, 0};
+        for (uint32_t t = 0; t < x->tiles; ++t) {
+            cudaEvent_t* ev = x->events.data() + 4ull * t;
+            CUDA_TRY(cudaEventSynchronize(ev[3]));
+            for (int s = 0; s < 3; ++s) {
+                float f = 0.f;
+                CUDA_TRY(cudaEventElapsedTime(&f, ev[s], ev[s + 1]));
+                acc[s] += f;
+            }
+        }
+        if (ms) {
+            for (int s = 0; s < 3; ++s) ms[s] = acc[s];
+        }
+        if (stats) {
+            unsigned long long c = 0;
+            CUDA_TRY(cudaMemcpy(&c, x->stat_cum.p, sizeof c, cudaMemcpyDeviceToHost));
+            stats[0] = c;
+            stats[1] = x->last_nq;
+            stats[2] = x->last_m;
+        }
+    });
+}
+
+int suco_gpu_synchronize(suco_gpu_index* x) {
+    return guarded([&] {
+        if (!x) raise(SUCO_ERR_CONTRACT, "index is null");
+        DeviceGuard g(x->device);
+        CUDA_TRY(cudaStreamSynchronize(x->stream));
+    });
+}
+
+int suco_gpu_knn_query_batch_device(suco_gpu_index* x, const float* d_queries, uint64_t nq, uint32_t qlen,
+                                    const suco_collision_params* p, uint32_t* d_ids, double* d_dists, void* stream) {
+    return guarded([&] {
+        check_query_args(x, qlen, p);
+        DeviceGuard g(x->device);
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : x->stream;
+        const uint64_t n = x->host.n;
+        const uint64_t m = suco_candidate_count(p->beta, n, p->k);
+        const uint64_t target = suco_collision_count(p->alpha, n);
+        const uint64_t tile = tile_size(x, nq, m, p->k);
+        begin_call(x, nq, m, st);
+        for (uint64_t q0 = 0; q0 < nq; q0 += tile) {
+            const uint64_t nt = std::min(tile, nq - q0);
+            run_tile(x, d_queries + q0 * qlen, nt, target, m, p->k, d_ids + q0 * p->k, d_dists + q0 * p->k, st, nullptr);
+        }
+    });
+}
+
+int suco_gpu_knn_query_batch(suco_gpu_index* x, const float* queries, uint64_t nq, uint32_t qlen,
+                             const suco_collision_params* p, uint32_t* ids, double* dists) {
+    return guarded([&] {
+        check_query_args(x, qlen, p);
+        if (nq == 0) return;
+        DeviceGuard g(x->device);
+        cudaStream_t st = x->stream;
+        const uint64_t n = x->host.n;
+        const uint32_t k = p->k;
+        const uint64_t m = suco_candidate_count(p->beta, n, k);
+        const uint64_t target = suco_collision_count(p->alpha, n);
+        const uint64_t tile = tile_size(x, nq, m, k);
+        const uint64_t cap = std::min(tile, nq);
+        x->q.reserve(cap * qlen);
+        x->out_ids.reserve(cap * k);
+        x->out_d.reserve(cap * k);
+        begin_call(x, nq, m, st);
+        for (uint64_t q0 = 0; q0 < nq; q0 += tile) {
+            const uint64_t nt = std::min(tile, nq - q0);
+            CUDA_TRY(cudaMemcpyAsync(x->q.p, queries + q0 * qlen, nt * qlen * 4, cudaMemcpyHostToDevice, st));
+            run_tile(x, x->q.p, nt, target, m, k, x->out_ids.p, x->out_d.p, st, nullptr);
+            CUDA_TRY(cudaMemcpyAsync(ids + q0 * k, x->out_ids.p, nt * k * 4, cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaMemcpyAsync(dists + q0 * k, x->out_d.p, nt * k * 8, cudaMemcpyDeviceToHost, st));
+        }
+        CUDA_TRY(cudaStreamSynchronize(st));
+    });
+}
+
+int suco_gpu_query_intermediates(suco_gpu_index* x, const float* query, uint32_t qlen, const suco_collision_params* p,
+                                 uint32_t* scores, uint32_t* cands, uint64_t* m_out, uint32_t* cells_per_subspace,
+                                 uint64_t* cumulative) {
+    return guarded([&] {
+        check_query_args(x, qlen, p);
+        DeviceGuard g(x->device);
+        cudaStream_t st = x->stream;
+        const uint64_t n = x->host.n;
+        const uint32_t ns = x->host.layout.ns;
+        const uint64_t m = suco_candidate_count(p->beta, n, p->k);
+        const uint64_t target = suco_collision_count(p->alpha, n);
+        DevBuf<uint8_t> sc;
+        DevBuf<double> sums;
+        DevBuf<uint64_t> cum;
+        sc.reserve(n);
+        sums.reserve(uint64_t(ns) * x->K);
+        cum.reserve(uint64_t(ns) * x->K);
+        Dbg dbg{sc.p, sums.p, cum.p};
+        x->q.reserve(qlen);
+        x->out_ids.reserve(p->k);
+        x->out_d.reserve(p->k);
+        CUDA_TRY(cudaMemcpyAsync(x->q.p, query, qlen * 4, cudaMemcpyHostToDevice, st));
+        run_tile(x, x->q.p, 1, target, m, p->k, x->out_ids.p, x->out_d.p, st, &dbg);
+        CUDA_TRY(cudaStreamSynchronize(st));
+        if (scores) {
+            std::vector<uint8_t> s8(n);
+            CUDA_TRY(cudaMemcpy(s8.data(), sc.p, n, cudaMemcpyDeviceToHost));
+            for (uint64_t i = 0; i < n; ++i) scores[i] = s8[i];
+        }
+        if (cands) CUDA_TRY(cudaMemcpy(cands, x->cands.p, m * 4, cudaMemcpyDeviceToHost));
+        if (m_out) *m_out = m;
+        std::vector<uint32_t> nc(ns);
+        CUDA_TRY(cudaMemcpy(nc.data(), x->ncells.p, ns * 4, cudaMemcpyDeviceToHost));
+        if (cells_per_subspace) std::memcpy(cells_per_subspace, nc.data(), ns * 4);
+        if (cumulative) {
+            for (uint32_t s = 0; s < ns; ++s) {
+                cumulative[s] = 0;
+                if (nc[s]) CUDA_TRY(cudaMemcpy(cumulative + s, cum.p + uint64_t(s) * x->K + nc[s] - 1, 8, cudaMemcpyDeviceToHost));
+            }
+        }
+    });
+}
+
+int suco_gpu_centroid_distances(const float* half_query, uint32_t dim, const float* centroids, uint32_t k_half,
+                                double* dists, uint32_t* order) {
+    return guarded([&] {
+        if (k_half < 1) raise(SUCO_ERR_CONTRACT, "k_half must be >= 1");   // query.cpp:44-49
+        if (dim == 0) raise(SUCO_ERR_CONTRACT, "query half is empty");
+        DeviceGuard g(0);
+        DevBuf<float> q, c;
+        DevBuf<double> dd;
+        DevBuf<uint32_t> oo;
+        q.reserve(dim);
+        c.reserve(uint64_t(k_half) * dim);
+        dd.reserve(k_half);
+        oo.reserve(k_half);
+        CUDA_TRY(cudaMemcpy(q.p, half_query, dim * 4, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(c.p, centroids, uint64_t(k_half) * dim * 4, cudaMemcpyHostToDevice));
+        CUDA_TRY(launch_centroid_distances(q.p, dim, c.p, k_half, dd.p, oo.p, 0));
+        CUDA_TRY(cudaMemcpy(dists, dd.p, k_half * 8, cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpy(order, oo.p, k_half * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+int suco_gpu_dynamic_activation(double alpha, uint64_t n, const double* d1, const uint32_t* o1, const double* d2,
+                                const uint32_t* o2, uint32_t k_half, const uint64_t* offsets, uint32_t* c1, uint32_t* c2,
+                                uint64_t* cumulative, double* sum_dist, uint64_t cap, uint64_t* count) {
+    return guarded([&] {
+        // check_traversal_args, query.cpp:16-30
+        if (!(alpha > 0.0) || alpha > 1.0) raise(SUCO_ERR_CONTRACT, "alpha must be in (0, 1]");
+        if (k_half < 1) raise(SUCO_ERR_CONTRACT, "imi has no cells");
+        const uint64_t K = uint64_t(k_half) * k_half;
+        if (offsets[K] != n) {
+            raise(SUCO_ERR_CONTRACT, "imi holds " + std::to_string(offsets[K]) + " ids but n = " + std::to_string(n));
+        }
+        if (n > 0xFFFFFFFFull) raise(SUCO_ERR_CONTRACT, "n exceeds 32-bit point-id capacity");
+        DeviceGuard g(0);
+        std::vector<uint32_t> sizes(K);
+        for (uint64_t c = 0; c < K; ++c) sizes[c] = static_cast<uint32_t>(offsets[c + 1] - offsets[c]);
+        DevBuf<double> dd1, dd2, sums;
+        DevBuf<uint32_t> oo1, oo2, sz, cells, nc;
+        DevBuf<uint64_t> cum;
+        dd1.reserve(k_half), dd2.reserve(k_half), oo1.reserve(k_half), oo2.reserve(k_half);
+        sz.reserve(K), cells.reserve(K), sums.reserve(K), cum.reserve(K), nc.reserve(1);
+        CUDA_TRY(cudaMemcpy(dd1.p, d1, k_half * 8, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(dd2.p, d2, k_half * 8, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(oo1.p, o1, k_half * 4, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(oo2.p, o2, k_half * 4, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(sz.p, sizes.data(), K * 4, cudaMemcpyHostToDevice));
+        CUDA_TRY(launch_da_only(dd1.p, oo1.p, dd2.p, oo2.p, k_half, sz.p, suco_collision_count(alpha, n), cells.p, nc.p,
+                                sums.p, cum.p, 0));
+        uint32_t got = 0;
+        CUDA_TRY(cudaMemcpy(&got, nc.p, 4, cudaMemcpyDeviceToHost));
+        *count = got;
+        const uint64_t w = std::min<uint64_t>(got, cap);
+        std::vector<uint32_t> cl(w);
+        if (w) {
+            CUDA_TRY(cudaMemcpy(cl.data(), cells.p, w * 4, cudaMemcpyDeviceToHost));
+            CUDA_TRY(cudaMemcpy(sum_dist, sums.p, w * 8, cudaMemcpyDeviceToHost));
+            CUDA_TRY(cudaMemcpy(cumulative, cum.p, w * 8, cudaMemcpyDeviceToHost));
+        }
+        for (uint64_t i = 0; i < w; ++i) {
+            c1[i] = cl[i] / k_half;
+            c2[i] = cl[i] % k_half;
+        }
+        if (got > cap) raise(SUCO_ERR_CONTRACT, "cell output capacity too small");
+    });
+}
+
+int suco_gpu_rerank(const float* data, uint64_t n, uint32_t d, const float* query, uint32_t qlen,
+                    const uint32_t* candidates, uint64_t m, uint32_t k, uint32_t* ids, double* dists) {
+    return guarded([&] {
+        // query.cpp:159-176
+        if (qlen != d) {
+            raise(SUCO_ERR_CONTRACT, "query length " + std::to_string(qlen) + " does not match dataset d = " +
+                                         std::to_string(d));
+        }
+        if (k < 1) raise(SUCO_ERR_CONTRACT, "k must be >= 1");
+        if (m < k) raise(SUCO_ERR_CONTRACT, "k = " + std::to_string(k) + " exceeds the " + std::to_string(m) + " candidates");
+        for (uint64_t i = 0; i < m; ++i) {
+            if (candidates[i] >= n) raise(SUCO_ERR_CONTRACT, "candidate id " + std::to_string(candidates[i]) + " out of range");
+        }
+        DeviceGuard g(0);
+        DevBuf<float> dd, qq;
+        DevBuf<uint32_t> cc, oi, ai;
+        DevBuf<double> od, ad;
+        dd.reserve(n * d), qq.reserve(d), cc.reserve(m), oi.reserve(k), od.reserve(k);
+        CUDA_TRY(cudaMemcpy(dd.p, data, n * d * 4, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(qq.p, query, d * 4, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(cc.p, candidates, m * 4, cudaMemcpyHostToDevice));
+        RerankArgs ra{};
+        ra.data = dd.p;
+        ra.n = n;
+        ra.d = d;
+        ra.queries = qq.p;
+        ra.cands = cc.p;
+        ra.m = m;
+        ra.k = k;
+        ra.out_ids = oi.p;
+        ra.out_dists = od.p;
+        if (k > 32) {
+            ad.reserve(m), ai.reserve(m);
+            ra.all_d = ad.p;
+            ra.all_id = ai.p;
+        }
+        CUDA_TRY(launch_rerank(ra, 1, 0));
+        CUDA_TRY(cudaMemcpy(ids, oi.p, k * 4, cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpy(dists, od.p, k * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+int suco_gpu_kmeans(const float* points, uint64_t n, uint32_t dim, uint32_t k, uint32_t iterations, uint64_t seed,
+                    int device, float* centroids, uint32_t* assignments, uint32_t* repaired, uint32_t* num_repaired) {
+    return guarded([&] {
+        // kmeans.cpp:121-126
+        if (k < 1) raise(SUCO_ERR_CONFIG, "kmeans: k must be >= 1");
+        if (iterations < 1) raise(SUCO_ERR_CONFIG, "kmeans: iterations must be >= 1");
+        if (n < k) raise(SUCO_ERR_CONFIG, "kmeans: n = " + std::to_string(n) + " is smaller than k = " + std::to_string(k));
+        if (n > 0xFFFFFFFFull) raise(SUCO_ERR_CONTRACT, "kmeans: n exceeds 32-bit point-id capacity");
+        DeviceGuard g(device);
+        kmeans_device_host_io(points, n, dim, k, iterations, seed, centroids, assignments, repaired, num_repaired);
+    });
+}
+
+int suco_gpu_build_imi(const uint32_t* first, const uint32_t* second, uint64_t n, uint32_t k_half, uint64_t* offsets,
+                       uint32_t* ids) {
+    return guarded([&] {
+        if (k_half < 1) raise(SUCO_ERR_CONTRACT, "build_imi: k_half must be >= 1");  // index.cpp:72-76
+        if (n > 0xFFFFFFFFull) raise(SUCO_ERR_CONTRACT, "build_imi: n exceeds 32-bit point-id capacity");
+        for (uint64_t i = 0; i < n; ++i) {
+            if (first[i] >= k_half || second[i] >= k_half) {
+                raise(SUCO_ERR_CONTRACT, "assignment out of range at point " + std::to_string(i));
+            }
+        }
+        DeviceGuard g(0);
+        build_imi_host_io(first, second, n, k_half, offsets, ids);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,93 @@
+// Launch interfaces of the query-path and build-path kernels (host side).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace suco_gpu {
+
+// ---------------------------------------------------------------- traverse
+// One warp per (query, subspace): project the query halves, exact fp64
+// centroid distances + (dist, id) ranking (query.cpp:42-64), then Dynamic
+// Activation (query.cpp:66-121) until the cumulative global cell size
+// reaches `target` = collision_count(alpha, n). Emits retrieved cell indices
+// (c1 * k_half + c2) in retrieval order.
+struct TraverseArgs {
+    const float* queries;  // nq x d
+    uint32_t d;
+    uint64_t nq;
+    const uint32_t* dims;  // concatenated layout dims
+    const SubDesc* sub;    // ns
+    const float* cent;     // concatenated centroids
+    const uint32_t* cell_size;  // ns x K
+    uint32_t ns, k_half, K, hmax;
+    uint64_t target;
+    uint32_t* cells;   // nq x ns x K
+    uint32_t* ncells;  // nq x ns
+    double* dbg_sum;   // optional, nq x ns x K
+    uint64_t* dbg_cum; // optional, nq x ns x K
+    unsigned long long* stat_cum;  // optional: += final cumulative of every traversal
+};
+cudaError_t launch_traverse(const TraverseArgs& a, cudaStream_t st);
+
+// Stand-alone stages for parity tests.
+cudaError_t launch_centroid_distances(const float* d_q, uint32_t dim, const float* d_cent, uint32_t k_half,
+                                      double* d_dists, uint32_t* d_order, cudaStream_t st);
+cudaError_t launch_da_only(const double* d1, const uint32_t* o1, const double* d2, const uint32_t* o2,
+                           uint32_t k_half, const uint32_t* cell_size, uint64_t target, uint32_t* cells,
+                           uint32_t* ncells, double* sums, uint64_t* cum, cudaStream_t st);
+
+// ------------------------------------------------------------------ select
+// Cluster kernel: each cluster of CS CTAs owns one query; CTA r owns id slabs
+// r, r+CS, ... of CH ids with u8 collision counters in shared memory.
+// Counting (query.cpp:229-239), then the global top-m by (score desc, id asc)
+// (query.cpp:242-260) via a per-slab score histogram exchanged over DSMEM, a
+// threshold score T and an id-ordered tie quota per slab.
+struct SelectArgs {
+    const uint32_t* ids;       // ns x n   (IMI ids, ascending within a cell)
+    const uint32_t* slab_off;  // ns x K x (nslabs + 1): start of slab j inside each cell
+    const uint32_t* cells;     // nq x ns x cells_cap
+    const uint32_t* ncells;    // nq x ns
+    uint32_t cells_cap;
+    uint64_t n;
+    uint32_t ns, K, nslabs, CH, rounds, CS;
+    uint64_t m;
+    uint32_t* cands;      // nq x m (ascending ids)
+    uint8_t* scores_dbg;  // optional nq x n
+};
+struct SelectConfig {
+    uint32_t CS, CH, nslabs, rounds;
+    size_t smem;
+};
+SelectConfig plan_select(uint64_t n, uint32_t ns, int cluster_size);
+cudaError_t launch_select(const SelectArgs& a, const SelectConfig& cfg, uint64_t nq, cudaStream_t st);
+cudaError_t launch_slab_offsets(const uint32_t* cell_off, const uint32_t* ids, uint64_t n, uint32_t ns,
+                                uint32_t K, uint32_t CH, uint32_t nslabs, uint32_t* slab_off,
+                                cudaStream_t st);
+
+// ------------------------------------------------------------------ rerank
+// Exact fp64 re-rank of the candidate rows (query.cpp:159-197) with a
+// warp-level (dist, id) top-k; k > 32 takes a generic selection path.
+struct RerankArgs {
+    const float* data;  // n x d
+    uint64_t n;
+    uint32_t d;
+    const float* queries;   // nq x d
+    const uint32_t* cands;  // nq x m
+    uint64_t m;
+    uint32_t k;
+    uint32_t* out_ids;    // nq x k
+    double* out_dists;    // nq x k
+    double* all_d;        // generic path scratch nq x m
+    uint32_t* all_id;     // generic path scratch nq x m
+};
+cudaError_t launch_rerank(const RerankArgs& a, uint64_t nq, cudaStream_t st);
+
+// ------------------------------------------------------------------- build
+cudaError_t launch_cell_sizes(const uint32_t* cell_off, uint32_t ns, uint32_t K, uint32_t* cell_size,
+                              cudaStream_t st);
+cudaError_t launch_check_finite(const float* data, uint64_t count, int* flag, cudaStream_t st);
+
+}  // namespace suco_gpu

@@ -1,0 +1,240 @@
+// Stage 3 of the query path: exact re-rank of the candidate rows and top-k
+// (query.cpp:159-197): squared distance with the reference's 4-accumulator
+// fp64 kernel over the full d, top-k by (squared distance, id), sqrt last.
+//
+// One CTA (8 warps) per query; the query row is staged once as doubles in
+// shared memory. A warp re-ranks 8 candidate rows per step: the 8 rows are
+// gathered with coalesced 16-byte loads (one 512-byte row per warp-load at
+// d = 128) into a padded shared tile, then lane (r, a) = (lane/4, lane%4)
+// folds accumulator a of row r in index order — exactly the reference's
+// acc0..acc3 chains — and the four partials combine as (a0+a1)+(a2+a3).
+// The tile stride of 132 floats makes both the row stores and the strided
+// chain reads bank-conflict free. Each warp keeps a sorted top-k (k <= 32)
+// in registers, one entry per lane; warps merge through shared memory.
+// k > 32 writes every (dist, id) to scratch and a second kernel selects.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace suco_gpu {
+namespace {
+
+constexpr uint32_t kWarps = 8;
+constexpr uint32_t kThreads = 32 * kWarps;
+constexpr uint32_t kRows = 8;     // rows per warp step
+constexpr uint32_t kChunk = 128;  // dims per staged chunk
+constexpr uint32_t kStride = 132; // padded tile row (floats)
+constexpr uint32_t kFull = 0xffffffffu;
+
+__device__ __forceinline__ float4 ld_stream4(const float* p) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p));
+    return v;
+}
+
+// Inserts (d, id) into the warp's sorted list (lane i holds entry i, k <= 32).
+__device__ __forceinline__ void warp_insert(double d, uint32_t id, double& ld, uint32_t& lid, uint32_t k,
+                                            uint32_t lane) {
+    const double wd = __shfl_sync(kFull, ld, k - 1);
+    const uint32_t wi = __shfl_sync(kFull, lid, k - 1);
+    if (!dist_id_less(d, id, wd, wi)) return;  // warp-uniform
+    const bool less = lane < k && dist_id_less(ld, lid, d, id);
+    const uint32_t pos = __popc(__ballot_sync(kFull, less));
+    const double ud = __shfl_up_sync(kFull, ld, 1);
+    const uint32_t ui = __shfl_up_sync(kFull, lid, 1);
+    if (lane > pos) {
+        ld = ud;
+        lid = ui;
+    } else if (lane == pos) {
+        ld = d;
+        lid = id;
+    }
+}
+
+template <bool VEC, bool GENERIC>
+__global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* qd = reinterpret_cast<double*>(smem);                                  // d
+    float* tile = reinterpret_cast<float*>(smem + ((a.d * 8 + 15) / 16) * 16);     // warps x rows x stride
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint64_t q = blockIdx.x;
+    const float* query = a.queries + q * a.d;
+    for (uint32_t i = tid; i < a.d; i += kThreads) qd[i] = static_cast<double>(query[i]);
+    __syncthreads();
+
+    float* wt = tile + warp * kRows * kStride;
+    const uint32_t r = lane >> 2, acc_i = lane & 3u;
+    const uint32_t main4 = a.d & ~3u;  // dims covered by the four chains
+    const uint32_t* cands = a.cands + q * a.m;
+    double ld = kInf;
+    uint32_t lid = 0xffffffffu;
+
+    for (uint64_t base = static_cast<uint64_t>(warp) * kRows; base < a.m; base += kRows * kWarps) {
+        // candidate ids of the 8 rows (lanes 0..7 load, broadcast)
+        uint32_t my_id = 0;
+        if (lane < kRows && base + lane < a.m) my_id = __ldg(cands + base + lane);
+        uint32_t rid[kRows];
+#pragma unroll
+        for (uint32_t j = 0; j < kRows; ++j) rid[j] = __shfl_sync(kFull, my_id, j);
+        const uint32_t nrows = static_cast<uint32_t>(min_u64(kRows, a.m - base));
+        double acc = 0.0;
+        for (uint32_t c0 = 0; c0 < a.d; c0 += kChunk) {
+            const uint32_t cl = min(kChunk, a.d - c0);
+            if constexpr (VEC) {
+                float4 v[kRows];
+#pragma unroll
+                for (uint32_t j = 0; j < kRows; ++j) {
+                    if (j < nrows && 4 * lane < cl) v[j] = ld_stream4(a.data + static_cast<uint64_t>(rid[j]) * a.d + c0 + 4 * lane);
+                }
+#pragma unroll
+                for (uint32_t j = 0; j < kRows; ++j) {
+                    if (j < nrows && 4 * lane < cl) *reinterpret_cast<float4*>(wt + j * kStride + 4 * lane) = v[j];
+                }
+            } else {
+#pragma unroll
+                for (uint32_t j = 0; j < kRows; ++j) {
+                    if (j < nrows) {
+                        const float* src = a.data + static_cast<uint64_t>(rid[j]) * a.d + c0;
+                        for (uint32_t e = lane; e < cl; e += 32) wt[j * kStride + e] = __ldg(src + e);
+                    }
+                }
+            }
+            __syncwarp();
+            if (r < nrows) {
+                const float* row = wt + r * kStride;
+                // chain acc_i over global dims c0 + 4t + acc_i < main4, in order
+                const uint32_t lim = main4 > c0 ? min(cl, main4 - c0) : 0u;
+#pragma unroll 8
+                for (uint32_t e = acc_i; e < lim; e += 4) acc = __dadd_rn(acc, sqdiff_d(row[e], qd[c0 + e]));
+            }
+            __syncwarp();
+        }
+        // tail dims (d % 4) fold into acc0 after its main chain (core.hpp:79-82)
+        if (acc_i == 0 && r < nrows && main4 < a.d) {
+            const float* src = a.data + static_cast<uint64_t>(rid[r]) * a.d;
+            for (uint32_t g = main4; g < a.d; ++g) acc = __dadd_rn(acc, sqdiff_d(__ldg(src + g), qd[g]));
+        }
+        const double a1 = __shfl_down_sync(kFull, acc, 1);
+        const double a2 = __shfl_down_sync(kFull, acc, 2);
+        const double a3 = __shfl_down_sync(kFull, acc, 3);
+        const double dist = __dadd_rn(__dadd_rn(acc, a1), __dadd_rn(a2, a3));  // valid on lanes 4r
+        if constexpr (GENERIC) {
+            if (acc_i == 0 && r < nrows) {
+                a.all_d[q * a.m + base + r] = dist;
+                a.all_id[q * a.m + base + r] = rid[r];
+            }
+        } else {
+#pragma unroll
+            for (uint32_t j = 0; j < kRows; ++j) {
+                const double dj = __shfl_sync(kFull, dist, 4 * j);
+                if (j < nrows) warp_insert(dj, rid[j], ld, lid, a.k, lane);
+            }
+        }
+    }
+    if constexpr (!GENERIC) {
+        // merge the 8 warp lists through shared memory (reuse the tile area)
+        __syncthreads();
+        double* md = reinterpret_cast<double*>(tile);
+        uint32_t* mi = reinterpret_cast<uint32_t*>(md + kWarps * 32);
+        md[warp * 32 + lane] = ld;
+        mi[warp * 32 + lane] = lid;
+        __syncthreads();
+        if (warp == 0) {
+            for (uint32_t w = 1; w < kWarps; ++w) {
+                for (uint32_t i = 0; i < a.k; ++i) {
+                    const double dv = md[w * 32 + i];
+                    if (dv == kInf) break;
+                    warp_insert(dv, mi[w * 32 + i], ld, lid, a.k, lane);
+                }
+            }
+            if (lane < a.k) {
+                a.out_ids[q * a.k + lane] = lid;
+                a.out_dists[q * a.k + lane] = __dsqrt_rn(ld);
+            }
+        }
+    }
+}
+
+// k > 32: k rounds of "smallest (dist, id) strictly after the previous pick"
+// over the m scored candidates of one query; (dist, id) is a strict total
+// order so this reproduces nth_element + sort (query.cpp:185-189).
+__global__ void __launch_bounds__(256) topk_generic_kernel(RerankArgs a) {
+    __shared__ double sd[8];
+    __shared__ uint32_t si[8];
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint64_t q = blockIdx.x;
+    const double* dd = a.all_d + q * a.m;
+    const uint32_t* ii = a.all_id + q * a.m;
+    double pd = -1.0;
+    uint32_t pi = 0;
+    for (uint32_t r = 0; r < a.k; ++r) {
+        double bd = kInf;
+        uint32_t bi = 0xffffffffu;
+        for (uint64_t c = tid; c < a.m; c += 256) {
+            const double d = dd[c];
+            const uint32_t i = ii[c];
+            if (dist_id_less(pd, pi, d, i) && dist_id_less(d, i, bd, bi)) {
+                bd = d;
+                bi = i;
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double od = __shfl_xor_sync(kFull, bd, off);
+            const uint32_t oi = __shfl_xor_sync(kFull, bi, off);
+            if (dist_id_less(od, oi, bd, bi)) {
+                bd = od;
+                bi = oi;
+            }
+        }
+        if (lane == 0) {
+            sd[warp] = bd;
+            si[warp] = bi;
+        }
+        __syncthreads();
+        bd = sd[0];
+        bi = si[0];
+        for (int w = 1; w < 8; ++w) {
+            if (dist_id_less(sd[w], si[w], bd, bi)) {
+                bd = sd[w];
+                bi = si[w];
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            a.out_ids[q * a.k + r] = bi;
+            a.out_dists[q * a.k + r] = __dsqrt_rn(bd);
+        }
+        pd = bd;
+        pi = bi;
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_rerank(const RerankArgs& a, uint64_t nq, cudaStream_t st) {
+    if (nq == 0) return cudaSuccess;
+    const size_t smem = ((a.d * 8 + 15) / 16) * 16 + static_cast<size_t>(kWarps) * kRows * kStride * 4;
+    const bool vec = (a.d % 4) == 0;
+    const bool generic = a.k > 32;
+    auto launch = [&](auto kern) -> cudaError_t {
+        if (smem > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            if (e != cudaSuccess) return e;
+        }
+        kern<<<static_cast<unsigned>(nq), kThreads, smem, st>>>(a);
+        return cudaGetLastError();
+    };
+    cudaError_t e;
+    if (vec) e = generic ? launch(rerank_kernel<true, true>) : launch(rerank_kernel<true, false>);
+    else e = generic ? launch(rerank_kernel<false, true>) : launch(rerank_kernel<false, false>);
+    if (e != cudaSuccess || !generic) return e;
+    topk_generic_kernel<<<static_cast<unsigned>(nq), 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace suco_gpu

@@ -1,0 +1,47 @@
+// Small device utilities used while uploading/building an index.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace suco_gpu {
+namespace {
+
+__global__ void cell_sizes_kernel(const uint32_t* cell_off, uint32_t ns, uint32_t K, uint32_t* cell_size) {
+    const uint64_t total = static_cast<uint64_t>(ns) * K;
+    for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t < total;
+         t += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t s = t / K, c = t % K;
+        const uint32_t* off = cell_off + s * (K + 1);
+        cell_size[t] = off[c + 1] - off[c];
+    }
+}
+
+// flag <- lowest index of a non-finite value (core.cpp:15-19 reports the index).
+__global__ void check_finite_kernel(const float* data, uint64_t count, unsigned long long* first_bad) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t bits = __float_as_uint(data[i]);
+        if ((bits & 0x7f800000u) == 0x7f800000u) atomicMin(first_bad, static_cast<unsigned long long>(i));
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_cell_sizes(const uint32_t* cell_off, uint32_t ns, uint32_t K, uint32_t* cell_size, cudaStream_t st) {
+    const uint64_t total = static_cast<uint64_t>(ns) * K;
+    const uint64_t blocks = min_u64((total + 255) / 256, 148ull * 8);
+    cell_sizes_kernel<<<static_cast<unsigned>(blocks ? blocks : 1), 256, 0, st>>>(cell_off, ns, K, cell_size);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_check_finite(const float* data, uint64_t count, int* flag, cudaStream_t st) {
+    // `flag` points at an unsigned long long initialised to ~0 by the caller
+    const uint64_t blocks = min_u64((count + 255) / 256, 148ull * 16);
+    check_finite_kernel<<<static_cast<unsigned>(blocks ? blocks : 1), 256, 0, st>>>(
+        data, count, reinterpret_cast<unsigned long long*>(flag));
+    return cudaGetLastError();
+}
+
+}  // namespace suco_gpu

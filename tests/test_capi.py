@@ -1,0 +1,85 @@
+"""CPU-side checks of the drop-in boundary: the C-ABI library loads, exports
+every entry point include/suco_b200.h declares, its host arithmetic matches
+the reference KATs, and compute calls fail loudly without a GPU."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+from test_oracle import CANDIDATE_KATS, COLLISION_KATS
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "suco_b200.h")).read()
+    return sorted(set(re.findall(r"\b(suco_\w+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2411_14754_b200 import _capi
+    lib = ctypes.CDLL(_capi.LIB_PATH)
+    syms = declared_symbols()
+    assert len(syms) >= 20
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+    assert sorted(_capi.EXPORTED) == syms
+
+
+def test_cpp_header_mirrors_every_c_entry_point():
+    hpp = open(os.path.join(ROOT, "include", "suco_b200.hpp")).read()
+    for s in declared_symbols():
+        assert s in hpp, s
+
+
+@pytest.mark.parametrize("alpha,n,want", COLLISION_KATS)
+def test_collision_count(suco, alpha, n, want):
+    assert suco.collision_count(alpha, n) == want
+
+
+@pytest.mark.parametrize("beta,n,k,want", CANDIDATE_KATS)
+def test_candidate_count(suco, beta, n, k, want):
+    assert suco.candidate_count(beta, n, k) == want
+
+
+def test_params_validation(suco):
+    suco.CollisionParams().validate(1000)
+    for bad in (0.0, -0.5, 1.5):
+        with pytest.raises(suco.ConfigError):
+            suco.CollisionParams(alpha=bad).validate(1000)
+        with pytest.raises(suco.ConfigError):
+            suco.CollisionParams(beta=bad).validate(1000)
+    with pytest.raises(suco.ConfigError):
+        suco.CollisionParams(k=0).validate(1000)
+    with pytest.raises(suco.ConfigError):
+        suco.CollisionParams(k=1001).validate(1000)
+    suco.CollisionParams(k=1000).validate(1000)
+
+
+def test_defaults_match_reference(suco):  # index.hpp:53-61, sc_linear.hpp:22-31
+    p = suco.IndexParams()
+    assert (p.num_subspaces, p.k_half, p.iterations, p.seed, int(p.mode)) == (8, 50, 10, 42, 0)
+    c = suco.CollisionParams()
+    assert (c.alpha, c.beta, c.k) == (0.05, 0.005, 50)
+
+
+def test_compute_fails_loudly_without_gpu(suco):
+    if suco.device_count() > 0:
+        pytest.skip("a GPU is visible")
+    with pytest.raises(suco.Error, match="no CUDA device"):
+        suco.rerank(np.zeros((4, 4), np.float32), np.zeros(4, np.float32), [0, 1], 1)
+    with pytest.raises(suco.Error, match="no CUDA device"):
+        suco.build_index(np.zeros((100, 8), np.float32), suco.IndexParams(num_subspaces=2, k_half=4))
+
+
+def test_contract_checks_precede_device_use(suco):
+    """Argument validation happens on the host in the reference's order, GPU or not."""
+    with pytest.raises(suco.ContractError):
+        suco.rerank(np.zeros((4, 4), np.float32), np.zeros(3, np.float32), [0, 1], 1)
+    with pytest.raises(suco.ContractError):
+        suco.centroid_distances([1.0], [0.0, 1.0], 0)
+    with pytest.raises(suco.ConfigError):
+        suco.kmeans(np.zeros((10, 2), np.float32), 11, 5, 1)
+    with pytest.raises(suco.ContractError):
+        suco.build_imi([0, 1], [0, 2], 2)

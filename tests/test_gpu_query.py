@@ -1,0 +1,277 @@
+"""GPU parity of the query path against the oracle and the reference's golden outputs.
+
+Bar (BASELINE.json north_star): identical retrieved cells, SC-scores, candidate
+sets and top-k ids; distances bit-identical here (stricter than the stated
+1e-5 relative tolerance, which TOL below records for the record).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5  # north_star tolerance on distances; every check below is exact equality
+
+
+def make_cd(d):
+    d = np.asarray(d, np.float64)
+    return d, np.array(sorted(range(len(d)), key=lambda i: (d[i], i)), np.uint32)
+
+
+def cells_equal(got, c1, c2, cum, sums):
+    assert len(got) == len(c1)
+    assert [g.c1 for g in got] == c1.tolist()
+    assert [g.c2 for g in got] == c2.tolist()
+    assert [g.cumulative for g in got] == cum.tolist()
+    assert np.array_equal(np.array([g.sum_dist for g in got], np.float64), sums)
+
+
+# ------------------------------------------------------------ stage: centroids
+def test_centroid_distances(gpu):
+    g = golden("centroid_distances.npz")
+    d, o = gpu.centroid_distances(g["q"], g["cent"], 50)
+    assert np.array_equal(d, g["dists"]) and np.array_equal(o, g["order"])
+    d, o = gpu.centroid_distances([2.0], [0.0, 3.0], 2)  # test_query.cpp:53-69
+    assert d.tolist() == [2.0, 1.0] and o.tolist() == [1, 0]
+    assert gpu.centroid_distances([2.0], [1.0, 3.0], 2)[1].tolist() == [0, 1]
+    with pytest.raises(gpu.ContractError):
+        gpu.centroid_distances([2.0], [0.0, 3.0], 3)
+
+
+@pytest.mark.parametrize("k,h", [(50, 8), (64, 6), (100, 30), (7, 3), (300, 5)])
+def test_centroid_distances_vs_oracle(gpu, oracle, k, h):
+    rng = np.random.default_rng(k * 31 + h)
+    cent = rng.integers(0, 6, size=(k, h)).astype(np.float32)  # coarse grid: many exact ties
+    q = rng.integers(0, 6, size=h).astype(np.float32)
+    d1, o1 = gpu.centroid_distances(q, cent, k)
+    d2, o2 = oracle.centroid_distances(q, cent, k)
+    assert np.array_equal(d1, d2) and np.array_equal(o1, o2)
+
+
+# ------------------------------------------------------------ stage: traversal
+def test_traversal_hand_fixture(gpu, oracle):  # test_query.cpp:71-88
+    off = oracle.build_imi([0, 0, 1, 1], [0, 1, 0, 1], 2)[0]
+    r = gpu.dynamic_activation(0.75, 4, make_cd([0.2, 0.4]), make_cd([0.5, 0.8]), off)
+    assert [(c.c1, c.c2, c.cumulative) for c in r] == [(0, 0, 1), (1, 0, 2), (0, 1, 3)]
+    assert [c.sum_dist for c in r] == [0.2 + 0.5, 0.4 + 0.5, 0.2 + 0.8]
+    r = gpu.dynamic_activation(1.0, 4, make_cd([0.4, 0.2]), make_cd([0.5, 0.8]), off)  # :90-103
+    assert (r[0].c1, r[0].c2) == (1, 0) and r[-1].cumulative == 4 and len(r) == 4
+
+
+def test_traversal_golden(gpu):
+    """56 random instances incl. quantised ties: identical to the reference's DA."""
+    g = golden("traversal.npz")
+    for i in range(int(g["count"][0])):
+        k, n, alpha = g[f"t{i}_meta"]
+        got = gpu.dynamic_activation(alpha, int(n), (g[f"t{i}_d1"], g[f"t{i}_o1"]), (g[f"t{i}_d2"], g[f"t{i}_o2"]),
+                                     g[f"t{i}_off"])
+        cells_equal(got, g[f"t{i}_c1"], g[f"t{i}_c2"], g[f"t{i}_cum"], g[f"t{i}_sums"])
+
+
+@pytest.mark.parametrize("k_half,n,alpha,quant", [(33, 3000, 0.2, True), (100, 20000, 0.05, False),
+                                                  (200, 5000, 0.3, True), (300, 9000, 0.02, False),
+                                                  (1024, 200000, 0.005, False)])
+def test_traversal_vs_oracle(gpu, oracle, k_half, n, alpha, quant):
+    rng = np.random.default_rng(k_half + n)
+
+    def cd():
+        d = (rng.integers(0, 10, k_half) * 0.1) if quant else rng.random(k_half)
+        return make_cd(d)
+
+    off = oracle.build_imi(rng.integers(0, k_half, n), rng.integers(0, k_half, n), k_half)[0]
+    cd1, cd2 = cd(), cd()
+    got = gpu.dynamic_activation(alpha, n, cd1, cd2, off)
+    want = oracle.traverse(0, alpha, n, cd1[0], cd1[1], cd2[0], cd2[1], k_half, off)
+    cells_equal(got, *want)
+    assert got[-1].cumulative >= gpu.collision_count(alpha, n)
+
+
+def test_traversal_validation(gpu, oracle):  # test_query.cpp:175-186
+    rng = np.random.default_rng(5)
+    off = oracle.build_imi(rng.integers(0, 4, 20), rng.integers(0, 4, 20), 4)[0]
+    cd1, cd2 = make_cd(rng.random(4)), make_cd(rng.random(4))
+    for bad_alpha in (0.0, 1.5):
+        with pytest.raises(gpu.ContractError):
+            gpu.dynamic_activation(bad_alpha, 20, cd1, cd2, off)
+    with pytest.raises(gpu.ContractError):
+        gpu.dynamic_activation(0.5, 21, cd1, cd2, off)
+    with pytest.raises(gpu.ContractError):
+        gpu.dynamic_activation(0.5, 20, make_cd(rng.random(3)), cd2, off)
+
+
+# ------------------------------------------------------------ stage: rerank
+def test_rerank_golden(gpu):
+    g = golden("rerank.npz")
+    for j in range(3):
+        r = gpu.rerank(g["data"], g["queries"][j], g["cands"], 15)
+        assert [x.id for x in r] == g[f"ids{j}"].tolist()
+        assert np.array_equal(np.array([x.distance for x in r]), g[f"dists{j}"])
+
+
+@pytest.mark.parametrize("n,d,m,k", [(500, 128, 300, 10), (700, 22, 500, 7), (300, 3, 200, 5), (400, 960, 130, 32),
+                                     (900, 96, 800, 40), (64, 16, 64, 64), (2000, 8, 1500, 1)])
+def test_rerank_vs_oracle(gpu, oracle, n, d, m, k):
+    rng = np.random.default_rng(n + d)
+    data = rng.integers(0, 4, size=(n, d)).astype(np.float32)  # coarse values: distance ties
+    q = rng.integers(0, 4, size=d).astype(np.float32)
+    cands = rng.permutation(n)[:m].astype(np.uint32)
+    r = gpu.rerank(data, q, cands, k)
+    ids, dd = oracle.rerank(data, q, cands, k)
+    assert [x.id for x in r] == ids.tolist()
+    assert np.array_equal(np.array([x.distance for x in r]), dd)
+
+
+def test_rerank_validation(gpu):  # test_query.cpp:207-213
+    g = golden("rerank.npz")
+    with pytest.raises(gpu.ContractError):
+        gpu.rerank(g["data"], g["queries"][0], [1, 2, 3], 4)
+    with pytest.raises(gpu.ContractError):
+        gpu.rerank(g["data"], g["queries"][0], [1, 2, 3], 0)
+    with pytest.raises(gpu.ContractError):
+        gpu.rerank(g["data"], g["queries"][0], [1, 200], 1)
+    with pytest.raises(gpu.ContractError):
+        gpu.rerank(g["data"], np.zeros(6, np.float32), [1, 2, 3], 2)
+
+
+# ------------------------------------------------------------ end to end
+def test_knn_golden_small(gpu):
+    g = golden("e2e_small.npz")
+    idx = gpu.load_index(g["index"].tobytes(), g["base"])
+    assert idx.serialize() == g["index"].tobytes()
+    for tag in ("p0", "p1", "p2"):
+        a, b, k = g[f"{tag}_params"]
+        ids, d = idx.knn_query_batch(g["queries"], gpu.CollisionParams(a, b, int(k)))
+        assert np.array_equal(ids, g[f"{tag}_ids"]), tag
+        assert np.array_equal(d, g[f"{tag}_dists"]), tag
+        assert np.allclose(d, g[f"{tag}_dists"], rtol=TOL, atol=0)
+
+
+def test_intermediates_golden(gpu):
+    g = golden("e2e_small.npz")
+    idx = gpu.load_index(g["index"].tobytes(), g["base"])
+    scores, cands, cps, cum = idx.query_intermediates(g["queries"][0], gpu.CollisionParams(0.05, 0.05, 10))
+    assert np.array_equal(scores, g["scores_q0"])
+    assert np.array_equal(cands, g["cands_q0"])
+    assert np.array_equal(cps, g["cells_q0"]) and np.array_equal(cum, g["cum_q0"])
+    assert int(scores.sum()) == int(cum.sum())  # each retrieved id scores once per subspace
+
+
+def test_knn_golden_shuffled(gpu):
+    g = golden("e2e_shuffled.npz")
+    idx = gpu.load_index(g["index"].tobytes(), g["base"])
+    a, b, k = g["params"]
+    ids, d = idx.knn_query_batch(g["queries"], gpu.CollisionParams(a, b, int(k)))
+    assert np.array_equal(ids, g["ids"]) and np.array_equal(d, g["dists"])
+
+
+CASES = {
+    # name: (n, d, clusters, lo, hi, sigma, quant, ns, k_half, iters, mode, [(alpha, beta, k)])
+    "sift_like": (6000, 32, 30, 20, 140, 18, True, 4, 16, 4, 0, [(0.05, 0.005, 10), (0.02, 0.05, 50), (0.3, 0.001, 1)]),
+    "float": (4000, 24, 20, 0, 1, 0.05, False, 3, 12, 3, 1, [(0.05, 0.01, 10), (0.5, 0.2, 33)]),
+    "ns16": (3000, 64, 10, 0, 100, 8, False, 16, 6, 3, 0, [(0.05, 0.01, 10), (0.1, 0.004, 12)]),
+    "ns40": (1200, 80, 10, 0, 100, 8, True, 40, 3, 2, 0, [(0.05, 0.05, 10)]),
+    "tiny_touch": (2500, 16, 8, 0, 50, 3, False, 2, 8, 3, 0, [(0.0005, 0.4, 10), (0.001, 1.0, 25)]),
+}
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_knn_vs_oracle(gpu, oracle, case):
+    n, d, cl, lo, hi, sig, quant, ns, kh, it, mode, plist = CASES[case]
+    full = oracle.clustered(n + 40, d, cl, 1000 + n, lo, hi, sig, quant)
+    base, qs = oracle.hold_out(full, 40, 1001 + n)
+    oidx = oracle.build_index(base, ns, kh, it, 42, mode)
+    idx = gpu.load_index(oidx.serialize(), base)
+    for a, b, k in plist:
+        ids, dd = idx.knn_query_batch(qs, gpu.CollisionParams(a, b, k))
+        oi, od, _ = oidx.knn_query_batch(base, qs, a, b, k)
+        assert np.array_equal(ids, oi), (case, a, b, k)
+        assert np.array_equal(dd, od), (case, a, b, k)
+    for qi in (0, 7):
+        a, b, k = plist[0]
+        s1, c1, p1, u1 = idx.query_intermediates(qs[qi], gpu.CollisionParams(a, b, k))
+        s2, c2, p2, u2 = oidx.query_intermediates(base, qs[qi], a, b, k)
+        assert np.array_equal(s1, s2) and np.array_equal(c1, c2)
+        assert np.array_equal(p1, p2) and np.array_equal(u1, u2)
+
+
+def test_exhaustive_degeneracy(gpu, oracle, ref):
+    """alpha = beta = 1 equals exact kNN (test_query.cpp:216-238, acceptance.cpp:87-136)."""
+    data = oracle.clustered(300, 16, 4, 19, 0.0, 20.0, 2.0, False)
+    qs = oracle.uniform(5, 16, 20, 0.0, 20.0)
+    idx = gpu.load_index(oracle.build_index(data, 4, 5, 3, 42, 0).serialize(), data)
+    ids, dd = idx.knn_query_batch(qs, gpu.CollisionParams(1.0, 1.0, 10))
+    for qi in range(5):
+        ei, ed = ref.exact_knn(data, qs[qi], 10)
+        assert np.array_equal(ids[qi], ei) and np.array_equal(dd[qi], ed)
+
+
+def test_self_query_returns_itself(gpu, oracle):  # test_query.cpp:262-282
+    data = oracle.clustered(400, 16, 4, 31, 0.0, 40.0, 3.0, False)
+    idx = gpu.load_index(oracle.build_index(data, 4, 8, 4, 42, 0).serialize(), data)
+    ids, dd = idx.knn_query_batch(data[[0, 137, 399]], gpu.CollisionParams(0.1, 0.05, 5))
+    for row, pid in enumerate((0, 137, 399)):
+        assert dd[row, 0] == 0.0 and ids[row, 0] <= pid
+
+
+@pytest.mark.parametrize("cluster", ["1", "2", "4", "16"])
+def test_cluster_sizes_and_multi_round(gpu, oracle, cluster, monkeypatch):
+    """Every cluster size, and the two-pass (rounds > 1) select, give identical results."""
+    monkeypatch.setenv("SUCO_CLUSTER", cluster)
+    n = 230000 if cluster == "1" else 60000  # CS = 1 and n > 200 KiB of counters: 2 rounds
+    full = oracle.clustered(n + 16, 8, 64, 7, 0, 100, 6, True)
+    base, qs = oracle.hold_out(full, 16, 8)
+    oidx = oracle.build_index(base, 2, 16, 2, 42, 0)
+    idx = gpu.load_index(oidx.serialize(), base)
+    for a, b, k in ((0.05, 0.005, 10), (0.01, 0.02, 20)):
+        ids, dd = idx.knn_query_batch(qs, gpu.CollisionParams(a, b, k))
+        oi, od, _ = oidx.knn_query_batch(base, qs, a, b, k)
+        assert np.array_equal(ids, oi) and np.array_equal(dd, od)
+    s1, c1, _, _ = idx.query_intermediates(qs[3], gpu.CollisionParams(0.05, 0.005, 10))
+    s2, c2, _, _ = oidx.query_intermediates(base, qs[3], 0.05, 0.005, 10)
+    assert np.array_equal(s1, s2) and np.array_equal(c1, c2)
+
+
+def test_device_batch_api(gpu):
+    torch = pytest.importorskip("torch")
+    g = golden("e2e_small.npz")
+    idx = gpu.load_index(g["index"].tobytes(), g["base"])
+    q = torch.from_numpy(g["queries"]).cuda()
+    ids = torch.empty((q.shape[0], 10), dtype=torch.int32, device="cuda")
+    dd = torch.empty((q.shape[0], 10), dtype=torch.float64, device="cuda")
+    s = torch.cuda.Stream()
+    idx.knn_query_batch_device(q.data_ptr(), q.shape[0], q.shape[1], gpu.CollisionParams(0.05, 0.05, 10),
+                               ids.data_ptr(), dd.data_ptr(), s.cuda_stream)
+    s.synchronize()
+    assert np.array_equal(ids.cpu().numpy().view(np.uint32), g["p0_ids"])
+    assert np.array_equal(dd.cpu().numpy(), g["p0_dists"])
+
+
+def test_query_errors(gpu):  # test_query.cpp:314-332, query.cpp:202-208
+    g = golden("e2e_small.npz")
+    idx = gpu.load_index(g["index"].tobytes(), g["base"])
+    with pytest.raises(gpu.ContractError):
+        idx.knn_query_batch(np.zeros((1, 31), np.float32), gpu.CollisionParams())
+    for bad in (gpu.CollisionParams(alpha=0.0), gpu.CollisionParams(beta=1.5), gpu.CollisionParams(k=0),
+                gpu.CollisionParams(k=10**7)):
+        with pytest.raises(gpu.ConfigError):
+            idx.knn_query_batch(g["queries"][:1], bad)
+    with pytest.raises(gpu.IncompatibilityError):
+        gpu.knn_query(idx, g["base"][:-1], g["queries"][0], gpu.CollisionParams())
+
+
+def test_load_errors(gpu):
+    g = golden("e2e_small.npz")
+    blob = g["index"].tobytes()
+    with pytest.raises(gpu.IncompatibilityError):
+        gpu.load_index(blob, g["base"][:-1])
+    with pytest.raises(gpu.IncompatibilityError):
+        gpu.load_index(blob, g["base"][:, :-1])
+    for cut in (0, 4, 40, len(blob) // 3, len(blob) - 1):
+        with pytest.raises(gpu.CorruptIndexError):
+            gpu.load_index(blob[:cut], g["base"])
+    bad = g["base"].copy()
+    bad[5, 3] = np.nan
+    with pytest.raises(gpu.ContractError, match="component 163 is not finite"):
+        gpu.load_index(blob, bad)
