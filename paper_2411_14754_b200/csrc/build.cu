@@ -1,20 +1,831 @@
-// Index build on the device — placeholder until the k-means kernels land.
+// Index build on the device: all 2*N_s (subspace, half) k-means jobs at once,
+// then the IMI of every subspace by a stable counting sort.
+//
+// Exactness plan (SURVEY §7 hard parts 1-3), per reference step:
+//   project          index.cpp:126-129   gather each half's dims into a
+//                                        contiguous n x h job array
+//   k-means++        kmeans.cpp:58-114   min_dist update: exact fp64 per point
+//                                        (parallel). total/prefix walk: a
+//                                        strictly serial fp64 fold on one lane
+//                                        (other lanes prefetch), or — when the
+//                                        job's data is integer-valued and small
+//                                        enough that every partial sum is an
+//                                        exact integer < 2^53 — a parallel
+//                                        scan, which then gives the identical
+//                                        doubles. The RNG stream is replayed on
+//                                        the host (mt19937_64(derive_seed)); the
+//                                        device consumes a uniform only when
+//                                        total > 0, exactly like the reference.
+//   assign           kmeans.cpp:19-54    exact fp64 distance to every centroid
+//                                        (centroids in smem as doubles), strict
+//                                        '<' so ties keep the lower id.
+//   update           kmeans.cpp:153-168  stable bucket sort by cluster, then one
+//                                        lane per (cluster, dim) folds the sum in
+//                                        point order; float(sum * (1/count)).
+//   repair           kmeans.cpp:172-188  farthest point from the stale centroid,
+//                                        strict '>' (lowest id on ties).
+//   build_imi        index.cpp:69-96     stable counting sort by c1*k + c2.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
 #include "build.h"
+#include "common.cuh"
 
 namespace suco_gpu {
+namespace {
 
-void build_index_device(const float*, uint64_t, uint32_t, const HostLayout&, const suco_index_params&, BuildOutputs&,
-                        cudaStream_t) {
-    raise(SUCO_ERR_INTERNAL, "GPU index build not implemented yet");
+#define BCUDA(x)                                                                                               \
+    do {                                                                                                       \
+        const cudaError_t e_ = (x);                                                                            \
+        if (e_ != cudaSuccess) raise(SUCO_ERR_INTERNAL, std::string("CUDA error '") + cudaGetErrorString(e_) + \
+                                                            "' in " #x);                                       \
+    } while (0)
+
+constexpr uint32_t kFull = 0xffffffffu;
+
+template <typename T>
+struct Dev {
+    T* p = nullptr;
+    size_t n = 0;
+    Dev() = default;
+    explicit Dev(size_t count) { alloc(count); }
+    void alloc(size_t count) {
+        release();
+        BCUDA(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+        n = count;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~Dev() { release(); }
+    Dev(const Dev&) = delete;
+    Dev& operator=(const Dev&) = delete;
+};
+
+struct KJob {
+    uint32_t h;
+    uint32_t pad;
+    uint64_t off;   // float offset of this job's n x h points
+    uint64_t coff;  // float offset of this job's k x h centroids
+};
+
+// ------------------------------------------------------------------ project
+__global__ void project_kernel(const float* __restrict__ data, uint64_t n, uint32_t d, const uint32_t* __restrict__ dims,
+                               const uint32_t* __restrict__ dim_off, const KJob* __restrict__ jobs, float* __restrict__ proj) {
+    const uint32_t j = blockIdx.y;
+    const KJob jb = jobs[j];
+    const uint32_t* dl = dims + dim_off[j];
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        const float* row = data + i * d;
+        float* out = proj + jb.off + i * jb.h;
+        for (uint32_t t = 0; t < jb.h; ++t) out[t] = row[dl[t]];
+    }
 }
 
-void kmeans_device_host_io(const float*, uint64_t, uint32_t, uint32_t, uint32_t, uint64_t, float*, uint32_t*, uint32_t*,
-                           uint32_t*) {
-    raise(SUCO_ERR_INTERNAL, "GPU kmeans not implemented yet");
+// integer certificate input: any non-integer value, and the largest |value|
+__global__ void int_check_kernel(const float* __restrict__ proj, const KJob* __restrict__ jobs, uint64_t n,
+                                 unsigned int* nonint, unsigned int* maxabs_bits) {
+    const uint32_t j = blockIdx.y;
+    const KJob jb = jobs[j];
+    const uint64_t cnt = n * jb.h;
+    bool bad = false;
+    float mx = 0.f;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < cnt; i += uint64_t(gridDim.x) * blockDim.x) {
+        const float v = proj[jb.off + i];
+        bad |= (v != truncf(v));
+        mx = fmaxf(mx, fabsf(v));
+    }
+    bad = __any_sync(kFull, bad);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
+    if ((threadIdx.x & 31) == 0) {
+        if (bad) atomicOr(nonint + j, 1u);
+        atomicMax(maxabs_bits + j, __float_as_uint(mx));  // non-negative floats order like their bits
+    }
 }
 
-void build_imi_host_io(const uint32_t*, const uint32_t*, uint64_t, uint32_t, uint64_t*, uint32_t*) {
-    raise(SUCO_ERR_INTERNAL, "GPU build_imi not implemented yet");
+// ---------------------------------------------------------------- k-means++
+__global__ void kpp_init_kernel(double* min_dist, uint8_t* chosen, uint64_t n, uint32_t J) {
+    const uint64_t total = n * J;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total; i += uint64_t(gridDim.x) * blockDim.x) {
+        min_dist[i] = kInf;
+        chosen[i] = 0;
+    }
+}
+
+// place(): centroid c <- point pick[j]  (kmeans.cpp:64-67)
+__global__ void copy_centroid_kernel(const float* proj, const KJob* jobs, const uint32_t* pick, uint32_t c, float* cent) {
+    const uint32_t j = blockIdx.x;
+    const KJob jb = jobs[j];
+    for (uint32_t t = threadIdx.x; t < jb.h; t += blockDim.x) {
+        cent[jb.coff + uint64_t(c) * jb.h + t] = proj[jb.off + uint64_t(pick[j]) * jb.h + t];
+    }
+}
+
+// place(): min_dist[i] = min(min_dist[i], D(x_i, x_pick)), chosen[pick] = 1  (kmeans.cpp:68-72)
+__global__ void kpp_update_kernel(const float* __restrict__ proj, const KJob* __restrict__ jobs, uint64_t n,
+                                  const uint32_t* __restrict__ pick, double* __restrict__ min_dist, uint8_t* chosen) {
+    __shared__ float src[64];
+    const uint32_t j = blockIdx.y;
+    const KJob jb = jobs[j];
+    const uint32_t p = pick[j];
+    const float* x = proj + jb.off;
+    const bool small = jb.h <= 64;
+    if (small) {
+        for (uint32_t t = threadIdx.x; t < jb.h; t += blockDim.x) src[t] = x[uint64_t(p) * jb.h + t];
+        __syncthreads();
+    }
+    const float* s = small ? src : x + uint64_t(p) * jb.h;
+    double* md = min_dist + uint64_t(j) * n;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        const double dist = sqdist4(x + i * jb.h, s, jb.h);
+        if (dist < md[i]) md[i] = dist;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) chosen[uint64_t(j) * n + p] = 1;
+}
+
+__device__ inline double block_sum_exact(double v, double* sh) {
+    // order-free: only used on certified integer-valued data (every partial sum exact)
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (lane == 0) sh[warp] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (uint32_t w = 0; w < nw; ++w) t += sh[w];
+    return t;
+}
+
+// Chooses the next seed of job blockIdx.x (kmeans.cpp:75-111); one CTA per job.
+// prefix[i] receives the running fold; pick is the first i with prefix > target.
+__global__ void __launch_bounds__(256) kpp_select_kernel(const float* proj, const KJob* jobs, uint64_t n, uint32_t c,
+                                                         const double* __restrict__ min_dist, const uint8_t* chosen,
+                                                         const uint8_t* exact, const double* uniforms, uint32_t kmax,
+                                                         uint32_t* used, uint32_t* pick, double* prefix_all, float* cent) {
+    __shared__ double buf[2][256];
+    __shared__ double shd[8];
+    __shared__ uint32_t shu[8];
+    __shared__ double s_total;
+    __shared__ uint32_t s_pick;
+    const uint32_t j = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const double* md = min_dist + uint64_t(j) * n;
+    double* prefix = prefix_all + uint64_t(j) * n;
+    if (exact[j]) {
+        // parallel exact prefix, tiles of 256 x 8 elements
+        double carry = 0.0;
+        for (uint64_t base = 0; base < n; base += 2048) {
+            double v[8];
+            double loc = 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint64_t i = base + tid * 8 + u;
+                v[u] = i < n ? md[i] : 0.0;
+                loc += v[u];
+            }
+            // block exclusive scan of loc
+            double x = loc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double y = __shfl_up_sync(kFull, x, o);
+                if (lane >= (uint32_t)o) x += y;
+            }
+            if (lane == 31) shd[warp] = x;
+            __syncthreads();
+            double wpre = 0.0, tot = 0.0;
+            for (uint32_t w = 0; w < 8; ++w) {
+                if (w < warp) wpre += shd[w];
+                tot += shd[w];
+            }
+            double run = carry + wpre + (x - loc);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint64_t i = base + tid * 8 + u;
+                run += v[u];
+                if (i < n) prefix[i] = run;
+            }
+            carry += tot;
+            __syncthreads();
+        }
+        if (tid == 0) s_total = carry;
+    } else if (warp == 0) {
+        // strictly serial left-to-right fold (kmeans.cpp:77, :83-84): lane 0 adds,
+        // the other lanes keep the next 256 values in flight
+        double run = 0.0;
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint64_t i = lane + 32u * u;
+            v[u] = i < n ? md[i] : 0.0;
+        }
+        int b = 0;
+        for (uint64_t base = 0; base < n; base += 256, b ^= 1) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) buf[b][lane + 32 * u] = v[u];
+            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint64_t i = base + 256 + lane + 32u * u;
+                v[u] = i < n ? md[i] : 0.0;
+            }
+            if (lane == 0) {
+                const uint32_t cnt = static_cast<uint32_t>(min_u64(256, n - base));
+                for (uint32_t t = 0; t < cnt; ++t) {
+                    run = __dadd_rn(run, buf[b][t]);
+                    prefix[base + t] = run;
+                }
+            }
+            __syncwarp();
+        }
+        if (lane == 0) s_total = run;
+    }
+    __syncthreads();
+    const double total = s_total;
+    uint32_t p = 0xffffffffu;  // "n" sentinel
+    if (total > 0.0) {
+        if (tid == 0) {
+            const double u = uniforms[uint64_t(j) * kmax + used[j]];
+            used[j] += 1;
+            const double target = __dmul_rn(u, total);
+            uint64_t lo = 0, hi = n;  // first index with prefix > target (prefix is non-decreasing)
+            while (lo < hi) {
+                const uint64_t mid = (lo + hi) >> 1;
+                if (prefix[mid] > target) hi = mid;
+                else lo = mid + 1;
+            }
+            s_pick = lo < n ? static_cast<uint32_t>(lo) : 0xffffffffu;
+        }
+        __syncthreads();
+        p = s_pick;
+        if (p == 0xffffffffu) {  // round-off overran the walk: last positive-weight point
+            uint32_t best = 0;
+            bool found = false;
+            for (uint64_t i = tid; i < n; i += blockDim.x) {
+                if (md[i] > 0.0) {
+                    best = static_cast<uint32_t>(i);
+                    found = true;
+                }
+            }
+            uint32_t key = found ? best + 1 : 0;
+            for (int o = 16; o > 0; o >>= 1) key = max(key, __shfl_xor_sync(kFull, key, o));
+            if (lane == 0) shu[warp] = key;
+            __syncthreads();
+            if (tid == 0) {
+                uint32_t k2 = 0;
+                for (int w = 0; w < 8; ++w) k2 = max(k2, shu[w]);
+                s_pick = k2 ? k2 - 1 : 0xffffffffu;
+            }
+            __syncthreads();
+            p = s_pick;
+        }
+    }
+    if (p == 0xffffffffu) {  // all remaining points coincide with chosen centroids: lowest unchosen id
+        const uint8_t* ch = chosen + uint64_t(j) * n;
+        uint32_t best = 0xffffffffu;
+        for (uint64_t i = tid; i < n; i += blockDim.x) {
+            if (!ch[i]) {
+                best = static_cast<uint32_t>(i);
+                break;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(kFull, best, o));
+        if (lane == 0) shu[warp] = best;
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t b2 = 0xffffffffu;
+            for (int w = 0; w < 8; ++w) b2 = min(b2, shu[w]);
+            s_pick = b2 == 0xffffffffu ? 0u : b2;
+        }
+        __syncthreads();
+        p = s_pick;
+    }
+    if (tid == 0) pick[j] = p;
+    const KJob jb = jobs[j];
+    for (uint32_t t = tid; t < jb.h; t += blockDim.x) cent[jb.coff + uint64_t(c) * jb.h + t] = proj[jb.off + uint64_t(p) * jb.h + t];
+}
+
+// ------------------------------------------------------------------- assign
+// nearest_centroid (kmeans.cpp:19-33) for every point of every job.
+template <int HB>
+__global__ void __launch_bounds__(256) assign_kernel(const float* __restrict__ proj, const KJob* __restrict__ jobs,
+                                                     uint64_t n, uint32_t k, const float* __restrict__ cent,
+                                                     uint32_t* __restrict__ assign) {
+    extern __shared__ __align__(16) double cs[];  // k x h centroids as doubles
+    const uint32_t j = blockIdx.y;
+    const KJob jb = jobs[j];
+    const uint32_t h = jb.h;
+    for (uint32_t t = threadIdx.x; t < k * h; t += blockDim.x) cs[t] = static_cast<double>(cent[jb.coff + t]);
+    __syncthreads();
+    const float* x = proj + jb.off;
+    uint32_t* as = assign + uint64_t(j) * n;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        double p[HB > 0 ? HB : 1];
+        if constexpr (HB > 0) {
+#pragma unroll
+            for (int t = 0; t < HB; ++t) p[t] = t < (int)h ? static_cast<double>(x[i * h + t]) : 0.0;
+        }
+        uint32_t best = 0;
+        double bd = kInf;
+        for (uint32_t c = 0; c < k; ++c) {
+            const double* cc = cs + c * h;
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            uint32_t t = 0;
+            if constexpr (HB > 0) {
+#pragma unroll
+                for (int tt = 0; tt + 4 <= HB; tt += 4) {
+                    if ((uint32_t)tt + 4 <= h) {
+                        double e0 = __dsub_rn(p[tt], cc[tt]), e1 = __dsub_rn(p[tt + 1], cc[tt + 1]);
+                        double e2 = __dsub_rn(p[tt + 2], cc[tt + 2]), e3 = __dsub_rn(p[tt + 3], cc[tt + 3]);
+                        a0 = __dadd_rn(a0, __dmul_rn(e0, e0));
+                        a1 = __dadd_rn(a1, __dmul_rn(e1, e1));
+                        a2 = __dadd_rn(a2, __dmul_rn(e2, e2));
+                        a3 = __dadd_rn(a3, __dmul_rn(e3, e3));
+                        t = tt + 4;
+                    }
+                }
+#pragma unroll
+                for (int tt = 0; tt < HB; ++tt) {
+                    if ((uint32_t)tt >= t && (uint32_t)tt < h) {
+                        const double e = __dsub_rn(p[tt], cc[tt]);
+                        a0 = __dadd_rn(a0, __dmul_rn(e, e));
+                    }
+                }
+            } else {
+                const float* xi = x + i * h;
+                for (; t + 4 <= h; t += 4) {
+                    double e0 = __dsub_rn((double)xi[t], cc[t]), e1 = __dsub_rn((double)xi[t + 1], cc[t + 1]);
+                    double e2 = __dsub_rn((double)xi[t + 2], cc[t + 2]), e3 = __dsub_rn((double)xi[t + 3], cc[t + 3]);
+                    a0 = __dadd_rn(a0, __dmul_rn(e0, e0));
+                    a1 = __dadd_rn(a1, __dmul_rn(e1, e1));
+                    a2 = __dadd_rn(a2, __dmul_rn(e2, e2));
+                    a3 = __dadd_rn(a3, __dmul_rn(e3, e3));
+                }
+                for (; t < h; ++t) {
+                    const double e = __dsub_rn((double)xi[t], cc[t]);
+                    a0 = __dadd_rn(a0, __dmul_rn(e, e));
+                }
+            }
+            const double dist = __dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3));
+            if (dist < bd) {
+                bd = dist;
+                best = c;
+            }
+        }
+        as[i] = best;
+    }
+}
+
+// ------------------------------------------------------- stable bucket sort
+// J independent problems of n keys < B; chunk = `chunk` consecutive items.
+__global__ void bsort_hist_kernel(const uint32_t* __restrict__ keys, uint64_t n, uint32_t B, uint32_t chunk,
+                                  uint32_t nch, uint32_t* __restrict__ counts, bool use_smem) {
+    extern __shared__ uint32_t hs[];
+    const uint32_t j = blockIdx.y, ch = blockIdx.x;
+    uint32_t* row = counts + (uint64_t(j) * nch + ch) * B;
+    if (use_smem) {
+        for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) hs[b] = 0;
+        __syncthreads();
+    }
+    const uint64_t lo = uint64_t(ch) * chunk, hi = min_u64(n, lo + chunk);
+    const uint32_t* kk = keys + uint64_t(j) * n;
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) atomicAdd(use_smem ? hs + kk[i] : row + kk[i], 1u);
+    if (use_smem) {
+        __syncthreads();
+        for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) row[b] = hs[b];
+    }
+}
+
+// per (job, bucket): exclusive prefix over chunks; totals per bucket
+__global__ void bsort_colscan_kernel(uint32_t* counts, uint32_t B, uint32_t nch, uint32_t J, uint32_t* totals) {
+    const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (t >= uint64_t(J) * B) return;
+    const uint32_t j = static_cast<uint32_t>(t / B), b = static_cast<uint32_t>(t % B);
+    uint32_t run = 0;
+    for (uint32_t ch = 0; ch < nch; ++ch) {
+        uint32_t* p = counts + (uint64_t(j) * nch + ch) * B + b;
+        const uint32_t v = *p;
+        *p = run;
+        run += v;
+    }
+    totals[t] = run;
+}
+
+// per job: offsets[b] = sum of totals below b; offsets[B] = n
+__global__ void bsort_offsets_kernel(const uint32_t* totals, uint32_t B, uint32_t* offsets) {
+    __shared__ uint32_t sh[32];
+    const uint32_t j = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t* tt = totals + uint64_t(j) * B;
+    uint32_t* off = offsets + uint64_t(j) * (B + 1);
+    uint32_t carry = 0;
+    for (uint32_t b0 = 0; b0 < B; b0 += blockDim.x) {
+        const uint32_t b = b0 + tid;
+        const uint32_t v = b < B ? tt[b] : 0;
+        uint32_t x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, x, o);
+            if (lane >= (uint32_t)o) x += y;
+        }
+        if (lane == 31) sh[warp] = x;
+        __syncthreads();
+        uint32_t wpre = 0, tot = 0;
+        for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) {
+            if (w < warp) wpre += sh[w];
+            tot += sh[w];
+        }
+        if (b < B) off[b] = carry + wpre + x - v;
+        carry += tot;
+        __syncthreads();
+    }
+    if (tid == 0) off[B] = carry;
+}
+
+// stable scatter: one warp walks its chunk in order; per-bucket running
+// counters start at offsets[b] + (items of bucket b in earlier chunks).
+__global__ void bsort_scatter_kernel(const uint32_t* __restrict__ keys, uint64_t n, uint32_t B, uint32_t chunk,
+                                     uint32_t nch, uint32_t* counts, const uint32_t* __restrict__ offsets,
+                                     uint32_t* __restrict__ perm, bool use_smem) {
+    extern __shared__ uint32_t run[];
+    const uint32_t j = blockIdx.y, ch = blockIdx.x, lane = threadIdx.x;
+    uint32_t* row = counts + (uint64_t(j) * nch + ch) * B;
+    const uint32_t* off = offsets + uint64_t(j) * (B + 1);
+    uint32_t* ctr = use_smem ? run : row;
+    for (uint32_t b = lane; b < B; b += 32) ctr[b] = off[b] + row[b];
+    __syncwarp();
+    const uint64_t lo = uint64_t(ch) * chunk, hi = min_u64(n, lo + chunk);
+    const uint32_t* kk = keys + uint64_t(j) * n;
+    uint32_t* pp = perm + uint64_t(j) * n;
+    for (uint64_t i0 = lo; i0 < hi; i0 += 32) {
+        const uint64_t i = i0 + lane;
+        const bool ok = i < hi;
+        const uint32_t key = ok ? kk[i] : 0xffffffffu;
+        const uint32_t peers = __match_any_sync(kFull, key);
+        const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+        const uint32_t base = ok ? ctr[key] : 0u;
+        __syncwarp();
+        if (ok) {
+            pp[base + rank] = static_cast<uint32_t>(i);
+            if (rank == 0) ctr[key] = base + __popc(peers);
+        }
+        __syncwarp();
+    }
+}
+
+// ------------------------------------------------------------------- update
+// sums[c][t] = serial fold over cluster c's points in id order (kmeans.cpp:155-161),
+// centroid = float(sum * (1 / count)) (kmeans.cpp:163-168); empty clusters untouched.
+__global__ void update_kernel(const float* __restrict__ proj, const KJob* __restrict__ jobs, uint64_t n, uint32_t k,
+                              const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ perm, float* cent) {
+    const uint32_t j = blockIdx.y;
+    const KJob jb = jobs[j];
+    const uint32_t h = jb.h;
+    const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (t >= uint64_t(k) * h) return;
+    const uint32_t c = static_cast<uint32_t>(t / h), dim = static_cast<uint32_t>(t % h);
+    const uint32_t* off = offsets + uint64_t(j) * (k + 1);
+    const uint32_t b = off[c], e = off[c + 1];
+    if (b == e) return;
+    const uint32_t* pp = perm + uint64_t(j) * n;
+    const float* x = proj + jb.off + dim;
+    double sum = 0.0;
+    uint32_t p = b;
+    for (; p + 8 <= e; p += 8) {
+        uint32_t id[8];
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) id[u] = __ldg(pp + p + u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldg(x + uint64_t(id[u]) * h);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sum = __dadd_rn(sum, static_cast<double>(v[u]));
+    }
+    for (; p < e; ++p) sum = __dadd_rn(sum, static_cast<double>(__ldg(x + uint64_t(__ldg(pp + p)) * h)));
+    const double inv = 1.0 / static_cast<double>(e - b);
+    cent[jb.coff + uint64_t(c) * h + dim] = __double2float_rn(__dmul_rn(sum, inv));
+}
+
+// ------------------------------------------------------------------- repair
+struct FarArgs {
+    uint32_t job, cluster;
+};
+
+// farthest point from the stale centroid, strict '>' => lowest id on ties
+__global__ void farthest_partial_kernel(const float* __restrict__ proj, const KJob* __restrict__ jobs, uint64_t n,
+                                        const float* __restrict__ cent, FarArgs fa, double* pd, uint32_t* pi) {
+    __shared__ double sd[8];
+    __shared__ uint32_t si[8];
+    const KJob jb = jobs[fa.job];
+    const float* stale = cent + jb.coff + uint64_t(fa.cluster) * jb.h;
+    const float* x = proj + jb.off;
+    double bd = -1.0;
+    uint32_t bi = 0xffffffffu;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        const double dist = sqdist4(x + i * jb.h, stale, jb.h);
+        if (dist > bd) {
+            bd = dist;
+            bi = static_cast<uint32_t>(i);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const double od = __shfl_xor_sync(kFull, bd, o);
+        const uint32_t oi = __shfl_xor_sync(kFull, bi, o);
+        if (od > bd || (od == bd && oi < bi)) {
+            bd = od;
+            bi = oi;
+        }
+    }
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        sd[warp] = bd;
+        si[warp] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w) {
+            if (sd[w] > bd || (sd[w] == bd && si[w] < bi)) {
+                bd = sd[w];
+                bi = si[w];
+            }
+        }
+        pd[blockIdx.x] = bd;
+        pi[blockIdx.x] = bi;
+    }
+}
+
+__global__ void farthest_final_kernel(const float* proj, const KJob* jobs, FarArgs fa, const double* pd,
+                                      const uint32_t* pi, uint32_t parts, float* cent) {
+    __shared__ uint32_t far;
+    if (threadIdx.x == 0) {
+        double bd = -1.0;
+        uint32_t bi = 0xffffffffu;
+        for (uint32_t b = 0; b < parts; ++b) {
+            if (pd[b] > bd || (pd[b] == bd && pi[b] < bi)) {
+                bd = pd[b];
+                bi = pi[b];
+            }
+        }
+        far = bi;
+    }
+    __syncthreads();
+    const KJob jb = jobs[fa.job];
+    for (uint32_t t = threadIdx.x; t < jb.h; t += blockDim.x) {
+        cent[jb.coff + uint64_t(fa.cluster) * jb.h + t] = proj[jb.off + uint64_t(far) * jb.h + t];
+    }
+}
+
+// ---------------------------------------------------------------------- IMI
+__global__ void cell_keys_kernel(const uint32_t* __restrict__ assign, uint64_t n, uint32_t k, uint32_t ns,
+                                 uint32_t* __restrict__ keys) {
+    const uint32_t s = blockIdx.y;
+    const uint32_t* a1 = assign + uint64_t(2 * s) * n;
+    const uint32_t* a2 = assign + uint64_t(2 * s + 1) * n;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        keys[uint64_t(s) * n + i] = a1[i] * k + a2[i];
+    }
+}
+
+// ==================================================================== host
+unsigned grid_for(uint64_t n, unsigned per = 256, unsigned cap = 148 * 8) {
+    const uint64_t b = (n + per - 1) / per;
+    return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(b, cap)));
+}
+
+// Stable bucket sort of J problems (keys < B) -> offsets J x (B+1), perm J x n.
+void bucket_sort(const uint32_t* keys, uint64_t n, uint32_t B, uint32_t J, uint32_t* offsets, uint32_t* perm,
+                 cudaStream_t st) {
+    uint64_t chunk = 2048;
+    const uint64_t budget = 16ull << 20;  // count-matrix entries per problem
+    if ((n + chunk - 1) / chunk * B > budget) chunk = ((n * B + budget - 1) / budget + 31) / 32 * 32;
+    const uint32_t nch = static_cast<uint32_t>((n + chunk - 1) / chunk);
+    const bool use_smem = uint64_t(B) * 4 <= 48 * 1024;
+    Dev<uint32_t> counts(uint64_t(J) * nch * B), totals(uint64_t(J) * B);
+    if (!use_smem) BCUDA(cudaMemsetAsync(counts.p, 0, counts.n * 4, st));
+    const dim3 g(nch, J);
+    bsort_hist_kernel<<<g, 256, use_smem ? B * 4 : 0, st>>>(keys, n, B, static_cast<uint32_t>(chunk), nch, counts.p,
+                                                            use_smem);
+    BCUDA(cudaGetLastError());
+    bsort_colscan_kernel<<<grid_for(uint64_t(J) * B, 256, 1u << 30), 256, 0, st>>>(counts.p, B, nch, J, totals.p);
+    BCUDA(cudaGetLastError());
+    bsort_offsets_kernel<<<J, 1024, 0, st>>>(totals.p, B, offsets);
+    BCUDA(cudaGetLastError());
+    bsort_scatter_kernel<<<g, 32, use_smem ? B * 4 : 0, st>>>(keys, n, B, static_cast<uint32_t>(chunk), nch, counts.p,
+                                                            offsets, perm, use_smem);
+    BCUDA(cudaGetLastError());
+    BCUDA(cudaStreamSynchronize(st));
+}
+
+void launch_assign(const float* proj, const KJob* jobs, uint64_t n, uint32_t k, uint32_t hmax, const float* cent,
+                   uint32_t* assign, uint32_t J, cudaStream_t st) {
+    const size_t smem = size_t(k) * hmax * 8;
+    if (smem > 200 * 1024) raise(SUCO_ERR_INTERNAL, "k x h centroid table exceeds shared memory");
+    const dim3 g(grid_for(n, 256, 148 * 4), J);
+    auto go = [&](auto kern) {
+        if (smem > 48 * 1024) BCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        kern<<<g, 256, smem, st>>>(proj, jobs, n, k, cent, assign);
+        BCUDA(cudaGetLastError());
+    };
+    if (hmax <= 8) go(assign_kernel<8>);
+    else if (hmax <= 16) go(assign_kernel<16>);
+    else if (hmax <= 32) go(assign_kernel<32>);
+    else go(assign_kernel<0>);
+}
+
+// The whole k-means of J jobs sharing n and k (kmeans.cpp:118-194).
+// proj/jobs/cent are device arrays; host_jobs mirrors jobs; seeds per job.
+void kmeans_jobs(const float* proj, const std::vector<KJob>& host_jobs, const KJob* jobs, uint64_t n, uint32_t k,
+                 uint32_t iterations, const std::vector<uint64_t>& seeds, float* cent, uint32_t* assign,
+                 std::vector<std::vector<uint32_t>>* repaired, cudaStream_t st) {
+    const uint32_t J = static_cast<uint32_t>(host_jobs.size());
+    uint32_t hmax = 0;
+    for (const KJob& jb : host_jobs) hmax = std::max(hmax, jb.h);
+
+    // integer certificate per job: integer values with n * h * (2 max|v|)^2 < 2^52
+    Dev<unsigned int> nonint(J), maxbits(J);
+    BCUDA(cudaMemsetAsync(nonint.p, 0, J * 4, st));
+    BCUDA(cudaMemsetAsync(maxbits.p, 0, J * 4, st));
+    int_check_kernel<<<dim3(grid_for(n * hmax, 256, 148 * 4), J), 256, 0, st>>>(proj, jobs, n, nonint.p, maxbits.p);
+    BCUDA(cudaGetLastError());
+    std::vector<unsigned int> hn(J), hm(J);
+    BCUDA(cudaMemcpyAsync(hn.data(), nonint.p, J * 4, cudaMemcpyDeviceToHost, st));
+    BCUDA(cudaMemcpyAsync(hm.data(), maxbits.p, J * 4, cudaMemcpyDeviceToHost, st));
+    BCUDA(cudaStreamSynchronize(st));
+    std::vector<uint8_t> exact(J);
+    for (uint32_t j = 0; j < J; ++j) {
+        float mx;
+        std::memcpy(&mx, &hm[j], 4);
+        const double span = 2.0 * double(mx);
+        exact[j] = (hn[j] == 0) && (double(n) * host_jobs[j].h * span * span < 4503599627370496.0);  // 2^52
+    }
+
+    // host replay of each job's RNG stream: first pick, then k-1 uniforms
+    std::vector<uint32_t> pick0(J);
+    std::vector<double> unis(uint64_t(J) * std::max<uint32_t>(k, 1));
+    for (uint32_t j = 0; j < J; ++j) {
+        Mt64 g(seeds[j]);
+        pick0[j] = static_cast<uint32_t>(g.uniform_below(n));
+        for (uint32_t c = 0; c + 1 < k; ++c) unis[uint64_t(j) * k + c] = g.uniform_unit();
+    }
+    Dev<double> min_dist(uint64_t(J) * n), prefix(uint64_t(J) * n), d_unis(unis.size());
+    Dev<uint8_t> chosen(uint64_t(J) * n), d_exact(J);
+    Dev<uint32_t> pick(J), used(J);
+    BCUDA(cudaMemcpyAsync(d_unis.p, unis.data(), unis.size() * 8, cudaMemcpyHostToDevice, st));
+    BCUDA(cudaMemcpyAsync(d_exact.p, exact.data(), J, cudaMemcpyHostToDevice, st));
+    BCUDA(cudaMemcpyAsync(pick.p, pick0.data(), J * 4, cudaMemcpyHostToDevice, st));
+    BCUDA(cudaMemsetAsync(used.p, 0, J * 4, st));
+    kpp_init_kernel<<<grid_for(n * J), 256, 0, st>>>(min_dist.p, chosen.p, n, J);
+    copy_centroid_kernel<<<J, 64, 0, st>>>(proj, jobs, pick.p, 0, cent);
+    BCUDA(cudaGetLastError());
+    const dim3 gu(grid_for(n, 256, 148 * 4), J);
+    for (uint32_t c = 1; c < k; ++c) {
+        kpp_update_kernel<<<gu, 256, 0, st>>>(proj, jobs, n, pick.p, min_dist.p, chosen.p);
+        kpp_select_kernel<<<J, 256, 0, st>>>(proj, jobs, n, c, min_dist.p, chosen.p, d_exact.p, d_unis.p, k, used.p,
+                                             pick.p, prefix.p, cent);
+        BCUDA(cudaGetLastError());
+    }
+    min_dist.release();
+    prefix.release();
+    chosen.release();
+
+    // Lloyd rounds
+    Dev<uint32_t> offsets(uint64_t(J) * (k + 1)), perm(uint64_t(J) * n);
+    std::vector<uint32_t> hoff(uint64_t(J) * (k + 1));
+    Dev<double> pd(148 * 4);
+    Dev<uint32_t> pi(148 * 4);
+    const unsigned fparts = grid_for(n, 256, 148 * 4);
+    for (uint32_t it = 0; it < iterations; ++it) {
+        launch_assign(proj, jobs, n, k, hmax, cent, assign, J, st);
+        bucket_sort(assign, n, k, J, offsets.p, perm.p, st);
+        update_kernel<<<dim3(grid_for(uint64_t(k) * hmax, 128, 1u << 30), J), 128, 0, st>>>(proj, jobs, n, k, offsets.p,
+                                                                                           perm.p, cent);
+        BCUDA(cudaGetLastError());
+        BCUDA(cudaMemcpyAsync(hoff.data(), offsets.p, hoff.size() * 4, cudaMemcpyDeviceToHost, st));
+        BCUDA(cudaStreamSynchronize(st));
+        for (uint32_t j = 0; j < J; ++j) {
+            for (uint32_t c = 0; c < k; ++c) {
+                if (hoff[uint64_t(j) * (k + 1) + c + 1] != hoff[uint64_t(j) * (k + 1) + c]) continue;
+                const FarArgs fa{j, c};
+                farthest_partial_kernel<<<fparts, 256, 0, st>>>(proj, jobs, n, cent, fa, pd.p, pi.p);
+                farthest_final_kernel<<<1, 64, 0, st>>>(proj, jobs, fa, pd.p, pi.p, fparts, cent);
+                BCUDA(cudaGetLastError());
+                if (repaired) (*repaired)[j].push_back(c);
+            }
+        }
+    }
+    launch_assign(proj, jobs, n, k, hmax, cent, assign, J, st);
+    BCUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace
+
+void build_index_device(const float* d_data, uint64_t n, uint32_t d, const HostLayout& L, const suco_index_params& p,
+                        BuildOutputs& out, cudaStream_t st) {
+    const uint32_t ns = L.ns, J = 2 * ns, k = p.k_half;
+    std::vector<KJob> hj(J);
+    std::vector<uint32_t> dim_off(J + 1), dims;
+    uint64_t off = 0, coff = 0;
+    uint32_t pos = 0;
+    for (uint32_t s = 0; s < ns; ++s) {
+        for (uint32_t half = 0; half < 2; ++half) {
+            const uint32_t j = 2 * s + half;
+            const uint32_t h = half == 0 ? L.h1(s) : L.h2(s);
+            hj[j] = KJob{h, 0, off, coff};
+            off += n * h;
+            coff += uint64_t(k) * h;
+            dim_off[j] = static_cast<uint32_t>(dims.size());
+            const uint32_t b = pos + (half == 0 ? 0 : L.split[s]);
+            for (uint32_t t = 0; t < h; ++t) dims.push_back(L.dims[b + t]);
+        }
+        pos += L.sizes[s];
+    }
+    dim_off[J] = static_cast<uint32_t>(dims.size());
+    Dev<KJob> jobs(J);
+    Dev<uint32_t> ddims(dims.size()), ddoff(J + 1);
+    Dev<float> proj(off), cent(coff);
+    BCUDA(cudaMemcpyAsync(jobs.p, hj.data(), J * sizeof(KJob), cudaMemcpyHostToDevice, st));
+    BCUDA(cudaMemcpyAsync(ddims.p, dims.data(), dims.size() * 4, cudaMemcpyHostToDevice, st));
+    BCUDA(cudaMemcpyAsync(ddoff.p, dim_off.data(), (J + 1) * 4, cudaMemcpyHostToDevice, st));
+    project_kernel<<<dim3(grid_for(n, 256, 148 * 4), J), 256, 0, st>>>(d_data, n, d, ddims.p, ddoff.p, jobs.p, proj.p);
+    BCUDA(cudaGetLastError());
+
+    std::vector<uint64_t> seeds(J);
+    for (uint32_t j = 0; j < J; ++j) seeds[j] = derive_seed(p.seed, j);  // index.cpp:131
+    Dev<uint32_t> assign(uint64_t(J) * n);
+    kmeans_jobs(proj.p, hj, jobs.p, n, k, p.iterations, seeds, cent.p, assign.p, nullptr, st);
+    proj.release();
+
+    // centroids to the host (tiny)
+    std::vector<float> hc(coff);
+    BCUDA(cudaMemcpyAsync(hc.data(), cent.p, coff * 4, cudaMemcpyDeviceToHost, st));
+    BCUDA(cudaStreamSynchronize(st));
+    out.cent1->assign(ns, {});
+    out.cent2->assign(ns, {});
+    for (uint32_t s = 0; s < ns; ++s) {
+        const KJob& a = hj[2 * s];
+        const KJob& b = hj[2 * s + 1];
+        (*out.cent1)[s].assign(hc.begin() + a.coff, hc.begin() + a.coff + uint64_t(k) * a.h);
+        (*out.cent2)[s].assign(hc.begin() + b.coff, hc.begin() + b.coff + uint64_t(k) * b.h);
+    }
+
+    // IMI per subspace: stable counting sort by c1 * k + c2 (index.cpp:69-96)
+    Dev<uint32_t> keys(uint64_t(ns) * n);
+    cell_keys_kernel<<<dim3(grid_for(n, 256, 148 * 4), ns), 256, 0, st>>>(assign.p, n, k, ns, keys.p);
+    BCUDA(cudaGetLastError());
+    bucket_sort(keys.p, n, k * k, ns, out.cell_off, out.ids, st);
+}
+
+void kmeans_device_host_io(const float* points, uint64_t n, uint32_t dim, uint32_t k, uint32_t iterations, uint64_t seed,
+                           float* centroids, uint32_t* assignments, uint32_t* repaired, uint32_t* num_repaired) {
+    cudaStream_t st = nullptr;
+    BCUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct StreamGuard {
+        cudaStream_t s;
+        ~StreamGuard() { cudaStreamDestroy(s); }
+    } sg{st};
+    std::vector<KJob> hj{KJob{dim, 0, 0, 0}};
+    Dev<KJob> jobs(1);
+    Dev<float> proj(n * dim), cent(uint64_t(k) * dim);
+    Dev<uint32_t> assign(n);
+    BCUDA(cudaMemcpyAsync(jobs.p, hj.data(), sizeof(KJob), cudaMemcpyHostToDevice, st));
+    BCUDA(cudaMemcpyAsync(proj.p, points, n * dim * 4, cudaMemcpyHostToDevice, st));
+    std::vector<std::vector<uint32_t>> rep(1);
+    kmeans_jobs(proj.p, hj, jobs.p, n, k, iterations, {seed}, cent.p, assign.p, &rep, st);
+    BCUDA(cudaMemcpyAsync(centroids, cent.p, uint64_t(k) * dim * 4, cudaMemcpyDeviceToHost, st));
+    BCUDA(cudaMemcpyAsync(assignments, assign.p, n * 4, cudaMemcpyDeviceToHost, st));
+    BCUDA(cudaStreamSynchronize(st));
+    if (num_repaired) *num_repaired = static_cast<uint32_t>(rep[0].size());
+    if (repaired) std::copy(rep[0].begin(), rep[0].end(), repaired);
+}
+
+void build_imi_host_io(const uint32_t* first, const uint32_t* second, uint64_t n, uint32_t k_half, uint64_t* offsets,
+                       uint32_t* ids) {
+    cudaStream_t st = nullptr;
+    BCUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct StreamGuard {
+        cudaStream_t s;
+        ~StreamGuard() { cudaStreamDestroy(s); }
+    } sg{st};
+    const uint64_t K = uint64_t(k_half) * k_half;
+    if (K > 0xFFFFFFFFull) raise(SUCO_ERR_CONTRACT, "build_imi: k_half^2 exceeds 32-bit cell ids");
+    Dev<uint32_t> assign(2 * std::max<uint64_t>(n, 1)), keys(std::max<uint64_t>(n, 1)), off(K + 1), perm(std::max<uint64_t>(n, 1));
+    if (n) {
+        BCUDA(cudaMemcpyAsync(assign.p, first, n * 4, cudaMemcpyHostToDevice, st));
+        BCUDA(cudaMemcpyAsync(assign.p + n, second, n * 4, cudaMemcpyHostToDevice, st));
+        cell_keys_kernel<<<dim3(grid_for(n, 256, 148 * 4), 1), 256, 0, st>>>(assign.p, n, k_half, 1, keys.p);
+        BCUDA(cudaGetLastError());
+        bucket_sort(keys.p, n, static_cast<uint32_t>(K), 1, off.p, perm.p, st);
+    } else {
+        BCUDA(cudaMemsetAsync(off.p, 0, (K + 1) * 4, st));
+    }
+    std::vector<uint32_t> o32(K + 1);
+    BCUDA(cudaMemcpyAsync(o32.data(), off.p, (K + 1) * 4, cudaMemcpyDeviceToHost, st));
+    if (n) BCUDA(cudaMemcpyAsync(ids, perm.p, n * 4, cudaMemcpyDeviceToHost, st));
+    BCUDA(cudaStreamSynchronize(st));
+    for (uint64_t c = 0; c <= K; ++c) offsets[c] = o32[c];
 }
 
 }  // namespace suco_gpu
