@@ -85,11 +85,11 @@ struct DeviceGuard {
     }
 };
 
-int cluster_size_from_env() {
+int cluster_size_from_env() {  // 0 = choose by occupancy (plan_select)
     const char* v = std::getenv("SUCO_CLUSTER");
-    if (!v) return 8;
+    if (!v) return 0;
     const int c = std::atoi(v);
-    return (c == 1 || c == 2 || c == 4 || c == 8 || c == 16) ? c : 8;
+    return (c >= 1 && c <= 16) ? c : 0;
 }
 
 }  // namespace
@@ -109,6 +109,7 @@ struct suco_gpu_index {
     DevBuf<uint32_t> ids;        // ns x n
     DevBuf<uint32_t> slab_off;   // ns x K x (nslabs+1)
     SelectConfig sel{};
+    float data_int_max = -1.f;  // integer certificate of the dataset (rerank fp32 path)
     // query scratch
     DevBuf<float> q;
     DevBuf<uint32_t> cells, ncells, cands, out_ids, all_id;
@@ -157,6 +158,17 @@ void upload_data(suco_gpu_index* x, const float* data, uint64_t n, uint32_t d) {
     x->data.reserve(n * d);
     CUDA_TRY(cudaMemcpyAsync(x->data.p, data, n * d * sizeof(float), cudaMemcpyHostToDevice, x->stream));
     check_finite_device(x->data.p, n * d, x->stream);
+    // integer certificate (values integral, |v| <= 2^20) for the exact fp32 rerank chains
+    DevBuf<unsigned int> st;
+    st.reserve(2);
+    unsigned int h[2] = {0, 0};
+    CUDA_TRY(cudaMemsetAsync(st.p, 0, 8, x->stream));
+    CUDA_TRY(launch_int_stats(x->data.p, n * d, st.p, x->stream));
+    CUDA_TRY(cudaMemcpyAsync(h, st.p, 8, cudaMemcpyDeviceToHost, x->stream));
+    CUDA_TRY(cudaStreamSynchronize(x->stream));
+    float mx;
+    std::memcpy(&mx, &h[1], 4);
+    x->data_int_max = (h[0] == 0 && mx <= 1048576.f) ? mx : -1.f;
 }
 
 // Layout + centroid tables on the device, from x->host.
@@ -330,6 +342,7 @@ void run_tile(suco_gpu_index* x, const float* d_q, uint64_t nt, uint64_t target,
     ra.k = k;
     ra.out_ids = d_ids;
     ra.out_dists = d_dists;
+    ra.data_int_max = x->data_int_max;
     if (k > 32) {
         x->all_d.reserve(nt * m);
         x->all_id.reserve(nt * m);
@@ -661,7 +674,10 @@ int suco_gpu_query_intermediates(suco_gpu_index* x, const float* query, uint32_t
             CUDA_TRY(cudaMemcpy(s8.data(), sc.p, n, cudaMemcpyDeviceToHost));
             for (uint64_t i = 0; i < n; ++i) scores[i] = s8[i];
         }
-        if (cands) CUDA_TRY(cudaMemcpy(cands, x->cands.p, m * 4, cudaMemcpyDeviceToHost));
+        if (cands) {  // the select kernel emits the candidate SET; report it ascending
+            CUDA_TRY(cudaMemcpy(cands, x->cands.p, m * 4, cudaMemcpyDeviceToHost));
+            std::sort(cands, cands + m);
+        }
         if (m_out) *m_out = m;
         std::vector<uint32_t> nc(ns);
         CUDA_TRY(cudaMemcpy(nc.data(), x->ncells.p, ns * 4, cudaMemcpyDeviceToHost));
@@ -772,6 +788,17 @@ int suco_gpu_rerank(const float* data, uint64_t n, uint32_t d, const float* quer
         ra.k = k;
         ra.out_ids = oi.p;
         ra.out_dists = od.p;
+        {
+            DevBuf<unsigned int> st;
+            st.reserve(2);
+            unsigned int h[2] = {0, 0};
+            CUDA_TRY(cudaMemset(st.p, 0, 8));
+            CUDA_TRY(launch_int_stats(dd.p, n * d, st.p, 0));
+            CUDA_TRY(cudaMemcpy(h, st.p, 8, cudaMemcpyDeviceToHost));
+            float mx;
+            std::memcpy(&mx, &h[1], 4);
+            ra.data_int_max = (h[0] == 0 && mx <= 1048576.f) ? mx : -1.f;
+        }
         if (k > 32) {
             ad.reserve(m), ai.reserve(m);
             ra.all_d = ad.p;

@@ -82,6 +82,7 @@ struct RerankArgs {
     double* out_dists;    // nq x k
     double* all_d;        // generic path scratch nq x m
     uint32_t* all_id;     // generic path scratch nq x m
+    float data_int_max;   // >= 0: every data value is an integer with |v| <= this; < 0: not certified
 };
 cudaError_t launch_rerank(const RerankArgs& a, uint64_t nq, cudaStream_t st);
 
@@ -89,5 +90,7 @@ cudaError_t launch_rerank(const RerankArgs& a, uint64_t nq, cudaStream_t st);
 cudaError_t launch_cell_sizes(const uint32_t* cell_off, uint32_t ns, uint32_t K, uint32_t* cell_size,
                               cudaStream_t st);
 cudaError_t launch_check_finite(const float* data, uint64_t count, int* flag, cudaStream_t st);
+// out2[0] |= 1 if any value is non-integral; out2[1] = max |value| as float bits (both pre-zeroed)
+cudaError_t launch_int_stats(const float* data, uint64_t count, unsigned int* out2, cudaStream_t st);
 
 }  // namespace suco_gpu

@@ -59,12 +59,39 @@ template <bool VEC, bool GENERIC>
 __global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     double* qd = reinterpret_cast<double*>(smem);                                  // d
-    float* tile = reinterpret_cast<float*>(smem + ((a.d * 8 + 15) / 16) * 16);     // warps x rows x stride
+    float* qf = reinterpret_cast<float*>(smem + ((a.d * 8 + 15) / 16) * 16);       // d
+    float* tile = qf + ((a.d + 3) / 4) * 4;                                          // warps x rows x stride
+    __shared__ unsigned int qstat[2];
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint64_t q = blockIdx.x;
     const float* query = a.queries + q * a.d;
-    for (uint32_t i = tid; i < a.d; i += kThreads) qd[i] = static_cast<double>(query[i]);
+    if (tid < 2) qstat[tid] = 0;
     __syncthreads();
+    bool qbad = false;
+    float qmax = 0.f;
+    for (uint32_t i = tid; i < a.d; i += kThreads) {
+        const float v = query[i];
+        qd[i] = static_cast<double>(v);
+        qf[i] = v;
+        qbad |= (v != truncf(v));
+        qmax = fmaxf(qmax, fabsf(v));
+    }
+    qbad = __any_sync(kFull, qbad);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) qmax = fmaxf(qmax, __shfl_xor_sync(kFull, qmax, o));
+    if (lane == 0) {
+        if (qbad) atomicOr(&qstat[0], 1u);
+        atomicMax(&qstat[1], __float_as_uint(qmax));
+    }
+    __syncthreads();
+    // Certified-exact fp32 chains: with integer data and query, every term
+    // (a-b)^2 and every partial sum of a chain is an integer below 2^24, so
+    // fp32 FFMA reproduces the reference's fp64 chain values bit for bit.
+    bool use32 = false;
+    if (a.data_int_max >= 0.f && qstat[0] == 0) {
+        const double span = static_cast<double>(a.data_int_max) + static_cast<double>(__uint_as_float(qstat[1]));
+        use32 = (static_cast<double>(a.d / 4 + 4) * span * span) < 16777216.0;
+    }
 
     float* wt = tile + warp * kRows * kStride;
     const uint32_t r = lane >> 2, acc_i = lane & 3u;
@@ -82,6 +109,7 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
         for (uint32_t j = 0; j < kRows; ++j) rid[j] = __shfl_sync(kFull, my_id, j);
         const uint32_t nrows = static_cast<uint32_t>(min_u64(kRows, a.m - base));
         double acc = 0.0;
+        float acc32 = 0.f;
         for (uint32_t c0 = 0; c0 < a.d; c0 += kChunk) {
             const uint32_t cl = min(kChunk, a.d - c0);
             if constexpr (VEC) {
@@ -108,11 +136,20 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
                 const float* row = wt + r * kStride;
                 // chain acc_i over global dims c0 + 4t + acc_i < main4, in order
                 const uint32_t lim = main4 > c0 ? min(cl, main4 - c0) : 0u;
+                if (use32) {
 #pragma unroll 8
-                for (uint32_t e = acc_i; e < lim; e += 4) acc = __dadd_rn(acc, sqdiff_d(row[e], qd[c0 + e]));
+                    for (uint32_t e = acc_i; e < lim; e += 4) {
+                        const float df = row[e] - qf[c0 + e];
+                        acc32 = __fmaf_rn(df, df, acc32);
+                    }
+                } else {
+#pragma unroll 8
+                    for (uint32_t e = acc_i; e < lim; e += 4) acc = __dadd_rn(acc, sqdiff_d(row[e], qd[c0 + e]));
+                }
             }
             __syncwarp();
         }
+        if (use32) acc = static_cast<double>(acc32);  // exact integer
         // tail dims (d % 4) fold into acc0 after its main chain (core.hpp:79-82)
         if (acc_i == 0 && r < nrows && main4 < a.d) {
             const float* src = a.data + static_cast<uint64_t>(rid[r]) * a.d;
@@ -218,7 +255,7 @@ __global__ void __launch_bounds__(256) topk_generic_kernel(RerankArgs a) {
 
 cudaError_t launch_rerank(const RerankArgs& a, uint64_t nq, cudaStream_t st) {
     if (nq == 0) return cudaSuccess;
-    const size_t smem = ((a.d * 8 + 15) / 16) * 16 + static_cast<size_t>(kWarps) * kRows * kStride * 4;
+    const size_t smem = ((a.d * 8 + 15) / 16) * 16 + ((a.d + 3) / 4) * 16 + static_cast<size_t>(kWarps) * kRows * kStride * 4;
     const bool vec = (a.d % 4) == 0;
     const bool generic = a.k > 32;
     auto launch = [&](auto kern) -> cudaError_t {

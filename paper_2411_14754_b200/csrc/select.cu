@@ -41,26 +41,12 @@ namespace {
 
 constexpr uint32_t kThreads = 512;
 constexpr uint32_t kWarps = kThreads / 32;
-constexpr uint32_t kCap = 1024;  // retrieved cells staged per chunk
+constexpr uint32_t kCap = 2048;  // retrieved cells staged per chunk (4 per thread)
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr uint32_t kChAlign = 4 * 32 * kWarps;  // CH multiple of this: whole words per lane-step
 constexpr uint32_t kChMax = 100 * 2048;         // 200 KiB of counters per CTA at most
 
 __host__ __device__ inline uint32_t hist_stride(uint32_t ns) { return ns + 2; }
-
-// #bytes of w that are >= t (bytes <= 127, 1 <= t <= 128): SWAR high-bit test.
-__device__ __forceinline__ uint32_t swar_ge(uint32_t w, uint32_t t) {
-    return __popc((w + (0x80u - t) * 0x01010101u) & 0x80808080u);
-}
-
-__device__ __forceinline__ uint32_t bytes_ge(uint32_t w, uint32_t t, bool swar) {
-    if (t == 0) return 4;
-    if (swar) return swar_ge(w, t);
-    uint32_t c = 0;
-#pragma unroll
-    for (int b = 0; b < 4; ++b) c += ((w >> (8 * b)) & 0xffu) >= t;
-    return c;
-}
 
 struct Smem {
     uint8_t* cnt;        // CH
@@ -71,10 +57,12 @@ struct Smem {
     uint32_t* rquota;    // rounds
     uint32_t* roff;      // rounds
     uint32_t* misc;      // 8
+    uint32_t* sub_start; // ns + 1 (<= 256)
+    uint32_t* hscratch;  // ns + 2: histogram sink of the recount pass
 };
 
 __host__ __device__ inline size_t smem_bytes(uint32_t CH, uint32_t rounds, uint32_t ns) {
-    return CH + 4ull * (rounds * hist_stride(ns) + kCap + kCap + 1 + 2 * kWarps + 2 * rounds + 8) + 16;
+    return CH + 4ull * (rounds * hist_stride(ns) + kCap + kCap + 1 + 2 * kWarps + 2 * rounds + 8 + 257 + 257) + 16;
 }
 
 __device__ inline Smem carve(unsigned char* base, uint32_t CH, uint32_t rounds, uint32_t ns) {
@@ -87,6 +75,8 @@ __device__ inline Smem carve(unsigned char* base, uint32_t CH, uint32_t rounds, 
     s.rquota = s.wtmp + 2 * kWarps;
     s.roff = s.rquota + rounds;
     s.misc = s.roff + rounds;
+    s.sub_start = s.misc + 8;
+    s.hscratch = s.sub_start + 257;
     return s;
 }
 
@@ -119,205 +109,329 @@ __device__ inline uint32_t block_excl_scan(uint32_t v, uint32_t* wtmp, uint32_t*
     return res;
 }
 
-// Counts one slab into s.cnt: cnt[id - lo] = #subspaces whose retrieved
-// cells contain id (query.cpp:235-239 restricted to the slab).
-__device__ void count_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint32_t slab, uint64_t lo, uint32_t len) {
+// ---------------------------------------------------------------- counting
+// Packed per-thread histogram of the values produced by increments: bin v-1
+// in 16-bit field (v-1)&3 of word (v-1)>>2. An id with final score s is
+// incremented through 1..s, so #increments producing v == #ids with score >= v.
+template <int NSB>
+struct IncHist {
+    static constexpr int W = NSB > 0 ? (NSB + 3) / 4 : 1;
+    uint64_t h[W];
+    __device__ void clear() {
+#pragma unroll
+        for (int i = 0; i < W; ++i) h[i] = 0;
+    }
+    __device__ __forceinline__ void add(uint32_t v, uint32_t* hist_smem) {
+        if constexpr (NSB > 0) {
+            const uint32_t b = v - 1;
+            const uint64_t inc = 1ull << ((b & 3u) * 16u);
+#pragma unroll
+            for (int i = 0; i < W; ++i) h[i] += ((b >> 2) == (uint32_t)i) ? inc : 0ull;
+        } else {
+            atomicAdd(hist_smem + v, 1u);
+        }
+    }
+    // warp-reduce and add into hist[1..ns]
+    __device__ void flush(uint32_t* hist, uint32_t ns) {
+        if constexpr (NSB > 0) {
+            const uint32_t lane = threadIdx.x & 31u;
+#pragma unroll
+            for (int b = 0; b < NSB; ++b) {
+                uint32_t v = static_cast<uint32_t>((h[b >> 2] >> ((b & 3) * 16)) & 0xffffu);
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+                if (lane == 0 && v && (uint32_t)b < ns) atomicAdd(hist + b + 1, v);
+            }
+        }
+    }
+};
+
+constexpr int kU = 16;  // ids in flight per lane per wave
+
+struct Cursor {
+    uint32_t ci;        // cell (staged index) holding flat position f
+    uint32_t next_pre;  // seg_pre[ci + 1]
+    uint32_t delta;     // seg_beg[ci] - seg_pre[ci]: id position = delta + f
+};
+
+__device__ __forceinline__ void cursor_seek(const Smem& s, uint32_t f, uint32_t lo_i, uint32_t hi_i, Cursor& c) {
+    // largest staged cell index in [lo_i, hi_i) with seg_pre <= f
+    while (hi_i - lo_i > 1) {
+        const uint32_t mid = (lo_i + hi_i) >> 1;
+        if (s.seg_pre[mid] <= f) lo_i = mid;
+        else hi_i = mid;
+    }
+    c.ci = lo_i;
+    c.next_pre = s.seg_pre[lo_i + 1];
+    c.delta = s.seg_beg[lo_i] - s.seg_pre[lo_i];
+}
+
+struct Wave {
+    uint32_t id[kU];
+    uint32_t n;  // valid entries (entries u < n are valid: f = base + lane + 32u < end)
+};
+
+// Loads up to kU ids for flat positions base + lane + 32u (< end) of one subspace.
+__device__ __forceinline__ void load_wave(const Smem& s, const uint32_t* ids, uint32_t base, uint32_t end, Cursor& c,
+                                          Wave& w) {
+    const uint32_t lane = threadIdx.x & 31u;
+    w.n = 0;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+        const uint32_t f = base + lane + 32u * u;
+        if (f < end) {
+            while (f >= c.next_pre) {
+                ++c.ci;
+                c.next_pre = s.seg_pre[c.ci + 1];
+                c.delta = s.seg_beg[c.ci] - s.seg_pre[c.ci];
+            }
+            w.id[u] = __ldg(ids + c.delta + f);
+            w.n = u + 1;
+        }
+    }
+}
+
+template <int NSB>
+__device__ __forceinline__ void rmw_wave(const Smem& s, const Wave& w, uint32_t lo, IncHist<NSB>& ih, uint32_t* hist) {
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+        if ((uint32_t)u < w.n) {
+            const uint32_t l = w.id[u] - lo;
+            const uint32_t v = s.cnt[l] + 1u;
+            s.cnt[l] = static_cast<uint8_t>(v);
+            ih.add(v, hist);
+        }
+    }
+}
+
+// Counts one slab into s.cnt (query.cpp:235-239 restricted to the slab) and
+// fills hist[t] = #counters >= t (t = 1..ns), hist[0] = len.
+//
+// All retrieved cells of all subspaces are staged at once (their slab
+// slices' begin + a block-wide prefix of lengths), then each subspace's flat
+// id range is split evenly over the 16 warps; lanes stream ids kU deep and
+// the first wave of subspace s+1 is already in flight while subspace s does
+// its counter RMWs. A barrier separates subspaces (an id repeats only across
+// subspaces).
+template <int NSB>
+__device__ void count_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint32_t slab, uint64_t lo, uint32_t len,
+                           uint32_t* hist) {
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     uint4* c4 = reinterpret_cast<uint4*>(s.cnt);
     for (uint32_t i = tid; i < a.CH / 16; i += kThreads) c4[i] = make_uint4(0, 0, 0, 0);
+    if (tid <= a.ns) hist[tid] = tid == 0 ? len : 0u;
+    if (tid == 0) {  // concatenated cell index where each subspace starts
+        uint32_t acc = 0;
+        for (uint32_t sub = 0; sub < a.ns; ++sub) {
+            s.sub_start[sub] = acc;
+            acc += a.ncells[q * a.ns + sub];
+        }
+        s.sub_start[a.ns] = acc;
+    }
     __syncthreads();
     if (len == 0) return;
+    const uint32_t TC = s.sub_start[a.ns];
     const uint32_t stride = a.nslabs + 1;
-    for (uint32_t sub = 0; sub < a.ns; ++sub) {
-        const uint64_t t = q * a.ns + sub;
-        const uint32_t nc = a.ncells[t];
-        const uint32_t* clist = a.cells + t * a.cells_cap;
-        const uint32_t* ids = a.ids + static_cast<uint64_t>(sub) * a.n;
-        const uint32_t* soff = a.slab_off + static_cast<uint64_t>(sub) * a.K * stride + slab;
-        for (uint32_t c0 = 0; c0 < nc; c0 += kCap) {
-            const uint32_t cc = min(kCap, nc - c0);
-            // stage the (begin, length) of each retrieved cell's slice in this slab
-            uint32_t l0 = 0, l1 = 0;
-            const uint32_t i0 = 2 * tid, i1 = 2 * tid + 1;
-            if (i0 < cc) {
-                const uint32_t* p = soff + static_cast<uint64_t>(__ldg(clist + c0 + i0)) * stride;
-                const uint32_t b = __ldg(p), e = __ldg(p + 1);
-                s.seg_beg[i0] = b;
-                l0 = e - b;
+    IncHist<NSB> ih;
+    ih.clear();
+    for (uint32_t c0 = 0; c0 < TC; c0 += kCap) {
+        const uint32_t c1 = min(TC, c0 + kCap), cc = c1 - c0;
+        // stage 4 consecutive cells per thread
+        uint32_t len4[4] = {0, 0, 0, 0};
+        {
+            const uint32_t g0 = c0 + 4 * tid;
+            uint32_t sub = 0;
+            while (sub + 1 < a.ns && s.sub_start[sub + 1] <= g0) ++sub;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t g = g0 + u;
+                if (g < c1) {
+                    while (s.sub_start[sub + 1] <= g) ++sub;
+                    const uint32_t cell = __ldg(a.cells + (q * a.ns + sub) * a.cells_cap + (g - s.sub_start[sub]));
+                    const uint32_t* p = a.slab_off + (static_cast<uint64_t>(sub) * a.K + cell) * stride + slab;
+                    const uint32_t b = __ldg(p), e = __ldg(p + 1);
+                    s.seg_beg[g - c0] = b;
+                    len4[u] = e - b;
+                }
             }
-            if (i1 < cc) {
-                const uint32_t* p = soff + static_cast<uint64_t>(__ldg(clist + c0 + i1)) * stride;
-                const uint32_t b = __ldg(p), e = __ldg(p + 1);
-                s.seg_beg[i1] = b;
-                l1 = e - b;
+        }
+        uint32_t total;
+        const uint32_t ex = block_excl_scan(len4[0] + len4[1] + len4[2] + len4[3], s.wtmp, &total);
+        {
+            uint32_t run = ex;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t g = 4 * tid + u;
+                if (g < cc) s.seg_pre[g] = run;
+                run += len4[u];
             }
-            uint32_t total;
-            const uint32_t ex = block_excl_scan(l0 + l1, s.wtmp, &total);
-            if (i0 < cc) s.seg_pre[i0] = ex;
-            if (i1 < cc) s.seg_pre[i1] = ex + l0;
             if (tid == 0) s.seg_pre[cc] = total;
-            __syncthreads();
-            // flatten: warp w takes ids [total*w/16, total*(w+1)/16)
-            const uint32_t fa = static_cast<uint32_t>((static_cast<uint64_t>(total) * warp) / kWarps);
-            const uint32_t fb = static_cast<uint32_t>((static_cast<uint64_t>(total) * (warp + 1)) / kWarps);
-            uint32_t f = fa + lane;
-            // first cell with seg_pre[cur] <= f < seg_pre[cur+1]
-            uint32_t lo_i = 0, hi_i = cc;
-            if (f < fb) {
-                while (hi_i - lo_i > 1) {
-                    const uint32_t mid = (lo_i + hi_i) >> 1;
-                    if (s.seg_pre[mid] <= f) lo_i = mid;
-                    else hi_i = mid;
-                }
-            }
-            uint32_t cur = lo_i;
-            for (; f < fb; f += 128) {
-                uint32_t pidx[4];
-                bool ok[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const uint32_t g = f + 32u * u;
-                    ok[u] = g < fb;
-                    pidx[u] = 0;
-                    if (ok[u]) {
-                        while (s.seg_pre[cur + 1] <= g) ++cur;
-                        pidx[u] = s.seg_beg[cur] + (g - s.seg_pre[cur]);
-                    }
-                }
-                uint32_t idv[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) idv[u] = ok[u] ? __ldg(ids + pidx[u]) : 0u;
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    if (ok[u]) {
-                        const uint32_t l = idv[u] - static_cast<uint32_t>(lo);
-                        s.cnt[l] = static_cast<uint8_t>(s.cnt[l] + 1);
-                    }
-                }
-            }
-            __syncthreads();
-        }
-    }
-}
-
-// hist[t] = #counters >= t over the slab (t = 1..ns); hist[0] = len.
-template <int NSB>
-__device__ void slab_histogram(const SelectArgs& a, const Smem& s, uint32_t* hist, uint32_t len) {
-    const uint32_t tid = threadIdx.x, lane = tid & 31u;
-    if (tid < hist_stride(a.ns)) hist[tid] = tid == 0 ? len : 0u;
-    __syncthreads();
-    const uint32_t* w32 = reinterpret_cast<const uint32_t*>(s.cnt);
-    const uint32_t words = (len + 3) / 4;  // bytes beyond len are zero: they add nothing for t >= 1
-    if constexpr (NSB > 0) {
-        uint32_t h[NSB];
-#pragma unroll
-        for (int t = 0; t < NSB; ++t) h[t] = 0;
-        for (uint32_t i = tid; i < words; i += kThreads) {
-            const uint32_t w = w32[i];
-            if (w == 0) continue;
-#pragma unroll
-            for (int t = 0; t < NSB; ++t) h[t] += swar_ge(w, t + 1);
-        }
-#pragma unroll
-        for (int t = 0; t < NSB; ++t) {
-            uint32_t v = h[t];
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
-            if (lane == 0 && v && (uint32_t)t < a.ns) atomicAdd(hist + t + 1, v);
-        }
-    } else {
-        for (uint32_t i = tid; i < words; i += kThreads) {
-            const uint32_t w = w32[i];
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                const uint32_t v = (w >> (8 * b)) & 0xffu;
-                if (v) atomicAdd(hist + v, 1u);  // exact-value histogram, suffix-summed below
-            }
         }
         __syncthreads();
-        if (tid == 0) {
-            for (uint32_t t = a.ns; t >= 2; --t) hist[t - 1] += hist[t];
+
+        // subspaces overlapping [c0, c1)
+        uint32_t sb = 0;
+        while (sb + 1 < a.ns && s.sub_start[sb + 1] <= c0) ++sb;
+        uint32_t se = sb;
+        while (se < a.ns && s.sub_start[se] < c1) ++se;  // [sb, se)
+        auto range = [&](uint32_t sub, uint32_t& fa, uint32_t& fb, uint32_t& ca, uint32_t& cb) {
+            ca = max(s.sub_start[sub], c0) - c0;
+            cb = min(s.sub_start[sub + 1], c1) - c0;
+            const uint32_t P0 = s.seg_pre[ca], P1 = s.seg_pre[cb], T = P1 - P0;
+            fa = P0 + static_cast<uint32_t>((static_cast<uint64_t>(T) * warp) / kWarps);
+            fb = P0 + static_cast<uint32_t>((static_cast<uint64_t>(T) * (warp + 1)) / kWarps);
+        };
+        Wave cur, nxt;
+        Cursor cr;
+        uint32_t fa, fb, ca, cb;
+        range(sb, fa, fb, ca, cb);
+        if (fa + lane < fb) cursor_seek(s, fa + lane, ca, cb, cr);
+        const uint32_t* ids = a.ids + static_cast<uint64_t>(sb) * a.n;
+        load_wave(s, ids, fa, fb, cr, cur);
+        uint32_t base = fa;
+        for (uint32_t sub = sb; sub < se; ++sub) {
+            for (;;) {
+                const uint32_t nbase = base + 32u * kU;
+                const bool more = nbase < fb;
+                if (more) {
+                    load_wave(s, ids, nbase, fb, cr, nxt);
+                } else if (sub + 1 < se) {
+                    // prefetch the first wave of the next subspace
+                    uint32_t fa2, fb2, ca2, cb2;
+                    range(sub + 1, fa2, fb2, ca2, cb2);
+                    Cursor c2;
+                    if (fa2 + lane < fb2) cursor_seek(s, fa2 + lane, ca2, cb2, c2);
+                    const uint32_t* ids2 = a.ids + static_cast<uint64_t>(sub + 1) * a.n;
+                    load_wave(s, ids2, fa2, fb2, c2, nxt);
+                    rmw_wave<NSB>(s, cur, static_cast<uint32_t>(lo), ih, hist);
+                    cur = nxt;
+                    cr = c2;
+                    ids = ids2;
+                    fa = fa2, fb = fb2, ca = ca2, cb = cb2;
+                    base = fa2;
+                    break;
+                }
+                rmw_wave<NSB>(s, cur, static_cast<uint32_t>(lo), ih, hist);
+                if (!more) break;
+                cur = nxt;
+                base = nbase;
+            }
+            __syncthreads();  // counters of `sub` final before `sub + 1` increments
         }
+        // seg arrays are restaged by the next chunk (the loop barrier above covers it)
     }
+    ih.flush(hist, a.ns);
     __syncthreads();
 }
 
-// Emits this slab's share of the candidate set: every counter > T and the
-// first `quota` counters == T, in id order, starting at cands[base].
+// Mask (0x80 per byte) of the bytes of word `wi` that are >= t and inside the slab.
+__device__ __forceinline__ uint32_t sel_mask(uint32_t w, uint32_t wi, uint32_t t, uint32_t len, bool swar) {
+    uint32_t m;
+    if (t == 0) {
+        m = 0x80808080u;
+    } else if (swar) {
+        m = (w + (0x80u - t) * 0x01010101u) & 0x80808080u;
+    } else {
+        m = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) m |= (((w >> (8 * b)) & 0xffu) >= t) ? (0x80u << (8 * b)) : 0u;
+    }
+    const uint32_t valid = wi * 4 + 4 <= len ? 4u : (len > wi * 4 ? len - wi * 4 : 0u);
+    if (valid < 4) m &= (1u << (8 * valid)) - 1u;
+    return m;
+}
+
+// Emits this slab's share of the candidate set into cands[base, base + gt + quota):
+// every counter > T (and, when the slab's whole tie class is taken, every
+// counter == T) goes out unordered through a warp-aggregated shared counter —
+// the candidate SET is what the reference defines (query.cpp:242-260); only
+// the slab where the tie quota is cut needs id order, and only for its ties,
+// which a two-pass warp-ordered scan emits after the unordered region.
 __device__ void emit_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint64_t lo, uint32_t len, uint32_t T,
-                          uint32_t quota, uint32_t base, bool swar) {
+                          uint32_t quota, uint32_t base, uint32_t gt, uint32_t ties, bool swar) {
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t* w32 = reinterpret_cast<const uint32_t*>(s.cnt);
+    const uint4* w128 = reinterpret_cast<const uint4*>(s.cnt);
     const uint32_t words = (len + 3) / 4;
-    const uint32_t wpw = (words + kWarps - 1) / kWarps;  // words per warp (contiguous range)
-    const uint32_t wa = min(words, warp * wpw), wb = min(words, wa + wpw);
-    auto word_counts = [&](uint32_t wi, uint32_t w, uint32_t& g, uint32_t& e) {
-        if (wi * 4 + 4 <= len) {
-            const uint32_t geT = bytes_ge(w, T, swar), geT1 = bytes_ge(w, T + 1, swar);
-            g = geT1;
-            e = geT - geT1;
-        } else {
-            g = e = 0;
-            for (uint32_t b = 0; wi * 4 + b < len; ++b) {
-                const uint32_t v = (w >> (8 * b)) & 0xffu;
-                g += v > T;
-                e += v == T;
-            }
-        }
-    };
-    // pass A: warp totals
-    uint32_t g_tot = 0, e_tot = 0;
-    for (uint32_t wi = wa + lane; wi < wb; wi += 32) {
-        uint32_t g, e;
-        word_counts(wi, w32[wi], g, e);
-        g_tot += g;
-        e_tot += e;
-    }
+    const uint32_t nvec = (words + 3) / 4;
+    uint32_t* out = a.cands + q * a.m + base;
+    const bool all_ties = quota == ties;
+    const uint32_t tsel = all_ties ? T : T + 1;
+    if (tid == 0) s.misc[1] = 0;
+    __syncthreads();
+    if (gt + (all_ties ? ties : 0u) > 0) {
+        for (uint32_t v0 = 0; v0 < nvec; v0 += kThreads) {
+            const uint32_t vi = v0 + tid;
+            uint32_t m[4] = {0, 0, 0, 0};
+            uint32_t c = 0;
+            if (vi < nvec) {
+                const uint4 v = w128[vi];
+                const uint32_t ww[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        g_tot += __shfl_xor_sync(kFull, g_tot, off);
-        e_tot += __shfl_xor_sync(kFull, e_tot, off);
-    }
-    uint32_t tmp;
-    const uint32_t g_base = block_excl_scan(lane == 0 ? g_tot : 0u, s.wtmp, &tmp);
-    const uint32_t e_base = block_excl_scan(lane == 0 ? e_tot : 0u, s.wtmp, &tmp);
-    uint32_t gb = __shfl_sync(kFull, g_base, 0), eb = __shfl_sync(kFull, e_base, 0);
-    uint32_t* out = a.cands + q * a.m;
-    // pass B: lane-ordered placement within each 32-word step
-    for (uint32_t w0 = wa; w0 < wb; w0 += 32) {
-        const uint32_t wi = w0 + lane;
-        uint32_t w = 0, g = 0, e = 0;
-        if (wi < wb) {
-            w = w32[wi];
-            word_counts(wi, w, g, e);
-        }
-        uint32_t gx = g, ex = e;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const uint32_t yg = __shfl_up_sync(kFull, gx, off), ye = __shfl_up_sync(kFull, ex, off);
-            if (lane >= (uint32_t)off) {
-                gx += yg;
-                ex += ye;
+                for (int u = 0; u < 4; ++u) {
+                    m[u] = sel_mask(ww[u], vi * 4 + u, tsel, len, swar);
+                    c += __popc(m[u]);
+                }
             }
-        }
-        const uint32_t gsum = __shfl_sync(kFull, gx, 31), esum = __shfl_sync(kFull, ex, 31);
-        gx -= g;
-        ex -= e;
-        const uint32_t tie_before = eb + ex;
-        uint32_t allow = tie_before >= quota ? 0u : min(e, quota - tie_before);
-        uint32_t pos = base + gb + gx + min(tie_before, quota);
-        if (g + allow > 0) {
-            for (uint32_t b = 0; b < 4 && wi * 4 + b < len; ++b) {
-                const uint32_t v = (w >> (8 * b)) & 0xffu;
-                if (v > T) {
-                    out[pos++] = static_cast<uint32_t>(lo) + wi * 4 + b;
-                } else if (v == T && allow > 0) {
-                    out[pos++] = static_cast<uint32_t>(lo) + wi * 4 + b;
-                    --allow;
+            // warp-aggregated slot reservation
+            uint32_t x = c;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t y = __shfl_up_sync(kFull, x, off);
+                if (lane >= (uint32_t)off) x += y;
+            }
+            const uint32_t wsum = __shfl_sync(kFull, x, 31);
+            uint32_t wbase = 0;
+            if (lane == 31 && wsum) wbase = atomicAdd(&s.misc[1], wsum);
+            wbase = __shfl_sync(kFull, wbase, 31);
+            uint32_t pos = wbase + x - c;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                uint32_t mm = m[u];
+                while (mm) {
+                    const uint32_t bit = __ffs(mm) - 1;
+                    out[pos++] = static_cast<uint32_t>(lo) + (vi * 4 + u) * 4 + (bit >> 3);
+                    mm &= mm - 1;
                 }
             }
         }
-        gb += gsum;
+    }
+    if (all_ties || quota == 0) return;
+    // boundary slab: the first `quota` ties (== T) in id order, after the gt region
+    uint32_t* tout = out + gt;
+    const uint32_t wpw = (words + kWarps - 1) / kWarps;
+    const uint32_t wa = min(words, warp * wpw), wb = min(words, wa + wpw);
+    uint32_t e_tot = 0;
+    for (uint32_t wi = wa + lane; wi < wb; wi += 32) {
+        const uint32_t w = w32[wi];
+        e_tot += __popc(sel_mask(w, wi, T, len, swar) & ~sel_mask(w, wi, T + 1, len, swar));
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) e_tot += __shfl_xor_sync(kFull, e_tot, off);
+    uint32_t tmp;
+    const uint32_t e_base = block_excl_scan(lane == 0 ? e_tot : 0u, s.wtmp, &tmp);
+    uint32_t eb = __shfl_sync(kFull, e_base, 0);
+    for (uint32_t w0 = wa; w0 < wb && eb < quota; w0 += 32) {
+        const uint32_t wi = w0 + lane;
+        uint32_t mt = 0;
+        if (wi < wb) {
+            const uint32_t w = w32[wi];
+            mt = sel_mask(w, wi, T, len, swar) & ~sel_mask(w, wi, T + 1, len, swar);
+        }
+        const uint32_t e = __popc(mt);
+        uint32_t ex = e;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, ex, off);
+            if (lane >= (uint32_t)off) ex += y;
+        }
+        const uint32_t esum = __shfl_sync(kFull, ex, 31);
+        uint32_t r = eb + ex - e;
+        while (mt && r < quota) {
+            const uint32_t bit = __ffs(mt) - 1;
+            tout[r++] = static_cast<uint32_t>(lo) + wi * 4 + (bit >> 3);
+            mt &= mt - 1;
+        }
         eb += esum;
     }
 }
@@ -331,18 +445,24 @@ __global__ void __launch_bounds__(kThreads, 1) select_kernel(SelectArgs a) {
     const Smem s = carve(smem, a.CH, a.rounds, a.ns);
     const uint32_t hs = hist_stride(a.ns);
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    const bool swar = NSB > 0;
+    const bool swar = a.ns <= 127;
 
     // pass 1: count + histogram every owned slab
     for (uint32_t r = 0; r < a.rounds; ++r) {
         const uint32_t slab = r * a.CS + rank;
         const uint64_t lo = static_cast<uint64_t>(slab) * a.CH;
         const uint32_t len = slab < a.nslabs ? static_cast<uint32_t>(min_u64(a.CH, a.n - lo)) : 0u;
-        count_slab(a, s, q, slab, lo, len);
+        count_slab<NSB>(a, s, q, slab, lo, len, s.hist + r * hs);
         if (a.scores_dbg) {
             for (uint32_t i = tid; i < len; i += kThreads) a.scores_dbg[q * a.n + lo + i] = s.cnt[i];
         }
-        slab_histogram<NSB>(a, s, s.hist + r * hs, len);
+        if constexpr (NSB == 0) {  // exact-value counts -> suffix sums (#score >= t)
+            if (tid == 0) {
+                uint32_t* h = s.hist + r * hs;
+                for (uint32_t t = a.ns; t >= 2; --t) h[t - 1] += h[t];
+            }
+            __syncthreads();
+        }
     }
     cluster.sync();
 
@@ -448,8 +568,12 @@ __global__ void __launch_bounds__(kThreads, 1) select_kernel(SelectArgs a) {
         if (slab >= a.nslabs) break;
         const uint64_t lo = static_cast<uint64_t>(slab) * a.CH;
         const uint32_t len = static_cast<uint32_t>(min_u64(a.CH, a.n - lo));
-        if (a.rounds > 1) count_slab(a, s, q, slab, lo, len);
-        emit_slab(a, s, q, lo, len, T, s.rquota[r], s.roff[r], swar);
+        if (a.rounds > 1) {
+            count_slab<NSB>(a, s, q, slab, lo, len, s.hscratch);  // recount; histogram discarded
+        }
+        const uint32_t* h = s.hist + r * hs;
+        const uint32_t gt = T + 1 <= a.ns ? h[T + 1] : 0u;
+        emit_slab(a, s, q, lo, len, T, s.rquota[r], s.roff[r], gt, h[T] - gt, swar);
         __syncthreads();
     }
 }
@@ -503,9 +627,9 @@ cudaError_t launch_select_t(const SelectArgs& a, const SelectConfig& cfg, uint64
 
 }  // namespace
 
-SelectConfig plan_select(uint64_t n, uint32_t ns, int cluster_size) {
+static SelectConfig plan_for(uint64_t n, uint32_t ns, uint32_t CS) {
     SelectConfig c;
-    c.CS = cluster_size > 0 ? static_cast<uint32_t>(cluster_size) : 8u;
+    c.CS = CS;
     const uint64_t per = (n + c.CS - 1) / c.CS;
     if (per <= kChMax) {
         c.CH = static_cast<uint32_t>(((per + kChAlign - 1) / kChAlign) * kChAlign);
@@ -519,6 +643,58 @@ SelectConfig plan_select(uint64_t n, uint32_t ns, int cluster_size) {
     }
     c.smem = smem_bytes(c.CH, c.rounds, ns);
     return c;
+}
+
+template <int NSB>
+static int active_clusters(const SelectConfig& c) {
+    if (cudaFuncSetAttribute(select_kernel<NSB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(c.smem)) != cudaSuccess ||
+        (c.CS > 8 && cudaFuncSetAttribute(select_kernel<NSB>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)) {
+        cudaGetLastError();
+        return 0;
+    }
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(c.CS * 1024);
+    lc.blockDim = dim3(kThreads);
+    lc.dynamicSmemBytes = c.smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = c.CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    int num = 0;
+    if (cudaOccupancyMaxActiveClusters(&num, select_kernel<NSB>, &lc) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return num;
+}
+
+static int active_clusters_ns(uint32_t ns, const SelectConfig& c) {
+    if (ns <= 8) return active_clusters<8>(c);
+    if (ns <= 16) return active_clusters<16>(c);
+    if (ns <= 32) return active_clusters<32>(c);
+    return active_clusters<0>(c);
+}
+
+// Cluster size: the one that keeps the most SMs busy with a single counting
+// round (clusters must fit inside a GPC, so 8-CTA clusters strand SMs on a
+// 148-SM B200); SUCO_CLUSTER (cluster_size > 0) forces a size.
+SelectConfig plan_select(uint64_t n, uint32_t ns, int cluster_size) {
+    if (cluster_size > 0) return plan_for(n, ns, static_cast<uint32_t>(cluster_size));
+    SelectConfig best = plan_for(n, ns, 8);
+    long best_score = -1;
+    for (uint32_t cs = 8; cs >= 1; --cs) {
+        const SelectConfig c = plan_for(n, ns, cs);
+        if (c.rounds > 1 && cs != 8) continue;
+        const long score = static_cast<long>(active_clusters_ns(ns, c)) * cs * (c.rounds == 1 ? 2 : 1);
+        if (score > best_score) {
+            best_score = score;
+            best = c;
+        }
+    }
+    return best;
 }
 
 cudaError_t launch_select(const SelectArgs& a, const SelectConfig& cfg, uint64_t nq, cudaStream_t st) {

@@ -27,7 +27,32 @@ __global__ void check_finite_kernel(const float* data, uint64_t count, unsigned 
     }
 }
 
+// integer certificate: any non-integer value; largest |value| (as float bits)
+__global__ void int_stats_kernel(const float* data, uint64_t count, unsigned int* out) {
+    bool bad = false;
+    float mx = 0.f;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const float v = data[i];
+        bad |= (v != truncf(v));
+        mx = fmaxf(mx, fabsf(v));
+    }
+    bad = __any_sync(0xffffffffu, bad);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) {
+        if (bad) atomicOr(out, 1u);
+        atomicMax(out + 1, __float_as_uint(mx));
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_int_stats(const float* data, uint64_t count, unsigned int* out2, cudaStream_t st) {
+    const uint64_t blocks = min_u64((count + 255) / 256, 148ull * 16);
+    int_stats_kernel<<<static_cast<unsigned>(blocks ? blocks : 1), 256, 0, st>>>(data, count, out2);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_cell_sizes(const uint32_t* cell_off, uint32_t ns, uint32_t K, uint32_t* cell_size, cudaStream_t st) {
     const uint64_t total = static_cast<uint64_t>(ns) * K;

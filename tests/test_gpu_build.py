@@ -1,0 +1,119 @@
+"""GPU index build parity: k-means, IMI and whole indexes byte-identical to the reference."""
+import numpy as np
+import pytest
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+
+def test_kmeans_golden(gpu):
+    g = golden("kmeans.npz")
+    km = gpu.kmeans(g["pts"], 20, 8, 5)  # test_kmeans.cpp:70-83 shape
+    assert np.array_equal(km["centroids"], g["centroids"])
+    assert np.array_equal(km["assignments"], g["assignments"])
+    km2 = gpu.kmeans(g["dup"], 8, 5, 13)  # test_kmeans.cpp:93-110: empty clusters repaired
+    assert np.array_equal(km2["centroids"], g["dup_centroids"])
+    assert np.array_equal(km2["assignments"], g["dup_assignments"])
+    assert np.array_equal(km2["repaired"], g["dup_repaired"]) and km2["repaired"].size > 0
+    assert km2["assignments"][0] != km2["assignments"][1]
+
+
+@pytest.mark.parametrize("n,dim,k,iters,kind", [(5000, 8, 50, 4, "int"), (3000, 6, 64, 3, "float"),
+                                                (4000, 30, 50, 2, "float"), (2000, 3, 7, 5, "unit"),
+                                                (600, 4, 3, 10, "float"), (12, 2, 12, 3, "float"),
+                                                (20000, 8, 100, 2, "int"), (800, 40, 10, 3, "int")])
+def test_kmeans_vs_oracle(gpu, oracle, n, dim, k, iters, kind):
+    rng = np.random.default_rng(n + dim + k)
+    if kind == "int":
+        pts = np.clip(np.rint(rng.normal(100, 30, (n, dim))), 0, 255).astype(np.float32)
+    elif kind == "unit":
+        pts = rng.random((n, dim)).astype(np.float32)
+    else:
+        pts = (rng.normal(0, 1, (n, dim)) * 10).astype(np.float32)
+    for seed in (1, 99):
+        a = gpu.kmeans(pts, k, iters, seed)
+        b = oracle.kmeans(pts, k, iters, seed)
+        assert np.array_equal(a["centroids"], b["centroids"]), (kind, seed)
+        assert np.array_equal(a["assignments"], b["assignments"]), (kind, seed)
+        assert np.array_equal(a["repaired"], b["repaired"]), (kind, seed)
+
+
+def test_kmeans_k_equals_n(gpu):  # test_kmeans.cpp:112-119
+    pts = np.random.default_rng(3).random((12, 2)).astype(np.float32)
+    km = gpu.kmeans(pts, 12, 3, 9)
+    assert len(set(km["assignments"].tolist())) == 12
+
+
+def test_kmeans_validation(gpu):  # test_kmeans.cpp:121-126
+    pts = np.zeros((10, 2), np.float32)
+    for k, it in ((0, 5), (3, 0), (11, 5)):
+        with pytest.raises(gpu.ConfigError):
+            gpu.kmeans(pts, k, it, 1)
+
+
+def test_build_imi(gpu, oracle):  # test_index.cpp:44-74
+    off, ids = gpu.build_imi([0, 1, 0, 1], [0, 1, 0, 0], 2)
+    assert off.tolist() == [0, 2, 2, 3, 4] and ids.tolist() == [0, 2, 3, 1]
+    rng = np.random.default_rng(15)
+    for k_half in (1, 2, 7, 32, 120):
+        a, b = rng.integers(0, k_half, 5000), rng.integers(0, k_half, 5000)
+        o1, i1 = gpu.build_imi(a, b, k_half)
+        o2, i2 = oracle.build_imi(a, b, k_half)
+        assert np.array_equal(o1, o2) and np.array_equal(i1, i2)
+    with pytest.raises(gpu.ContractError):
+        gpu.build_imi([0, 1], [0, 2], 2)
+    with pytest.raises(gpu.ContractError):
+        gpu.build_imi([0, 1], [0], 2)
+
+
+def test_build_index_golden(gpu):
+    g = golden("e2e_small.npz")
+    idx = gpu.build_index(g["base"], gpu.IndexParams(4, 12, 5, 42))
+    assert idx.serialize() == g["index"].tobytes()
+    ids, d = idx.knn_query_batch(g["queries"], gpu.CollisionParams(0.05, 0.05, 10))
+    assert np.array_equal(ids, g["p0_ids"]) and np.array_equal(d, g["p0_dists"])
+
+
+def test_build_index_shuffled_golden(gpu):
+    g = golden("e2e_shuffled.npz")
+    idx = gpu.build_index(g["base"], gpu.IndexParams(3, 7, 4, 9, gpu.SubspaceMode.Shuffled))
+    assert idx.serialize() == g["index"].tobytes()
+
+
+@pytest.mark.parametrize("case", [
+    (3000, 32, 20, 0, 100, 8, False, 4, 16, 4, 0),
+    (5000, 16, 30, 20, 140, 18, True, 2, 40, 3, 1),
+    (2000, 60, 10, 0, 1, 0.05, False, 3, 10, 2, 0),
+    (1500, 16, 8, 0, 100, 10, False, 8, 20, 5, 0),
+])
+def test_build_index_vs_oracle(gpu, oracle, case):
+    n, d, cl, lo, hi, sig, q, ns, kh, it, mode = case
+    data = oracle.clustered(n, d, cl, n + d, lo, hi, sig, q)
+    ours = gpu.build_index(data, gpu.IndexParams(ns, kh, it, 7, gpu.SubspaceMode(mode)))
+    theirs = oracle.build_index(data, ns, kh, it, 7, mode)
+    assert ours.serialize() == theirs.serialize()
+
+
+def test_build_index_vs_reference(gpu, ref):
+    """The reference's own build_index on a descriptor corpus (acceptance.cpp:70-74 shape)."""
+    full = ref.clustered(10100, 128, 64, 7, 20.0, 140.0, 18.0, True)
+    base, queries = ref.hold_out(full, 100, 8)
+    ours = gpu.build_index(base, gpu.IndexParams())
+    theirs = ref.build_index(base, 8, 50, 10, 42, 0)
+    assert ours.serialize() == theirs.serialize()
+    ids, d = ours.knn_query_batch(queries, gpu.CollisionParams(0.05, 0.05, 50))
+    ri, rd, _ = theirs.knn_query_batch(base, queries, 0.05, 0.05, 50)
+    assert np.array_equal(ids, ri) and np.array_equal(d, rd)
+
+
+def test_build_index_errors(gpu):  # index.cpp:100-111, subspace.cpp:12-21, core.cpp:8-21
+    data = np.random.default_rng(0).random((100, 8)).astype(np.float32)
+    for p in (gpu.IndexParams(2, 0, 3), gpu.IndexParams(2, 5, 0), gpu.IndexParams(2, 101, 3),
+              gpu.IndexParams(1, 5, 3), gpu.IndexParams(5, 5, 3)):
+        with pytest.raises(gpu.ConfigError):
+            gpu.build_index(data, p)
+    bad = data.copy()
+    bad[3, 1] = np.inf
+    with pytest.raises(gpu.ContractError):
+        gpu.build_index(bad, gpu.IndexParams(2, 5, 3))
