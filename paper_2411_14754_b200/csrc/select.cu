@@ -185,7 +185,7 @@ __device__ __forceinline__ void load_wave(const Smem& s, const uint32_t* ids, ui
                 c.next_pre = s.seg_pre[c.ci + 1];
                 c.delta = s.seg_beg[c.ci] - s.seg_pre[c.ci];
             }
-            w.id[u] = __ldg(ids + c.delta + f);
+            w.id[u] = __ldg(ids + static_cast<uint32_t>(c.delta + f));  // wraps mod 2^32 by design
             w.n = u + 1;
         }
     }
