@@ -456,13 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1) select_kernel(SelectArgs a) {
         if (a.scores_dbg) {
             for (uint32_t i = tid; i < len; i += kThreads) a.scores_dbg[q * a.n + lo + i] = s.cnt[i];
         }
-        if constexpr (NSB == 0) {  // exact-value counts -> suffix sums (#score >= t)
-            if (tid == 0) {
-                uint32_t* h = s.hist + r * hs;
-                for (uint32_t t = a.ns; t >= 2; --t) h[t - 1] += h[t];
-            }
-            __syncthreads();
-        }
+
     }
     cluster.sync();
 
