@@ -41,42 +41,45 @@ namespace {
 
 constexpr uint32_t kThreads = 512;
 constexpr uint32_t kWarps = kThreads / 32;
-constexpr uint32_t kCap = 2048;  // retrieved cells staged per chunk (4 per thread)
+constexpr uint32_t kCap = 2048;    // retrieved cells staged per chunk (4 per thread)
+constexpr uint32_t kUnits = 4096;  // 32-id units described per window
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr uint32_t kChAlign = 4 * 32 * kWarps;  // CH multiple of this: whole words per lane-step
-constexpr uint32_t kChMax = 100 * 2048;         // 200 KiB of counters per CTA at most
+constexpr uint32_t kChMax = 96 * 2048;          // 192 KiB of counters per CTA at most
 
 __host__ __device__ inline uint32_t hist_stride(uint32_t ns) { return ns + 2; }
 
 struct Smem {
     uint8_t* cnt;        // CH
     uint32_t* hist;      // rounds x hist_stride: [0] = slab length, [t] = #score >= t
-    uint32_t* seg_beg;   // kCap
-    uint32_t* seg_pre;   // kCap + 1
+    uint32_t* ubeg;      // kUnits: id position of each 32-id unit
+    uint8_t* ucnt;       // kUnits: ids in the unit (1..32)
     uint32_t* wtmp;      // 2 * kWarps
     uint32_t* rquota;    // rounds
     uint32_t* roff;      // rounds
     uint32_t* misc;      // 8
-    uint32_t* sub_start; // ns + 1 (<= 256)
+    uint32_t* sub_start; // ns + 1: first staged cell of each subspace
+    uint32_t* sub_unit;  // ns + 1: first unit of each subspace (chunk-relative)
     uint32_t* hscratch;  // ns + 2: histogram sink of the recount pass
 };
 
 __host__ __device__ inline size_t smem_bytes(uint32_t CH, uint32_t rounds, uint32_t ns) {
-    return CH + 4ull * (rounds * hist_stride(ns) + kCap + kCap + 1 + 2 * kWarps + 2 * rounds + 8 + 257 + 257) + 16;
+    return CH + 5ull * kUnits + 4ull * (rounds * hist_stride(ns) + 2 * kWarps + 2 * rounds + 8 + 3 * 257) + 16;
 }
 
 __device__ inline Smem carve(unsigned char* base, uint32_t CH, uint32_t rounds, uint32_t ns) {
     Smem s;
     s.cnt = base;
-    s.hist = reinterpret_cast<uint32_t*>(base + CH);
-    s.seg_beg = s.hist + rounds * hist_stride(ns);
-    s.seg_pre = s.seg_beg + kCap;
-    s.wtmp = s.seg_pre + kCap + 1;
+    s.ubeg = reinterpret_cast<uint32_t*>(base + CH);
+    s.hist = s.ubeg + kUnits;
+    s.wtmp = s.hist + rounds * hist_stride(ns);
     s.rquota = s.wtmp + 2 * kWarps;
     s.roff = s.rquota + rounds;
     s.misc = s.roff + rounds;
     s.sub_start = s.misc + 8;
-    s.hscratch = s.sub_start + 257;
+    s.sub_unit = s.sub_start + 257;
+    s.hscratch = s.sub_unit + 257;
+    s.ucnt = reinterpret_cast<uint8_t*>(s.hscratch + 257);
     return s;
 }
 
@@ -110,12 +113,13 @@ __device__ inline uint32_t block_excl_scan(uint32_t v, uint32_t* wtmp, uint32_t*
 }
 
 // ---------------------------------------------------------------- counting
-// Packed per-thread histogram of the values produced by increments: bin v-1
-// in 16-bit field (v-1)&3 of word (v-1)>>2. An id with final score s is
+// Per-thread histogram of the values produced by increments, 8-bit fields
+// (bin v-1 in byte (v-1)&7 of word (v-1)>>3). An id with final score s is
 // incremented through 1..s, so #increments producing v == #ids with score >= v.
+// A lane adds at most 16 per wave, so flushing every 15 waves cannot overflow.
 template <int NSB>
 struct IncHist {
-    static constexpr int W = NSB > 0 ? (NSB + 3) / 4 : 1;
+    static constexpr int W = NSB > 0 ? (NSB + 7) / 8 : 1;
     uint64_t h[W];
     __device__ void clear() {
 #pragma unroll
@@ -124,69 +128,56 @@ struct IncHist {
     __device__ __forceinline__ void add(uint32_t v, uint32_t* hist_smem) {
         if constexpr (NSB > 0) {
             const uint32_t b = v - 1;
-            const uint64_t inc = 1ull << ((b & 3u) * 16u);
+            if constexpr (W == 1) {
+                h[0] += 1ull << (8u * b);
+            } else {
+                const uint64_t inc = 1ull << (8u * (b & 7u));
 #pragma unroll
-            for (int i = 0; i < W; ++i) h[i] += ((b >> 2) == (uint32_t)i) ? inc : 0ull;
+                for (int i = 0; i < W; ++i) h[i] += ((b >> 3) == (uint32_t)i) ? inc : 0ull;
+            }
         } else {
             atomicAdd(hist_smem + v, 1u);
         }
     }
-    // warp-reduce and add into hist[1..ns]
+    // warp-reduce and add into hist[1..ns]; clears the fields
     __device__ void flush(uint32_t* hist, uint32_t ns) {
         if constexpr (NSB > 0) {
             const uint32_t lane = threadIdx.x & 31u;
 #pragma unroll
             for (int b = 0; b < NSB; ++b) {
-                uint32_t v = static_cast<uint32_t>((h[b >> 2] >> ((b & 3) * 16)) & 0xffffu);
+                uint32_t v = static_cast<uint32_t>((h[b >> 3] >> ((b & 7) * 8)) & 0xffu);
+                if (__any_sync(kFull, v != 0)) {
 #pragma unroll
-                for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
-                if (lane == 0 && v && (uint32_t)b < ns) atomicAdd(hist + b + 1, v);
+                    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+                    if (lane == 0 && (uint32_t)b < ns) atomicAdd(hist + b + 1, v);
+                }
             }
+            clear();
         }
     }
 };
 
-constexpr int kU = 16;  // ids in flight per lane per wave
-
-struct Cursor {
-    uint32_t ci;        // cell (staged index) holding flat position f
-    uint32_t next_pre;  // seg_pre[ci + 1]
-    uint32_t delta;     // seg_beg[ci] - seg_pre[ci]: id position = delta + f
-};
-
-__device__ __forceinline__ void cursor_seek(const Smem& s, uint32_t f, uint32_t lo_i, uint32_t hi_i, Cursor& c) {
-    // largest staged cell index in [lo_i, hi_i) with seg_pre <= f
-    while (hi_i - lo_i > 1) {
-        const uint32_t mid = (lo_i + hi_i) >> 1;
-        if (s.seg_pre[mid] <= f) lo_i = mid;
-        else hi_i = mid;
-    }
-    c.ci = lo_i;
-    c.next_pre = s.seg_pre[lo_i + 1];
-    c.delta = s.seg_beg[lo_i] - s.seg_pre[lo_i];
-}
+constexpr int kU = 16;  // units in flight per warp per wave
 
 struct Wave {
     uint32_t id[kU];
-    uint32_t n;  // valid entries (entries u < n are valid: f = base + lane + 32u < end)
+    uint32_t mask;  // bit u: entry u valid for this lane
 };
 
-// Loads up to kU ids for flat positions base + lane + 32u (< end) of one subspace.
-__device__ __forceinline__ void load_wave(const Smem& s, const uint32_t* ids, uint32_t base, uint32_t end, Cursor& c,
-                                          Wave& w) {
+// Loads wave [ua, ub) of 32-id units (at most kU units): lane l takes id l of each unit.
+__device__ __forceinline__ void load_wave(const Smem& s, const uint32_t* ids, uint32_t ua, uint32_t ub, Wave& w) {
     const uint32_t lane = threadIdx.x & 31u;
-    w.n = 0;
+    w.mask = 0;
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-        const uint32_t f = base + lane + 32u * u;
-        if (f < end) {
-            while (f >= c.next_pre) {
-                ++c.ci;
-                c.next_pre = s.seg_pre[c.ci + 1];
-                c.delta = s.seg_beg[c.ci] - s.seg_pre[c.ci];
+        const uint32_t unit = ua + u;
+        if (unit < ub) {
+            const uint32_t cnt = s.ucnt[unit];
+            const uint32_t beg = s.ubeg[unit];
+            if (lane < cnt) {
+                w.id[u] = __ldg(ids + beg + lane);
+                w.mask |= 1u << u;
             }
-            w.id[u] = __ldg(ids + static_cast<uint32_t>(c.delta + f));  // wraps mod 2^32 by design
-            w.n = u + 1;
         }
     }
 }
@@ -195,7 +186,7 @@ template <int NSB>
 __device__ __forceinline__ void rmw_wave(const Smem& s, const Wave& w, uint32_t lo, IncHist<NSB>& ih, uint32_t* hist) {
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-        if ((uint32_t)u < w.n) {
+        if (w.mask & (1u << u)) {
             const uint32_t l = w.id[u] - lo;
             const uint32_t v = s.cnt[l] + 1u;
             s.cnt[l] = static_cast<uint8_t>(v);
@@ -207,12 +198,14 @@ __device__ __forceinline__ void rmw_wave(const Smem& s, const Wave& w, uint32_t 
 // Counts one slab into s.cnt (query.cpp:235-239 restricted to the slab) and
 // fills hist[t] = #counters >= t (t = 1..ns), hist[0] = len.
 //
-// All retrieved cells of all subspaces are staged at once (their slab
-// slices' begin + a block-wide prefix of lengths), then each subspace's flat
-// id range is split evenly over the 16 warps; lanes stream ids kU deep and
-// the first wave of subspace s+1 is already in flight while subspace s does
-// its counter RMWs. A barrier separates subspaces (an id repeats only across
-// subspaces).
+// Staging: each thread loads the slab slice (begin, length) of 4 retrieved
+// cells (all subspaces at once), a block scan over ceil(length/32) cuts every
+// slice into 32-id "units", and the unit descriptors (begin, count) go to
+// shared memory. Counting: each subspace's units are split evenly over the
+// 16 warps; a warp loads kU units (one id per lane per unit, coalesced) and
+// then does the counter RMWs, with the first wave of subspace s+1 already in
+// flight while subspace s does its RMWs. A barrier separates subspaces (an id
+// repeats only across subspaces).
 template <int NSB>
 __device__ void count_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint32_t slab, uint64_t lo, uint32_t len,
                            uint32_t* hist) {
@@ -220,7 +213,7 @@ __device__ void count_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint3
     uint4* c4 = reinterpret_cast<uint4*>(s.cnt);
     for (uint32_t i = tid; i < a.CH / 16; i += kThreads) c4[i] = make_uint4(0, 0, 0, 0);
     if (tid <= a.ns) hist[tid] = tid == 0 ? len : 0u;
-    if (tid == 0) {  // concatenated cell index where each subspace starts
+    if (tid == 0) {
         uint32_t acc = 0;
         for (uint32_t sub = 0; sub < a.ns; ++sub) {
             s.sub_start[sub] = acc;
@@ -234,91 +227,118 @@ __device__ void count_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint3
     const uint32_t stride = a.nslabs + 1;
     IncHist<NSB> ih;
     ih.clear();
+    uint32_t waves_since_flush = 0;
     for (uint32_t c0 = 0; c0 < TC; c0 += kCap) {
-        const uint32_t c1 = min(TC, c0 + kCap), cc = c1 - c0;
-        // stage 4 consecutive cells per thread
-        uint32_t len4[4] = {0, 0, 0, 0};
+        const uint32_t c1 = min(TC, c0 + kCap);
+        // stage 4 consecutive cells per thread: (begin, length) -> units
+        uint32_t beg4[4] = {0, 0, 0, 0}, len4[4] = {0, 0, 0, 0}, nu4[4] = {0, 0, 0, 0};
+        const uint32_t g0 = c0 + 4 * tid;
+        uint32_t sub = 0;
+        while (sub + 1 < a.ns && s.sub_start[sub + 1] <= g0) ++sub;
+        const uint32_t sub_first = sub;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t g = g0 + u;
+            if (g < c1) {
+                while (s.sub_start[sub + 1] <= g) ++sub;
+                const uint32_t cell = __ldg(a.cells + (q * a.ns + sub) * a.cells_cap + (g - s.sub_start[sub]));
+                const uint32_t* p = a.slab_off + (static_cast<uint64_t>(sub) * a.K + cell) * stride + slab;
+                beg4[u] = __ldg(p);
+                len4[u] = __ldg(p + 1) - beg4[u];
+                nu4[u] = (len4[u] + 31) >> 5;
+            }
+        }
+        uint32_t UT;
+        const uint32_t up0 = block_excl_scan(nu4[0] + nu4[1] + nu4[2] + nu4[3], s.wtmp, &UT);
+        // unit index where each subspace starts within this chunk
         {
-            const uint32_t g0 = c0 + 4 * tid;
-            uint32_t sub = 0;
-            while (sub + 1 < a.ns && s.sub_start[sub + 1] <= g0) ++sub;
+            uint32_t up = up0, sb2 = sub_first;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const uint32_t g = g0 + u;
                 if (g < c1) {
-                    while (s.sub_start[sub + 1] <= g) ++sub;
-                    const uint32_t cell = __ldg(a.cells + (q * a.ns + sub) * a.cells_cap + (g - s.sub_start[sub]));
-                    const uint32_t* p = a.slab_off + (static_cast<uint64_t>(sub) * a.K + cell) * stride + slab;
-                    const uint32_t b = __ldg(p), e = __ldg(p + 1);
-                    s.seg_beg[g - c0] = b;
-                    len4[u] = e - b;
+                    while (s.sub_start[sb2 + 1] <= g) ++sb2;
+                    if (g == s.sub_start[sb2] || g == c0) s.sub_unit[sb2] = up;
+                }
+                up += nu4[u];
+            }
+            if (tid == 0) {
+                // subspaces that start at or before c0 begin at unit 0; those past c1 at UT
+                for (uint32_t t = 0; t <= a.ns; ++t) {
+                    if (s.sub_start[t] >= c1) s.sub_unit[t] = UT;
                 }
             }
         }
-        uint32_t total;
-        const uint32_t ex = block_excl_scan(len4[0] + len4[1] + len4[2] + len4[3], s.wtmp, &total);
-        {
-            uint32_t run = ex;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t g = 4 * tid + u;
-                if (g < cc) s.seg_pre[g] = run;
-                run += len4[u];
-            }
-            if (tid == 0) s.seg_pre[cc] = total;
-        }
         __syncthreads();
-
-        // subspaces overlapping [c0, c1)
         uint32_t sb = 0;
         while (sb + 1 < a.ns && s.sub_start[sb + 1] <= c0) ++sb;
         uint32_t se = sb;
-        while (se < a.ns && s.sub_start[se] < c1) ++se;  // [sb, se)
-        auto range = [&](uint32_t sub, uint32_t& fa, uint32_t& fb, uint32_t& ca, uint32_t& cb) {
-            ca = max(s.sub_start[sub], c0) - c0;
-            cb = min(s.sub_start[sub + 1], c1) - c0;
-            const uint32_t P0 = s.seg_pre[ca], P1 = s.seg_pre[cb], T = P1 - P0;
-            fa = P0 + static_cast<uint32_t>((static_cast<uint64_t>(T) * warp) / kWarps);
-            fb = P0 + static_cast<uint32_t>((static_cast<uint64_t>(T) * (warp + 1)) / kWarps);
-        };
-        Wave cur, nxt;
-        Cursor cr;
-        uint32_t fa, fb, ca, cb;
-        range(sb, fa, fb, ca, cb);
-        if (fa + lane < fb) cursor_seek(s, fa + lane, ca, cb, cr);
-        const uint32_t* ids = a.ids + static_cast<uint64_t>(sb) * a.n;
-        load_wave(s, ids, fa, fb, cr, cur);
-        uint32_t base = fa;
-        for (uint32_t sub = sb; sub < se; ++sub) {
-            for (;;) {
-                const uint32_t nbase = base + 32u * kU;
-                const bool more = nbase < fb;
-                if (more) {
-                    load_wave(s, ids, nbase, fb, cr, nxt);
-                } else if (sub + 1 < se) {
-                    // prefetch the first wave of the next subspace
-                    uint32_t fa2, fb2, ca2, cb2;
-                    range(sub + 1, fa2, fb2, ca2, cb2);
-                    Cursor c2;
-                    if (fa2 + lane < fb2) cursor_seek(s, fa2 + lane, ca2, cb2, c2);
-                    const uint32_t* ids2 = a.ids + static_cast<uint64_t>(sub + 1) * a.n;
-                    load_wave(s, ids2, fa2, fb2, c2, nxt);
-                    rmw_wave<NSB>(s, cur, static_cast<uint32_t>(lo), ih, hist);
-                    cur = nxt;
-                    cr = c2;
-                    ids = ids2;
-                    fa = fa2, fb = fb2, ca = ca2, cb = cb2;
-                    base = fa2;
-                    break;
+        while (se < a.ns && s.sub_start[se] < c1) ++se;  // subspaces [sb, se) overlap the chunk
+
+        for (uint32_t u0 = 0; u0 < UT; u0 += kUnits) {
+            const uint32_t u1 = min(UT, u0 + kUnits);
+            // describe the units of this window
+            {
+                uint32_t up = up0;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    for (uint32_t j = 0; j < nu4[u]; ++j) {
+                        const uint32_t unit = up + j;
+                        if (unit >= u0 && unit < u1) {
+                            s.ubeg[unit - u0] = beg4[u] + 32u * j;
+                            s.ucnt[unit - u0] = static_cast<uint8_t>(min(32u, len4[u] - 32u * j));
+                        }
+                    }
+                    up += nu4[u];
                 }
-                rmw_wave<NSB>(s, cur, static_cast<uint32_t>(lo), ih, hist);
-                if (!more) break;
-                cur = nxt;
-                base = nbase;
             }
-            __syncthreads();  // counters of `sub` final before `sub + 1` increments
+            __syncthreads();
+            auto range = [&](uint32_t sb3, uint32_t& ua, uint32_t& ub) {
+                const uint32_t A = max(s.sub_unit[sb3], u0) - u0;
+                const uint32_t B = max(min(s.sub_unit[sb3 + 1], u1), u0) - u0;
+                const uint32_t T = B > A ? B - A : 0;
+                ua = A + static_cast<uint32_t>((static_cast<uint64_t>(T) * warp) / kWarps);
+                ub = A + static_cast<uint32_t>((static_cast<uint64_t>(T) * (warp + 1)) / kWarps);
+            };
+            Wave cur, nxt;
+            uint32_t ua, ub;
+            range(sb, ua, ub);
+            const uint32_t* ids = a.ids + static_cast<uint64_t>(sb) * a.n;
+            load_wave(s, ids, ua, ub, cur);
+            for (uint32_t sb3 = sb; sb3 < se; ++sb3) {
+                for (;;) {
+                    const uint32_t nua = ua + kU;
+                    const bool more = nua < ub;
+                    if (more) {
+                        load_wave(s, ids, nua, ub, nxt);
+                    } else if (sb3 + 1 < se) {
+                        uint32_t ua2, ub2;
+                        range(sb3 + 1, ua2, ub2);
+                        const uint32_t* ids2 = a.ids + static_cast<uint64_t>(sb3 + 1) * a.n;
+                        load_wave(s, ids2, ua2, ub2, nxt);
+                        rmw_wave<NSB>(s, cur, static_cast<uint32_t>(lo), ih, hist);
+                        cur = nxt;
+                        ids = ids2;
+                        ua = ua2;
+                        ub = ub2;
+                        break;
+                    }
+                    rmw_wave<NSB>(s, cur, static_cast<uint32_t>(lo), ih, hist);
+                    if (++waves_since_flush == 15) {
+                        ih.flush(hist, a.ns);
+                        waves_since_flush = 0;
+                    }
+                    if (!more) break;
+                    cur = nxt;
+                    ua = nua;
+                }
+                if (++waves_since_flush >= 15) {
+                    ih.flush(hist, a.ns);
+                    waves_since_flush = 0;
+                }
+                __syncthreads();  // counters of sb3 final before sb3 + 1 increments (and units reusable)
+            }
         }
-        // seg arrays are restaged by the next chunk (the loop barrier above covers it)
     }
     ih.flush(hist, a.ns);
     __syncthreads();
@@ -360,19 +380,32 @@ __device__ void emit_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint64
     if (tid == 0) s.misc[1] = 0;
     __syncthreads();
     if (gt + (all_ties ? ties : 0u) > 0) {
+        const uint32_t last_vi = (len - 1) / 16;
+        const uint32_t kq = (0x80u - (tsel ? tsel : 1u)) * 0x01010101u;
         for (uint32_t v0 = 0; v0 < nvec; v0 += kThreads) {
             const uint32_t vi = v0 + tid;
             uint32_t m[4] = {0, 0, 0, 0};
-            uint32_t c = 0;
             if (vi < nvec) {
                 const uint4 v = w128[vi];
-                const uint32_t ww[4] = {v.x, v.y, v.z, v.w};
+                if (tsel == 0) {
+                    m[0] = m[1] = m[2] = m[3] = 0x80808080u;
+                } else if (swar) {
+                    m[0] = (v.x + kq) & 0x80808080u;
+                    m[1] = (v.y + kq) & 0x80808080u;
+                    m[2] = (v.z + kq) & 0x80808080u;
+                    m[3] = (v.w + kq) & 0x80808080u;
+                } else {
+                    const uint32_t ww[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    m[u] = sel_mask(ww[u], vi * 4 + u, tsel, len, swar);
-                    c += __popc(m[u]);
+                    for (int u = 0; u < 4; ++u) m[u] = sel_mask(ww[u], 0, tsel, 4, false);
+                }
+                if (vi == last_vi) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) m[u] = sel_mask(0xffffffffu, vi * 4 + u, 0, len, true) & m[u];
                 }
             }
+            const uint32_t c = __popc(m[0]) + __popc(m[1]) + __popc(m[2]) + __popc(m[3]);
+            if (!__any_sync(kFull, c != 0)) continue;
             // warp-aggregated slot reservation
             uint32_t x = c;
 #pragma unroll
@@ -382,16 +415,18 @@ __device__ void emit_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint64
             }
             const uint32_t wsum = __shfl_sync(kFull, x, 31);
             uint32_t wbase = 0;
-            if (lane == 31 && wsum) wbase = atomicAdd(&s.misc[1], wsum);
+            if (lane == 31) wbase = atomicAdd(&s.misc[1], wsum);
             wbase = __shfl_sync(kFull, wbase, 31);
             uint32_t pos = wbase + x - c;
+            if (c) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                uint32_t mm = m[u];
-                while (mm) {
-                    const uint32_t bit = __ffs(mm) - 1;
-                    out[pos++] = static_cast<uint32_t>(lo) + (vi * 4 + u) * 4 + (bit >> 3);
-                    mm &= mm - 1;
+                for (int u = 0; u < 4; ++u) {
+                    uint32_t mm = m[u];
+                    while (mm) {
+                        const uint32_t bit = __ffs(mm) - 1;
+                        out[pos++] = static_cast<uint32_t>(lo) + (vi * 4 + u) * 4 + (bit >> 3);
+                        mm &= mm - 1;
+                    }
                 }
             }
         }
