@@ -42,7 +42,7 @@ namespace {
 constexpr uint32_t kThreads = 512;
 constexpr uint32_t kWarps = kThreads / 32;
 constexpr uint32_t kCap = 2048;    // retrieved cells staged per chunk (4 per thread)
-constexpr uint32_t kUnits = 4096;  // 32-id units described per window
+constexpr uint32_t kUnits = 2048;  // 32-id units described per window
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr uint32_t kChAlign = 4 * 32 * kWarps;  // CH multiple of this: whole words per lane-step
 constexpr uint32_t kChMax = 96 * 2048;          // 192 KiB of counters per CTA at most
@@ -52,8 +52,7 @@ __host__ __device__ inline uint32_t hist_stride(uint32_t ns) { return ns + 2; }
 struct Smem {
     uint8_t* cnt;        // CH
     uint32_t* hist;      // rounds x hist_stride: [0] = slab length, [t] = #score >= t
-    uint32_t* ubeg;      // kUnits: id position of each 32-id unit
-    uint8_t* ucnt;       // kUnits: ids in the unit (1..32)
+    uint2* udesc;        // kUnits: (id position, id count 1..32) of each 32-id unit
     uint32_t* wtmp;      // 2 * kWarps
     uint32_t* rquota;    // rounds
     uint32_t* roff;      // rounds
@@ -64,14 +63,14 @@ struct Smem {
 };
 
 __host__ __device__ inline size_t smem_bytes(uint32_t CH, uint32_t rounds, uint32_t ns) {
-    return CH + 5ull * kUnits + 4ull * (rounds * hist_stride(ns) + 2 * kWarps + 2 * rounds + 8 + 3 * 257) + 16;
+    return CH + 8ull * kUnits + 4ull * (rounds * hist_stride(ns) + 2 * kWarps + 2 * rounds + 8 + 3 * 257) + 16;
 }
 
 __device__ inline Smem carve(unsigned char* base, uint32_t CH, uint32_t rounds, uint32_t ns) {
     Smem s;
     s.cnt = base;
-    s.ubeg = reinterpret_cast<uint32_t*>(base + CH);
-    s.hist = s.ubeg + kUnits;
+    s.udesc = reinterpret_cast<uint2*>(base + CH);
+    s.hist = reinterpret_cast<uint32_t*>(s.udesc + kUnits);
     s.wtmp = s.hist + rounds * hist_stride(ns);
     s.rquota = s.wtmp + 2 * kWarps;
     s.roff = s.rquota + rounds;
@@ -79,7 +78,6 @@ __device__ inline Smem carve(unsigned char* base, uint32_t CH, uint32_t rounds, 
     s.sub_start = s.misc + 8;
     s.sub_unit = s.sub_start + 257;
     s.hscratch = s.sub_unit + 257;
-    s.ucnt = reinterpret_cast<uint8_t*>(s.hscratch + 257);
     return s;
 }
 
@@ -164,22 +162,21 @@ struct Wave {
     uint32_t mask;  // bit u: entry u valid for this lane
 };
 
-// Loads wave [ua, ub) of 32-id units (at most kU units): lane l takes id l of each unit.
+// Loads wave [ua, ub) of 32-id units (at most kU units): lane l takes id l of
+// each unit. Predicated, branch-free: invalid slots read unit ua (always a
+// real descriptor) and issue no global load.
 __device__ __forceinline__ void load_wave(const Smem& s, const uint32_t* ids, uint32_t ua, uint32_t ub, Wave& w) {
     const uint32_t lane = threadIdx.x & 31u;
-    w.mask = 0;
+    uint32_t mask = 0;
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-        const uint32_t unit = ua + u;
-        if (unit < ub) {
-            const uint32_t cnt = s.ucnt[unit];
-            const uint32_t beg = s.ubeg[unit];
-            if (lane < cnt) {
-                w.id[u] = __ldg(ids + beg + lane);
-                w.mask |= 1u << u;
-            }
-        }
+        const uint32_t unit = ua + u < ub ? ua + u : ua;
+        const uint2 d = s.udesc[unit];  // (begin, count)
+        const bool ok = (ua + u < ub) && (lane < d.y);
+        w.id[u] = ok ? __ldg(ids + d.x + lane) : 0u;
+        mask |= static_cast<uint32_t>(ok) << u;
     }
+    w.mask = mask;
 }
 
 template <int NSB>
@@ -285,8 +282,7 @@ __device__ void count_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint3
                     for (uint32_t j = 0; j < nu4[u]; ++j) {
                         const uint32_t unit = up + j;
                         if (unit >= u0 && unit < u1) {
-                            s.ubeg[unit - u0] = beg4[u] + 32u * j;
-                            s.ucnt[unit - u0] = static_cast<uint8_t>(min(32u, len4[u] - 32u * j));
+                            s.udesc[unit - u0] = make_uint2(beg4[u] + 32u * j, min(32u, len4[u] - 32u * j));
                         }
                     }
                     up += nu4[u];
@@ -382,29 +378,35 @@ __device__ void emit_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint64
     if (gt + (all_ties ? ties : 0u) > 0) {
         const uint32_t last_vi = (len - 1) / 16;
         const uint32_t kq = (0x80u - (tsel ? tsel : 1u)) * 0x01010101u;
-        for (uint32_t v0 = 0; v0 < nvec; v0 += kThreads) {
-            const uint32_t vi = v0 + tid;
-            uint32_t m[4] = {0, 0, 0, 0};
-            if (vi < nvec) {
-                const uint4 v = w128[vi];
-                if (tsel == 0) {
-                    m[0] = m[1] = m[2] = m[3] = 0x80808080u;
-                } else if (swar) {
-                    m[0] = (v.x + kq) & 0x80808080u;
-                    m[1] = (v.y + kq) & 0x80808080u;
-                    m[2] = (v.z + kq) & 0x80808080u;
-                    m[3] = (v.w + kq) & 0x80808080u;
-                } else {
-                    const uint32_t ww[4] = {v.x, v.y, v.z, v.w};
+        constexpr uint32_t kV = 4;  // uint4 vectors per lane per step (64 counters)
+        for (uint32_t v0 = 0; v0 < nvec; v0 += kThreads * kV) {
+            uint32_t m[kV][4];
+            uint32_t c = 0;
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) m[u] = sel_mask(ww[u], 0, tsel, 4, false);
-                }
-                if (vi == last_vi) {
+            for (uint32_t j = 0; j < kV; ++j) {
+                const uint32_t vi = v0 + j * kThreads + tid;
+                m[j][0] = m[j][1] = m[j][2] = m[j][3] = 0;
+                if (vi < nvec) {
+                    const uint4 v = w128[vi];
+                    if (tsel == 0) {
+                        m[j][0] = m[j][1] = m[j][2] = m[j][3] = 0x80808080u;
+                    } else if (swar) {
+                        m[j][0] = (v.x + kq) & 0x80808080u;
+                        m[j][1] = (v.y + kq) & 0x80808080u;
+                        m[j][2] = (v.z + kq) & 0x80808080u;
+                        m[j][3] = (v.w + kq) & 0x80808080u;
+                    } else {
+                        const uint32_t ww[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) m[u] = sel_mask(0xffffffffu, vi * 4 + u, 0, len, true) & m[u];
+                        for (int u = 0; u < 4; ++u) m[j][u] = sel_mask(ww[u], 0, tsel, 4, false);
+                    }
+                    if (vi == last_vi) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) m[j][u] &= sel_mask(0xffffffffu, vi * 4 + u, 0, len, true);
+                    }
+                    c += __popc(m[j][0]) + __popc(m[j][1]) + __popc(m[j][2]) + __popc(m[j][3]);
                 }
             }
-            const uint32_t c = __popc(m[0]) + __popc(m[1]) + __popc(m[2]) + __popc(m[3]);
             if (!__any_sync(kFull, c != 0)) continue;
             // warp-aggregated slot reservation
             uint32_t x = c;
@@ -420,12 +422,16 @@ __device__ void emit_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint64
             uint32_t pos = wbase + x - c;
             if (c) {
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    uint32_t mm = m[u];
-                    while (mm) {
-                        const uint32_t bit = __ffs(mm) - 1;
-                        out[pos++] = static_cast<uint32_t>(lo) + (vi * 4 + u) * 4 + (bit >> 3);
-                        mm &= mm - 1;
+                for (uint32_t j = 0; j < kV; ++j) {
+                    const uint32_t vi = v0 + j * kThreads + tid;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        uint32_t mm = m[j][u];
+                        while (mm) {
+                            const uint32_t bit = __ffs(mm) - 1;
+                            out[pos++] = static_cast<uint32_t>(lo) + (vi * 4 + u) * 4 + (bit >> 3);
+                            mm &= mm - 1;
+                        }
                     }
                 }
             }
