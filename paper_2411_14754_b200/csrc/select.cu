@@ -28,6 +28,8 @@
 // When n > CS * CH_MAX the cluster walks `rounds` slabs per CTA twice
 // (histogram pass, then recount + emit) instead of spilling counters.
 #include <cooperative_groups.h>
+#include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -42,7 +44,7 @@ namespace {
 constexpr uint32_t kThreads = 512;
 constexpr uint32_t kWarps = kThreads / 32;
 constexpr uint32_t kCap = 2048;    // retrieved cells staged per chunk (4 per thread)
-constexpr uint32_t kUnits = 2048;  // 32-id units described per window
+constexpr uint32_t kUnits = 4096;  // 32-id units described per window
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr uint32_t kChAlign = 4 * 32 * kWarps;  // CH multiple of this: whole words per lane-step
 constexpr uint32_t kChMax = 96 * 2048;          // 192 KiB of counters per CTA at most
@@ -155,34 +157,45 @@ struct IncHist {
     }
 };
 
-constexpr int kU = 16;  // units in flight per warp per wave
-
+template <int KU>
 struct Wave {
-    uint32_t id[kU];
+    uint32_t id[KU];
     uint32_t mask;  // bit u: entry u valid for this lane
 };
 
-// Loads wave [ua, ub) of 32-id units (at most kU units): lane l takes id l of
-// each unit. Predicated, branch-free: invalid slots read unit ua (always a
-// real descriptor) and issue no global load.
-__device__ __forceinline__ void load_wave(const Smem& s, const uint32_t* ids, uint32_t ua, uint32_t ub, Wave& w) {
+// Loads wave [ua, ub) of 32-id units (at most KU units): lane l takes id l of
+// each unit. BRANCHY skips invalid slots with a branch; otherwise every slot
+// is predicated (invalid slots re-read unit ua and issue no global load).
+template <int KU, bool BRANCHY>
+__device__ __forceinline__ void load_wave(const Smem& s, const uint32_t* ids, uint32_t ua, uint32_t ub, Wave<KU>& w) {
     const uint32_t lane = threadIdx.x & 31u;
     uint32_t mask = 0;
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
-        const uint32_t unit = ua + u < ub ? ua + u : ua;
-        const uint2 d = s.udesc[unit];  // (begin, count)
-        const bool ok = (ua + u < ub) && (lane < d.y);
-        w.id[u] = ok ? __ldg(ids + d.x + lane) : 0u;
-        mask |= static_cast<uint32_t>(ok) << u;
+    for (int u = 0; u < KU; ++u) {
+        if constexpr (BRANCHY) {
+            if (ua + u < ub) {
+                const uint2 d = s.udesc[ua + u];
+                if (lane < d.y) {
+                    w.id[u] = __ldg(ids + d.x + lane);
+                    mask |= 1u << u;
+                }
+            }
+        } else {
+            const uint32_t unit = ua + u < ub ? ua + u : ua;
+            const uint2 d = s.udesc[unit];  // (begin, count)
+            const bool ok = (ua + u < ub) && (lane < d.y);
+            w.id[u] = ok ? __ldg(ids + d.x + lane) : 0u;
+            mask |= static_cast<uint32_t>(ok) << u;
+        }
     }
     w.mask = mask;
 }
 
-template <int NSB>
-__device__ __forceinline__ void rmw_wave(const Smem& s, const Wave& w, uint32_t lo, IncHist<NSB>& ih, uint32_t* hist) {
+template <int NSB, int KU>
+__device__ __forceinline__ void rmw_wave(const Smem& s, const Wave<KU>& w, uint32_t lo, IncHist<NSB>& ih,
+                                         uint32_t* hist) {
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
+    for (int u = 0; u < KU; ++u) {
         if (w.mask & (1u << u)) {
             const uint32_t l = w.id[u] - lo;
             const uint32_t v = s.cnt[l] + 1u;
@@ -203,7 +216,7 @@ __device__ __forceinline__ void rmw_wave(const Smem& s, const Wave& w, uint32_t 
 // then does the counter RMWs, with the first wave of subspace s+1 already in
 // flight while subspace s does its RMWs. A barrier separates subspaces (an id
 // repeats only across subspaces).
-template <int NSB>
+template <int NSB, int KU, bool BRANCHY, bool PREFETCH>
 __device__ void count_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint32_t slab, uint64_t lo, uint32_t len,
                            uint32_t* hist) {
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
@@ -296,43 +309,61 @@ __device__ void count_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint3
                 ua = A + static_cast<uint32_t>((static_cast<uint64_t>(T) * warp) / kWarps);
                 ub = A + static_cast<uint32_t>((static_cast<uint64_t>(T) * (warp + 1)) / kWarps);
             };
-            Wave cur, nxt;
-            uint32_t ua, ub;
-            range(sb, ua, ub);
-            const uint32_t* ids = a.ids + static_cast<uint64_t>(sb) * a.n;
-            load_wave(s, ids, ua, ub, cur);
-            for (uint32_t sb3 = sb; sb3 < se; ++sb3) {
-                for (;;) {
-                    const uint32_t nua = ua + kU;
-                    const bool more = nua < ub;
-                    if (more) {
-                        load_wave(s, ids, nua, ub, nxt);
-                    } else if (sb3 + 1 < se) {
-                        uint32_t ua2, ub2;
-                        range(sb3 + 1, ua2, ub2);
-                        const uint32_t* ids2 = a.ids + static_cast<uint64_t>(sb3 + 1) * a.n;
-                        load_wave(s, ids2, ua2, ub2, nxt);
-                        rmw_wave<NSB>(s, cur, static_cast<uint32_t>(lo), ih, hist);
+            if constexpr (PREFETCH) {
+                Wave<KU> cur, nxt;
+                uint32_t ua, ub;
+                range(sb, ua, ub);
+                const uint32_t* ids = a.ids + static_cast<uint64_t>(sb) * a.n;
+                load_wave<KU, BRANCHY>(s, ids, ua, ub, cur);
+                for (uint32_t sb3 = sb; sb3 < se; ++sb3) {
+                    for (;;) {
+                        const uint32_t nua = ua + KU;
+                        const bool more = nua < ub;
+                        if (more) {
+                            load_wave<KU, BRANCHY>(s, ids, nua, ub, nxt);
+                        } else if (sb3 + 1 < se) {
+                            uint32_t ua2, ub2;
+                            range(sb3 + 1, ua2, ub2);
+                            const uint32_t* ids2 = a.ids + static_cast<uint64_t>(sb3 + 1) * a.n;
+                            load_wave<KU, BRANCHY>(s, ids2, ua2, ub2, nxt);
+                            rmw_wave<NSB, KU>(s, cur, static_cast<uint32_t>(lo), ih, hist);
+                            cur = nxt;
+                            ids = ids2;
+                            ua = ua2;
+                            ub = ub2;
+                            break;
+                        }
+                        rmw_wave<NSB, KU>(s, cur, static_cast<uint32_t>(lo), ih, hist);
+                        if (++waves_since_flush * KU >= 240) {
+                            ih.flush(hist, a.ns);
+                            waves_since_flush = 0;
+                        }
+                        if (!more) break;
                         cur = nxt;
-                        ids = ids2;
-                        ua = ua2;
-                        ub = ub2;
-                        break;
+                        ua = nua;
                     }
-                    rmw_wave<NSB>(s, cur, static_cast<uint32_t>(lo), ih, hist);
-                    if (++waves_since_flush == 15) {
+                    if (++waves_since_flush * KU >= 240) {
                         ih.flush(hist, a.ns);
                         waves_since_flush = 0;
                     }
-                    if (!more) break;
-                    cur = nxt;
-                    ua = nua;
+                    __syncthreads();  // counters of sb3 final before sb3 + 1 increments
                 }
-                if (++waves_since_flush >= 15) {
-                    ih.flush(hist, a.ns);
-                    waves_since_flush = 0;
+            } else {
+                for (uint32_t sb3 = sb; sb3 < se; ++sb3) {
+                    uint32_t ua, ub;
+                    range(sb3, ua, ub);
+                    const uint32_t* ids = a.ids + static_cast<uint64_t>(sb3) * a.n;
+                    for (uint32_t u0 = ua; u0 < ub; u0 += KU) {
+                        Wave<KU> w;
+                        load_wave<KU, BRANCHY>(s, ids, u0, ub, w);
+                        rmw_wave<NSB, KU>(s, w, static_cast<uint32_t>(lo), ih, hist);
+                        if (++waves_since_flush * KU >= 240) {
+                            ih.flush(hist, a.ns);
+                            waves_since_flush = 0;
+                        }
+                    }
+                    __syncthreads();  // counters of sb3 final before sb3 + 1 increments
                 }
-                __syncthreads();  // counters of sb3 final before sb3 + 1 increments (and units reusable)
             }
         }
     }
@@ -477,7 +508,7 @@ __device__ void emit_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint64
     }
 }
 
-template <int NSB>
+template <int NSB, int KU = 16, bool BRANCHY = true, bool PREFETCH = true>
 __global__ void __launch_bounds__(kThreads, 1) select_kernel(SelectArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     cg::cluster_group cluster = cg::this_cluster();
@@ -493,7 +524,7 @@ __global__ void __launch_bounds__(kThreads, 1) select_kernel(SelectArgs a) {
         const uint32_t slab = r * a.CS + rank;
         const uint64_t lo = static_cast<uint64_t>(slab) * a.CH;
         const uint32_t len = slab < a.nslabs ? static_cast<uint32_t>(min_u64(a.CH, a.n - lo)) : 0u;
-        count_slab<NSB>(a, s, q, slab, lo, len, s.hist + r * hs);
+        count_slab<NSB, KU, BRANCHY, PREFETCH>(a, s, q, slab, lo, len, s.hist + r * hs);
         if (a.scores_dbg) {
             for (uint32_t i = tid; i < len; i += kThreads) a.scores_dbg[q * a.n + lo + i] = s.cnt[i];
         }
@@ -604,7 +635,7 @@ __global__ void __launch_bounds__(kThreads, 1) select_kernel(SelectArgs a) {
         const uint64_t lo = static_cast<uint64_t>(slab) * a.CH;
         const uint32_t len = static_cast<uint32_t>(min_u64(a.CH, a.n - lo));
         if (a.rounds > 1) {
-            count_slab<NSB>(a, s, q, slab, lo, len, s.hscratch);  // recount; histogram discarded
+            count_slab<NSB, KU, BRANCHY, PREFETCH>(a, s, q, slab, lo, len, s.hscratch);  // recount
         }
         const uint32_t* h = s.hist + r * hs;
         const uint32_t gt = T + 1 <= a.ns ? h[T + 1] : 0u;
@@ -636,13 +667,39 @@ __global__ void slab_offsets_kernel(const uint32_t* cell_off, const uint32_t* id
     }
 }
 
+using SelectFn = void (*)(SelectArgs);
+
+template <int NSB>
+SelectFn pick_variant() {
+    // SUCO_SELECT_VARIANT="KU,BRANCHY,PREFETCH" (tuning knob; N_s <= 8 only)
+    if constexpr (NSB == 8) {
+        const char* v = std::getenv("SUCO_SELECT_VARIANT");
+        if (v) {
+            int ku = 16, br = 1, pf = 1;
+            std::sscanf(v, "%d,%d,%d", &ku, &br, &pf);
+            const int key = (ku == 8 ? 0 : 4) | (br ? 2 : 0) | (pf ? 1 : 0);
+            switch (key) {
+                case 0: return select_kernel<8, 8, false, false>;
+                case 1: return select_kernel<8, 8, false, true>;
+                case 2: return select_kernel<8, 8, true, false>;
+                case 3: return select_kernel<8, 8, true, true>;
+                case 4: return select_kernel<8, 16, false, false>;
+                case 5: return select_kernel<8, 16, false, true>;
+                case 6: return select_kernel<8, 16, true, false>;
+                default: return select_kernel<8, 16, true, true>;
+            }
+        }
+    }
+    return select_kernel<NSB>;
+}
+
 template <int NSB>
 cudaError_t launch_select_t(const SelectArgs& a, const SelectConfig& cfg, uint64_t nq, cudaStream_t st) {
-    cudaError_t e = cudaFuncSetAttribute(select_kernel<NSB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(cfg.smem));
+    const SelectFn fn = pick_variant<NSB>();
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cfg.smem));
     if (e != cudaSuccess) return e;
     if (cfg.CS > 8) {
-        e = cudaFuncSetAttribute(select_kernel<NSB>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
     }
     cudaLaunchConfig_t lc = {};
@@ -657,7 +714,7 @@ cudaError_t launch_select_t(const SelectArgs& a, const SelectConfig& cfg, uint64
     attr[0].val.clusterDim.z = 1;
     lc.attrs = attr;
     lc.numAttrs = 1;
-    return cudaLaunchKernelEx(&lc, select_kernel<NSB>, a);
+    return cudaLaunchKernelEx(&lc, fn, a);
 }
 
 }  // namespace
