@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsuco_b200.so")
+LIB_PATH = os.environ.get("SUCO_LIB") or os.path.join(HERE, "libsuco_b200.so")  # SUCO_LIB: tuning builds only
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

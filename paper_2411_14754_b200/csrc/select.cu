@@ -41,13 +41,16 @@ namespace cg = cooperative_groups;
 namespace suco_gpu {
 namespace {
 
-constexpr uint32_t kThreads = 512;
+#ifndef SUCO_SELECT_THREADS
+#define SUCO_SELECT_THREADS 512
+#endif
+constexpr uint32_t kThreads = SUCO_SELECT_THREADS;
 constexpr uint32_t kWarps = kThreads / 32;
-constexpr uint32_t kCap = 2048;    // retrieved cells staged per chunk (4 per thread)
+constexpr uint32_t kCap = 4 * kThreads;  // retrieved cells staged per chunk (4 per thread)
 constexpr uint32_t kUnits = 4096;  // 32-id units described per window
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr uint32_t kChAlign = 4 * 32 * kWarps;  // CH multiple of this: whole words per lane-step
-constexpr uint32_t kChMax = 96 * 2048;          // 192 KiB of counters per CTA at most
+constexpr uint32_t kSmemLimit = 232448;        // opt-in dynamic shared memory per block on sm_100
 
 __host__ __device__ inline uint32_t hist_stride(uint32_t ns) { return ns + 2; }
 
@@ -723,6 +726,13 @@ static SelectConfig plan_for(uint64_t n, uint32_t ns, uint32_t CS) {
     SelectConfig c;
     c.CS = CS;
     const uint64_t per = (n + c.CS - 1) / c.CS;
+    // largest slab whose counters + unit descriptors + bookkeeping fit the opt-in limit
+    uint32_t kChMax = ((kSmemLimit - static_cast<uint32_t>(smem_bytes(0, 1, ns)) - 4096) / kChAlign) * kChAlign;
+    {
+        const uint64_t slabs = (n + kChMax - 1) / kChMax;
+        const uint32_t rounds = static_cast<uint32_t>((slabs + CS - 1) / CS);
+        while (kChMax > kChAlign && smem_bytes(kChMax, rounds, ns) > kSmemLimit) kChMax -= kChAlign;
+    }
     if (per <= kChMax) {
         c.CH = static_cast<uint32_t>(((per + kChAlign - 1) / kChAlign) * kChAlign);
         if (c.CH == 0) c.CH = kChAlign;
