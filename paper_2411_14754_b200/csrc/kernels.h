@@ -54,12 +54,14 @@ struct SelectArgs {
     uint64_t n;
     uint32_t ns, K, nslabs, CH, rounds, CS;
     uint64_t m;
-    uint32_t* cands;      // nq x m (ascending ids)
+    uint64_t nq;          // queries in this launch (persistent clusters loop over them)
+    uint32_t* cands;      // nq x m (candidate set, unordered)
     uint8_t* scores_dbg;  // optional nq x n
 };
 struct SelectConfig {
     uint32_t CS, CH, nslabs, rounds;
     size_t smem;
+    int clusters;  // resident clusters (persistent grid); 0 = unknown
 };
 SelectConfig plan_select(uint64_t n, uint32_t ns, int cluster_size);
 cudaError_t launch_select(const SelectArgs& a, const SelectConfig& cfg, uint64_t nq, cudaStream_t st);

@@ -516,134 +516,137 @@ __global__ void __launch_bounds__(kThreads, 1) select_kernel(SelectArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     cg::cluster_group cluster = cg::this_cluster();
     const uint32_t rank = cluster.block_rank();
-    const uint64_t q = blockIdx.x / a.CS;
     const Smem s = carve(smem, a.CH, a.rounds, a.ns);
     const uint32_t hs = hist_stride(a.ns);
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const bool swar = a.ns <= 127;
+    // persistent clusters: cluster c handles queries c, c + C, c + 2C, ...
+    const uint64_t nclusters = gridDim.x / a.CS;
+    for (uint64_t q = blockIdx.x / a.CS; q < a.nq; q += nclusters) {
 
-    // pass 1: count + histogram every owned slab
-    for (uint32_t r = 0; r < a.rounds; ++r) {
-        const uint32_t slab = r * a.CS + rank;
-        const uint64_t lo = static_cast<uint64_t>(slab) * a.CH;
-        const uint32_t len = slab < a.nslabs ? static_cast<uint32_t>(min_u64(a.CH, a.n - lo)) : 0u;
-        count_slab<NSB, KU, BRANCHY, PREFETCH>(a, s, q, slab, lo, len, s.hist + r * hs);
-        if (a.scores_dbg) {
-            for (uint32_t i = tid; i < len; i += kThreads) a.scores_dbg[q * a.n + lo + i] = s.cnt[i];
+        // pass 1: count + histogram every owned slab
+        for (uint32_t r = 0; r < a.rounds; ++r) {
+            const uint32_t slab = r * a.CS + rank;
+            const uint64_t lo = static_cast<uint64_t>(slab) * a.CH;
+            const uint32_t len = slab < a.nslabs ? static_cast<uint32_t>(min_u64(a.CH, a.n - lo)) : 0u;
+            count_slab<NSB, KU, BRANCHY, PREFETCH>(a, s, q, slab, lo, len, s.hist + r * hs);
+            if (a.scores_dbg) {
+                for (uint32_t i = tid; i < len; i += kThreads) a.scores_dbg[q * a.n + lo + i] = s.cnt[i];
+            }
+
         }
+        cluster.sync();
 
-    }
-    cluster.sync();
-
-    // threshold and per-slab quotas (warp 0), from every slab's histogram
-    if (warp == 0) {
-        const uint32_t G = a.nslabs;
-        uint32_t tot[NSB > 0 ? NSB + 1 : 1];
-        uint32_t T = 0;
-        uint64_t need = 0;
-        if constexpr (NSB > 0) {
-#pragma unroll
-            for (int t = 0; t <= NSB; ++t) tot[t] = 0;
-            for (uint32_t g = lane; g < G; g += 32) {
-                const uint32_t* h = cluster.map_shared_rank(s.hist, g % a.CS) + (g / a.CS) * hs;
-#pragma unroll
-                for (int t = 1; t <= NSB; ++t) {
-                    if ((uint32_t)t <= a.ns) tot[t] += h[t];
-                }
-            }
-#pragma unroll
-            for (int t = 1; t <= NSB; ++t) {
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) tot[t] += __shfl_xor_sync(kFull, tot[t], off);
-            }
-            for (int t = NSB; t >= 1; --t) {
-                if ((uint32_t)t <= a.ns && tot[t] >= a.m) {
-                    T = t;
-                    break;
-                }
-            }
-            uint32_t gt_total = 0;
-#pragma unroll
-            for (int t = 1; t <= NSB; ++t) {
-                if ((uint32_t)t == T + 1 && (uint32_t)t <= a.ns) gt_total = tot[t];
-            }
-            need = a.m - gt_total;
-        } else {
-            // generic (N_s > 32): one level at a time, top down
-            uint64_t prev = 0;
-            T = 0;
-            need = a.m;
-            for (uint32_t t = a.ns; t >= 1; --t) {
-                uint32_t c = 0;
+        // threshold and per-slab quotas (warp 0), from every slab's histogram
+        if (warp == 0) {
+            const uint32_t G = a.nslabs;
+            uint32_t tot[NSB > 0 ? NSB + 1 : 1];
+            uint32_t T = 0;
+            uint64_t need = 0;
+            if constexpr (NSB > 0) {
+    #pragma unroll
+                for (int t = 0; t <= NSB; ++t) tot[t] = 0;
                 for (uint32_t g = lane; g < G; g += 32) {
-                    c += (cluster.map_shared_rank(s.hist, g % a.CS) + (g / a.CS) * hs)[t];
+                    const uint32_t* h = cluster.map_shared_rank(s.hist, g % a.CS) + (g / a.CS) * hs;
+    #pragma unroll
+                    for (int t = 1; t <= NSB; ++t) {
+                        if ((uint32_t)t <= a.ns) tot[t] += h[t];
+                    }
                 }
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(kFull, c, off);
-                if (c >= a.m) {
-                    T = t;
-                    need = a.m - prev;
-                    break;
+    #pragma unroll
+                for (int t = 1; t <= NSB; ++t) {
+    #pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) tot[t] += __shfl_xor_sync(kFull, tot[t], off);
                 }
-                prev = c;
+                for (int t = NSB; t >= 1; --t) {
+                    if ((uint32_t)t <= a.ns && tot[t] >= a.m) {
+                        T = t;
+                        break;
+                    }
+                }
+                uint32_t gt_total = 0;
+    #pragma unroll
+                for (int t = 1; t <= NSB; ++t) {
+                    if ((uint32_t)t == T + 1 && (uint32_t)t <= a.ns) gt_total = tot[t];
+                }
+                need = a.m - gt_total;
+            } else {
+                // generic (N_s > 32): one level at a time, top down
+                uint64_t prev = 0;
+                T = 0;
+                need = a.m;
+                for (uint32_t t = a.ns; t >= 1; --t) {
+                    uint32_t c = 0;
+                    for (uint32_t g = lane; g < G; g += 32) {
+                        c += (cluster.map_shared_rank(s.hist, g % a.CS) + (g / a.CS) * hs)[t];
+                    }
+    #pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(kFull, c, off);
+                    if (c >= a.m) {
+                        T = t;
+                        need = a.m - prev;
+                        break;
+                    }
+                    prev = c;
+                }
+                if (T == 0) need = a.m - prev;
             }
-            if (T == 0) need = a.m - prev;
+            // quotas in global slab (= id) order
+            uint64_t ties_run = 0, out_run = 0;
+            for (uint32_t g0 = 0; g0 < G; g0 += 32) {
+                const uint32_t g = g0 + lane;
+                uint32_t ties = 0, gt = 0;
+                if (g < G) {
+                    const uint32_t* h = cluster.map_shared_rank(s.hist, g % a.CS) + (g / a.CS) * hs;
+                    const uint32_t geT = h[T];
+                    const uint32_t geT1 = T + 1 <= a.ns ? h[T + 1] : 0u;
+                    gt = geT1;
+                    ties = geT - geT1;
+                }
+                uint64_t tx = ties;
+    #pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const uint64_t y = __shfl_up_sync(kFull, tx, off);
+                    if (lane >= (uint32_t)off) tx += y;
+                }
+                const uint64_t tsum = __shfl_sync(kFull, tx, 31);
+                tx -= ties;
+                const uint64_t before = ties_run + tx;
+                const uint32_t quota = before >= need ? 0u : static_cast<uint32_t>(min_u64(ties, need - before));
+                uint64_t ox = gt + quota;
+                const uint64_t mine = ox;
+    #pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const uint64_t y = __shfl_up_sync(kFull, ox, off);
+                    if (lane >= (uint32_t)off) ox += y;
+                }
+                const uint64_t osum = __shfl_sync(kFull, ox, 31);
+                ox -= mine;
+                if (g < G && g % a.CS == rank) {
+                    s.rquota[g / a.CS] = quota;
+                    s.roff[g / a.CS] = static_cast<uint32_t>(out_run + ox);
+                }
+                ties_run += tsum;
+                out_run += osum;
+            }
+            if (lane == 0) s.misc[0] = T;
         }
-        // quotas in global slab (= id) order
-        uint64_t ties_run = 0, out_run = 0;
-        for (uint32_t g0 = 0; g0 < G; g0 += 32) {
-            const uint32_t g = g0 + lane;
-            uint32_t ties = 0, gt = 0;
-            if (g < G) {
-                const uint32_t* h = cluster.map_shared_rank(s.hist, g % a.CS) + (g / a.CS) * hs;
-                const uint32_t geT = h[T];
-                const uint32_t geT1 = T + 1 <= a.ns ? h[T + 1] : 0u;
-                gt = geT1;
-                ties = geT - geT1;
-            }
-            uint64_t tx = ties;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const uint64_t y = __shfl_up_sync(kFull, tx, off);
-                if (lane >= (uint32_t)off) tx += y;
-            }
-            const uint64_t tsum = __shfl_sync(kFull, tx, 31);
-            tx -= ties;
-            const uint64_t before = ties_run + tx;
-            const uint32_t quota = before >= need ? 0u : static_cast<uint32_t>(min_u64(ties, need - before));
-            uint64_t ox = gt + quota;
-            const uint64_t mine = ox;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const uint64_t y = __shfl_up_sync(kFull, ox, off);
-                if (lane >= (uint32_t)off) ox += y;
-            }
-            const uint64_t osum = __shfl_sync(kFull, ox, 31);
-            ox -= mine;
-            if (g < G && g % a.CS == rank) {
-                s.rquota[g / a.CS] = quota;
-                s.roff[g / a.CS] = static_cast<uint32_t>(out_run + ox);
-            }
-            ties_run += tsum;
-            out_run += osum;
-        }
-        if (lane == 0) s.misc[0] = T;
-    }
-    cluster.sync();  // peers finished reading our histograms
-    const uint32_t T = s.misc[0];
+        cluster.sync();  // peers finished reading our histograms
+        const uint32_t T = s.misc[0];
 
-    for (uint32_t r = 0; r < a.rounds; ++r) {
-        const uint32_t slab = r * a.CS + rank;
-        if (slab >= a.nslabs) break;
-        const uint64_t lo = static_cast<uint64_t>(slab) * a.CH;
-        const uint32_t len = static_cast<uint32_t>(min_u64(a.CH, a.n - lo));
-        if (a.rounds > 1) {
-            count_slab<NSB, KU, BRANCHY, PREFETCH>(a, s, q, slab, lo, len, s.hscratch);  // recount
+        for (uint32_t r = 0; r < a.rounds; ++r) {
+            const uint32_t slab = r * a.CS + rank;
+            if (slab >= a.nslabs) break;
+            const uint64_t lo = static_cast<uint64_t>(slab) * a.CH;
+            const uint32_t len = static_cast<uint32_t>(min_u64(a.CH, a.n - lo));
+            if (a.rounds > 1) {
+                count_slab<NSB, KU, BRANCHY, PREFETCH>(a, s, q, slab, lo, len, s.hscratch);  // recount
+            }
+            const uint32_t* h = s.hist + r * hs;
+            const uint32_t gt = T + 1 <= a.ns ? h[T + 1] : 0u;
+            emit_slab(a, s, q, lo, len, T, s.rquota[r], s.roff[r], gt, h[T] - gt, swar);
+            __syncthreads();
         }
-        const uint32_t* h = s.hist + r * hs;
-        const uint32_t gt = T + 1 <= a.ns ? h[T + 1] : 0u;
-        emit_slab(a, s, q, lo, len, T, s.rquota[r], s.roff[r], gt, h[T] - gt, swar);
-        __syncthreads();
     }
 }
 
@@ -706,7 +709,9 @@ cudaError_t launch_select_t(const SelectArgs& a, const SelectConfig& cfg, uint64
         if (e != cudaSuccess) return e;
     }
     cudaLaunchConfig_t lc = {};
-    lc.gridDim = dim3(static_cast<unsigned>(nq * cfg.CS));
+    uint64_t nclusters = nq;
+    if (cfg.clusters > 0) nclusters = min_u64(nq, static_cast<uint64_t>(cfg.clusters));
+    lc.gridDim = dim3(static_cast<unsigned>(nclusters * cfg.CS));
     lc.blockDim = dim3(kThreads);
     lc.dynamicSmemBytes = cfg.smem;
     lc.stream = st;
@@ -725,6 +730,7 @@ cudaError_t launch_select_t(const SelectArgs& a, const SelectConfig& cfg, uint64
 static SelectConfig plan_for(uint64_t n, uint32_t ns, uint32_t CS) {
     SelectConfig c;
     c.CS = CS;
+    c.clusters = 0;
     const uint64_t per = (n + c.CS - 1) / c.CS;
     // largest slab whose counters + unit descriptors + bookkeeping fit the opt-in limit
     uint32_t kChMax = ((kSmemLimit - static_cast<uint32_t>(smem_bytes(0, 1, ns)) - 4096) / kChAlign) * kChAlign;
@@ -784,7 +790,11 @@ static int active_clusters_ns(uint32_t ns, const SelectConfig& c) {
 // round (clusters must fit inside a GPC, so 8-CTA clusters strand SMs on a
 // 148-SM B200); SUCO_CLUSTER (cluster_size > 0) forces a size.
 SelectConfig plan_select(uint64_t n, uint32_t ns, int cluster_size) {
-    if (cluster_size > 0) return plan_for(n, ns, static_cast<uint32_t>(cluster_size));
+    if (cluster_size > 0) {
+        SelectConfig c = plan_for(n, ns, static_cast<uint32_t>(cluster_size));
+        c.clusters = active_clusters_ns(ns, c);
+        return c;
+    }
     SelectConfig best = plan_for(n, ns, 8);
     long best_score = -1;
     for (uint32_t cs = 8; cs >= 1; --cs) {
@@ -794,6 +804,7 @@ SelectConfig plan_select(uint64_t n, uint32_t ns, int cluster_size) {
         if (score > best_score) {
             best_score = score;
             best = c;
+            best.clusters = static_cast<int>(score / (cs * (c.rounds == 1 ? 2 : 1)));
         }
     }
     return best;
