@@ -160,8 +160,14 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline query time (rank 0)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="no L2 flush/e2e/cpu legs (for ncu)")
+    ap.add_argument("--alpha", type=float, default=None, help="experiment: override the config's alpha")
+    ap.add_argument("--beta", type=float, default=None, help="experiment: override the config's beta")
     args = ap.parse_args()
     cfg = bench_data.CONFIGS[args.config]
+    if args.alpha is not None or args.beta is not None:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, alpha=args.alpha if args.alpha is not None else cfg.alpha,
+                                  beta=args.beta if args.beta is not None else cfg.beta)
 
     if args.impl == "reference":
         run_reference_arm(args, cfg)

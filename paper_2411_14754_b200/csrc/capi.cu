@@ -327,7 +327,7 @@ void run_tile(suco_gpu_index* x, const float* d_q, uint64_t nt, uint64_t target,
     sa.rounds = x->sel.rounds;
     sa.CS = x->sel.CS;
     sa.m = m;
-    sa.nq = nt;
+    sa.nq = nt;  // non-persistent grid below: one cluster per query (hardware cluster scheduling)
     sa.cands = x->cands.p;
     sa.scores_dbg = dbg ? dbg->scores : nullptr;
     CUDA_TRY(launch_select(sa, x->sel, nt, st));

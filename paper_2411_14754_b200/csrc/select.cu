@@ -709,8 +709,10 @@ cudaError_t launch_select_t(const SelectArgs& a, const SelectConfig& cfg, uint64
         if (e != cudaSuccess) return e;
     }
     cudaLaunchConfig_t lc = {};
-    uint64_t nclusters = nq;
-    if (cfg.clusters > 0) nclusters = min_u64(nq, static_cast<uint64_t>(cfg.clusters));
+    // One cluster per query: measured faster than a persistent grid of resident
+    // clusters (the hardware re-fills freed GPC slots dynamically; static
+    // round-robin over queries left SMs idle behind the slowest cluster).
+    const uint64_t nclusters = nq;
     lc.gridDim = dim3(static_cast<unsigned>(nclusters * cfg.CS));
     lc.blockDim = dim3(kThreads);
     lc.dynamicSmemBytes = cfg.smem;
