@@ -45,9 +45,12 @@ namespace {
 #define SUCO_SELECT_THREADS 512
 #endif
 constexpr uint32_t kThreads = SUCO_SELECT_THREADS;
+#ifndef SUCO_SELECT_MINB
+#define SUCO_SELECT_MINB 1
+#endif
 constexpr uint32_t kWarps = kThreads / 32;
 constexpr uint32_t kCap = 4 * kThreads;  // retrieved cells staged per chunk (4 per thread)
-constexpr uint32_t kUnits = 4096;  // 32-id units described per window
+constexpr uint32_t kUnits = 8 * kThreads;  // 32-id units described per window
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr uint32_t kChAlign = 4 * 32 * kWarps;  // CH multiple of this: whole words per lane-step
 constexpr uint32_t kSmemLimit = 232448;        // opt-in dynamic shared memory per block on sm_100
@@ -512,7 +515,7 @@ __device__ void emit_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint64
 }
 
 template <int NSB, int KU = 16, bool BRANCHY = true, bool PREFETCH = true>
-__global__ void __launch_bounds__(kThreads, 1) select_kernel(SelectArgs a) {
+__global__ void __launch_bounds__(kThreads, SUCO_SELECT_MINB) select_kernel(SelectArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     cg::cluster_group cluster = cg::this_cluster();
     const uint32_t rank = cluster.block_rank();
