@@ -57,6 +57,7 @@ struct SelectArgs {
     uint64_t nq;          // queries in this launch (persistent clusters loop over them)
     uint32_t* cands;      // nq x m (candidate set, unordered)
     uint8_t* scores_dbg;  // optional nq x n
+    long long* prof;      // optional debug phase timers (8 x u64)
 };
 struct SelectConfig {
     uint32_t CS, CH, nslabs, rounds;

@@ -57,6 +57,18 @@ constexpr uint32_t kSmemLimit = 232448;        // opt-in dynamic shared memory p
 
 __host__ __device__ inline uint32_t hist_stride(uint32_t ns) { return ns + 2; }
 
+// Debug phase timing (SelectArgs::prof != nullptr): thread 0 of every CTA adds
+// clock64 deltas per phase into prof[0..7].
+#define SEL_MARK(i)                                                                     \
+    do {                                                                                \
+        if (a.prof && threadIdx.x == 0) {                                               \
+            const long long now = clock64();                                            \
+            atomicAdd(reinterpret_cast<unsigned long long*>(a.prof) + (i),              \
+                      static_cast<unsigned long long>(now - t_mark));                   \
+            t_mark = now;                                                               \
+        }                                                                               \
+    } while (0)
+
 struct Smem {
     uint8_t* cnt;        // CH
     uint32_t* hist;      // rounds x hist_stride: [0] = slab length, [t] = #score >= t
@@ -224,7 +236,7 @@ __device__ __forceinline__ void rmw_wave(const Smem& s, const Wave<KU>& w, uint3
 // repeats only across subspaces).
 template <int NSB, int KU, bool BRANCHY, bool PREFETCH>
 __device__ void count_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint32_t slab, uint64_t lo, uint32_t len,
-                           uint32_t* hist) {
+                           uint32_t* hist, long long& t_mark) {
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     uint4* c4 = reinterpret_cast<uint4*>(s.cnt);
     for (uint32_t i = tid; i < a.CH / 16; i += kThreads) c4[i] = make_uint4(0, 0, 0, 0);
@@ -238,6 +250,7 @@ __device__ void count_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint3
         s.sub_start[a.ns] = acc;
     }
     __syncthreads();
+    SEL_MARK(0);
     if (len == 0) return;
     const uint32_t TC = s.sub_start[a.ns];
     const uint32_t stride = a.nslabs + 1;
@@ -266,6 +279,7 @@ __device__ void count_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint3
         }
         uint32_t UT;
         const uint32_t up0 = block_excl_scan(nu4[0] + nu4[1] + nu4[2] + nu4[3], s.wtmp, &UT);
+        SEL_MARK(1);
         // unit index where each subspace starts within this chunk
         {
             uint32_t up = up0, sb2 = sub_first;
@@ -375,6 +389,7 @@ __device__ void count_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint3
     }
     ih.flush(hist, a.ns);
     __syncthreads();
+    SEL_MARK(2);
 }
 
 // Mask (0x80 per byte) of the bytes of word `wi` that are >= t and inside the slab.
@@ -526,19 +541,21 @@ __global__ void __launch_bounds__(kThreads, SUCO_SELECT_MINB) select_kernel(Sele
     // persistent clusters: cluster c handles queries c, c + C, c + 2C, ...
     const uint64_t nclusters = gridDim.x / a.CS;
     for (uint64_t q = blockIdx.x / a.CS; q < a.nq; q += nclusters) {
+        long long t_mark = a.prof ? clock64() : 0;
 
         // pass 1: count + histogram every owned slab
         for (uint32_t r = 0; r < a.rounds; ++r) {
             const uint32_t slab = r * a.CS + rank;
             const uint64_t lo = static_cast<uint64_t>(slab) * a.CH;
             const uint32_t len = slab < a.nslabs ? static_cast<uint32_t>(min_u64(a.CH, a.n - lo)) : 0u;
-            count_slab<NSB, KU, BRANCHY, PREFETCH>(a, s, q, slab, lo, len, s.hist + r * hs);
+            count_slab<NSB, KU, BRANCHY, PREFETCH>(a, s, q, slab, lo, len, s.hist + r * hs, t_mark);
             if (a.scores_dbg) {
                 for (uint32_t i = tid; i < len; i += kThreads) a.scores_dbg[q * a.n + lo + i] = s.cnt[i];
             }
 
         }
         cluster.sync();
+        SEL_MARK(3);
 
         // threshold and per-slab quotas (warp 0), from every slab's histogram
         if (warp == 0) {
@@ -635,6 +652,7 @@ __global__ void __launch_bounds__(kThreads, SUCO_SELECT_MINB) select_kernel(Sele
             if (lane == 0) s.misc[0] = T;
         }
         cluster.sync();  // peers finished reading our histograms
+        SEL_MARK(4);
         const uint32_t T = s.misc[0];
 
         for (uint32_t r = 0; r < a.rounds; ++r) {
@@ -643,11 +661,12 @@ __global__ void __launch_bounds__(kThreads, SUCO_SELECT_MINB) select_kernel(Sele
             const uint64_t lo = static_cast<uint64_t>(slab) * a.CH;
             const uint32_t len = static_cast<uint32_t>(min_u64(a.CH, a.n - lo));
             if (a.rounds > 1) {
-                count_slab<NSB, KU, BRANCHY, PREFETCH>(a, s, q, slab, lo, len, s.hscratch);  // recount
+                count_slab<NSB, KU, BRANCHY, PREFETCH>(a, s, q, slab, lo, len, s.hscratch, t_mark);  // recount
             }
             const uint32_t* h = s.hist + r * hs;
             const uint32_t gt = T + 1 <= a.ns ? h[T + 1] : 0u;
             emit_slab(a, s, q, lo, len, T, s.rquota[r], s.roff[r], gt, h[T] - gt, swar);
+            SEL_MARK(5);
             __syncthreads();
         }
     }
@@ -732,6 +751,8 @@ cudaError_t launch_select_t(const SelectArgs& a, const SelectConfig& cfg, uint64
 
 }  // namespace
 
+cudaError_t launch_select_dispatch(const SelectArgs& a, const SelectConfig& cfg, uint64_t nq, cudaStream_t st);
+
 static SelectConfig plan_for(uint64_t n, uint32_t ns, uint32_t CS) {
     SelectConfig c;
     c.CS = CS;
@@ -815,8 +836,28 @@ SelectConfig plan_select(uint64_t n, uint32_t ns, int cluster_size) {
     return best;
 }
 
-cudaError_t launch_select(const SelectArgs& a, const SelectConfig& cfg, uint64_t nq, cudaStream_t st) {
+cudaError_t launch_select(const SelectArgs& a0, const SelectConfig& cfg, uint64_t nq, cudaStream_t st) {
     if (nq == 0) return cudaSuccess;
+    SelectArgs a = a0;
+    unsigned long long* prof = nullptr;
+    if (std::getenv("SUCO_SELECT_PROF")) {  // debug: per-phase clock64 totals to stderr
+        cudaMalloc(&prof, 64);
+        cudaMemsetAsync(prof, 0, 64, st);
+        a.prof = reinterpret_cast<long long*>(prof);
+        cudaError_t e = launch_select_dispatch(a, cfg, nq, st);
+        unsigned long long h[8];
+        cudaMemcpyAsync(h, prof, 64, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        cudaFree(prof);
+        const double ctas = double(nq) * cfg.CS;
+        std::fprintf(stderr, "[select prof] cycles per CTA: zero+init %.0f staging %.0f counting %.0f csync1 %.0f quota+csync2 %.0f emit %.0f\n",
+                     h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas, h[4] / ctas, h[5] / ctas);
+        return e;
+    }
+    return launch_select_dispatch(a, cfg, nq, st);
+}
+
+cudaError_t launch_select_dispatch(const SelectArgs& a, const SelectConfig& cfg, uint64_t nq, cudaStream_t st) {
     if (a.ns <= 8) return launch_select_t<8>(a, cfg, nq, st);
     if (a.ns <= 16) return launch_select_t<16>(a, cfg, nq, st);
     if (a.ns <= 32) return launch_select_t<32>(a, cfg, nq, st);
