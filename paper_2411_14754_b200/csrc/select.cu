@@ -490,28 +490,47 @@ __device__ void emit_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint64
         }
     }
     if (all_ties || quota == 0) return;
-    // boundary slab: the first `quota` ties (== T) in id order, after the gt region
+    // boundary slab: the first `quota` ties (== T) in id order, after the gt
+    // region. Warps own contiguous vector ranges; lanes step over 16-counter
+    // vectors, so both passes read shared memory conflict-free.
     uint32_t* tout = out + gt;
-    const uint32_t wpw = (words + kWarps - 1) / kWarps;
-    const uint32_t wa = min(words, warp * wpw), wb = min(words, wa + wpw);
+    const uint32_t last_vi = (len - 1) / 16;
+    const uint32_t kT = (0x80u - (T ? T : 1u)) * 0x01010101u, kT1 = (0x80u - (T + 1)) * 0x01010101u;
+    auto tie_mask = [&](uint32_t w) -> uint32_t {
+        if (!swar) return sel_mask(w, 0, T, 4, false) & ~sel_mask(w, 0, T + 1, 4, false);
+        const uint32_t ge1 = (w + kT1) & 0x80808080u;
+        const uint32_t ge0 = T ? ((w + kT) & 0x80808080u) : 0x80808080u;
+        return ge0 & ~ge1;
+    };
+    auto vec_ties = [&](uint32_t vi, uint32_t (&mt)[4]) {
+        const uint4 v = w128[vi];
+        mt[0] = tie_mask(v.x);
+        mt[1] = tie_mask(v.y);
+        mt[2] = tie_mask(v.z);
+        mt[3] = tie_mask(v.w);
+        if (vi == last_vi) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) mt[u] &= sel_mask(0xffffffffu, vi * 4 + u, 0, len, true);
+        }
+    };
+    const uint32_t vpw = (nvec + kWarps - 1) / kWarps;
+    const uint32_t va = min(nvec, warp * vpw), vb = min(nvec, va + vpw);
     uint32_t e_tot = 0;
-    for (uint32_t wi = wa + lane; wi < wb; wi += 32) {
-        const uint32_t w = w32[wi];
-        e_tot += __popc(sel_mask(w, wi, T, len, swar) & ~sel_mask(w, wi, T + 1, len, swar));
+    for (uint32_t vi = va + lane; vi < vb; vi += 32) {
+        uint32_t mt[4];
+        vec_ties(vi, mt);
+        e_tot += __popc(mt[0]) + __popc(mt[1]) + __popc(mt[2]) + __popc(mt[3]);
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) e_tot += __shfl_xor_sync(kFull, e_tot, off);
     uint32_t tmp;
     const uint32_t e_base = block_excl_scan(lane == 0 ? e_tot : 0u, s.wtmp, &tmp);
     uint32_t eb = __shfl_sync(kFull, e_base, 0);
-    for (uint32_t w0 = wa; w0 < wb && eb < quota; w0 += 32) {
-        const uint32_t wi = w0 + lane;
-        uint32_t mt = 0;
-        if (wi < wb) {
-            const uint32_t w = w32[wi];
-            mt = sel_mask(w, wi, T, len, swar) & ~sel_mask(w, wi, T + 1, len, swar);
-        }
-        const uint32_t e = __popc(mt);
+    for (uint32_t v0 = va; v0 < vb && eb < quota; v0 += 32) {
+        const uint32_t vi = v0 + lane;
+        uint32_t mt[4] = {0, 0, 0, 0};
+        if (vi < vb) vec_ties(vi, mt);
+        const uint32_t e = __popc(mt[0]) + __popc(mt[1]) + __popc(mt[2]) + __popc(mt[3]);
         uint32_t ex = e;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
@@ -520,10 +539,14 @@ __device__ void emit_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint64
         }
         const uint32_t esum = __shfl_sync(kFull, ex, 31);
         uint32_t r = eb + ex - e;
-        while (mt && r < quota) {
-            const uint32_t bit = __ffs(mt) - 1;
-            tout[r++] = static_cast<uint32_t>(lo) + wi * 4 + (bit >> 3);
-            mt &= mt - 1;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            uint32_t mm = mt[u];
+            while (mm && r < quota) {
+                const uint32_t bit = __ffs(mm) - 1;
+                tout[r++] = static_cast<uint32_t>(lo) + (vi * 4 + u) * 4 + (bit >> 3);
+                mm &= mm - 1;
+            }
         }
         eb += esum;
     }
