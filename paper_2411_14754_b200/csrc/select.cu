@@ -209,6 +209,22 @@ __device__ __forceinline__ void load_wave(const Smem& s, const uint32_t* ids, ui
     w.mask = mask;
 }
 
+// Shared-memory atomic variant: safe across subspaces, so no barriers needed.
+template <int NSB, int KU>
+__device__ __forceinline__ void atomic_wave(const Smem& s, const Wave<KU>& w, uint32_t lo, IncHist<NSB>& ih,
+                                            uint32_t* hist) {
+    uint32_t* c32 = reinterpret_cast<uint32_t*>(s.cnt);
+#pragma unroll
+    for (int u = 0; u < KU; ++u) {
+        if (w.mask & (1u << u)) {
+            const uint32_t l = w.id[u] - lo;
+            const uint32_t sh = (l & 3u) * 8u;
+            const uint32_t old = atomicAdd(c32 + (l >> 2), 1u << sh);
+            ih.add(((old >> sh) & 0xffu) + 1u, hist);
+        }
+    }
+}
+
 template <int NSB, int KU>
 __device__ __forceinline__ void rmw_wave(const Smem& s, const Wave<KU>& w, uint32_t lo, IncHist<NSB>& ih,
                                          uint32_t* hist) {
@@ -234,7 +250,7 @@ __device__ __forceinline__ void rmw_wave(const Smem& s, const Wave<KU>& w, uint3
 // then does the counter RMWs, with the first wave of subspace s+1 already in
 // flight while subspace s does its RMWs. A barrier separates subspaces (an id
 // repeats only across subspaces).
-template <int NSB, int KU, bool BRANCHY, bool PREFETCH>
+template <int NSB, int KU, bool BRANCHY, bool PREFETCH, bool ATOMIC = false>
 __device__ void count_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint32_t slab, uint64_t lo, uint32_t len,
                            uint32_t* hist, long long& t_mark) {
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
@@ -329,7 +345,35 @@ __device__ void count_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint3
                 ua = A + static_cast<uint32_t>((static_cast<uint64_t>(T) * warp) / kWarps);
                 ub = A + static_cast<uint32_t>((static_cast<uint64_t>(T) * (warp + 1)) / kWarps);
             };
-            if constexpr (PREFETCH) {
+            if constexpr (ATOMIC) {
+                // all units of the window as one flat list split over the warps; 2-deep pipeline
+                const uint32_t nu = u1 - u0;
+                const uint32_t wa = static_cast<uint32_t>((static_cast<uint64_t>(nu) * warp) / kWarps);
+                const uint32_t wb = static_cast<uint32_t>((static_cast<uint64_t>(nu) * (warp + 1)) / kWarps);
+                // units never straddle subspaces; find each wave's subspace by its first unit
+                auto ids_of = [&](uint32_t unit) {
+                    uint32_t sb4 = sb;
+                    while (sb4 + 1 < se && s.sub_unit[sb4 + 1] <= unit + u0) ++sb4;
+                    return a.ids + static_cast<uint64_t>(sb4) * a.n;
+                };
+                for (uint32_t ua = wa; ua < wb; ua += KU) {
+                    // a wave may cross a subspace boundary: split it
+                    uint32_t ub = min(wb, ua + KU);
+                    const uint32_t* ids = ids_of(ua);
+                    uint32_t sb4 = sb;
+                    while (sb4 + 1 < se && s.sub_unit[sb4 + 1] <= ua + u0) ++sb4;
+                    if (sb4 + 1 < se && s.sub_unit[sb4 + 1] - u0 < ub) ub = s.sub_unit[sb4 + 1] - u0;
+                    Wave<KU> w;
+                    load_wave<KU, BRANCHY>(s, ids, ua, ub, w);
+                    atomic_wave<NSB, KU>(s, w, static_cast<uint32_t>(lo), ih, hist);
+                    ua = ub - KU;  // resume right after the split point
+                    if (++waves_since_flush * KU >= 240) {
+                        ih.flush(hist, a.ns);
+                        waves_since_flush = 0;
+                    }
+                }
+                __syncthreads();
+            } else if constexpr (PREFETCH) {
                 Wave<KU> cur, nxt;
                 uint32_t ua, ub;
                 range(sb, ua, ub);
@@ -416,7 +460,7 @@ __device__ __forceinline__ uint32_t sel_mask(uint32_t w, uint32_t wi, uint32_t t
 // the slab where the tie quota is cut needs id order, and only for its ties,
 // which a two-pass warp-ordered scan emits after the unordered region.
 __device__ void emit_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint64_t lo, uint32_t len, uint32_t T,
-                          uint32_t quota, uint32_t base, uint32_t gt, uint32_t ties, bool swar) {
+                          uint32_t quota, uint32_t base, uint32_t gt, uint32_t ties, bool swar, long long& t_mark) {
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t* w32 = reinterpret_cast<const uint32_t*>(s.cnt);
     const uint4* w128 = reinterpret_cast<const uint4*>(s.cnt);
@@ -428,9 +472,25 @@ __device__ void emit_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint64
     if (tid == 0) s.misc[1] = 0;
     __syncthreads();
     if (gt + (all_ties ? ties : 0u) > 0) {
-        const uint32_t last_vi = (len - 1) / 16;
+        // vectors [0, full) lie inside the slab; at most one partial vector follows
+        const uint32_t full = len / 16;
         const uint32_t kq = (0x80u - (tsel ? tsel : 1u)) * 0x01010101u;
         constexpr uint32_t kV = 4;  // uint4 vectors per lane per step (64 counters)
+        auto sel4 = [&](const uint4& v, uint32_t (&m)[4]) {
+            if (tsel == 0) {
+                m[0] = m[1] = m[2] = m[3] = 0x80808080u;
+            } else if (swar) {
+                m[0] = (v.x + kq) & 0x80808080u;
+                m[1] = (v.y + kq) & 0x80808080u;
+                m[2] = (v.z + kq) & 0x80808080u;
+                m[3] = (v.w + kq) & 0x80808080u;
+            } else {
+                m[0] = sel_mask(v.x, 0, tsel, 4, false);
+                m[1] = sel_mask(v.y, 0, tsel, 4, false);
+                m[2] = sel_mask(v.z, 0, tsel, 4, false);
+                m[3] = sel_mask(v.w, 0, tsel, 4, false);
+            }
+        };
         for (uint32_t v0 = 0; v0 < nvec; v0 += kThreads * kV) {
             uint32_t m[kV][4];
             uint32_t c = 0;
@@ -438,45 +498,29 @@ __device__ void emit_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint64
             for (uint32_t j = 0; j < kV; ++j) {
                 const uint32_t vi = v0 + j * kThreads + tid;
                 m[j][0] = m[j][1] = m[j][2] = m[j][3] = 0;
-                if (vi < nvec) {
-                    const uint4 v = w128[vi];
-                    if (tsel == 0) {
-                        m[j][0] = m[j][1] = m[j][2] = m[j][3] = 0x80808080u;
-                    } else if (swar) {
-                        m[j][0] = (v.x + kq) & 0x80808080u;
-                        m[j][1] = (v.y + kq) & 0x80808080u;
-                        m[j][2] = (v.z + kq) & 0x80808080u;
-                        m[j][3] = (v.w + kq) & 0x80808080u;
-                    } else {
-                        const uint32_t ww[4] = {v.x, v.y, v.z, v.w};
+                if (vi < full) {
+                    sel4(w128[vi], m[j]);
+                } else if (vi < nvec) {  // the partial tail vector
+                    sel4(w128[vi], m[j]);
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) m[j][u] = sel_mask(ww[u], 0, tsel, 4, false);
-                    }
-                    if (vi == last_vi) {
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) m[j][u] &= sel_mask(0xffffffffu, vi * 4 + u, 0, len, true);
-                    }
-                    c += __popc(m[j][0]) + __popc(m[j][1]) + __popc(m[j][2]) + __popc(m[j][3]);
+                    for (int u = 0; u < 4; ++u) m[j][u] &= sel_mask(0xffffffffu, vi * 4 + u, 0, len, true);
                 }
+                c += __popc(m[j][0]) + __popc(m[j][1]) + __popc(m[j][2]) + __popc(m[j][3]);
             }
             if (!__any_sync(kFull, c != 0)) continue;
-            // warp-aggregated slot reservation
-            uint32_t x = c;
+            uint32_t x = c;  // warp-aggregated slot reservation
 #pragma unroll
             for (int off = 1; off < 32; off <<= 1) {
                 const uint32_t y = __shfl_up_sync(kFull, x, off);
                 if (lane >= (uint32_t)off) x += y;
             }
-            const uint32_t wsum = __shfl_sync(kFull, x, 31);
             uint32_t wbase = 0;
-            if (lane == 31) wbase = atomicAdd(&s.misc[1], wsum);
+            if (lane == 31) wbase = atomicAdd(&s.misc[1], x);
             wbase = __shfl_sync(kFull, wbase, 31);
-            uint32_t pos = wbase + x - c;
             if (c) {
-#pragma unroll
+                uint32_t pos = wbase + x - c;
                 for (uint32_t j = 0; j < kV; ++j) {
                     const uint32_t vi = v0 + j * kThreads + tid;
-#pragma unroll
                     for (int u = 0; u < 4; ++u) {
                         uint32_t mm = m[j][u];
                         while (mm) {
@@ -489,6 +533,7 @@ __device__ void emit_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint64
             }
         }
     }
+    SEL_MARK(5);
     if (all_ties || quota == 0) return;
     // boundary slab: the first `quota` ties (== T) in id order, after the gt
     // region. Warps own contiguous vector ranges; lanes step over 16-counter
@@ -552,7 +597,7 @@ __device__ void emit_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint64
     }
 }
 
-template <int NSB, int KU = 16, bool BRANCHY = true, bool PREFETCH = true>
+template <int NSB, int KU = 8, bool BRANCHY = true, bool PREFETCH = false, bool ATOMIC = false>
 __global__ void __launch_bounds__(kThreads, SUCO_SELECT_MINB) select_kernel(SelectArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     cg::cluster_group cluster = cg::this_cluster();
@@ -571,7 +616,7 @@ __global__ void __launch_bounds__(kThreads, SUCO_SELECT_MINB) select_kernel(Sele
             const uint32_t slab = r * a.CS + rank;
             const uint64_t lo = static_cast<uint64_t>(slab) * a.CH;
             const uint32_t len = slab < a.nslabs ? static_cast<uint32_t>(min_u64(a.CH, a.n - lo)) : 0u;
-            count_slab<NSB, KU, BRANCHY, PREFETCH>(a, s, q, slab, lo, len, s.hist + r * hs, t_mark);
+            count_slab<NSB, KU, BRANCHY, PREFETCH, ATOMIC>(a, s, q, slab, lo, len, s.hist + r * hs, t_mark);
             if (a.scores_dbg) {
                 for (uint32_t i = tid; i < len; i += kThreads) a.scores_dbg[q * a.n + lo + i] = s.cnt[i];
             }
@@ -684,12 +729,12 @@ __global__ void __launch_bounds__(kThreads, SUCO_SELECT_MINB) select_kernel(Sele
             const uint64_t lo = static_cast<uint64_t>(slab) * a.CH;
             const uint32_t len = static_cast<uint32_t>(min_u64(a.CH, a.n - lo));
             if (a.rounds > 1) {
-                count_slab<NSB, KU, BRANCHY, PREFETCH>(a, s, q, slab, lo, len, s.hscratch, t_mark);  // recount
+                count_slab<NSB, KU, BRANCHY, PREFETCH, ATOMIC>(a, s, q, slab, lo, len, s.hscratch, t_mark);  // recount
             }
             const uint32_t* h = s.hist + r * hs;
             const uint32_t gt = T + 1 <= a.ns ? h[T + 1] : 0u;
-            emit_slab(a, s, q, lo, len, T, s.rquota[r], s.roff[r], gt, h[T] - gt, swar);
-            SEL_MARK(5);
+            emit_slab(a, s, q, lo, len, T, s.rquota[r], s.roff[r], gt, h[T] - gt, swar, t_mark);
+            SEL_MARK(6);
             __syncthreads();
         }
     }
@@ -726,8 +771,9 @@ SelectFn pick_variant() {
     if constexpr (NSB == 8) {
         const char* v = std::getenv("SUCO_SELECT_VARIANT");
         if (v) {
-            int ku = 16, br = 1, pf = 1;
-            std::sscanf(v, "%d,%d,%d", &ku, &br, &pf);
+            int ku = 16, br = 1, pf = 1, at = 0;
+            std::sscanf(v, "%d,%d,%d,%d", &ku, &br, &pf, &at);
+            if (at) return ku == 8 ? select_kernel<8, 8, true, false, true> : select_kernel<8, 16, true, false, true>;
             const int key = (ku == 8 ? 0 : 4) | (br ? 2 : 0) | (pf ? 1 : 0);
             switch (key) {
                 case 0: return select_kernel<8, 8, false, false>;
@@ -873,8 +919,8 @@ cudaError_t launch_select(const SelectArgs& a0, const SelectConfig& cfg, uint64_
         cudaStreamSynchronize(st);
         cudaFree(prof);
         const double ctas = double(nq) * cfg.CS;
-        std::fprintf(stderr, "[select prof] cycles per CTA: zero+init %.0f staging %.0f counting %.0f csync1 %.0f quota+csync2 %.0f emit %.0f\n",
-                     h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas, h[4] / ctas, h[5] / ctas);
+        std::fprintf(stderr, "[select prof] cycles per CTA: zero+init %.0f staging %.0f counting %.0f csync1 %.0f quota+csync2 %.0f emit-unordered %.0f emit-ordered(boundary) %.0f\n",
+                     h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas, h[4] / ctas, h[5] / ctas, h[6] / ctas);
         return e;
     }
     return launch_select_dispatch(a, cfg, nq, st);
