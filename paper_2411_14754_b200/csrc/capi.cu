@@ -110,19 +110,37 @@ struct suco_gpu_index {
     DevBuf<uint32_t> slab_off;   // ns x K x (nslabs+1)
     SelectConfig sel{};
     float data_int_max = -1.f;  // integer certificate of the dataset (rerank fp32 path)
-    // query scratch
-    DevBuf<float> q;
-    DevBuf<uint32_t> cells, ncells, cands, out_ids, all_id;
-    DevBuf<double> out_d, all_d;
+    // query pipeline: tiles flow traverse -> select -> rerank on three streams,
+    // double-buffered scratch, so neighbouring tiles overlap on the device.
+    struct Slot {
+        DevBuf<float> q;
+        DevBuf<uint32_t> cells, ncells, cands, out_ids, all_id;
+        DevBuf<double> out_d, all_d;
+        cudaEvent_t trav = nullptr, sel = nullptr, rr = nullptr;
+    };
+    Slot slot[2];
+    cudaStream_t pipe[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     // stage profiling (suco_gpu_set_profiling)
     bool profile = false;
-    std::vector<cudaEvent_t> events;  // 4 per tile: before traverse/select/rerank, after rerank
-    uint32_t tiles = 0;
+    std::vector<cudaEvent_t> events;  // pairs (start, end) per profiled stage launch
+    std::vector<int> event_stage;     // stage of each pair
+    uint32_t pairs = 0;
     DevBuf<unsigned long long> stat_cum;
     uint64_t last_nq = 0, last_m = 0;
 
     ~suco_gpu_index() {
         for (cudaEvent_t e : events) cudaEventDestroy(e);
+        for (Slot& sl : slot) {
+            if (sl.trav) cudaEventDestroy(sl.trav);
+            if (sl.sel) cudaEventDestroy(sl.sel);
+            if (sl.rr) cudaEventDestroy(sl.rr);
+        }
+        if (ev_in) cudaEventDestroy(ev_in);
+        if (ev_out) cudaEventDestroy(ev_out);
+        for (cudaStream_t t : pipe) {
+            if (t) cudaStreamDestroy(t);
+        }
         if (own) cudaStreamDestroy(own);
     }
 };
@@ -152,6 +170,22 @@ void check_finite_device(const float* d_data, uint64_t count, cudaStream_t st) {
 void create_stream(suco_gpu_index* x) {
     CUDA_TRY(cudaStreamCreateWithFlags(&x->own, cudaStreamNonBlocking));
     x->stream = x->own;
+    int least = 0, greatest = 0;
+    CUDA_TRY(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    const char* pr = std::getenv("SUCO_PIPE_PRIO");
+    const bool prio = !pr || std::atoi(pr) != 0;
+    // traverse and rerank (short, many small CTAs) get priority so they fill the
+    // SMs that select's GPC-bound clusters leave idle
+    CUDA_TRY(cudaStreamCreateWithPriority(&x->pipe[0], cudaStreamNonBlocking, prio ? greatest : least));
+    CUDA_TRY(cudaStreamCreateWithPriority(&x->pipe[1], cudaStreamNonBlocking, least));
+    CUDA_TRY(cudaStreamCreateWithPriority(&x->pipe[2], cudaStreamNonBlocking, prio ? greatest : least));
+    for (auto& sl : x->slot) {
+        CUDA_TRY(cudaEventCreateWithFlags(&sl.trav, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&sl.sel, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&sl.rr, cudaEventDisableTiming));
+    }
+    CUDA_TRY(cudaEventCreateWithFlags(&x->ev_in, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&x->ev_out, cudaEventDisableTiming));
 }
 
 void upload_data(suco_gpu_index* x, const float* data, uint64_t n, uint32_t d) {
@@ -273,24 +307,37 @@ uint64_t tile_size(const suco_gpu_index* x, uint64_t nq, uint64_t m, uint32_t k)
     return std::max<uint64_t>(1, std::min<uint64_t>(nq, budget / per));
 }
 
-// Runs the three stages for nt device-resident queries.
-void run_tile(suco_gpu_index* x, const float* d_q, uint64_t nt, uint64_t target, uint64_t m, uint32_t k,
-              uint32_t* d_ids, double* d_dists, cudaStream_t st, const Dbg* dbg) {
+// Resets the per-call profiling state (events + work counters).
+void begin_call(suco_gpu_index* x, uint64_t nq, uint64_t m, cudaStream_t st) {
+    x->pairs = 0;
+    x->last_nq = nq;
+    x->last_m = m;
+    if (x->profile) {
+        x->stat_cum.reserve(1);
+        CUDA_TRY(cudaMemsetAsync(x->stat_cum.p, 0, sizeof(unsigned long long), st));
+    }
+}
+
+// Profiling pair for one stage launch (nullptr when profiling is off).
+cudaEvent_t* prof_pair(suco_gpu_index* x, int stage) {
+    if (!x->profile) return nullptr;
+    while (x->events.size() < 2ull * (x->pairs + 1)) {
+        cudaEvent_t e;
+        CUDA_TRY(cudaEventCreate(&e));
+        x->events.push_back(e);
+    }
+    if (x->event_stage.size() < x->pairs + 1) x->event_stage.resize(x->pairs + 1);
+    x->event_stage[x->pairs] = stage;
+    return x->events.data() + 2ull * x->pairs++;
+}
+
+void stage_traverse(suco_gpu_index* x, suco_gpu_index::Slot& sl, const float* d_q, uint64_t nt, uint64_t target,
+                    cudaStream_t st, const Dbg* dbg) {
     const HostIndex& h = x->host;
     const uint32_t ns = h.layout.ns;
-    cudaEvent_t* ev = nullptr;
-    if (x->profile && !dbg) {
-        while (x->events.size() < 4ull * (x->tiles + 1)) {
-            cudaEvent_t e;
-            CUDA_TRY(cudaEventCreate(&e));
-            x->events.push_back(e);
-        }
-        ev = x->events.data() + 4ull * x->tiles;
-        ++x->tiles;
-    }
-    x->cells.reserve(nt * ns * x->K);
-    x->ncells.reserve(nt * ns);
-    x->cands.reserve(nt * m);
+    sl.cells.reserve(nt * ns * x->K);
+    sl.ncells.reserve(nt * ns);
+    cudaEvent_t* ev = dbg ? nullptr : prof_pair(x, 0);
     TraverseArgs ta{};
     ta.queries = d_q;
     ta.d = h.d;
@@ -304,65 +351,138 @@ void run_tile(suco_gpu_index* x, const float* d_q, uint64_t nt, uint64_t target,
     ta.K = x->K;
     ta.hmax = x->hmax;
     ta.target = target;
-    ta.cells = x->cells.p;
-    ta.ncells = x->ncells.p;
+    ta.cells = sl.cells.p;
+    ta.ncells = sl.ncells.p;
     ta.dbg_sum = dbg ? dbg->sums : nullptr;
     ta.dbg_cum = dbg ? dbg->cum : nullptr;
     ta.stat_cum = ev ? x->stat_cum.p : nullptr;
     if (ev) CUDA_TRY(cudaEventRecord(ev[0], st));
     CUDA_TRY(launch_traverse(ta, st));
     if (ev) CUDA_TRY(cudaEventRecord(ev[1], st));
+}
 
+void stage_select(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nt, uint64_t m, cudaStream_t st,
+                  const Dbg* dbg) {
+    const HostIndex& h = x->host;
+    sl.cands.reserve(nt * m);
+    cudaEvent_t* ev = dbg ? nullptr : prof_pair(x, 1);
     SelectArgs sa{};
     sa.ids = x->ids.p;
     sa.slab_off = x->slab_off.p;
-    sa.cells = x->cells.p;
-    sa.ncells = x->ncells.p;
+    sa.cells = sl.cells.p;
+    sa.ncells = sl.ncells.p;
     sa.cells_cap = x->K;
     sa.n = h.n;
-    sa.ns = ns;
+    sa.ns = h.layout.ns;
     sa.K = x->K;
     sa.nslabs = x->sel.nslabs;
     sa.CH = x->sel.CH;
     sa.rounds = x->sel.rounds;
     sa.CS = x->sel.CS;
     sa.m = m;
-    sa.nq = nt;  // non-persistent grid below: one cluster per query (hardware cluster scheduling)
-    sa.cands = x->cands.p;
+    sa.nq = nt;
+    sa.cands = sl.cands.p;
     sa.scores_dbg = dbg ? dbg->scores : nullptr;
+    if (ev) CUDA_TRY(cudaEventRecord(ev[0], st));
     CUDA_TRY(launch_select(sa, x->sel, nt, st));
-    if (ev) CUDA_TRY(cudaEventRecord(ev[2], st));
+    if (ev) CUDA_TRY(cudaEventRecord(ev[1], st));
+}
 
+void stage_rerank(suco_gpu_index* x, suco_gpu_index::Slot& sl, const float* d_q, uint64_t nt, uint64_t m, uint32_t k,
+                  uint32_t* d_ids, double* d_dists, cudaStream_t st, bool profiled) {
+    const HostIndex& h = x->host;
+    cudaEvent_t* ev = profiled ? prof_pair(x, 2) : nullptr;
     RerankArgs ra{};
     ra.data = x->data.p;
     ra.n = h.n;
     ra.d = h.d;
     ra.queries = d_q;
-    ra.cands = x->cands.p;
+    ra.cands = sl.cands.p;
     ra.m = m;
     ra.k = k;
     ra.out_ids = d_ids;
     ra.out_dists = d_dists;
     ra.data_int_max = x->data_int_max;
     if (k > 32) {
-        x->all_d.reserve(nt * m);
-        x->all_id.reserve(nt * m);
-        ra.all_d = x->all_d.p;
-        ra.all_id = x->all_id.p;
+        sl.all_d.reserve(nt * m);
+        sl.all_id.reserve(nt * m);
+        ra.all_d = sl.all_d.p;
+        ra.all_id = sl.all_id.p;
     }
+    if (ev) CUDA_TRY(cudaEventRecord(ev[0], st));
     CUDA_TRY(launch_rerank(ra, nt, st));
-    if (ev) CUDA_TRY(cudaEventRecord(ev[3], st));
+    if (ev) CUDA_TRY(cudaEventRecord(ev[1], st));
 }
 
-// Resets the per-call profiling state (events + work counters).
-void begin_call(suco_gpu_index* x, uint64_t nq, uint64_t m, cudaStream_t st) {
-    x->tiles = 0;
-    x->last_nq = nq;
-    x->last_m = m;
-    if (x->profile) {
-        x->stat_cum.reserve(1);
-        CUDA_TRY(cudaMemsetAsync(x->stat_cum.p, 0, sizeof(unsigned long long), st));
+// One tile through all three stages on a single stream (intermediates/debug).
+void run_tile(suco_gpu_index* x, const float* d_q, uint64_t nt, uint64_t target, uint64_t m, uint32_t k,
+              uint32_t* d_ids, double* d_dists, cudaStream_t st, const Dbg* dbg) {
+    auto& sl = x->slot[0];
+    stage_traverse(x, sl, d_q, nt, target, st, dbg);
+    stage_select(x, sl, nt, m, st, dbg);
+    stage_rerank(x, sl, d_q, nt, m, k, d_ids, d_dists, st, dbg == nullptr);
+}
+
+uint64_t pipeline_tiles(uint64_t nq, uint64_t mem_tile) {
+    uint64_t want = 4;
+    if (const char* t = std::getenv("SUCO_TILES")) want = std::max(1, std::atoi(t));
+    uint64_t tiles = std::max<uint64_t>(1, std::min<uint64_t>(want, nq / 512));
+    tiles = std::max<uint64_t>(tiles, (nq + mem_tile - 1) / mem_tile);
+    return tiles;
+}
+
+// The batched query pipeline. Queries are either device-resident (h_q == nullptr,
+// d_q given) or host (h_q given: copied per tile on the traverse stream).
+// Outputs go to d_ids/d_dists, or to host h_ids/h_dists (copied per tile).
+void run_pipeline(suco_gpu_index* x, const float* h_q, const float* d_q, uint64_t nq, uint32_t qlen,
+                  const suco_collision_params* p, uint32_t* d_ids, double* d_dists, uint32_t* h_ids, double* h_dists,
+                  cudaStream_t user) {
+    const uint64_t n = x->host.n;
+    const uint32_t k = p->k;
+    const uint64_t m = suco_candidate_count(p->beta, n, k);
+    const uint64_t target = suco_collision_count(p->alpha, n);
+    const uint64_t tiles = pipeline_tiles(nq, tile_size(x, nq, m, k));
+    const uint64_t tile = (nq + tiles - 1) / tiles;
+    begin_call(x, nq, m, user);
+    CUDA_TRY(cudaEventRecord(x->ev_in, user));
+    for (cudaStream_t t : x->pipe) CUDA_TRY(cudaStreamWaitEvent(t, x->ev_in, 0));
+    cudaStream_t s_trav = x->pipe[0], s_sel = x->pipe[1], s_rr = x->pipe[2];
+    for (uint64_t t = 0; t * tile < nq; ++t) {
+        const uint64_t q0 = t * tile, nt = std::min(tile, nq - q0);
+        auto& sl = x->slot[t & 1];
+        // slot reuse: tile t-2's select read `cells`, its rerank read `q`/`cands`
+        CUDA_TRY(cudaStreamWaitEvent(s_trav, sl.sel, 0));
+        CUDA_TRY(cudaStreamWaitEvent(s_trav, sl.rr, 0));
+        const float* tq = d_q ? d_q + q0 * qlen : nullptr;
+        if (h_q) {
+            sl.q.reserve(tile * qlen);
+            CUDA_TRY(cudaMemcpyAsync(sl.q.p, h_q + q0 * qlen, nt * qlen * 4, cudaMemcpyHostToDevice, s_trav));
+            tq = sl.q.p;
+        }
+        stage_traverse(x, sl, tq, nt, target, s_trav, nullptr);
+        CUDA_TRY(cudaEventRecord(sl.trav, s_trav));
+        CUDA_TRY(cudaStreamWaitEvent(s_sel, sl.trav, 0));
+        CUDA_TRY(cudaStreamWaitEvent(s_sel, sl.rr, 0));
+        stage_select(x, sl, nt, m, s_sel, nullptr);
+        CUDA_TRY(cudaEventRecord(sl.sel, s_sel));
+        CUDA_TRY(cudaStreamWaitEvent(s_rr, sl.sel, 0));
+        uint32_t* oi = d_ids ? d_ids + q0 * k : nullptr;
+        double* od = d_dists ? d_dists + q0 * k : nullptr;
+        if (h_ids) {
+            sl.out_ids.reserve(tile * k);
+            sl.out_d.reserve(tile * k);
+            oi = sl.out_ids.p;
+            od = sl.out_d.p;
+        }
+        stage_rerank(x, sl, tq, nt, m, k, oi, od, s_rr, true);
+        if (h_ids) {
+            CUDA_TRY(cudaMemcpyAsync(h_ids + q0 * k, oi, nt * k * 4, cudaMemcpyDeviceToHost, s_rr));
+            CUDA_TRY(cudaMemcpyAsync(h_dists + q0 * k, od, nt * k * 8, cudaMemcpyDeviceToHost, s_rr));
+        }
+        CUDA_TRY(cudaEventRecord(sl.rr, s_rr));
     }
+    CUDA_TRY(cudaEventRecord(x->ev_out, s_rr));
+    CUDA_TRY(cudaStreamWaitEvent(user, x->ev_out, 0));
 }
 
 void check_query_args(const suco_gpu_index* x, uint32_t qlen, const suco_collision_params* p) {
@@ -570,17 +690,15 @@ int suco_gpu_stage_times(suco_gpu_index* x, double* ms, uint64_t* stats) {
         if (!x->profile) raise(SUCO_ERR_CONTRACT, "profiling is not enabled on this index");
         DeviceGuard g(x->device);
         double acc[3] = {0, 0, 0};
-        for (uint32_t t = 0; t < x->tiles; ++t) {
-            cudaEvent_t* ev = x->events.data() + 4ull * t;
-            CUDA_TRY(cudaEventSynchronize(ev[3]));
-            for (int s = 0; s < 3; ++s) {
-                float f = 0.f;
-                CUDA_TRY(cudaEventElapsedTime(&f, ev[s], ev[s + 1]));
-                acc[s] += f;
-            }
+        for (uint32_t i = 0; i < x->pairs; ++i) {
+            cudaEvent_t* ev = x->events.data() + 2ull * i;
+            CUDA_TRY(cudaEventSynchronize(ev[1]));
+            float f = 0.f;
+            CUDA_TRY(cudaEventElapsedTime(&f, ev[0], ev[1]));
+            acc[x->event_stage[i]] += f;
         }
         if (ms) {
-            for (int s = 0; s < 3; ++s) ms[s] = acc[s];
+            for (int st = 0; st < 3; ++st) ms[st] = acc[st];
         }
         if (stats) {
             unsigned long long c = 0;
@@ -604,17 +722,10 @@ int suco_gpu_knn_query_batch_device(suco_gpu_index* x, const float* d_queries, u
                                     const suco_collision_params* p, uint32_t* d_ids, double* d_dists, void* stream) {
     return guarded([&] {
         check_query_args(x, qlen, p);
+        if (nq == 0) return;
         DeviceGuard g(x->device);
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : x->stream;
-        const uint64_t n = x->host.n;
-        const uint64_t m = suco_candidate_count(p->beta, n, p->k);
-        const uint64_t target = suco_collision_count(p->alpha, n);
-        const uint64_t tile = tile_size(x, nq, m, p->k);
-        begin_call(x, nq, m, st);
-        for (uint64_t q0 = 0; q0 < nq; q0 += tile) {
-            const uint64_t nt = std::min(tile, nq - q0);
-            run_tile(x, d_queries + q0 * qlen, nt, target, m, p->k, d_ids + q0 * p->k, d_dists + q0 * p->k, st, nullptr);
-        }
+        run_pipeline(x, nullptr, d_queries, nq, qlen, p, d_ids, d_dists, nullptr, nullptr, st);
     });
 }
 
@@ -624,25 +735,8 @@ int suco_gpu_knn_query_batch(suco_gpu_index* x, const float* queries, uint64_t n
         check_query_args(x, qlen, p);
         if (nq == 0) return;
         DeviceGuard g(x->device);
-        cudaStream_t st = x->stream;
-        const uint64_t n = x->host.n;
-        const uint32_t k = p->k;
-        const uint64_t m = suco_candidate_count(p->beta, n, k);
-        const uint64_t target = suco_collision_count(p->alpha, n);
-        const uint64_t tile = tile_size(x, nq, m, k);
-        const uint64_t cap = std::min(tile, nq);
-        x->q.reserve(cap * qlen);
-        x->out_ids.reserve(cap * k);
-        x->out_d.reserve(cap * k);
-        begin_call(x, nq, m, st);
-        for (uint64_t q0 = 0; q0 < nq; q0 += tile) {
-            const uint64_t nt = std::min(tile, nq - q0);
-            CUDA_TRY(cudaMemcpyAsync(x->q.p, queries + q0 * qlen, nt * qlen * 4, cudaMemcpyHostToDevice, st));
-            run_tile(x, x->q.p, nt, target, m, k, x->out_ids.p, x->out_d.p, st, nullptr);
-            CUDA_TRY(cudaMemcpyAsync(ids + q0 * k, x->out_ids.p, nt * k * 4, cudaMemcpyDeviceToHost, st));
-            CUDA_TRY(cudaMemcpyAsync(dists + q0 * k, x->out_d.p, nt * k * 8, cudaMemcpyDeviceToHost, st));
-        }
-        CUDA_TRY(cudaStreamSynchronize(st));
+        run_pipeline(x, queries, nullptr, nq, qlen, p, nullptr, nullptr, ids, dists, x->stream);
+        CUDA_TRY(cudaStreamSynchronize(x->stream));
     });
 }
 
@@ -664,11 +758,12 @@ int suco_gpu_query_intermediates(suco_gpu_index* x, const float* query, uint32_t
         sums.reserve(uint64_t(ns) * x->K);
         cum.reserve(uint64_t(ns) * x->K);
         Dbg dbg{sc.p, sums.p, cum.p};
-        x->q.reserve(qlen);
-        x->out_ids.reserve(p->k);
-        x->out_d.reserve(p->k);
-        CUDA_TRY(cudaMemcpyAsync(x->q.p, query, qlen * 4, cudaMemcpyHostToDevice, st));
-        run_tile(x, x->q.p, 1, target, m, p->k, x->out_ids.p, x->out_d.p, st, &dbg);
+        auto& sl = x->slot[0];
+        sl.q.reserve(qlen);
+        sl.out_ids.reserve(p->k);
+        sl.out_d.reserve(p->k);
+        CUDA_TRY(cudaMemcpyAsync(sl.q.p, query, qlen * 4, cudaMemcpyHostToDevice, st));
+        run_tile(x, sl.q.p, 1, target, m, p->k, sl.out_ids.p, sl.out_d.p, st, &dbg);
         CUDA_TRY(cudaStreamSynchronize(st));
         if (scores) {
             std::vector<uint8_t> s8(n);
@@ -676,12 +771,12 @@ int suco_gpu_query_intermediates(suco_gpu_index* x, const float* query, uint32_t
             for (uint64_t i = 0; i < n; ++i) scores[i] = s8[i];
         }
         if (cands) {  // the select kernel emits the candidate SET; report it ascending
-            CUDA_TRY(cudaMemcpy(cands, x->cands.p, m * 4, cudaMemcpyDeviceToHost));
+            CUDA_TRY(cudaMemcpy(cands, x->slot[0].cands.p, m * 4, cudaMemcpyDeviceToHost));
             std::sort(cands, cands + m);
         }
         if (m_out) *m_out = m;
         std::vector<uint32_t> nc(ns);
-        CUDA_TRY(cudaMemcpy(nc.data(), x->ncells.p, ns * 4, cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpy(nc.data(), x->slot[0].ncells.p, ns * 4, cudaMemcpyDeviceToHost));
         if (cells_per_subspace) std::memcpy(cells_per_subspace, nc.data(), ns * 4);
         if (cumulative) {
             for (uint32_t s = 0; s < ns; ++s) {
