@@ -424,7 +424,7 @@ void run_tile(suco_gpu_index* x, const float* d_q, uint64_t nt, uint64_t target,
 }
 
 uint64_t pipeline_tiles(uint64_t nq, uint64_t mem_tile) {
-    uint64_t want = 4;
+    uint64_t want = 1;  // measured: overlapping tiles only stretches select (all SMs busy)
     if (const char* t = std::getenv("SUCO_TILES")) want = std::max(1, std::atoi(t));
     uint64_t tiles = std::max<uint64_t>(1, std::min<uint64_t>(want, nq / 512));
     tiles = std::max<uint64_t>(tiles, (nq + mem_tile - 1) / mem_tile);

@@ -69,6 +69,13 @@ __host__ __device__ inline uint32_t hist_stride(uint32_t ns) { return ns + 2; }
         }                                                                               \
     } while (0)
 
+// Cluster-wide barrier with release/acquire at cluster scope (what DSMEM
+// visibility needs); cg::cluster_group::sync() additionally fences at GPU scope.
+__device__ __forceinline__ void cluster_barrier() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
 struct Smem {
     uint8_t* cnt;        // CH
     uint32_t* hist;      // rounds x hist_stride: [0] = slab length, [t] = #score >= t
@@ -228,13 +235,16 @@ __device__ __forceinline__ void atomic_wave(const Smem& s, const Wave<KU>& w, ui
 template <int NSB, int KU>
 __device__ __forceinline__ void rmw_wave(const Smem& s, const Wave<KU>& w, uint32_t lo, IncHist<NSB>& ih,
                                          uint32_t* hist) {
+    // Every slot of a wave holds a different id (one subspace, distinct units /
+    // lanes), so all counter reads can be issued before any write.
+    uint32_t v[KU];
+#pragma unroll
+    for (int u = 0; u < KU; ++u) v[u] = (w.mask & (1u << u)) ? s.cnt[w.id[u] - lo] + 1u : 0u;
 #pragma unroll
     for (int u = 0; u < KU; ++u) {
         if (w.mask & (1u << u)) {
-            const uint32_t l = w.id[u] - lo;
-            const uint32_t v = s.cnt[l] + 1u;
-            s.cnt[l] = static_cast<uint8_t>(v);
-            ih.add(v, hist);
+            s.cnt[w.id[u] - lo] = static_cast<uint8_t>(v[u]);
+            ih.add(v[u], hist);
         }
     }
 }
@@ -622,7 +632,7 @@ __global__ void __launch_bounds__(kThreads, SUCO_SELECT_MINB) select_kernel(Sele
             }
 
         }
-        cluster.sync();
+        cluster_barrier();
         SEL_MARK(3);
 
         // threshold and per-slab quotas (warp 0), from every slab's histogram
@@ -719,7 +729,7 @@ __global__ void __launch_bounds__(kThreads, SUCO_SELECT_MINB) select_kernel(Sele
             }
             if (lane == 0) s.misc[0] = T;
         }
-        cluster.sync();  // peers finished reading our histograms
+        cluster_barrier();  // peers finished reading our histograms
         SEL_MARK(4);
         const uint32_t T = s.misc[0];
 
