@@ -235,6 +235,32 @@ void upload_codebooks(suco_gpu_index* x) {
     CUDA_TRY(cudaStreamSynchronize(x->stream));
 }
 
+// Keep the IMI ids (+ slab offsets) L2-resident across the query stream: the
+// select kernel's id loads are L2-latency bound, and the candidate writes and
+// re-rank row gathers would otherwise evict them (measured: 93 % L2 hits, i.e.
+// nearly every 256-load wave waited on a DRAM miss).
+void set_l2_window(suco_gpu_index* x) {
+    int max_persist = 0, max_window = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, x->device));
+    CUDA_TRY(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, x->device));
+    if (const char* v = std::getenv("SUCO_L2_PERSIST")) {
+        if (std::atoi(v) == 0) max_persist = 0;
+    }
+    if (max_persist <= 0 || max_window <= 0) return;
+    const size_t want = x->ids.cap * sizeof(uint32_t);
+    const size_t persist = std::min<size_t>(want, static_cast<size_t>(max_persist));
+    CUDA_TRY(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist));
+    cudaStreamAttrValue v{};
+    v.accessPolicyWindow.base_ptr = x->ids.p;
+    v.accessPolicyWindow.num_bytes = std::min<size_t>(want, static_cast<size_t>(max_window));
+    v.accessPolicyWindow.hitRatio = std::min(1.0f, static_cast<float>(persist) / static_cast<float>(v.accessPolicyWindow.num_bytes));
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    for (cudaStream_t t : {x->own, x->pipe[0], x->pipe[1], x->pipe[2]}) {
+        CUDA_TRY(cudaStreamSetAttribute(t, cudaStreamAttributeAccessPolicyWindow, &v));
+    }
+}
+
 // Cell sizes and slab offsets from the device-resident CSR.
 void finalize_device(suco_gpu_index* x) {
     const uint32_t ns = x->host.layout.ns;
@@ -246,6 +272,7 @@ void finalize_device(suco_gpu_index* x) {
     CUDA_TRY(launch_slab_offsets(x->cell_off.p, x->ids.p, x->host.n, ns, x->K, x->sel.CH, x->sel.nslabs, x->slab_off.p,
                                  x->stream));
     CUDA_TRY(cudaStreamSynchronize(x->stream));
+    set_l2_window(x);
 }
 
 void upload_imi(suco_gpu_index* x) {

@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
     for (uint64_t base = static_cast<uint64_t>(warp) * kRows; base < a.m; base += kRows * kWarps) {
         // candidate ids of the 8 rows (lanes 0..7 load, broadcast)
         uint32_t my_id = 0;
-        if (lane < kRows && base + lane < a.m) my_id = __ldg(cands + base + lane);
+        if (lane < kRows && base + lane < a.m) my_id = __ldcs(cands + base + lane);  // read once: evict first
         uint32_t rid[kRows];
 #pragma unroll
         for (uint32_t j = 0; j < kRows; ++j) rid[j] = __shfl_sync(kFull, my_id, j);

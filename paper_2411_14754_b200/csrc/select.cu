@@ -535,7 +535,7 @@ __device__ void emit_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint64
                         uint32_t mm = m[j][u];
                         while (mm) {
                             const uint32_t bit = __ffs(mm) - 1;
-                            out[pos++] = static_cast<uint32_t>(lo) + (vi * 4 + u) * 4 + (bit >> 3);
+                            __stcs(out + pos++, static_cast<uint32_t>(lo) + (vi * 4 + u) * 4 + (bit >> 3));  // streaming: keep ids in L2
                             mm &= mm - 1;
                         }
                     }
@@ -599,7 +599,7 @@ __device__ void emit_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint64
             uint32_t mm = mt[u];
             while (mm && r < quota) {
                 const uint32_t bit = __ffs(mm) - 1;
-                tout[r++] = static_cast<uint32_t>(lo) + (vi * 4 + u) * 4 + (bit >> 3);
+                __stcs(tout + r++, static_cast<uint32_t>(lo) + (vi * 4 + u) * 4 + (bit >> 3));
                 mm &= mm - 1;
             }
         }
