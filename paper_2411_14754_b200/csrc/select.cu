@@ -436,7 +436,9 @@ __device__ void count_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint3
                             waves_since_flush = 0;
                         }
                     }
+                    SEL_MARK(8);  // warp 0's own load+RMW work for this subspace
                     __syncthreads();  // counters of sb3 final before sb3 + 1 increments
+                    SEL_MARK(9);  // waiting for the slowest warp
                 }
             }
         }
@@ -920,17 +922,19 @@ cudaError_t launch_select(const SelectArgs& a0, const SelectConfig& cfg, uint64_
     SelectArgs a = a0;
     unsigned long long* prof = nullptr;
     if (std::getenv("SUCO_SELECT_PROF")) {  // debug: per-phase clock64 totals to stderr
-        cudaMalloc(&prof, 64);
-        cudaMemsetAsync(prof, 0, 64, st);
+        cudaMalloc(&prof, 128);
+        cudaMemsetAsync(prof, 0, 128, st);
         a.prof = reinterpret_cast<long long*>(prof);
         cudaError_t e = launch_select_dispatch(a, cfg, nq, st);
-        unsigned long long h[8];
-        cudaMemcpyAsync(h, prof, 64, cudaMemcpyDeviceToHost, st);
+        unsigned long long h[16];
+        cudaMemcpyAsync(h, prof, 128, cudaMemcpyDeviceToHost, st);
         cudaStreamSynchronize(st);
         cudaFree(prof);
         const double ctas = double(nq) * cfg.CS;
         std::fprintf(stderr, "[select prof] cycles per CTA: zero+init %.0f staging %.0f counting %.0f csync1 %.0f quota+csync2 %.0f emit-unordered %.0f emit-ordered(boundary) %.0f\n",
                      h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas, h[4] / ctas, h[5] / ctas, h[6] / ctas);
+        std::fprintf(stderr, "[select prof] counting split: warp0 own waves %.0f, subspace barrier waits %.0f (remaining = staging tail/descriptors/flush)\n",
+                     h[8] / ctas, h[9] / ctas);
         return e;
     }
     return launch_select_dispatch(a, cfg, nq, st);
