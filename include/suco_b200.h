@@ -139,6 +139,39 @@ int suco_gpu_query_intermediates(suco_gpu_index* index, const float* query, uint
                                  const suco_collision_params* params, uint32_t* scores, uint32_t* cands,
                                  uint64_t* m, uint32_t* cells_per_subspace, uint64_t* cumulative);
 
+/* ------------------------------------------------- multi-GPU shard protocol
+ * The reference runs on one host (no distributed API); this is the sharded
+ * form of knn_query. Points are split block-cyclically: global
+ * block j = ids [j*block, (j+1)*block) belongs to shard j % num_shards. Every
+ * shard keeps the layout, centroids and GLOBAL cell sizes, so its traversal
+ * makes the global Dynamic-Activation cut; it counts SC-scores only for its
+ * own points. Per query batch:
+ *   1. suco_gpu_shard_histograms -> hist[q][local block][t] = #points with
+ *      score >= t (t = 0..N_s+1; t = 0 is the block length);
+ *   2. the caller exchanges histograms (sum over shards -> threshold T =
+ *      max{t : #score>=t >= m}; per-block ties at T in GLOBAL block order ->
+ *      each local block's quota), and computes per (q, local block) the output
+ *      offset `base` and per query the candidate count;
+ *   3. suco_gpu_shard_topk -> local candidates (score > T, first `quota` ties
+ *      per block in id order) re-ranked exactly: local top-min(k, count),
+ *      GLOBAL ids + SQUARED distances, padded with (0xffffffff, +inf);
+ *   4. the caller gathers every shard's lists and keeps the k smallest
+ *      (squared distance, id), then takes sqrt — identical to knn_query.
+ * paper_2411_14754_b200.sharded implements 2 and 4 over torch.distributed. */
+int suco_gpu_make_shard(const suco_gpu_index* full, uint32_t shard, uint32_t num_shards, uint32_t block,
+                        suco_gpu_index** out);
+int suco_gpu_shard_info(const suco_gpu_index* index, uint64_t* n_global, uint64_t* n_local, uint32_t* nblocks_local,
+                        uint32_t* block, uint32_t* shard, uint32_t* num_shards);
+/* d_queries nq x qlen, d_hist nq x nblocks_local x (N_s + 2) u32 (device). */
+int suco_gpu_shard_histograms(suco_gpu_index* shard, const float* d_queries, uint64_t nq, uint32_t qlen,
+                              const suco_collision_params* params, uint32_t* d_hist, void* stream);
+/* d_T nq, d_quota / d_base nq x nblocks_local, d_counts nq (all device, u32);
+ * candidate rows of `stride` entries; d_ids nq x k, d_sqdists nq x k. */
+int suco_gpu_shard_topk(suco_gpu_index* shard, const float* d_queries, uint64_t nq, uint32_t qlen,
+                        const suco_collision_params* params, const uint32_t* d_T, const uint32_t* d_quota,
+                        const uint32_t* d_base, const uint32_t* d_counts, uint64_t stride, uint32_t* d_ids,
+                        double* d_sqdists, void* stream);
+
 /* ------------------------------------------------ stage-level entry points
  * Each runs the device kernel of one stage on host inputs (parity tests of
  * the reference's free functions). */

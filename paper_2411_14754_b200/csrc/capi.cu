@@ -110,6 +110,11 @@ struct suco_gpu_index {
     DevBuf<uint32_t> slab_off;   // ns x K x (nslabs+1)
     SelectConfig sel{};
     float data_int_max = -1.f;  // integer certificate of the dataset (rerank fp32 path)
+    // block-cyclic shard (suco_gpu_make_shard): global blocks j with j % num_shards == shard
+    uint32_t shard = 0, num_shards = 1, block = 0;
+    uint64_t n_global = 0;          // dataset size the index describes (== host.n unsharded)
+    DevBuf<uint8_t> shard_scores;   // phase-1 SC-scores, nq x n_local
+    DevBuf<uint32_t> shard_cands;   // phase-2 candidates, nq x stride
     // query pipeline: tiles flow traverse -> select -> rerank on three streams,
     // double-buffered scratch, so neighbouring tiles overlap on the device.
     struct Slot {
@@ -464,6 +469,7 @@ uint64_t pipeline_tiles(uint64_t nq, uint64_t mem_tile) {
 void run_pipeline(suco_gpu_index* x, const float* h_q, const float* d_q, uint64_t nq, uint32_t qlen,
                   const suco_collision_params* p, uint32_t* d_ids, double* d_dists, uint32_t* h_ids, double* h_dists,
                   cudaStream_t user) {
+    if (x->num_shards > 1) raise(SUCO_ERR_CONTRACT, "a shard answers only through the two-phase shard protocol");
     const uint64_t n = x->host.n;
     const uint32_t k = p->k;
     const uint64_t m = suco_candidate_count(p->beta, n, k);
@@ -584,6 +590,7 @@ int suco_gpu_load_index(const unsigned char* bytes, uint64_t len, const float* d
             upload_codebooks(x);
             upload_imi(x);
             finalize_device(x);
+            x->n_global = n;
         } catch (...) {
             delete x;
             throw;
@@ -623,6 +630,7 @@ int suco_gpu_build_index(const float* data, uint64_t n, uint32_t d, const suco_i
             build_index_device(x->data.p, n, d, x->host.layout, *params, bo, x->stream);
             upload_codebooks(x);
             finalize_device(x);
+            x->n_global = n;
         } catch (...) {
             delete x;
             throw;
@@ -811,6 +819,188 @@ int suco_gpu_query_intermediates(suco_gpu_index* x, const float* query, uint32_t
                 if (nc[s]) CUDA_TRY(cudaMemcpy(cumulative + s, cum.p + uint64_t(s) * x->K + nc[s] - 1, 8, cudaMemcpyDeviceToHost));
             }
         }
+    });
+}
+
+// ------------------------------------------------------------------ shards
+int suco_gpu_make_shard(const suco_gpu_index* full, uint32_t shard, uint32_t num_shards, uint32_t block,
+                        suco_gpu_index** out) {
+    return guarded([&] {
+        if (!full || !out) raise(SUCO_ERR_CONTRACT, "null argument");
+        if (full->num_shards != 1) raise(SUCO_ERR_CONTRACT, "shards are cut from an unsharded index");
+        if (num_shards < 1 || shard >= num_shards) raise(SUCO_ERR_CONFIG, "shard must be < num_shards");
+        if (block < 1) raise(SUCO_ERR_CONFIG, "block size must be >= 1");
+        *out = nullptr;
+        DeviceGuard g(full->device);
+        const uint64_t n = full->host.n;
+        const uint32_t d = full->host.d, ns = full->host.layout.ns;
+        const uint64_t nb = (n + block - 1) / block;
+        uint64_t n_local = 0;
+        for (uint64_t j = shard; j < nb; j += num_shards) n_local += std::min<uint64_t>(block, n - j * block);
+        if (n_local == 0) raise(SUCO_ERR_CONFIG, "shard owns no points (n too small for this block size)");
+        suco_gpu_index* x = new_index(full->device);
+        try {
+            create_stream(x);
+            x->host.n = n_local;
+            x->host.d = d;
+            x->host.p = full->host.p;
+            x->host.layout = full->host.layout;
+            x->host.cent1 = full->host.cent1;
+            x->host.cent2 = full->host.cent2;
+            x->shard = shard;
+            x->num_shards = num_shards;
+            x->block = block;
+            x->n_global = n;
+            x->data_int_max = full->data_int_max;
+            // rows of the owned blocks, back to back
+            x->data.reserve(n_local * d);
+            uint64_t lo = 0;
+            for (uint64_t j = shard; j < nb; j += num_shards) {
+                const uint64_t len = std::min<uint64_t>(block, n - j * block);
+                CUDA_TRY(cudaMemcpyAsync(x->data.p + lo * d, full->data.p + j * block * d, len * d * 4,
+                                         cudaMemcpyDeviceToDevice, x->stream));
+                lo += len;
+            }
+            upload_codebooks(x);
+            x->K = full->K;
+            const uint64_t K = x->K;
+            // GLOBAL cell sizes: every shard makes the global Dynamic-Activation cut
+            x->cell_size.reserve(ns * K);
+            CUDA_TRY(cudaMemcpyAsync(x->cell_size.p, full->cell_size.p, ns * K * 4, cudaMemcpyDeviceToDevice, x->stream));
+            // local IMI: owned ids of every cell, as local ids, ascending
+            DevBuf<uint32_t> counts;
+            counts.reserve(ns * K);
+            CUDA_TRY(launch_shard_imi(full->ids.p, full->cell_off.p, n, ns, x->K, block, num_shards, shard, counts.p,
+                                      nullptr, 0, nullptr, x->stream));
+            std::vector<uint32_t> hc(ns * K), hoff(ns * (K + 1));
+            CUDA_TRY(cudaMemcpyAsync(hc.data(), counts.p, ns * K * 4, cudaMemcpyDeviceToHost, x->stream));
+            CUDA_TRY(cudaStreamSynchronize(x->stream));
+            for (uint32_t sub = 0; sub < ns; ++sub) {
+                uint32_t run = 0;
+                for (uint64_t c = 0; c < K; ++c) {
+                    hoff[sub * (K + 1) + c] = run;
+                    run += hc[sub * K + c];
+                }
+                hoff[sub * (K + 1) + K] = run;
+            }
+            x->cell_off.reserve(ns * (K + 1));
+            CUDA_TRY(cudaMemcpyAsync(x->cell_off.p, hoff.data(), hoff.size() * 4, cudaMemcpyHostToDevice, x->stream));
+            x->ids.reserve(ns * n_local);
+            CUDA_TRY(launch_shard_imi(full->ids.p, full->cell_off.p, n, ns, x->K, block, num_shards, shard, nullptr,
+                                      x->cell_off.p, n_local, x->ids.p, x->stream));
+            x->sel = plan_select(n_local, ns, cluster_size_from_env());
+            x->slab_off.reserve(uint64_t(ns) * K * (x->sel.nslabs + 1));
+            CUDA_TRY(launch_slab_offsets(x->cell_off.p, x->ids.p, n_local, ns, x->K, x->sel.CH, x->sel.nslabs,
+                                         x->slab_off.p, x->stream));
+            CUDA_TRY(cudaStreamSynchronize(x->stream));
+            set_l2_window(x);
+        } catch (...) {
+            delete x;
+            throw;
+        }
+        *out = x;
+    });
+}
+
+int suco_gpu_shard_info(const suco_gpu_index* x, uint64_t* n_global, uint64_t* n_local, uint32_t* nblocks_local,
+                        uint32_t* block, uint32_t* shard, uint32_t* num_shards) {
+    return guarded([&] {
+        if (!x) raise(SUCO_ERR_CONTRACT, "index is null");
+        const uint32_t b = x->num_shards > 1 ? x->block : static_cast<uint32_t>(std::min<uint64_t>(x->host.n, 0xFFFFFFFFull));
+        if (n_global) *n_global = x->n_global;
+        if (n_local) *n_local = x->host.n;
+        if (nblocks_local) *nblocks_local = static_cast<uint32_t>((x->host.n + b - 1) / b);
+        if (block) *block = b;
+        if (shard) *shard = x->shard;
+        if (num_shards) *num_shards = x->num_shards;
+    });
+}
+
+int suco_gpu_shard_histograms(suco_gpu_index* x, const float* d_queries, uint64_t nq, uint32_t qlen,
+                              const suco_collision_params* p, uint32_t* d_hist, void* stream) {
+    return guarded([&] {
+        if (!x) raise(SUCO_ERR_CONTRACT, "index is null");
+        if (qlen != x->host.d) {
+            raise(SUCO_ERR_CONTRACT, "query length " + std::to_string(qlen) + " does not match dataset d = " +
+                                         std::to_string(x->host.d));
+        }
+        validate_params(p, x->n_global);
+        if (nq == 0) return;
+        DeviceGuard g(x->device);
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : x->stream;
+        const uint64_t nl = x->host.n;
+        const uint32_t ns = x->host.layout.ns;
+        const uint32_t b = x->num_shards > 1 ? x->block : static_cast<uint32_t>(nl);
+        const uint32_t nblocks = static_cast<uint32_t>((nl + b - 1) / b);
+        auto& sl = x->slot[0];
+        x->shard_scores.reserve(nq * nl);
+        stage_traverse(x, sl, d_queries, nq, suco_collision_count(p->alpha, x->n_global), st, nullptr);
+        sl.cands.reserve(1);
+        SelectArgs sa{};
+        sa.ids = x->ids.p;
+        sa.slab_off = x->slab_off.p;
+        sa.cells = sl.cells.p;
+        sa.ncells = sl.ncells.p;
+        sa.cells_cap = x->K;
+        sa.n = nl;
+        sa.ns = ns;
+        sa.K = x->K;
+        sa.nslabs = x->sel.nslabs;
+        sa.CH = x->sel.CH;
+        sa.rounds = x->sel.rounds;
+        sa.CS = x->sel.CS;
+        sa.m = 1;
+        sa.nq = nq;
+        sa.cands = sl.cands.p;
+        sa.scores_dbg = x->shard_scores.p;
+        sa.count_only = true;
+        CUDA_TRY(launch_select(sa, x->sel, nq, st));
+        CUDA_TRY(launch_block_hist(x->shard_scores.p, nq, nl, b, nblocks, ns, d_hist, st));
+    });
+}
+
+int suco_gpu_shard_topk(suco_gpu_index* x, const float* d_queries, uint64_t nq, uint32_t qlen,
+                        const suco_collision_params* p, const uint32_t* d_T, const uint32_t* d_quota,
+                        const uint32_t* d_base, const uint32_t* d_counts, uint64_t stride, uint32_t* d_ids,
+                        double* d_sqdists, void* stream) {
+    return guarded([&] {
+        if (!x) raise(SUCO_ERR_CONTRACT, "index is null");
+        if (qlen != x->host.d) raise(SUCO_ERR_CONTRACT, "query length does not match dataset d");
+        validate_params(p, x->n_global);
+        if (nq == 0) return;
+        if (x->shard_scores.cap < nq * x->host.n) raise(SUCO_ERR_CONTRACT, "suco_gpu_shard_topk needs phase 1 first");
+        DeviceGuard g(x->device);
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : x->stream;
+        const uint64_t nl = x->host.n;
+        const uint32_t b = x->num_shards > 1 ? x->block : static_cast<uint32_t>(nl);
+        const uint32_t nblocks = static_cast<uint32_t>((nl + b - 1) / b);
+        const uint64_t sd = std::max<uint64_t>(stride, 1);
+        x->shard_cands.reserve(nq * sd);
+        CUDA_TRY(launch_shard_emit(x->shard_scores.p, nq, nl, b, nblocks, x->shard, x->num_shards, d_T, d_quota, d_base,
+                                   x->shard_cands.p, sd, st));
+        RerankArgs ra{};
+        ra.data = x->data.p;
+        ra.n = nl;
+        ra.d = x->host.d;
+        ra.queries = d_queries;
+        ra.cands = x->shard_cands.p;
+        ra.m = sd;
+        ra.k = p->k;
+        ra.out_ids = d_ids;
+        ra.out_dists = d_sqdists;
+        ra.data_int_max = x->data_int_max;
+        ra.counts = d_counts;
+        ra.squared = true;
+        ra.shard_b = x->num_shards > 1 ? b : 0;
+        ra.shard_G = x->num_shards > 1 ? x->num_shards : 0;
+        auto& sl = x->slot[0];
+        if (p->k > 32) {
+            sl.all_d.reserve(nq * sd);
+            sl.all_id.reserve(nq * sd);
+            ra.all_d = sl.all_d.p;
+            ra.all_id = sl.all_id.p;
+        }
+        CUDA_TRY(launch_rerank(ra, nq, st));
     });
 }
 

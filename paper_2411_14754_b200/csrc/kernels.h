@@ -58,6 +58,7 @@ struct SelectArgs {
     uint32_t* cands;      // nq x m (candidate set, unordered)
     uint8_t* scores_dbg;  // optional nq x n
     long long* prof;      // optional debug phase timers (8 x u64)
+    bool count_only;      // stop after counting (scores_dbg receives the scores): shard phase 1
 };
 struct SelectConfig {
     uint32_t CS, CH, nslabs, rounds;
@@ -86,8 +87,23 @@ struct RerankArgs {
     double* all_d;        // generic path scratch nq x m
     uint32_t* all_id;     // generic path scratch nq x m
     float data_int_max;   // >= 0: every data value is an integer with |v| <= this; < 0: not certified
+    const uint32_t* counts;  // optional per-query candidate counts (<= m; m is then the row stride)
+    bool squared;            // output squared distances (shard-local top-k for the cross-shard merge)
+    uint32_t shard_b, shard_G; // shards: row of global id g = ((g / b) / G) * b + g % b; shard_G = 0: row = g
 };
 cudaError_t launch_rerank(const RerankArgs& a, uint64_t nq, cudaStream_t st);
+
+// ------------------------------------------------------------------- shards
+cudaError_t launch_block_hist(const uint8_t* scores, uint64_t nq, uint64_t n_local, uint32_t b, uint32_t nblocks,
+                              uint32_t ns, uint32_t* hist, cudaStream_t st);
+cudaError_t launch_shard_emit(const uint8_t* scores, uint64_t nq, uint64_t n_local, uint32_t b, uint32_t nblocks,
+                              uint32_t shard, uint32_t num_shards, const uint32_t* T, const uint32_t* quota,
+                              const uint32_t* base, uint32_t* cands, uint64_t stride, cudaStream_t st);
+
+// counts == phase A (per-cell owned counts); local_ids != nullptr: phase B (compaction)
+cudaError_t launch_shard_imi(const uint32_t* ids, const uint32_t* cell_off, uint64_t n, uint32_t ns, uint32_t K,
+                             uint32_t b, uint32_t G, uint32_t shard, uint32_t* counts, const uint32_t* local_off,
+                             uint64_t n_local, uint32_t* local_ids, cudaStream_t st);
 
 // ------------------------------------------------------------------- build
 cudaError_t launch_cell_sizes(const uint32_t* cell_off, uint32_t ns, uint32_t K, uint32_t* cell_size,

@@ -97,17 +97,22 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
     const uint32_t r = lane >> 2, acc_i = lane & 3u;
     const uint32_t main4 = a.d & ~3u;  // dims covered by the four chains
     const uint32_t* cands = a.cands + q * a.m;
+    const uint64_t mq = a.counts ? a.counts[q] : a.m;
     double ld = kInf;
     uint32_t lid = 0xffffffffu;
 
-    for (uint64_t base = static_cast<uint64_t>(warp) * kRows; base < a.m; base += kRows * kWarps) {
-        // candidate ids of the 8 rows (lanes 0..7 load, broadcast)
+    for (uint64_t base = static_cast<uint64_t>(warp) * kRows; base < mq; base += kRows * kWarps) {
+        // candidate ids of the 8 rows (lanes 0..7 load, broadcast); `gid` is the
+        // reported id, `rid` the row in `data` (differs on shards)
         uint32_t my_id = 0;
-        if (lane < kRows && base + lane < a.m) my_id = __ldcs(cands + base + lane);  // read once: evict first
-        uint32_t rid[kRows];
+        if (lane < kRows && base + lane < mq) my_id = __ldcs(cands + base + lane);  // read once: evict first
+        uint32_t gid[kRows], rid[kRows];
 #pragma unroll
-        for (uint32_t j = 0; j < kRows; ++j) rid[j] = __shfl_sync(kFull, my_id, j);
-        const uint32_t nrows = static_cast<uint32_t>(min_u64(kRows, a.m - base));
+        for (uint32_t j = 0; j < kRows; ++j) {
+            gid[j] = __shfl_sync(kFull, my_id, j);
+            rid[j] = a.shard_G ? ((gid[j] / a.shard_b) / a.shard_G) * a.shard_b + gid[j] % a.shard_b : gid[j];
+        }
+        const uint32_t nrows = static_cast<uint32_t>(min_u64(kRows, mq - base));
         double acc = 0.0;
         float acc32 = 0.f;
         for (uint32_t c0 = 0; c0 < a.d; c0 += kChunk) {
@@ -162,13 +167,13 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
         if constexpr (GENERIC) {
             if (acc_i == 0 && r < nrows) {
                 a.all_d[q * a.m + base + r] = dist;
-                a.all_id[q * a.m + base + r] = rid[r];
+                a.all_id[q * a.m + base + r] = gid[r];
             }
         } else {
 #pragma unroll
             for (uint32_t j = 0; j < kRows; ++j) {
                 const double dj = __shfl_sync(kFull, dist, 4 * j);
-                if (j < nrows) warp_insert(dj, rid[j], ld, lid, a.k, lane);
+                if (j < nrows) warp_insert(dj, gid[j], ld, lid, a.k, lane);
             }
         }
     }
@@ -190,7 +195,7 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
             }
             if (lane < a.k) {
                 a.out_ids[q * a.k + lane] = lid;
-                a.out_dists[q * a.k + lane] = __dsqrt_rn(ld);
+                a.out_dists[q * a.k + lane] = a.squared ? ld : __dsqrt_rn(ld);
             }
         }
     }
@@ -206,12 +211,13 @@ __global__ void __launch_bounds__(256) topk_generic_kernel(RerankArgs a) {
     const uint64_t q = blockIdx.x;
     const double* dd = a.all_d + q * a.m;
     const uint32_t* ii = a.all_id + q * a.m;
+    const uint64_t mq = a.counts ? a.counts[q] : a.m;
     double pd = -1.0;
     uint32_t pi = 0;
     for (uint32_t r = 0; r < a.k; ++r) {
         double bd = kInf;
         uint32_t bi = 0xffffffffu;
-        for (uint64_t c = tid; c < a.m; c += 256) {
+        for (uint64_t c = tid; c < mq; c += 256) {
             const double d = dd[c];
             const uint32_t i = ii[c];
             if (dist_id_less(pd, pi, d, i) && dist_id_less(d, i, bd, bi)) {
@@ -244,7 +250,7 @@ __global__ void __launch_bounds__(256) topk_generic_kernel(RerankArgs a) {
         __syncthreads();
         if (tid == 0) {
             a.out_ids[q * a.k + r] = bi;
-            a.out_dists[q * a.k + r] = __dsqrt_rn(bd);
+            a.out_dists[q * a.k + r] = a.squared ? bd : __dsqrt_rn(bd);
         }
         pd = bd;
         pi = bi;

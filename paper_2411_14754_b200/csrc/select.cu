@@ -634,6 +634,7 @@ __global__ void __launch_bounds__(kThreads, SUCO_SELECT_MINB) select_kernel(Sele
             }
 
         }
+        if (a.count_only) continue;  // shard phase 1: scores written, no cluster exchange
         cluster_barrier();
         SEL_MARK(3);
 

@@ -1,0 +1,187 @@
+"""Multi-GPU SuCo queries: the block-cyclic shard protocol.
+
+The reference is single-host (no distributed API); this module is the sharded
+form of `knn_query` and gives bit-identical results for any number of shards.
+Global id block j = [j*b, (j+1)*b) lives on shard j % G. Each shard runs the
+C-ABI shard entry points (include/suco_b200.h: suco_gpu_shard_histograms /
+suco_gpu_shard_topk) on its own GPU; between them this module does the
+exchange — the only cross-shard data the reference's selection needs:
+
+  * per query, the sum over shards of #points with score >= t gives the global
+    threshold T = max{t : #(score >= t) >= m} and need = m - #(score > T)
+    (query.cpp:242-260: top-m by (score desc, id asc));
+  * the per-block tie counts at T, laid out in GLOBAL block order, give each
+    block's quota = the first `need` ties in id order (an allreduce of totals
+    alone would lose which shard holds the lowest-id ties);
+  * every shard re-ranks only its own candidates and returns its top-min(k, c)
+    as (squared distance, id); the k smallest pairs over all shards, then sqrt,
+    are exactly the reference's result (query.cpp:181-192).
+
+Collectives go through `Comm`: `TorchComm` wraps torch.distributed (NCCL on
+GPUs, gloo on CPU for tests); `emulate()` runs G shards in one process (CI on
+one GPU, as SURVEY §8(e) suggests). The math is plain torch tensor ops on the
+shards' device (small: nq x blocks x (N_s + 2) counters).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Optional, Sequence, Tuple
+
+import torch
+
+from . import _capi as _c
+from . import CollisionParams, GpuIndex, _check, candidate_count
+
+
+# ----------------------------------------------------------------- exchange math
+@dataclass
+class Plan:
+    T: torch.Tensor       # [nq] u32 threshold score
+    quota: torch.Tensor   # [nq, nb_local] ties to take per local block
+    base: torch.Tensor    # [nq, nb_local] output offset of each local block
+    counts: torch.Tensor  # [nq] local candidates per query
+    stride: int           # candidate row length (>= max counts)
+
+
+def global_threshold(total_ge: torch.Tensor, m: int) -> Tuple[torch.Tensor, torch.Tensor]:
+    """total_ge [nq, ns+2] (#score >= t summed over all points) -> (T [nq], need [nq])."""
+    ns = total_ge.shape[1] - 2
+    t = torch.arange(ns + 2, device=total_ge.device)
+    ok = (total_ge >= m) & (t >= 1) & (t <= ns)
+    T = torch.where(ok, t.expand_as(ok), torch.zeros_like(t).expand_as(ok)).max(dim=1).values
+    gt_total = total_ge.gather(1, (T + 1).unsqueeze(1)).squeeze(1)
+    return T, m - gt_total
+
+
+def plan_for_shard(hists: Sequence[torch.Tensor], shard: int, m: int) -> Plan:
+    """hists[r] = shard r's [nq, nb_r, ns+2] block histograms (all shards' copies)."""
+    G = len(hists)
+    nq = hists[0].shape[0]
+    h64 = [h.to(torch.int64) for h in hists]
+    total_ge = sum(h.sum(dim=1) for h in h64)  # [nq, ns+2]
+    T, need = global_threshold(total_ge, m)
+    Tidx = T.view(nq, 1, 1)
+    ties, gts = [], []
+    for h in h64:
+        at_T = h.gather(2, Tidx.expand(nq, h.shape[1], 1)).squeeze(2)
+        above = h.gather(2, (Tidx + 1).expand(nq, h.shape[1], 1)).squeeze(2)
+        ties.append(at_T - above)
+        gts.append(above)
+    # global block order: global block j = local block j // G of shard j % G
+    nb_max = max(t.shape[1] for t in ties)
+    glob = torch.zeros((nq, nb_max * G), dtype=torch.int64, device=T.device)
+    for r, t in enumerate(ties):
+        glob[:, r: r + G * t.shape[1]: G] = t
+    before = torch.cumsum(glob, dim=1) - glob
+    quota_glob = torch.clamp(torch.minimum(glob, need.unsqueeze(1) - before), min=0)
+    nb = ties[shard].shape[1]
+    quota = quota_glob[:, shard: shard + G * nb: G]
+    take = gts[shard] + quota
+    base = torch.cumsum(take, dim=1) - take
+    counts = take.sum(dim=1)
+    stride = int(counts.max().item()) if nq else 0
+    u32 = torch.int32  # device buffers are read as u32 by the kernels (all values < 2^31)
+    return Plan(T.to(u32).contiguous(), quota.to(u32).contiguous(), base.to(u32).contiguous(),
+                counts.to(u32).contiguous(), max(stride, 1))
+
+
+def merge_topk(ids: Sequence[torch.Tensor], sq: Sequence[torch.Tensor], k: int) -> Tuple[torch.Tensor, torch.Tensor]:
+    """Per query, the k smallest (squared distance, id) over all shards' lists; sqrt last."""
+    I = torch.cat([i.to(torch.int64) & 0xFFFFFFFF for i in ids], dim=1)
+    D = torch.cat(list(sq), dim=1)
+    o = torch.sort(I, dim=1, stable=True).indices          # secondary key: id
+    I, D = I.gather(1, o), D.gather(1, o)
+    o = torch.sort(D, dim=1, stable=True).indices          # primary key: squared distance
+    I, D = I.gather(1, o)[:, :k], D.gather(1, o)[:, :k]
+    return I.to(torch.int64), ieee_sqrt(D)
+
+
+def ieee_sqrt(D: torch.Tensor) -> torch.Tensor:
+    """Correctly rounded sqrt (std::sqrt / query.cpp:192). CUDA's double sqrt is IEEE;
+    torch's CPU float64 sqrt is not (vectorised, ~1 ulp), so CPU tensors go through numpy."""
+    if D.is_cuda:
+        return torch.sqrt(D)
+    import numpy as np
+    return torch.from_numpy(np.sqrt(D.numpy()))
+
+
+# ----------------------------------------------------------------- GPU shard
+class GpuShard:
+    """One block-cyclic shard of a device index (suco_gpu_make_shard)."""
+
+    def __init__(self, full: GpuIndex, shard: int, num_shards: int, block: int):
+        h = C.c_void_p()
+        _check(_c.make_shard(full.handle, shard, num_shards, block, C.byref(h)))
+        self.index = GpuIndex(h)
+        ng, nl, nb, b, s, G = (C.c_uint64(), C.c_uint64(), C.c_uint32(), C.c_uint32(), C.c_uint32(), C.c_uint32())
+        _check(_c.shard_info(h, C.byref(ng), C.byref(nl), C.byref(nb), C.byref(b), C.byref(s), C.byref(G)))
+        self.n_global, self.n_local, self.nblocks = ng.value, nl.value, nb.value
+        self.block, self.shard, self.num_shards = b.value, s.value, G.value
+        self.ns = full.params.num_subspaces
+        self.d = full.d
+
+    def histograms(self, q: torch.Tensor, params: CollisionParams, stream: Optional[int] = None) -> torch.Tensor:
+        stream = stream or torch.cuda.current_stream(q.device).cuda_stream  # ordered with the plan math
+        nq = q.shape[0]
+        hist = torch.empty((nq, self.nblocks, self.ns + 2), dtype=torch.int32, device=q.device)
+        cp = params._c()
+        _check(_c.shard_histograms(self.index.handle, C.c_void_p(q.data_ptr()), nq, self.d, C.byref(cp),
+                                   C.c_void_p(hist.data_ptr()), C.c_void_p(stream or 0)))
+        return hist
+
+    def topk(self, q: torch.Tensor, params: CollisionParams, plan: Plan, stream: Optional[int] = None):
+        stream = stream or torch.cuda.current_stream(q.device).cuda_stream
+        nq, k = q.shape[0], int(params.k)
+        ids = torch.empty((nq, k), dtype=torch.int32, device=q.device)
+        sq = torch.empty((nq, k), dtype=torch.float64, device=q.device)
+        cp = params._c()
+        _check(_c.shard_topk(self.index.handle, C.c_void_p(q.data_ptr()), nq, self.d, C.byref(cp),
+                             C.c_void_p(plan.T.data_ptr()), C.c_void_p(plan.quota.data_ptr()),
+                             C.c_void_p(plan.base.data_ptr()), C.c_void_p(plan.counts.data_ptr()), plan.stride,
+                             C.c_void_p(ids.data_ptr()), C.c_void_p(sq.data_ptr()), C.c_void_p(stream or 0)))
+        return ids, sq
+
+
+# ----------------------------------------------------------------- protocols
+class TorchComm:
+    """torch.distributed collectives (NCCL for CUDA tensors, gloo for CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.size = dist.get_world_size(group)
+
+    def allgather_var(self, t: torch.Tensor) -> List[torch.Tensor]:
+        """all_gather of tensors whose dim 1 may differ per rank (padded on the wire)."""
+        d1 = torch.tensor([t.shape[1]], dtype=torch.int64, device=t.device)
+        sizes = [torch.zeros_like(d1) for _ in range(self.size)]
+        self.dist.all_gather(sizes, d1, group=self.group)
+        mx = int(max(s.item() for s in sizes))
+        pad = torch.zeros((t.shape[0], mx) + tuple(t.shape[2:]), dtype=t.dtype, device=t.device)
+        pad[:, : t.shape[1]] = t
+        out = [torch.empty_like(pad) for _ in range(self.size)]
+        self.dist.all_gather(out, pad.contiguous(), group=self.group)
+        return [o[:, : int(s.item())] for o, s in zip(out, sizes)]
+
+
+def knn_query_distributed(engine, comm: TorchComm, queries: torch.Tensor, params: CollisionParams):
+    """Every rank calls this with the same queries; returns the global (ids int64 [nq,k], dists f64 [nq,k])."""
+    m = candidate_count(params.beta, engine.n_global, params.k)
+    hist = engine.histograms(queries, params)
+    hists = comm.allgather_var(hist)
+    plan = plan_for_shard(hists, comm.rank, m)
+    ids, sq = engine.topk(queries, params, plan)
+    all_ids = comm.allgather_var(ids)
+    all_sq = comm.allgather_var(sq)
+    return merge_topk(all_ids, all_sq, int(params.k))
+
+
+def emulate(engines: Sequence, queries: torch.Tensor, params: CollisionParams):
+    """Run the protocol for G shard engines in one process (single-GPU CI of the multi-GPU path)."""
+    m = candidate_count(params.beta, engines[0].n_global, params.k)
+    hists = [e.histograms(queries, params) for e in engines]
+    tops = [e.topk(queries, params, plan_for_shard(hists, r, m)) for r, e in enumerate(engines)]
+    return merge_topk([t[0] for t in tops], [t[1] for t in tops], int(params.k))

@@ -1,0 +1,2 @@
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_u.log 2>&1
+echo done
