@@ -112,7 +112,8 @@ int suco_gpu_knn_query_batch(suco_gpu_index* index, const float* queries, uint64
                              const suco_collision_params* params, uint32_t* ids, double* dists);
 
 /* Same, with device-resident queries/outputs, enqueued on `stream`
- * (cudaStream_t; NULL = the index's stream). Returns once enqueued. */
+ * (cudaStream_t; NULL = the index's stream — pass cudaStreamLegacy to order
+ * with the legacy default stream). Returns once enqueued. */
 int suco_gpu_knn_query_batch_device(suco_gpu_index* index, const float* d_queries, uint64_t nq, uint32_t qlen,
                                     const suco_collision_params* params, uint32_t* d_ids, double* d_dists,
                                     void* stream);

@@ -253,7 +253,9 @@ class GpuIndex:
 
     def knn_query_batch_device(self, d_queries: int, nq: int, qlen: int, params: CollisionParams, d_ids: int,
                                d_dists: int, stream: Optional[int] = None) -> None:
-        """Device-resident variant: raw device pointers (e.g. torch tensor .data_ptr())."""
+        """Device-resident variant: raw device pointers (e.g. torch tensor .data_ptr()). `stream` is a
+        cudaStream_t handle; None / 0 = the index's own stream (pass 1 = cudaStreamLegacy for torch's
+        default stream)."""
         cp = params._c()
         _check(_c.knn_query_batch_device(self._h, C.c_void_p(d_queries), nq, qlen, C.byref(cp), C.c_void_p(d_ids),
                                          C.c_void_p(d_dists), C.c_void_p(stream or 0)))

@@ -107,6 +107,13 @@ def ieee_sqrt(D: torch.Tensor) -> torch.Tensor:
 
 
 # ----------------------------------------------------------------- GPU shard
+def _torch_stream(device) -> int:
+    """torch's current stream as a cudaStream_t for the C-ABI. Handle 0 (the legacy
+    default stream) would mean "the index's own stream" there, so it maps to
+    cudaStreamLegacy (1)."""
+    return torch.cuda.current_stream(device).cuda_stream or 1
+
+
 class GpuShard:
     """One block-cyclic shard of a device index (suco_gpu_make_shard)."""
 
@@ -122,7 +129,7 @@ class GpuShard:
         self.d = full.d
 
     def histograms(self, q: torch.Tensor, params: CollisionParams, stream: Optional[int] = None) -> torch.Tensor:
-        stream = stream or torch.cuda.current_stream(q.device).cuda_stream  # ordered with the plan math
+        stream = stream or _torch_stream(q.device)  # ordered with the plan math
         nq = q.shape[0]
         hist = torch.empty((nq, self.nblocks, self.ns + 2), dtype=torch.int32, device=q.device)
         cp = params._c()
@@ -131,7 +138,7 @@ class GpuShard:
         return hist
 
     def topk(self, q: torch.Tensor, params: CollisionParams, plan: Plan, stream: Optional[int] = None):
-        stream = stream or torch.cuda.current_stream(q.device).cuda_stream
+        stream = stream or _torch_stream(q.device)
         nq, k = q.shape[0], int(params.k)
         ids = torch.empty((nq, k), dtype=torch.int32, device=q.device)
         sq = torch.empty((nq, k), dtype=torch.float64, device=q.device)
