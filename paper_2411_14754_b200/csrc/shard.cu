@@ -25,8 +25,10 @@ namespace {
 constexpr uint32_t kFull = 0xffffffffu;
 
 // hist[q][blk][t] = #local points of block blk with score >= t (t <= ns + 1).
-__global__ void block_hist_kernel(const uint8_t* __restrict__ scores, uint64_t n_local, uint32_t b, uint32_t nblocks,
-                                  uint32_t ns, uint32_t* __restrict__ hist) {
+// 16 scores per thread-step (uint4), SWAR high-bit tests per level (scores <= 127).
+__global__ void __launch_bounds__(256) block_hist_kernel(const uint8_t* __restrict__ scores, uint64_t n_local,
+                                                         uint32_t b, uint32_t nblocks, uint32_t ns,
+                                                         uint32_t* __restrict__ hist) {
     extern __shared__ uint32_t hs[];  // ns + 2
     const uint64_t q = blockIdx.y;
     const uint32_t blk = blockIdx.x;
@@ -35,6 +37,31 @@ __global__ void block_hist_kernel(const uint8_t* __restrict__ scores, uint64_t n
     const uint64_t lo = uint64_t(blk) * b;
     const uint32_t len = static_cast<uint32_t>(min_u64(b, n_local - lo));
     const uint8_t* sc = scores + q * n_local + lo;
+    const bool vec = ((reinterpret_cast<uintptr_t>(sc) & 15u) == 0) && ns <= 127;
+    if (vec) {
+        const uint32_t nv = len / 16;
+        for (uint32_t t = 1; t <= ns; ++t) {
+            const uint32_t kq = (0x80u - t) * 0x01010101u;
+            uint32_t c = 0;
+            for (uint32_t i = threadIdx.x; i < nv; i += blockDim.x) {
+                const uint4 v = reinterpret_cast<const uint4*>(sc)[i];
+                c += __popc((v.x + kq) & 0x80808080u) + __popc((v.y + kq) & 0x80808080u) +
+                     __popc((v.z + kq) & 0x80808080u) + __popc((v.w + kq) & 0x80808080u);
+            }
+            for (uint32_t i = nv * 16 + threadIdx.x; i < len; i += blockDim.x) c += sc[i] >= t;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+            if ((threadIdx.x & 31) == 0 && c) atomicAdd(hs + t, c);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t* out = hist + (q * nblocks + blk) * (ns + 2);
+            out[0] = len;
+            for (uint32_t t = 1; t <= ns; ++t) out[t] = hs[t];
+            out[ns + 1] = 0;
+        }
+        return;
+    }
     for (uint32_t i = threadIdx.x; i < len; i += blockDim.x) {
         const uint32_t v = sc[i];
         if (v) atomicAdd(hs + v, 1u);  // exact-value counts, suffix-summed below
@@ -52,16 +79,18 @@ __global__ void block_hist_kernel(const uint8_t* __restrict__ scores, uint64_t n
     }
 }
 
-// One warp per (query, local block): emits score > T unordered-by-slot but
-// block-contiguous, then the first quota ties in id order, all as GLOBAL ids,
-// into cands[q][base_q_blk ...). counts[q] receives the query's total.
-__global__ void shard_emit_kernel(const uint8_t* __restrict__ scores, uint64_t n_local, uint32_t b, uint32_t nblocks,
-                                  uint32_t shard, uint32_t num_shards, const uint32_t* __restrict__ T,
-                                  const uint32_t* __restrict__ quota, const uint32_t* __restrict__ base,
-                                  uint32_t* __restrict__ cands, uint64_t stride) {
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t blk = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (blk >= nblocks) return;
+// One CTA per (query, local block): every score > T and the first `quota`
+// ties (score == T) of the block, in id order, as GLOBAL ids at
+// cands[q][base[q][blk] ...). Each thread owns a contiguous run of scores.
+__global__ void __launch_bounds__(256) shard_emit_kernel(const uint8_t* __restrict__ scores, uint64_t n_local,
+                                                         uint32_t b, uint32_t nblocks, uint32_t shard,
+                                                         uint32_t num_shards, const uint32_t* __restrict__ T,
+                                                         const uint32_t* __restrict__ quota,
+                                                         const uint32_t* __restrict__ base,
+                                                         uint32_t* __restrict__ cands, uint64_t stride) {
+    __shared__ uint32_t wg[8], wt[8];
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint32_t blk = blockIdx.x;
     const uint64_t q = blockIdx.y;
     const uint64_t lo = uint64_t(blk) * b;
     const uint32_t len = static_cast<uint32_t>(min_u64(b, n_local - lo));
@@ -70,20 +99,46 @@ __global__ void shard_emit_kernel(const uint8_t* __restrict__ scores, uint64_t n
     const uint32_t qu = quota[q * nblocks + blk];
     uint32_t* out = cands + q * stride + base[q * nblocks + blk];
     const uint64_t gbase = (uint64_t(blk) * num_shards + shard) * b;  // global id of the block's first point
-    uint32_t pos = 0, ties = 0;
-    for (uint32_t i0 = 0; i0 < len; i0 += 32) {
-        const uint32_t i = i0 + lane;
-        const uint32_t v = i < len ? sc[i] : 0u;
-        const bool gt = i < len && v > t;
-        const bool tie = i < len && v == t;
-        const uint32_t gm = __ballot_sync(kFull, gt), tm = __ballot_sync(kFull, tie);
-        const uint32_t lt = (1u << lane) - 1u;
-        const uint32_t tie_rank = ties + __popc(tm & lt);
-        const bool take_tie = tie && tie_rank < qu;
-        const uint32_t take = gm | __ballot_sync(kFull, take_tie);
-        if (gt || take_tie) out[pos + __popc(take & lt)] = static_cast<uint32_t>(gbase + i);
-        pos += __popc(take);
-        ties += __popc(tm);
+    const uint32_t per = (len + blockDim.x - 1) / blockDim.x;
+    const uint32_t i0 = min(len, tid * per), i1 = min(len, i0 + per);
+    uint32_t g = 0, e = 0;
+    for (uint32_t i = i0; i < i1; ++i) {
+        const uint32_t v = sc[i];
+        g += v > t;
+        e += v == t;
+    }
+    // block exclusive scans of (g, e) in thread (= id) order
+    uint32_t xg = g, xe = e;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t yg = __shfl_up_sync(kFull, xg, o), ye = __shfl_up_sync(kFull, xe, o);
+        if (lane >= (uint32_t)o) {
+            xg += yg;
+            xe += ye;
+        }
+    }
+    if (lane == 31) {
+        wg[warp] = xg;
+        wt[warp] = xe;
+    }
+    __syncthreads();
+    uint32_t bg = 0, be = 0;
+    for (uint32_t w = 0; w < warp; ++w) {
+        bg += wg[w];
+        be += wt[w];
+    }
+    uint32_t tie_rank = be + xe - e;
+    uint32_t pos = bg + xg - g + min(tie_rank, qu);
+    if (g + (tie_rank < qu ? e : 0u)) {
+        for (uint32_t i = i0; i < i1; ++i) {
+            const uint32_t v = sc[i];
+            if (v > t) {
+                out[pos++] = static_cast<uint32_t>(gbase + i);
+            } else if (v == t && tie_rank < qu) {
+                out[pos++] = static_cast<uint32_t>(gbase + i);
+                ++tie_rank;
+            }
+        }
     }
 }
 
@@ -152,11 +207,9 @@ cudaError_t launch_shard_emit(const uint8_t* scores, uint64_t nq, uint64_t n_loc
                               uint32_t shard, uint32_t num_shards, const uint32_t* T, const uint32_t* quota,
                               const uint32_t* base, uint32_t* cands, uint64_t stride, cudaStream_t st) {
     if (nq == 0 || nblocks == 0) return cudaSuccess;
-    const unsigned warps_per_block = 8;
-    const unsigned gx = (nblocks + warps_per_block - 1) / warps_per_block;
     for (uint64_t q0 = 0; q0 < nq; q0 += 65535) {
         const uint64_t nt = min_u64(65535, nq - q0);
-        shard_emit_kernel<<<dim3(gx, static_cast<unsigned>(nt)), 32 * warps_per_block, 0, st>>>(
+        shard_emit_kernel<<<dim3(nblocks, static_cast<unsigned>(nt)), 256, 0, st>>>(
             scores + q0 * n_local, n_local, b, nblocks, shard, num_shards, T + q0, quota + q0 * nblocks,
             base + q0 * nblocks, cands + q0 * stride, stride);
     }
