@@ -66,7 +66,23 @@ class ClockSampler:
     def __init__(self, device: int):
         self.device = device
         self.proc = None
-        self.lines = []
+        self.lines = []  # (arrival time, csv line)
+        self.window = None
+
+    def start(self):
+        """Start sampling early (before warm-up): nvidia-smi's start-up takes driver locks that
+        would otherwise stall the first timed step; summary() keeps the timed window only."""
+        self.__enter__()
+        time.sleep(1.0)
+        return self
+
+    def mark(self):
+        self.window = (time.time(), None)
+
+    def stop(self):
+        if self.window:
+            self.window = (self.window[0], time.time())
+        self.__exit__()
 
     def __enter__(self):
         try:
@@ -81,7 +97,7 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
     def __exit__(self, *exc):
         if self.proc:
@@ -94,7 +110,9 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lo, hi = self.window if self.window and self.window[1] else (0.0, float("inf"))
+        lines = [ln for t, ln in self.lines if lo <= t <= hi + 0.25] or [ln for _, ln in self.lines[-3:]]
+        for ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -161,7 +179,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="no L2 flush/e2e/cpu legs (for ncu)")
     ap.add_argument("--sharded", action="store_true", help="use the multi-GPU shard protocol even at N = 1")
-    ap.add_argument("--block", type=int, default=8192, help="block-cyclic shard block size (ids)")
+    ap.add_argument("--block", type=int, default=0,
+                    help="block-cyclic shard block size (ids); 0 = suco_gpu_shard_block_hint (slabs == blocks)")
     ap.add_argument("--alpha", type=float, default=None, help="experiment: override the config's alpha")
     ap.add_argument("--beta", type=float, default=None, help="experiment: override the config's beta")
     args = ap.parse_args()
@@ -223,6 +242,7 @@ def main():
     def step():
         idx.knn_query_batch_device(dq.data_ptr(), nq, d, cp, dids.data_ptr(), dd.data_ptr(), stream.cuda_stream)
 
+    clocks = ClockSampler(local).start()
     for _ in range(args.warmup):
         step()
     stream.synchronize()
@@ -230,23 +250,24 @@ def main():
     idx.set_profiling(True)
     step_ms, stage_ms = [], np.zeros(3)
     stats = None
-    with ClockSampler(local) as clocks:
-        for _ in range(args.steps):
-            if not args.profile_only:
-                with torch.cuda.stream(stream):
-                    flush.fill_(1)
-            if ws > 1:
-                torch.distributed.barrier()
-            stream.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            step()
-            e1.record(stream)
-            e1.synchronize()
-            step_ms.append(e0.elapsed_time(e1))
-            ms, cum, sq, m = idx.stage_times()
-            stage_ms += ms
-            stats = (cum, sq, m)
+    clocks.mark()
+    for _ in range(args.steps):
+        if not args.profile_only:
+            with torch.cuda.stream(stream):
+                flush.fill_(1)
+        if ws > 1:
+            torch.distributed.barrier()
+        stream.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        ms, cum, sq, m = idx.stage_times()
+        stage_ms += ms
+        stats = (cum, sq, m)
+    clocks.stop()
     idx.set_profiling(False)
     total_ms = sum(step_ms)
     if ws > 1:
@@ -385,7 +406,7 @@ def run_sharded(args, cfg, base, queries, idx, build_s, ws, rank, local):
     if rank == 0:
         want = idx.knn_query_batch(queries, cp)
     t0 = time.time()
-    eng = GpuShard(idx, rank, ws, args.block)
+    eng = GpuShard(idx, rank, ws, args.block or None)
     torch.cuda.synchronize()
     shard_s = time.time() - t0
     idx.close()
@@ -395,6 +416,7 @@ def run_sharded(args, cfg, base, queries, idx, build_s, ws, rank, local):
         with torch.cuda.stream(stream):
             return knn_query_distributed(eng, comm, qdev, cp)
 
+    clocks = ClockSampler(local).start()
     for _ in range(args.warmup):
         step(dq)
     stream.synchronize()
@@ -417,8 +439,9 @@ def run_sharded(args, cfg, base, queries, idx, build_s, ws, rank, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item()), out
 
-    with ClockSampler(local) as clocks:
-        total_ms, (ids, dd) = timed(lambda: step(dq))
+    clocks.mark()
+    total_ms, (ids, dd) = timed(lambda: step(dq))
+    clocks.stop()
     hq = torch.from_numpy(queries).pin_memory()
 
     def e2e_step():
@@ -440,7 +463,7 @@ def run_sharded(args, cfg, base, queries, idx, build_s, ws, rank, local):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded Gaussian mixture, bench_data.py)",
         "config": {"workload": cfg.describe(), "queries_per_step": nq, "index_build_s": build_s,
-                   "shard_cut_s": shard_s, "parallelism": f"{ws} block-cyclic point shards (block {args.block}), "
+                   "shard_cut_s": shard_s, "parallelism": f"{ws} block-cyclic point shards (block {eng.block}), "
                    "NCCL allgather of block histograms + local top-k", "l2": "256 MiB flush write between timed steps"},
         "roofline": {"bound": "hbm", "kernel": "whole query path (per-kernel times need N = 1)", "achieved": None,
                      "peak": peak * ws, "unit": "GB/s", "frac": None, "traffic": None, "peak_source": peak_src},

@@ -161,6 +161,11 @@ int suco_gpu_query_intermediates(suco_gpu_index* index, const float* query, uint
  * paper_2411_14754_b200.sharded implements 2 and 4 over torch.distributed. */
 int suco_gpu_make_shard(const suco_gpu_index* full, uint32_t shard, uint32_t num_shards, uint32_t block,
                         suco_gpu_index** out);
+/* Recommended block size for num_shards shards of `full`: the slab length the
+ * shard's select kernel would use, so slabs coincide with blocks and phase 1
+ * writes its block histograms without a separate pass. Any block size is
+ * correct; this one is fastest. */
+int suco_gpu_shard_block_hint(const suco_gpu_index* full, uint32_t num_shards, uint32_t* block);
 int suco_gpu_shard_info(const suco_gpu_index* index, uint64_t* n_global, uint64_t* n_local, uint32_t* nblocks_local,
                         uint32_t* block, uint32_t* shard, uint32_t* num_shards);
 /* d_queries nq x qlen, d_hist nq x nblocks_local x (N_s + 2) u32 (device). */

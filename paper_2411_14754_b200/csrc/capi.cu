@@ -112,6 +112,7 @@ struct suco_gpu_index {
     float data_int_max = -1.f;  // integer certificate of the dataset (rerank fp32 path)
     // block-cyclic shard (suco_gpu_make_shard): global blocks j with j % num_shards == shard
     uint32_t shard = 0, num_shards = 1, block = 0;
+    bool slab_is_block = false;     // select slabs == shard blocks (phase 1 needs no histogram pass)
     uint64_t n_global = 0;          // dataset size the index describes (== host.n unsharded)
     DevBuf<uint8_t> shard_scores;   // phase-1 SC-scores, nq x n_local
     DevBuf<uint32_t> shard_cands;   // phase-2 candidates, nq x stride
@@ -888,7 +889,10 @@ int suco_gpu_make_shard(const suco_gpu_index* full, uint32_t shard, uint32_t num
             x->ids.reserve(ns * n_local);
             CUDA_TRY(launch_shard_imi(full->ids.p, full->cell_off.p, n, ns, x->K, block, num_shards, shard, nullptr,
                                       x->cell_off.p, n_local, x->ids.p, x->stream));
-            x->sel = plan_select(n_local, ns, cluster_size_from_env());
+            x->sel = SelectConfig{};
+            if (block % select_slab_align() == 0) x->sel = plan_select_fixed(n_local, ns, block);
+            x->slab_is_block = x->sel.CH != 0;  // slab histograms are the block histograms
+            if (!x->slab_is_block) x->sel = plan_select(n_local, ns, cluster_size_from_env());
             x->slab_off.reserve(uint64_t(ns) * K * (x->sel.nslabs + 1));
             CUDA_TRY(launch_slab_offsets(x->cell_off.p, x->ids.p, n_local, ns, x->K, x->sel.CH, x->sel.nslabs,
                                          x->slab_off.p, x->stream));
@@ -902,11 +906,26 @@ int suco_gpu_make_shard(const suco_gpu_index* full, uint32_t shard, uint32_t num
     });
 }
 
+int suco_gpu_shard_block_hint(const suco_gpu_index* full, uint32_t num_shards, uint32_t* block) {
+    return guarded([&] {
+        if (!full || !block) raise(SUCO_ERR_CONTRACT, "null argument");
+        if (num_shards < 1) raise(SUCO_ERR_CONFIG, "num_shards must be >= 1");
+        DeviceGuard g(full->device);
+        const uint64_t n = full->host.n;
+        const uint32_t ns = full->host.layout.ns;
+        // slab length the select kernel picks for one shard's share; the shard then has at most
+        // CS blocks, so one counting round (plan_select_fixed with CH = block)
+        const uint64_t share = (n + num_shards - 1) / num_shards;
+        const SelectConfig c = plan_select(std::max<uint64_t>(share, 1), ns, cluster_size_from_env());
+        *block = c.rounds == 1 ? c.CH : select_slab_align() * 4;
+    });
+}
+
 int suco_gpu_shard_info(const suco_gpu_index* x, uint64_t* n_global, uint64_t* n_local, uint32_t* nblocks_local,
                         uint32_t* block, uint32_t* shard, uint32_t* num_shards) {
     return guarded([&] {
         if (!x) raise(SUCO_ERR_CONTRACT, "index is null");
-        const uint32_t b = x->num_shards > 1 ? x->block : static_cast<uint32_t>(std::min<uint64_t>(x->host.n, 0xFFFFFFFFull));
+        const uint32_t b = x->block ? x->block : static_cast<uint32_t>(std::min<uint64_t>(x->host.n, 0xFFFFFFFFull));
         if (n_global) *n_global = x->n_global;
         if (n_local) *n_local = x->host.n;
         if (nblocks_local) *nblocks_local = static_cast<uint32_t>((x->host.n + b - 1) / b);
@@ -930,10 +949,11 @@ int suco_gpu_shard_histograms(suco_gpu_index* x, const float* d_queries, uint64_
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : x->stream;
         const uint64_t nl = x->host.n;
         const uint32_t ns = x->host.layout.ns;
-        const uint32_t b = x->num_shards > 1 ? x->block : static_cast<uint32_t>(nl);
+        const uint32_t b = x->block ? x->block : static_cast<uint32_t>(nl);
         const uint32_t nblocks = static_cast<uint32_t>((nl + b - 1) / b);
         auto& sl = x->slot[0];
-        x->shard_scores.reserve(nq * nl);
+        const uint64_t ss = (nl + 15) / 16 * 16;  // 16-byte score rows
+        x->shard_scores.reserve(nq * ss);
         stage_traverse(x, sl, d_queries, nq, suco_collision_count(p->alpha, x->n_global), st, nullptr);
         sl.cands.reserve(1);
         SelectArgs sa{};
@@ -953,9 +973,15 @@ int suco_gpu_shard_histograms(suco_gpu_index* x, const float* d_queries, uint64_
         sa.nq = nq;
         sa.cands = sl.cands.p;
         sa.scores_dbg = x->shard_scores.p;
+        sa.scores_stride = ss;
         sa.count_only = true;
-        CUDA_TRY(launch_select(sa, x->sel, nq, st));
-        CUDA_TRY(launch_block_hist(x->shard_scores.p, nq, nl, b, nblocks, ns, d_hist, st));
+        if (x->slab_is_block && x->sel.nslabs == nblocks) {
+            sa.slab_hist = d_hist;
+            CUDA_TRY(launch_select(sa, x->sel, nq, st));
+        } else {
+            CUDA_TRY(launch_select(sa, x->sel, nq, st));
+            CUDA_TRY(launch_block_hist(x->shard_scores.p, nq, nl, ss, b, nblocks, ns, d_hist, st));
+        }
     });
 }
 
@@ -968,15 +994,16 @@ int suco_gpu_shard_topk(suco_gpu_index* x, const float* d_queries, uint64_t nq, 
         if (qlen != x->host.d) raise(SUCO_ERR_CONTRACT, "query length does not match dataset d");
         validate_params(p, x->n_global);
         if (nq == 0) return;
-        if (x->shard_scores.cap < nq * x->host.n) raise(SUCO_ERR_CONTRACT, "suco_gpu_shard_topk needs phase 1 first");
+        const uint64_t ss = (x->host.n + 15) / 16 * 16;
+        if (x->shard_scores.cap < nq * ss) raise(SUCO_ERR_CONTRACT, "suco_gpu_shard_topk needs phase 1 first");
         DeviceGuard g(x->device);
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : x->stream;
         const uint64_t nl = x->host.n;
-        const uint32_t b = x->num_shards > 1 ? x->block : static_cast<uint32_t>(nl);
+        const uint32_t b = x->block ? x->block : static_cast<uint32_t>(nl);
         const uint32_t nblocks = static_cast<uint32_t>((nl + b - 1) / b);
         const uint64_t sd = std::max<uint64_t>(stride, 1);
         x->shard_cands.reserve(nq * sd);
-        CUDA_TRY(launch_shard_emit(x->shard_scores.p, nq, nl, b, nblocks, x->shard, x->num_shards, d_T, d_quota, d_base,
+        CUDA_TRY(launch_shard_emit(x->shard_scores.p, nq, nl, ss, b, nblocks, x->shard, x->num_shards, d_T, d_quota, d_base,
                                    x->shard_cands.p, sd, st));
         RerankArgs ra{};
         ra.data = x->data.p;

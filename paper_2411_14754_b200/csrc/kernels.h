@@ -59,6 +59,8 @@ struct SelectArgs {
     uint8_t* scores_dbg;  // optional nq x n
     long long* prof;      // optional debug phase timers (8 x u64)
     bool count_only;      // stop after counting (scores_dbg receives the scores): shard phase 1
+    uint64_t scores_stride;  // row stride of scores_dbg (0 = n); a multiple of 16 enables 16-byte stores
+    uint32_t* slab_hist;     // count_only: optional nq x nslabs x (ns + 2) copy of the slab histograms
 };
 struct SelectConfig {
     uint32_t CS, CH, nslabs, rounds;
@@ -66,6 +68,11 @@ struct SelectConfig {
     int clusters;  // resident clusters (persistent grid); 0 = unknown
 };
 SelectConfig plan_select(uint64_t n, uint32_t ns, int cluster_size);
+// Plan with a given slab length (a multiple of select_slab_align() that fits shared
+// memory); CH = 0 in the result when it does not. Shards use CH = block size so that
+// every slab is one block and the slab histograms are the block histograms.
+SelectConfig plan_select_fixed(uint64_t n, uint32_t ns, uint32_t CH);
+uint32_t select_slab_align();
 cudaError_t launch_select(const SelectArgs& a, const SelectConfig& cfg, uint64_t nq, cudaStream_t st);
 cudaError_t launch_slab_offsets(const uint32_t* cell_off, const uint32_t* ids, uint64_t n, uint32_t ns,
                                 uint32_t K, uint32_t CH, uint32_t nslabs, uint32_t* slab_off,
@@ -94,9 +101,10 @@ struct RerankArgs {
 cudaError_t launch_rerank(const RerankArgs& a, uint64_t nq, cudaStream_t st);
 
 // ------------------------------------------------------------------- shards
-cudaError_t launch_block_hist(const uint8_t* scores, uint64_t nq, uint64_t n_local, uint32_t b, uint32_t nblocks,
-                              uint32_t ns, uint32_t* hist, cudaStream_t st);
-cudaError_t launch_shard_emit(const uint8_t* scores, uint64_t nq, uint64_t n_local, uint32_t b, uint32_t nblocks,
+cudaError_t launch_block_hist(const uint8_t* scores, uint64_t nq, uint64_t n_local, uint64_t stride, uint32_t b,
+                              uint32_t nblocks, uint32_t ns, uint32_t* hist, cudaStream_t st);
+cudaError_t launch_shard_emit(const uint8_t* scores, uint64_t nq, uint64_t n_local, uint64_t sstride, uint32_t b,
+                              uint32_t nblocks,
                               uint32_t shard, uint32_t num_shards, const uint32_t* T, const uint32_t* quota,
                               const uint32_t* base, uint32_t* cands, uint64_t stride, cudaStream_t st);
 

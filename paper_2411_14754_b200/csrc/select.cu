@@ -27,6 +27,7 @@
 //             position, so the candidate list comes out sorted by id.
 // When n > CS * CH_MAX the cluster walks `rounds` slabs per CTA twice
 // (histogram pass, then recount + emit) instead of spilling counters.
+#include <algorithm>
 #include <cooperative_groups.h>
 #include <cstdio>
 #include <cstdlib>
@@ -630,11 +631,33 @@ __global__ void __launch_bounds__(kThreads, SUCO_SELECT_MINB) select_kernel(Sele
             const uint32_t len = slab < a.nslabs ? static_cast<uint32_t>(min_u64(a.CH, a.n - lo)) : 0u;
             count_slab<NSB, KU, BRANCHY, PREFETCH, ATOMIC>(a, s, q, slab, lo, len, s.hist + r * hs, t_mark);
             if (a.scores_dbg) {
-                for (uint32_t i = tid; i < len; i += kThreads) a.scores_dbg[q * a.n + lo + i] = s.cnt[i];
+                const uint64_t ss = a.scores_stride ? a.scores_stride : a.n;
+                uint8_t* dst = a.scores_dbg + q * ss + lo;
+                if ((ss & 15u) == 0) {  // 16-byte rows: vector copy (lo is a multiple of CH)
+                    const uint32_t nv = len / 16;
+                    for (uint32_t i = tid; i < nv; i += kThreads) {
+                        reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(s.cnt)[i];
+                    }
+                    for (uint32_t i = nv * 16 + tid; i < len; i += kThreads) dst[i] = s.cnt[i];
+                } else {
+                    for (uint32_t i = tid; i < len; i += kThreads) dst[i] = s.cnt[i];
+                }
             }
 
         }
-        if (a.count_only) continue;  // shard phase 1: scores written, no cluster exchange
+        if (a.count_only) {  // shard phase 1: scores (and slab histograms) written, no cluster exchange
+            if (a.slab_hist) {
+                __syncthreads();
+                for (uint32_t r = 0; r < a.rounds; ++r) {
+                    const uint32_t slab = r * a.CS + rank;
+                    if (slab < a.nslabs && tid < hs) {
+                        a.slab_hist[(q * a.nslabs + slab) * hs + tid] = tid <= a.ns ? s.hist[r * hs + tid] : 0u;
+                    }
+                }
+                __syncthreads();
+            }
+            continue;
+        }
         cluster_barrier();
         SEL_MARK(3);
 
@@ -892,6 +915,25 @@ static int active_clusters_ns(uint32_t ns, const SelectConfig& c) {
     if (ns <= 16) return active_clusters<16>(c);
     if (ns <= 32) return active_clusters<32>(c);
     return active_clusters<0>(c);
+}
+
+uint32_t select_slab_align() { return kChAlign; }
+
+SelectConfig plan_select_fixed(uint64_t n, uint32_t ns, uint32_t CH) {
+    SelectConfig c{};
+    if (CH == 0 || CH % kChAlign != 0 || n == 0) return c;
+    const uint64_t nslabs = (n + CH - 1) / CH;
+    const uint32_t CS = static_cast<uint32_t>(std::min<uint64_t>(nslabs, 8));
+    const uint32_t rounds = static_cast<uint32_t>((nslabs + CS - 1) / CS);
+    if (smem_bytes(CH, rounds, ns) > kSmemLimit) return c;
+    c.CS = CS;
+    c.CH = CH;
+    c.nslabs = static_cast<uint32_t>(nslabs);
+    c.rounds = rounds;
+    c.smem = smem_bytes(CH, rounds, ns);
+    c.clusters = active_clusters_ns(ns, c);
+    if (c.clusters <= 0) c = SelectConfig{};
+    return c;
 }
 
 // Cluster size: the one that keeps the most SMs busy with a single counting

@@ -114,10 +114,19 @@ def _torch_stream(device) -> int:
     return torch.cuda.current_stream(device).cuda_stream or 1
 
 
-class GpuShard:
-    """One block-cyclic shard of a device index (suco_gpu_make_shard)."""
+def block_hint(full: GpuIndex, num_shards: int) -> int:
+    """Fastest block size for `num_shards` shards (suco_gpu_shard_block_hint): slabs == blocks."""
+    b = C.c_uint32()
+    _check(_c.shard_block_hint(full.handle, num_shards, C.byref(b)))
+    return b.value
 
-    def __init__(self, full: GpuIndex, shard: int, num_shards: int, block: int):
+
+class GpuShard:
+    """One block-cyclic shard of a device index (suco_gpu_make_shard); block=None picks block_hint."""
+
+    def __init__(self, full: GpuIndex, shard: int, num_shards: int, block: Optional[int] = None):
+        if block is None:
+            block = block_hint(full, num_shards)
         h = C.c_void_p()
         _check(_c.make_shard(full.handle, shard, num_shards, block, C.byref(h)))
         self.index = GpuIndex(h)

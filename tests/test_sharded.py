@@ -102,7 +102,10 @@ def test_gloo_world_size_2_matches_unsharded(oracle):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("G,block", [(1, 4096), (2, 512), (3, 1000), (4, 256), (8, 2048)])
+# blocks that are multiples of 2048 (and None = suco_gpu_shard_block_hint) take the
+# fused path: select slabs == blocks, histograms written by the select kernel
+@pytest.mark.parametrize("G,block", [(1, 4096), (2, 512), (3, 1000), (4, 256), (8, 2048), (1, None), (2, None),
+                                     (3, None), (3, 6144)])
 def test_gpu_emulated_shards_match_unsharded(gpu, oracle, G, block):
     from paper_2411_14754_b200.sharded import GpuShard, emulate
     full = oracle.clustered(20000 + 50, 32, 40, 77 + G, 20, 140, 18, True)
@@ -110,7 +113,8 @@ def test_gpu_emulated_shards_match_unsharded(gpu, oracle, G, block):
     idx = gpu.build_index(base, gpu.IndexParams(4, 16, 3, 42))
     shards = [GpuShard(idx, r, G, block) for r in range(G)]
     q = torch.from_numpy(qs).cuda()
-    for a, b, k in ((0.05, 0.005, 10), (0.02, 0.05, 40), (0.3, 0.001, 3)):
+    # last case: fewer than m points collide at all, so T = 0 and zero-score ties fill the quota
+    for a, b, k in ((0.05, 0.005, 10), (0.02, 0.05, 40), (0.3, 0.001, 3), (0.001, 0.4, 5)):
         want_i, want_d = idx.knn_query_batch(qs, gpu.CollisionParams(a, b, k))
         ids, dd = emulate(shards, q, gpu.CollisionParams(a, b, k))
         assert np.array_equal(ids.cpu().numpy().astype(np.uint32), want_i), (G, block, a, b, k)
