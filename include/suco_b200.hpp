@@ -12,7 +12,7 @@
 //   suco::dynamic_activation query.hpp:57       suco::gpu::dynamic_activation   -> suco_gpu_dynamic_activation
 //   suco::rerank           query.hpp:83         suco::gpu::rerank               -> suco_gpu_rerank
 //   suco::kmeans           kmeans.hpp:46        suco::gpu::kmeans               -> suco_gpu_kmeans
-//   suco::build_imi        index.hpp:38         suco::gpu::build_imi            -> suco_gpu_build_imi
+//   suco::build_imi        index.hpp:39         suco::gpu::build_imi            -> suco_gpu_build_imi
 //   suco::collision_count / candidate_count / CollisionParams::validate (sc_linear.hpp:30-40)
 //                                               -> suco_collision_count / suco_candidate_count /
 //                                                  suco_validate_collision_params
