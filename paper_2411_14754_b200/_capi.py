@@ -37,7 +37,14 @@ class CollisionParamsC(C.Structure):
 
 
 def _sig(name, restype, *argtypes):
-    f = getattr(lib, name)
+    try:
+        f = getattr(lib, name)
+    except AttributeError:
+        if LIB_PATH == os.path.join(HERE, "libsuco_b200.so"):
+            raise
+        def missing(*_a, _n=name):  # an older SUCO_LIB build (A/B timing only)
+            raise ImportError(f"{LIB_PATH} does not export {_n}")
+        return missing
     f.restype = restype
     f.argtypes = list(argtypes)
     return f

@@ -1020,6 +1020,7 @@ int suco_gpu_shard_topk(suco_gpu_index* x, const float* d_queries, uint64_t nq, 
         ra.squared = true;
         ra.shard_b = x->num_shards > 1 ? b : 0;
         ra.shard_G = x->num_shards > 1 ? x->num_shards : 0;
+        ra.shard_s = x->shard;
         auto& sl = x->slot[0];
         if (p->k > 32) {
             sl.all_d.reserve(nq * sd);
@@ -1028,6 +1029,7 @@ int suco_gpu_shard_topk(suco_gpu_index* x, const float* d_queries, uint64_t nq, 
             ra.all_id = sl.all_id.p;
         }
         CUDA_TRY(launch_rerank(ra, nq, st));
+        if (x->num_shards > 1) CUDA_TRY(launch_shard_ids(d_ids, nq * p->k, b, x->num_shards, x->shard, st));
     });
 }
 

@@ -96,11 +96,14 @@ struct RerankArgs {
     float data_int_max;   // >= 0: every data value is an integer with |v| <= this; < 0: not certified
     const uint32_t* counts;  // optional per-query candidate counts (<= m; m is then the row stride)
     bool squared;            // output squared distances (shard-local top-k for the cross-shard merge)
-    uint32_t shard_b, shard_G; // shards: row of global id g = ((g / b) / G) * b + g % b; shard_G = 0: row = g
+    uint32_t shard_b, shard_G, shard_s; // unused by the kernels: shards re-rank LOCAL rows (local order ==
+                                        // global order) and launch_shard_ids maps the k outputs to global ids
 };
 cudaError_t launch_rerank(const RerankArgs& a, uint64_t nq, cudaStream_t st);
 
 // ------------------------------------------------------------------- shards
+// ids[i] = ((l / b) * G + shard) * b + l % b for the n local ids l (0xffffffff kept).
+cudaError_t launch_shard_ids(uint32_t* ids, uint64_t n, uint32_t b, uint32_t G, uint32_t shard, cudaStream_t st);
 cudaError_t launch_block_hist(const uint8_t* scores, uint64_t nq, uint64_t n_local, uint64_t stride, uint32_t b,
                               uint32_t nblocks, uint32_t ns, uint32_t* hist, cudaStream_t st);
 cudaError_t launch_shard_emit(const uint8_t* scores, uint64_t nq, uint64_t n_local, uint64_t sstride, uint32_t b,

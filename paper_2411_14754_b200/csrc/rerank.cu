@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
 #pragma unroll
         for (uint32_t j = 0; j < kRows; ++j) {
             gid[j] = __shfl_sync(kFull, my_id, j);
-            rid[j] = a.shard_G ? ((gid[j] / a.shard_b) / a.shard_G) * a.shard_b + gid[j] % a.shard_b : gid[j];
+            rid[j] = gid[j];
         }
         const uint32_t nrows = static_cast<uint32_t>(min_u64(kRows, mq - base));
         double acc = 0.0;

@@ -217,6 +217,84 @@ __device__ __forceinline__ void load_wave(const Smem& s, const uint32_t* ids, ui
     w.mask = mask;
 }
 
+// ---- lean (branch-free) waves. Shared memory is addressed with 32-bit
+// shared-window addresses computed once (plain pointers made the compiler
+// rebuild the cluster window base, S2R SR_CgaCtaId + LEA, on every access), one
+// LDS.64 per unit descriptor, a predicated global load per slot, and invalid
+// slots redirected to a scratch byte with produced value 0 (whose histogram
+// increment is shl(1, 0xfffffff8) = 0 under PTX's clamped shifts).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint2 lds_v2(uint32_t a) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v));
+}
+__device__ __forceinline__ uint32_t ldg_if(const uint32_t* p, bool ok) {
+    uint32_t v = 0;
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.nc.u32 %0, [%1];\n\t}"
+        : "+r"(v)
+        : "l"(p), "r"(static_cast<uint32_t>(ok)));
+    return v;
+}
+__device__ __forceinline__ uint64_t one_shl(uint32_t sh) {  // 1 << sh, 0 when sh >= 64
+    uint64_t r;
+    asm("shl.b64 %0, %1, %2;" : "=l"(r) : "l"(1ull), "r"(sh));
+    return r;
+}
+
+template <int NSB>
+__device__ __forceinline__ void hist_add_lean(IncHist<NSB>& ih, uint32_t v) {  // v = 0: no-op
+    const uint32_t b = v - 1u;
+    if constexpr (IncHist<NSB>::W == 1) {
+        ih.h[0] += one_shl(8u * b);
+    } else {
+        const uint64_t inc = one_shl(8u * (b & 7u));
+#pragma unroll
+        for (int i = 0; i < IncHist<NSB>::W; ++i) ih.h[i] += ((b >> 3) == (uint32_t)i) ? inc : 0ull;
+    }
+}
+
+template <int KU>
+__device__ __forceinline__ void load_wave_lean(uint32_t ud_sa, const uint32_t* ids, uint32_t ua, uint32_t ub,
+                                               uint32_t lane, Wave<KU>& w) {
+    uint32_t mask = 0;
+#pragma unroll
+    for (int u = 0; u < KU; ++u) {
+        const bool in = ua + u < ub;  // warp-uniform
+        const uint2 d = lds_v2(ud_sa + 8u * (in ? ua + u : ua));
+        const bool ok = in && lane < d.y;
+        w.id[u] = ldg_if(ids + (d.x + lane), ok);
+        mask |= static_cast<uint32_t>(ok) << u;
+    }
+    w.mask = mask;
+}
+
+// cbase = shared address of counter 0 minus the slab's first id (wraps mod 2^32).
+template <int NSB, int KU>
+__device__ __forceinline__ void rmw_wave_lean(uint32_t cbase, uint32_t dummy, const Wave<KU>& w, IncHist<NSB>& ih) {
+    uint32_t ad[KU], v[KU];
+#pragma unroll
+    for (int u = 0; u < KU; ++u) ad[u] = ((w.mask >> u) & 1u) ? cbase + w.id[u] : dummy;
+#pragma unroll
+    for (int u = 0; u < KU; ++u) v[u] = lds_u8(ad[u]);
+#pragma unroll
+    for (int u = 0; u < KU; ++u) v[u] = ((w.mask >> u) & 1u) ? v[u] + 1u : 0u;
+#pragma unroll
+    for (int u = 0; u < KU; ++u) sts_u8(ad[u], v[u]);
+#pragma unroll
+    for (int u = 0; u < KU; ++u) hist_add_lean<NSB>(ih, v[u]);
+}
+
 // Shared-memory atomic variant: safe across subspaces, so no barriers needed.
 template <int NSB, int KU>
 __device__ __forceinline__ void atomic_wave(const Smem& s, const Wave<KU>& w, uint32_t lo, IncHist<NSB>& ih,
@@ -424,14 +502,23 @@ __device__ void count_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint3
                     __syncthreads();  // counters of sb3 final before sb3 + 1 increments
                 }
             } else {
+                const uint32_t ud_sa = smem_addr(s.udesc);
+                const uint32_t cbase = smem_addr(s.cnt) - static_cast<uint32_t>(lo);
+                const uint32_t dummy = smem_addr(s.misc + 7);
                 for (uint32_t sb3 = sb; sb3 < se; ++sb3) {
                     uint32_t ua, ub;
                     range(sb3, ua, ub);
                     const uint32_t* ids = a.ids + static_cast<uint64_t>(sb3) * a.n;
                     for (uint32_t u0 = ua; u0 < ub; u0 += KU) {
                         Wave<KU> w;
-                        load_wave<KU, BRANCHY>(s, ids, u0, ub, w);
-                        rmw_wave<NSB, KU>(s, w, static_cast<uint32_t>(lo), ih, hist);
+                        if constexpr (!BRANCHY && NSB > 0) {
+                            load_wave_lean<KU>(ud_sa, ids, u0, ub, lane, w);
+                            __syncwarp();  // keeps ptxas from hoisting a slot's RMW above the other slots' loads
+                            rmw_wave_lean<NSB, KU>(cbase, dummy, w, ih);
+                        } else {
+                            load_wave<KU, BRANCHY>(s, ids, u0, ub, w);
+                            rmw_wave<NSB, KU>(s, w, static_cast<uint32_t>(lo), ih, hist);
+                        }
                         if (++waves_since_flush * KU >= 240) {
                             ih.flush(hist, a.ns);
                             waves_since_flush = 0;
@@ -610,7 +697,7 @@ __device__ void emit_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint64
     }
 }
 
-template <int NSB, int KU = 8, bool BRANCHY = true, bool PREFETCH = false, bool ATOMIC = false>
+template <int NSB, int KU = 8, bool BRANCHY = false, bool PREFETCH = false, bool ATOMIC = false>
 __global__ void __launch_bounds__(kThreads, SUCO_SELECT_MINB) select_kernel(SelectArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     cg::cluster_group cluster = cg::this_cluster();

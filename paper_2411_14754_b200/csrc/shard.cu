@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(256) shard_emit_vec_kernel(const uint8_t* __re
     const uint32_t t = T[q];
     const uint32_t qu = quota[q * nblocks + blk];
     uint32_t* out = cands + q * stride + base[q * nblocks + blk];
-    const uint32_t gbase = static_cast<uint32_t>((uint64_t(blk) * num_shards + shard) * b);
+    const uint32_t gbase = static_cast<uint32_t>(lo);  // local ids (rerank reports global ids)
     const uint32_t ngroups = (len + 15) / 16;
     const uint32_t nfull = len / 16;
     uint32_t taken_run = 0, tie_run = 0;  // warp-uniform running totals
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(256) shard_emit_kernel(const uint8_t* __restri
     const uint32_t t = T[q];
     const uint32_t qu = quota[q * nblocks + blk];
     uint32_t* out = cands + q * stride + base[q * nblocks + blk];
-    const uint64_t gbase = (uint64_t(blk) * num_shards + shard) * b;  // global id of the block's first point
+    const uint64_t gbase = lo;  // local id of the block's first point (rerank reports global ids)
     const uint32_t per = (len + blockDim.x - 1) / blockDim.x;
     const uint32_t i0 = min(len, tid * per), i1 = min(len, i0 + per);
     uint32_t g = 0, e = 0;
@@ -316,7 +316,20 @@ __global__ void shard_compact_kernel(const uint32_t* __restrict__ ids, const uin
     }
 }
 
+__global__ void shard_ids_kernel(uint32_t* ids, uint64_t n, uint32_t b, uint32_t G, uint32_t shard) {
+    const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t l = ids[i];
+    if (l != 0xffffffffu) ids[i] = ((l / b) * G + shard) * b + l % b;
+}
+
 }  // namespace
+
+cudaError_t launch_shard_ids(uint32_t* ids, uint64_t n, uint32_t b, uint32_t G, uint32_t shard, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    shard_ids_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(ids, n, b, G, shard);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_shard_imi(const uint32_t* ids, const uint32_t* cell_off, uint64_t n, uint32_t ns, uint32_t K,
                              uint32_t b, uint32_t G, uint32_t shard, uint32_t* counts, const uint32_t* local_off,
