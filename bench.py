@@ -47,6 +47,19 @@ def dist_env():
     return ws, rank, local
 
 
+def ncu_traffic(workload: str) -> dict:
+    """Per-launch DRAM bytes (read + write) of each query kernel from the committed ncu
+    --set full capture of this workload (profiles/ncu_traffic.json), else {}."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)
+    except (OSError, ValueError):
+        return {}
+    if t.get("workload") != workload:
+        return {}
+    return {k: v["dram_read_bytes"] + v["dram_write_bytes"] for k, v in t["kernels"].items()}
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -332,8 +345,12 @@ def main():
     dom_bytes = [bytes_select, bytes_select, bytes_rerank][dom] if dom else bytes_select
     achieved = dom_bytes / (stage_avg[dom] / 1000.0) / 1e9
     path_bytes = bytes_select + bytes_rerank
+    traffic = ncu_traffic(cfg.name)
+    for nm in names:
+        per_kernel[nm]["dram_bytes_ncu"] = traffic.get(nm)
     roofline = {"bound": "hbm", "kernel": dom_name if dom else "traverse (bytes of select shown)",
-                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic.get(dom_name), "traffic_source": "profiles/ncu_traffic.json" if traffic else None,
                 "peak_source": peak_src,
                 "query_path": {"bytes_per_step": path_bytes, "achieved": path_bytes / (total_ms / ws / args.steps / 1e3) / 1e9,
                                "frac": path_bytes / (total_ms / ws / args.steps / 1e3) / 1e9 / peak},
