@@ -359,6 +359,8 @@ __device__ void count_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint3
     if (len == 0) return;
     const uint32_t TC = s.sub_start[a.ns];
     const uint32_t stride = a.nslabs + 1;
+    // lean waves address ids by one 32-bit offset into the N_s x n array when it fits
+    const bool abs_ids = !BRANCHY && !PREFETCH && !ATOMIC && NSB > 0 && static_cast<uint64_t>(a.ns) * a.n <= 0xffffffffull;
     IncHist<NSB> ih;
     ih.clear();
     uint32_t waves_since_flush = 0;
@@ -380,6 +382,7 @@ __device__ void count_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint3
                 beg4[u] = __ldg(p);
                 len4[u] = __ldg(p + 1) - beg4[u];
                 nu4[u] = (len4[u] + 31) >> 5;
+                if (abs_ids) beg4[u] += sub * static_cast<uint32_t>(a.n);  // offset into the whole N_s x n array
             }
         }
         uint32_t UT;
@@ -501,24 +504,40 @@ __device__ void count_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint3
                     }
                     __syncthreads();  // counters of sb3 final before sb3 + 1 increments
                 }
-            } else {
+            } else if constexpr (!BRANCHY && NSB > 0) {
+                // lean waves (a wave is loaded then RMW'd; one barrier per subspace). Measured
+                // slower: carrying the next subspace's first wave over the barrier (register
+                // pressure) and an mbarrier split arrive/wait (1024 threads polling).
                 const uint32_t ud_sa = smem_addr(s.udesc);
                 const uint32_t cbase = smem_addr(s.cnt) - static_cast<uint32_t>(lo);
                 const uint32_t dummy = smem_addr(s.misc + 7);
                 for (uint32_t sb3 = sb; sb3 < se; ++sb3) {
                     uint32_t ua, ub;
                     range(sb3, ua, ub);
+                    const uint32_t* ids = abs_ids ? a.ids : a.ids + static_cast<uint64_t>(sb3) * a.n;
+                    for (uint32_t u0 = ua; u0 < ub; u0 += KU) {
+                        Wave<KU> w;
+                        load_wave_lean<KU>(ud_sa, ids, u0, ub, lane, w);
+                        __syncwarp();  // keeps ptxas from hoisting a slot's RMW above the other slots' loads
+                        rmw_wave_lean<NSB, KU>(cbase, dummy, w, ih);
+                        if (++waves_since_flush * KU >= 240) {
+                            ih.flush(hist, a.ns);
+                            waves_since_flush = 0;
+                        }
+                    }
+                    SEL_MARK(8);  // warp 0's own load+RMW work for this subspace
+                    __syncthreads();  // counters of sb3 final before sb3 + 1 increments
+                    SEL_MARK(9);  // waiting for the slowest warp
+                }
+            } else {
+                for (uint32_t sb3 = sb; sb3 < se; ++sb3) {
+                    uint32_t ua, ub;
+                    range(sb3, ua, ub);
                     const uint32_t* ids = a.ids + static_cast<uint64_t>(sb3) * a.n;
                     for (uint32_t u0 = ua; u0 < ub; u0 += KU) {
                         Wave<KU> w;
-                        if constexpr (!BRANCHY && NSB > 0) {
-                            load_wave_lean<KU>(ud_sa, ids, u0, ub, lane, w);
-                            __syncwarp();  // keeps ptxas from hoisting a slot's RMW above the other slots' loads
-                            rmw_wave_lean<NSB, KU>(cbase, dummy, w, ih);
-                        } else {
-                            load_wave<KU, BRANCHY>(s, ids, u0, ub, w);
-                            rmw_wave<NSB, KU>(s, w, static_cast<uint32_t>(lo), ih, hist);
-                        }
+                        load_wave<KU, BRANCHY>(s, ids, u0, ub, w);
+                        rmw_wave<NSB, KU>(s, w, static_cast<uint32_t>(lo), ih, hist);
                         if (++waves_since_flush * KU >= 240) {
                             ih.flush(hist, a.ns);
                             waves_since_flush = 0;
