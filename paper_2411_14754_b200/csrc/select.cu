@@ -591,43 +591,52 @@ __device__ void emit_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint64
     if (tid == 0) s.misc[1] = 0;
     __syncthreads();
     if (gt + (all_ties ? ties : 0u) > 0) {
-        // vectors [0, full) lie inside the slab; at most one partial vector follows
+        // vectors [0, full) lie inside the slab; at most one partial vector follows.
+        // One flag word per 16-counter vector: the four 0x80-per-byte masks folded as
+        // m0 | m1 >> 1 | m2 >> 2 | m3 >> 3, so bit p <-> counter (7 - p % 8) * 4 + p / 8
+        // and a single POPC counts the vector (POPC is quarter rate).
         const uint32_t full = len / 16;
         const uint32_t kq = (0x80u - (tsel ? tsel : 1u)) * 0x01010101u;
-        constexpr uint32_t kV = 4;  // uint4 vectors per lane per step (64 counters)
-        auto sel4 = [&](const uint4& v, uint32_t (&m)[4]) {
+        const uint32_t w_sa = smem_addr(s.cnt);
+        auto flags = [&](uint32_t vi) -> uint32_t {
+            uint4 v;
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                         : "r"(w_sa + 16u * vi));
+            uint32_t m0, m1, m2, m3;
             if (tsel == 0) {
-                m[0] = m[1] = m[2] = m[3] = 0x80808080u;
+                m0 = m1 = m2 = m3 = 0x80808080u;
             } else if (swar) {
-                m[0] = (v.x + kq) & 0x80808080u;
-                m[1] = (v.y + kq) & 0x80808080u;
-                m[2] = (v.z + kq) & 0x80808080u;
-                m[3] = (v.w + kq) & 0x80808080u;
+                m0 = (v.x + kq) & 0x80808080u;
+                m1 = (v.y + kq) & 0x80808080u;
+                m2 = (v.z + kq) & 0x80808080u;
+                m3 = (v.w + kq) & 0x80808080u;
             } else {
-                m[0] = sel_mask(v.x, 0, tsel, 4, false);
-                m[1] = sel_mask(v.y, 0, tsel, 4, false);
-                m[2] = sel_mask(v.z, 0, tsel, 4, false);
-                m[3] = sel_mask(v.w, 0, tsel, 4, false);
+                m0 = sel_mask(v.x, 0, tsel, 4, false);
+                m1 = sel_mask(v.y, 0, tsel, 4, false);
+                m2 = sel_mask(v.z, 0, tsel, 4, false);
+                m3 = sel_mask(v.w, 0, tsel, 4, false);
             }
+            if (vi >= full) {  // the partial tail vector
+                m0 &= sel_mask(0xffffffffu, vi * 4 + 0, 0, len, true);
+                m1 &= sel_mask(0xffffffffu, vi * 4 + 1, 0, len, true);
+                m2 &= sel_mask(0xffffffffu, vi * 4 + 2, 0, len, true);
+                m3 &= sel_mask(0xffffffffu, vi * 4 + 3, 0, len, true);
+            }
+            return m0 | (m1 >> 1) | (m2 >> 2) | (m3 >> 3);
         };
+        constexpr uint32_t kV = 4;  // vectors per lane per step (64 counters)
         for (uint32_t v0 = 0; v0 < nvec; v0 += kThreads * kV) {
-            uint32_t m[kV][4];
+            uint32_t f[kV];
             uint32_t c = 0;
 #pragma unroll
             for (uint32_t j = 0; j < kV; ++j) {
                 const uint32_t vi = v0 + j * kThreads + tid;
-                m[j][0] = m[j][1] = m[j][2] = m[j][3] = 0;
-                if (vi < full) {
-                    sel4(w128[vi], m[j]);
-                } else if (vi < nvec) {  // the partial tail vector
-                    sel4(w128[vi], m[j]);
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) m[j][u] &= sel_mask(0xffffffffu, vi * 4 + u, 0, len, true);
-                }
-                c += __popc(m[j][0]) + __popc(m[j][1]) + __popc(m[j][2]) + __popc(m[j][3]);
+                f[j] = vi < nvec ? flags(vi) : 0u;
+                c += __popc(f[j]);
             }
             if (!__any_sync(kFull, c != 0)) continue;
-            uint32_t x = c;  // warp-aggregated slot reservation
+            uint32_t x = c;  // warp-aggregated slot reservation (emission order is free)
 #pragma unroll
             for (int off = 1; off < 32; off <<= 1) {
                 const uint32_t y = __shfl_up_sync(kFull, x, off);
@@ -636,18 +645,15 @@ __device__ void emit_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint64
             uint32_t wbase = 0;
             if (lane == 31) wbase = atomicAdd(&s.misc[1], x);
             wbase = __shfl_sync(kFull, wbase, 31);
-            if (c) {
-                uint32_t pos = wbase + x - c;
-                for (uint32_t j = 0; j < kV; ++j) {
-                    const uint32_t vi = v0 + j * kThreads + tid;
-                    for (int u = 0; u < 4; ++u) {
-                        uint32_t mm = m[j][u];
-                        while (mm) {
-                            const uint32_t bit = __ffs(mm) - 1;
-                            __stcs(out + pos++, static_cast<uint32_t>(lo) + (vi * 4 + u) * 4 + (bit >> 3));  // streaming: keep ids in L2
-                            mm &= mm - 1;
-                        }
-                    }
+            uint32_t pos = wbase + x - c;
+#pragma unroll
+            for (uint32_t j = 0; j < kV; ++j) {
+                uint32_t mm = f[j];
+                const uint32_t idb = static_cast<uint32_t>(lo) + (v0 + j * kThreads + tid) * 16u;
+                while (mm) {
+                    const uint32_t p = __ffs(mm) - 1;
+                    __stcs(out + pos++, idb + (7u - (p & 7u)) * 4u + (p >> 3));  // streaming: keep ids in L2
+                    mm &= mm - 1;
                 }
             }
         }
@@ -1086,6 +1092,7 @@ cudaError_t launch_select(const SelectArgs& a0, const SelectConfig& cfg, uint64_
                      h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas, h[4] / ctas, h[5] / ctas, h[6] / ctas);
         std::fprintf(stderr, "[select prof] counting split: warp0 own waves %.0f, subspace barrier waits %.0f (remaining = staging tail/descriptors/flush)\n",
                      h[8] / ctas, h[9] / ctas);
+
         return e;
     }
     return launch_select_dispatch(a, cfg, nq, st);
