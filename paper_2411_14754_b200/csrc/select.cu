@@ -239,12 +239,20 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
 __device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v) {
     asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v));
 }
+// Predicated load; the result is undefined when !ok (callers mask it).
 __device__ __forceinline__ uint32_t ldg_if(const uint32_t* p, bool ok) {
     uint32_t v = 0;
     asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.nc.u32 %0, [%1];\n\t}"
         : "+r"(v)
         : "l"(p), "r"(static_cast<uint32_t>(ok)));
     return v;
+}
+// Opaque copy: keeps a loop invariant in a register (otherwise the compiler
+// rematerializes shared-window addresses from SR_CgaCtaId inside the loop).
+__device__ __forceinline__ uint32_t pin(uint32_t x) {
+    uint32_t y;
+    asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
 }
 __device__ __forceinline__ uint64_t one_shl(uint32_t sh) {  // 1 << sh, 0 when sh >= 64
     uint64_t r;
@@ -270,8 +278,8 @@ __device__ __forceinline__ void load_wave_lean(uint32_t ud_sa, const uint32_t* i
     uint32_t mask = 0;
 #pragma unroll
     for (int u = 0; u < KU; ++u) {
-        const bool in = ua + u < ub;  // warp-uniform
-        const uint2 d = lds_v2(ud_sa + 8u * (in ? ua + u : ua));
+        const bool in = ua + u < ub;  // warp-uniform; past-the-end descriptors read in-bounds junk, masked below
+        const uint2 d = lds_v2(ud_sa + 8u * (ua + u));
         const bool ok = in && lane < d.y;
         w.id[u] = ldg_if(ids + (d.x + lane), ok);
         mask |= static_cast<uint32_t>(ok) << u;
@@ -509,7 +517,7 @@ __device__ void count_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint3
                 // slower: carrying the next subspace's first wave over the barrier (register
                 // pressure) and an mbarrier split arrive/wait (1024 threads polling).
                 const uint32_t ud_sa = smem_addr(s.udesc);
-                const uint32_t cbase = smem_addr(s.cnt) - static_cast<uint32_t>(lo);
+                const uint32_t cbase = pin(smem_addr(s.cnt) - static_cast<uint32_t>(lo));
                 const uint32_t dummy = smem_addr(s.misc + 7);
                 for (uint32_t sb3 = sb; sb3 < se; ++sb3) {
                     uint32_t ua, ub;
