@@ -60,6 +60,17 @@ def ncu_traffic(workload: str) -> dict:
     return {k: v["dram_read_bytes"] + v["dram_write_bytes"] for k, v in t["kernels"].items()}
 
 
+def u8_row_bytes(base, queries):
+    """Row bytes of the byte re-rank path (d padded to 16) when data and queries are integers in
+    [0, 255] and d <= 512 — the library's own certification rule (capi.cu upload_data) — else 0."""
+    d = base.shape[1]
+    def ok(a):
+        return bool(np.all(a == np.trunc(a)) and a.min() >= 0 and a.max() <= 255)
+    if d > 512 or os.environ.get("SUCO_NO_U8") or not ok(base) or not ok(queries):
+        return 0
+    return (d + 15) // 16 * 16
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -334,11 +345,14 @@ def main():
     cum, sq, m = stats
     stage_avg = stage_ms / args.steps
     bytes_select = 4.0 * cum                      # u32 inverted-list ids streamed (query.cpp:235-239)
-    bytes_rerank = 4.0 * d * m * sq + 4.0 * d * sq  # candidate rows + query (query.cpp:177-182)
+    # candidate rows + query (query.cpp:177-182): 4-byte floats, or the byte rows the library keeps
+    # when the data and queries are integers in [0, 255] (exact integer re-rank)
+    row_bytes = u8_row_bytes(base, queries) or 4 * d
+    bytes_rerank = float(row_bytes) * m * sq + 4.0 * d * sq
     names = ["traverse", "select", "rerank"]
     per_kernel = {}
     for i, (nm, b) in enumerate(zip(names, [None, bytes_select, bytes_rerank])):
-        per_kernel[nm] = {"ms": stage_avg[i], "algorithmic_bytes": b,
+        per_kernel[nm] = {"ms": stage_avg[i], "algorithmic_bytes": b, **({"row_bytes": row_bytes} if nm == "rerank" else {}),
                           "achieved_gbs": (b / (stage_avg[i] / 1000.0) / 1e9) if b else None}
     dom = int(np.argmax(stage_avg))
     dom_name = names[dom]

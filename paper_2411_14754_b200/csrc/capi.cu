@@ -110,6 +110,8 @@ struct suco_gpu_index {
     DevBuf<uint32_t> slab_off;   // ns x K x (nslabs+1)
     SelectConfig sel{};
     float data_int_max = -1.f;  // integer certificate of the dataset (rerank fp32 path)
+    DevBuf<uint8_t> data8;      // u8 copy of the rows when they are integers in [0, 255] (rerank u8 path)
+    uint32_t dpad = 0;          // row bytes of data8 (0: no u8 copy)
     // block-cyclic shard (suco_gpu_make_shard): global blocks j with j % num_shards == shard
     uint32_t shard = 0, num_shards = 1, block = 0;
     bool slab_is_block = false;     // select slabs == shard blocks (phase 1 needs no histogram pass)
@@ -200,15 +202,23 @@ void upload_data(suco_gpu_index* x, const float* data, uint64_t n, uint32_t d) {
     check_finite_device(x->data.p, n * d, x->stream);
     // integer certificate (values integral, |v| <= 2^20) for the exact fp32 rerank chains
     DevBuf<unsigned int> st;
-    st.reserve(2);
-    unsigned int h[2] = {0, 0};
-    CUDA_TRY(cudaMemsetAsync(st.p, 0, 8, x->stream));
+    st.reserve(3);
+    unsigned int h[3] = {0, 0, 0};
+    CUDA_TRY(cudaMemsetAsync(st.p, 0, 12, x->stream));
     CUDA_TRY(launch_int_stats(x->data.p, n * d, st.p, x->stream));
-    CUDA_TRY(cudaMemcpyAsync(h, st.p, 8, cudaMemcpyDeviceToHost, x->stream));
+    CUDA_TRY(cudaMemcpyAsync(h, st.p, 12, cudaMemcpyDeviceToHost, x->stream));
     CUDA_TRY(cudaStreamSynchronize(x->stream));
     float mx;
     std::memcpy(&mx, &h[1], 4);
     x->data_int_max = (h[0] == 0 && mx <= 1048576.f) ? mx : -1.f;
+    // u8-valued rows (integers in [0, 255]): a byte copy for the exact integer re-rank, whose
+    // squared distances (< 2^32) are the reference's fp64 values in any summation order
+    x->dpad = 0;
+    if (h[0] == 0 && h[2] == 0 && mx <= 255.f && d <= 512 && !std::getenv("SUCO_NO_U8")) {
+        x->dpad = (d + 15) / 16 * 16;
+        x->data8.reserve(n * x->dpad);
+        CUDA_TRY(launch_pack_u8(x->data.p, n, d, x->dpad, x->data8.p, x->stream));
+    }
 }
 
 // Layout + centroid tables on the device, from x->host.
@@ -436,6 +446,8 @@ void stage_rerank(suco_gpu_index* x, suco_gpu_index::Slot& sl, const float* d_q,
     ra.out_ids = d_ids;
     ra.out_dists = d_dists;
     ra.data_int_max = x->data_int_max;
+    ra.data8 = x->dpad ? x->data8.p : nullptr;
+    ra.dpad = x->dpad;
     if (k > 32) {
         sl.all_d.reserve(nt * m);
         sl.all_id.reserve(nt * m);
@@ -853,13 +865,19 @@ int suco_gpu_make_shard(const suco_gpu_index* full, uint32_t shard, uint32_t num
             x->block = block;
             x->n_global = n;
             x->data_int_max = full->data_int_max;
-            // rows of the owned blocks, back to back
+            x->dpad = full->dpad;
+            // rows of the owned blocks, back to back (and their u8 copies)
             x->data.reserve(n_local * d);
+            if (x->dpad) x->data8.reserve(n_local * x->dpad);
             uint64_t lo = 0;
             for (uint64_t j = shard; j < nb; j += num_shards) {
                 const uint64_t len = std::min<uint64_t>(block, n - j * block);
                 CUDA_TRY(cudaMemcpyAsync(x->data.p + lo * d, full->data.p + j * block * d, len * d * 4,
                                          cudaMemcpyDeviceToDevice, x->stream));
+                if (x->dpad) {
+                    CUDA_TRY(cudaMemcpyAsync(x->data8.p + lo * x->dpad, full->data8.p + j * block * x->dpad,
+                                             len * x->dpad, cudaMemcpyDeviceToDevice, x->stream));
+                }
                 lo += len;
             }
             upload_codebooks(x);
@@ -1016,6 +1034,8 @@ int suco_gpu_shard_topk(suco_gpu_index* x, const float* d_queries, uint64_t nq, 
         ra.out_ids = d_ids;
         ra.out_dists = d_sqdists;
         ra.data_int_max = x->data_int_max;
+        ra.data8 = x->dpad ? x->data8.p : nullptr;
+        ra.dpad = x->dpad;
         ra.counts = d_counts;
         ra.squared = true;
         ra.shard_b = x->num_shards > 1 ? b : 0;
@@ -1130,16 +1150,23 @@ int suco_gpu_rerank(const float* data, uint64_t n, uint32_t d, const float* quer
         ra.k = k;
         ra.out_ids = oi.p;
         ra.out_dists = od.p;
+        DevBuf<uint8_t> d8;
         {
             DevBuf<unsigned int> st;
-            st.reserve(2);
-            unsigned int h[2] = {0, 0};
-            CUDA_TRY(cudaMemset(st.p, 0, 8));
+            st.reserve(3);
+            unsigned int h[3] = {0, 0, 0};
+            CUDA_TRY(cudaMemset(st.p, 0, 12));
             CUDA_TRY(launch_int_stats(dd.p, n * d, st.p, 0));
-            CUDA_TRY(cudaMemcpy(h, st.p, 8, cudaMemcpyDeviceToHost));
+            CUDA_TRY(cudaMemcpy(h, st.p, 12, cudaMemcpyDeviceToHost));
             float mx;
             std::memcpy(&mx, &h[1], 4);
             ra.data_int_max = (h[0] == 0 && mx <= 1048576.f) ? mx : -1.f;
+            if (h[0] == 0 && h[2] == 0 && mx <= 255.f && d <= 512 && !std::getenv("SUCO_NO_U8")) {
+                ra.dpad = (d + 15) / 16 * 16;
+                d8.reserve(n * ra.dpad);
+                CUDA_TRY(launch_pack_u8(dd.p, n, d, ra.dpad, d8.p, 0));
+                ra.data8 = d8.p;
+            }
         }
         if (k > 32) {
             ad.reserve(m), ai.reserve(m);

@@ -98,6 +98,8 @@ struct RerankArgs {
     bool squared;            // output squared distances (shard-local top-k for the cross-shard merge)
     uint32_t shard_b, shard_G, shard_s; // unused by the kernels: shards re-rank LOCAL rows (local order ==
                                         // global order) and launch_shard_ids maps the k outputs to global ids
+    const uint8_t* data8;  // optional u8 copy of the rows (data certified integer in [0, 255]), n x dpad
+    uint32_t dpad;         // row bytes of data8 (d rounded up to 16)
 };
 cudaError_t launch_rerank(const RerankArgs& a, uint64_t nq, cudaStream_t st);
 
@@ -121,6 +123,8 @@ cudaError_t launch_cell_sizes(const uint32_t* cell_off, uint32_t ns, uint32_t K,
                               cudaStream_t st);
 cudaError_t launch_check_finite(const float* data, uint64_t count, int* flag, cudaStream_t st);
 // out2[0] |= 1 if any value is non-integral; out2[1] = max |value| as float bits (both pre-zeroed)
-cudaError_t launch_int_stats(const float* data, uint64_t count, unsigned int* out2, cudaStream_t st);
+// out3[0] |= 1 non-integer, out3[1] = max |v| bits, out3[2] |= 1 negative (zero out3 first)
+cudaError_t launch_int_stats(const float* data, uint64_t count, unsigned int* out3, cudaStream_t st);
+cudaError_t launch_pack_u8(const float* data, uint64_t n, uint32_t d, uint32_t dpad, uint8_t* out, cudaStream_t st);
 
 }  // namespace suco_gpu

@@ -36,6 +36,8 @@ __device__ __forceinline__ float4 ld_stream4(const float* p) {
     return v;
 }
 
+__device__ __forceinline__ bool is_u8(float v) { return v == truncf(v) && v >= 0.f && v <= 255.f; }
+
 // Inserts (d, id) into the warp's sorted list (lane i holds entry i, k <= 32).
 __device__ __forceinline__ void warp_insert(double d, uint32_t id, double& ld, uint32_t& lid, uint32_t k,
                                             uint32_t lane) {
@@ -67,15 +69,17 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
     const float* query = a.queries + q * a.d;
     if (tid < 2) qstat[tid] = 0;
     __syncthreads();
-    bool qbad = false;
+    bool qbad = false, qu8 = true;
     float qmax = 0.f;
     for (uint32_t i = tid; i < a.d; i += kThreads) {
         const float v = query[i];
         qd[i] = static_cast<double>(v);
         qf[i] = v;
         qbad |= (v != truncf(v));
+        qu8 &= is_u8(v);
         qmax = fmaxf(qmax, fabsf(v));
     }
+    if (a.data8 && __syncthreads_and(qu8)) return;  // rerank_u8_kernel owns this query
     qbad = __any_sync(kFull, qbad);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) qmax = fmaxf(qmax, __shfl_xor_sync(kFull, qmax, o));
@@ -201,6 +205,121 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
     }
 }
 
+// ---------------------------------------------------------------- u8 rows
+// Data certified integer in [0, 255] at upload and a query of the same kind:
+// every (x - q)^2 is an integer and every partial sum stays below 2^32, so
+// the integer sum — in ANY order — is the exact value of the reference's fp64
+// 4-accumulator sum. Rows are read as bytes (a quarter of the fp32 traffic):
+// L = lanes per row (16 bytes each), R = 32 / L rows per warp load, U loads in
+// flight per lane; |x - q| and the 4-byte dot product are one VABSDIFF4 and
+// one IDP.4A per word; L lanes reduce a row with log2(L) shuffles.
+
+__device__ __forceinline__ uint4 ld_nc_u4(const uint8_t* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+
+template <uint32_t L, bool GENERIC>
+__global__ void __launch_bounds__(kThreads) rerank_u8_kernel(RerankArgs a) {
+    constexpr uint32_t R = 32 / L;
+    constexpr uint32_t U = L >= 4 ? 4 : L;  // loads in flight per lane, with at most 32 rows per step
+    constexpr uint32_t kStep = R * U;       // rows per warp step (<= 32: one candidate id per lane)
+    static_assert(kStep <= 32, "one candidate id per lane");
+    __shared__ double md[kWarps * 32];
+    __shared__ uint32_t mi[kWarps * 32];
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint64_t q = blockIdx.x;
+    const float* query = a.queries + q * a.d;
+    bool ok = true;
+    for (uint32_t i = tid; i < a.d; i += kThreads) ok &= is_u8(query[i]);
+    if (!__syncthreads_and(ok)) return;  // the fp32/fp64 kernel owns this query
+    const uint32_t c = lane % L, g = lane / L;
+    const bool live = 16u * c < a.dpad;  // L is dpad/16 rounded up to a power of two
+    uint32_t qw[4];
+#pragma unroll
+    for (uint32_t w = 0; w < 4; ++w) {
+        uint32_t v = 0;
+#pragma unroll
+        for (uint32_t b = 0; b < 4; ++b) {
+            const uint32_t i = 16u * c + 4u * w + b;
+            if (i < a.d) v |= static_cast<uint32_t>(query[i]) << (8u * b);
+        }
+        qw[w] = v;
+    }
+    const uint32_t* cands = a.cands + q * a.m;
+    const uint64_t mq = a.counts ? a.counts[q] : a.m;
+    double ld = kInf;
+    uint32_t lid = 0xffffffffu;
+    for (uint64_t base = static_cast<uint64_t>(warp) * kStep; base < mq; base += kStep * kWarps) {
+        const uint32_t my = (lane < kStep && base + lane < mq) ? __ldcs(cands + base + lane) : 0u;
+        uint32_t idr[U];
+        bool vr[U];
+        uint4 x[U];
+#pragma unroll
+        for (uint32_t u = 0; u < U; ++u) {
+            const uint32_t r = u * R + g;
+            idr[u] = __shfl_sync(kFull, my, r);
+            vr[u] = base + r < mq;
+            x[u] = (vr[u] && live) ? ld_nc_u4(a.data8 + static_cast<uint64_t>(idr[u]) * a.dpad + 16u * c)
+                                   : make_uint4(0, 0, 0, 0);
+        }
+        double dist[U];
+#pragma unroll
+        for (uint32_t u = 0; u < U; ++u) {
+            uint32_t acc = 0;
+            acc = __dp4a(__vabsdiffu4(x[u].x, qw[0]), __vabsdiffu4(x[u].x, qw[0]), acc);
+            acc = __dp4a(__vabsdiffu4(x[u].y, qw[1]), __vabsdiffu4(x[u].y, qw[1]), acc);
+            acc = __dp4a(__vabsdiffu4(x[u].z, qw[2]), __vabsdiffu4(x[u].z, qw[2]), acc);
+            acc = __dp4a(__vabsdiffu4(x[u].w, qw[3]), __vabsdiffu4(x[u].w, qw[3]), acc);
+#pragma unroll
+            for (uint32_t o = L / 2; o >= 1; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+            dist[u] = vr[u] ? static_cast<double>(acc) : kInf;
+        }
+        if constexpr (GENERIC) {
+#pragma unroll
+            for (uint32_t u = 0; u < U; ++u) {
+                if (c == 0 && vr[u]) {
+                    a.all_d[q * a.m + base + u * R + g] = dist[u];
+                    a.all_id[q * a.m + base + u * R + g] = idr[u];
+                }
+            }
+        } else {
+#pragma unroll
+            for (uint32_t u = 0; u < U; ++u) {
+                const double wd = __shfl_sync(kFull, ld, a.k - 1);
+                const uint32_t wi = __shfl_sync(kFull, lid, a.k - 1);
+                uint32_t bal = __ballot_sync(kFull, c == 0 && vr[u] && dist_id_less(dist[u], idr[u], wd, wi));
+                while (bal) {  // rows that beat the current k-th best (rare once the list fills)
+                    const uint32_t src = __ffs(bal) - 1;
+                    bal &= bal - 1;
+                    warp_insert(__shfl_sync(kFull, dist[u], src), __shfl_sync(kFull, idr[u], src), ld, lid, a.k, lane);
+                }
+            }
+        }
+    }
+    if constexpr (!GENERIC) {
+        md[warp * 32 + lane] = ld;
+        mi[warp * 32 + lane] = lid;
+        __syncthreads();
+        if (warp == 0) {
+            for (uint32_t w = 1; w < kWarps; ++w) {
+                for (uint32_t i = 0; i < a.k; ++i) {
+                    const double dv = md[w * 32 + i];
+                    if (dv == kInf) break;
+                    warp_insert(dv, mi[w * 32 + i], ld, lid, a.k, lane);
+                }
+            }
+            if (lane < a.k) {
+                a.out_ids[q * a.k + lane] = lid;
+                a.out_dists[q * a.k + lane] = a.squared ? ld : __dsqrt_rn(ld);
+            }
+        }
+    }
+}
+
 // k > 32: k rounds of "smallest (dist, id) strictly after the previous pick"
 // over the m scored candidates of one query; (dist, id) is a strict total
 // order so this reproduces nth_element + sort (query.cpp:185-189).
@@ -272,7 +391,24 @@ cudaError_t launch_rerank(const RerankArgs& a, uint64_t nq, cudaStream_t st) {
         kern<<<static_cast<unsigned>(nq), kThreads, smem, st>>>(a);
         return cudaGetLastError();
     };
-    cudaError_t e;
+    cudaError_t e = cudaSuccess;
+    if (a.data8) {  // u8 queries here; the fp32/fp64 kernel below takes the others
+        uint32_t L = 1;
+        while (L < a.dpad / 16) L <<= 1;
+        auto u8 = [&](auto kg, auto kn) {
+            (generic ? kg : kn)<<<static_cast<unsigned>(nq), kThreads, 0, st>>>(a);
+            return cudaGetLastError();
+        };
+        switch (L) {
+            case 1: e = u8(rerank_u8_kernel<1, true>, rerank_u8_kernel<1, false>); break;
+            case 2: e = u8(rerank_u8_kernel<2, true>, rerank_u8_kernel<2, false>); break;
+            case 4: e = u8(rerank_u8_kernel<4, true>, rerank_u8_kernel<4, false>); break;
+            case 8: e = u8(rerank_u8_kernel<8, true>, rerank_u8_kernel<8, false>); break;
+            case 16: e = u8(rerank_u8_kernel<16, true>, rerank_u8_kernel<16, false>); break;
+            default: e = u8(rerank_u8_kernel<32, true>, rerank_u8_kernel<32, false>); break;
+        }
+        if (e != cudaSuccess) return e;
+    }
     if (vec) e = generic ? launch(rerank_kernel<true, true>) : launch(rerank_kernel<true, false>);
     else e = generic ? launch(rerank_kernel<false, true>) : launch(rerank_kernel<false, false>);
     if (e != cudaSuccess || !generic) return e;

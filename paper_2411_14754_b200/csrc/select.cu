@@ -51,7 +51,10 @@ constexpr uint32_t kThreads = SUCO_SELECT_THREADS;
 #endif
 constexpr uint32_t kWarps = kThreads / 32;
 constexpr uint32_t kCap = 4 * kThreads;  // retrieved cells staged per chunk (4 per thread)
-constexpr uint32_t kUnits = 8 * kThreads < 4096 ? 8 * kThreads : 4096;  // 32-id units described per window
+#ifndef SUCO_SELECT_UNITS
+#define SUCO_SELECT_UNITS 4096
+#endif
+constexpr uint32_t kUnits = 8 * kThreads < SUCO_SELECT_UNITS ? 8 * kThreads : SUCO_SELECT_UNITS;  // 32-id units per window
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr uint32_t kChAlign = 4 * 32 * kWarps;  // CH multiple of this: whole words per lane-step
 constexpr uint32_t kSmemLimit = 232448;        // opt-in dynamic shared memory per block on sm_100

@@ -28,25 +28,46 @@ __global__ void check_finite_kernel(const float* data, uint64_t count, unsigned 
 }
 
 // integer certificate: any non-integer value; largest |value| (as float bits)
+// out[0] |= 1: some value is not an integer; out[1] = max |v| (float bits); out[2] |= 1: some v < 0.
 __global__ void int_stats_kernel(const float* data, uint64_t count, unsigned int* out) {
-    bool bad = false;
+    bool bad = false, neg = false;
     float mx = 0.f;
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const float v = data[i];
         bad |= (v != truncf(v));
+        neg |= (v < 0.f);
         mx = fmaxf(mx, fabsf(v));
     }
     bad = __any_sync(0xffffffffu, bad);
+    neg = __any_sync(0xffffffffu, neg);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if ((threadIdx.x & 31) == 0) {
         if (bad) atomicOr(out, 1u);
         atomicMax(out + 1, __float_as_uint(mx));
+        if (neg) atomicOr(out + 2, 1u);
+    }
+}
+
+// rows of u8-valued floats -> bytes, rows padded with zeros to dpad (a multiple of 16)
+__global__ void pack_u8_kernel(const float* data, uint64_t n, uint32_t d, uint32_t dpad, uint8_t* out) {
+    const uint64_t total = n * dpad;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t r = i / dpad;
+        const uint32_t c = static_cast<uint32_t>(i % dpad);
+        out[i] = c < d ? static_cast<uint8_t>(data[r * d + c]) : uint8_t(0);
     }
 }
 
 }  // namespace
+
+cudaError_t launch_pack_u8(const float* data, uint64_t n, uint32_t d, uint32_t dpad, uint8_t* out, cudaStream_t st) {
+    const uint64_t blocks = min_u64((n * dpad + 255) / 256, 148ull * 16);
+    pack_u8_kernel<<<static_cast<unsigned>(blocks ? blocks : 1), 256, 0, st>>>(data, n, d, dpad, out);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_int_stats(const float* data, uint64_t count, unsigned int* out2, cudaStream_t st) {
     const uint64_t blocks = min_u64((count + 255) / 256, 148ull * 16);

@@ -275,3 +275,22 @@ def test_load_errors(gpu):
     bad[5, 3] = np.nan
     with pytest.raises(gpu.ContractError, match="component 163 is not finite"):
         gpu.load_index(blob, bad)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d,shift", [(40, 0.0), (128, 0.0), (17, 0.0), (40, -128.0)])
+def test_u8_rows_rerank_mixed_queries(gpu, oracle, d, shift):
+    """u8-valued rows take the byte re-rank (rerank_u8_kernel) for integer queries and the
+    fp32/fp64 chains for the others, in the same batch; negative integers take no byte path."""
+    full = oracle.clustered(5000 + 40, d, 25, 300 + d, 10, 240, 14, True)
+    base, qs = oracle.hold_out(full, 40, 301 + d)
+    base = (base + np.float32(shift)).astype(np.float32)
+    qs = (qs + np.float32(shift)).astype(np.float32)
+    qs[20:] += np.float32(0.375)  # half the queries fractional
+    oidx = oracle.build_index(base, 4, 10, 3, 42, 0)
+    idx = gpu.load_index(oidx.serialize(), base)
+    for a, b, k in ((0.05, 0.01, 10), (0.05, 0.02, 40), (0.2, 0.05, 1)):
+        ids, dd = idx.knn_query_batch(qs, gpu.CollisionParams(a, b, k))
+        oi, od, _ = oidx.knn_query_batch(base, qs, a, b, k)
+        assert np.array_equal(ids, oi), (d, shift, a, b, k)
+        assert np.array_equal(dd, od), (d, shift, a, b, k)
