@@ -111,6 +111,8 @@ struct suco_gpu_index {
     SelectConfig sel{};
     float data_int_max = -1.f;  // integer certificate of the dataset (rerank fp32 path)
     DevBuf<uint8_t> data8;      // u8 copy of the rows when they are integers in [0, 255] (rerank u8 path)
+    DevBuf<uint16_t> codes;     // n x 8: s*K + cell of every point (dense select, N_s <= 8)
+    bool dense = false;         // select stage = dense bit-sliced 32-query blocks (dense.cu)
     uint32_t dpad = 0;          // row bytes of data8 (0: no u8 copy)
     // block-cyclic shard (suco_gpu_make_shard): global blocks j with j % num_shards == shard
     uint32_t shard = 0, num_shards = 1, block = 0;
@@ -123,6 +125,8 @@ struct suco_gpu_index {
     struct Slot {
         DevBuf<float> q;
         DevBuf<uint32_t> cells, ncells, cands, out_ids, all_id;
+        DevBuf<uint16_t> dhist;               // dense select: nq x P x 8
+        DevBuf<uint32_t> dT, dquota, dbase;   // dense select plan
         DevBuf<double> out_d, all_d;
         cudaEvent_t trav = nullptr, sel = nullptr, rr = nullptr;
     };
@@ -287,6 +291,12 @@ void finalize_device(suco_gpu_index* x) {
     x->slab_off.reserve(uint64_t(ns) * x->K * (x->sel.nslabs + 1));
     CUDA_TRY(launch_slab_offsets(x->cell_off.p, x->ids.p, x->host.n, ns, x->K, x->sel.CH, x->sel.nslabs, x->slab_off.p,
                                  x->stream));
+    const char* dv = std::getenv("SUCO_DENSE");
+    x->dense = dense_supported(ns, x->K) && !(dv && std::atoi(dv) == 0);
+    if (x->dense) {
+        x->codes.reserve(x->host.n * 8);
+        CUDA_TRY(launch_dense_codes(x->ids.p, x->cell_off.p, x->host.n, ns, x->K, x->codes.p, x->stream));
+    }
     CUDA_TRY(cudaStreamSynchronize(x->stream));
     set_l2_window(x);
 }
@@ -345,7 +355,9 @@ struct Dbg {
 
 uint64_t tile_size(const suco_gpu_index* x, uint64_t nq, uint64_t m, uint32_t k) {
     const uint64_t ns = x->host.layout.ns;
-    const uint64_t per = ns * x->K * 4 + ns * 4 + m * 4 + (k > 32 ? m * 12 : 0) + uint64_t(x->host.d) * 4 + k * 12;
+    const uint64_t pieces = (x->host.n + 2047) / 2048;  // dense select scratch: hist (16 B) + quota/base per piece
+    const uint64_t per = ns * x->K * 4 + ns * 4 + m * 4 + (k > 32 ? m * 12 : 0) + uint64_t(x->host.d) * 4 + k * 12 +
+                         (x->dense ? pieces * 24 + 4 : 0);
     const uint64_t budget = 4ull << 30;
     return std::max<uint64_t>(1, std::min<uint64_t>(nq, budget / per));
 }
@@ -409,6 +421,33 @@ void stage_select(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nt, uint
     const HostIndex& h = x->host;
     sl.cands.reserve(nt * m);
     cudaEvent_t* ev = dbg ? nullptr : prof_pair(x, 1);
+    if (x->dense && !(dbg && dbg->scores)) {
+        DenseArgs da{};
+        da.codes = reinterpret_cast<const uint4*>(x->codes.p);
+        da.cells = sl.cells.p;
+        da.ncells = sl.ncells.p;
+        da.cells_cap = x->K;
+        da.ns = h.layout.ns;
+        da.K = x->K;
+        da.n = h.n;
+        da.nq = nt;
+        da.m = m;
+        da.WP = 2048;
+        da.P = static_cast<uint32_t>((h.n + da.WP - 1) / da.WP);
+        sl.dhist.reserve(nt * da.P * 8);
+        sl.dT.reserve(nt);
+        sl.dquota.reserve(nt * da.P);
+        sl.dbase.reserve(nt * da.P);
+        da.hist = sl.dhist.p;
+        da.T = sl.dT.p;
+        da.quota = sl.dquota.p;
+        da.base = sl.dbase.p;
+        da.cands = sl.cands.p;
+        if (ev) CUDA_TRY(cudaEventRecord(ev[0], st));
+        CUDA_TRY(launch_dense_select(da, st));
+        if (ev) CUDA_TRY(cudaEventRecord(ev[1], st));
+        return;
+    }
     SelectArgs sa{};
     sa.ids = x->ids.p;
     sa.slab_off = x->slab_off.p;
@@ -819,6 +858,11 @@ int suco_gpu_query_intermediates(suco_gpu_index* x, const float* query, uint32_t
             for (uint64_t i = 0; i < n; ++i) scores[i] = s8[i];
         }
         if (cands) {  // the select kernel emits the candidate SET; report it ascending
+            if (x->dense) {  // the production select (dense.cu) on the same traversal output
+                Dbg nodbg{};
+                stage_select(x, sl, 1, m, st, &nodbg);
+                CUDA_TRY(cudaStreamSynchronize(st));
+            }
             CUDA_TRY(cudaMemcpy(cands, x->slot[0].cands.p, m * 4, cudaMemcpyDeviceToHost));
             std::sort(cands, cands + m);
         }

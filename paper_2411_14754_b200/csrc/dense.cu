@@ -1,0 +1,310 @@
+// Dense bit-sliced selection over 32-query blocks (the select stage when
+// N_s <= 8 and the per-cell masks fit shared memory).
+//
+// The SC-score of point p for query q is the number of subspaces s whose
+// retrieved cells contain cell_s(p) (query.cpp:229-239: every id of a
+// retrieved cell gets one collision, and every id lies in exactly one cell
+// per subspace). A CTA owns 32 queries: for every (subspace, cell) it keeps a
+// 32-bit mask M[s*K + cell] whose bit j says "query j retrieved this cell".
+// A point's 8 masks summed bit-wise by a carry-save adder tree are its 4-bit
+// scores for all 32 queries at once (bit-planes b0..b3, bit j = query j); a
+// 32x32 bit transpose across the warp turns the planes of 32 consecutive
+// points into, per lane = query, the planes of that query's 32 scores. So one
+// table lookup serves 32 queries, and every point is visited in id order.
+//
+// The top-m by (score desc, id asc) (query.cpp:242-260) is cut exactly like
+// the shard protocol: points are split into id-contiguous pieces (one per
+// warp); K1 writes each piece's #(score >= t), K2 derives per query the
+// threshold T, need = m - #(score > T) and each piece's tie quota (the first
+// `need` ties in id order) and output offset, K3 re-scores the piece and
+// each lane emits its query's candidates: every score > T and the first
+// quota ties of the piece in id order.
+//
+// Point codes: codes[p][s] = s*K + cell_s(p) (u16; s >= N_s -> N_s*K, a
+// mask slot that is always zero).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace suco_gpu {
+namespace {
+
+constexpr uint32_t kDT = 512;        // threads per CTA (2 CTAs / SM)
+constexpr uint32_t kDW = kDT / 32;   // warps = pieces per CTA
+constexpr uint32_t kFull = 0xffffffffu;
+
+__device__ __forceinline__ void fadd(uint32_t a, uint32_t b, uint32_t c, uint32_t& s, uint32_t& cy) {
+    s = a ^ b ^ c;
+    cy = (a & b) | (c & (a ^ b));
+}
+
+// Row r = lane (bit c = column c) -> lane c holds column c (bit r = row r).
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, uint32_t lane) {
+    uint32_t m = 0x0000ffffu;
+#pragma unroll
+    for (uint32_t j = 16; j != 0; j >>= 1) {
+        const uint32_t y = __shfl_xor_sync(kFull, x, j);
+        x = (lane & j) ? ((x & ~m) | ((y >> j) & m)) : ((x & m) | ((y & m) << j));
+        m ^= m << (j >> 1);
+    }
+    return x;
+}
+
+// Bit-sliced x >= t over 32 4-bit numbers (planes B0..B3), t in [0, 15].
+__device__ __forceinline__ uint32_t ge_mask(uint32_t B0, uint32_t B1, uint32_t B2, uint32_t B3, uint32_t t) {
+    uint32_t gt = 0, eq = kFull;
+    const uint32_t B[4] = {B0, B1, B2, B3};
+#pragma unroll
+    for (int i = 3; i >= 0; --i) {
+        const uint32_t tm = ((t >> i) & 1u) ? kFull : 0u;
+        gt |= eq & B[i] & ~tm;
+        eq &= ~(B[i] ^ tm);
+    }
+    return gt | eq;
+}
+
+// Masks of the CTA's query block: M[s*K + cell] bit j <=> query q0 + j retrieved (s, cell).
+__device__ void build_masks(const DenseArgs& a, uint32_t* M, uint64_t q0, uint32_t nqb) {
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint32_t slots = a.ns * a.K + 1;
+    for (uint32_t i = tid; i < slots; i += kDT) M[i] = 0;
+    __syncthreads();
+    for (uint32_t j = warp; j < nqb; j += kDW) {
+        const uint64_t q = q0 + j;
+        for (uint32_t s = 0; s < a.ns; ++s) {
+            const uint32_t cnt = a.ncells[q * a.ns + s];
+            const uint32_t* cp = a.cells + (q * a.ns + s) * a.cells_cap;
+            for (uint32_t i = lane; i < cnt; i += 32) atomicOr(M + s * a.K + cp[i], 1u << j);
+        }
+    }
+    __syncthreads();
+}
+
+// Scores of the 32 points [t0, t0 + 32) for the block's 32 queries; returns
+// with lane = query: planes B0..B3 (bit r = point t0 + r).
+__device__ __forceinline__ void score_tile(const DenseArgs& a, const uint32_t* M, uint64_t t0, uint64_t p_hi,
+                                           uint32_t lane, uint32_t& B0, uint32_t& B1, uint32_t& B2, uint32_t& B3) {
+    const uint64_t p = t0 + lane;
+    const uint32_t none = a.ns * a.K;
+    uint4 c = make_uint4(none | (none << 16), none | (none << 16), none | (none << 16), none | (none << 16));
+    if (p < p_hi) c = __ldg(a.codes + p);
+    const uint32_t m0 = M[c.x & 0xffffu], m1 = M[c.x >> 16];
+    const uint32_t m2 = M[c.y & 0xffffu], m3 = M[c.y >> 16];
+    const uint32_t m4 = M[c.z & 0xffffu], m5 = M[c.z >> 16];
+    const uint32_t m6 = M[c.w & 0xffffu], m7 = M[c.w >> 16];
+    uint32_t s1, c1, s2, c2, b0, c4, s5, c5;
+    fadd(m0, m1, m2, s1, c1);
+    fadd(m3, m4, m5, s2, c2);
+    const uint32_t s3 = m6 ^ m7, c3 = m6 & m7;
+    fadd(s1, s2, s3, b0, c4);  // weight 1
+    fadd(c1, c2, c3, s5, c5);  // weight 2 (+ carry weight 4)
+    const uint32_t b1 = s5 ^ c4, c6 = s5 & c4;
+    const uint32_t b2 = c5 ^ c6, b3 = c5 & c6;
+    B0 = transpose32(b0, lane);
+    B1 = transpose32(b1, lane);
+    B2 = transpose32(b2, lane);
+    B3 = transpose32(b3, lane);
+}
+
+// K1: per (query, piece) #points with score >= t, t = 1..8 (u16 x 8).
+__global__ void __launch_bounds__(kDT, 2) dense_hist_kernel(DenseArgs a) {
+    extern __shared__ uint32_t M[];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint64_t q0 = uint64_t(blockIdx.x) * 32;
+    const uint32_t nqb = static_cast<uint32_t>(min_u64(32, a.nq - q0));
+    build_masks(a, M, q0, nqb);
+    const uint32_t piece = blockIdx.y * kDW + warp;
+    if (piece >= a.P) return;
+    const uint64_t lo = uint64_t(piece) * a.WP;
+    const uint64_t hi = min_u64(a.n, lo + a.WP);
+    uint32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (uint64_t t0 = lo; t0 < hi; t0 += 32) {
+        uint32_t B0, B1, B2, B3;
+        score_tile(a, M, t0, hi, lane, B0, B1, B2, B3);
+        // points past `hi` score 0: they never count for t >= 1
+        const uint32_t g8 = B3, g4 = B3 | B2, g2 = g4 | B1, g1 = g2 | B0;
+        const uint32_t g6 = B3 | (B2 & B1), g5 = B3 | (B2 & (B1 | B0)), g7 = B3 | (B2 & B1 & B0);
+        const uint32_t g3 = g4 | (B1 & B0);
+        cnt[0] += __popc(g1);
+        cnt[1] += __popc(g2);
+        cnt[2] += __popc(g3);
+        cnt[3] += __popc(g4);
+        cnt[4] += __popc(g5);
+        cnt[5] += __popc(g6);
+        cnt[6] += __popc(g7);
+        cnt[7] += __popc(g8);
+    }
+    if (lane < nqb) {
+        uint4 v;
+        v.x = cnt[0] | (cnt[1] << 16);
+        v.y = cnt[2] | (cnt[3] << 16);
+        v.z = cnt[4] | (cnt[5] << 16);
+        v.w = cnt[6] | (cnt[7] << 16);
+        reinterpret_cast<uint4*>(a.hist)[(q0 + lane) * a.P + piece] = v;
+    }
+}
+
+__device__ __forceinline__ uint32_t level(const uint4& v, uint32_t t) {  // #score >= t, t in 1..8
+    const uint32_t w = t <= 2 ? v.x : t <= 4 ? v.y : t <= 6 ? v.z : v.w;
+    return (t & 1u) ? (w & 0xffffu) : (w >> 16);
+}
+
+// K2: warp per query — T, need, per-piece tie quota (id order) and output offset.
+__global__ void __launch_bounds__(256) dense_plan_kernel(DenseArgs a) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t q = uint64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (q >= a.nq) return;
+    const uint4* h = reinterpret_cast<const uint4*>(a.hist) + q * a.P;
+    uint32_t tot[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (uint32_t p = lane; p < a.P; p += 32) {
+        const uint4 v = h[p];
+#pragma unroll
+        for (uint32_t t = 1; t <= 8; ++t) tot[t - 1] += level(v, t);
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tot[t] += __shfl_xor_sync(kFull, tot[t], o);
+    }
+    uint32_t T = 0;
+#pragma unroll
+    for (int t = 8; t >= 1; --t) {
+        if (T == 0 && static_cast<uint32_t>(t) <= a.ns && tot[t - 1] >= a.m) T = t;
+    }
+    uint32_t gtT = 0;
+#pragma unroll
+    for (int t = 1; t <= 8; ++t) {
+        if (static_cast<uint32_t>(t) == T + 1) gtT = tot[t - 1];
+    }
+    const uint64_t need = a.m - gtT;
+    uint64_t ties_run = 0, out_run = 0;
+    for (uint32_t p0 = 0; p0 < a.P; p0 += 32) {
+        const uint32_t p = p0 + lane;
+        uint32_t ties = 0, gt = 0;
+        if (p < a.P) {
+            const uint4 v = h[p];
+            const uint32_t len = static_cast<uint32_t>(min_u64(a.WP, a.n - uint64_t(p) * a.WP));
+            const uint32_t geT = T ? level(v, T) : len;
+            gt = T + 1 <= 8 ? level(v, T + 1) : 0u;
+            ties = geT - gt;
+        }
+        uint32_t tx = ties;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, tx, o);
+            if (lane >= static_cast<uint32_t>(o)) tx += y;
+        }
+        const uint32_t tsum = __shfl_sync(kFull, tx, 31);
+        const uint64_t before = ties_run + tx - ties;
+        const uint32_t quota = before >= need ? 0u : static_cast<uint32_t>(min_u64(ties, need - before));
+        const uint32_t take = gt + quota;
+        uint32_t ox = take;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, ox, o);
+            if (lane >= static_cast<uint32_t>(o)) ox += y;
+        }
+        const uint32_t osum = __shfl_sync(kFull, ox, 31);
+        if (p < a.P) {
+            a.quota[q * a.P + p] = quota;
+            a.base[q * a.P + p] = static_cast<uint32_t>(out_run + ox - take);
+        }
+        ties_run += tsum;
+        out_run += osum;
+    }
+    if (lane == 0) a.T[q] = T;
+}
+
+// K3: re-score each piece; lane = query emits score > T and the first quota ties (id order).
+__global__ void __launch_bounds__(kDT, 2) dense_emit_kernel(DenseArgs a) {
+    extern __shared__ uint32_t M[];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint64_t q0 = uint64_t(blockIdx.x) * 32;
+    const uint32_t nqb = static_cast<uint32_t>(min_u64(32, a.nq - q0));
+    build_masks(a, M, q0, nqb);
+    const uint32_t piece = blockIdx.y * kDW + warp;
+    if (piece >= a.P) return;
+    const uint64_t lo = uint64_t(piece) * a.WP;
+    const uint64_t hi = min_u64(a.n, lo + a.WP);
+    const uint64_t q = q0 + lane;
+    const bool mine = lane < nqb;
+    const uint32_t T = mine ? a.T[q] : 0u;
+    const uint32_t quota = mine ? a.quota[q * a.P + piece] : 0u;
+    uint32_t pos = mine ? a.base[q * a.P + piece] : 0u;
+    uint32_t* out = a.cands + (mine ? q : 0) * a.m;
+    uint32_t tseen = 0;
+    for (uint64_t t0 = lo; t0 < hi; t0 += 32) {
+        uint32_t B0, B1, B2, B3;
+        score_tile(a, M, t0, hi, lane, B0, B1, B2, B3);
+        if (!mine) continue;  // lanes past the block's last query only feed the transposes
+        const uint32_t vmask = hi - t0 >= 32 ? kFull : ((1u << (hi - t0)) - 1u);
+        const uint32_t geT = ge_mask(B0, B1, B2, B3, T) & vmask;
+        const uint32_t gt = ge_mask(B0, B1, B2, B3, T + 1) & vmask;
+        const uint32_t eq = geT & ~gt;
+        uint32_t take = gt;
+        if (eq && tseen < quota) {
+            const uint32_t r = quota - tseen;
+            uint32_t rest = eq;
+            for (uint32_t i = 0; i < r && rest; ++i) rest &= rest - 1;  // drop the first r ties
+            take |= eq ^ rest;
+        }
+        tseen += __popc(eq);
+        while (take) {
+            const uint32_t b = __ffs(take) - 1;
+            take &= take - 1;
+            __stcs(out + pos++, static_cast<uint32_t>(t0) + b);
+        }
+    }
+}
+
+__global__ void dense_codes_fill_kernel(uint16_t* codes, uint64_t count, uint16_t none) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count; i += uint64_t(gridDim.x) * blockDim.x)
+        codes[i] = none;
+}
+
+__global__ void dense_codes_kernel(const uint32_t* ids, const uint32_t* cell_off, uint64_t n, uint32_t ns, uint32_t K,
+                                   uint16_t* codes) {
+    const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (t >= uint64_t(ns) * K) return;
+    const uint32_t s = static_cast<uint32_t>(t / K), cell = static_cast<uint32_t>(t % K);
+    const uint32_t* off = cell_off + uint64_t(s) * (K + 1);
+    const uint32_t* sid = ids + uint64_t(s) * n;
+    const uint16_t code = static_cast<uint16_t>(s * K + cell);
+    for (uint32_t i = off[cell]; i < off[cell + 1]; ++i) codes[uint64_t(sid[i]) * 8 + s] = code;
+}
+
+}  // namespace
+
+bool dense_supported(uint32_t ns, uint32_t K) {
+    return ns >= 1 && ns <= 8 && uint64_t(ns) * K + 1 <= 65535 && (uint64_t(ns) * K + 1) * 4 <= 110 * 1024;
+}
+
+size_t dense_smem(uint32_t ns, uint32_t K) { return (size_t(ns) * K + 1) * 4; }
+
+cudaError_t launch_dense_codes(const uint32_t* ids, const uint32_t* cell_off, uint64_t n, uint32_t ns, uint32_t K,
+                               uint16_t* codes, cudaStream_t st) {
+    const uint64_t count = n * 8;
+    const unsigned fb = static_cast<unsigned>(min_u64((count + 255) / 256, 148ull * 16));
+    dense_codes_fill_kernel<<<fb ? fb : 1, 256, 0, st>>>(codes, count, static_cast<uint16_t>(ns * K));
+    const uint64_t total = uint64_t(ns) * K;
+    dense_codes_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(ids, cell_off, n, ns, K, codes);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dense_select(const DenseArgs& a, cudaStream_t st) {
+    if (a.nq == 0) return cudaSuccess;
+    const size_t smem = dense_smem(a.ns, a.K);
+    cudaError_t e = cudaFuncSetAttribute(dense_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(dense_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    const dim3 grid(static_cast<unsigned>((a.nq + 31) / 32), (a.P + kDW - 1) / kDW);
+    dense_hist_kernel<<<grid, kDT, smem, st>>>(a);
+    dense_plan_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(a);
+    dense_emit_kernel<<<grid, kDT, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace suco_gpu

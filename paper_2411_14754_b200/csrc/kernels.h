@@ -78,6 +78,28 @@ cudaError_t launch_slab_offsets(const uint32_t* cell_off, const uint32_t* ids, u
                                 uint32_t K, uint32_t CH, uint32_t nslabs, uint32_t* slab_off,
                                 cudaStream_t st);
 
+// ------------------------------------------------------------------ dense select
+// Bit-sliced dense selection over 32-query blocks (dense.cu): same output as
+// select_kernel (the top-m candidate set, unordered) when N_s <= 8.
+struct DenseArgs {
+    const uint4* codes;        // n x 8 u16: s*K + cell of the point in subspace s (N_s*K when s >= N_s)
+    const uint32_t* cells;     // nq x ns x cells_cap (traversal output)
+    const uint32_t* ncells;    // nq x ns
+    uint32_t cells_cap, ns, K;
+    uint64_t n, nq, m;
+    uint32_t P, WP;            // pieces of WP consecutive points (one warp each)
+    uint16_t* hist;            // nq x P x 8: #score >= t, t = 1..8
+    uint32_t* T;               // nq
+    uint32_t* quota;           // nq x P
+    uint32_t* base;            // nq x P
+    uint32_t* cands;           // nq x m
+};
+bool dense_supported(uint32_t ns, uint32_t K);
+size_t dense_smem(uint32_t ns, uint32_t K);
+cudaError_t launch_dense_codes(const uint32_t* ids, const uint32_t* cell_off, uint64_t n, uint32_t ns, uint32_t K,
+                               uint16_t* codes, cudaStream_t st);
+cudaError_t launch_dense_select(const DenseArgs& a, cudaStream_t st);
+
 // ------------------------------------------------------------------ rerank
 // Exact fp64 re-rank of the candidate rows (query.cpp:159-197) with a
 // warp-level (dist, id) top-k; k > 32 takes a generic selection path.
