@@ -40,17 +40,36 @@ __device__ __forceinline__ void fadd(uint32_t a, uint32_t b, uint32_t c, uint32_
     cy = (a & b) | (c & (a ^ b));
 }
 
-// Row r = lane (bit c = column c) -> lane c holds column c (bit r = row r).
-__device__ __forceinline__ uint32_t transpose32(uint32_t x, uint32_t lane) {
-    uint32_t m = 0x0000ffffu;
-#pragma unroll
-    for (uint32_t j = 16; j != 0; j >>= 1) {
-        const uint32_t y = __shfl_xor_sync(kFull, x, j);
-        x = (lane & j) ? ((x & ~m) | ((y >> j) & m)) : ((x & m) | ((y & m) << j));
-        m ^= m << (j >> 1);
+// 32x32 bit transpose across a warp: row r = lane (bit c = column c) ->
+// lane c holds column c (bit r = row r). Five butterfly stages; the byte
+// stages (16, 8) are one PRMT with a per-lane selector, the bit stages
+// (4, 2, 1) a rotate by a per-lane amount and one LOP3 with a per-lane mask
+// (bits that wrap around land only where the mask keeps x).
+struct Xpose {
+    uint32_t sel16, sel8, amt4, amt2, amt1, msk4, msk2, msk1;
+    __device__ explicit Xpose(uint32_t lane) {
+        sel16 = (lane & 16) ? 0x3276u : 0x5410u;
+        sel8 = (lane & 8) ? 0x3715u : 0x6240u;
+        amt4 = (lane & 4) ? 28u : 4u;
+        amt2 = (lane & 2) ? 30u : 2u;
+        amt1 = (lane & 1) ? 31u : 1u;
+        msk4 = (lane & 4) ? ~0x0f0f0f0fu : 0x0f0f0f0fu;
+        msk2 = (lane & 2) ? ~0x33333333u : 0x33333333u;
+        msk1 = (lane & 1) ? ~0x55555555u : 0x55555555u;
     }
-    return x;
-}
+    __device__ __forceinline__ static uint32_t bits(uint32_t x, uint32_t y, uint32_t amt, uint32_t msk) {
+        const uint32_t r = __funnelshift_l(y, y, amt);
+        return (x & msk) | (r & ~msk);
+    }
+    __device__ __forceinline__ uint32_t operator()(uint32_t x) const {
+        x = __byte_perm(x, __shfl_xor_sync(kFull, x, 16), sel16);
+        x = __byte_perm(x, __shfl_xor_sync(kFull, x, 8), sel8);
+        x = bits(x, __shfl_xor_sync(kFull, x, 4), amt4, msk4);
+        x = bits(x, __shfl_xor_sync(kFull, x, 2), amt2, msk2);
+        x = bits(x, __shfl_xor_sync(kFull, x, 1), amt1, msk1);
+        return x;
+    }
+};
 
 // Bit-sliced x >= t over 32 4-bit numbers (planes B0..B3), t in [0, 15].
 __device__ __forceinline__ uint32_t ge_mask(uint32_t B0, uint32_t B1, uint32_t B2, uint32_t B3, uint32_t t) {
@@ -85,7 +104,8 @@ __device__ void build_masks(const DenseArgs& a, uint32_t* M, uint64_t q0, uint32
 // Scores of the 32 points [t0, t0 + 32) for the block's 32 queries; returns
 // with lane = query: planes B0..B3 (bit r = point t0 + r).
 __device__ __forceinline__ void score_tile(const DenseArgs& a, const uint32_t* M, uint64_t t0, uint64_t p_hi,
-                                           uint32_t lane, uint32_t& B0, uint32_t& B1, uint32_t& B2, uint32_t& B3) {
+                                           uint32_t lane, const Xpose& xp, uint32_t& B0, uint32_t& B1, uint32_t& B2,
+                                           uint32_t& B3) {
     const uint64_t p = t0 + lane;
     const uint32_t none = a.ns * a.K;
     uint4 c = make_uint4(none | (none << 16), none | (none << 16), none | (none << 16), none | (none << 16));
@@ -102,10 +122,10 @@ __device__ __forceinline__ void score_tile(const DenseArgs& a, const uint32_t* M
     fadd(c1, c2, c3, s5, c5);  // weight 2 (+ carry weight 4)
     const uint32_t b1 = s5 ^ c4, c6 = s5 & c4;
     const uint32_t b2 = c5 ^ c6, b3 = c5 & c6;
-    B0 = transpose32(b0, lane);
-    B1 = transpose32(b1, lane);
-    B2 = transpose32(b2, lane);
-    B3 = transpose32(b3, lane);
+    B0 = xp(b0);
+    B1 = xp(b1);
+    B2 = xp(b2);
+    B3 = xp(b3);
 }
 
 // K1: per (query, piece) #points with score >= t, t = 1..8 (u16 x 8).
@@ -120,9 +140,10 @@ __global__ void __launch_bounds__(kDT, 2) dense_hist_kernel(DenseArgs a) {
     const uint64_t lo = uint64_t(piece) * a.WP;
     const uint64_t hi = min_u64(a.n, lo + a.WP);
     uint32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const Xpose xp(lane);
     for (uint64_t t0 = lo; t0 < hi; t0 += 32) {
         uint32_t B0, B1, B2, B3;
-        score_tile(a, M, t0, hi, lane, B0, B1, B2, B3);
+        score_tile(a, M, t0, hi, lane, xp, B0, B1, B2, B3);
         // points past `hi` score 0: they never count for t >= 1
         const uint32_t g8 = B3, g4 = B3 | B2, g2 = g4 | B1, g1 = g2 | B0;
         const uint32_t g6 = B3 | (B2 & B1), g5 = B3 | (B2 & (B1 | B0)), g7 = B3 | (B2 & B1 & B0);
@@ -235,9 +256,10 @@ __global__ void __launch_bounds__(kDT, 2) dense_emit_kernel(DenseArgs a) {
     uint32_t pos = mine ? a.base[q * a.P + piece] : 0u;
     uint32_t* out = a.cands + (mine ? q : 0) * a.m;
     uint32_t tseen = 0;
+    const Xpose xp(lane);
     for (uint64_t t0 = lo; t0 < hi; t0 += 32) {
         uint32_t B0, B1, B2, B3;
-        score_tile(a, M, t0, hi, lane, B0, B1, B2, B3);
+        score_tile(a, M, t0, hi, lane, xp, B0, B1, B2, B3);
         if (!mine) continue;  // lanes past the block's last query only feed the transposes
         const uint32_t vmask = hi - t0 >= 32 ? kFull : ((1u << (hi - t0)) - 1u);
         const uint32_t geT = ge_mask(B0, B1, B2, B3, T) & vmask;
