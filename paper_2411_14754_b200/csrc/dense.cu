@@ -31,8 +31,8 @@
 namespace suco_gpu {
 namespace {
 
-constexpr uint32_t kDT = 512;        // threads per CTA (2 CTAs / SM)
-constexpr uint32_t kDW = kDT / 32;   // warps = pieces per CTA
+// CTA shapes: 512 threads x 2 CTAs/SM when the masks fit 110 KB, else one
+// 1024-thread CTA per SM (masks up to 200 KB); a warp = one piece either way.
 constexpr uint32_t kFull = 0xffffffffu;
 
 __device__ __forceinline__ void fadd(uint32_t a, uint32_t b, uint32_t c, uint32_t& s, uint32_t& cy) {
@@ -85,7 +85,9 @@ __device__ __forceinline__ uint32_t ge_mask(uint32_t B0, uint32_t B1, uint32_t B
 }
 
 // Masks of the CTA's query block: M[s*K + cell] bit j <=> query q0 + j retrieved (s, cell).
+template <uint32_t kDT>
 __device__ void build_masks(const DenseArgs& a, uint32_t* M, uint64_t q0, uint32_t nqb) {
+    constexpr uint32_t kDW = kDT / 32;
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t slots = a.ns * a.K + 1;
     for (uint32_t i = tid; i < slots; i += kDT) M[i] = 0;
@@ -129,12 +131,14 @@ __device__ __forceinline__ void score_tile(const DenseArgs& a, const uint32_t* M
 }
 
 // K1: per (query, piece) #points with score >= t, t = 1..8 (u16 x 8).
-__global__ void __launch_bounds__(kDT, 2) dense_hist_kernel(DenseArgs a) {
+template <uint32_t kDT>
+__global__ void __launch_bounds__(kDT, 1024 / kDT) dense_hist_kernel(DenseArgs a) {
+    constexpr uint32_t kDW = kDT / 32;
     extern __shared__ uint32_t M[];
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const uint64_t q0 = uint64_t(blockIdx.x) * 32;
     const uint32_t nqb = static_cast<uint32_t>(min_u64(32, a.nq - q0));
-    build_masks(a, M, q0, nqb);
+    build_masks<kDT>(a, M, q0, nqb);
     const uint32_t piece = blockIdx.y * kDW + warp;
     if (piece >= a.P) return;
     const uint64_t lo = uint64_t(piece) * a.WP;
@@ -239,12 +243,14 @@ __global__ void __launch_bounds__(256) dense_plan_kernel(DenseArgs a) {
 }
 
 // K3: re-score each piece; lane = query emits score > T and the first quota ties (id order).
-__global__ void __launch_bounds__(kDT, 2) dense_emit_kernel(DenseArgs a) {
+template <uint32_t kDT>
+__global__ void __launch_bounds__(kDT, 1024 / kDT) dense_emit_kernel(DenseArgs a) {
+    constexpr uint32_t kDW = kDT / 32;
     extern __shared__ uint32_t M[];
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const uint64_t q0 = uint64_t(blockIdx.x) * 32;
     const uint32_t nqb = static_cast<uint32_t>(min_u64(32, a.nq - q0));
-    build_masks(a, M, q0, nqb);
+    build_masks<kDT>(a, M, q0, nqb);
     const uint32_t piece = blockIdx.y * kDW + warp;
     if (piece >= a.P) return;
     const uint64_t lo = uint64_t(piece) * a.WP;
@@ -300,7 +306,7 @@ __global__ void dense_codes_kernel(const uint32_t* ids, const uint32_t* cell_off
 }  // namespace
 
 bool dense_supported(uint32_t ns, uint32_t K) {
-    return ns >= 1 && ns <= 8 && uint64_t(ns) * K + 1 <= 65535 && (uint64_t(ns) * K + 1) * 4 <= 110 * 1024;
+    return ns >= 1 && ns <= 8 && uint64_t(ns) * K + 1 <= 65535 && (uint64_t(ns) * K + 1) * 4 <= 200 * 1024;
 }
 
 size_t dense_smem(uint32_t ns, uint32_t K) { return (size_t(ns) * K + 1) * 4; }
@@ -315,18 +321,24 @@ cudaError_t launch_dense_codes(const uint32_t* ids, const uint32_t* cell_off, ui
     return cudaGetLastError();
 }
 
+template <uint32_t kDT>
+static cudaError_t launch_dense_t(const DenseArgs& a, size_t smem, cudaStream_t st) {
+    cudaError_t e = cudaFuncSetAttribute(dense_hist_kernel<kDT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(dense_emit_kernel<kDT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    constexpr uint32_t kDW = kDT / 32;
+    const dim3 grid(static_cast<unsigned>((a.nq + 31) / 32), (a.P + kDW - 1) / kDW);
+    dense_hist_kernel<kDT><<<grid, kDT, smem, st>>>(a);
+    dense_plan_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(a);
+    dense_emit_kernel<kDT><<<grid, kDT, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_dense_select(const DenseArgs& a, cudaStream_t st) {
     if (a.nq == 0) return cudaSuccess;
     const size_t smem = dense_smem(a.ns, a.K);
-    cudaError_t e = cudaFuncSetAttribute(dense_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(dense_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    const dim3 grid(static_cast<unsigned>((a.nq + 31) / 32), (a.P + kDW - 1) / kDW);
-    dense_hist_kernel<<<grid, kDT, smem, st>>>(a);
-    dense_plan_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(a);
-    dense_emit_kernel<<<grid, kDT, smem, st>>>(a);
-    return cudaGetLastError();
+    return smem <= 110 * 1024 ? launch_dense_t<512>(a, smem, st) : launch_dense_t<1024>(a, smem, st);
 }
 
 }  // namespace suco_gpu

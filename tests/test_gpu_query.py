@@ -173,6 +173,8 @@ CASES = {
     "ns16": (3000, 64, 10, 0, 100, 8, False, 16, 6, 3, 0, [(0.05, 0.01, 10), (0.1, 0.004, 12)]),
     "ns40": (1200, 80, 10, 0, 100, 8, True, 40, 3, 2, 0, [(0.05, 0.05, 10)]),
     "tiny_touch": (2500, 16, 8, 0, 50, 3, False, 2, 8, 3, 0, [(0.0005, 0.4, 10), (0.001, 1.0, 25)]),
+    # 64 x 64 cells: 128 KB of dense-select masks -> the 1024-thread, 1 CTA/SM variant
+    "dense_1024": (20000, 32, 40, 0, 100, 8, False, 8, 64, 2, 0, [(0.05, 0.005, 10), (0.02, 0.05, 40)]),
 }
 
 
