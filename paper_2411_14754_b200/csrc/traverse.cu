@@ -104,17 +104,17 @@ __device__ void da_warp(const double* d1r, const uint32_t* o1, const double* d2r
                 brow = lane + 32u * r;
             }
         }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            const double ob = __shfl_xor_sync(kFull, best, off);
-            const uint32_t orow = __shfl_xor_sync(kFull, brow, off);
-            if (ob < best || (ob == best && orow < brow)) {
-                best = ob;
-                brow = orow;
-            }
-        }
+        // warp argmin by (distance, row): distances are >= 0, so their IEEE bit patterns order like
+        // the values; three single-instruction reductions (high word, low word, row) replace a
+        // five-stage shuffle butterfly on doubles
+        const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(best));
+        const uint32_t hi = static_cast<uint32_t>(bits >> 32), lo = static_cast<uint32_t>(bits);
+        const uint32_t whi = __reduce_min_sync(kFull, hi);
+        const uint32_t wlo = __reduce_min_sync(kFull, hi == whi ? lo : 0xffffffffu);
+        const uint32_t pos = __reduce_min_sync(kFull, (hi == whi && lo == wlo) ? brow : 0xffffffffu);
+        best = __longlong_as_double(static_cast<long long>((static_cast<uint64_t>(whi) << 32) | wlo));
         if (best == kInf) break;  // unreachable while the IMI partitions all n points
-        const uint32_t pos = brow, owner = pos & 31u, slot = pos >> 5;
+        const uint32_t owner = pos & 31u, slot = pos >> 5;
         uint32_t jm = 0, sm = 0;
 #pragma unroll
         for (int r = 0; r < RPL; ++r) {
