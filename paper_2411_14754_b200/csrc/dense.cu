@@ -25,6 +25,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -84,90 +86,122 @@ __device__ __forceinline__ uint32_t ge_mask(uint32_t B0, uint32_t B1, uint32_t B
     return gt | eq;
 }
 
-// Masks of the CTA's query block: M[s*K + cell] bit j <=> query q0 + j retrieved (s, cell).
-template <uint32_t kDT>
+// Masks of the CTA's query block (32*W queries): W words per (subspace, cell)
+// slot; bit j of word w <=> query q0 + 32w + j retrieved (s, cell).
+template <uint32_t kDT, uint32_t W>
 __device__ void build_masks(const DenseArgs& a, uint32_t* M, uint64_t q0, uint32_t nqb) {
     constexpr uint32_t kDW = kDT / 32;
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    const uint32_t slots = a.ns * a.K + 1;
-    for (uint32_t i = tid; i < slots; i += kDT) M[i] = 0;
+    const uint32_t words = (a.ns * a.K + 1) * W;
+    for (uint32_t i = tid; i < words; i += kDT) M[i] = 0;
     __syncthreads();
     for (uint32_t j = warp; j < nqb; j += kDW) {
         const uint64_t q = q0 + j;
         for (uint32_t s = 0; s < a.ns; ++s) {
             const uint32_t cnt = a.ncells[q * a.ns + s];
             const uint32_t* cp = a.cells + (q * a.ns + s) * a.cells_cap;
-            for (uint32_t i = lane; i < cnt; i += 32) atomicOr(M + s * a.K + cp[i], 1u << j);
+            for (uint32_t i = lane; i < cnt; i += 32) atomicOr(M + (s * a.K + cp[i]) * W + (j >> 5), 1u << (j & 31u));
         }
     }
     __syncthreads();
 }
 
-// Scores of the 32 points [t0, t0 + 32) for the block's 32 queries; returns
-// with lane = query: planes B0..B3 (bit r = point t0 + r).
+template <uint32_t W>
+__device__ __forceinline__ void mask_at(const uint32_t* M, uint32_t slot, uint32_t (&m)[W]) {
+    if constexpr (W == 1) {
+        m[0] = M[slot];
+    } else {
+        const uint2 v = reinterpret_cast<const uint2*>(M)[slot];
+        m[0] = v.x;
+        m[1] = v.y;
+    }
+}
+
+// Scores of the 32 points [t0, t0 + 32) for the block's 32*W queries; returns
+// with lane = query (word w: query 32w + lane): planes B[w][0..3] (bit r = point t0 + r).
+template <uint32_t W>
 __device__ __forceinline__ void score_tile(const DenseArgs& a, const uint32_t* M, uint64_t t0, uint64_t p_hi,
-                                           uint32_t lane, const Xpose& xp, uint32_t& B0, uint32_t& B1, uint32_t& B2,
-                                           uint32_t& B3) {
+                                           const Xpose& xp, uint32_t (&B)[W][4], uint32_t lane) {
     const uint64_t p = t0 + lane;
     const uint32_t none = a.ns * a.K;
     uint4 c = make_uint4(none | (none << 16), none | (none << 16), none | (none << 16), none | (none << 16));
     if (p < p_hi) c = __ldg(a.codes + p);
-    const uint32_t m0 = M[c.x & 0xffffu], m1 = M[c.x >> 16];
-    const uint32_t m2 = M[c.y & 0xffffu], m3 = M[c.y >> 16];
-    const uint32_t m4 = M[c.z & 0xffffu], m5 = M[c.z >> 16];
-    const uint32_t m6 = M[c.w & 0xffffu], m7 = M[c.w >> 16];
-    uint32_t s1, c1, s2, c2, b0, c4, s5, c5;
-    fadd(m0, m1, m2, s1, c1);
-    fadd(m3, m4, m5, s2, c2);
-    const uint32_t s3 = m6 ^ m7, c3 = m6 & m7;
-    fadd(s1, s2, s3, b0, c4);  // weight 1
-    fadd(c1, c2, c3, s5, c5);  // weight 2 (+ carry weight 4)
-    const uint32_t b1 = s5 ^ c4, c6 = s5 & c4;
-    const uint32_t b2 = c5 ^ c6, b3 = c5 & c6;
-    B0 = xp(b0);
-    B1 = xp(b1);
-    B2 = xp(b2);
-    B3 = xp(b3);
+    uint32_t m[8][W];
+    mask_at<W>(M, c.x & 0xffffu, m[0]);
+    mask_at<W>(M, c.x >> 16, m[1]);
+    mask_at<W>(M, c.y & 0xffffu, m[2]);
+    mask_at<W>(M, c.y >> 16, m[3]);
+    mask_at<W>(M, c.z & 0xffffu, m[4]);
+    mask_at<W>(M, c.z >> 16, m[5]);
+    mask_at<W>(M, c.w & 0xffffu, m[6]);
+    mask_at<W>(M, c.w >> 16, m[7]);
+#pragma unroll
+    for (uint32_t w = 0; w < W; ++w) {
+        uint32_t s1, c1, s2, c2, b0, c4, s5, c5;
+        fadd(m[0][w], m[1][w], m[2][w], s1, c1);
+        fadd(m[3][w], m[4][w], m[5][w], s2, c2);
+        const uint32_t s3 = m[6][w] ^ m[7][w], c3 = m[6][w] & m[7][w];
+        fadd(s1, s2, s3, b0, c4);  // weight 1
+        fadd(c1, c2, c3, s5, c5);  // weight 2 (+ carry weight 4)
+        const uint32_t b1 = s5 ^ c4, c6 = s5 & c4;
+        const uint32_t b2 = c5 ^ c6, b3 = c5 & c6;
+        B[w][0] = xp(b0);
+        B[w][1] = xp(b1);
+        B[w][2] = xp(b2);
+        B[w][3] = xp(b3);
+    }
 }
 
 // K1: per (query, piece) #points with score >= t, t = 1..8 (u16 x 8).
-template <uint32_t kDT>
+template <uint32_t kDT, uint32_t W>
 __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_hist_kernel(DenseArgs a) {
     constexpr uint32_t kDW = kDT / 32;
     extern __shared__ uint32_t M[];
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    const uint64_t q0 = uint64_t(blockIdx.x) * 32;
-    const uint32_t nqb = static_cast<uint32_t>(min_u64(32, a.nq - q0));
-    build_masks<kDT>(a, M, q0, nqb);
+    const uint64_t q0 = uint64_t(blockIdx.x) * 32 * W;
+    const uint32_t nqb = static_cast<uint32_t>(min_u64(32 * W, a.nq - q0));
+    build_masks<kDT, W>(a, M, q0, nqb);
     const uint32_t piece = blockIdx.y * kDW + warp;
     if (piece >= a.P) return;
     const uint64_t lo = uint64_t(piece) * a.WP;
     const uint64_t hi = min_u64(a.n, lo + a.WP);
-    uint32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint32_t cnt[W][8];
+#pragma unroll
+    for (uint32_t w = 0; w < W; ++w) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) cnt[w][t] = 0;
+    }
     const Xpose xp(lane);
     for (uint64_t t0 = lo; t0 < hi; t0 += 32) {
-        uint32_t B0, B1, B2, B3;
-        score_tile(a, M, t0, hi, lane, xp, B0, B1, B2, B3);
+        uint32_t B[W][4];
+        score_tile<W>(a, M, t0, hi, xp, B, lane);
         // points past `hi` score 0: they never count for t >= 1
-        const uint32_t g8 = B3, g4 = B3 | B2, g2 = g4 | B1, g1 = g2 | B0;
-        const uint32_t g6 = B3 | (B2 & B1), g5 = B3 | (B2 & (B1 | B0)), g7 = B3 | (B2 & B1 & B0);
-        const uint32_t g3 = g4 | (B1 & B0);
-        cnt[0] += __popc(g1);
-        cnt[1] += __popc(g2);
-        cnt[2] += __popc(g3);
-        cnt[3] += __popc(g4);
-        cnt[4] += __popc(g5);
-        cnt[5] += __popc(g6);
-        cnt[6] += __popc(g7);
-        cnt[7] += __popc(g8);
+#pragma unroll
+        for (uint32_t w = 0; w < W; ++w) {
+            const uint32_t B0 = B[w][0], B1 = B[w][1], B2 = B[w][2], B3 = B[w][3];
+            const uint32_t g8 = B3, g4 = B3 | B2, g2 = g4 | B1, g1 = g2 | B0;
+            const uint32_t g6 = B3 | (B2 & B1), g5 = B3 | (B2 & (B1 | B0)), g7 = B3 | (B2 & B1 & B0);
+            const uint32_t g3 = g4 | (B1 & B0);
+            cnt[w][0] += __popc(g1);
+            cnt[w][1] += __popc(g2);
+            cnt[w][2] += __popc(g3);
+            cnt[w][3] += __popc(g4);
+            cnt[w][4] += __popc(g5);
+            cnt[w][5] += __popc(g6);
+            cnt[w][6] += __popc(g7);
+            cnt[w][7] += __popc(g8);
+        }
     }
-    if (lane < nqb) {
-        uint4 v;
-        v.x = cnt[0] | (cnt[1] << 16);
-        v.y = cnt[2] | (cnt[3] << 16);
-        v.z = cnt[4] | (cnt[5] << 16);
-        v.w = cnt[6] | (cnt[7] << 16);
-        reinterpret_cast<uint4*>(a.hist)[(q0 + lane) * a.P + piece] = v;
+#pragma unroll
+    for (uint32_t w = 0; w < W; ++w) {
+        if (32 * w + lane < nqb) {
+            uint4 v;
+            v.x = cnt[w][0] | (cnt[w][1] << 16);
+            v.y = cnt[w][2] | (cnt[w][3] << 16);
+            v.z = cnt[w][4] | (cnt[w][5] << 16);
+            v.w = cnt[w][6] | (cnt[w][7] << 16);
+            reinterpret_cast<uint4*>(a.hist)[(q0 + 32 * w + lane) * a.P + piece] = v;
+        }
     }
 }
 
@@ -243,46 +277,55 @@ __global__ void __launch_bounds__(256) dense_plan_kernel(DenseArgs a) {
 }
 
 // K3: re-score each piece; lane = query emits score > T and the first quota ties (id order).
-template <uint32_t kDT>
+template <uint32_t kDT, uint32_t W>
 __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_emit_kernel(DenseArgs a) {
     constexpr uint32_t kDW = kDT / 32;
     extern __shared__ uint32_t M[];
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    const uint64_t q0 = uint64_t(blockIdx.x) * 32;
-    const uint32_t nqb = static_cast<uint32_t>(min_u64(32, a.nq - q0));
-    build_masks<kDT>(a, M, q0, nqb);
+    const uint64_t q0 = uint64_t(blockIdx.x) * 32 * W;
+    const uint32_t nqb = static_cast<uint32_t>(min_u64(32 * W, a.nq - q0));
+    build_masks<kDT, W>(a, M, q0, nqb);
     const uint32_t piece = blockIdx.y * kDW + warp;
     if (piece >= a.P) return;
     const uint64_t lo = uint64_t(piece) * a.WP;
     const uint64_t hi = min_u64(a.n, lo + a.WP);
-    const uint64_t q = q0 + lane;
-    const bool mine = lane < nqb;
-    const uint32_t T = mine ? a.T[q] : 0u;
-    const uint32_t quota = mine ? a.quota[q * a.P + piece] : 0u;
-    uint32_t pos = mine ? a.base[q * a.P + piece] : 0u;
-    uint32_t* out = a.cands + (mine ? q : 0) * a.m;
-    uint32_t tseen = 0;
+    bool mine[W];
+    uint32_t T[W], quota[W], pos[W], tseen[W];
+    uint32_t* out[W];
+#pragma unroll
+    for (uint32_t w = 0; w < W; ++w) {
+        const uint64_t q = q0 + 32 * w + lane;
+        mine[w] = 32 * w + lane < nqb;
+        T[w] = mine[w] ? a.T[q] : 0u;
+        quota[w] = mine[w] ? a.quota[q * a.P + piece] : 0u;
+        pos[w] = mine[w] ? a.base[q * a.P + piece] : 0u;
+        tseen[w] = 0;
+        out[w] = a.cands + (mine[w] ? q : 0) * a.m;
+    }
     const Xpose xp(lane);
     for (uint64_t t0 = lo; t0 < hi; t0 += 32) {
-        uint32_t B0, B1, B2, B3;
-        score_tile(a, M, t0, hi, lane, xp, B0, B1, B2, B3);
-        if (!mine) continue;  // lanes past the block's last query only feed the transposes
+        uint32_t B[W][4];
+        score_tile<W>(a, M, t0, hi, xp, B, lane);
         const uint32_t vmask = hi - t0 >= 32 ? kFull : ((1u << (hi - t0)) - 1u);
-        const uint32_t geT = ge_mask(B0, B1, B2, B3, T) & vmask;
-        const uint32_t gt = ge_mask(B0, B1, B2, B3, T + 1) & vmask;
-        const uint32_t eq = geT & ~gt;
-        uint32_t take = gt;
-        if (eq && tseen < quota) {
-            const uint32_t r = quota - tseen;
-            uint32_t rest = eq;
-            for (uint32_t i = 0; i < r && rest; ++i) rest &= rest - 1;  // drop the first r ties
-            take |= eq ^ rest;
-        }
-        tseen += __popc(eq);
-        while (take) {
-            const uint32_t b = __ffs(take) - 1;
-            take &= take - 1;
-            __stcs(out + pos++, static_cast<uint32_t>(t0) + b);
+#pragma unroll
+        for (uint32_t w = 0; w < W; ++w) {
+            if (!mine[w]) continue;  // lanes past the block's last query only feed the transposes
+            const uint32_t geT = ge_mask(B[w][0], B[w][1], B[w][2], B[w][3], T[w]) & vmask;
+            const uint32_t gt = ge_mask(B[w][0], B[w][1], B[w][2], B[w][3], T[w] + 1) & vmask;
+            const uint32_t eq = geT & ~gt;
+            uint32_t take = gt;
+            if (eq && tseen[w] < quota[w]) {
+                const uint32_t r = quota[w] - tseen[w];
+                uint32_t rest = eq;
+                for (uint32_t i = 0; i < r && rest; ++i) rest &= rest - 1;  // drop the first r ties
+                take |= eq ^ rest;
+            }
+            tseen[w] += __popc(eq);
+            while (take) {
+                const uint32_t b = __ffs(take) - 1;
+                take &= take - 1;
+                __stcs(out[w] + pos[w]++, static_cast<uint32_t>(t0) + b);
+            }
         }
     }
 }
@@ -321,24 +364,29 @@ cudaError_t launch_dense_codes(const uint32_t* ids, const uint32_t* cell_off, ui
     return cudaGetLastError();
 }
 
-template <uint32_t kDT>
+template <uint32_t kDT, uint32_t W>
 static cudaError_t launch_dense_t(const DenseArgs& a, size_t smem, cudaStream_t st) {
-    cudaError_t e = cudaFuncSetAttribute(dense_hist_kernel<kDT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaError_t e = cudaFuncSetAttribute(dense_hist_kernel<kDT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(dense_emit_kernel<kDT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    e = cudaFuncSetAttribute(dense_emit_kernel<kDT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     constexpr uint32_t kDW = kDT / 32;
-    const dim3 grid(static_cast<unsigned>((a.nq + 31) / 32), (a.P + kDW - 1) / kDW);
-    dense_hist_kernel<kDT><<<grid, kDT, smem, st>>>(a);
+    const dim3 grid(static_cast<unsigned>((a.nq + 32 * W - 1) / (32 * W)), (a.P + kDW - 1) / kDW);
+    dense_hist_kernel<kDT, W><<<grid, kDT, smem, st>>>(a);
     dense_plan_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(a);
-    dense_emit_kernel<kDT><<<grid, kDT, smem, st>>>(a);
+    dense_emit_kernel<kDT, W><<<grid, kDT, smem, st>>>(a);
     return cudaGetLastError();
 }
 
+// 64-query blocks (two mask words per slot) when those masks fit 200 KB: each
+// random mask lookup then serves 64 queries; else 32-query blocks.
 cudaError_t launch_dense_select(const DenseArgs& a, cudaStream_t st) {
     if (a.nq == 0) return cudaSuccess;
-    const size_t smem = dense_smem(a.ns, a.K);
-    return smem <= 110 * 1024 ? launch_dense_t<512>(a, smem, st) : launch_dense_t<1024>(a, smem, st);
+    const size_t smem1 = dense_smem(a.ns, a.K);
+    const char* wv = std::getenv("SUCO_DENSE_WORDS");
+    const bool allow2 = !(wv && std::atoi(wv) == 1);
+    if (allow2 && 2 * smem1 <= 200 * 1024) return launch_dense_t<1024, 2>(a, 2 * smem1, st);
+    return smem1 <= 110 * 1024 ? launch_dense_t<512, 1>(a, smem1, st) : launch_dense_t<1024, 1>(a, smem1, st);
 }
 
 }  // namespace suco_gpu

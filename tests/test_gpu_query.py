@@ -296,3 +296,21 @@ def test_u8_rows_rerank_mixed_queries(gpu, oracle, d, shift):
         oi, od, _ = oidx.knn_query_batch(base, qs, a, b, k)
         assert np.array_equal(ids, oi), (d, shift, a, b, k)
         assert np.array_equal(dd, od), (d, shift, a, b, k)
+
+
+@pytest.mark.parametrize("words", ["1", "2"])
+def test_dense_select_block_widths(gpu, oracle, words, monkeypatch):
+    """32-query (one mask word) and 64-query (two words) dense blocks give the same candidate sets
+    and answers as the reference; a partial last block (nq % 64 != 0) included."""
+    monkeypatch.setenv("SUCO_DENSE_WORDS", words)
+    full = oracle.clustered(9000 + 77, 24, 30, 2024, 0, 100, 9, True)
+    base, qs = oracle.hold_out(full, 77, 2025)
+    oidx = oracle.build_index(base, 6, 20, 3, 42, 0)
+    idx = gpu.load_index(oidx.serialize(), base)
+    for a, b, k in ((0.05, 0.01, 10), (0.01, 0.2, 33)):
+        ids, dd = idx.knn_query_batch(qs, gpu.CollisionParams(a, b, k))
+        oi, od, _ = oidx.knn_query_batch(base, qs, a, b, k)
+        assert np.array_equal(ids, oi) and np.array_equal(dd, od), (words, a, b, k)
+    s1, c1, _, _ = idx.query_intermediates(qs[5], gpu.CollisionParams(0.05, 0.01, 10))
+    s2, c2, _, _ = oidx.query_intermediates(base, qs[5], 0.05, 0.01, 10)
+    assert np.array_equal(c1, c2)
