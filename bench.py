@@ -202,12 +202,16 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline query time (rank 0)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="no L2 flush/e2e/cpu legs (for ncu)")
+    ap.add_argument("--no-u8", action="store_true",
+                    help="re-rank from the f32 rows even for u8-valued data (the f32-row variant, SURVEY §8(d))")
     ap.add_argument("--sharded", action="store_true", help="use the multi-GPU shard protocol even at N = 1")
     ap.add_argument("--block", type=int, default=0,
                     help="block-cyclic shard block size (ids); 0 = suco_gpu_shard_block_hint (slabs == blocks)")
     ap.add_argument("--alpha", type=float, default=None, help="experiment: override the config's alpha")
     ap.add_argument("--beta", type=float, default=None, help="experiment: override the config's beta")
     args = ap.parse_args()
+    if args.no_u8:
+        os.environ["SUCO_NO_U8"] = "1"  # read by the library at index upload
     cfg = bench_data.CONFIGS[args.config]
     if args.alpha is not None or args.beta is not None:
         import dataclasses
@@ -345,14 +349,16 @@ def main():
     cum, sq, m = stats
     stage_avg = stage_ms / args.steps
     bytes_select = 4.0 * cum                      # u32 inverted-list ids streamed (query.cpp:235-239)
-    # candidate rows + query (query.cpp:177-182): 4-byte floats, or the byte rows the library keeps
-    # when the data and queries are integers in [0, 255] (exact integer re-rank)
+    # candidate rows + query (query.cpp:177-182), defined on the f32 API type; when
+    # the data and queries are integers in [0, 255] the library re-ranks from byte rows instead
+    # (exact) and moves `row_bytes` per row — reported beside, not substituted
     row_bytes = u8_row_bytes(base, queries) or 4 * d
-    bytes_rerank = float(row_bytes) * m * sq + 4.0 * d * sq
+    bytes_rerank = 4.0 * d * m * sq + 4.0 * d * sq
     names = ["traverse", "select", "rerank"]
     per_kernel = {}
     for i, (nm, b) in enumerate(zip(names, [None, bytes_select, bytes_rerank])):
-        per_kernel[nm] = {"ms": stage_avg[i], "algorithmic_bytes": b, **({"row_bytes": row_bytes} if nm == "rerank" else {}),
+        per_kernel[nm] = {"ms": stage_avg[i], "algorithmic_bytes": b,
+                          **({"row_bytes_moved": row_bytes, "row_bytes_f32": 4 * d} if nm == "rerank" else {}),
                           "achieved_gbs": (b / (stage_avg[i] / 1000.0) / 1e9) if b else None}
     dom = int(np.argmax(stage_avg))
     dom_name = names[dom]
@@ -399,7 +405,7 @@ def main():
         except Exception as e:  # the baseline must not mask the GPU number
             cpu = {"error": repr(e)}
 
-    launches_per_step = 3 + (1 if k > 32 else 0)
+    launches_per_step = idx.last_launches()  # counted by the library for the last call
     line = {
         "metric": "batched queries/sec at k=10 (oracle-exact IDs)", "value": value, "unit": "queries/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
@@ -407,6 +413,7 @@ def main():
         "data": "synthetic (seeded Gaussian mixture, bench_data.py; stands in for SIFT1M-shape corpus)",
         "config": {"workload": cfg.describe(), "queries_per_step": nq, "index_build_s": build_s,
                    "index_source": args.index_source, "l2": "256 MiB flush write between timed steps",
+                   "rerank_rows": "u8" if row_bytes != 4 * d else "f32",
                    "parallelism": f"replicas x{ws}"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "parity": parity,
         "gpu_launches": launches_per_step * args.steps, "clocks": clocks.summary(),

@@ -130,6 +130,9 @@ int suco_gpu_synchronize(suco_gpu_index* index);
  * over queries and subspaces of the retrieved ids (the final cumulative of
  * every traversal, query.cpp:105-106), stats[1] = queries, stats[2] = m. */
 int suco_gpu_set_profiling(suco_gpu_index* index, int enabled);
+/* Number of CUDA kernels the last query call on this index enqueued (all of
+ * them this library's own sm_100a kernels). */
+int suco_gpu_last_launches(const suco_gpu_index* index, uint64_t* launches);
 int suco_gpu_stage_times(suco_gpu_index* index, double* ms /*3*/, uint64_t* stats /*3*/);
 
 /* Per-query intermediates of knn_query for parity checks: SC-scores (n u32,

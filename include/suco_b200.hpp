@@ -21,7 +21,7 @@
 // exchange between shards lives in paper_2411_14754_b200.sharded).
 // Also wrapped: suco_last_error, suco_gpu_device_count, suco_gpu_index_info,
 // suco_gpu_index_subspace, suco_gpu_free_index, suco_gpu_set_stream,
-// suco_gpu_synchronize, suco_gpu_query_intermediates.
+// suco_gpu_synchronize, suco_gpu_query_intermediates, suco_gpu_last_launches.
 #pragma once
 
 #include <cstdint>

@@ -277,6 +277,12 @@ class GpuIndex:
         _check(_c.stage_times(self._h, _p(ms, _c.f64p), _p(st, _c.u64p)))
         return ms, int(st[0]), int(st[1]), int(st[2])
 
+    def last_launches(self) -> int:
+        """Kernels (all this library's) the last query call enqueued (suco_gpu_last_launches)."""
+        n = C.c_uint64()
+        _check(_c.last_launches(self._h, C.byref(n)))
+        return n.value
+
     def query_intermediates(self, query, params: CollisionParams):
         """(scores n, candidates ascending, cells per subspace, cumulative per subspace) of one query."""
         q = _f32(query).ravel()

@@ -140,6 +140,7 @@ struct suco_gpu_index {
     uint32_t pairs = 0;
     DevBuf<unsigned long long> stat_cum;
     uint64_t last_nq = 0, last_m = 0;
+    uint64_t launches = 0;  // kernels enqueued by the last query call (suco_gpu_last_launches)
 
     ~suco_gpu_index() {
         for (cudaEvent_t e : events) cudaEventDestroy(e);
@@ -365,6 +366,7 @@ uint64_t tile_size(const suco_gpu_index* x, uint64_t nq, uint64_t m, uint32_t k)
 // Resets the per-call profiling state (events + work counters).
 void begin_call(suco_gpu_index* x, uint64_t nq, uint64_t m, cudaStream_t st) {
     x->pairs = 0;
+    x->launches = 0;
     x->last_nq = nq;
     x->last_m = m;
     if (x->profile) {
@@ -413,6 +415,7 @@ void stage_traverse(suco_gpu_index* x, suco_gpu_index::Slot& sl, const float* d_
     ta.stat_cum = ev ? x->stat_cum.p : nullptr;
     if (ev) CUDA_TRY(cudaEventRecord(ev[0], st));
     CUDA_TRY(launch_traverse(ta, st));
+    x->launches += 1;
     if (ev) CUDA_TRY(cudaEventRecord(ev[1], st));
 }
 
@@ -445,6 +448,7 @@ void stage_select(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nt, uint
         da.cands = sl.cands.p;
         if (ev) CUDA_TRY(cudaEventRecord(ev[0], st));
         CUDA_TRY(launch_dense_select(da, st));
+        x->launches += 3;  // piece histograms, plan, emission
         if (ev) CUDA_TRY(cudaEventRecord(ev[1], st));
         return;
     }
@@ -467,6 +471,7 @@ void stage_select(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nt, uint
     sa.scores_dbg = dbg ? dbg->scores : nullptr;
     if (ev) CUDA_TRY(cudaEventRecord(ev[0], st));
     CUDA_TRY(launch_select(sa, x->sel, nt, st));
+    x->launches += 1;
     if (ev) CUDA_TRY(cudaEventRecord(ev[1], st));
 }
 
@@ -495,6 +500,7 @@ void stage_rerank(suco_gpu_index* x, suco_gpu_index::Slot& sl, const float* d_q,
     }
     if (ev) CUDA_TRY(cudaEventRecord(ev[0], st));
     CUDA_TRY(launch_rerank(ra, nt, st));
+    x->launches += (ra.data8 ? 2 : 1) + (k > 32 ? 1 : 0);  // u8 + fp32/fp64 kernels, generic top-k
     if (ev) CUDA_TRY(cudaEventRecord(ev[1], st));
 }
 
@@ -768,6 +774,13 @@ int suco_gpu_set_profiling(suco_gpu_index* x, int enabled) {
         DeviceGuard g(x->device);
         x->profile = enabled != 0;
         if (x->profile) x->stat_cum.reserve(1);
+    });
+}
+
+int suco_gpu_last_launches(const suco_gpu_index* x, uint64_t* launches) {
+    return guarded([&] {
+        if (!x || !launches) raise(SUCO_ERR_CONTRACT, "null argument");
+        *launches = x->launches;
     });
 }
 
