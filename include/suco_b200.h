@@ -171,10 +171,17 @@ int suco_gpu_make_shard(const suco_gpu_index* full, uint32_t shard, uint32_t num
 int suco_gpu_shard_block_hint(const suco_gpu_index* full, uint32_t num_shards, uint32_t* block);
 int suco_gpu_shard_info(const suco_gpu_index* index, uint64_t* n_global, uint64_t* n_local, uint32_t* nblocks_local,
                         uint32_t* block, uint32_t* shard, uint32_t* num_shards);
-/* d_queries nq x qlen, d_hist nq x nblocks_local x (N_s + 2) u32 (device). */
+/* Histogram rows: shard_info's nblocks_local counts the id-contiguous PIECES a
+ * shard reports per query — whole blocks, or (dense select, blocks a multiple
+ * of 2048 ids) 2048-id pieces, pieces_per_block of them per block, so local
+ * piece p sits in global order at ((p / ppb) * num_shards + shard) * ppb + p % ppb. */
+int suco_gpu_shard_pieces(const suco_gpu_index* shard, uint32_t* pieces_per_block);
+/* d_queries nq x qlen, d_hist nq x nblocks_local x (N_s + 2) u32 (device): per piece
+ * [length, #score >= 1, ..., #score >= N_s, 0]. */
 int suco_gpu_shard_histograms(suco_gpu_index* shard, const float* d_queries, uint64_t nq, uint32_t qlen,
                               const suco_collision_params* params, uint32_t* d_hist, void* stream);
-/* d_T nq, d_quota / d_base nq x nblocks_local, d_counts nq (all device, u32);
+/* Must follow suco_gpu_shard_histograms of the same queries on the same shard.
+ * d_T nq, d_quota / d_base nq x nblocks_local, d_counts nq (all device, u32);
  * candidate rows of `stride` entries; d_ids nq x k, d_sqdists nq x k. */
 int suco_gpu_shard_topk(suco_gpu_index* shard, const float* d_queries, uint64_t nq, uint32_t qlen,
                         const suco_collision_params* params, const uint32_t* d_T, const uint32_t* d_quota,

@@ -76,6 +76,7 @@ query_intermediates = _sig("suco_gpu_query_intermediates", C.c_int, vp, f32p, C.
                            C.POINTER(CollisionParamsC), u32p, u32p, u64p, u32p, u64p)
 make_shard = _sig("suco_gpu_make_shard", C.c_int, vp, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(vp))
 shard_block_hint = _sig("suco_gpu_shard_block_hint", C.c_int, vp, C.c_uint32, u32p)
+shard_pieces = _sig("suco_gpu_shard_pieces", C.c_int, vp, u32p)
 shard_info = _sig("suco_gpu_shard_info", C.c_int, vp, u64p, u64p, u32p, u32p, u32p, u32p)
 shard_histograms = _sig("suco_gpu_shard_histograms", C.c_int, vp, vp, C.c_uint64, C.c_uint32,
                         C.POINTER(CollisionParamsC), vp, vp)
@@ -98,6 +99,6 @@ EXPORTED = [
     "suco_gpu_stage_times", "suco_gpu_last_launches",
     "suco_gpu_query_intermediates", "suco_gpu_centroid_distances", "suco_gpu_dynamic_activation", "suco_gpu_rerank",
     "suco_gpu_kmeans", "suco_gpu_build_imi", "suco_gpu_make_shard", "suco_gpu_shard_block_hint",
-    "suco_gpu_shard_info", "suco_gpu_shard_histograms",
+    "suco_gpu_shard_info", "suco_gpu_shard_pieces", "suco_gpu_shard_histograms",
     "suco_gpu_shard_topk",
 ]

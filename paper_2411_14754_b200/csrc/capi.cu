@@ -113,6 +113,7 @@ struct suco_gpu_index {
     DevBuf<uint8_t> data8;      // u8 copy of the rows when they are integers in [0, 255] (rerank u8 path)
     DevBuf<uint16_t> codes;     // n x 8: s*K + cell of every point (dense select, N_s <= 8)
     bool dense = false;         // select stage = dense bit-sliced 32-query blocks (dense.cu)
+    uint64_t phase1_nq = 0;     // shard: queries of the last dense phase 1 (phase 2 re-scores them)
     uint32_t dpad = 0;          // row bytes of data8 (0: no u8 copy)
     // block-cyclic shard (suco_gpu_make_shard): global blocks j with j % num_shards == shard
     uint32_t shard = 0, num_shards = 1, block = 0;
@@ -435,7 +436,7 @@ void stage_select(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nt, uint
         da.n = h.n;
         da.nq = nt;
         da.m = m;
-        da.WP = 2048;
+        da.WP = kDensePiece;
         da.P = static_cast<uint32_t>((h.n + da.WP - 1) / da.WP);
         sl.dhist.reserve(nt * da.P * 8);
         sl.dT.reserve(nt);
@@ -964,6 +965,13 @@ int suco_gpu_make_shard(const suco_gpu_index* full, uint32_t shard, uint32_t num
             x->ids.reserve(ns * n_local);
             CUDA_TRY(launch_shard_imi(full->ids.p, full->cell_off.p, n, ns, x->K, block, num_shards, shard, nullptr,
                                       x->cell_off.p, n_local, x->ids.p, x->stream));
+            // dense select when the blocks are whole pieces (pieces never straddle blocks)
+            const char* dv = std::getenv("SUCO_DENSE");
+            x->dense = dense_supported(ns, x->K) && block % kDensePiece == 0 && !(dv && std::atoi(dv) == 0);
+            if (x->dense) {
+                x->codes.reserve(n_local * 8);
+                CUDA_TRY(launch_dense_codes(x->ids.p, x->cell_off.p, n_local, ns, x->K, x->codes.p, x->stream));
+            }
             x->sel = SelectConfig{};
             if (block % select_slab_align() == 0) x->sel = plan_select_fixed(n_local, ns, block);
             x->slab_is_block = x->sel.CH != 0;  // slab histograms are the block histograms
@@ -1003,11 +1011,36 @@ int suco_gpu_shard_info(const suco_gpu_index* x, uint64_t* n_global, uint64_t* n
         const uint32_t b = x->block ? x->block : static_cast<uint32_t>(std::min<uint64_t>(x->host.n, 0xFFFFFFFFull));
         if (n_global) *n_global = x->n_global;
         if (n_local) *n_local = x->host.n;
-        if (nblocks_local) *nblocks_local = static_cast<uint32_t>((x->host.n + b - 1) / b);
+        // histogram rows per query: dense pieces of kDensePiece ids, else whole blocks
+        const uint32_t unit = x->dense ? kDensePiece : b;
+        if (nblocks_local) *nblocks_local = static_cast<uint32_t>((x->host.n + unit - 1) / unit);
         if (block) *block = b;
         if (shard) *shard = x->shard;
         if (num_shards) *num_shards = x->num_shards;
     });
+}
+
+int suco_gpu_shard_pieces(const suco_gpu_index* x, uint32_t* pieces_per_block) {
+    return guarded([&] {
+        if (!x || !pieces_per_block) raise(SUCO_ERR_CONTRACT, "null argument");
+        const uint32_t b = x->block ? x->block : static_cast<uint32_t>(std::min<uint64_t>(x->host.n, 0xFFFFFFFFull));
+        *pieces_per_block = x->dense ? b / kDensePiece : 1u;
+    });
+}
+
+DenseArgs shard_dense_args(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nq) {
+    DenseArgs da{};
+    da.codes = reinterpret_cast<const uint4*>(x->codes.p);
+    da.cells = sl.cells.p;
+    da.ncells = sl.ncells.p;
+    da.cells_cap = x->K;
+    da.ns = x->host.layout.ns;
+    da.K = x->K;
+    da.n = x->host.n;
+    da.nq = nq;
+    da.WP = kDensePiece;
+    da.P = static_cast<uint32_t>((x->host.n + kDensePiece - 1) / kDensePiece);
+    return da;
 }
 
 int suco_gpu_shard_histograms(suco_gpu_index* x, const float* d_queries, uint64_t nq, uint32_t qlen,
@@ -1027,6 +1060,16 @@ int suco_gpu_shard_histograms(suco_gpu_index* x, const float* d_queries, uint64_
         const uint32_t b = x->block ? x->block : static_cast<uint32_t>(nl);
         const uint32_t nblocks = static_cast<uint32_t>((nl + b - 1) / b);
         auto& sl = x->slot[0];
+        if (x->dense) {  // traverse + dense piece histograms (dense.cu K1), in the exchange format
+            stage_traverse(x, sl, d_queries, nq, suco_collision_count(p->alpha, x->n_global), st, nullptr);
+            DenseArgs da = shard_dense_args(x, sl, nq);
+            sl.dhist.reserve(nq * da.P * 8);
+            da.hist = sl.dhist.p;
+            CUDA_TRY(launch_dense_hist(da, st));
+            CUDA_TRY(launch_dense_hist_rows(da, d_hist, st));
+            x->phase1_nq = nq;
+            return;
+        }
         const uint64_t ss = (nl + 15) / 16 * 16;  // 16-byte score rows
         x->shard_scores.reserve(nq * ss);
         stage_traverse(x, sl, d_queries, nq, suco_collision_count(p->alpha, x->n_global), st, nullptr);
@@ -1070,7 +1113,9 @@ int suco_gpu_shard_topk(suco_gpu_index* x, const float* d_queries, uint64_t nq, 
         validate_params(p, x->n_global);
         if (nq == 0) return;
         const uint64_t ss = (x->host.n + 15) / 16 * 16;
-        if (x->shard_scores.cap < nq * ss) raise(SUCO_ERR_CONTRACT, "suco_gpu_shard_topk needs phase 1 first");
+        if (x->dense ? x->phase1_nq != nq : x->shard_scores.cap < nq * ss) {
+            raise(SUCO_ERR_CONTRACT, "suco_gpu_shard_topk needs phase 1 (suco_gpu_shard_histograms) of the same queries");
+        }
         DeviceGuard g(x->device);
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : x->stream;
         const uint64_t nl = x->host.n;
@@ -1078,8 +1123,18 @@ int suco_gpu_shard_topk(suco_gpu_index* x, const float* d_queries, uint64_t nq, 
         const uint32_t nblocks = static_cast<uint32_t>((nl + b - 1) / b);
         const uint64_t sd = std::max<uint64_t>(stride, 1);
         x->shard_cands.reserve(nq * sd);
-        CUDA_TRY(launch_shard_emit(x->shard_scores.p, nq, nl, ss, b, nblocks, x->shard, x->num_shards, d_T, d_quota, d_base,
-                                   x->shard_cands.p, sd, st));
+        if (x->dense) {  // re-score each piece against the traversal of phase 1 (dense.cu K3)
+            DenseArgs da = shard_dense_args(x, x->slot[0], nq);
+            da.m = sd;
+            da.T = const_cast<uint32_t*>(d_T);
+            da.quota = const_cast<uint32_t*>(d_quota);
+            da.base = const_cast<uint32_t*>(d_base);
+            da.cands = x->shard_cands.p;
+            CUDA_TRY(launch_dense_emit(da, st));
+        } else {
+            CUDA_TRY(launch_shard_emit(x->shard_scores.p, nq, nl, ss, b, nblocks, x->shard, x->num_shards, d_T, d_quota,
+                                       d_base, x->shard_cands.p, sd, st));
+        }
         RerankArgs ra{};
         ra.data = x->data.p;
         ra.n = nl;

@@ -364,29 +364,68 @@ cudaError_t launch_dense_codes(const uint32_t* ids, const uint32_t* cell_off, ui
     return cudaGetLastError();
 }
 
-template <uint32_t kDT, uint32_t W>
-static cudaError_t launch_dense_t(const DenseArgs& a, size_t smem, cudaStream_t st) {
-    cudaError_t e = cudaFuncSetAttribute(dense_hist_kernel<kDT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(dense_emit_kernel<kDT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    constexpr uint32_t kDW = kDT / 32;
-    const dim3 grid(static_cast<unsigned>((a.nq + 32 * W - 1) / (32 * W)), (a.P + kDW - 1) / kDW);
-    dense_hist_kernel<kDT, W><<<grid, kDT, smem, st>>>(a);
-    dense_plan_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(a);
-    dense_emit_kernel<kDT, W><<<grid, kDT, smem, st>>>(a);
-    return cudaGetLastError();
-}
-
 // 64-query blocks (two mask words per slot) when those masks fit 200 KB: each
 // random mask lookup then serves 64 queries; else 32-query blocks.
-cudaError_t launch_dense_select(const DenseArgs& a, cudaStream_t st) {
-    if (a.nq == 0) return cudaSuccess;
+struct Shape {
+    uint32_t threads, words;
+    size_t smem;
+};
+static Shape dense_shape(const DenseArgs& a) {
     const size_t smem1 = dense_smem(a.ns, a.K);
     const char* wv = std::getenv("SUCO_DENSE_WORDS");
     const bool allow2 = !(wv && std::atoi(wv) == 1);
-    if (allow2 && 2 * smem1 <= 200 * 1024) return launch_dense_t<1024, 2>(a, 2 * smem1, st);
-    return smem1 <= 110 * 1024 ? launch_dense_t<512, 1>(a, smem1, st) : launch_dense_t<1024, 1>(a, smem1, st);
+    if (allow2 && 2 * smem1 <= 200 * 1024) return {1024, 2, 2 * smem1};
+    return {smem1 <= 110 * 1024 ? 512u : 1024u, 1, smem1};
+}
+
+template <uint32_t kDT, uint32_t W, bool EMIT>
+static cudaError_t launch_scan(const DenseArgs& a, size_t smem, cudaStream_t st) {
+    auto kern = EMIT ? dense_emit_kernel<kDT, W> : dense_hist_kernel<kDT, W>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    constexpr uint32_t kDW = kDT / 32;
+    const dim3 grid(static_cast<unsigned>((a.nq + 32 * W - 1) / (32 * W)), (a.P + kDW - 1) / kDW);
+    kern<<<grid, kDT, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <bool EMIT>
+static cudaError_t launch_scan_any(const DenseArgs& a, cudaStream_t st) {
+    if (a.nq == 0) return cudaSuccess;
+    const Shape sh = dense_shape(a);
+    if (sh.words == 2) return launch_scan<1024, 2, EMIT>(a, sh.smem, st);
+    return sh.threads == 512 ? launch_scan<512, 1, EMIT>(a, sh.smem, st) : launch_scan<1024, 1, EMIT>(a, sh.smem, st);
+}
+
+__global__ void dense_rows_kernel(DenseArgs a, uint32_t* out) {  // u16 x 8 -> [len, #>=1..#>=ns, 0] u32
+    const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (i >= a.nq * a.P) return;
+    const uint32_t p = static_cast<uint32_t>(i % a.P);
+    const uint4 v = reinterpret_cast<const uint4*>(a.hist)[i];
+    uint32_t* o = out + i * (a.ns + 2);
+    o[0] = static_cast<uint32_t>(min_u64(a.WP, a.n - uint64_t(p) * a.WP));
+    for (uint32_t t = 1; t <= a.ns; ++t) o[t] = level(v, t);
+    o[a.ns + 1] = 0;
+}
+
+cudaError_t launch_dense_hist(const DenseArgs& a, cudaStream_t st) { return launch_scan_any<false>(a, st); }
+cudaError_t launch_dense_emit(const DenseArgs& a, cudaStream_t st) { return launch_scan_any<true>(a, st); }
+
+cudaError_t launch_dense_hist_rows(const DenseArgs& a, uint32_t* out, cudaStream_t st) {
+    const uint64_t total = a.nq * a.P;
+    if (total == 0) return cudaSuccess;
+    dense_rows_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(a, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dense_select(const DenseArgs& a, cudaStream_t st) {
+    if (a.nq == 0) return cudaSuccess;
+    cudaError_t e = launch_dense_hist(a, st);
+    if (e != cudaSuccess) return e;
+    dense_plan_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(a);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return launch_dense_emit(a, st);
 }
 
 }  // namespace suco_gpu

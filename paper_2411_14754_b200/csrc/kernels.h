@@ -98,7 +98,13 @@ bool dense_supported(uint32_t ns, uint32_t K);
 size_t dense_smem(uint32_t ns, uint32_t K);
 cudaError_t launch_dense_codes(const uint32_t* ids, const uint32_t* cell_off, uint64_t n, uint32_t ns, uint32_t K,
                                uint16_t* codes, cudaStream_t st);
-cudaError_t launch_dense_select(const DenseArgs& a, cudaStream_t st);
+cudaError_t launch_dense_select(const DenseArgs& a, cudaStream_t st);  // hist + plan + emit
+// Shard protocol pieces: K1 alone (+ its histograms as [nq][P][N_s + 2] u32 rows with the
+// piece length first, the exchange format) and K3 alone with the globally planned T/quota/base.
+cudaError_t launch_dense_hist(const DenseArgs& a, cudaStream_t st);
+cudaError_t launch_dense_hist_rows(const DenseArgs& a, uint32_t* out, cudaStream_t st);
+cudaError_t launch_dense_emit(const DenseArgs& a, cudaStream_t st);
+constexpr uint32_t kDensePiece = 2048;  // points per piece (one warp)
 
 // ------------------------------------------------------------------ rerank
 // Exact fp64 re-rank of the candidate rows (query.cpp:159-197) with a

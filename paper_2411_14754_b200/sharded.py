@@ -54,8 +54,16 @@ def global_threshold(total_ge: torch.Tensor, m: int) -> Tuple[torch.Tensor, torc
     return T, m - gt_total
 
 
-def plan_for_shard(hists: Sequence[torch.Tensor], shard: int, m: int) -> Plan:
-    """hists[r] = shard r's [nq, nb_r, ns+2] block histograms (all shards' copies)."""
+def piece_order(np_local: int, G: int, r: int, ppb: int, device) -> torch.Tensor:
+    """Global position of each of shard r's pieces: local piece p is sub-piece p % ppb of local
+    block p // ppb, i.e. of global block (p // ppb) * G + r."""
+    p = torch.arange(np_local, device=device)
+    return ((p // ppb) * G + r) * ppb + p % ppb
+
+
+def plan_for_shard(hists: Sequence[torch.Tensor], shard: int, m: int, ppb: int = 1) -> Plan:
+    """hists[r] = shard r's [nq, pieces_r, ns+2] piece histograms (all shards' copies); ppb =
+    pieces per block (1: the pieces are the blocks)."""
     G = len(hists)
     nq = hists[0].shape[0]
     h64 = [h.to(torch.int64) for h in hists]
@@ -68,15 +76,15 @@ def plan_for_shard(hists: Sequence[torch.Tensor], shard: int, m: int) -> Plan:
         above = h.gather(2, (Tidx + 1).expand(nq, h.shape[1], 1)).squeeze(2)
         ties.append(at_T - above)
         gts.append(above)
-    # global block order: global block j = local block j // G of shard j % G
-    nb_max = max(t.shape[1] for t in ties)
-    glob = torch.zeros((nq, nb_max * G), dtype=torch.int64, device=T.device)
-    for r, t in enumerate(ties):
-        glob[:, r: r + G * t.shape[1]: G] = t
+    # pieces laid out in global id order
+    orders = [piece_order(t.shape[1], G, r, ppb, T.device) for r, t in enumerate(ties)]
+    width = int(max(int(o.max()) + 1 if o.numel() else 0 for o in orders))
+    glob = torch.zeros((nq, max(width, 1)), dtype=torch.int64, device=T.device)
+    for o, t in zip(orders, ties):
+        glob[:, o] = t
     before = torch.cumsum(glob, dim=1) - glob
     quota_glob = torch.clamp(torch.minimum(glob, need.unsqueeze(1) - before), min=0)
-    nb = ties[shard].shape[1]
-    quota = quota_glob[:, shard: shard + G * nb: G]
+    quota = quota_glob[:, orders[shard]]
     take = gts[shard] + quota
     base = torch.cumsum(take, dim=1) - take
     counts = take.sum(dim=1)
@@ -136,6 +144,9 @@ class GpuShard:
         self.block, self.shard, self.num_shards = b.value, s.value, G.value
         self.ns = full.params.num_subspaces
         self.d = full.d
+        ppb = C.c_uint32()
+        _check(_c.shard_pieces(h, C.byref(ppb)))
+        self.ppb = ppb.value  # histogram pieces per block (dense select: 2048-id pieces)
 
     def histograms(self, q: torch.Tensor, params: CollisionParams, stream: Optional[int] = None) -> torch.Tensor:
         stream = stream or _torch_stream(q.device)  # ordered with the plan math
@@ -188,7 +199,7 @@ def knn_query_distributed(engine, comm: TorchComm, queries: torch.Tensor, params
     m = candidate_count(params.beta, engine.n_global, params.k)
     hist = engine.histograms(queries, params)
     hists = comm.allgather_var(hist)
-    plan = plan_for_shard(hists, comm.rank, m)
+    plan = plan_for_shard(hists, comm.rank, m, getattr(engine, "ppb", 1))
     ids, sq = engine.topk(queries, params, plan)
     all_ids = comm.allgather_var(ids)
     all_sq = comm.allgather_var(sq)
@@ -199,5 +210,5 @@ def emulate(engines: Sequence, queries: torch.Tensor, params: CollisionParams):
     """Run the protocol for G shard engines in one process (single-GPU CI of the multi-GPU path)."""
     m = candidate_count(params.beta, engines[0].n_global, params.k)
     hists = [e.histograms(queries, params) for e in engines]
-    tops = [e.topk(queries, params, plan_for_shard(hists, r, m)) for r, e in enumerate(engines)]
+    tops = [e.topk(queries, params, plan_for_shard(hists, r, m, getattr(e, "ppb", 1))) for r, e in enumerate(engines)]
     return merge_topk([t[0] for t in tops], [t[1] for t in tops], int(params.k))

@@ -15,36 +15,47 @@ def _corpus(oracle, n=1500, d=16, seed=5):
     return oracle.hold_out(full, 12, seed + 1)
 
 
-def test_plan_matches_reference_selection_rule():
-    """T and id-ordered quotas from per-block histograms == top-m by (score desc, id asc)."""
+@pytest.mark.parametrize("ppb", [1, 3])
+def test_plan_matches_reference_selection_rule(ppb):
+    """T and id-ordered quotas from per-piece histograms == top-m by (score desc, id asc); pieces
+    are whole blocks (ppb = 1) or ppb consecutive sub-pieces of each block (dense select)."""
     from paper_2411_14754_b200.sharded import plan_for_shard
-    rng = np.random.default_rng(0)
-    ns, n, b, G, m = 6, 997, 37, 3, 61
+    rng = np.random.default_rng(ppb)
+    ns, n, ps, G, m = 6, 997, 13, 3, 61
+    b = ps * ppb
     for _ in range(20):
         scores = rng.integers(0, ns + 1, size=n)
         order = sorted(range(n), key=lambda i: (-scores[i], i))
         want = set(order[:m])
         nb = -(-n // b)
+
+        def pieces_of(r):  # (global start, end) of shard r's pieces in local order
+            out = []
+            for j in (j for j in range(nb) if j % G == r):
+                for sub in range(ppb):
+                    lo = j * b + sub * ps
+                    if lo < n:
+                        out.append((lo, min(n, lo + ps, (j + 1) * b)))
+            return out
         hists = []
         for r in range(G):
-            blocks = [j for j in range(nb) if j % G == r]
-            h = np.zeros((1, len(blocks), ns + 2), np.int32)
-            for bi, j in enumerate(blocks):
-                s = scores[j * b: min(n, (j + 1) * b)]
+            pcs = pieces_of(r)
+            h = np.zeros((1, len(pcs), ns + 2), np.int32)
+            for pi, (lo, hi) in enumerate(pcs):
                 for t in range(ns + 1):
-                    h[0, bi, t] = (s >= t).sum()
+                    h[0, pi, t] = (scores[lo:hi] >= t).sum()
             hists.append(torch.from_numpy(h))
         got = set()
         for r in range(G):
-            plan = plan_for_shard(hists, r, m)
+            plan = plan_for_shard(hists, r, m, ppb)
             T = int(plan.T[0])
-            blocks = [j for j in range(nb) if j % G == r]
-            for bi, j in enumerate(blocks):
-                lo = j * b
-                s = scores[lo: min(n, lo + b)]
-                got |= set((np.nonzero(s > T)[0] + lo).tolist())
-                got |= set((np.nonzero(s == T)[0] + lo)[: int(plan.quota[0, bi])].tolist())
-            assert int(plan.counts[0]) == sum(1 for i in got if (i // b) % G == r)
+            mine = set()
+            for pi, (lo, hi) in enumerate(pieces_of(r)):
+                s = scores[lo:hi]
+                mine |= set((np.nonzero(s > T)[0] + lo).tolist())
+                mine |= set((np.nonzero(s == T)[0] + lo)[: int(plan.quota[0, pi])].tolist())
+            assert int(plan.counts[0]) == len(mine)
+            got |= mine
         assert got == want
 
 
