@@ -344,6 +344,18 @@ def main():
                "ms_per_step": tot / args.steps}
         assert np.array_equal(hi.numpy().view(np.uint32), gpu_ids) and np.array_equal(hd.numpy(), gpu_d)
 
+    # answer quality against the GPU exact kNN, on a query sample
+    quality = None
+    if not args.profile_only and rank == 0:
+        sample = min(nq, 1000)
+        t0 = time.time()
+        ti, td = idx.exact_knn_batch(queries[:sample], k)
+        gt_s = time.time() - t0
+        rec = [suco.recall(gpu_ids[i], ti[i], k) for i in range(sample)]
+        err = [suco.mre(gpu_d[i], td[i], k) for i in range(sample)]
+        quality = {"queries": sample, "recall_at_k": float(np.mean(rec)), "mre": float(np.mean(err)),
+                   "ground_truth": "suco_gpu_exact_knn_batch", "ground_truth_s": gt_s}
+
     # roofline of the dominant kernel (SURVEY §8(d) algorithmic bytes)
     peak, peak_src = measured_peaks()
     cum, sq, m = stats
@@ -415,7 +427,7 @@ def main():
                    "index_source": args.index_source, "l2": "256 MiB flush write between timed steps",
                    "rerank_rows": "u8" if row_bytes != 4 * d else "f32",
                    "parallelism": f"replicas x{ws}"},
-        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "parity": parity,
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "parity": parity, "quality": quality,
         "gpu_launches": launches_per_step * args.steps, "clocks": clocks.summary(),
     }
     if rank == 0:

@@ -188,6 +188,17 @@ int suco_gpu_shard_topk(suco_gpu_index* shard, const float* d_queries, uint64_t 
                         const uint32_t* d_base, const uint32_t* d_counts, uint64_t stride, uint32_t* d_ids,
                         double* d_sqdists, void* stream);
 
+/* ------------------------------------------------------------ evaluation
+ * exact_knn (eval.hpp:29, eval.cpp:28-62) over a batch, on the index's device
+ * copy of the dataset: the k nearest ids by exact fp64 squared distance (the
+ * reference's 4-accumulator kernel, or its exact integer equal for u8 data),
+ * ties by id, distances = sqrt. k < 1, k > n or a wrong query length ->
+ * CONTRACT. Host buffers: queries nq x qlen, ids / dists nq x k. The GPU
+ * ground truth of SURVEY §8(f)2; recall/MRE are host arithmetic
+ * (paper_2411_14754_b200.recall / mre, eval.cpp:64-102). */
+int suco_gpu_exact_knn_batch(suco_gpu_index* index, const float* queries, uint64_t nq, uint32_t qlen, uint32_t k,
+                             uint32_t* ids, double* dists);
+
 /* ------------------------------------------------ stage-level entry points
  * Each runs the device kernel of one stage on host inputs (parity tests of
  * the reference's free functions). */

@@ -22,10 +22,12 @@
 // exchange between shards lives in paper_2411_14754_b200.sharded).
 // Also wrapped: suco_last_error, suco_gpu_device_count, suco_gpu_index_info,
 // suco_gpu_index_subspace, suco_gpu_free_index, suco_gpu_set_stream,
-// suco_gpu_synchronize, suco_gpu_query_intermediates, suco_gpu_last_launches.
+// suco_gpu_synchronize, suco_gpu_query_intermediates, suco_gpu_last_launches,
+// suco_gpu_exact_knn_batch (GpuIndex::exact_knn_batch; recall / mre as in eval.cpp:64-102).
 #pragma once
 
 #include <cstdint>
+#include <limits>
 #include <memory>
 #include <span>
 #include <stdexcept>
@@ -180,6 +182,20 @@ public:
         return out;
     }
 
+    // exact_knn (eval.hpp:29) for every row: the GPU ground truth, ascending by (distance, id).
+    std::vector<QueryResult> exact_knn_batch(std::span<const float> queries, std::uint64_t nq, std::uint32_t k) const {
+        const std::uint32_t qlen = nq ? static_cast<std::uint32_t>(queries.size() / nq) : 0;
+        std::vector<std::uint32_t> ids(nq * k);
+        std::vector<double> dists(nq * k);
+        check(suco_gpu_exact_knn_batch(h_.get(), queries.data(), nq, qlen, k, ids.data(), dists.data()));
+        std::vector<QueryResult> out(nq);
+        for (std::uint64_t q = 0; q < nq; ++q) {
+            out[q].entries.resize(k);
+            for (std::uint32_t i = 0; i < k; ++i) out[q].entries[i] = {ids[q * k + i], dists[q * k + i]};
+        }
+        return out;
+    }
+
     // Device-resident queries/outputs (nq x qlen f32 in, nq x k u32/f64 out), enqueued on `stream`.
     void knn_query_batch_device(const float* d_queries, std::uint64_t nq, std::uint32_t qlen,
                                 const CollisionParams& params, std::uint32_t* d_ids, double* d_dists,
@@ -239,6 +255,36 @@ inline std::vector<unsigned char> serialize_index(const GpuIndex& index) {
     std::vector<unsigned char> b(len);
     check(suco_gpu_serialize_index(index.handle(), b.data(), b.size(), &len));
     return b;
+}
+
+// recall / mre (eval.hpp:33-39, eval.cpp:64-102): host arithmetic on one query's lists.
+inline double recall(const QueryResult& result, std::span<const Neighbor> truth, std::uint32_t k) {
+    if (k < 1) throw ContractError("recall: k must be >= 1");
+    if (truth.size() < k) throw ContractError("recall: ground truth has fewer than k entries");
+    if (result.entries.size() > k) throw ContractError("recall: result holds more than k entries");
+    std::uint32_t hits = 0;
+    for (const Neighbor& nb : result.entries) {
+        for (std::uint32_t r = 0; r < k; ++r) hits += truth[r].id == nb.id;
+    }
+    return static_cast<double>(hits) / static_cast<double>(k);
+}
+
+inline double mre(const QueryResult& result, std::span<const Neighbor> truth, std::uint32_t k) {
+    if (k < 1) throw ContractError("mre: k must be >= 1");
+    if (truth.size() < k || result.entries.size() < k) throw ContractError("mre: both lists must hold at least k entries");
+    double sum = 0.0;
+    std::uint32_t included = 0;
+    bool clean = true;
+    for (std::uint32_t r = 0; r < k; ++r) {
+        if (truth[r].distance == 0.0) {
+            clean = clean && result.entries[r].distance == 0.0;
+            continue;
+        }
+        sum += (result.entries[r].distance - truth[r].distance) / truth[r].distance;
+        ++included;
+    }
+    if (included) return sum / included;
+    return clean ? 0.0 : std::numeric_limits<double>::infinity();
 }
 
 inline QueryResult knn_query(const GpuIndex& index, std::span<const float> query, const CollisionParams& params) {

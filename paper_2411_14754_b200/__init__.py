@@ -251,6 +251,18 @@ class GpuIndex:
                                   _p(dists, _c.f64p)))
         return ids[:, :k], dists[:, :k]
 
+    def exact_knn_batch(self, queries, k: int) -> Tuple[np.ndarray, np.ndarray]:
+        """exact_knn (eval.hpp:29, eval.cpp:28-62) for every row on the GPU: (ids nq x k, distances
+        nq x k), ascending by (distance, id) — the ground truth for recall / mre."""
+        q = _f32(queries)
+        if q.ndim == 1:
+            q = q[None, :]
+        nq, qlen = q.shape
+        ids = np.zeros((nq, max(k, 1)), np.uint32)
+        dists = np.zeros((nq, max(k, 1)), np.float64)
+        _check(_c.exact_knn_batch(self._h, _p(q, _c.f32p), nq, qlen, int(k), _p(ids, _c.u32p), _p(dists, _c.f64p)))
+        return ids[:, :k], dists[:, :k]
+
     def knn_query_batch_device(self, d_queries: int, nq: int, qlen: int, params: CollisionParams, d_ids: int,
                                d_dists: int, stream: Optional[int] = None) -> None:
         """Device-resident variant: raw device pointers (e.g. torch tensor .data_ptr()). `stream` is a
@@ -406,3 +418,38 @@ def build_imi(first, second, k_half: int):
     ids = np.empty(a.size, np.uint32)
     _check(_c.build_imi(_p(a, _c.u32p), _p(b, _c.u32p), a.size, k_half, _p(off, _c.u64p), _p(ids, _c.u32p)))
     return off, ids
+
+
+# ------------------------------------------------------------------ evaluation (host arithmetic)
+def recall(result_ids, truth_ids, k: int) -> float:
+    """|result ids ∩ exact top-k ids| / k (eval.hpp:33, eval.cpp:64-79); one query's rows."""
+    if k < 1:
+        raise ContractError("recall: k must be >= 1")
+    truth_ids = np.asarray(truth_ids).ravel()
+    result_ids = np.asarray(result_ids).ravel()
+    if truth_ids.size < k:
+        raise ContractError("recall: ground truth has fewer than k entries")
+    if result_ids.size > k:
+        raise ContractError("recall: result holds more than k entries")
+    return float(np.isin(result_ids, truth_ids[:k]).sum()) / float(k)
+
+
+def mre(result_dists, truth_dists, k: int) -> float:
+    """Mean over ranks of (result - truth) / truth for the first k entries, ranks with a zero true
+    distance dropped; all dropped -> 0 if the result is 0 there, +inf otherwise (eval.cpp:81-102)."""
+    if k < 1:
+        raise ContractError("mre: k must be >= 1")
+    r = np.asarray(result_dists, np.float64).ravel()
+    t = np.asarray(truth_dists, np.float64).ravel()
+    if t.size < k or r.size < k:
+        raise ContractError("mre: both lists must hold at least k entries")
+    total, included, clean = 0.0, 0, True
+    for i in range(k):  # in rank order, like the reference's accumulation
+        if t[i] == 0.0:
+            clean &= r[i] == 0.0
+            continue
+        total += (r[i] - t[i]) / t[i]
+        included += 1
+    if included:
+        return total / included
+    return 0.0 if clean else float("inf")

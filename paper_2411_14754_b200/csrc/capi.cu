@@ -841,6 +841,63 @@ int suco_gpu_knn_query_batch(suco_gpu_index* x, const float* queries, uint64_t n
     });
 }
 
+// exact_knn (eval.hpp:29, eval.cpp:28-62) for a batch: the re-rank kernels over every id.
+int suco_gpu_exact_knn_batch(suco_gpu_index* x, const float* queries, uint64_t nq, uint32_t qlen, uint32_t k,
+                             uint32_t* ids, double* dists) {
+    return guarded([&] {
+        if (!x) raise(SUCO_ERR_CONTRACT, "index is null");
+        const uint64_t n = x->host.n;
+        if (qlen != x->host.d) {
+            raise(SUCO_ERR_CONTRACT, "query length " + std::to_string(qlen) + " does not match dataset d = " +
+                                         std::to_string(x->host.d));
+        }
+        if (k < 1 || k > n) {
+            raise(SUCO_ERR_CONTRACT, "k must be in [1, n]; got k = " + std::to_string(k) + ", n = " + std::to_string(n));
+        }
+        if (nq == 0) return;
+        if (!queries || !ids || !dists) raise(SUCO_ERR_CONTRACT, "null buffer");
+        DeviceGuard g(x->device);
+        cudaStream_t st = x->stream;
+        // tiles of queries (k > 32: one query per launch, its n scored rows in scratch)
+        const uint64_t tile = k > 32 ? 1 : std::min<uint64_t>(nq, 8192);
+        DevBuf<float> dq;
+        DevBuf<uint32_t> di;
+        DevBuf<double> dd, all_d;
+        DevBuf<uint32_t> all_id;
+        dq.reserve(tile * qlen);
+        di.reserve(tile * k);
+        dd.reserve(tile * k);
+        if (k > 32) {
+            all_d.reserve(n);
+            all_id.reserve(n);
+        }
+        for (uint64_t q0 = 0; q0 < nq; q0 += tile) {
+            const uint64_t nt = std::min<uint64_t>(tile, nq - q0);
+            CUDA_TRY(cudaMemcpyAsync(dq.p, queries + q0 * qlen, nt * qlen * 4, cudaMemcpyHostToDevice, st));
+            RerankArgs ra{};
+            ra.data = x->data.p;
+            ra.n = n;
+            ra.d = x->host.d;
+            ra.queries = dq.p;
+            ra.cands = nullptr;
+            ra.identity = true;
+            ra.m = n;
+            ra.k = k;
+            ra.out_ids = di.p;
+            ra.out_dists = dd.p;
+            ra.data_int_max = x->data_int_max;
+            ra.data8 = x->dpad ? x->data8.p : nullptr;
+            ra.dpad = x->dpad;
+            ra.all_d = all_d.p;
+            ra.all_id = all_id.p;
+            CUDA_TRY(launch_rerank(ra, nt, st));
+            CUDA_TRY(cudaMemcpyAsync(ids + q0 * k, di.p, nt * k * 4, cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaMemcpyAsync(dists + q0 * k, dd.p, nt * k * 8, cudaMemcpyDeviceToHost, st));
+        }
+        CUDA_TRY(cudaStreamSynchronize(st));
+    });
+}
+
 int suco_gpu_query_intermediates(suco_gpu_index* x, const float* query, uint32_t qlen, const suco_collision_params* p,
                                  uint32_t* scores, uint32_t* cands, uint64_t* m_out, uint32_t* cells_per_subspace,
                                  uint64_t* cumulative) {

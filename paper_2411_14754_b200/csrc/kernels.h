@@ -128,6 +128,7 @@ struct RerankArgs {
                                         // global order) and launch_shard_ids maps the k outputs to global ids
     const uint8_t* data8;  // optional u8 copy of the rows (data certified integer in [0, 255]), n x dpad
     uint32_t dpad;         // row bytes of data8 (d rounded up to 16)
+    bool identity;         // exact kNN: candidate i of every query is id i (cands unused, m = n)
 };
 cudaError_t launch_rerank(const RerankArgs& a, uint64_t nq, cudaStream_t st);
 

@@ -109,7 +109,9 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
         // candidate ids of the 8 rows (lanes 0..7 load, broadcast); `gid` is the
         // reported id, `rid` the row in `data` (differs on shards)
         uint32_t my_id = 0;
-        if (lane < kRows && base + lane < mq) my_id = __ldcs(cands + base + lane);  // read once: evict first
+        if (lane < kRows && base + lane < mq) {
+            my_id = a.identity ? static_cast<uint32_t>(base + lane) : __ldcs(cands + base + lane);  // read once
+        }
         uint32_t gid[kRows], rid[kRows];
 #pragma unroll
         for (uint32_t j = 0; j < kRows; ++j) {
@@ -254,7 +256,9 @@ __global__ void __launch_bounds__(kThreads) rerank_u8_kernel(RerankArgs a) {
     double ld = kInf;
     uint32_t lid = 0xffffffffu;
     for (uint64_t base = static_cast<uint64_t>(warp) * kStep; base < mq; base += kStep * kWarps) {
-        const uint32_t my = (lane < kStep && base + lane < mq) ? __ldcs(cands + base + lane) : 0u;
+        const uint32_t my = (lane < kStep && base + lane < mq)
+                                ? (a.identity ? static_cast<uint32_t>(base + lane) : __ldcs(cands + base + lane))
+                                : 0u;
         uint32_t idr[U];
         bool vr[U];
         uint4 x[U];
