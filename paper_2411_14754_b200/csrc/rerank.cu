@@ -225,7 +225,7 @@ __device__ __forceinline__ uint4 ld_nc_u4(const uint8_t* p) {
 }
 
 template <uint32_t L, bool GENERIC>
-__global__ void __launch_bounds__(kThreads) rerank_u8_kernel(RerankArgs a) {
+__global__ void __launch_bounds__(kThreads, 6) rerank_u8_kernel(RerankArgs a) {
     constexpr uint32_t R = 32 / L;
     constexpr uint32_t U = L >= 4 ? 4 : L;  // loads in flight per lane, with at most 32 rows per step
     constexpr uint32_t kStep = R * U;       // rows per warp step (<= 32: one candidate id per lane)

@@ -257,7 +257,7 @@ __device__ inline void run_da(const WarpSmem& w, uint32_t k, const uint32_t* cel
     }
 }
 
-__global__ void traverse_kernel(TraverseArgs a, uint32_t warps_per_block, size_t per_warp) {
+__global__ void __launch_bounds__(256, 5) traverse_kernel(TraverseArgs a, uint32_t warps_per_block, size_t per_warp) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const uint64_t task = static_cast<uint64_t>(blockIdx.x) * warps_per_block + warp;
