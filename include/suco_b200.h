@@ -175,7 +175,7 @@ int suco_gpu_shard_info(const suco_gpu_index* index, uint64_t* n_global, uint64_
  * shard reports per query — whole blocks, or (dense select, blocks a multiple
  * of 2048 ids) 2048-id pieces, pieces_per_block of them per block, so local
  * piece p sits in global order at ((p / ppb) * num_shards + shard) * ppb + p % ppb. */
-int suco_gpu_shard_pieces(const suco_gpu_index* shard, uint32_t* pieces_per_block);
+int suco_gpu_shard_pieces(const suco_gpu_index* shard, uint32_t* pieces_per_block, int* dense /* may be NULL */);
 /* d_queries nq x qlen, d_hist nq x nblocks_local x (N_s + 2) u32 (device): per piece
  * [length, #score >= 1, ..., #score >= N_s, 0]. */
 int suco_gpu_shard_histograms(suco_gpu_index* shard, const float* d_queries, uint64_t nq, uint32_t qlen,
@@ -187,6 +187,23 @@ int suco_gpu_shard_topk(suco_gpu_index* shard, const float* d_queries, uint64_t 
                         const suco_collision_params* params, const uint32_t* d_T, const uint32_t* d_quota,
                         const uint32_t* d_base, const uint32_t* d_counts, uint64_t stride, uint32_t* d_ids,
                         double* d_sqdists, void* stream);
+
+/* Query-split variant (multi-GPU): each rank traverses only its slice of the
+ * batch (suco_gpu_shard_traverse: d_cells nq x N_s x K padded, d_ncells
+ * nq x N_s, against the GLOBAL cell sizes); the ranks exchange the compact
+ * cell lists (query order, then subspace order; d_cells_off = nq*N_s + 1
+ * u64 offsets) and run phases 1 and 2 on them. Needs the dense select
+ * (N_s <= 8, blocks a multiple of 2048 ids). */
+int suco_gpu_shard_traverse(suco_gpu_index* shard, const float* d_queries, uint64_t nq, uint32_t qlen,
+                            const suco_collision_params* params, uint32_t* d_cells, uint32_t* d_ncells, void* stream);
+int suco_gpu_shard_histograms_cells(suco_gpu_index* shard, uint64_t nq, const suco_collision_params* params,
+                                    const uint32_t* d_cells, const uint64_t* d_cells_off, uint32_t* d_hist,
+                                    void* stream);
+int suco_gpu_shard_topk_cells(suco_gpu_index* shard, const float* d_queries, uint64_t nq, uint32_t qlen,
+                              const suco_collision_params* params, const uint32_t* d_cells,
+                              const uint64_t* d_cells_off, const uint32_t* d_T, const uint32_t* d_quota,
+                              const uint32_t* d_base, const uint32_t* d_counts, uint64_t stride, uint32_t* d_ids,
+                              double* d_sqdists, void* stream);
 
 /* ------------------------------------------------------------ evaluation
  * exact_knn (eval.hpp:29, eval.cpp:28-62) over a batch, on the index's device

@@ -17,7 +17,8 @@
 //                                               -> suco_collision_count / suco_candidate_count /
 //                                                  suco_validate_collision_params
 // Multi-GPU shard protocol: suco_gpu_make_shard / suco_gpu_shard_block_hint / suco_gpu_shard_info /
-// suco_gpu_shard_pieces /
+// suco_gpu_shard_pieces / suco_gpu_shard_traverse / suco_gpu_shard_histograms_cells /
+// suco_gpu_shard_topk_cells /
 // suco_gpu_shard_histograms / suco_gpu_shard_topk (raw C entry points; the
 // exchange between shards lives in paper_2411_14754_b200.sharded).
 // Also wrapped: suco_last_error, suco_gpu_device_count, suco_gpu_index_info,

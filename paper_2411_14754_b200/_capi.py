@@ -77,7 +77,11 @@ query_intermediates = _sig("suco_gpu_query_intermediates", C.c_int, vp, f32p, C.
                            C.POINTER(CollisionParamsC), u32p, u32p, u64p, u32p, u64p)
 make_shard = _sig("suco_gpu_make_shard", C.c_int, vp, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(vp))
 shard_block_hint = _sig("suco_gpu_shard_block_hint", C.c_int, vp, C.c_uint32, u32p)
-shard_pieces = _sig("suco_gpu_shard_pieces", C.c_int, vp, u32p)
+shard_pieces = _sig("suco_gpu_shard_pieces", C.c_int, vp, u32p, C.POINTER(C.c_int))
+shard_traverse = _sig("suco_gpu_shard_traverse", C.c_int, vp, vp, C.c_uint64, C.c_uint32, vp, vp, vp, vp)
+shard_histograms_cells = _sig("suco_gpu_shard_histograms_cells", C.c_int, vp, C.c_uint64, vp, vp, vp, vp, vp)
+shard_topk_cells = _sig("suco_gpu_shard_topk_cells", C.c_int, vp, vp, C.c_uint64, C.c_uint32, vp, vp, vp, vp, vp, vp,
+                        vp, C.c_uint64, vp, vp, vp)
 shard_info = _sig("suco_gpu_shard_info", C.c_int, vp, u64p, u64p, u32p, u32p, u32p, u32p)
 shard_histograms = _sig("suco_gpu_shard_histograms", C.c_int, vp, vp, C.c_uint64, C.c_uint32,
                         C.POINTER(CollisionParamsC), vp, vp)
@@ -100,6 +104,7 @@ EXPORTED = [
     "suco_gpu_stage_times", "suco_gpu_last_launches", "suco_gpu_exact_knn_batch",
     "suco_gpu_query_intermediates", "suco_gpu_centroid_distances", "suco_gpu_dynamic_activation", "suco_gpu_rerank",
     "suco_gpu_kmeans", "suco_gpu_build_imi", "suco_gpu_make_shard", "suco_gpu_shard_block_hint",
-    "suco_gpu_shard_info", "suco_gpu_shard_pieces", "suco_gpu_shard_histograms",
+    "suco_gpu_shard_info", "suco_gpu_shard_pieces", "suco_gpu_shard_traverse", "suco_gpu_shard_histograms_cells",
+    "suco_gpu_shard_topk_cells", "suco_gpu_shard_histograms",
     "suco_gpu_shard_topk",
 ]

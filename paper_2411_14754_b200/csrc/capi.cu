@@ -1077,12 +1077,44 @@ int suco_gpu_shard_info(const suco_gpu_index* x, uint64_t* n_global, uint64_t* n
     });
 }
 
-int suco_gpu_shard_pieces(const suco_gpu_index* x, uint32_t* pieces_per_block) {
+int suco_gpu_shard_pieces(const suco_gpu_index* x, uint32_t* pieces_per_block, int* dense) {
     return guarded([&] {
         if (!x || !pieces_per_block) raise(SUCO_ERR_CONTRACT, "null argument");
         const uint32_t b = x->block ? x->block : static_cast<uint32_t>(std::min<uint64_t>(x->host.n, 0xFFFFFFFFull));
         *pieces_per_block = x->dense ? b / kDensePiece : 1u;
+        if (dense) *dense = x->dense ? 1 : 0;
     });
+}
+
+// Local exact re-rank of a shard's candidates (squared distances, local ids -> global ids).
+void shard_rerank(suco_gpu_index* x, const float* d_queries, uint64_t nq, uint32_t k, const uint32_t* d_counts,
+                  uint64_t sd, uint32_t* d_ids, double* d_sqdists, cudaStream_t st) {
+    const uint64_t nl = x->host.n;
+    const uint32_t b = x->block ? x->block : static_cast<uint32_t>(nl);
+    RerankArgs ra{};
+    ra.data = x->data.p;
+    ra.n = nl;
+    ra.d = x->host.d;
+    ra.queries = d_queries;
+    ra.cands = x->shard_cands.p;
+    ra.m = sd;
+    ra.k = k;
+    ra.out_ids = d_ids;
+    ra.out_dists = d_sqdists;
+    ra.data_int_max = x->data_int_max;
+    ra.data8 = x->dpad ? x->data8.p : nullptr;
+    ra.dpad = x->dpad;
+    ra.counts = d_counts;
+    ra.squared = true;
+    auto& sl = x->slot[0];
+    if (k > 32) {
+        sl.all_d.reserve(nq * sd);
+        sl.all_id.reserve(nq * sd);
+        ra.all_d = sl.all_d.p;
+        ra.all_id = sl.all_id.p;
+    }
+    CUDA_TRY(launch_rerank(ra, nq, st));
+    if (x->num_shards > 1) CUDA_TRY(launch_shard_ids(d_ids, nq * k, b, x->num_shards, x->shard, st));
 }
 
 DenseArgs shard_dense_args(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nq) {
@@ -1098,6 +1130,86 @@ DenseArgs shard_dense_args(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t
     da.WP = kDensePiece;
     da.P = static_cast<uint32_t>((x->host.n + kDensePiece - 1) / kDensePiece);
     return da;
+}
+
+// Query-split traversal for the multi-GPU protocol: rank r traverses its slice of the
+// batch; the compact cell lists are exchanged and phases 1/2 take them (_cells variants).
+int suco_gpu_shard_traverse(suco_gpu_index* x, const float* d_queries, uint64_t nq, uint32_t qlen,
+                            const suco_collision_params* p, uint32_t* d_cells, uint32_t* d_ncells, void* stream) {
+    return guarded([&] {
+        if (!x) raise(SUCO_ERR_CONTRACT, "index is null");
+        if (qlen != x->host.d) raise(SUCO_ERR_CONTRACT, "query length does not match dataset d");
+        validate_params(p, x->n_global);
+        if (nq == 0) return;
+        DeviceGuard g(x->device);
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : x->stream;
+        const HostIndex& h = x->host;
+        TraverseArgs ta{};
+        ta.queries = d_queries;
+        ta.d = h.d;
+        ta.nq = nq;
+        ta.dims = x->dims.p;
+        ta.sub = x->sub.p;
+        ta.cent = x->cent.p;
+        ta.cell_size = x->cell_size.p;  // GLOBAL cell sizes: the global Dynamic-Activation cut
+        ta.ns = h.layout.ns;
+        ta.k_half = h.p.k_half;
+        ta.K = x->K;
+        ta.hmax = x->hmax;
+        ta.target = suco_collision_count(p->alpha, x->n_global);
+        ta.cells = d_cells;
+        ta.ncells = d_ncells;
+        CUDA_TRY(launch_traverse(ta, st));
+    });
+}
+
+int suco_gpu_shard_histograms_cells(suco_gpu_index* x, uint64_t nq, const suco_collision_params* p,
+                                    const uint32_t* d_cells, const uint64_t* d_cells_off, uint32_t* d_hist,
+                                    void* stream) {
+    return guarded([&] {
+        if (!x) raise(SUCO_ERR_CONTRACT, "index is null");
+        if (!x->dense) raise(SUCO_ERR_CONTRACT, "the _cells shard entry points need the dense select (N_s <= 8, blocks of 2048k ids)");
+        validate_params(p, x->n_global);
+        if (nq == 0) return;
+        DeviceGuard g(x->device);
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : x->stream;
+        auto& sl = x->slot[0];
+        DenseArgs da = shard_dense_args(x, sl, nq);
+        da.cells = d_cells;
+        da.cells_off = d_cells_off;
+        sl.dhist.reserve(nq * da.P * 8);
+        da.hist = sl.dhist.p;
+        CUDA_TRY(launch_dense_hist(da, st));
+        CUDA_TRY(launch_dense_hist_rows(da, d_hist, st));
+    });
+}
+
+int suco_gpu_shard_topk_cells(suco_gpu_index* x, const float* d_queries, uint64_t nq, uint32_t qlen,
+                              const suco_collision_params* p, const uint32_t* d_cells, const uint64_t* d_cells_off,
+                              const uint32_t* d_T, const uint32_t* d_quota, const uint32_t* d_base,
+                              const uint32_t* d_counts, uint64_t stride, uint32_t* d_ids, double* d_sqdists,
+                              void* stream) {
+    return guarded([&] {
+        if (!x) raise(SUCO_ERR_CONTRACT, "index is null");
+        if (!x->dense) raise(SUCO_ERR_CONTRACT, "the _cells shard entry points need the dense select");
+        if (qlen != x->host.d) raise(SUCO_ERR_CONTRACT, "query length does not match dataset d");
+        validate_params(p, x->n_global);
+        if (nq == 0) return;
+        DeviceGuard g(x->device);
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : x->stream;
+        const uint64_t sd = std::max<uint64_t>(stride, 1);
+        x->shard_cands.reserve(nq * sd);
+        DenseArgs da = shard_dense_args(x, x->slot[0], nq);
+        da.cells = d_cells;
+        da.cells_off = d_cells_off;
+        da.m = sd;
+        da.T = const_cast<uint32_t*>(d_T);
+        da.quota = const_cast<uint32_t*>(d_quota);
+        da.base = const_cast<uint32_t*>(d_base);
+        da.cands = x->shard_cands.p;
+        CUDA_TRY(launch_dense_emit(da, st));
+        shard_rerank(x, d_queries, nq, p->k, d_counts, sd, d_ids, d_sqdists, st);
+    });
 }
 
 int suco_gpu_shard_histograms(suco_gpu_index* x, const float* d_queries, uint64_t nq, uint32_t qlen,
@@ -1192,33 +1304,7 @@ int suco_gpu_shard_topk(suco_gpu_index* x, const float* d_queries, uint64_t nq, 
             CUDA_TRY(launch_shard_emit(x->shard_scores.p, nq, nl, ss, b, nblocks, x->shard, x->num_shards, d_T, d_quota,
                                        d_base, x->shard_cands.p, sd, st));
         }
-        RerankArgs ra{};
-        ra.data = x->data.p;
-        ra.n = nl;
-        ra.d = x->host.d;
-        ra.queries = d_queries;
-        ra.cands = x->shard_cands.p;
-        ra.m = sd;
-        ra.k = p->k;
-        ra.out_ids = d_ids;
-        ra.out_dists = d_sqdists;
-        ra.data_int_max = x->data_int_max;
-        ra.data8 = x->dpad ? x->data8.p : nullptr;
-        ra.dpad = x->dpad;
-        ra.counts = d_counts;
-        ra.squared = true;
-        ra.shard_b = x->num_shards > 1 ? b : 0;
-        ra.shard_G = x->num_shards > 1 ? x->num_shards : 0;
-        ra.shard_s = x->shard;
-        auto& sl = x->slot[0];
-        if (p->k > 32) {
-            sl.all_d.reserve(nq * sd);
-            sl.all_id.reserve(nq * sd);
-            ra.all_d = sl.all_d.p;
-            ra.all_id = sl.all_id.p;
-        }
-        CUDA_TRY(launch_rerank(ra, nq, st));
-        if (x->num_shards > 1) CUDA_TRY(launch_shard_ids(d_ids, nq * p->k, b, x->num_shards, x->shard, st));
+        shard_rerank(x, d_queries, nq, p->k, d_counts, sd, d_ids, d_sqdists, st);
     });
 }
 

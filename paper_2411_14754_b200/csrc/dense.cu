@@ -98,8 +98,9 @@ __device__ void build_masks(const DenseArgs& a, uint32_t* M, uint64_t q0, uint32
     for (uint32_t j = warp; j < nqb; j += kDW) {
         const uint64_t q = q0 + j;
         for (uint32_t s = 0; s < a.ns; ++s) {
-            const uint32_t cnt = a.ncells[q * a.ns + s];
-            const uint32_t* cp = a.cells + (q * a.ns + s) * a.cells_cap;
+            const uint64_t t = q * a.ns + s;
+            const uint32_t cnt = a.cells_off ? static_cast<uint32_t>(a.cells_off[t + 1] - a.cells_off[t]) : a.ncells[t];
+            const uint32_t* cp = a.cells + (a.cells_off ? a.cells_off[t] : t * a.cells_cap);
             for (uint32_t i = lane; i < cnt; i += 32) atomicOr(M + (s * a.K + cp[i]) * W + (j >> 5), 1u << (j & 31u));
         }
     }

@@ -83,8 +83,9 @@ cudaError_t launch_slab_offsets(const uint32_t* cell_off, const uint32_t* ids, u
 // select_kernel (the top-m candidate set, unordered) when N_s <= 8.
 struct DenseArgs {
     const uint4* codes;        // n x 8 u16: s*K + cell of the point in subspace s (N_s*K when s >= N_s)
-    const uint32_t* cells;     // nq x ns x cells_cap (traversal output)
+    const uint32_t* cells;     // nq x ns x cells_cap (traversal output), or compact (cells_off)
     const uint32_t* ncells;    // nq x ns
+    const uint64_t* cells_off; // optional nq*ns+1 offsets into a compact `cells` (then ncells unused)
     uint32_t cells_cap, ns, K;
     uint64_t n, nq, m;
     uint32_t P, WP;            // pieces of WP consecutive points (one warp each)

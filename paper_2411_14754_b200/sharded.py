@@ -144,9 +144,11 @@ class GpuShard:
         self.block, self.shard, self.num_shards = b.value, s.value, G.value
         self.ns = full.params.num_subspaces
         self.d = full.d
-        ppb = C.c_uint32()
-        _check(_c.shard_pieces(h, C.byref(ppb)))
+        ppb, dense = C.c_uint32(), C.c_int()
+        _check(_c.shard_pieces(h, C.byref(ppb), C.byref(dense)))
         self.ppb = ppb.value  # histogram pieces per block (dense select: 2048-id pieces)
+        self.dense = bool(dense.value)
+        self.K = full.params.k_half ** 2
 
     def histograms(self, q: torch.Tensor, params: CollisionParams, stream: Optional[int] = None) -> torch.Tensor:
         stream = stream or _torch_stream(q.device)  # ordered with the plan math
@@ -168,6 +170,63 @@ class GpuShard:
                              C.c_void_p(plan.base.data_ptr()), C.c_void_p(plan.counts.data_ptr()), plan.stride,
                              C.c_void_p(ids.data_ptr()), C.c_void_p(sq.data_ptr()), C.c_void_p(stream or 0)))
         return ids, sq
+
+
+    # ---- query-split traversal (multi-GPU): every rank traverses a slice of the batch
+    @property
+    def split_traversal(self) -> bool:
+        """The query-split protocol needs the dense select (its phases take exchanged cell lists)."""
+        return self.dense
+
+    def traverse_slice(self, q: torch.Tensor, params: CollisionParams, stream: Optional[int] = None):
+        """Traversal of this rank's query slice -> (compact cells u32 [L], counts [nq_slice, ns])."""
+        stream = stream or _torch_stream(q.device)
+        nq = q.shape[0]
+        K = self.K
+        cells = torch.empty((max(nq, 1), self.ns, K), dtype=torch.int32, device=q.device)
+        ncells = torch.zeros((max(nq, 1), self.ns), dtype=torch.int32, device=q.device)
+        if nq:
+            cp = params._c()
+            _check(_c.shard_traverse(self.index.handle, C.c_void_p(q.data_ptr()), nq, self.d, C.byref(cp),
+                                     C.c_void_p(cells.data_ptr()), C.c_void_p(ncells.data_ptr()), C.c_void_p(stream)))
+        cells, ncells = cells[:nq], ncells[:nq]
+        keep = torch.arange(K, device=q.device).view(1, 1, K) < ncells.unsqueeze(2)
+        return cells[keep], ncells
+
+    def histograms_cells(self, nq: int, params: CollisionParams, cells: torch.Tensor, off: torch.Tensor,
+                         stream: Optional[int] = None) -> torch.Tensor:
+        stream = stream or _torch_stream(cells.device)
+        hist = torch.empty((nq, self.nblocks, self.ns + 2), dtype=torch.int32, device=cells.device)
+        cp = params._c()
+        _check(_c.shard_histograms_cells(self.index.handle, nq, C.byref(cp), C.c_void_p(cells.data_ptr()),
+                                         C.c_void_p(off.data_ptr()), C.c_void_p(hist.data_ptr()), C.c_void_p(stream)))
+        return hist
+
+    def topk_cells(self, q: torch.Tensor, params: CollisionParams, plan: Plan, cells: torch.Tensor,
+                   off: torch.Tensor, stream: Optional[int] = None):
+        stream = stream or _torch_stream(q.device)
+        nq, k = q.shape[0], int(params.k)
+        ids = torch.empty((nq, k), dtype=torch.int32, device=q.device)
+        sq = torch.empty((nq, k), dtype=torch.float64, device=q.device)
+        cp = params._c()
+        _check(_c.shard_topk_cells(self.index.handle, C.c_void_p(q.data_ptr()), nq, self.d, C.byref(cp),
+                                   C.c_void_p(cells.data_ptr()), C.c_void_p(off.data_ptr()),
+                                   C.c_void_p(plan.T.data_ptr()), C.c_void_p(plan.quota.data_ptr()),
+                                   C.c_void_p(plan.base.data_ptr()), C.c_void_p(plan.counts.data_ptr()), plan.stride,
+                                   C.c_void_p(ids.data_ptr()), C.c_void_p(sq.data_ptr()), C.c_void_p(stream)))
+        return ids, sq
+
+
+def query_slice(nq: int, rank: int, size: int) -> Tuple[int, int]:
+    """Rank `rank`'s contiguous slice of a batch of nq queries."""
+    return nq * rank // size, nq * (rank + 1) // size
+
+
+def cell_offsets(ncells: torch.Tensor) -> torch.Tensor:
+    """[nq, ns] counts -> nq*ns + 1 u64 offsets into the compact cell array."""
+    off = torch.zeros(ncells.numel() + 1, dtype=torch.int64, device=ncells.device)
+    off[1:] = torch.cumsum(ncells.reshape(-1).to(torch.int64), dim=0)
+    return off
 
 
 # ----------------------------------------------------------------- protocols
@@ -195,8 +254,23 @@ class TorchComm:
 
 
 def knn_query_distributed(engine, comm: TorchComm, queries: torch.Tensor, params: CollisionParams):
-    """Every rank calls this with the same queries; returns the global (ids int64 [nq,k], dists f64 [nq,k])."""
+    """Every rank calls this with the same queries; returns the global (ids int64 [nq,k], dists f64 [nq,k]).
+    Engines with `split_traversal` traverse only their slice of the batch and exchange the cell lists."""
     m = candidate_count(params.beta, engine.n_global, params.k)
+    if getattr(engine, "split_traversal", False):
+        nq = queries.shape[0]
+        lo, hi = query_slice(nq, comm.rank, comm.size)
+        mine, nc = engine.traverse_slice(queries[lo:hi], params)
+        cells = torch.cat(comm.allgather_var(mine.view(1, -1)), dim=1).view(-1)
+        ncells = torch.cat([t.t() for t in comm.allgather_var(nc.t().contiguous())], dim=0)
+        off = cell_offsets(ncells)
+        hist = engine.histograms_cells(nq, params, cells, off)
+        hists = comm.allgather_var(hist)
+        plan = plan_for_shard(hists, comm.rank, m, getattr(engine, "ppb", 1))
+        ids, sq = engine.topk_cells(queries, params, plan, cells, off)
+        all_ids = comm.allgather_var(ids)
+        all_sq = comm.allgather_var(sq)
+        return merge_topk(all_ids, all_sq, int(params.k))
     hist = engine.histograms(queries, params)
     hists = comm.allgather_var(hist)
     plan = plan_for_shard(hists, comm.rank, m, getattr(engine, "ppb", 1))
@@ -206,9 +280,19 @@ def knn_query_distributed(engine, comm: TorchComm, queries: torch.Tensor, params
     return merge_topk(all_ids, all_sq, int(params.k))
 
 
-def emulate(engines: Sequence, queries: torch.Tensor, params: CollisionParams):
-    """Run the protocol for G shard engines in one process (single-GPU CI of the multi-GPU path)."""
+def emulate(engines: Sequence, queries: torch.Tensor, params: CollisionParams, split: bool = False):
+    """Run the protocol for G shard engines in one process (single-GPU CI of the multi-GPU path);
+    split=True: each engine traverses its slice of the batch and the cell lists are concatenated."""
     m = candidate_count(params.beta, engines[0].n_global, params.k)
+    if split:
+        G, nq = len(engines), queries.shape[0]
+        parts = [e.traverse_slice(queries[slice(*query_slice(nq, r, G))], params) for r, e in enumerate(engines)]
+        cells = torch.cat([p[0] for p in parts])
+        off = cell_offsets(torch.cat([p[1] for p in parts]))
+        hists = [e.histograms_cells(nq, params, cells, off) for e in engines]
+        tops = [e.topk_cells(queries, params, plan_for_shard(hists, r, m, e.ppb), cells, off)
+                for r, e in enumerate(engines)]
+        return merge_topk([t[0] for t in tops], [t[1] for t in tops], int(params.k))
     hists = [e.histograms(queries, params) for e in engines]
     tops = [e.topk(queries, params, plan_for_shard(hists, r, m, getattr(e, "ppb", 1))) for r, e in enumerate(engines)]
     return merge_topk([t[0] for t in tops], [t[1] for t in tops], int(params.k))

@@ -56,3 +56,47 @@ class OracleShard:
             for r, (dd, c) in enumerate(pairs):
                 ids[i, r], sq[i, r] = c, dd
         return torch.from_numpy(ids.view(np.int32)), torch.from_numpy(sq)
+
+
+class OracleSplitShard(OracleShard):
+    """OracleShard with the query-split traversal interface. The C oracle does not expose its
+    retrieved-cell lists, so traverse_slice returns a stand-in payload per (query, subspace):
+    as many entries as the oracle retrieves, with values derived from the query. histograms_cells
+    asserts that the payload gathered from every rank is exactly each query's own (the exchange
+    and offset plumbing), then scores the shard with the oracle."""
+
+    split_traversal = True
+
+    def _payload(self, qrow, cps):
+        tag = int(np.abs(qrow).sum() * 1000) % 1000003
+        return [np.arange(c, dtype=np.int64) * 7 + tag * 31 + s for s, c in enumerate(cps)]
+
+    def _cps(self, qrow, params):
+        _, _, cps, _ = self.idx.query_intermediates(self.data, qrow, params.alpha, params.beta, params.k)
+        return cps
+
+    def traverse_slice(self, q, params):
+        qs = q.numpy()
+        parts, counts = [], np.zeros((len(qs), self.ns), np.int32)
+        for i, row in enumerate(qs):
+            cps = self._cps(row, params)
+            counts[i] = cps
+            parts.extend(self._payload(row, cps))
+        flat = np.concatenate(parts) if parts else np.zeros(0, np.int64)
+        return torch.from_numpy(flat.astype(np.int32)), torch.from_numpy(counts)
+
+    def _check_cells(self, queries, params, cells, off):
+        cells, off = cells.numpy(), off.numpy()
+        for i, row in enumerate(queries.numpy()):
+            want = self._payload(row, self._cps(row, params))
+            for s in range(self.ns):
+                got = cells[off[i * self.ns + s]: off[i * self.ns + s + 1]]
+                assert np.array_equal(got, want[s].astype(np.int32)), (i, s)
+
+    def histograms_cells(self, nq, params, cells, off):
+        self._check_cells(self._queries, params, cells, off)
+        return self.histograms(self._queries, params)
+
+    def topk_cells(self, q, params, plan, cells, off):
+        self._check_cells(q, params, cells, off)
+        return self.topk(q, params, plan)

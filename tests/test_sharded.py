@@ -59,7 +59,7 @@ def test_plan_matches_reference_selection_rule(ppb):
         assert got == want
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, split=False):
     try:
         import torch.distributed as dist
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -68,13 +68,14 @@ def _worker(rank, world, port, q):
         sys.path.insert(0, ROOT)
         sys.path.insert(0, os.path.join(ROOT, "tests"))
         from oracle.oracle import oracle
-        from shard_oracle_engine import OracleShard
+        from shard_oracle_engine import OracleShard, OracleSplitShard
         from paper_2411_14754_b200 import CollisionParams
         from paper_2411_14754_b200.sharded import TorchComm, knn_query_distributed
         O = oracle()
         base, qs = _corpus(O)
         oidx = O.build_index(base, 4, 8, 3, 42, 0)
-        eng = OracleShard(O, oidx, base, rank, world, 64)
+        eng = (OracleSplitShard if split else OracleShard)(O, oidx, base, rank, world, 64)
+        eng._queries = torch.from_numpy(qs)
         comm = TorchComm()
         out = []
         for a, bta, k in ((0.05, 0.02, 10), (0.1, 0.005, 7), (0.002, 0.3, 12)):
@@ -87,14 +88,17 @@ def _worker(rank, world, port, q):
         q.put((rank, traceback.format_exc()))
 
 
-def test_gloo_world_size_2_matches_unsharded(oracle):
+@pytest.mark.parametrize("split", [False, True])
+def test_gloo_world_size_2_matches_unsharded(oracle, split):
+    """Both protocols over gloo: replicated traversal, and the query-split traversal whose cell
+    lists are all-gathered (split=True)."""
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, split)) for r in range(2)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in procs)
@@ -128,6 +132,25 @@ def test_gpu_emulated_shards_match_unsharded(gpu, oracle, G, block):
     for a, b, k in ((0.05, 0.005, 10), (0.02, 0.05, 40), (0.3, 0.001, 3), (0.001, 0.4, 5)):
         want_i, want_d = idx.knn_query_batch(qs, gpu.CollisionParams(a, b, k))
         ids, dd = emulate(shards, q, gpu.CollisionParams(a, b, k))
+        assert np.array_equal(ids.cpu().numpy().astype(np.uint32), want_i), (G, block, a, b, k)
+        assert np.array_equal(dd.cpu().numpy(), want_d), (G, block, a, b, k)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("G,block", [(1, 4096), (2, 2048), (3, 6144), (4, None), (8, 2048)])
+def test_gpu_emulated_split_traversal_matches_unsharded(gpu, oracle, G, block):
+    """Query-split protocol: each emulated shard traverses its slice of the batch; phases 1 and 2
+    run on the concatenated cell lists (dense select)."""
+    from paper_2411_14754_b200.sharded import GpuShard, emulate
+    full = oracle.clustered(20000 + 50, 32, 40, 177 + G, 20, 140, 18, True)
+    base, qs = oracle.hold_out(full, 50, 178)
+    idx = gpu.build_index(base, gpu.IndexParams(4, 16, 3, 42))
+    shards = [GpuShard(idx, r, G, block) for r in range(G)]
+    assert all(s.split_traversal for s in shards)
+    q = torch.from_numpy(qs).cuda()
+    for a, b, k in ((0.05, 0.005, 10), (0.02, 0.05, 40), (0.001, 0.4, 5)):
+        want_i, want_d = idx.knn_query_batch(qs, gpu.CollisionParams(a, b, k))
+        ids, dd = emulate(shards, q, gpu.CollisionParams(a, b, k), split=True)
         assert np.array_equal(ids.cpu().numpy().astype(np.uint32), want_i), (G, block, a, b, k)
         assert np.array_equal(dd.cpu().numpy(), want_d), (G, block, a, b, k)
 
