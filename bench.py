@@ -520,7 +520,7 @@ def run_sharded(args, cfg, base, queries, idx, build_s, ws, rank, local):
         "cpu_baseline": None,
         "e2e": {"value": nq * args.steps / (e2e_ms / 1000.0), "unit": "queries/s", "h2d_bytes_per_step": nq * d * 4,
                 "d2h_bytes_per_step": nq * k * 16, "ms_per_step": e2e_ms / args.steps},
-        "parity": parity, "gpu_launches": 5 * args.steps, "clocks": clocks.summary(),
+        "parity": parity, "gpu_launches": eng.index.last_launches() * args.steps, "clocks": clocks.summary(),
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

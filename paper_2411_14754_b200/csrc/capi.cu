@@ -1114,7 +1114,11 @@ void shard_rerank(suco_gpu_index* x, const float* d_queries, uint64_t nq, uint32
         ra.all_id = sl.all_id.p;
     }
     CUDA_TRY(launch_rerank(ra, nq, st));
-    if (x->num_shards > 1) CUDA_TRY(launch_shard_ids(d_ids, nq * k, b, x->num_shards, x->shard, st));
+    x->launches += (ra.data8 ? 2 : 1) + (k > 32 ? 1 : 0);
+    if (x->num_shards > 1) {
+        CUDA_TRY(launch_shard_ids(d_ids, nq * k, b, x->num_shards, x->shard, st));
+        x->launches += 1;
+    }
 }
 
 DenseArgs shard_dense_args(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nq) {
@@ -1160,6 +1164,7 @@ int suco_gpu_shard_traverse(suco_gpu_index* x, const float* d_queries, uint64_t 
         ta.cells = d_cells;
         ta.ncells = d_ncells;
         CUDA_TRY(launch_traverse(ta, st));
+        x->launches = 1;  // a split-protocol round starts here (suco_gpu_last_launches)
     });
 }
 
@@ -1181,6 +1186,7 @@ int suco_gpu_shard_histograms_cells(suco_gpu_index* x, uint64_t nq, const suco_c
         da.hist = sl.dhist.p;
         CUDA_TRY(launch_dense_hist(da, st));
         CUDA_TRY(launch_dense_hist_rows(da, d_hist, st));
+        x->launches += 2;
     });
 }
 
@@ -1209,6 +1215,7 @@ int suco_gpu_shard_topk_cells(suco_gpu_index* x, const float* d_queries, uint64_
         da.cands = x->shard_cands.p;
         CUDA_TRY(launch_dense_emit(da, st));
         shard_rerank(x, d_queries, nq, p->k, d_counts, sd, d_ids, d_sqdists, st);
+        x->launches += 1;
     });
 }
 
