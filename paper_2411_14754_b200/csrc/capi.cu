@@ -128,6 +128,8 @@ struct suco_gpu_index {
         DevBuf<uint32_t> cells, ncells, cands, out_ids, all_id;
         DevBuf<uint16_t> dhist;               // dense select: nq x P x 8
         DevBuf<uint32_t> dT, dquota, dbase;   // dense select plan
+        DevBuf<uint16_t> dsample, dslots, dscnt;  // single-pass select: sampled hist, supersets, sizes
+        DevBuf<uint32_t> dL, dflag;               // single-pass select: bound, fallback flags
         DevBuf<double> out_d, all_d;
         cudaEvent_t trav = nullptr, sel = nullptr, rr = nullptr;
     };
@@ -359,7 +361,7 @@ uint64_t tile_size(const suco_gpu_index* x, uint64_t nq, uint64_t m, uint32_t k)
     const uint64_t ns = x->host.layout.ns;
     const uint64_t pieces = (x->host.n + 2047) / 2048;  // dense select scratch: hist (16 B) + quota/base per piece
     const uint64_t per = ns * x->K * 4 + ns * 4 + m * 4 + (k > 32 ? m * 12 : 0) + uint64_t(x->host.d) * 4 + k * 12 +
-                         (x->dense ? pieces * 24 + 4 : 0);
+                         (x->dense ? pieces * (24 + 130) + pieces / 16 * 16 + 16 : 0);  // + single-pass supersets
     const uint64_t budget = 4ull << 30;
     return std::max<uint64_t>(1, std::min<uint64_t>(nq, budget / per));
 }
@@ -447,9 +449,30 @@ void stage_select(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nt, uint
         da.quota = sl.dquota.p;
         da.base = sl.dbase.p;
         da.cands = sl.cands.p;
+        const char* fv = std::getenv("SUCO_DENSE_FUSED");
+        const bool fused = !(fv && std::atoi(fv) == 0);
+        if (fused) {
+            da.pstride = 16;
+            da.Ps = (da.P + da.pstride - 1) / da.pstride;
+            da.C = 64;
+            sl.dsample.reserve(nt * da.Ps * 8);
+            sl.dslots.reserve(nt * da.P * da.C);
+            sl.dscnt.reserve(nt * da.P);
+            sl.dL.reserve(nt);
+            sl.dflag.reserve(2 * nt + 1);  // flags, flagged list, its count
+            da.hsample = sl.dsample.p;
+            da.qmap = sl.dflag.p + nt;
+            da.nmap = sl.dflag.p + 2 * nt;
+            da.slots = sl.dslots.p;
+            da.scnt = sl.dscnt.p;
+            da.L = sl.dL.p;
+            da.qflag = sl.dflag.p;
+        }
         if (ev) CUDA_TRY(cudaEventRecord(ev[0], st));
-        CUDA_TRY(launch_dense_select(da, st));
-        x->launches += 3;  // piece histograms, plan, emission
+        CUDA_TRY(fused ? launch_dense_select_fused(da, st) : launch_dense_select(da, st));
+        // two-pass: piece histograms, plan, emission; single pass: sample, bound, fused pass, plan,
+        // compaction, flagged list, fallback emission
+        x->launches += fused ? 7 : 3;
         if (ev) CUDA_TRY(cudaEventRecord(ev[1], st));
         return;
     }

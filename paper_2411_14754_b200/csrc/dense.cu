@@ -96,7 +96,7 @@ __device__ void build_masks(const DenseArgs& a, uint32_t* M, uint64_t q0, uint32
     for (uint32_t i = tid; i < words; i += kDT) M[i] = 0;
     __syncthreads();
     for (uint32_t j = warp; j < nqb; j += kDW) {
-        const uint64_t q = q0 + j;
+        const uint64_t q = a.qmap ? a.qmap[q0 + j] : q0 + j;
         for (uint32_t s = 0; s < a.ns; ++s) {
             const uint64_t t = q * a.ns + s;
             const uint32_t cnt = a.cells_off ? static_cast<uint32_t>(a.cells_off[t + 1] - a.cells_off[t]) : a.ncells[t];
@@ -162,10 +162,12 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_hist_kernel(DenseArgs a
     const uint64_t q0 = uint64_t(blockIdx.x) * 32 * W;
     const uint32_t nqb = static_cast<uint32_t>(min_u64(32 * W, a.nq - q0));
     build_masks<kDT, W>(a, M, q0, nqb);
-    const uint32_t piece = blockIdx.y * kDW + warp;
-    if (piece >= a.P) return;
-    const uint64_t lo = uint64_t(piece) * a.WP;
+    const uint32_t row = blockIdx.y * kDW + warp;  // histogram row
+    if (row >= a.P) return;
+    const uint64_t lo = uint64_t(row) * (a.pstride ? a.pstride : 1u) * a.WP;  // its piece (a sample when pstride > 1)
+    if (lo >= a.n) return;
     const uint64_t hi = min_u64(a.n, lo + a.WP);
+    const uint32_t piece = row;
     uint32_t cnt[W][8];
 #pragma unroll
     for (uint32_t w = 0; w < W; ++w) {
@@ -239,6 +241,8 @@ __global__ void __launch_bounds__(256) dense_plan_kernel(DenseArgs a) {
         if (static_cast<uint32_t>(t) == T + 1) gtT = tot[t - 1];
     }
     const uint64_t need = a.m - gtT;
+    const uint32_t Lq = a.qflag ? a.L[q] : 0u;
+    bool bad = a.qflag && (Lq == 0 || T < Lq);  // the superset (score >= L) must cover score >= T
     uint64_t ties_run = 0, out_run = 0;
     for (uint32_t p0 = 0; p0 < a.P; p0 += 32) {
         const uint32_t p = p0 + lane;
@@ -270,11 +274,16 @@ __global__ void __launch_bounds__(256) dense_plan_kernel(DenseArgs a) {
         if (p < a.P) {
             a.quota[q * a.P + p] = quota;
             a.base[q * a.P + p] = static_cast<uint32_t>(out_run + ox - take);
+            if (a.qflag && take && a.scnt[q * a.P + p] > a.C) bad = true;  // a needed slot overflowed
         }
         ties_run += tsum;
         out_run += osum;
     }
     if (lane == 0) a.T[q] = T;
+    if (a.qflag) {
+        bad = __any_sync(kFull, bad);
+        if (lane == 0) a.qflag[q] = bad ? 1u : 0u;
+    }
 }
 
 // K3: re-score each piece; lane = query emits score > T and the first quota ties (id order).
@@ -284,7 +293,9 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_emit_kernel(DenseArgs a
     extern __shared__ uint32_t M[];
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const uint64_t q0 = uint64_t(blockIdx.x) * 32 * W;
-    const uint32_t nqb = static_cast<uint32_t>(min_u64(32 * W, a.nq - q0));
+    const uint64_t nvalid = a.qmap ? *a.nmap : a.nq;  // fallback run: only the listed queries
+    if (q0 >= nvalid) return;
+    const uint32_t nqb = static_cast<uint32_t>(min_u64(32 * W, nvalid - q0));
     build_masks<kDT, W>(a, M, q0, nqb);
     const uint32_t piece = blockIdx.y * kDW + warp;
     if (piece >= a.P) return;
@@ -295,8 +306,8 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_emit_kernel(DenseArgs a
     uint32_t* out[W];
 #pragma unroll
     for (uint32_t w = 0; w < W; ++w) {
-        const uint64_t q = q0 + 32 * w + lane;
         mine[w] = 32 * w + lane < nqb;
+        const uint64_t q = !mine[w] ? 0 : a.qmap ? a.qmap[q0 + 32 * w + lane] : q0 + 32 * w + lane;
         T[w] = mine[w] ? a.T[q] : 0u;
         quota[w] = mine[w] ? a.quota[q * a.P + piece] : 0u;
         pos[w] = mine[w] ? a.base[q * a.P + piece] : 0u;
@@ -329,6 +340,139 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_emit_kernel(DenseArgs a
             }
         }
     }
+}
+
+// K0 -> L: per query, the largest t whose sampled #(score >= t), scaled to n, reaches m (0 if none).
+__global__ void __launch_bounds__(256) dense_bound_kernel(DenseArgs a) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t q = uint64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (q >= a.nq) return;
+    const uint4* h = reinterpret_cast<const uint4*>(a.hsample) + q * a.Ps;
+    uint32_t tot[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (uint32_t p = lane; p < a.Ps; p += 32) {
+        const uint4 v = h[p];
+#pragma unroll
+        for (uint32_t t = 1; t <= 8; ++t) tot[t - 1] += level(v, t);
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tot[t] += __shfl_xor_sync(kFull, tot[t], o);
+    }
+    uint64_t sampled = 0;  // points the sample scanned
+    for (uint32_t p = 0; p < a.Ps; ++p) {
+        const uint64_t lo = uint64_t(p) * a.pstride * a.WP;
+        if (lo < a.n) sampled += min_u64(a.WP, a.n - lo);
+    }
+    uint32_t L = 0;
+#pragma unroll
+    for (int t = 8; t >= 1; --t) {
+        if (L == 0 && static_cast<uint32_t>(t) <= a.ns && sampled &&
+            static_cast<double>(tot[t - 1]) * static_cast<double>(a.n) / static_cast<double>(sampled) >=
+                static_cast<double>(a.m))
+            L = t;
+    }
+    if (lane == 0) a.L[q] = L;
+}
+
+// K3': one pass — the piece histograms (as K1) plus, per (query, piece), every point with
+// score >= L[q] in id order into its slot (in-piece offset << 4 | score; count may exceed C).
+template <uint32_t kDT, uint32_t W>
+__global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs a) {
+    constexpr uint32_t kDW = kDT / 32;
+    extern __shared__ uint32_t M[];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint64_t q0 = uint64_t(blockIdx.x) * 32 * W;
+    const uint32_t nqb = static_cast<uint32_t>(min_u64(32 * W, a.nq - q0));
+    build_masks<kDT, W>(a, M, q0, nqb);
+    const uint32_t piece = blockIdx.y * kDW + warp;
+    if (piece >= a.P) return;
+    const uint64_t lo = uint64_t(piece) * a.WP;
+    const uint64_t hi = min_u64(a.n, lo + a.WP);
+    uint32_t cnt[W][8], Lw[W], sc[W];
+    uint16_t* slot[W];
+#pragma unroll
+    for (uint32_t w = 0; w < W; ++w) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) cnt[w][t] = 0;
+        const uint64_t q = q0 + 32 * w + lane;
+        const bool mine = 32 * w + lane < nqb;
+        Lw[w] = mine ? a.L[q] : 0u;  // 0: this query falls back, emit nothing
+        sc[w] = 0;
+        slot[w] = a.slots + ((mine ? q : 0) * a.P + piece) * a.C;
+    }
+    const Xpose xp(lane);
+    for (uint64_t t0 = lo; t0 < hi; t0 += 32) {
+        uint32_t B[W][4];
+        score_tile<W>(a, M, t0, hi, xp, B, lane);
+        const uint32_t vmask = hi - t0 >= 32 ? kFull : ((1u << (hi - t0)) - 1u);
+#pragma unroll
+        for (uint32_t w = 0; w < W; ++w) {
+            const uint32_t B0 = B[w][0], B1 = B[w][1], B2 = B[w][2], B3 = B[w][3];
+            const uint32_t g8 = B3, g4 = B3 | B2, g2 = g4 | B1, g1 = g2 | B0;
+            const uint32_t g6 = B3 | (B2 & B1), g5 = B3 | (B2 & (B1 | B0)), g7 = B3 | (B2 & B1 & B0);
+            const uint32_t g3 = g4 | (B1 & B0);
+            cnt[w][0] += __popc(g1);
+            cnt[w][1] += __popc(g2);
+            cnt[w][2] += __popc(g3);
+            cnt[w][3] += __popc(g4);
+            cnt[w][4] += __popc(g5);
+            cnt[w][5] += __popc(g6);
+            cnt[w][6] += __popc(g7);
+            cnt[w][7] += __popc(g8);
+            if (Lw[w]) {
+                const uint32_t L = Lw[w];  // the level masks above, selected by L (score >= L)
+                uint32_t sel = L == 1 ? g1 : L == 2 ? g2 : L == 3 ? g3 : L == 4 ? g4 : L == 5 ? g5 : L == 6 ? g6 : L == 7 ? g7 : g8;
+                sel &= vmask;
+                while (sel) {
+                    const uint32_t b = __ffs(sel) - 1;
+                    sel &= sel - 1;
+                    const uint32_t score = ((B0 >> b) & 1u) | (((B1 >> b) & 1u) << 1) | (((B2 >> b) & 1u) << 2) |
+                                           (((B3 >> b) & 1u) << 3);
+                    if (sc[w] < a.C) slot[w][sc[w]] = static_cast<uint16_t>(((t0 - lo + b) << 4) | score);
+                    ++sc[w];
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (uint32_t w = 0; w < W; ++w) {
+        if (32 * w + lane < nqb) {
+            const uint64_t q = q0 + 32 * w + lane;
+            uint4 v;
+            v.x = cnt[w][0] | (cnt[w][1] << 16);
+            v.y = cnt[w][2] | (cnt[w][3] << 16);
+            v.z = cnt[w][4] | (cnt[w][5] << 16);
+            v.w = cnt[w][6] | (cnt[w][7] << 16);
+            reinterpret_cast<uint4*>(a.hist)[q * a.P + piece] = v;
+            a.scnt[q * a.P + piece] = static_cast<uint16_t>(min(sc[w], 65535u));
+        }
+    }
+}
+
+// K4: thread per (query, piece): score > T, then the first quota ties, from the slot (id order).
+__global__ void __launch_bounds__(256) dense_compact_kernel(DenseArgs a) {
+    const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (i >= a.nq * a.P) return;
+    const uint64_t q = i / a.P;
+    const uint32_t p = static_cast<uint32_t>(i % a.P);
+    if (a.qflag[q]) return;
+    const uint32_t T = a.T[q], quota = a.quota[i];
+    uint32_t pos = a.base[i], ties = 0;
+    const uint32_t cnt = min(static_cast<uint32_t>(a.scnt[i]), a.C);
+    const uint16_t* sl = a.slots + i * a.C;
+    uint32_t* out = a.cands + q * a.m;
+    const uint32_t pbase = p * a.WP;
+    for (uint32_t e = 0; e < cnt; ++e) {
+        const uint32_t v = sl[e];
+        const uint32_t score = v & 15u;
+        if (score > T || (score == T && ties++ < quota)) __stcs(out + pos++, pbase + (v >> 4));
+    }
+}
+
+__global__ void dense_flag_list_kernel(DenseArgs a) {  // qmap <- flagged queries (any order)
+    const uint64_t q = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (q < a.nq && a.qflag[q]) a.qmap[atomicAdd(a.nmap, 1u)] = static_cast<uint32_t>(q);
 }
 
 __global__ void dense_codes_fill_kernel(uint16_t* codes, uint64_t count, uint16_t none) {
@@ -417,6 +561,47 @@ cudaError_t launch_dense_hist_rows(const DenseArgs& a, uint32_t* out, cudaStream
     if (total == 0) return cudaSuccess;
     dense_rows_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(a, out);
     return cudaGetLastError();
+}
+
+template <uint32_t kDT, uint32_t W>
+static cudaError_t launch_fused_t(const DenseArgs& a, size_t smem, cudaStream_t st) {
+    cudaError_t e = cudaFuncSetAttribute(dense_fused_kernel<kDT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    constexpr uint32_t kDW = kDT / 32;
+    const dim3 grid(static_cast<unsigned>((a.nq + 32 * W - 1) / (32 * W)), (a.P + kDW - 1) / kDW);
+    dense_fused_kernel<kDT, W><<<grid, kDT, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dense_select_fused(const DenseArgs& args, cudaStream_t st) {
+    if (args.nq == 0) return cudaSuccess;
+    DenseArgs a = args;  // every pass but the fallback emission sees the queries unmapped
+    a.qmap = nullptr;
+    // K0: histograms of every pstride-th piece, then the speculative bound L per query
+    DenseArgs s0 = a;
+    s0.P = a.Ps;
+    s0.hist = a.hsample;
+    cudaError_t e = launch_dense_hist(s0, st);
+    if (e != cudaSuccess) return e;
+    dense_bound_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(a);
+    // K3': histograms + supersets in one pass
+    const Shape sh = dense_shape(a);
+    if (sh.words == 2) e = launch_fused_t<1024, 2>(a, sh.smem, st);
+    else e = sh.threads == 512 ? launch_fused_t<512, 1>(a, sh.smem, st) : launch_fused_t<1024, 1>(a, sh.smem, st);
+    if (e != cudaSuccess) return e;
+    // plan (+ fallback flags), compaction, exact emission for flagged query blocks
+    dense_plan_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(a);
+    dense_compact_kernel<<<static_cast<unsigned>((a.nq * a.P + 255) / 256), 256, 0, st>>>(a);
+    e = cudaMemsetAsync(args.nmap, 0, 4, st);
+    if (e != cudaSuccess) return e;
+    dense_flag_list_kernel<<<static_cast<unsigned>((a.nq + 255) / 256), 256, 0, st>>>(args);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    // exact two-pass emission for the flagged queries only, 32*W per block via qmap; blocks past
+    // the flagged count exit at once
+    DenseArgs fb = args;
+    fb.qflag = nullptr;
+    return launch_dense_emit(fb, st);
 }
 
 cudaError_t launch_dense_select(const DenseArgs& a, cudaStream_t st) {

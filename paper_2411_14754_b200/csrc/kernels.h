@@ -94,12 +94,27 @@ struct DenseArgs {
     uint32_t* quota;           // nq x P
     uint32_t* base;            // nq x P
     uint32_t* cands;           // nq x m
+    // single-pass (fused) select: a speculative lower bound L on T per query, a superset slot of
+    // C entries (in-piece offset << 4 | score, id order) per (query, piece), and a fallback flag
+    uint32_t pstride;          // K1 over a sample: hist row j scans piece j * pstride (0 = 1)
+    uint16_t* hsample;         // nq x Ps x 8 sampled histograms (K0)
+    uint32_t Ps;               // sampled pieces
+    uint32_t* L;               // nq
+    uint16_t* slots;           // nq x P x C
+    uint16_t* scnt;            // nq x P superset sizes (> C: overflow)
+    uint32_t* qflag;           // nq: 1 = fall back to the exact two-pass emission for this query
+    uint32_t C;
+    uint32_t* qmap;            // fallback emission: block-local query j -> query qmap[q0 + j]
+    uint32_t* nmap;            // device count of qmap entries
 };
 bool dense_supported(uint32_t ns, uint32_t K);
 size_t dense_smem(uint32_t ns, uint32_t K);
 cudaError_t launch_dense_codes(const uint32_t* ids, const uint32_t* cell_off, uint64_t n, uint32_t ns, uint32_t K,
                                uint16_t* codes, cudaStream_t st);
 cudaError_t launch_dense_select(const DenseArgs& a, cudaStream_t st);  // hist + plan + emit
+// single pass: K0 sample -> L estimate -> fused hist + superset -> plan + checks -> compaction ->
+// exact emission for the flagged query blocks (rare); needs hsample/L/slots/scnt/qflag/C
+cudaError_t launch_dense_select_fused(const DenseArgs& a, cudaStream_t st);
 // Shard protocol pieces: K1 alone (+ its histograms as [nq][P][N_s + 2] u32 rows with the
 // piece length first, the exchange format) and K3 alone with the globally planned T/quota/base.
 cudaError_t launch_dense_hist(const DenseArgs& a, cudaStream_t st);
