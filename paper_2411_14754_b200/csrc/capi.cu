@@ -128,7 +128,9 @@ struct suco_gpu_index {
         DevBuf<uint32_t> cells, ncells, cands, out_ids, all_id;
         DevBuf<uint16_t> dhist;               // dense select: nq x P x 8
         DevBuf<uint32_t> dT, dquota, dbase;   // dense select plan
-        DevBuf<uint16_t> dsample, dslots, dscnt;  // single-pass select: sampled hist, supersets, sizes
+        DevBuf<uint16_t> dsample, dscnt;          // single-pass select: sampled hist, record counts
+        DevBuf<uint2> dslots;                     // single-pass select: tile records
+        DevBuf<uint8_t> dstile;                   // single-pass select: record tiles
         DevBuf<uint32_t> dL, dflag;               // single-pass select: bound, fallback flags
         DevBuf<double> out_d, all_d;
         cudaEvent_t trav = nullptr, sel = nullptr, rr = nullptr;
@@ -361,7 +363,7 @@ uint64_t tile_size(const suco_gpu_index* x, uint64_t nq, uint64_t m, uint32_t k)
     const uint64_t ns = x->host.layout.ns;
     const uint64_t pieces = (x->host.n + 2047) / 2048;  // dense select scratch: hist (16 B) + quota/base per piece
     const uint64_t per = ns * x->K * 4 + ns * 4 + m * 4 + (k > 32 ? m * 12 : 0) + uint64_t(x->host.d) * 4 + k * 12 +
-                         (x->dense ? pieces * (24 + 130) + pieces / 16 * 16 + 16 : 0);  // + single-pass supersets
+                         (x->dense ? pieces * (24 + 64 * 9 + 2) + pieces / 16 * 16 + 16 : 0);  // + tile records
     const uint64_t budget = 4ull << 30;
     return std::max<uint64_t>(1, std::min<uint64_t>(nq, budget / per));
 }
@@ -454,9 +456,11 @@ void stage_select(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nt, uint
         if (fused) {
             da.pstride = 16;
             da.Ps = (da.P + da.pstride - 1) / da.pstride;
-            da.C = 64;
+            da.C = kDensePiece / 32;  // records per (query, piece): one per tile at most, never overflows
             sl.dsample.reserve(nt * da.Ps * 8);
             sl.dslots.reserve(nt * da.P * da.C);
+            sl.dstile.reserve(nt * da.P * da.C);
+            da.stile = sl.dstile.p;
             sl.dscnt.reserve(nt * da.P);
             sl.dL.reserve(nt);
             sl.dflag.reserve(2 * nt + 1);  // flags, flagged list, its count

@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(256) dense_plan_kernel(DenseArgs a) {
     }
     const uint64_t need = a.m - gtT;
     const uint32_t Lq = a.qflag ? a.L[q] : 0u;
-    bool bad = a.qflag && (Lq == 0 || T < Lq);  // the superset (score >= L) must cover score >= T
+    bool bad = a.qflag && (Lq == 0 || T != Lq);  // the records split score >= L into > L and == L
     uint64_t ties_run = 0, out_run = 0;
     for (uint32_t p0 = 0; p0 < a.P; p0 += 32) {
         const uint32_t p = p0 + lane;
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(256) dense_plan_kernel(DenseArgs a) {
         if (p < a.P) {
             a.quota[q * a.P + p] = quota;
             a.base[q * a.P + p] = static_cast<uint32_t>(out_run + ox - take);
-            if (a.qflag && take && a.scnt[q * a.P + p] > a.C) bad = true;  // a needed slot overflowed
+
         }
         ties_run += tsum;
         out_run += osum;
@@ -389,47 +389,40 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs 
     if (piece >= a.P) return;
     const uint64_t lo = uint64_t(piece) * a.WP;
     const uint64_t hi = min_u64(a.n, lo + a.WP);
-    uint32_t cnt[W][8], Lw[W], sc[W];
-    uint16_t* slot[W];
+    // level counters two per register (a piece holds <= 2048 points: 16-bit fields)
+    uint32_t c01[W], c23[W], c45[W], c67[W], Lw[W], sc[W], rec[W];
 #pragma unroll
     for (uint32_t w = 0; w < W; ++w) {
-#pragma unroll
-        for (int t = 0; t < 8; ++t) cnt[w][t] = 0;
+        c01[w] = c23[w] = c45[w] = c67[w] = 0;
         const uint64_t q = q0 + 32 * w + lane;
         const bool mine = 32 * w + lane < nqb;
         Lw[w] = mine ? a.L[q] : 0u;  // 0: this query falls back, emit nothing
         sc[w] = 0;
-        slot[w] = a.slots + ((mine ? q : 0) * a.P + piece) * a.C;
+        rec[w] = static_cast<uint32_t>((mine ? q : 0) * a.C * a.P + piece);  // record e at + e*P (< 2^32)
     }
     const Xpose xp(lane);
     for (uint64_t t0 = lo; t0 < hi; t0 += 32) {
         uint32_t B[W][4];
         score_tile<W>(a, M, t0, hi, xp, B, lane);
-        const uint32_t vmask = hi - t0 >= 32 ? kFull : ((1u << (hi - t0)) - 1u);
 #pragma unroll
         for (uint32_t w = 0; w < W; ++w) {
             const uint32_t B0 = B[w][0], B1 = B[w][1], B2 = B[w][2], B3 = B[w][3];
             const uint32_t g8 = B3, g4 = B3 | B2, g2 = g4 | B1, g1 = g2 | B0;
             const uint32_t g6 = B3 | (B2 & B1), g5 = B3 | (B2 & (B1 | B0)), g7 = B3 | (B2 & B1 & B0);
             const uint32_t g3 = g4 | (B1 & B0);
-            cnt[w][0] += __popc(g1);
-            cnt[w][1] += __popc(g2);
-            cnt[w][2] += __popc(g3);
-            cnt[w][3] += __popc(g4);
-            cnt[w][4] += __popc(g5);
-            cnt[w][5] += __popc(g6);
-            cnt[w][6] += __popc(g7);
-            cnt[w][7] += __popc(g8);
+            c01[w] += __popc(g1) | (__popc(g2) << 16);
+            c23[w] += __popc(g3) | (__popc(g4) << 16);
+            c45[w] += __popc(g5) | (__popc(g6) << 16);
+            c67[w] += __popc(g7) | (__popc(g8) << 16);
             if (Lw[w]) {
-                const uint32_t L = Lw[w];  // the level masks above, selected by L (score >= L)
-                uint32_t sel = L == 1 ? g1 : L == 2 ? g2 : L == 3 ? g3 : L == 4 ? g4 : L == 5 ? g5 : L == 6 ? g6 : L == 7 ? g7 : g8;
-                sel &= vmask;
-                while (sel) {
-                    const uint32_t b = __ffs(sel) - 1;
-                    sel &= sel - 1;
-                    const uint32_t score = ((B0 >> b) & 1u) | (((B1 >> b) & 1u) << 1) | (((B2 >> b) & 1u) << 2) |
-                                           (((B3 >> b) & 1u) << 3);
-                    if (sc[w] < a.C) slot[w][sc[w]] = static_cast<uint16_t>(((t0 - lo + b) << 4) | score);
+                // the level masks above, selected by L: score >= L and score >= L + 1 (points past
+                // the piece end score 0 and never appear); one record per non-empty tile
+                const uint32_t L = Lw[w];
+                const uint32_t ge0 = L == 1 ? g1 : L == 2 ? g2 : L == 3 ? g3 : L == 4 ? g4 : L == 5 ? g5 : L == 6 ? g6 : L == 7 ? g7 : g8;
+                const uint32_t ge1 = L == 1 ? g2 : L == 2 ? g3 : L == 3 ? g4 : L == 4 ? g5 : L == 5 ? g6 : L == 6 ? g7 : L == 7 ? g8 : 0u;
+                if (ge0) {
+                    a.slots[rec[w] + sc[w] * a.P] = make_uint2(ge0, ge1);
+                    a.stile[rec[w] + sc[w] * a.P] = static_cast<uint8_t>((t0 - lo) >> 5);
                     ++sc[w];
                 }
             }
@@ -439,34 +432,42 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs 
     for (uint32_t w = 0; w < W; ++w) {
         if (32 * w + lane < nqb) {
             const uint64_t q = q0 + 32 * w + lane;
-            uint4 v;
-            v.x = cnt[w][0] | (cnt[w][1] << 16);
-            v.y = cnt[w][2] | (cnt[w][3] << 16);
-            v.z = cnt[w][4] | (cnt[w][5] << 16);
-            v.w = cnt[w][6] | (cnt[w][7] << 16);
-            reinterpret_cast<uint4*>(a.hist)[q * a.P + piece] = v;
-            a.scnt[q * a.P + piece] = static_cast<uint16_t>(min(sc[w], 65535u));
+            reinterpret_cast<uint4*>(a.hist)[q * a.P + piece] = make_uint4(c01[w], c23[w], c45[w], c67[w]);
+            a.scnt[q * a.P + piece] = static_cast<uint16_t>(sc[w]);
         }
     }
 }
 
-// K4: thread per (query, piece): score > T, then the first quota ties, from the slot (id order).
+// K4: thread per (query, piece), T == L: every score > T (the L+1 masks), then the first quota
+// ties (score == T) in id order, expanded from the piece's tile records. Records are laid out
+// [query][record][piece], so neighbouring threads (pieces) read neighbouring words.
 __global__ void __launch_bounds__(256) dense_compact_kernel(DenseArgs a) {
     const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
     if (i >= a.nq * a.P) return;
     const uint64_t q = i / a.P;
     const uint32_t p = static_cast<uint32_t>(i % a.P);
     if (a.qflag[q]) return;
-    const uint32_t T = a.T[q], quota = a.quota[i];
-    uint32_t pos = a.base[i], ties = 0;
-    const uint32_t cnt = min(static_cast<uint32_t>(a.scnt[i]), a.C);
-    const uint16_t* sl = a.slots + i * a.C;
+    uint32_t quota = a.quota[i];
+    uint32_t pos = a.base[i];
+    const uint32_t cnt = a.scnt[i];
+    const uint64_t r0 = q * a.C * a.P + p;  // record e at r0 + e * P
     uint32_t* out = a.cands + q * a.m;
     const uint32_t pbase = p * a.WP;
     for (uint32_t e = 0; e < cnt; ++e) {
-        const uint32_t v = sl[e];
-        const uint32_t score = v & 15u;
-        if (score > T || (score == T && ties++ < quota)) __stcs(out + pos++, pbase + (v >> 4));
+        const uint2 r = a.slots[r0 + uint64_t(e) * a.P];
+        const uint32_t tb = pbase + (static_cast<uint32_t>(a.stile[r0 + uint64_t(e) * a.P]) << 5);
+        uint32_t take = r.y;  // score > T
+        uint32_t ties = r.x & ~r.y;
+        while (ties && quota) {  // first ties in id order
+            take |= ties & (0u - ties);
+            ties &= ties - 1;
+            --quota;
+        }
+        while (take) {
+            const uint32_t b = __ffs(take) - 1;
+            take &= take - 1;
+            __stcs(out + pos++, tb + b);
+        }
     }
 }
 
@@ -518,7 +519,9 @@ struct Shape {
 static Shape dense_shape(const DenseArgs& a) {
     const size_t smem1 = dense_smem(a.ns, a.K);
     const char* wv = std::getenv("SUCO_DENSE_WORDS");
-    const bool allow2 = !(wv && std::atoi(wv) == 1);
+    // the single-pass pipeline measured faster with 32-query blocks (3.75 vs 3.89 ms at cfg2),
+    // the two-pass one with 64-query blocks (5.04 vs 5.52 ms)
+    const bool allow2 = wv ? std::atoi(wv) == 2 : a.slots == nullptr;
     if (allow2 && 2 * smem1 <= 200 * 1024) return {1024, 2, 2 * smem1};
     return {smem1 <= 110 * 1024 ? 512u : 1024u, 1, smem1};
 }

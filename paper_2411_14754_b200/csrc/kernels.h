@@ -100,8 +100,9 @@ struct DenseArgs {
     uint16_t* hsample;         // nq x Ps x 8 sampled histograms (K0)
     uint32_t Ps;               // sampled pieces
     uint32_t* L;               // nq
-    uint16_t* slots;           // nq x P x C
-    uint16_t* scnt;            // nq x P superset sizes (> C: overflow)
+    uint2* slots;              // nq x P x C records (score >= L mask, score >= L+1 mask) of non-empty tiles
+    uint8_t* stile;            // nq x P x C: tile of each record
+    uint16_t* scnt;            // nq x P records per (query, piece)
     uint32_t* qflag;           // nq: 1 = fall back to the exact two-pass emission for this query
     uint32_t C;
     uint32_t* qmap;            // fallback emission: block-local query j -> query qmap[q0 + j]
