@@ -131,7 +131,7 @@ struct suco_gpu_index {
         DevBuf<uint16_t> dsample, dscnt;          // single-pass select: sampled hist, record counts
         DevBuf<uint2> dslots;                     // single-pass select: tile records
         DevBuf<uint8_t> dstile;                   // single-pass select: record tiles
-        DevBuf<uint32_t> dL, dflag;               // single-pass select: bound, fallback flags
+        DevBuf<uint32_t> dL, dflag, dh2;          // single-pass select: bound, fallback flags, two-level counts
         DevBuf<double> out_d, all_d;
         cudaEvent_t trav = nullptr, sel = nullptr, rr = nullptr;
     };
@@ -463,6 +463,8 @@ void stage_select(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nt, uint
             da.stile = sl.dstile.p;
             sl.dscnt.reserve(nt * da.P);
             sl.dL.reserve(nt);
+            sl.dh2.reserve(nt * da.P);
+            da.h2 = sl.dh2.p;
             sl.dflag.reserve(2 * nt + 1);  // flags, flagged list, its count
             da.hsample = sl.dsample.p;
             da.qmap = sl.dflag.p + nt;
@@ -475,8 +477,8 @@ void stage_select(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nt, uint
         if (ev) CUDA_TRY(cudaEventRecord(ev[0], st));
         CUDA_TRY(fused ? launch_dense_select_fused(da, st) : launch_dense_select(da, st));
         // two-pass: piece histograms, plan, emission; single pass: sample, bound, fused pass, plan,
-        // compaction, flagged list, fallback emission
-        x->launches += fused ? 7 : 3;
+        // compaction, flagged list, fallback histograms, plan, emission
+        x->launches += fused ? 9 : 3;
         if (ev) CUDA_TRY(cudaEventRecord(ev[1], st));
         return;
     }

@@ -160,7 +160,9 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_hist_kernel(DenseArgs a
     extern __shared__ uint32_t M[];
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const uint64_t q0 = uint64_t(blockIdx.x) * 32 * W;
-    const uint32_t nqb = static_cast<uint32_t>(min_u64(32 * W, a.nq - q0));
+    const uint64_t nvalid = a.qmap ? *a.nmap : a.nq;  // fallback run: only the listed queries
+    if (q0 >= nvalid) return;
+    const uint32_t nqb = static_cast<uint32_t>(min_u64(32 * W, nvalid - q0));
     build_masks<kDT, W>(a, M, q0, nqb);
     const uint32_t row = blockIdx.y * kDW + warp;  // histogram row
     if (row >= a.P) return;
@@ -203,7 +205,8 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_hist_kernel(DenseArgs a
             v.y = cnt[w][2] | (cnt[w][3] << 16);
             v.z = cnt[w][4] | (cnt[w][5] << 16);
             v.w = cnt[w][6] | (cnt[w][7] << 16);
-            reinterpret_cast<uint4*>(a.hist)[(q0 + 32 * w + lane) * a.P + piece] = v;
+            const uint64_t q = a.qmap ? a.qmap[q0 + 32 * w + lane] : q0 + 32 * w + lane;
+            reinterpret_cast<uint4*>(a.hist)[q * a.P + piece] = v;
         }
     }
 }
@@ -216,8 +219,9 @@ __device__ __forceinline__ uint32_t level(const uint4& v, uint32_t t) {  // #sco
 // K2: warp per query — T, need, per-piece tie quota (id order) and output offset.
 __global__ void __launch_bounds__(256) dense_plan_kernel(DenseArgs a) {
     const uint32_t lane = threadIdx.x & 31u;
-    const uint64_t q = uint64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
-    if (q >= a.nq) return;
+    const uint64_t qi = uint64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (qi >= (a.qmap ? *a.nmap : a.nq)) return;
+    const uint64_t q = a.qmap ? a.qmap[qi] : qi;
     const uint4* h = reinterpret_cast<const uint4*>(a.hist) + q * a.P;
     uint32_t tot[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (uint32_t p = lane; p < a.P; p += 32) {
@@ -241,8 +245,6 @@ __global__ void __launch_bounds__(256) dense_plan_kernel(DenseArgs a) {
         if (static_cast<uint32_t>(t) == T + 1) gtT = tot[t - 1];
     }
     const uint64_t need = a.m - gtT;
-    const uint32_t Lq = a.qflag ? a.L[q] : 0u;
-    bool bad = a.qflag && (Lq == 0 || T != Lq);  // the records split score >= L into > L and == L
     uint64_t ties_run = 0, out_run = 0;
     for (uint32_t p0 = 0; p0 < a.P; p0 += 32) {
         const uint32_t p = p0 + lane;
@@ -280,10 +282,65 @@ __global__ void __launch_bounds__(256) dense_plan_kernel(DenseArgs a) {
         out_run += osum;
     }
     if (lane == 0) a.T[q] = T;
-    if (a.qflag) {
-        bad = __any_sync(kFull, bad);
-        if (lane == 0) a.qflag[q] = bad ? 1u : 0u;
+}
+
+// Single-pass plan: T == L exactly when #(score >= L) >= m > #(score >= L+1); then the quotas and
+// offsets come from those two levels; otherwise the query is flagged for the exact fallback.
+__global__ void __launch_bounds__(256) dense_plan_fused_kernel(DenseArgs a) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t q = uint64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (q >= a.nq) return;
+    const uint32_t* h = a.h2 + q * a.P;
+    uint64_t geL = 0, geL1 = 0;
+    for (uint32_t p = lane; p < a.P; p += 32) {
+        const uint32_t v = h[p];
+        geL += v & 0xffffu;
+        geL1 += v >> 16;
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        geL += __shfl_xor_sync(kFull, geL, o);
+        geL1 += __shfl_xor_sync(kFull, geL1, o);
+    }
+    const uint32_t L = a.L[q];
+    const bool ok = L >= 1 && geL >= a.m && geL1 < a.m;
+    if (lane == 0) a.qflag[q] = ok ? 0u : 1u;
+    if (!ok) return;
+    const uint64_t need = a.m - geL1;
+    uint64_t ties_run = 0, out_run = 0;
+    for (uint32_t p0 = 0; p0 < a.P; p0 += 32) {
+        const uint32_t p = p0 + lane;
+        uint32_t ties = 0, gt = 0;
+        if (p < a.P) {
+            const uint32_t v = h[p];
+            gt = v >> 16;
+            ties = (v & 0xffffu) - gt;
+        }
+        uint32_t tx = ties;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, tx, o);
+            if (lane >= static_cast<uint32_t>(o)) tx += y;
+        }
+        const uint32_t tsum = __shfl_sync(kFull, tx, 31);
+        const uint64_t before = ties_run + tx - ties;
+        const uint32_t quota = before >= need ? 0u : static_cast<uint32_t>(min_u64(ties, need - before));
+        const uint32_t take = gt + quota;
+        uint32_t ox = take;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, ox, o);
+            if (lane >= static_cast<uint32_t>(o)) ox += y;
+        }
+        const uint32_t osum = __shfl_sync(kFull, ox, 31);
+        if (p < a.P) {
+            a.quota[q * a.P + p] = quota;
+            a.base[q * a.P + p] = static_cast<uint32_t>(out_run + ox - take);
+        }
+        ties_run += tsum;
+        out_run += osum;
+    }
+    if (lane == 0) a.T[q] = L;
 }
 
 // K3: re-score each piece; lane = query emits score > T and the first quota ties (id order).
@@ -389,14 +446,21 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs 
     if (piece >= a.P) return;
     const uint64_t lo = uint64_t(piece) * a.WP;
     const uint64_t hi = min_u64(a.n, lo + a.WP);
-    // level counters two per register (a piece holds <= 2048 points: 16-bit fields)
-    uint32_t c01[W], c23[W], c45[W], c67[W], Lw[W], sc[W], rec[W];
+    // per lane = query: the bits of L as masks for one bit-sliced comparison per tile, which gives
+    // score > L and score == L together; counts #(score >= L) | #(score >= L+1) << 16
+    uint32_t tm0[W], tm1[W], tm2[W], tm3[W], cnt[W], sc[W], rec[W];
+    bool live[W];
 #pragma unroll
     for (uint32_t w = 0; w < W; ++w) {
-        c01[w] = c23[w] = c45[w] = c67[w] = 0;
         const uint64_t q = q0 + 32 * w + lane;
         const bool mine = 32 * w + lane < nqb;
-        Lw[w] = mine ? a.L[q] : 0u;  // 0: this query falls back, emit nothing
+        const uint32_t L = mine ? a.L[q] : 0u;  // 0: this query falls back, nothing to record
+        live[w] = L != 0;
+        tm0[w] = (L & 1u) ? kFull : 0u;
+        tm1[w] = (L & 2u) ? kFull : 0u;
+        tm2[w] = (L & 4u) ? kFull : 0u;
+        tm3[w] = (L & 8u) ? kFull : 0u;
+        cnt[w] = 0;
         sc[w] = 0;
         rec[w] = static_cast<uint32_t>((mine ? q : 0) * a.C * a.P + piece);  // record e at + e*P (< 2^32)
     }
@@ -406,25 +470,21 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs 
         score_tile<W>(a, M, t0, hi, xp, B, lane);
 #pragma unroll
         for (uint32_t w = 0; w < W; ++w) {
-            const uint32_t B0 = B[w][0], B1 = B[w][1], B2 = B[w][2], B3 = B[w][3];
-            const uint32_t g8 = B3, g4 = B3 | B2, g2 = g4 | B1, g1 = g2 | B0;
-            const uint32_t g6 = B3 | (B2 & B1), g5 = B3 | (B2 & (B1 | B0)), g7 = B3 | (B2 & B1 & B0);
-            const uint32_t g3 = g4 | (B1 & B0);
-            c01[w] += __popc(g1) | (__popc(g2) << 16);
-            c23[w] += __popc(g3) | (__popc(g4) << 16);
-            c45[w] += __popc(g5) | (__popc(g6) << 16);
-            c67[w] += __popc(g7) | (__popc(g8) << 16);
-            if (Lw[w]) {
-                // the level masks above, selected by L: score >= L and score >= L + 1 (points past
-                // the piece end score 0 and never appear); one record per non-empty tile
-                const uint32_t L = Lw[w];
-                const uint32_t ge0 = L == 1 ? g1 : L == 2 ? g2 : L == 3 ? g3 : L == 4 ? g4 : L == 5 ? g5 : L == 6 ? g6 : L == 7 ? g7 : g8;
-                const uint32_t ge1 = L == 1 ? g2 : L == 2 ? g3 : L == 3 ? g4 : L == 4 ? g5 : L == 5 ? g6 : L == 6 ? g7 : L == 7 ? g8 : 0u;
-                if (ge0) {
-                    a.slots[rec[w] + sc[w] * a.P] = make_uint2(ge0, ge1);
-                    a.stile[rec[w] + sc[w] * a.P] = static_cast<uint8_t>((t0 - lo) >> 5);
-                    ++sc[w];
-                }
+            if (!live[w]) continue;
+            // bit-sliced compare of the 32 scores with L, most significant plane first
+            uint32_t gt = B[w][3] & ~tm3[w], eq = ~(B[w][3] ^ tm3[w]);
+            gt |= eq & B[w][2] & ~tm2[w];
+            eq &= ~(B[w][2] ^ tm2[w]);
+            gt |= eq & B[w][1] & ~tm1[w];
+            eq &= ~(B[w][1] ^ tm1[w]);
+            gt |= eq & B[w][0] & ~tm0[w];
+            eq &= ~(B[w][0] ^ tm0[w]);
+            const uint32_t ge0 = gt | eq;  // score >= L (points past the piece end score 0 < L)
+            cnt[w] += __popc(ge0) | (__popc(gt) << 16);
+            if (ge0) {
+                a.slots[rec[w] + sc[w] * a.P] = make_uint2(ge0, gt);
+                a.stile[rec[w] + sc[w] * a.P] = static_cast<uint8_t>((t0 - lo) >> 5);
+                ++sc[w];
             }
         }
     }
@@ -432,7 +492,7 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs 
     for (uint32_t w = 0; w < W; ++w) {
         if (32 * w + lane < nqb) {
             const uint64_t q = q0 + 32 * w + lane;
-            reinterpret_cast<uint4*>(a.hist)[q * a.P + piece] = make_uint4(c01[w], c23[w], c45[w], c67[w]);
+            a.h2[q * a.P + piece] = cnt[w];
             a.scnt[q * a.P + piece] = static_cast<uint16_t>(sc[w]);
         }
     }
@@ -592,18 +652,24 @@ cudaError_t launch_dense_select_fused(const DenseArgs& args, cudaStream_t st) {
     if (sh.words == 2) e = launch_fused_t<1024, 2>(a, sh.smem, st);
     else e = sh.threads == 512 ? launch_fused_t<512, 1>(a, sh.smem, st) : launch_fused_t<1024, 1>(a, sh.smem, st);
     if (e != cudaSuccess) return e;
-    // plan (+ fallback flags), compaction, exact emission for flagged query blocks
-    dense_plan_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(a);
+    // plan (+ fallback flags) from the two levels, compaction
+    dense_plan_fused_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(a);
     dense_compact_kernel<<<static_cast<unsigned>((a.nq * a.P + 255) / 256), 256, 0, st>>>(a);
     e = cudaMemsetAsync(args.nmap, 0, 4, st);
     if (e != cudaSuccess) return e;
     dense_flag_list_kernel<<<static_cast<unsigned>((a.nq + 255) / 256), 256, 0, st>>>(args);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    // exact two-pass emission for the flagged queries only, 32*W per block via qmap; blocks past
-    // the flagged count exit at once
+    // the flagged queries (T != L) get the exact two-pass select — full histograms, plan,
+    // emission — through qmap; blocks past the flagged count exit at once
     DenseArgs fb = args;
     fb.qflag = nullptr;
+    fb.pstride = 1;
+    e = launch_dense_hist(fb, st);
+    if (e != cudaSuccess) return e;
+    dense_plan_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(fb);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
     return launch_dense_emit(fb, st);
 }
 

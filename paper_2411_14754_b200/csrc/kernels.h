@@ -105,6 +105,7 @@ struct DenseArgs {
     uint16_t* scnt;            // nq x P records per (query, piece)
     uint32_t* qflag;           // nq: 1 = fall back to the exact two-pass emission for this query
     uint32_t C;
+    uint32_t* h2;              // single pass: nq x P, #score >= L | #score >= L+1 << 16
     uint32_t* qmap;            // fallback emission: block-local query j -> query qmap[q0 + j]
     uint32_t* nmap;            // device count of qmap entries
 };
