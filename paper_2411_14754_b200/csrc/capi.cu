@@ -363,8 +363,8 @@ uint64_t tile_size(const suco_gpu_index* x, uint64_t nq, uint64_t m, uint32_t k)
     const uint64_t ns = x->host.layout.ns;
     const uint64_t pieces = (x->host.n + 2047) / 2048;  // dense select scratch: hist (16 B) + quota/base per piece
     const uint64_t per = ns * x->K * 4 + ns * 4 + m * 4 + (k > 32 ? m * 12 : 0) + uint64_t(x->host.d) * 4 + k * 12 +
-                         (x->dense ? pieces * (24 + 64 * 9 + 2) + pieces / 16 * 16 + 16 : 0);  // + tile records
-    const uint64_t budget = 4ull << 30;
+                         (x->dense ? pieces * (24 + 32 * 9 + 6) + pieces / 16 * 16 + 16 : 0);  // + tile records
+    const uint64_t budget = 16ull << 30;  // per-batch scratch on a 180 GB part
     return std::max<uint64_t>(1, std::min<uint64_t>(nq, budget / per));
 }
 
@@ -456,7 +456,7 @@ void stage_select(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nt, uint
         if (fused) {
             da.pstride = 16;
             da.Ps = (da.P + da.pstride - 1) / da.pstride;
-            da.C = kDensePiece / 32;  // records per (query, piece): one per tile at most, never overflows
+            da.C = 32;  // records per (query, piece); more (dense supersets) flag the query
             sl.dsample.reserve(nt * da.Ps * 8);
             sl.dslots.reserve(nt * da.P * da.C);
             sl.dstile.reserve(nt * da.P * da.C);

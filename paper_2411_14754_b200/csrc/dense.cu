@@ -303,9 +303,7 @@ __global__ void __launch_bounds__(256) dense_plan_fused_kernel(DenseArgs a) {
         geL1 += __shfl_xor_sync(kFull, geL1, o);
     }
     const uint32_t L = a.L[q];
-    const bool ok = L >= 1 && geL >= a.m && geL1 < a.m;
-    if (lane == 0) a.qflag[q] = ok ? 0u : 1u;
-    if (!ok) return;
+    bool ok = L >= 1 && geL >= a.m && geL1 < a.m;
     const uint64_t need = a.m - geL1;
     uint64_t ties_run = 0, out_run = 0;
     for (uint32_t p0 = 0; p0 < a.P; p0 += 32) {
@@ -336,11 +334,16 @@ __global__ void __launch_bounds__(256) dense_plan_fused_kernel(DenseArgs a) {
         if (p < a.P) {
             a.quota[q * a.P + p] = quota;
             a.base[q * a.P + p] = static_cast<uint32_t>(out_run + ox - take);
+            if (take && a.scnt[q * a.P + p] > a.C) ok = false;  // a contributing piece overflowed
         }
         ties_run += tsum;
         out_run += osum;
     }
-    if (lane == 0) a.T[q] = L;
+    ok = __all_sync(kFull, ok);
+    if (lane == 0) {
+        a.qflag[q] = ok ? 0u : 1u;
+        a.T[q] = L;
+    }
 }
 
 // K3: re-score each piece; lane = query emits score > T and the first quota ties (id order).
@@ -422,13 +425,20 @@ __global__ void __launch_bounds__(256) dense_bound_kernel(DenseArgs a) {
         if (lo < a.n) sampled += min_u64(a.WP, a.n - lo);
     }
     uint32_t L = 0;
+    uint32_t atL = 0;
 #pragma unroll
     for (int t = 8; t >= 1; --t) {
         if (L == 0 && static_cast<uint32_t>(t) <= a.ns && sampled &&
             static_cast<double>(tot[t - 1]) * static_cast<double>(a.n) / static_cast<double>(sampled) >=
-                static_cast<double>(a.m))
+                static_cast<double>(a.m)) {
             L = t;
+            atL = tot[t - 1];
+        }
     }
+    // The single pass writes one record per tile holding a point with score >= L: worth it while
+    // those points are sparse (cfg2: 0.65% of points, ~12 of 64 tiles per piece). Denser supersets
+    // (cfg4: 2.2%, about half the tiles) go to the two-pass select (L = 0).
+    if (L && static_cast<double>(atL) > 0.01 * static_cast<double>(sampled)) L = 0;
     if (lane == 0) a.L[q] = L;
 }
 
@@ -441,6 +451,7 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs 
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const uint64_t q0 = uint64_t(blockIdx.x) * 32 * W;
     const uint32_t nqb = static_cast<uint32_t>(min_u64(32 * W, a.nq - q0));
+    if (!__syncthreads_or(threadIdx.x < nqb && a.L[q0 + threadIdx.x] != 0)) return;  // all two-pass
     build_masks<kDT, W>(a, M, q0, nqb);
     const uint32_t piece = blockIdx.y * kDW + warp;
     if (piece >= a.P) return;
@@ -482,9 +493,11 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs 
             const uint32_t ge0 = gt | eq;  // score >= L (points past the piece end score 0 < L)
             cnt[w] += __popc(ge0) | (__popc(gt) << 16);
             if (ge0) {
-                a.slots[rec[w] + sc[w] * a.P] = make_uint2(ge0, gt);
-                a.stile[rec[w] + sc[w] * a.P] = static_cast<uint8_t>((t0 - lo) >> 5);
-                ++sc[w];
+                if (sc[w] < a.C) {
+                    a.slots[rec[w] + sc[w] * a.P] = make_uint2(ge0, gt);
+                    a.stile[rec[w] + sc[w] * a.P] = static_cast<uint8_t>((t0 - lo) >> 5);
+                }
+                ++sc[w];  // > C: overflow, the plan flags the query if the piece contributes
             }
         }
     }
@@ -509,7 +522,7 @@ __global__ void __launch_bounds__(256) dense_compact_kernel(DenseArgs a) {
     if (a.qflag[q]) return;
     uint32_t quota = a.quota[i];
     uint32_t pos = a.base[i];
-    const uint32_t cnt = a.scnt[i];
+    const uint32_t cnt = min(static_cast<uint32_t>(a.scnt[i]), a.C);  // == scnt (overflow is flagged)
     const uint64_t r0 = q * a.C * a.P + p;  // record e at r0 + e * P
     uint32_t* out = a.cands + q * a.m;
     const uint32_t pbase = p * a.WP;

@@ -10,7 +10,7 @@ idx = suco.build_index(base, suco.IndexParams(cfg.num_subspaces, cfg.k_half, cfg
 cp = suco.CollisionParams(cfg.alpha, cfg.beta, cfg.k)
 m = suco.candidate_count(cfg.beta, len(base), cfg.k)
 rows = []
-for i in range(50):
+for i in range(int(os.environ.get("NQ", "50"))):
     sc, cands, cps, cum = idx.query_intermediates(qs[i], cp)
     ge = [int((sc >= t).sum()) for t in range(cfg.num_subspaces + 1)]
     T = max([t for t in range(1, cfg.num_subspaces + 1) if ge[t] >= m] or [0])
