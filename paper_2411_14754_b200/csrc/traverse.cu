@@ -170,6 +170,85 @@ __device__ void da_warp(const double* d1r, const uint32_t* o1, const double* d2r
     }
 }
 
+// k <= 64 (two rows per lane: lane and lane + 32): the frontier of both rows in named registers
+// (the generic RPL arrays ended up in local memory), updated by selects.
+__device__ void da_warp2(const double* d1r, const uint32_t* o1, const double* d2r, const uint32_t* o2, uint32_t k,
+                         const uint32_t* cell_size, uint64_t target, uint32_t* out_cells, uint32_t* out_n,
+                         double* dbg_sum, uint64_t* dbg_cum, unsigned long long* stat_cum, uint32_t lane) {
+    double a0 = kInf, a1 = kInf;          // next sum of row lane / row lane + 32
+    uint32_t c0 = 0, c1 = 0;              // their cursors (second-half rank)
+    uint32_t s00 = 0, s01 = 0, s10 = 0, s11 = 0;  // sizes of each row's next two cells
+    if (lane == 0) {
+        a0 = __dadd_rn(d1r[0], d2r[0]);
+        s00 = cell_sz(cell_size, o1, o2, k, 0, 0);
+        s01 = cell_sz(cell_size, o1, o2, k, 0, 1);
+    }
+    uint32_t activated = 1, ncell = 0;
+    uint64_t cum = 0;
+    while (cum < target) {
+        const bool second = a1 < a0;  // ties keep the lower row (lane < lane + 32)
+        const double best = second ? a1 : a0;
+        const uint32_t brow = second ? lane + 32u : lane;
+        // warp argmin by (distance, row) on the non-negative distances' bit patterns
+        const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(best));
+        const uint32_t hi = static_cast<uint32_t>(bits >> 32), lo = static_cast<uint32_t>(bits);
+        const uint32_t whi = __reduce_min_sync(kFull, hi);
+        const uint32_t wlo = __reduce_min_sync(kFull, hi == whi ? lo : 0xffffffffu);
+        const uint32_t pos = __reduce_min_sync(kFull, (hi == whi && lo == wlo) ? brow : 0xffffffffu);
+        if (whi >= 0x7ff00000u) break;  // +inf: unreachable while the IMI partitions all n points
+        const uint32_t owner = pos & 31u;
+        const bool slot1 = pos >= 32u;
+        const uint32_t j = __shfl_sync(kFull, slot1 ? c1 : c0, owner);
+        const uint32_t sz = __shfl_sync(kFull, slot1 ? s10 : s00, owner);
+        cum += sz;
+        if (lane == 0) {
+            out_cells[ncell] = o1[pos] * k + o2[j];
+            if (dbg_sum) {
+                dbg_sum[ncell] = __longlong_as_double(static_cast<long long>((static_cast<uint64_t>(whi) << 32) | wlo));
+                dbg_cum[ncell] = cum;
+            }
+        }
+        ++ncell;
+        if (j == 0 && activated < k) {  // query.cpp:108-112: the next row joins the frontier
+            const uint32_t row = activated;
+            if (lane == (row & 31u)) {
+                const double v = __dadd_rn(d1r[row], d2r[0]);
+                const uint32_t z0 = cell_sz(cell_size, o1, o2, k, row, 0), z1 = cell_sz(cell_size, o1, o2, k, row, 1);
+                if (row >= 32u) {
+                    a1 = v;
+                    s10 = z0;
+                    s11 = z1;
+                } else {
+                    a0 = v;
+                    s00 = z0;
+                    s01 = z1;
+                }
+            }
+            ++activated;
+        }
+        if (lane == owner) {  // query.cpp:113-118: advance the retrieved row
+            const bool done = j + 1 == k;
+            const double v = done ? kInf : __dadd_rn(d1r[pos], d2r[j + 1]);
+            const uint32_t z = done ? 0u : cell_sz(cell_size, o1, o2, k, pos, j + 2);
+            if (slot1) {
+                c1 = j + 1;
+                a1 = v;
+                s10 = s11;
+                s11 = z;
+            } else {
+                c0 = j + 1;
+                a0 = v;
+                s00 = s01;
+                s01 = z;
+            }
+        }
+    }
+    if (lane == 0) {
+        *out_n = ncell;
+        if (stat_cum) atomicAdd(stat_cum, static_cast<unsigned long long>(cum));
+    }
+}
+
 // Frontier in shared memory for k > 256 (rare: large k_half traversal tests).
 __device__ void da_warp_smem(const double* d1r, const uint32_t* o1, const double* d2r, const uint32_t* o2, uint32_t k,
                              const uint32_t* cell_size, uint64_t target, uint32_t* out_cells, uint32_t* out_n,
@@ -236,12 +315,8 @@ __device__ void da_warp_smem(const double* d1r, const uint32_t* o1, const double
 __device__ inline void run_da(const WarpSmem& w, uint32_t k, const uint32_t* cell_size, uint64_t target,
                               uint32_t* out_cells, uint32_t* out_n, double* dbg_sum, uint64_t* dbg_cum,
                               unsigned long long* stat_cum, uint32_t lane) {
-    if (k <= 32) {
-        da_warp<1>(w.d1r, w.o1, w.d2r, w.o2, k, cell_size, target, out_cells, out_n, dbg_sum, dbg_cum, stat_cum,
-                    lane);
-    } else if (k <= 64) {
-        da_warp<2>(w.d1r, w.o1, w.d2r, w.o2, k, cell_size, target, out_cells, out_n, dbg_sum, dbg_cum, stat_cum,
-                    lane);
+    if (k <= 64) {
+        da_warp2(w.d1r, w.o1, w.d2r, w.o2, k, cell_size, target, out_cells, out_n, dbg_sum, dbg_cum, stat_cum, lane);
     } else if (k <= 128) {
         da_warp<4>(w.d1r, w.o1, w.d2r, w.o2, k, cell_size, target, out_cells, out_n, dbg_sum, dbg_cum, stat_cum,
                     lane);
