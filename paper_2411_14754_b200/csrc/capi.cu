@@ -130,7 +130,7 @@ struct suco_gpu_index {
         DevBuf<uint32_t> dT, dquota, dbase;   // dense select plan
         DevBuf<uint16_t> dsample, dscnt;          // single-pass select: sampled hist, record counts
         DevBuf<uint2> dslots;                     // single-pass select: tile records
-        DevBuf<uint8_t> dstile;                   // single-pass select: record tiles
+        DevBuf<uint64_t> dtmask;                  // single-pass select: tiles with records
         DevBuf<uint32_t> dL, dflag, dh2;          // single-pass select: bound, fallback flags, two-level counts
         DevBuf<double> out_d, all_d;
         cudaEvent_t trav = nullptr, sel = nullptr, rr = nullptr;
@@ -363,7 +363,7 @@ uint64_t tile_size(const suco_gpu_index* x, uint64_t nq, uint64_t m, uint32_t k)
     const uint64_t ns = x->host.layout.ns;
     const uint64_t pieces = (x->host.n + 2047) / 2048;  // dense select scratch: hist (16 B) + quota/base per piece
     const uint64_t per = ns * x->K * 4 + ns * 4 + m * 4 + (k > 32 ? m * 12 : 0) + uint64_t(x->host.d) * 4 + k * 12 +
-                         (x->dense ? pieces * (24 + 32 * 9 + 6) + pieces / 16 * 16 + 16 : 0);  // + tile records
+                         (x->dense ? pieces * (24 + 32 * 8 + 14) + pieces / 16 * 16 + 16 : 0);  // + tile records
     const uint64_t budget = 16ull << 30;  // per-batch scratch on a 180 GB part
     return std::max<uint64_t>(1, std::min<uint64_t>(nq, budget / per));
 }
@@ -459,8 +459,8 @@ void stage_select(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nt, uint
             da.C = 32;  // records per (query, piece); more (dense supersets) flag the query
             sl.dsample.reserve(nt * da.Ps * 8);
             sl.dslots.reserve(nt * da.P * da.C);
-            sl.dstile.reserve(nt * da.P * da.C);
-            da.stile = sl.dstile.p;
+            sl.dtmask.reserve(nt * da.P);
+            da.tmask = sl.dtmask.p;
             sl.dscnt.reserve(nt * da.P);
             sl.dL.reserve(nt);
             sl.dh2.reserve(nt * da.P);

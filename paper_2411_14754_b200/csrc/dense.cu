@@ -460,6 +460,7 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs 
     // per lane = query: the bits of L as masks for one bit-sliced comparison per tile, which gives
     // score > L and score == L together; counts #(score >= L) | #(score >= L+1) << 16
     uint32_t tm0[W], tm1[W], tm2[W], tm3[W], cnt[W], sc[W], rec[W];
+    uint64_t tiles[W];  // bit t: tile t produced a record
     bool live[W];
 #pragma unroll
     for (uint32_t w = 0; w < W; ++w) {
@@ -473,6 +474,7 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs 
         tm3[w] = (L & 8u) ? kFull : 0u;
         cnt[w] = 0;
         sc[w] = 0;
+        tiles[w] = 0;
         rec[w] = static_cast<uint32_t>((mine ? q : 0) * a.C * a.P + piece);  // record e at + e*P (< 2^32)
     }
     const Xpose xp(lane);
@@ -493,10 +495,8 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs 
             const uint32_t ge0 = gt | eq;  // score >= L (points past the piece end score 0 < L)
             cnt[w] += __popc(ge0) | (__popc(gt) << 16);
             if (ge0) {
-                if (sc[w] < a.C) {
-                    a.slots[rec[w] + sc[w] * a.P] = make_uint2(ge0, gt);
-                    a.stile[rec[w] + sc[w] * a.P] = static_cast<uint8_t>((t0 - lo) >> 5);
-                }
+                if (sc[w] < a.C) a.slots[rec[w] + sc[w] * a.P] = make_uint2(ge0, gt);
+                tiles[w] |= 1ull << ((t0 - lo) >> 5);
                 ++sc[w];  // > C: overflow, the plan flags the query if the piece contributes
             }
         }
@@ -507,6 +507,7 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs 
             const uint64_t q = q0 + 32 * w + lane;
             a.h2[q * a.P + piece] = cnt[w];
             a.scnt[q * a.P + piece] = static_cast<uint16_t>(sc[w]);
+            a.tmask[q * a.P + piece] = tiles[w];
         }
     }
 }
@@ -526,9 +527,11 @@ __global__ void __launch_bounds__(256) dense_compact_kernel(DenseArgs a) {
     const uint64_t r0 = q * a.C * a.P + p;  // record e at r0 + e * P
     uint32_t* out = a.cands + q * a.m;
     const uint32_t pbase = p * a.WP;
+    uint64_t tiles = a.tmask[i];
     for (uint32_t e = 0; e < cnt; ++e) {
         const uint2 r = a.slots[r0 + uint64_t(e) * a.P];
-        const uint32_t tb = pbase + (static_cast<uint32_t>(a.stile[r0 + uint64_t(e) * a.P]) << 5);
+        const uint32_t tb = pbase + (static_cast<uint32_t>(__ffsll(static_cast<long long>(tiles)) - 1) << 5);
+        tiles &= tiles - 1;
         uint32_t take = r.y;  // score > T
         uint32_t ties = r.x & ~r.y;
         while (ties && quota) {  // first ties in id order

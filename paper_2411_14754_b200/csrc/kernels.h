@@ -101,7 +101,7 @@ struct DenseArgs {
     uint32_t Ps;               // sampled pieces
     uint32_t* L;               // nq
     uint2* slots;              // nq x P x C records (score >= L mask, score >= L+1 mask) of non-empty tiles
-    uint8_t* stile;            // nq x P x C: tile of each record
+    uint64_t* tmask;           // nq x P: tiles that produced a record (record e = e-th set bit)
     uint16_t* scnt;            // nq x P records per (query, piece)
     uint32_t* qflag;           // nq: 1 = fall back to the exact two-pass emission for this query
     uint32_t C;
