@@ -298,12 +298,15 @@ def test_u8_rows_rerank_mixed_queries(gpu, oracle, d, shift):
         assert np.array_equal(dd, od), (d, shift, a, b, k)
 
 
+@pytest.mark.parametrize("fused", ["1", "0"])
 @pytest.mark.parametrize("words", ["1", "2"])
-def test_dense_select_block_widths(gpu, oracle, words, monkeypatch):
-    """32-query (one mask word) and 64-query (two words) dense blocks give the same candidate sets
-    and answers as the reference; a partial last block (nq % 64 != 0) included."""
+def test_dense_select_block_widths(gpu, oracle, words, fused, monkeypatch):
+    """32-query (one mask word) and 64-query (two words) dense blocks, single-pass (with its
+    fallback) and two-pass, give the same candidate sets and answers as the reference; a partial
+    last block (nq % 64 != 0) included."""
     monkeypatch.setenv("SUCO_DENSE_WORDS", words)
-    full = oracle.clustered(9000 + 77, 24, 30, 2024, 0, 100, 9, True)
+    monkeypatch.setenv("SUCO_DENSE_FUSED", fused)
+    full = oracle.clustered(60000 + 77, 24, 30, 2024, 0, 100, 9, True)  # 30 pieces: a real sample
     base, qs = oracle.hold_out(full, 77, 2025)
     oidx = oracle.build_index(base, 6, 20, 3, 42, 0)
     idx = gpu.load_index(oidx.serialize(), base)
