@@ -216,6 +216,27 @@ int suco_gpu_shard_topk_cells(suco_gpu_index* shard, const float* d_queries, uin
 int suco_gpu_exact_knn_batch(suco_gpu_index* index, const float* queries, uint64_t nq, uint32_t qlen, uint32_t k,
                              uint32_t* ids, double* dists);
 
+/* ------------------------------------------------------------- vecs I/O
+ * read_vecs / write_vecs (io.hpp:22-40, io.cpp:99-160): kind 0 = fvecs
+ * (f32), 1 = bvecs (u8), 2 = ivecs (i32, |v| <= 2^24). Records parse in
+ * order with the reference's checks and messages (FORMAT: open failure,
+ * empty file, invalid or inconsistent dim naming the record, truncation
+ * naming the byte offset, non-finite f32, ivecs beyond 2^24); at most `limit`
+ * records (UINT64_MAX: all; 0: none, a FORMAT error like the reference's).
+ * suco_read_vecs fills `out` (cap_rows rows) or, with out == NULL, only
+ * reports n and d. */
+int suco_read_vecs(const char* path, int kind, uint64_t limit, float* out, uint64_t cap_rows, uint64_t* n, uint32_t* d);
+int suco_write_vecs(const char* path, int kind, uint64_t n, uint32_t d, const float* values);
+/* Device upload straight from a vecs file: the file streams
+ * through two pinned 32 MB stages into the index's device rows (parse of one
+ * chunk overlaps the copy of the previous), then build / load as
+ * suco_gpu_build_index / suco_gpu_load_index — the host never holds the
+ * float matrix. */
+int suco_gpu_build_index_from_vecs(const char* path, int kind, uint64_t limit, const suco_index_params* params,
+                                   int device, suco_gpu_index** out);
+int suco_gpu_load_index_from_vecs(const unsigned char* bytes, uint64_t len, const char* path, int kind, uint64_t limit,
+                                  int device, suco_gpu_index** out);
+
 /* ------------------------------------------------ stage-level entry points
  * Each runs the device kernel of one stage on host inputs (parity tests of
  * the reference's free functions). */

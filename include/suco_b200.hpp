@@ -24,7 +24,9 @@
 // Also wrapped: suco_last_error, suco_gpu_device_count, suco_gpu_index_info,
 // suco_gpu_index_subspace, suco_gpu_free_index, suco_gpu_set_stream,
 // suco_gpu_synchronize, suco_gpu_query_intermediates, suco_gpu_last_launches,
-// suco_gpu_exact_knn_batch (GpuIndex::exact_knn_batch; recall / mre as in eval.cpp:64-102).
+// suco_gpu_exact_knn_batch (GpuIndex::exact_knn_batch; recall / mre as in eval.cpp:64-102),
+// suco_read_vecs / suco_write_vecs / suco_gpu_build_index_from_vecs / suco_gpu_load_index_from_vecs
+// (vecs I/O, io.hpp:22-40; raw C entry points).
 #pragma once
 
 #include <cstdint>

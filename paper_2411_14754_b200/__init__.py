@@ -333,6 +333,62 @@ def load_index(blob: bytes, dataset, device: int = 0) -> GpuIndex:
     return GpuIndex(h)
 
 
+# ------------------------------------------------------------------ vecs I/O (io.hpp:15-40)
+VECS_KINDS = {"fvecs": 0, "f32": 0, "bvecs": 1, "u8": 1, "ivecs": 2, "i32": 2}
+
+
+def _kind(kind) -> int:
+    if isinstance(kind, str):
+        if kind not in VECS_KINDS:
+            raise ContractError(f"unknown vecs kind {kind!r}")
+        return VECS_KINDS[kind]
+    return int(kind)
+
+
+def _limit(limit: Optional[int]) -> int:
+    return 0xFFFFFFFFFFFFFFFF if limit is None else int(limit)
+
+
+def read_vecs(path: str, kind="fvecs", limit: Optional[int] = None) -> np.ndarray:
+    """read_vecs (io.hpp:22-33, io.cpp:99-137): n x d float32 (bvecs / ivecs widened)."""
+    k = _kind(kind)
+    n, d = C.c_uint64(), C.c_uint32()
+    _check(_c.read_vecs(path.encode(), k, _limit(limit), None, 0, C.byref(n), C.byref(d)))
+    out = np.empty((n.value, d.value), np.float32)
+    _check(_c.read_vecs(path.encode(), k, _limit(limit), _p(out, _c.f32p), n.value, C.byref(n), C.byref(d)))
+    return out
+
+
+def write_vecs(path: str, kind, values) -> None:
+    """write_vecs (io.hpp:35-40): the inverse of read_vecs."""
+    v = np.ascontiguousarray(values, np.float32)
+    if v.ndim != 2:
+        raise ContractError("write_vecs: values must be an n x d matrix")
+    _check(_c.write_vecs(path.encode(), _kind(kind), v.shape[0], v.shape[1], _p(v, _c.f32p)))
+
+
+def build_index_from_vecs(path: str, kind="fvecs", params: IndexParams = IndexParams(), limit: Optional[int] = None,
+                          device: int = 0) -> GpuIndex:
+    """build_index over a vecs file streamed straight into device memory (pinned, chunked)."""
+    h = C.c_void_p()
+    ip = params._c()
+    _check(_c.build_index_from_vecs(path.encode(), _kind(kind), _limit(limit), C.byref(ip), device, C.byref(h)))
+    return GpuIndex(h)
+
+
+def load_index_from_vecs(blob: bytes, path: str, kind="fvecs", limit: Optional[int] = None,
+                         device: int = 0) -> GpuIndex:
+    """load_index with the dataset streamed from a vecs file into device memory."""
+    if isinstance(blob, str):
+        with open(blob, "rb") as f:
+            blob = f.read()
+    buf = np.frombuffer(blob, np.uint8)
+    h = C.c_void_p()
+    _check(_c.load_index_from_vecs(_p(buf, _c.u8p), len(blob), path.encode(), _kind(kind), _limit(limit), device,
+                                   C.byref(h)))
+    return GpuIndex(h)
+
+
 def knn_query(index: GpuIndex, dataset, query, params: CollisionParams) -> List[Neighbor]:
     """knn_query (query.hpp:93-96) for one query; the index owns the dataset rows on the device,
     `dataset` is checked for compatibility (index.cpp:295-305) like the reference."""
