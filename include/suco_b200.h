@@ -216,6 +216,24 @@ int suco_gpu_shard_topk_cells(suco_gpu_index* shard, const float* d_queries, uin
 int suco_gpu_exact_knn_batch(suco_gpu_index* index, const float* queries, uint64_t nq, uint32_t qlen, uint32_t k,
                              uint32_t* ids, double* dists);
 
+/* ------------------------------------------------------------- SC-Linear
+ * compute_sc_scores (sc_linear.hpp:45-50, sc_linear.cpp:49-93): for one
+ * query, scores[i] = the number of subspaces in which point i is among the
+ * collision_count(alpha, n) nearest by exact fp64 distance of the whole
+ * subspace projection, ties by id. Uses the reference's two distance orders
+ * (sq_euclidean_raw for a consecutive subspace, sq_euclidean_projected
+ * otherwise), so the tally is identical. Wrong query length -> CONTRACT;
+ * alpha outside (0, 1] -> CONFIG. scores: n host u32s. */
+int suco_gpu_sc_scores(suco_gpu_index* index, const float* query, uint32_t qlen, double alpha, uint32_t* scores);
+
+/* sc_linear_query (sc_linear.hpp:52-53, sc_linear.cpp:95-121) over a batch:
+ * the candidate_count(beta, n, k) best points by (score desc, id asc),
+ * re-ranked exactly like knn_query. Params are validated first (CONFIG), then
+ * the query length (CONTRACT). Host buffers: queries nq x qlen, ids / dists
+ * nq x k. The index-free quality baseline of SURVEY §8(f)4. */
+int suco_gpu_sc_linear_batch(suco_gpu_index* index, const float* queries, uint64_t nq, uint32_t qlen,
+                             const suco_collision_params* params, uint32_t* ids, double* dists);
+
 /* ------------------------------------------------------------- vecs I/O
  * read_vecs / write_vecs (io.hpp:22-40, io.cpp:99-160): kind 0 = fvecs
  * (f32), 1 = bvecs (u8), 2 = ivecs (i32, |v| <= 2^24). Records parse in

@@ -25,6 +25,7 @@
 // suco_gpu_index_subspace, suco_gpu_free_index, suco_gpu_set_stream,
 // suco_gpu_synchronize, suco_gpu_query_intermediates, suco_gpu_last_launches,
 // suco_gpu_exact_knn_batch (GpuIndex::exact_knn_batch; recall / mre as in eval.cpp:64-102),
+// suco_gpu_sc_scores / suco_gpu_sc_linear_batch (GpuIndex::sc_scores / sc_linear_batch, sc_linear.hpp:45-53),
 // suco_read_vecs / suco_write_vecs / suco_gpu_build_index_from_vecs / suco_gpu_load_index_from_vecs
 // (vecs I/O, io.hpp:22-40; raw C entry points).
 #pragma once
@@ -195,6 +196,30 @@ public:
         for (std::uint64_t q = 0; q < nq; ++q) {
             out[q].entries.resize(k);
             for (std::uint32_t i = 0; i < k; ++i) out[q].entries[i] = {ids[q * k + i], dists[q * k + i]};
+        }
+        return out;
+    }
+
+    // compute_sc_scores (sc_linear.hpp:45-50) for one query: n per-point collision counts.
+    std::vector<std::uint32_t> sc_scores(std::span<const float> query, double alpha) const {
+        std::vector<std::uint32_t> scores(n());
+        check(suco_gpu_sc_scores(h_.get(), query.data(), static_cast<std::uint32_t>(query.size()), alpha,
+                                 scores.data()));
+        return scores;
+    }
+
+    // sc_linear_query (sc_linear.hpp:52-53) for every row: the SC-Linear baseline.
+    std::vector<QueryResult> sc_linear_batch(std::span<const float> queries, std::uint64_t nq,
+                                             const CollisionParams& params) const {
+        const std::uint32_t qlen = nq ? static_cast<std::uint32_t>(queries.size() / nq) : 0;
+        std::vector<std::uint32_t> ids(nq * params.k);
+        std::vector<double> dists(nq * params.k);
+        const auto cp = params.c();
+        check(suco_gpu_sc_linear_batch(h_.get(), queries.data(), nq, qlen, &cp, ids.data(), dists.data()));
+        std::vector<QueryResult> out(nq);
+        for (std::uint64_t q = 0; q < nq; ++q) {
+            out[q].entries.resize(params.k);
+            for (std::uint32_t i = 0; i < params.k; ++i) out[q].entries[i] = {ids[q * params.k + i], dists[q * params.k + i]};
         }
         return out;
     }

@@ -528,6 +528,29 @@ class RefIndex:
             C.byref(wall)))
         return ids, dists, wall.value
 
+    def sc_scores(self, data, query, alpha):
+        """compute_sc_scores (sc_linear.hpp:45) over this index's layout."""
+        data = np.ascontiguousarray(data, np.float32)
+        ds = self._dataset(data)
+        q = np.ascontiguousarray(query, np.float32)
+        scores = np.empty(data.shape[0], np.uint32)
+        self.lib._check(self.lib._fn("sc_scores")(self.h, ds, _p(q, f32p), C.c_uint32(q.size), C.c_double(alpha),
+                                                  _p(scores, u32p)))
+        return scores
+
+    def sc_linear_query(self, data, query, alpha, beta, k):
+        """sc_linear_query (sc_linear.hpp:52) over this index's layout -> (ids, dists)."""
+        data = np.ascontiguousarray(data, np.float32)
+        ds = self._dataset(data)
+        q = np.ascontiguousarray(query, np.float32)
+        ids = np.empty(k, np.uint32)
+        dists = np.empty(k, np.float64)
+        cnt = C.c_uint32()
+        self.lib._check(self.lib._fn("sc_linear_query")(self.h, ds, _p(q, f32p), C.c_uint32(q.size), C.c_double(alpha),
+                                                        C.c_double(beta), C.c_uint32(k), _p(ids, u32p),
+                                                        _p(dists, f64p), C.byref(cnt)))
+        return ids[: cnt.value].copy(), dists[: cnt.value].copy()
+
     def query_intermediates(self, data, query, alpha, beta, k):
         data = np.ascontiguousarray(data, np.float32)
         ds = self._dataset(data)

@@ -475,4 +475,29 @@ int ref_rng_imi(void* h, std::uint32_t k_half, std::uint64_t n, std::uint64_t* o
 
 unsigned ref_hardware_threads() { return suco::effective_threads(0); }
 
+// SC-Linear (sc_linear.hpp:45-53) over an index's layout and a dataset handle.
+int ref_sc_scores(void* hidx, void* hdata, const float* query, std::uint32_t qlen, double alpha,
+                  std::uint32_t* scores) {
+    return guarded([&] {
+        const auto& idx = static_cast<RefIndex*>(hidx)->index;
+        const auto& ds = *static_cast<suco::Dataset*>(hdata);
+        const auto sc = suco::compute_sc_scores(ds, idx.layout, {query, qlen}, alpha);
+        for (std::size_t i = 0; i < sc.scores.size(); ++i) scores[i] = static_cast<std::uint32_t>(sc.scores[i]);
+    });
+}
+
+int ref_sc_linear_query(void* hidx, void* hdata, const float* query, std::uint32_t qlen, double alpha,
+                        double beta, std::uint32_t k, std::uint32_t* ids, double* dists, std::uint32_t* count) {
+    return guarded([&] {
+        const auto& idx = static_cast<RefIndex*>(hidx)->index;
+        const auto& ds = *static_cast<suco::Dataset*>(hdata);
+        const auto r = suco::sc_linear_query(ds, idx.layout, {query, qlen}, suco::CollisionParams{alpha, beta, k});
+        for (std::size_t i = 0; i < r.entries.size(); ++i) {
+            ids[i] = r.entries[i].id;
+            dists[i] = r.entries[i].distance;
+        }
+        *count = static_cast<std::uint32_t>(r.entries.size());
+    });
+}
+
 }  // extern "C"

@@ -263,6 +263,30 @@ class GpuIndex:
         _check(_c.exact_knn_batch(self._h, _p(q, _c.f32p), nq, qlen, int(k), _p(ids, _c.u32p), _p(dists, _c.f64p)))
         return ids[:, :k], dists[:, :k]
 
+    def sc_scores(self, query, alpha: float) -> np.ndarray:
+        """compute_sc_scores (sc_linear.cpp:49-93) on the GPU: per point, the number of subspaces in which
+        it is among the collision_count(alpha, n) nearest (exact fp64, ties by id). u32 array of n."""
+        q = _f32(query).reshape(-1)
+        n = self.n
+        out = np.zeros(max(n, 1), np.uint32)
+        _check(_c.sc_scores(self._h, _p(q, _c.f32p), q.shape[0], float(alpha), _p(out, _c.u32p)))
+        return out[:n]
+
+    def sc_linear_batch(self, queries, params: CollisionParams) -> Tuple[np.ndarray, np.ndarray]:
+        """sc_linear_query (sc_linear.cpp:95-121) for every row on the GPU — the index-free SC-Linear
+        baseline: (ids nq x k, distances nq x k)."""
+        q = _f32(queries)
+        if q.ndim == 1:
+            q = q[None, :]
+        nq, qlen = q.shape
+        k = int(params.k)
+        ids = np.zeros((nq, max(k, 1)), np.uint32)
+        dists = np.zeros((nq, max(k, 1)), np.float64)
+        cp = params._c()
+        _check(_c.sc_linear_batch(self._h, _p(q, _c.f32p), nq, qlen, C.byref(cp), _p(ids, _c.u32p),
+                                  _p(dists, _c.f64p)))
+        return ids[:, :k], dists[:, :k]
+
     def knn_query_batch_device(self, d_queries: int, nq: int, qlen: int, params: CollisionParams, d_ids: int,
                                d_dists: int, stream: Optional[int] = None) -> None:
         """Device-resident variant: raw device pointers (e.g. torch tensor .data_ptr()). `stream` is a

@@ -73,6 +73,9 @@ set_profiling = _sig("suco_gpu_set_profiling", C.c_int, vp, C.c_int)
 stage_times = _sig("suco_gpu_stage_times", C.c_int, vp, f64p, u64p)
 last_launches = _sig("suco_gpu_last_launches", C.c_int, vp, u64p)
 exact_knn_batch = _sig("suco_gpu_exact_knn_batch", C.c_int, vp, f32p, C.c_uint64, C.c_uint32, C.c_uint32, u32p, f64p)
+sc_scores = _sig("suco_gpu_sc_scores", C.c_int, vp, f32p, C.c_uint32, C.c_double, u32p)
+sc_linear_batch = _sig("suco_gpu_sc_linear_batch", C.c_int, vp, f32p, C.c_uint64, C.c_uint32,
+                       C.POINTER(CollisionParamsC), u32p, f64p)
 read_vecs = _sig("suco_read_vecs", C.c_int, C.c_char_p, C.c_int, C.c_uint64, f32p, C.c_uint64, u64p, u32p)
 write_vecs = _sig("suco_write_vecs", C.c_int, C.c_char_p, C.c_int, C.c_uint64, C.c_uint32, f32p)
 build_index_from_vecs = _sig("suco_gpu_build_index_from_vecs", C.c_int, C.c_char_p, C.c_int, C.c_uint64,
@@ -107,7 +110,8 @@ EXPORTED = [
     "suco_validate_collision_params", "suco_gpu_build_index", "suco_gpu_load_index", "suco_gpu_serialize_index",
     "suco_gpu_index_subspace", "suco_gpu_index_info", "suco_gpu_free_index", "suco_gpu_knn_query_batch",
     "suco_gpu_knn_query_batch_device", "suco_gpu_set_stream", "suco_gpu_synchronize", "suco_gpu_set_profiling",
-    "suco_gpu_stage_times", "suco_gpu_last_launches", "suco_gpu_exact_knn_batch", "suco_read_vecs", "suco_write_vecs",
+    "suco_gpu_stage_times", "suco_gpu_last_launches", "suco_gpu_exact_knn_batch", "suco_gpu_sc_scores",
+    "suco_gpu_sc_linear_batch", "suco_read_vecs", "suco_write_vecs",
     "suco_gpu_build_index_from_vecs", "suco_gpu_load_index_from_vecs",
     "suco_gpu_query_intermediates", "suco_gpu_centroid_distances", "suco_gpu_dynamic_activation", "suco_gpu_rerank",
     "suco_gpu_kmeans", "suco_gpu_build_imi", "suco_gpu_make_shard", "suco_gpu_shard_block_hint",

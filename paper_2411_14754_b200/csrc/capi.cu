@@ -626,6 +626,63 @@ suco_gpu_index* new_index(int device) {
     return x;
 }
 
+// SC-Linear (sc_linear.cpp:49-121) over the index's device rows and layout.
+struct ScScratch {
+    DevBuf<uint32_t> sub_off, vals, vals_alt, scores, cands;
+    DevBuf<uint8_t> consec, temp;
+    DevBuf<unsigned long long> keys, keys_alt;
+    DevBuf<float> q;
+    ScArgs a{};
+};
+
+void sc_setup(suco_gpu_index* x, ScScratch& w) {
+    const HostLayout& L = x->host.layout;
+    const uint64_t n = x->host.n;
+    std::vector<uint32_t> off(L.ns + 1, 0);
+    std::vector<uint8_t> consec(L.ns, 0);
+    for (uint32_t s = 0; s < L.ns; ++s) {
+        off[s + 1] = off[s] + L.sizes[s];
+        bool run = L.sizes[s] > 0;  // consecutive_start (subspace.cpp:93-102)
+        for (uint32_t j = off[s] + 1; j < off[s + 1]; ++j) run = run && L.dims[j] == L.dims[j - 1] + 1;
+        consec[s] = run;
+    }
+    cudaStream_t st = x->stream;
+    w.sub_off.reserve(L.ns + 1);
+    w.consec.reserve(L.ns);
+    CUDA_TRY(cudaMemcpyAsync(w.sub_off.p, off.data(), off.size() * 4, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(w.consec.p, consec.data(), consec.size(), cudaMemcpyHostToDevice, st));
+    w.keys.reserve(n);
+    w.keys_alt.reserve(n);
+    w.vals.reserve(n);
+    w.vals_alt.reserve(n);
+    w.scores.reserve(n);
+    w.q.reserve(x->host.d);
+    const size_t tb = sc_temp_bytes(n);
+    w.temp.reserve(tb);
+    w.a.data = x->data.p;
+    w.a.n = n;
+    w.a.d = x->host.d;
+    w.a.ns = L.ns;
+    w.a.dims = x->dims.p;
+    w.a.sub_off = w.sub_off.p;
+    w.a.consec = w.consec.p;
+    w.a.q = w.q.p;
+    w.a.keys = w.keys.p;
+    w.a.keys_alt = w.keys_alt.p;
+    w.a.vals = w.vals.p;
+    w.a.vals_alt = w.vals_alt.p;
+    w.a.temp = w.temp.p;
+    w.a.temp_bytes = tb;
+}
+
+void check_sc_query(const suco_gpu_index* x, uint32_t qlen) {
+    if (!x) raise(SUCO_ERR_CONTRACT, "index is null");
+    if (qlen != x->host.d) {  // sc_linear.cpp:55-58
+        raise(SUCO_ERR_CONTRACT, "query length " + std::to_string(qlen) + " does not match dataset d = " +
+                                     std::to_string(x->host.d));
+    }
+}
+
 }  // namespace
 
 // ======================================================================= C ABI
@@ -941,6 +998,76 @@ int suco_gpu_exact_knn_batch(suco_gpu_index* x, const float* queries, uint64_t n
             CUDA_TRY(launch_rerank(ra, nt, st));
             CUDA_TRY(cudaMemcpyAsync(ids + q0 * k, di.p, nt * k * 4, cudaMemcpyDeviceToHost, st));
             CUDA_TRY(cudaMemcpyAsync(dists + q0 * k, dd.p, nt * k * 8, cudaMemcpyDeviceToHost, st));
+        }
+        CUDA_TRY(cudaStreamSynchronize(st));
+    });
+}
+
+int suco_gpu_sc_scores(suco_gpu_index* x, const float* query, uint32_t qlen, double alpha, uint32_t* scores) {
+    return guarded([&] {
+        check_sc_query(x, qlen);
+        // the reference leaves alpha unchecked here (c > n would index past the order array)
+        if (!(alpha > 0.0) || alpha > 1.0) raise(SUCO_ERR_CONFIG, "alpha must be in (0, 1], got " + std::to_string(alpha));
+        if (!query || !scores) raise(SUCO_ERR_CONTRACT, "null buffer");
+        DeviceGuard g(x->device);
+        cudaStream_t st = x->stream;
+        ScScratch w;
+        sc_setup(x, w);
+        const uint64_t c = std::min<uint64_t>(suco_collision_count(alpha, x->host.n), x->host.n);
+        CUDA_TRY(cudaMemcpyAsync(w.q.p, query, qlen * 4, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(launch_sc_scores(w.a, c, w.scores.p, st));
+        CUDA_TRY(cudaMemcpyAsync(scores, w.scores.p, x->host.n * 4, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+    });
+}
+
+int suco_gpu_sc_linear_batch(suco_gpu_index* x, const float* queries, uint64_t nq, uint32_t qlen,
+                             const suco_collision_params* p, uint32_t* ids, double* dists) {
+    return guarded([&] {
+        if (!x) raise(SUCO_ERR_CONTRACT, "index is null");
+        validate_params(p, x->host.n);  // sc_linear.cpp:97, before the query-length check
+        check_sc_query(x, qlen);
+        if (nq == 0) return;
+        if (!queries || !ids || !dists) raise(SUCO_ERR_CONTRACT, "null buffer");
+        DeviceGuard g(x->device);
+        cudaStream_t st = x->stream;
+        const uint64_t n = x->host.n;
+        const uint64_t c = std::min<uint64_t>(suco_collision_count(p->alpha, n), n);
+        const uint64_t m = std::min<uint64_t>(suco_candidate_count(p->beta, n, p->k), n);
+        ScScratch w;
+        sc_setup(x, w);
+        w.cands.reserve(n);
+        DevBuf<uint32_t> di, all_id;
+        DevBuf<double> dd, all_d;
+        di.reserve(p->k);
+        dd.reserve(p->k);
+        if (p->k > 32) {
+            all_d.reserve(m);
+            all_id.reserve(m);
+        }
+        for (uint64_t q = 0; q < nq; ++q) {
+            CUDA_TRY(cudaMemcpyAsync(w.q.p, queries + q * qlen, qlen * 4, cudaMemcpyHostToDevice, st));
+            CUDA_TRY(launch_sc_scores(w.a, c, w.scores.p, st));
+            // the m best by (score desc, id asc): the first m of a stable sort on N_s - score
+            CUDA_TRY(launch_sc_candidates(w.a, w.scores.p, w.cands.p, st));
+            RerankArgs ra{};
+            ra.data = x->data.p;
+            ra.n = n;
+            ra.d = x->host.d;
+            ra.queries = w.q.p;
+            ra.cands = w.cands.p;
+            ra.m = m;
+            ra.k = p->k;
+            ra.out_ids = di.p;
+            ra.out_dists = dd.p;
+            ra.data_int_max = x->data_int_max;
+            ra.data8 = x->dpad ? x->data8.p : nullptr;
+            ra.dpad = x->dpad;
+            ra.all_d = all_d.p;
+            ra.all_id = all_id.p;
+            CUDA_TRY(launch_rerank(ra, 1, st));
+            CUDA_TRY(cudaMemcpyAsync(ids + q * p->k, di.p, p->k * 4, cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaMemcpyAsync(dists + q * p->k, dd.p, p->k * 8, cudaMemcpyDeviceToHost, st));
         }
         CUDA_TRY(cudaStreamSynchronize(st));
     });

@@ -174,4 +174,24 @@ cudaError_t launch_check_finite(const float* data, uint64_t count, int* flag, cu
 cudaError_t launch_int_stats(const float* data, uint64_t count, unsigned int* out3, cudaStream_t st);
 cudaError_t launch_pack_u8(const float* data, uint64_t n, uint32_t d, uint32_t dpad, uint8_t* out, cudaStream_t st);
 
+// SC-Linear (sclinear.cu): exact per-subspace distances, top-c by stable sort.
+struct ScArgs {
+    const float* data;             // n x d rows
+    uint64_t n;
+    uint32_t d, ns;
+    const uint32_t* dims;          // concatenated whole-subspace dims (layout order)
+    const uint32_t* sub_off;       // ns + 1 prefix offsets into dims
+    const uint8_t* consec;         // ns: dims form one consecutive run -> sq_euclidean_raw
+    const float* q;                // one query, d floats
+    unsigned long long* keys;      // n distance bit patterns of one subspace (reused as u32 rank keys)
+    unsigned long long* keys_alt;  // n sort output
+    uint32_t* vals;                // n ids
+    uint32_t* vals_alt;            // n sorted ids
+    void* temp;                    // CUB scratch
+    size_t temp_bytes;
+};
+size_t sc_temp_bytes(uint64_t n);
+cudaError_t launch_sc_scores(ScArgs a, uint64_t c, uint32_t* scores, cudaStream_t st);
+cudaError_t launch_sc_candidates(ScArgs a, const uint32_t* scores, uint32_t* cands_sorted, cudaStream_t st);
+
 }  // namespace suco_gpu
