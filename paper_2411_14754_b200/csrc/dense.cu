@@ -118,11 +118,11 @@ __device__ __forceinline__ void mask_at(const uint32_t* M, uint32_t slot, uint32
     }
 }
 
-// Scores of the 32 points [t0, t0 + 32) for the block's 32*W queries; returns
-// with lane = query (word w: query 32w + lane): planes B[w][0..3] (bit r = point t0 + r).
+// Bit-planes of the scores of the 32 points [t0, t0 + 32) (lane = point t0 + lane) for the
+// block's 32*W queries: b[w][i] bit j = bit i of query (32w + j)'s score.
 template <uint32_t W>
-__device__ __forceinline__ void score_tile(const DenseArgs& a, const uint32_t* M, uint64_t t0, uint64_t p_hi,
-                                           const Xpose& xp, uint32_t (&B)[W][4], uint32_t lane) {
+__device__ __forceinline__ void score_planes(const DenseArgs& a, const uint32_t* M, uint64_t t0, uint64_t p_hi,
+                                             uint32_t (&b)[W][4], uint32_t lane) {
     const uint64_t p = t0 + lane;
     const uint32_t none = a.ns * a.K;
     uint4 c = make_uint4(none | (none << 16), none | (none << 16), none | (none << 16), none | (none << 16));
@@ -144,12 +144,27 @@ __device__ __forceinline__ void score_tile(const DenseArgs& a, const uint32_t* M
         const uint32_t s3 = m[6][w] ^ m[7][w], c3 = m[6][w] & m[7][w];
         fadd(s1, s2, s3, b0, c4);  // weight 1
         fadd(c1, c2, c3, s5, c5);  // weight 2 (+ carry weight 4)
-        const uint32_t b1 = s5 ^ c4, c6 = s5 & c4;
-        const uint32_t b2 = c5 ^ c6, b3 = c5 & c6;
-        B[w][0] = xp(b0);
-        B[w][1] = xp(b1);
-        B[w][2] = xp(b2);
-        B[w][3] = xp(b3);
+        const uint32_t c6 = s5 & c4;
+        b[w][0] = b0;
+        b[w][1] = s5 ^ c4;
+        b[w][2] = c5 ^ c6;
+        b[w][3] = c5 & c6;
+    }
+}
+
+// The same scores with lane = query (word w: query 32w + lane): planes B[w][0..3] (bit r =
+// point t0 + r).
+template <uint32_t W>
+__device__ __forceinline__ void score_tile(const DenseArgs& a, const uint32_t* M, uint64_t t0, uint64_t p_hi,
+                                           const Xpose& xp, uint32_t (&B)[W][4], uint32_t lane) {
+    uint32_t b[W][4];
+    score_planes<W>(a, M, t0, p_hi, b, lane);
+#pragma unroll
+    for (uint32_t w = 0; w < W; ++w) {
+        B[w][0] = xp(b[w][0]);
+        B[w][1] = xp(b[w][1]);
+        B[w][2] = xp(b[w][2]);
+        B[w][3] = xp(b[w][3]);
     }
 }
 
@@ -457,21 +472,22 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs 
     if (piece >= a.P) return;
     const uint64_t lo = uint64_t(piece) * a.WP;
     const uint64_t hi = min_u64(a.n, lo + a.WP);
-    // per lane = query: the bits of L as masks for one bit-sliced comparison per tile, which gives
-    // score > L and score == L together; counts #(score >= L) | #(score >= L+1) << 16
-    uint32_t tm0[W], tm1[W], tm2[W], tm3[W], cnt[W], sc[W], rec[W];
+    // The bits of L[q] across the block's queries (word w, bit j = query 32w + j): one bit-sliced
+    // comparison per tile, BEFORE the transpose (lane = point, bit = query), gives score > L and
+    // score == L for all 32*W queries at once; only the two results are transposed (10 shuffles,
+    // not 20 for the four planes). Counts per lane = query: #(score >= L) | #(score >= L+1) << 16.
+    uint32_t T0[W], T1[W], T2[W], T3[W], live[W], cnt[W], sc[W], rec[W];
     uint64_t tiles[W];  // bit t: tile t produced a record
-    bool live[W];
 #pragma unroll
     for (uint32_t w = 0; w < W; ++w) {
         const uint64_t q = q0 + 32 * w + lane;
         const bool mine = 32 * w + lane < nqb;
         const uint32_t L = mine ? a.L[q] : 0u;  // 0: this query falls back, nothing to record
-        live[w] = L != 0;
-        tm0[w] = (L & 1u) ? kFull : 0u;
-        tm1[w] = (L & 2u) ? kFull : 0u;
-        tm2[w] = (L & 4u) ? kFull : 0u;
-        tm3[w] = (L & 8u) ? kFull : 0u;
+        T0[w] = __ballot_sync(kFull, L & 1u);
+        T1[w] = __ballot_sync(kFull, L & 2u);
+        T2[w] = __ballot_sync(kFull, L & 4u);
+        T3[w] = __ballot_sync(kFull, L & 8u);
+        live[w] = __ballot_sync(kFull, L != 0);
         cnt[w] = 0;
         sc[w] = 0;
         tiles[w] = 0;
@@ -479,23 +495,23 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs 
     }
     const Xpose xp(lane);
     for (uint64_t t0 = lo; t0 < hi; t0 += 32) {
-        uint32_t B[W][4];
-        score_tile<W>(a, M, t0, hi, xp, B, lane);
+        uint32_t b[W][4];
+        score_planes<W>(a, M, t0, hi, b, lane);
 #pragma unroll
         for (uint32_t w = 0; w < W; ++w) {
-            if (!live[w]) continue;
-            // bit-sliced compare of the 32 scores with L, most significant plane first
-            uint32_t gt = B[w][3] & ~tm3[w], eq = ~(B[w][3] ^ tm3[w]);
-            gt |= eq & B[w][2] & ~tm2[w];
-            eq &= ~(B[w][2] ^ tm2[w]);
-            gt |= eq & B[w][1] & ~tm1[w];
-            eq &= ~(B[w][1] ^ tm1[w]);
-            gt |= eq & B[w][0] & ~tm0[w];
-            eq &= ~(B[w][0] ^ tm0[w]);
-            const uint32_t ge0 = gt | eq;  // score >= L (points past the piece end score 0 < L)
-            cnt[w] += __popc(ge0) | (__popc(gt) << 16);
+            // most significant plane first; points past the piece end score 0 < L
+            uint32_t gt = b[w][3] & ~T3[w], eq = ~(b[w][3] ^ T3[w]);
+            gt |= eq & b[w][2] & ~T2[w];
+            eq &= ~(b[w][2] ^ T2[w]);
+            gt |= eq & b[w][1] & ~T1[w];
+            eq &= ~(b[w][1] ^ T1[w]);
+            gt |= eq & b[w][0] & ~T0[w];
+            eq &= ~(b[w][0] ^ T0[w]);
+            const uint32_t ge0 = xp((gt | eq) & live[w]);  // lane = query, bit r = point t0 + r
+            const uint32_t g1 = xp(gt & live[w]);
+            cnt[w] += __popc(ge0) | (__popc(g1) << 16);
             if (ge0) {
-                if (sc[w] < a.C) a.slots[rec[w] + sc[w] * a.P] = make_uint2(ge0, gt);
+                if (sc[w] < a.C) a.slots[rec[w] + sc[w] * a.P] = make_uint2(ge0, g1);
                 tiles[w] |= 1ull << ((t0 - lo) >> 5);
                 ++sc[w];  // > C: overflow, the plan flags the query if the piece contributes
             }
