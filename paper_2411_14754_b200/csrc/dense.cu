@@ -36,6 +36,10 @@ namespace {
 // CTA shapes: 512 threads x 2 CTAs/SM when the masks fit 110 KB, else one
 // 1024-thread CTA per SM (masks up to 200 KB); a warp = one piece either way.
 constexpr uint32_t kFull = 0xffffffffu;
+#ifndef SUCO_FUSED_PPW
+#define SUCO_FUSED_PPW 2
+#endif
+constexpr uint32_t kFusedPPW = SUCO_FUSED_PPW;  // pieces per warp in the fused pass
 
 __device__ __forceinline__ void fadd(uint32_t a, uint32_t b, uint32_t c, uint32_t& s, uint32_t& cy) {
     s = a ^ b ^ c;
@@ -120,13 +124,15 @@ __device__ __forceinline__ void mask_at(const uint32_t* M, uint32_t slot, uint32
 
 // Bit-planes of the scores of the 32 points [t0, t0 + 32) (lane = point t0 + lane) for the
 // block's 32*W queries: b[w][i] bit j = bit i of query (32w + j)'s score.
-template <uint32_t W>
-__device__ __forceinline__ void score_planes(const DenseArgs& a, const uint32_t* M, uint64_t t0, uint64_t p_hi,
-                                             uint32_t (&b)[W][4], uint32_t lane) {
-    const uint64_t p = t0 + lane;
+__device__ __forceinline__ uint4 load_codes(const DenseArgs& a, uint64_t p, uint64_t p_hi) {
     const uint32_t none = a.ns * a.K;
     uint4 c = make_uint4(none | (none << 16), none | (none << 16), none | (none << 16), none | (none << 16));
     if (p < p_hi) c = __ldg(a.codes + p);
+    return c;
+}
+
+template <uint32_t W>
+__device__ __forceinline__ void planes_of(const uint32_t* M, uint4 c, uint32_t (&b)[W][4]) {
     uint32_t m[8][W];
     mask_at<W>(M, c.x & 0xffffu, m[0]);
     mask_at<W>(M, c.x >> 16, m[1]);
@@ -150,6 +156,12 @@ __device__ __forceinline__ void score_planes(const DenseArgs& a, const uint32_t*
         b[w][2] = c5 ^ c6;
         b[w][3] = c5 & c6;
     }
+}
+
+template <uint32_t W>
+__device__ __forceinline__ void score_planes(const DenseArgs& a, const uint32_t* M, uint64_t t0, uint64_t p_hi,
+                                             uint32_t (&b)[W][4], uint32_t lane) {
+    planes_of<W>(M, load_codes(a, t0 + lane, p_hi), b);
 }
 
 // The same scores with lane = query (word w: query 32w + lane): planes B[w][0..3] (bit r =
@@ -468,62 +480,71 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs 
     const uint32_t nqb = static_cast<uint32_t>(min_u64(32 * W, a.nq - q0));
     if (!__syncthreads_or(threadIdx.x < nqb && a.L[q0 + threadIdx.x] != 0)) return;  // all two-pass
     build_masks<kDT, W>(a, M, q0, nqb);
-    const uint32_t piece = blockIdx.y * kDW + warp;
-    if (piece >= a.P) return;
-    const uint64_t lo = uint64_t(piece) * a.WP;
-    const uint64_t hi = min_u64(a.n, lo + a.WP);
     // The bits of L[q] across the block's queries (word w, bit j = query 32w + j): one bit-sliced
     // comparison per tile, BEFORE the transpose (lane = point, bit = query), gives score > L and
     // score == L for all 32*W queries at once; only the two results are transposed (10 shuffles,
     // not 20 for the four planes). Counts per lane = query: #(score >= L) | #(score >= L+1) << 16.
-    uint32_t T0[W], T1[W], T2[W], T3[W], live[W], cnt[W], sc[W], rec[W];
-    uint64_t tiles[W];  // bit t: tile t produced a record
+    uint32_t T0[W], T1[W], T2[W], T3[W], live[W];
 #pragma unroll
     for (uint32_t w = 0; w < W; ++w) {
-        const uint64_t q = q0 + 32 * w + lane;
-        const bool mine = 32 * w + lane < nqb;
-        const uint32_t L = mine ? a.L[q] : 0u;  // 0: this query falls back, nothing to record
+        const uint32_t L = 32 * w + lane < nqb ? a.L[q0 + 32 * w + lane] : 0u;  // 0: falls back, no records
         T0[w] = __ballot_sync(kFull, L & 1u);
         T1[w] = __ballot_sync(kFull, L & 2u);
         T2[w] = __ballot_sync(kFull, L & 4u);
         T3[w] = __ballot_sync(kFull, L & 8u);
         live[w] = __ballot_sync(kFull, L != 0);
-        cnt[w] = 0;
-        sc[w] = 0;
-        tiles[w] = 0;
-        rec[w] = static_cast<uint32_t>((mine ? q : 0) * a.C * a.P + piece);  // record e at + e*P (< 2^32)
     }
     const Xpose xp(lane);
-    for (uint64_t t0 = lo; t0 < hi; t0 += 32) {
-        uint32_t b[W][4];
-        score_planes<W>(a, M, t0, hi, b, lane);
+    // a warp walks kFusedPPW consecutive pieces: the masks are built once per CTA for them all
+    for (uint32_t k = 0; k < kFusedPPW; ++k) {
+        const uint32_t piece = (blockIdx.y * kDW + warp) * kFusedPPW + k;
+        if (piece >= a.P) return;
+        const uint64_t lo = uint64_t(piece) * a.WP;
+        const uint64_t hi = min_u64(a.n, lo + a.WP);
+        uint32_t cnt[W], sc[W], rec[W];
+        uint64_t tiles[W];  // bit t: tile t produced a record
 #pragma unroll
         for (uint32_t w = 0; w < W; ++w) {
-            // most significant plane first; points past the piece end score 0 < L
-            uint32_t gt = b[w][3] & ~T3[w], eq = ~(b[w][3] ^ T3[w]);
-            gt |= eq & b[w][2] & ~T2[w];
-            eq &= ~(b[w][2] ^ T2[w]);
-            gt |= eq & b[w][1] & ~T1[w];
-            eq &= ~(b[w][1] ^ T1[w]);
-            gt |= eq & b[w][0] & ~T0[w];
-            eq &= ~(b[w][0] ^ T0[w]);
-            const uint32_t ge0 = xp((gt | eq) & live[w]);  // lane = query, bit r = point t0 + r
-            const uint32_t g1 = xp(gt & live[w]);
-            cnt[w] += __popc(ge0) | (__popc(g1) << 16);
-            if (ge0) {
-                if (sc[w] < a.C) a.slots[rec[w] + sc[w] * a.P] = make_uint2(ge0, g1);
-                tiles[w] |= 1ull << ((t0 - lo) >> 5);
-                ++sc[w];  // > C: overflow, the plan flags the query if the piece contributes
+            const bool mine = 32 * w + lane < nqb;
+            cnt[w] = 0;
+            sc[w] = 0;
+            tiles[w] = 0;
+            rec[w] = static_cast<uint32_t>((mine ? q0 + 32 * w + lane : 0) * a.C * a.P + piece);  // record e at + e*P
+        }
+        uint4 code = load_codes(a, lo + lane, hi);
+        for (uint64_t t0 = lo; t0 < hi; t0 += 32) {
+            const uint4 next = load_codes(a, t0 + 32 + lane, hi);  // one tile ahead
+            uint32_t b[W][4];
+            planes_of<W>(M, code, b);
+            code = next;
+#pragma unroll
+            for (uint32_t w = 0; w < W; ++w) {
+                // most significant plane first; points past the piece end score 0 < L
+                uint32_t gt = b[w][3] & ~T3[w], eq = ~(b[w][3] ^ T3[w]);
+                gt |= eq & b[w][2] & ~T2[w];
+                eq &= ~(b[w][2] ^ T2[w]);
+                gt |= eq & b[w][1] & ~T1[w];
+                eq &= ~(b[w][1] ^ T1[w]);
+                gt |= eq & b[w][0] & ~T0[w];
+                eq &= ~(b[w][0] ^ T0[w]);
+                const uint32_t ge0 = xp((gt | eq) & live[w]);  // lane = query, bit r = point t0 + r
+                const uint32_t g1 = xp(gt & live[w]);
+                cnt[w] += __popc(ge0) | (__popc(g1) << 16);
+                if (ge0) {
+                    if (sc[w] < a.C) a.slots[rec[w] + sc[w] * a.P] = make_uint2(ge0, g1);
+                    tiles[w] |= 1ull << ((t0 - lo) >> 5);
+                    ++sc[w];  // > C: overflow, the plan flags the query if the piece contributes
+                }
             }
         }
-    }
 #pragma unroll
-    for (uint32_t w = 0; w < W; ++w) {
-        if (32 * w + lane < nqb) {
-            const uint64_t q = q0 + 32 * w + lane;
-            a.h2[q * a.P + piece] = cnt[w];
-            a.scnt[q * a.P + piece] = static_cast<uint16_t>(sc[w]);
-            a.tmask[q * a.P + piece] = tiles[w];
+        for (uint32_t w = 0; w < W; ++w) {
+            if (32 * w + lane < nqb) {
+                const uint64_t q = q0 + 32 * w + lane;
+                a.h2[q * a.P + piece] = cnt[w];
+                a.scnt[q * a.P + piece] = static_cast<uint16_t>(sc[w]);
+                a.tmask[q * a.P + piece] = tiles[w];
+            }
         }
     }
 }
@@ -663,7 +684,8 @@ static cudaError_t launch_fused_t(const DenseArgs& a, size_t smem, cudaStream_t 
     cudaError_t e = cudaFuncSetAttribute(dense_fused_kernel<kDT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     constexpr uint32_t kDW = kDT / 32;
-    const dim3 grid(static_cast<unsigned>((a.nq + 32 * W - 1) / (32 * W)), (a.P + kDW - 1) / kDW);
+    const uint32_t per_cta = kDW * kFusedPPW;
+    const dim3 grid(static_cast<unsigned>((a.nq + 32 * W - 1) / (32 * W)), (a.P + per_cta - 1) / per_cta);
     dense_fused_kernel<kDT, W><<<grid, kDT, smem, st>>>(a);
     return cudaGetLastError();
 }
