@@ -39,7 +39,7 @@ constexpr uint32_t kFull = 0xffffffffu;
 #ifndef SUCO_FUSED_PPW
 #define SUCO_FUSED_PPW 2
 #endif
-constexpr uint32_t kFusedPPW = SUCO_FUSED_PPW;  // pieces per warp in the fused pass
+constexpr uint32_t kFusedPPW = SUCO_FUSED_PPW;  // pieces per warp in the fused pass (large batches)
 
 __device__ __forceinline__ void fadd(uint32_t a, uint32_t b, uint32_t c, uint32_t& s, uint32_t& cy) {
     s = a ^ b ^ c;
@@ -496,8 +496,8 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs 
     }
     const Xpose xp(lane);
     // a warp walks kFusedPPW consecutive pieces: the masks are built once per CTA for them all
-    for (uint32_t k = 0; k < kFusedPPW; ++k) {
-        const uint32_t piece = (blockIdx.y * kDW + warp) * kFusedPPW + k;
+    for (uint32_t k = 0; k < a.ppw; ++k) {
+        const uint32_t piece = (blockIdx.y * kDW + warp) * a.ppw + k;
         if (piece >= a.P) return;
         const uint64_t lo = uint64_t(piece) * a.WP;
         const uint64_t hi = min_u64(a.n, lo + a.WP);
@@ -684,9 +684,17 @@ static cudaError_t launch_fused_t(const DenseArgs& a, size_t smem, cudaStream_t 
     cudaError_t e = cudaFuncSetAttribute(dense_fused_kernel<kDT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     constexpr uint32_t kDW = kDT / 32;
-    const uint32_t per_cta = kDW * kFusedPPW;
-    const dim3 grid(static_cast<unsigned>((a.nq + 32 * W - 1) / (32 * W)), (a.P + per_cta - 1) / per_cta);
-    dense_fused_kernel<kDT, W><<<grid, kDT, smem, st>>>(a);
+    // pieces per warp: kFusedPPW amortises the mask build, unless that leaves fewer than about
+    // four CTAs per SM in the grid (small batches / corpora: one piece per warp)
+    const uint64_t qblocks = (a.nq + 32 * W - 1) / (32 * W);
+    int sms = 148, dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    DenseArgs b = a;
+    b.ppw = kFusedPPW;
+    if (qblocks * ((a.P + kDW * b.ppw - 1) / (kDW * b.ppw)) < 4ull * sms) b.ppw = 1;
+    const uint32_t per_cta = kDW * b.ppw;
+    const dim3 grid(static_cast<unsigned>(qblocks), (a.P + per_cta - 1) / per_cta);
+    dense_fused_kernel<kDT, W><<<grid, kDT, smem, st>>>(b);
     return cudaGetLastError();
 }
 

@@ -108,6 +108,7 @@ struct DenseArgs {
     uint32_t* h2;              // single pass: nq x P, #score >= L | #score >= L+1 << 16
     uint32_t* qmap;            // fallback emission: block-local query j -> query qmap[q0 + j]
     uint32_t* nmap;            // device count of qmap entries
+    uint32_t ppw;                 // fused pass: pieces per warp (set by the launcher)
 };
 bool dense_supported(uint32_t ns, uint32_t K);
 size_t dense_smem(uint32_t ns, uint32_t K);

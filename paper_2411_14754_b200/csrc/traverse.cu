@@ -12,6 +12,8 @@
 // each row keeps the global sizes of its next two cells prefetched, so the
 // serial cumulative check rarely waits on L2.
 #include <cuda_runtime.h>
+
+#include <cstdlib>
 #include <stdint.h>
 
 #include "common.cuh"
@@ -364,6 +366,166 @@ __global__ void __launch_bounds__(256, 5) traverse_kernel(TraverseArgs a, uint32
            a.dbg_sum ? a.dbg_sum + t * a.K : nullptr, a.dbg_cum ? a.dbg_cum + t * a.K : nullptr, a.stat_cum, lane);
 }
 
+// ---------------------------------------------------------------------------
+// Thread-per-task traversal (k_half <= 128): one thread owns one (query,
+// subspace) task end to end; a CTA holds tasks of ONE subspace, so that
+// subspace's cell sizes sit in shared memory and the cumulative check never
+// waits on L2.
+//
+// Dynamic Activation is the k-way merge of the k rows (row r = cells
+// (r, 0..k-1) in second-half rank order) by (d1r[r] + d2r[j], r): an
+// unactivated row r's head (r, 0) never beats row r-1's, which is still at
+// (r-1, 0) while r is unactivated (d1r ascending, rounding monotone, ties to
+// the lower row) — so merging all rows from the start pops exactly the
+// reference's sequence (query.cpp:66-121), and the debug outputs match too.
+// The merge is a loser tree over L >= k leaves: the initial heads are already
+// in (key, row) order, so every node's loser is the leftmost leaf of its right
+// subtree (closed form, no comparisons). A pop replays one leaf-to-root path
+// whose nodes depend only on the row, so all its loads issue at once.
+//
+// Per-thread arrays are interleaved [element][thread]: threads reading the
+// same element index hit consecutive words.
+template <uint32_t L>
+__global__ void traverse_thread_kernel(TraverseArgs a) {
+    constexpr uint32_t LOG = L == 64 ? 6 : 7;
+    static_assert(L == 64 || L == 128, "leaves");
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t T = blockDim.x, t = threadIdx.x;
+    const uint32_t s = blockIdx.y, k = a.k_half, K = a.K;
+    double* tkey = reinterpret_cast<double*>(smem);  // [L][T]: loser keys (nodes 1..L-1); ranking scratch
+    double* d1r = tkey + L * T;                       // [k][T]
+    double* d2r = d1r + k * T;                        // [k][T]
+    uint32_t* cs = reinterpret_cast<uint32_t*>(d2r + k * T);  // [K] this subspace's cell sizes
+    float* qh = reinterpret_cast<float*>(cs + K);              // [hmax][T]
+    uint8_t* trow = reinterpret_cast<uint8_t*>(qh + a.hmax * T);  // [L][T]
+    uint8_t* o1 = trow + L * T;  // [k][T]
+    uint8_t* o2 = o1 + k * T;
+    uint8_t* cur = o2 + k * T;
+    for (uint32_t i = t; i < K; i += T) cs[i] = __ldg(a.cell_size + static_cast<size_t>(s) * K + i);
+    __syncthreads();
+    const uint64_t q = static_cast<uint64_t>(blockIdx.x) * T + t;
+    if (q >= a.nq) return;
+    const SubDesc sd = a.sub[s];
+    const float* query = a.queries + q * a.d;
+
+    // centroid_distances (query.cpp:42-64) for both halves, ranked by (dist, id)
+#pragma unroll 1
+    for (uint32_t half = 0; half < 2; ++half) {
+        const uint32_t h = half ? sd.h2 : sd.h1;
+        const uint32_t* dims = a.dims + (half ? sd.dims2 : sd.dims1);
+        const float* cent = a.cent + (half ? sd.cent2 : sd.cent1);
+        double* dr = half ? d2r : d1r;
+        uint8_t* ord = half ? o2 : o1;
+        for (uint32_t i = 0; i < h; ++i) qh[i * T + t] = query[__ldg(dims + i)];
+        for (uint32_t c = 0; c < k; ++c) {  // sq_euclidean_raw (core.hpp:66-84) then sqrt
+            const float* cc = cent + static_cast<size_t>(c) * h;
+            double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+            uint32_t i = 0;
+            for (; i + 4 <= h; i += 4) {
+                acc0 = __dadd_rn(acc0, sqdiff(__ldg(cc + i), qh[i * T + t]));
+                acc1 = __dadd_rn(acc1, sqdiff(__ldg(cc + i + 1), qh[(i + 1) * T + t]));
+                acc2 = __dadd_rn(acc2, sqdiff(__ldg(cc + i + 2), qh[(i + 2) * T + t]));
+                acc3 = __dadd_rn(acc3, sqdiff(__ldg(cc + i + 3), qh[(i + 3) * T + t]));
+            }
+            for (; i < h; ++i) acc0 = __dadd_rn(acc0, sqdiff(__ldg(cc + i), qh[i * T + t]));
+            tkey[c * T + t] = __dsqrt_rn(__dadd_rn(__dadd_rn(acc0, acc1), __dadd_rn(acc2, acc3)));
+        }
+        // rank of c = #{o : (d_o, o) < (d_c, c)}; four c per pass over o, the id tie-break folded
+        // into the loop bounds (o < c0: <=, o >= c0 + 4: <, the group itself: exact)
+        for (uint32_t c0 = 0; c0 < k; c0 += 4) {
+            double dc[4];
+            uint32_t r[4];
+#pragma unroll
+            for (uint32_t u = 0; u < 4; ++u) {
+                dc[u] = c0 + u < k ? tkey[(c0 + u) * T + t] : kInf;
+                r[u] = 0;
+            }
+            for (uint32_t o = 0; o < c0; ++o) {
+                const double v = tkey[o * T + t];
+#pragma unroll
+                for (uint32_t u = 0; u < 4; ++u) r[u] += v <= dc[u];
+            }
+            for (uint32_t o = c0; o < c0 + 4 && o < k; ++o) {
+                const double v = tkey[o * T + t];
+#pragma unroll
+                for (uint32_t u = 0; u < 4; ++u) r[u] += v < dc[u] || (v == dc[u] && o < c0 + u);
+            }
+            for (uint32_t o = c0 + 4; o < k; ++o) {
+                const double v = tkey[o * T + t];
+#pragma unroll
+                for (uint32_t u = 0; u < 4; ++u) r[u] += v < dc[u];
+            }
+#pragma unroll
+            for (uint32_t u = 0; u < 4; ++u) {
+                if (c0 + u < k) {
+                    dr[r[u] * T + t] = dc[u];
+                    ord[r[u] * T + t] = static_cast<uint8_t>(c0 + u);
+                }
+            }
+        }
+    }
+
+    // loser tree over the row heads (r, 0): node n at level lv loses with the leftmost leaf of its
+    // right child
+    const double d20 = d2r[t];
+    for (uint32_t lv = 0; lv < LOG; ++lv) {
+        for (uint32_t n = 1u << lv; n < (2u << lv); ++n) {
+            const uint32_t leaf = ((2 * n + 1) << (LOG - lv - 1)) - L;
+            tkey[n * T + t] = leaf < k ? __dadd_rn(d1r[leaf * T + t], d20) : kInf;
+            trow[n * T + t] = static_cast<uint8_t>(leaf);
+        }
+    }
+    for (uint32_t r = 0; r < k; ++r) cur[r * T + t] = 0;
+    double wkey = __dadd_rn(d1r[t], d20);
+    uint32_t wrow = 0;
+
+    const uint64_t task = q * a.ns + s;
+    uint32_t* out = a.cells + task * K;
+    double* dbg_sum = a.dbg_sum ? a.dbg_sum + task * K : nullptr;
+    uint64_t* dbg_cum = a.dbg_cum ? a.dbg_cum + task * K : nullptr;
+    uint32_t ncell = 0;
+    uint64_t cum = 0;
+    while (cum < a.target) {
+        if (wkey == kInf) break;  // unreachable while the IMI partitions all n points
+        const uint32_t row = wrow, j = cur[row * T + t];
+        const uint32_t cell = static_cast<uint32_t>(o1[row * T + t]) * k + o2[j * T + t];
+        cum += cs[cell];
+        out[ncell] = cell;
+        if (dbg_sum) {
+            dbg_sum[ncell] = wkey;
+            dbg_cum[ncell] = cum;
+        }
+        ++ncell;
+        // the row's next cell (query.cpp:113-118), then replay its leaf-to-root path
+        const uint32_t j1 = j + 1;
+        cur[row * T + t] = static_cast<uint8_t>(j1);
+        double ck = j1 < k ? __dadd_rn(d1r[row * T + t], d2r[j1 * T + t]) : kInf;
+        uint32_t cr = row;
+        const uint32_t n0 = (row + L) >> 1;
+        double pk[LOG];
+        uint32_t pr[LOG];
+#pragma unroll
+        for (uint32_t lv = 0; lv < LOG; ++lv) {
+            pk[lv] = tkey[(n0 >> lv) * T + t];
+            pr[lv] = trow[(n0 >> lv) * T + t];
+        }
+#pragma unroll
+        for (uint32_t lv = 0; lv < LOG; ++lv) {
+            if (pk[lv] < ck || (pk[lv] == ck && pr[lv] < cr)) {  // the stored loser wins: swap
+                const uint32_t n = n0 >> lv;
+                tkey[n * T + t] = ck;
+                trow[n * T + t] = static_cast<uint8_t>(cr);
+                ck = pk[lv];
+                cr = pr[lv];
+            }
+        }
+        wkey = ck;
+        wrow = cr;
+    }
+    a.ncells[task] = ncell;
+    if (a.stat_cum) atomicAdd(a.stat_cum, static_cast<unsigned long long>(cum));
+}
+
 __global__ void centroid_distances_kernel(const float* q, uint32_t dim, const float* cent, uint32_t k,
                                           double* dists, uint32_t* order) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -398,6 +560,33 @@ static size_t da_extra_bytes(uint32_t k) { return k > 256 ? static_cast<size_t>(
 
 cudaError_t launch_traverse(const TraverseArgs& a, cudaStream_t st) {
     if (a.nq == 0) return cudaSuccess;
+    const char* tv = std::getenv("SUCO_TRAVERSE");  // A/B and tests: "warp" forces the warp-per-task kernel
+    const bool warp_path = tv && tv[0] == 'w';
+    if (a.k_half <= 128 && !warp_path) {
+        const uint32_t L = a.k_half <= 64 ? 64 : 128;
+        // per thread: tkey (L f64), d1r/d2r (2k f64), qh (hmax f32), trow (L), o1/o2/cur (3k u8)
+        const size_t per_t = size_t(L) * 9 + size_t(a.k_half) * 19 + size_t(a.hmax) * 4;
+        const size_t fixed = size_t(a.K) * 4 + 16;
+        uint32_t best_T = 0, best_res = 0;
+        for (uint32_t T = 32; T <= 256; T += 32) {  // most resident tasks per SM within 227 KB / CTA
+            const size_t smem = fixed + per_t * T;
+            if (smem > 227 * 1024) break;
+            const uint32_t res = static_cast<uint32_t>((228 * 1024) / (smem + 1024)) * T;
+            if (res > best_res) {
+                best_res = res;
+                best_T = T;
+            }
+        }
+        if (best_T) {  // measured faster at every bench config (cfg1 0.22 -> 0.19 ms, cfg2 1.25 -> 0.64)
+            const size_t smem = fixed + per_t * best_T;
+            auto kern = L == 64 ? traverse_thread_kernel<64> : traverse_thread_kernel<128>;
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            if (e != cudaSuccess) return e;
+            const dim3 grid(static_cast<unsigned>((a.nq + best_T - 1) / best_T), a.ns);
+            kern<<<grid, best_T, smem, st>>>(a);
+            return cudaGetLastError();
+        }
+    }
     const size_t per_warp = ((warp_smem_bytes(a.k_half, a.hmax) + da_extra_bytes(a.k_half) + 15) / 16) * 16;
     uint32_t wpb = static_cast<uint32_t>(48 * 1024 / per_warp);
     if (wpb > 8) wpb = 8;

@@ -175,11 +175,17 @@ CASES = {
     "tiny_touch": (2500, 16, 8, 0, 50, 3, False, 2, 8, 3, 0, [(0.0005, 0.4, 10), (0.001, 1.0, 25)]),
     # 64 x 64 cells: 128 KB of dense-select masks -> the 1024-thread, 1 CTA/SM variant
     "dense_1024": (20000, 32, 40, 0, 100, 8, False, 8, 64, 2, 0, [(0.05, 0.005, 10), (0.02, 0.05, 40)]),
+    # 100 x 100 cells: the 128-leaf merge tree of the thread-per-task traversal
+    "k100": (12000, 16, 20, 0, 100, 8, False, 2, 100, 2, 1, [(0.05, 0.01, 10), (0.2, 0.003, 5)]),
 }
 
 
+@pytest.mark.parametrize("trav", ["warp", "thread"])
 @pytest.mark.parametrize("case", list(CASES))
-def test_knn_vs_oracle(gpu, oracle, case):
+def test_knn_vs_oracle(gpu, oracle, case, trav, monkeypatch):
+    """Both traversal kernels (warp per task; thread per task with the merge tree, which large batches
+    use) against the reference, cell order and cumulative sizes included."""
+    monkeypatch.setenv("SUCO_TRAVERSE", trav)
     n, d, cl, lo, hi, sig, quant, ns, kh, it, mode, plist = CASES[case]
     full = oracle.clustered(n + 40, d, cl, 1000 + n, lo, hi, sig, quant)
     base, qs = oracle.hold_out(full, 40, 1001 + n)
