@@ -129,9 +129,8 @@ struct suco_gpu_index {
         DevBuf<uint32_t> cells, ncells, cands, out_ids, all_id;
         DevBuf<uint16_t> dhist;               // dense select: nq x P x 8
         DevBuf<uint32_t> dT, dquota, dbase;   // dense select plan
-        DevBuf<uint16_t> dsample, dscnt;          // single-pass select: sampled hist, record counts
-        DevBuf<uint2> dslots;                     // single-pass select: tile records
-        DevBuf<uint64_t> dtmask;                  // single-pass select: tiles with records
+        DevBuf<uint16_t> dsample;                 // single-pass select: sampled histograms
+        DevBuf<uint16_t> dcbuf, dccnt;            // single-pass select: candidate buffers and their counts
         DevBuf<uint32_t> dL, dflag, dh2;          // single-pass select: bound, fallback flags, two-level counts
         DevBuf<double> out_d, all_d;
         cudaEvent_t trav = nullptr, sel = nullptr, rr = nullptr;
@@ -367,7 +366,7 @@ uint64_t tile_size(const suco_gpu_index* x, uint64_t nq, uint64_t m, uint32_t k)
     const uint64_t ns = x->host.layout.ns;
     const uint64_t pieces = (x->host.n + 2047) / 2048;  // dense select scratch: hist (16 B) + quota/base per piece
     const uint64_t per = ns * x->K * 4 + ns * 4 + m * 4 + (k > 32 ? m * 12 : 0) + uint64_t(x->host.d) * 4 + k * 12 +
-                         (x->dense ? pieces * (24 + 32 * 8 + 14) + pieces / 16 * 16 + 16 : 0);  // + tile records
+                         (x->dense ? pieces * (24 + kDenseBuf * 2 + 14) + pieces / 16 * 16 + 16 : 0);  // + buffers
     const uint64_t budget = 16ull << 30;  // per-batch scratch on a 180 GB part
     return std::max<uint64_t>(1, std::min<uint64_t>(nq, budget / per));
 }
@@ -458,14 +457,17 @@ void stage_select(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nt, uint
         const char* fv = std::getenv("SUCO_DENSE_FUSED");
         const bool fused = !(fv && std::atoi(fv) == 0);
         if (fused) {
-            da.pstride = 16;
+            // the sampled histograms (every pstride-th piece) predict the threshold; at least ~32
+            // sampled pieces (small corpora: all of them, so the prediction is exact)
+            da.pstride = std::max<uint32_t>(1, std::min<uint32_t>(16, da.P / 32));
             da.Ps = (da.P + da.pstride - 1) / da.pstride;
-            da.C = 32;  // records per (query, piece); more (dense supersets) flag the query
             sl.dsample.reserve(nt * da.Ps * 8);
-            sl.dslots.reserve(nt * da.P * da.C);
-            sl.dtmask.reserve(nt * da.P);
-            da.tmask = sl.dtmask.p;
-            sl.dscnt.reserve(nt * da.P);
+            da.stage_all = std::getenv("SUCO_DENSE_STAGE") != nullptr;
+            da.B = kDenseBuf;  // entries per (piece, query): ~6 sigma above cfg4's mean of 46
+            sl.dcbuf.reserve(nt * da.P * da.B);
+            sl.dccnt.reserve(nt * da.P);
+            da.cbuf = sl.dcbuf.p;
+            da.ccnt = sl.dccnt.p;
             sl.dL.reserve(nt);
             sl.dh2.reserve(nt * da.P);
             da.h2 = sl.dh2.p;
@@ -473,8 +475,6 @@ void stage_select(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nt, uint
             da.hsample = sl.dsample.p;
             da.qmap = sl.dflag.p + nt;
             da.nmap = sl.dflag.p + 2 * nt;
-            da.slots = sl.dslots.p;
-            da.scnt = sl.dscnt.p;
             da.L = sl.dL.p;
             da.qflag = sl.dflag.p;
         }
@@ -483,6 +483,28 @@ void stage_select(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nt, uint
         // two-pass: piece histograms, plan, emission; single pass: sample, bound, fused pass, plan,
         // compaction, flagged list, fallback histograms, plan, emission
         x->launches += fused ? 9 : 3;
+        const bool stats = std::getenv("SUCO_DENSE_STATS") != nullptr;  // diagnostics: fallback rate
+        if (stats && fused) {
+            uint32_t nflag = 0;
+            std::vector<uint32_t> Lh(nt);
+            CUDA_TRY(cudaMemcpyAsync(&nflag, da.nmap, 4, cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaMemcpyAsync(Lh.data(), da.L, nt * 4, cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaStreamSynchronize(st));
+            uint64_t gated = 0, hist[9] = {};
+            for (uint32_t v : Lh) {
+                v &= 0xffu;
+                gated += v == 0;
+                hist[std::min<uint32_t>(v, 8)]++;
+            }
+            std::fprintf(stderr,
+                         "[suco] dense select: %u of %llu queries took the two-pass fallback (pstride %u; L = 0 "
+                         "(density gate / no bound) for %llu; L histogram 0..8: %llu %llu %llu %llu %llu %llu %llu "
+                         "%llu %llu)\n",
+                         nflag, static_cast<unsigned long long>(nt), da.pstride, static_cast<unsigned long long>(gated),
+                         (unsigned long long)hist[0], (unsigned long long)hist[1], (unsigned long long)hist[2],
+                         (unsigned long long)hist[3], (unsigned long long)hist[4], (unsigned long long)hist[5],
+                         (unsigned long long)hist[6], (unsigned long long)hist[7], (unsigned long long)hist[8]);
+        }
         if (ev) CUDA_TRY(cudaEventRecord(ev[1], st));
         return;
     }

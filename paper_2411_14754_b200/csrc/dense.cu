@@ -36,6 +36,7 @@ namespace {
 // CTA shapes: 512 threads x 2 CTAs/SM when the masks fit 110 KB, else one
 // 1024-thread CTA per SM (masks up to 200 KB); a warp = one piece either way.
 constexpr uint32_t kFull = 0xffffffffu;
+constexpr uint32_t kDenseStage = 0x100u;  // L[q] flag: dense superset (the fused pass stages stores)
 #ifndef SUCO_FUSED_PPW
 #define SUCO_FUSED_PPW 2
 #endif
@@ -329,7 +330,7 @@ __global__ void __launch_bounds__(256) dense_plan_fused_kernel(DenseArgs a) {
         geL += __shfl_xor_sync(kFull, geL, o);
         geL1 += __shfl_xor_sync(kFull, geL1, o);
     }
-    const uint32_t L = a.L[q];
+    const uint32_t L = a.L[q] & 0xffu;
     bool ok = L >= 1 && geL >= a.m && geL1 < a.m;
     const uint64_t need = a.m - geL1;
     uint64_t ties_run = 0, out_run = 0;
@@ -361,7 +362,7 @@ __global__ void __launch_bounds__(256) dense_plan_fused_kernel(DenseArgs a) {
         if (p < a.P) {
             a.quota[q * a.P + p] = quota;
             a.base[q * a.P + p] = static_cast<uint32_t>(out_run + ox - take);
-            if (take && a.scnt[q * a.P + p] > a.C) ok = false;  // a contributing piece overflowed
+            if (take && a.ccnt[q * a.P + p] > a.B) ok = false;  // a contributing buffer overflowed
         }
         ties_run += tsum;
         out_run += osum;
@@ -462,54 +463,38 @@ __global__ void __launch_bounds__(256) dense_bound_kernel(DenseArgs a) {
             atL = tot[t - 1];
         }
     }
-    // The single pass writes one record per tile holding a point with score >= L: worth it while
-    // those points are sparse (cfg2: 0.65% of points, ~12 of 64 tiles per piece). Denser supersets
-    // (cfg4: 2.2%, about half the tiles) go to the two-pass select (L = 0).
-    if (L && static_cast<double>(atL) > 0.01 * static_cast<double>(sampled)) L = 0;
-    if (lane == 0) a.L[q] = L;
+    // The single pass writes one 8-byte record per tile holding a point with score >= L, at most
+    // 0.25 B per (point, query) even when every tile has one; a second scoring pass costs more.
+    // dense supersets (> 1% of the points at L) make the fused pass stage its stores
+    const bool dense = L && (a.stage_all || static_cast<double>(atL) > 0.01 * static_cast<double>(sampled));
+    if (lane == 0) a.L[q] = L | (dense ? kDenseStage : 0u);
 }
 
-// K3': one pass — the piece histograms (as K1) plus, per (query, piece), every point with
-// score >= L[q] in id order into its slot (in-piece offset << 4 | score; count may exceed C).
-template <uint32_t kDT, uint32_t W>
-__global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs a) {
-    constexpr uint32_t kDW = kDT / 32;
-    extern __shared__ uint32_t M[];
-    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    const uint64_t q0 = uint64_t(blockIdx.x) * 32 * W;
-    const uint32_t nqb = static_cast<uint32_t>(min_u64(32 * W, a.nq - q0));
-    if (!__syncthreads_or(threadIdx.x < nqb && a.L[q0 + threadIdx.x] != 0)) return;  // all two-pass
-    build_masks<kDT, W>(a, M, q0, nqb);
-    // The bits of L[q] across the block's queries (word w, bit j = query 32w + j): one bit-sliced
-    // comparison per tile, BEFORE the transpose (lane = point, bit = query), gives score > L and
-    // score == L for all 32*W queries at once; only the two results are transposed (10 shuffles,
-    // not 20 for the four planes). Counts per lane = query: #(score >= L) | #(score >= L+1) << 16.
-    uint32_t T0[W], T1[W], T2[W], T3[W], live[W];
-#pragma unroll
-    for (uint32_t w = 0; w < W; ++w) {
-        const uint32_t L = 32 * w + lane < nqb ? a.L[q0 + 32 * w + lane] : 0u;  // 0: falls back, no records
-        T0[w] = __ballot_sync(kFull, L & 1u);
-        T1[w] = __ballot_sync(kFull, L & 2u);
-        T2[w] = __ballot_sync(kFull, L & 4u);
-        T3[w] = __ballot_sync(kFull, L & 8u);
-        live[w] = __ballot_sync(kFull, L != 0);
-    }
+// The fused pass's walk over a warp's pieces (below). STAGE: entries go through a 64-bit register
+// (four per 8-byte store) — for dense supersets, where 2-byte stores multiply DRAM traffic; sparse
+// ones store each entry directly (fewer instructions per tile).
+template <uint32_t kDW, uint32_t W, bool STAGE>
+__device__ __forceinline__ void fused_pieces(const DenseArgs& a, const uint32_t* M, uint64_t q0, uint32_t nqb,
+                                             const uint32_t (&T0)[W], const uint32_t (&T1)[W],
+                                             const uint32_t (&T2)[W], const uint32_t (&T3)[W],
+                                             const uint32_t (&live)[W], uint32_t lane, uint32_t warp) {
     const Xpose xp(lane);
-    // a warp walks kFusedPPW consecutive pieces: the masks are built once per CTA for them all
+    // a warp walks ppw consecutive pieces: the masks are built once per CTA for them all
     for (uint32_t k = 0; k < a.ppw; ++k) {
         const uint32_t piece = (blockIdx.y * kDW + warp) * a.ppw + k;
         if (piece >= a.P) return;
         const uint64_t lo = uint64_t(piece) * a.WP;
         const uint64_t hi = min_u64(a.n, lo + a.WP);
-        uint32_t cnt[W], sc[W], rec[W];
-        uint64_t tiles[W];  // bit t: tile t produced a record
+        uint32_t cnt[W], nb[W];
+        uint16_t* buf[W];  // [query][piece][B]: a lane appends to its own contiguous buffer
+        uint64_t sw[W];    // STAGE: four entries shifted in from the top
 #pragma unroll
         for (uint32_t w = 0; w < W; ++w) {
-            const bool mine = 32 * w + lane < nqb;
             cnt[w] = 0;
-            sc[w] = 0;
-            tiles[w] = 0;
-            rec[w] = static_cast<uint32_t>((mine ? q0 + 32 * w + lane : 0) * a.C * a.P + piece);  // record e at + e*P
+            nb[w] = 0;
+            sw[w] = 0;
+            const uint64_t q = 32 * w + lane < nqb ? q0 + 32 * w + lane : q0;  // idle lanes append nothing
+            buf[w] = a.cbuf + (q * a.P + piece) * a.B;
         }
         uint4 code = load_codes(a, lo + lane, hi);
         for (uint64_t t0 = lo; t0 < hi; t0 += 32) {
@@ -517,6 +502,7 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs 
             uint32_t b[W][4];
             planes_of<W>(M, code, b);
             code = next;
+            const uint32_t tb = static_cast<uint32_t>(t0 - lo);
 #pragma unroll
             for (uint32_t w = 0; w < W; ++w) {
                 // most significant plane first; points past the piece end score 0 < L
@@ -530,56 +516,102 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs 
                 const uint32_t ge0 = xp((gt | eq) & live[w]);  // lane = query, bit r = point t0 + r
                 const uint32_t g1 = xp(gt & live[w]);
                 cnt[w] += __popc(ge0) | (__popc(g1) << 16);
-                if (ge0) {
-                    if (sc[w] < a.C) a.slots[rec[w] + sc[w] * a.P] = make_uint2(ge0, g1);
-                    tiles[w] |= 1ull << ((t0 - lo) >> 5);
-                    ++sc[w];  // > C: overflow, the plan flags the query if the piece contributes
+                uint32_t bits = ge0;
+                while (bits) {  // id order
+                    const uint32_t r = __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    if (nb[w] < a.B) {
+                        const uint32_t v = (tb + r) | (((g1 >> r) & 1u) << 15);
+                        if constexpr (STAGE) {
+                            sw[w] = (sw[w] >> 16) | (static_cast<uint64_t>(v) << 48);
+                            if ((nb[w] & 3u) == 3u) *reinterpret_cast<uint64_t*>(buf[w] + (nb[w] & ~3u)) = sw[w];
+                        } else {
+                            buf[w][nb[w]] = static_cast<uint16_t>(v);
+                        }
+                    }
+                    ++nb[w];
                 }
             }
         }
 #pragma unroll
         for (uint32_t w = 0; w < W; ++w) {
             if (32 * w + lane < nqb) {
-                const uint64_t q = q0 + 32 * w + lane;
-                a.h2[q * a.P + piece] = cnt[w];
-                a.scnt[q * a.P + piece] = static_cast<uint16_t>(sc[w]);
-                a.tmask[q * a.P + piece] = tiles[w];
+                const uint64_t i = (q0 + 32 * w + lane) * a.P + piece;
+                if constexpr (STAGE) {
+                    const uint32_t kept = min(nb[w], a.B), part = kept & 3u;
+                    if (part)  // the last, partial chunk: its entries down to the low end
+                        *reinterpret_cast<uint64_t*>(buf[w] + (kept & ~3u)) = sw[w] >> (16 * (4 - part));
+                }
+                a.h2[i] = cnt[w];
+                a.ccnt[i] = static_cast<uint16_t>(nb[w]);  // <= WP = 2048
             }
         }
     }
 }
 
-// K4: thread per (query, piece), T == L: every score > T (the L+1 masks), then the first quota
-// ties (score == T) in id order, expanded from the piece's tile records. Records are laid out
-// [query][record][piece], so neighbouring threads (pieces) read neighbouring words.
+// K3': one pass — the piece histograms (as K1) plus, per (query, piece), every point with
+// score >= L[q] appended in id order to the pair's candidate buffer: the in-piece offset, bit 15
+// set when the score is > L. A buffer holds B entries; a contributing piece that found more flags
+// its query for the exact fallback.
+template <uint32_t kDT, uint32_t W>
+__global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs a) {
+    constexpr uint32_t kDW = kDT / 32;
+    extern __shared__ uint32_t M[];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint64_t q0 = uint64_t(blockIdx.x) * 32 * W;
+    const uint32_t nqb = static_cast<uint32_t>(min_u64(32 * W, a.nq - q0));
+    const uint32_t myL = threadIdx.x < nqb ? a.L[q0 + threadIdx.x] : 0u;
+    if (!__syncthreads_or((myL & 0xffu) != 0)) return;  // all two-pass
+    const bool stage = __syncthreads_or(myL & kDenseStage);  // a dense superset in the block
+    build_masks<kDT, W>(a, M, q0, nqb);
+    // The bits of L[q] across the block's queries (word w, bit j = query 32w + j): one bit-sliced
+    // comparison per tile, BEFORE the transpose (lane = point, bit = query), gives score > L and
+    // score == L for all 32*W queries at once; only the two results are transposed (10 shuffles,
+    // not 20 for the four planes). Counts per lane = query: #(score >= L) | #(score >= L+1) << 16.
+    uint32_t T0[W], T1[W], T2[W], T3[W], live[W];
+#pragma unroll
+    for (uint32_t w = 0; w < W; ++w) {
+        const uint32_t L = 32 * w + lane < nqb ? a.L[q0 + 32 * w + lane] & 0xffu : 0u;  // 0: falls back
+        T0[w] = __ballot_sync(kFull, L & 1u);
+        T1[w] = __ballot_sync(kFull, L & 2u);
+        T2[w] = __ballot_sync(kFull, L & 4u);
+        T3[w] = __ballot_sync(kFull, L & 8u);
+        live[w] = __ballot_sync(kFull, L != 0);
+    }
+    if (stage) fused_pieces<kDW, W, true>(a, M, q0, nqb, T0, T1, T2, T3, live, lane, warp);
+    else fused_pieces<kDW, W, false>(a, M, q0, nqb, T0, T1, T2, T3, live, lane, warp);
+}
+
+// K4: thread per (query, piece), T == L: the piece's buffer holds its score >= T points in id
+// order; keep every score > T and the first quota ties. Neighbouring threads take neighbouring
+// pieces: contiguous buffers in, contiguous candidate runs out.
 __global__ void __launch_bounds__(256) dense_compact_kernel(DenseArgs a) {
     const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
     if (i >= a.nq * a.P) return;
     const uint64_t q = i / a.P;
     const uint32_t p = static_cast<uint32_t>(i % a.P);
-    if (a.qflag[q]) return;
+    const uint32_t n = a.ccnt[i];
+    if (!n || a.qflag[q]) return;  // (n <= B: an overflowing contributing piece flags its query)
     uint32_t quota = a.quota[i];
     uint32_t pos = a.base[i];
-    const uint32_t cnt = min(static_cast<uint32_t>(a.scnt[i]), a.C);  // == scnt (overflow is flagged)
-    const uint64_t r0 = q * a.C * a.P + p;  // record e at r0 + e * P
     uint32_t* out = a.cands + q * a.m;
     const uint32_t pbase = p * a.WP;
-    uint64_t tiles = a.tmask[i];
-    for (uint32_t e = 0; e < cnt; ++e) {
-        const uint2 r = a.slots[r0 + uint64_t(e) * a.P];
-        const uint32_t tb = pbase + (static_cast<uint32_t>(__ffsll(static_cast<long long>(tiles)) - 1) << 5);
-        tiles &= tiles - 1;
-        uint32_t take = r.y;  // score > T
-        uint32_t ties = r.x & ~r.y;
-        while (ties && quota) {  // first ties in id order
-            take |= ties & (0u - ties);
-            ties &= ties - 1;
-            --quota;
-        }
-        while (take) {
-            const uint32_t b = __ffs(take) - 1;
-            take &= take - 1;
-            __stcs(out + pos++, tb + b);
+    const uint4* buf = reinterpret_cast<const uint4*>(a.cbuf + i * a.B);
+    const uint32_t lim = min(n, a.B);
+    for (uint32_t e0 = 0; e0 < lim; e0 += 8) {
+        const uint4 v = buf[e0 >> 3];
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (uint32_t e = 0; e < 8; ++e) {
+            if (e0 + e < lim) {
+                const uint32_t x = (w[e >> 1] >> ((e & 1) * 16)) & 0xffffu;
+                if (x & 0x8000u) {
+                    __stcs(out + pos++, pbase + (x & 0x7fffu));
+                } else if (quota) {  // first ties in id order
+                    --quota;
+                    __stcs(out + pos++, pbase + x);
+                }
+            }
         }
     }
 }
@@ -634,7 +666,7 @@ static Shape dense_shape(const DenseArgs& a) {
     const char* wv = std::getenv("SUCO_DENSE_WORDS");
     // the single-pass pipeline measured faster with 32-query blocks (3.75 vs 3.89 ms at cfg2),
     // the two-pass one with 64-query blocks (5.04 vs 5.52 ms)
-    const bool allow2 = wv ? std::atoi(wv) == 2 : a.slots == nullptr;
+    const bool allow2 = wv ? std::atoi(wv) == 2 : a.cbuf == nullptr;
     if (allow2 && 2 * smem1 <= 200 * 1024) return {1024, 2, 2 * smem1};
     return {smem1 <= 110 * 1024 ? 512u : 1024u, 1, smem1};
 }

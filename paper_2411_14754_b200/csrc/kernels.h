@@ -100,15 +100,15 @@ struct DenseArgs {
     uint16_t* hsample;         // nq x Ps x 8 sampled histograms (K0)
     uint32_t Ps;               // sampled pieces
     uint32_t* L;               // nq
-    uint2* slots;              // nq x P x C records (score >= L mask, score >= L+1 mask) of non-empty tiles
-    uint64_t* tmask;           // nq x P: tiles that produced a record (record e = e-th set bit)
-    uint16_t* scnt;            // nq x P records per (query, piece)
+    uint16_t* cbuf;            // single pass: [query][piece][B] in-piece offsets of score >= L (bit 15: > L)
+    uint16_t* ccnt;            // single pass: nq x P entries found (may exceed B)
     uint32_t* qflag;           // nq: 1 = fall back to the exact two-pass emission for this query
-    uint32_t C;
+    uint32_t B;                // single pass: candidate buffer entries per (piece, query), multiple of 8
     uint32_t* h2;              // single pass: nq x P, #score >= L | #score >= L+1 << 16
     uint32_t* qmap;            // fallback emission: block-local query j -> query qmap[q0 + j]
     uint32_t* nmap;            // device count of qmap entries
     uint32_t ppw;                 // fused pass: pieces per warp (set by the launcher)
+    uint32_t stage_all;           // fused pass: stage every block's stores (tests; else by density)
 };
 bool dense_supported(uint32_t ns, uint32_t K);
 size_t dense_smem(uint32_t ns, uint32_t K);
@@ -116,7 +116,7 @@ cudaError_t launch_dense_codes(const uint32_t* ids, const uint32_t* cell_off, ui
                                uint16_t* codes, cudaStream_t st);
 cudaError_t launch_dense_select(const DenseArgs& a, cudaStream_t st);  // hist + plan + emit
 // single pass: K0 sample -> L estimate -> fused hist + superset -> plan + checks -> compaction ->
-// exact emission for the flagged query blocks (rare); needs hsample/L/slots/scnt/qflag/C
+// exact emission for the flagged query blocks (rare); needs hsample/L/cbuf/ccnt/qflag/B
 cudaError_t launch_dense_select_fused(const DenseArgs& a, cudaStream_t st);
 // Shard protocol pieces: K1 alone (+ its histograms as [nq][P][N_s + 2] u32 rows with the
 // piece length first, the exchange format) and K3 alone with the globally planned T/quota/base.
@@ -124,6 +124,7 @@ cudaError_t launch_dense_hist(const DenseArgs& a, cudaStream_t st);
 cudaError_t launch_dense_hist_rows(const DenseArgs& a, uint32_t* out, cudaStream_t st);
 cudaError_t launch_dense_emit(const DenseArgs& a, cudaStream_t st);
 constexpr uint32_t kDensePiece = 2048;  // points per piece (one warp)
+constexpr uint32_t kDenseBuf = 96;      // single-pass candidate buffer entries per (piece, query)
 
 // ------------------------------------------------------------------ rerank
 // Exact fp64 re-rank of the candidate rows (query.cpp:159-197) with a

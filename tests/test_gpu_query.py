@@ -304,14 +304,16 @@ def test_u8_rows_rerank_mixed_queries(gpu, oracle, d, shift):
         assert np.array_equal(dd, od), (d, shift, a, b, k)
 
 
-@pytest.mark.parametrize("fused", ["1", "0"])
+@pytest.mark.parametrize("fused", ["1", "0", "stage"])
 @pytest.mark.parametrize("words", ["1", "2"])
 def test_dense_select_block_widths(gpu, oracle, words, fused, monkeypatch):
     """32-query (one mask word) and 64-query (two words) dense blocks, single-pass (with its
-    fallback) and two-pass, give the same candidate sets and answers as the reference; a partial
+    fallback; direct or staged buffer stores) and two-pass, give the same candidate sets and answers as the reference; a partial
     last block (nq % 64 != 0) included."""
     monkeypatch.setenv("SUCO_DENSE_WORDS", words)
-    monkeypatch.setenv("SUCO_DENSE_FUSED", fused)
+    monkeypatch.setenv("SUCO_DENSE_FUSED", "0" if fused == "0" else "1")
+    if fused == "stage":  # the fused pass's staged (8-byte) buffer stores, normally for dense supersets
+        monkeypatch.setenv("SUCO_DENSE_STAGE", "1")
     full = oracle.clustered(60000 + 77, 24, 30, 2024, 0, 100, 9, True)  # 30 pieces: a real sample
     base, qs = oracle.hold_out(full, 77, 2025)
     oidx = oracle.build_index(base, 6, 20, 3, 42, 0)
@@ -323,3 +325,26 @@ def test_dense_select_block_widths(gpu, oracle, words, fused, monkeypatch):
     s1, c1, _, _ = idx.query_intermediates(qs[5], gpu.CollisionParams(0.05, 0.01, 10))
     s2, c2, _, _ = oidx.query_intermediates(base, qs[5], 0.05, 0.01, 10)
     assert np.array_equal(c1, c2)
+
+
+def test_dense_buffer_overflow_falls_back(gpu, oracle, monkeypatch, capfd):
+    """Rows sorted along one coordinate put a query's high scorers in a few neighbouring pieces:
+    more than B = 96 of them in one (query, piece) buffer flags the query, which then takes the exact
+    two-pass select. Answers stay identical to the reference."""
+    monkeypatch.setenv("SUCO_DENSE_STATS", "1")
+    full = oracle.clustered(40000 + 64, 16, 8, 77, 0, 100, 6, True)
+    full = full[np.argsort(full[:, 0], kind="stable")]
+    rng = np.random.default_rng(5)
+    pick = np.sort(rng.choice(len(full), 64, replace=False))
+    qs = full[pick]
+    base = np.delete(full, pick, axis=0)
+    oidx = oracle.build_index(base, 4, 12, 3, 42, 0)
+    idx = gpu.load_index(oidx.serialize(), base)
+    for a, b, k in ((0.2, 0.01, 10), (0.05, 0.02, 20)):
+        ids, dd = idx.knn_query_batch(qs, gpu.CollisionParams(a, b, k))
+        oi, od, _ = oidx.knn_query_batch(base, qs, a, b, k)
+        assert np.array_equal(ids, oi) and np.array_equal(dd, od), (a, b, k)
+    err = capfd.readouterr().err
+    flagged = [int(line.split("dense select: ")[1].split(" of")[0]) for line in err.splitlines()
+               if "dense select:" in line]
+    assert flagged and max(flagged) > 0, err
