@@ -209,6 +209,8 @@ def main():
                     help="block-cyclic shard block size (ids); 0 = suco_gpu_shard_block_hint (slabs == blocks)")
     ap.add_argument("--alpha", type=float, default=None, help="experiment: override the config's alpha")
     ap.add_argument("--beta", type=float, default=None, help="experiment: override the config's beta")
+    ap.add_argument("--n", type=int, default=None, help="experiment: override the config's point count")
+    ap.add_argument("--queries", type=int, default=None, help="experiment: override the config's query count")
     args = ap.parse_args()
     if args.no_u8:
         os.environ["SUCO_NO_U8"] = "1"  # read by the library at index upload
@@ -217,8 +219,17 @@ def main():
         import dataclasses
         cfg = dataclasses.replace(cfg, alpha=args.alpha if args.alpha is not None else cfg.alpha,
                                   beta=args.beta if args.beta is not None else cfg.beta)
+    if args.n is not None or args.queries is not None:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, n=args.n or cfg.n, queries=args.queries or cfg.queries)
+    sampled = cfg.train_sample < 1.0  # cfg5: centroids trained on a seeded sample (sampled build)
 
     if args.impl == "reference":
+        if sampled:
+            print(json.dumps({"impl": "reference", "unavailable": f"{cfg.name}'s sampled build has no reference "
+                              "API (bench.py --config {cfg.name} reports the reference knn_query on the GPU-built "
+                              "index as its cpu_baseline)"}))
+            return
         run_reference_arm(args, cfg)
         return
 
@@ -249,9 +260,13 @@ def main():
         ref_build_s = time.time() - t0
         idx = suco.load_index(ref_idx.serialize(), base, device=local)
     else:
+        train = bench_data.train_ids(cfg, len(base)) if sampled else None
         torch.cuda.synchronize()
         t0 = time.time()
-        idx = suco.build_index(base, params, device=local)
+        if sampled:
+            idx = suco.build_index_sampled(base, train, params, device=local)
+        else:
+            idx = suco.build_index(base, params, device=local)
         torch.cuda.synchronize()
         build_s = time.time() - t0
     log(f"[rank {rank}] index ready (gpu build {build_s}, reference build {ref_build_s})")
@@ -347,7 +362,7 @@ def main():
     # answer quality against the GPU exact kNN, on a query sample
     quality = None
     if not args.profile_only and rank == 0:
-        sample = min(nq, 1000)
+        sample = min(nq, 1000 if cfg.n <= 20_000_000 else 100)
         t0 = time.time()
         ti, td = idx.exact_knn_batch(queries[:sample], k)
         gt_s = time.time() - t0
@@ -396,23 +411,45 @@ def main():
             from oracle.oracle import ref, ref_available
             if ref_available():
                 R = ref()
-                if ref_idx is None:
+                centroids_equal = None
+                if ref_idx is None and sampled:
+                    # no reference API for the sampled build: the reference's own build_index over the
+                    # training rows gives the centroids (they must equal ours), and the reference's
+                    # load_index + knn_query run on the GPU-built index bytes
+                    sys.path.insert(0, os.path.join(ROOT, "tests"))
+                    from suco_bytes import parse
+                    t0 = time.time()
+                    rs = R.build_index(base[train], cfg.num_subspaces, cfg.k_half, cfg.iterations, 42, 0, 0)
+                    ref_build_s = time.time() - t0
+                    blob = idx.serialize()
+                    a, b = parse(blob), parse(rs.serialize())
+                    centroids_equal = all(np.array_equal(x["cent1"], y["cent1"]) and np.array_equal(x["cent2"], y["cent2"])
+                                          for x, y in zip(a["subspaces"], b["subspaces"]))
+                    del a, b, rs
+                    ref_idx = R.load_index(blob)
+                    del blob
+                elif ref_idx is None:
                     t0 = time.time()
                     ref_idx = R.build_index(base, cfg.num_subspaces, cfg.k_half, cfg.iterations, 42, 0, 0)
                     ref_build_s = time.time() - t0
                 threads = R.hardware_threads()
-                probe = min(nq, 200)
+                probe = min(nq, 200 if cfg.n <= 20_000_000 else 16)
                 _, _, w = ref_idx.knn_query_batch(base, queries[:probe], cfg.alpha, cfg.beta, k, threads=0)
                 sample = int(min(nq, max(probe, args.cpu_seconds * probe / max(w, 1e-6))))
                 sel = np.arange(sample)
                 ri, rd, wall = ref_idx.knn_query_batch(base, queries[sel], cfg.alpha, cfg.beta, k, threads=0)
+                built = (f"reference build_index over the {len(train):,}-row training sample (k-means only) "
+                         f"{ref_build_s:.1f} s; queries on the GPU-built index loaded by the reference's load_index"
+                         if sampled else f"reference build_index {ref_build_s:.1f} s")
                 cpu = {"value": sample / wall, "unit": "queries/s", "cores": threads, "kind": "reference",
                        "sample": f"first {sample} of {nq} {cfg.name} queries through the reference knn_query "
-                                 f"(run_suco_batch parallel_chunks, {threads} threads); reference build_index "
-                                 f"{ref_build_s:.1f} s", "build_s": ref_build_s}
+                                 f"(run_suco_batch parallel_chunks, {threads} threads); {built}",
+                       "build_s": ref_build_s}
                 parity = {"checked_queries": sample, "ids_equal": bool(np.array_equal(ri, gpu_ids[sel])),
                           "dists_equal": bool(np.array_equal(rd, gpu_d[sel]))}
-                if args.index_source == "gpu":
+                if sampled:
+                    parity["centroids_equal_reference_sample_build"] = centroids_equal
+                elif args.index_source == "gpu":
                     parity["index_bytes_equal"] = idx.serialize() == ref_idx.serialize()
         except Exception as e:  # the baseline must not mask the GPU number
             cpu = {"error": repr(e)}

@@ -39,6 +39,7 @@ class Config:
     seed: int
     iterations: int = 10
     train_sample: float = 1.0  # cfg5: k-means trained on a 1% sample
+    parallel: bool = False     # cfg5: chunk-seeded streams generated on all host cores
 
     def describe(self) -> str:
         kind = "u8-valued" if self.quantize else ("unit-norm" if self.normalize else "float32")
@@ -53,8 +54,46 @@ CONFIGS = {
     "cfg3": Config("cfg3", 1_000_000, 960, 1000, 0.0, 1.0, 0.05, False, False, 1_000, 16, 50, 0.05, 0.01, 10, 1003),
     "cfg4": Config("cfg4", 10_000_000, 96, 10_000, -1.0, 1.0, 0.2, False, True, 10_000, 8, 64, 0.03, 0.005, 10, 1004),
     "cfg5": Config("cfg5", 100_000_000, 128, 100_000, 20.0, 140.0, 18.0, True, False, 10_000, 8, 100, 0.02, 0.002,
-                   10, 1005, train_sample=0.01),
+                   10, 1005, train_sample=0.01, parallel=True),
 }
+
+
+def train_ids(cfg: Config, n: int) -> np.ndarray:
+    """The seeded training sample of a sampled build (cfg5: 1 % of the rows), ascending u32 ids."""
+    size = max(cfg.k_half, int(round(n * cfg.train_sample)))
+    if size >= n:
+        return np.arange(n, dtype=np.uint32)
+    rng = np.random.default_rng(cfg.seed + 7)
+    return np.sort(rng.choice(n, size=size, replace=False)).astype(np.uint32)
+
+
+def _generate_parallel(cfg: Config, n: int, nq: int, chunk: int = 1 << 16) -> Tuple[np.ndarray, np.ndarray]:
+    """cfg5 (10^8 points): the same mixture recipe, float32 normals, one PCG64 stream per
+    65,536-row chunk (SeedSequence([seed, chunk])) so all host cores generate at once; the queries
+    are a separate stream (SeedSequence([seed, 2^32])) of the same mixture."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    centers = np.random.default_rng(cfg.seed).uniform(cfg.lo, cfg.hi, size=(cfg.clusters, cfg.d)).astype(np.float32)
+    sigma = np.float32(cfg.sigma)
+
+    def fill(out, lo, hi, key):
+        g = np.random.default_rng(np.random.SeedSequence([cfg.seed, key]))
+        v = g.standard_normal((hi - lo, cfg.d), dtype=np.float32)
+        v *= sigma
+        v += centers[g.integers(0, cfg.clusters, size=hi - lo)]
+        if cfg.quantize:
+            np.clip(np.rint(v, out=v), 0.0, 255.0, out=v)
+        if cfg.normalize:
+            v /= np.sqrt(np.einsum("ij,ij->i", v, v))[:, None]
+        out[lo:hi] = v
+
+    base = np.empty((n, cfg.d), np.float32)
+    with ThreadPoolExecutor(os.cpu_count() or 1) as ex:
+        list(ex.map(lambda i: fill(base, i * chunk, min(n, (i + 1) * chunk), i), range((n + chunk - 1) // chunk)))
+    queries = np.empty((nq, cfg.d), np.float32)
+    fill(queries, 0, nq, 1 << 32)
+    return base, queries
 
 
 def generate(cfg: Config, n: int | None = None, queries: int | None = None,
@@ -62,6 +101,8 @@ def generate(cfg: Config, n: int | None = None, queries: int | None = None,
     """(base n x d float32, queries Q x d float32) for `cfg` (optionally resized for tests)."""
     n = cfg.n if n is None else n
     nq = cfg.queries if queries is None else queries
+    if cfg.parallel:
+        return _generate_parallel(cfg, n, nq)
     total = n + nq
     rng = np.random.default_rng(cfg.seed)
     centers = rng.uniform(cfg.lo, cfg.hi, size=(cfg.clusters, cfg.d))

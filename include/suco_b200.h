@@ -75,6 +75,19 @@ int suco_validate_collision_params(const suco_collision_params* p, uint64_t n);
 int suco_gpu_build_index(const float* data, uint64_t n, uint32_t d, const suco_index_params* params,
                          int device, suco_gpu_index** out);
 
+/* Config 5's sampled build (BASELINE.json configs[4]: "centroids trained on a seeded 1% sample").
+ * The reference has no API for it; this composes the reference's own steps: the 2*N_s k-means
+ * jobs of build_index (index.cpp:120-137, kmeans.cpp:118-194, seeds derive_seed(seed, job)) run
+ * on the rows train_ids[0..n_train) only (strictly ascending, in that order), then EVERY row is
+ * assigned to its nearest centroid by kmeans.cpp:19-33's rule (fp64, strict '<') and build_imi
+ * (index.cpp:69-96) runs over all n. train_ids = 0..n-1 gives exactly suco_gpu_build_index.
+ * Checks: as suco_gpu_build_index with n_train in place of n for the k_half test (CONFIG), then
+ * ids not strictly ascending or >= n -> CONTRACT. The result serializes like any index (the
+ * `.suco` format has no sample field) and the reference's load_index/knn_query accept it.
+ * For both build entry points `data` may be host memory or device memory on `device`. */
+int suco_gpu_build_index_sampled(const float* data, uint64_t n, uint32_t d, const suco_index_params* params,
+                                 const uint32_t* train_ids, uint64_t n_train, int device, suco_gpu_index** out);
+
 /* deserialize_index (index.hpp:107, index.cpp:191-293) + check_compatible
  * (index.hpp:108, index.cpp:295-305): uploads a serialized `.suco` index and
  * the dataset it was built from. Corrupt bytes -> FORMAT naming the section;

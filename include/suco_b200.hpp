@@ -270,6 +270,16 @@ inline GpuIndex build_index(std::span<const float> data, std::uint64_t n, std::u
     return GpuIndex(h);
 }
 
+// Config 5's sampled build (suco_gpu_build_index_sampled).
+inline GpuIndex build_index_sampled(std::span<const float> data, std::uint64_t n, std::uint32_t d,
+                                    std::span<const std::uint32_t> train_ids, const IndexParams& params = {},
+                                    int device = 0) {
+    const auto p = params.c();
+    suco_gpu_index* h = nullptr;
+    check(suco_gpu_build_index_sampled(data.data(), n, d, &p, train_ids.data(), train_ids.size(), device, &h));
+    return GpuIndex(h);
+}
+
 inline GpuIndex load_index(std::span<const unsigned char> bytes, std::span<const float> data, std::uint64_t n,
                            std::uint32_t d, int device = 0) {
     suco_gpu_index* h = nullptr;

@@ -175,6 +175,17 @@ class Oracle(_Lib):
                                             C.c_uint32(mode), C.c_uint(threads), C.byref(h)))
         return OracleIndex(self, h)
 
+    def build_index_sampled(self, data, train_ids, ns, k_half, iters, seed, mode=0, threads=0) -> "OracleIndex":
+        """Config 5's sampled build (suco_oracle.h: so_build_index_sampled)."""
+        data = np.ascontiguousarray(data, np.float32)
+        train = np.ascontiguousarray(train_ids, np.uint32)
+        h = C.c_void_p()
+        self._check(self._fn("build_index_sampled")(
+            _p(data, f32p), C.c_uint64(data.shape[0]), C.c_uint32(data.shape[1]), C.c_uint32(ns), C.c_uint32(k_half),
+            C.c_uint32(iters), C.c_uint64(seed), C.c_uint32(mode), _p(train, u32p), C.c_uint64(train.size),
+            C.c_uint(threads), C.byref(h)))
+        return OracleIndex(self, h)
+
     def load_index(self, blob: bytes) -> "OracleIndex":
         h = C.c_void_p()
         buf = np.frombuffer(blob, np.uint8)

@@ -502,6 +502,8 @@ typedef struct {
     const float* data;
     uint64_t n;
     uint32_t* const* assign; /* 2*ns arrays */
+    const uint32_t* train;   /* sampled build: ascending training-row ids (NULL: every row trains) */
+    uint64_t n_train;
     int rc;
     char err[512];
     unsigned next;
@@ -514,14 +516,32 @@ static int build_job(build_ctx* b, unsigned job) {
     const uint32_t s = job / 2;
     const int half = (int)(job % 2);
     const uint32_t h = half_dim(x, s, half);
-    const uint64_t n = b->n;
+    const uint64_t n = b->train ? b->n_train : b->n;
     float* proj = malloc(sizeof(float) * n * h);
     if (!proj) return fail(SO_INTERNAL, "out of memory");
-    for (uint64_t i = 0; i < n; ++i) project(x, b->data + i * x->d, s, half, proj + i * h);
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint64_t row = b->train ? b->train[i] : i;
+        project(x, b->data + row * x->d, s, half, proj + i * h);
+    }
     float* cent = malloc(sizeof(float) * (size_t)x->k_half * h);
-    const int rc = so_kmeans(proj, n, h, x->k_half, x->iters, so_derive_seed(x->seed, job), cent,
-                             b->assign[job], NULL, NULL, NULL);
+    uint32_t* kassign = b->train ? malloc(sizeof(uint32_t) * n) : b->assign[job];
+    int rc = kassign ? so_kmeans(proj, n, h, x->k_half, x->iters, so_derive_seed(x->seed, job), cent, kassign, NULL,
+                                 NULL, NULL)
+                     : fail(SO_INTERNAL, "out of memory");
     free(proj);
+    if (b->train) {
+        /* sampled build: every row goes to its nearest trained centroid, kmeans.cpp:19-33's rule
+           (the same rule as the k-means final assignment pass, kmeans.cpp:190-191) */
+        float* tmp = malloc(sizeof(float) * (h ? h : 1));
+        if (!tmp && !rc) rc = fail(SO_INTERNAL, "out of memory");
+        for (uint64_t i = 0; !rc && i < b->n; ++i) {
+            double dist;
+            project(x, b->data + i * x->d, s, half, tmp);
+            b->assign[job][i] = nearest(tmp, cent, x->k_half, h, &dist);
+        }
+        free(tmp);
+        free(kassign);
+    }
     if (half == 0) x->cent1[s] = cent;
     else x->cent2[s] = cent;
     return rc;
@@ -556,17 +576,26 @@ static int check_dataset(const float* data, uint64_t n, uint32_t d) {
     return SO_OK;
 }
 
-/* index.cpp:98-145 */
-int so_build_index(const float* data, uint64_t n, uint32_t d, uint32_t ns, uint32_t k_half, uint32_t iters,
-                   uint64_t seed, uint32_t mode, unsigned threads, so_index** out) {
+/* index.cpp:98-145; train != NULL: the sampled build (see so_build_index_sampled) */
+static int build_index_impl(const float* data, uint64_t n, uint32_t d, uint32_t ns, uint32_t k_half, uint32_t iters,
+                            uint64_t seed, uint32_t mode, unsigned threads, const uint32_t* train, uint64_t n_train,
+                            so_index** out) {
     int rc = check_dataset(data, n, d);
     if (rc) return rc;
     if (k_half < 1) return fail(SO_CONFIG, "k_half must be >= 1");
     if (iters < 1) return fail(SO_CONFIG, "iterations must be >= 1");
-    if (n < k_half) {
-        return fail(SO_CONFIG, "dataset has n = %llu points, fewer than k_half = %u", (unsigned long long)n, k_half);
+    const uint64_t n_fit = train ? n_train : n;
+    if (n_fit < k_half) {
+        return fail(SO_CONFIG, "%s has n = %llu points, fewer than k_half = %u", train ? "training sample" : "dataset",
+                    (unsigned long long)n_fit, k_half);
     }
     if (n > 0xFFFFFFFFULL) return fail(SO_CONTRACT, "dataset exceeds 32-bit point-id capacity");
+    for (uint64_t i = 0; train && i < n_train; ++i) {
+        if (train[i] >= n || (i && train[i] <= train[i - 1])) {
+            return fail(SO_CONTRACT, "training ids must be strictly ascending and < n (entry %llu)",
+                        (unsigned long long)i);
+        }
+    }
     if (ns < 2) return fail(SO_CONFIG, "sample_subspaces: need at least 2 subspaces, got %u", ns);
     so_index* x = index_alloc(d, ns);
     if (!x) return fail(SO_INTERNAL, "out of memory");
@@ -584,7 +613,8 @@ int so_build_index(const float* data, uint64_t n, uint32_t d, uint32_t ns, uint3
 
     uint32_t** assign = calloc(2 * ns, sizeof(uint32_t*));
     for (uint32_t j = 0; j < 2 * ns; ++j) assign[j] = malloc(sizeof(uint32_t) * n);
-    build_ctx b = {.x = x, .data = data, .n = n, .assign = assign, .rc = 0, .next = 0};
+    build_ctx b = {.x = x, .data = data, .n = n, .assign = assign, .train = train, .n_train = n_train, .rc = 0,
+                   .next = 0};
     pthread_mutex_init(&b.mu, NULL);
     unsigned nt = threads == 0 ? 8 : threads;
     if (nt > 2 * ns) nt = 2 * ns;
@@ -609,6 +639,18 @@ int so_build_index(const float* data, uint64_t n, uint32_t d, uint32_t ns, uint3
     }
     *out = x;
     return SO_OK;
+}
+
+int so_build_index(const float* data, uint64_t n, uint32_t d, uint32_t ns, uint32_t k_half, uint32_t iters,
+                   uint64_t seed, uint32_t mode, unsigned threads, so_index** out) {
+    return build_index_impl(data, n, d, ns, k_half, iters, seed, mode, threads, NULL, 0, out);
+}
+
+int so_build_index_sampled(const float* data, uint64_t n, uint32_t d, uint32_t ns, uint32_t k_half, uint32_t iters,
+                           uint64_t seed, uint32_t mode, const uint32_t* train, uint64_t n_train, unsigned threads,
+                           so_index** out) {
+    if (!train) return fail(SO_CONTRACT, "training ids are null");
+    return build_index_impl(data, n, d, ns, k_half, iters, seed, mode, threads, train, n_train, out);
 }
 
 /* ------------------------------------------------------------ persistence */

@@ -71,6 +71,14 @@ typedef struct so_index so_index;
 /* index.cpp:98-145 ; `threads` jobs run concurrently, output independent of it */
 int so_build_index(const float* data, uint64_t n, uint32_t d, uint32_t ns, uint32_t k_half,
                    uint32_t iters, uint64_t seed, uint32_t mode, unsigned threads, so_index** out);
+/* Config 5's sampled build (BASELINE.json configs[4]; no reference API — composed from the
+ * reference's own steps): the 2*N_s k-means jobs of index.cpp:120-137 run on the training rows
+ * train[0..n_train) only (strictly ascending ids, in that order), then EVERY row is assigned to
+ * its nearest centroid by kmeans.cpp:19-33's rule and build_imi (index.cpp:69-96) runs over all n.
+ * With train = 0..n-1 it equals so_build_index. */
+int so_build_index_sampled(const float* data, uint64_t n, uint32_t d, uint32_t ns, uint32_t k_half,
+                           uint32_t iters, uint64_t seed, uint32_t mode, const uint32_t* train,
+                           uint64_t n_train, unsigned threads, so_index** out);
 /* index.cpp:147-170 (two-call: buf == NULL -> size only) */
 int so_serialize_index(const so_index* idx, unsigned char* buf, uint64_t cap, uint64_t* len);
 /* index.cpp:191-293 */

@@ -334,14 +334,42 @@ class GpuIndex:
         return scores, cands[: m.value].copy(), cps, cum
 
 
-def build_index(dataset, params: IndexParams = IndexParams(), device: int = 0) -> GpuIndex:
-    """build_index (index.hpp:85, index.cpp:98-145) on the GPU."""
+def _rows(dataset):
+    """(f32 pointer, n, d, keep-alive) for a host matrix or a CUDA float32 tensor (any object with
+    data_ptr() / is_cuda: its rows are copied device to device, never through the host)."""
+    if getattr(dataset, "is_cuda", False):
+        t = dataset
+        if t.dim() != 2 or not t.is_contiguous() or str(t.dtype) != "torch.float32":
+            raise ContractError("device dataset must be a contiguous 2-D float32 tensor")
+        return C.cast(C.c_void_p(t.data_ptr()), _c.f32p), t.shape[0], t.shape[1], t
     v = _values(dataset)
     if v.ndim != 2:
         raise ContractError("dataset must be a 2-D n x d matrix")
+    return _p(v, _c.f32p), v.shape[0], v.shape[1], v
+
+
+def build_index(dataset, params: IndexParams = IndexParams(), device: int = 0) -> GpuIndex:
+    """build_index (index.hpp:85, index.cpp:98-145) on the GPU. `dataset`: host n x d matrix or a
+    CUDA float32 tensor on `device`."""
+    ptr, n, d, _keep = _rows(dataset)
     h = C.c_void_p()
     ip = params._c()
-    _check(_c.build_index(_p(v, _c.f32p), v.shape[0], v.shape[1], C.byref(ip), device, C.byref(h)))
+    _check(_c.build_index(ptr, n, d, C.byref(ip), device, C.byref(h)))
+    return GpuIndex(h)
+
+
+def build_index_sampled(dataset, train_ids, params: IndexParams = IndexParams(), device: int = 0) -> GpuIndex:
+    """Config 5's sampled build (include/suco_b200.h: suco_gpu_build_index_sampled): k-means on the
+    rows `train_ids` (strictly ascending) only, then every row assigned to its nearest centroid
+    (kmeans.cpp:19-33) and the IMI built over all of them (index.cpp:69-96)."""
+    ptr, n, d, _keep = _rows(dataset)
+    tr = np.asarray(train_ids)
+    if tr.ndim != 1 or (tr.size and (tr.min() < 0 or tr.max() > 0xFFFFFFFF)):
+        raise ContractError("training ids must be a 1-D array of row ids")
+    tr = np.ascontiguousarray(tr, np.uint32)
+    h = C.c_void_p()
+    ip = params._c()
+    _check(_c.build_index_sampled(ptr, n, d, C.byref(ip), _p(tr, _c.u32p), tr.size, device, C.byref(h)))
     return GpuIndex(h)
 
 

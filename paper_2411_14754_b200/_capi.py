@@ -57,6 +57,8 @@ candidate_count = _sig("suco_candidate_count", C.c_uint64, C.c_double, C.c_uint6
 validate_collision_params = _sig("suco_validate_collision_params", C.c_int, C.POINTER(CollisionParamsC), C.c_uint64)
 build_index = _sig("suco_gpu_build_index", C.c_int, f32p, C.c_uint64, C.c_uint32, C.POINTER(IndexParamsC), C.c_int,
                    C.POINTER(vp))
+build_index_sampled = _sig("suco_gpu_build_index_sampled", C.c_int, f32p, C.c_uint64, C.c_uint32, C.POINTER(IndexParamsC),
+                           u32p, C.c_uint64, C.c_int, C.POINTER(vp))
 load_index = _sig("suco_gpu_load_index", C.c_int, u8p, C.c_uint64, f32p, C.c_uint64, C.c_uint32, C.c_int,
                   C.POINTER(vp))
 serialize_index = _sig("suco_gpu_serialize_index", C.c_int, vp, u8p, C.c_uint64, u64p)
@@ -107,7 +109,7 @@ build_imi = _sig("suco_gpu_build_imi", C.c_int, u32p, u32p, C.c_uint64, C.c_uint
 
 EXPORTED = [
     "suco_last_error", "suco_gpu_device_count", "suco_collision_count", "suco_candidate_count",
-    "suco_validate_collision_params", "suco_gpu_build_index", "suco_gpu_load_index", "suco_gpu_serialize_index",
+    "suco_validate_collision_params", "suco_gpu_build_index", "suco_gpu_build_index_sampled", "suco_gpu_load_index", "suco_gpu_serialize_index",
     "suco_gpu_index_subspace", "suco_gpu_index_info", "suco_gpu_free_index", "suco_gpu_knn_query_batch",
     "suco_gpu_knn_query_batch_device", "suco_gpu_set_stream", "suco_gpu_synchronize", "suco_gpu_set_profiling",
     "suco_gpu_stage_times", "suco_gpu_last_launches", "suco_gpu_exact_knn_batch", "suco_gpu_sc_scores",

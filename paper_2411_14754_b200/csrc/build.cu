@@ -26,6 +26,8 @@
 //                                        strict '>' (lowest id on ties).
 //   build_imi        index.cpp:69-96     stable counting sort by c1*k + c2.
 #include <cuda_runtime.h>
+
+#include <cstdlib>
 #include <stdint.h>
 
 #include <algorithm>
@@ -77,13 +79,15 @@ struct KJob {
 };
 
 // ------------------------------------------------------------------ project
+// rows == nullptr: point i is row i; else row rows[i] (the sampled build's training rows)
 __global__ void project_kernel(const float* __restrict__ data, uint64_t n, uint32_t d, const uint32_t* __restrict__ dims,
-                               const uint32_t* __restrict__ dim_off, const KJob* __restrict__ jobs, float* __restrict__ proj) {
+                               const uint32_t* __restrict__ dim_off, const KJob* __restrict__ jobs, float* __restrict__ proj,
+                               const uint32_t* __restrict__ rows) {
     const uint32_t j = blockIdx.y;
     const KJob jb = jobs[j];
     const uint32_t* dl = dims + dim_off[j];
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
-        const float* row = data + i * d;
+        const float* row = data + (rows ? uint64_t(rows[i]) : i) * d;
         float* out = proj + jb.off + i * jb.h;
         for (uint32_t t = 0; t < jb.h; ++t) out[t] = row[dl[t]];
     }
@@ -722,11 +726,13 @@ void kmeans_jobs(const float* proj, const std::vector<KJob>& host_jobs, const KJ
 
 }  // namespace
 
-void build_index_device(const float* d_data, uint64_t n, uint32_t d, const HostLayout& L, const suco_index_params& p,
-                        BuildOutputs& out, cudaStream_t st) {
-    const uint32_t ns = L.ns, J = 2 * ns, k = p.k_half;
-    std::vector<KJob> hj(J);
-    std::vector<uint32_t> dim_off(J + 1), dims;
+// The 2*N_s jobs' KJob table for `rows` points (job-major projections, rows x h each).
+static uint64_t job_table(const HostLayout& L, uint32_t k, uint64_t rows, std::vector<KJob>& hj,
+                          std::vector<uint32_t>& dim_off, std::vector<uint32_t>& dims, uint64_t* coff_out) {
+    const uint32_t ns = L.ns, J = 2 * ns;
+    hj.assign(J, KJob{});
+    dim_off.assign(J + 1, 0);
+    dims.clear();
     uint64_t off = 0, coff = 0;
     uint32_t pos = 0;
     for (uint32_t s = 0; s < ns; ++s) {
@@ -734,7 +740,7 @@ void build_index_device(const float* d_data, uint64_t n, uint32_t d, const HostL
             const uint32_t j = 2 * s + half;
             const uint32_t h = half == 0 ? L.h1(s) : L.h2(s);
             hj[j] = KJob{h, 0, off, coff};
-            off += n * h;
+            off += rows * h;
             coff += uint64_t(k) * h;
             dim_off[j] = static_cast<uint32_t>(dims.size());
             const uint32_t b = pos + (half == 0 ? 0 : L.split[s]);
@@ -743,20 +749,66 @@ void build_index_device(const float* d_data, uint64_t n, uint32_t d, const HostL
         pos += L.sizes[s];
     }
     dim_off[J] = static_cast<uint32_t>(dims.size());
+    *coff_out = coff;
+    return off;
+}
+
+void build_index_device(const float* d_data, uint64_t n, uint32_t d, const HostLayout& L, const suco_index_params& p,
+                        BuildOutputs& out, cudaStream_t st, const uint32_t* train, uint64_t n_train) {
+    const uint32_t ns = L.ns, J = 2 * ns, k = p.k_half;
+    // k-means fits on every row, or (sampled build) on the training rows only
+    const uint64_t nfit = train ? n_train : n;
+    std::vector<KJob> hj;
+    std::vector<uint32_t> dim_off, dims;
+    uint64_t coff = 0;
+    const uint64_t off = job_table(L, k, nfit, hj, dim_off, dims, &coff);
     Dev<KJob> jobs(J);
-    Dev<uint32_t> ddims(dims.size()), ddoff(J + 1);
+    Dev<uint32_t> ddims(dims.size()), ddoff(J + 1), dtrain(train ? n_train : 1);
     Dev<float> proj(off), cent(coff);
     BCUDA(cudaMemcpyAsync(jobs.p, hj.data(), J * sizeof(KJob), cudaMemcpyHostToDevice, st));
     BCUDA(cudaMemcpyAsync(ddims.p, dims.data(), dims.size() * 4, cudaMemcpyHostToDevice, st));
     BCUDA(cudaMemcpyAsync(ddoff.p, dim_off.data(), (J + 1) * 4, cudaMemcpyHostToDevice, st));
-    project_kernel<<<dim3(grid_for(n, 256, 148 * 4), J), 256, 0, st>>>(d_data, n, d, ddims.p, ddoff.p, jobs.p, proj.p);
+    if (train) BCUDA(cudaMemcpyAsync(dtrain.p, train, n_train * 4, cudaMemcpyHostToDevice, st));
+    project_kernel<<<dim3(grid_for(nfit, 256, 148 * 4), J), 256, 0, st>>>(d_data, nfit, d, ddims.p, ddoff.p, jobs.p,
+                                                                          proj.p, train ? dtrain.p : nullptr);
     BCUDA(cudaGetLastError());
 
     std::vector<uint64_t> seeds(J);
     for (uint32_t j = 0; j < J; ++j) seeds[j] = derive_seed(p.seed, j);  // index.cpp:131
     Dev<uint32_t> assign(uint64_t(J) * n);
-    kmeans_jobs(proj.p, hj, jobs.p, n, k, p.iterations, seeds, cent.p, assign.p, nullptr, st);
+    {
+        Dev<uint32_t> fit_assign(train ? uint64_t(J) * n_train : 1);
+        kmeans_jobs(proj.p, hj, jobs.p, nfit, k, p.iterations, seeds, cent.p, train ? fit_assign.p : assign.p, nullptr,
+                    st);
+    }
     proj.release();
+    dtrain.release();
+    if (train) {
+        // every row to its nearest trained centroid (kmeans.cpp:19-33, the final-pass rule), in
+        // row chunks: project the chunk, assign it, scatter its J columns into assign (J x n)
+        uint32_t hmax = 0;
+        for (const KJob& jb : hj) hmax = std::max(hmax, jb.h);
+        uint64_t chunk = std::max<uint64_t>(1, (2ull << 30) / (uint64_t(d) * 4));  // 2 GB of projections
+        if (const char* c = std::getenv("SUCO_BUILD_CHUNK")) chunk = std::max<long long>(1, std::atoll(c));  // tests
+        chunk = std::min<uint64_t>(n, chunk);
+        std::vector<KJob> cj;
+        std::vector<uint32_t> cdo, cdims;
+        uint64_t ccoff = 0;
+        const uint64_t coffs = job_table(L, k, chunk, cj, cdo, cdims, &ccoff);
+        Dev<KJob> cjobs(J);
+        Dev<float> cproj(coffs);
+        Dev<uint32_t> cassign(uint64_t(J) * chunk);
+        BCUDA(cudaMemcpyAsync(cjobs.p, cj.data(), J * sizeof(KJob), cudaMemcpyHostToDevice, st));
+        for (uint64_t r0 = 0; r0 < n; r0 += chunk) {
+            const uint64_t nc = std::min(chunk, n - r0);
+            project_kernel<<<dim3(grid_for(nc, 256, 148 * 4), J), 256, 0, st>>>(d_data + r0 * d, nc, d, ddims.p,
+                                                                                ddoff.p, cjobs.p, cproj.p, nullptr);
+            BCUDA(cudaGetLastError());
+            launch_assign(cproj.p, cjobs.p, nc, k, hmax, cent.p, cassign.p, J, st);
+            BCUDA(cudaMemcpy2DAsync(assign.p + r0, n * 4, cassign.p, nc * 4, nc * 4, J, cudaMemcpyDeviceToDevice, st));
+        }
+        BCUDA(cudaStreamSynchronize(st));
+    }
 
     // centroids to the host (tiny)
     std::vector<float> hc(coff);

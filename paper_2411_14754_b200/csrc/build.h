@@ -19,8 +19,11 @@ struct BuildOutputs {
 
 // All 2*N_s (subspace, half) k-means jobs run concurrently on one device,
 // then one stable bucket sort per subspace emits the IMI CSR.
+// train != nullptr (host, n_train strictly ascending row ids): the sampled build — k-means on
+// those rows only, then every row assigned to its nearest centroid (kmeans.cpp:19-33).
 void build_index_device(const float* d_data, uint64_t n, uint32_t d, const HostLayout& L,
-                        const suco_index_params& p, BuildOutputs& out, cudaStream_t st);
+                        const suco_index_params& p, BuildOutputs& out, cudaStream_t st,
+                        const uint32_t* train = nullptr, uint64_t n_train = 0);
 
 // Stand-alone kmeans / build_imi on host buffers (parity entry points).
 void kmeans_device_host_io(const float* points, uint64_t n, uint32_t dim, uint32_t k, uint32_t iterations,

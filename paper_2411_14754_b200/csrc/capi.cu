@@ -114,6 +114,7 @@ struct suco_gpu_index {
     DevBuf<uint8_t> data8;      // u8 copy of the rows when they are integers in [0, 255] (rerank u8 path)
     DevBuf<uint16_t> codes;     // n x 8: s*K + cell of every point (dense select, N_s <= 8)
     bool dense = false;         // select stage = dense bit-sliced 32-query blocks (dense.cu)
+    bool dense_half = false;    // ... in the half-width mode (16-query blocks, u16 masks; large N_s*K)
     uint64_t phase1_nq = 0;     // shard: queries of the last dense phase 1 (phase 2 re-scores them)
     uint32_t dpad = 0;          // row bytes of data8 (0: no u8 copy)
     // block-cyclic shard (suco_gpu_make_shard): global blocks j with j % num_shards == shard
@@ -210,7 +211,8 @@ void create_stream(suco_gpu_index* x) {
 void upload_data(suco_gpu_index* x, const float* data, uint64_t n, uint32_t d) {
     if (data) {
         x->data.reserve(n * d);
-        CUDA_TRY(cudaMemcpyAsync(x->data.p, data, n * d * sizeof(float), cudaMemcpyHostToDevice, x->stream));
+        // host or device memory (UVA): rows already on the GPU are copied device to device
+        CUDA_TRY(cudaMemcpyAsync(x->data.p, data, n * d * sizeof(float), cudaMemcpyDefault, x->stream));
     }
     check_finite_device(x->data.p, n * d, x->stream);
     // integer certificate (values integral, |v| <= 2^20) for the exact fp32 rerank chains
@@ -301,8 +303,19 @@ void finalize_device(suco_gpu_index* x) {
     CUDA_TRY(launch_slab_offsets(x->cell_off.p, x->ids.p, x->host.n, ns, x->K, x->sel.CH, x->sel.nslabs, x->slab_off.p,
                                  x->stream));
     const char* dv = std::getenv("SUCO_DENSE");
-    x->dense = dense_supported(ns, x->K) && !(dv && std::atoi(dv) == 0);
-    if (x->dense) {
+    const bool allow = !(dv && std::atoi(dv) == 0);
+    x->dense = dense_supported(ns, x->K) && allow;
+    // tables past 32-bit masks in shared memory (config 5: 8 x 10,000 cells) take the half-width
+    // mode; SUCO_DENSE_HALF=0 keeps them on the cluster-counting select
+    const char* hv = std::getenv("SUCO_DENSE_HALF");  // 2: force it (tests)
+    const bool force = hv && std::atoi(hv) == 2;
+    x->dense_half = (!x->dense || force) && allow && dense_half_supported(ns, x->K) && !(hv && std::atoi(hv) == 0);
+    if (x->dense_half) {
+        x->dense = true;
+        const uint64_t n_pad = (x->host.n + kDensePiece - 1) / kDensePiece * kDensePiece;  // whole last piece
+        x->codes.reserve(n_pad * 8);
+        CUDA_TRY(launch_dense_codes_half(x->ids.p, x->cell_off.p, x->host.n, n_pad, ns, x->K, x->codes.p, x->stream));
+    } else if (x->dense) {
         x->codes.reserve(x->host.n * 8);
         CUDA_TRY(launch_dense_codes(x->ids.p, x->cell_off.p, x->host.n, ns, x->K, x->codes.p, x->stream));
     }
@@ -445,6 +458,7 @@ void stage_select(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nt, uint
         da.m = m;
         da.WP = kDensePiece;
         da.P = static_cast<uint32_t>((h.n + da.WP - 1) / da.WP);
+        da.half = x->dense_half ? 1u : 0u;
         sl.dhist.reserve(nt * da.P * 8);
         sl.dT.reserve(nt);
         sl.dquota.reserve(nt * da.P);
@@ -774,7 +788,8 @@ int suco_gpu_load_index(const unsigned char* bytes, uint64_t len, const float* d
     });
 }
 
-void build_core(suco_gpu_index* x, uint64_t n, uint32_t d, const suco_index_params* params);
+void build_core(suco_gpu_index* x, uint64_t n, uint32_t d, const suco_index_params* params,
+                const uint32_t* train = nullptr, uint64_t n_train = 0);
 
 int suco_gpu_build_index(const float* data, uint64_t n, uint32_t d, const suco_index_params* params, int device,
                          suco_gpu_index** out) {
@@ -797,18 +812,50 @@ int suco_gpu_build_index(const float* data, uint64_t n, uint32_t d, const suco_i
     });
 }
 
-// build_index (index.cpp:98-145) over rows already on the device.
-void build_core(suco_gpu_index* x, uint64_t n, uint32_t d, const suco_index_params* params) {
+int suco_gpu_build_index_sampled(const float* data, uint64_t n, uint32_t d, const suco_index_params* params,
+                                 const uint32_t* train_ids, uint64_t n_train, int device, suco_gpu_index** out) {
+    return guarded([&] {
+        if (!out) raise(SUCO_ERR_CONTRACT, "output handle pointer is null");
+        *out = nullptr;
+        if (!params) raise(SUCO_ERR_CONTRACT, "index params are null");
+        if (!train_ids) raise(SUCO_ERR_CONTRACT, "training ids are null");
+        check_dataset(data, n, d);
+        DeviceGuard g(device);
+        suco_gpu_index* x = new_index(device);
+        try {
+            create_stream(x);
+            upload_data(x, data, n, d);
+            build_core(x, n, d, params, train_ids, n_train);
+        } catch (...) {
+            delete x;
+            throw;
+        }
+        *out = x;
+    });
+}
+
+// build_index (index.cpp:98-145) over rows already on the device; train != nullptr: the sampled
+// build (k-means on those rows, every row assigned to its nearest centroid).
+void build_core(suco_gpu_index* x, uint64_t n, uint32_t d, const suco_index_params* params, const uint32_t* train,
+                uint64_t n_train) {
     {
         {
             // index.cpp:100-108
             if (params->k_half < 1) raise(SUCO_ERR_CONFIG, "k_half must be >= 1");
             if (params->iterations < 1) raise(SUCO_ERR_CONFIG, "iterations must be >= 1");
-            if (n < params->k_half) {
-                raise(SUCO_ERR_CONFIG, "dataset has n = " + std::to_string(n) + " points, fewer than k_half = " +
+            const uint64_t nfit = train ? n_train : n;
+            if (nfit < params->k_half) {
+                raise(SUCO_ERR_CONFIG, std::string(train ? "training sample" : "dataset") + " has n = " +
+                                           std::to_string(nfit) + " points, fewer than k_half = " +
                                            std::to_string(params->k_half));
             }
             if (n > 0xFFFFFFFFull) raise(SUCO_ERR_CONTRACT, "dataset exceeds 32-bit point-id capacity");
+            for (uint64_t i = 0; train && i < n_train; ++i) {
+                if (train[i] >= n || (i && train[i] <= train[i - 1])) {
+                    raise(SUCO_ERR_CONTRACT, "training ids must be strictly ascending and < n (entry " +
+                                                 std::to_string(i) + ")");
+                }
+            }
             x->host.layout = sample_subspaces(d, params->num_subspaces, params->mode, params->seed);
             x->host.n = n;
             x->host.d = d;
@@ -817,7 +864,7 @@ void build_core(suco_gpu_index* x, uint64_t n, uint32_t d, const suco_index_para
             x->cell_off.reserve(uint64_t(params->num_subspaces) * (K + 1));
             x->ids.reserve(uint64_t(params->num_subspaces) * n);
             BuildOutputs bo{x->cell_off.p, x->ids.p, &x->host.cent1, &x->host.cent2};
-            build_index_device(x->data.p, n, d, x->host.layout, *params, bo, x->stream);
+            build_index_device(x->data.p, n, d, x->host.layout, *params, bo, x->stream, train, n_train);
             upload_codebooks(x);
             finalize_device(x);
             x->n_global = n;
@@ -1222,6 +1269,7 @@ int suco_gpu_make_shard(const suco_gpu_index* full, uint32_t shard, uint32_t num
             // dense select when the blocks are whole pieces (pieces never straddle blocks)
             const char* dv = std::getenv("SUCO_DENSE");
             x->dense = dense_supported(ns, x->K) && block % kDensePiece == 0 && !(dv && std::atoi(dv) == 0);
+            x->dense_half = false;  // shards: 32-query blocks or the cluster-counting select
             if (x->dense) {
                 x->codes.reserve(n_local * 8);
                 CUDA_TRY(launch_dense_codes(x->ids.p, x->cell_off.p, n_local, ns, x->K, x->codes.p, x->stream));

@@ -637,7 +637,298 @@ __global__ void dense_codes_kernel(const uint32_t* ids, const uint32_t* cell_off
     for (uint32_t i = off[cell]; i < off[cell + 1]; ++i) codes[uint64_t(sid[i]) * 8 + s] = code;
 }
 
+// ------------------------------------------------------------ half-width mode
+// For mask tables beyond shared memory at 32 bits per slot (config 5: 8 x 10,000 cells): a CTA
+// owns 16 queries and keeps one u16 mask per (subspace, cell). Region s of the table holds K + 1
+// slots at s * (K + 1); slot 0 of a region is always zero and a point's code in subspace s is
+// cell + 1 (0 for s >= N_s and for the padding rows past n). A lane looks up TWO points of a
+// 64-point tile, A = t0 + lane (bits 0-15) and B = t0 + 32 + lane (bits 16-31), so the carry-save
+// adders and the 32x32 transpose work on full 32-bit words exactly as in the 32-query kernels.
+// After the transpose lane c holds query c & 15 over the 32 points t0 + 32 * (c >> 4) + r.
+template <uint32_t kDT>
+__device__ void build_masks_h(const DenseArgs& a, uint32_t* M, uint64_t q0, uint32_t nqb) {
+    constexpr uint32_t kDW = kDT / 32;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint32_t R = a.K + 1;
+    const uint32_t words = (a.ns * R + 1) / 2;
+    for (uint32_t i = tid; i < words; i += kDT) M[i] = 0;
+    __syncthreads();
+    for (uint32_t j = warp; j < nqb; j += kDW) {
+        const uint64_t q = a.qmap ? a.qmap[q0 + j] : q0 + j;
+        for (uint32_t s = 0; s < a.ns; ++s) {
+            const uint64_t t = q * a.ns + s;
+            const uint32_t cnt = a.cells_off ? static_cast<uint32_t>(a.cells_off[t + 1] - a.cells_off[t]) : a.ncells[t];
+            const uint32_t* cp = a.cells + (a.cells_off ? a.cells_off[t] : t * a.cells_cap);
+            for (uint32_t i = lane; i < cnt; i += 32) {
+                const uint32_t slot = s * R + cp[i] + 1;
+                atomicOr(M + (slot >> 1), 1u << (j + ((slot & 1u) << 4)));
+            }
+        }
+    }
+    __syncthreads();
+}
+
+// Region offsets of the 8 code positions (positions >= N_s read region 0's zero slot).
+struct RegionOff {
+    uint32_t o[8];
+    __device__ RegionOff(uint32_t ns, uint32_t K) {
+#pragma unroll
+        for (uint32_t s = 0; s < 8; ++s) o[s] = s < ns ? s * (K + 1) : 0u;
+    }
+};
+
+__device__ __forceinline__ void planes_h(const uint16_t* M16, const RegionOff& ro, uint4 ca, uint4 cb,
+                                         uint32_t (&b)[4]) {
+    const uint32_t xa[4] = {ca.x, ca.y, ca.z, ca.w}, xb[4] = {cb.x, cb.y, cb.z, cb.w};
+    uint32_t m[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        m[2 * i] = uint32_t(M16[ro.o[2 * i] + (xa[i] & 0xffffu)]) | (uint32_t(M16[ro.o[2 * i] + (xb[i] & 0xffffu)]) << 16);
+        m[2 * i + 1] = uint32_t(M16[ro.o[2 * i + 1] + (xa[i] >> 16)]) | (uint32_t(M16[ro.o[2 * i + 1] + (xb[i] >> 16)]) << 16);
+    }
+    uint32_t s1, c1, s2, c2, b0, c4, s5, c5;
+    fadd(m[0], m[1], m[2], s1, c1);
+    fadd(m[3], m[4], m[5], s2, c2);
+    const uint32_t s3 = m[6] ^ m[7], c3 = m[6] & m[7];
+    fadd(s1, s2, s3, b0, c4);
+    fadd(c1, c2, c3, s5, c5);
+    const uint32_t c6 = s5 & c4;
+    b[0] = b0;
+    b[1] = s5 ^ c4;
+    b[2] = c5 ^ c6;
+    b[3] = c5 & c6;
+}
+
+// K1 (half width): per (query, piece) #points with score >= t, t = 1..8.
+template <uint32_t kDT>
+__global__ void __launch_bounds__(kDT, 1024 / kDT) dense_hist_h_kernel(DenseArgs a) {
+    constexpr uint32_t kDW = kDT / 32;
+    extern __shared__ uint32_t M[];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint64_t q0 = uint64_t(blockIdx.x) * 16;
+    const uint64_t nvalid = a.qmap ? *a.nmap : a.nq;
+    if (q0 >= nvalid) return;
+    const uint32_t nqb = static_cast<uint32_t>(min_u64(16, nvalid - q0));
+    build_masks_h<kDT>(a, M, q0, nqb);
+    const uint32_t row = blockIdx.y * kDW + warp;
+    if (row >= a.P) return;
+    const uint64_t lo = uint64_t(row) * (a.pstride ? a.pstride : 1u) * a.WP;
+    if (lo >= a.n) return;
+    const uint64_t hi = min_u64(a.n, lo + a.WP);  // rows past n are zero-code padding: score 0
+    const uint16_t* M16 = reinterpret_cast<const uint16_t*>(M);
+    const RegionOff ro(a.ns, a.K);
+    const Xpose xp(lane);
+    uint32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (uint64_t t0 = lo; t0 < hi; t0 += 64) {
+        uint32_t b[4];
+        planes_h(M16, ro, __ldg(a.codes + t0 + lane), __ldg(a.codes + t0 + 32 + lane), b);
+        const uint32_t B0 = xp(b[0]), B1 = xp(b[1]), B2 = xp(b[2]), B3 = xp(b[3]);
+        const uint32_t g8 = B3, g4 = B3 | B2, g2 = g4 | B1, g1 = g2 | B0;
+        const uint32_t g6 = B3 | (B2 & B1), g5 = B3 | (B2 & (B1 | B0)), g7 = B3 | (B2 & B1 & B0);
+        const uint32_t g3 = g4 | (B1 & B0);
+        cnt[0] += __popc(g1);
+        cnt[1] += __popc(g2);
+        cnt[2] += __popc(g3);
+        cnt[3] += __popc(g4);
+        cnt[4] += __popc(g5);
+        cnt[5] += __popc(g6);
+        cnt[6] += __popc(g7);
+        cnt[7] += __popc(g8);
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) cnt[t] += __shfl_xor_sync(kFull, cnt[t], 16);  // the tile's two halves
+    if (lane < nqb) {
+        uint4 v;
+        v.x = cnt[0] | (cnt[1] << 16);
+        v.y = cnt[2] | (cnt[3] << 16);
+        v.z = cnt[4] | (cnt[5] << 16);
+        v.w = cnt[6] | (cnt[7] << 16);
+        const uint64_t q = a.qmap ? a.qmap[q0 + lane] : q0 + lane;
+        reinterpret_cast<uint4*>(a.hist)[q * a.P + row] = v;
+    }
+}
+
+// K3 (half width): lanes c and c + 16 share query c; ties and output slots are taken in id order
+// (the first half of a tile before the second).
+template <uint32_t kDT>
+__global__ void __launch_bounds__(kDT, 1024 / kDT) dense_emit_h_kernel(DenseArgs a) {
+    constexpr uint32_t kDW = kDT / 32;
+    extern __shared__ uint32_t M[];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint64_t q0 = uint64_t(blockIdx.x) * 16;
+    const uint64_t nvalid = a.qmap ? *a.nmap : a.nq;
+    if (q0 >= nvalid) return;
+    const uint32_t nqb = static_cast<uint32_t>(min_u64(16, nvalid - q0));
+    build_masks_h<kDT>(a, M, q0, nqb);
+    const uint32_t piece = blockIdx.y * kDW + warp;
+    if (piece >= a.P) return;
+    const uint64_t lo = uint64_t(piece) * a.WP;
+    const uint64_t hi = min_u64(a.n, lo + a.WP);
+    const uint32_t qj = lane & 15u, half = lane >> 4;
+    const bool mine = qj < nqb;
+    const uint64_t q = !mine ? 0 : a.qmap ? a.qmap[q0 + qj] : q0 + qj;
+    const uint32_t T = mine ? a.T[q] : 0u;
+    const uint32_t quota = mine ? a.quota[q * a.P + piece] : 0u;
+    uint32_t pos = mine ? a.base[q * a.P + piece] : 0u, tseen = 0;
+    uint32_t* out = a.cands + q * a.m;
+    const uint16_t* M16 = reinterpret_cast<const uint16_t*>(M);
+    const RegionOff ro(a.ns, a.K);
+    const Xpose xp(lane);
+    for (uint64_t t0 = lo; t0 < hi; t0 += 64) {
+        uint32_t b[4];
+        planes_h(M16, ro, __ldg(a.codes + t0 + lane), __ldg(a.codes + t0 + 32 + lane), b);
+        const uint32_t B0 = xp(b[0]), B1 = xp(b[1]), B2 = xp(b[2]), B3 = xp(b[3]);
+        const uint64_t pb = t0 + 32 * half;  // this lane's first point
+        const uint32_t vmask = !mine || pb >= hi ? 0u : hi - pb >= 32 ? kFull : ((1u << (hi - pb)) - 1u);
+        const uint32_t geT = ge_mask(B0, B1, B2, B3, T) & vmask;
+        const uint32_t gt = ge_mask(B0, B1, B2, B3, T + 1) & vmask;
+        const uint32_t eq = geT & ~gt;
+        const uint32_t ec = __popc(eq), eo = __shfl_xor_sync(kFull, ec, 16);
+        const uint32_t seen = tseen + (half ? eo : 0u);  // ties before this lane's points
+        uint32_t take = gt;
+        if (eq && seen < quota) {
+            const uint32_t r = quota - seen;
+            uint32_t rest = eq;
+            for (uint32_t i = 0; i < r && rest; ++i) rest &= rest - 1;
+            take |= eq ^ rest;
+        }
+        tseen += ec + eo;
+        const uint32_t tc = __popc(take), to = __shfl_xor_sync(kFull, tc, 16);
+        uint32_t p = pos + (half ? to : 0u);
+        while (take) {
+            const uint32_t bit = __ffs(take) - 1;
+            take &= take - 1;
+            __stcs(out + p++, static_cast<uint32_t>(pb) + bit);
+        }
+        pos += tc + to;
+    }
+}
+
+// K3' (half width): histograms + per-(query, piece) supersets in one pass (as fused_pieces, 2-byte
+// stores; lanes c and c + 16 append to query c's buffer in id order).
+template <uint32_t kDT>
+__global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_h_kernel(DenseArgs a) {
+    constexpr uint32_t kDW = kDT / 32;
+    extern __shared__ uint32_t M[];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint64_t q0 = uint64_t(blockIdx.x) * 16;
+    const uint32_t nqb = static_cast<uint32_t>(min_u64(16, a.nq - q0));
+    const uint32_t myL = threadIdx.x < nqb ? a.L[q0 + threadIdx.x] : 0u;
+    if (!__syncthreads_or((myL & 0xffu) != 0)) return;  // all two-pass
+    build_masks_h<kDT>(a, M, q0, nqb);
+    const uint32_t qj = lane & 15u, half = lane >> 4;
+    const bool mine = qj < nqb;
+    // bits j and 16 + j of each word = query j's L bits (the ballot of lanes j and j + 16)
+    const uint32_t L = mine ? a.L[q0 + qj] & 0xffu : 0u;
+    const uint32_t T0 = __ballot_sync(kFull, L & 1u), T1 = __ballot_sync(kFull, L & 2u);
+    const uint32_t T2 = __ballot_sync(kFull, L & 4u), T3 = __ballot_sync(kFull, L & 8u);
+    const uint32_t live = __ballot_sync(kFull, L != 0);
+    const uint16_t* M16 = reinterpret_cast<const uint16_t*>(M);
+    const RegionOff ro(a.ns, a.K);
+    const Xpose xp(lane);
+    for (uint32_t k = 0; k < a.ppw; ++k) {
+        const uint32_t piece = (blockIdx.y * kDW + warp) * a.ppw + k;
+        if (piece >= a.P) return;
+        const uint64_t lo = uint64_t(piece) * a.WP;
+        const uint64_t hi = min_u64(a.n, lo + a.WP);
+        uint32_t cnt = 0, nb = 0;
+        uint16_t* buf = a.cbuf + ((mine ? q0 + qj : q0) * a.P + piece) * a.B;
+        uint4 ca = __ldg(a.codes + lo + lane), cb = __ldg(a.codes + lo + 32 + lane);
+        for (uint64_t t0 = lo; t0 < hi; t0 += 64) {
+            // one tile ahead (the padded code rows cover a whole last piece)
+            const bool more = t0 + 64 < hi;
+            const uint4 na = more ? __ldg(a.codes + t0 + 64 + lane) : ca;
+            const uint4 nbv = more ? __ldg(a.codes + t0 + 96 + lane) : cb;
+            uint32_t b[4];
+            planes_h(M16, ro, ca, cb, b);
+            ca = na;
+            cb = nbv;
+            uint32_t gt = b[3] & ~T3, eq = ~(b[3] ^ T3);
+            gt |= eq & b[2] & ~T2;
+            eq &= ~(b[2] ^ T2);
+            gt |= eq & b[1] & ~T1;
+            eq &= ~(b[1] ^ T1);
+            gt |= eq & b[0] & ~T0;
+            eq &= ~(b[0] ^ T0);
+            // queries past the block's last have no live bits: their lanes see empty words
+            const uint32_t ge0 = xp((gt | eq) & live);
+            const uint32_t g1 = xp(gt & live);
+            const uint32_t c0 = __popc(ge0), o0 = __shfl_xor_sync(kFull, c0, 16);
+            cnt += c0 | (__popc(g1) << 16);
+            uint32_t at = nb + (half ? o0 : 0u);
+            const uint32_t tb = static_cast<uint32_t>(t0 - lo) + 32 * half;
+            uint32_t bits = ge0;
+            while (bits) {  // id order
+                const uint32_t r = __ffs(bits) - 1;
+                bits &= bits - 1;
+                if (at < a.B) buf[at] = static_cast<uint16_t>((tb + r) | (((g1 >> r) & 1u) << 15));
+                ++at;
+            }
+            nb += c0 + o0;
+        }
+        cnt += __shfl_xor_sync(kFull, cnt, 16);  // packed 16-bit halves, each <= 2048
+        if (half == 0 && mine) {
+            const uint64_t i = (q0 + qj) * a.P + piece;
+            a.h2[i] = cnt;
+            a.ccnt[i] = static_cast<uint16_t>(nb);
+        }
+    }
+}
+
+__global__ void dense_codes_half_kernel(const uint32_t* ids, const uint32_t* cell_off, uint64_t n, uint32_t ns,
+                                        uint32_t K, uint16_t* codes) {
+    const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (t >= uint64_t(ns) * K) return;
+    const uint32_t s = static_cast<uint32_t>(t / K), cell = static_cast<uint32_t>(t % K);
+    const uint32_t* off = cell_off + uint64_t(s) * (K + 1);
+    const uint32_t* sid = ids + uint64_t(s) * n;
+    for (uint32_t i = off[cell]; i < off[cell + 1]; ++i) codes[uint64_t(sid[i]) * 8 + s] = static_cast<uint16_t>(cell + 1);
+}
+
 }  // namespace
+
+bool dense_half_supported(uint32_t ns, uint32_t K) {
+    return ns >= 1 && ns <= 8 && K + 1 <= 65535 && (uint64_t(ns) * (K + 1) + 1) * 2 <= 200 * 1024;
+}
+
+static size_t dense_half_smem(uint32_t ns, uint32_t K) { return ((size_t(ns) * (K + 1) + 1) / 2) * 4; }
+
+cudaError_t launch_dense_codes_half(const uint32_t* ids, const uint32_t* cell_off, uint64_t n, uint64_t n_pad,
+                                    uint32_t ns, uint32_t K, uint16_t* codes, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(codes, 0, n_pad * 8 * sizeof(uint16_t), st);
+    if (e != cudaSuccess) return e;
+    const uint64_t total = uint64_t(ns) * K;
+    dense_codes_half_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(ids, cell_off, n, ns, K, codes);
+    return cudaGetLastError();
+}
+
+template <uint32_t kDT, int KIND>  // 0 hist, 1 emit, 2 fused
+static cudaError_t launch_h_t(const DenseArgs& a, size_t smem, cudaStream_t st) {
+    auto kern = KIND == 0 ? dense_hist_h_kernel<kDT> : KIND == 1 ? dense_emit_h_kernel<kDT> : dense_fused_h_kernel<kDT>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    constexpr uint32_t kDW = kDT / 32;
+    const uint64_t qblocks = (a.nq + 15) / 16;
+    DenseArgs b = a;
+    uint32_t per_cta = kDW;
+    if (KIND == 2) {
+        int sms = 148, dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        b.ppw = kFusedPPW;
+        if (qblocks * ((a.P + kDW * b.ppw - 1) / (kDW * b.ppw)) < 4ull * sms) b.ppw = 1;
+        per_cta = kDW * b.ppw;
+    }
+    const dim3 grid(static_cast<unsigned>(qblocks), (a.P + per_cta - 1) / per_cta);
+    kern<<<grid, kDT, smem, st>>>(b);
+    return cudaGetLastError();
+}
+
+template <int KIND>
+static cudaError_t launch_h(const DenseArgs& a, cudaStream_t st) {
+    if (a.nq == 0) return cudaSuccess;
+    const size_t smem = dense_half_smem(a.ns, a.K);
+    return smem <= 110 * 1024 ? launch_h_t<512, KIND>(a, smem, st) : launch_h_t<1024, KIND>(a, smem, st);
+}
 
 bool dense_supported(uint32_t ns, uint32_t K) {
     return ns >= 1 && ns <= 8 && uint64_t(ns) * K + 1 <= 65535 && (uint64_t(ns) * K + 1) * 4 <= 200 * 1024;
@@ -701,8 +992,12 @@ __global__ void dense_rows_kernel(DenseArgs a, uint32_t* out) {  // u16 x 8 -> [
     o[a.ns + 1] = 0;
 }
 
-cudaError_t launch_dense_hist(const DenseArgs& a, cudaStream_t st) { return launch_scan_any<false>(a, st); }
-cudaError_t launch_dense_emit(const DenseArgs& a, cudaStream_t st) { return launch_scan_any<true>(a, st); }
+cudaError_t launch_dense_hist(const DenseArgs& a, cudaStream_t st) {
+    return a.half ? launch_h<0>(a, st) : launch_scan_any<false>(a, st);
+}
+cudaError_t launch_dense_emit(const DenseArgs& a, cudaStream_t st) {
+    return a.half ? launch_h<1>(a, st) : launch_scan_any<true>(a, st);
+}
 
 cudaError_t launch_dense_hist_rows(const DenseArgs& a, uint32_t* out, cudaStream_t st) {
     const uint64_t total = a.nq * a.P;
@@ -742,9 +1037,13 @@ cudaError_t launch_dense_select_fused(const DenseArgs& args, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     dense_bound_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(a);
     // K3': histograms + supersets in one pass
-    const Shape sh = dense_shape(a);
-    if (sh.words == 2) e = launch_fused_t<1024, 2>(a, sh.smem, st);
-    else e = sh.threads == 512 ? launch_fused_t<512, 1>(a, sh.smem, st) : launch_fused_t<1024, 1>(a, sh.smem, st);
+    if (a.half) {
+        e = launch_h<2>(a, st);
+    } else {
+        const Shape sh = dense_shape(a);
+        if (sh.words == 2) e = launch_fused_t<1024, 2>(a, sh.smem, st);
+        else e = sh.threads == 512 ? launch_fused_t<512, 1>(a, sh.smem, st) : launch_fused_t<1024, 1>(a, sh.smem, st);
+    }
     if (e != cudaSuccess) return e;
     // plan (+ fallback flags) from the two levels, compaction
     dense_plan_fused_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(a);

@@ -109,9 +109,16 @@ struct DenseArgs {
     uint32_t* nmap;            // device count of qmap entries
     uint32_t ppw;                 // fused pass: pieces per warp (set by the launcher)
     uint32_t stage_all;           // fused pass: stage every block's stores (tests; else by density)
+    uint32_t half;                // 16-query blocks, u16 masks, codes = cell + 1 per subspace (large N_s*K)
 };
 bool dense_supported(uint32_t ns, uint32_t K);
 size_t dense_smem(uint32_t ns, uint32_t K);
+// Half-width mode for tables too large for 32-bit masks (config 5: N_s*K = 80,000 cells): 16-query
+// blocks, one u16 mask per (subspace, cell), two points per lane; codes hold cell + 1 per subspace
+// (0 = no cell), n_pad = rows rounded up to whole pieces (padding rows are all 0).
+bool dense_half_supported(uint32_t ns, uint32_t K);
+cudaError_t launch_dense_codes_half(const uint32_t* ids, const uint32_t* cell_off, uint64_t n, uint64_t n_pad,
+                                    uint32_t ns, uint32_t K, uint16_t* codes, cudaStream_t st);
 cudaError_t launch_dense_codes(const uint32_t* ids, const uint32_t* cell_off, uint64_t n, uint32_t ns, uint32_t K,
                                uint16_t* codes, cudaStream_t st);
 cudaError_t launch_dense_select(const DenseArgs& a, cudaStream_t st);  // hist + plan + emit

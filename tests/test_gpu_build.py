@@ -117,3 +117,64 @@ def test_build_index_errors(gpu):  # index.cpp:100-111, subspace.cpp:12-21, core
     bad[3, 1] = np.inf
     with pytest.raises(gpu.ContractError):
         gpu.build_index(bad, gpu.IndexParams(2, 5, 3))
+
+
+# ---------------------------------------- config 5's sampled build (suco_gpu_build_index_sampled)
+@pytest.mark.parametrize("case", [
+    # n, d, clusters, lo, hi, sigma, quantize, ns, k_half, iters, mode, n_train, chunk
+    (6000, 32, 20, 0, 100, 8, False, 4, 16, 4, 0, 700, None),
+    (8000, 16, 30, 20, 140, 18, True, 2, 40, 3, 1, 1200, 999),     # several assignment chunks, ragged last
+    (3000, 60, 10, 0, 1, 0.05, False, 3, 10, 2, 0, 10, 3000),      # n_train == k_half; h = 10
+    (2500, 16, 8, 0, 100, 10, False, 8, 20, 5, 0, 2500, None),     # every row trains
+])
+def test_sampled_build_vs_oracle(gpu, oracle, monkeypatch, case):
+    n, d, cl, lo, hi, sig, q, ns, kh, it, mode, nt, chunk = case
+    if chunk:
+        monkeypatch.setenv("SUCO_BUILD_CHUNK", str(chunk))
+    data = oracle.clustered(n, d, cl, n + d, lo, hi, sig, q)
+    train = np.sort(np.random.default_rng(n).choice(n, nt, replace=False)).astype(np.uint32)
+    ours = gpu.build_index_sampled(data, train, gpu.IndexParams(ns, kh, it, 7, gpu.SubspaceMode(mode)))
+    theirs = oracle.build_index_sampled(data, train, ns, kh, it, 7, mode)
+    assert ours.serialize() == theirs.serialize()
+
+
+def test_sampled_build_from_device_rows(gpu, oracle):
+    torch = pytest.importorskip("torch")
+    data = oracle.clustered(5000, 24, 12, 5, 0, 100, 8, False)
+    train = np.arange(0, 5000, 7, dtype=np.uint32)
+    p = gpu.IndexParams(3, 16, 3, 11)
+    host = gpu.build_index_sampled(data, train, p).serialize()
+    dev = torch.from_numpy(data).cuda()
+    assert gpu.build_index_sampled(dev, train, p).serialize() == host
+    assert gpu.build_index(dev, p).serialize() == gpu.build_index(data, p).serialize()
+
+
+def test_sampled_build_errors(gpu):
+    data = np.random.default_rng(0).random((300, 8)).astype(np.float32)
+    p = gpu.IndexParams(2, 5, 3)
+    with pytest.raises(gpu.ConfigError):  # fewer training rows than k_half
+        gpu.build_index_sampled(data, np.arange(4), p)
+    for bad in (np.arange(10)[::-1], np.array([1, 1, 2, 3, 4, 5]), np.array([0, 1, 2, 3, 4, 300])):
+        with pytest.raises(gpu.ContractError):
+            gpu.build_index_sampled(data, bad, p)
+    nan = data.copy()
+    nan[5, 2] = np.nan
+    with pytest.raises(gpu.ContractError):  # dataset invariants first (core.cpp:15-19)
+        gpu.build_index_sampled(nan, np.arange(50), p)
+
+
+def test_sampled_cfg5_shape_query_vs_reference(gpu, ref):
+    """Config 5's shape scaled down (u8 descriptors, N_s = 8, 100 x 100 centroids on a 1 % sample,
+    alpha = 0.02, beta = 0.002): K = 10,000 cells per subspace takes the cluster-counting select.
+    The reference's own load_index + knn_query on the GPU-built bytes give the same answers."""
+    import bench_data
+
+    cfg = bench_data.CONFIGS["cfg5"]
+    base, queries = bench_data.generate(cfg, n=300_000, queries=48)
+    train = bench_data.train_ids(cfg, base.shape[0])
+    idx = gpu.build_index_sampled(base, train, gpu.IndexParams(8, 100, 10, 42))
+    blob = idx.serialize()
+    cp = gpu.CollisionParams(cfg.alpha, cfg.beta, cfg.k)
+    ids, dists = idx.knn_query_batch(queries, cp)
+    ri, rd, _ = ref.load_index(blob).knn_query_batch(base, queries, cfg.alpha, cfg.beta, cfg.k)
+    assert np.array_equal(ids, ri) and np.array_equal(dists, rd)

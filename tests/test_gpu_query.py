@@ -348,3 +348,45 @@ def test_dense_buffer_overflow_falls_back(gpu, oracle, monkeypatch, capfd):
     flagged = [int(line.split("dense select: ")[1].split(" of")[0]) for line in err.splitlines()
                if "dense select:" in line]
     assert flagged and max(flagged) > 0, err
+
+
+@pytest.mark.parametrize("fused", ["1", "0"])
+@pytest.mark.parametrize("ns,kh,nq", [(6, 20, 77), (8, 30, 40), (3, 45, 16)])
+def test_dense_half_width_mode(gpu, oracle, ns, kh, fused, nq, monkeypatch):
+    """The half-width dense select (16-query blocks, u16 masks, two points per lane — the mode config
+    5's 8 x 10,000 cells take) forced on small tables: single-pass and two-pass, N_s < 8 (code
+    positions past N_s), a partial last query block and a partial last 64-point tile."""
+    monkeypatch.setenv("SUCO_DENSE_HALF", "2")
+    monkeypatch.setenv("SUCO_DENSE_FUSED", fused)
+    full = oracle.clustered(60000 + nq, 24, 30, 2024 + ns, 0, 100, 9, True)
+    base, qs = oracle.hold_out(full, nq, 2025)
+    oidx = oracle.build_index(base, ns, kh, 3, 42, 0)
+    idx = gpu.load_index(oidx.serialize(), base)
+    for a, b, k in ((0.05, 0.01, 10), (0.01, 0.2, 33), (0.3, 0.002, 5)):
+        ids, dd = idx.knn_query_batch(qs, gpu.CollisionParams(a, b, k))
+        oi, od, _ = oidx.knn_query_batch(base, qs, a, b, k)
+        assert np.array_equal(ids, oi) and np.array_equal(dd, od), (ns, a, b, k)
+    s1, c1, _, _ = idx.query_intermediates(qs[3], gpu.CollisionParams(0.05, 0.01, 10))
+    s2, c2, _, _ = oidx.query_intermediates(base, qs[3], 0.05, 0.01, 10)
+    assert np.array_equal(c1, c2)
+
+
+def test_dense_half_width_overflow_falls_back(gpu, oracle, monkeypatch, capfd):
+    """Half-width mode: an overflowing (query, piece) buffer flags its query for the exact two-pass
+    select (as test_dense_buffer_overflow_falls_back)."""
+    monkeypatch.setenv("SUCO_DENSE_HALF", "2")
+    monkeypatch.setenv("SUCO_DENSE_STATS", "1")
+    full = oracle.clustered(40000 + 40, 16, 8, 77, 0, 100, 6, True)
+    full = full[np.argsort(full[:, 0], kind="stable")]
+    pick = np.sort(np.random.default_rng(5).choice(len(full), 40, replace=False))
+    qs, base = full[pick], np.delete(full, pick, axis=0)
+    oidx = oracle.build_index(base, 4, 12, 3, 42, 0)
+    idx = gpu.load_index(oidx.serialize(), base)
+    for a, b, k in ((0.2, 0.01, 10), (0.05, 0.02, 20)):
+        ids, dd = idx.knn_query_batch(qs, gpu.CollisionParams(a, b, k))
+        oi, od, _ = oidx.knn_query_batch(base, qs, a, b, k)
+        assert np.array_equal(ids, oi) and np.array_equal(dd, od), (a, b, k)
+    err = capfd.readouterr().err
+    flagged = [int(line.split("dense select: ")[1].split(" of")[0]) for line in err.splitlines()
+               if "dense select:" in line]
+    assert flagged and max(flagged) > 0, err

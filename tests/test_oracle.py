@@ -206,3 +206,61 @@ def test_random_builds_match_reference(oracle, ref, seed):
         i1, d1, _ = io.knn_query_batch(data, qs, a, b, k)
         i2, d2, _ = ir.knn_query_batch(data, qs, a, b, k, threads=2)
         assert np.array_equal(i1, i2) and np.array_equal(d1, d2)
+
+
+# ------------------------------- config 5's sampled build (no reference API; pinned by composition)
+def _sampled_case(oracle, seed, n=2400, d=16, ns=4, k_half=12, n_train=500, quantize=False, mode=0):
+    data = oracle.clustered(n, d, 9, seed, 0.0, 100.0, 10.0, quantize)
+    train = np.sort(np.random.default_rng(seed).choice(n, n_train, replace=False)).astype(np.uint32)
+    return data, train, dict(ns=ns, k_half=k_half, iters=4, seed=seed, mode=mode)
+
+
+def test_sampled_build_with_every_row_is_build_index(oracle):
+    data, _, p = _sampled_case(oracle, 31)
+    full = np.arange(data.shape[0], dtype=np.uint32)
+    a = oracle.build_index_sampled(data, full, p["ns"], p["k_half"], p["iters"], p["seed"], p["mode"]).serialize()
+    assert a == oracle.build_index(data, p["ns"], p["k_half"], p["iters"], p["seed"], p["mode"]).serialize()
+
+
+@pytest.mark.parametrize("seed,quantize,mode", [(41, False, 0), (42, True, 0), (43, False, 1)])
+def test_sampled_build_pinned_to_reference(oracle, ref, seed, quantize, mode):
+    """Centroids = the reference's build_index over the training rows (same jobs, same seeds);
+    each training row's cell = its cell in that reference index; every other row's half-subspace
+    cell = the first entry of the reference's own centroid_distances order (query.cpp:42-64)."""
+    from suco_bytes import cell_of, parse
+
+    data, train, p = _sampled_case(oracle, seed, quantize=quantize, mode=mode)
+    mine = parse(oracle.build_index_sampled(data, train, p["ns"], p["k_half"], p["iters"], p["seed"], p["mode"])
+                 .serialize())
+    theirs = parse(ref.build_index(data[train], p["ns"], p["k_half"], p["iters"], p["seed"], p["mode"]).serialize())
+    n, kh = data.shape[0], p["k_half"]
+    assert mine["n"] == n and theirs["n"] == train.size
+    others = np.setdiff1d(np.arange(n), train)[::23]
+    for s in range(p["ns"]):
+        a, b = mine["subspaces"][s], theirs["subspaces"][s]
+        assert np.array_equal(a["cent1"], b["cent1"]) and np.array_equal(a["cent2"], b["cent2"])
+        ca, cb = cell_of(a, n), cell_of(b, train.size)
+        assert np.array_equal(ca[train], cb)
+        dims = mine["dims"][s]
+        h1 = len(dims) // 2
+        for i in others:
+            row = data[i, dims]
+            _, o1 = ref.centroid_distances(row[:h1], a["cent1"], kh)
+            _, o2 = ref.centroid_distances(row[h1:], a["cent2"], kh)
+            assert ca[i] == int(o1[0]) * kh + int(o2[0])
+
+
+def test_sampled_build_validation(oracle):
+    from oracle.oracle import OracleError
+
+    data, train, p = _sampled_case(oracle, 51)
+    args = (p["ns"], p["k_half"], p["iters"], p["seed"], p["mode"])
+    with pytest.raises(OracleError) as e:  # fewer training rows than k_half -> ConfigError
+        oracle.build_index_sampled(data, train[: p["k_half"] - 1], *args)
+    assert e.value.code == 2
+    oracle.build_index_sampled(data, train[: p["k_half"]], *args)  # exactly k_half trains
+    for bad in (train[::-1].copy(), np.array([0, 0] + list(range(2, 40)), np.uint32),
+                np.array(list(range(30)) + [data.shape[0]], np.uint32)):
+        with pytest.raises(OracleError) as e:  # not strictly ascending / out of range -> ContractError
+            oracle.build_index_sampled(data, bad, *args)
+        assert e.value.code == 5
