@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -203,6 +205,452 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
                 a.out_ids[q * a.k + lane] = lid;
                 a.out_dists[q * a.k + lane] = a.squared ? ld : __dsqrt_rn(ld);
             }
+        }
+    }
+}
+
+// ------------------------------------------------------- pipelined f32 rows
+// The same arithmetic as rerank_kernel (rows d % 4 == 0), with the row gathers moved off the
+// critical path: a warp's work is a sequence of items (8-row group, 128-dim chunk); each item is
+// copied global -> shared with 16-byte cp.async into one of kStages ring slots, kStages - 1 items
+// ahead of the one being folded, and the candidate ids of the next kIdAhead groups are loaded
+// into the warp's registers (lane 8t + j holds id j of group g with g % kIdAhead == t) long
+// before their rows are requested. One CTA per query, 2 CTAs per SM.
+constexpr uint32_t kStages = 3;
+constexpr uint32_t kIdAhead = 4;
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <bool GENERIC>
+__global__ void __launch_bounds__(kThreads, 2) rerank_pipe_kernel(RerankArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* qd = reinterpret_cast<double*>(smem);                             // d
+    float* qf = reinterpret_cast<float*>(smem + ((a.d * 8 + 15) / 16) * 16);  // d
+    float* ring = qf + ((a.d + 3) / 4) * 4;                                     // warps x stages x rows x stride
+    __shared__ unsigned int qstat[2];
+    __shared__ uint32_t idbuf[kWarps][kStages][kRows];  // the ids of each ring slot's rows
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint64_t q = blockIdx.x;
+    const float* query = a.queries + q * a.d;
+    if (tid < 2) qstat[tid] = 0;
+    __syncthreads();
+    bool qbad = false, qu8 = true;
+    float qmax = 0.f;
+    for (uint32_t i = tid; i < a.d; i += kThreads) {
+        const float v = query[i];
+        qd[i] = static_cast<double>(v);
+        qf[i] = v;
+        qbad |= (v != truncf(v));
+        qu8 &= is_u8(v);
+        qmax = fmaxf(qmax, fabsf(v));
+    }
+    if (a.data8 && __syncthreads_and(qu8)) return;  // rerank_u8_kernel owns this query
+    qbad = __any_sync(kFull, qbad);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) qmax = fmaxf(qmax, __shfl_xor_sync(kFull, qmax, o));
+    if (lane == 0) {
+        if (qbad) atomicOr(&qstat[0], 1u);
+        atomicMax(&qstat[1], __float_as_uint(qmax));
+    }
+    __syncthreads();
+    bool use32 = false;  // certified-exact fp32 chains (see rerank_kernel)
+    if (a.data_int_max >= 0.f && qstat[0] == 0) {
+        const double span = static_cast<double>(a.data_int_max) + static_cast<double>(__uint_as_float(qstat[1]));
+        use32 = (static_cast<double>(a.d / 4 + 4) * span * span) < 16777216.0;
+    }
+
+    float* wr = ring + warp * kStages * kRows * kStride;
+    const uint32_t r = lane >> 2, acc_i = lane & 3u;
+    const uint32_t* cands = a.cands + q * a.m;
+    const uint64_t mq = a.counts ? a.counts[q] : a.m;
+    const uint32_t nch = (a.d + kChunk - 1) / kChunk;
+    const uint64_t first = uint64_t(warp) * kRows;
+    const uint64_t groups = mq > first ? (mq - first + kRows * kWarps - 1) / (kRows * kWarps) : 0;
+    const uint64_t items = groups * nch;
+    auto gbase = [&](uint64_t g) { return first + g * kRows * kWarps; };
+    auto load_id = [&](uint64_t g) -> uint32_t {  // this lane's id slot of group g
+        const uint64_t i = gbase(g) + (lane & 7u);
+        if (g >= groups || i >= mq) return 0u;
+        return a.identity ? static_cast<uint32_t>(i) : __ldcs(cands + i);
+    };
+    uint32_t idreg = 0;
+#pragma unroll
+    for (uint32_t t = 0; t < kIdAhead; ++t) {
+        if ((lane >> 3) == t) idreg = load_id(t);
+    }
+    auto issue = [&](uint64_t i) {
+        const uint64_t g = i / nch;
+        const uint32_t c0 = static_cast<uint32_t>(i % nch) * kChunk;
+        const uint32_t cl = min(kChunk, a.d - c0);
+        const uint32_t slot = (g % kIdAhead) * 8u;
+        const uint64_t b = gbase(g);
+        const uint32_t si = static_cast<uint32_t>(i % kStages);
+        float* st = wr + si * kRows * kStride;
+#pragma unroll
+        for (uint32_t j = 0; j < kRows; ++j) {
+            const uint32_t id = __shfl_sync(kFull, idreg, slot + j);
+            if (b + j < mq && 4 * lane < cl) cp_async16(st + j * kStride + 4 * lane, a.data + uint64_t(id) * a.d + c0 + 4 * lane);
+            if (lane == j) idbuf[warp][si][j] = id;
+        }
+        if (c0 + cl == a.d) {  // the group's last chunk is in flight: its id slots take group g + kIdAhead
+            if ((lane >> 3) == g % kIdAhead) idreg = load_id(g + kIdAhead);
+        }
+    };
+    double ld = kInf;
+    uint32_t lid = 0xffffffffu;
+    double acc = 0.0;
+    float acc32 = 0.f;
+    for (uint32_t i = 0; i + 1 < kStages; ++i) {
+        if (i < items) issue(i);
+        cp_async_commit();
+    }
+    for (uint64_t i = 0; i < items; ++i) {
+        if (i + kStages - 1 < items) issue(i + kStages - 1);
+        cp_async_commit();
+        cp_async_wait<kStages - 1>();  // item i has landed (this lane's copies)
+        __syncwarp();                  // ... and every lane's
+        const uint64_t g = i / nch;
+        const uint32_t c0 = static_cast<uint32_t>(i % nch) * kChunk;
+        const uint32_t cl = min(kChunk, a.d - c0);
+        const uint64_t b = gbase(g);
+        const uint32_t nrows = static_cast<uint32_t>(min_u64(kRows, mq - b));
+        if (r < nrows) {
+            const float* row = wr + static_cast<uint32_t>(i % kStages) * kRows * kStride + r * kStride;
+            if (use32) {
+#pragma unroll 8
+                for (uint32_t e = acc_i; e < cl; e += 4) {
+                    const float df = row[e] - qf[c0 + e];
+                    acc32 = __fmaf_rn(df, df, acc32);
+                }
+            } else {
+#pragma unroll 8
+                for (uint32_t e = acc_i; e < cl; e += 4) acc = __dadd_rn(acc, sqdiff_d(row[e], qd[c0 + e]));
+            }
+        }
+        if (c0 + cl == a.d) {  // group done: combine the four chains, keep the top-k
+            if (use32) acc = static_cast<double>(acc32);
+            const double a1 = __shfl_down_sync(kFull, acc, 1);
+            const double a2 = __shfl_down_sync(kFull, acc, 2);
+            const double a3 = __shfl_down_sync(kFull, acc, 3);
+            const double dist = __dadd_rn(__dadd_rn(acc, a1), __dadd_rn(a2, a3));  // valid on lanes 4r
+            const uint32_t* ids = idbuf[warp][static_cast<uint32_t>(i % kStages)];
+            acc = 0.0;
+            acc32 = 0.f;
+            if constexpr (GENERIC) {
+                if (acc_i == 0 && r < nrows) {
+                    a.all_d[q * a.m + b + r] = dist;
+                    a.all_id[q * a.m + b + r] = ids[r];
+                }
+            } else {
+#pragma unroll
+                for (uint32_t j = 0; j < kRows; ++j) {
+                    const double dj = __shfl_sync(kFull, dist, 4 * j);
+                    if (j < nrows) warp_insert(dj, ids[j], ld, lid, a.k, lane);
+                }
+            }
+        }
+        __syncwarp();  // the slot (rows and ids) is refilled by the next iteration's issue
+    }
+    cp_async_wait<0>();
+    if constexpr (!GENERIC) {
+        __syncthreads();
+        double* md = reinterpret_cast<double*>(ring);
+        uint32_t* mi = reinterpret_cast<uint32_t*>(md + kWarps * 32);
+        md[warp * 32 + lane] = ld;
+        mi[warp * 32 + lane] = lid;
+        __syncthreads();
+        if (warp == 0) {
+            for (uint32_t w = 1; w < kWarps; ++w) {
+                for (uint32_t i = 0; i < a.k; ++i) {
+                    const double dv = md[w * 32 + i];
+                    if (dv == kInf) break;
+                    warp_insert(dv, mi[w * 32 + i], ld, lid, a.k, lane);
+                }
+            }
+            if (lane < a.k) {
+                a.out_ids[q * a.k + lane] = lid;
+                a.out_dists[q * a.k + lane] = a.squared ? ld : __dsqrt_rn(ld);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------- screened f32 rows
+// k <= 32, d % 4 == 0. The pipelined gathers of rerank_pipe_kernel feed an fp32 SCREEN instead of
+// the fp64 chains: each lane folds its chain with FFMA (t = fl(x - q), acc = fl(acc + t*t)) and
+// the four chains combine in fp32. With u = 2^-24 and n = d/4 terms per chain, the screened value
+// s satisfies |s - D| <= G*D + E for the reference's fp64 value D, where G = (n + 8) * u * 1.01 and
+// E = 1e-38 covers underflow (non-finite s: the row always passes). Every warp keeps the k smallest
+// upper bounds s*(1+G)+E it has seen; tau, their largest, bounds the final k-th distance from
+// above (k rows are known to lie below it), so a row whose lower bound s*(1-G)-E exceeds tau can
+// never enter the top-k. Rows that pass are kept (id, lower bound) in a per-warp buffer; at the
+// end the CTA merges the warps' bounds into one tau, and only buffered rows still below it get
+// the exact fp64 4-accumulator distance (rerank_kernel's chains, bit-identical to the reference).
+// About k + a few rows per query reach fp64. If a warp's buffer overflows (masses of exact ties),
+// the query is re-ranked exactly from scratch.
+constexpr uint32_t kSurvCap = 128;
+
+__device__ __forceinline__ void list_insert_val(double v, double& sl, uint32_t k, uint32_t lane) {
+    const bool before = lane < k && sl <= v;
+    const uint32_t pos = __popc(__ballot_sync(kFull, before));
+    const double up = __shfl_up_sync(kFull, sl, 1);
+    if (lane > pos) sl = up;
+    else if (lane == pos) sl = v;
+}
+
+__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+
+// Exact fp64 distances (the reference's 4 chains) of `count` rows id_at(0..count) into the warp's
+// (dist, id) list; `st` is 8 x stride floats of warp-private staging.
+template <class IdAt>
+__device__ void exact_rows(const RerankArgs& a, float* st, uint32_t stride, const double* qd, uint64_t count,
+                           IdAt id_at, double& ld, uint32_t& lid, uint32_t lane) {
+    const uint32_t r = lane >> 2, acc_i = lane & 3u;
+    for (uint64_t b = 0; b < count; b += kRows) {
+        const uint32_t nrows = static_cast<uint32_t>(min_u64(kRows, count - b));
+        const uint32_t my = lane < nrows ? id_at(b + lane) : 0u;
+        uint32_t id[kRows];
+#pragma unroll
+        for (uint32_t j = 0; j < kRows; ++j) id[j] = __shfl_sync(kFull, my, j);
+        double acc = 0.0;
+        for (uint32_t c0 = 0; c0 < a.d; c0 += kChunk) {
+            const uint32_t cl = min(kChunk, a.d - c0);
+#pragma unroll
+            for (uint32_t j = 0; j < kRows; ++j) {
+                if (j < nrows && 4 * lane < cl)
+                    *reinterpret_cast<float4*>(st + j * stride + 4 * lane) = ldg4(a.data + uint64_t(id[j]) * a.d + c0 + 4 * lane);
+            }
+            __syncwarp();
+            if (r < nrows) {
+                const float* row = st + r * stride;
+                for (uint32_t e = acc_i; e < cl; e += 4) acc = __dadd_rn(acc, sqdiff_d(row[e], qd[c0 + e]));
+            }
+            __syncwarp();
+        }
+        const double a1 = __shfl_down_sync(kFull, acc, 1);
+        const double a2 = __shfl_down_sync(kFull, acc, 2);
+        const double a3 = __shfl_down_sync(kFull, acc, 3);
+        const double dist = __dadd_rn(__dadd_rn(acc, a1), __dadd_rn(a2, a3));
+#pragma unroll
+        for (uint32_t j = 0; j < kRows; ++j) {
+            const double dj = __shfl_sync(kFull, dist, 4 * j);
+            if (j < nrows) warp_insert(dj, id[j], ld, lid, a.k, lane);
+        }
+    }
+}
+
+template <uint32_t S>
+__global__ void __launch_bounds__(kThreads, 2) rerank_screen_kernel(RerankArgs a, uint32_t stride) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    float* qf = reinterpret_cast<float*>(smem);                                                  // d
+    double* qd = reinterpret_cast<double*>(smem + ((a.d * 4 + 15) / 16) * 16);                   // d
+    float* ring = reinterpret_cast<float*>(smem + ((a.d * 4 + 15) / 16) * 16 + ((a.d * 8 + 15) / 16) * 16);
+    __shared__ uint32_t idbuf[kWarps][S][kRows];
+    __shared__ uint32_t sid[kWarps][kSurvCap];
+    __shared__ float slo[kWarps][kSurvCap];
+    __shared__ double md[kWarps * 32];
+    __shared__ uint32_t mi[kWarps * 32];
+    __shared__ double tau_cta;
+    __shared__ int ovf;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint64_t q = blockIdx.x;
+    const float* query = a.queries + q * a.d;
+    if (tid == 0) ovf = 0;
+    bool qu8 = true;
+    for (uint32_t i = tid; i < a.d; i += kThreads) {
+        const float v = query[i];
+        qd[i] = static_cast<double>(v);
+        qf[i] = v;
+        qu8 &= is_u8(v);
+    }
+    if (a.data8 && __syncthreads_and(qu8)) return;  // rerank_u8_kernel owns this query
+    __syncthreads();
+
+    const double G = (static_cast<double>(a.d / 4) + 8.0) * 5.9604644775390625e-08 * 1.01;  // (n + 8) u, u = 2^-24
+    const double E = 1e-38;
+    float* wr = ring + warp * S * kRows * stride;
+    const uint32_t r = lane >> 2, acc_i = lane & 3u;
+    const uint32_t* cands = a.cands + q * a.m;
+    const uint64_t mq = a.counts ? a.counts[q] : a.m;
+    const uint32_t nch = (a.d + kChunk - 1) / kChunk;
+    const uint64_t first = uint64_t(warp) * kRows;
+    const uint64_t groups = mq > first ? (mq - first + kRows * kWarps - 1) / (kRows * kWarps) : 0;
+    const uint64_t items = groups * nch;
+    auto gbase = [&](uint64_t g) { return first + g * kRows * kWarps; };
+    auto load_id = [&](uint64_t g) -> uint32_t {
+        const uint64_t i = gbase(g) + (lane & 7u);
+        if (g >= groups || i >= mq) return 0u;
+        return a.identity ? static_cast<uint32_t>(i) : __ldcs(cands + i);
+    };
+    uint32_t idreg = 0;
+#pragma unroll
+    for (uint32_t t = 0; t < kIdAhead; ++t) {
+        if ((lane >> 3) == t) idreg = load_id(t);
+    }
+    auto issue = [&](uint64_t i) {
+        const uint64_t g = i / nch;
+        const uint32_t c0 = static_cast<uint32_t>(i % nch) * kChunk;
+        const uint32_t cl = min(kChunk, a.d - c0);
+        const uint32_t slot = (g % kIdAhead) * 8u;
+        const uint64_t b = gbase(g);
+        const uint32_t si = static_cast<uint32_t>(i % S);
+        float* st = wr + si * kRows * stride;
+#pragma unroll
+        for (uint32_t j = 0; j < kRows; ++j) {
+            const uint32_t id = __shfl_sync(kFull, idreg, slot + j);
+            if (b + j < mq && 4 * lane < cl) cp_async16(st + j * stride + 4 * lane, a.data + uint64_t(id) * a.d + c0 + 4 * lane);
+            if (lane == j) idbuf[warp][si][j] = id;
+        }
+        if (c0 + cl == a.d) {
+            if ((lane >> 3) == g % kIdAhead) idreg = load_id(g + kIdAhead);
+        }
+    };
+    double sl = kInf;  // screen list: the k smallest upper bounds (lane i = entry i)
+    uint32_t nsurv = 0;
+    bool overflow = false;
+    float acc = 0.f;
+    for (uint32_t i = 0; i + 1 < S; ++i) {
+        if (i < items) issue(i);
+        cp_async_commit();
+    }
+    for (uint64_t i = 0; i < items; ++i) {
+        if (i + S - 1 < items) issue(i + S - 1);
+        cp_async_commit();
+        cp_async_wait<S - 1>();
+        __syncwarp();
+        const uint64_t g = i / nch;
+        const uint32_t c0 = static_cast<uint32_t>(i % nch) * kChunk;
+        const uint32_t cl = min(kChunk, a.d - c0);
+        const uint64_t b = gbase(g);
+        const uint32_t nrows = static_cast<uint32_t>(min_u64(kRows, mq - b));
+        const uint32_t si = static_cast<uint32_t>(i % S);
+        if (r < nrows) {
+            const float* row = wr + si * kRows * stride + r * stride;
+#pragma unroll 8
+            for (uint32_t e = acc_i; e < cl; e += 4) {
+                const float t = row[e] - qf[c0 + e];
+                acc = __fmaf_rn(t, t, acc);
+            }
+        }
+        if (c0 + cl == a.d) {
+            const float a1 = __shfl_down_sync(kFull, acc, 1);
+            const float a2 = __shfl_down_sync(kFull, acc, 2);
+            const float a3 = __shfl_down_sync(kFull, acc, 3);
+            const float sv = __fadd_rn(__fadd_rn(acc, a1), __fadd_rn(a2, a3));  // valid on lanes 4r
+            acc = 0.f;
+            const bool valid = acc_i == 0 && r < nrows;
+            const bool fin = isfinite(sv);
+            const double sd = static_cast<double>(sv);
+            const double lo = fin ? sd * (1.0 - G) - E : 0.0;
+            const double up = fin ? sd * (1.0 + G) + E : kInf;
+            // the k smallest upper bounds so far
+            const double tau0 = __shfl_sync(kFull, sl, a.k - 1);  // (every lane: never inside a && chain)
+            uint32_t bal = __ballot_sync(kFull, valid && up < tau0);
+            while (bal) {
+                const uint32_t src = __ffs(bal) - 1;
+                bal &= bal - 1;
+                const double v = __shfl_sync(kFull, up, src);
+                if (v < __shfl_sync(kFull, sl, a.k - 1)) list_insert_val(v, sl, a.k, lane);
+            }
+            const double tau = __shfl_sync(kFull, sl, a.k - 1);
+            const uint32_t pass = __ballot_sync(kFull, valid && lo <= tau);
+            if (pass && !overflow) {
+                const uint32_t cnt = __popc(pass);
+                if (nsurv + cnt > kSurvCap) {  // drop buffered rows the tighter tau now excludes
+                    uint32_t kept = 0;
+                    for (uint32_t t0 = 0; t0 < nsurv; t0 += 32) {
+                        const uint32_t t = t0 + lane;
+                        const bool in = t < nsurv;
+                        const uint32_t idv = in ? sid[warp][t] : 0u;
+                        const float lv = in ? slo[warp][t] : 0.f;
+                        const bool keep = in && static_cast<double>(lv) <= tau;
+                        const uint32_t kb = __ballot_sync(kFull, keep);
+                        __syncwarp();
+                        if (keep) {
+                            const uint32_t p = kept + __popc(kb & ((1u << lane) - 1u));
+                            sid[warp][p] = idv;
+                            slo[warp][p] = lv;
+                        }
+                        kept += __popc(kb);
+                        __syncwarp();
+                    }
+                    nsurv = kept;
+                }
+                if (nsurv + cnt > kSurvCap) {
+                    overflow = true;
+                } else {
+                    if ((pass >> lane) & 1u) {
+                        const uint32_t p = nsurv + __popc(pass & ((1u << lane) - 1u));
+                        sid[warp][p] = idbuf[warp][si][r];
+                        slo[warp][p] = __double2float_rd(lo);
+                    }
+                    nsurv += cnt;
+                }
+            }
+        }
+        __syncwarp();  // the slot (rows and ids) is refilled by the next iteration's issue
+    }
+    cp_async_wait<0>();
+    // one tau for the CTA: the k smallest upper bounds over every warp
+    if (overflow && lane == 0) atomicOr(&ovf, 1);
+    md[warp * 32 + lane] = sl;
+    __syncthreads();
+    if (warp == 0) {
+        for (uint32_t w = 1; w < kWarps; ++w) {
+            for (uint32_t i = 0; i < a.k; ++i) {
+                const double v = md[w * 32 + i];
+                if (!(v < __shfl_sync(kFull, sl, a.k - 1))) break;  // lists are sorted
+                list_insert_val(v, sl, a.k, lane);
+            }
+        }
+        const double t = __shfl_sync(kFull, sl, a.k - 1);
+        if (lane == 0) tau_cta = t;
+    }
+    __syncthreads();
+    const double tau = tau_cta;
+    double ld = kInf;
+    uint32_t lid = 0xffffffffu;
+    float* st = wr;  // the drained ring is staging now
+    if (ovf) {  // exact re-rank of the whole query, the warps splitting the candidates
+        const uint64_t per = (mq + kWarps - 1) / kWarps, lo = min_u64(mq, warp * per), hi = min_u64(mq, lo + per);
+        exact_rows(a, st, stride, qd, hi - lo,
+                   [&](uint64_t t) { return a.identity ? static_cast<uint32_t>(lo + t) : cands[lo + t]; }, ld, lid, lane);
+    } else {
+        uint32_t kept = 0;  // survivors: buffered rows whose lower bound is within the CTA's tau
+        for (uint32_t t0 = 0; t0 < nsurv; t0 += 32) {
+            const uint32_t t = t0 + lane;
+            const bool in = t < nsurv;
+            const uint32_t idv = in ? sid[warp][t] : 0u;
+            const bool keep = in && static_cast<double>(slo[warp][t]) <= tau;
+            const uint32_t kb = __ballot_sync(kFull, keep);
+            __syncwarp();
+            if (keep) sid[warp][kept + __popc(kb & ((1u << lane) - 1u))] = idv;
+            kept += __popc(kb);
+            __syncwarp();
+        }
+        exact_rows(a, st, stride, qd, kept, [&](uint64_t t) { return sid[warp][t]; }, ld, lid, lane);
+    }
+    __syncthreads();
+    md[warp * 32 + lane] = ld;
+    mi[warp * 32 + lane] = lid;
+    __syncthreads();
+    if (warp == 0) {
+        for (uint32_t w = 1; w < kWarps; ++w) {
+            for (uint32_t i = 0; i < a.k; ++i) {
+                const double dv = md[w * 32 + i];
+                if (dv == kInf) break;
+                warp_insert(dv, mi[w * 32 + i], ld, lid, a.k, lane);
+            }
+        }
+        if (lane < a.k) {
+            a.out_ids[q * a.k + lane] = lid;
+            a.out_dists[q * a.k + lane] = a.squared ? ld : __dsqrt_rn(ld);
         }
     }
 }
@@ -413,8 +861,34 @@ cudaError_t launch_rerank(const RerankArgs& a, uint64_t nq, cudaStream_t st) {
         }
         if (e != cudaSuccess) return e;
     }
-    if (vec) e = generic ? launch(rerank_kernel<true, true>) : launch(rerank_kernel<true, false>);
-    else e = generic ? launch(rerank_kernel<false, true>) : launch(rerank_kernel<false, false>);
+    const char* pv = std::getenv("SUCO_RERANK_PIPE");  // 0: unpipelined, 1: pipelined fp64, else screened
+    const int pmode = pv ? std::atoi(pv) : 2;
+    if (vec && !generic && pmode == 2) {
+        const uint32_t stride = 32 * ((min(a.d, kChunk) + 31) / 32) + 4;  // = 4 (mod 32): conflict-free chains
+        const size_t qbytes = ((a.d * 4 + 15) / 16) * 16 + ((a.d * 8 + 15) / 16) * 16;
+        const size_t s3 = qbytes + size_t(kWarps) * 3 * kRows * stride * 4;
+        // 3 stages when two CTAs still fit an SM (228 KB, about 14 KB static + 1 KB reserved each)
+        const bool three = s3 <= 98 * 1024;
+        const size_t ssmem = three ? s3 : qbytes + size_t(kWarps) * 2 * kRows * stride * 4;
+        auto kern = three ? rerank_screen_kernel<3> : rerank_screen_kernel<2>;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ssmem));
+        if (e != cudaSuccess) return e;
+        kern<<<static_cast<unsigned>(nq), kThreads, ssmem, st>>>(a, stride);
+        return cudaGetLastError();
+    }
+    if (vec && pmode != 0) {
+        const size_t psmem = ((a.d * 8 + 15) / 16) * 16 + ((a.d + 3) / 4) * 16 +
+                             static_cast<size_t>(kWarps) * kStages * kRows * kStride * 4;
+        auto kern = generic ? rerank_pipe_kernel<true> : rerank_pipe_kernel<false>;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(psmem));
+        if (e != cudaSuccess) return e;
+        kern<<<static_cast<unsigned>(nq), kThreads, psmem, st>>>(a);
+        e = cudaGetLastError();
+    } else if (vec) {
+        e = generic ? launch(rerank_kernel<true, true>) : launch(rerank_kernel<true, false>);
+    } else {
+        e = generic ? launch(rerank_kernel<false, true>) : launch(rerank_kernel<false, false>);
+    }
     if (e != cudaSuccess || !generic) return e;
     topk_generic_kernel<<<static_cast<unsigned>(nq), 256, 0, st>>>(a);
     return cudaGetLastError();

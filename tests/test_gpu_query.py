@@ -390,3 +390,39 @@ def test_dense_half_width_overflow_falls_back(gpu, oracle, monkeypatch, capfd):
     flagged = [int(line.split("dense select: ")[1].split(" of")[0]) for line in err.splitlines()
                if "dense select:" in line]
     assert flagged and max(flagged) > 0, err
+
+
+@pytest.mark.parametrize("dups", [40, 3000])
+def test_screened_rerank_ties(gpu, oracle, ref, dups):
+    """The fp32-screened re-rank (float rows, k <= 32) with masses of exact distance ties: `dups`
+    copies of one row next to the queries. 3000 copies overflow the per-warp buffers of rows that
+    pass the screen, so those queries are re-ranked exactly from scratch; answers stay identical
+    to the reference either way (ids by (distance, id))."""
+    full = oracle.clustered(8000 + 12, 32, 10, 99, 0, 1, 0.05, False)
+    base, qs = oracle.hold_out(full, 12, 100)
+    base = np.concatenate([base, np.repeat(base[17:18], dups, axis=0)])
+    qs = np.concatenate([qs, base[17:18] + np.float32(1e-3), base[17:18]])
+    oidx = oracle.build_index(base, 4, 10, 3, 42, 0)
+    idx = gpu.load_index(oidx.serialize(), base)
+    for a, b, k in ((1.0, 1.0, 10), (0.3, 0.2, 32), (0.05, 0.01, 1)):
+        ids, dd = idx.knn_query_batch(qs, gpu.CollisionParams(a, b, k))
+        oi, od, _ = oidx.knn_query_batch(base, qs, a, b, k)
+        assert np.array_equal(ids, oi) and np.array_equal(dd, od), (dups, a, b, k)
+    ids, dd = idx.exact_knn_batch(qs, 10)
+    for i, q in enumerate(qs):
+        wi, wd = ref.exact_knn(base, q, 10)
+        assert np.array_equal(ids[i], wi) and np.array_equal(dd[i], wd), (dups, i)
+
+
+@pytest.mark.parametrize("scale", [1e-22, 1e20])
+def test_screened_rerank_extreme_magnitudes(gpu, oracle, scale):
+    """Float rows whose squared distances underflow (1e-22) or overflow (1e20) fp32: the screen's
+    absolute slack and its 'non-finite always passes' rule keep the answers exact."""
+    full = oracle.clustered(3000 + 8, 16, 6, 7, 0, 1, 0.1, False) * np.float32(scale)
+    base, qs = oracle.hold_out(full, 8, 8)
+    oidx = oracle.build_index(base, 2, 6, 2, 42, 0)
+    idx = gpu.load_index(oidx.serialize(), base)
+    for a, b, k in ((1.0, 1.0, 10), (0.2, 0.05, 5)):
+        ids, dd = idx.knn_query_batch(qs, gpu.CollisionParams(a, b, k))
+        oi, od, _ = oidx.knn_query_batch(base, qs, a, b, k)
+        assert np.array_equal(ids, oi) and np.array_equal(dd, od), (scale, a, b, k)
