@@ -772,6 +772,152 @@ __global__ void __launch_bounds__(kThreads, 6) rerank_u8_kernel(RerankArgs a) {
     }
 }
 
+// Pipelined byte rows (dpad <= 128): one candidate per lane. A warp step is 32 rows, copied
+// global -> shared with coalesced 16-byte cp.async (8 lanes per 128-byte row) kU8Stages - 1 steps
+// ahead, their ids loaded two steps before that; then every lane folds ITS row from shared memory
+// (row stride an odd number of 16-byte units: conflict-free LDS.128) against the query words held in
+// registers — VABSDIFF4 + IDP.4A per word, no cross-lane reduction — and one ballot per step finds
+// the rows that beat the warp's k-th best.
+constexpr uint32_t kU8Stages = 3;
+
+template <uint32_t NW, bool GENERIC>
+__global__ void __launch_bounds__(kThreads, 2) rerank_u8_pipe_kernel(RerankArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint64_t q = blockIdx.x;
+    const float* query = a.queries + q * a.d;
+    bool ok = true;
+    for (uint32_t i = tid; i < a.d; i += kThreads) ok &= is_u8(query[i]);
+    if (!__syncthreads_and(ok)) return;  // the fp32/fp64 kernel owns this query
+    constexpr uint32_t nw = NW;                    // 16-byte units per row (dpad / 16 <= 8)
+    constexpr uint32_t su = NW | 1u;               // row stride in 16-byte units (odd)
+    __shared__ uint32_t qpack[32];                 // the query as bytes, packed once per CTA
+    if (tid < 32) {
+        uint32_t v = 0;
+#pragma unroll
+        for (uint32_t b = 0; b < 4; ++b) {
+            const uint32_t i = 4u * tid + b;
+            if (i < a.d) v |= static_cast<uint32_t>(query[i]) << (8u * b);
+        }
+        qpack[tid] = v;
+    }
+    __syncthreads();
+    uint4 qv[8];
+#pragma unroll
+    for (uint32_t w = 0; w < 8; ++w) qv[w] = reinterpret_cast<const uint4*>(qpack)[w];
+    uint4* ring = reinterpret_cast<uint4*>(smem) + warp * kU8Stages * 32 * su;
+    const uint32_t* cands = a.cands + q * a.m;
+    const uint64_t mq = a.counts ? a.counts[q] : a.m;
+    const uint64_t first = uint64_t(warp) * 32;
+    const uint64_t steps = mq > first ? (mq - first + 32 * kWarps - 1) / (32 * kWarps) : 0;
+    auto sbase = [&](uint64_t g) { return first + g * 32 * kWarps; };
+    auto load_id = [&](uint64_t g) -> uint32_t {
+        const uint64_t i = sbase(g) + lane;
+        if (g >= steps || i >= mq) return 0u;
+        return a.identity ? static_cast<uint32_t>(i) : __ldcs(cands + i);
+    };
+    uint32_t id0 = load_id(0), id1 = load_id(1);  // ids of the steps g with g % 2 == 0 / 1 next in line
+    auto issue = [&](uint64_t g) {
+        const uint32_t myid = (g & 1u) ? id1 : id0;
+        uint4* st = ring + static_cast<uint32_t>(g % kU8Stages) * 32 * su;
+        const uint64_t b = sbase(g);
+#pragma unroll
+        for (uint32_t t = lane; t < 32 * nw; t += 32) {
+            const uint32_t row = t / nw, col = t % nw;  // constant divisor
+            const uint32_t id = __shfl_sync(kFull, myid, row);
+            if (b + row < mq) cp_async16(st + row * su + col, a.data8 + uint64_t(id) * a.dpad + 16u * col);
+        }
+        if (g & 1u) id1 = load_id(g + 2);
+        else id0 = load_id(g + 2);
+        return myid;
+    };
+    uint32_t rowid[kU8Stages];  // each lane's row id per ring slot
+#pragma unroll
+    for (uint32_t i = 0; i < kU8Stages; ++i) rowid[i] = 0;
+    for (uint32_t i = 0; i + 1 < kU8Stages; ++i) {
+        if (i < steps) rowid[i] = issue(i);
+        cp_async_commit();
+    }
+    double ld = kInf;
+    uint32_t lid = 0xffffffffu;
+    for (uint64_t g = 0; g < steps; ++g) {
+        if (g + kU8Stages - 1 < steps) {
+            const uint32_t v = issue(g + kU8Stages - 1);
+            const uint32_t sl = static_cast<uint32_t>((g + kU8Stages - 1) % kU8Stages);
+#pragma unroll
+            for (uint32_t i = 0; i < kU8Stages; ++i) {
+                if (i == sl) rowid[i] = v;
+            }
+        }
+        cp_async_commit();
+        cp_async_wait<kU8Stages - 1>();
+        __syncwarp();
+        const uint32_t sl = static_cast<uint32_t>(g % kU8Stages);
+        uint32_t myid = rowid[0];
+#pragma unroll
+        for (uint32_t i = 1; i < kU8Stages; ++i) {
+            if (i == sl) myid = rowid[i];
+        }
+        const uint4* row = ring + sl * 32 * su + lane * su;
+        uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;  // four independent chains (integer sums: any order)
+#pragma unroll
+        for (uint32_t w = 0; w < nw; ++w) {
+            const uint4 x = row[w];
+            uint32_t t;
+            t = __vabsdiffu4(x.x, qv[w].x);
+            c0 = __dp4a(t, t, c0);
+            t = __vabsdiffu4(x.y, qv[w].y);
+            c1 = __dp4a(t, t, c1);
+            t = __vabsdiffu4(x.z, qv[w].z);
+            c2 = __dp4a(t, t, c2);
+            t = __vabsdiffu4(x.w, qv[w].w);
+            c3 = __dp4a(t, t, c3);
+        }
+        const uint32_t acc = (c0 + c1) + (c2 + c3);
+        __syncwarp();  // the slot is refilled by the next step's issue
+        const uint64_t b = sbase(g);
+        const bool valid = b + lane < mq;
+        const double dist = valid ? static_cast<double>(acc) : kInf;
+        if constexpr (GENERIC) {
+            if (valid) {
+                a.all_d[q * a.m + b + lane] = dist;
+                a.all_id[q * a.m + b + lane] = myid;
+            }
+        } else {
+            const double wd = __shfl_sync(kFull, ld, a.k - 1);
+            const uint32_t wi = __shfl_sync(kFull, lid, a.k - 1);
+            uint32_t bal = __ballot_sync(kFull, valid && dist_id_less(dist, myid, wd, wi));
+            while (bal) {  // rows that beat the k-th best (rare once the list fills)
+                const uint32_t src = __ffs(bal) - 1;
+                bal &= bal - 1;
+                warp_insert(__shfl_sync(kFull, dist, src), __shfl_sync(kFull, myid, src), ld, lid, a.k, lane);
+            }
+        }
+    }
+    cp_async_wait<0>();
+    if constexpr (!GENERIC) {
+        __syncthreads();  // every warp's copies are done: the ring becomes the merge area
+        double* md = reinterpret_cast<double*>(smem);
+        uint32_t* mi = reinterpret_cast<uint32_t*>(md + kWarps * 32);
+        md[warp * 32 + lane] = ld;
+        mi[warp * 32 + lane] = lid;
+        __syncthreads();
+        if (warp == 0) {
+            for (uint32_t w = 1; w < kWarps; ++w) {
+                for (uint32_t i = 0; i < a.k; ++i) {
+                    const double dv = md[w * 32 + i];
+                    if (dv == kInf) break;
+                    warp_insert(dv, mi[w * 32 + i], ld, lid, a.k, lane);
+                }
+            }
+            if (lane < a.k) {
+                a.out_ids[q * a.k + lane] = lid;
+                a.out_dists[q * a.k + lane] = a.squared ? ld : __dsqrt_rn(ld);
+            }
+        }
+    }
+}
+
 // k > 32: k rounds of "smallest (dist, id) strictly after the previous pick"
 // over the m scored candidates of one query; (dist, id) is a strict total
 // order so this reproduces nth_element + sort (query.cpp:185-189).
@@ -844,7 +990,24 @@ cudaError_t launch_rerank(const RerankArgs& a, uint64_t nq, cudaStream_t st) {
         return cudaGetLastError();
     };
     cudaError_t e = cudaSuccess;
-    if (a.data8) {  // u8 queries here; the fp32/fp64 kernel below takes the others
+    const char* uv = std::getenv("SUCO_RERANK_U8_PIPE");  // 0: the register kernel (A/B)
+    if (a.data8 && a.dpad <= 128 && !(uv && std::atoi(uv) == 0)) {
+        const uint32_t nwr = a.dpad / 16, su = nwr | 1u;
+        const size_t usmem = size_t(kWarps) * kU8Stages * 32 * su * 16;
+        using K = void (*)(RerankArgs);
+        const K kg[8] = {rerank_u8_pipe_kernel<1, true>, rerank_u8_pipe_kernel<2, true>, rerank_u8_pipe_kernel<3, true>,
+                         rerank_u8_pipe_kernel<4, true>, rerank_u8_pipe_kernel<5, true>, rerank_u8_pipe_kernel<6, true>,
+                         rerank_u8_pipe_kernel<7, true>, rerank_u8_pipe_kernel<8, true>};
+        const K kn[8] = {rerank_u8_pipe_kernel<1, false>, rerank_u8_pipe_kernel<2, false>, rerank_u8_pipe_kernel<3, false>,
+                         rerank_u8_pipe_kernel<4, false>, rerank_u8_pipe_kernel<5, false>, rerank_u8_pipe_kernel<6, false>,
+                         rerank_u8_pipe_kernel<7, false>, rerank_u8_pipe_kernel<8, false>};
+        const K kern = generic ? kg[nwr - 1] : kn[nwr - 1];
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(usmem));
+        if (e != cudaSuccess) return e;
+        kern<<<static_cast<unsigned>(nq), kThreads, usmem, st>>>(a);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    } else if (a.data8) {  // u8 queries here; the fp32/fp64 kernel below takes the others
         uint32_t L = 1;
         while (L < a.dpad / 16) L <<= 1;
         auto u8 = [&](auto kg, auto kn) {
