@@ -304,7 +304,7 @@ void finalize_device(suco_gpu_index* x) {
                                  x->stream));
     const char* dv = std::getenv("SUCO_DENSE");
     const bool allow = !(dv && std::atoi(dv) == 0);
-    x->dense = dense_supported(ns, x->K) && allow;
+    x->dense = (dense_supported(ns, x->K) || dense_wide_supported(ns, x->K)) && allow;
     // tables past 32-bit masks in shared memory (config 5: 8 x 10,000 cells) take the half-width
     // mode; SUCO_DENSE_HALF=0 keeps them on the cluster-counting select
     const char* hv = std::getenv("SUCO_DENSE_HALF");  // 2: force it (tests)
@@ -316,7 +316,7 @@ void finalize_device(suco_gpu_index* x) {
         x->codes.reserve(n_pad * 8);
         CUDA_TRY(launch_dense_codes_half(x->ids.p, x->cell_off.p, x->host.n, n_pad, ns, x->K, x->codes.p, x->stream));
     } else if (x->dense) {
-        x->codes.reserve(x->host.n * 8);
+        x->codes.reserve(x->host.n * (ns > 8 ? 16 : 8));
         CUDA_TRY(launch_dense_codes(x->ids.p, x->cell_off.p, x->host.n, ns, x->K, x->codes.p, x->stream));
     }
     CUDA_TRY(cudaStreamSynchronize(x->stream));
@@ -379,7 +379,8 @@ uint64_t tile_size(const suco_gpu_index* x, uint64_t nq, uint64_t m, uint32_t k)
     const uint64_t ns = x->host.layout.ns;
     const uint64_t pieces = (x->host.n + 2047) / 2048;  // dense select scratch: hist (16 B) + quota/base per piece
     const uint64_t per = ns * x->K * 4 + ns * 4 + m * 4 + (k > 32 ? m * 12 : 0) + uint64_t(x->host.d) * 4 + k * 12 +
-                         (x->dense ? pieces * (24 + kDenseBuf * 2 + 14) + pieces / 16 * 16 + 16 : 0);  // + buffers
+                         (x->dense ? pieces * (24 + kDenseBuf * 2 + 14 + (ns > 8 ? 16 : 0)) + pieces / 16 * 32 + 16
+                                   : 0);  // + buffers
     const uint64_t budget = 16ull << 30;  // per-batch scratch on a 180 GB part
     return std::max<uint64_t>(1, std::min<uint64_t>(nq, budget / per));
 }
@@ -459,7 +460,8 @@ void stage_select(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nt, uint
         da.WP = kDensePiece;
         da.P = static_cast<uint32_t>((h.n + da.WP - 1) / da.WP);
         da.half = x->dense_half ? 1u : 0u;
-        sl.dhist.reserve(nt * da.P * 8);
+        da.nc = h.layout.ns > 8 ? 2u : 1u;  // 9..16 subspaces: two code vectors, 16 histogram levels
+        sl.dhist.reserve(nt * da.P * 8 * da.nc);
         sl.dT.reserve(nt);
         sl.dquota.reserve(nt * da.P);
         sl.dbase.reserve(nt * da.P);
@@ -475,7 +477,7 @@ void stage_select(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nt, uint
             // sampled pieces (small corpora: all of them, so the prediction is exact)
             da.pstride = std::max<uint32_t>(1, std::min<uint32_t>(16, da.P / 32));
             da.Ps = (da.P + da.pstride - 1) / da.pstride;
-            sl.dsample.reserve(nt * da.Ps * 8);
+            sl.dsample.reserve(nt * da.Ps * 8 * da.nc);
             da.stage_all = std::getenv("SUCO_DENSE_STAGE") != nullptr;
             da.B = kDenseBuf;  // entries per (piece, query): ~6 sigma above cfg4's mean of 46
             sl.dcbuf.reserve(nt * da.P * da.B);

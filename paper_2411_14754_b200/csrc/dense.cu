@@ -78,18 +78,30 @@ struct Xpose {
     }
 };
 
-// Bit-sliced x >= t over 32 4-bit numbers (planes B0..B3), t in [0, 15].
-__device__ __forceinline__ uint32_t ge_mask(uint32_t B0, uint32_t B1, uint32_t B2, uint32_t B3, uint32_t t) {
+// Bit-sliced x >= t over 32 NP-bit numbers (planes B[0..NP)), t in [0, 2^NP + 1].
+template <uint32_t NP>
+__device__ __forceinline__ uint32_t ge_mask_n(const uint32_t (&B)[NP], uint32_t t) {
+    if (t >> NP) return 0u;  // above every representable score
     uint32_t gt = 0, eq = kFull;
-    const uint32_t B[4] = {B0, B1, B2, B3};
 #pragma unroll
-    for (int i = 3; i >= 0; --i) {
+    for (int i = NP - 1; i >= 0; --i) {
         const uint32_t tm = ((t >> i) & 1u) ? kFull : 0u;
         gt |= eq & B[i] & ~tm;
         eq &= ~(B[i] ^ tm);
     }
     return gt | eq;
 }
+
+// Up to 8 subspaces: one uint4 of u16 codes per point (NC = 1, 4 score planes); up to 16: two
+// (NC = 2, 5 planes).
+template <uint32_t NC>
+struct Np {
+    static constexpr uint32_t v = NC == 1 ? 4 : 5;
+};
+template <uint32_t NC>
+struct Codes {
+    uint4 v[NC];
+};
 
 // Masks of the CTA's query block (32*W queries): W words per (subspace, cell)
 // slot; bit j of word w <=> query q0 + 32w + j retrieved (s, cell).
@@ -125,66 +137,90 @@ __device__ __forceinline__ void mask_at(const uint32_t* M, uint32_t slot, uint32
 
 // Bit-planes of the scores of the 32 points [t0, t0 + 32) (lane = point t0 + lane) for the
 // block's 32*W queries: b[w][i] bit j = bit i of query (32w + j)'s score.
-__device__ __forceinline__ uint4 load_codes(const DenseArgs& a, uint64_t p, uint64_t p_hi) {
+template <uint32_t NC>
+__device__ __forceinline__ Codes<NC> load_codes(const DenseArgs& a, uint64_t p, uint64_t p_hi) {
     const uint32_t none = a.ns * a.K;
-    uint4 c = make_uint4(none | (none << 16), none | (none << 16), none | (none << 16), none | (none << 16));
-    if (p < p_hi) c = __ldg(a.codes + p);
+    Codes<NC> c;
+#pragma unroll
+    for (uint32_t i = 0; i < NC; ++i) c.v[i] = make_uint4(none | (none << 16), none | (none << 16), none | (none << 16), none | (none << 16));
+    if (p < p_hi) {
+#pragma unroll
+        for (uint32_t i = 0; i < NC; ++i) c.v[i] = __ldg(a.codes + p * NC + i);
+    }
     return c;
 }
 
-template <uint32_t W>
-__device__ __forceinline__ void planes_of(const uint32_t* M, uint4 c, uint32_t (&b)[W][4]) {
-    uint32_t m[8][W];
-    mask_at<W>(M, c.x & 0xffffu, m[0]);
-    mask_at<W>(M, c.x >> 16, m[1]);
-    mask_at<W>(M, c.y & 0xffffu, m[2]);
-    mask_at<W>(M, c.y >> 16, m[3]);
-    mask_at<W>(M, c.z & 0xffffu, m[4]);
-    mask_at<W>(M, c.z >> 16, m[5]);
-    mask_at<W>(M, c.w & 0xffffu, m[6]);
-    mask_at<W>(M, c.w >> 16, m[7]);
+template <uint32_t W, uint32_t NC>
+__device__ __forceinline__ void planes_of(const uint32_t* M, const Codes<NC>& c, uint32_t (&b)[W][Np<NC>::v]) {
+    uint32_t m[8 * NC][W];
+#pragma unroll
+    for (uint32_t i = 0; i < NC; ++i) {
+        mask_at<W>(M, c.v[i].x & 0xffffu, m[8 * i + 0]);
+        mask_at<W>(M, c.v[i].x >> 16, m[8 * i + 1]);
+        mask_at<W>(M, c.v[i].y & 0xffffu, m[8 * i + 2]);
+        mask_at<W>(M, c.v[i].y >> 16, m[8 * i + 3]);
+        mask_at<W>(M, c.v[i].z & 0xffffu, m[8 * i + 4]);
+        mask_at<W>(M, c.v[i].z >> 16, m[8 * i + 5]);
+        mask_at<W>(M, c.v[i].w & 0xffffu, m[8 * i + 6]);
+        mask_at<W>(M, c.v[i].w >> 16, m[8 * i + 7]);
+    }
 #pragma unroll
     for (uint32_t w = 0; w < W; ++w) {
-        uint32_t s1, c1, s2, c2, b0, c4, s5, c5;
-        fadd(m[0][w], m[1][w], m[2][w], s1, c1);
-        fadd(m[3][w], m[4][w], m[5][w], s2, c2);
-        const uint32_t s3 = m[6][w] ^ m[7][w], c3 = m[6][w] & m[7][w];
-        fadd(s1, s2, s3, b0, c4);  // weight 1
-        fadd(c1, c2, c3, s5, c5);  // weight 2 (+ carry weight 4)
-        const uint32_t c6 = s5 & c4;
-        b[w][0] = b0;
-        b[w][1] = s5 ^ c4;
-        b[w][2] = c5 ^ c6;
-        b[w][3] = c5 & c6;
+        if constexpr (NC == 1) {
+            uint32_t s1, c1, s2, c2, b0, c4, s5, c5;
+            fadd(m[0][w], m[1][w], m[2][w], s1, c1);
+            fadd(m[3][w], m[4][w], m[5][w], s2, c2);
+            const uint32_t s3 = m[6][w] ^ m[7][w], c3 = m[6][w] & m[7][w];
+            fadd(s1, s2, s3, b0, c4);  // weight 1
+            fadd(c1, c2, c3, s5, c5);  // weight 2 (+ carry weight 4)
+            const uint32_t c6 = s5 & c4;
+            b[w][0] = b0;
+            b[w][1] = s5 ^ c4;
+            b[w][2] = c5 ^ c6;
+            b[w][3] = c5 & c6;
+        } else {  // 16 inputs -> 5 planes (carry-save tree)
+            uint32_t s1, c1, s2, c2, s3, c3, s4, c4, s5, c5, t1, d1, t2, d2, u1, e1, u2, e2, u3, e3, v1, f1;
+            fadd(m[0][w], m[1][w], m[2][w], s1, c1);
+            fadd(m[3][w], m[4][w], m[5][w], s2, c2);
+            fadd(m[6][w], m[7][w], m[8][w], s3, c3);
+            fadd(m[9][w], m[10][w], m[11][w], s4, c4);
+            fadd(m[12][w], m[13][w], m[14][w], s5, c5);
+            fadd(s1, s2, s3, t1, d1);  // weight 1
+            fadd(s4, s5, m[15][w], t2, d2);
+            const uint32_t d3 = t1 & t2;
+            b[w][0] = t1 ^ t2;
+            fadd(c1, c2, c3, u1, e1);  // weight 2
+            fadd(c4, c5, d1, u2, e2);
+            fadd(d2, d3, u1, u3, e3);
+            const uint32_t e4 = u2 & u3;
+            b[w][1] = u2 ^ u3;
+            fadd(e1, e2, e3, v1, f1);  // weight 4
+            const uint32_t f2 = v1 & e4;
+            b[w][2] = v1 ^ e4;
+            b[w][3] = f1 ^ f2;  // weight 8
+            b[w][4] = f1 & f2;  // weight 16
+        }
     }
 }
 
-template <uint32_t W>
-__device__ __forceinline__ void score_planes(const DenseArgs& a, const uint32_t* M, uint64_t t0, uint64_t p_hi,
-                                             uint32_t (&b)[W][4], uint32_t lane) {
-    planes_of<W>(M, load_codes(a, t0 + lane, p_hi), b);
-}
-
-// The same scores with lane = query (word w: query 32w + lane): planes B[w][0..3] (bit r =
+// The same scores with lane = query (word w: query 32w + lane): planes B[w][*] (bit r =
 // point t0 + r).
-template <uint32_t W>
+template <uint32_t W, uint32_t NC>
 __device__ __forceinline__ void score_tile(const DenseArgs& a, const uint32_t* M, uint64_t t0, uint64_t p_hi,
-                                           const Xpose& xp, uint32_t (&B)[W][4], uint32_t lane) {
-    uint32_t b[W][4];
-    score_planes<W>(a, M, t0, p_hi, b, lane);
+                                           const Xpose& xp, uint32_t (&B)[W][Np<NC>::v], uint32_t lane) {
+    uint32_t b[W][Np<NC>::v];
+    planes_of<W, NC>(M, load_codes<NC>(a, t0 + lane, p_hi), b);
 #pragma unroll
     for (uint32_t w = 0; w < W; ++w) {
-        B[w][0] = xp(b[w][0]);
-        B[w][1] = xp(b[w][1]);
-        B[w][2] = xp(b[w][2]);
-        B[w][3] = xp(b[w][3]);
+#pragma unroll
+        for (uint32_t i = 0; i < Np<NC>::v; ++i) B[w][i] = xp(b[w][i]);
     }
 }
 
-// K1: per (query, piece) #points with score >= t, t = 1..8 (u16 x 8).
-template <uint32_t kDT, uint32_t W>
+// K1: per (query, piece) #points with score >= t, t = 1..8*NC (u16 each, NC uint4 per row).
+template <uint32_t kDT, uint32_t W, uint32_t NC>
 __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_hist_kernel(DenseArgs a) {
-    constexpr uint32_t kDW = kDT / 32;
+    constexpr uint32_t kDW = kDT / 32, NP = Np<NC>::v, LV = 8 * NC;
     extern __shared__ uint32_t M[];
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const uint64_t q0 = uint64_t(blockIdx.x) * 32 * W;
@@ -198,43 +234,60 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_hist_kernel(DenseArgs a
     if (lo >= a.n) return;
     const uint64_t hi = min_u64(a.n, lo + a.WP);
     const uint32_t piece = row;
-    uint32_t cnt[W][8];
+    uint32_t cnt[W][LV];
 #pragma unroll
     for (uint32_t w = 0; w < W; ++w) {
 #pragma unroll
-        for (int t = 0; t < 8; ++t) cnt[w][t] = 0;
+        for (uint32_t t = 0; t < LV; ++t) cnt[w][t] = 0;
     }
     const Xpose xp(lane);
     for (uint64_t t0 = lo; t0 < hi; t0 += 32) {
-        uint32_t B[W][4];
-        score_tile<W>(a, M, t0, hi, xp, B, lane);
+        uint32_t B[W][NP];
+        score_tile<W, NC>(a, M, t0, hi, xp, B, lane);
         // points past `hi` score 0: they never count for t >= 1
 #pragma unroll
         for (uint32_t w = 0; w < W; ++w) {
-            const uint32_t B0 = B[w][0], B1 = B[w][1], B2 = B[w][2], B3 = B[w][3];
-            const uint32_t g8 = B3, g4 = B3 | B2, g2 = g4 | B1, g1 = g2 | B0;
-            const uint32_t g6 = B3 | (B2 & B1), g5 = B3 | (B2 & (B1 | B0)), g7 = B3 | (B2 & B1 & B0);
-            const uint32_t g3 = g4 | (B1 & B0);
-            cnt[w][0] += __popc(g1);
-            cnt[w][1] += __popc(g2);
-            cnt[w][2] += __popc(g3);
-            cnt[w][3] += __popc(g4);
-            cnt[w][4] += __popc(g5);
-            cnt[w][5] += __popc(g6);
-            cnt[w][6] += __popc(g7);
-            cnt[w][7] += __popc(g8);
+            if constexpr (NC == 1) {
+                const uint32_t B0 = B[w][0], B1 = B[w][1], B2 = B[w][2], B3 = B[w][3];
+                const uint32_t g8 = B3, g4 = B3 | B2, g2 = g4 | B1, g1 = g2 | B0;
+                const uint32_t g6 = B3 | (B2 & B1), g5 = B3 | (B2 & (B1 | B0)), g7 = B3 | (B2 & B1 & B0);
+                const uint32_t g3 = g4 | (B1 & B0);
+                cnt[w][0] += __popc(g1);
+                cnt[w][1] += __popc(g2);
+                cnt[w][2] += __popc(g3);
+                cnt[w][3] += __popc(g4);
+                cnt[w][4] += __popc(g5);
+                cnt[w][5] += __popc(g6);
+                cnt[w][6] += __popc(g7);
+                cnt[w][7] += __popc(g8);
+            } else {  // #(score == v), v = 1..16; suffix sums at the end
+#pragma unroll
+                for (uint32_t v = 1; v <= LV; ++v) {
+                    uint32_t e = kFull;
+#pragma unroll
+                    for (uint32_t i = 0; i < NP; ++i) e &= ((v >> i) & 1u) ? B[w][i] : ~B[w][i];
+                    cnt[w][v - 1] += __popc(e);
+                }
+            }
         }
     }
 #pragma unroll
     for (uint32_t w = 0; w < W; ++w) {
+        if constexpr (NC != 1) {
+#pragma unroll
+            for (int t = LV - 2; t >= 0; --t) cnt[w][t] += cnt[w][t + 1];
+        }
         if (32 * w + lane < nqb) {
-            uint4 v;
-            v.x = cnt[w][0] | (cnt[w][1] << 16);
-            v.y = cnt[w][2] | (cnt[w][3] << 16);
-            v.z = cnt[w][4] | (cnt[w][5] << 16);
-            v.w = cnt[w][6] | (cnt[w][7] << 16);
             const uint64_t q = a.qmap ? a.qmap[q0 + 32 * w + lane] : q0 + 32 * w + lane;
-            reinterpret_cast<uint4*>(a.hist)[q * a.P + piece] = v;
+#pragma unroll
+            for (uint32_t i = 0; i < NC; ++i) {
+                uint4 v;
+                v.x = cnt[w][8 * i + 0] | (cnt[w][8 * i + 1] << 16);
+                v.y = cnt[w][8 * i + 2] | (cnt[w][8 * i + 3] << 16);
+                v.z = cnt[w][8 * i + 4] | (cnt[w][8 * i + 5] << 16);
+                v.w = cnt[w][8 * i + 6] | (cnt[w][8 * i + 7] << 16);
+                reinterpret_cast<uint4*>(a.hist)[(q * a.P + piece) * NC + i] = v;
+            }
         }
     }
 }
@@ -244,33 +297,44 @@ __device__ __forceinline__ uint32_t level(const uint4& v, uint32_t t) {  // #sco
     return (t & 1u) ? (w & 0xffffu) : (w >> 16);
 }
 
+// #score >= t, t in 1..8*nc, from a histogram row of nc uint4
+__device__ __forceinline__ uint32_t level_n(const uint4* row, uint32_t t) {
+    return level(row[(t - 1) >> 3], ((t - 1) & 7u) + 1);
+}
+
+__device__ __forceinline__ uint32_t nc_of(const DenseArgs& a) { return a.nc ? a.nc : 1u; }
+
 // K2: warp per query — T, need, per-piece tie quota (id order) and output offset.
 __global__ void __launch_bounds__(256) dense_plan_kernel(DenseArgs a) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t qi = uint64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
     if (qi >= (a.qmap ? *a.nmap : a.nq)) return;
     const uint64_t q = a.qmap ? a.qmap[qi] : qi;
-    const uint4* h = reinterpret_cast<const uint4*>(a.hist) + q * a.P;
-    uint32_t tot[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (uint32_t p = lane; p < a.P; p += 32) {
-        const uint4 v = h[p];
+    const uint32_t nc = nc_of(a), LV = 8 * nc;
+    const uint4* h = reinterpret_cast<const uint4*>(a.hist) + q * a.P * nc;
+    uint32_t tot[16];
 #pragma unroll
-        for (uint32_t t = 1; t <= 8; ++t) tot[t - 1] += level(v, t);
+    for (int t = 0; t < 16; ++t) tot[t] = 0;
+    for (uint32_t p = lane; p < a.P; p += 32) {
+#pragma unroll
+        for (uint32_t t = 1; t <= 16; ++t) {
+            if (t <= LV) tot[t - 1] += level_n(h + p * nc, t);
+        }
     }
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
+    for (int t = 0; t < 16; ++t) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) tot[t] += __shfl_xor_sync(kFull, tot[t], o);
     }
     uint32_t T = 0;
 #pragma unroll
-    for (int t = 8; t >= 1; --t) {
-        if (T == 0 && static_cast<uint32_t>(t) <= a.ns && tot[t - 1] >= a.m) T = t;
+    for (int t = 16; t >= 1; --t) {
+        if (T == 0 && static_cast<uint32_t>(t) <= min(a.ns, LV) && tot[t - 1] >= a.m) T = t;
     }
     uint32_t gtT = 0;
 #pragma unroll
-    for (int t = 1; t <= 8; ++t) {
-        if (static_cast<uint32_t>(t) == T + 1) gtT = tot[t - 1];
+    for (int t = 1; t <= 16; ++t) {
+        if (static_cast<uint32_t>(t) == T + 1 && static_cast<uint32_t>(t) <= LV) gtT = tot[t - 1];
     }
     const uint64_t need = a.m - gtT;
     uint64_t ties_run = 0, out_run = 0;
@@ -278,10 +342,9 @@ __global__ void __launch_bounds__(256) dense_plan_kernel(DenseArgs a) {
         const uint32_t p = p0 + lane;
         uint32_t ties = 0, gt = 0;
         if (p < a.P) {
-            const uint4 v = h[p];
             const uint32_t len = static_cast<uint32_t>(min_u64(a.WP, a.n - uint64_t(p) * a.WP));
-            const uint32_t geT = T ? level(v, T) : len;
-            gt = T + 1 <= 8 ? level(v, T + 1) : 0u;
+            const uint32_t geT = T ? level_n(h + p * nc, T) : len;
+            gt = T + 1 <= LV ? level_n(h + p * nc, T + 1) : 0u;
             ties = geT - gt;
         }
         uint32_t tx = ties;
@@ -375,9 +438,9 @@ __global__ void __launch_bounds__(256) dense_plan_fused_kernel(DenseArgs a) {
 }
 
 // K3: re-score each piece; lane = query emits score > T and the first quota ties (id order).
-template <uint32_t kDT, uint32_t W>
+template <uint32_t kDT, uint32_t W, uint32_t NC>
 __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_emit_kernel(DenseArgs a) {
-    constexpr uint32_t kDW = kDT / 32;
+    constexpr uint32_t kDW = kDT / 32, NP = Np<NC>::v;
     extern __shared__ uint32_t M[];
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const uint64_t q0 = uint64_t(blockIdx.x) * 32 * W;
@@ -404,14 +467,14 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_emit_kernel(DenseArgs a
     }
     const Xpose xp(lane);
     for (uint64_t t0 = lo; t0 < hi; t0 += 32) {
-        uint32_t B[W][4];
-        score_tile<W>(a, M, t0, hi, xp, B, lane);
+        uint32_t B[W][NP];
+        score_tile<W, NC>(a, M, t0, hi, xp, B, lane);
         const uint32_t vmask = hi - t0 >= 32 ? kFull : ((1u << (hi - t0)) - 1u);
 #pragma unroll
         for (uint32_t w = 0; w < W; ++w) {
             if (!mine[w]) continue;  // lanes past the block's last query only feed the transposes
-            const uint32_t geT = ge_mask(B[w][0], B[w][1], B[w][2], B[w][3], T[w]) & vmask;
-            const uint32_t gt = ge_mask(B[w][0], B[w][1], B[w][2], B[w][3], T[w] + 1) & vmask;
+            const uint32_t geT = ge_mask_n<NP>(B[w], T[w]) & vmask;
+            const uint32_t gt = ge_mask_n<NP>(B[w], T[w] + 1) & vmask;
             const uint32_t eq = geT & ~gt;
             uint32_t take = gt;
             if (eq && tseen[w] < quota[w]) {
@@ -435,15 +498,19 @@ __global__ void __launch_bounds__(256) dense_bound_kernel(DenseArgs a) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t q = uint64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
     if (q >= a.nq) return;
-    const uint4* h = reinterpret_cast<const uint4*>(a.hsample) + q * a.Ps;
-    uint32_t tot[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (uint32_t p = lane; p < a.Ps; p += 32) {
-        const uint4 v = h[p];
+    const uint32_t nc = nc_of(a), LV = 8 * nc;
+    const uint4* h = reinterpret_cast<const uint4*>(a.hsample) + q * a.Ps * nc;
+    uint32_t tot[16];
 #pragma unroll
-        for (uint32_t t = 1; t <= 8; ++t) tot[t - 1] += level(v, t);
+    for (int t = 0; t < 16; ++t) tot[t] = 0;
+    for (uint32_t p = lane; p < a.Ps; p += 32) {
+#pragma unroll
+        for (uint32_t t = 1; t <= 16; ++t) {
+            if (t <= LV) tot[t - 1] += level_n(h + p * nc, t);
+        }
     }
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
+    for (int t = 0; t < 16; ++t) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) tot[t] += __shfl_xor_sync(kFull, tot[t], o);
     }
@@ -455,8 +522,8 @@ __global__ void __launch_bounds__(256) dense_bound_kernel(DenseArgs a) {
     uint32_t L = 0;
     uint32_t atL = 0;
 #pragma unroll
-    for (int t = 8; t >= 1; --t) {
-        if (L == 0 && static_cast<uint32_t>(t) <= a.ns && sampled &&
+    for (int t = 16; t >= 1; --t) {
+        if (L == 0 && static_cast<uint32_t>(t) <= min(a.ns, LV) && sampled &&
             static_cast<double>(tot[t - 1]) * static_cast<double>(a.n) / static_cast<double>(sampled) >=
                 static_cast<double>(a.m)) {
             L = t;
@@ -473,11 +540,11 @@ __global__ void __launch_bounds__(256) dense_bound_kernel(DenseArgs a) {
 // The fused pass's walk over a warp's pieces (below). STAGE: entries go through a 64-bit register
 // (four per 8-byte store) — for dense supersets, where 2-byte stores multiply DRAM traffic; sparse
 // ones store each entry directly (fewer instructions per tile).
-template <uint32_t kDW, uint32_t W, bool STAGE>
+template <uint32_t kDW, uint32_t W, bool STAGE, uint32_t NC>
 __device__ __forceinline__ void fused_pieces(const DenseArgs& a, const uint32_t* M, uint64_t q0, uint32_t nqb,
-                                             const uint32_t (&T0)[W], const uint32_t (&T1)[W],
-                                             const uint32_t (&T2)[W], const uint32_t (&T3)[W],
-                                             const uint32_t (&live)[W], uint32_t lane, uint32_t warp) {
+                                             const uint32_t (&TL)[W][Np<NC>::v], const uint32_t (&live)[W],
+                                             uint32_t lane, uint32_t warp) {
+    constexpr uint32_t NP = Np<NC>::v;
     const Xpose xp(lane);
     // a warp walks ppw consecutive pieces: the masks are built once per CTA for them all
     for (uint32_t k = 0; k < a.ppw; ++k) {
@@ -496,23 +563,22 @@ __device__ __forceinline__ void fused_pieces(const DenseArgs& a, const uint32_t*
             const uint64_t q = 32 * w + lane < nqb ? q0 + 32 * w + lane : q0;  // idle lanes append nothing
             buf[w] = a.cbuf + (q * a.P + piece) * a.B;
         }
-        uint4 code = load_codes(a, lo + lane, hi);
+        Codes<NC> code = load_codes<NC>(a, lo + lane, hi);
         for (uint64_t t0 = lo; t0 < hi; t0 += 32) {
-            const uint4 next = load_codes(a, t0 + 32 + lane, hi);  // one tile ahead
-            uint32_t b[W][4];
-            planes_of<W>(M, code, b);
+            const Codes<NC> next = load_codes<NC>(a, t0 + 32 + lane, hi);  // one tile ahead
+            uint32_t b[W][NP];
+            planes_of<W, NC>(M, code, b);
             code = next;
             const uint32_t tb = static_cast<uint32_t>(t0 - lo);
 #pragma unroll
             for (uint32_t w = 0; w < W; ++w) {
                 // most significant plane first; points past the piece end score 0 < L
-                uint32_t gt = b[w][3] & ~T3[w], eq = ~(b[w][3] ^ T3[w]);
-                gt |= eq & b[w][2] & ~T2[w];
-                eq &= ~(b[w][2] ^ T2[w]);
-                gt |= eq & b[w][1] & ~T1[w];
-                eq &= ~(b[w][1] ^ T1[w]);
-                gt |= eq & b[w][0] & ~T0[w];
-                eq &= ~(b[w][0] ^ T0[w]);
+                uint32_t gt = b[w][NP - 1] & ~TL[w][NP - 1], eq = ~(b[w][NP - 1] ^ TL[w][NP - 1]);
+#pragma unroll
+                for (int i = NP - 2; i >= 0; --i) {
+                    gt |= eq & b[w][i] & ~TL[w][i];
+                    eq &= ~(b[w][i] ^ TL[w][i]);
+                }
                 const uint32_t ge0 = xp((gt | eq) & live[w]);  // lane = query, bit r = point t0 + r
                 const uint32_t g1 = xp(gt & live[w]);
                 cnt[w] += __popc(ge0) | (__popc(g1) << 16);
@@ -553,9 +619,9 @@ __device__ __forceinline__ void fused_pieces(const DenseArgs& a, const uint32_t*
 // score >= L[q] appended in id order to the pair's candidate buffer: the in-piece offset, bit 15
 // set when the score is > L. A buffer holds B entries; a contributing piece that found more flags
 // its query for the exact fallback.
-template <uint32_t kDT, uint32_t W>
+template <uint32_t kDT, uint32_t W, uint32_t NC>
 __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs a) {
-    constexpr uint32_t kDW = kDT / 32;
+    constexpr uint32_t kDW = kDT / 32, NP = Np<NC>::v;
     extern __shared__ uint32_t M[];
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const uint64_t q0 = uint64_t(blockIdx.x) * 32 * W;
@@ -568,18 +634,16 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs 
     // comparison per tile, BEFORE the transpose (lane = point, bit = query), gives score > L and
     // score == L for all 32*W queries at once; only the two results are transposed (10 shuffles,
     // not 20 for the four planes). Counts per lane = query: #(score >= L) | #(score >= L+1) << 16.
-    uint32_t T0[W], T1[W], T2[W], T3[W], live[W];
+    uint32_t TL[W][NP], live[W];
 #pragma unroll
     for (uint32_t w = 0; w < W; ++w) {
         const uint32_t L = 32 * w + lane < nqb ? a.L[q0 + 32 * w + lane] & 0xffu : 0u;  // 0: falls back
-        T0[w] = __ballot_sync(kFull, L & 1u);
-        T1[w] = __ballot_sync(kFull, L & 2u);
-        T2[w] = __ballot_sync(kFull, L & 4u);
-        T3[w] = __ballot_sync(kFull, L & 8u);
+#pragma unroll
+        for (uint32_t i = 0; i < NP; ++i) TL[w][i] = __ballot_sync(kFull, (L >> i) & 1u);
         live[w] = __ballot_sync(kFull, L != 0);
     }
-    if (stage) fused_pieces<kDW, W, true>(a, M, q0, nqb, T0, T1, T2, T3, live, lane, warp);
-    else fused_pieces<kDW, W, false>(a, M, q0, nqb, T0, T1, T2, T3, live, lane, warp);
+    if (stage) fused_pieces<kDW, W, true, NC>(a, M, q0, nqb, TL, live, lane, warp);
+    else fused_pieces<kDW, W, false, NC>(a, M, q0, nqb, TL, live, lane, warp);
 }
 
 // K4: thread per (query, piece), T == L: the piece's buffer holds its score >= T points in id
@@ -627,14 +691,14 @@ __global__ void dense_codes_fill_kernel(uint16_t* codes, uint64_t count, uint16_
 }
 
 __global__ void dense_codes_kernel(const uint32_t* ids, const uint32_t* cell_off, uint64_t n, uint32_t ns, uint32_t K,
-                                   uint16_t* codes) {
+                                   uint16_t* codes, uint32_t cw) {  // cw = codes per point (8 or 16)
     const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
     if (t >= uint64_t(ns) * K) return;
     const uint32_t s = static_cast<uint32_t>(t / K), cell = static_cast<uint32_t>(t % K);
     const uint32_t* off = cell_off + uint64_t(s) * (K + 1);
     const uint32_t* sid = ids + uint64_t(s) * n;
     const uint16_t code = static_cast<uint16_t>(s * K + cell);
-    for (uint32_t i = off[cell]; i < off[cell + 1]; ++i) codes[uint64_t(sid[i]) * 8 + s] = code;
+    for (uint32_t i = off[cell]; i < off[cell + 1]; ++i) codes[uint64_t(sid[i]) * cw + s] = code;
 }
 
 // ------------------------------------------------------------ half-width mode
@@ -780,8 +844,9 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_emit_h_kernel(DenseArgs
         const uint32_t B0 = xp(b[0]), B1 = xp(b[1]), B2 = xp(b[2]), B3 = xp(b[3]);
         const uint64_t pb = t0 + 32 * half;  // this lane's first point
         const uint32_t vmask = !mine || pb >= hi ? 0u : hi - pb >= 32 ? kFull : ((1u << (hi - pb)) - 1u);
-        const uint32_t geT = ge_mask(B0, B1, B2, B3, T) & vmask;
-        const uint32_t gt = ge_mask(B0, B1, B2, B3, T + 1) & vmask;
+        const uint32_t Bh[4] = {B0, B1, B2, B3};
+        const uint32_t geT = ge_mask_n<4>(Bh, T) & vmask;
+        const uint32_t gt = ge_mask_n<4>(Bh, T + 1) & vmask;
         const uint32_t eq = geT & ~gt;
         const uint32_t ec = __popc(eq), eo = __shfl_xor_sync(kFull, ec, 16);
         const uint32_t seen = tseen + (half ? eo : 0u);  // ties before this lane's points
@@ -934,15 +999,20 @@ bool dense_supported(uint32_t ns, uint32_t K) {
     return ns >= 1 && ns <= 8 && uint64_t(ns) * K + 1 <= 65535 && (uint64_t(ns) * K + 1) * 4 <= 200 * 1024;
 }
 
+bool dense_wide_supported(uint32_t ns, uint32_t K) {
+    return ns >= 9 && ns <= 16 && uint64_t(ns) * K + 1 <= 65535 && (uint64_t(ns) * K + 1) * 4 <= 200 * 1024;
+}
+
 size_t dense_smem(uint32_t ns, uint32_t K) { return (size_t(ns) * K + 1) * 4; }
 
 cudaError_t launch_dense_codes(const uint32_t* ids, const uint32_t* cell_off, uint64_t n, uint32_t ns, uint32_t K,
                                uint16_t* codes, cudaStream_t st) {
-    const uint64_t count = n * 8;
+    const uint32_t cw = ns > 8 ? 16 : 8;
+    const uint64_t count = n * cw;
     const unsigned fb = static_cast<unsigned>(min_u64((count + 255) / 256, 148ull * 16));
     dense_codes_fill_kernel<<<fb ? fb : 1, 256, 0, st>>>(codes, count, static_cast<uint16_t>(ns * K));
     const uint64_t total = uint64_t(ns) * K;
-    dense_codes_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(ids, cell_off, n, ns, K, codes);
+    dense_codes_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(ids, cell_off, n, ns, K, codes, cw);
     return cudaGetLastError();
 }
 
@@ -957,14 +1027,14 @@ static Shape dense_shape(const DenseArgs& a) {
     const char* wv = std::getenv("SUCO_DENSE_WORDS");
     // the single-pass pipeline measured faster with 32-query blocks (3.75 vs 3.89 ms at cfg2),
     // the two-pass one with 64-query blocks (5.04 vs 5.52 ms)
-    const bool allow2 = wv ? std::atoi(wv) == 2 : a.cbuf == nullptr;
+    const bool allow2 = (wv ? std::atoi(wv) == 2 : a.cbuf == nullptr) && a.nc != 2;  // 16 subspaces: one word
     if (allow2 && 2 * smem1 <= 200 * 1024) return {1024, 2, 2 * smem1};
     return {smem1 <= 110 * 1024 ? 512u : 1024u, 1, smem1};
 }
 
-template <uint32_t kDT, uint32_t W, bool EMIT>
+template <uint32_t kDT, uint32_t W, bool EMIT, uint32_t NC = 1>
 static cudaError_t launch_scan(const DenseArgs& a, size_t smem, cudaStream_t st) {
-    auto kern = EMIT ? dense_emit_kernel<kDT, W> : dense_hist_kernel<kDT, W>;
+    auto kern = EMIT ? dense_emit_kernel<kDT, W, NC> : dense_hist_kernel<kDT, W, NC>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     constexpr uint32_t kDW = kDT / 32;
@@ -977,6 +1047,10 @@ template <bool EMIT>
 static cudaError_t launch_scan_any(const DenseArgs& a, cudaStream_t st) {
     if (a.nq == 0) return cudaSuccess;
     const Shape sh = dense_shape(a);
+    if (a.nc == 2) {
+        return sh.threads == 512 ? launch_scan<512, 1, EMIT, 2>(a, sh.smem, st)
+                                 : launch_scan<1024, 1, EMIT, 2>(a, sh.smem, st);
+    }
     if (sh.words == 2) return launch_scan<1024, 2, EMIT>(a, sh.smem, st);
     return sh.threads == 512 ? launch_scan<512, 1, EMIT>(a, sh.smem, st) : launch_scan<1024, 1, EMIT>(a, sh.smem, st);
 }
@@ -1006,9 +1080,9 @@ cudaError_t launch_dense_hist_rows(const DenseArgs& a, uint32_t* out, cudaStream
     return cudaGetLastError();
 }
 
-template <uint32_t kDT, uint32_t W>
+template <uint32_t kDT, uint32_t W, uint32_t NC = 1>
 static cudaError_t launch_fused_t(const DenseArgs& a, size_t smem, cudaStream_t st) {
-    cudaError_t e = cudaFuncSetAttribute(dense_fused_kernel<kDT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaError_t e = cudaFuncSetAttribute(dense_fused_kernel<kDT, W, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     constexpr uint32_t kDW = kDT / 32;
     // pieces per warp: kFusedPPW amortises the mask build, unless that leaves fewer than about
@@ -1021,7 +1095,7 @@ static cudaError_t launch_fused_t(const DenseArgs& a, size_t smem, cudaStream_t 
     if (qblocks * ((a.P + kDW * b.ppw - 1) / (kDW * b.ppw)) < 4ull * sms) b.ppw = 1;
     const uint32_t per_cta = kDW * b.ppw;
     const dim3 grid(static_cast<unsigned>(qblocks), (a.P + per_cta - 1) / per_cta);
-    dense_fused_kernel<kDT, W><<<grid, kDT, smem, st>>>(b);
+    dense_fused_kernel<kDT, W, NC><<<grid, kDT, smem, st>>>(b);
     return cudaGetLastError();
 }
 
@@ -1041,7 +1115,8 @@ cudaError_t launch_dense_select_fused(const DenseArgs& args, cudaStream_t st) {
         e = launch_h<2>(a, st);
     } else {
         const Shape sh = dense_shape(a);
-        if (sh.words == 2) e = launch_fused_t<1024, 2>(a, sh.smem, st);
+        if (a.nc == 2) e = sh.threads == 512 ? launch_fused_t<512, 1, 2>(a, sh.smem, st) : launch_fused_t<1024, 1, 2>(a, sh.smem, st);
+        else if (sh.words == 2) e = launch_fused_t<1024, 2>(a, sh.smem, st);
         else e = sh.threads == 512 ? launch_fused_t<512, 1>(a, sh.smem, st) : launch_fused_t<1024, 1>(a, sh.smem, st);
     }
     if (e != cudaSuccess) return e;

@@ -110,8 +110,11 @@ struct DenseArgs {
     uint32_t ppw;                 // fused pass: pieces per warp (set by the launcher)
     uint32_t stage_all;           // fused pass: stage every block's stores (tests; else by density)
     uint32_t half;                // 16-query blocks, u16 masks, codes = cell + 1 per subspace (large N_s*K)
+    uint32_t nc;                  // uint4 code vectors per point: 1 (N_s <= 8, default) or 2 (N_s <= 16)
 };
 bool dense_supported(uint32_t ns, uint32_t K);
+// 9..16 subspaces: two code vectors per point, 5 score planes, 16 histogram levels (config 3)
+bool dense_wide_supported(uint32_t ns, uint32_t K);
 size_t dense_smem(uint32_t ns, uint32_t K);
 // Half-width mode for tables too large for 32-bit masks (config 5: N_s*K = 80,000 cells): 16-query
 // blocks, one u16 mask per (subspace, cell), two points per lane; codes hold cell + 1 per subspace

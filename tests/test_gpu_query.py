@@ -426,3 +426,23 @@ def test_screened_rerank_extreme_magnitudes(gpu, oracle, scale):
         ids, dd = idx.knn_query_batch(qs, gpu.CollisionParams(a, b, k))
         oi, od, _ = oidx.knn_query_batch(base, qs, a, b, k)
         assert np.array_equal(ids, oi) and np.array_equal(dd, od), (scale, a, b, k)
+
+
+@pytest.mark.parametrize("fused", ["1", "0"])
+@pytest.mark.parametrize("ns,kh", [(16, 12), (12, 20), (9, 7)])
+def test_dense_select_16_subspaces(gpu, oracle, ns, kh, fused, monkeypatch):
+    """9..16 subspaces (config 3 has 16): two code vectors per point, five score planes and 16
+    histogram levels in the dense select, single-pass and two-pass; partial last query block."""
+    monkeypatch.setenv("SUCO_DENSE_FUSED", fused)
+    d = 4 * ns
+    full = oracle.clustered(50000 + 45, d, 30, 3030 + ns, 0, 100, 9, False)
+    base, qs = oracle.hold_out(full, 45, 3031)
+    oidx = oracle.build_index(base, ns, kh, 3, 42, 0)
+    idx = gpu.load_index(oidx.serialize(), base)
+    for a, b, k in ((0.05, 0.01, 10), (0.3, 0.002, 7), (0.01, 0.2, 20)):
+        ids, dd = idx.knn_query_batch(qs, gpu.CollisionParams(a, b, k))
+        oi, od, _ = oidx.knn_query_batch(base, qs, a, b, k)
+        assert np.array_equal(ids, oi) and np.array_equal(dd, od), (ns, a, b, k)
+    s1, c1, _, _ = idx.query_intermediates(qs[4], gpu.CollisionParams(0.05, 0.01, 10))
+    s2, c2, _, _ = oidx.query_intermediates(base, qs[4], 0.05, 0.01, 10)
+    assert np.array_equal(c1, c2)
