@@ -479,7 +479,12 @@ void stage_select(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nt, uint
             da.Ps = (da.P + da.pstride - 1) / da.pstride;
             sl.dsample.reserve(nt * da.Ps * 8 * da.nc);
             da.stage_all = std::getenv("SUCO_DENSE_STAGE") != nullptr;
-            da.B = kDenseBuf;  // entries per (piece, query): ~6 sigma above cfg4's mean of 46
+            // entries per (piece, query): at least kDenseBuf (~6 sigma above cfg4's mean of 46); small
+            // batches x corpora (cfg3: 1K queries x 489 pieces) get up to 2048 (one whole piece)
+            // within 1 GB of buffers, so dense supersets do not overflow into the two-pass fallback
+            const uint64_t fit = (1ull << 30) / (2ull * nt * da.P) / 8 * 8;
+            da.B = static_cast<uint32_t>(std::min<uint64_t>(kDensePiece, std::max<uint64_t>(kDenseBuf, fit)));
+            if (const char* bv = std::getenv("SUCO_DENSE_BUF")) da.B = std::max(8, std::atoi(bv) / 8 * 8);  // tests
             sl.dcbuf.reserve(nt * da.P * da.B);
             sl.dccnt.reserve(nt * da.P);
             da.cbuf = sl.dcbuf.p;
@@ -487,7 +492,9 @@ void stage_select(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nt, uint
             sl.dL.reserve(nt);
             sl.dh2.reserve(nt * da.P);
             da.h2 = sl.dh2.p;
-            sl.dflag.reserve(2 * nt + 1);  // flags, flagged list, its count
+            sl.dflag.reserve(3 * nt + 1);  // flags, flagged list, its count, tie cuts
+            da.pcut = sl.dflag.p + 2 * nt + 1;
+            da.no_cut = std::getenv("SUCO_DENSE_NOCUT") != nullptr;
             da.hsample = sl.dsample.p;
             da.qmap = sl.dflag.p + nt;
             da.nmap = sl.dflag.p + 2 * nt;

@@ -426,6 +426,7 @@ __global__ void __launch_bounds__(256) dense_plan_fused_kernel(DenseArgs a) {
             a.quota[q * a.P + p] = quota;
             a.base[q * a.P + p] = static_cast<uint32_t>(out_run + ox - take);
             if (take && a.ccnt[q * a.P + p] > a.B) ok = false;  // a contributing buffer overflowed
+            if (quota && a.pcut && p >= a.pcut[q]) ok = false;   // ties needed past the tie cut
         }
         ties_run += tsum;
         out_run += osum;
@@ -534,7 +535,29 @@ __global__ void __launch_bounds__(256) dense_bound_kernel(DenseArgs a) {
     // 0.25 B per (point, query) even when every tile has one; a second scoring pass costs more.
     // dense supersets (> 1% of the points at L) make the fused pass stage its stores
     const bool dense = L && (a.stage_all || static_cast<double>(atL) > 0.01 * static_cast<double>(sampled));
-    if (lane == 0) a.L[q] = L | (dense ? kDenseStage : 0u);
+    // Tie cut: the quota takes the first `need` score == L points in id order, so the fused pass
+    // stores tie entries only in the pieces the quota is expected to reach (x1.25 + 8 pieces of
+    // margin); later pieces keep just their score > L entries. A quota that reaches past the cut
+    // flags the query for the exact fallback.
+    uint32_t cut = a.P;
+    if (L && sampled && a.pcut && !a.no_cut) {
+        uint32_t above = 0;  // sampled #(score >= L + 1)
+#pragma unroll
+        for (int t = 1; t <= 16; ++t) {
+            if (static_cast<uint32_t>(t) == L + 1 && static_cast<uint32_t>(t) <= LV) above = tot[t - 1];
+        }
+        const double scale = static_cast<double>(a.n) / static_cast<double>(sampled);
+        const double ties = (static_cast<double>(atL) - static_cast<double>(above)) * scale;
+        const double need = static_cast<double>(a.m) - static_cast<double>(above) * scale;
+        if (ties > 0.0 && need < ties) {
+            const double c = static_cast<double>(a.P) * (need > 0.0 ? need / ties : 0.0) * 1.25 + 8.0;
+            cut = c < static_cast<double>(a.P) ? static_cast<uint32_t>(c) : a.P;
+        }
+    }
+    if (lane == 0) {
+        a.L[q] = L | (dense ? kDenseStage : 0u);
+        if (a.pcut) a.pcut[q] = cut;
+    }
 }
 
 // The fused pass's walk over a warp's pieces (below). STAGE: entries go through a 64-bit register
@@ -543,7 +566,7 @@ __global__ void __launch_bounds__(256) dense_bound_kernel(DenseArgs a) {
 template <uint32_t kDW, uint32_t W, bool STAGE, uint32_t NC>
 __device__ __forceinline__ void fused_pieces(const DenseArgs& a, const uint32_t* M, uint64_t q0, uint32_t nqb,
                                              const uint32_t (&TL)[W][Np<NC>::v], const uint32_t (&live)[W],
-                                             uint32_t lane, uint32_t warp) {
+                                             const uint32_t (&cut)[W], uint32_t lane, uint32_t warp) {
     constexpr uint32_t NP = Np<NC>::v;
     const Xpose xp(lane);
     // a warp walks ppw consecutive pieces: the masks are built once per CTA for them all
@@ -582,7 +605,7 @@ __device__ __forceinline__ void fused_pieces(const DenseArgs& a, const uint32_t*
                 const uint32_t ge0 = xp((gt | eq) & live[w]);  // lane = query, bit r = point t0 + r
                 const uint32_t g1 = xp(gt & live[w]);
                 cnt[w] += __popc(ge0) | (__popc(g1) << 16);
-                uint32_t bits = ge0;
+                uint32_t bits = piece < cut[w] ? ge0 : g1;  // past the tie cut: score > L only
                 while (bits) {  // id order
                     const uint32_t r = __ffs(bits) - 1;
                     bits &= bits - 1;
@@ -634,16 +657,17 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs 
     // comparison per tile, BEFORE the transpose (lane = point, bit = query), gives score > L and
     // score == L for all 32*W queries at once; only the two results are transposed (10 shuffles,
     // not 20 for the four planes). Counts per lane = query: #(score >= L) | #(score >= L+1) << 16.
-    uint32_t TL[W][NP], live[W];
+    uint32_t TL[W][NP], live[W], cut[W];
 #pragma unroll
     for (uint32_t w = 0; w < W; ++w) {
         const uint32_t L = 32 * w + lane < nqb ? a.L[q0 + 32 * w + lane] & 0xffu : 0u;  // 0: falls back
 #pragma unroll
         for (uint32_t i = 0; i < NP; ++i) TL[w][i] = __ballot_sync(kFull, (L >> i) & 1u);
         live[w] = __ballot_sync(kFull, L != 0);
+        cut[w] = a.pcut && 32 * w + lane < nqb ? a.pcut[q0 + 32 * w + lane] : a.P;
     }
-    if (stage) fused_pieces<kDW, W, true, NC>(a, M, q0, nqb, TL, live, lane, warp);
-    else fused_pieces<kDW, W, false, NC>(a, M, q0, nqb, TL, live, lane, warp);
+    if (stage) fused_pieces<kDW, W, true, NC>(a, M, q0, nqb, TL, live, cut, lane, warp);
+    else fused_pieces<kDW, W, false, NC>(a, M, q0, nqb, TL, live, cut, lane, warp);
 }
 
 // K4: thread per (query, piece), T == L: the piece's buffer holds its score >= T points in id
@@ -888,6 +912,7 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_h_kernel(DenseArg
     const uint32_t T0 = __ballot_sync(kFull, L & 1u), T1 = __ballot_sync(kFull, L & 2u);
     const uint32_t T2 = __ballot_sync(kFull, L & 4u), T3 = __ballot_sync(kFull, L & 8u);
     const uint32_t live = __ballot_sync(kFull, L != 0);
+    const uint32_t cut = a.pcut && mine ? a.pcut[q0 + qj] : a.P;
     const uint16_t* M16 = reinterpret_cast<const uint16_t*>(M);
     const RegionOff ro(a.ns, a.K);
     const Xpose xp(lane);
@@ -918,11 +943,12 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_h_kernel(DenseArg
             // queries past the block's last have no live bits: their lanes see empty words
             const uint32_t ge0 = xp((gt | eq) & live);
             const uint32_t g1 = xp(gt & live);
-            const uint32_t c0 = __popc(ge0), o0 = __shfl_xor_sync(kFull, c0, 16);
-            cnt += c0 | (__popc(g1) << 16);
+            cnt += __popc(ge0) | (__popc(g1) << 16);
+            const uint32_t kept = piece < cut ? ge0 : g1;  // past the tie cut: score > L only
+            const uint32_t c0 = __popc(kept), o0 = __shfl_xor_sync(kFull, c0, 16);
             uint32_t at = nb + (half ? o0 : 0u);
             const uint32_t tb = static_cast<uint32_t>(t0 - lo) + 32 * half;
-            uint32_t bits = ge0;
+            uint32_t bits = kept;
             while (bits) {  // id order
                 const uint32_t r = __ffs(bits) - 1;
                 bits &= bits - 1;

@@ -111,6 +111,8 @@ struct DenseArgs {
     uint32_t stage_all;           // fused pass: stage every block's stores (tests; else by density)
     uint32_t half;                // 16-query blocks, u16 masks, codes = cell + 1 per subspace (large N_s*K)
     uint32_t nc;                  // uint4 code vectors per point: 1 (N_s <= 8, default) or 2 (N_s <= 16)
+    uint32_t* pcut;               // single pass: nq, tie entries are stored only in pieces < pcut[q]
+    uint32_t no_cut;              // tests: store every tie (pcut = P)
 };
 bool dense_supported(uint32_t ns, uint32_t K);
 // 9..16 subspaces: two code vectors per point, 5 score planes, 16 histogram levels (config 3)

@@ -332,6 +332,7 @@ def test_dense_buffer_overflow_falls_back(gpu, oracle, monkeypatch, capfd):
     more than B = 96 of them in one (query, piece) buffer flags the query, which then takes the exact
     two-pass select. Answers stay identical to the reference."""
     monkeypatch.setenv("SUCO_DENSE_STATS", "1")
+    monkeypatch.setenv("SUCO_DENSE_BUF", "96")  # small batches would otherwise get whole-piece buffers
     full = oracle.clustered(40000 + 64, 16, 8, 77, 0, 100, 6, True)
     full = full[np.argsort(full[:, 0], kind="stable")]
     rng = np.random.default_rng(5)
@@ -376,6 +377,7 @@ def test_dense_half_width_overflow_falls_back(gpu, oracle, monkeypatch, capfd):
     select (as test_dense_buffer_overflow_falls_back)."""
     monkeypatch.setenv("SUCO_DENSE_HALF", "2")
     monkeypatch.setenv("SUCO_DENSE_STATS", "1")
+    monkeypatch.setenv("SUCO_DENSE_BUF", "96")
     full = oracle.clustered(40000 + 40, 16, 8, 77, 0, 100, 6, True)
     full = full[np.argsort(full[:, 0], kind="stable")]
     pick = np.sort(np.random.default_rng(5).choice(len(full), 40, replace=False))
@@ -446,3 +448,24 @@ def test_dense_select_16_subspaces(gpu, oracle, ns, kh, fused, monkeypatch):
     s1, c1, _, _ = idx.query_intermediates(qs[4], gpu.CollisionParams(0.05, 0.01, 10))
     s2, c2, _, _ = oidx.query_intermediates(base, qs[4], 0.05, 0.01, 10)
     assert np.array_equal(c1, c2)
+
+
+@pytest.mark.parametrize("nocut", ["0", "1"])
+def test_dense_tie_cut_sorted_corpus(gpu, oracle, monkeypatch, capfd, nocut):
+    """The single pass stores score == L entries only in the pieces the tie quota is expected to
+    reach. Rows sorted along one coordinate concentrate a query's ties in a few pieces, so the
+    estimate misses for some queries, which take the exact fallback; answers are identical to the
+    reference with and without the cut."""
+    monkeypatch.setenv("SUCO_DENSE_STATS", "1")
+    if nocut == "1":
+        monkeypatch.setenv("SUCO_DENSE_NOCUT", "1")
+    full = oracle.clustered(120000 + 64, 16, 8, 78, 0, 100, 6, True)
+    full = full[np.argsort(-full[:, 0], kind="stable")]
+    pick = np.sort(np.random.default_rng(6).choice(len(full), 64, replace=False))
+    qs, base = full[pick], np.delete(full, pick, axis=0)
+    oidx = oracle.build_index(base, 4, 12, 3, 42, 0)
+    idx = gpu.load_index(oidx.serialize(), base)
+    for a, b, k in ((0.2, 0.01, 10), (0.05, 0.02, 20), (0.5, 0.001, 5)):
+        ids, dd = idx.knn_query_batch(qs, gpu.CollisionParams(a, b, k))
+        oi, od, _ = oidx.knn_query_batch(base, qs, a, b, k)
+        assert np.array_equal(ids, oi) and np.array_equal(dd, od), (a, b, k)
