@@ -493,43 +493,51 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_screen_kernel(RerankArgs a
     for (uint32_t t = 0; t < kIdAhead; ++t) {
         if ((lane >> 3) == t) idreg = load_id(t);
     }
-    auto issue = [&](uint64_t i) {
-        const uint64_t g = i / nch;
-        const uint32_t c0 = static_cast<uint32_t>(i % nch) * kChunk;
+    // issue / compute positions kept as counters (group, chunk, ring slot): no 64-bit div/mod
+    uint32_t ig = 0, ic = 0, is = 0;
+    auto issue_next = [&]() {
+        const uint32_t c0 = ic * kChunk;
         const uint32_t cl = min(kChunk, a.d - c0);
-        const uint32_t slot = (g % kIdAhead) * 8u;
-        const uint64_t b = gbase(g);
-        const uint32_t si = static_cast<uint32_t>(i % S);
-        float* st = wr + si * kRows * stride;
+        const uint32_t slot = (ig % kIdAhead) * 8u;
+        float* st = wr + is * kRows * stride;
+        uint32_t id[kRows];
 #pragma unroll
-        for (uint32_t j = 0; j < kRows; ++j) {
-            const uint32_t id = __shfl_sync(kFull, idreg, slot + j);
-            if (b + j < mq && 4 * lane < cl) cp_async16(st + j * stride + 4 * lane, a.data + uint64_t(id) * a.d + c0 + 4 * lane);
-            if (lane == j) idbuf[warp][si][j] = id;
+        for (uint32_t j = 0; j < kRows; ++j) id[j] = __shfl_sync(kFull, idreg, slot + j);
+        const uint32_t id8 = __shfl_sync(kFull, idreg, slot + (lane & 7u));
+        if (4 * lane < cl) {  // rows past mq read row 0 (ids are 0 there): their results are ignored
+#pragma unroll
+            for (uint32_t j = 0; j < kRows; ++j)
+                cp_async16(st + j * stride + 4 * lane, a.data + uint64_t(id[j]) * a.d + c0 + 4 * lane);
         }
-        if (c0 + cl == a.d) {
-            if ((lane >> 3) == g % kIdAhead) idreg = load_id(g + kIdAhead);
+        if (lane < kRows) idbuf[warp][is][lane] = id8;
+        if (c0 + cl == a.d) {  // the group's last chunk is in flight: its id slots take group ig + kIdAhead
+            if ((lane >> 3) == ig % kIdAhead) idreg = load_id(ig + kIdAhead);
+            ++ig;
+            ic = 0;
+        } else {
+            ++ic;
         }
+        is = is + 1 == S ? 0u : is + 1;
     };
     double sl = kInf;  // screen list: the k smallest upper bounds (lane i = entry i)
     uint32_t nsurv = 0;
     bool overflow = false;
     float acc = 0.f;
     for (uint32_t i = 0; i + 1 < S; ++i) {
-        if (i < items) issue(i);
+        if (i < items) issue_next();
         cp_async_commit();
     }
+    uint32_t cg = 0, cc = 0, cs = 0;  // compute position
     for (uint64_t i = 0; i < items; ++i) {
-        if (i + S - 1 < items) issue(i + S - 1);
+        if (i + S - 1 < items) issue_next();
         cp_async_commit();
         cp_async_wait<S - 1>();
         __syncwarp();
-        const uint64_t g = i / nch;
-        const uint32_t c0 = static_cast<uint32_t>(i % nch) * kChunk;
+        const uint32_t c0 = cc * kChunk;
         const uint32_t cl = min(kChunk, a.d - c0);
-        const uint64_t b = gbase(g);
+        const uint64_t b = gbase(cg);
         const uint32_t nrows = static_cast<uint32_t>(min_u64(kRows, mq - b));
-        const uint32_t si = static_cast<uint32_t>(i % S);
+        const uint32_t si = cs;
         if (r < nrows) {
             const float* row = wr + si * kRows * stride + r * stride;
 #pragma unroll 8
@@ -595,6 +603,13 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_screen_kernel(RerankArgs a
             }
         }
         __syncwarp();  // the slot (rows and ids) is refilled by the next iteration's issue
+        if (c0 + cl == a.d) {
+            ++cg;
+            cc = 0;
+        } else {
+            ++cc;
+        }
+        cs = cs + 1 == S ? 0u : cs + 1;
     }
     cp_async_wait<0>();
     // one tau for the CTA: the k smallest upper bounds over every warp
