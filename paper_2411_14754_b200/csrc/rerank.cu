@@ -807,6 +807,10 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_u8_pipe_kernel(RerankArgs 
     constexpr uint32_t nw = NW;                    // 16-byte units per row (dpad / 16 <= 8)
     constexpr uint32_t su = NW | 1u;               // row stride in 16-byte units (odd)
     __shared__ uint32_t qpack[32];                 // the query as bytes, packed once per CTA
+    // (distance << 32 | id) of the best k-th entry over the CTA's warps: every warp already holds k
+    // rows at or below its own k-th, so a row above this bound cannot reach the final top-k
+    __shared__ unsigned long long kbound;
+    if (tid == 0) kbound = ~0ull;
     if (tid < 32) {
         uint32_t v = 0;
 #pragma unroll
@@ -899,13 +903,19 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_u8_pipe_kernel(RerankArgs 
                 a.all_id[q * a.m + b + lane] = myid;
             }
         } else {
-            const double wd = __shfl_sync(kFull, ld, a.k - 1);
-            const uint32_t wi = __shfl_sync(kFull, lid, a.k - 1);
-            uint32_t bal = __ballot_sync(kFull, valid && dist_id_less(dist, myid, wd, wi));
-            while (bal) {  // rows that beat the k-th best (rare once the list fills)
-                const uint32_t src = __ffs(bal) - 1;
-                bal &= bal - 1;
-                warp_insert(__shfl_sync(kFull, dist, src), __shfl_sync(kFull, myid, src), ld, lid, a.k, lane);
+            const unsigned long long kb = *reinterpret_cast<volatile unsigned long long*>(&kbound);
+            const unsigned long long key = (static_cast<unsigned long long>(acc) << 32) | myid;
+            uint32_t bal = __ballot_sync(kFull, valid && key < kb);
+            if (bal) {
+                while (bal) {  // rows that beat the bound (rare once the lists fill)
+                    const uint32_t src = __ffs(bal) - 1;
+                    bal &= bal - 1;
+                    warp_insert(__shfl_sync(kFull, dist, src), __shfl_sync(kFull, myid, src), ld, lid, a.k, lane);
+                }
+                const double wd = __shfl_sync(kFull, ld, a.k - 1);
+                const uint32_t wi = __shfl_sync(kFull, lid, a.k - 1);
+                if (lane == 0 && wd != kInf)  // integer distances below 2^32: exact as u32
+                    atomicMin(&kbound, (static_cast<unsigned long long>(static_cast<uint32_t>(wd)) << 32) | wi);
             }
         }
     }
