@@ -793,10 +793,10 @@ __global__ void __launch_bounds__(kThreads, 6) rerank_u8_kernel(RerankArgs a) {
 // (row stride an odd number of 16-byte units: conflict-free LDS.128) against the query words held in
 // registers — VABSDIFF4 + IDP.4A per word, no cross-lane reduction — and one ballot per step finds
 // the rows that beat the warp's k-th best.
-constexpr uint32_t kU8Stages = 3;
+constexpr uint32_t kU8Stages = 2;
 
 template <uint32_t NW, bool GENERIC>
-__global__ void __launch_bounds__(kThreads, 2) rerank_u8_pipe_kernel(RerankArgs a) {
+__global__ void __launch_bounds__(kThreads, 3) rerank_u8_pipe_kernel(RerankArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint64_t q = blockIdx.x;
