@@ -445,8 +445,8 @@ __device__ void exact_rows(const RerankArgs& a, float* st, uint32_t stride, cons
     }
 }
 
-template <uint32_t S>
-__global__ void __launch_bounds__(kThreads, 2) rerank_screen_kernel(RerankArgs a, uint32_t stride) {
+template <uint32_t S, uint32_t MINB>
+__global__ void __launch_bounds__(kThreads, MINB) rerank_screen_kernel(RerankArgs a, uint32_t stride) {
     extern __shared__ __align__(16) unsigned char smem[];
     float* qf = reinterpret_cast<float*>(smem);                                                  // d
     double* qd = reinterpret_cast<double*>(smem + ((a.d * 4 + 15) / 16) * 16);                   // d
@@ -1055,10 +1055,20 @@ cudaError_t launch_rerank(const RerankArgs& a, uint64_t nq, cudaStream_t st) {
         const uint32_t stride = 32 * ((min(a.d, kChunk) + 31) / 32) + 4;  // = 4 (mod 32): conflict-free chains
         const size_t qbytes = ((a.d * 4 + 15) / 16) * 16 + ((a.d * 8 + 15) / 16) * 16;
         const size_t s3 = qbytes + size_t(kWarps) * 3 * kRows * stride * 4;
-        // 3 stages when two CTAs still fit an SM (228 KB, about 14 KB static + 1 KB reserved each)
-        const bool three = s3 <= 98 * 1024;
-        const size_t ssmem = three ? s3 : qbytes + size_t(kWarps) * 2 * kRows * stride * 4;
-        auto kern = three ? rerank_screen_kernel<3> : rerank_screen_kernel<2>;
+        const size_t s2 = qbytes + size_t(kWarps) * 2 * kRows * stride * 4;
+        // occupancy first (measured: 2 stages x 3 CTAs per SM beat 3 x 2 for the byte rows): 3 CTAs
+        // when 2 stages fit 60 KB (228 KB per SM, about 14 KB static + 1 KB reserved each), else 3
+        // stages x 2 CTAs when that fits 98 KB, else 2 x 2. SUCO_SCREEN_STAGES=3 forces 3 x 2.
+        const char* sv = std::getenv("SUCO_SCREEN_STAGES");
+        const int force3 = sv && std::atoi(sv) == 3;
+        void (*kern)(RerankArgs, uint32_t) = rerank_screen_kernel<2, 2>;
+        size_t ssmem = s2;
+        if (!force3 && s2 <= 60 * 1024) {
+            kern = rerank_screen_kernel<2, 3>;
+        } else if (s3 <= 98 * 1024) {
+            kern = rerank_screen_kernel<3, 2>;
+            ssmem = s3;
+        }
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ssmem));
         if (e != cudaSuccess) return e;
         kern<<<static_cast<unsigned>(nq), kThreads, ssmem, st>>>(a, stride);
