@@ -9,8 +9,13 @@ index and queries resident in HBM (`value`), and again end to end through the
 C-ABI with pinned host buffers (`e2e`: H2D queries + D2H ids/distances inside
 the timed region). Timing: CUDA events on the stream the library launches on,
 W untimed warm-up steps, an L2 flush (256 MiB write, outside the events)
-between timed steps, max over ranks. Multi-GPU: N independent replicas (the
-sharded protocol is not wired into bench yet), scaling "weak".
+between timed steps, max over ranks. Multi-GPU (one process per GPU under
+torchrun): cfg1-cfg3 run query-parallel replicas — every rank holds the whole
+index (it fits one GPU) and answers its own 10,000-query batch, no data-path
+collective, scaling "weak"; cfg4/cfg5 (the configs BASELINE.json shards by
+point) and `--sharded` run the point-sharded protocol (paper_2411_14754_b200.sharded:
+block-cyclic point shards, NCCL all-gathers of the SC-score histograms and of
+the local top-k), scaling "strong". `--replicas` forces the replica mode.
 
 `--impl reference` times the reference's own CPU implementation
 (oracle/_ref/libsuco_ref.so, built from /root/reference sources) on this
@@ -205,6 +210,8 @@ def main():
     ap.add_argument("--no-u8", action="store_true",
                     help="re-rank from the f32 rows even for u8-valued data (the f32-row variant, SURVEY §8(d))")
     ap.add_argument("--sharded", action="store_true", help="use the multi-GPU shard protocol even at N = 1")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: query-parallel full replicas even for the point-sharded configs (cfg4, cfg5)")
     ap.add_argument("--block", type=int, default=0,
                     help="block-cyclic shard block size (ids); 0 = suco_gpu_shard_block_hint (slabs == blocks)")
     ap.add_argument("--alpha", type=float, default=None, help="experiment: override the config's alpha")
@@ -271,10 +278,13 @@ def main():
         build_s = time.time() - t0
     log(f"[rank {rank}] index ready (gpu build {build_s}, reference build {ref_build_s})")
 
-    if ws > 1 or args.sharded:
+    point_sharded = cfg.name in ("cfg4", "cfg5") and not args.replicas  # BASELINE.json: points sharded
+    if args.sharded or (ws > 1 and point_sharded):
         run_sharded(args, cfg, base, queries, idx, build_s, ws, rank, local)
         return
 
+    if ws > 1:  # replicas: each rank answers its own batch (the same set, rotated by rank)
+        queries = np.ascontiguousarray(np.roll(queries, rank * (nq // ws), axis=0))
     stream = torch.cuda.Stream()
     idx.set_stream(stream.cuda_stream)
     dq = torch.from_numpy(queries).cuda()
