@@ -195,6 +195,9 @@ def run_reference_arm(args, cfg):
 
 
 def main():
+    # the driver parses ONE JSON line from stdout: NCCL's own messages go to stderr
+    os.environ.setdefault("NCCL_DEBUG", "WARN")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
