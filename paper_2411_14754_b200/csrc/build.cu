@@ -172,7 +172,8 @@ __device__ inline double block_sum_exact(double v, double* sh) {
 __global__ void __launch_bounds__(256) kpp_select_kernel(const float* proj, const KJob* jobs, uint64_t n, uint32_t c,
                                                          const double* __restrict__ min_dist, const uint8_t* chosen,
                                                          const uint8_t* exact, const double* uniforms, uint32_t kmax,
-                                                         uint32_t* used, uint32_t* pick, double* prefix_all, float* cent) {
+                                                         uint32_t* used, uint32_t* pick, double* prefix_all, float* cent,
+                                                         int serial) {
     __shared__ double buf[2][256];
     __shared__ double shd[8];
     __shared__ uint32_t shu[8];
@@ -218,6 +219,116 @@ __global__ void __launch_bounds__(256) kpp_select_kernel(const float* proj, cons
             __syncthreads();
         }
         if (tid == 0) s_total = carry;
+    } else if (serial == 0) {
+        // The strictly serial fold (kmeans.cpp:77, :83-84) computed exactly in parallel. While the
+        // running sum s stays in one binade [2^e, 2^(e+1)), every representable value there is a
+        // multiple of U = ulp(s), so fl(s + a) = s + U * rint(a / U) — independent of s except on an
+        // exact tie (a / U = m + 1/2, rounded to even) — and the fold is an exact integer prefix sum
+        // of rint(a_i / U). Each 2048-value tile is scanned that way up to its first element that
+        // crosses into the next binade, is a tie, or meets s == 0 / a subnormal s; that element is
+        // added serially (one __dadd_rn) and the scan resumes after it. Crossings are O(log n) per
+        // pass, ties rare, so the pass runs at block-scan speed with the serial fold's exact values.
+        __shared__ long long wsum[8];
+        __shared__ uint32_t s_bad;
+        __shared__ double s_run;
+        if (tid == 0) s_run = 0.0;
+        __syncthreads();
+        constexpr double kTwo53 = 9007199254740992.0;
+        for (uint64_t base = 0; base < n; base += 2048) {
+            const uint32_t len = static_cast<uint32_t>(min_u64(2048, n - base));
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t i = tid * 8 + u;
+                v[u] = i < len ? md[base + i] : 0.0;
+            }
+            uint32_t start = 0;
+            while (start < len) {
+                const double s0 = s_run;  // exact running sum before element `start`
+                const bool tiny = !(s0 >= 2.2250738585072014e-308);  // 0 or subnormal
+                const double U = tiny ? 0.0 : ldexp(1.0, ilogb(s0) - 52);  // ulp of s0
+                const double S0 = tiny ? 0.0 : s0 / U;  // exact: power-of-two scaling
+                // per element: integer increment r (clamped) and a "needs the serial add" flag
+                long long r[8];
+                bool badv[8];
+                long long loc = 0;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const uint32_t i = tid * 8 + u;
+                    const bool live = i >= start && i < len;
+                    r[u] = 0;
+                    badv[u] = false;
+                    if (live) {
+                        if (tiny) {
+                            badv[u] = v[u] != 0.0;  // 0 + 0 stays exact; anything else goes serial
+                        } else {
+                            const double q = v[u] / U;  // exact
+                            const double m = floor(q);
+                            const double f = q - m;  // exact
+                            badv[u] = f == 0.5 || q >= 4503599627370496.0;  // tie, or surely crossing
+                            const double rr = f > 0.5 ? m + 1.0 : m;
+                            r[u] = badv[u] ? 0 : static_cast<long long>(rr);
+                        }
+                    }
+                    loc += r[u];
+                }
+                // block exclusive scan of the per-thread sums
+                long long x = loc;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const long long y = __shfl_up_sync(kFull, x, o);
+                    if (lane >= static_cast<uint32_t>(o)) x += y;
+                }
+                if (lane == 31) wsum[warp] = x;
+                if (tid == 0) s_bad = 0xffffffffu;
+                __syncthreads();
+                long long wpre = 0;
+                for (uint32_t w = 0; w < warp; ++w) wpre += wsum[w];
+                long long run = wpre + (x - loc);  // exclusive prefix of this thread's first element
+                // crossing: S0 + run_before + q >= 2^53 (exact comparisons on integers < 2^53)
+                uint32_t first_bad = 0xffffffffu;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const uint32_t i = tid * 8 + u;
+                    if (i >= start && i < len && first_bad == 0xffffffffu) {
+                        const double before = S0 + static_cast<double>(run);  // exact while < 2^53
+                        if (badv[u] || (!tiny && static_cast<double>(r[u]) + before >= kTwo53) ||
+                            (!tiny && before >= kTwo53))
+                            first_bad = i;
+                        run += r[u];
+                    }
+                }
+                if (first_bad != 0xffffffffu) atomicMin(&s_bad, first_bad);
+                __syncthreads();
+                const uint32_t bad = s_bad;
+                // write the exact prefix of the good elements [start, bad)
+                run = wpre + (x - loc);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const uint32_t i = tid * 8 + u;
+                    if (i >= start && i < len) {
+                        run += r[u];
+                        if (i < bad) prefix[base + i] = tiny ? s0 : __dmul_rn(S0 + static_cast<double>(run), U);
+                    }
+                }
+                __syncthreads();
+                if (bad == 0xffffffffu || bad >= len) {  // the whole rest of the tile was good
+                    if (tid == 0) s_run = len > start ? prefix[base + len - 1] : s0;
+                    __syncthreads();
+                    break;
+                }
+                // the bad element: its predecessor's exact value, then one serial add
+                if (tid == (bad >> 3)) {
+                    const double prev = bad > start ? prefix[base + bad - 1] : s0;
+                    const double nv = __dadd_rn(prev, v[bad & 7u]);
+                    prefix[base + bad] = nv;
+                    s_run = nv;
+                }
+                __syncthreads();
+                start = bad + 1;
+            }
+        }
+        if (tid == 0) s_total = s_run;
     } else if (warp == 0) {
         // strictly serial left-to-right fold (kmeans.cpp:77, :83-84): lane 0 adds,
         // the other lanes keep the next 256 values in flight
@@ -685,10 +796,12 @@ void kmeans_jobs(const float* proj, const std::vector<KJob>& host_jobs, const KJ
     copy_centroid_kernel<<<J, 64, 0, st>>>(proj, jobs, pick.p, 0, cent);
     BCUDA(cudaGetLastError());
     const dim3 gu(grid_for(n, 256, 148 * 4), J);
+    const char* ks = std::getenv("SUCO_KPP_SERIAL");  // 1: the one-lane serial fold (A/B, tests)
+    const int kpp_serial = ks && std::atoi(ks) == 1;
     for (uint32_t c = 1; c < k; ++c) {
         kpp_update_kernel<<<gu, 256, 0, st>>>(proj, jobs, n, pick.p, min_dist.p, chosen.p);
         kpp_select_kernel<<<J, 256, 0, st>>>(proj, jobs, n, c, min_dist.p, chosen.p, d_exact.p, d_unis.p, k, used.p,
-                                             pick.p, prefix.p, cent);
+                                             pick.p, prefix.p, cent, kpp_serial);
         BCUDA(cudaGetLastError());
     }
     min_dist.release();

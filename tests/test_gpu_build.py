@@ -22,13 +22,23 @@ def test_kmeans_golden(gpu):
 @pytest.mark.parametrize("n,dim,k,iters,kind", [(5000, 8, 50, 4, "int"), (3000, 6, 64, 3, "float"),
                                                 (4000, 30, 50, 2, "float"), (2000, 3, 7, 5, "unit"),
                                                 (600, 4, 3, 10, "float"), (12, 2, 12, 3, "float"),
-                                                (20000, 8, 100, 2, "int"), (800, 40, 10, 3, "int")])
+                                                (20000, 8, 100, 2, "int"), (800, 40, 10, 3, "int"),
+                                                (60000, 4, 20, 2, "dyadic"), (50000, 6, 16, 2, "float"),
+                                                (30000, 2, 9, 2, "huge")])
 def test_kmeans_vs_oracle(gpu, oracle, n, dim, k, iters, kind):
+    """Exact k-means against the restated reference. "dyadic" (quarter-integers plus halves: few
+    mantissa bits, so the running k-means++ sum meets exact rounding ties) and "huge" (magnitudes
+    spanning 1e-30..1e30: binade crossings and serial adds everywhere) stress the parallel exact
+    fold of the k-means++ sums; the larger float corpora cross many binades."""
     rng = np.random.default_rng(n + dim + k)
     if kind == "int":
         pts = np.clip(np.rint(rng.normal(100, 30, (n, dim))), 0, 255).astype(np.float32)
     elif kind == "unit":
         pts = rng.random((n, dim)).astype(np.float32)
+    elif kind == "dyadic":
+        pts = (np.rint(rng.normal(0, 40, (n, dim))) / 4 + 0.5).astype(np.float32)
+    elif kind == "huge":
+        pts = (rng.normal(0, 1, (n, dim)) * 10.0 ** rng.integers(-15, 15, (n, 1))).astype(np.float32)
     else:
         pts = (rng.normal(0, 1, (n, dim)) * 10).astype(np.float32)
     for seed in (1, 99):
