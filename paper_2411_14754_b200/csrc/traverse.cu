@@ -385,23 +385,27 @@ __global__ void __launch_bounds__(256, 5) traverse_kernel(TraverseArgs a, uint32
 //
 // Per-thread arrays are interleaved [element][thread]: threads reading the
 // same element index hit consecutive words.
-template <uint32_t L>
+// SPLIT: two threads per task (adjacent lanes) compute and rank one half each — the centroid
+// distances and the O(k^2) ranking are most of a task's latency — then the even thread runs
+// Dynamic Activation alone; each half has its own ranking scratch and projected query.
+template <uint32_t L, bool SPLIT>
 __global__ void traverse_thread_kernel(TraverseArgs a) {
     constexpr uint32_t LOG = L == 64 ? 6 : 7;
     static_assert(L == 64 || L == 128, "leaves");
     extern __shared__ __align__(16) unsigned char smem[];
-    const uint32_t T = blockDim.x, t = threadIdx.x;
+    const uint32_t T = SPLIT ? blockDim.x / 2 : blockDim.x, t = SPLIT ? threadIdx.x >> 1 : threadIdx.x;
     const uint32_t s = blockIdx.y, k = a.k_half, K = a.K;
     double* tkey = reinterpret_cast<double*>(smem);  // [L][T]: loser keys (nodes 1..L-1); ranking scratch
     double* d1r = tkey + L * T;                       // [k][T]
     double* d2r = d1r + k * T;                        // [k][T]
-    uint32_t* cs = reinterpret_cast<uint32_t*>(d2r + k * T);  // [K] this subspace's cell sizes
-    float* qh = reinterpret_cast<float*>(cs + K);              // [hmax][T]
-    uint8_t* trow = reinterpret_cast<uint8_t*>(qh + a.hmax * T);  // [L][T]
+    double* scr2 = d2r + k * T;                       // SPLIT: [k][T] the second half's ranking scratch
+    uint32_t* cs = reinterpret_cast<uint32_t*>(scr2 + (SPLIT ? k * T : 0));  // [K] this subspace's cell sizes
+    float* qh = reinterpret_cast<float*>(cs + K);              // [hmax][T] (x2 with SPLIT)
+    uint8_t* trow = reinterpret_cast<uint8_t*>(qh + a.hmax * T * (SPLIT ? 2 : 1));  // [L][T]
     uint8_t* o1 = trow + L * T;  // [k][T]
     uint8_t* o2 = o1 + k * T;
     uint8_t* cur = o2 + k * T;
-    for (uint32_t i = t; i < K; i += T) cs[i] = __ldg(a.cell_size + static_cast<size_t>(s) * K + i);
+    for (uint32_t i = threadIdx.x; i < K; i += blockDim.x) cs[i] = __ldg(a.cell_size + static_cast<size_t>(s) * K + i);
     __syncthreads();
     const uint64_t q = static_cast<uint64_t>(blockIdx.x) * T + t;
     if (q >= a.nq) return;
@@ -409,26 +413,29 @@ __global__ void traverse_thread_kernel(TraverseArgs a) {
     const float* query = a.queries + q * a.d;
 
     // centroid_distances (query.cpp:42-64) for both halves, ranked by (dist, id)
+    const uint32_t h_lo = SPLIT ? (threadIdx.x & 1u) : 0u, h_hi = SPLIT ? h_lo + 1 : 2u;
 #pragma unroll 1
-    for (uint32_t half = 0; half < 2; ++half) {
+    for (uint32_t half = h_lo; half < h_hi; ++half) {
         const uint32_t h = half ? sd.h2 : sd.h1;
         const uint32_t* dims = a.dims + (half ? sd.dims2 : sd.dims1);
         const float* cent = a.cent + (half ? sd.cent2 : sd.cent1);
         double* dr = half ? d2r : d1r;
         uint8_t* ord = half ? o2 : o1;
-        for (uint32_t i = 0; i < h; ++i) qh[i * T + t] = query[__ldg(dims + i)];
+        double* scr = SPLIT && half ? scr2 : tkey;  // ranking scratch of this half
+        float* qp = SPLIT && half ? qh + a.hmax * T : qh;
+        for (uint32_t i = 0; i < h; ++i) qp[i * T + t] = query[__ldg(dims + i)];
         for (uint32_t c = 0; c < k; ++c) {  // sq_euclidean_raw (core.hpp:66-84) then sqrt
             const float* cc = cent + static_cast<size_t>(c) * h;
             double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
             uint32_t i = 0;
             for (; i + 4 <= h; i += 4) {
-                acc0 = __dadd_rn(acc0, sqdiff(__ldg(cc + i), qh[i * T + t]));
-                acc1 = __dadd_rn(acc1, sqdiff(__ldg(cc + i + 1), qh[(i + 1) * T + t]));
-                acc2 = __dadd_rn(acc2, sqdiff(__ldg(cc + i + 2), qh[(i + 2) * T + t]));
-                acc3 = __dadd_rn(acc3, sqdiff(__ldg(cc + i + 3), qh[(i + 3) * T + t]));
+                acc0 = __dadd_rn(acc0, sqdiff(__ldg(cc + i), qp[i * T + t]));
+                acc1 = __dadd_rn(acc1, sqdiff(__ldg(cc + i + 1), qp[(i + 1) * T + t]));
+                acc2 = __dadd_rn(acc2, sqdiff(__ldg(cc + i + 2), qp[(i + 2) * T + t]));
+                acc3 = __dadd_rn(acc3, sqdiff(__ldg(cc + i + 3), qp[(i + 3) * T + t]));
             }
-            for (; i < h; ++i) acc0 = __dadd_rn(acc0, sqdiff(__ldg(cc + i), qh[i * T + t]));
-            tkey[c * T + t] = __dsqrt_rn(__dadd_rn(__dadd_rn(acc0, acc1), __dadd_rn(acc2, acc3)));
+            for (; i < h; ++i) acc0 = __dadd_rn(acc0, sqdiff(__ldg(cc + i), qp[i * T + t]));
+            scr[c * T + t] = __dsqrt_rn(__dadd_rn(__dadd_rn(acc0, acc1), __dadd_rn(acc2, acc3)));
         }
         // rank of c = #{o : (d_o, o) < (d_c, c)}; four c per pass over o, the id tie-break folded
         // into the loop bounds (o < c0: <=, o >= c0 + 4: <, the group itself: exact)
@@ -437,21 +444,21 @@ __global__ void traverse_thread_kernel(TraverseArgs a) {
             uint32_t r[4];
 #pragma unroll
             for (uint32_t u = 0; u < 4; ++u) {
-                dc[u] = c0 + u < k ? tkey[(c0 + u) * T + t] : kInf;
+                dc[u] = c0 + u < k ? scr[(c0 + u) * T + t] : kInf;
                 r[u] = 0;
             }
             for (uint32_t o = 0; o < c0; ++o) {
-                const double v = tkey[o * T + t];
+                const double v = scr[o * T + t];
 #pragma unroll
                 for (uint32_t u = 0; u < 4; ++u) r[u] += v <= dc[u];
             }
             for (uint32_t o = c0; o < c0 + 4 && o < k; ++o) {
-                const double v = tkey[o * T + t];
+                const double v = scr[o * T + t];
 #pragma unroll
                 for (uint32_t u = 0; u < 4; ++u) r[u] += v < dc[u] || (v == dc[u] && o < c0 + u);
             }
             for (uint32_t o = c0 + 4; o < k; ++o) {
-                const double v = tkey[o * T + t];
+                const double v = scr[o * T + t];
 #pragma unroll
                 for (uint32_t u = 0; u < 4; ++u) r[u] += v < dc[u];
             }
@@ -465,6 +472,10 @@ __global__ void traverse_thread_kernel(TraverseArgs a) {
         }
     }
 
+    if constexpr (SPLIT) {  // the pair's other half is in shared memory; the odd thread is done
+        __syncwarp(3u << ((threadIdx.x & 31u) & ~1u));
+        if (threadIdx.x & 1u) return;
+    }
     // loser tree over the row heads (r, 0): node n at level lv loses with the leftmost leaf of its
     // right child
     const double d20 = d2r[t];
@@ -564,8 +575,10 @@ cudaError_t launch_traverse(const TraverseArgs& a, cudaStream_t st) {
     const bool warp_path = tv && tv[0] == 'w';
     if (a.k_half <= 128 && !warp_path) {
         const uint32_t L = a.k_half <= 64 ? 64 : 128;
-        // per thread: tkey (L f64), d1r/d2r (2k f64), qh (hmax f32), trow (L), o1/o2/cur (3k u8)
-        const size_t per_t = size_t(L) * 9 + size_t(a.k_half) * 19 + size_t(a.hmax) * 4;
+        const bool split = !(tv && tv[0] == 'n');  // "nosplit": one thread per task (A/B)
+        // per task: tkey (L f64), d1r/d2r (2k f64), qh (hmax f32), trow (L), o1/o2/cur (3k u8);
+        // split: + the second half's scratch (k f64) and projected query (hmax f32)
+        const size_t per_t = size_t(L) * 9 + size_t(a.k_half) * (split ? 27 : 19) + size_t(a.hmax) * (split ? 8 : 4);
         const size_t fixed = size_t(a.K) * 4 + 16;
         uint32_t best_T = 0, best_res = 0;
         for (uint32_t T = 32; T <= 256; T += 32) {  // most resident tasks per SM within 227 KB / CTA
@@ -579,11 +592,12 @@ cudaError_t launch_traverse(const TraverseArgs& a, cudaStream_t st) {
         }
         if (best_T) {  // measured faster at every bench config (cfg1 0.22 -> 0.19 ms, cfg2 1.25 -> 0.64)
             const size_t smem = fixed + per_t * best_T;
-            auto kern = L == 64 ? traverse_thread_kernel<64> : traverse_thread_kernel<128>;
+            auto kern = split ? (L == 64 ? traverse_thread_kernel<64, true> : traverse_thread_kernel<128, true>)
+                              : (L == 64 ? traverse_thread_kernel<64, false> : traverse_thread_kernel<128, false>);
             cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
             if (e != cudaSuccess) return e;
             const dim3 grid(static_cast<unsigned>((a.nq + best_T - 1) / best_T), a.ns);
-            kern<<<grid, best_T, smem, st>>>(a);
+            kern<<<grid, best_T * (split ? 2 : 1), smem, st>>>(a);
             return cudaGetLastError();
         }
     }
