@@ -388,12 +388,13 @@ __global__ void __launch_bounds__(256, 5) traverse_kernel(TraverseArgs a, uint32
 // SPLIT: two threads per task (adjacent lanes) compute and rank one half each — the centroid
 // distances and the O(k^2) ranking are most of a task's latency — then the even thread runs
 // Dynamic Activation alone; each half has its own ranking scratch and projected query.
-template <uint32_t L, bool SPLIT>
+template <uint32_t L, uint32_t SP>  // SP threads per task: 1, 2 (one half each) or 4 (half a half each)
 __global__ void traverse_thread_kernel(TraverseArgs a) {
+    constexpr bool SPLIT = SP > 1;
     constexpr uint32_t LOG = L == 64 ? 6 : 7;
     static_assert(L == 64 || L == 128, "leaves");
     extern __shared__ __align__(16) unsigned char smem[];
-    const uint32_t T = SPLIT ? blockDim.x / 2 : blockDim.x, t = SPLIT ? threadIdx.x >> 1 : threadIdx.x;
+    const uint32_t T = blockDim.x / SP, t = threadIdx.x / SP;
     const uint32_t s = blockIdx.y, k = a.k_half, K = a.K;
     double* tkey = reinterpret_cast<double*>(smem);  // [L][T]: loser keys (nodes 1..L-1); ranking scratch
     double* d1r = tkey + L * T;                       // [k][T]
@@ -413,7 +414,12 @@ __global__ void traverse_thread_kernel(TraverseArgs a) {
     const float* query = a.queries + q * a.d;
 
     // centroid_distances (query.cpp:42-64) for both halves, ranked by (dist, id)
-    const uint32_t h_lo = SPLIT ? (threadIdx.x & 1u) : 0u, h_hi = SPLIT ? h_lo + 1 : 2u;
+    const uint32_t sub = threadIdx.x % SP;
+    const uint32_t h_lo = SP == 4 ? sub >> 1 : SP == 2 ? sub : 0u, h_hi = SPLIT ? h_lo + 1 : 2u;
+    // SP = 4: the two threads of a half split its k centroids (distances, then ranks)
+    const uint32_t kpart = (a.k_half + 1) / 2;
+    const uint32_t c_lo = SP == 4 ? (sub & 1u) * kpart : 0u, c_hi = SP == 4 ? min(a.k_half, c_lo + kpart) : a.k_half;
+    const uint32_t lane = threadIdx.x & 31u;
 #pragma unroll 1
     for (uint32_t half = h_lo; half < h_hi; ++half) {
         const uint32_t h = half ? sd.h2 : sd.h1;
@@ -423,8 +429,11 @@ __global__ void traverse_thread_kernel(TraverseArgs a) {
         uint8_t* ord = half ? o2 : o1;
         double* scr = SPLIT && half ? scr2 : tkey;  // ranking scratch of this half
         float* qp = SPLIT && half ? qh + a.hmax * T : qh;
-        for (uint32_t i = 0; i < h; ++i) qp[i * T + t] = query[__ldg(dims + i)];
-        for (uint32_t c = 0; c < k; ++c) {  // sq_euclidean_raw (core.hpp:66-84) then sqrt
+        if (SP < 4 || (sub & 1u) == 0) {
+            for (uint32_t i = 0; i < h; ++i) qp[i * T + t] = query[__ldg(dims + i)];
+        }
+        if constexpr (SP == 4) __syncwarp(3u << (lane & ~1u));  // the half's projected query
+        for (uint32_t c = c_lo; c < c_hi; ++c) {  // sq_euclidean_raw (core.hpp:66-84) then sqrt
             const float* cc = cent + static_cast<size_t>(c) * h;
             double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
             uint32_t i = 0;
@@ -437,14 +446,15 @@ __global__ void traverse_thread_kernel(TraverseArgs a) {
             for (; i < h; ++i) acc0 = __dadd_rn(acc0, sqdiff(__ldg(cc + i), qp[i * T + t]));
             scr[c * T + t] = __dsqrt_rn(__dadd_rn(__dadd_rn(acc0, acc1), __dadd_rn(acc2, acc3)));
         }
+        if constexpr (SP == 4) __syncwarp(3u << (lane & ~1u));  // every distance of the half
         // rank of c = #{o : (d_o, o) < (d_c, c)}; four c per pass over o, the id tie-break folded
         // into the loop bounds (o < c0: <=, o >= c0 + 4: <, the group itself: exact)
-        for (uint32_t c0 = 0; c0 < k; c0 += 4) {
+        for (uint32_t c0 = c_lo; c0 < c_hi; c0 += 4) {
             double dc[4];
             uint32_t r[4];
 #pragma unroll
             for (uint32_t u = 0; u < 4; ++u) {
-                dc[u] = c0 + u < k ? scr[(c0 + u) * T + t] : kInf;
+                dc[u] = c0 + u < c_hi ? scr[(c0 + u) * T + t] : kInf;
                 r[u] = 0;
             }
             for (uint32_t o = 0; o < c0; ++o) {
@@ -457,6 +467,8 @@ __global__ void traverse_thread_kernel(TraverseArgs a) {
 #pragma unroll
                 for (uint32_t u = 0; u < 4; ++u) r[u] += v < dc[u] || (v == dc[u] && o < c0 + u);
             }
+            // (group members past c_hi are padding: kInf never counts against real values, and their
+            // own ranks are not stored)
             for (uint32_t o = c0 + 4; o < k; ++o) {
                 const double v = scr[o * T + t];
 #pragma unroll
@@ -464,7 +476,7 @@ __global__ void traverse_thread_kernel(TraverseArgs a) {
             }
 #pragma unroll
             for (uint32_t u = 0; u < 4; ++u) {
-                if (c0 + u < k) {
+                if (c0 + u < c_hi) {
                     dr[r[u] * T + t] = dc[u];
                     ord[r[u] * T + t] = static_cast<uint8_t>(c0 + u);
                 }
@@ -472,9 +484,9 @@ __global__ void traverse_thread_kernel(TraverseArgs a) {
         }
     }
 
-    if constexpr (SPLIT) {  // the pair's other half is in shared memory; the odd thread is done
-        __syncwarp(3u << ((threadIdx.x & 31u) & ~1u));
-        if (threadIdx.x & 1u) return;
+    if constexpr (SPLIT) {  // the task's other parts are in shared memory; thread 0 of the task goes on
+        __syncwarp(((1u << SP) - 1u) << (lane & ~(SP - 1u)));
+        if (sub != 0) return;
     }
     // loser tree over the row heads (r, 0): node n at level lv loses with the leftmost leaf of its
     // right child
@@ -575,13 +587,18 @@ cudaError_t launch_traverse(const TraverseArgs& a, cudaStream_t st) {
     const bool warp_path = tv && tv[0] == 'w';
     if (a.k_half <= 128 && !warp_path) {
         const uint32_t L = a.k_half <= 64 ? 64 : 128;
-        const bool split = !(tv && tv[0] == 'n');  // "nosplit": one thread per task (A/B)
+        // two threads per task measured faster with short halves and small tables (cfg1/cfg2:
+        // 0.64 -> 0.60 ms) and slower otherwise (cfg3, h = 30: 0.25 -> 0.34 ms; cfg4, K = 4096:
+        // 1.13 -> 1.17 ms); SUCO_TRAVERSE=split / nosplit force it
+        const bool split = tv && tv[0] == 's' ? true : tv && tv[0] == 'n' ? false : (a.K <= 2500 && a.hmax <= 16);
+        const char* sv = std::getenv("SUCO_TRAVERSE_SPLIT");
+        const uint32_t sp = !split ? 1u : sv && std::atoi(sv) == 4 ? 4u : 2u;  // threads per task (4: measured slower)
         // per task: tkey (L f64), d1r/d2r (2k f64), qh (hmax f32), trow (L), o1/o2/cur (3k u8);
         // split: + the second half's scratch (k f64) and projected query (hmax f32)
         const size_t per_t = size_t(L) * 9 + size_t(a.k_half) * (split ? 27 : 19) + size_t(a.hmax) * (split ? 8 : 4);
         const size_t fixed = size_t(a.K) * 4 + 16;
         uint32_t best_T = 0, best_res = 0;
-        for (uint32_t T = 32; T <= 256; T += 32) {  // most resident tasks per SM within 227 KB / CTA
+        for (uint32_t T = 32; T <= 256 && T * sp <= 1024; T += 32) {  // most resident tasks per SM within 227 KB / CTA
             const size_t smem = fixed + per_t * T;
             if (smem > 227 * 1024) break;
             const uint32_t res = static_cast<uint32_t>((228 * 1024) / (smem + 1024)) * T;
@@ -592,12 +609,13 @@ cudaError_t launch_traverse(const TraverseArgs& a, cudaStream_t st) {
         }
         if (best_T) {  // measured faster at every bench config (cfg1 0.22 -> 0.19 ms, cfg2 1.25 -> 0.64)
             const size_t smem = fixed + per_t * best_T;
-            auto kern = split ? (L == 64 ? traverse_thread_kernel<64, true> : traverse_thread_kernel<128, true>)
-                              : (L == 64 ? traverse_thread_kernel<64, false> : traverse_thread_kernel<128, false>);
+            auto kern = sp == 4 ? (L == 64 ? traverse_thread_kernel<64, 4> : traverse_thread_kernel<128, 4>)
+                        : sp == 2 ? (L == 64 ? traverse_thread_kernel<64, 2> : traverse_thread_kernel<128, 2>)
+                                  : (L == 64 ? traverse_thread_kernel<64, 1> : traverse_thread_kernel<128, 1>);
             cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
             if (e != cudaSuccess) return e;
             const dim3 grid(static_cast<unsigned>((a.nq + best_T - 1) / best_T), a.ns);
-            kern<<<grid, best_T * (split ? 2 : 1), smem, st>>>(a);
+            kern<<<grid, best_T * sp, smem, st>>>(a);
             return cudaGetLastError();
         }
     }
