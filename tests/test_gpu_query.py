@@ -469,3 +469,17 @@ def test_dense_tie_cut_sorted_corpus(gpu, oracle, monkeypatch, capfd, nocut):
         ids, dd = idx.knn_query_batch(qs, gpu.CollisionParams(a, b, k))
         oi, od, _ = oidx.knn_query_batch(base, qs, a, b, k)
         assert np.array_equal(ids, oi) and np.array_equal(dd, od), (a, b, k)
+
+
+def test_host_batch_chunked_io(gpu, oracle):
+    """Host-buffer calls of >= 2048 queries upload queries and download results in chunks that
+    overlap the traversal and re-rank of their neighbours; answers equal the reference's, including
+    a ragged last chunk, k > 32 and k = 1."""
+    full = oracle.clustered(8000 + 2503, 24, 20, 4242, 0, 100, 8, True)
+    base, qs = oracle.hold_out(full, 2503, 4243)
+    oidx = oracle.build_index(base, 4, 10, 3, 42, 0)
+    idx = gpu.load_index(oidx.serialize(), base)
+    for a, b, k in ((0.05, 0.01, 10), (0.2, 0.05, 40), (0.1, 0.002, 1)):
+        ids, dd = idx.knn_query_batch(qs, gpu.CollisionParams(a, b, k))
+        oi, od, _ = oidx.knn_query_batch(base, qs, a, b, k)
+        assert np.array_equal(ids, oi) and np.array_equal(dd, od), (a, b, k)
