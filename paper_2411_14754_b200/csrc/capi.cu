@@ -505,7 +505,7 @@ void stage_select(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nt, uint
         CUDA_TRY(fused ? launch_dense_select_fused(da, st) : launch_dense_select(da, st));
         // two-pass: piece histograms, plan, emission; single pass: sample, bound, fused pass, plan,
         // compaction, flagged list, fallback histograms, plan, emission
-        x->launches += fused ? 9 : 3;
+        x->launches += fused ? 10 : 3;
         const bool stats = std::getenv("SUCO_DENSE_STATS") != nullptr;  // diagnostics: fallback rate
         if (stats && fused) {
             uint32_t nflag = 0;

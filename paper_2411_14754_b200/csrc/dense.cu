@@ -673,32 +673,85 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs 
 // K4: thread per (query, piece), T == L: the piece's buffer holds its score >= T points in id
 // order; keep every score > T and the first quota ties. Neighbouring threads take neighbouring
 // pieces: contiguous buffers in, contiguous candidate runs out.
-__global__ void __launch_bounds__(256) dense_compact_kernel(DenseArgs a) {
-    const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-    if (i >= a.nq * a.P) return;
-    const uint64_t q = i / a.P;
-    const uint32_t p = static_cast<uint32_t>(i % a.P);
-    const uint32_t n = a.ccnt[i];
-    if (!n || a.qflag[q]) return;  // (n <= B: an overflowing contributing piece flags its query)
-    uint32_t quota = a.quota[i];
-    uint32_t pos = a.base[i];
-    uint32_t* out = a.cands + q * a.m;
+// K4 for sparse supersets: thread per (query, piece); its few entries (cfg2: about 13) are read
+// and written by the one thread. Queries with dense supersets (L's kDenseStage flag) are left to
+// the warp kernel below.
+__global__ void __launch_bounds__(256) dense_compact_thread_kernel(DenseArgs a) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= a.P) return;
     const uint32_t pbase = p * a.WP;
-    const uint4* buf = reinterpret_cast<const uint4*>(a.cbuf + i * a.B);
-    const uint32_t lim = min(n, a.B);
-    for (uint32_t e0 = 0; e0 < lim; e0 += 8) {
-        const uint4 v = buf[e0 >> 3];
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    for (uint64_t q = blockIdx.y; q < a.nq; q += gridDim.y) {
+        if (a.L[q] & kDenseStage) continue;
+        const uint64_t i = q * a.P + p;
+        const uint32_t n = a.ccnt[i];
+        if (!n || a.qflag[q]) continue;  // (n <= B: an overflowing contributing piece flags its query)
+        uint32_t quota = a.quota[i];
+        uint32_t pos = a.base[i];
+        uint32_t* out = a.cands + q * a.m;
+        const uint4* buf = reinterpret_cast<const uint4*>(a.cbuf + i * a.B);
+        const uint32_t lim = min(n, a.B);
+        for (uint32_t e0 = 0; e0 < lim; e0 += 8) {
+            const uint4 v = buf[e0 >> 3];
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (uint32_t e = 0; e < 8; ++e) {
-            if (e0 + e < lim) {
-                const uint32_t x = (w[e >> 1] >> ((e & 1) * 16)) & 0xffffu;
-                if (x & 0x8000u) {
-                    __stcs(out + pos++, pbase + (x & 0x7fffu));
-                } else if (quota) {  // first ties in id order
-                    --quota;
-                    __stcs(out + pos++, pbase + x);
+            for (uint32_t e = 0; e < 8; ++e) {
+                if (e0 + e < lim) {
+                    const uint32_t x = (w[e >> 1] >> ((e & 1) * 16)) & 0xffffu;
+                    if (x & 0x8000u) {
+                        __stcs(out + pos++, pbase + (x & 0x7fffu));
+                    } else if (quota) {  // first ties in id order
+                        --quota;
+                        __stcs(out + pos++, pbase + x);
+                    }
                 }
+            }
+        }
+    }
+}
+
+// K4 for dense supersets (cfg4: pieces before the tie cut hold about 80 entries). A warp takes one
+// query's 32 consecutive pieces: lane j holds
+// piece j's count, tie quota and output offset; then piece by piece the lanes read its buffer in
+// coalesced 32-entry rows and keep every score > T entry plus the first `quota` ties (id order:
+// the buffer order), writing consecutive output positions.
+__global__ void __launch_bounds__(256) dense_compact_kernel(DenseArgs a) {
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint32_t p0 = (blockIdx.x * 8 + warp) * 32;
+    if (p0 >= a.P) return;
+    const uint32_t lt = (1u << lane) - 1u;
+    for (uint64_t q = blockIdx.y; q < a.nq; q += gridDim.y) {
+        if (!(a.L[q] & kDenseStage) || a.qflag[q]) continue;  // (overflow flags the query)
+        const uint32_t p = p0 + lane;
+        const uint64_t i = q * a.P + p;
+        uint32_t n = 0, quota = 0, base = 0;
+        if (p < a.P) {
+            n = min(static_cast<uint32_t>(a.ccnt[i]), a.B);
+            if (n) {
+                quota = a.quota[i];
+                base = a.base[i];
+            }
+        }
+        uint32_t* out = a.cands + q * a.m;
+        uint32_t todo = __ballot_sync(kFull, n != 0);
+        while (todo) {
+            const uint32_t src = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const uint32_t pn = __shfl_sync(kFull, n, src), pq = __shfl_sync(kFull, quota, src);
+            uint32_t pos = __shfl_sync(kFull, base, src);
+            const uint16_t* buf = a.cbuf + (q * a.P + p0 + src) * a.B;
+            const uint32_t pbase = (p0 + src) * a.WP;
+            uint32_t ties = 0;
+            for (uint32_t e0 = 0; e0 < pn; e0 += 32) {
+                const uint32_t e = e0 + lane;
+                const uint32_t x = e < pn ? buf[e] : 0u;
+                const bool gt = e < pn && (x & 0x8000u);
+                const bool tie = e < pn && !(x & 0x8000u);
+                const uint32_t tb = __ballot_sync(kFull, tie);
+                const bool keep = gt || (tie && ties + __popc(tb & lt) < pq);
+                const uint32_t kb = __ballot_sync(kFull, keep);
+                if (keep) __stcs(out + pos + __popc(kb & lt), pbase + (x & 0x7fffu));
+                pos += __popc(kb);
+                ties += __popc(tb);
             }
         }
     }
@@ -1148,7 +1201,9 @@ cudaError_t launch_dense_select_fused(const DenseArgs& args, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     // plan (+ fallback flags) from the two levels, compaction
     dense_plan_fused_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(a);
-    dense_compact_kernel<<<static_cast<unsigned>((a.nq * a.P + 255) / 256), 256, 0, st>>>(a);
+    const dim3 cgrid((a.P + 255) / 256, static_cast<unsigned>(min_u64(a.nq, 65535)));
+    dense_compact_thread_kernel<<<cgrid, 256, 0, st>>>(a);  // sparse supersets
+    dense_compact_kernel<<<cgrid, 256, 0, st>>>(a);         // dense supersets
     e = cudaMemsetAsync(args.nmap, 0, 4, st);
     if (e != cudaSuccess) return e;
     dense_flag_list_kernel<<<static_cast<unsigned>((a.nq + 255) / 256), 256, 0, st>>>(args);
