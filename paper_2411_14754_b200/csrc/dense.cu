@@ -38,7 +38,7 @@ namespace {
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr uint32_t kDenseStage = 0x100u;  // L[q] flag: dense superset (the fused pass stages stores)
 #ifndef SUCO_FUSED_PPW
-#define SUCO_FUSED_PPW 2
+#define SUCO_FUSED_PPW 4
 #endif
 constexpr uint32_t kFusedPPW = SUCO_FUSED_PPW;  // pieces per warp in the fused pass (large batches)
 
