@@ -475,7 +475,11 @@ void stage_select(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nt, uint
         if (fused) {
             // the sampled histograms (every pstride-th piece) predict the threshold; at least ~32
             // sampled pieces (small corpora: all of them, so the prediction is exact)
-            da.pstride = std::max<uint32_t>(1, std::min<uint32_t>(16, da.P / 32));
+            // about 16 sampled pieces when that is enough (cfg2: 489 pieces -> every 30th), and
+            // every 64th piece at most for large corpora (measured: cfg2 2.31M -> 2.36M q/s, cfg4
+            // 167K -> 174K; fewer samples mis-estimate T and send queries to the fallback)
+            da.pstride = da.P <= 64 ? 1u : std::min<uint32_t>(64, da.P / 16);  // small corpora: exact
+            if (const char* ps = std::getenv("SUCO_DENSE_PSTRIDE")) da.pstride = std::max(1, std::atoi(ps));  // A/B
             da.Ps = (da.P + da.pstride - 1) / da.pstride;
             sl.dsample.reserve(nt * da.Ps * 8 * da.nc);
             da.stage_all = std::getenv("SUCO_DENSE_STAGE") != nullptr;

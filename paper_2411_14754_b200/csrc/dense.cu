@@ -1108,6 +1108,8 @@ static Shape dense_shape(const DenseArgs& a) {
     // the two-pass one with 64-query blocks (5.04 vs 5.52 ms)
     const bool allow2 = (wv ? std::atoi(wv) == 2 : a.cbuf == nullptr) && a.nc != 2;  // 16 subspaces: one word
     if (allow2 && 2 * smem1 <= 200 * 1024) return {1024, 2, 2 * smem1};
+    const char* tv = std::getenv("SUCO_DENSE_THREADS");  // A/B: 1024 forces one big CTA per SM
+    if (tv && std::atoi(tv) == 1024) return {1024u, 1, smem1};
     return {smem1 <= 110 * 1024 ? 512u : 1024u, 1, smem1};
 }
 
