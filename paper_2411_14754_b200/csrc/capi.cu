@@ -499,6 +499,11 @@ void stage_select(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nt, uint
             sl.dflag.reserve(3 * nt + 1);  // flags, flagged list, its count, tie cuts
             da.pcut = sl.dflag.p + 2 * nt + 1;
             da.no_cut = std::getenv("SUCO_DENSE_NOCUT") != nullptr;
+            if (const char* cv = std::getenv("SUCO_TIE_CUT")) {  // A/B: "scale,pad"
+                da.cut_scale = static_cast<float>(std::atof(cv));
+                const char* comma = std::strchr(cv, ',');
+                da.cut_pad = comma ? static_cast<uint32_t>(std::atoi(comma + 1)) : 0u;
+            }
             da.hsample = sl.dsample.p;
             da.qmap = sl.dflag.p + nt;
             da.nmap = sl.dflag.p + 2 * nt;

@@ -550,7 +550,9 @@ __global__ void __launch_bounds__(256) dense_bound_kernel(DenseArgs a) {
         const double ties = (static_cast<double>(atL) - static_cast<double>(above)) * scale;
         const double need = static_cast<double>(a.m) - static_cast<double>(above) * scale;
         if (ties > 0.0 && need < ties) {
-            const double c = static_cast<double>(a.P) * (need > 0.0 ? need / ties : 0.0) * 1.25 + 8.0;
+            const double cs = a.cut_scale > 0.f ? static_cast<double>(a.cut_scale) : 1.25;
+            const double cp = a.cut_scale > 0.f ? static_cast<double>(a.cut_pad) : 8.0;
+            const double c = static_cast<double>(a.P) * (need > 0.0 ? need / ties : 0.0) * cs + cp;
             cut = c < static_cast<double>(a.P) ? static_cast<uint32_t>(c) : a.P;
         }
     }

@@ -113,6 +113,8 @@ struct DenseArgs {
     uint32_t nc;                  // uint4 code vectors per point: 1 (N_s <= 8, default) or 2 (N_s <= 16)
     uint32_t* pcut;               // single pass: nq, tie entries are stored only in pieces < pcut[q]
     uint32_t no_cut;              // tests: store every tie (pcut = P)
+    float cut_scale;              // tie cut = P * need/ties * cut_scale + cut_pad pieces (0: defaults 1.25, 8)
+    uint32_t cut_pad;
 };
 bool dense_supported(uint32_t ns, uint32_t K);
 // 9..16 subspaces: two code vectors per point, 5 score planes, 16 histogram levels (config 3)
