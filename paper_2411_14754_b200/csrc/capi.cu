@@ -381,7 +381,8 @@ uint64_t tile_size(const suco_gpu_index* x, uint64_t nq, uint64_t m, uint32_t k)
     const uint64_t per = ns * x->K * 4 + ns * 4 + m * 4 + (k > 32 ? m * 12 : 0) + uint64_t(x->host.d) * 4 + k * 12 +
                          (x->dense ? pieces * (24 + kDenseBuf * 2 + 14 + (ns > 8 ? 16 : 0)) + pieces / 16 * 32 + 16
                                    : 0);  // + buffers
-    const uint64_t budget = 16ull << 30;  // per-batch scratch on a 180 GB part
+    uint64_t budget = 16ull << 30;  // per-batch scratch on a 180 GB part
+    if (const char* b = std::getenv("SUCO_SCRATCH_GB")) budget = std::max(1ll, std::atoll(b)) << 30;  // A/B
     return std::max<uint64_t>(1, std::min<uint64_t>(nq, budget / per));
 }
 

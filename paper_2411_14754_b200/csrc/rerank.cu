@@ -793,10 +793,10 @@ __global__ void __launch_bounds__(kThreads, 6) rerank_u8_kernel(RerankArgs a) {
 // (row stride an odd number of 16-byte units: conflict-free LDS.128) against the query words held in
 // registers — VABSDIFF4 + IDP.4A per word, no cross-lane reduction — and one ballot per step finds
 // the rows that beat the warp's k-th best.
-constexpr uint32_t kU8Stages = 2;
+constexpr uint32_t kU8Stages = 2;  // default ring depth (x 3 CTAs per SM); 3 x 2 via SUCO_U8_STAGES=3
 
-template <uint32_t NW, bool GENERIC>
-__global__ void __launch_bounds__(kThreads, 3) rerank_u8_pipe_kernel(RerankArgs a) {
+template <uint32_t NW, bool GENERIC, uint32_t kU8Stages = kU8Stages, uint32_t MINB = 3>
+__global__ void __launch_bounds__(kThreads, MINB) rerank_u8_pipe_kernel(RerankArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint64_t q = blockIdx.x;
@@ -1018,7 +1018,9 @@ cudaError_t launch_rerank(const RerankArgs& a, uint64_t nq, cudaStream_t st) {
     const char* uv = std::getenv("SUCO_RERANK_U8_PIPE");  // 0: the register kernel (A/B)
     if (a.data8 && a.dpad <= 128 && !(uv && std::atoi(uv) == 0)) {
         const uint32_t nwr = a.dpad / 16, su = nwr | 1u;
-        const size_t usmem = size_t(kWarps) * kU8Stages * 32 * su * 16;
+        const char* sv = std::getenv("SUCO_U8_STAGES");
+        const bool deep = sv && std::atoi(sv) == 3;  // A/B: 3 ring stages x 2 CTAs per SM
+        const size_t usmem = size_t(kWarps) * (deep ? 3 : kU8Stages) * 32 * su * 16;
         using K = void (*)(RerankArgs);
         const K kg[8] = {rerank_u8_pipe_kernel<1, true>, rerank_u8_pipe_kernel<2, true>, rerank_u8_pipe_kernel<3, true>,
                          rerank_u8_pipe_kernel<4, true>, rerank_u8_pipe_kernel<5, true>, rerank_u8_pipe_kernel<6, true>,
@@ -1026,7 +1028,8 @@ cudaError_t launch_rerank(const RerankArgs& a, uint64_t nq, cudaStream_t st) {
         const K kn[8] = {rerank_u8_pipe_kernel<1, false>, rerank_u8_pipe_kernel<2, false>, rerank_u8_pipe_kernel<3, false>,
                          rerank_u8_pipe_kernel<4, false>, rerank_u8_pipe_kernel<5, false>, rerank_u8_pipe_kernel<6, false>,
                          rerank_u8_pipe_kernel<7, false>, rerank_u8_pipe_kernel<8, false>};
-        const K kern = generic ? kg[nwr - 1] : kn[nwr - 1];
+        K kern = generic ? kg[nwr - 1] : kn[nwr - 1];
+        if (deep && nwr == 8) kern = generic ? rerank_u8_pipe_kernel<8, true, 3, 2> : rerank_u8_pipe_kernel<8, false, 3, 2>;
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(usmem));
         if (e != cudaSuccess) return e;
         kern<<<static_cast<unsigned>(nq), kThreads, usmem, st>>>(a);
