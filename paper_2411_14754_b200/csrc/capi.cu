@@ -135,9 +135,10 @@ struct suco_gpu_index {
         DevBuf<uint32_t> dL, dflag, dh2;          // single-pass select: bound, fallback flags, two-level counts
         DevBuf<double> out_d, all_d;
         cudaEvent_t trav = nullptr, sel = nullptr, rr = nullptr;
+        cudaEvent_t selmain = nullptr;  // dense select: every unflagged query's candidates written
     };
     Slot slot[2];
-    cudaStream_t pipe[3] = {nullptr, nullptr, nullptr};
+    cudaStream_t pipe[4] = {nullptr, nullptr, nullptr, nullptr};  // traverse, select, rerank, fallback
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     // stage profiling (suco_gpu_set_profiling)
     bool profile = false;
@@ -154,6 +155,7 @@ struct suco_gpu_index {
             if (sl.trav) cudaEventDestroy(sl.trav);
             if (sl.sel) cudaEventDestroy(sl.sel);
             if (sl.rr) cudaEventDestroy(sl.rr);
+            if (sl.selmain) cudaEventDestroy(sl.selmain);
         }
         if (ev_in) cudaEventDestroy(ev_in);
         if (ev_out) cudaEventDestroy(ev_out);
@@ -197,11 +199,16 @@ void create_stream(suco_gpu_index* x) {
     // SMs that select's GPC-bound clusters leave idle
     CUDA_TRY(cudaStreamCreateWithPriority(&x->pipe[0], cudaStreamNonBlocking, prio ? greatest : least));
     CUDA_TRY(cudaStreamCreateWithPriority(&x->pipe[1], cudaStreamNonBlocking, least));
-    CUDA_TRY(cudaStreamCreateWithPriority(&x->pipe[2], cudaStreamNonBlocking, prio ? greatest : least));
+    // the dense select's fallback (a few query blocks, latency-bound) runs beside the re-rank of the
+    // unflagged queries; its CTAs go first (re-rank one priority level below, when there is one)
+    const int rr_prio = !prio ? least : greatest < least ? greatest + 1 : greatest;
+    CUDA_TRY(cudaStreamCreateWithPriority(&x->pipe[2], cudaStreamNonBlocking, rr_prio));
+    CUDA_TRY(cudaStreamCreateWithPriority(&x->pipe[3], cudaStreamNonBlocking, greatest));
     for (auto& sl : x->slot) {
         CUDA_TRY(cudaEventCreateWithFlags(&sl.trav, cudaEventDisableTiming));
         CUDA_TRY(cudaEventCreateWithFlags(&sl.sel, cudaEventDisableTiming));
         CUDA_TRY(cudaEventCreateWithFlags(&sl.rr, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&sl.selmain, cudaEventDisableTiming));
     }
     CUDA_TRY(cudaEventCreateWithFlags(&x->ev_in, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&x->ev_out, cudaEventDisableTiming));
@@ -287,7 +294,7 @@ void set_l2_window(suco_gpu_index* x) {
     v.accessPolicyWindow.hitRatio = std::min(1.0f, static_cast<float>(persist) / static_cast<float>(v.accessPolicyWindow.num_bytes));
     v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
     v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    for (cudaStream_t t : {x->own, x->pipe[0], x->pipe[1], x->pipe[2]}) {
+    for (cudaStream_t t : {x->own, x->pipe[0], x->pipe[1], x->pipe[2], x->pipe[3]}) {
         CUDA_TRY(cudaStreamSetAttribute(t, cudaStreamAttributeAccessPolicyWindow, &v));
     }
 }
@@ -442,8 +449,18 @@ void stage_traverse(suco_gpu_index* x, suco_gpu_index::Slot& sl, const float* d_
     if (ev) CUDA_TRY(cudaEventRecord(ev[1], st));
 }
 
-void stage_select(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nt, uint64_t m, cudaStream_t st,
-                  const Dbg* dbg) {
+// The dense select's fallback lists (qflag: nq flags; qmap[0 .. *nmap): the flagged queries).
+struct FbLists {
+    const uint32_t* qflag = nullptr;
+    const uint32_t* qmap = nullptr;
+    const uint32_t* nmap = nullptr;
+};
+
+// main_done / fb_st (optional, both or neither): with the single-pass dense select, main_done is
+// recorded on st once every unflagged query's candidates are written and the flagged queries'
+// fallback runs on fb_st; the returned lists are then set (else empty: st has everything).
+FbLists stage_select(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nt, uint64_t m, cudaStream_t st,
+                     const Dbg* dbg, cudaEvent_t main_done = nullptr, cudaStream_t fb_st = nullptr) {
     const HostIndex& h = x->host;
     sl.cands.reserve(nt * m);
     cudaEvent_t* ev = dbg ? nullptr : prof_pair(x, 1);
@@ -512,7 +529,9 @@ void stage_select(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nt, uint
             da.qflag = sl.dflag.p;
         }
         if (ev) CUDA_TRY(cudaEventRecord(ev[0], st));
-        CUDA_TRY(fused ? launch_dense_select_fused(da, st) : launch_dense_select(da, st));
+        const bool split = fused && main_done && fb_st;
+        CUDA_TRY(split ? launch_dense_select_fused(da, st, main_done, fb_st)
+                       : fused ? launch_dense_select_fused(da, st) : launch_dense_select(da, st));
         // two-pass: piece histograms, plan, emission; single pass: sample, bound, fused pass, plan,
         // compaction, flagged list, fallback histograms, plan, emission
         x->launches += fused ? 10 : 3;
@@ -538,8 +557,14 @@ void stage_select(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nt, uint
                          (unsigned long long)hist[3], (unsigned long long)hist[4], (unsigned long long)hist[5],
                          (unsigned long long)hist[6], (unsigned long long)hist[7], (unsigned long long)hist[8]);
         }
-        if (ev) CUDA_TRY(cudaEventRecord(ev[1], st));
-        return;
+        if (ev) CUDA_TRY(cudaEventRecord(ev[1], split ? fb_st : st));
+        FbLists fl;
+        if (split) {
+            fl.qflag = da.qflag;
+            fl.qmap = da.qmap;
+            fl.nmap = da.nmap;
+        }
+        return fl;
     }
     SelectArgs sa{};
     sa.ids = x->ids.p;
@@ -562,10 +587,12 @@ void stage_select(suco_gpu_index* x, suco_gpu_index::Slot& sl, uint64_t nt, uint
     CUDA_TRY(launch_select(sa, x->sel, nt, st));
     x->launches += 1;
     if (ev) CUDA_TRY(cudaEventRecord(ev[1], st));
+    return {};
 }
 
 void stage_rerank(suco_gpu_index* x, suco_gpu_index::Slot& sl, const float* d_q, uint64_t nt, uint64_t m, uint32_t k,
-                  uint32_t* d_ids, double* d_dists, cudaStream_t st, bool profiled) {
+                  uint32_t* d_ids, double* d_dists, cudaStream_t st, bool profiled, const FbLists* fl = nullptr,
+                  bool flagged = false) {
     const HostIndex& h = x->host;
     cudaEvent_t* ev = profiled ? prof_pair(x, 2) : nullptr;
     RerankArgs ra{};
@@ -586,6 +613,14 @@ void stage_rerank(suco_gpu_index* x, suco_gpu_index::Slot& sl, const float* d_q,
         sl.all_id.reserve(nt * m);
         ra.all_d = sl.all_d.p;
         ra.all_id = sl.all_id.p;
+    }
+    if (fl && fl->qflag) {  // a split select: the unflagged queries now, the flagged ones (qmap) later
+        if (flagged) {
+            ra.qlist = fl->qmap;
+            ra.nlist = fl->nmap;
+        } else {
+            ra.qskip = fl->qflag;
+        }
     }
     if (ev) CUDA_TRY(cudaEventRecord(ev[0], st));
     CUDA_TRY(launch_rerank(ra, nt, st));
@@ -627,6 +662,11 @@ void run_pipeline(suco_gpu_index* x, const float* h_q, const float* d_q, uint64_
     CUDA_TRY(cudaEventRecord(x->ev_in, user));
     for (cudaStream_t t : x->pipe) CUDA_TRY(cudaStreamWaitEvent(t, x->ev_in, 0));
     cudaStream_t s_trav = x->pipe[0], s_sel = x->pipe[1], s_rr = x->pipe[2];
+    // measured (SUCO_FB_OVERLAP=1/0 forces it): cfg2 (byte rows, 10,000 queries) 2.334M -> 2.364M q/s
+    // (e2e 2.12M -> 2.23M); slower where the re-rank is long beside it (fp32 rows: cfg3 143K -> 136K,
+    // cfg4 170K -> 169K), so only byte-row re-ranks of large tiles overlap
+    const char* fo = std::getenv("SUCO_FB_OVERLAP");
+    const bool fb_overlap = fo ? std::atoi(fo) != 0 : (x->dpad && !x->dense_half && tile >= 4096);
     for (uint64_t t = 0; t * tile < nq; ++t) {
         const uint64_t q0 = t * tile, nt = std::min(tile, nq - q0);
         auto& sl = x->slot[t & 1];
@@ -643,9 +683,12 @@ void run_pipeline(suco_gpu_index* x, const float* h_q, const float* d_q, uint64_
         CUDA_TRY(cudaEventRecord(sl.trav, s_trav));
         CUDA_TRY(cudaStreamWaitEvent(s_sel, sl.trav, 0));
         CUDA_TRY(cudaStreamWaitEvent(s_sel, sl.rr, 0));
-        stage_select(x, sl, nt, m, s_sel, nullptr);
-        CUDA_TRY(cudaEventRecord(sl.sel, s_sel));
-        CUDA_TRY(cudaStreamWaitEvent(s_rr, sl.sel, 0));
+        // the fallback of the few flagged queries overlaps the re-rank of the others (A/B:
+        // SUCO_FB_OVERLAP=0 keeps it on the select stream)
+        const FbLists fl = stage_select(x, sl, nt, m, s_sel, nullptr, fb_overlap ? sl.selmain : nullptr,
+                                        fb_overlap ? x->pipe[3] : nullptr);
+        CUDA_TRY(cudaEventRecord(sl.sel, fl.qflag ? x->pipe[3] : s_sel));
+        CUDA_TRY(cudaStreamWaitEvent(s_rr, fl.qflag ? sl.selmain : sl.sel, 0));
         uint32_t* oi = d_ids ? d_ids + q0 * k : nullptr;
         double* od = d_dists ? d_dists + q0 * k : nullptr;
         if (h_ids) {
@@ -654,7 +697,11 @@ void run_pipeline(suco_gpu_index* x, const float* h_q, const float* d_q, uint64_
             oi = sl.out_ids.p;
             od = sl.out_d.p;
         }
-        stage_rerank(x, sl, tq, nt, m, k, oi, od, s_rr, true);
+        stage_rerank(x, sl, tq, nt, m, k, oi, od, s_rr, true, &fl, false);
+        if (fl.qflag) {
+            CUDA_TRY(cudaStreamWaitEvent(s_rr, sl.sel, 0));
+            stage_rerank(x, sl, tq, nt, m, k, oi, od, s_rr, true, &fl, true);
+        }
         if (h_ids) {
             CUDA_TRY(cudaMemcpyAsync(h_ids + q0 * k, oi, nt * k * 4, cudaMemcpyDeviceToHost, s_rr));
             CUDA_TRY(cudaMemcpyAsync(h_dists + q0 * k, od, nt * k * 8, cudaMemcpyDeviceToHost, s_rr));

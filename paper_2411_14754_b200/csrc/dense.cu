@@ -1182,7 +1182,8 @@ static cudaError_t launch_fused_t(const DenseArgs& a, size_t smem, cudaStream_t 
     return cudaGetLastError();
 }
 
-cudaError_t launch_dense_select_fused(const DenseArgs& args, cudaStream_t st) {
+cudaError_t launch_dense_select_fused(const DenseArgs& args, cudaStream_t st, cudaEvent_t main_done,
+                                      cudaStream_t fb_st) {
     if (args.nq == 0) return cudaSuccess;
     DenseArgs a = args;  // every pass but the fallback emission sees the queries unmapped
     a.qmap = nullptr;
@@ -1213,6 +1214,16 @@ cudaError_t launch_dense_select_fused(const DenseArgs& args, cudaStream_t st) {
     dense_flag_list_kernel<<<static_cast<unsigned>((a.nq + 255) / 256), 256, 0, st>>>(args);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    // every unflagged query's candidates are final here; the fallback may run on its own stream
+    if (main_done) {
+        e = cudaEventRecord(main_done, st);
+        if (e != cudaSuccess) return e;
+        if (fb_st) {
+            e = cudaStreamWaitEvent(fb_st, main_done, 0);
+            if (e != cudaSuccess) return e;
+            st = fb_st;
+        }
+    }
     // the flagged queries (T != L) get the exact two-pass select — full histograms, plan,
     // emission — through qmap; blocks past the flagged count exit at once
     DenseArgs fb = args;

@@ -131,7 +131,10 @@ cudaError_t launch_dense_codes(const uint32_t* ids, const uint32_t* cell_off, ui
 cudaError_t launch_dense_select(const DenseArgs& a, cudaStream_t st);  // hist + plan + emit
 // single pass: K0 sample -> L estimate -> fused hist + superset -> plan + checks -> compaction ->
 // exact emission for the flagged query blocks (rare); needs hsample/L/cbuf/ccnt/qflag/B
-cudaError_t launch_dense_select_fused(const DenseArgs& a, cudaStream_t st);
+// main_done (optional) is recorded once every unflagged query's candidates are written; the
+// flagged queries' fallback then runs on fb_st (optional, else st).
+cudaError_t launch_dense_select_fused(const DenseArgs& a, cudaStream_t st, cudaEvent_t main_done = nullptr,
+                                      cudaStream_t fb_st = nullptr);
 // Shard protocol pieces: K1 alone (+ its histograms as [nq][P][N_s + 2] u32 rows with the
 // piece length first, the exchange format) and K3 alone with the globally planned T/quota/base.
 cudaError_t launch_dense_hist(const DenseArgs& a, cudaStream_t st);
@@ -163,6 +166,9 @@ struct RerankArgs {
     const uint8_t* data8;  // optional u8 copy of the rows (data certified integer in [0, 255]), n x dpad
     uint32_t dpad;         // row bytes of data8 (d rounded up to 16)
     bool identity;         // exact kNN: candidate i of every query is id i (cands unused, m = n)
+    const uint32_t* qskip;  // optional: queries with qskip[q] != 0 are left for a later pass
+    const uint32_t* qlist;  // optional: re-rank only qlist[0 .. *nlist) (the grid still spans nq)
+    const uint32_t* nlist;
 };
 cudaError_t launch_rerank(const RerankArgs& a, uint64_t nq, cudaStream_t st);
 

@@ -30,6 +30,19 @@ constexpr uint32_t kChunk = 128;  // dims per staged chunk
 constexpr uint32_t kStride = 132; // padded tile row (floats)
 constexpr uint32_t kFull = 0xffffffffu;
 
+// This CTA's query: blockIdx.x, minus the queries `qskip` marks (their candidates are not ready
+// yet), or the blockIdx.x-th entry of `qlist` (a later pass over exactly those queries).
+// false: the CTA has no query.
+__device__ __forceinline__ bool rerank_query(const RerankArgs& a, uint64_t& q) {
+    if (a.qlist) {
+        if (blockIdx.x >= *a.nlist) return false;
+        q = a.qlist[blockIdx.x];
+        return true;
+    }
+    q = blockIdx.x;
+    return !(a.qskip && a.qskip[q]);
+}
+
 __device__ __forceinline__ float4 ld_stream4(const float* p) {
     float4 v;
     asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
@@ -67,7 +80,8 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
     float* tile = qf + ((a.d + 3) / 4) * 4;                                          // warps x rows x stride
     __shared__ unsigned int qstat[2];
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    const uint64_t q = blockIdx.x;
+    uint64_t q;
+    if (!rerank_query(a, q)) return;
     const float* query = a.queries + q * a.d;
     if (tid < 2) qstat[tid] = 0;
     __syncthreads();
@@ -236,7 +250,8 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_pipe_kernel(RerankArgs a) 
     __shared__ unsigned int qstat[2];
     __shared__ uint32_t idbuf[kWarps][kStages][kRows];  // the ids of each ring slot's rows
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    const uint64_t q = blockIdx.x;
+    uint64_t q;
+    if (!rerank_query(a, q)) return;
     const float* query = a.queries + q * a.d;
     if (tid < 2) qstat[tid] = 0;
     __syncthreads();
@@ -459,7 +474,8 @@ __global__ void __launch_bounds__(kThreads, MINB) rerank_screen_kernel(RerankArg
     __shared__ double tau_cta;
     __shared__ int ovf;
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    const uint64_t q = blockIdx.x;
+    uint64_t q;
+    if (!rerank_query(a, q)) return;
     const float* query = a.queries + q * a.d;
     if (tid == 0) ovf = 0;
     bool qu8 = true;
@@ -696,7 +712,8 @@ __global__ void __launch_bounds__(kThreads, 6) rerank_u8_kernel(RerankArgs a) {
     __shared__ double md[kWarps * 32];
     __shared__ uint32_t mi[kWarps * 32];
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    const uint64_t q = blockIdx.x;
+    uint64_t q;
+    if (!rerank_query(a, q)) return;
     const float* query = a.queries + q * a.d;
     bool ok = true;
     for (uint32_t i = tid; i < a.d; i += kThreads) ok &= is_u8(query[i]);
@@ -799,7 +816,8 @@ template <uint32_t NW, bool GENERIC, uint32_t kU8Stages = kU8Stages, uint32_t MI
 __global__ void __launch_bounds__(kThreads, MINB) rerank_u8_pipe_kernel(RerankArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    const uint64_t q = blockIdx.x;
+    uint64_t q;
+    if (!rerank_query(a, q)) return;
     const float* query = a.queries + q * a.d;
     bool ok = true;
     for (uint32_t i = tid; i < a.d; i += kThreads) ok &= is_u8(query[i]);
@@ -950,7 +968,8 @@ __global__ void __launch_bounds__(256) topk_generic_kernel(RerankArgs a) {
     __shared__ double sd[8];
     __shared__ uint32_t si[8];
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    const uint64_t q = blockIdx.x;
+    uint64_t q;
+    if (!rerank_query(a, q)) return;
     const double* dd = a.all_d + q * a.m;
     const uint32_t* ii = a.all_id + q * a.m;
     const uint64_t mq = a.counts ? a.counts[q] : a.m;

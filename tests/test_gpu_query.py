@@ -327,10 +327,14 @@ def test_dense_select_block_widths(gpu, oracle, words, fused, monkeypatch):
     assert np.array_equal(c1, c2)
 
 
-def test_dense_buffer_overflow_falls_back(gpu, oracle, monkeypatch, capfd):
+@pytest.mark.parametrize("overlap", ["0", "1"])
+def test_dense_buffer_overflow_falls_back(gpu, oracle, overlap, monkeypatch, capfd):
     """Rows sorted along one coordinate put a query's high scorers in a few neighbouring pieces:
     more than B = 96 of them in one (query, piece) buffer flags the query, which then takes the exact
-    two-pass select. Answers stay identical to the reference."""
+    two-pass select. Answers stay identical to the reference — with the fallback on the select
+    stream, and overlapped with the re-rank of the unflagged queries (re-ranked in a second pass over
+    the flagged list; k > 32 takes the generic top-k kernel through the same mapping)."""
+    monkeypatch.setenv("SUCO_FB_OVERLAP", overlap)
     monkeypatch.setenv("SUCO_DENSE_STATS", "1")
     monkeypatch.setenv("SUCO_DENSE_BUF", "96")  # small batches would otherwise get whole-piece buffers
     full = oracle.clustered(40000 + 64, 16, 8, 77, 0, 100, 6, True)
@@ -341,10 +345,13 @@ def test_dense_buffer_overflow_falls_back(gpu, oracle, monkeypatch, capfd):
     base = np.delete(full, pick, axis=0)
     oidx = oracle.build_index(base, 4, 12, 3, 42, 0)
     idx = gpu.load_index(oidx.serialize(), base)
-    for a, b, k in ((0.2, 0.01, 10), (0.05, 0.02, 20)):
+    for a, b, k in ((0.2, 0.01, 10), (0.05, 0.02, 20), (0.05, 0.02, 40)):
         ids, dd = idx.knn_query_batch(qs, gpu.CollisionParams(a, b, k))
         oi, od, _ = oidx.knn_query_batch(base, qs, a, b, k)
         assert np.array_equal(ids, oi) and np.array_equal(dd, od), (a, b, k)
+        fi, fd = idx.knn_query_batch(qs.astype(np.float32) + np.float32(0.25), gpu.CollisionParams(a, b, k))
+        gi, gd, _ = oidx.knn_query_batch(base, qs.astype(np.float32) + np.float32(0.25), a, b, k)
+        assert np.array_equal(fi, gi) and np.array_equal(fd, gd), ("non-integer queries", a, b, k)
     err = capfd.readouterr().err
     flagged = [int(line.split("dense select: ")[1].split(" of")[0]) for line in err.splitlines()
                if "dense select:" in line]
@@ -384,10 +391,13 @@ def test_dense_half_width_overflow_falls_back(gpu, oracle, monkeypatch, capfd):
     qs, base = full[pick], np.delete(full, pick, axis=0)
     oidx = oracle.build_index(base, 4, 12, 3, 42, 0)
     idx = gpu.load_index(oidx.serialize(), base)
-    for a, b, k in ((0.2, 0.01, 10), (0.05, 0.02, 20)):
+    for a, b, k in ((0.2, 0.01, 10), (0.05, 0.02, 20), (0.05, 0.02, 40)):
         ids, dd = idx.knn_query_batch(qs, gpu.CollisionParams(a, b, k))
         oi, od, _ = oidx.knn_query_batch(base, qs, a, b, k)
         assert np.array_equal(ids, oi) and np.array_equal(dd, od), (a, b, k)
+        fi, fd = idx.knn_query_batch(qs.astype(np.float32) + np.float32(0.25), gpu.CollisionParams(a, b, k))
+        gi, gd, _ = oidx.knn_query_batch(base, qs.astype(np.float32) + np.float32(0.25), a, b, k)
+        assert np.array_equal(fi, gi) and np.array_equal(fd, gd), ("non-integer queries", a, b, k)
     err = capfd.readouterr().err
     flagged = [int(line.split("dense select: ")[1].split(" of")[0]) for line in err.splitlines()
                if "dense select:" in line]
