@@ -202,12 +202,16 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg2", choices=sorted(bench_data.CONFIGS))
+    ap.add_argument("--config", default="cfg4", choices=sorted(bench_data.CONFIGS),
+                    help="cfg4 (10M x 96, the largest BASELINE config with an N = 1 point) by default")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--index-source", default="gpu", choices=["gpu", "reference"],
                     help="gpu: suco_gpu_build_index (timed); reference: load the reference CPU build's bytes")
     ap.add_argument("--ref-sample", type=int, default=256, help="queries per step in the reference arm")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline query time (rank 0)")
+    ap.add_argument("--parity-queries", type=int, default=-1,
+                    help="queries re-checked against the reference after the timed run (-1: all of them for "
+                         "n <= 20M, the CPU-baseline sample otherwise)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="no L2 flush/e2e/cpu legs (for ncu)")
     ap.add_argument("--no-u8", action="store_true",
@@ -451,6 +455,18 @@ def main():
                 sample = int(min(nq, max(probe, args.cpu_seconds * probe / max(w, 1e-6))))
                 sel = np.arange(sample)
                 ri, rd, wall = ref_idx.knn_query_batch(base, queries[sel], cfg.alpha, cfg.beta, k, threads=0)
+                # parity beyond the timed sample: the rest of the batch (untimed), so every query of
+                # the step is checked against the reference (--parity-queries bounds it)
+                want = args.parity_queries if args.parity_queries >= 0 else (nq if cfg.n <= 20_000_000 else sample)
+                want = int(min(nq, max(want, sample)))
+                parity_s = wall
+                if want > sample:
+                    t0 = time.time()
+                    ri2, rd2, _ = ref_idx.knn_query_batch(base, queries[sample:want], cfg.alpha, cfg.beta, k,
+                                                          threads=0)
+                    parity_s += time.time() - t0
+                    ri, rd = np.concatenate([ri, ri2]), np.concatenate([rd, rd2])
+                    sel = np.arange(want)
                 built = (f"reference build_index over the {len(train):,}-row training sample (k-means only) "
                          f"{ref_build_s:.1f} s; queries on the GPU-built index loaded by the reference's load_index"
                          if sampled else f"reference build_index {ref_build_s:.1f} s")
@@ -458,8 +474,12 @@ def main():
                        "sample": f"first {sample} of {nq} {cfg.name} queries through the reference knn_query "
                                  f"(run_suco_batch parallel_chunks, {threads} threads); {built}",
                        "build_s": ref_build_s}
-                parity = {"checked_queries": sample, "ids_equal": bool(np.array_equal(ri, gpu_ids[sel])),
-                          "dists_equal": bool(np.array_equal(rd, gpu_d[sel]))}
+                parity = {"checked_queries": int(len(sel)), "of": nq,
+                          "ids_equal": bool(np.array_equal(ri, gpu_ids[sel])),
+                          "dists_equal": bool(np.array_equal(rd, gpu_d[sel])),
+                          "mismatched_queries": int(np.sum(np.any(ri != gpu_ids[sel], axis=1) |
+                                                           np.any(rd != gpu_d[sel], axis=1))),
+                          "reference_s": parity_s}
                 if sampled:
                     parity["centroids_equal_reference_sample_build"] = centroids_equal
                 elif args.index_source == "gpu":

@@ -57,7 +57,6 @@ struct SelectArgs {
     uint64_t nq;          // queries in this launch (persistent clusters loop over them)
     uint32_t* cands;      // nq x m (candidate set, unordered)
     uint8_t* scores_dbg;  // optional nq x n
-    long long* prof;      // optional debug phase timers (8 x u64)
     bool count_only;      // stop after counting (scores_dbg receives the scores): shard phase 1
     uint64_t scores_stride;  // row stride of scores_dbg (0 = n); a multiple of 16 enables 16-byte stores
     uint32_t* slab_hist;     // count_only: optional nq x nslabs x (ns + 2) copy of the slab histograms

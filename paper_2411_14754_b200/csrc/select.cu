@@ -61,18 +61,6 @@ constexpr uint32_t kSmemLimit = 232448;        // opt-in dynamic shared memory p
 
 __host__ __device__ inline uint32_t hist_stride(uint32_t ns) { return ns + 2; }
 
-// Debug phase timing (SelectArgs::prof != nullptr): thread 0 of every CTA adds
-// clock64 deltas per phase into prof[0..7].
-#define SEL_MARK(i)                                                                     \
-    do {                                                                                \
-        if (a.prof && threadIdx.x == 0) {                                               \
-            const long long now = clock64();                                            \
-            atomicAdd(reinterpret_cast<unsigned long long*>(a.prof) + (i),              \
-                      static_cast<unsigned long long>(now - t_mark));                   \
-            t_mark = now;                                                               \
-        }                                                                               \
-    } while (0)
-
 // Cluster-wide barrier with release/acquire at cluster scope (what DSMEM
 // visibility needs); cg::cluster_group::sync() additionally fences at GPU scope.
 __device__ __forceinline__ void cluster_barrier() {
@@ -193,29 +181,19 @@ struct Wave {
 };
 
 // Loads wave [ua, ub) of 32-id units (at most KU units): lane l takes id l of
-// each unit. BRANCHY skips invalid slots with a branch; otherwise every slot
-// is predicated (invalid slots re-read unit ua and issue no global load).
-template <int KU, bool BRANCHY>
+// each unit; every slot is predicated (invalid slots re-read unit ua and issue no
+// global load). Used by the generic (N_s > 32) counting loop.
+template <int KU>
 __device__ __forceinline__ void load_wave(const Smem& s, const uint32_t* ids, uint32_t ua, uint32_t ub, Wave<KU>& w) {
     const uint32_t lane = threadIdx.x & 31u;
     uint32_t mask = 0;
 #pragma unroll
     for (int u = 0; u < KU; ++u) {
-        if constexpr (BRANCHY) {
-            if (ua + u < ub) {
-                const uint2 d = s.udesc[ua + u];
-                if (lane < d.y) {
-                    w.id[u] = __ldg(ids + d.x + lane);
-                    mask |= 1u << u;
-                }
-            }
-        } else {
-            const uint32_t unit = ua + u < ub ? ua + u : ua;
-            const uint2 d = s.udesc[unit];  // (begin, count)
-            const bool ok = (ua + u < ub) && (lane < d.y);
-            w.id[u] = ok ? __ldg(ids + d.x + lane) : 0u;
-            mask |= static_cast<uint32_t>(ok) << u;
-        }
+        const uint32_t unit = ua + u < ub ? ua + u : ua;
+        const uint2 d = s.udesc[unit];  // (begin, count)
+        const bool ok = (ua + u < ub) && (lane < d.y);
+        w.id[u] = ok ? __ldg(ids + d.x + lane) : 0u;
+        mask |= static_cast<uint32_t>(ok) << u;
     }
     w.mask = mask;
 }
@@ -306,22 +284,6 @@ __device__ __forceinline__ void rmw_wave_lean(uint32_t cbase, uint32_t dummy, co
     for (int u = 0; u < KU; ++u) hist_add_lean<NSB>(ih, v[u]);
 }
 
-// Shared-memory atomic variant: safe across subspaces, so no barriers needed.
-template <int NSB, int KU>
-__device__ __forceinline__ void atomic_wave(const Smem& s, const Wave<KU>& w, uint32_t lo, IncHist<NSB>& ih,
-                                            uint32_t* hist) {
-    uint32_t* c32 = reinterpret_cast<uint32_t*>(s.cnt);
-#pragma unroll
-    for (int u = 0; u < KU; ++u) {
-        if (w.mask & (1u << u)) {
-            const uint32_t l = w.id[u] - lo;
-            const uint32_t sh = (l & 3u) * 8u;
-            const uint32_t old = atomicAdd(c32 + (l >> 2), 1u << sh);
-            ih.add(((old >> sh) & 0xffu) + 1u, hist);
-        }
-    }
-}
-
 template <int NSB, int KU>
 __device__ __forceinline__ void rmw_wave(const Smem& s, const Wave<KU>& w, uint32_t lo, IncHist<NSB>& ih,
                                          uint32_t* hist) {
@@ -350,9 +312,9 @@ __device__ __forceinline__ void rmw_wave(const Smem& s, const Wave<KU>& w, uint3
 // then does the counter RMWs, with the first wave of subspace s+1 already in
 // flight while subspace s does its RMWs. A barrier separates subspaces (an id
 // repeats only across subspaces).
-template <int NSB, int KU, bool BRANCHY, bool PREFETCH, bool ATOMIC = false>
+template <int NSB, int KU>
 __device__ void count_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint32_t slab, uint64_t lo, uint32_t len,
-                           uint32_t* hist, long long& t_mark) {
+                           uint32_t* hist) {
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     uint4* c4 = reinterpret_cast<uint4*>(s.cnt);
     for (uint32_t i = tid; i < a.CH / 16; i += kThreads) c4[i] = make_uint4(0, 0, 0, 0);
@@ -366,12 +328,11 @@ __device__ void count_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint3
         s.sub_start[a.ns] = acc;
     }
     __syncthreads();
-    SEL_MARK(0);
     if (len == 0) return;
     const uint32_t TC = s.sub_start[a.ns];
     const uint32_t stride = a.nslabs + 1;
     // lean waves address ids by one 32-bit offset into the N_s x n array when it fits
-    const bool abs_ids = !BRANCHY && !PREFETCH && !ATOMIC && NSB > 0 && static_cast<uint64_t>(a.ns) * a.n <= 0xffffffffull;
+    const bool abs_ids = NSB > 0 && static_cast<uint64_t>(a.ns) * a.n <= 0xffffffffull;
     IncHist<NSB> ih;
     ih.clear();
     uint32_t waves_since_flush = 0;
@@ -398,7 +359,6 @@ __device__ void count_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint3
         }
         uint32_t UT;
         const uint32_t up0 = block_excl_scan(nu4[0] + nu4[1] + nu4[2] + nu4[3], s.wtmp, &UT);
-        SEL_MARK(1);
         // unit index where each subspace starts within this chunk
         {
             uint32_t up = up0, sb2 = sub_first;
@@ -448,74 +408,7 @@ __device__ void count_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint3
                 ua = A + static_cast<uint32_t>((static_cast<uint64_t>(T) * warp) / kWarps);
                 ub = A + static_cast<uint32_t>((static_cast<uint64_t>(T) * (warp + 1)) / kWarps);
             };
-            if constexpr (ATOMIC) {
-                // all units of the window as one flat list split over the warps; 2-deep pipeline
-                const uint32_t nu = u1 - u0;
-                const uint32_t wa = static_cast<uint32_t>((static_cast<uint64_t>(nu) * warp) / kWarps);
-                const uint32_t wb = static_cast<uint32_t>((static_cast<uint64_t>(nu) * (warp + 1)) / kWarps);
-                // units never straddle subspaces; find each wave's subspace by its first unit
-                auto ids_of = [&](uint32_t unit) {
-                    uint32_t sb4 = sb;
-                    while (sb4 + 1 < se && s.sub_unit[sb4 + 1] <= unit + u0) ++sb4;
-                    return a.ids + static_cast<uint64_t>(sb4) * a.n;
-                };
-                for (uint32_t ua = wa; ua < wb; ua += KU) {
-                    // a wave may cross a subspace boundary: split it
-                    uint32_t ub = min(wb, ua + KU);
-                    const uint32_t* ids = ids_of(ua);
-                    uint32_t sb4 = sb;
-                    while (sb4 + 1 < se && s.sub_unit[sb4 + 1] <= ua + u0) ++sb4;
-                    if (sb4 + 1 < se && s.sub_unit[sb4 + 1] - u0 < ub) ub = s.sub_unit[sb4 + 1] - u0;
-                    Wave<KU> w;
-                    load_wave<KU, BRANCHY>(s, ids, ua, ub, w);
-                    atomic_wave<NSB, KU>(s, w, static_cast<uint32_t>(lo), ih, hist);
-                    ua = ub - KU;  // resume right after the split point
-                    if (++waves_since_flush * KU >= 240) {
-                        ih.flush(hist, a.ns);
-                        waves_since_flush = 0;
-                    }
-                }
-                __syncthreads();
-            } else if constexpr (PREFETCH) {
-                Wave<KU> cur, nxt;
-                uint32_t ua, ub;
-                range(sb, ua, ub);
-                const uint32_t* ids = a.ids + static_cast<uint64_t>(sb) * a.n;
-                load_wave<KU, BRANCHY>(s, ids, ua, ub, cur);
-                for (uint32_t sb3 = sb; sb3 < se; ++sb3) {
-                    for (;;) {
-                        const uint32_t nua = ua + KU;
-                        const bool more = nua < ub;
-                        if (more) {
-                            load_wave<KU, BRANCHY>(s, ids, nua, ub, nxt);
-                        } else if (sb3 + 1 < se) {
-                            uint32_t ua2, ub2;
-                            range(sb3 + 1, ua2, ub2);
-                            const uint32_t* ids2 = a.ids + static_cast<uint64_t>(sb3 + 1) * a.n;
-                            load_wave<KU, BRANCHY>(s, ids2, ua2, ub2, nxt);
-                            rmw_wave<NSB, KU>(s, cur, static_cast<uint32_t>(lo), ih, hist);
-                            cur = nxt;
-                            ids = ids2;
-                            ua = ua2;
-                            ub = ub2;
-                            break;
-                        }
-                        rmw_wave<NSB, KU>(s, cur, static_cast<uint32_t>(lo), ih, hist);
-                        if (++waves_since_flush * KU >= 240) {
-                            ih.flush(hist, a.ns);
-                            waves_since_flush = 0;
-                        }
-                        if (!more) break;
-                        cur = nxt;
-                        ua = nua;
-                    }
-                    if (++waves_since_flush * KU >= 240) {
-                        ih.flush(hist, a.ns);
-                        waves_since_flush = 0;
-                    }
-                    __syncthreads();  // counters of sb3 final before sb3 + 1 increments
-                }
-            } else if constexpr (!BRANCHY && NSB > 0) {
+            if constexpr (NSB > 0) {
                 // lean waves (a wave is loaded then RMW'd; one barrier per subspace). Measured
                 // slower: carrying the next subspace's first wave over the barrier (register
                 // pressure) and an mbarrier split arrive/wait (1024 threads polling).
@@ -536,9 +429,7 @@ __device__ void count_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint3
                             waves_since_flush = 0;
                         }
                     }
-                    SEL_MARK(8);  // warp 0's own load+RMW work for this subspace
                     __syncthreads();  // counters of sb3 final before sb3 + 1 increments
-                    SEL_MARK(9);  // waiting for the slowest warp
                 }
             } else {
                 for (uint32_t sb3 = sb; sb3 < se; ++sb3) {
@@ -547,23 +438,20 @@ __device__ void count_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint3
                     const uint32_t* ids = a.ids + static_cast<uint64_t>(sb3) * a.n;
                     for (uint32_t u0 = ua; u0 < ub; u0 += KU) {
                         Wave<KU> w;
-                        load_wave<KU, BRANCHY>(s, ids, u0, ub, w);
+                        load_wave<KU>(s, ids, u0, ub, w);
                         rmw_wave<NSB, KU>(s, w, static_cast<uint32_t>(lo), ih, hist);
                         if (++waves_since_flush * KU >= 240) {
                             ih.flush(hist, a.ns);
                             waves_since_flush = 0;
                         }
                     }
-                    SEL_MARK(8);  // warp 0's own load+RMW work for this subspace
                     __syncthreads();  // counters of sb3 final before sb3 + 1 increments
-                    SEL_MARK(9);  // waiting for the slowest warp
                 }
             }
         }
     }
     ih.flush(hist, a.ns);
     __syncthreads();
-    SEL_MARK(2);
 }
 
 // Mask (0x80 per byte) of the bytes of word `wi` that are >= t and inside the slab.
@@ -590,7 +478,7 @@ __device__ __forceinline__ uint32_t sel_mask(uint32_t w, uint32_t wi, uint32_t t
 // the slab where the tie quota is cut needs id order, and only for its ties,
 // which a two-pass warp-ordered scan emits after the unordered region.
 __device__ void emit_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint64_t lo, uint32_t len, uint32_t T,
-                          uint32_t quota, uint32_t base, uint32_t gt, uint32_t ties, bool swar, long long& t_mark) {
+                          uint32_t quota, uint32_t base, uint32_t gt, uint32_t ties, bool swar) {
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t* w32 = reinterpret_cast<const uint32_t*>(s.cnt);
     const uint4* w128 = reinterpret_cast<const uint4*>(s.cnt);
@@ -669,7 +557,6 @@ __device__ void emit_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint64
             }
         }
     }
-    SEL_MARK(5);
     if (all_ties || quota == 0) return;
     // boundary slab: the first `quota` ties (== T) in id order, after the gt
     // region. Warps own contiguous vector ranges; lanes step over 16-counter
@@ -733,7 +620,7 @@ __device__ void emit_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint64
     }
 }
 
-template <int NSB, int KU = 4, bool BRANCHY = false, bool PREFETCH = false, bool ATOMIC = false>
+template <int NSB, int KU = 4>
 __global__ void __launch_bounds__(kThreads, SUCO_SELECT_MINB) select_kernel(SelectArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     cg::cluster_group cluster = cg::this_cluster();
@@ -745,14 +632,13 @@ __global__ void __launch_bounds__(kThreads, SUCO_SELECT_MINB) select_kernel(Sele
     // persistent clusters: cluster c handles queries c, c + C, c + 2C, ...
     const uint64_t nclusters = gridDim.x / a.CS;
     for (uint64_t q = blockIdx.x / a.CS; q < a.nq; q += nclusters) {
-        long long t_mark = a.prof ? clock64() : 0;
 
         // pass 1: count + histogram every owned slab
         for (uint32_t r = 0; r < a.rounds; ++r) {
             const uint32_t slab = r * a.CS + rank;
             const uint64_t lo = static_cast<uint64_t>(slab) * a.CH;
             const uint32_t len = slab < a.nslabs ? static_cast<uint32_t>(min_u64(a.CH, a.n - lo)) : 0u;
-            count_slab<NSB, KU, BRANCHY, PREFETCH, ATOMIC>(a, s, q, slab, lo, len, s.hist + r * hs, t_mark);
+            count_slab<NSB, KU>(a, s, q, slab, lo, len, s.hist + r * hs);
             if (a.scores_dbg) {
                 const uint64_t ss = a.scores_stride ? a.scores_stride : a.n;
                 uint8_t* dst = a.scores_dbg + q * ss + lo;
@@ -782,7 +668,6 @@ __global__ void __launch_bounds__(kThreads, SUCO_SELECT_MINB) select_kernel(Sele
             continue;
         }
         cluster_barrier();
-        SEL_MARK(3);
 
         // threshold and per-slab quotas (warp 0), from every slab's histogram
         if (warp == 0) {
@@ -879,7 +764,6 @@ __global__ void __launch_bounds__(kThreads, SUCO_SELECT_MINB) select_kernel(Sele
             if (lane == 0) s.misc[0] = T;
         }
         cluster_barrier();  // peers finished reading our histograms
-        SEL_MARK(4);
         const uint32_t T = s.misc[0];
 
         for (uint32_t r = 0; r < a.rounds; ++r) {
@@ -888,12 +772,11 @@ __global__ void __launch_bounds__(kThreads, SUCO_SELECT_MINB) select_kernel(Sele
             const uint64_t lo = static_cast<uint64_t>(slab) * a.CH;
             const uint32_t len = static_cast<uint32_t>(min_u64(a.CH, a.n - lo));
             if (a.rounds > 1) {
-                count_slab<NSB, KU, BRANCHY, PREFETCH, ATOMIC>(a, s, q, slab, lo, len, s.hscratch, t_mark);  // recount
+                count_slab<NSB, KU>(a, s, q, slab, lo, len, s.hscratch);  // recount
             }
             const uint32_t* h = s.hist + r * hs;
             const uint32_t gt = T + 1 <= a.ns ? h[T + 1] : 0u;
-            emit_slab(a, s, q, lo, len, T, s.rquota[r], s.roff[r], gt, h[T] - gt, swar, t_mark);
-            SEL_MARK(6);
+            emit_slab(a, s, q, lo, len, T, s.rquota[r], s.roff[r], gt, h[T] - gt, swar);
             __syncthreads();
         }
     }
@@ -925,35 +808,8 @@ __global__ void slab_offsets_kernel(const uint32_t* cell_off, const uint32_t* id
 using SelectFn = void (*)(SelectArgs);
 
 template <int NSB>
-SelectFn pick_variant() {
-    // SUCO_SELECT_VARIANT="KU,BRANCHY,PREFETCH" (tuning knob; N_s <= 8 only)
-    if constexpr (NSB == 8) {
-        const char* v = std::getenv("SUCO_SELECT_VARIANT");
-        if (v) {
-            int ku = 16, br = 1, pf = 1, at = 0;
-            std::sscanf(v, "%d,%d,%d,%d", &ku, &br, &pf, &at);
-            if (at) return ku == 8 ? select_kernel<8, 8, true, false, true> : select_kernel<8, 16, true, false, true>;
-            if (ku == 4) return select_kernel<8, 4, false, false>;
-            if (ku == 2) return select_kernel<8, 2, false, false>;
-            const int key = (ku == 8 ? 0 : 4) | (br ? 2 : 0) | (pf ? 1 : 0);
-            switch (key) {
-                case 0: return select_kernel<8, 8, false, false>;
-                case 1: return select_kernel<8, 8, false, true>;
-                case 2: return select_kernel<8, 8, true, false>;
-                case 3: return select_kernel<8, 8, true, true>;
-                case 4: return select_kernel<8, 16, false, false>;
-                case 5: return select_kernel<8, 16, false, true>;
-                case 6: return select_kernel<8, 16, true, false>;
-                default: return select_kernel<8, 16, true, true>;
-            }
-        }
-    }
-    return select_kernel<NSB>;
-}
-
-template <int NSB>
 cudaError_t launch_select_t(const SelectArgs& a, const SelectConfig& cfg, uint64_t nq, cudaStream_t st) {
-    const SelectFn fn = pick_variant<NSB>();
+    const SelectFn fn = select_kernel<NSB>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cfg.smem));
     if (e != cudaSuccess) return e;
     if (cfg.CS > 8) {
@@ -1085,27 +941,8 @@ SelectConfig plan_select(uint64_t n, uint32_t ns, int cluster_size) {
     return best;
 }
 
-cudaError_t launch_select(const SelectArgs& a0, const SelectConfig& cfg, uint64_t nq, cudaStream_t st) {
+cudaError_t launch_select(const SelectArgs& a, const SelectConfig& cfg, uint64_t nq, cudaStream_t st) {
     if (nq == 0) return cudaSuccess;
-    SelectArgs a = a0;
-    unsigned long long* prof = nullptr;
-    if (std::getenv("SUCO_SELECT_PROF")) {  // debug: per-phase clock64 totals to stderr
-        cudaMalloc(&prof, 128);
-        cudaMemsetAsync(prof, 0, 128, st);
-        a.prof = reinterpret_cast<long long*>(prof);
-        cudaError_t e = launch_select_dispatch(a, cfg, nq, st);
-        unsigned long long h[16];
-        cudaMemcpyAsync(h, prof, 128, cudaMemcpyDeviceToHost, st);
-        cudaStreamSynchronize(st);
-        cudaFree(prof);
-        const double ctas = double(nq) * cfg.CS;
-        std::fprintf(stderr, "[select prof] cycles per CTA: zero+init %.0f staging %.0f counting %.0f csync1 %.0f quota+csync2 %.0f emit-unordered %.0f emit-ordered(boundary) %.0f\n",
-                     h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas, h[4] / ctas, h[5] / ctas, h[6] / ctas);
-        std::fprintf(stderr, "[select prof] counting split: warp0 own waves %.0f, subspace barrier waits %.0f (remaining = staging tail/descriptors/flush)\n",
-                     h[8] / ctas, h[9] / ctas);
-
-        return e;
-    }
     return launch_select_dispatch(a, cfg, nq, st);
 }
 
