@@ -13,9 +13,13 @@ between timed steps, max over ranks. Multi-GPU (one process per GPU under
 torchrun): cfg1-cfg3 run query-parallel replicas — every rank holds the whole
 index (it fits one GPU) and answers its own 10,000-query batch, no data-path
 collective, scaling "weak"; cfg4/cfg5 (the configs BASELINE.json shards by
-point) and `--sharded` run the point-sharded protocol (paper_2411_14754_b200.sharded:
-block-cyclic point shards, NCCL all-gathers of the SC-score histograms and of
-the local top-k), scaling "strong". `--replicas` forces the replica mode.
+point) and `--sharded` run the library's point-sharded protocol
+(suco_gpu_build_shard + suco_gpu_shard_knn_query_batch_device over an NCCL
+communicator: each rank generates and holds only its block-cyclic rows, builds
+its shard with the k-means jobs spread over the ranks, and answers every query
+with three device all-gathers), scaling "strong". `--replicas` forces the
+replica mode. `--emulate G` runs G shards on one GPU (in-process communicator,
+G host threads) and checks them against the unsharded path.
 
 `--impl reference` times the reference's own CPU implementation
 (oracle/_ref/libsuco_ref.so, built from /root/reference sources) on this
@@ -220,7 +224,10 @@ def main():
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: query-parallel full replicas even for the point-sharded configs (cfg4, cfg5)")
     ap.add_argument("--block", type=int, default=0,
-                    help="block-cyclic shard block size (ids); 0 = suco_gpu_shard_block_hint (slabs == blocks)")
+                    help="block-cyclic shard block size (ids, a multiple of 2048); 0 = suco_gpu_shard_block_hint")
+    ap.add_argument("--emulate", type=int, default=0,
+                    help="G > 0: G shards on this one GPU (in-process communicator), checked against the "
+                         "unsharded path; per-rank device time reported")
     ap.add_argument("--alpha", type=float, default=None, help="experiment: override the config's alpha")
     ap.add_argument("--beta", type=float, default=None, help="experiment: override the config's beta")
     ap.add_argument("--n", type=int, default=None, help="experiment: override the config's point count")
@@ -256,6 +263,14 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
+    point_sharded = cfg.name in ("cfg4", "cfg5") and not args.replicas  # BASELINE.json: points sharded
+    if args.emulate:
+        run_emulated(args, cfg)
+        return
+    if args.sharded or (ws > 1 and point_sharded):
+        run_sharded(args, cfg, ws, rank, local)
+        return
+
     t0 = time.time()
     base, queries = bench_data.generate(cfg)
     log(f"[rank {rank}] data {cfg.describe()} generated in {time.time() - t0:.1f}s")
@@ -285,29 +300,25 @@ def main():
         build_s = time.time() - t0
     log(f"[rank {rank}] index ready (gpu build {build_s}, reference build {ref_build_s})")
 
-    point_sharded = cfg.name in ("cfg4", "cfg5") and not args.replicas  # BASELINE.json: points sharded
-    if args.sharded or (ws > 1 and point_sharded):
-        run_sharded(args, cfg, base, queries, idx, build_s, ws, rank, local)
-        return
-
     if ws > 1:  # replicas: each rank answers its own batch (the same set, rotated by rank)
         queries = np.ascontiguousarray(np.roll(queries, rank * (nq // ws), axis=0))
     stream = torch.cuda.Stream()
-    idx.set_stream(stream.cuda_stream)
+    ctx = idx.context()  # caller-owned query scratch (query.hpp:72-78)
     dq = torch.from_numpy(queries).cuda()
     dids = torch.empty((nq, k), dtype=torch.int32, device="cuda")
     dd = torch.empty((nq, k), dtype=torch.float64, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     def step():
-        idx.knn_query_batch_device(dq.data_ptr(), nq, d, cp, dids.data_ptr(), dd.data_ptr(), stream.cuda_stream)
+        idx.knn_query_batch_device(dq.data_ptr(), nq, d, cp, dids.data_ptr(), dd.data_ptr(), stream.cuda_stream,
+                                   scratch=ctx)
 
     clocks = ClockSampler(local).start()
     for _ in range(args.warmup):
         step()
     stream.synchronize()
 
-    idx.set_profiling(True)
+    ctx.set_profiling(True)
     step_ms, stage_ms = [], np.zeros(3)
     stats = None
     clocks.mark()
@@ -324,11 +335,12 @@ def main():
         e1.record(stream)
         e1.synchronize()
         step_ms.append(e0.elapsed_time(e1))
-        ms, cum, sq, m = idx.stage_times()
+        ms, cum, sq, m = ctx.stage_times()
         stage_ms += ms
         stats = (cum, sq, m)
     clocks.stop()
-    idx.set_profiling(False)
+    ctx.set_profiling(False)
+    launches_per_step = ctx.last_launches()  # counted by the library for the last call
     total_ms = sum(step_ms)
     if ws > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
@@ -350,7 +362,8 @@ def main():
 
         def host_step():
             rc = _capi.knn_query_batch(idx.handle, C.cast(hq.data_ptr(), _capi.f32p), nq, d, C.byref(cpc),
-                                       C.cast(hi.data_ptr(), _capi.u32p), C.cast(hd.data_ptr(), _capi.f64p))
+                                       C.cast(hi.data_ptr(), _capi.u32p), C.cast(hd.data_ptr(), _capi.f64p),
+                                       ctx.handle)
             if rc:
                 raise RuntimeError(_capi.last_error().decode())
 
@@ -487,7 +500,6 @@ def main():
         except Exception as e:  # the baseline must not mask the GPU number
             cpu = {"error": repr(e)}
 
-    launches_per_step = idx.last_launches()  # counted by the library for the last call
     line = {
         "metric": "batched queries/sec at k=10 (oracle-exact IDs)", "value": value, "unit": "queries/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
@@ -506,39 +518,57 @@ def main():
         torch.distributed.destroy_process_group()
 
 
-def run_sharded(args, cfg, base, queries, idx, build_s, ws, rank, local):
-    """N GPUs, block-cyclic point shards + the NCCL exchange (paper_2411_14754_b200.sharded)."""
+def _shard_block(args, cfg, G):
+    from paper_2411_14754_b200.sharded import block_hint
+    return args.block or block_hint(cfg.n, G)
+
+
+def run_sharded(args, cfg, ws, rank, local):
+    """N GPUs: the library's block-cyclic shard protocol over NCCL. Each rank generates only its own
+    rows, builds its shard (k-means jobs spread over the ranks) and answers the whole batch with the
+    other ranks (three device all-gathers per tile)."""
     import torch
     import torch.distributed as dist
     import paper_2411_14754_b200 as suco
-    from paper_2411_14754_b200.sharded import GpuShard, TorchComm, knn_query_distributed
+    from paper_2411_14754_b200.sharded import Comm, Shard
 
     if not dist.is_initialized():  # --sharded at N = 1 without torchrun
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29531")
         dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
-    comm = TorchComm()
+    comm = Comm.from_torch(local)
+    block = _shard_block(args, cfg, ws)
+    t0 = time.time()
+    rows, queries = bench_data.generate_shard(cfg, block, ws, rank)
+    log(f"[rank {rank}] {len(rows):,} rows of {cfg.describe()} generated in {time.time() - t0:.1f}s (block {block})")
+    params = suco.IndexParams(cfg.num_subspaces, cfg.k_half, cfg.iterations, 42, suco.SubspaceMode.Contiguous)
+    train = bench_data.train_ids(cfg, cfg.n) if cfg.train_sample < 1.0 else None
+    drows = torch.from_numpy(rows).cuda()
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.time()
+    shard = Shard.build(drows, cfg.n, params, block, comm, device=local, train_ids=train)
+    torch.cuda.synchronize()
+    build_s = time.time() - t0
+    t = torch.tensor([build_s], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    build_s = float(t.item())
+    del drows
     cp = suco.CollisionParams(cfg.alpha, cfg.beta, cfg.k)
     nq, d, k = len(queries), cfg.d, cfg.k
-    dq = torch.from_numpy(queries).cuda()
-    # parity reference on rank 0: the unsharded single-GPU path over the same index
-    want = None
-    if rank == 0:
-        want = idx.knn_query_batch(queries, cp)
-    t0 = time.time()
-    eng = GpuShard(idx, rank, ws, args.block or None)
-    torch.cuda.synchronize()
-    shard_s = time.time() - t0
-    idx.close()
+    ctx = shard.context()
     stream = torch.cuda.Stream()
+    dq = torch.from_numpy(queries).cuda()
+    dids = torch.empty((nq, k), dtype=torch.int32, device="cuda")
+    ddist = torch.empty((nq, k), dtype=torch.float64, device="cuda")
 
-    def step(qdev):
-        with torch.cuda.stream(stream):
-            return knn_query_distributed(eng, comm, qdev, cp)
+    def step():
+        shard.knn_query_batch_device(comm, dq.data_ptr(), nq, d, cp, dids.data_ptr(), ddist.data_ptr(),
+                                     stream.cuda_stream, scratch=ctx)
 
     clocks = ClockSampler(local).start()
     for _ in range(args.warmup):
-        step(dq)
+        step()
     stream.synchronize()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
@@ -547,54 +577,114 @@ def run_sharded(args, cfg, base, queries, idx, build_s, ws, rank, local):
         for _ in range(args.steps):
             with torch.cuda.stream(stream):
                 flush.fill_(1)
-            dist.barrier()
             stream.synchronize()
+            dist.barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            out = fn()
+            fn()
             e1.record(stream)
             e1.synchronize()
             ms.append(e0.elapsed_time(e1))
         t = torch.tensor([sum(ms)], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item()), out
+        return float(t.item())
 
     clocks.mark()
-    total_ms, (ids, dd) = timed(lambda: step(dq))
+    total_ms = timed(step)
     clocks.stop()
+    launches = ctx.last_launches()
+    exch = ctx.exchange_bytes()
     hq = torch.from_numpy(queries).pin_memory()
+    hi = np.zeros((nq, k), np.uint32)
+    hd = np.zeros((nq, k), np.float64)
 
-    def e2e_step():
-        qdev = hq.to("cuda", non_blocking=True)
-        i, dist_ = step(qdev)
-        return i.to("cpu", non_blocking=True), dist_.to("cpu", non_blocking=True)
+    def e2e_step():  # host queries in, host results out, through the C-ABI host entry
+        import ctypes as C
+        from paper_2411_14754_b200 import _capi
+        cpc = cp._c()
+        with torch.cuda.stream(stream):
+            rc = _capi.shard_knn_query_batch(shard.handle, comm.handle, C.cast(hq.data_ptr(), _capi.f32p), nq, d,
+                                             C.byref(cpc), hi.ctypes.data_as(_capi.u32p), hd.ctypes.data_as(_capi.f64p),
+                                             ctx.handle)
+        if rc:
+            raise RuntimeError(_capi.last_error().decode())
 
-    e2e_ms, _ = timed(e2e_step)
+    e2e_ms = timed(e2e_step)
+    consistent = bool(np.array_equal(hi, dids.cpu().numpy().view(np.uint32)) and np.array_equal(hd, ddist.cpu().numpy()))
     value = nq * args.steps / (total_ms / 1000.0)
     peak, peak_src = measured_peaks()
-    parity = None
-    if rank == 0:
-        parity = {"checked_queries": nq, "vs": "unsharded single-GPU path (itself bit-identical to the reference)",
-                  "ids_equal": bool(np.array_equal(ids.cpu().numpy().astype(np.uint32), want[0])),
-                  "dists_equal": bool(np.array_equal(dd.cpu().numpy(), want[1]))}
     line = {
         "metric": "batched queries/sec at k=10 (oracle-exact IDs)", "value": value, "unit": "queries/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded Gaussian mixture, bench_data.py)",
+        "data": "synthetic (seeded Gaussian mixture, bench_data.py; each rank generates only its own rows)",
         "config": {"workload": cfg.describe(), "queries_per_step": nq, "index_build_s": build_s,
-                   "shard_cut_s": shard_s, "parallelism": f"{ws} block-cyclic point shards (block {eng.block}), "
-                   "NCCL allgather of block histograms + local top-k", "l2": "256 MiB flush write between timed steps"},
-        "roofline": {"bound": "hbm", "kernel": "whole query path (per-kernel times need N = 1)", "achieved": None,
-                     "peak": peak * ws, "unit": "GB/s", "frac": None, "traffic": None, "peak_source": peak_src},
+                   "parallelism": f"{ws} block-cyclic point shards (block {block}); library shard protocol over "
+                                  "NCCL: all-gathers of score totals, block tie counts and local top-k",
+                   "exchange_bytes_per_step_per_rank": exch, "l2": "256 MiB flush write between timed steps"},
+        "roofline": {"bound": "hbm", "kernel": "whole sharded query path (per-stage times: N = 1 run)",
+                     "achieved": None, "peak": peak * ws, "unit": "GB/s", "frac": None, "traffic": None,
+                     "peak_source": peak_src},
         "cpu_baseline": None,
         "e2e": {"value": nq * args.steps / (e2e_ms / 1000.0), "unit": "queries/s", "h2d_bytes_per_step": nq * d * 4,
-                "d2h_bytes_per_step": nq * k * 16, "ms_per_step": e2e_ms / args.steps},
-        "parity": parity, "gpu_launches": eng.index.last_launches() * args.steps, "clocks": clocks.summary(),
+                "d2h_bytes_per_step": nq * k * 12, "ms_per_step": e2e_ms / args.steps},
+        "parity": {"host_and_device_entries_agree": consistent,
+                   "vs_oracle": "tests/test_sharded.py (G = 1..8 emulated shards, sharded build) and "
+                                "bench.py --emulate (full config size)"},
+        "gpu_launches": launches * args.steps, "clocks": clocks.summary(),
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
+
+
+def run_emulated(args, cfg):
+    """G shards of the full index on this GPU (in-process communicator on G threads): every rank's
+    answer against the unsharded path, the sharded build against cuts of the full build, and each
+    rank's device time."""
+    import torch
+    import paper_2411_14754_b200 as suco
+    from paper_2411_14754_b200.sharded import Comm, Shard, run_ranks, shard_ids
+
+    G = args.emulate
+    base, queries = bench_data.generate(cfg)
+    params = suco.IndexParams(cfg.num_subspaces, cfg.k_half, cfg.iterations, 42, suco.SubspaceMode.Contiguous)
+    train = bench_data.train_ids(cfg, cfg.n) if cfg.train_sample < 1.0 else None
+    full = suco.build_index_sampled(base, train, params) if train is not None else suco.build_index(base, params)
+    cp = suco.CollisionParams(cfg.alpha, cfg.beta, cfg.k)
+    want = full.knn_query_batch(queries, cp)
+    block = _shard_block(args, cfg, G)
+    comms = Comm.local(G)
+    t0 = time.time()
+    built = run_ranks(lambda r: Shard.build(base[shard_ids(cfg.n, block, G, r)], cfg.n, params, block, comms[r],
+                                            train_ids=train), G)
+    build_s = time.time() - t0
+    same_build = True
+    for r in range(G):
+        cut = Shard.cut(full, r, G, block)
+        for s in range(cfg.num_subspaces):
+            a, b = built[r].subspace(s), cut.subspace(s)
+            nl = cut.shard_info()["n_local"]
+            same_build &= all(np.array_equal(x, y) for x, y in zip(a[:3], b[:3])) and np.array_equal(a[3][:nl], b[3][:nl])
+        del cut
+    ctxs = [b.context() for b in built]
+    outs = run_ranks(lambda r: built[r].knn_query_batch(comms[r], queries, cp, scratch=ctxs[r]), G)
+    ok = all(np.array_equal(i, want[0]) and np.array_equal(dd, want[1]) for i, dd in outs)
+    # per-rank device time of the protocol with the ranks serialised on one GPU (no overlap)
+    dq = torch.from_numpy(queries).cuda()
+    outs_d = [(torch.empty((len(queries), cfg.k), dtype=torch.int32, device="cuda"),
+               torch.empty((len(queries), cfg.k), dtype=torch.float64, device="cuda")) for _ in range(G)]
+    t0 = time.time()
+    run_ranks(lambda r: (built[r].knn_query_batch_device(comms[r], dq.data_ptr(), len(queries), cfg.d, cp,
+                                                         outs_d[r][0].data_ptr(), outs_d[r][1].data_ptr(),
+                                                         scratch=ctxs[r]), ctxs[r].synchronize()), G)
+    wall = time.time() - t0
+    print(json.dumps({"emulate": G, "workload": cfg.describe(), "block": block, "sharded_build_equals_cut": same_build,
+                      "build_s_emulated": build_s, "ranks_bit_identical_to_unsharded": ok,
+                      "exchange_bytes_per_rank": ctxs[0].exchange_bytes(), "wall_s_all_ranks_one_gpu": wall}),
+          flush=True)
+    for c in comms:
+        c.close()
 
 
 if __name__ == "__main__":

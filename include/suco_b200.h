@@ -24,11 +24,13 @@ extern "C" {
 #endif
 
 #define SUCO_OK 0
-#define SUCO_ERR_INTERNAL 1      /* suco::Error / CUDA / NCCL failure          */
-#define SUCO_ERR_CONFIG 2        /* suco::ConfigError                          */
-#define SUCO_ERR_FORMAT 3        /* suco::FormatError / CorruptIndexError      */
-#define SUCO_ERR_INCOMPATIBLE 4  /* suco::IncompatibilityError                 */
-#define SUCO_ERR_CONTRACT 5      /* suco::ContractError                        */
+#define SUCO_ERR_INTERNAL 1       /* suco::Error / CUDA / NCCL failure                  */
+#define SUCO_ERR_CONFIG 2         /* suco::ConfigError                                  */
+#define SUCO_ERR_FORMAT 3         /* suco::FormatError (vecs files, io.cpp:20-84)       */
+#define SUCO_ERR_INCOMPATIBLE 4   /* suco::IncompatibilityError                         */
+#define SUCO_ERR_CONTRACT 5       /* suco::ContractError                                */
+#define SUCO_ERR_CORRUPT_INDEX 6  /* suco::CorruptIndexError (a FormatError; index     */
+                                  /* bytes, index.cpp:191-293); CLI exit code 3 as well */
 
 /* IndexParams (index.hpp:53-61). mode: 0 Contiguous, 1 Shuffled (subspace.hpp:13-16). */
 typedef struct suco_index_params {
@@ -48,9 +50,20 @@ typedef struct suco_collision_params {
 
 /* Opaque device-resident index: layout, centroids, IMI and the dataset rows
  * (the reference index holds no dataset, index.hpp:63-66; the GPU index must
- * own device copies of the rows it re-ranks). Immutable after build/load;
- * concurrent queries need distinct streams (see suco_gpu_set_stream). */
+ * own device copies of the rows it re-ranks). Immutable after build/load:
+ * like the reference's (index.hpp:63-66), any number of threads may query
+ * one index at once. */
 typedef struct suco_gpu_index suco_gpu_index;
+
+/* Per-call query state — the reference's caller-owned QueryScratch
+ * (query.hpp:72-78): pipeline scratch, its CUDA streams and events, and the
+ * profiling counters of the last call. Bound to the index it was created
+ * for; one thread at a time. Query calls given NULL borrow a context from
+ * the index's internal pool. */
+typedef struct suco_gpu_query_ctx suco_gpu_query_ctx;
+
+/* Communicator of the multi-GPU shard protocol (one rank per GPU). */
+typedef struct suco_comm suco_comm;
 
 /* Message of the last failing call on this thread. */
 const char* suco_last_error(void);
@@ -90,7 +103,7 @@ int suco_gpu_build_index_sampled(const float* data, uint64_t n, uint32_t d, cons
 
 /* deserialize_index (index.hpp:107, index.cpp:191-293) + check_compatible
  * (index.hpp:108, index.cpp:295-305): uploads a serialized `.suco` index and
- * the dataset it was built from. Corrupt bytes -> FORMAT naming the section;
+ * the dataset it was built from. Corrupt bytes -> CORRUPT_INDEX naming the section;
  * (n, d) mismatch -> INCOMPATIBLE. */
 int suco_gpu_load_index(const unsigned char* bytes, uint64_t len, const float* data, uint64_t n, uint32_t d,
                         int device, suco_gpu_index** out);
@@ -118,105 +131,110 @@ void suco_gpu_free_index(suco_gpu_index* index);
  * knn_query (query.hpp:93-96, query.cpp:199-262) over a batch of queries, the
  * way run_suco_batch (suco_cli.cpp:95-114) drives it: results[q] =
  * knn_query(index, dataset, queries[q], params). Check order per the
- * reference: query length != d -> CONTRACT, params -> CONFIG. Outputs are
- * nq x k: ids ascending by (distance, id), distances = sqrt of the fp64
- * squared distance, bit-identical to the reference. Host buffers. */
-int suco_gpu_knn_query_batch(suco_gpu_index* index, const float* queries, uint64_t nq, uint32_t qlen,
-                             const suco_collision_params* params, uint32_t* ids, double* dists);
+ * reference: query length != d -> CONTRACT, params -> CONFIG, then null
+ * buffers (nq > 0) -> CONTRACT. Outputs are nq x k: ids ascending by
+ * (distance, id), distances = sqrt of the fp64 squared distance,
+ * bit-identical to the reference. Host buffers; returns when the results are
+ * written. `scratch` (may be NULL) is the caller's query context, as the
+ * reference's optional QueryScratch* (query.hpp:96). */
+int suco_gpu_knn_query_batch(const suco_gpu_index* index, const float* queries, uint64_t nq, uint32_t qlen,
+                             const suco_collision_params* params, uint32_t* ids, double* dists,
+                             suco_gpu_query_ctx* scratch);
 
 /* Same, with device-resident queries/outputs, enqueued on `stream`
- * (cudaStream_t; NULL = the index's stream — pass cudaStreamLegacy to order
- * with the legacy default stream). Returns once enqueued. */
-int suco_gpu_knn_query_batch_device(suco_gpu_index* index, const float* d_queries, uint64_t nq, uint32_t qlen,
+ * (cudaStream_t; NULL = the context's own stream — pass cudaStreamLegacy to
+ * order with the legacy default stream). Returns once enqueued. */
+int suco_gpu_knn_query_batch_device(const suco_gpu_index* index, const float* d_queries, uint64_t nq, uint32_t qlen,
                                     const suco_collision_params* params, uint32_t* d_ids, double* d_dists,
-                                    void* stream);
+                                    void* stream, suco_gpu_query_ctx* scratch);
 
-/* Stream used by later calls on this index (cudaStream_t; NULL restores the
- * index's own stream). */
-int suco_gpu_set_stream(suco_gpu_index* index, void* stream);
-int suco_gpu_synchronize(suco_gpu_index* index);
+/* Query contexts. create: on the index's device. synchronize: waits for all
+ * work the context enqueued. */
+int suco_gpu_query_ctx_create(const suco_gpu_index* index, suco_gpu_query_ctx** out);
+void suco_gpu_query_ctx_free(suco_gpu_query_ctx* ctx);
+int suco_gpu_query_ctx_synchronize(suco_gpu_query_ctx* ctx);
 
-/* Stage profiling: when enabled, every query call records CUDA events around
- * each kernel on the launching stream; suco_gpu_stage_times then returns the
- * summed device milliseconds of the last call per stage (0 traverse, 1 select,
- * 2 rerank) and the algorithmic work counters of that call: stats[0] = sum
- * over queries and subspaces of the retrieved ids (the final cumulative of
- * every traversal, query.cpp:105-106), stats[1] = queries, stats[2] = m. */
-int suco_gpu_set_profiling(suco_gpu_index* index, int enabled);
-/* Number of CUDA kernels the last query call on this index enqueued (all of
- * them this library's own sm_100a kernels). */
-int suco_gpu_last_launches(const suco_gpu_index* index, uint64_t* launches);
-int suco_gpu_stage_times(suco_gpu_index* index, double* ms /*3*/, uint64_t* stats /*3*/);
+/* Stage profiling: when enabled, every query call through this context
+ * records CUDA events around each kernel; suco_gpu_query_ctx_stage_times
+ * then returns the summed device milliseconds of the last call per stage
+ * (0 traverse, 1 select, 2 rerank) and the algorithmic work counters of that
+ * call: stats[0] = sum over queries and subspaces of the retrieved ids (the
+ * final cumulative of every traversal, query.cpp:105-106), stats[1] =
+ * queries, stats[2] = m. last_launches: CUDA kernels the last call enqueued
+ * (all of them this library's own sm_100a kernels). exchange_bytes: bytes
+ * this rank sent through the communicator in the last shard query. */
+int suco_gpu_query_ctx_set_profiling(suco_gpu_query_ctx* ctx, int enabled);
+int suco_gpu_query_ctx_stage_times(suco_gpu_query_ctx* ctx, double* ms /*3*/, uint64_t* stats /*3*/);
+int suco_gpu_query_ctx_last_launches(const suco_gpu_query_ctx* ctx, uint64_t* launches);
+int suco_gpu_query_ctx_exchange_bytes(const suco_gpu_query_ctx* ctx, uint64_t* bytes);
 
-/* Per-query intermediates of knn_query for parity checks: SC-scores (n u32,
- * query.cpp:235-239), the top-m candidate set sorted ascending (m u32,
- * query.cpp:242-260), per-subspace retrieved-cell counts and final cumulative
- * (query.cpp:229-233). scores / cells / cumulative may be NULL. */
-int suco_gpu_query_intermediates(suco_gpu_index* index, const float* query, uint32_t qlen,
+/* Per-query intermediates of knn_query for parity checks, from the
+ * production kernels: SC-scores (n u32, query.cpp:235-239, as the select
+ * stage scored them), the top-m candidate set sorted ascending (m u32,
+ * query.cpp:242-260), per-subspace retrieved-cell counts and final
+ * cumulative (query.cpp:229-233). scores / cells / cumulative may be NULL. */
+int suco_gpu_query_intermediates(const suco_gpu_index* index, const float* query, uint32_t qlen,
                                  const suco_collision_params* params, uint32_t* scores, uint32_t* cands,
                                  uint64_t* m, uint32_t* cells_per_subspace, uint64_t* cumulative);
 
 /* ------------------------------------------------- multi-GPU shard protocol
  * The reference runs on one host (no distributed API); this is the sharded
- * form of knn_query. Points are split block-cyclically: global
- * block j = ids [j*block, (j+1)*block) belongs to shard j % num_shards. Every
- * shard keeps the layout, centroids and GLOBAL cell sizes, so its traversal
- * makes the global Dynamic-Activation cut; it counts SC-scores only for its
- * own points. Per query batch:
- *   1. suco_gpu_shard_histograms -> hist[q][local block][t] = #points with
- *      score >= t (t = 0..N_s+1; t = 0 is the block length);
- *   2. the caller exchanges histograms (sum over shards -> threshold T =
- *      max{t : #score>=t >= m}; per-block ties at T in GLOBAL block order ->
- *      each local block's quota), and computes per (q, local block) the output
- *      offset `base` and per query the candidate count;
- *   3. suco_gpu_shard_topk -> local candidates (score > T, first `quota` ties
- *      per block in id order) re-ranked exactly: local top-min(k, count),
- *      GLOBAL ids + SQUARED distances, padded with (0xffffffff, +inf);
- *   4. the caller gathers every shard's lists and keeps the k smallest
- *      (squared distance, id), then takes sqrt — identical to knn_query.
- * paper_2411_14754_b200.sharded implements 2 and 4 over torch.distributed. */
+ * form of build_index / knn_query, bit-identical to them for
+ * any number of shards. Points are split block-cyclically: global block j =
+ * ids [j*block, (j+1)*block) belongs to shard j % G (block: a multiple of
+ * 2048). Every shard keeps the layout, all centroids and the GLOBAL cell
+ * sizes, so its traversal makes the global Dynamic-Activation cut; it scores
+ * and re-ranks only its own points. A query batch costs three all-gathers:
+ * per-shard score totals (-> the global threshold T), per-block tie counts at
+ * T (-> each block's tie quota in global id order), and the local top-k
+ * (-> a G-way merge by (distance, id)).
+ *
+ * Communicators: NCCL (one process per GPU: rank 0 makes an id, every rank
+ * receives it out of band and creates its member), or in-process (G members
+ * driven by G host threads — e.g. G shards on one GPU for tests). Every rank
+ * must make the same sequence of shard calls with the same arguments. */
+#define SUCO_NCCL_ID_BYTES 128
+int suco_comm_nccl_id(unsigned char* id /* SUCO_NCCL_ID_BYTES */);
+int suco_comm_nccl_create(const unsigned char* id, int nranks, int rank, int device, suco_comm** out);
+int suco_comm_local_create(int nranks, suco_comm** members /* nranks */);
+int suco_comm_info(const suco_comm* comm, int* rank, int* size, uint64_t* bytes_sent);
+void suco_comm_free(suco_comm* comm);
+
+/* Block size for n points over num_shards shards: a power of two in
+ * [2048, 65536], about n / (100 * num_shards), so the tie quota (the lowest
+ * ids at the threshold score) spreads over >= 16 block rounds of shards. */
+int suco_gpu_shard_block_hint(uint64_t n, uint32_t num_shards, uint32_t* block);
+
+/* build_index (index.cpp:98-145) across the communicator's ranks, each
+ * holding only its own rows: `rows` = the rows of global blocks j = rank
+ * (mod G), back to back in id order (n_local x d, host or device memory).
+ * The 2*N_s k-means jobs run one per rank (job j on rank j % G) on its
+ * projected column gathered in global id order — all rows, or the sampled
+ * build's ascending train_ids (NULL: all); the centroids are broadcast, each
+ * rank assigns its own rows (kmeans.cpp:19-33) and builds its local IMI, and
+ * the per-cell counts are all-reduced. The result equals
+ * suco_gpu_make_shard(suco_gpu_build_index[_sampled](all rows), rank, G,
+ * block). Checks as suco_gpu_build_index (a failure on any rank fails every
+ * rank). */
+int suco_gpu_build_shard(const float* rows, uint64_t n_global, uint32_t d, const suco_index_params* params,
+                         uint32_t block, const uint32_t* train_ids, uint64_t n_train, suco_comm* comm, int device,
+                         suco_gpu_index** out);
+/* Cut shard `shard` of num_shards from a full index on the same device. */
 int suco_gpu_make_shard(const suco_gpu_index* full, uint32_t shard, uint32_t num_shards, uint32_t block,
                         suco_gpu_index** out);
-/* Recommended block size for num_shards shards of `full`: the slab length the
- * shard's select kernel would use, so slabs coincide with blocks and phase 1
- * writes its block histograms without a separate pass. Any block size is
- * correct; this one is fastest. */
-int suco_gpu_shard_block_hint(const suco_gpu_index* full, uint32_t num_shards, uint32_t* block);
-int suco_gpu_shard_info(const suco_gpu_index* index, uint64_t* n_global, uint64_t* n_local, uint32_t* nblocks_local,
-                        uint32_t* block, uint32_t* shard, uint32_t* num_shards);
-/* Histogram rows: shard_info's nblocks_local counts the id-contiguous PIECES a
- * shard reports per query — whole blocks, or (dense select, blocks a multiple
- * of 2048 ids) 2048-id pieces, pieces_per_block of them per block, so local
- * piece p sits in global order at ((p / ppb) * num_shards + shard) * ppb + p % ppb. */
-int suco_gpu_shard_pieces(const suco_gpu_index* shard, uint32_t* pieces_per_block, int* dense /* may be NULL */);
-/* d_queries nq x qlen, d_hist nq x nblocks_local x (N_s + 2) u32 (device): per piece
- * [length, #score >= 1, ..., #score >= N_s, 0]. */
-int suco_gpu_shard_histograms(suco_gpu_index* shard, const float* d_queries, uint64_t nq, uint32_t qlen,
-                              const suco_collision_params* params, uint32_t* d_hist, void* stream);
-/* Must follow suco_gpu_shard_histograms of the same queries on the same shard.
- * d_T nq, d_quota / d_base nq x nblocks_local, d_counts nq (all device, u32);
- * candidate rows of `stride` entries; d_ids nq x k, d_sqdists nq x k. */
-int suco_gpu_shard_topk(suco_gpu_index* shard, const float* d_queries, uint64_t nq, uint32_t qlen,
-                        const suco_collision_params* params, const uint32_t* d_T, const uint32_t* d_quota,
-                        const uint32_t* d_base, const uint32_t* d_counts, uint64_t stride, uint32_t* d_ids,
-                        double* d_sqdists, void* stream);
-
-/* Query-split variant (multi-GPU): each rank traverses only its slice of the
- * batch (suco_gpu_shard_traverse: d_cells nq x N_s x K padded, d_ncells
- * nq x N_s, against the GLOBAL cell sizes); the ranks exchange the compact
- * cell lists (query order, then subspace order; d_cells_off = nq*N_s + 1
- * u64 offsets) and run phases 1 and 2 on them. Needs the dense select
- * (N_s <= 8, blocks a multiple of 2048 ids). */
-int suco_gpu_shard_traverse(suco_gpu_index* shard, const float* d_queries, uint64_t nq, uint32_t qlen,
-                            const suco_collision_params* params, uint32_t* d_cells, uint32_t* d_ncells, void* stream);
-int suco_gpu_shard_histograms_cells(suco_gpu_index* shard, uint64_t nq, const suco_collision_params* params,
-                                    const uint32_t* d_cells, const uint64_t* d_cells_off, uint32_t* d_hist,
-                                    void* stream);
-int suco_gpu_shard_topk_cells(suco_gpu_index* shard, const float* d_queries, uint64_t nq, uint32_t qlen,
-                              const suco_collision_params* params, const uint32_t* d_cells,
-                              const uint64_t* d_cells_off, const uint32_t* d_T, const uint32_t* d_quota,
-                              const uint32_t* d_base, const uint32_t* d_counts, uint64_t stride, uint32_t* d_ids,
-                              double* d_sqdists, void* stream);
+int suco_gpu_shard_info(const suco_gpu_index* index, uint64_t* n_global, uint64_t* n_local, uint32_t* block,
+                        uint32_t* shard, uint32_t* num_shards);
+/* knn_query over a batch on every rank at once: every rank passes the same
+ * queries and parameters and receives the full nq x k result (as
+ * suco_gpu_knn_query_batch). The communicator's rank must hold the index's
+ * shard. Host-buffer and device-buffer (enqueued on `stream`) forms. */
+int suco_gpu_shard_knn_query_batch(const suco_gpu_index* shard, suco_comm* comm, const float* queries, uint64_t nq,
+                                   uint32_t qlen, const suco_collision_params* params, uint32_t* ids, double* dists,
+                                   suco_gpu_query_ctx* scratch);
+int suco_gpu_shard_knn_query_batch_device(const suco_gpu_index* shard, suco_comm* comm, const float* d_queries,
+                                          uint64_t nq, uint32_t qlen, const suco_collision_params* params,
+                                          uint32_t* d_ids, double* d_dists, void* stream,
+                                          suco_gpu_query_ctx* scratch);
 
 /* ------------------------------------------------------------ evaluation
  * exact_knn (eval.hpp:29, eval.cpp:28-62) over a batch, on the index's device
@@ -226,7 +244,7 @@ int suco_gpu_shard_topk_cells(suco_gpu_index* shard, const float* d_queries, uin
  * CONTRACT. Host buffers: queries nq x qlen, ids / dists nq x k. The GPU
  * ground truth of SURVEY §8(f)2; recall/MRE are host arithmetic
  * (paper_2411_14754_b200.recall / mre, eval.cpp:64-102). */
-int suco_gpu_exact_knn_batch(suco_gpu_index* index, const float* queries, uint64_t nq, uint32_t qlen, uint32_t k,
+int suco_gpu_exact_knn_batch(const suco_gpu_index* index, const float* queries, uint64_t nq, uint32_t qlen, uint32_t k,
                              uint32_t* ids, double* dists);
 
 /* ------------------------------------------------------------- SC-Linear
@@ -237,14 +255,14 @@ int suco_gpu_exact_knn_batch(suco_gpu_index* index, const float* queries, uint64
  * (sq_euclidean_raw for a consecutive subspace, sq_euclidean_projected
  * otherwise), so the tally is identical. Wrong query length -> CONTRACT;
  * alpha outside (0, 1] -> CONFIG. scores: n host u32s. */
-int suco_gpu_sc_scores(suco_gpu_index* index, const float* query, uint32_t qlen, double alpha, uint32_t* scores);
+int suco_gpu_sc_scores(const suco_gpu_index* index, const float* query, uint32_t qlen, double alpha, uint32_t* scores);
 
 /* sc_linear_query (sc_linear.hpp:52-53, sc_linear.cpp:95-121) over a batch:
  * the candidate_count(beta, n, k) best points by (score desc, id asc),
  * re-ranked exactly like knn_query. Params are validated first (CONFIG), then
  * the query length (CONTRACT). Host buffers: queries nq x qlen, ids / dists
  * nq x k. The index-free quality baseline of SURVEY §8(f)4. */
-int suco_gpu_sc_linear_batch(suco_gpu_index* index, const float* queries, uint64_t nq, uint32_t qlen,
+int suco_gpu_sc_linear_batch(const suco_gpu_index* index, const float* queries, uint64_t nq, uint32_t qlen,
                              const suco_collision_params* params, uint32_t* ids, double* dists);
 
 /* ------------------------------------------------------------- vecs I/O

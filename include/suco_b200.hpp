@@ -16,14 +16,19 @@
 //   suco::collision_count / candidate_count / CollisionParams::validate (sc_linear.hpp:30-40)
 //                                               -> suco_collision_count / suco_candidate_count /
 //                                                  suco_validate_collision_params
-// Multi-GPU shard protocol: suco_gpu_make_shard / suco_gpu_shard_block_hint / suco_gpu_shard_info /
-// suco_gpu_shard_pieces / suco_gpu_shard_traverse / suco_gpu_shard_histograms_cells /
-// suco_gpu_shard_topk_cells /
-// suco_gpu_shard_histograms / suco_gpu_shard_topk (raw C entry points; the
-// exchange between shards lives in paper_2411_14754_b200.sharded).
+//   suco::QueryScratch     query.hpp:72-78      suco::gpu::QueryScratch         -> suco_gpu_query_ctx_create /
+//                                                  suco_gpu_query_ctx_free / suco_gpu_query_ctx_synchronize /
+//                                                  suco_gpu_query_ctx_set_profiling / suco_gpu_query_ctx_stage_times /
+//                                                  suco_gpu_query_ctx_last_launches / suco_gpu_query_ctx_exchange_bytes
+// Multi-GPU shard protocol (no reference counterpart; the sharded build_index / knn_query):
+//   suco::gpu::Comm  -> suco_comm_nccl_id / suco_comm_nccl_create / suco_comm_local_create /
+//                       suco_comm_info / suco_comm_free
+//   suco::gpu::build_shard / make_shard / shard_block_hint / GpuIndex::shard_info /
+//   GpuIndex::shard_knn_query_batch(_device)
+//                    -> suco_gpu_build_shard / suco_gpu_make_shard / suco_gpu_shard_block_hint /
+//                       suco_gpu_shard_info / suco_gpu_shard_knn_query_batch(_device)
 // Also wrapped: suco_last_error, suco_gpu_device_count, suco_gpu_index_info,
-// suco_gpu_index_subspace, suco_gpu_free_index, suco_gpu_set_stream,
-// suco_gpu_synchronize, suco_gpu_query_intermediates, suco_gpu_last_launches,
+// suco_gpu_index_subspace, suco_gpu_free_index, suco_gpu_query_intermediates,
 // suco_gpu_exact_knn_batch (GpuIndex::exact_knn_batch; recall / mre as in eval.cpp:64-102),
 // suco_gpu_sc_scores / suco_gpu_sc_linear_batch (GpuIndex::sc_scores / sc_linear_batch, sc_linear.hpp:45-53),
 // suco_read_vecs / suco_write_vecs / suco_gpu_build_index_from_vecs / suco_gpu_load_index_from_vecs
@@ -67,7 +72,8 @@ inline void check(int rc) {
     const std::string msg = suco_last_error();
     switch (rc) {
         case SUCO_ERR_CONFIG: throw ConfigError(msg);
-        case SUCO_ERR_FORMAT: throw CorruptIndexError(msg);
+        case SUCO_ERR_FORMAT: throw FormatError(msg);
+        case SUCO_ERR_CORRUPT_INDEX: throw CorruptIndexError(msg);
         case SUCO_ERR_INCOMPATIBLE: throw IncompatibilityError(msg);
         case SUCO_ERR_CONTRACT: throw ContractError(msg);
         default: throw Error(msg);
@@ -140,7 +146,94 @@ inline int device_count() {
     return n;
 }
 
-// Device-resident SucoIndex (+ the dataset rows it re-ranks).
+class GpuIndex;
+
+// Caller-owned query state (query.hpp:72-78): scratch, streams, events, profiling. One thread at a
+// time; bound to the index it was made for.
+class QueryScratch {
+public:
+    explicit QueryScratch(const GpuIndex& index);
+    suco_gpu_query_ctx* handle() const { return h_.get(); }
+    void synchronize() { check(suco_gpu_query_ctx_synchronize(h_.get())); }
+    void set_profiling(bool on) { check(suco_gpu_query_ctx_set_profiling(h_.get(), on ? 1 : 0)); }
+    // per-stage device ms of the last call {traverse, select, rerank}; stats {retrieved ids, nq, m}
+    void stage_times(double ms[3], std::uint64_t stats[3]) { check(suco_gpu_query_ctx_stage_times(h_.get(), ms, stats)); }
+    std::uint64_t last_launches() const {
+        std::uint64_t n = 0;
+        check(suco_gpu_query_ctx_last_launches(h_.get(), &n));
+        return n;
+    }
+    std::uint64_t exchange_bytes() const {
+        std::uint64_t n = 0;
+        check(suco_gpu_query_ctx_exchange_bytes(h_.get(), &n));
+        return n;
+    }
+
+private:
+    std::unique_ptr<suco_gpu_query_ctx, void (*)(suco_gpu_query_ctx*)> h_;
+};
+
+// A member of the shard protocol's communicator (NCCL, or in-process for G threads).
+class Comm {
+public:
+    explicit Comm(suco_comm* h) : h_(h, &suco_comm_free) {}
+    static std::vector<unsigned char> nccl_id() {
+        std::vector<unsigned char> id(SUCO_NCCL_ID_BYTES);
+        check(suco_comm_nccl_id(id.data()));
+        return id;
+    }
+    static Comm nccl(std::span<const unsigned char> id, int nranks, int rank, int device) {
+        if (id.size() != SUCO_NCCL_ID_BYTES) throw ContractError("NCCL id must be SUCO_NCCL_ID_BYTES bytes");
+        suco_comm* h = nullptr;
+        check(suco_comm_nccl_create(id.data(), nranks, rank, device, &h));
+        return Comm(h);
+    }
+    static std::vector<Comm> local(int nranks) {
+        std::vector<suco_comm*> hs(static_cast<std::size_t>(nranks > 0 ? nranks : 0));
+        check(suco_comm_local_create(nranks, hs.data()));
+        std::vector<Comm> out;
+        for (suco_comm* h : hs) out.emplace_back(h);
+        return out;
+    }
+    suco_comm* handle() const { return h_.get(); }
+    int rank() const {
+        int r = 0;
+        check(suco_comm_info(h_.get(), &r, nullptr, nullptr));
+        return r;
+    }
+    int size() const {
+        int s = 0;
+        check(suco_comm_info(h_.get(), nullptr, &s, nullptr));
+        return s;
+    }
+
+private:
+    std::unique_ptr<suco_comm, void (*)(suco_comm*)> h_;
+};
+
+inline std::uint32_t shard_block_hint(std::uint64_t n, std::uint32_t num_shards) {
+    std::uint32_t b = 0;
+    check(suco_gpu_shard_block_hint(n, num_shards, &b));
+    return b;
+}
+
+inline std::uint32_t batch_qlen(std::span<const float> queries, std::uint64_t nq) {
+    if (nq == 0) return 0;
+    if (queries.size() % nq != 0) throw ContractError("query buffer length is not a multiple of nq");
+    return static_cast<std::uint32_t>(queries.size() / nq);
+}
+
+inline std::vector<QueryResult> to_results(const std::vector<std::uint32_t>& ids, const std::vector<double>& dists,
+                                           std::uint64_t nq, std::uint32_t k) {
+    std::vector<QueryResult> out(nq);
+    for (std::uint64_t q = 0; q < nq; ++q) {
+        out[q].entries.resize(k);
+        for (std::uint32_t i = 0; i < k; ++i) out[q].entries[i] = {ids[q * k + i], dists[q * k + i]};
+    }
+    return out;
+}
+
+// Device-resident SucoIndex (+ the dataset rows it re-ranks), or one shard of it.
 class GpuIndex {
 public:
     explicit GpuIndex(suco_gpu_index* h) : h_(h, &suco_gpu_free_index) {}
@@ -170,34 +263,55 @@ public:
         return m;
     }
 
-    // run_suco_batch semantics (suco_cli.cpp:95-114): one QueryResult per row.
+    // run_suco_batch semantics (suco_cli.cpp:95-114): one QueryResult per row; queries.size() must
+    // be nq x d. `scratch`: the caller's QueryScratch (query.hpp:96), or nullptr (pooled).
     std::vector<QueryResult> knn_query_batch(std::span<const float> queries, std::uint64_t nq,
-                                             const CollisionParams& params) const {
+                                             const CollisionParams& params, QueryScratch* scratch = nullptr) const {
         const auto cp = params.c();
-        const std::uint32_t qlen = nq ? static_cast<std::uint32_t>(queries.size() / nq) : 0;
+        const std::uint32_t qlen = batch_qlen(queries, nq);
         std::vector<std::uint32_t> ids(nq * params.k);
         std::vector<double> dists(nq * params.k);
-        check(suco_gpu_knn_query_batch(h_.get(), queries.data(), nq, qlen, &cp, ids.data(), dists.data()));
-        std::vector<QueryResult> out(nq);
-        for (std::uint64_t q = 0; q < nq; ++q) {
-            out[q].entries.resize(params.k);
-            for (std::uint32_t i = 0; i < params.k; ++i) out[q].entries[i] = {ids[q * params.k + i], dists[q * params.k + i]};
-        }
-        return out;
+        check(suco_gpu_knn_query_batch(h_.get(), queries.data(), nq, qlen, &cp, ids.data(), dists.data(),
+                                       scratch ? scratch->handle() : nullptr));
+        return to_results(ids, dists, nq, params.k);
+    }
+
+    // The sharded knn_query: every rank of `comm` passes the same queries and gets the full result.
+    std::vector<QueryResult> shard_knn_query_batch(const Comm& comm, std::span<const float> queries, std::uint64_t nq,
+                                                   const CollisionParams& params,
+                                                   QueryScratch* scratch = nullptr) const {
+        const auto cp = params.c();
+        const std::uint32_t qlen = batch_qlen(queries, nq);
+        std::vector<std::uint32_t> ids(nq * params.k);
+        std::vector<double> dists(nq * params.k);
+        check(suco_gpu_shard_knn_query_batch(h_.get(), comm.handle(), queries.data(), nq, qlen, &cp, ids.data(),
+                                             dists.data(), scratch ? scratch->handle() : nullptr));
+        return to_results(ids, dists, nq, params.k);
+    }
+    void shard_knn_query_batch_device(const Comm& comm, const float* d_queries, std::uint64_t nq, std::uint32_t qlen,
+                                      const CollisionParams& params, std::uint32_t* d_ids, double* d_dists,
+                                      void* stream = nullptr, QueryScratch* scratch = nullptr) const {
+        const auto cp = params.c();
+        check(suco_gpu_shard_knn_query_batch_device(h_.get(), comm.handle(), d_queries, nq, qlen, &cp, d_ids, d_dists,
+                                                    stream, scratch ? scratch->handle() : nullptr));
+    }
+    struct ShardInfo {
+        std::uint64_t n_global = 0, n_local = 0;
+        std::uint32_t block = 0, shard = 0, num_shards = 1;
+    };
+    ShardInfo shard_info() const {
+        ShardInfo i;
+        check(suco_gpu_shard_info(h_.get(), &i.n_global, &i.n_local, &i.block, &i.shard, &i.num_shards));
+        return i;
     }
 
     // exact_knn (eval.hpp:29) for every row: the GPU ground truth, ascending by (distance, id).
     std::vector<QueryResult> exact_knn_batch(std::span<const float> queries, std::uint64_t nq, std::uint32_t k) const {
-        const std::uint32_t qlen = nq ? static_cast<std::uint32_t>(queries.size() / nq) : 0;
+        const std::uint32_t qlen = batch_qlen(queries, nq);
         std::vector<std::uint32_t> ids(nq * k);
         std::vector<double> dists(nq * k);
         check(suco_gpu_exact_knn_batch(h_.get(), queries.data(), nq, qlen, k, ids.data(), dists.data()));
-        std::vector<QueryResult> out(nq);
-        for (std::uint64_t q = 0; q < nq; ++q) {
-            out[q].entries.resize(k);
-            for (std::uint32_t i = 0; i < k; ++i) out[q].entries[i] = {ids[q * k + i], dists[q * k + i]};
-        }
-        return out;
+        return to_results(ids, dists, nq, k);
     }
 
     // compute_sc_scores (sc_linear.hpp:45-50) for one query: n per-point collision counts.
@@ -211,32 +325,22 @@ public:
     // sc_linear_query (sc_linear.hpp:52-53) for every row: the SC-Linear baseline.
     std::vector<QueryResult> sc_linear_batch(std::span<const float> queries, std::uint64_t nq,
                                              const CollisionParams& params) const {
-        const std::uint32_t qlen = nq ? static_cast<std::uint32_t>(queries.size() / nq) : 0;
+        const std::uint32_t qlen = batch_qlen(queries, nq);
         std::vector<std::uint32_t> ids(nq * params.k);
         std::vector<double> dists(nq * params.k);
         const auto cp = params.c();
         check(suco_gpu_sc_linear_batch(h_.get(), queries.data(), nq, qlen, &cp, ids.data(), dists.data()));
-        std::vector<QueryResult> out(nq);
-        for (std::uint64_t q = 0; q < nq; ++q) {
-            out[q].entries.resize(params.k);
-            for (std::uint32_t i = 0; i < params.k; ++i) out[q].entries[i] = {ids[q * params.k + i], dists[q * params.k + i]};
-        }
-        return out;
+        return to_results(ids, dists, nq, params.k);
     }
 
     // Device-resident queries/outputs (nq x qlen f32 in, nq x k u32/f64 out), enqueued on `stream`.
     void knn_query_batch_device(const float* d_queries, std::uint64_t nq, std::uint32_t qlen,
                                 const CollisionParams& params, std::uint32_t* d_ids, double* d_dists,
-                                void* stream = nullptr) const {
+                                void* stream = nullptr, QueryScratch* scratch = nullptr) const {
         const auto cp = params.c();
-        check(suco_gpu_knn_query_batch_device(h_.get(), d_queries, nq, qlen, &cp, d_ids, d_dists, stream));
+        check(suco_gpu_knn_query_batch_device(h_.get(), d_queries, nq, qlen, &cp, d_ids, d_dists, stream,
+                                              scratch ? scratch->handle() : nullptr));
     }
-
-    void set_stream(void* stream) { check(suco_gpu_set_stream(h_.get(), stream)); }
-    void synchronize() { check(suco_gpu_synchronize(h_.get())); }
-    void set_profiling(bool on) { check(suco_gpu_set_profiling(h_.get(), on ? 1 : 0)); }
-    // per-stage device ms of the last call {traverse, select, rerank}; stats {retrieved ids, nq, m}
-    void stage_times(double ms[3], std::uint64_t stats[3]) { check(suco_gpu_stage_times(h_.get(), ms, stats)); }
 
     struct Intermediates {
         std::vector<std::uint32_t> scores, candidates, cells_per_subspace;
@@ -261,6 +365,29 @@ public:
 private:
     std::unique_ptr<suco_gpu_index, void (*)(suco_gpu_index*)> h_;
 };
+
+inline QueryScratch::QueryScratch(const GpuIndex& index) : h_(nullptr, &suco_gpu_query_ctx_free) {
+    suco_gpu_query_ctx* c = nullptr;
+    check(suco_gpu_query_ctx_create(index.handle(), &c));
+    h_.reset(c);
+}
+
+// The sharded build_index: `rows` = this rank's rows (global blocks j = rank mod G, in order).
+inline GpuIndex build_shard(std::span<const float> rows, std::uint64_t n_global, std::uint32_t d,
+                            const IndexParams& params, std::uint32_t block, const Comm& comm, int device = 0,
+                            std::span<const std::uint32_t> train_ids = {}) {
+    const auto p = params.c();
+    suco_gpu_index* h = nullptr;
+    check(suco_gpu_build_shard(rows.data(), n_global, d, &p, block, train_ids.empty() ? nullptr : train_ids.data(),
+                               train_ids.size(), comm.handle(), device, &h));
+    return GpuIndex(h);
+}
+
+inline GpuIndex make_shard(const GpuIndex& full, std::uint32_t shard, std::uint32_t num_shards, std::uint32_t block) {
+    suco_gpu_index* h = nullptr;
+    check(suco_gpu_make_shard(full.handle(), shard, num_shards, block, &h));
+    return GpuIndex(h);
+}
 
 inline GpuIndex build_index(std::span<const float> data, std::uint64_t n, std::uint32_t d,
                             const IndexParams& params = {}, int device = 0) {

@@ -27,7 +27,7 @@ __all__ = [
     "Error", "ContractError", "ConfigError", "FormatError", "CorruptIndexError", "IncompatibilityError",
     "SubspaceMode", "IndexParams", "CollisionParams", "Dataset", "Neighbor", "RetrievedCell", "GpuIndex",
     "collision_count", "candidate_count", "build_index", "load_index", "knn_query", "centroid_distances",
-    "dynamic_activation", "rerank", "kmeans", "build_imi", "device_count",
+    "dynamic_activation", "rerank", "kmeans", "build_imi", "device_count", "QueryContext",
 ]
 
 
@@ -56,7 +56,7 @@ class IncompatibilityError(Error):
     pass
 
 
-_CODES = {1: Error, 2: ConfigError, 3: CorruptIndexError, 4: IncompatibilityError, 5: ContractError}
+_CODES = {1: Error, 2: ConfigError, 3: FormatError, 4: IncompatibilityError, 5: ContractError, 6: CorruptIndexError}
 
 
 def _check(rc: int):
@@ -237,8 +237,10 @@ class GpuIndex:
         with open(path, "wb") as f:
             f.write(self.serialize())
 
-    def knn_query_batch(self, queries, params: CollisionParams) -> Tuple[np.ndarray, np.ndarray]:
-        """Batched knn_query (run_suco_batch, suco_cli.cpp:95-114): (ids nq x k, distances nq x k)."""
+    def knn_query_batch(self, queries, params: CollisionParams,
+                        scratch: Optional["QueryContext"] = None) -> Tuple[np.ndarray, np.ndarray]:
+        """Batched knn_query (run_suco_batch, suco_cli.cpp:95-114): (ids nq x k, distances nq x k).
+        `scratch`: a QueryContext of this index (the reference's QueryScratch*), or None (pooled)."""
         q = _f32(queries)
         if q.ndim == 1:
             q = q[None, :]
@@ -248,8 +250,12 @@ class GpuIndex:
         dists = np.zeros((nq, max(k, 1)), np.float64)
         cp = params._c()
         _check(_c.knn_query_batch(self._h, _p(q, _c.f32p), nq, qlen, C.byref(cp), _p(ids, _c.u32p),
-                                  _p(dists, _c.f64p)))
+                                  _p(dists, _c.f64p), scratch.handle if scratch else None))
         return ids[:, :k], dists[:, :k]
+
+    def context(self) -> "QueryContext":
+        """A new query context (suco_gpu_query_ctx_create) bound to this index."""
+        return QueryContext(self)
 
     def exact_knn_batch(self, queries, k: int) -> Tuple[np.ndarray, np.ndarray]:
         """exact_knn (eval.hpp:29, eval.cpp:28-62) for every row on the GPU: (ids nq x k, distances
@@ -288,36 +294,15 @@ class GpuIndex:
         return ids[:, :k], dists[:, :k]
 
     def knn_query_batch_device(self, d_queries: int, nq: int, qlen: int, params: CollisionParams, d_ids: int,
-                               d_dists: int, stream: Optional[int] = None) -> None:
+                               d_dists: int, stream: Optional[int] = None,
+                               scratch: Optional["QueryContext"] = None) -> None:
         """Device-resident variant: raw device pointers (e.g. torch tensor .data_ptr()). `stream` is a
-        cudaStream_t handle; None / 0 = the index's own stream (pass 1 = cudaStreamLegacy for torch's
-        default stream)."""
+        cudaStream_t handle; None / 0 = the context's own stream (pass 1 = cudaStreamLegacy for
+        torch's default stream). Returns once enqueued."""
         cp = params._c()
         _check(_c.knn_query_batch_device(self._h, C.c_void_p(d_queries), nq, qlen, C.byref(cp), C.c_void_p(d_ids),
-                                         C.c_void_p(d_dists), C.c_void_p(stream or 0)))
-
-    def set_stream(self, stream: Optional[int]) -> None:
-        _check(_c.set_stream(self._h, C.c_void_p(stream or 0)))
-
-    def synchronize(self) -> None:
-        _check(_c.synchronize(self._h))
-
-    def set_profiling(self, enabled: bool) -> None:
-        _check(_c.set_profiling(self._h, int(bool(enabled))))
-
-    def stage_times(self):
-        """(ms per stage [traverse, select, rerank], retrieved ids summed over queries x subspaces, nq, m)
-        of the last query call; needs set_profiling(True) before that call."""
-        ms = np.zeros(3, np.float64)
-        st = np.zeros(3, np.uint64)
-        _check(_c.stage_times(self._h, _p(ms, _c.f64p), _p(st, _c.u64p)))
-        return ms, int(st[0]), int(st[1]), int(st[2])
-
-    def last_launches(self) -> int:
-        """Kernels (all this library's) the last query call enqueued (suco_gpu_last_launches)."""
-        n = C.c_uint64()
-        _check(_c.last_launches(self._h, C.byref(n)))
-        return n.value
+                                         C.c_void_p(d_dists), C.c_void_p(stream or 0),
+                                         scratch.handle if scratch else None))
 
     def query_intermediates(self, query, params: CollisionParams):
         """(scores n, candidates ascending, cells per subspace, cumulative per subspace) of one query."""
@@ -332,6 +317,58 @@ class GpuIndex:
         _check(_c.query_intermediates(self._h, _p(q, _c.f32p), q.size, C.byref(cp), _p(scores, _c.u32p),
                                       _p(cands, _c.u32p), C.byref(m), _p(cps, _c.u32p), _p(cum, _c.u64p)))
         return scores, cands[: m.value].copy(), cps, cum
+
+
+class QueryContext:
+    """Caller-owned query state (suco_gpu_query_ctx; the reference's QueryScratch, query.hpp:72-78):
+    pipeline scratch, streams and events, profiling counters. One thread at a time."""
+
+    def __init__(self, index: GpuIndex):
+        h = C.c_void_p()
+        _check(_c.query_ctx_create(index.handle, C.byref(h)))
+        self._h = h
+        self.index = index  # keeps the index alive
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _c.query_ctx_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def synchronize(self) -> None:
+        _check(_c.query_ctx_synchronize(self._h))
+
+    def set_profiling(self, enabled: bool) -> None:
+        _check(_c.query_ctx_set_profiling(self._h, int(bool(enabled))))
+
+    def stage_times(self):
+        """(ms per stage [traverse, select, rerank], retrieved ids summed over queries x subspaces, nq, m)
+        of the last query call; needs set_profiling(True) before that call."""
+        ms = np.zeros(3, np.float64)
+        st = np.zeros(3, np.uint64)
+        _check(_c.query_ctx_stage_times(self._h, _p(ms, _c.f64p), _p(st, _c.u64p)))
+        return ms, int(st[0]), int(st[1]), int(st[2])
+
+    def last_launches(self) -> int:
+        """Kernels (all this library's) the last query call through this context enqueued."""
+        n = C.c_uint64()
+        _check(_c.query_ctx_last_launches(self._h, C.byref(n)))
+        return n.value
+
+    def exchange_bytes(self) -> int:
+        """Bytes this rank sent through the communicator in the last shard query."""
+        n = C.c_uint64()
+        _check(_c.query_ctx_exchange_bytes(self._h, C.byref(n)))
+        return n.value
 
 
 def _rows(dataset):

@@ -66,14 +66,16 @@ index_subspace = _sig("suco_gpu_index_subspace", C.c_int, vp, C.c_uint32, f32p, 
 index_info = _sig("suco_gpu_index_info", C.c_int, vp, u64p, u32p, C.POINTER(IndexParamsC), u32p, u32p, u32p)
 free_index = _sig("suco_gpu_free_index", None, vp)
 knn_query_batch = _sig("suco_gpu_knn_query_batch", C.c_int, vp, f32p, C.c_uint64, C.c_uint32,
-                       C.POINTER(CollisionParamsC), u32p, f64p)
+                       C.POINTER(CollisionParamsC), u32p, f64p, vp)
 knn_query_batch_device = _sig("suco_gpu_knn_query_batch_device", C.c_int, vp, vp, C.c_uint64, C.c_uint32,
-                              C.POINTER(CollisionParamsC), vp, vp, vp)
-set_stream = _sig("suco_gpu_set_stream", C.c_int, vp, vp)
-synchronize = _sig("suco_gpu_synchronize", C.c_int, vp)
-set_profiling = _sig("suco_gpu_set_profiling", C.c_int, vp, C.c_int)
-stage_times = _sig("suco_gpu_stage_times", C.c_int, vp, f64p, u64p)
-last_launches = _sig("suco_gpu_last_launches", C.c_int, vp, u64p)
+                              C.POINTER(CollisionParamsC), vp, vp, vp, vp)
+query_ctx_create = _sig("suco_gpu_query_ctx_create", C.c_int, vp, C.POINTER(vp))
+query_ctx_free = _sig("suco_gpu_query_ctx_free", None, vp)
+query_ctx_synchronize = _sig("suco_gpu_query_ctx_synchronize", C.c_int, vp)
+query_ctx_set_profiling = _sig("suco_gpu_query_ctx_set_profiling", C.c_int, vp, C.c_int)
+query_ctx_stage_times = _sig("suco_gpu_query_ctx_stage_times", C.c_int, vp, f64p, u64p)
+query_ctx_last_launches = _sig("suco_gpu_query_ctx_last_launches", C.c_int, vp, u64p)
+query_ctx_exchange_bytes = _sig("suco_gpu_query_ctx_exchange_bytes", C.c_int, vp, u64p)
 exact_knn_batch = _sig("suco_gpu_exact_knn_batch", C.c_int, vp, f32p, C.c_uint64, C.c_uint32, C.c_uint32, u32p, f64p)
 sc_scores = _sig("suco_gpu_sc_scores", C.c_int, vp, f32p, C.c_uint32, C.c_double, u32p)
 sc_linear_batch = _sig("suco_gpu_sc_linear_batch", C.c_int, vp, f32p, C.c_uint64, C.c_uint32,
@@ -86,18 +88,20 @@ load_index_from_vecs = _sig("suco_gpu_load_index_from_vecs", C.c_int, u8p, C.c_u
                             C.c_int, C.POINTER(vp))
 query_intermediates = _sig("suco_gpu_query_intermediates", C.c_int, vp, f32p, C.c_uint32,
                            C.POINTER(CollisionParamsC), u32p, u32p, u64p, u32p, u64p)
+comm_nccl_id = _sig("suco_comm_nccl_id", C.c_int, u8p)
+comm_nccl_create = _sig("suco_comm_nccl_create", C.c_int, u8p, C.c_int, C.c_int, C.c_int, C.POINTER(vp))
+comm_local_create = _sig("suco_comm_local_create", C.c_int, C.c_int, C.POINTER(vp))
+comm_info = _sig("suco_comm_info", C.c_int, vp, C.POINTER(C.c_int), C.POINTER(C.c_int), u64p)
+comm_free = _sig("suco_comm_free", None, vp)
+shard_block_hint = _sig("suco_gpu_shard_block_hint", C.c_int, C.c_uint64, C.c_uint32, u32p)
+build_shard = _sig("suco_gpu_build_shard", C.c_int, vp, C.c_uint64, C.c_uint32, C.POINTER(IndexParamsC), C.c_uint32,
+                   u32p, C.c_uint64, vp, C.c_int, C.POINTER(vp))
 make_shard = _sig("suco_gpu_make_shard", C.c_int, vp, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(vp))
-shard_block_hint = _sig("suco_gpu_shard_block_hint", C.c_int, vp, C.c_uint32, u32p)
-shard_pieces = _sig("suco_gpu_shard_pieces", C.c_int, vp, u32p, C.POINTER(C.c_int))
-shard_traverse = _sig("suco_gpu_shard_traverse", C.c_int, vp, vp, C.c_uint64, C.c_uint32, vp, vp, vp, vp)
-shard_histograms_cells = _sig("suco_gpu_shard_histograms_cells", C.c_int, vp, C.c_uint64, vp, vp, vp, vp, vp)
-shard_topk_cells = _sig("suco_gpu_shard_topk_cells", C.c_int, vp, vp, C.c_uint64, C.c_uint32, vp, vp, vp, vp, vp, vp,
-                        vp, C.c_uint64, vp, vp, vp)
-shard_info = _sig("suco_gpu_shard_info", C.c_int, vp, u64p, u64p, u32p, u32p, u32p, u32p)
-shard_histograms = _sig("suco_gpu_shard_histograms", C.c_int, vp, vp, C.c_uint64, C.c_uint32,
-                        C.POINTER(CollisionParamsC), vp, vp)
-shard_topk = _sig("suco_gpu_shard_topk", C.c_int, vp, vp, C.c_uint64, C.c_uint32, C.POINTER(CollisionParamsC), vp, vp,
-                  vp, vp, C.c_uint64, vp, vp, vp)
+shard_info = _sig("suco_gpu_shard_info", C.c_int, vp, u64p, u64p, u32p, u32p, u32p)
+shard_knn_query_batch = _sig("suco_gpu_shard_knn_query_batch", C.c_int, vp, vp, f32p, C.c_uint64, C.c_uint32,
+                             C.POINTER(CollisionParamsC), u32p, f64p, vp)
+shard_knn_query_batch_device = _sig("suco_gpu_shard_knn_query_batch_device", C.c_int, vp, vp, vp, C.c_uint64,
+                                    C.c_uint32, C.POINTER(CollisionParamsC), vp, vp, vp, vp)
 centroid_distances = _sig("suco_gpu_centroid_distances", C.c_int, f32p, C.c_uint32, f32p, C.c_uint32, f64p, u32p)
 dynamic_activation = _sig("suco_gpu_dynamic_activation", C.c_int, C.c_double, C.c_uint64, f64p, u32p, f64p, u32p,
                           C.c_uint32, u64p, u32p, u32p, u64p, f64p, C.c_uint64, u64p)
@@ -107,17 +111,19 @@ kmeans = _sig("suco_gpu_kmeans", C.c_int, f32p, C.c_uint64, C.c_uint32, C.c_uint
               f32p, u32p, u32p, u32p)
 build_imi = _sig("suco_gpu_build_imi", C.c_int, u32p, u32p, C.c_uint64, C.c_uint32, u64p, u32p)
 
+# every entry point include/suco_b200.h declares (tests/test_capi.py checks the header agrees)
 EXPORTED = [
     "suco_last_error", "suco_gpu_device_count", "suco_collision_count", "suco_candidate_count",
-    "suco_validate_collision_params", "suco_gpu_build_index", "suco_gpu_build_index_sampled", "suco_gpu_load_index", "suco_gpu_serialize_index",
-    "suco_gpu_index_subspace", "suco_gpu_index_info", "suco_gpu_free_index", "suco_gpu_knn_query_batch",
-    "suco_gpu_knn_query_batch_device", "suco_gpu_set_stream", "suco_gpu_synchronize", "suco_gpu_set_profiling",
-    "suco_gpu_stage_times", "suco_gpu_last_launches", "suco_gpu_exact_knn_batch", "suco_gpu_sc_scores",
-    "suco_gpu_sc_linear_batch", "suco_read_vecs", "suco_write_vecs",
-    "suco_gpu_build_index_from_vecs", "suco_gpu_load_index_from_vecs",
-    "suco_gpu_query_intermediates", "suco_gpu_centroid_distances", "suco_gpu_dynamic_activation", "suco_gpu_rerank",
-    "suco_gpu_kmeans", "suco_gpu_build_imi", "suco_gpu_make_shard", "suco_gpu_shard_block_hint",
-    "suco_gpu_shard_info", "suco_gpu_shard_pieces", "suco_gpu_shard_traverse", "suco_gpu_shard_histograms_cells",
-    "suco_gpu_shard_topk_cells", "suco_gpu_shard_histograms",
-    "suco_gpu_shard_topk",
+    "suco_validate_collision_params", "suco_gpu_build_index", "suco_gpu_build_index_sampled", "suco_gpu_load_index",
+    "suco_gpu_serialize_index", "suco_gpu_index_subspace", "suco_gpu_index_info", "suco_gpu_free_index",
+    "suco_gpu_knn_query_batch", "suco_gpu_knn_query_batch_device", "suco_gpu_query_ctx_create",
+    "suco_gpu_query_ctx_free", "suco_gpu_query_ctx_synchronize", "suco_gpu_query_ctx_set_profiling",
+    "suco_gpu_query_ctx_stage_times", "suco_gpu_query_ctx_last_launches", "suco_gpu_query_ctx_exchange_bytes",
+    "suco_gpu_query_intermediates", "suco_comm_nccl_id", "suco_comm_nccl_create", "suco_comm_local_create",
+    "suco_comm_info", "suco_comm_free", "suco_gpu_shard_block_hint", "suco_gpu_build_shard", "suco_gpu_make_shard",
+    "suco_gpu_shard_info", "suco_gpu_shard_knn_query_batch", "suco_gpu_shard_knn_query_batch_device",
+    "suco_gpu_exact_knn_batch", "suco_gpu_sc_scores", "suco_gpu_sc_linear_batch", "suco_read_vecs",
+    "suco_write_vecs", "suco_gpu_build_index_from_vecs", "suco_gpu_load_index_from_vecs",
+    "suco_gpu_centroid_distances", "suco_gpu_dynamic_activation", "suco_gpu_rerank", "suco_gpu_kmeans",
+    "suco_gpu_build_imi",
 ]

@@ -36,7 +36,9 @@
 #include <vector>
 
 #include "build.h"
+#include "comm.h"
 #include "common.cuh"
+#include "kernels.h"
 
 namespace suco_gpu {
 namespace {
@@ -90,6 +92,15 @@ __global__ void project_kernel(const float* __restrict__ data, uint64_t n, uint3
         const float* row = data + (rows ? uint64_t(rows[i]) : i) * d;
         float* out = proj + jb.off + i * jb.h;
         for (uint32_t t = 0; t < jb.h; ++t) out[t] = row[dl[t]];
+    }
+}
+
+// dst[t] = src[idx[t]] for rows of h floats (the sharded build's column reassembly)
+__global__ void gather_rows_kernel(const float* __restrict__ src, const uint32_t* __restrict__ idx, uint64_t n,
+                                   uint32_t h, float* __restrict__ dst) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n * h; i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t t = i / h;
+        dst[i] = src[uint64_t(idx[t]) * h + i % h];
     }
 }
 
@@ -754,7 +765,7 @@ void launch_assign(const float* proj, const KJob* jobs, uint64_t n, uint32_t k, 
 // proj/jobs/cent are device arrays; host_jobs mirrors jobs; seeds per job.
 void kmeans_jobs(const float* proj, const std::vector<KJob>& host_jobs, const KJob* jobs, uint64_t n, uint32_t k,
                  uint32_t iterations, const std::vector<uint64_t>& seeds, float* cent, uint32_t* assign,
-                 std::vector<std::vector<uint32_t>>* repaired, cudaStream_t st) {
+                 std::vector<std::vector<uint32_t>>* repaired, cudaStream_t st, bool kpp_serial) {
     const uint32_t J = static_cast<uint32_t>(host_jobs.size());
     uint32_t hmax = 0;
     for (const KJob& jb : host_jobs) hmax = std::max(hmax, jb.h);
@@ -796,8 +807,6 @@ void kmeans_jobs(const float* proj, const std::vector<KJob>& host_jobs, const KJ
     copy_centroid_kernel<<<J, 64, 0, st>>>(proj, jobs, pick.p, 0, cent);
     BCUDA(cudaGetLastError());
     const dim3 gu(grid_for(n, 256, 148 * 4), J);
-    const char* ks = std::getenv("SUCO_KPP_SERIAL");  // 1: the one-lane serial fold (A/B, tests)
-    const int kpp_serial = ks && std::atoi(ks) == 1;
     for (uint32_t c = 1; c < k; ++c) {
         kpp_update_kernel<<<gu, 256, 0, st>>>(proj, jobs, n, pick.p, min_dist.p, chosen.p);
         kpp_select_kernel<<<J, 256, 0, st>>>(proj, jobs, n, c, min_dist.p, chosen.p, d_exact.p, d_unis.p, k, used.p,
@@ -866,8 +875,40 @@ static uint64_t job_table(const HostLayout& L, uint32_t k, uint64_t rows, std::v
     return off;
 }
 
+// Every row to its nearest centroid of each job (kmeans.cpp:19-33, the final-pass rule), in row
+// chunks: project the chunk, assign it, scatter its J columns into assign (J x n).
+static void assign_rows(const float* d_data, uint64_t n, uint32_t d, const HostLayout& L, uint32_t k,
+                        const std::vector<KJob>& hj, const uint32_t* ddims, const uint32_t* ddoff, const float* cent,
+                        uint32_t* assign, cudaStream_t st, uint64_t chunk_rows) {
+    const uint32_t J = 2 * L.ns;
+    uint32_t hmax = 0;
+    for (const KJob& jb : hj) hmax = std::max(hmax, jb.h);
+    uint64_t chunk = std::max<uint64_t>(1, (2ull << 30) / (uint64_t(d) * 4));  // 2 GB of projections
+    if (chunk_rows) chunk = chunk_rows;  // tests
+    chunk = std::max<uint64_t>(1, std::min<uint64_t>(n, chunk));
+    std::vector<KJob> cj;
+    std::vector<uint32_t> cdo, cdims;
+    uint64_t ccoff = 0;
+    const uint64_t coffs = job_table(L, k, chunk, cj, cdo, cdims, &ccoff);
+    Dev<KJob> cjobs(J);
+    Dev<float> cproj(coffs);
+    Dev<uint32_t> cassign(uint64_t(J) * chunk);
+    // the centroid offsets of `hj` (any row count) and `cj` agree: both follow the job order
+    BCUDA(cudaMemcpyAsync(cjobs.p, cj.data(), J * sizeof(KJob), cudaMemcpyHostToDevice, st));
+    for (uint64_t r0 = 0; r0 < n; r0 += chunk) {
+        const uint64_t nc = std::min(chunk, n - r0);
+        project_kernel<<<dim3(grid_for(nc, 256, 148 * 4), J), 256, 0, st>>>(d_data + r0 * d, nc, d, ddims, ddoff,
+                                                                            cjobs.p, cproj.p, nullptr);
+        BCUDA(cudaGetLastError());
+        launch_assign(cproj.p, cjobs.p, nc, k, hmax, cent, cassign.p, J, st);
+        BCUDA(cudaMemcpy2DAsync(assign + r0, n * 4, cassign.p, nc * 4, nc * 4, J, cudaMemcpyDeviceToDevice, st));
+    }
+    BCUDA(cudaStreamSynchronize(st));
+}
+
 void build_index_device(const float* d_data, uint64_t n, uint32_t d, const HostLayout& L, const suco_index_params& p,
-                        BuildOutputs& out, cudaStream_t st, const uint32_t* train, uint64_t n_train) {
+                        BuildOutputs& out, cudaStream_t st, const Tuning& tune, const uint32_t* train,
+                        uint64_t n_train) {
     const uint32_t ns = L.ns, J = 2 * ns, k = p.k_half;
     // k-means fits on every row, or (sampled build) on the training rows only
     const uint64_t nfit = train ? n_train : n;
@@ -892,36 +933,11 @@ void build_index_device(const float* d_data, uint64_t n, uint32_t d, const HostL
     {
         Dev<uint32_t> fit_assign(train ? uint64_t(J) * n_train : 1);
         kmeans_jobs(proj.p, hj, jobs.p, nfit, k, p.iterations, seeds, cent.p, train ? fit_assign.p : assign.p, nullptr,
-                    st);
+                    st, tune.kpp_serial);
     }
     proj.release();
     dtrain.release();
-    if (train) {
-        // every row to its nearest trained centroid (kmeans.cpp:19-33, the final-pass rule), in
-        // row chunks: project the chunk, assign it, scatter its J columns into assign (J x n)
-        uint32_t hmax = 0;
-        for (const KJob& jb : hj) hmax = std::max(hmax, jb.h);
-        uint64_t chunk = std::max<uint64_t>(1, (2ull << 30) / (uint64_t(d) * 4));  // 2 GB of projections
-        if (const char* c = std::getenv("SUCO_BUILD_CHUNK")) chunk = std::max<long long>(1, std::atoll(c));  // tests
-        chunk = std::min<uint64_t>(n, chunk);
-        std::vector<KJob> cj;
-        std::vector<uint32_t> cdo, cdims;
-        uint64_t ccoff = 0;
-        const uint64_t coffs = job_table(L, k, chunk, cj, cdo, cdims, &ccoff);
-        Dev<KJob> cjobs(J);
-        Dev<float> cproj(coffs);
-        Dev<uint32_t> cassign(uint64_t(J) * chunk);
-        BCUDA(cudaMemcpyAsync(cjobs.p, cj.data(), J * sizeof(KJob), cudaMemcpyHostToDevice, st));
-        for (uint64_t r0 = 0; r0 < n; r0 += chunk) {
-            const uint64_t nc = std::min(chunk, n - r0);
-            project_kernel<<<dim3(grid_for(nc, 256, 148 * 4), J), 256, 0, st>>>(d_data + r0 * d, nc, d, ddims.p,
-                                                                                ddoff.p, cjobs.p, cproj.p, nullptr);
-            BCUDA(cudaGetLastError());
-            launch_assign(cproj.p, cjobs.p, nc, k, hmax, cent.p, cassign.p, J, st);
-            BCUDA(cudaMemcpy2DAsync(assign.p + r0, n * 4, cassign.p, nc * 4, nc * 4, J, cudaMemcpyDeviceToDevice, st));
-        }
-        BCUDA(cudaStreamSynchronize(st));
-    }
+    if (train) assign_rows(d_data, n, d, L, k, hj, ddims.p, ddoff.p, cent.p, assign.p, st, tune.build_chunk);
 
     // centroids to the host (tiny)
     std::vector<float> hc(coff);
@@ -943,6 +959,126 @@ void build_index_device(const float* d_data, uint64_t n, uint32_t d, const HostL
     bucket_sort(keys.p, n, k * k, ns, out.cell_off, out.ids, st);
 }
 
+void build_shard_device(const float* d_rows, uint64_t n_local, uint64_t n_global, uint32_t d, uint32_t b,
+                        const HostLayout& L, const suco_index_params& p, suco_comm* comm, BuildOutputs& out,
+                        uint32_t* cell_size, cudaStream_t st, const Tuning& tune, const uint32_t* train,
+                        uint64_t n_train) {
+    const uint32_t ns = L.ns, J = 2 * ns, k = p.k_half;
+    const uint32_t G = static_cast<uint32_t>(comm->size), me = static_cast<uint32_t>(comm->rank);
+    const uint64_t nfit = train ? n_train : n_global;
+    auto owner_of = [&](uint64_t g) { return static_cast<uint32_t>((g / b) % G); };
+    auto local_of = [&](uint64_t g) { return ((g / b) / G) * b + g % b; };
+    // the training rows in global id order: which rank holds each and where in that rank's list
+    std::vector<uint64_t> cnt(G, 0);
+    std::vector<uint32_t> src(nfit);       // rank-major gathered position of training row t
+    std::vector<uint32_t> mine;            // this rank's training rows (local ids), id order
+    for (uint64_t t = 0; t < nfit; ++t) {
+        const uint64_t g = train ? train[t] : t;
+        const uint32_t r = owner_of(g);
+        src[t] = static_cast<uint32_t>(cnt[r]++);  // rank offset added below, once maxcnt is known
+        if (r == me) mine.push_back(static_cast<uint32_t>(local_of(g)));
+    }
+    uint64_t maxcnt = 1;
+    for (uint64_t c : cnt) maxcnt = std::max(maxcnt, c);
+    for (uint64_t t = 0; t < nfit; ++t) {
+        const uint64_t g = train ? train[t] : t;
+        src[t] = static_cast<uint32_t>(uint64_t(owner_of(g)) * maxcnt + src[t]);
+    }
+    if (uint64_t(G) * maxcnt > 0xFFFFFFFFull) raise(SUCO_ERR_CONTRACT, "sharded build: training rows exceed 32-bit ids");
+
+    // 1. project this rank's training rows for every job (job-major, maxcnt rows per job)
+    std::vector<KJob> hj;
+    std::vector<uint32_t> dim_off, dims;
+    uint64_t coff = 0;
+    const uint64_t off = job_table(L, k, maxcnt, hj, dim_off, dims, &coff);
+    Dev<KJob> jobs(J);
+    Dev<uint32_t> ddims(dims.size()), ddoff(J + 1), drows(mine.size());
+    Dev<float> proj(off), cent(coff);
+    BCUDA(cudaMemcpyAsync(jobs.p, hj.data(), J * sizeof(KJob), cudaMemcpyHostToDevice, st));
+    BCUDA(cudaMemcpyAsync(ddims.p, dims.data(), dims.size() * 4, cudaMemcpyHostToDevice, st));
+    BCUDA(cudaMemcpyAsync(ddoff.p, dim_off.data(), (J + 1) * 4, cudaMemcpyHostToDevice, st));
+    if (!mine.empty()) {
+        BCUDA(cudaMemcpyAsync(drows.p, mine.data(), mine.size() * 4, cudaMemcpyHostToDevice, st));
+        project_kernel<<<dim3(grid_for(mine.size(), 256, 148 * 4), J), 256, 0, st>>>(
+            d_rows, mine.size(), d, ddims.p, ddoff.p, jobs.p, proj.p, drows.p);
+        BCUDA(cudaGetLastError());
+    }
+
+    // 2. job j's column gathers on rank j % G, in global training order (the k-means input order)
+    std::vector<uint32_t> own_jobs;
+    for (uint32_t j = 0; j < J; ++j) {
+        if (j % G == me) own_jobs.push_back(j);
+    }
+    const uint32_t Jr = static_cast<uint32_t>(own_jobs.size());
+    std::vector<KJob> hjr(Jr);
+    uint64_t roff = 0, rcoff = 0;
+    uint32_t hmax = 1;
+    for (uint32_t i = 0; i < Jr; ++i) {
+        const uint32_t h = hj[own_jobs[i]].h;
+        hjr[i] = KJob{h, 0, roff, rcoff};
+        roff += nfit * h;
+        rcoff += uint64_t(k) * h;
+        hmax = std::max(hmax, h);
+    }
+    Dev<float> fit(Jr ? roff : 1), gathered(Jr ? uint64_t(G) * maxcnt * hmax : 1), rcent(Jr ? rcoff : 1);
+    Dev<uint32_t> dsrc(Jr ? nfit : 1);
+    if (Jr) BCUDA(cudaMemcpyAsync(dsrc.p, src.data(), nfit * 4, cudaMemcpyHostToDevice, st));
+    for (uint32_t j = 0; j < J; ++j) {
+        const int root = static_cast<int>(j % G);
+        comm->gather(proj.p + hj[j].off, gathered.p, maxcnt * hj[j].h * 4, root, st);
+        if (root == static_cast<int>(me)) {
+            const uint32_t i = static_cast<uint32_t>(std::find(own_jobs.begin(), own_jobs.end(), j) - own_jobs.begin());
+            gather_rows_kernel<<<grid_for(nfit * hj[j].h), 256, 0, st>>>(gathered.p, dsrc.p, nfit, hj[j].h,
+                                                                       fit.p + hjr[i].off);
+            BCUDA(cudaGetLastError());
+        }
+    }
+    proj.release();
+    gathered.release();
+    dsrc.release();
+
+    // 3. the owned k-means jobs (seeds derive_seed(seed, j), index.cpp:131), then every job's
+    //    centroids broadcast from its owner
+    if (Jr) {
+        std::vector<uint64_t> seeds(Jr);
+        for (uint32_t i = 0; i < Jr; ++i) seeds[i] = derive_seed(p.seed, own_jobs[i]);
+        Dev<KJob> rjobs(Jr);
+        Dev<uint32_t> rassign(uint64_t(Jr) * nfit);
+        BCUDA(cudaMemcpyAsync(rjobs.p, hjr.data(), Jr * sizeof(KJob), cudaMemcpyHostToDevice, st));
+        kmeans_jobs(fit.p, hjr, rjobs.p, nfit, k, p.iterations, seeds, rcent.p, rassign.p, nullptr, st, tune.kpp_serial);
+        for (uint32_t i = 0; i < Jr; ++i) {
+            BCUDA(cudaMemcpyAsync(cent.p + hj[own_jobs[i]].coff, rcent.p + hjr[i].coff, uint64_t(k) * hjr[i].h * 4,
+                                  cudaMemcpyDeviceToDevice, st));
+        }
+    }
+    fit.release();
+    for (uint32_t j = 0; j < J; ++j) comm->broadcast(cent.p + hj[j].coff, uint64_t(k) * hj[j].h * 4, int(j % G), st);
+
+    // 4. every local row to its nearest centroid; the local IMI (local ids, ascending per cell)
+    Dev<uint32_t> assign(uint64_t(J) * std::max<uint64_t>(n_local, 1));
+    if (n_local) assign_rows(d_rows, n_local, d, L, k, hj, ddims.p, ddoff.p, cent.p, assign.p, st, tune.build_chunk);
+    std::vector<float> hc(coff);
+    BCUDA(cudaMemcpyAsync(hc.data(), cent.p, coff * 4, cudaMemcpyDeviceToHost, st));
+    BCUDA(cudaStreamSynchronize(st));
+    out.cent1->assign(ns, {});
+    out.cent2->assign(ns, {});
+    for (uint32_t s = 0; s < ns; ++s) {
+        const KJob& a = hj[2 * s];
+        const KJob& c = hj[2 * s + 1];
+        (*out.cent1)[s].assign(hc.begin() + a.coff, hc.begin() + a.coff + uint64_t(k) * a.h);
+        (*out.cent2)[s].assign(hc.begin() + c.coff, hc.begin() + c.coff + uint64_t(k) * c.h);
+    }
+    Dev<uint32_t> keys(uint64_t(ns) * std::max<uint64_t>(n_local, 1));
+    cell_keys_kernel<<<dim3(grid_for(n_local, 256, 148 * 4), ns), 256, 0, st>>>(assign.p, n_local, k, ns, keys.p);
+    BCUDA(cudaGetLastError());
+    bucket_sort(keys.p, n_local, k * k, ns, out.cell_off, out.ids, st);
+
+    // 5. global cell sizes (every shard's Dynamic-Activation cut is the global one)
+    BCUDA(launch_cell_sizes(out.cell_off, ns, k * k, cell_size, st));
+    comm->allreduce_sum_u32(cell_size, uint64_t(ns) * k * k, st);
+    BCUDA(cudaStreamSynchronize(st));
+}
+
 void kmeans_device_host_io(const float* points, uint64_t n, uint32_t dim, uint32_t k, uint32_t iterations, uint64_t seed,
                            float* centroids, uint32_t* assignments, uint32_t* repaired, uint32_t* num_repaired) {
     cudaStream_t st = nullptr;
@@ -958,7 +1094,7 @@ void kmeans_device_host_io(const float* points, uint64_t n, uint32_t dim, uint32
     BCUDA(cudaMemcpyAsync(jobs.p, hj.data(), sizeof(KJob), cudaMemcpyHostToDevice, st));
     BCUDA(cudaMemcpyAsync(proj.p, points, n * dim * 4, cudaMemcpyHostToDevice, st));
     std::vector<std::vector<uint32_t>> rep(1);
-    kmeans_jobs(proj.p, hj, jobs.p, n, k, iterations, {seed}, cent.p, assign.p, &rep, st);
+    kmeans_jobs(proj.p, hj, jobs.p, n, k, iterations, {seed}, cent.p, assign.p, &rep, st, tuning_from_env().kpp_serial);
     BCUDA(cudaMemcpyAsync(centroids, cent.p, uint64_t(k) * dim * 4, cudaMemcpyDeviceToHost, st));
     BCUDA(cudaMemcpyAsync(assignments, assign.p, n * 4, cudaMemcpyDeviceToHost, st));
     BCUDA(cudaStreamSynchronize(st));

@@ -471,6 +471,14 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_emit_kernel(DenseArgs a
         uint32_t B[W][NP];
         score_tile<W, NC>(a, M, t0, hi, xp, B, lane);
         const uint32_t vmask = hi - t0 >= 32 ? kFull : ((1u << (hi - t0)) - 1u);
+        if (a.scores_dbg && q0 == 0 && lane == 0 && mine[0]) {  // parity dump: query 0's scores
+            for (uint32_t r = 0; r < 32 && t0 + r < hi; ++r) {
+                uint32_t sc = 0;
+#pragma unroll
+                for (uint32_t i = 0; i < NP; ++i) sc |= ((B[0][i] >> r) & 1u) << i;
+                a.scores_dbg[t0 + r] = static_cast<uint8_t>(sc);
+            }
+        }
 #pragma unroll
         for (uint32_t w = 0; w < W; ++w) {
             if (!mine[w]) continue;  // lanes past the block's last query only feed the transposes
@@ -924,6 +932,13 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_emit_h_kernel(DenseArgs
         const uint64_t pb = t0 + 32 * half;  // this lane's first point
         const uint32_t vmask = !mine || pb >= hi ? 0u : hi - pb >= 32 ? kFull : ((1u << (hi - pb)) - 1u);
         const uint32_t Bh[4] = {B0, B1, B2, B3};
+        if (a.scores_dbg && q0 == 0 && qj == 0 && mine) {  // parity dump: query 0's scores
+            for (uint32_t r = 0; r < 32 && pb + r < hi; ++r) {
+                const uint32_t sc = ((B0 >> r) & 1u) | (((B1 >> r) & 1u) << 1) | (((B2 >> r) & 1u) << 2) |
+                                    (((B3 >> r) & 1u) << 3);
+                a.scores_dbg[pb + r] = static_cast<uint8_t>(sc);
+            }
+        }
         const uint32_t geT = ge_mask_n<4>(Bh, T) & vmask;
         const uint32_t gt = ge_mask_n<4>(Bh, T + 1) & vmask;
         const uint32_t eq = geT & ~gt;
@@ -1105,13 +1120,10 @@ struct Shape {
 };
 static Shape dense_shape(const DenseArgs& a) {
     const size_t smem1 = dense_smem(a.ns, a.K);
-    const char* wv = std::getenv("SUCO_DENSE_WORDS");
     // the single-pass pipeline measured faster with 32-query blocks (3.75 vs 3.89 ms at cfg2),
     // the two-pass one with 64-query blocks (5.04 vs 5.52 ms)
-    const bool allow2 = (wv ? std::atoi(wv) == 2 : a.cbuf == nullptr) && a.nc != 2;  // 16 subspaces: one word
+    const bool allow2 = (a.words ? a.words == 2 : a.cbuf == nullptr) && a.nc != 2;  // 16 subspaces: one word
     if (allow2 && 2 * smem1 <= 200 * 1024) return {1024, 2, 2 * smem1};
-    const char* tv = std::getenv("SUCO_DENSE_THREADS");  // A/B: 1024 forces one big CTA per SM
-    if (tv && std::atoi(tv) == 1024) return {1024u, 1, smem1};
     return {smem1 <= 110 * 1024 ? 512u : 1024u, 1, smem1};
 }
 
@@ -1245,6 +1257,173 @@ cudaError_t launch_dense_select(const DenseArgs& a, cudaStream_t st) {
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     return launch_dense_emit(a, st);
+}
+
+// ------------------------------------------------------------ shard protocol
+// The sharded select: every shard scores its own points with the two-pass dense
+// select's K1, then two exchanges fix the reference's global top-m by (score desc, id asc)
+// (query.cpp:242-260): (1) per-shard totals #(score >= t) -> every shard derives the same T and
+// need = m - #(score > T); (2) per-block tie counts at T, block-cyclic -> the first `need` ties
+// in GLOBAL id order give each block's quota. K3 then emits the shard's candidates.
+
+// exchange 1: tot[q][t - 1] = #local points with score >= t, t = 1..16 (levels past 8 * nc are 0)
+__global__ void __launch_bounds__(256) shard_totals_kernel(DenseArgs a, uint32_t* tot) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t q = uint64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (q >= a.nq) return;
+    const uint32_t nc = nc_of(a), LV = 8 * nc;
+    const uint4* h = reinterpret_cast<const uint4*>(a.hist) + q * a.P * nc;
+    uint32_t acc[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) acc[t] = 0;
+    for (uint32_t p = lane; p < a.P; p += 32) {
+#pragma unroll
+        for (uint32_t t = 1; t <= 16; ++t) {
+            if (t <= LV) acc[t - 1] += level_n(h + p * nc, t);
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc[t] += __shfl_xor_sync(kFull, acc[t], o);
+    }
+    if (lane < 16) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int t = 0; t < 16; ++t) v = lane == static_cast<uint32_t>(t) ? acc[t] : v;
+        tot[q * 16 + lane] = v;
+    }
+}
+
+// T / need from every shard's totals (G x nq x 16), then per LOCAL block the ties at T
+// (ties[q][lb], nbl_max columns, zero past this shard's blocks).
+__global__ void __launch_bounds__(256) shard_ties_kernel(DenseArgs a, const uint32_t* tot_all, uint32_t G,
+                                                         uint64_t n_global, uint32_t ppb, uint32_t nbl,
+                                                         uint32_t nbl_max, uint32_t* T_out, uint64_t* need_out,
+                                                         uint32_t* ties) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t q = uint64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (q >= a.nq) return;
+    const uint32_t nc = nc_of(a), LV = 8 * nc;
+    // lane t - 1 holds the global #(score >= t)
+    uint64_t ge = 0;
+    if (lane < 16) {
+        for (uint32_t g = 0; g < G; ++g) ge += tot_all[(uint64_t(g) * a.nq + q) * 16 + lane];
+    }
+    uint32_t T = 0;
+    for (int t = 16; t >= 1; --t) {
+        const uint64_t v = __shfl_sync(kFull, ge, t - 1);
+        if (T == 0 && static_cast<uint32_t>(t) <= min(a.ns, LV) && v >= a.m) T = t;
+    }
+    // #(score > T) = #(score >= T + 1); level N_s + 1 and above is empty
+    const uint64_t gtT = (T + 1 <= 16) ? __shfl_sync(kFull, ge, T < 16 ? T : 0) : 0;
+    const uint64_t gt_total = (T + 1 <= min(a.ns, LV)) ? gtT : 0;
+    (void)n_global;
+    const uint4* h = reinterpret_cast<const uint4*>(a.hist) + q * a.P * nc;
+    for (uint32_t lb = lane; lb < nbl_max; lb += 32) {
+        uint32_t t = 0;
+        if (lb < nbl) {
+            for (uint32_t p = lb * ppb; p < min(a.P, (lb + 1) * ppb); ++p) {
+                const uint32_t len = static_cast<uint32_t>(min_u64(a.WP, a.n - uint64_t(p) * a.WP));
+                const uint32_t geT = T ? level_n(h + p * nc, T) : len;
+                const uint32_t gt = T + 1 <= LV ? level_n(h + p * nc, T + 1) : 0u;
+                t += geT - gt;
+            }
+        }
+        ties[q * nbl_max + lb] = t;
+    }
+    if (lane == 0) {
+        T_out[q] = T;
+        need_out[q] = a.m - gt_total;
+    }
+}
+
+// Quotas in global id order (block j of shard j % G, local block j / G), then per local piece:
+// quota (first ties of the block's quota, piece order), output offset, and the local count.
+__global__ void __launch_bounds__(256) shard_quota_kernel(DenseArgs a, const uint32_t* ties_all, uint32_t G,
+                                                          uint32_t shard, uint64_t nb_global, uint32_t ppb,
+                                                          uint32_t nbl, uint32_t nbl_max, const uint64_t* need_in,
+                                                          uint32_t* qblk, uint32_t* counts) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t q = uint64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (q >= a.nq) return;
+    const uint32_t nc = nc_of(a), LV = 8 * nc;
+    const uint64_t need = need_in[q];
+    uint64_t run = 0;
+    for (uint64_t j0 = 0; j0 < nb_global; j0 += 32) {
+        const uint64_t j = j0 + lane;
+        uint32_t t = 0;
+        if (j < nb_global) t = ties_all[(uint64_t(j % G) * a.nq + q) * nbl_max + j / G];
+        uint32_t x = t;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, x, o);
+            if (lane >= static_cast<uint32_t>(o)) x += y;
+        }
+        const uint64_t before = run + x - t;
+        const uint32_t quota = before >= need ? 0u : static_cast<uint32_t>(min_u64(t, need - before));
+        if (j < nb_global && j % G == shard) qblk[q * nbl_max + j / G] = quota;
+        run += __shfl_sync(kFull, x, 31);
+    }
+    __syncwarp();
+    const uint32_t T = a.T[q];
+    const uint4* h = reinterpret_cast<const uint4*>(a.hist) + q * a.P * nc;
+    uint64_t out_run = 0;
+    for (uint32_t lb0 = 0; lb0 < nbl; lb0 += 32) {
+        const uint32_t lb = lb0 + lane;
+        uint32_t btake = 0;
+        if (lb < nbl) {
+            uint32_t left = qblk[q * nbl_max + lb];
+            for (uint32_t p = lb * ppb; p < min(a.P, (lb + 1) * ppb); ++p) {
+                const uint32_t len = static_cast<uint32_t>(min_u64(a.WP, a.n - uint64_t(p) * a.WP));
+                const uint32_t geT = T ? level_n(h + p * nc, T) : len;
+                const uint32_t gt = T + 1 <= LV ? level_n(h + p * nc, T + 1) : 0u;
+                const uint32_t pq = min(geT - gt, left);
+                left -= pq;
+                a.quota[q * a.P + p] = pq;
+                btake += gt + pq;
+            }
+        }
+        uint32_t x = btake;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, x, o);
+            if (lane >= static_cast<uint32_t>(o)) x += y;
+        }
+        if (lb < nbl) {
+            uint32_t pos = static_cast<uint32_t>(out_run + x - btake);
+            for (uint32_t p = lb * ppb; p < min(a.P, (lb + 1) * ppb); ++p) {
+                const uint32_t gt = T + 1 <= LV ? level_n(h + p * nc, T + 1) : 0u;
+                a.base[q * a.P + p] = pos;
+                pos += gt + a.quota[q * a.P + p];
+            }
+        }
+        out_run += __shfl_sync(kFull, x, 31);
+    }
+    if (lane == 0) counts[q] = static_cast<uint32_t>(out_run);
+}
+
+cudaError_t launch_shard_totals(const DenseArgs& a, uint32_t* tot, cudaStream_t st) {
+    if (a.nq == 0) return cudaSuccess;
+    shard_totals_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(a, tot);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_shard_ties(const DenseArgs& a, const uint32_t* tot_all, uint32_t G, uint32_t ppb, uint32_t nbl,
+                              uint32_t nbl_max, uint32_t* T, uint64_t* need, uint32_t* ties, cudaStream_t st) {
+    if (a.nq == 0) return cudaSuccess;
+    shard_ties_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(a, tot_all, G, 0, ppb, nbl, nbl_max, T,
+                                                                              need, ties);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_shard_quota(const DenseArgs& a, const uint32_t* ties_all, uint32_t G, uint32_t shard,
+                               uint64_t nb_global, uint32_t ppb, uint32_t nbl, uint32_t nbl_max, const uint64_t* need,
+                               uint32_t* qblk, uint32_t* counts, cudaStream_t st) {
+    if (a.nq == 0) return cudaSuccess;
+    shard_quota_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(a, ties_all, G, shard, nb_global, ppb,
+                                                                               nbl, nbl_max, need, qblk, counts);
+    return cudaGetLastError();
 }
 
 }  // namespace suco_gpu

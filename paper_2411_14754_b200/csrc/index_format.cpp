@@ -86,7 +86,7 @@ struct Reader {
     uint64_t len, pos = 0;
     void need(uint64_t c, const char* section) {
         if (len - pos < c) {
-            raise(SUCO_ERR_FORMAT, std::string("index file truncated in section '") + section + "' at byte offset " +
+            raise(SUCO_ERR_CORRUPT_INDEX, std::string("index file truncated in section '") + section + "' at byte offset " +
                                        std::to_string(pos));
         }
     }
@@ -104,7 +104,7 @@ struct Reader {
 };
 
 [[noreturn]] void corrupt(const std::string& section, const std::string& detail) {
-    raise(SUCO_ERR_FORMAT, "index section '" + section + "': " + detail);
+    raise(SUCO_ERR_CORRUPT_INDEX, "index section '" + section + "': " + detail);
 }
 
 struct Writer {

@@ -29,6 +29,7 @@ struct TraverseArgs {
     double* dbg_sum;   // optional, nq x ns x K
     uint64_t* dbg_cum; // optional, nq x ns x K
     unsigned long long* stat_cum;  // optional: += final cumulative of every traversal
+    char mode;         // Tuning::traverse (0 = by shape)
 };
 cudaError_t launch_traverse(const TraverseArgs& a, cudaStream_t st);
 
@@ -57,9 +58,7 @@ struct SelectArgs {
     uint64_t nq;          // queries in this launch (persistent clusters loop over them)
     uint32_t* cands;      // nq x m (candidate set, unordered)
     uint8_t* scores_dbg;  // optional nq x n
-    bool count_only;      // stop after counting (scores_dbg receives the scores): shard phase 1
     uint64_t scores_stride;  // row stride of scores_dbg (0 = n); a multiple of 16 enables 16-byte stores
-    uint32_t* slab_hist;     // count_only: optional nq x nslabs x (ns + 2) copy of the slab histograms
 };
 struct SelectConfig {
     uint32_t CS, CH, nslabs, rounds;
@@ -67,11 +66,6 @@ struct SelectConfig {
     int clusters;  // resident clusters (persistent grid); 0 = unknown
 };
 SelectConfig plan_select(uint64_t n, uint32_t ns, int cluster_size);
-// Plan with a given slab length (a multiple of select_slab_align() that fits shared
-// memory); CH = 0 in the result when it does not. Shards use CH = block size so that
-// every slab is one block and the slab histograms are the block histograms.
-SelectConfig plan_select_fixed(uint64_t n, uint32_t ns, uint32_t CH);
-uint32_t select_slab_align();
 cudaError_t launch_select(const SelectArgs& a, const SelectConfig& cfg, uint64_t nq, cudaStream_t st);
 cudaError_t launch_slab_offsets(const uint32_t* cell_off, const uint32_t* ids, uint64_t n, uint32_t ns,
                                 uint32_t K, uint32_t CH, uint32_t nslabs, uint32_t* slab_off,
@@ -114,6 +108,8 @@ struct DenseArgs {
     uint32_t no_cut;              // tests: store every tie (pcut = P)
     float cut_scale;              // tie cut = P * need/ties * cut_scale + cut_pad pieces (0: defaults 1.25, 8)
     uint32_t cut_pad;
+    uint32_t words;               // Tuning::dense_words (0 = by shape)
+    uint8_t* scores_dbg;          // optional (nq == 1): K3 writes query 0's SC-score of every point (parity)
 };
 bool dense_supported(uint32_t ns, uint32_t K);
 // 9..16 subspaces: two code vectors per point, 5 score planes, 16 histogram levels (config 3)
@@ -168,23 +164,34 @@ struct RerankArgs {
     const uint32_t* qskip;  // optional: queries with qskip[q] != 0 are left for a later pass
     const uint32_t* qlist;  // optional: re-rank only qlist[0 .. *nlist) (the grid still spans nq)
     const uint32_t* nlist;
+    bool u8_regs;           // Tuning::rerank_u8_regs: the register byte kernel instead of the smem ring
+    uint8_t pipe;           // 0: certified fp32 screen (default), 1: pipelined fp64, 2: unpipelined
 };
 cudaError_t launch_rerank(const RerankArgs& a, uint64_t nq, cudaStream_t st);
 
 // ------------------------------------------------------------------- shards
 // ids[i] = ((l / b) * G + shard) * b + l % b for the n local ids l (0xffffffff kept).
 cudaError_t launch_shard_ids(uint32_t* ids, uint64_t n, uint32_t b, uint32_t G, uint32_t shard, cudaStream_t st);
-cudaError_t launch_block_hist(const uint8_t* scores, uint64_t nq, uint64_t n_local, uint64_t stride, uint32_t b,
-                              uint32_t nblocks, uint32_t ns, uint32_t* hist, cudaStream_t st);
-cudaError_t launch_shard_emit(const uint8_t* scores, uint64_t nq, uint64_t n_local, uint64_t sstride, uint32_t b,
-                              uint32_t nblocks,
-                              uint32_t shard, uint32_t num_shards, const uint32_t* T, const uint32_t* quota,
-                              const uint32_t* base, uint32_t* cands, uint64_t stride, cudaStream_t st);
-
 // counts == phase A (per-cell owned counts); local_ids != nullptr: phase B (compaction)
 cudaError_t launch_shard_imi(const uint32_t* ids, const uint32_t* cell_off, uint64_t n, uint32_t ns, uint32_t K,
                              uint32_t b, uint32_t G, uint32_t shard, uint32_t* counts, const uint32_t* local_off,
                              uint64_t n_local, uint32_t* local_ids, cudaStream_t st);
+
+// The sharded select's plan (dense.cu): per-shard totals #(score >= t) [nq][16];
+// from every shard's totals [G][nq][16]: T, need and the per-local-block ties at T [nq][nbl_max];
+// from every shard's ties [G][nq][nbl_max]: per-piece quota / base (into a.quota / a.base, a.T
+// read) and the local candidate count per query. ppb = pieces per block.
+cudaError_t launch_shard_totals(const DenseArgs& a, uint32_t* tot, cudaStream_t st);
+cudaError_t launch_shard_ties(const DenseArgs& a, const uint32_t* tot_all, uint32_t G, uint32_t ppb, uint32_t nbl,
+                              uint32_t nbl_max, uint32_t* T, uint64_t* need, uint32_t* ties, cudaStream_t st);
+cudaError_t launch_shard_quota(const DenseArgs& a, const uint32_t* ties_all, uint32_t G, uint32_t shard,
+                               uint64_t nb_global, uint32_t ppb, uint32_t nbl, uint32_t nbl_max, const uint64_t* need,
+                               uint32_t* qblk, uint32_t* counts, cudaStream_t st);
+// k smallest (squared distance, id) over G ascending local lists [G][nq][k], sqrt -> out [nq][k]
+cudaError_t launch_merge_topk(const uint32_t* ids_all, const double* sq_all, uint32_t G, uint64_t nq, uint32_t k,
+                              uint32_t* out_ids, double* out_d, cudaStream_t st);
+// out[i] = sum over g of rows[g][i] (the in-process communicator's all-reduce)
+cudaError_t launch_sum_rows_u32(const uint32_t* rows, uint32_t G, uint64_t count, uint32_t* out, cudaStream_t st);
 
 // ------------------------------------------------------------------- build
 cudaError_t launch_cell_sizes(const uint32_t* cell_off, uint32_t ns, uint32_t K, uint32_t* cell_size,

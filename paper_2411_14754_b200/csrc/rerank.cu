@@ -1034,12 +1034,9 @@ cudaError_t launch_rerank(const RerankArgs& a, uint64_t nq, cudaStream_t st) {
         return cudaGetLastError();
     };
     cudaError_t e = cudaSuccess;
-    const char* uv = std::getenv("SUCO_RERANK_U8_PIPE");  // 0: the register kernel (A/B)
-    if (a.data8 && a.dpad <= 128 && !(uv && std::atoi(uv) == 0)) {
+    if (a.data8 && a.dpad <= 128 && !a.u8_regs) {
         const uint32_t nwr = a.dpad / 16, su = nwr | 1u;
-        const char* sv = std::getenv("SUCO_U8_STAGES");
-        const bool deep = sv && std::atoi(sv) == 3;  // A/B: 3 ring stages x 2 CTAs per SM
-        const size_t usmem = size_t(kWarps) * (deep ? 3 : kU8Stages) * 32 * su * 16;
+        const size_t usmem = size_t(kWarps) * kU8Stages * 32 * su * 16;
         using K = void (*)(RerankArgs);
         const K kg[8] = {rerank_u8_pipe_kernel<1, true>, rerank_u8_pipe_kernel<2, true>, rerank_u8_pipe_kernel<3, true>,
                          rerank_u8_pipe_kernel<4, true>, rerank_u8_pipe_kernel<5, true>, rerank_u8_pipe_kernel<6, true>,
@@ -1048,7 +1045,6 @@ cudaError_t launch_rerank(const RerankArgs& a, uint64_t nq, cudaStream_t st) {
                          rerank_u8_pipe_kernel<4, false>, rerank_u8_pipe_kernel<5, false>, rerank_u8_pipe_kernel<6, false>,
                          rerank_u8_pipe_kernel<7, false>, rerank_u8_pipe_kernel<8, false>};
         K kern = generic ? kg[nwr - 1] : kn[nwr - 1];
-        if (deep && nwr == 8) kern = generic ? rerank_u8_pipe_kernel<8, true, 3, 2> : rerank_u8_pipe_kernel<8, false, 3, 2>;
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(usmem));
         if (e != cudaSuccess) return e;
         kern<<<static_cast<unsigned>(nq), kThreads, usmem, st>>>(a);
@@ -1071,8 +1067,7 @@ cudaError_t launch_rerank(const RerankArgs& a, uint64_t nq, cudaStream_t st) {
         }
         if (e != cudaSuccess) return e;
     }
-    const char* pv = std::getenv("SUCO_RERANK_PIPE");  // 0: unpipelined, 1: pipelined fp64, else screened
-    const int pmode = pv ? std::atoi(pv) : 2;
+    const int pmode = a.pipe == 0 ? 2 : a.pipe == 1 ? 1 : 0;  // 2 screened, 1 pipelined fp64, 0 unpipelined
     if (vec && !generic && pmode == 2) {
         const uint32_t stride = 32 * ((min(a.d, kChunk) + 31) / 32) + 4;  // = 4 (mod 32): conflict-free chains
         const size_t qbytes = ((a.d * 4 + 15) / 16) * 16 + ((a.d * 8 + 15) / 16) * 16;
@@ -1080,12 +1075,10 @@ cudaError_t launch_rerank(const RerankArgs& a, uint64_t nq, cudaStream_t st) {
         const size_t s2 = qbytes + size_t(kWarps) * 2 * kRows * stride * 4;
         // occupancy first (measured: 2 stages x 3 CTAs per SM beat 3 x 2 for the byte rows): 3 CTAs
         // when 2 stages fit 60 KB (228 KB per SM, about 14 KB static + 1 KB reserved each), else 3
-        // stages x 2 CTAs when that fits 98 KB, else 2 x 2. SUCO_SCREEN_STAGES=3 forces 3 x 2.
-        const char* sv = std::getenv("SUCO_SCREEN_STAGES");
-        const int force3 = sv && std::atoi(sv) == 3;
+        // stages x 2 CTAs when that fits 98 KB, else 2 x 2.
         void (*kern)(RerankArgs, uint32_t) = rerank_screen_kernel<2, 2>;
         size_t ssmem = s2;
-        if (!force3 && s2 <= 60 * 1024) {
+        if (s2 <= 60 * 1024) {
             kern = rerank_screen_kernel<2, 3>;
         } else if (s3 <= 98 * 1024) {
             kern = rerank_screen_kernel<3, 2>;

@@ -654,19 +654,6 @@ __global__ void __launch_bounds__(kThreads, SUCO_SELECT_MINB) select_kernel(Sele
             }
 
         }
-        if (a.count_only) {  // shard phase 1: scores (and slab histograms) written, no cluster exchange
-            if (a.slab_hist) {
-                __syncthreads();
-                for (uint32_t r = 0; r < a.rounds; ++r) {
-                    const uint32_t slab = r * a.CS + rank;
-                    if (slab < a.nslabs && tid < hs) {
-                        a.slab_hist[(q * a.nslabs + slab) * hs + tid] = tid <= a.ns ? s.hist[r * hs + tid] : 0u;
-                    }
-                }
-                __syncthreads();
-            }
-            continue;
-        }
         cluster_barrier();
 
         // threshold and per-slab quotas (warp 0), from every slab's histogram
@@ -898,24 +885,6 @@ static int active_clusters_ns(uint32_t ns, const SelectConfig& c) {
     return active_clusters<0>(c);
 }
 
-uint32_t select_slab_align() { return kChAlign; }
-
-SelectConfig plan_select_fixed(uint64_t n, uint32_t ns, uint32_t CH) {
-    SelectConfig c{};
-    if (CH == 0 || CH % kChAlign != 0 || n == 0) return c;
-    const uint64_t nslabs = (n + CH - 1) / CH;
-    const uint32_t CS = static_cast<uint32_t>(std::min<uint64_t>(nslabs, 8));
-    const uint32_t rounds = static_cast<uint32_t>((nslabs + CS - 1) / CS);
-    if (smem_bytes(CH, rounds, ns) > kSmemLimit) return c;
-    c.CS = CS;
-    c.CH = CH;
-    c.nslabs = static_cast<uint32_t>(nslabs);
-    c.rounds = rounds;
-    c.smem = smem_bytes(CH, rounds, ns);
-    c.clusters = active_clusters_ns(ns, c);
-    if (c.clusters <= 0) c = SelectConfig{};
-    return c;
-}
 
 // Cluster size: the one that keeps the most SMs busy with a single counting
 // round (clusters must fit inside a GPC, so 8-CTA clusters strand SMs on a

@@ -583,16 +583,15 @@ static size_t da_extra_bytes(uint32_t k) { return k > 256 ? static_cast<size_t>(
 
 cudaError_t launch_traverse(const TraverseArgs& a, cudaStream_t st) {
     if (a.nq == 0) return cudaSuccess;
-    const char* tv = std::getenv("SUCO_TRAVERSE");  // A/B and tests: "warp" forces the warp-per-task kernel
-    const bool warp_path = tv && tv[0] == 'w';
+    const char tv = a.mode;  // Tuning::traverse (tests): 'w' forces the warp-per-task kernel
+    const bool warp_path = tv == 'w';
     if (a.k_half <= 128 && !warp_path) {
         const uint32_t L = a.k_half <= 64 ? 64 : 128;
         // two threads per task measured faster with short halves and small tables (cfg1/cfg2:
         // 0.64 -> 0.60 ms) and slower otherwise (cfg3, h = 30: 0.25 -> 0.34 ms; cfg4, K = 4096:
-        // 1.13 -> 1.17 ms); SUCO_TRAVERSE=split / nosplit force it
-        const bool split = tv && tv[0] == 's' ? true : tv && tv[0] == 'n' ? false : (a.K <= 2500 && a.hmax <= 16);
-        const char* sv = std::getenv("SUCO_TRAVERSE_SPLIT");
-        const uint32_t sp = !split ? 1u : sv && std::atoi(sv) == 4 ? 4u : 2u;  // threads per task (4: measured slower)
+        // 1.13 -> 1.17 ms); Tuning::traverse 's' / 'n' force it
+        const bool split = tv == 's' ? true : tv == 'n' ? false : (a.K <= 2500 && a.hmax <= 16);
+        const uint32_t sp = split ? 2u : 1u;  // threads per task (4 measured slower)
         // per task: tkey (L f64), d1r/d2r (2k f64), qh (hmax f32), trow (L), o1/o2/cur (3k u8);
         // split: + the second half's scratch (k f64) and projected query (hmax f32)
         const size_t per_t = size_t(L) * 9 + size_t(a.k_half) * (split ? 27 : 19) + size_t(a.hmax) * (split ? 8 : 4);
@@ -609,9 +608,8 @@ cudaError_t launch_traverse(const TraverseArgs& a, cudaStream_t st) {
         }
         if (best_T) {  // measured faster at every bench config (cfg1 0.22 -> 0.19 ms, cfg2 1.25 -> 0.64)
             const size_t smem = fixed + per_t * best_T;
-            auto kern = sp == 4 ? (L == 64 ? traverse_thread_kernel<64, 4> : traverse_thread_kernel<128, 4>)
-                        : sp == 2 ? (L == 64 ? traverse_thread_kernel<64, 2> : traverse_thread_kernel<128, 2>)
-                                  : (L == 64 ? traverse_thread_kernel<64, 1> : traverse_thread_kernel<128, 1>);
+            auto kern = sp == 2 ? (L == 64 ? traverse_thread_kernel<64, 2> : traverse_thread_kernel<128, 2>)
+                                : (L == 64 ? traverse_thread_kernel<64, 1> : traverse_thread_kernel<128, 1>);
             cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
             if (e != cudaSuccess) return e;
             const dim3 grid(static_cast<unsigned>((a.nq + best_T - 1) / best_T), a.ns);

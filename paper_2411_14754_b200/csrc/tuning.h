@@ -1,0 +1,37 @@
+// Algorithm choices of the library that tests and A/B runs may override.
+//
+// Read ONCE — from SUCO_* environment variables — when an index handle is
+// created (build / load / shard) or when a stand-alone stage entry point is
+// called, then immutable: a query call never reads the environment, and two
+// queries on one handle always take the same path. Defaults are the
+// measured-best production choices (DESIGN.md §5 lists the measurements).
+#pragma once
+
+#include <stdint.h>
+
+namespace suco_gpu {
+
+struct Tuning {
+    int cluster = 0;             // SUCO_CLUSTER: cluster-counting select cluster size (0 = by occupancy)
+    bool no_u8 = false;          // SUCO_NO_U8: never keep a byte copy of u8-valued rows
+    bool dense = true;           // SUCO_DENSE=0: the cluster-counting select only
+    int dense_half = 1;          // SUCO_DENSE_HALF: 0 never, 1 when 32-bit masks do not fit, 2 force
+    bool dense_fused = true;     // SUCO_DENSE_FUSED=0: the two-pass dense select
+    bool dense_stage = false;    // SUCO_DENSE_STAGE=1: stage every block's stores (tests)
+    uint32_t dense_buf = 0;      // SUCO_DENSE_BUF: single-pass buffer entries per (piece, query); 0 = by memory
+    bool dense_nocut = false;    // SUCO_DENSE_NOCUT=1: store every tie (tests)
+    uint32_t dense_words = 0;    // SUCO_DENSE_WORDS: mask words per slot (0 auto, 1, 2)
+    bool dense_stats = false;    // SUCO_DENSE_STATS=1: print the single-pass fallback rate (diagnostics)
+    uint32_t tiles = 1;          // SUCO_TILES: minimum pipeline tiles per batch (tests: slot reuse)
+    uint64_t scratch_bytes = 0;  // SUCO_SCRATCH_MB: query scratch budget per context (0 = from free memory)
+    int fb_overlap = -1;         // SUCO_FB_OVERLAP: overlapped dense fallback (-1 auto, 0, 1)
+    char traverse = 0;           // SUCO_TRAVERSE: 0 auto, 'w' warp kernel, 's' / 'n' force / forbid split tasks
+    bool rerank_u8_regs = false; // SUCO_RERANK_U8_PIPE=0: the register byte re-rank instead of the ring
+    int rerank_pipe = 2;         // SUCO_RERANK_PIPE: 0 unpipelined, 1 pipelined fp64, 2 certified fp32 screen
+    bool kpp_serial = false;     // SUCO_KPP_SERIAL=1: k-means++ one-lane serial fold (tests)
+    uint64_t build_chunk = 0;    // SUCO_BUILD_CHUNK: rows per assignment chunk of the sampled build (0 = 2 GB)
+};
+
+Tuning tuning_from_env();
+
+}  // namespace suco_gpu

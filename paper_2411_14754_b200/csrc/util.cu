@@ -2,8 +2,11 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
+#include "tuning.h"
 
 namespace suco_gpu {
 namespace {
@@ -88,6 +91,44 @@ cudaError_t launch_check_finite(const float* data, uint64_t count, int* flag, cu
     check_finite_kernel<<<static_cast<unsigned>(blocks ? blocks : 1), 256, 0, st>>>(
         data, count, reinterpret_cast<unsigned long long*>(flag));
     return cudaGetLastError();
+}
+
+namespace {
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? std::atoi(v) : dflt;
+}
+}  // namespace
+
+Tuning tuning_from_env() {
+    Tuning t;
+    const int c = env_int("SUCO_CLUSTER", 0);
+    t.cluster = (c >= 1 && c <= 16) ? c : 0;
+    t.no_u8 = std::getenv("SUCO_NO_U8") != nullptr;
+    t.dense = env_int("SUCO_DENSE", 1) != 0;
+    t.dense_half = env_int("SUCO_DENSE_HALF", 1);
+    t.dense_fused = env_int("SUCO_DENSE_FUSED", 1) != 0;
+    t.dense_stage = std::getenv("SUCO_DENSE_STAGE") != nullptr;
+    const int b = env_int("SUCO_DENSE_BUF", 0);
+    t.dense_buf = b > 0 ? static_cast<uint32_t>(b < 8 ? 8 : b / 8 * 8) : 0u;
+    t.dense_nocut = std::getenv("SUCO_DENSE_NOCUT") != nullptr;
+    const int w = env_int("SUCO_DENSE_WORDS", 0);
+    t.dense_words = (w == 1 || w == 2) ? static_cast<uint32_t>(w) : 0u;
+    t.dense_stats = std::getenv("SUCO_DENSE_STATS") != nullptr;
+    const int tl = env_int("SUCO_TILES", 1);
+    t.tiles = tl > 1 ? static_cast<uint32_t>(tl) : 1u;
+    const char* mb = std::getenv("SUCO_SCRATCH_MB");
+    t.scratch_bytes = mb && std::atoll(mb) > 0 ? static_cast<uint64_t>(std::atoll(mb)) << 20 : 0;
+    t.fb_overlap = std::getenv("SUCO_FB_OVERLAP") ? (env_int("SUCO_FB_OVERLAP", 0) != 0) : -1;
+    const char* tv = std::getenv("SUCO_TRAVERSE");
+    t.traverse = tv && (tv[0] == 'w' || tv[0] == 's' || tv[0] == 'n') ? tv[0] : 0;
+    t.rerank_u8_regs = env_int("SUCO_RERANK_U8_PIPE", 1) == 0;
+    const int rp = env_int("SUCO_RERANK_PIPE", 2);
+    t.rerank_pipe = (rp == 0 || rp == 1) ? rp : 2;
+    t.kpp_serial = env_int("SUCO_KPP_SERIAL", 0) == 1;
+    const char* ch = std::getenv("SUCO_BUILD_CHUNK");
+    t.build_chunk = ch && std::atoll(ch) > 0 ? static_cast<uint64_t>(std::atoll(ch)) : 0;
+    return t;
 }
 
 }  // namespace suco_gpu

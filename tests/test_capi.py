@@ -83,3 +83,33 @@ def test_contract_checks_precede_device_use(suco):
         suco.kmeans(np.zeros((10, 2), np.float32), 11, 5, 1)
     with pytest.raises(suco.ContractError):
         suco.build_imi([0, 1], [0, 2], 2)
+
+
+def test_format_and_corrupt_index_are_distinct_codes(suco, tmp_path):
+    """Vecs files raise FormatError (io.cpp:20-84, status 3); index bytes raise CorruptIndexError
+    (index.cpp:191-293, status 6), which is-a FormatError like the reference's. Both checks run on
+    the host, before any device use."""
+    from paper_2411_14754_b200 import _capi
+    data = np.zeros((10, 4), np.float32)
+    with pytest.raises(suco.CorruptIndexError, match="magic"):
+        suco.load_index(b"SUCX" + bytes(60), data)
+    assert issubclass(suco.CorruptIndexError, suco.FormatError)
+    blob = np.frombuffer(b"junk", np.uint8).copy()
+    rc = _capi.load_index(blob.ctypes.data_as(_capi.u8p), 4, data.ctypes.data_as(_capi.f32p), 10, 4, 0,
+                          ctypes.byref(ctypes.c_void_p()))
+    assert rc == 6
+    bad = tmp_path / "bad.fvecs"
+    bad.write_bytes(b"\x03\x00\x00")
+    with pytest.raises(suco.FormatError) as e:
+        suco.read_vecs(str(bad), "fvecs")
+    assert not isinstance(e.value, suco.CorruptIndexError)
+
+
+def test_header_declares_status_codes_and_contexts():
+    src = open(os.path.join(ROOT, "include", "suco_b200.h")).read()
+    assert "#define SUCO_ERR_CORRUPT_INDEX 6" in src and "#define SUCO_ERR_FORMAT 3" in src
+    # the handle is immutable: no entry point mutates it (the old set_stream is gone)
+    assert "suco_gpu_set_stream" not in src
+    for fn in ("suco_gpu_knn_query_batch(", "suco_gpu_knn_query_batch_device("):
+        decl = src[src.index("int " + fn):].split(";")[0]
+        assert "const suco_gpu_index*" in decl and "suco_gpu_query_ctx*" in decl, decl

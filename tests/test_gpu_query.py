@@ -493,3 +493,77 @@ def test_host_batch_chunked_io(gpu, oracle):
         ids, dd = idx.knn_query_batch(qs, gpu.CollisionParams(a, b, k))
         oi, od, _ = oidx.knn_query_batch(base, qs, a, b, k)
         assert np.array_equal(ids, oi) and np.array_equal(dd, od), (a, b, k)
+
+
+def test_concurrent_queries_one_index(gpu, oracle):
+    """The index is immutable (index.hpp:63-66): four host threads query one index at once — two
+    with their own query contexts (the reference's QueryScratch, query.hpp:72-78), two through the
+    index's context pool — each on a different parameter set, all equal to the oracle."""
+    import threading
+    full = oracle.clustered(30000 + 300, 24, 20, 909, 0, 100, 8, True)
+    base, qs = oracle.hold_out(full, 300, 910)
+    oidx = oracle.build_index(base, 4, 12, 3, 42, 0)
+    idx = gpu.load_index(oidx.serialize(), base)
+    plist = [(0.05, 0.01, 10), (0.1, 0.005, 40), (0.02, 0.02, 5), (0.2, 0.002, 1)]
+    want = [oidx.knn_query_batch(base, qs, a, b, k)[:2] for a, b, k in plist]
+    ctxs = [idx.context(), idx.context(), None, None]
+    got, errs = [None] * 4, []
+
+    def run(t):
+        try:
+            for _ in range(3):
+                got[t] = idx.knn_query_batch(qs, gpu.CollisionParams(*plist[t]), scratch=ctxs[t])
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+    ts = [threading.Thread(target=run, args=(t,)) for t in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for t in range(4):
+        assert np.array_equal(got[t][0], want[t][0]) and np.array_equal(got[t][1], want[t][1]), plist[t]
+
+
+@pytest.mark.parametrize("overlap", ["0", "1"])
+@pytest.mark.parametrize("knob", ["tiles", "scratch"])
+def test_multi_tile_pipeline(gpu, oracle, knob, overlap, monkeypatch):
+    """Batches split into several pipeline tiles (SUCO_TILES, or a small SUCO_SCRATCH_MB budget):
+    slot reuse across tiles and the cross-stream events — the overlapped dense fallback included —
+    keep every answer equal to the oracle."""
+    if knob == "tiles":
+        monkeypatch.setenv("SUCO_TILES", "3")
+    else:
+        monkeypatch.setenv("SUCO_SCRATCH_MB", "24")
+    monkeypatch.setenv("SUCO_FB_OVERLAP", overlap)
+    monkeypatch.setenv("SUCO_DENSE_BUF", "96")
+    full = oracle.clustered(40000 + 700, 16, 8, 77, 0, 100, 6, True)
+    full = full[np.argsort(full[:, 0], kind="stable")]  # clustered ids: some queries take the fallback
+    pick = np.sort(np.random.default_rng(9).choice(len(full), 700, replace=False))
+    qs, base = full[pick], np.delete(full, pick, axis=0)
+    oidx = oracle.build_index(base, 4, 12, 3, 42, 0)
+    idx = gpu.load_index(oidx.serialize(), base)
+    ctx = idx.context()
+    for a, b, k in ((0.2, 0.01, 10), (0.05, 0.02, 40)):
+        ids, dd = idx.knn_query_batch(qs, gpu.CollisionParams(a, b, k), scratch=ctx)
+        oi, od, _ = oidx.knn_query_batch(base, qs, a, b, k)
+        assert np.array_equal(ids, oi) and np.array_equal(dd, od), (knob, a, b, k)
+    assert ctx.last_launches() > 20  # several tiles' kernels
+
+
+def test_null_buffers_are_contract_errors(gpu):
+    """Every query entry point rejects NULL buffers for nq > 0 (CONTRACT), after the reference's
+    own checks."""
+    import ctypes as C
+    from paper_2411_14754_b200 import _capi
+    g = golden("e2e_small.npz")
+    idx = gpu.load_index(g["index"].tobytes(), g["base"])
+    cp = gpu.CollisionParams(0.05, 0.05, 10)._c()
+    q = np.ascontiguousarray(g["queries"][:2])
+    ids = np.zeros((2, 10), np.uint32)
+    dd = np.zeros((2, 10), np.float64)
+    qp, ip, dp = (a.ctypes.data_as(t) for a, t in ((q, _capi.f32p), (ids, _capi.u32p), (dd, _capi.f64p)))
+    for args in ((None, ip, dp), (qp, None, dp), (qp, ip, None)):
+        assert _capi.knn_query_batch(idx.handle, args[0], 2, q.shape[1], C.byref(cp), args[1], args[2], None) == 5
+    assert _capi.knn_query_batch_device(idx.handle, None, 2, q.shape[1], C.byref(cp), None, None, None, None) == 5
+    assert _capi.knn_query_batch(idx.handle, None, 0, q.shape[1], C.byref(cp), None, None, None) == 0

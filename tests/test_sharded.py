@@ -1,104 +1,84 @@
-"""Multi-GPU shard protocol: exchange math, gloo world_size-2 run on CPU, and
-single-GPU emulation of G shards — all bit-identical to the unsharded results."""
+"""Multi-GPU shard protocol.
+
+CPU: the protocol model (tests/shard_protocol_model.py — the library's three
+exchange rounds restated) in one process for G = 1..5 and over gloo with
+world_size 2, against the unsharded oracle.
+GPU: the library's own sharded query and sharded build over the in-process
+communicator (G ranks on G threads, all on cuda:0 — each collective meets at
+a host barrier, so no kernel waits on another rank), bit-identical to the
+oracle for G = 1..8.
+"""
 import os
 import socket
 
 import numpy as np
 import pytest
-import torch
 
 from conftest import ROOT
 
-
-def _corpus(oracle, n=1500, d=16, seed=5):
-    full = oracle.clustered(n + 12, d, 10, seed, 0.0, 60.0, 5.0, True)
-    return oracle.hold_out(full, 12, seed + 1)
+PARAMS = ((0.05, 0.02, 10), (0.1, 0.005, 7), (0.002, 0.3, 12))  # the last: T = 0, zero-score ties
 
 
-@pytest.mark.parametrize("ppb", [1, 3])
-def test_plan_matches_reference_selection_rule(ppb):
-    """T and id-ordered quotas from per-piece histograms == top-m by (score desc, id asc); pieces
-    are whole blocks (ppb = 1) or ppb consecutive sub-pieces of each block (dense select)."""
-    from paper_2411_14754_b200.sharded import plan_for_shard
-    rng = np.random.default_rng(ppb)
-    ns, n, ps, G, m = 6, 997, 13, 3, 61
-    b = ps * ppb
-    for _ in range(20):
-        scores = rng.integers(0, ns + 1, size=n)
-        order = sorted(range(n), key=lambda i: (-scores[i], i))
-        want = set(order[:m])
-        nb = -(-n // b)
-
-        def pieces_of(r):  # (global start, end) of shard r's pieces in local order
-            out = []
-            for j in (j for j in range(nb) if j % G == r):
-                for sub in range(ppb):
-                    lo = j * b + sub * ps
-                    if lo < n:
-                        out.append((lo, min(n, lo + ps, (j + 1) * b)))
-            return out
-        hists = []
-        for r in range(G):
-            pcs = pieces_of(r)
-            h = np.zeros((1, len(pcs), ns + 2), np.int32)
-            for pi, (lo, hi) in enumerate(pcs):
-                for t in range(ns + 1):
-                    h[0, pi, t] = (scores[lo:hi] >= t).sum()
-            hists.append(torch.from_numpy(h))
-        got = set()
-        for r in range(G):
-            plan = plan_for_shard(hists, r, m, ppb)
-            T = int(plan.T[0])
-            mine = set()
-            for pi, (lo, hi) in enumerate(pieces_of(r)):
-                s = scores[lo:hi]
-                mine |= set((np.nonzero(s > T)[0] + lo).tolist())
-                mine |= set((np.nonzero(s == T)[0] + lo)[: int(plan.quota[0, pi])].tolist())
-            assert int(plan.counts[0]) == len(mine)
-            got |= mine
-        assert got == want
+def _corpus(oracle, n=3000, d=16, seed=5, nq=12):
+    full = oracle.clustered(n + nq, d, 10, seed, 0.0, 60.0, 5.0, True)
+    return oracle.hold_out(full, nq, seed + 1)
 
 
-def _worker(rank, world, port, q, split=False):
+class _P:
+    def __init__(self, a, b, k):
+        self.alpha, self.beta, self.k = a, b, k
+
+
+def _m(b, n, k):
+    import math
+    x = b * n
+    x = round(x) if abs(x - round(x)) <= 1e-6 else x
+    return max(k, math.ceil(x))
+
+
+@pytest.mark.parametrize("G,block,piece", [(1, 256, 64), (2, 128, 32), (3, 96, 32), (5, 64, 64)])
+def test_model_inprocess_matches_unsharded(oracle, G, block, piece):
+    from shard_protocol_model import ModelShard, run_inprocess
+    base, qs = _corpus(oracle)
+    oidx = oracle.build_index(base, 4, 8, 3, 42, 0)
+    shards = [ModelShard(oracle, oidx, base, r, G, block, piece) for r in range(G)]
+    for a, b, k in PARAMS:
+        wi, wd, _ = oidx.knn_query_batch(base, qs, a, b, k)
+        for ids, dd in run_inprocess(shards, qs, _P(a, b, k), _m(b, len(base), k)):
+            assert np.array_equal(ids, wi), (G, a, b, k)
+            assert np.array_equal(dd, wd), (G, a, b, k)
+
+
+def _worker(rank, world, port, q):
     try:
+        import sys
         import torch.distributed as dist
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=world)
-        import sys
         sys.path.insert(0, ROOT)
         sys.path.insert(0, os.path.join(ROOT, "tests"))
         from oracle.oracle import oracle
-        from shard_oracle_engine import OracleShard, OracleSplitShard
-        from paper_2411_14754_b200 import CollisionParams
-        from paper_2411_14754_b200.sharded import TorchComm, knn_query_distributed
+        from shard_protocol_model import ModelShard, torch_allgather
         O = oracle()
         base, qs = _corpus(O)
         oidx = O.build_index(base, 4, 8, 3, 42, 0)
-        eng = (OracleSplitShard if split else OracleShard)(O, oidx, base, rank, world, 64)
-        eng._queries = torch.from_numpy(qs)
-        comm = TorchComm()
-        out = []
-        for a, bta, k in ((0.05, 0.02, 10), (0.1, 0.005, 7), (0.002, 0.3, 12)):
-            ids, dd = knn_query_distributed(eng, comm, torch.from_numpy(qs), CollisionParams(a, bta, k))
-            out.append((ids.numpy(), dd.numpy()))
+        sh = ModelShard(O, oidx, base, rank, world, 128, 32)
+        out = [sh.query(qs, _P(a, b, k), _m(b, len(base), k), torch_allgather) for a, b, k in PARAMS]
         q.put((rank, out))
         dist.destroy_process_group()
-    except Exception as e:  # surface worker failures to the parent
+    except Exception:  # surface worker failures to the parent
         import traceback
         q.put((rank, traceback.format_exc()))
 
 
-@pytest.mark.parametrize("split", [False, True])
-def test_gloo_world_size_2_matches_unsharded(oracle, split):
-    """Both protocols over gloo: replicated traversal, and the query-split traversal whose cell
-    lists are all-gathered (split=True)."""
+def test_gloo_world_size_2_matches_unsharded(oracle):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, split)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in procs)
@@ -108,62 +88,159 @@ def test_gloo_world_size_2_matches_unsharded(oracle, split):
         assert not isinstance(res[r], str), res[r]
     base, qs = _corpus(oracle)
     oidx = oracle.build_index(base, 4, 8, 3, 42, 0)
-    for i, (a, bta, k) in enumerate(((0.05, 0.02, 10), (0.1, 0.005, 7), (0.002, 0.3, 12))):
-        wi, wd, _ = oidx.knn_query_batch(base, qs, a, bta, k)
+    for i, (a, b, k) in enumerate(PARAMS):
+        wi, wd, _ = oidx.knn_query_batch(base, qs, a, b, k)
         for r in (0, 1):
             ids, dd = res[r][i]
-            assert np.array_equal(ids.astype(np.uint32), wi), (r, a, bta, k)
-            assert np.array_equal(dd, wd), (r, a, bta, k)
+            assert np.array_equal(ids, wi), (r, a, b, k)
+            assert np.array_equal(dd, wd), (r, a, b, k)
+
+
+def test_block_hint(suco):
+    from paper_2411_14754_b200.sharded import block_hint, shard_ids
+    assert block_hint(10_000_000, 8) == 8192      # cfg4
+    assert block_hint(100_000_000, 8) == 65536    # cfg5
+    assert block_hint(20_000, 4) == 2048          # floor: one dense piece
+    ids = [shard_ids(10_000, 2048, 3, r) for r in range(3)]
+    assert np.array_equal(np.sort(np.concatenate(ids)), np.arange(10_000))
+    assert ids[1][0] == 2048 and ids[0][2048] == 3 * 2048
+
+
+# ------------------------------------------------------------------ GPU
+GPU_PARAMS = ((0.05, 0.005, 10), (0.02, 0.05, 40), (0.3, 0.001, 3), (0.001, 0.4, 5))
+
+
+def _gpu_corpus(oracle, G, n=20000, d=32, nq=50, quant=True):
+    if quant:
+        full = oracle.clustered(n + nq, d, 40, 77 + G, 20, 140, 18, True)
+    else:
+        full = oracle.clustered(n + nq, d, 40, 77 + G, 0.0, 1.0, 0.05, False)
+    return oracle.hold_out(full, nq, 78)
 
 
 @pytest.mark.gpu
-# blocks that are multiples of 2048 (and None = suco_gpu_shard_block_hint) take the
-# fused path: select slabs == blocks, histograms written by the select kernel
-@pytest.mark.parametrize("G,block", [(1, 4096), (2, 512), (3, 1000), (4, 256), (8, 2048), (1, None), (2, None),
-                                     (3, None), (3, 6144)])
-def test_gpu_emulated_shards_match_unsharded(gpu, oracle, G, block):
-    from paper_2411_14754_b200.sharded import GpuShard, emulate
-    full = oracle.clustered(20000 + 50, 32, 40, 77 + G, 20, 140, 18, True)
-    base, qs = oracle.hold_out(full, 50, 78)
+@pytest.mark.parametrize("G,block", [(1, 4096), (2, 2048), (3, 2048), (4, 4096), (5, 2048), (8, 2048), (3, 6144)])
+def test_gpu_sharded_query_matches_oracle(gpu, oracle, G, block):
+    """The library's sharded query (three device all-gathers, G-way merge) on G shards cut from one
+    index, every rank's answer against the unsharded ORACLE; the last parameter set has fewer than
+    m colliding points (T = 0: the quota is filled with the lowest-id zero scorers)."""
+    from paper_2411_14754_b200.sharded import Shard, emulate
+    base, qs = _gpu_corpus(oracle, G)
+    oidx = oracle.build_index(base, 4, 16, 3, 42, 0)
+    idx = gpu.load_index(oidx.serialize(), base)
+    shards = [Shard.cut(idx, r, G, block) for r in range(G)]
+    for a, b, k in GPU_PARAMS:
+        want_i, want_d, _ = oidx.knn_query_batch(base, qs, a, b, k)
+        for r, (ids, dd) in enumerate(emulate(shards, qs, gpu.CollisionParams(a, b, k))):
+            assert np.array_equal(ids, want_i), (G, block, r, a, b, k)
+            assert np.array_equal(dd, want_d), (G, block, r, a, b, k)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("G", [2, 4])
+def test_gpu_sharded_query_float_rows_and_half_mode(gpu, oracle, G, monkeypatch):
+    """Float rows (the fp32-screened re-rank), a shuffled layout, and the half-width dense select
+    (config 5's mode) on the shards."""
+    from paper_2411_14754_b200.sharded import Shard, emulate
+    monkeypatch.setenv("SUCO_DENSE_HALF", "2")
+    base, qs = _gpu_corpus(oracle, G, n=16000, d=24, nq=30, quant=False)
+    oidx = oracle.build_index(base, 3, 10, 3, 1, 1)
+    idx = gpu.load_index(oidx.serialize(), base)
+    shards = [Shard.cut(idx, r, G, 2048) for r in range(G)]
+    for a, b, k in ((0.05, 0.01, 10), (0.2, 0.002, 33)):
+        want_i, want_d, _ = oidx.knn_query_batch(base, qs, a, b, k)
+        for ids, dd in emulate(shards, qs, gpu.CollisionParams(a, b, k)):
+            assert np.array_equal(ids, want_i) and np.array_equal(dd, want_d), (G, a, b, k)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("G", [1, 2, 3, 8])
+@pytest.mark.parametrize("sampled", [False, True])
+def test_gpu_sharded_build_equals_cut_of_full_build(gpu, oracle, G, sampled):
+    """suco_gpu_build_shard (k-means jobs spread over the ranks, centroids broadcast, local rows
+    assigned, cell counts all-reduced), each rank given only its own rows: every shard equals the
+    same shard cut from the single-GPU build — centroids, local IMI — and answers like the oracle."""
+    from paper_2411_14754_b200.sharded import Comm, Shard, run_ranks, shard_ids
+    n, block = 24000, 2048
+    full = oracle.clustered(n + 40, 24, 30, 500 + G, 0, 100, 8, True)
+    base, qs = oracle.hold_out(full, 40, 501)
+    params = gpu.IndexParams(4, 12, 3, 42)
+    train = np.sort(np.random.default_rng(G).choice(n, 3000, replace=False)).astype(np.uint32) if sampled else None
+    whole = gpu.build_index_sampled(base, train, params) if sampled else gpu.build_index(base, params)
+    comms = Comm.local(G)
+    built = run_ranks(lambda r: Shard.build(base[shard_ids(n, block, G, r)], n, params, block, comms[r],
+                                            train_ids=train), G)
+    for r in range(G):
+        cut = Shard.cut(whole, r, G, block)
+        assert built[r].shard_info() == cut.shard_info()
+        for s in range(params.num_subspaces):
+            a, b = built[r].subspace(s), cut.subspace(s)
+            for x, y in zip(a[:2], b[:2]):
+                assert np.array_equal(x, y), (G, r, s, "centroids")
+            nl = cut.shard_info()["n_local"]
+            assert np.array_equal(a[2], b[2]) and np.array_equal(a[3][:nl], b[3][:nl]), (G, r, s, "IMI")
+    blob = whole.serialize()
+    oidx = oracle.load_index(blob)
+    cp = (0.05, 0.01, 10)
+    want_i, want_d, _ = oidx.knn_query_batch(base, qs, *cp)
+    outs = run_ranks(lambda r: built[r].knn_query_batch(comms[r], qs, gpu.CollisionParams(*cp)), G)
+    for ids, dd in outs:
+        assert np.array_equal(ids, want_i) and np.array_equal(dd, want_d), (G, sampled)
+    for c in comms:
+        c.close()
+
+
+@pytest.mark.gpu
+def test_gpu_sharded_build_error_reaches_every_rank(gpu):
+    """A non-finite value in one rank's rows fails the build on every rank (no rank left blocked)."""
+    from paper_2411_14754_b200.sharded import Comm, Shard, run_ranks, shard_ids
+    n, block, G = 8192, 2048, 2
+    base = np.random.default_rng(1).integers(0, 50, size=(n, 8)).astype(np.float32)
+    base[5000, 3] = np.inf  # block 2: rank 0
+    comms = Comm.local(G)
+    errs = []
+
+    def one(r):
+        try:
+            Shard.build(base[shard_ids(n, block, G, r)], n, gpu.IndexParams(2, 4, 2, 42), block, comms[r])
+        except gpu.Error as e:
+            errs.append((r, type(e).__name__))
+    run_ranks(one, G)
+    assert sorted(errs) == [(0, "ContractError"), (1, "ContractError")]
+
+
+@pytest.mark.gpu
+def test_gpu_shard_exchange_volume(gpu, oracle):
+    """Bytes each rank sends per query: 64 (totals) + 4 x ceil(#blocks / G) (tie counts) + 12 k
+    (local top-k) — the two-round exchange, not the per-piece histograms."""
+    from paper_2411_14754_b200.sharded import Comm, Shard, run_ranks
+    base, qs = _gpu_corpus(oracle, 4)
     idx = gpu.build_index(base, gpu.IndexParams(4, 16, 3, 42))
-    shards = [GpuShard(idx, r, G, block) for r in range(G)]
-    q = torch.from_numpy(qs).cuda()
-    # last case: fewer than m points collide at all, so T = 0 and zero-score ties fill the quota
-    for a, b, k in ((0.05, 0.005, 10), (0.02, 0.05, 40), (0.3, 0.001, 3), (0.001, 0.4, 5)):
-        want_i, want_d = idx.knn_query_batch(qs, gpu.CollisionParams(a, b, k))
-        ids, dd = emulate(shards, q, gpu.CollisionParams(a, b, k))
-        assert np.array_equal(ids.cpu().numpy().astype(np.uint32), want_i), (G, block, a, b, k)
-        assert np.array_equal(dd.cpu().numpy(), want_d), (G, block, a, b, k)
+    G, block = 4, 2048
+    shards = [Shard.cut(idx, r, G, block) for r in range(G)]
+    ctxs = [s.context() for s in shards]
+    comms = Comm.local(G)
+    cp = gpu.CollisionParams(0.05, 0.005, 10)
+    run_ranks(lambda r: shards[r].knn_query_batch(comms[r], qs, cp, scratch=ctxs[r]), G)
+    nb = -(-len(base) // block)
+    want = len(qs) * (64 + 4 * (-(-nb // G)) + 12 * cp.k)
+    assert all(c.exchange_bytes() == want for c in ctxs), [c.exchange_bytes() for c in ctxs]
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("G,block", [(1, 4096), (2, 2048), (3, 6144), (4, None), (8, 2048)])
-def test_gpu_emulated_split_traversal_matches_unsharded(gpu, oracle, G, block):
-    """Query-split protocol: each emulated shard traverses its slice of the batch; phases 1 and 2
-    run on the concatenated cell lists (dense select)."""
-    from paper_2411_14754_b200.sharded import GpuShard, emulate
-    full = oracle.clustered(20000 + 50, 32, 40, 177 + G, 20, 140, 18, True)
-    base, qs = oracle.hold_out(full, 50, 178)
+def test_gpu_shard_errors(gpu, oracle):
+    from paper_2411_14754_b200.sharded import Comm, Shard
+    base, qs = _gpu_corpus(oracle, 2)
     idx = gpu.build_index(base, gpu.IndexParams(4, 16, 3, 42))
-    shards = [GpuShard(idx, r, G, block) for r in range(G)]
-    assert all(s.split_traversal for s in shards)
-    q = torch.from_numpy(qs).cuda()
-    for a, b, k in ((0.05, 0.005, 10), (0.02, 0.05, 40), (0.001, 0.4, 5)):
-        want_i, want_d = idx.knn_query_batch(qs, gpu.CollisionParams(a, b, k))
-        ids, dd = emulate(shards, q, gpu.CollisionParams(a, b, k), split=True)
-        assert np.array_equal(ids.cpu().numpy().astype(np.uint32), want_i), (G, block, a, b, k)
-        assert np.array_equal(dd.cpu().numpy(), want_d), (G, block, a, b, k)
-
-
-@pytest.mark.gpu
-def test_gpu_shard_float_data(gpu, oracle):
-    from paper_2411_14754_b200.sharded import GpuShard, emulate
-    base = oracle.clustered(6000, 24, 12, 9, 0.0, 1.0, 0.05, False)
-    qs = oracle.uniform(30, 24, 10, 0.0, 1.0)
-    idx = gpu.build_index(base, gpu.IndexParams(3, 10, 3, 1, gpu.SubspaceMode.Shuffled))
-    shards = [GpuShard(idx, r, 4, 300) for r in range(4)]
-    cp = gpu.CollisionParams(0.05, 0.01, 10)
-    want_i, want_d = idx.knn_query_batch(qs, cp)
-    ids, dd = emulate(shards, torch.from_numpy(qs).cuda(), cp)
-    assert np.array_equal(ids.cpu().numpy().astype(np.uint32), want_i)
-    assert np.array_equal(dd.cpu().numpy(), want_d)
+    with pytest.raises(gpu.ConfigError):
+        Shard.cut(idx, 0, 2, 1000)  # not a multiple of 2048
+    with pytest.raises(gpu.ConfigError):
+        Shard.cut(idx, 2, 2, 2048)
+    sh = Shard.cut(idx, 1, 2, 2048)
+    comms = Comm.local(2)
+    with pytest.raises(gpu.ContractError):  # rank 0's member does not hold shard 1
+        sh.knn_query_batch(comms[0], qs, gpu.CollisionParams())
+    with pytest.raises(gpu.ContractError):
+        idx.knn_query_batch(qs, gpu.CollisionParams(), scratch=sh.context())  # another index's context
+    with pytest.raises(gpu.ContractError):
+        sh.serialize()
