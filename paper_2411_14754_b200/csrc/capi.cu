@@ -616,16 +616,23 @@ uint64_t per_query_bytes(const suco_gpu_index* x, uint64_t m, uint32_t k) {
     return per;
 }
 
-// Tile size from the memory budget: SUCO_SCRATCH_MB, else half of what is free on the device
-// (plus what this context already holds), at most 16 GB per slot.
-uint64_t tile_size(const suco_gpu_index* x, const suco_gpu_query_ctx* c, uint64_t nq, uint64_t m, uint32_t k) {
-    uint64_t budget = x->tune.scratch_bytes;
-    if (!budget) {
+// Scratch budget of a context: SUCO_SCRATCH_MB, else (first use) half of the device memory free
+// at that time, at most 32 GB; a failed allocation halves it (run_pipeline). Cached, so a query
+// call makes no cudaMemGetInfo round trip.
+uint64_t ctx_budget(const suco_gpu_index* x, suco_gpu_query_ctx* c) {
+    if (x->tune.scratch_bytes) return x->tune.scratch_bytes;
+    if (!c->budget) {
         size_t free_b = 0, total_b = 0;
         CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
-        const uint64_t held = c->slot[0].bytes() + c->slot[1].bytes();
-        budget = std::min<uint64_t>(32ull << 30, (free_b + held) / 2);
-        if (x->dense) budget = budget > 2 * kDenseBufExtra ? budget - 2 * kDenseBufExtra : budget / 2;
+        c->budget = std::max<uint64_t>(64ull << 20, std::min<uint64_t>(32ull << 30, free_b / 2));
+    }
+    return c->budget;
+}
+
+uint64_t tile_size(const suco_gpu_index* x, suco_gpu_query_ctx* c, uint64_t nq, uint64_t m, uint32_t k) {
+    uint64_t budget = ctx_budget(x, c);
+    if (x->dense && !x->tune.scratch_bytes) {
+        budget = budget > 2 * kDenseBufExtra ? budget - 2 * kDenseBufExtra : budget / 2;
     }
     const uint64_t per = per_query_bytes(x, m, k);
     return std::max<uint64_t>(1, std::min<uint64_t>(nq, budget / 2 / per));
@@ -704,6 +711,7 @@ void run_pipeline(const suco_gpu_index* x, suco_gpu_query_ctx* c, const float* h
             for (cudaStream_t s : c->pipe) CUDA_TRY(cudaStreamSynchronize(s));
             for (auto& sl : c->slot) sl.release_all();
             tile = (tile + 1) / 2;  // resume at the tile whose scratch did not fit
+            c->budget = std::max<uint64_t>(64ull << 20, c->budget / 2);
         }
     }
     CUDA_TRY(cudaEventRecord(c->ev_out, s_rr));

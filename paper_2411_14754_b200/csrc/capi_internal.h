@@ -143,6 +143,8 @@ struct suco_gpu_query_ctx {
     suco_gpu::DevBuf<uint64_t> sh_need;
     suco_gpu::DevBuf<double> sh_sq, sh_sq_all;
     uint64_t exchange_bytes = 0;  // bytes this rank sent through the communicator in the last call
+    uint64_t budget = 0;          // scratch budget (bytes): set on first use from free memory, halved on OOM
+    uint64_t sh_key[3] = {0, 0, 0}, sh_tiles = 0;  // shard tile count agreed for (nq, m, k)
     // stage profiling (suco_gpu_query_ctx_set_profiling)
     bool profile = false;
     std::vector<cudaEvent_t> events;  // pairs (start, end) per profiled stage launch

@@ -76,14 +76,22 @@ void shard_run(const suco_gpu_index* x, suco_gpu_query_ctx* c, suco_comm* comm, 
     const uint64_t nc = x->host.layout.ns > 8 ? 2 : 1;
     const uint64_t per = uint64_t(x->host.layout.ns) * x->K * 4 + 64 + m * 4 + (k > 32 ? m * 12 : 0) + qlen * 4 +
                          uint64_t(G) * (64 + nbl_max * 4 + k * 12) + nbl_max * 8 + P * (16 * nc + 8) + k * 12;
-    uint64_t budget = x->tune.scratch_bytes;
-    if (!budget) {
-        size_t free_b = 0, total_b = 0;
-        CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
-        budget = std::min<uint64_t>(32ull << 30, (free_b + c->slot[0].bytes()) / 2);
+    // the tile count is agreed once per (nq, m, k) and cached (the agreement is a host round trip)
+    if (c->sh_key[0] != nq || c->sh_key[1] != m || c->sh_key[2] != k || !c->sh_tiles) {
+        uint64_t budget = x->tune.scratch_bytes;
+        if (!budget) {
+            if (!c->budget) {
+                size_t free_b = 0, total_b = 0;
+                CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+                c->budget = std::max<uint64_t>(64ull << 20, std::min<uint64_t>(32ull << 30, free_b / 2));
+            }
+            budget = c->budget;
+        }
+        const uint64_t fit = std::max<uint64_t>(1, budget / per);
+        c->sh_tiles = agree_max(comm, (nq + fit - 1) / fit, s);
+        c->sh_key[0] = nq, c->sh_key[1] = m, c->sh_key[2] = k;
     }
-    const uint64_t tiles = agree_max(comm, (nq + std::max<uint64_t>(1, budget / per) - 1) /
-                                               std::max<uint64_t>(1, budget / per), s);
+    const uint64_t tiles = c->sh_tiles;
     const uint64_t tile = (nq + tiles - 1) / tiles;
     begin_call(c, nq, m, s);
     const uint64_t sent0 = comm->bytes_sent;
