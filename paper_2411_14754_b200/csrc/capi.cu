@@ -203,6 +203,16 @@ void upload_data(suco_gpu_index* x, const float* data, uint64_t n, uint32_t d) {
         x->data8.reserve(n * x->dpad);
         CUDA_TRY(launch_pack_u8(x->data.p, n, d, x->dpad, x->data8.p, x->own));
     }
+    // other rows: an int8 copy with per-row bound terms for the re-rank's certified screen (a
+    // quarter of the f32 row bytes; rerank_q8_kernel)
+    x->qpad = x->qrec = 0;
+    if (!x->dpad && x->tune.q8 && d % 4 == 0 && d <= 128) {
+        x->qpad = (d + 15) / 16 * 16;
+        x->qrec = (x->qpad + 16 + 63) / 64 * 64;  // whole 64-byte DRAM granules per record
+        x->q8.reserve(n * x->qrec);
+        CUDA_TRY(launch_pack_q8(x->data.p, n, d, x->qpad, x->qrec, x->q8.p, x->own));
+        CUDA_TRY(cudaStreamSynchronize(x->own));
+    }
 }
 
 // Layout + centroid tables on the device, from x->host.
@@ -449,6 +459,9 @@ void rerank_args(const suco_gpu_index* x, RerankArgs& ra) {
     ra.data_int_max = x->data_int_max;
     ra.data8 = x->dpad ? x->data8.p : nullptr;
     ra.dpad = x->dpad;
+    ra.q8 = x->qpad ? x->q8.p : nullptr;
+    ra.qpad = x->qpad;
+    ra.qrec = x->qrec;
     ra.u8_regs = x->tune.rerank_u8_regs;
     ra.pipe = x->tune.rerank_pipe == 2 ? 0 : x->tune.rerank_pipe == 1 ? 1 : 2;
 }
@@ -596,10 +609,23 @@ void stage_rerank(const suco_gpu_index* x, suco_gpu_query_ctx* c, suco_gpu_query
             ra.qskip = fl->qflag;
         }
     }
+    DevBuf<unsigned long long> stats;
+    if (x->tune.rerank_stats && ra.q8) {
+        stats.reserve(2);
+        CUDA_TRY(cudaMemsetAsync(stats.p, 0, 16, st));
+        ra.screen_stats = stats.p;
+    }
     if (ev) CUDA_TRY(cudaEventRecord(ev[0], st));
     CUDA_TRY(launch_rerank(ra, nt, st));
     c->launches += (ra.data8 ? 2 : 1) + (k > 32 ? 1 : 0);  // u8 + fp32/fp64 kernels, generic top-k
     if (ev) CUDA_TRY(cudaEventRecord(ev[1], st));
+    if (ra.screen_stats) {  // diagnostics
+        unsigned long long h[2] = {0, 0};
+        CUDA_TRY(cudaMemcpyAsync(h, stats.p, 16, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        std::fprintf(stderr, "[suco] int8 screen: %llu queries, %.1f exact re-ranks per query, %llu re-ranked in full\n",
+                     static_cast<unsigned long long>(nt), double(h[0]) / double(nt), h[1]);
+    }
 }
 
 // Per-query scratch bytes of one pipeline tile (both slots hold one tile).

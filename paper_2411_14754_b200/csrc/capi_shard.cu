@@ -239,9 +239,12 @@ int suco_gpu_make_shard(const suco_gpu_index* full, uint32_t shard, uint32_t num
             x->n_global = n;
             x->data_int_max = full->data_int_max;
             x->dpad = full->dpad;
-            // rows of the owned blocks, back to back (and their u8 copies)
+            x->qpad = full->qpad;
+            x->qrec = full->qrec;
+            // rows of the owned blocks, back to back (and their u8 / int8 copies)
             x->data.reserve(n_local * d);
             if (x->dpad) x->data8.reserve(n_local * x->dpad);
+            if (x->qpad) x->q8.reserve(n_local * x->qrec);
             uint64_t lo = 0;
             for (uint64_t j = shard; j < nb; j += num_shards) {
                 const uint64_t len = std::min<uint64_t>(block, n - j * block);
@@ -250,6 +253,10 @@ int suco_gpu_make_shard(const suco_gpu_index* full, uint32_t shard, uint32_t num
                 if (x->dpad) {
                     CUDA_TRY(cudaMemcpyAsync(x->data8.p + lo * x->dpad, full->data8.p + j * block * x->dpad,
                                              len * x->dpad, cudaMemcpyDeviceToDevice, x->own));
+                }
+                if (x->qpad) {
+                    CUDA_TRY(cudaMemcpyAsync(x->q8.p + lo * x->qrec, full->q8.p + j * block * x->qrec, len * x->qrec,
+                                             cudaMemcpyDeviceToDevice, x->own));
                 }
                 lo += len;
             }

@@ -164,6 +164,12 @@ struct RerankArgs {
     const uint32_t* qskip;  // optional: queries with qskip[q] != 0 are left for a later pass
     const uint32_t* qlist;  // optional: re-rank only qlist[0 .. *nlist) (the grid still spans nq)
     const uint32_t* nlist;
+    const int8_t* q8;       // optional int8 screen records of float rows (n x qrec), rerank_q8_kernel's input:
+                            // qpad int8 values, then {s, |x|^2, ||s a|| (up), ||x - s a|| (up)} (s < 0: no
+                            // bounds), padded to a multiple of 64 bytes (the DRAM access granule)
+    uint32_t qpad;          // int8 bytes of a record (d rounded up to 16)
+    uint32_t qrec;          // record stride (qpad + 16 rounded up to 64)
+    unsigned long long* screen_stats;  // optional diagnostics: [0] += exact re-ranks, [1] += queries re-ranked in full
     bool u8_regs;           // Tuning::rerank_u8_regs: the register byte kernel instead of the smem ring
     uint8_t pipe;           // 0: certified fp32 screen (default), 1: pipelined fp64, 2: unpipelined
 };
@@ -201,6 +207,9 @@ cudaError_t launch_check_finite(const float* data, uint64_t count, int* flag, cu
 // out3[0] |= 1 non-integer, out3[1] = max |v| bits, out3[2] |= 1 negative (zero out3 first)
 cudaError_t launch_int_stats(const float* data, uint64_t count, unsigned int* out3, cudaStream_t st);
 cudaError_t launch_pack_u8(const float* data, uint64_t n, uint32_t d, uint32_t dpad, uint8_t* out, cudaStream_t st);
+// int8 screen records of float rows: n x qrec bytes (see RerankArgs::q8)
+cudaError_t launch_pack_q8(const float* data, uint64_t n, uint32_t d, uint32_t qpad, uint32_t qrec, int8_t* out,
+                           cudaStream_t st);
 
 // SC-Linear (sclinear.cu): exact per-subspace distances, top-c by stable sort.
 struct ScArgs {

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -686,6 +687,277 @@ __global__ void __launch_bounds__(kThreads, MINB) rerank_screen_kernel(RerankArg
     }
 }
 
+
+// ------------------------------------------------------- int8-screened float rows
+// Float rows (not u8-valued), d % 4 == 0, d <= 128: the screen reads an int8 copy of every row
+// (a quarter of the f32 bytes) instead of the f32 row. Row x = s*a + e_x with a = rint(x / s) in
+// [-127, 127], s = max|x| / 127; the query likewise q = t*b + e_q. With I = a.b (one IDP.4A per 4
+// dims, exact int32) and ||x - q||^2 = |x|^2 + |q|^2 - 2 x.q,
+//     |x.q - s t I| <= ||s a|| ||e_q|| + ||t b|| ||e_x|| + ||e_x|| ||e_q||          (Cauchy-Schwarz)
+// so every candidate gets certified bounds lo <= D <= up of the reference's fp64 distance D; the
+// per-row |x|^2, ||s a|| and ||e_x|| are stored beside the int8 row (rounded up where they bound),
+// and a relative slack of 2^-20 covers every fp32 / fp64 rounding involved (the reference's own
+// 4-chain sum is within ~1e-14 of the real value). The screen / survivor / exact-fp64 logic is
+// rerank_screen_kernel's: the k smallest upper bounds give tau; rows with lo <= tau survive into
+// a per-warp buffer; the CTA merges tau and re-ranks the survivors exactly from the f32 rows. A
+// row or query whose bounds are not finite always survives; a full buffer re-ranks the query
+// exactly from scratch.
+constexpr uint32_t kQ8Stages = 2;
+constexpr uint32_t kQ8Cap = 192;
+
+template <uint32_t NW>
+__global__ void __launch_bounds__(kThreads, 2) rerank_q8_kernel(RerankArgs a, uint32_t stride) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr uint32_t su = (NW + 1) | 1u;  // NW row words + 1 meta word, odd 16-byte stride
+    double* qd = reinterpret_cast<double*>(smem);                                     // d
+    const uint32_t per_warp = max(kQ8Stages * 32 * su * 16, kRows * stride * 4);      // ring / staging
+    unsigned char* wbase = smem + ((a.d * 8 + 15) / 16) * 16;
+    __shared__ uint32_t qpack[32];
+    __shared__ uint32_t sid[kWarps][kQ8Cap];
+    __shared__ float slo[kWarps][kQ8Cap];
+    __shared__ double md[kWarps * 32];
+    __shared__ uint32_t mi[kWarps * 32];
+    __shared__ double qpar[4];  // t, |q|^2, ||t b|| (up), ||e_q|| (up)
+    __shared__ double tau_cta;
+    __shared__ int ovf, qok;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    uint64_t q;
+    if (!rerank_query(a, q)) return;
+    const float* query = a.queries + q * a.d;
+    for (uint32_t i = tid; i < a.d; i += kThreads) qd[i] = static_cast<double>(query[i]);
+    if (warp == 0) {  // quantise the query (d <= 128: lane owns dims 4 lane .. 4 lane + 3)
+        float v[4], mx = 0.f;
+#pragma unroll
+        for (uint32_t j = 0; j < 4; ++j) {
+            const uint32_t i = 4 * lane + j;
+            v[j] = i < a.d ? query[i] : 0.f;
+            mx = fmaxf(mx, fabsf(v[j]));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
+        const float t = mx / 127.f;
+        double e2 = 0.0, b2 = 0.0, n2 = 0.0;
+        uint32_t packed = 0;
+#pragma unroll
+        for (uint32_t j = 0; j < 4; ++j) {
+            const float bq = t > 0.f ? fminf(127.f, fmaxf(-127.f, rintf(v[j] / t))) : 0.f;
+            const double e = static_cast<double>(v[j]) - static_cast<double>(t) * static_cast<double>(bq);
+            e2 += e * e;
+            b2 += static_cast<double>(bq) * static_cast<double>(bq);
+            n2 += static_cast<double>(v[j]) * static_cast<double>(v[j]);
+            packed |= (static_cast<uint32_t>(static_cast<int>(bq)) & 0xffu) << (8 * j);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            e2 += __shfl_xor_sync(kFull, e2, o);
+            b2 += __shfl_xor_sync(kFull, b2, o);
+            n2 += __shfl_xor_sync(kFull, n2, o);
+        }
+        qpack[lane] = packed;
+        if (lane == 0) {
+            qpar[0] = static_cast<double>(t);
+            qpar[1] = n2;
+            qpar[2] = static_cast<double>(t) * sqrt(b2) * (1.0 + 1e-12);
+            qpar[3] = sqrt(e2) * (1.0 + 1e-12);
+            qok = isfinite(n2) && isfinite(e2) && isfinite(qpar[2]);
+            ovf = 0;
+        }
+    }
+    __syncthreads();
+    int qv[NW][4];
+#pragma unroll
+    for (uint32_t w = 0; w < NW; ++w) {
+#pragma unroll
+        for (uint32_t j = 0; j < 4; ++j) qv[w][j] = static_cast<int>(qpack[4 * w + j]);
+    }
+    const double qt = qpar[0], n2q = qpar[1], Bq = qpar[2], rq = qpar[3];
+    const bool qfin = qok != 0;
+    uint4* ring = reinterpret_cast<uint4*>(wbase + warp * per_warp);
+    const uint32_t* cands = a.cands + q * a.m;
+    const uint64_t mq = a.counts ? a.counts[q] : a.m;
+    const uint64_t first = uint64_t(warp) * 32;
+    const uint64_t steps = mq > first ? (mq - first + 32 * kWarps - 1) / (32 * kWarps) : 0;
+    auto sbase = [&](uint64_t g) { return first + g * 32 * kWarps; };
+    auto load_id = [&](uint64_t g) -> uint32_t {
+        const uint64_t i = sbase(g) + lane;
+        if (g >= steps || i >= mq) return 0u;
+        return a.identity ? static_cast<uint32_t>(i) : __ldcs(cands + i);
+    };
+    uint32_t id0 = load_id(0), id1 = load_id(1);
+    auto issue = [&](uint64_t g) {
+        const uint32_t myid = (g & 1u) ? id1 : id0;
+        uint4* st = ring + static_cast<uint32_t>(g % kQ8Stages) * 32 * su;
+        const uint64_t b = sbase(g);
+#pragma unroll
+        for (uint32_t t = lane; t < 32 * (NW + 1); t += 32) {
+            const uint32_t row = t / (NW + 1), col = t % (NW + 1);
+            const uint32_t id = __shfl_sync(kFull, myid, row);
+            if (b + row < mq) cp_async16(st + row * su + col, a.q8 + uint64_t(id) * a.qrec + 16u * col);
+        }
+        if (g & 1u) id1 = load_id(g + 2);
+        else id0 = load_id(g + 2);
+        return myid;
+    };
+    uint32_t rowid[kQ8Stages];
+#pragma unroll
+    for (uint32_t i = 0; i < kQ8Stages; ++i) rowid[i] = 0;
+    for (uint32_t i = 0; i + 1 < kQ8Stages; ++i) {
+        if (i < steps) rowid[i] = issue(i);
+        cp_async_commit();
+    }
+    double sl = kInf;  // the k smallest upper bounds (lane i = entry i)
+    uint32_t nsurv = 0;
+    bool overflow = false;
+    for (uint64_t g = 0; g < steps; ++g) {
+        if (g + kQ8Stages - 1 < steps) {
+            const uint32_t v = issue(g + kQ8Stages - 1);
+            const uint32_t slot = static_cast<uint32_t>((g + kQ8Stages - 1) % kQ8Stages);
+#pragma unroll
+            for (uint32_t i = 0; i < kQ8Stages; ++i) {
+                if (i == slot) rowid[i] = v;
+            }
+        }
+        cp_async_commit();
+        cp_async_wait<kQ8Stages - 1>();
+        __syncwarp();
+        const uint32_t slot = static_cast<uint32_t>(g % kQ8Stages);
+        uint32_t myid = rowid[0];
+#pragma unroll
+        for (uint32_t i = 1; i < kQ8Stages; ++i) {
+            if (i == slot) myid = rowid[i];
+        }
+        const uint4* row = ring + slot * 32 * su + lane * su;
+        int c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+#pragma unroll
+        for (uint32_t w = 0; w < NW; ++w) {
+            const uint4 x = row[w];
+            c0 = __dp4a(static_cast<int>(x.x), qv[w][0], c0);
+            c1 = __dp4a(static_cast<int>(x.y), qv[w][1], c1);
+            c2 = __dp4a(static_cast<int>(x.z), qv[w][2], c2);
+            c3 = __dp4a(static_cast<int>(x.w), qv[w][3], c3);
+        }
+        const uint4 mw = row[NW];
+        __syncwarp();  // the slot is refilled by the next step's issue
+        const int I = (c0 + c1) + (c2 + c3);
+        const float rs = __uint_as_float(mw.x), rn2 = __uint_as_float(mw.y);
+        const float rA = __uint_as_float(mw.z), rR = __uint_as_float(mw.w);
+        const uint64_t b = sbase(g);
+        const bool valid = b + lane < mq;
+        double lo = 0.0, up = kInf;
+        if (qfin && rs >= 0.f) {
+            const double dot = static_cast<double>(rs) * qt * static_cast<double>(I);
+            const double approx = static_cast<double>(rn2) + n2q - 2.0 * dot;
+            const double err = 2.0 * (static_cast<double>(rA) * rq + Bq * static_cast<double>(rR) +
+                                      static_cast<double>(rR) * rq);
+            const double slack = 9.5367431640625e-07 * (static_cast<double>(rn2) + n2q + 2.0 * fabs(dot)) + 1e-300;
+            lo = approx - err - slack;
+            up = approx + err + slack;
+        }
+        const double tau0 = __shfl_sync(kFull, sl, a.k - 1);
+        uint32_t bal = __ballot_sync(kFull, valid && up < tau0);
+        while (bal) {
+            const uint32_t src = __ffs(bal) - 1;
+            bal &= bal - 1;
+            const double v = __shfl_sync(kFull, up, src);
+            if (v < __shfl_sync(kFull, sl, a.k - 1)) list_insert_val(v, sl, a.k, lane);
+        }
+        const double tau = __shfl_sync(kFull, sl, a.k - 1);
+        const uint32_t pass = __ballot_sync(kFull, valid && lo <= tau);
+        if (pass && !overflow) {
+            const uint32_t cnt = __popc(pass);
+            if (nsurv + cnt > kQ8Cap) {  // drop buffered rows the tighter tau now excludes
+                uint32_t kept = 0;
+                for (uint32_t t0 = 0; t0 < nsurv; t0 += 32) {
+                    const uint32_t t = t0 + lane;
+                    const bool in = t < nsurv;
+                    const uint32_t idv = in ? sid[warp][t] : 0u;
+                    const float lv = in ? slo[warp][t] : 0.f;
+                    const bool keep = in && static_cast<double>(lv) <= tau;
+                    const uint32_t kb = __ballot_sync(kFull, keep);
+                    __syncwarp();
+                    if (keep) {
+                        const uint32_t p = kept + __popc(kb & ((1u << lane) - 1u));
+                        sid[warp][p] = idv;
+                        slo[warp][p] = lv;
+                    }
+                    kept += __popc(kb);
+                    __syncwarp();
+                }
+                nsurv = kept;
+            }
+            if (nsurv + cnt > kQ8Cap) {
+                overflow = true;
+            } else {
+                if ((pass >> lane) & 1u) {
+                    const uint32_t p = nsurv + __popc(pass & ((1u << lane) - 1u));
+                    sid[warp][p] = myid;
+                    slo[warp][p] = __double2float_rd(lo);
+                }
+                nsurv += cnt;
+            }
+            __syncwarp();
+        }
+    }
+    cp_async_wait<0>();
+    if (overflow && lane == 0) atomicOr(&ovf, 1);
+    md[warp * 32 + lane] = sl;
+    __syncthreads();
+    if (warp == 0) {
+        for (uint32_t w = 1; w < kWarps; ++w) {
+            for (uint32_t i = 0; i < a.k; ++i) {
+                const double v = md[w * 32 + i];
+                if (!(v < __shfl_sync(kFull, sl, a.k - 1))) break;  // lists are sorted
+                list_insert_val(v, sl, a.k, lane);
+            }
+        }
+        const double t = __shfl_sync(kFull, sl, a.k - 1);
+        if (lane == 0) tau_cta = t;
+    }
+    __syncthreads();
+    const double tau = tau_cta;
+    double ld = kInf;
+    uint32_t lid = 0xffffffffu;
+    float* st = reinterpret_cast<float*>(ring);  // the drained ring is staging now
+    if (ovf) {  // exact re-rank of the whole query, the warps splitting the candidates
+        const uint64_t per = (mq + kWarps - 1) / kWarps, lo = min_u64(mq, warp * per), hi = min_u64(mq, lo + per);
+        if (a.screen_stats && tid == 0) atomicAdd(a.screen_stats + 1, 1ull);
+        exact_rows(a, st, stride, qd, hi - lo,
+                   [&](uint64_t t) { return a.identity ? static_cast<uint32_t>(lo + t) : cands[lo + t]; }, ld, lid, lane);
+    } else {
+        uint32_t kept = 0;  // survivors: buffered rows whose lower bound is within the CTA's tau
+        for (uint32_t t0 = 0; t0 < nsurv; t0 += 32) {
+            const uint32_t t = t0 + lane;
+            const bool in = t < nsurv;
+            const uint32_t idv = in ? sid[warp][t] : 0u;
+            const bool keep = in && static_cast<double>(slo[warp][t]) <= tau;
+            const uint32_t kb = __ballot_sync(kFull, keep);
+            __syncwarp();
+            if (keep) sid[warp][kept + __popc(kb & ((1u << lane) - 1u))] = idv;
+            kept += __popc(kb);
+            __syncwarp();
+        }
+        if (a.screen_stats && lane == 0) atomicAdd(a.screen_stats, static_cast<unsigned long long>(kept));
+        exact_rows(a, st, stride, qd, kept, [&](uint64_t t) { return sid[warp][t]; }, ld, lid, lane);
+    }
+    __syncthreads();
+    md[warp * 32 + lane] = ld;
+    mi[warp * 32 + lane] = lid;
+    __syncthreads();
+    if (warp == 0) {
+        for (uint32_t w = 1; w < kWarps; ++w) {
+            for (uint32_t i = 0; i < a.k; ++i) {
+                const double dv = md[w * 32 + i];
+                if (dv == kInf) break;
+                warp_insert(dv, mi[w * 32 + i], ld, lid, a.k, lane);
+            }
+        }
+        if (lane < a.k) {
+            a.out_ids[q * a.k + lane] = lid;
+            a.out_dists[q * a.k + lane] = a.squared ? ld : __dsqrt_rn(ld);
+        }
+    }
+}
+
 // ---------------------------------------------------------------- u8 rows
 // Data certified integer in [0, 255] at upload and a query of the same kind:
 // every (x - q)^2 is an integer and every partial sum stays below 2^32, so
@@ -1068,6 +1340,19 @@ cudaError_t launch_rerank(const RerankArgs& a, uint64_t nq, cudaStream_t st) {
         if (e != cudaSuccess) return e;
     }
     const int pmode = a.pipe == 0 ? 2 : a.pipe == 1 ? 1 : 0;  // 2 screened, 1 pipelined fp64, 0 unpipelined
+    if (vec && !generic && pmode == 2 && a.q8 && a.qpad >= 16 && a.qpad <= 128) {  // int8 screen
+        const uint32_t stride = 32 * ((min(a.d, kChunk) + 31) / 32) + 4;
+        const uint32_t nwq = a.qpad / 16, su = (nwq + 1) | 1u;
+        const size_t per_warp = std::max<size_t>(size_t(kQ8Stages) * 32 * su * 16, size_t(kRows) * stride * 4);
+        const size_t qsmem = ((a.d * 8 + 15) / 16) * 16 + kWarps * per_warp;
+        using KQ = void (*)(RerankArgs, uint32_t);
+        const KQ kq[8] = {rerank_q8_kernel<1>, rerank_q8_kernel<2>, rerank_q8_kernel<3>, rerank_q8_kernel<4>,
+                          rerank_q8_kernel<5>, rerank_q8_kernel<6>, rerank_q8_kernel<7>, rerank_q8_kernel<8>};
+        e = cudaFuncSetAttribute(kq[nwq - 1], cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(qsmem));
+        if (e != cudaSuccess) return e;
+        kq[nwq - 1]<<<static_cast<unsigned>(nq), kThreads, qsmem, st>>>(a, stride);
+        return cudaGetLastError();
+    }
     if (vec && !generic && pmode == 2) {
         const uint32_t stride = 32 * ((min(a.d, kChunk) + 31) / 32) + 4;  // = 4 (mod 32): conflict-free chains
         const size_t qbytes = ((a.d * 4 + 15) / 16) * 16 + ((a.d * 8 + 15) / 16) * 16;

@@ -14,6 +14,7 @@ namespace suco_gpu {
 struct Tuning {
     int cluster = 0;             // SUCO_CLUSTER: cluster-counting select cluster size (0 = by occupancy)
     bool no_u8 = false;          // SUCO_NO_U8: never keep a byte copy of u8-valued rows
+    bool q8 = true;              // SUCO_Q8=0: no int8 screen copy of float rows (the fp32 screen reads f32 rows)
     bool dense = true;           // SUCO_DENSE=0: the cluster-counting select only
     int dense_half = 1;          // SUCO_DENSE_HALF: 0 never, 1 when 32-bit masks do not fit, 2 force
     bool dense_fused = true;     // SUCO_DENSE_FUSED=0: the two-pass dense select
@@ -22,6 +23,7 @@ struct Tuning {
     bool dense_nocut = false;    // SUCO_DENSE_NOCUT=1: store every tie (tests)
     uint32_t dense_words = 0;    // SUCO_DENSE_WORDS: mask words per slot (0 auto, 1, 2)
     bool dense_stats = false;    // SUCO_DENSE_STATS=1: print the single-pass fallback rate (diagnostics)
+    bool rerank_stats = false;   // SUCO_RERANK_STATS=1: print the int8 screen's exact re-rank counts (diagnostics)
     uint32_t tiles = 1;          // SUCO_TILES: minimum pipeline tiles per batch (tests: slot reuse)
     uint64_t scratch_bytes = 0;  // SUCO_SCRATCH_MB: query scratch budget per context (0 = from free memory)
     int fb_overlap = -1;         // SUCO_FB_OVERLAP: overlapped dense fallback (-1 auto, 0, 1)

@@ -66,6 +66,58 @@ __global__ void pack_u8_kernel(const float* data, uint64_t n, uint32_t d, uint32
 
 }  // namespace
 
+// One warp per row: s = max|x| / 127, a = rint(x / s) in [-127, 127] (zero padding to qpad), and
+// the row's bound terms (rerank_q8_kernel): |x|^2 (fp64 sum, rounded to f32), ||s a|| and
+// ||x - s a|| (fp64, rounded up). A row whose terms are not finite gets s = -1: it always survives
+// the screen.
+__global__ void pack_q8_kernel(const float* __restrict__ data, uint64_t n, uint32_t d, uint32_t qpad, uint32_t qrec,
+                               int8_t* __restrict__ out) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x / 32);
+    for (uint64_t r = blockIdx.x * uint64_t(blockDim.x / 32) + (threadIdx.x >> 5); r < n; r += warps) {
+        const float* x = data + r * d;
+        float mx = 0.f;
+        for (uint32_t i = lane; i < d; i += 32) mx = fmaxf(mx, fabsf(x[i]));
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        const float s = mx / 127.f;
+        double e2 = 0.0, a2 = 0.0, n2 = 0.0;
+        for (uint32_t i = lane; i < qpad; i += 32) {
+            float av = 0.f;
+            if (i < d) {
+                const float v = x[i];
+                av = s > 0.f ? fminf(127.f, fmaxf(-127.f, rintf(v / s))) : 0.f;
+                const double e = static_cast<double>(v) - static_cast<double>(s) * static_cast<double>(av);
+                e2 += e * e;
+                a2 += static_cast<double>(av) * static_cast<double>(av);
+                n2 += static_cast<double>(v) * static_cast<double>(v);
+            }
+            out[r * qrec + i] = static_cast<int8_t>(av);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+            a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+            n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+        }
+        if (lane == 0) {
+            const double A = static_cast<double>(s) * sqrt(a2) * (1.0 + 1e-12);
+            const double R = sqrt(e2) * (1.0 + 1e-12);
+            const float fn2 = __double2float_rn(n2), fA = __double2float_ru(A), fR = __double2float_ru(R);
+            const bool ok = isfinite(fn2) && isfinite(fA) && isfinite(fR) && isfinite(s);
+            *reinterpret_cast<float4*>(out + r * qrec + qpad) = ok ? make_float4(s, fn2, fA, fR)
+                                                                     : make_float4(-1.f, 0.f, 0.f, 0.f);
+            for (uint32_t i = qpad + 16; i < qrec; ++i) out[r * qrec + i] = 0;
+        }
+    }
+}
+
+cudaError_t launch_pack_q8(const float* data, uint64_t n, uint32_t d, uint32_t qpad, uint32_t qrec, int8_t* out,
+                           cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    const uint64_t blocks = min_u64((n + 7) / 8, 148ull * 16);
+    pack_q8_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(data, n, d, qpad, qrec, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_pack_u8(const float* data, uint64_t n, uint32_t d, uint32_t dpad, uint8_t* out, cudaStream_t st) {
     const uint64_t blocks = min_u64((n * dpad + 255) / 256, 148ull * 16);
     pack_u8_kernel<<<static_cast<unsigned>(blocks ? blocks : 1), 256, 0, st>>>(data, n, d, dpad, out);
@@ -105,6 +157,7 @@ Tuning tuning_from_env() {
     const int c = env_int("SUCO_CLUSTER", 0);
     t.cluster = (c >= 1 && c <= 16) ? c : 0;
     t.no_u8 = std::getenv("SUCO_NO_U8") != nullptr;
+    t.q8 = env_int("SUCO_Q8", 1) != 0;
     t.dense = env_int("SUCO_DENSE", 1) != 0;
     t.dense_half = env_int("SUCO_DENSE_HALF", 1);
     t.dense_fused = env_int("SUCO_DENSE_FUSED", 1) != 0;
@@ -115,6 +168,7 @@ Tuning tuning_from_env() {
     const int w = env_int("SUCO_DENSE_WORDS", 0);
     t.dense_words = (w == 1 || w == 2) ? static_cast<uint32_t>(w) : 0u;
     t.dense_stats = std::getenv("SUCO_DENSE_STATS") != nullptr;
+    t.rerank_stats = std::getenv("SUCO_RERANK_STATS") != nullptr;
     const int tl = env_int("SUCO_TILES", 1);
     t.tiles = tl > 1 ? static_cast<uint32_t>(tl) : 1u;
     const char* mb = std::getenv("SUCO_SCRATCH_MB");
