@@ -57,16 +57,32 @@ def dist_env():
 
 
 def ncu_traffic(workload: str) -> dict:
-    """Per-launch DRAM bytes (read + write) of each query kernel from the committed ncu
-    --set full capture of this workload (profiles/ncu_traffic.json), else {}."""
+    """Per-stage ncu evidence of one query step of this config (profiles/ncu_traffic.json, written by
+    tools/ncu_traffic.py): DRAM bytes (read + write) and, where captured, the binding pipes of the
+    stage's top kernel. {} if the config was not profiled."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             t = json.load(f)
     except (OSError, ValueError):
         return {}
-    if t.get("workload") != workload:
+    w = t.get("workloads", {}).get(workload)
+    if not w:
         return {}
-    return {k: v["dram_read_bytes"] + v["dram_write_bytes"] for k, v in t["kernels"].items()}
+    return {k: {"dram_bytes": v["dram_read_bytes"] + v["dram_write_bytes"], "pipes": v.get("pipes"),
+                "ncu_ms": v.get("duration_ms")} for k, v in w["kernels"].items()}
+
+
+def rerank_row_bytes(base, queries):
+    """Bytes the re-rank reads per candidate row: the u8 copy (d padded to 16) for u8-valued data,
+    else the int8 screen record (d padded to 16, + 16 bytes of bound terms, padded to 64) when
+    d % 4 == 0 and d <= 128 (capi.cu upload_data), else the f32 row."""
+    d = base.shape[1]
+    u8 = u8_row_bytes(base, queries)
+    if u8:
+        return u8, "u8 rows"
+    if d % 4 == 0 and d <= 128 and not os.environ.get("SUCO_Q8") == "0":
+        return ((d + 15) // 16 * 16 + 16 + 63) // 64 * 64, "int8 screen records (+ exact f32 rows of the survivors)"
+    return 4 * d, "f32 rows"
 
 
 def u8_row_bytes(base, queries):
@@ -401,36 +417,44 @@ def main():
         quality = {"queries": sample, "recall_at_k": float(np.mean(rec)), "mre": float(np.mean(err)),
                    "ground_truth": "suco_gpu_exact_knn_batch", "ground_truth_s": gt_s}
 
-    # roofline of the dominant kernel (SURVEY §8(d) algorithmic bytes)
+    # roofline of the dominant stage against the bytes it really moves: the re-rank's rows (u8 /
+    # int8-record / f32 bytes per candidate), the select's DRAM bytes measured by ncu (it reads
+    # L2-resident point codes, not inverted lists); SURVEY §8(d)'s id-equivalent bytes (u32
+    # inverted-list ids + f32 candidate rows) are kept as a labelled secondary figure
     peak, peak_src = measured_peaks()
     cum, sq, m = stats
     stage_avg = stage_ms / args.steps
-    bytes_select = 4.0 * cum                      # u32 inverted-list ids streamed (query.cpp:235-239)
-    # candidate rows + query (query.cpp:177-182), defined on the f32 API type; when
-    # the data and queries are integers in [0, 255] the library re-ranks from byte rows instead
-    # (exact) and moves `row_bytes` per row — reported beside, not substituted
-    row_bytes = u8_row_bytes(base, queries) or 4 * d
-    bytes_rerank = 4.0 * d * m * sq + 4.0 * d * sq
+    row_bytes, row_kind = rerank_row_bytes(base, queries)
+    traffic = ncu_traffic(cfg.name)
     names = ["traverse", "select", "rerank"]
+    id_equiv = {"select": 4.0 * cum, "rerank": 4.0 * d * m * sq + 4.0 * d * sq}
+    moved = {"traverse": (traffic.get("traverse") or {}).get("dram_bytes", 0.0),
+             "select": (traffic.get("select") or {}).get("dram_bytes"),
+             "rerank": float(row_bytes) * m * sq + 4.0 * d * sq}
     per_kernel = {}
-    for i, (nm, b) in enumerate(zip(names, [None, bytes_select, bytes_rerank])):
-        per_kernel[nm] = {"ms": stage_avg[i], "algorithmic_bytes": b,
-                          **({"row_bytes_moved": row_bytes, "row_bytes_f32": 4 * d} if nm == "rerank" else {}),
-                          "achieved_gbs": (b / (stage_avg[i] / 1000.0) / 1e9) if b else None}
+    for i, nm in enumerate(names):
+        t = stage_avg[i] / 1000.0
+        b = moved[nm]
+        per_kernel[nm] = {"ms": stage_avg[i], "moved_bytes": b,
+                          "moved_source": "ncu dram bytes" if nm != "rerank" else f"model: {row_kind}, {row_bytes} B/row",
+                          "achieved_gbs": b / t / 1e9 if b else None, "frac": b / t / 1e9 / peak if b else None,
+                          "dram_bytes_ncu": (traffic.get(nm) or {}).get("dram_bytes"),
+                          "binding_pipes_ncu": (traffic.get(nm) or {}).get("pipes")}
+        if nm in id_equiv:
+            per_kernel[nm]["id_equivalent"] = {"bytes": id_equiv[nm], "gbs": id_equiv[nm] / t / 1e9,
+                                               "note": "SURVEY 8(d) bytes (u32 ids / f32 rows), not what moves"}
     dom = int(np.argmax(stage_avg))
     dom_name = names[dom]
-    dom_bytes = [bytes_select, bytes_select, bytes_rerank][dom] if dom else bytes_select
-    achieved = dom_bytes / (stage_avg[dom] / 1000.0) / 1e9
-    path_bytes = bytes_select + bytes_rerank
-    traffic = ncu_traffic(cfg.name)
-    for nm in names:
-        per_kernel[nm]["dram_bytes_ncu"] = traffic.get(nm)
-    roofline = {"bound": "hbm", "kernel": dom_name if dom else "traverse (bytes of select shown)",
-                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic.get(dom_name), "traffic_source": "profiles/ncu_traffic.json" if traffic else None,
-                "peak_source": peak_src,
-                "query_path": {"bytes_per_step": path_bytes, "achieved": path_bytes / (total_ms / ws / args.steps / 1e3) / 1e9,
-                               "frac": path_bytes / (total_ms / ws / args.steps / 1e3) / 1e9 / peak},
+    dk = per_kernel[dom_name]
+    step_s = total_ms / ws / args.steps / 1e3
+    path_bytes = sum(v for v in moved.values() if v)
+    roofline = {"bound": "hbm", "kernel": dom_name, "achieved": dk["achieved_gbs"], "peak": peak, "unit": "GB/s",
+                "frac": dk["frac"], "traffic": dk["dram_bytes_ncu"],
+                "traffic_source": "profiles/ncu_traffic.json" if traffic else None, "peak_source": peak_src,
+                "binding": dk["binding_pipes_ncu"],
+                "query_path": {"bytes_per_step": path_bytes, "achieved": path_bytes / step_s / 1e9,
+                               "frac": path_bytes / step_s / 1e9 / peak,
+                               "id_equivalent_frac": sum(id_equiv.values()) / step_s / 1e9 / peak},
                 "per_kernel": per_kernel}
 
     # CPU baseline (rank 0, N = 1): the reference itself on a bounded sample of the same queries
@@ -507,7 +531,7 @@ def main():
         "data": "synthetic (seeded Gaussian mixture, bench_data.py; stands in for SIFT1M-shape corpus)",
         "config": {"workload": cfg.describe(), "queries_per_step": nq, "index_build_s": build_s,
                    "index_source": args.index_source, "l2": "256 MiB flush write between timed steps",
-                   "rerank_rows": "u8" if row_bytes != 4 * d else "f32",
+                   "rerank_rows": row_kind,
                    "parallelism": f"replicas x{ws}"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "parity": parity, "quality": quality,
         "gpu_launches": launches_per_step * args.steps, "clocks": clocks.summary(),
