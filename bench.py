@@ -248,6 +248,7 @@ def main():
     ap.add_argument("--beta", type=float, default=None, help="experiment: override the config's beta")
     ap.add_argument("--n", type=int, default=None, help="experiment: override the config's point count")
     ap.add_argument("--queries", type=int, default=None, help="experiment: override the config's query count")
+    ap.add_argument("--k", type=int, default=None, help="override the config's k (the reference default is 50)")
     args = ap.parse_args()
     if args.no_u8:
         os.environ["SUCO_NO_U8"] = "1"  # read by the library at index upload
@@ -256,9 +257,9 @@ def main():
         import dataclasses
         cfg = dataclasses.replace(cfg, alpha=args.alpha if args.alpha is not None else cfg.alpha,
                                   beta=args.beta if args.beta is not None else cfg.beta)
-    if args.n is not None or args.queries is not None:
+    if args.n is not None or args.queries is not None or args.k is not None:
         import dataclasses
-        cfg = dataclasses.replace(cfg, n=args.n or cfg.n, queries=args.queries or cfg.queries)
+        cfg = dataclasses.replace(cfg, n=args.n or cfg.n, queries=args.queries or cfg.queries, k=args.k or cfg.k)
     sampled = cfg.train_sample < 1.0  # cfg5: centroids trained on a seeded sample (sampled build)
 
     if args.impl == "reference":

@@ -166,18 +166,6 @@ __global__ void kpp_update_kernel(const float* __restrict__ proj, const KJob* __
     if (blockIdx.x == 0 && threadIdx.x == 0) chosen[uint64_t(j) * n + p] = 1;
 }
 
-__device__ inline double block_sum_exact(double v, double* sh) {
-    // order-free: only used on certified integer-valued data (every partial sum exact)
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    __syncthreads();
-    if (lane == 0) sh[warp] = v;
-    __syncthreads();
-    double t = 0.0;
-    for (uint32_t w = 0; w < nw; ++w) t += sh[w];
-    return t;
-}
-
 // Chooses the next seed of job blockIdx.x (kmeans.cpp:75-111); one CTA per job.
 // prefix[i] receives the running fold; pick is the first i with prefix > target.
 __global__ void __launch_bounds__(256) kpp_select_kernel(const float* proj, const KJob* jobs, uint64_t n, uint32_t c,

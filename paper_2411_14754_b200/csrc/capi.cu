@@ -543,12 +543,34 @@ FbLists stage_select(const suco_gpu_index* x, suco_gpu_query_ctx* c, suco_gpu_qu
         // two-pass: piece histograms, plan, emission; single pass: sample, bound, fused pass, plan,
         // compaction, flagged list, fallback histograms, plan, emission
         c->launches += fused ? 10 : 3;
-        if (tn.dense_stats && fused) {  // diagnostics: the fallback rate
+        if (tn.dense_stats && fused) {  // diagnostics: the fallback rate, superset sizes
             uint32_t nflag = 0;
-            CUDA_TRY(cudaMemcpyAsync(&nflag, da.nmap, 4, cudaMemcpyDeviceToHost, split ? fb_st : st));
-            CUDA_TRY(cudaStreamSynchronize(split ? fb_st : st));
-            std::fprintf(stderr, "[suco] dense select: %u of %llu queries took the two-pass fallback (pstride %u)\n",
-                         nflag, static_cast<unsigned long long>(nt), da.pstride);
+            cudaStream_t ds = split ? fb_st : st;
+            std::vector<uint16_t> cc(nt * da.P);
+            std::vector<uint32_t> cut(nt), Lh(nt);
+            CUDA_TRY(cudaMemcpyAsync(&nflag, da.nmap, 4, cudaMemcpyDeviceToHost, ds));
+            CUDA_TRY(cudaMemcpyAsync(cc.data(), da.ccnt, cc.size() * 2, cudaMemcpyDeviceToHost, ds));
+            CUDA_TRY(cudaMemcpyAsync(cut.data(), da.pcut, nt * 4, cudaMemcpyDeviceToHost, ds));
+            CUDA_TRY(cudaMemcpyAsync(Lh.data(), da.L, nt * 4, cudaMemcpyDeviceToHost, ds));
+            CUDA_TRY(cudaStreamSynchronize(ds));
+            double entries = 0, nonzero = 0, before = 0, cuts = 0, dense = 0;
+            for (uint64_t q = 0; q < nt; ++q) {
+                cuts += cut[q];
+                dense += (Lh[q] & 0x100u) != 0;
+                for (uint32_t p = 0; p < da.P; ++p) {
+                    const uint16_t v = cc[q * da.P + p];
+                    entries += v;
+                    nonzero += v != 0;
+                    if (p < cut[q]) before += v;
+                }
+            }
+            std::fprintf(stderr,
+                         "[suco] dense select: %u of %llu queries took the two-pass fallback (pstride %u); superset "
+                         "%.0f entries/query (%.0f before the tie cut), %.1f%% of (query, piece) buffers used, mean "
+                         "cut %.0f of %u pieces, %.0f%% dense-staged queries, m = %llu, B = %u\n",
+                         nflag, static_cast<unsigned long long>(nt), da.pstride, entries / nt, before / nt,
+                         100.0 * nonzero / (double(nt) * da.P), cuts / nt, da.P, 100.0 * dense / nt,
+                         static_cast<unsigned long long>(m), da.B);
         }
         if (ev) CUDA_TRY(cudaEventRecord(ev[1], split ? fb_st : st));
         FbLists fl;

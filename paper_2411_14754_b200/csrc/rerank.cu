@@ -1290,7 +1290,160 @@ __global__ void __launch_bounds__(256) topk_generic_kernel(RerankArgs a) {
     }
 }
 
+// k > 32: the k smallest (dist, id) of a query's m scored candidates by MSB radix select on the
+// distance bits (non-negative doubles order like their bit patterns): 8-bit digits narrow the
+// bucket holding the k-th distance until it has at most kRxCap members (usually 3 passes over the
+// m distances), then one pass gathers the bucket and every smaller distance into shared memory,
+// where a bitonic sort by (dist, id) — a strict total order, so this is the reference's
+// nth_element + sort (query.cpp:185-189) — yields the k. A bucket that never fits (masses of
+// equal distances) or k > kRxCap / 2 takes the k-round kernel above.
+constexpr uint32_t kRxCap = 2048;
+
+__device__ __forceinline__ unsigned long long dbits(double d) {
+    return static_cast<unsigned long long>(__double_as_longlong(d));
+}
+
+__global__ void __launch_bounds__(1024) topk_radix_kernel(RerankArgs a, uint32_t* fallback) {
+    __shared__ uint32_t hist[256];
+    __shared__ unsigned long long key[kRxCap];
+    __shared__ uint32_t kid[kRxCap];
+    __shared__ uint32_t nsel, sbin, sbefore;
+    const uint32_t tid = threadIdx.x, nt = blockDim.x;
+    uint64_t q;
+    if (!rerank_query(a, q)) return;
+    const double* dd = a.all_d + q * a.m;
+    const uint32_t* ii = a.all_id + q * a.m;
+    const uint64_t mq = a.counts ? a.counts[q] : a.m;
+    const uint32_t kk = static_cast<uint32_t>(min_u64(a.k, mq));
+    unsigned long long prefix = 0, mask = 0;
+    uint32_t need = kk;           // rank of the k-th inside the current bucket (1-based)
+    uint64_t lt = 0;              // elements below the bucket
+    for (int shift = 56; shift >= 0 && kk; shift -= 8) {
+        for (uint32_t b = tid; b < 256; b += nt) hist[b] = 0;
+        __syncthreads();
+        for (uint64_t c = tid; c < mq; c += nt) {
+            const unsigned long long u = dbits(dd[c]);
+            if ((u & mask) == prefix) atomicAdd(&hist[(u >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (tid < 32) {  // the bin holding rank `need`: warp scan over 8 bins per lane
+            uint32_t loc[8], sum = 0;
+#pragma unroll
+            for (uint32_t j = 0; j < 8; ++j) {
+                loc[j] = hist[tid * 8 + j];
+                sum += loc[j];
+            }
+            uint32_t incl = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(kFull, incl, o);
+                if (tid >= static_cast<uint32_t>(o)) incl += y;
+            }
+            uint32_t run = incl - sum;
+#pragma unroll
+            for (uint32_t j = 0; j < 8; ++j) {
+                if (run < need && need <= run + loc[j]) {
+                    sbin = tid * 8 + j;
+                    sbefore = run;
+                }
+                run += loc[j];
+            }
+        }
+        __syncthreads();
+        const uint32_t bin = sbin, before = sbefore;
+        need -= before;
+        lt += before;
+        prefix |= static_cast<unsigned long long>(bin) << shift;
+        mask |= 255ull << shift;
+        if (hist[bin] + lt <= kRxCap) break;  // bucket + everything below it fits shared memory
+        __syncthreads();
+    }
+    // gather: every element below the bucket, and the bucket
+    if (tid == 0) nsel = 0;
+    __syncthreads();
+    const bool fits = kk == 0 || lt + hist[sbin] <= kRxCap;
+    if (fits) {
+        for (uint64_t c = tid; c < mq; c += nt) {
+            const unsigned long long u = dbits(dd[c]);
+            if ((u & mask) < prefix || (u & mask) == prefix) {
+                // below the bucket: a prefix-masked value below the bucket's prefix means u is smaller
+                const uint32_t pos = atomicAdd(&nsel, 1u);
+                if (pos < kRxCap) {
+                    key[pos] = u;
+                    kid[pos] = ii[c];
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (!fits || nsel > kRxCap) {  // a huge bucket of equal distances: the k-round kernel
+        if (tid == 0) fallback[atomicAdd(fallback, 1u) + 1] = static_cast<uint32_t>(q);
+        return;
+    }
+    // bitonic sort of nsel (<= kRxCap) entries by (dist bits, id), padded to a power of two
+    const uint32_t n = nsel;
+    uint32_t np2 = 1;
+    while (np2 < n) np2 <<= 1;
+    for (uint32_t i = n + tid; i < np2; i += nt) {
+        key[i] = ~0ull;
+        kid[i] = 0xffffffffu;
+    }
+    __syncthreads();
+    for (uint32_t size = 2; size <= np2; size <<= 1) {
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t i = tid; i < np2; i += nt) {
+                const uint32_t j = i ^ stride;
+                if (j > i) {
+                    const bool up = (i & size) == 0;
+                    const bool gt = key[i] > key[j] || (key[i] == key[j] && kid[i] > kid[j]);
+                    if (gt == up) {
+                        const unsigned long long tk = key[i];
+                        key[i] = key[j];
+                        key[j] = tk;
+                        const uint32_t ti = kid[i];
+                        kid[i] = kid[j];
+                        kid[j] = ti;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (uint32_t r = tid; r < a.k; r += nt) {
+        const bool in = r < kk;
+        const double dv = in ? __longlong_as_double(static_cast<long long>(key[r])) : kInf;
+        a.out_ids[q * a.k + r] = in ? kid[r] : 0xffffffffu;
+        a.out_dists[q * a.k + r] = a.squared || !in ? dv : __dsqrt_rn(dv);
+    }
+}
+
 }  // namespace
+
+// k > 32 selection over the scored candidates: radix select, the k-round kernel for the rest
+static cudaError_t launch_topk(const RerankArgs& a, uint64_t nq, cudaStream_t st) {
+    if (a.k > kRxCap / 2 || a.qlist) {
+        topk_generic_kernel<<<static_cast<unsigned>(nq), 256, 0, st>>>(a);
+        return cudaGetLastError();
+    }
+    uint32_t* fb = nullptr;  // [count, queries...] of the queries the radix kernel hands back
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&fb), (nq + 1) * 4, st);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(fb, 0, 4, st);
+    if (e == cudaSuccess) {
+        topk_radix_kernel<<<static_cast<unsigned>(nq), 1024, 0, st>>>(a, fb);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) {
+        RerankArgs b = a;
+        b.qlist = fb + 1;
+        b.nlist = fb;
+        b.qskip = nullptr;
+        topk_generic_kernel<<<static_cast<unsigned>(nq), 256, 0, st>>>(b);  // CTAs past *nlist exit at once
+        e = cudaGetLastError();
+    }
+    cudaFreeAsync(fb, st);
+    return e;
+}
 
 cudaError_t launch_rerank(const RerankArgs& a, uint64_t nq, cudaStream_t st) {
     if (nq == 0) return cudaSuccess;
@@ -1388,8 +1541,7 @@ cudaError_t launch_rerank(const RerankArgs& a, uint64_t nq, cudaStream_t st) {
         e = generic ? launch(rerank_kernel<false, true>) : launch(rerank_kernel<false, false>);
     }
     if (e != cudaSuccess || !generic) return e;
-    topk_generic_kernel<<<static_cast<unsigned>(nq), 256, 0, st>>>(a);
-    return cudaGetLastError();
+    return launch_topk(a, nq, st);
 }
 
 }  // namespace suco_gpu

@@ -480,7 +480,6 @@ __device__ __forceinline__ uint32_t sel_mask(uint32_t w, uint32_t wi, uint32_t t
 __device__ void emit_slab(const SelectArgs& a, const Smem& s, uint64_t q, uint64_t lo, uint32_t len, uint32_t T,
                           uint32_t quota, uint32_t base, uint32_t gt, uint32_t ties, bool swar) {
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    const uint32_t* w32 = reinterpret_cast<const uint32_t*>(s.cnt);
     const uint4* w128 = reinterpret_cast<const uint4*>(s.cnt);
     const uint32_t words = (len + 3) / 4;
     const uint32_t nvec = (words + 3) / 4;

@@ -416,7 +416,8 @@ def test_screened_rerank_ties(gpu, oracle, ref, dups):
     qs = np.concatenate([qs, base[17:18] + np.float32(1e-3), base[17:18]])
     oidx = oracle.build_index(base, 4, 10, 3, 42, 0)
     idx = gpu.load_index(oidx.serialize(), base)
-    for a, b, k in ((1.0, 1.0, 10), (0.3, 0.2, 32), (0.05, 0.01, 1)):
+    # k > 32: the radix top-k; 3000 equal distances overflow its bucket into the k-round kernel
+    for a, b, k in ((1.0, 1.0, 10), (0.3, 0.2, 32), (0.05, 0.01, 1), (0.3, 0.2, 64), (1.0, 1.0, 200)):
         ids, dd = idx.knn_query_batch(qs, gpu.CollisionParams(a, b, k))
         oi, od, _ = oidx.knn_query_batch(base, qs, a, b, k)
         assert np.array_equal(ids, oi) and np.array_equal(dd, od), (dups, a, b, k)
