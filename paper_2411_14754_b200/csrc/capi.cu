@@ -530,6 +530,7 @@ FbLists stage_select(const suco_gpu_index* x, suco_gpu_query_ctx* c, suco_gpu_qu
             sl.dflag.reserve(3 * nt + 1);  // flags, flagged list, its count, tie cuts
             da.pcut = sl.dflag.p + 2 * nt + 1;
             da.no_cut = tn.dense_nocut;
+            da.compact_mode = tn.dense_compact;
             da.hsample = sl.dsample.p;
             da.qmap = sl.dflag.p + nt;
             da.nmap = sl.dflag.p + 2 * nt;

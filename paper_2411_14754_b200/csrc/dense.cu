@@ -297,20 +297,6 @@ __device__ __forceinline__ uint32_t level(const uint4& v, uint32_t t) {  // #sco
     return (t & 1u) ? (w & 0xffffu) : (w >> 16);
 }
 
-// Bulk prefetch of `bytes` (multiple of 16, 16-byte aligned) into L2: a warp announces its next
-// piece's point codes (32 KB) while it scores the current one, so the per-tile code loads hit L2.
-__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
-// The codes of piece `piece` (rows [piece * WP, min(n_rows, (piece + 1) * WP)) x NC uint4).
-__device__ __forceinline__ void prefetch_piece(const DenseArgs& a, uint64_t piece, uint64_t n_rows, uint32_t nc) {
-    const uint64_t lo = piece * a.WP;
-    if (lo >= n_rows) return;
-    const uint64_t rows = min_u64(a.WP, n_rows - lo);
-    prefetch_l2(a.codes + lo * nc, static_cast<uint32_t>(rows * nc * 16));
-}
-
 // #score >= t, t in 1..8*nc, from a histogram row of nc uint4
 __device__ __forceinline__ uint32_t level_n(const uint4* row, uint32_t t) {
     return level(row[(t - 1) >> 3], ((t - 1) & 7u) + 1);
@@ -599,7 +585,6 @@ __device__ __forceinline__ void fused_pieces(const DenseArgs& a, const uint32_t*
         if (piece >= a.P) return;
         const uint64_t lo = uint64_t(piece) * a.WP;
         const uint64_t hi = min_u64(a.n, lo + a.WP);
-        if (lane == 0 && k + 1 < a.ppw) prefetch_piece(a, piece + 1, a.n, NC);
         uint32_t cnt[W], nb[W];
         uint16_t* buf[W];  // [query][piece][B]: a lane appends to its own contiguous buffer
         uint64_t sw[W];    // STAGE: four entries shifted in from the top
@@ -677,10 +662,6 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs 
     const uint32_t myL = threadIdx.x < nqb ? a.L[q0 + threadIdx.x] : 0u;
     if (!__syncthreads_or((myL & 0xffu) != 0)) return;  // all two-pass
     const bool stage = __syncthreads_or(myL & kDenseStage);  // a dense superset in the block
-    {  // the warp's first piece streams into L2 while the masks are built
-        const uint64_t p0 = uint64_t(blockIdx.y * kDW + (threadIdx.x >> 5)) * a.ppw;
-        if ((threadIdx.x & 31u) == 0 && p0 < a.P) prefetch_piece(a, p0, a.n, NC);
-    }
     build_masks<kDT, W>(a, M, q0, nqb);
     // The bits of L[q] across the block's queries (word w, bit j = query 32w + j): one bit-sliced
     // comparison per tile, BEFORE the transpose (lane = point, bit = query), gives score > L and
@@ -710,7 +691,7 @@ __global__ void __launch_bounds__(256) dense_compact_thread_kernel(DenseArgs a) 
     if (p >= a.P) return;
     const uint32_t pbase = p * a.WP;
     for (uint64_t q = blockIdx.y; q < a.nq; q += gridDim.y) {
-        if (a.L[q] & kDenseStage) continue;
+        if (a.compact_mode == 2 || (a.compact_mode == 0 && (a.L[q] & kDenseStage))) continue;
         const uint64_t i = q * a.P + p;
         const uint32_t n = a.ccnt[i];
         if (!n || a.qflag[q]) continue;  // (n <= B: an overflowing contributing piece flags its query)
@@ -749,7 +730,8 @@ __global__ void __launch_bounds__(256) dense_compact_kernel(DenseArgs a) {
     if (p0 >= a.P) return;
     const uint32_t lt = (1u << lane) - 1u;
     for (uint64_t q = blockIdx.y; q < a.nq; q += gridDim.y) {
-        if (!(a.L[q] & kDenseStage) || a.qflag[q]) continue;  // (overflow flags the query)
+        const bool warp_mode = a.compact_mode == 2 || (a.compact_mode == 0 && (a.L[q] & kDenseStage));
+        if (!warp_mode || a.qflag[q]) continue;  // (overflow flags the query)
         const uint32_t p = p0 + lane;
         const uint64_t i = q * a.P + p;
         uint32_t n = 0, quota = 0, base = 0;
@@ -993,10 +975,6 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_h_kernel(DenseArg
     const uint32_t nqb = static_cast<uint32_t>(min_u64(16, a.nq - q0));
     const uint32_t myL = threadIdx.x < nqb ? a.L[q0 + threadIdx.x] : 0u;
     if (!__syncthreads_or((myL & 0xffu) != 0)) return;  // all two-pass
-    {  // the warp's first piece streams into L2 while the masks are built
-        const uint64_t p0 = uint64_t(blockIdx.y * kDW + (threadIdx.x >> 5)) * a.ppw;
-        if ((threadIdx.x & 31u) == 0 && p0 < a.P) prefetch_piece(a, p0, uint64_t(a.P) * a.WP, 1);
-    }
     build_masks_h<kDT>(a, M, q0, nqb);
     const uint32_t qj = lane & 15u, half = lane >> 4;
     const bool mine = qj < nqb;
@@ -1014,8 +992,6 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_h_kernel(DenseArg
         if (piece >= a.P) return;
         const uint64_t lo = uint64_t(piece) * a.WP;
         const uint64_t hi = min_u64(a.n, lo + a.WP);
-        // the padded code rows cover whole pieces
-        if (lane == 0 && k + 1 < a.ppw) prefetch_piece(a, piece + 1, uint64_t(a.P) * a.WP, 1);
         uint32_t cnt = 0, nb = 0;
         uint16_t* buf = a.cbuf + ((mine ? q0 + qj : q0) * a.P + piece) * a.B;
         uint4 ca = __ldg(a.codes + lo + lane), cb = __ldg(a.codes + lo + 32 + lane);

@@ -106,6 +106,7 @@ struct DenseArgs {
     uint32_t nc;                  // uint4 code vectors per point: 1 (N_s <= 8, default) or 2 (N_s <= 16)
     uint32_t* pcut;               // single pass: nq, tie entries are stored only in pieces < pcut[q]
     uint32_t no_cut;              // tests: store every tie (pcut = P)
+    uint32_t compact_mode;        // Tuning::dense_compact: 0 by superset density, 1 thread per piece, 2 warp
     float cut_scale;              // tie cut = P * need/ties * cut_scale + cut_pad pieces (0: defaults 1.25, 8)
     uint32_t cut_pad;
     uint32_t words;               // Tuning::dense_words (0 = by shape)

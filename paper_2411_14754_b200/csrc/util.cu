@@ -168,6 +168,8 @@ Tuning tuning_from_env() {
     const int w = env_int("SUCO_DENSE_WORDS", 0);
     t.dense_words = (w == 1 || w == 2) ? static_cast<uint32_t>(w) : 0u;
     t.dense_stats = std::getenv("SUCO_DENSE_STATS") != nullptr;
+    const int cm = env_int("SUCO_DENSE_COMPACT", 0);
+    t.dense_compact = (cm == 1 || cm == 2) ? static_cast<uint32_t>(cm) : 0u;
     t.rerank_stats = std::getenv("SUCO_RERANK_STATS") != nullptr;
     const int tl = env_int("SUCO_TILES", 1);
     t.tiles = tl > 1 ? static_cast<uint32_t>(tl) : 1u;
