@@ -463,6 +463,7 @@ void rerank_args(const suco_gpu_index* x, RerankArgs& ra) {
     ra.qpad = x->qpad;
     ra.qrec = x->qrec;
     ra.u8_regs = x->tune.rerank_u8_regs;
+    ra.no_tma = !x->tune.rerank_tma;
     ra.pipe = x->tune.rerank_pipe == 2 ? 0 : x->tune.rerank_pipe == 1 ? 1 : 2;
 }
 

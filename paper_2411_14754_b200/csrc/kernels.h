@@ -170,6 +170,7 @@ struct RerankArgs {
                             // bounds), padded to a multiple of 64 bytes (the DRAM access granule)
     uint32_t qpad;          // int8 bytes of a record (d rounded up to 16)
     uint32_t qrec;          // record stride (qpad + 16 rounded up to 64)
+    bool no_tma;            // !Tuning::rerank_tma: 16-byte cp.async row gathers instead of per-row TMA bulk copies
     unsigned long long* screen_stats;  // optional diagnostics: [0] += exact re-ranks, [1] += queries re-ranked in full
     bool u8_regs;           // Tuning::rerank_u8_regs: the register byte kernel instead of the smem ring
     uint8_t pipe;           // 0: certified fp32 screen (default), 1: pipelined fp64, 2: unpipelined

@@ -705,7 +705,45 @@ __global__ void __launch_bounds__(kThreads, MINB) rerank_screen_kernel(RerankArg
 constexpr uint32_t kQ8Stages = 2;
 constexpr uint32_t kQ8Cap = 192;
 
-template <uint32_t NW>
+// TMA bulk copies (sm_90+ async proxy) with mbarrier completion: a warp's ring slot is filled by
+// one cp.async.bulk per row (the row's int8 words + bound terms, one 112-byte copy at d = 96)
+// instead of seven 16-byte cp.async per row.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(unsigned long long* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+    while (!mbar_try(bar, parity)) {
+    }
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <uint32_t NW, bool TMA>
 __global__ void __launch_bounds__(kThreads, 2) rerank_q8_kernel(RerankArgs a, uint32_t stride) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr uint32_t su = (NW + 1) | 1u;  // NW row words + 1 meta word, odd 16-byte stride
@@ -720,10 +758,15 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_q8_kernel(RerankArgs a, ui
     __shared__ double qpar[4];  // t, |q|^2, ||t b|| (up), ||e_q|| (up)
     __shared__ double tau_cta;
     __shared__ int ovf, qok;
+    __shared__ __align__(8) unsigned long long mbar[kWarps][kQ8Stages];  // TMA: one per ring slot
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     uint64_t q;
     if (!rerank_query(a, q)) return;
     const float* query = a.queries + q * a.d;
+    if constexpr (TMA) {
+        if (lane < kQ8Stages) mbar_init(&mbar[warp][lane], 1);
+        mbar_fence_init();
+    }
     for (uint32_t i = tid; i < a.d; i += kThreads) qd[i] = static_cast<double>(query[i]);
     if (warp == 0) {  // quantise the query (d <= 128: lane owns dims 4 lane .. 4 lane + 3)
         float v[4], mx = 0.f;
@@ -786,13 +829,23 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_q8_kernel(RerankArgs a, ui
     uint32_t id0 = load_id(0), id1 = load_id(1);
     auto issue = [&](uint64_t g) {
         const uint32_t myid = (g & 1u) ? id1 : id0;
-        uint4* st = ring + static_cast<uint32_t>(g % kQ8Stages) * 32 * su;
+        const uint32_t slot = static_cast<uint32_t>(g % kQ8Stages);
+        uint4* st = ring + slot * 32 * su;
         const uint64_t b = sbase(g);
+        if constexpr (TMA) {
+            const uint32_t nvalid = static_cast<uint32_t>(min_u64(32, mq - b));
+            fence_proxy_async();  // the slot's previous contents were read by the generic proxy
+            __syncwarp();
+            if (lane == 0) mbar_expect_tx(&mbar[warp][slot], nvalid * (NW + 1) * 16u);
+            __syncwarp();
+            if (lane < nvalid) bulk_g2s(st + lane * su, a.q8 + uint64_t(myid) * a.qrec, (NW + 1) * 16u, &mbar[warp][slot]);
+        } else {
 #pragma unroll
-        for (uint32_t t = lane; t < 32 * (NW + 1); t += 32) {
-            const uint32_t row = t / (NW + 1), col = t % (NW + 1);
-            const uint32_t id = __shfl_sync(kFull, myid, row);
-            if (b + row < mq) cp_async16(st + row * su + col, a.q8 + uint64_t(id) * a.qrec + 16u * col);
+            for (uint32_t t = lane; t < 32 * (NW + 1); t += 32) {
+                const uint32_t row = t / (NW + 1), col = t % (NW + 1);
+                const uint32_t id = __shfl_sync(kFull, myid, row);
+                if (b + row < mq) cp_async16(st + row * su + col, a.q8 + uint64_t(id) * a.qrec + 16u * col);
+            }
         }
         if (g & 1u) id1 = load_id(g + 2);
         else id0 = load_id(g + 2);
@@ -801,9 +854,10 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_q8_kernel(RerankArgs a, ui
     uint32_t rowid[kQ8Stages];
 #pragma unroll
     for (uint32_t i = 0; i < kQ8Stages; ++i) rowid[i] = 0;
+    if constexpr (TMA) __syncwarp();  // the barriers are initialised
     for (uint32_t i = 0; i + 1 < kQ8Stages; ++i) {
         if (i < steps) rowid[i] = issue(i);
-        cp_async_commit();
+        if constexpr (!TMA) cp_async_commit();
     }
     double sl = kInf;  // the k smallest upper bounds (lane i = entry i)
     uint32_t nsurv = 0;
@@ -817,8 +871,12 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_q8_kernel(RerankArgs a, ui
                 if (i == slot) rowid[i] = v;
             }
         }
-        cp_async_commit();
-        cp_async_wait<kQ8Stages - 1>();
+        if constexpr (TMA) {
+            mbar_wait(&mbar[warp][g % kQ8Stages], static_cast<uint32_t>((g / kQ8Stages) & 1u));
+        } else {
+            cp_async_commit();
+            cp_async_wait<kQ8Stages - 1>();
+        }
         __syncwarp();
         const uint32_t slot = static_cast<uint32_t>(g % kQ8Stages);
         uint32_t myid = rowid[0];
@@ -898,7 +956,7 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_q8_kernel(RerankArgs a, ui
             __syncwarp();
         }
     }
-    cp_async_wait<0>();
+    if constexpr (!TMA) cp_async_wait<0>();  // (TMA: every issued slot was waited on in the loop)
     if (overflow && lane == 0) atomicOr(&ovf, 1);
     md[warp * 32 + lane] = sl;
     __syncthreads();
@@ -1499,11 +1557,16 @@ cudaError_t launch_rerank(const RerankArgs& a, uint64_t nq, cudaStream_t st) {
         const size_t per_warp = std::max<size_t>(size_t(kQ8Stages) * 32 * su * 16, size_t(kRows) * stride * 4);
         const size_t qsmem = ((a.d * 8 + 15) / 16) * 16 + kWarps * per_warp;
         using KQ = void (*)(RerankArgs, uint32_t);
-        const KQ kq[8] = {rerank_q8_kernel<1>, rerank_q8_kernel<2>, rerank_q8_kernel<3>, rerank_q8_kernel<4>,
-                          rerank_q8_kernel<5>, rerank_q8_kernel<6>, rerank_q8_kernel<7>, rerank_q8_kernel<8>};
-        e = cudaFuncSetAttribute(kq[nwq - 1], cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(qsmem));
+        const KQ kt[8] = {rerank_q8_kernel<1, true>, rerank_q8_kernel<2, true>, rerank_q8_kernel<3, true>,
+                          rerank_q8_kernel<4, true>, rerank_q8_kernel<5, true>, rerank_q8_kernel<6, true>,
+                          rerank_q8_kernel<7, true>, rerank_q8_kernel<8, true>};
+        const KQ kc[8] = {rerank_q8_kernel<1, false>, rerank_q8_kernel<2, false>, rerank_q8_kernel<3, false>,
+                          rerank_q8_kernel<4, false>, rerank_q8_kernel<5, false>, rerank_q8_kernel<6, false>,
+                          rerank_q8_kernel<7, false>, rerank_q8_kernel<8, false>};
+        const KQ kern = a.no_tma ? kc[nwq - 1] : kt[nwq - 1];
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(qsmem));
         if (e != cudaSuccess) return e;
-        kq[nwq - 1]<<<static_cast<unsigned>(nq), kThreads, qsmem, st>>>(a, stride);
+        kern<<<static_cast<unsigned>(nq), kThreads, qsmem, st>>>(a, stride);
         return cudaGetLastError();
     }
     if (vec && !generic && pmode == 2) {

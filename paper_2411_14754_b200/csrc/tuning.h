@@ -30,6 +30,8 @@ struct Tuning {
     int fb_overlap = -1;         // SUCO_FB_OVERLAP: overlapped dense fallback (-1 auto, 0, 1)
     char traverse = 0;           // SUCO_TRAVERSE: 0 auto, 'w' warp kernel, 's' / 'n' force / forbid split tasks
     bool rerank_u8_regs = false; // SUCO_RERANK_U8_PIPE=0: the register byte re-rank instead of the ring
+    bool rerank_tma = false;     // SUCO_RERANK_TMA=1: int8-screen rows by per-row TMA bulk copies (measured slower:
+                                 // cfg4 re-rank 12.96 vs 8.58 ms with the warp's coalesced 16-byte cp.async)
     int rerank_pipe = 2;         // SUCO_RERANK_PIPE: 0 unpipelined, 1 pipelined fp64, 2 certified fp32 screen
     bool kpp_serial = false;     // SUCO_KPP_SERIAL=1: k-means++ one-lane serial fold (tests)
     uint64_t build_chunk = 0;    // SUCO_BUILD_CHUNK: rows per assignment chunk of the sampled build (0 = 2 GB)

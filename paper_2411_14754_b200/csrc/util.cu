@@ -179,6 +179,7 @@ Tuning tuning_from_env() {
     const char* tv = std::getenv("SUCO_TRAVERSE");
     t.traverse = tv && (tv[0] == 'w' || tv[0] == 's' || tv[0] == 'n') ? tv[0] : 0;
     t.rerank_u8_regs = env_int("SUCO_RERANK_U8_PIPE", 1) == 0;
+    t.rerank_tma = env_int("SUCO_RERANK_TMA", 0) != 0;
     const int rp = env_int("SUCO_RERANK_PIPE", 2);
     t.rerank_pipe = (rp == 0 || rp == 1) ? rp : 2;
     t.kpp_serial = env_int("SUCO_KPP_SERIAL", 0) == 1;
