@@ -18,14 +18,13 @@ namespace {
 
 // SC-Linear (sc_linear.cpp:49-121) over the index's device rows and layout.
 struct ScScratch {
-    DevBuf<uint32_t> sub_off, vals, vals_alt, scores, cands;
-    DevBuf<uint8_t> consec, temp;
-    DevBuf<unsigned long long> keys, keys_alt;
+    DevBuf<uint32_t> sub_off;
+    DevBuf<uint8_t> consec, scratch;
     DevBuf<float> q;
     ScArgs a{};
 };
 
-void sc_setup(const suco_gpu_index* x, ScScratch& w, cudaStream_t st) {
+void sc_setup(const suco_gpu_index* x, ScScratch& w, uint32_t B, uint64_t m, cudaStream_t st) {
     const HostLayout& L = x->host.layout;
     const uint64_t n = x->host.n;
     std::vector<uint32_t> off(L.ns + 1, 0);
@@ -40,14 +39,8 @@ void sc_setup(const suco_gpu_index* x, ScScratch& w, cudaStream_t st) {
     w.consec.reserve(L.ns);
     CUDA_TRY(cudaMemcpyAsync(w.sub_off.p, off.data(), off.size() * 4, cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemcpyAsync(w.consec.p, consec.data(), consec.size(), cudaMemcpyHostToDevice, st));
-    w.keys.reserve(n);
-    w.keys_alt.reserve(n);
-    w.vals.reserve(n);
-    w.vals_alt.reserve(n);
-    w.scores.reserve(n);
-    w.q.reserve(x->host.d);
-    const size_t tb = sc_temp_bytes(n);
-    w.temp.reserve(tb);
+    w.q.reserve(uint64_t(B) * x->host.d);
+    w.scratch.reserve(sc_batch_bytes(n, B, m));
     w.a.data = x->data.p;
     w.a.n = n;
     w.a.d = x->host.d;
@@ -56,12 +49,13 @@ void sc_setup(const suco_gpu_index* x, ScScratch& w, cudaStream_t st) {
     w.a.sub_off = w.sub_off.p;
     w.a.consec = w.consec.p;
     w.a.q = w.q.p;
-    w.a.keys = w.keys.p;
-    w.a.keys_alt = w.keys_alt.p;
-    w.a.vals = w.vals.p;
-    w.a.vals_alt = w.vals_alt.p;
-    w.a.temp = w.temp.p;
-    w.a.temp_bytes = tb;
+    w.a.scratch = w.scratch.p;
+}
+
+// queries per SC-Linear batch: the n distance keys (+ scores) of each within about 2 GB
+uint32_t sc_batch_size(uint64_t n, uint64_t nq) {
+    const uint64_t per = n * 9 + 64;
+    return static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(nq, (2ull << 30) / per)));
 }
 
 void check_sc_query(const suco_gpu_index* x, uint32_t qlen) {
@@ -134,13 +128,18 @@ int suco_gpu_sc_scores(const suco_gpu_index* x, const float* query, uint32_t qle
         DeviceGuard g(x->device);
         OwnStream os;
         cudaStream_t st = os.s;
+        const uint64_t n = x->host.n;
         ScScratch w;
-        sc_setup(x, w, st);
-        const uint64_t c = std::min<uint64_t>(suco_collision_count(alpha, x->host.n), x->host.n);
+        sc_setup(x, w, 1, 1, st);
+        DevBuf<uint8_t> sc;
+        sc.reserve(n);
+        const uint64_t c = std::min<uint64_t>(suco_collision_count(alpha, n), n);
         CUDA_TRY(cudaMemcpyAsync(w.q.p, query, qlen * 4, cudaMemcpyHostToDevice, st));
-        CUDA_TRY(launch_sc_scores(w.a, c, w.scores.p, st));
-        CUDA_TRY(cudaMemcpyAsync(scores, w.scores.p, x->host.n * 4, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(launch_sc_batch(w.a, 1, c, 1, nullptr, sc.p, st));
+        std::vector<uint8_t> h(n);
+        CUDA_TRY(cudaMemcpyAsync(h.data(), sc.p, n, cudaMemcpyDeviceToHost, st));
         CUDA_TRY(cudaStreamSynchronize(st));
+        for (uint64_t i = 0; i < n; ++i) scores[i] = h[i];
     });
 }
 
@@ -158,35 +157,36 @@ int suco_gpu_sc_linear_batch(const suco_gpu_index* x, const float* queries, uint
         const uint64_t n = x->host.n;
         const uint64_t c = std::min<uint64_t>(suco_collision_count(p->alpha, n), n);
         const uint64_t m = std::min<uint64_t>(suco_candidate_count(p->beta, n, p->k), n);
+        const uint32_t B = x->tune.sc_batch ? static_cast<uint32_t>(std::min<uint64_t>(x->tune.sc_batch, nq))
+                                            : sc_batch_size(n, nq);
         ScScratch w;
-        sc_setup(x, w, st);
-        w.cands.reserve(n);
-        DevBuf<uint32_t> di, all_id;
+        sc_setup(x, w, B, m, st);
+        DevBuf<uint32_t> cands, di, all_id;
         DevBuf<double> dd, all_d;
-        di.reserve(p->k);
-        dd.reserve(p->k);
+        cands.reserve(uint64_t(B) * m);
+        di.reserve(uint64_t(B) * p->k);
+        dd.reserve(uint64_t(B) * p->k);
         if (p->k > 32) {
-            all_d.reserve(m);
-            all_id.reserve(m);
+            all_d.reserve(uint64_t(B) * m);
+            all_id.reserve(uint64_t(B) * m);
         }
-        for (uint64_t q = 0; q < nq; ++q) {
-            CUDA_TRY(cudaMemcpyAsync(w.q.p, queries + q * qlen, qlen * 4, cudaMemcpyHostToDevice, st));
-            CUDA_TRY(launch_sc_scores(w.a, c, w.scores.p, st));
-            // the m best by (score desc, id asc): the first m of a stable sort on N_s - score
-            CUDA_TRY(launch_sc_candidates(w.a, w.scores.p, w.cands.p, st));
+        for (uint64_t q0 = 0; q0 < nq; q0 += B) {
+            const uint32_t nb = static_cast<uint32_t>(std::min<uint64_t>(B, nq - q0));
+            CUDA_TRY(cudaMemcpyAsync(w.q.p, queries + q0 * qlen, uint64_t(nb) * qlen * 4, cudaMemcpyHostToDevice, st));
+            CUDA_TRY(launch_sc_batch(w.a, nb, c, m, cands.p, nullptr, st));
             RerankArgs ra{};
             rerank_args(x, ra);
             ra.queries = w.q.p;
-            ra.cands = w.cands.p;
+            ra.cands = cands.p;
             ra.m = m;
             ra.k = p->k;
             ra.out_ids = di.p;
             ra.out_dists = dd.p;
             ra.all_d = all_d.p;
             ra.all_id = all_id.p;
-            CUDA_TRY(launch_rerank(ra, 1, st));
-            CUDA_TRY(cudaMemcpyAsync(ids + q * p->k, di.p, p->k * 4, cudaMemcpyDeviceToHost, st));
-            CUDA_TRY(cudaMemcpyAsync(dists + q * p->k, dd.p, p->k * 8, cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(launch_rerank(ra, nb, st));
+            CUDA_TRY(cudaMemcpyAsync(ids + q0 * p->k, di.p, uint64_t(nb) * p->k * 4, cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaMemcpyAsync(dists + q0 * p->k, dd.p, uint64_t(nb) * p->k * 8, cudaMemcpyDeviceToHost, st));
         }
         CUDA_TRY(cudaStreamSynchronize(st));
     });

@@ -213,7 +213,8 @@ cudaError_t launch_pack_u8(const float* data, uint64_t n, uint32_t d, uint32_t d
 cudaError_t launch_pack_q8(const float* data, uint64_t n, uint32_t d, uint32_t qpad, uint32_t qrec, int8_t* out,
                            cudaStream_t st);
 
-// SC-Linear (sclinear.cu): exact per-subspace distances, top-c by stable sort.
+// SC-Linear (sclinear.cu): exact per-subspace distances, top-c per (query, subspace) by a radix
+// select with id-ordered ties, scores, then the m candidates; batches of B queries.
 struct ScArgs {
     const float* data;             // n x d rows
     uint64_t n;
@@ -221,16 +222,13 @@ struct ScArgs {
     const uint32_t* dims;          // concatenated whole-subspace dims (layout order)
     const uint32_t* sub_off;       // ns + 1 prefix offsets into dims
     const uint8_t* consec;         // ns: dims form one consecutive run -> sq_euclidean_raw
-    const float* q;                // one query, d floats
-    unsigned long long* keys;      // n distance bit patterns of one subspace (reused as u32 rank keys)
-    unsigned long long* keys_alt;  // n sort output
-    uint32_t* vals;                // n ids
-    uint32_t* vals_alt;            // n sorted ids
-    void* temp;                    // CUB scratch
-    size_t temp_bytes;
+    const float* q;                // B queries, d floats each
+    unsigned long long* keys;      // (set by launch_sc_batch) B x n distance bit patterns of one subspace
+    void* scratch;                 // sc_batch_bytes(n, B, m)
 };
-size_t sc_temp_bytes(uint64_t n);
-cudaError_t launch_sc_scores(ScArgs a, uint64_t c, uint32_t* scores, cudaStream_t st);
-cudaError_t launch_sc_candidates(ScArgs a, const uint32_t* scores, uint32_t* cands_sorted, cudaStream_t st);
+size_t sc_batch_bytes(uint64_t n, uint32_t B, uint64_t m);
+// scores_out (optional, B x n u8): the SC-scores; cands (optional, B x m): the candidate sets
+cudaError_t launch_sc_batch(ScArgs a, uint32_t B, uint64_t c, uint64_t m, uint32_t* cands, uint8_t* scores_out,
+                            cudaStream_t st);
 
 }  // namespace suco_gpu

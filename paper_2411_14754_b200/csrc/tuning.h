@@ -35,6 +35,7 @@ struct Tuning {
     int rerank_pipe = 2;         // SUCO_RERANK_PIPE: 0 unpipelined, 1 pipelined fp64, 2 certified fp32 screen
     bool kpp_serial = false;     // SUCO_KPP_SERIAL=1: k-means++ one-lane serial fold (tests)
     uint64_t build_chunk = 0;    // SUCO_BUILD_CHUNK: rows per assignment chunk of the sampled build (0 = 2 GB)
+    uint32_t sc_batch = 0;       // SUCO_SC_BATCH: SC-Linear queries per batch (0 = about 2 GB of keys; tests)
 };
 
 Tuning tuning_from_env();

@@ -183,6 +183,8 @@ Tuning tuning_from_env() {
     const int rp = env_int("SUCO_RERANK_PIPE", 2);
     t.rerank_pipe = (rp == 0 || rp == 1) ? rp : 2;
     t.kpp_serial = env_int("SUCO_KPP_SERIAL", 0) == 1;
+    const int scb = env_int("SUCO_SC_BATCH", 0);
+    t.sc_batch = scb > 0 ? static_cast<uint32_t>(scb) : 0u;
     const char* ch = std::getenv("SUCO_BUILD_CHUNK");
     t.build_chunk = ch && std::atoll(ch) > 0 ? static_cast<uint64_t>(std::atoll(ch)) : 0;
     return t;

@@ -113,3 +113,13 @@ def test_header_declares_status_codes_and_contexts():
     for fn in ("suco_gpu_knn_query_batch(", "suco_gpu_knn_query_batch_device("):
         decl = src[src.index("int " + fn):].split(";")[0]
         assert "const suco_gpu_index*" in decl and "suco_gpu_query_ctx*" in decl, decl
+
+
+def test_library_then_torch_import_order():
+    """libsuco_b200.so links the NCCL copy torch bundles (one libnccl.so.2 per process): importing
+    the library BEFORE torch must not shadow torch's NCCL with an older one."""
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, "-c", "import paper_2411_14754_b200, torch; print(torch.__version__)"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]

@@ -39,7 +39,8 @@ def test_sc_scores_match_reference(gpu, oracle, ref, mode, quant, d, ns):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("mode,quant,k", [(0, False, 10), (0, True, 10), (1, False, 10), (1, True, 40), (0, False, 1)])
-def test_sc_linear_matches_reference(gpu, oracle, ref, mode, quant, k):
+def test_sc_linear_matches_reference(gpu, oracle, ref, mode, quant, k, monkeypatch):
+    monkeypatch.setenv("SUCO_SC_BATCH", "5")  # 12 queries: batches of 5, 5 and 2
     full = oracle.clustered(3000 + 12, 24, 15, 40 + k, 0, 200, 12, quant)
     base, qs = oracle.hold_out(full, 12, 41)
     idx, ridx = _pair(gpu, ref, base, gpu.IndexParams(4, 8, 2, 42, gpu.SubspaceMode(mode)))

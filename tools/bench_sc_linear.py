@@ -31,7 +31,7 @@ def main():
     qs = queries[: args.queries]
     cp = suco.CollisionParams(cfg.alpha, cfg.beta, cfg.k)
     idx = suco.build_index(base, suco.IndexParams(cfg.num_subspaces, cfg.k_half, cfg.iterations, 42))
-    idx.sc_linear_batch(qs[:2], cp)  # warm-up (CUB temp sizing, module load)
+    idx.sc_linear_batch(qs[:2], cp)  # warm-up (module load)
     t0 = time.perf_counter()
     sl_ids, sl_d = idx.sc_linear_batch(qs, cp)
     gpu_s = time.perf_counter() - t0
