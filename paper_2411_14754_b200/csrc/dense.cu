@@ -150,6 +150,16 @@ __device__ __forceinline__ Codes<NC> load_codes(const DenseArgs& a, uint64_t p, 
     return c;
 }
 
+template <uint32_t NC>
+__device__ __forceinline__ Codes<NC> load_codes_at(const DenseArgs& a, const uint4* p, bool valid) {
+    const uint32_t none = a.ns * a.K;
+    const uint32_t nn = none | (none << 16);
+    Codes<NC> c;
+#pragma unroll
+    for (uint32_t i = 0; i < NC; ++i) c.v[i] = valid ? __ldg(p + i) : make_uint4(nn, nn, nn, nn);
+    return c;
+}
+
 template <uint32_t W, uint32_t NC>
 __device__ __forceinline__ void planes_of(const uint32_t* M, const Codes<NC>& c, uint32_t (&b)[W][Np<NC>::v]) {
     uint32_t m[8 * NC][W];
@@ -596,13 +606,16 @@ __device__ __forceinline__ void fused_pieces(const DenseArgs& a, const uint32_t*
             const uint64_t q = 32 * w + lane < nqb ? q0 + 32 * w + lane : q0;  // idle lanes append nothing
             buf[w] = a.cbuf + (q * a.P + piece) * a.B;
         }
-        Codes<NC> code = load_codes<NC>(a, lo + lane, hi);
-        for (uint64_t t0 = lo; t0 < hi; t0 += 32) {
-            const Codes<NC> next = load_codes<NC>(a, t0 + 32 + lane, hi);  // one tile ahead
+        // 32-bit tile loop over the piece: a running code pointer, the piece's point count
+        const uint32_t len = static_cast<uint32_t>(hi - lo);
+        const uint4* cptr = a.codes + (lo + lane) * NC;
+        Codes<NC> code = load_codes_at<NC>(a, cptr, lane < len);
+        for (uint32_t tb = 0; tb < len; tb += 32) {
+            cptr += 32 * NC;
+            const Codes<NC> next = load_codes_at<NC>(a, cptr, tb + 32 + lane < len);  // one tile ahead
             uint32_t b[W][NP];
             planes_of<W, NC>(M, code, b);
             code = next;
-            const uint32_t tb = static_cast<uint32_t>(t0 - lo);
 #pragma unroll
             for (uint32_t w = 0; w < W; ++w) {
                 // most significant plane first; points past the piece end score 0 < L
@@ -994,12 +1007,15 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_h_kernel(DenseArg
         const uint64_t hi = min_u64(a.n, lo + a.WP);
         uint32_t cnt = 0, nb = 0;
         uint16_t* buf = a.cbuf + ((mine ? q0 + qj : q0) * a.P + piece) * a.B;
-        uint4 ca = __ldg(a.codes + lo + lane), cb = __ldg(a.codes + lo + 32 + lane);
-        for (uint64_t t0 = lo; t0 < hi; t0 += 64) {
-            // one tile ahead (the padded code rows cover a whole last piece)
-            const bool more = t0 + 64 < hi;
-            const uint4 na = more ? __ldg(a.codes + t0 + 64 + lane) : ca;
-            const uint4 nbv = more ? __ldg(a.codes + t0 + 96 + lane) : cb;
+        // 32-bit tile loop (the padded code rows cover a whole last piece)
+        const uint32_t len = static_cast<uint32_t>(hi - lo);
+        const uint4* cptr = a.codes + lo + lane;
+        uint4 ca = __ldg(cptr), cb = __ldg(cptr + 32);
+        for (uint32_t tb0 = 0; tb0 < len; tb0 += 64) {
+            cptr += 64;
+            const bool more = tb0 + 64 < len;  // one tile ahead
+            const uint4 na = more ? __ldg(cptr) : ca;
+            const uint4 nbv = more ? __ldg(cptr + 32) : cb;
             uint32_t b[4];
             planes_h(M16, ro, ca, cb, b);
             ca = na;
@@ -1018,7 +1034,7 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_h_kernel(DenseArg
             const uint32_t kept = piece < cut ? ge0 : g1;  // past the tie cut: score > L only
             const uint32_t c0 = __popc(kept), o0 = __shfl_xor_sync(kFull, c0, 16);
             uint32_t at = nb + (half ? o0 : 0u);
-            const uint32_t tb = static_cast<uint32_t>(t0 - lo) + 32 * half;
+            const uint32_t tb = tb0 + 32 * half;
             uint32_t bits = kept;
             while (bits) {  // id order
                 const uint32_t r = __ffs(bits) - 1;
