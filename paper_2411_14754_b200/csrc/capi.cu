@@ -449,6 +449,7 @@ DenseArgs dense_args(const suco_gpu_index* x, suco_gpu_query_ctx::Slot& sl, uint
     da.half = x->dense_half ? 1u : 0u;
     da.nc = h.layout.ns > 8 ? 2u : 1u;  // 9..16 subspaces: two code vectors, 16 histogram levels
     da.words = x->tune.dense_words;
+    da.pair = x->dense_half && x->tune.dense_pair != 0 && dense_pair_supported(h.layout.ns, x->K) ? 1u : 0u;
     return da;
 }
 

@@ -1053,6 +1053,212 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_h_kernel(DenseArg
     }
 }
 
+// ----------------------------------------------------- cluster-pair fused pass
+// Config 5's tables (8 x 10,000 cells) in a 2-CTA cluster instead of the half-width mode: CTA r of
+// the pair keeps 32-bit masks (32 queries) for subspaces 4r .. 4r+3 only (4 x 10,001 slots,
+// 160 KB), so one shared-memory lookup serves 32 queries instead of 16 — half the lookups (and
+// their bank conflicts) per point and query. A warp of each CTA walks the same piece pairs
+// (2p, 2p+1); CTA r finalises piece 2p + r. Per 32-point tile it computes its 3-bit partial scores
+// (its four subspaces: 0..4, bit-sliced, lane = point, bit = query) of both pieces' tiles, sends the
+// partial of the peer's tile into the peer's ring slot with st.async (completing the peer's
+// mbarrier transaction), and adds the peer's partial of its own tile to its own: the 4-bit
+// scores of the 32 queries, from which the single pass proceeds exactly as in fused_pieces
+// (comparison with L before the transpose, counts, id-ordered buffer entries). The ring runs
+// kPairRing - 1 tiles ahead; a consumed slot is released to the producer with a remote
+// mbarrier arrive. Uses the half-width mode's point codes (cell + 1 per subspace, 0 = none).
+constexpr uint32_t kPairRing = 3;
+
+__device__ __forceinline__ uint32_t cta_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ uint32_t map_peer(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void pbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void pbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void pbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n"
+            "}\n"
+            : "=r"(ok)
+            : "r"(smem_addr(bar)), "r"(parity)
+            : "memory");
+    }
+}
+// relaxed: the slot's values are already consumed (data dependence) when the consumer releases it
+__device__ __forceinline__ void pbar_arrive_remote(uint32_t remote_bar) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
+}
+__device__ __forceinline__ void st_async_v4(uint32_t remote_addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d,
+                                            uint32_t remote_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                     remote_addr),
+                 "r"(a), "r"(b), "r"(c), "r"(d), "r"(remote_bar)
+                 : "memory");
+}
+
+// 3-bit partial score planes of 32 points (lane) x 32 queries (bit) over a CTA's four subspaces
+__device__ __forceinline__ void pair_partial(const uint32_t* M, uint32_t R, uint2 c, uint32_t (&p)[3]) {
+    const uint32_t m0 = M[c.x & 0xffffu], m1 = M[R + (c.x >> 16)];
+    const uint32_t m2 = M[2 * R + (c.y & 0xffffu)], m3 = M[3 * R + (c.y >> 16)];
+    uint32_t s1, c1;
+    fadd(m0, m1, m2, s1, c1);
+    p[0] = s1 ^ m3;
+    const uint32_t k = s1 & m3;
+    p[1] = c1 ^ k;
+    p[2] = c1 & k;
+}
+
+template <uint32_t kDT>
+__global__ void __launch_bounds__(kDT, 1) dense_fused_pair_kernel(DenseArgs a) {
+    constexpr uint32_t kDW = kDT / 32;
+    extern __shared__ __align__(16) uint32_t M[];
+    __shared__ __align__(8) uint64_t full[kDW][kPairRing], empty[kDW][kPairRing];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint32_t r = cta_rank(), peer = r ^ 1u;
+    const uint64_t q0 = uint64_t(blockIdx.x >> 1) * 32;
+    const uint32_t nqb = static_cast<uint32_t>(min_u64(32, a.nq - q0));
+    const uint32_t myL = threadIdx.x < nqb ? a.L[q0 + threadIdx.x] : 0u;
+    if (!__syncthreads_or((myL & 0xffu) != 0)) return;  // both CTAs of the pair see the same queries
+    const uint32_t R = a.K + 1;
+    const uint32_t regions = 4;
+    uint4* ring = reinterpret_cast<uint4*>(M + ((regions * R + 3) & ~3u));  // [kDW][kPairRing][32]
+    // masks of this CTA's subspaces 4r .. 4r+3 (code = cell + 1; slot 0 of a region stays zero)
+    for (uint32_t i = threadIdx.x; i < regions * R; i += kDT) M[i] = 0;
+    if (lane < kPairRing) {
+        pbar_init(&full[warp][lane], 1);
+        pbar_init(&empty[warp][lane], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    for (uint32_t j = warp; j < nqb; j += kDW) {
+        const uint64_t q = q0 + j;
+        for (uint32_t sl = 0; sl < 4; ++sl) {
+            const uint32_t s = 4 * r + sl;
+            if (s >= a.ns) break;
+            const uint64_t t = q * a.ns + s;
+            const uint32_t cnt = a.ncells[t];
+            const uint32_t* cp = a.cells + t * a.cells_cap;
+            for (uint32_t i = lane; i < cnt; i += 32) atomicOr(M + sl * R + cp[i] + 1, 1u << j);
+        }
+    }
+    __syncthreads();
+    cluster_sync_all();  // the peer's barriers are initialised before any remote operation
+    // the bits of L[q] across the block's queries: TL[i] bit j = bit i of L[q0 + j]
+    const uint32_t L = lane < nqb ? a.L[q0 + lane] & 0xffu : 0u;
+    uint32_t TL[4];
+#pragma unroll
+    for (uint32_t i = 0; i < 4; ++i) TL[i] = __ballot_sync(kFull, (L >> i) & 1u);
+    const uint32_t live = __ballot_sync(kFull, L != 0);
+    const uint32_t cut = a.pcut && lane < nqb ? a.pcut[q0 + lane] : a.P;
+    const Xpose xp(lane);
+    uint4* myring = ring + warp * kPairRing * 32;
+    const uint32_t peer_ring = map_peer(smem_addr(myring), peer);
+    const uint32_t peer_full = map_peer(smem_addr(&full[warp][0]), peer);
+    const uint32_t peer_empty = map_peer(smem_addr(&empty[warp][0]), peer);
+    const uint2* codes2 = reinterpret_cast<const uint2*>(a.codes);  // 8 u16 codes per point = 2 uint2
+    constexpr uint32_t kTiles = kDensePiece / 32, kTileLog = 6;      // tiles per piece (rows padded)
+    static_assert(kTiles == (1u << kTileLog), "tiles per piece");
+    const uint32_t total = a.ppw * kTiles;                           // the warp's tile sequence
+    const uint64_t pair0 = uint64_t(blockIdx.y * kDW + warp) * a.ppw;
+    auto piece_of = [&](uint32_t t, uint32_t who) { return (pair0 + (t >> kTileLog)) * 2 + who; };
+    auto codes_at = [&](uint32_t t, uint32_t who) -> uint2 {
+        const uint64_t pc = piece_of(t, who);
+        if (t >= total || pc >= a.P) return make_uint2(0u, 0u);
+        return __ldg(codes2 + ((pc << 11) + ((t & (kTiles - 1)) << 5) + lane) * 2 + r);
+    };
+    // send the partial of tile t of the PEER's piece (codes c) into the peer's ring
+    auto send = [&](uint32_t t, uint2 c) {
+        const uint32_t slot = t % kPairRing, use = t / kPairRing;
+        uint32_t p[3];
+        pair_partial(M, R, c, p);
+        if (use) pbar_wait(&empty[warp][slot], (use - 1) & 1u);  // the peer has read the slot's last use
+        st_async_v4(peer_ring + (slot * 32 + lane) * 16, p[0], p[1], p[2], 0u, peer_full + slot * 8);
+    };
+    // codes one tile ahead: the next send's (peer piece) and the next own tile's
+    uint2 pc_next = codes_at(0, peer);
+    for (uint32_t t = 0; t + 1 < kPairRing && t < total; ++t) {
+        const uint2 c = pc_next;
+        pc_next = codes_at(t + 1, peer);
+        send(t, c);
+    }
+    uint2 own_next = codes_at(0, r);
+    uint32_t cnt = 0, nb = 0;
+    uint16_t* buf = nullptr;
+    for (uint32_t t = 0; t < total; ++t) {
+        if (t + kPairRing - 1 < total) {
+            const uint2 c = pc_next;
+            pc_next = codes_at(t + kPairRing, peer);
+            send(t + kPairRing - 1, c);
+        }
+        const uint32_t j = t & (kTiles - 1);
+        const uint64_t piece = piece_of(t, r);
+        if (j == 0) {
+            cnt = 0;
+            nb = 0;
+            const uint64_t q = lane < nqb ? q0 + lane : q0;  // idle lanes append nothing
+            buf = a.cbuf + (q * a.P + (piece < a.P ? piece : 0)) * a.B;
+        }
+        const uint2 oc = own_next;
+        own_next = codes_at(t + 1, r);
+        uint32_t own[3];
+        pair_partial(M, R, oc, own);
+        const uint32_t slot = t % kPairRing;
+        if (lane == 0) pbar_expect_tx(&full[warp][slot], 32 * 16);
+        pbar_wait(&full[warp][slot], (t / kPairRing) & 1u);
+        const uint4 pv = myring[slot * 32 + lane];
+        // 4-bit scores = own + peer (3-bit + 3-bit)
+        const uint32_t b0 = own[0] ^ pv.x, k0 = own[0] & pv.x;
+        const uint32_t t1 = own[1] ^ pv.y, b1 = t1 ^ k0, k1 = (own[1] & pv.y) | (t1 & k0);
+        const uint32_t t2 = own[2] ^ pv.z, b2 = t2 ^ k1, k2 = (own[2] & pv.z) | (t2 & k1);
+        __syncwarp();  // every lane has consumed its word of the slot
+        if (lane == 0) pbar_arrive_remote(peer_empty + slot * 8);  // the slot is free for the peer
+        const uint32_t b[4] = {b0, b1, b2, k2};
+        uint32_t gt = b[3] & ~TL[3], eq = ~(b[3] ^ TL[3]);
+#pragma unroll
+        for (int i = 2; i >= 0; --i) {
+            gt |= eq & b[i] & ~TL[i];
+            eq &= ~(b[i] ^ TL[i]);
+        }
+        const uint32_t ge0 = xp((gt | eq) & live);  // lane = query, bit = point j * 32 + bit
+        const uint32_t g1 = xp(gt & live);
+        cnt += __popc(ge0) | (__popc(g1) << 16);
+        if (piece < a.P) {
+            uint32_t bits = piece < cut ? ge0 : g1;  // past the tie cut: score > L only
+            const uint32_t tb = j * 32;
+            while (bits) {  // id order
+                const uint32_t bit = __ffs(bits) - 1;
+                bits &= bits - 1;
+                if (nb < a.B) buf[nb] = static_cast<uint16_t>((tb + bit) | (((g1 >> bit) & 1u) << 15));
+                ++nb;
+            }
+            if (j + 1 == kTiles && lane < nqb) {
+                const uint64_t i = (q0 + lane) * a.P + piece;
+                a.h2[i] = cnt;
+                a.ccnt[i] = static_cast<uint16_t>(nb);
+            }
+        }
+    }
+    cluster_sync_all();  // no CTA leaves while its peer may still write into its ring
+}
+
 __global__ void dense_codes_half_kernel(const uint32_t* ids, const uint32_t* cell_off, uint64_t n, uint32_t ns,
                                         uint32_t K, uint16_t* codes) {
     const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
@@ -1211,6 +1417,43 @@ static cudaError_t launch_fused_t(const DenseArgs& a, size_t smem, cudaStream_t 
     return cudaGetLastError();
 }
 
+size_t dense_pair_smem(uint32_t K) {
+    return ((size_t(4) * (K + 1) + 3) & ~size_t(3)) * 4 + size_t(32) * kPairRing * 32 * 16;
+}
+
+bool dense_pair_supported(uint32_t ns, uint32_t K) {
+    return ns >= 5 && ns <= 8 && K + 1 <= 65535 && dense_pair_smem(K) <= 220 * 1024;
+}
+
+static cudaError_t launch_fused_pair(const DenseArgs& a, cudaStream_t st) {
+    constexpr uint32_t kDT = 1024, kDW = kDT / 32;
+    const size_t smem = dense_pair_smem(a.K);
+    auto kern = dense_fused_pair_kernel<kDT>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    DenseArgs b = a;
+    const uint64_t qblocks = (a.nq + 31) / 32;
+    const uint64_t pairs = (a.P + 1) / 2;
+    int sms = 148, dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // piece pairs per warp: kFusedPPW / 2 amortises the mask build unless that starves the grid
+    b.ppw = kFusedPPW / 2 ? kFusedPPW / 2 : 1;
+    if (2 * qblocks * ((pairs + kDW * b.ppw - 1) / (kDW * b.ppw)) < 4ull * sms) b.ppw = 1;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(2 * qblocks), static_cast<unsigned>((pairs + kDW * b.ppw - 1) / (kDW * b.ppw)));
+    cfg.blockDim = dim3(kDT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, b);
+}
+
 cudaError_t launch_dense_select_fused(const DenseArgs& args, cudaStream_t st, cudaEvent_t main_done,
                                       cudaStream_t fb_st) {
     if (args.nq == 0) return cudaSuccess;
@@ -1224,7 +1467,9 @@ cudaError_t launch_dense_select_fused(const DenseArgs& args, cudaStream_t st, cu
     if (e != cudaSuccess) return e;
     dense_bound_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(a);
     // K3': histograms + supersets in one pass
-    if (a.half) {
+    if (a.half && a.pair) {
+        e = launch_fused_pair(a, st);
+    } else if (a.half) {
         e = launch_h<2>(a, st);
     } else {
         const Shape sh = dense_shape(a);

@@ -107,6 +107,7 @@ struct DenseArgs {
     uint32_t* pcut;               // single pass: nq, tie entries are stored only in pieces < pcut[q]
     uint32_t no_cut;              // tests: store every tie (pcut = P)
     uint32_t compact_mode;        // Tuning::dense_compact: 0 by superset density, 1 thread per piece, 2 warp
+    uint32_t pair;                // half mode: the fused pass as 2-CTA clusters with 32-bit masks of 4 subspaces each
     float cut_scale;              // tie cut = P * need/ties * cut_scale + cut_pad pieces (0: defaults 1.25, 8)
     uint32_t cut_pad;
     uint32_t words;               // Tuning::dense_words (0 = by shape)
@@ -120,6 +121,8 @@ size_t dense_smem(uint32_t ns, uint32_t K);
 // blocks, one u16 mask per (subspace, cell), two points per lane; codes hold cell + 1 per subspace
 // (0 = no cell), n_pad = rows rounded up to whole pieces (padding rows are all 0).
 bool dense_half_supported(uint32_t ns, uint32_t K);
+// the cluster-pair fused pass for half-mode tables: 5..8 subspaces, 4 x (K + 1) 32-bit slots per CTA
+bool dense_pair_supported(uint32_t ns, uint32_t K);
 cudaError_t launch_dense_codes_half(const uint32_t* ids, const uint32_t* cell_off, uint64_t n, uint64_t n_pad,
                                     uint32_t ns, uint32_t K, uint16_t* codes, cudaStream_t st);
 cudaError_t launch_dense_codes(const uint32_t* ids, const uint32_t* cell_off, uint64_t n, uint32_t ns, uint32_t K,

@@ -17,6 +17,9 @@ struct Tuning {
     bool q8 = true;              // SUCO_Q8=0: no int8 screen copy of float rows (the fp32 screen reads f32 rows)
     bool dense = true;           // SUCO_DENSE=0: the cluster-counting select only
     int dense_half = 1;          // SUCO_DENSE_HALF: 0 never, 1 when 32-bit masks do not fit, 2 force
+    int dense_pair = 0;          // SUCO_DENSE_PAIR=1: half mode's fused pass on 2-CTA clusters (measured slower at
+                                 // cfg5: select 403.6 vs 389.1 ms; half the shared-memory lookups, but the
+                                 // per-tile DSMEM exchange costs more than the bank conflicts it saves)
     bool dense_fused = true;     // SUCO_DENSE_FUSED=0: the two-pass dense select
     bool dense_stage = false;    // SUCO_DENSE_STAGE=1: stage every block's stores (tests)
     uint32_t dense_buf = 0;      // SUCO_DENSE_BUF: single-pass buffer entries per (piece, query); 0 = by memory

@@ -160,6 +160,7 @@ Tuning tuning_from_env() {
     t.q8 = env_int("SUCO_Q8", 1) != 0;
     t.dense = env_int("SUCO_DENSE", 1) != 0;
     t.dense_half = env_int("SUCO_DENSE_HALF", 1);
+    t.dense_pair = env_int("SUCO_DENSE_PAIR", 0);
     t.dense_fused = env_int("SUCO_DENSE_FUSED", 1) != 0;
     t.dense_stage = std::getenv("SUCO_DENSE_STAGE") != nullptr;
     const int b = env_int("SUCO_DENSE_BUF", 0);

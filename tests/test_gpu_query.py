@@ -358,14 +358,16 @@ def test_dense_buffer_overflow_falls_back(gpu, oracle, overlap, monkeypatch, cap
     assert flagged and max(flagged) > 0, err
 
 
-@pytest.mark.parametrize("fused", ["1", "0"])
+@pytest.mark.parametrize("fused", ["1", "0", "pair"])
 @pytest.mark.parametrize("ns,kh,nq", [(6, 20, 77), (8, 30, 40), (3, 45, 16)])
 def test_dense_half_width_mode(gpu, oracle, ns, kh, fused, nq, monkeypatch):
     """The half-width dense select (16-query blocks, u16 masks, two points per lane — the mode config
     5's 8 x 10,000 cells take) forced on small tables: single-pass and two-pass, N_s < 8 (code
-    positions past N_s), a partial last query block and a partial last 64-point tile."""
+    positions past N_s), a partial last query block and a partial last 64-point tile; "pair": the
+    single pass on 2-CTA clusters (32-bit masks of 4 subspaces per CTA, DSMEM exchange; N_s >= 5)."""
     monkeypatch.setenv("SUCO_DENSE_HALF", "2")
-    monkeypatch.setenv("SUCO_DENSE_FUSED", fused)
+    monkeypatch.setenv("SUCO_DENSE_FUSED", "0" if fused == "0" else "1")
+    monkeypatch.setenv("SUCO_DENSE_PAIR", "1" if fused == "pair" else "0")
     full = oracle.clustered(60000 + nq, 24, 30, 2024 + ns, 0, 100, 9, True)
     base, qs = oracle.hold_out(full, nq, 2025)
     oidx = oracle.build_index(base, ns, kh, 3, 42, 0)
