@@ -63,7 +63,11 @@ struct Xpose {
         msk4 = (lane & 4) ? ~0x0f0f0f0fu : 0x0f0f0f0fu;
         msk2 = (lane & 2) ? ~0x33333333u : 0x33333333u;
         msk1 = (lane & 1) ? ~0x55555555u : 0x55555555u;
+        // opaque copies: ptxas would otherwise rematerialise the per-lane constants inside the
+        // scoring loops (S2R + R2P + SELs per tile, measured in the cfg4 fused pass's SASS)
+        pin(sel16), pin(sel8), pin(amt4), pin(amt2), pin(amt1), pin(msk4), pin(msk2), pin(msk1);
     }
+    __device__ __forceinline__ static void pin(uint32_t& v) { asm volatile("mov.b32 %0, %0;" : "+r"(v)); }
     __device__ __forceinline__ static uint32_t bits(uint32_t x, uint32_t y, uint32_t amt, uint32_t msk) {
         const uint32_t r = __funnelshift_l(y, y, amt);
         return (x & msk) | (r & ~msk);
@@ -109,7 +113,7 @@ template <uint32_t kDT, uint32_t W>
 __device__ void build_masks(const DenseArgs& a, uint32_t* M, uint64_t q0, uint32_t nqb) {
     constexpr uint32_t kDW = kDT / 32;
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    const uint32_t words = (a.ns * a.K + 1) * W;
+    const uint32_t words = (dense_none(a.ns, a.K) + 1) * W;
     for (uint32_t i = tid; i < words; i += kDT) M[i] = 0;
     __syncthreads();
     for (uint32_t j = warp; j < nqb; j += kDW) {
@@ -118,7 +122,8 @@ __device__ void build_masks(const DenseArgs& a, uint32_t* M, uint64_t q0, uint32
             const uint64_t t = q * a.ns + s;
             const uint32_t cnt = a.cells_off ? static_cast<uint32_t>(a.cells_off[t + 1] - a.cells_off[t]) : a.ncells[t];
             const uint32_t* cp = a.cells + (a.cells_off ? a.cells_off[t] : t * a.cells_cap);
-            for (uint32_t i = lane; i < cnt; i += 32) atomicOr(M + (s * a.K + cp[i]) * W + (j >> 5), 1u << (j & 31u));
+            for (uint32_t i = lane; i < cnt; i += 32)
+                atomicOr(M + dense_slot(a.ns, a.K, s, cp[i]) * W + (j >> 5), 1u << (j & 31u));
         }
     }
     __syncthreads();
@@ -139,7 +144,7 @@ __device__ __forceinline__ void mask_at(const uint32_t* M, uint32_t slot, uint32
 // block's 32*W queries: b[w][i] bit j = bit i of query (32w + j)'s score.
 template <uint32_t NC>
 __device__ __forceinline__ Codes<NC> load_codes(const DenseArgs& a, uint64_t p, uint64_t p_hi) {
-    const uint32_t none = a.ns * a.K;
+    const uint32_t none = dense_none(a.ns, a.K);
     Codes<NC> c;
 #pragma unroll
     for (uint32_t i = 0; i < NC; ++i) c.v[i] = make_uint4(none | (none << 16), none | (none << 16), none | (none << 16), none | (none << 16));
@@ -152,7 +157,7 @@ __device__ __forceinline__ Codes<NC> load_codes(const DenseArgs& a, uint64_t p, 
 
 template <uint32_t NC>
 __device__ __forceinline__ Codes<NC> load_codes_at(const DenseArgs& a, const uint4* p, bool valid) {
-    const uint32_t none = a.ns * a.K;
+    const uint32_t none = dense_none(a.ns, a.K);
     const uint32_t nn = none | (none << 16);
     Codes<NC> c;
 #pragma unroll
@@ -313,6 +318,14 @@ __device__ __forceinline__ uint32_t level_n(const uint4* row, uint32_t t) {
 }
 
 __device__ __forceinline__ uint32_t nc_of(const DenseArgs& a) { return a.nc ? a.nc : 1u; }
+
+// Single-pass candidate buffers, [query][piece][B]: entry e of (q, piece) at cb_base(q, piece) +
+// cb_off(e); a lane of the fused pass appends to its own contiguous buffer. (Measured against a
+// [query][chunk][piece] interleave at cfg4: the interleave wrote 5.7 GB instead of 4.4 GB.)
+__device__ __forceinline__ uint16_t* cb_base(const DenseArgs& a, uint64_t q, uint32_t piece) {
+    return a.cbuf + (q * a.P + piece) * a.B;
+}
+__device__ __forceinline__ uint32_t cb_off(const DenseArgs&, uint32_t e) { return e; }
 
 // K2: warp per query — T, need, per-piece tie quota (id order) and output offset.
 __global__ void __launch_bounds__(256) dense_plan_kernel(DenseArgs a) {
@@ -604,18 +617,21 @@ __device__ __forceinline__ void fused_pieces(const DenseArgs& a, const uint32_t*
             nb[w] = 0;
             sw[w] = 0;
             const uint64_t q = 32 * w + lane < nqb ? q0 + 32 * w + lane : q0;  // idle lanes append nothing
-            buf[w] = a.cbuf + (q * a.P + piece) * a.B;
+            buf[w] = cb_base(a, q, piece);
         }
         // 32-bit tile loop over the piece: a running code pointer, the piece's point count
         const uint32_t len = static_cast<uint32_t>(hi - lo);
         const uint4* cptr = a.codes + (lo + lane) * NC;
         Codes<NC> code = load_codes_at<NC>(a, cptr, lane < len);
+        Codes<NC> code1 = load_codes_at<NC>(a, cptr + 32 * NC, 32 + lane < len);
         for (uint32_t tb = 0; tb < len; tb += 32) {
             cptr += 32 * NC;
-            const Codes<NC> next = load_codes_at<NC>(a, cptr, tb + 32 + lane < len);  // one tile ahead
+            // two tiles ahead: the code loads miss L2 often enough that one tile did not cover them
+            const Codes<NC> next = load_codes_at<NC>(a, cptr + 32 * NC, tb + 64 + lane < len);
             uint32_t b[W][NP];
             planes_of<W, NC>(M, code, b);
-            code = next;
+            code = code1;
+            code1 = next;
 #pragma unroll
             for (uint32_t w = 0; w < W; ++w) {
                 // most significant plane first; points past the piece end score 0 < L
@@ -636,9 +652,9 @@ __device__ __forceinline__ void fused_pieces(const DenseArgs& a, const uint32_t*
                         const uint32_t v = (tb + r) | (((g1 >> r) & 1u) << 15);
                         if constexpr (STAGE) {
                             sw[w] = (sw[w] >> 16) | (static_cast<uint64_t>(v) << 48);
-                            if ((nb[w] & 3u) == 3u) *reinterpret_cast<uint64_t*>(buf[w] + (nb[w] & ~3u)) = sw[w];
+                            if ((nb[w] & 3u) == 3u) *reinterpret_cast<uint64_t*>(buf[w] + cb_off(a, nb[w] & ~3u)) = sw[w];
                         } else {
-                            buf[w][nb[w]] = static_cast<uint16_t>(v);
+                            buf[w][cb_off(a, nb[w])] = static_cast<uint16_t>(v);
                         }
                     }
                     ++nb[w];
@@ -652,7 +668,7 @@ __device__ __forceinline__ void fused_pieces(const DenseArgs& a, const uint32_t*
                 if constexpr (STAGE) {
                     const uint32_t kept = min(nb[w], a.B), part = kept & 3u;
                     if (part)  // the last, partial chunk: its entries down to the low end
-                        *reinterpret_cast<uint64_t*>(buf[w] + (kept & ~3u)) = sw[w] >> (16 * (4 - part));
+                        *reinterpret_cast<uint64_t*>(buf[w] + cb_off(a, kept & ~3u)) = sw[w] >> (16 * (4 - part));
                 }
                 a.h2[i] = cnt[w];
                 a.ccnt[i] = static_cast<uint16_t>(nb[w]);  // <= WP = 2048
@@ -694,57 +710,78 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs 
 }
 
 // K4: thread per (query, piece), T == L: the piece's buffer holds its score >= T points in id
-// order; keep every score > T and the first quota ties. Neighbouring threads take neighbouring
-// pieces: contiguous buffers in, contiguous candidate runs out.
-// K4 for sparse supersets: thread per (query, piece); its few entries (cfg2: about 13) are read
-// and written by the one thread. Queries with dense supersets (L's kDenseStage flag) are left to
-// the warp kernel below.
+// order; keep every score > T and the first quota ties. A block takes 256 consecutive pieces of
+// one query, whose outputs are one contiguous run of the query's candidates (pieces in order): each
+// thread loads its whole buffer (independent 16-byte loads), places its kept ids in a shared
+// staging copy of the run, and the block writes the run with coalesced stores. Runs longer than
+// the staging area write their tail directly.
+constexpr uint32_t kCompactStage = 8192;  // staged candidate ids per block (32 KB)
 __global__ void __launch_bounds__(256) dense_compact_thread_kernel(DenseArgs a) {
+    __shared__ uint32_t stage[kCompactStage];
+    __shared__ uint32_t run_lo, run_hi;
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= a.P) return;
     const uint32_t pbase = p * a.WP;
     for (uint64_t q = blockIdx.y; q < a.nq; q += gridDim.y) {
-        if (a.compact_mode == 2 || (a.compact_mode == 0 && (a.L[q] & kDenseStage))) continue;
+        if (a.compact_mode == 2 || a.qflag[q]) continue;  // (n <= B: an overflowing contributing piece flags its query)
+        if (threadIdx.x == 0) {
+            run_lo = 0xffffffffu;
+            run_hi = 0;
+        }
+        __syncthreads();
         const uint64_t i = q * a.P + p;
-        const uint32_t n = a.ccnt[i];
-        if (!n || a.qflag[q]) continue;  // (n <= B: an overflowing contributing piece flags its query)
-        uint32_t quota = a.quota[i];
-        uint32_t pos = a.base[i];
+        const uint32_t n = p < a.P ? min(static_cast<uint32_t>(a.ccnt[i]), a.B) : 0u;
+        uint32_t quota = 0, pos = 0;
+        if (n) {
+            quota = a.quota[i];
+            pos = a.base[i];
+            atomicMin(&run_lo, pos);
+        }
+        __syncthreads();
+        const uint32_t lo = run_lo;
         uint32_t* out = a.cands + q * a.m;
-        const uint4* buf = reinterpret_cast<const uint4*>(a.cbuf + i * a.B);
-        const uint32_t lim = min(n, a.B);
-        for (uint32_t e0 = 0; e0 < lim; e0 += 8) {
-            const uint4 v = buf[e0 >> 3];
-            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+        const uint4* buf = reinterpret_cast<const uint4*>(cb_base(a, q, p < a.P ? p : 0u));
+        uint32_t at = pos - lo;  // staging offset of this thread's next kept id
+        for (uint32_t e0 = 0; e0 < n; e0 += 64) {
+            uint4 v[8];
 #pragma unroll
-            for (uint32_t e = 0; e < 8; ++e) {
-                if (e0 + e < lim) {
-                    const uint32_t x = (w[e >> 1] >> ((e & 1) * 16)) & 0xffffu;
-                    if (x & 0x8000u) {
-                        __stcs(out + pos++, pbase + (x & 0x7fffu));
-                    } else if (quota) {  // first ties in id order
-                        --quota;
-                        __stcs(out + pos++, pbase + x);
+            for (uint32_t u = 0; u < 8; ++u) v[u] = e0 + 8 * u < n ? __ldcs(buf + (e0 >> 3) + u) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+            for (uint32_t u = 0; u < 8; ++u) {
+                const uint32_t w4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                for (uint32_t h = 0; h < 8; ++h) {
+                    const uint32_t x = (w4[h >> 1] >> (16 * (h & 1u))) & 0xffffu;
+                    const bool valid = e0 + 8 * u + h < n;
+                    const bool gt = (x & 0x8000u) != 0;
+                    const bool tie = valid && !gt && quota != 0;  // the first ties in id order
+                    if ((valid && gt) || tie) {
+                        const uint32_t id = pbase + (x & 0x7fffu);
+                        if (at < kCompactStage) stage[at] = id;
+                        else __stcs(out + lo + at, id);
+                        ++at;
                     }
+                    quota -= tie ? 1u : 0u;
                 }
             }
         }
+        if (n) atomicMax(&run_hi, at);
+        __syncthreads();
+        const uint32_t len = min(run_hi, kCompactStage);
+        for (uint32_t j = threadIdx.x; j < len; j += blockDim.x) __stcs(out + lo + j, stage[j]);
+        __syncthreads();  // the staging area and run bounds are reused by the next query
     }
 }
 
-// K4 for dense supersets (cfg4: pieces before the tie cut hold about 80 entries). A warp takes one
-// query's 32 consecutive pieces: lane j holds
-// piece j's count, tie quota and output offset; then piece by piece the lanes read its buffer in
-// coalesced 32-entry rows and keep every score > T entry plus the first `quota` ties (id order:
-// the buffer order), writing consecutive output positions.
+// K4, warp variant (Tuning::dense_compact = 2, A/B): a warp takes one query's 32 consecutive
+// pieces; piece by piece the lanes read 32 entries and keep every score > T entry plus the first
+// `quota` ties (id order: the buffer order), writing consecutive output positions.
 __global__ void __launch_bounds__(256) dense_compact_kernel(DenseArgs a) {
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const uint32_t p0 = (blockIdx.x * 8 + warp) * 32;
     if (p0 >= a.P) return;
     const uint32_t lt = (1u << lane) - 1u;
     for (uint64_t q = blockIdx.y; q < a.nq; q += gridDim.y) {
-        const bool warp_mode = a.compact_mode == 2 || (a.compact_mode == 0 && (a.L[q] & kDenseStage));
-        if (!warp_mode || a.qflag[q]) continue;  // (overflow flags the query)
+        if (a.compact_mode != 2 || a.qflag[q]) continue;  // (overflow flags the query)
         const uint32_t p = p0 + lane;
         const uint64_t i = q * a.P + p;
         uint32_t n = 0, quota = 0, base = 0;
@@ -762,12 +799,12 @@ __global__ void __launch_bounds__(256) dense_compact_kernel(DenseArgs a) {
             todo &= todo - 1;
             const uint32_t pn = __shfl_sync(kFull, n, src), pq = __shfl_sync(kFull, quota, src);
             uint32_t pos = __shfl_sync(kFull, base, src);
-            const uint16_t* buf = a.cbuf + (q * a.P + p0 + src) * a.B;
+            const uint16_t* buf = cb_base(a, q, p0 + src);
             const uint32_t pbase = (p0 + src) * a.WP;
             uint32_t ties = 0;
             for (uint32_t e0 = 0; e0 < pn; e0 += 32) {
                 const uint32_t e = e0 + lane;
-                const uint32_t x = e < pn ? buf[e] : 0u;
+                const uint32_t x = e < pn ? buf[cb_off(a, e)] : 0u;
                 const bool gt = e < pn && (x & 0x8000u);
                 const bool tie = e < pn && !(x & 0x8000u);
                 const uint32_t tb = __ballot_sync(kFull, tie);
@@ -798,8 +835,13 @@ __global__ void dense_codes_kernel(const uint32_t* ids, const uint32_t* cell_off
     const uint32_t s = static_cast<uint32_t>(t / K), cell = static_cast<uint32_t>(t % K);
     const uint32_t* off = cell_off + uint64_t(s) * (K + 1);
     const uint32_t* sid = ids + uint64_t(s) * n;
-    const uint16_t code = static_cast<uint16_t>(s * K + cell);
-    for (uint32_t i = off[cell]; i < off[cell + 1]; ++i) codes[uint64_t(sid[i]) * cw + s] = code;
+    const uint16_t code = static_cast<uint16_t>(dense_slot(ns, K, s, cell));
+    // grouped layout: point p keeps subspace s at position (s - p) % 8 (lane-rotated lookups)
+    if (dense_grouped(ns)) {
+        for (uint32_t i = off[cell]; i < off[cell + 1]; ++i) codes[uint64_t(sid[i]) * cw + ((s - sid[i]) & 7u)] = code;
+    } else {
+        for (uint32_t i = off[cell]; i < off[cell + 1]; ++i) codes[uint64_t(sid[i]) * cw + s] = code;
+    }
 }
 
 // ------------------------------------------------------------ half-width mode
@@ -1006,7 +1048,7 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_h_kernel(DenseArg
         const uint64_t lo = uint64_t(piece) * a.WP;
         const uint64_t hi = min_u64(a.n, lo + a.WP);
         uint32_t cnt = 0, nb = 0;
-        uint16_t* buf = a.cbuf + ((mine ? q0 + qj : q0) * a.P + piece) * a.B;
+        uint16_t* buf = cb_base(a, mine ? q0 + qj : q0, piece);
         // 32-bit tile loop (the padded code rows cover a whole last piece)
         const uint32_t len = static_cast<uint32_t>(hi - lo);
         const uint4* cptr = a.codes + lo + lane;
@@ -1039,7 +1081,7 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_h_kernel(DenseArg
             while (bits) {  // id order
                 const uint32_t r = __ffs(bits) - 1;
                 bits &= bits - 1;
-                if (at < a.B) buf[at] = static_cast<uint16_t>((tb + r) | (((g1 >> r) & 1u) << 15));
+                if (at < a.B) buf[cb_off(a, at)] = static_cast<uint16_t>((tb + r) | (((g1 >> r) & 1u) << 15));
                 ++at;
             }
             nb += c0 + o0;
@@ -1214,7 +1256,7 @@ __global__ void __launch_bounds__(kDT, 1) dense_fused_pair_kernel(DenseArgs a) {
             cnt = 0;
             nb = 0;
             const uint64_t q = lane < nqb ? q0 + lane : q0;  // idle lanes append nothing
-            buf = a.cbuf + (q * a.P + (piece < a.P ? piece : 0)) * a.B;
+            buf = cb_base(a, q, piece < a.P ? static_cast<uint32_t>(piece) : 0u);
         }
         const uint2 oc = own_next;
         own_next = codes_at(t + 1, r);
@@ -1246,7 +1288,7 @@ __global__ void __launch_bounds__(kDT, 1) dense_fused_pair_kernel(DenseArgs a) {
             while (bits) {  // id order
                 const uint32_t bit = __ffs(bits) - 1;
                 bits &= bits - 1;
-                if (nb < a.B) buf[nb] = static_cast<uint16_t>((tb + bit) | (((g1 >> bit) & 1u) << 15));
+                if (nb < a.B) buf[cb_off(a, nb)] = static_cast<uint16_t>((tb + bit) | (((g1 >> bit) & 1u) << 15));
                 ++nb;
             }
             if (j + 1 == kTiles && lane < nqb) {
@@ -1315,21 +1357,22 @@ static cudaError_t launch_h(const DenseArgs& a, cudaStream_t st) {
 }
 
 bool dense_supported(uint32_t ns, uint32_t K) {
-    return ns >= 1 && ns <= 8 && uint64_t(ns) * K + 1 <= 65535 && (uint64_t(ns) * K + 1) * 4 <= 200 * 1024;
+    const uint64_t slots = uint64_t(dense_none(ns, K)) + 1;
+    return ns >= 1 && ns <= 8 && slots <= 65535 && slots * 4 <= 200 * 1024;
 }
 
 bool dense_wide_supported(uint32_t ns, uint32_t K) {
     return ns >= 9 && ns <= 16 && uint64_t(ns) * K + 1 <= 65535 && (uint64_t(ns) * K + 1) * 4 <= 200 * 1024;
 }
 
-size_t dense_smem(uint32_t ns, uint32_t K) { return (size_t(ns) * K + 1) * 4; }
+size_t dense_smem(uint32_t ns, uint32_t K) { return (size_t(dense_none(ns, K)) + 1) * 4; }
 
 cudaError_t launch_dense_codes(const uint32_t* ids, const uint32_t* cell_off, uint64_t n, uint32_t ns, uint32_t K,
                                uint16_t* codes, cudaStream_t st) {
     const uint32_t cw = ns > 8 ? 16 : 8;
     const uint64_t count = n * cw;
     const unsigned fb = static_cast<unsigned>(min_u64((count + 255) / 256, 148ull * 16));
-    dense_codes_fill_kernel<<<fb ? fb : 1, 256, 0, st>>>(codes, count, static_cast<uint16_t>(ns * K));
+    dense_codes_fill_kernel<<<fb ? fb : 1, 256, 0, st>>>(codes, count, static_cast<uint16_t>(dense_none(ns, K)));
     const uint64_t total = uint64_t(ns) * K;
     dense_codes_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(ids, cell_off, n, ns, K, codes, cw);
     return cudaGetLastError();
@@ -1481,8 +1524,8 @@ cudaError_t launch_dense_select_fused(const DenseArgs& args, cudaStream_t st, cu
     // plan (+ fallback flags) from the two levels, compaction
     dense_plan_fused_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(a);
     const dim3 cgrid((a.P + 255) / 256, static_cast<unsigned>(min_u64(a.nq, 65535)));
-    dense_compact_thread_kernel<<<cgrid, 256, 0, st>>>(a);  // sparse supersets
-    dense_compact_kernel<<<cgrid, 256, 0, st>>>(a);         // dense supersets
+    if (a.compact_mode == 2) dense_compact_kernel<<<cgrid, 256, 0, st>>>(a);  // warp per 32 pieces (A/B)
+    else dense_compact_thread_kernel<<<cgrid, 256, 0, st>>>(a);
     e = cudaMemsetAsync(args.nmap, 0, 4, st);
     if (e != cudaSuccess) return e;
     dense_flag_list_kernel<<<static_cast<unsigned>((a.nq + 255) / 256), 256, 0, st>>>(args);

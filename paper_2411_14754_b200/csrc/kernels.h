@@ -106,13 +106,26 @@ struct DenseArgs {
     uint32_t nc;                  // uint4 code vectors per point: 1 (N_s <= 8, default) or 2 (N_s <= 16)
     uint32_t* pcut;               // single pass: nq, tie entries are stored only in pieces < pcut[q]
     uint32_t no_cut;              // tests: store every tie (pcut = P)
-    uint32_t compact_mode;        // Tuning::dense_compact: 0 by superset density, 1 thread per piece, 2 warp
+    uint32_t compact_mode;        // Tuning::dense_compact: 0/1 thread per piece, 2 warp per 32 pieces
     uint32_t pair;                // half mode: the fused pass as 2-CTA clusters with 32-bit masks of 4 subspaces each
     float cut_scale;              // tie cut = P * need/ties * cut_scale + cut_pad pieces (0: defaults 1.25, 8)
     uint32_t cut_pad;
     uint32_t words;               // Tuning::dense_words (0 = by shape)
     uint8_t* scores_dbg;          // optional (nq == 1): K3 writes query 0's SC-score of every point (parity)
 };
+// Mask-table slots of the 32-bit dense select. Eight subspaces (every NC = 1 configuration of the
+// bench) use a bank-grouped layout: subspace s owns banks 4s..4s+3, slot(s, c) = (c / 4) * 32 +
+// 4s + c % 4, and a point's code position j holds subspace (j + p) % 8, so lane l of a tile looks
+// up subspace (j + l) % 8 in load j: four lanes per 4-bank group instead of 32 lanes over 32
+// banks (expected worst bank load 2.95 instead of 3.53 for random cells). Other subspace counts
+// keep slot(s, c) = s * K + c with position j = subspace j. The last slot is the zero slot.
+__host__ __device__ inline bool dense_grouped(uint32_t ns) { return ns == 8; }
+__host__ __device__ inline uint32_t dense_none(uint32_t ns, uint32_t K) {
+    return dense_grouped(ns) ? 8u * ((K + 3u) & ~3u) : ns * K;
+}
+__host__ __device__ inline uint32_t dense_slot(uint32_t ns, uint32_t K, uint32_t s, uint32_t c) {
+    return dense_grouped(ns) ? ((c >> 2) << 5) | (s << 2) | (c & 3u) : s * K + c;
+}
 bool dense_supported(uint32_t ns, uint32_t K);
 // 9..16 subspaces: two code vectors per point, 5 score planes, 16 histogram levels (config 3)
 bool dense_wide_supported(uint32_t ns, uint32_t K);

@@ -25,7 +25,7 @@ struct Tuning {
     uint32_t dense_buf = 0;      // SUCO_DENSE_BUF: single-pass buffer entries per (piece, query); 0 = by memory
     bool dense_nocut = false;    // SUCO_DENSE_NOCUT=1: store every tie (tests)
     uint32_t dense_words = 0;    // SUCO_DENSE_WORDS: mask words per slot (0 auto, 1, 2)
-    uint32_t dense_compact = 0;  // SUCO_DENSE_COMPACT: 0 by superset density, 1 thread per piece, 2 warp per 32 pieces
+    uint32_t dense_compact = 0;  // SUCO_DENSE_COMPACT: 0/1 thread per piece (default), 2 warp per 32 pieces
     bool dense_stats = false;    // SUCO_DENSE_STATS=1: print the single-pass fallback rate (diagnostics)
     bool rerank_stats = false;   // SUCO_RERANK_STATS=1: print the int8 screen's exact re-rank counts (diagnostics)
     uint32_t tiles = 1;          // SUCO_TILES: minimum pipeline tiles per batch (tests: slot reuse)
