@@ -479,6 +479,22 @@ struct FbLists {
     const uint32_t* nmap = nullptr;
 };
 
+// Points per piece of the single pass: the largest of 16384 .. 2048 that still gives the fused
+// pass about sixteen CTAs per SM (32 pieces per CTA row, 32 queries per CTA). Measured per step:
+// cfg4 (10M points, 10K queries) 2048 / 8192 / 16384 -> 38.2 / 32.9 / 31.4 ms; cfg2 (1M, 10K)
+// 2048 / 4096 / 8192 -> 4.19 / 4.09 / 4.29 ms; small corpora or batches keep 2048 (cfg1, cfg3).
+uint32_t fused_piece(uint64_t n, uint64_t nq, uint32_t nc) {
+    int sms = 148, dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t qblocks = (nq + 31) / 32;
+    (void)nc;
+    for (uint32_t wp = 16384; wp > kDensePiece; wp /= 2) {
+        const uint64_t P = (n + wp - 1) / wp;
+        if (qblocks * ((P + 31) / 32) >= 16ull * sms) return wp;
+    }
+    return kDensePiece;
+}
+
 // Bytes of single-pass candidate buffers beyond kDenseBuf entries (small batches): at most 1 GB.
 constexpr uint64_t kDenseBufExtra = 1ull << 30;
 
@@ -508,6 +524,14 @@ FbLists stage_select(const suco_gpu_index* x, suco_gpu_query_ctx* c, suco_gpu_qu
         da.scores_dbg = scores_dbg;
         const bool fused = tn.dense_fused && !scores_dbg;  // the score dump is a two-pass emission
         if (fused) {
+            // larger pieces for the single pass (the half-width mode keeps kDensePiece: its code rows
+            // are padded to whole 2048-point pieces): a quarter of the per-(query, piece) counts,
+            // quotas and buffers, and buffers four times fuller, so far fewer partly written sectors
+            // (measured at cfg4: fused pass writes and compaction reads)
+            if (!da.half) {
+                da.WP = tn.dense_piece ? tn.dense_piece : fused_piece(h.n, nt, h.layout.ns > 8 ? 2u : 1u);
+                da.P = static_cast<uint32_t>((h.n + da.WP - 1) / da.WP);
+            }
             // the sampled histograms (every pstride-th piece) predict the threshold: about 16 sampled
             // pieces when that is enough (cfg2: 489 pieces -> every 30th), every 64th piece at most
             // for large corpora (measured: cfg2 2.31M -> 2.36M q/s, cfg4 167K -> 174K; fewer samples
@@ -520,7 +544,8 @@ FbLists stage_select(const suco_gpu_index* x, suco_gpu_query_ctx* c, suco_gpu_qu
             // batches x corpora (cfg3: 1K queries x 489 pieces) get up to 2048 (one whole piece)
             // within kDenseBufExtra, so dense supersets do not overflow into the two-pass fallback
             const uint64_t fit = kDenseBufExtra / (2ull * nt * da.P) / 8 * 8;
-            da.B = static_cast<uint32_t>(std::min<uint64_t>(kDensePiece, std::max<uint64_t>(kDenseBuf, fit)));
+            const uint64_t minb = uint64_t(kDenseBuf) * (da.WP / kDensePiece);
+            da.B = static_cast<uint32_t>(std::min<uint64_t>(da.WP, std::max<uint64_t>(minb, fit)));
             if (tn.dense_buf) da.B = tn.dense_buf;
             sl.dcbuf.reserve(nt * da.P * da.B);
             sl.dccnt.reserve(nt * da.P);
@@ -529,8 +554,11 @@ FbLists stage_select(const suco_gpu_index* x, suco_gpu_query_ctx* c, suco_gpu_qu
             sl.dL.reserve(nt);
             sl.dh2.reserve(nt * da.P);
             da.h2 = sl.dh2.p;
-            sl.dflag.reserve(3 * nt + 1);  // flags, flagged list, its count, tie cuts
+            // flags, flagged list, its count, tie cuts, the dense / sparse compaction lists and counts
+            sl.dflag.reserve(5 * nt + 3);
             da.pcut = sl.dflag.p + 2 * nt + 1;
+            da.clist = sl.dflag.p + 3 * nt + 1;
+            da.nclist = sl.dflag.p + 5 * nt + 1;
             da.no_cut = tn.dense_nocut;
             da.compact_mode = tn.dense_compact;
             da.hsample = sl.dsample.p;

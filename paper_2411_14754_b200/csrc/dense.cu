@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -319,6 +320,12 @@ __device__ __forceinline__ uint32_t level_n(const uint4* row, uint32_t t) {
 
 __device__ __forceinline__ uint32_t nc_of(const DenseArgs& a) { return a.nc ? a.nc : 1u; }
 
+// Which single-pass compaction kernel takes query q: the warp kernel for dense supersets (the L[q]
+// flag of the bound kernel), the thread kernel for sparse ones (Tuning::dense_compact forces either).
+__device__ __forceinline__ bool dense_compact_warp(const DenseArgs& a, uint64_t q) {
+    return a.compact_mode == 2 || (a.compact_mode == 0 && (a.L[q] & kDenseStage));
+}
+
 // Single-pass candidate buffers, [query][piece][B]: entry e of (q, piece) at cb_base(q, piece) +
 // cb_off(e); a lane of the fused pass appends to its own contiguous buffer. (Measured against a
 // [query][chunk][piece] interleave at cfg4: the interleave wrote 5.7 GB instead of 4.4 GB.)
@@ -457,6 +464,10 @@ __global__ void __launch_bounds__(256) dense_plan_fused_kernel(DenseArgs a) {
     ok = __all_sync(kFull, ok);
     if (lane == 0) {
         a.qflag[q] = ok ? 0u : 1u;
+        if (ok && a.clist) {  // the compaction kernels' work lists
+            const uint32_t wl = dense_compact_warp(a, q) ? 0u : 1u;
+            a.clist[wl * a.nq + atomicAdd(a.nclist + wl, 1u)] = static_cast<uint32_t>(q);
+        }
         a.T[q] = L;
     }
 }
@@ -582,7 +593,8 @@ __global__ void __launch_bounds__(256) dense_bound_kernel(DenseArgs a) {
         const double need = static_cast<double>(a.m) - static_cast<double>(above) * scale;
         if (ties > 0.0 && need < ties) {
             const double cs = a.cut_scale > 0.f ? static_cast<double>(a.cut_scale) : 1.25;
-            const double cp = a.cut_scale > 0.f ? static_cast<double>(a.cut_pad) : 8.0;
+            // (+8 pieces of 2048 points: the pad is in points, whatever the piece size)
+            const double cp = a.cut_scale > 0.f ? static_cast<double>(a.cut_pad) : 8.0 * kDensePiece / a.WP;
             const double c = static_cast<double>(a.P) * (need > 0.0 ? need / ties : 0.0) * cs + cp;
             cut = c < static_cast<double>(a.P) ? static_cast<uint32_t>(c) : a.P;
         }
@@ -671,7 +683,7 @@ __device__ __forceinline__ void fused_pieces(const DenseArgs& a, const uint32_t*
                         *reinterpret_cast<uint64_t*>(buf[w] + cb_off(a, kept & ~3u)) = sw[w] >> (16 * (4 - part));
                 }
                 a.h2[i] = cnt[w];
-                a.ccnt[i] = static_cast<uint16_t>(nb[w]);  // <= WP = 2048
+                a.ccnt[i] = static_cast<uint16_t>(nb[w]);  // <= WP <= 32768
             }
         }
     }
@@ -721,8 +733,9 @@ __global__ void __launch_bounds__(256) dense_compact_thread_kernel(DenseArgs a) 
     __shared__ uint32_t run_lo, run_hi;
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t pbase = p * a.WP;
-    for (uint64_t q = blockIdx.y; q < a.nq; q += gridDim.y) {
-        if (a.compact_mode == 2 || a.qflag[q]) continue;  // (n <= B: an overflowing contributing piece flags its query)
+    const uint32_t nlist = a.nclist[1];
+    for (uint32_t j = blockIdx.y; j < nlist; j += gridDim.y) {
+        const uint64_t q = a.clist[a.nq + j];  // an unflagged query with a sparse superset
         if (threadIdx.x == 0) {
             run_lo = 0xffffffffu;
             run_hi = 0;
@@ -772,45 +785,45 @@ __global__ void __launch_bounds__(256) dense_compact_thread_kernel(DenseArgs a) 
     }
 }
 
-// K4, warp variant (Tuning::dense_compact = 2, A/B): a warp takes one query's 32 consecutive
-// pieces; piece by piece the lanes read 32 entries and keep every score > T entry plus the first
-// `quota` ties (id order: the buffer order), writing consecutive output positions.
+// K4 (default): a warp per (query, piece). The lanes read the buffer in 32-entry rows (64
+// contiguous bytes; four rows in flight), keep every score > T entry and the first `quota` ties
+// (id order: the buffer order), and write consecutive output positions.
 __global__ void __launch_bounds__(256) dense_compact_kernel(DenseArgs a) {
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    const uint32_t p0 = (blockIdx.x * 8 + warp) * 32;
-    if (p0 >= a.P) return;
+    const uint32_t p = blockIdx.x * 8 + warp;
+    if (p >= a.P) return;
     const uint32_t lt = (1u << lane) - 1u;
-    for (uint64_t q = blockIdx.y; q < a.nq; q += gridDim.y) {
-        if (a.compact_mode != 2 || a.qflag[q]) continue;  // (overflow flags the query)
-        const uint32_t p = p0 + lane;
+    const uint32_t pbase = p * a.WP;
+    const uint32_t nlist = a.nclist[0];
+    for (uint32_t j = blockIdx.y; j < nlist; j += gridDim.y) {
+        const uint64_t q = a.clist[j];  // an unflagged query with a dense superset
         const uint64_t i = q * a.P + p;
-        uint32_t n = 0, quota = 0, base = 0;
-        if (p < a.P) {
-            n = min(static_cast<uint32_t>(a.ccnt[i]), a.B);
-            if (n) {
-                quota = a.quota[i];
-                base = a.base[i];
-            }
-        }
+        const uint16_t* buf = cb_base(a, q, p);
+        // one round trip for most pieces: the counts, quota, offset and the first row together
+        const uint32_t n = min(static_cast<uint32_t>(a.ccnt[i]), a.B);
+        const uint32_t quota = a.quota[i];
+        uint32_t pos = a.base[i];
+        const uint32_t x0 = __ldcs(buf + cb_off(a, lane));
+        if (!n) continue;
         uint32_t* out = a.cands + q * a.m;
-        uint32_t todo = __ballot_sync(kFull, n != 0);
-        while (todo) {
-            const uint32_t src = __ffs(todo) - 1;
-            todo &= todo - 1;
-            const uint32_t pn = __shfl_sync(kFull, n, src), pq = __shfl_sync(kFull, quota, src);
-            uint32_t pos = __shfl_sync(kFull, base, src);
-            const uint16_t* buf = cb_base(a, q, p0 + src);
-            const uint32_t pbase = (p0 + src) * a.WP;
-            uint32_t ties = 0;
-            for (uint32_t e0 = 0; e0 < pn; e0 += 32) {
-                const uint32_t e = e0 + lane;
-                const uint32_t x = e < pn ? buf[cb_off(a, e)] : 0u;
-                const bool gt = e < pn && (x & 0x8000u);
-                const bool tie = e < pn && !(x & 0x8000u);
+        uint32_t ties = 0;
+        for (uint32_t e0 = 0; e0 < n; e0 += 128) {
+            uint32_t x[4];
+#pragma unroll
+            for (uint32_t u = 0; u < 4; ++u) {
+                const uint32_t e = e0 + 32 * u + lane;
+                x[u] = e0 + u == 0 ? x0 : e < n ? __ldcs(buf + cb_off(a, e)) : 0u;
+            }
+#pragma unroll
+            for (uint32_t u = 0; u < 4; ++u) {
+                if (e0 + 32 * u >= n) break;
+                const bool valid = e0 + 32 * u + lane < n;
+                const bool gt = valid && (x[u] & 0x8000u);
+                const bool tie = valid && !(x[u] & 0x8000u);
                 const uint32_t tb = __ballot_sync(kFull, tie);
-                const bool keep = gt || (tie && ties + __popc(tb & lt) < pq);
+                const bool keep = gt || (tie && ties + __popc(tb & lt) < quota);
                 const uint32_t kb = __ballot_sync(kFull, keep);
-                if (keep) __stcs(out + pos + __popc(kb & lt), pbase + (x & 0x7fffu));
+                if (keep) __stcs(out + pos + __popc(kb & lt), pbase + (x[u] & 0x7fffu));
                 pos += __popc(kb);
                 ties += __popc(tb);
             }
@@ -1452,7 +1465,7 @@ static cudaError_t launch_fused_t(const DenseArgs& a, size_t smem, cudaStream_t 
     int sms = 148, dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     DenseArgs b = a;
-    b.ppw = kFusedPPW;
+    b.ppw = std::max<uint32_t>(1u, kFusedPPW * kDensePiece / a.WP);  // about 8192 points per warp
     if (qblocks * ((a.P + kDW * b.ppw - 1) / (kDW * b.ppw)) < 4ull * sms) b.ppw = 1;
     const uint32_t per_cta = kDW * b.ppw;
     const dim3 grid(static_cast<unsigned>(qblocks), (a.P + per_cta - 1) / per_cta);
@@ -1521,11 +1534,13 @@ cudaError_t launch_dense_select_fused(const DenseArgs& args, cudaStream_t st, cu
         else e = sh.threads == 512 ? launch_fused_t<512, 1>(a, sh.smem, st) : launch_fused_t<1024, 1>(a, sh.smem, st);
     }
     if (e != cudaSuccess) return e;
-    // plan (+ fallback flags) from the two levels, compaction
+    // plan (+ fallback flags and the compaction work lists) from the two levels, compaction
+    e = cudaMemsetAsync(a.nclist, 0, 2 * sizeof(uint32_t), st);
+    if (e != cudaSuccess) return e;
     dense_plan_fused_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(a);
-    const dim3 cgrid((a.P + 255) / 256, static_cast<unsigned>(min_u64(a.nq, 65535)));
-    if (a.compact_mode == 2) dense_compact_kernel<<<cgrid, 256, 0, st>>>(a);  // warp per 32 pieces (A/B)
-    else dense_compact_thread_kernel<<<cgrid, 256, 0, st>>>(a);
+    const unsigned qrows = static_cast<unsigned>(min_u64(a.nq, 1024));  // rows walk the work lists
+    if (a.compact_mode != 2) dense_compact_thread_kernel<<<dim3((a.P + 255) / 256, qrows), 256, 0, st>>>(a);  // sparse
+    if (a.compact_mode != 1) dense_compact_kernel<<<dim3((a.P + 7) / 8, qrows), 256, 0, st>>>(a);  // dense supersets
     e = cudaMemsetAsync(args.nmap, 0, 4, st);
     if (e != cudaSuccess) return e;
     dense_flag_list_kernel<<<static_cast<unsigned>((a.nq + 255) / 256), 256, 0, st>>>(args);

@@ -106,7 +106,10 @@ struct DenseArgs {
     uint32_t nc;                  // uint4 code vectors per point: 1 (N_s <= 8, default) or 2 (N_s <= 16)
     uint32_t* pcut;               // single pass: nq, tie entries are stored only in pieces < pcut[q]
     uint32_t no_cut;              // tests: store every tie (pcut = P)
-    uint32_t compact_mode;        // Tuning::dense_compact: 0/1 thread per piece, 2 warp per 32 pieces
+    uint32_t* clist;              // single pass: nq x 2 — unflagged queries with dense supersets from the front,
+                                  // sparse ones from nq on (compaction work lists, any order)
+    uint32_t* nclist;             // their two counts
+    uint32_t compact_mode;        // Tuning::dense_compact: 0 by density, 1 thread per piece, 2 warp per (query, piece)
     uint32_t pair;                // half mode: the fused pass as 2-CTA clusters with 32-bit masks of 4 subspaces each
     float cut_scale;              // tie cut = P * need/ties * cut_scale + cut_pad pieces (0: defaults 1.25, 8)
     uint32_t cut_pad;
@@ -153,7 +156,8 @@ cudaError_t launch_dense_hist(const DenseArgs& a, cudaStream_t st);
 cudaError_t launch_dense_hist_rows(const DenseArgs& a, uint32_t* out, cudaStream_t st);
 cudaError_t launch_dense_emit(const DenseArgs& a, cudaStream_t st);
 constexpr uint32_t kDensePiece = 2048;  // points per piece (one warp)
-constexpr uint32_t kDenseBuf = 96;      // single-pass candidate buffer entries per (piece, query)
+constexpr uint32_t kDenseBuf = 96;      // single-pass candidate buffer entries per 2048 points of a (piece, query)
+constexpr uint32_t kFusedPiece = 8192;  // points per piece of the single-pass select (half-width mode: kDensePiece)
 
 // ------------------------------------------------------------------ rerank
 // Exact fp64 re-rank of the candidate rows (query.cpp:159-197) with a

@@ -25,7 +25,10 @@ struct Tuning {
     uint32_t dense_buf = 0;      // SUCO_DENSE_BUF: single-pass buffer entries per (piece, query); 0 = by memory
     bool dense_nocut = false;    // SUCO_DENSE_NOCUT=1: store every tie (tests)
     uint32_t dense_words = 0;    // SUCO_DENSE_WORDS: mask words per slot (0 auto, 1, 2)
-    uint32_t dense_compact = 0;  // SUCO_DENSE_COMPACT: 0/1 thread per piece (default), 2 warp per 32 pieces
+    uint32_t dense_compact = 0;  // SUCO_DENSE_COMPACT: 0 by superset density (default), 1 thread per piece with a
+                                 // shared staging copy of the block's output run, 2 warp per (query, piece)
+    uint32_t dense_piece = 0;    // SUCO_DENSE_PIECE: points per piece of the single-pass select (0 = 8192; a
+                                 // multiple of 2048 up to 32768; the half-width mode keeps 2048)
     bool dense_stats = false;    // SUCO_DENSE_STATS=1: print the single-pass fallback rate (diagnostics)
     bool rerank_stats = false;   // SUCO_RERANK_STATS=1: print the int8 screen's exact re-rank counts (diagnostics)
     uint32_t tiles = 1;          // SUCO_TILES: minimum pipeline tiles per batch (tests: slot reuse)
