@@ -208,9 +208,14 @@ void upload_data(suco_gpu_index* x, const float* data, uint64_t n, uint32_t d) {
     x->qpad = x->qrec = 0;
     if (!x->dpad && x->tune.q8 && d % 4 == 0 && d <= 128) {
         x->qpad = (d + 15) / 16 * 16;
-        x->qrec = (x->qpad + 16 + 63) / 64 * 64;  // whole 64-byte DRAM granules per record
+        // Past the prefix: the prefix-bound layout (meta0 and the prefix dims in the first qsplit
+        // bytes, the rest and meta1 after them: pack_q8_kernel); whole 64-byte granules per record
+        const uint32_t nw = x->qpad / 16, pre = x->tune.q8_prefix;
+        x->qpre = nw > pre ? pre : 0u;
+        x->qsplit = x->qpre ? (16 + 16 * x->qpre + 31) / 32 * 32 : 0u;
+        x->qrec = x->qpre ? (x->qsplit + (nw - x->qpre + 1) * 16 + 63) / 64 * 64 : (x->qpad + 16 + 63) / 64 * 64;
         x->q8.reserve(n * x->qrec);
-        CUDA_TRY(launch_pack_q8(x->data.p, n, d, x->qpad, x->qrec, x->q8.p, x->own));
+        CUDA_TRY(launch_pack_q8(x->data.p, n, d, x->qpad, x->qrec, x->qpre, x->qsplit, x->q8.p, x->own));
         CUDA_TRY(cudaStreamSynchronize(x->own));
     }
 }
@@ -463,6 +468,8 @@ void rerank_args(const suco_gpu_index* x, RerankArgs& ra) {
     ra.q8 = x->qpad ? x->q8.p : nullptr;
     ra.qpad = x->qpad;
     ra.qrec = x->qrec;
+    ra.qpre = x->qpre;
+    ra.qsplit = x->qsplit;
     ra.u8_regs = x->tune.rerank_u8_regs;
     ra.no_tma = !x->tune.rerank_tma;
     ra.pipe = x->tune.rerank_pipe == 2 ? 0 : x->tune.rerank_pipe == 1 ? 1 : 2;
@@ -532,6 +539,11 @@ FbLists stage_select(const suco_gpu_index* x, suco_gpu_query_ctx* c, suco_gpu_qu
                 da.WP = tn.dense_piece ? tn.dense_piece : fused_piece(h.n, nt, h.layout.ns > 8 ? 2u : 1u);
                 da.P = static_cast<uint32_t>((h.n + da.WP - 1) / da.WP);
             }
+            // two output offsets per (query, piece): score > T entries fill the front of the query's
+            // candidate list, the quota ties the back (the re-rank meets the likely nearest first)
+            sl.dbase.reserve(2 * nt * da.P);
+            da.base = sl.dbase.p;
+            da.base2 = sl.dbase.p + nt * da.P;
             // the sampled histograms (every pstride-th piece) predict the threshold: about 16 sampled
             // pieces when that is enough (cfg2: 489 pieces -> every 30th), every 64th piece at most
             // for large corpora (measured: cfg2 2.31M -> 2.36M q/s, cfg4 167K -> 174K; fewer samples
@@ -664,8 +676,8 @@ void stage_rerank(const suco_gpu_index* x, suco_gpu_query_ctx* c, suco_gpu_query
     }
     DevBuf<unsigned long long> stats;
     if (x->tune.rerank_stats && ra.q8) {
-        stats.reserve(2);
-        CUDA_TRY(cudaMemsetAsync(stats.p, 0, 16, st));
+        stats.reserve(3);
+        CUDA_TRY(cudaMemsetAsync(stats.p, 0, 24, st));
         ra.screen_stats = stats.p;
     }
     if (ev) CUDA_TRY(cudaEventRecord(ev[0], st));
@@ -673,11 +685,13 @@ void stage_rerank(const suco_gpu_index* x, suco_gpu_query_ctx* c, suco_gpu_query
     c->launches += (ra.data8 ? 2 : 1) + (k > 32 ? 1 : 0);  // u8 + fp32/fp64 kernels, generic top-k
     if (ev) CUDA_TRY(cudaEventRecord(ev[1], st));
     if (ra.screen_stats) {  // diagnostics
-        unsigned long long h[2] = {0, 0};
-        CUDA_TRY(cudaMemcpyAsync(h, stats.p, 16, cudaMemcpyDeviceToHost, st));
+        unsigned long long h[3] = {0, 0, 0};
+        CUDA_TRY(cudaMemcpyAsync(h, stats.p, 24, cudaMemcpyDeviceToHost, st));
         CUDA_TRY(cudaStreamSynchronize(st));
-        std::fprintf(stderr, "[suco] int8 screen: %llu queries, %.1f exact re-ranks per query, %llu re-ranked in full\n",
-                     static_cast<unsigned long long>(nt), double(h[0]) / double(nt), h[1]);
+        std::fprintf(stderr,
+                     "[suco] int8 screen: %llu queries, %.1f exact re-ranks per query, %llu re-ranked in full, %.1f "
+                     "rows per query past the prefix bound\n",
+                     static_cast<unsigned long long>(nt), double(h[0]) / double(nt), h[1], double(h[2]) / double(nt));
     }
 }
 
@@ -690,7 +704,7 @@ uint64_t per_query_bytes(const suco_gpu_index* x, uint64_t m, uint32_t k) {
     if (x->dense) {
         // hist (16 B x nc) + quota/base + two-level counts + buffer counts per piece, kDenseBuf
         // buffer entries per piece, sampled histograms, flags
-        per += P * (16 * nc + 8 + 4 + 2 + kDenseBuf * 2) + (P / 16 + 1) * 16 * nc + 20;
+        per += P * (16 * nc + 12 + 4 + 2 + kDenseBuf * 2) + (P / 16 + 1) * 16 * nc + 20;
     }
     return per;
 }

@@ -176,6 +176,7 @@ struct suco_gpu_index {
     suco_gpu::DevBuf<uint8_t> data8;   // u8 copy of the rows when they are integers in [0, 255] (rerank u8 path)
     suco_gpu::DevBuf<int8_t> q8;       // int8 screen records of float rows (n x qrec; rerank_q8_kernel)
     uint32_t qpad = 0, qrec = 0;       // int8 bytes / record stride (0: no int8 copy)
+    uint32_t qpre = 0, qsplit = 0;     // prefix-bound record layout (pack_q8_kernel)
     suco_gpu::DevBuf<uint16_t> codes;  // n x 8: s*K + cell of every point (dense select, N_s <= 8)
     bool dense = false;         // select stage = dense bit-sliced 32-query blocks (dense.cu)
     bool dense_half = false;    // ... in the half-width mode (16-query blocks, u16 masks; large N_s*K)

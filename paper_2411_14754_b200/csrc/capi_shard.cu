@@ -241,6 +241,8 @@ int suco_gpu_make_shard(const suco_gpu_index* full, uint32_t shard, uint32_t num
             x->dpad = full->dpad;
             x->qpad = full->qpad;
             x->qrec = full->qrec;
+            x->qpre = full->qpre;
+            x->qsplit = full->qsplit;
             // rows of the owned blocks, back to back (and their u8 / int8 copies)
             x->data.reserve(n_local * d);
             if (x->dpad) x->data8.reserve(n_local * x->dpad);

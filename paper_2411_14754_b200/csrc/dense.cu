@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(256) dense_plan_fused_kernel(DenseArgs a) {
     const uint32_t L = a.L[q] & 0xffu;
     bool ok = L >= 1 && geL >= a.m && geL1 < a.m;
     const uint64_t need = a.m - geL1;
-    uint64_t ties_run = 0, out_run = 0;
+    uint64_t ties_run = 0, gt_run = 0, tie_run = 0;
     for (uint32_t p0 = 0; p0 < a.P; p0 += 32) {
         const uint32_t p = p0 + lane;
         uint32_t ties = 0, gt = 0;
@@ -445,21 +445,27 @@ __global__ void __launch_bounds__(256) dense_plan_fused_kernel(DenseArgs a) {
         const uint64_t before = ties_run + tx - ties;
         const uint32_t quota = before >= need ? 0u : static_cast<uint32_t>(min_u64(ties, need - before));
         const uint32_t take = gt + quota;
-        uint32_t ox = take;
+        // offsets: score > T entries from 0 in piece order, then the ties from #(score > T) = m - need
+        uint32_t gx = gt, qx = quota;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(kFull, ox, o);
-            if (lane >= static_cast<uint32_t>(o)) ox += y;
+            const uint32_t y = __shfl_up_sync(kFull, gx, o), z = __shfl_up_sync(kFull, qx, o);
+            if (lane >= static_cast<uint32_t>(o)) {
+                gx += y;
+                qx += z;
+            }
         }
-        const uint32_t osum = __shfl_sync(kFull, ox, 31);
+        const uint32_t gsum = __shfl_sync(kFull, gx, 31), qsum = __shfl_sync(kFull, qx, 31);
         if (p < a.P) {
             a.quota[q * a.P + p] = quota;
-            a.base[q * a.P + p] = static_cast<uint32_t>(out_run + ox - take);
+            a.base[q * a.P + p] = static_cast<uint32_t>(gt_run + gx - gt);
+            a.base2[q * a.P + p] = static_cast<uint32_t>(geL1 + tie_run + qx - quota);
             if (take && a.ccnt[q * a.P + p] > a.B) ok = false;  // a contributing buffer overflowed
             if (quota && a.pcut && p >= a.pcut[q]) ok = false;   // ties needed past the tie cut
         }
         ties_run += tsum;
-        out_run += osum;
+        gt_run += gsum;
+        tie_run += qsum;
     }
     ok = __all_sync(kFull, ok);
     if (lane == 0) {
@@ -722,38 +728,40 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs 
 }
 
 // K4: thread per (query, piece), T == L: the piece's buffer holds its score >= T points in id
-// order; keep every score > T and the first quota ties. A block takes 256 consecutive pieces of
-// one query, whose outputs are one contiguous run of the query's candidates (pieces in order): each
-// thread loads its whole buffer (independent 16-byte loads), places its kept ids in a shared
-// staging copy of the run, and the block writes the run with coalesced stores. Runs longer than
-// the staging area write their tail directly.
-constexpr uint32_t kCompactStage = 8192;  // staged candidate ids per block (32 KB)
+// order; keep every score > T entry and the first quota ties. A block takes 256 consecutive pieces
+// of one query, whose outputs are two contiguous runs of the query's candidates (its score > T
+// entries, its ties; pieces in order): each thread loads its whole buffer (independent 16-byte
+// loads), places its kept ids in shared staging copies of the two runs, and the block writes the
+// runs with coalesced stores. Runs longer than a staging half write their tail directly.
+constexpr uint32_t kCompactStage = 4096;  // staged candidate ids per run (2 x 16 KB)
 __global__ void __launch_bounds__(256) dense_compact_thread_kernel(DenseArgs a) {
-    __shared__ uint32_t stage[kCompactStage];
-    __shared__ uint32_t run_lo, run_hi;
+    __shared__ uint32_t stage[2][kCompactStage];
+    __shared__ uint32_t run_lo[2], run_hi[2];
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t pbase = p * a.WP;
     const uint32_t nlist = a.nclist[1];
     for (uint32_t j = blockIdx.y; j < nlist; j += gridDim.y) {
         const uint64_t q = a.clist[a.nq + j];  // an unflagged query with a sparse superset
-        if (threadIdx.x == 0) {
-            run_lo = 0xffffffffu;
-            run_hi = 0;
+        if (threadIdx.x < 2) {
+            run_lo[threadIdx.x] = 0xffffffffu;
+            run_hi[threadIdx.x] = 0;
         }
         __syncthreads();
         const uint64_t i = q * a.P + p;
         const uint32_t n = p < a.P ? min(static_cast<uint32_t>(a.ccnt[i]), a.B) : 0u;
-        uint32_t quota = 0, pos = 0;
+        uint32_t quota = 0, pos = 0, pos2 = 0;
         if (n) {
             quota = a.quota[i];
             pos = a.base[i];
-            atomicMin(&run_lo, pos);
+            pos2 = a.base2[i];
+            atomicMin(&run_lo[0], pos);
+            atomicMin(&run_lo[1], pos2);
         }
         __syncthreads();
-        const uint32_t lo = run_lo;
+        const uint32_t lo = run_lo[0], lo2 = run_lo[1];
         uint32_t* out = a.cands + q * a.m;
         const uint4* buf = reinterpret_cast<const uint4*>(cb_base(a, q, p < a.P ? p : 0u));
-        uint32_t at = pos - lo;  // staging offset of this thread's next kept id
+        uint32_t at = pos - lo, at2 = pos2 - lo2;  // staging offsets of this thread's next kept ids
         for (uint32_t e0 = 0; e0 < n; e0 += 64) {
             uint4 v[8];
 #pragma unroll
@@ -767,21 +775,29 @@ __global__ void __launch_bounds__(256) dense_compact_thread_kernel(DenseArgs a) 
                     const bool valid = e0 + 8 * u + h < n;
                     const bool gt = (x & 0x8000u) != 0;
                     const bool tie = valid && !gt && quota != 0;  // the first ties in id order
-                    if ((valid && gt) || tie) {
-                        const uint32_t id = pbase + (x & 0x7fffu);
-                        if (at < kCompactStage) stage[at] = id;
+                    const uint32_t id = pbase + (x & 0x7fffu);
+                    if (valid && gt) {
+                        if (at < kCompactStage) stage[0][at] = id;
                         else __stcs(out + lo + at, id);
                         ++at;
+                    } else if (tie) {
+                        if (at2 < kCompactStage) stage[1][at2] = id;
+                        else __stcs(out + lo2 + at2, id);
+                        ++at2;
                     }
                     quota -= tie ? 1u : 0u;
                 }
             }
         }
-        if (n) atomicMax(&run_hi, at);
+        if (n) {
+            atomicMax(&run_hi[0], at);
+            atomicMax(&run_hi[1], at2);
+        }
         __syncthreads();
-        const uint32_t len = min(run_hi, kCompactStage);
-        for (uint32_t j = threadIdx.x; j < len; j += blockDim.x) __stcs(out + lo + j, stage[j]);
-        __syncthreads();  // the staging area and run bounds are reused by the next query
+        const uint32_t len = min(run_hi[0], kCompactStage), len2 = min(run_hi[1], kCompactStage);
+        for (uint32_t t = threadIdx.x; t < len; t += blockDim.x) __stcs(out + lo + t, stage[0][t]);
+        for (uint32_t t = threadIdx.x; t < len2; t += blockDim.x) __stcs(out + lo2 + t, stage[1][t]);
+        __syncthreads();  // the staging areas and run bounds are reused by the next query
     }
 }
 
@@ -802,7 +818,7 @@ __global__ void __launch_bounds__(256) dense_compact_kernel(DenseArgs a) {
         // one round trip for most pieces: the counts, quota, offset and the first row together
         const uint32_t n = min(static_cast<uint32_t>(a.ccnt[i]), a.B);
         const uint32_t quota = a.quota[i];
-        uint32_t pos = a.base[i];
+        uint32_t pos = a.base[i], pos2 = a.base2[i];  // score > T entries, ties
         const uint32_t x0 = __ldcs(buf + cb_off(a, lane));
         if (!n) continue;
         uint32_t* out = a.cands + q * a.m;
@@ -821,10 +837,12 @@ __global__ void __launch_bounds__(256) dense_compact_kernel(DenseArgs a) {
                 const bool gt = valid && (x[u] & 0x8000u);
                 const bool tie = valid && !(x[u] & 0x8000u);
                 const uint32_t tb = __ballot_sync(kFull, tie);
-                const bool keep = gt || (tie && ties + __popc(tb & lt) < quota);
-                const uint32_t kb = __ballot_sync(kFull, keep);
-                if (keep) __stcs(out + pos + __popc(kb & lt), pbase + (x[u] & 0x7fffu));
-                pos += __popc(kb);
+                const bool keep = tie && ties + __popc(tb & lt) < quota;
+                const uint32_t gb = __ballot_sync(kFull, gt), kb = __ballot_sync(kFull, keep);
+                if (gt) __stcs(out + pos + __popc(gb & lt), pbase + (x[u] & 0x7fffu));
+                if (keep) __stcs(out + pos2 + __popc(kb & lt), pbase + (x[u] & 0x7fffu));
+                pos += __popc(gb);
+                pos2 += __popc(kb);
                 ties += __popc(tb);
             }
         }

@@ -86,6 +86,7 @@ struct DenseArgs {
     uint32_t* T;               // nq
     uint32_t* quota;           // nq x P
     uint32_t* base;            // nq x P
+    uint32_t* base2;           // single pass: nq x P, the offsets of the pieces' ties (base: their score > T entries)
     uint32_t* cands;           // nq x m
     // single-pass (fused) select: a speculative lower bound L on T per query, a superset slot of
     // C entries (in-piece offset << 4 | score, id order) per (query, piece), and a fallback flag
@@ -190,6 +191,8 @@ struct RerankArgs {
                             // bounds), padded to a multiple of 64 bytes (the DRAM access granule)
     uint32_t qpad;          // int8 bytes of a record (d rounded up to 16)
     uint32_t qrec;          // record stride (qpad + 16 rounded up to 64)
+    uint32_t qpre;          // prefix-bound layout: prefix words (16 dims each; 0 = plain records)
+    uint32_t qsplit;        // byte offset of the rest of the row (the second read of rerank_q8p_kernel)
     bool no_tma;            // !Tuning::rerank_tma: 16-byte cp.async row gathers instead of per-row TMA bulk copies
     unsigned long long* screen_stats;  // optional diagnostics: [0] += exact re-ranks, [1] += queries re-ranked in full
     bool u8_regs;           // Tuning::rerank_u8_regs: the register byte kernel instead of the smem ring
@@ -230,7 +233,8 @@ cudaError_t launch_check_finite(const float* data, uint64_t count, int* flag, cu
 cudaError_t launch_int_stats(const float* data, uint64_t count, unsigned int* out3, cudaStream_t st);
 cudaError_t launch_pack_u8(const float* data, uint64_t n, uint32_t d, uint32_t dpad, uint8_t* out, cudaStream_t st);
 // int8 screen records of float rows: n x qrec bytes (see RerankArgs::q8)
-cudaError_t launch_pack_q8(const float* data, uint64_t n, uint32_t d, uint32_t qpad, uint32_t qrec, int8_t* out,
+cudaError_t launch_pack_q8(const float* data, uint64_t n, uint32_t d, uint32_t qpad, uint32_t qrec, uint32_t qpre,
+                           uint32_t qsplit, int8_t* out,
                            cudaStream_t st);
 
 // SC-Linear (sclinear.cu): exact per-subspace distances, top-c per (query, subspace) by a radix

@@ -1016,6 +1016,363 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_q8_kernel(RerankArgs a, ui
     }
 }
 
+// ------------------------------------------- int8 screen with a prefix bound (NW >= 4)
+// Record (qrec bytes, a multiple of 64): [meta0][dims 0 .. 16 kQ8P) in the first qsplit bytes (32
+// for one prefix word, 64 for three), then [dims 16 kQ8P .. 16 NW)[meta1]; meta0 = (s, |a_S|^2
+// (u32 bits), ||e_x,S|| up, 0), meta1 = (|x|^2, ||s a|| up, ||e_x|| up, s), S = the prefix dims.
+// Stage 1 reads the first qsplit bytes of every candidate. The prefix alone bounds the distance from below:
+//     D >= sum_{i in S} (x_i - q_i)^2 >= (||s a_S - t b_S|| - ||e_x,S|| - ||e_q,S||)^2,
+//     ||s a_S - t b_S||^2 = s^2 |a_S|^2 + t^2 |b_S|^2 - 2 s t (a_S . b_S),   a_S . b_S exact (IDP.4A)
+// (at cfg4 the first 24 of 96 dims rule out about 98 % of the candidates against the final k-th
+// distance, tools/partial_bound.py; the compaction puts score > T candidates first, so tau is
+// close to final early). Rows still under tau queue (id, a_S . b_S); 32 queued rows
+// make one stage-2 batch, whose rest-of-row words and meta1 give rerank_q8_kernel's full
+// certified bounds (tau, exact survivors). A batch is issued in the same cp.async group as the
+// next prefix step and consumed one step later, so the copies never drain; tau is shared across
+// the CTA's warps (the minimum of their k-th upper bounds bounds the query's k-th distance).
+constexpr uint32_t kQ8QCap = 64;  // queued rows per warp (at most 63 by construction)
+
+template <uint32_t kQ8P, uint32_t NR>  // prefix words (16 dims each), rest words: NW = kQ8P + NR
+__global__ void __launch_bounds__(kThreads, 2) rerank_q8p_kernel(RerankArgs a, uint32_t stride) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr uint32_t NW = kQ8P + NR;
+    constexpr uint32_t suA = (kQ8P + 1) | 1u;  // meta0 + prefix words, odd 16-byte stride
+    constexpr uint32_t suB = (NR + 1) | 1u;  // NR words + meta1, odd stride
+    double* qd = reinterpret_cast<double*>(smem);  // d
+    const uint32_t ringA = kQ8Stages * 32 * suA, ringB = 2 * 32 * suB;  // uint4 units
+    const uint32_t per_warp = max((ringA + ringB) * 16, kRows * stride * 4);
+    unsigned char* wbase = smem + ((a.d * 8 + 15) / 16) * 16;
+    __shared__ uint32_t qpack[32];
+    __shared__ uint32_t sid[kWarps][kQ8Cap];
+    __shared__ float slo[kWarps][kQ8Cap];
+    __shared__ uint32_t qqid[kWarps][kQ8QCap];
+    __shared__ int qqI[kWarps][kQ8QCap];
+    __shared__ double md[kWarps * 32];
+    __shared__ uint32_t mi[kWarps * 32];
+    __shared__ double qpar[6];  // t, |q|^2, ||t b|| (up), ||e_q|| (up), t^2 |b_S|^2, ||e_q,S|| (up)
+    __shared__ double tau_cta;
+    __shared__ unsigned long long tau_sh;  // CTA-wide min of the warps' k-th upper bounds (bits of a double >= 0)
+    __shared__ int ovf, qok;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    uint64_t q;
+    if (!rerank_query(a, q)) return;
+    const float* query = a.queries + q * a.d;
+    for (uint32_t i = tid; i < a.d; i += kThreads) qd[i] = static_cast<double>(query[i]);
+    if (warp == 0) {  // quantise the query (d <= 128: lane owns dims 4 lane .. 4 lane + 3)
+        float v[4], mx = 0.f;
+#pragma unroll
+        for (uint32_t j = 0; j < 4; ++j) {
+            const uint32_t i = 4 * lane + j;
+            v[j] = i < a.d ? query[i] : 0.f;
+            mx = fmaxf(mx, fabsf(v[j]));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
+        const float t = mx / 127.f;
+        double e2 = 0.0, b2 = 0.0, n2 = 0.0;
+        uint32_t packed = 0;
+#pragma unroll
+        for (uint32_t j = 0; j < 4; ++j) {
+            const float bq = t > 0.f ? fminf(127.f, fmaxf(-127.f, rintf(v[j] / t))) : 0.f;
+            const double e = static_cast<double>(v[j]) - static_cast<double>(t) * static_cast<double>(bq);
+            e2 += e * e;
+            b2 += static_cast<double>(bq) * static_cast<double>(bq);
+            n2 += static_cast<double>(v[j]) * static_cast<double>(v[j]);
+            packed |= (static_cast<uint32_t>(static_cast<int>(bq)) & 0xffu) << (8 * j);
+        }
+        const bool pre = lane < 4 * kQ8P;  // this lane's dims are in the prefix
+        double e2s = pre ? e2 : 0.0, b2s = pre ? b2 : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            e2 += __shfl_xor_sync(kFull, e2, o);
+            b2 += __shfl_xor_sync(kFull, b2, o);
+            n2 += __shfl_xor_sync(kFull, n2, o);
+            e2s += __shfl_xor_sync(kFull, e2s, o);
+            b2s += __shfl_xor_sync(kFull, b2s, o);
+        }
+        qpack[lane] = packed;
+        if (lane == 0) {
+            qpar[0] = static_cast<double>(t);
+            qpar[1] = n2;
+            qpar[2] = static_cast<double>(t) * sqrt(b2) * (1.0 + 1e-12);
+            qpar[3] = sqrt(e2) * (1.0 + 1e-12);
+            qpar[4] = static_cast<double>(t) * static_cast<double>(t) * b2s;  // b2s: an exact integer
+            qpar[5] = sqrt(e2s) * (1.0 + 1e-12);
+            qok = isfinite(n2) && isfinite(e2) && isfinite(qpar[2]);
+            ovf = 0;
+            tau_sh = 0x7ff0000000000000ull;  // +inf
+        }
+    }
+    __syncthreads();
+    int qv[NW][4];
+#pragma unroll
+    for (uint32_t w = 0; w < NW; ++w) {
+#pragma unroll
+        for (uint32_t j = 0; j < 4; ++j) qv[w][j] = static_cast<int>(qpack[4 * w + j]);
+    }
+    const double qt = qpar[0], n2q = qpar[1], Bq = qpar[2], rq = qpar[3], tb2S = qpar[4], eqS = qpar[5];
+    const bool qfin = qok != 0;
+    uint4* ra = reinterpret_cast<uint4*>(wbase + warp * per_warp);
+    uint4* rb = ra + ringA;
+    uint32_t* qid = qqid[warp];
+    int* qI = qqI[warp];
+    const uint32_t* cands = a.cands + q * a.m;
+    const uint64_t mq = a.counts ? a.counts[q] : a.m;
+    const uint64_t first = uint64_t(warp) * 32;
+    const uint64_t steps = mq > first ? (mq - first + 32 * kWarps - 1) / (32 * kWarps) : 0;
+    auto sbase = [&](uint64_t g) { return first + g * 32 * kWarps; };
+    auto load_id = [&](uint64_t g) -> uint32_t {
+        const uint64_t i = sbase(g) + lane;
+        if (g >= steps || i >= mq) return 0u;
+        return a.identity ? static_cast<uint32_t>(i) : __ldcs(cands + i);
+    };
+    uint32_t id0 = load_id(0), id1 = load_id(1);
+    auto issue_a = [&](uint64_t g) {  // granule 0 of the step's 32 rows
+        const uint32_t myid = (g & 1u) ? id1 : id0;
+        uint4* st = ra + static_cast<uint32_t>(g % kQ8Stages) * 32 * suA;
+        const uint64_t b = sbase(g);
+#pragma unroll
+        for (uint32_t t = lane; t < 32 * (kQ8P + 1); t += 32) {
+            const uint32_t row = t / (kQ8P + 1), col = t % (kQ8P + 1);
+            const uint32_t id = __shfl_sync(kFull, myid, row);
+            if (b + row < mq) cp_async16(st + row * suA + col, a.q8 + uint64_t(id) * a.qrec + 16u * col);
+        }
+        if (g & 1u) id1 = load_id(g + 2);
+        else id0 = load_id(g + 2);
+        return myid;
+    };
+    auto issue_b = [&](uint32_t slot, uint32_t cnt, uint32_t bid) {  // the rest of the batch's rows
+        uint4* st = rb + slot * 32 * suB;
+#pragma unroll
+        for (uint32_t t = lane; t < 32 * (NR + 1); t += 32) {
+            const uint32_t row = t / (NR + 1), col = t % (NR + 1);
+            const uint32_t id = __shfl_sync(kFull, bid, row);
+            if (row < cnt) cp_async16(st + row * suB + col, a.q8 + uint64_t(id) * a.qrec + a.qsplit + 16u * col);
+        }
+    };
+    uint32_t rowid0 = 0, rowid1 = 0;
+    if (steps) rowid0 = issue_a(0);
+    cp_async_commit();
+    double sl = kInf;  // this warp's k smallest upper bounds (lane i = entry i)
+    uint32_t nsurv = 0, qn = 0;
+    bool overflow = false;
+    uint32_t fcnt = 0, fid = 0, fslot = 0, nslot = 0;  // the batch in flight (issued last iteration)
+    int fI = 0;
+    auto tau_now = [&]() {
+        const double own = __shfl_sync(kFull, sl, a.k - 1);
+        const double shared = __longlong_as_double(static_cast<long long>(*reinterpret_cast<volatile unsigned long long*>(&tau_sh)));
+        return fmin(own, shared);
+    };
+    for (uint64_t g = 0; g < steps || fcnt || qn; ++g) {
+        if (g + 1 < steps) {
+            const uint32_t v = issue_a(g + 1);
+            if (g & 1u) rowid0 = v;
+            else rowid1 = v;
+        }
+        // a new batch: 32 queued rows, or whatever is left once the prefix steps are done
+        uint32_t ncnt = 0, nid = 0;
+        int nI = 0;
+        if (qn >= 32 || (g >= steps && qn)) {
+            ncnt = min(qn, 32u);
+            if (lane < ncnt) {
+                nid = qid[lane];
+                nI = qI[lane];
+            }
+            const uint32_t r0 = 32 + lane < qn ? qid[32 + lane] : 0u;  // the rest moves to the front
+            const int r1 = 32 + lane < qn ? qI[32 + lane] : 0;
+            __syncwarp();
+            if (32 + lane < qn) {
+                qid[lane] = r0;
+                qI[lane] = r1;
+            }
+            __syncwarp();
+            qn -= ncnt;
+            issue_b(nslot, ncnt, nid);
+        }
+        cp_async_commit();
+        cp_async_wait<1>();  // the prefix step g and the batch issued last iteration have landed
+        __syncwarp();
+        if (fcnt) {  // stage 2: full certified bounds of the batch
+            if (a.screen_stats && lane == 0) atomicAdd(a.screen_stats + 2, static_cast<unsigned long long>(fcnt));
+            const uint4* row = rb + fslot * 32 * suB + lane * suB;
+            int c0 = fI, c1 = 0, c2 = 0, c3 = 0;
+#pragma unroll
+            for (uint32_t w = 0; w < NR; ++w) {
+                const uint4 x = row[w];
+                c0 = __dp4a(static_cast<int>(x.x), qv[kQ8P + w][0], c0);
+                c1 = __dp4a(static_cast<int>(x.y), qv[kQ8P + w][1], c1);
+                c2 = __dp4a(static_cast<int>(x.z), qv[kQ8P + w][2], c2);
+                c3 = __dp4a(static_cast<int>(x.w), qv[kQ8P + w][3], c3);
+            }
+            const uint4 mw = row[NR];
+            const int I = (c0 + c1) + (c2 + c3);
+            const float rn2 = __uint_as_float(mw.x), rA = __uint_as_float(mw.y), rR = __uint_as_float(mw.z);
+            const float rs = __uint_as_float(mw.w);
+            const bool valid = lane < fcnt;
+            double lo = 0.0, up = kInf;
+            if (qfin && rs >= 0.f) {
+                const double dot = static_cast<double>(rs) * qt * static_cast<double>(I);
+                const double approx = static_cast<double>(rn2) + n2q - 2.0 * dot;
+                const double err = 2.0 * (static_cast<double>(rA) * rq + Bq * static_cast<double>(rR) +
+                                          static_cast<double>(rR) * rq);
+                const double slack = 9.5367431640625e-07 * (static_cast<double>(rn2) + n2q + 2.0 * fabs(dot)) + 1e-300;
+                lo = approx - err - slack;
+                up = approx + err + slack;
+            }
+            const double tau0 = __shfl_sync(kFull, sl, a.k - 1);
+            uint32_t bal = __ballot_sync(kFull, valid && up < tau0);
+            if (bal) {
+                while (bal) {
+                    const uint32_t src = __ffs(bal) - 1;
+                    bal &= bal - 1;
+                    const double v = __shfl_sync(kFull, up, src);
+                    if (v < __shfl_sync(kFull, sl, a.k - 1)) list_insert_val(v, sl, a.k, lane);
+                }
+                const double own = __shfl_sync(kFull, sl, a.k - 1);
+                if (lane == 0 && own < kInf && own >= 0.0)
+                    atomicMin(&tau_sh, static_cast<unsigned long long>(__double_as_longlong(own)));
+            }
+            const double tau = tau_now();
+            const uint32_t pass = __ballot_sync(kFull, valid && lo <= tau);
+            if (pass && !overflow) {
+                const uint32_t cnt = __popc(pass);
+                if (nsurv + cnt > kQ8Cap) {  // drop buffered rows the tighter tau now excludes
+                    uint32_t kept = 0;
+                    for (uint32_t t0 = 0; t0 < nsurv; t0 += 32) {
+                        const uint32_t t = t0 + lane;
+                        const bool in = t < nsurv;
+                        const uint32_t idv = in ? sid[warp][t] : 0u;
+                        const float lv = in ? slo[warp][t] : 0.f;
+                        const bool keep = in && static_cast<double>(lv) <= tau;
+                        const uint32_t kb = __ballot_sync(kFull, keep);
+                        __syncwarp();
+                        if (keep) {
+                            const uint32_t p = kept + __popc(kb & ((1u << lane) - 1u));
+                            sid[warp][p] = idv;
+                            slo[warp][p] = lv;
+                        }
+                        kept += __popc(kb);
+                        __syncwarp();
+                    }
+                    nsurv = kept;
+                }
+                if (nsurv + cnt > kQ8Cap) {
+                    overflow = true;
+                } else {
+                    if ((pass >> lane) & 1u) {
+                        const uint32_t p = nsurv + __popc(pass & ((1u << lane) - 1u));
+                        sid[warp][p] = fid;
+                        slo[warp][p] = __double2float_rd(lo);
+                    }
+                    nsurv += cnt;
+                }
+                __syncwarp();
+            }
+        }
+        fcnt = ncnt;
+        fid = nid;
+        fI = nI;
+        fslot = nslot;
+        nslot ^= 1u;
+        if (g < steps) {  // stage 1: the prefix bound of step g's rows
+            const uint32_t myid = (g & 1u) ? rowid1 : rowid0;
+            const uint4* row = ra + static_cast<uint32_t>(g % kQ8Stages) * 32 * suA + lane * suA;
+            const uint4 m0 = row[0];
+            int c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+#pragma unroll
+            for (uint32_t w = 0; w < kQ8P; ++w) {
+                const uint4 x = row[1 + w];
+                c0 = __dp4a(static_cast<int>(x.x), qv[w][0], c0);
+                c1 = __dp4a(static_cast<int>(x.y), qv[w][1], c1);
+                c2 = __dp4a(static_cast<int>(x.z), qv[w][2], c2);
+                c3 = __dp4a(static_cast<int>(x.w), qv[w][3], c3);
+            }
+            __syncwarp();  // the slot is refilled by the next issue
+            const int IS = (c0 + c1) + (c2 + c3);
+            const float rs = __uint_as_float(m0.x), eS = __uint_as_float(m0.z);
+            const bool valid = sbase(g) + lane < mq;
+            double lb = 0.0;
+            if (qfin && rs >= 0.f) {
+                const double s = static_cast<double>(rs);
+                const double sa = s * s * static_cast<double>(m0.y);  // |a_S|^2: an exact integer
+                const double cr = 2.0 * s * qt * static_cast<double>(IS);
+                const double V = sa + tb2S - cr - 1.1368683772161603e-13 * (sa + tb2S + fabs(cr));  // 2^-43 slack
+                const double r = sqrt(fmax(V, 0.0)) * (1.0 - 1e-15) - static_cast<double>(eS) - eqS;
+                lb = r > 0.0 ? r * r * (1.0 - 1e-9) : 0.0;
+            }
+            const double tau = tau_now();
+            const uint32_t keep = __ballot_sync(kFull, valid && lb <= tau);
+            if (keep) {
+                if ((keep >> lane) & 1u) {
+                    const uint32_t p = qn + __popc(keep & ((1u << lane) - 1u));
+                    qid[p] = myid;
+                    qI[p] = IS;
+                }
+                qn += __popc(keep);
+                __syncwarp();
+            }
+        }
+    }
+    cp_async_wait<0>();
+    if (overflow && lane == 0) atomicOr(&ovf, 1);
+    md[warp * 32 + lane] = sl;
+    __syncthreads();
+    if (warp == 0) {
+        for (uint32_t w = 1; w < kWarps; ++w) {
+            for (uint32_t i = 0; i < a.k; ++i) {
+                const double v = md[w * 32 + i];
+                if (!(v < __shfl_sync(kFull, sl, a.k - 1))) break;  // lists are sorted
+                list_insert_val(v, sl, a.k, lane);
+            }
+        }
+        const double t = __shfl_sync(kFull, sl, a.k - 1);
+        if (lane == 0) tau_cta = t;
+    }
+    __syncthreads();
+    const double tau = tau_cta;
+    double ld = kInf;
+    uint32_t lid = 0xffffffffu;
+    float* st = reinterpret_cast<float*>(ra);  // the drained rings are staging now
+    if (ovf) {  // exact re-rank of the whole query, the warps splitting the candidates
+        const uint64_t per = (mq + kWarps - 1) / kWarps, lo = min_u64(mq, warp * per), hi = min_u64(mq, lo + per);
+        if (a.screen_stats && tid == 0) atomicAdd(a.screen_stats + 1, 1ull);
+        exact_rows(a, st, stride, qd, hi - lo,
+                   [&](uint64_t t) { return a.identity ? static_cast<uint32_t>(lo + t) : cands[lo + t]; }, ld, lid, lane);
+    } else {
+        uint32_t kept = 0;  // survivors: buffered rows whose lower bound is within the CTA's tau
+        for (uint32_t t0 = 0; t0 < nsurv; t0 += 32) {
+            const uint32_t t = t0 + lane;
+            const bool in = t < nsurv;
+            const uint32_t idv = in ? sid[warp][t] : 0u;
+            const bool keep = in && static_cast<double>(slo[warp][t]) <= tau;
+            const uint32_t kb = __ballot_sync(kFull, keep);
+            __syncwarp();
+            if (keep) sid[warp][kept + __popc(kb & ((1u << lane) - 1u))] = idv;
+            kept += __popc(kb);
+            __syncwarp();
+        }
+        if (a.screen_stats && lane == 0) atomicAdd(a.screen_stats, static_cast<unsigned long long>(kept));
+        exact_rows(a, st, stride, qd, kept, [&](uint64_t t) { return sid[warp][t]; }, ld, lid, lane);
+    }
+    __syncthreads();
+    md[warp * 32 + lane] = ld;
+    mi[warp * 32 + lane] = lid;
+    __syncthreads();
+    if (warp == 0) {
+        for (uint32_t w = 1; w < kWarps; ++w) {
+            for (uint32_t i = 0; i < a.k; ++i) {
+                const double dv = md[w * 32 + i];
+                if (dv == kInf) break;
+                warp_insert(dv, mi[w * 32 + i], ld, lid, a.k, lane);
+            }
+        }
+        if (lane < a.k) {
+            a.out_ids[q * a.k + lane] = lid;
+            a.out_dists[q * a.k + lane] = a.squared ? ld : __dsqrt_rn(ld);
+        }
+    }
+}
+
 // ---------------------------------------------------------------- u8 rows
 // Data certified integer in [0, 255] at upload and a query of the same kind:
 // every (x - q)^2 is an integer and every partial sum stays below 2^32, so
@@ -1563,10 +1920,22 @@ cudaError_t launch_rerank(const RerankArgs& a, uint64_t nq, cudaStream_t st) {
         const KQ kc[8] = {rerank_q8_kernel<1, false>, rerank_q8_kernel<2, false>, rerank_q8_kernel<3, false>,
                           rerank_q8_kernel<4, false>, rerank_q8_kernel<5, false>, rerank_q8_kernel<6, false>,
                           rerank_q8_kernel<7, false>, rerank_q8_kernel<8, false>};
-        const KQ kern = a.no_tma ? kc[nwq - 1] : kt[nwq - 1];
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(qsmem));
+        KQ kern = a.no_tma ? kc[nwq - 1] : kt[nwq - 1];
+        size_t ksmem = qsmem;
+        if (a.qpre) {  // the prefix-bound kernel (records in its layout, pack_q8_kernel)
+            const KQ k1[7] = {rerank_q8p_kernel<1, 1>, rerank_q8p_kernel<1, 2>, rerank_q8p_kernel<1, 3>,
+                              rerank_q8p_kernel<1, 4>, rerank_q8p_kernel<1, 5>, rerank_q8p_kernel<1, 6>,
+                              rerank_q8p_kernel<1, 7>};
+            const KQ k3[5] = {rerank_q8p_kernel<3, 1>, rerank_q8p_kernel<3, 2>, rerank_q8p_kernel<3, 3>,
+                              rerank_q8p_kernel<3, 4>, rerank_q8p_kernel<3, 5>};
+            kern = a.qpre == 1 ? k1[nwq - 2] : k3[nwq - 4];
+            const uint32_t nr = nwq - a.qpre, sub = (nr + 1) | 1u, sua = (a.qpre + 1) | 1u;
+            const size_t rings = (size_t(kQ8Stages) * 32 * sua + size_t(2) * 32 * sub) * 16;
+            ksmem = ((a.d * 8 + 15) / 16) * 16 + kWarps * std::max<size_t>(rings, size_t(kRows) * stride * 4);
+        }
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ksmem));
         if (e != cudaSuccess) return e;
-        kern<<<static_cast<unsigned>(nq), kThreads, qsmem, st>>>(a, stride);
+        kern<<<static_cast<unsigned>(nq), kThreads, ksmem, st>>>(a, stride);
         return cudaGetLastError();
     }
     if (vec && !generic && pmode == 2) {

@@ -70,17 +70,24 @@ __global__ void pack_u8_kernel(const float* data, uint64_t n, uint32_t d, uint32
 // the row's bound terms (rerank_q8_kernel): |x|^2 (fp64 sum, rounded to f32), ||s a|| and
 // ||x - s a|| (fp64, rounded up). A row whose terms are not finite gets s = -1: it always survives
 // the screen.
+// The int8 screen's records (rerank.cu). Plain (qpre = 0): [int8 row][meta = (s, |x|^2, ||s a|| up,
+// ||e_x|| up)]. Prefix-bound layout (rerank_q8p_kernel): [meta0 = (s, |a_S|^2, ||e_x,S|| up, 0)]
+// [dims 0 .. 16 qpre), then from byte qsplit [the other dims][meta1 = (|x|^2, ||s a|| up, ||e_x|| up,
+// s)], S = the first 16 qpre dims. A row with a non-finite term gets s = -1 (always re-ranked exactly).
 __global__ void pack_q8_kernel(const float* __restrict__ data, uint64_t n, uint32_t d, uint32_t qpad, uint32_t qrec,
-                               int8_t* __restrict__ out) {
+                               uint32_t qpre, uint32_t qsplit, int8_t* __restrict__ out) {
+    const uint32_t kPre = 16 * qpre;  // prefix dims
     const uint32_t lane = threadIdx.x & 31u;
+    const bool split = qpre != 0;
     const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x / 32);
     for (uint64_t r = blockIdx.x * uint64_t(blockDim.x / 32) + (threadIdx.x >> 5); r < n; r += warps) {
         const float* x = data + r * d;
+        int8_t* rec = out + r * qrec;
         float mx = 0.f;
         for (uint32_t i = lane; i < d; i += 32) mx = fmaxf(mx, fabsf(x[i]));
         for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         const float s = mx / 127.f;
-        double e2 = 0.0, a2 = 0.0, n2 = 0.0;
+        double e2 = 0.0, a2 = 0.0, n2 = 0.0, e2s = 0.0, a2s = 0.0;
         for (uint32_t i = lane; i < qpad; i += 32) {
             float av = 0.f;
             if (i < d) {
@@ -90,31 +97,48 @@ __global__ void pack_q8_kernel(const float* __restrict__ data, uint64_t n, uint3
                 e2 += e * e;
                 a2 += static_cast<double>(av) * static_cast<double>(av);
                 n2 += static_cast<double>(v) * static_cast<double>(v);
+                if (i < kPre) {
+                    e2s += e * e;
+                    a2s += static_cast<double>(av) * static_cast<double>(av);
+                }
             }
-            out[r * qrec + i] = static_cast<int8_t>(av);
+            rec[!split ? i : i < kPre ? 16 + i : qsplit + (i - kPre)] = static_cast<int8_t>(av);
         }
         for (int o = 16; o > 0; o >>= 1) {
             e2 += __shfl_xor_sync(0xffffffffu, e2, o);
             a2 += __shfl_xor_sync(0xffffffffu, a2, o);
             n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+            e2s += __shfl_xor_sync(0xffffffffu, e2s, o);
+            a2s += __shfl_xor_sync(0xffffffffu, a2s, o);
         }
         if (lane == 0) {
             const double A = static_cast<double>(s) * sqrt(a2) * (1.0 + 1e-12);
             const double R = sqrt(e2) * (1.0 + 1e-12);
+            const double RS = sqrt(e2s) * (1.0 + 1e-12);
             const float fn2 = __double2float_rn(n2), fA = __double2float_ru(A), fR = __double2float_ru(R);
-            const bool ok = isfinite(fn2) && isfinite(fA) && isfinite(fR) && isfinite(s);
-            *reinterpret_cast<float4*>(out + r * qrec + qpad) = ok ? make_float4(s, fn2, fA, fR)
-                                                                     : make_float4(-1.f, 0.f, 0.f, 0.f);
-            for (uint32_t i = qpad + 16; i < qrec; ++i) out[r * qrec + i] = 0;
+            const float fRS = __double2float_ru(RS);
+            const bool ok = isfinite(fn2) && isfinite(fA) && isfinite(fR) && isfinite(fRS) && isfinite(s);
+            const float fs = ok ? s : -1.f;
+            if (!split) {
+                *reinterpret_cast<float4*>(rec + qpad) = ok ? make_float4(s, fn2, fA, fR) : make_float4(-1.f, 0.f, 0.f, 0.f);
+                for (uint32_t i = qpad + 16; i < qrec; ++i) rec[i] = 0;
+            } else {
+                for (uint32_t i = 16 + kPre; i < qsplit; ++i) rec[i] = 0;
+                const uint32_t m1 = qsplit + (qpad - kPre);  // meta1 after the rest of the row
+                *reinterpret_cast<uint4*>(rec) =
+                    make_uint4(__float_as_uint(fs), static_cast<uint32_t>(a2s), __float_as_uint(fRS), 0u);
+                *reinterpret_cast<float4*>(rec + m1) = make_float4(fn2, fA, fR, fs);
+                for (uint32_t i = m1 + 16; i < qrec; ++i) rec[i] = 0;
+            }
         }
     }
 }
 
-cudaError_t launch_pack_q8(const float* data, uint64_t n, uint32_t d, uint32_t qpad, uint32_t qrec, int8_t* out,
-                           cudaStream_t st) {
+cudaError_t launch_pack_q8(const float* data, uint64_t n, uint32_t d, uint32_t qpad, uint32_t qrec, uint32_t qpre,
+                           uint32_t qsplit, int8_t* out, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
     const uint64_t blocks = min_u64((n + 7) / 8, 148ull * 16);
-    pack_q8_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(data, n, d, qpad, qrec, out);
+    pack_q8_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(data, n, d, qpad, qrec, qpre, qsplit, out);
     return cudaGetLastError();
 }
 
@@ -158,6 +182,8 @@ Tuning tuning_from_env() {
     t.cluster = (c >= 1 && c <= 16) ? c : 0;
     t.no_u8 = std::getenv("SUCO_NO_U8") != nullptr;
     t.q8 = env_int("SUCO_Q8", 1) != 0;
+    const int qp = env_int("SUCO_Q8_PREFIX", 3);
+    t.q8_prefix = (qp == 0 || qp == 1 || qp == 3) ? static_cast<uint32_t>(qp) : 3u;
     t.dense = env_int("SUCO_DENSE", 1) != 0;
     t.dense_half = env_int("SUCO_DENSE_HALF", 1);
     t.dense_pair = env_int("SUCO_DENSE_PAIR", 0);
