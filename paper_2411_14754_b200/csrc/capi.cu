@@ -297,7 +297,7 @@ void finalize_dense(suco_gpu_index* x, bool allow_half) {
         x->codes.reserve(n_pad * 8);
         CUDA_TRY(launch_dense_codes_half(x->ids.p, x->cell_off.p, n, n_pad, ns, x->K, x->codes.p, x->own));
     } else if (x->dense) {
-        x->codes.reserve(n * (ns > 8 ? 16 : 8));
+        x->codes.reserve((n + kDenseCodePad) * (ns > 8 ? 16 : 8));
         CUDA_TRY(launch_dense_codes(x->ids.p, x->cell_off.p, n, ns, x->K, x->codes.p, x->own));
     }
     if (!x->dense) {

@@ -166,9 +166,31 @@ __device__ __forceinline__ Codes<NC> load_codes_at(const DenseArgs& a, const uin
     return c;
 }
 
+// One 32-bit mask per slot at the shared-window address mb + 4 slot: the shift and add are one LEA
+// per lookup (through a generic pointer ptxas adds the window base to every address separately).
+__device__ __forceinline__ uint32_t lds_slot(uint32_t mb, uint32_t slot) {
+    uint32_t v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(mb + (slot << 2)));
+    return v;
+}
+
 template <uint32_t W, uint32_t NC>
-__device__ __forceinline__ void planes_of(const uint32_t* M, const Codes<NC>& c, uint32_t (&b)[W][Np<NC>::v]) {
-    uint32_t m[8 * NC][W];
+__device__ __forceinline__ void masks_of(const uint32_t* M, const Codes<NC>& c, uint32_t (&m)[8 * NC][W]) {
+    if constexpr (W == 1) {
+        const uint32_t mb = static_cast<uint32_t>(__cvta_generic_to_shared(M));
+#pragma unroll
+        for (uint32_t i = 0; i < NC; ++i) {
+            m[8 * i + 0][0] = lds_slot(mb, c.v[i].x & 0xffffu);
+            m[8 * i + 1][0] = lds_slot(mb, c.v[i].x >> 16);
+            m[8 * i + 2][0] = lds_slot(mb, c.v[i].y & 0xffffu);
+            m[8 * i + 3][0] = lds_slot(mb, c.v[i].y >> 16);
+            m[8 * i + 4][0] = lds_slot(mb, c.v[i].z & 0xffffu);
+            m[8 * i + 5][0] = lds_slot(mb, c.v[i].z >> 16);
+            m[8 * i + 6][0] = lds_slot(mb, c.v[i].w & 0xffffu);
+            m[8 * i + 7][0] = lds_slot(mb, c.v[i].w >> 16);
+        }
+        return;
+    }
 #pragma unroll
     for (uint32_t i = 0; i < NC; ++i) {
         mask_at<W>(M, c.v[i].x & 0xffffu, m[8 * i + 0]);
@@ -180,6 +202,11 @@ __device__ __forceinline__ void planes_of(const uint32_t* M, const Codes<NC>& c,
         mask_at<W>(M, c.v[i].w & 0xffffu, m[8 * i + 6]);
         mask_at<W>(M, c.v[i].w >> 16, m[8 * i + 7]);
     }
+}
+
+// The carry-save adder tree over a point's 8 * NC masks: its score bit-planes for the block.
+template <uint32_t W, uint32_t NC>
+__device__ __forceinline__ void csa_planes(const uint32_t (&m)[8 * NC][W], uint32_t (&b)[W][Np<NC>::v]) {
 #pragma unroll
     for (uint32_t w = 0; w < W; ++w) {
         if constexpr (NC == 1) {
@@ -217,6 +244,13 @@ __device__ __forceinline__ void planes_of(const uint32_t* M, const Codes<NC>& c,
             b[w][4] = f1 & f2;  // weight 16
         }
     }
+}
+
+template <uint32_t W, uint32_t NC>
+__device__ __forceinline__ void planes_of(const uint32_t* M, const Codes<NC>& c, uint32_t (&b)[W][Np<NC>::v]) {
+    uint32_t m[8 * NC][W];
+    masks_of<W, NC>(M, c, m);
+    csa_planes<W, NC>(m, b);
 }
 
 // The same scores with lane = query (word w: query 32w + lane): planes B[w][*] (bit r =
@@ -412,19 +446,14 @@ __global__ void __launch_bounds__(256) dense_plan_fused_kernel(DenseArgs a) {
     const uint64_t q = uint64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
     if (q >= a.nq) return;
     const uint32_t* h = a.h2 + q * a.P;
-    uint64_t geL = 0, geL1 = 0;
-    for (uint32_t p = lane; p < a.P; p += 32) {
-        const uint32_t v = h[p];
-        geL += v & 0xffffu;
-        geL1 += v >> 16;
-    }
+    uint64_t geL1 = 0;  // #(score > L)
+    for (uint32_t p = lane; p < a.P; p += 32) geL1 += h[p] >> 16;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        geL += __shfl_xor_sync(kFull, geL, o);
-        geL1 += __shfl_xor_sync(kFull, geL1, o);
-    }
+    for (int o = 16; o > 0; o >>= 1) geL1 += __shfl_xor_sync(kFull, geL1, o);
     const uint32_t L = a.L[q] & 0xffu;
-    bool ok = L >= 1 && geL >= a.m && geL1 < a.m;
+    // (#(score >= L) >= m is checked below as: the ties counted before the cut cover `need`; pieces
+    // past every tie cut of their block record #(score > L) in both halves)
+    bool ok = L >= 1 && geL1 < a.m;
     const uint64_t need = a.m - geL1;
     uint64_t ties_run = 0, gt_run = 0, tie_run = 0;
     for (uint32_t p0 = 0; p0 < a.P; p0 += 32) {
@@ -467,7 +496,7 @@ __global__ void __launch_bounds__(256) dense_plan_fused_kernel(DenseArgs a) {
         gt_run += gsum;
         tie_run += qsum;
     }
-    ok = __all_sync(kFull, ok);
+    ok = __all_sync(kFull, ok) && ties_run >= need;
     if (lane == 0) {
         a.qflag[q] = ok ? 0u : 1u;
         if (ok && a.clist) {  // the compaction kernels' work lists
@@ -640,15 +669,27 @@ __device__ __forceinline__ void fused_pieces(const DenseArgs& a, const uint32_t*
         // 32-bit tile loop over the piece: a running code pointer, the piece's point count
         const uint32_t len = static_cast<uint32_t>(hi - lo);
         const uint4* cptr = a.codes + (lo + lane) * NC;
-        Codes<NC> code = load_codes_at<NC>(a, cptr, lane < len);
-        Codes<NC> code1 = load_codes_at<NC>(a, cptr + 32 * NC, 32 + lane < len);
+        // software pipeline: the next tile's mask lookups are in flight while this tile's planes
+        // are compared, transposed and emitted; its codes were loaded a tile before that
+        uint32_t mk[8 * NC][W];
+        // (unconditional loads: the code rows are padded with zero-slot codes past n, and loads past
+        // a piece's end read the next piece's codes, never scored)
+        masks_of<W, NC>(M, load_codes_at<NC>(a, cptr, true), mk);
+        Codes<NC> code1 = load_codes_at<NC>(a, cptr + 32 * NC, true);
+        // Pieces past every lane's tie cut need only score > L (lane = query): one transpose per tile
+        // instead of two; their #(score >= L) is not needed by the plan (its ties are never taken:
+        // a quota that reaches past the cut flags the query) and is recorded as #(score > L).
+        bool need_ge = false;
+#pragma unroll
+        for (uint32_t w = 0; w < W; ++w) need_ge |= piece < cut[w];
+        need_ge = __any_sync(kFull, need_ge);
         for (uint32_t tb = 0; tb < len; tb += 32) {
             cptr += 32 * NC;
             // two tiles ahead: the code loads miss L2 often enough that one tile did not cover them
-            const Codes<NC> next = load_codes_at<NC>(a, cptr + 32 * NC, tb + 64 + lane < len);
+            const Codes<NC> next = load_codes_at<NC>(a, cptr + 32 * NC, true);
             uint32_t b[W][NP];
-            planes_of<W, NC>(M, code, b);
-            code = code1;
+            csa_planes<W, NC>(mk, b);
+            masks_of<W, NC>(M, code1, mk);  // (past the piece end: the zero slot)
             code1 = next;
 #pragma unroll
             for (uint32_t w = 0; w < W; ++w) {
@@ -659,10 +700,16 @@ __device__ __forceinline__ void fused_pieces(const DenseArgs& a, const uint32_t*
                     gt |= eq & b[w][i] & ~TL[w][i];
                     eq &= ~(b[w][i] ^ TL[w][i]);
                 }
-                const uint32_t ge0 = xp((gt | eq) & live[w]);  // lane = query, bit r = point t0 + r
-                const uint32_t g1 = xp(gt & live[w]);
-                cnt[w] += __popc(ge0) | (__popc(g1) << 16);
-                uint32_t bits = piece < cut[w] ? ge0 : g1;  // past the tie cut: score > L only
+                const uint32_t g1 = xp(gt & live[w]);  // lane = query, bit r = point t0 + r
+                uint32_t bits = g1;
+                if (need_ge) {
+                    const uint32_t ge0 = xp((gt | eq) & live[w]);
+                    cnt[w] += __popc(ge0) | (__popc(g1) << 16);
+                    if (piece < cut[w]) bits = ge0;  // before the tie cut: every score >= L
+                } else {
+                    const uint32_t c1 = __popc(g1);
+                    cnt[w] += c1 | (c1 << 16);
+                }
                 while (bits) {  // id order
                     const uint32_t r = __ffs(bits) - 1;
                     bits &= bits - 1;
@@ -1401,7 +1448,7 @@ size_t dense_smem(uint32_t ns, uint32_t K) { return (size_t(dense_none(ns, K)) +
 cudaError_t launch_dense_codes(const uint32_t* ids, const uint32_t* cell_off, uint64_t n, uint32_t ns, uint32_t K,
                                uint16_t* codes, cudaStream_t st) {
     const uint32_t cw = ns > 8 ? 16 : 8;
-    const uint64_t count = n * cw;
+    const uint64_t count = (n + kDenseCodePad) * cw;  // the padding rows: zero-slot codes
     const unsigned fb = static_cast<unsigned>(min_u64((count + 255) / 256, 148ull * 16));
     dense_codes_fill_kernel<<<fb ? fb : 1, 256, 0, st>>>(codes, count, static_cast<uint16_t>(dense_none(ns, K)));
     const uint64_t total = uint64_t(ns) * K;

@@ -158,6 +158,7 @@ cudaError_t launch_dense_hist_rows(const DenseArgs& a, uint32_t* out, cudaStream
 cudaError_t launch_dense_emit(const DenseArgs& a, cudaStream_t st);
 constexpr uint32_t kDensePiece = 2048;  // points per piece (one warp)
 constexpr uint32_t kDenseBuf = 96;      // single-pass candidate buffer entries per 2048 points of a (piece, query)
+constexpr uint32_t kDenseCodePad = 128;  // zero-slot code rows past n (the fused pass loads two tiles ahead)
 constexpr uint32_t kFusedPiece = 8192;  // points per piece of the single-pass select (half-width mode: kDensePiece)
 
 // ------------------------------------------------------------------ rerank
