@@ -81,6 +81,8 @@ def rerank_row_bytes(base, queries):
     if u8:
         return u8, "u8 rows"
     if d % 4 == 0 and d <= 128 and not os.environ.get("SUCO_Q8") == "0":
+        if d > 48:  # the prefix-bound layout: the first 64 bytes of every record, the rest for a few
+            return 64, "int8 screen record prefixes (+ the rest of the rows past the prefix bound)"
         return ((d + 15) // 16 * 16 + 16 + 63) // 64 * 64, "int8 screen records (+ exact f32 rows of the survivors)"
     return 4 * d, "f32 rows"
 
@@ -429,15 +431,16 @@ def main():
     traffic = ncu_traffic(cfg.name)
     names = ["traverse", "select", "rerank"]
     id_equiv = {"select": 4.0 * cum, "rerank": 4.0 * d * m * sq + 4.0 * d * sq}
+    rr_ncu = (traffic.get("rerank") or {}).get("dram_bytes")
     moved = {"traverse": (traffic.get("traverse") or {}).get("dram_bytes", 0.0),
              "select": (traffic.get("select") or {}).get("dram_bytes"),
-             "rerank": float(row_bytes) * m * sq + 4.0 * d * sq}
+             "rerank": rr_ncu or float(row_bytes) * m * sq + 4.0 * d * sq}
     per_kernel = {}
     for i, nm in enumerate(names):
         t = stage_avg[i] / 1000.0
         b = moved[nm]
         per_kernel[nm] = {"ms": stage_avg[i], "moved_bytes": b,
-                          "moved_source": "ncu dram bytes" if nm != "rerank" else f"model: {row_kind}, {row_bytes} B/row",
+                          "moved_source": "ncu dram bytes" if nm != "rerank" or rr_ncu else f"model: {row_kind}, {row_bytes} B/row",
                           "achieved_gbs": b / t / 1e9 if b else None, "frac": b / t / 1e9 / peak if b else None,
                           "dram_bytes_ncu": (traffic.get(nm) or {}).get("dram_bytes"),
                           "binding_pipes_ncu": (traffic.get(nm) or {}).get("pipes")}

@@ -548,8 +548,12 @@ FbLists stage_select(const suco_gpu_index* x, suco_gpu_query_ctx* c, suco_gpu_qu
             // pieces when that is enough (cfg2: 489 pieces -> every 30th), every 64th piece at most
             // for large corpora (measured: cfg2 2.31M -> 2.36M q/s, cfg4 167K -> 174K; fewer samples
             // mis-estimate T and send queries to the fallback); small corpora: all of them (exact)
-            da.pstride = da.P <= 64 ? 1u : std::min<uint32_t>(64, da.P / 16);
-            da.Ps = (da.P + da.pstride - 1) / da.pstride;
+            // (sampled pieces of kDensePiece points whatever the pass's piece size: measured at cfg4,
+            // 16 samples of 16384 points took 1.05 ms, the warps walking 512 tiles each)
+            const uint32_t P2 = static_cast<uint32_t>((h.n + kDensePiece - 1) / kDensePiece);
+            da.sWP = kDensePiece;
+            da.pstride = P2 <= 64 ? 1u : std::min<uint32_t>(64, P2 / 16);
+            da.Ps = (P2 + da.pstride - 1) / da.pstride;
             sl.dsample.reserve(nt * da.Ps * 8 * da.nc);
             da.stage_all = tn.dense_stage;
             // entries per (piece, query): at least kDenseBuf (~6 sigma above cfg4's mean of 46); small
@@ -573,6 +577,7 @@ FbLists stage_select(const suco_gpu_index* x, suco_gpu_query_ctx* c, suco_gpu_qu
             da.nclist = sl.dflag.p + 5 * nt + 1;
             da.no_cut = tn.dense_nocut;
             da.compact_mode = tn.dense_compact;
+            da.compact_rows = tn.dense_compact_rows;
             da.hsample = sl.dsample.p;
             da.qmap = sl.dflag.p + nt;
             da.nmap = sl.dflag.p + 2 * nt;

@@ -593,9 +593,10 @@ __global__ void __launch_bounds__(256) dense_bound_kernel(DenseArgs a) {
         for (int o = 16; o > 0; o >>= 1) tot[t] += __shfl_xor_sync(kFull, tot[t], o);
     }
     uint64_t sampled = 0;  // points the sample scanned
+    const uint32_t swp = a.sWP ? a.sWP : a.WP;
     for (uint32_t p = 0; p < a.Ps; ++p) {
-        const uint64_t lo = uint64_t(p) * a.pstride * a.WP;
-        if (lo < a.n) sampled += min_u64(a.WP, a.n - lo);
+        const uint64_t lo = uint64_t(p) * a.pstride * swp;
+        if (lo < a.n) sampled += min_u64(swp, a.n - lo);
     }
     uint32_t L = 0;
     uint32_t atL = 0;
@@ -858,27 +859,41 @@ __global__ void __launch_bounds__(256) dense_compact_kernel(DenseArgs a) {
     const uint32_t lt = (1u << lane) - 1u;
     const uint32_t pbase = p * a.WP;
     const uint32_t nlist = a.nclist[0];
+    // The next work item's counts, quota, offsets and first two rows are loaded while this one is
+    // processed (the loop is latency-bound otherwise: one dependent round trip per item).
+    struct Item {
+        uint64_t q;
+        uint32_t n, quota, pos, pos2, x0, x1;
+    };
+    auto fetch = [&](uint32_t j, Item& it) {
+        it.q = a.clist[j];  // an unflagged query with a dense superset
+        const uint64_t i = it.q * a.P + p;
+        const uint16_t* buf = cb_base(a, it.q, p);
+        it.n = min(static_cast<uint32_t>(a.ccnt[i]), a.B);
+        it.quota = a.quota[i];
+        it.pos = a.base[i];  // score > T entries
+        it.pos2 = a.base2[i];  // ties
+        it.x0 = __ldcs(buf + cb_off(a, lane));
+        it.x1 = 32 + lane < a.B ? __ldcs(buf + cb_off(a, 32 + lane)) : 0u;
+    };
+    Item cur;
+    if (blockIdx.y < nlist) fetch(blockIdx.y, cur);
     for (uint32_t j = blockIdx.y; j < nlist; j += gridDim.y) {
-        const uint64_t q = a.clist[j];  // an unflagged query with a dense superset
-        const uint64_t i = q * a.P + p;
-        const uint16_t* buf = cb_base(a, q, p);
-        // one round trip for most pieces: the counts, quota, offset and the first row together
-        const uint32_t n = min(static_cast<uint32_t>(a.ccnt[i]), a.B);
-        const uint32_t quota = a.quota[i];
-        uint32_t pos = a.base[i], pos2 = a.base2[i];  // score > T entries, ties
-        const uint32_t x0 = __ldcs(buf + cb_off(a, lane));
-        if (!n) continue;
-        uint32_t* out = a.cands + q * a.m;
-        uint32_t ties = 0;
-        for (uint32_t e0 = 0; e0 < n; e0 += 128) {
-            uint32_t x[4];
+        Item nxt;
+        if (j + gridDim.y < nlist) fetch(j + gridDim.y, nxt);
+        const uint32_t n = cur.n, quota = cur.quota;
+        uint32_t pos = cur.pos, pos2 = cur.pos2, ties = 0;
+        uint32_t* out = a.cands + cur.q * a.m;
+        const uint16_t* buf = cb_base(a, cur.q, p);
+        for (uint32_t e0 = 0; e0 < n; e0 += 256) {
+            uint32_t x[8];
 #pragma unroll
-            for (uint32_t u = 0; u < 4; ++u) {
+            for (uint32_t u = 0; u < 8; ++u) {
                 const uint32_t e = e0 + 32 * u + lane;
-                x[u] = e0 + u == 0 ? x0 : e < n ? __ldcs(buf + cb_off(a, e)) : 0u;
+                x[u] = e0 == 0 && u == 0 ? cur.x0 : e0 == 0 && u == 1 ? cur.x1 : e < n ? __ldcs(buf + cb_off(a, e)) : 0u;
             }
 #pragma unroll
-            for (uint32_t u = 0; u < 4; ++u) {
+            for (uint32_t u = 0; u < 8; ++u) {
                 if (e0 + 32 * u >= n) break;
                 const bool valid = e0 + 32 * u + lane < n;
                 const bool gt = valid && (x[u] & 0x8000u);
@@ -893,6 +908,7 @@ __global__ void __launch_bounds__(256) dense_compact_kernel(DenseArgs a) {
                 ties += __popc(tb);
             }
         }
+        cur = nxt;
     }
 }
 
@@ -1584,6 +1600,7 @@ cudaError_t launch_dense_select_fused(const DenseArgs& args, cudaStream_t st, cu
     DenseArgs s0 = a;
     s0.P = a.Ps;
     s0.hist = a.hsample;
+    if (a.sWP) s0.WP = a.sWP;  // short sampled pieces: many warps per CTA row, few tiles each
     cudaError_t e = launch_dense_hist(s0, st);
     if (e != cudaSuccess) return e;
     dense_bound_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(a);
@@ -1605,7 +1622,11 @@ cudaError_t launch_dense_select_fused(const DenseArgs& args, cudaStream_t st, cu
     dense_plan_fused_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(a);
     const unsigned qrows = static_cast<unsigned>(min_u64(a.nq, 1024));  // rows walk the work lists
     if (a.compact_mode != 2) dense_compact_thread_kernel<<<dim3((a.P + 255) / 256, qrows), 256, 0, st>>>(a);  // sparse
-    if (a.compact_mode != 1) dense_compact_kernel<<<dim3((a.P + 7) / 8, qrows), 256, 0, st>>>(a);  // dense supersets
+    if (a.compact_mode != 1) {  // dense supersets: a warp per (query, piece); rows walk the work list
+        // (measured at cfg4: 1024 / 4096 / 65535 grid rows -> 29.73 / 29.86 / 30.06 ms per step)
+        const unsigned wrows = static_cast<unsigned>(min_u64(a.nq, a.compact_rows ? a.compact_rows : 1024));
+        dense_compact_kernel<<<dim3((a.P + 7) / 8, wrows), 256, 0, st>>>(a);
+    }
     e = cudaMemsetAsync(args.nmap, 0, 4, st);
     if (e != cudaSuccess) return e;
     dense_flag_list_kernel<<<static_cast<unsigned>((a.nq + 255) / 256), 256, 0, st>>>(args);

@@ -93,6 +93,7 @@ struct DenseArgs {
     uint32_t pstride;          // K1 over a sample: hist row j scans piece j * pstride (0 = 1)
     uint16_t* hsample;         // nq x Ps x 8 sampled histograms (K0)
     uint32_t Ps;               // sampled pieces
+    uint32_t sWP;              // points per sampled piece (0 = WP): 2048 whatever the single pass's piece size
     uint32_t* L;               // nq
     uint16_t* cbuf;            // single pass: [query][piece][B] in-piece offsets of score >= L (bit 15: > L)
     uint16_t* ccnt;            // single pass: nq x P entries found (may exceed B)
@@ -110,6 +111,7 @@ struct DenseArgs {
     uint32_t* clist;              // single pass: nq x 2 — unflagged queries with dense supersets from the front,
                                   // sparse ones from nq on (compaction work lists, any order)
     uint32_t* nclist;             // their two counts
+    uint32_t compact_rows;        // Tuning::dense_compact_rows: grid rows of the warp compaction (0 = 1024)
     uint32_t compact_mode;        // Tuning::dense_compact: 0 by density, 1 thread per piece, 2 warp per (query, piece)
     uint32_t pair;                // half mode: the fused pass as 2-CTA clusters with 32-bit masks of 4 subspaces each
     float cut_scale;              // tie cut = P * need/ties * cut_scale + cut_pad pieces (0: defaults 1.25, 8)

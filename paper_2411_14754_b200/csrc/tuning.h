@@ -30,6 +30,7 @@ struct Tuning {
     uint32_t dense_words = 0;    // SUCO_DENSE_WORDS: mask words per slot (0 auto, 1, 2)
     uint32_t dense_compact = 0;  // SUCO_DENSE_COMPACT: 0 by superset density (default), 1 thread per piece with a
                                  // shared staging copy of the block's output run, 2 warp per (query, piece)
+    uint32_t dense_compact_rows = 0;  // SUCO_DENSE_COMPACT_ROWS: grid rows of the warp compaction (A/B)
     uint32_t dense_piece = 0;    // SUCO_DENSE_PIECE: points per piece of the single-pass select (0 = 8192; a
                                  // multiple of 2048 up to 32768; the half-width mode keeps 2048)
     bool dense_stats = false;    // SUCO_DENSE_STATS=1: print the single-pass fallback rate (diagnostics)

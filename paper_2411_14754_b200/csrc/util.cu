@@ -197,6 +197,8 @@ Tuning tuning_from_env() {
     t.dense_stats = std::getenv("SUCO_DENSE_STATS") != nullptr;
     const int cm = env_int("SUCO_DENSE_COMPACT", 0);
     t.dense_compact = (cm == 1 || cm == 2) ? static_cast<uint32_t>(cm) : 0u;
+    const int cr = env_int("SUCO_DENSE_COMPACT_ROWS", 0);
+    t.dense_compact_rows = cr > 0 ? static_cast<uint32_t>(cr) : 0u;
     const int dp = env_int("SUCO_DENSE_PIECE", 0);
     t.dense_piece = dp >= 2048 && dp <= 32768 && dp % 2048 == 0 ? static_cast<uint32_t>(dp) : 0u;
     t.rerank_stats = std::getenv("SUCO_RERANK_STATS") != nullptr;
