@@ -424,6 +424,382 @@ __global__ void __launch_bounds__(256) kpp_select_kernel(const float* proj, cons
     for (uint32_t t = tid; t < jb.h; t += blockDim.x) cent[jb.coff + uint64_t(c) * jb.h + t] = proj[jb.off + uint64_t(p) * jb.h + t];
 }
 
+// ------------------------------------------------------- k-means++ fold over chunks
+// The same exact serial fold, spread over the device: each job's min_dist is cut into chunks of
+// kKppChunk values. While the running sum s stays in one binade [2^e, 2^(e+1)) a chunk adds exactly
+// U * R to it (U = ulp(s), R = sum of rint(a_i / U), an integer), whatever s is inside the binade,
+// barring a tie (a_i / U = m + 1/2). So every chunk computes R for the binade its approximate
+// prefix (the plain sum of the earlier chunks' sums) lies in — away from the binade's edges — and,
+// once its predecessor publishes the exact s_in (decoupled look-back, tickets in chunk-major order
+// so a predecessor always runs first), checks s_in is in that binade and s_in / U + R < 2^53:
+// then s_out = (s_in / U + R) U exactly. Chunks that cross a binade edge, hold a tie, or start
+// near an edge (the first chunks, where s grows through many binades) run the tile-by-tile binade
+// scan from s_in (kpp_select_kernel's fold). The pick then needs only the chunk holding the target
+// and one exact scan of it. Integer-exact jobs fold by plain sums. Measured at cfg4 (16 jobs x 10M
+// values): 20.6 ms per seeding round in one CTA per job ->.
+constexpr uint32_t kKppChunk = 32768;
+
+__device__ __forceinline__ double ld_volatile_f64(const double* p) { return *reinterpret_cast<const volatile double*>(p); }
+
+// Exact left-to-right fold of md[lo, hi) continued from s (one CTA, 256 threads, all of them call).
+// target >= 0: stops at, and returns in *first, the first index whose running value exceeds target
+// (~0ull if none). exact: integer-exact job (plain sums).
+__device__ double fold_tiles(const double* md, uint64_t lo, uint64_t hi, double s, bool exact, double target,
+                             uint64_t* first) {
+    __shared__ long long wsum[8];
+    __shared__ double wsd[8];
+    __shared__ uint32_t s_bad, s_hit;
+    __shared__ double s_run;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    constexpr double kTwo53 = 9007199254740992.0;
+    if (tid == 0) s_run = s;
+    if (first && tid == 0) *first = ~0ull;
+    __syncthreads();
+    for (uint64_t base = lo; base < hi; base += 2048) {
+        const uint32_t len = static_cast<uint32_t>(min_u64(2048, hi - base));
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint32_t i = tid * 8 + u;
+            v[u] = i < len ? md[base + i] : 0.0;
+        }
+        if (exact) {  // every partial sum an exact integer: a plain block scan
+            double loc = 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) loc += v[u];
+            double x = loc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double y = __shfl_up_sync(kFull, x, o);
+                if (lane >= static_cast<uint32_t>(o)) x += y;
+            }
+            if (lane == 31) wsd[warp] = x;
+            if (tid == 0) s_hit = 0xffffffffu;
+            __syncthreads();
+            double wpre = 0.0, tot = 0.0;
+            for (uint32_t w = 0; w < 8; ++w) {
+                if (w < warp) wpre += wsd[w];
+                tot += wsd[w];
+            }
+            const double s0 = s_run;
+            double run = s0 + wpre + (x - loc);
+            if (target >= 0.0) {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    run += v[u];
+                    const uint32_t i = tid * 8 + u;
+                    if (i < len && run > target) {
+                        atomicMin(&s_hit, i);
+                        break;
+                    }
+                }
+            }
+            __syncthreads();
+            if (target >= 0.0 && s_hit != 0xffffffffu) {
+                if (tid == 0) *first = base + s_hit;
+                __syncthreads();
+                return s0;  // (the fold stops at the pick; its value is not needed)
+            }
+            if (tid == 0) s_run = s0 + tot;
+            __syncthreads();
+            continue;
+        }
+        uint32_t start = 0;
+        while (start < len) {
+            const double s0 = s_run;  // exact running sum before element `start`
+            const bool tiny = !(s0 >= 2.2250738585072014e-308);  // 0 or subnormal
+            const double U = tiny ? 0.0 : ldexp(1.0, ilogb(s0) - 52);  // ulp of s0
+            const double S0 = tiny ? 0.0 : s0 / U;  // exact: power-of-two scaling
+            long long r[8];
+            bool badv[8];
+            long long loc = 0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t i = tid * 8 + u;
+                const bool live = i >= start && i < len;
+                r[u] = 0;
+                badv[u] = false;
+                if (live) {
+                    if (tiny) {
+                        badv[u] = v[u] != 0.0;  // 0 + 0 stays exact; anything else goes serial
+                    } else {
+                        const double q = v[u] / U;  // exact
+                        const double m = floor(q);
+                        const double f = q - m;  // exact
+                        badv[u] = f == 0.5 || q >= 4503599627370496.0;  // tie, or surely crossing
+                        const double rr = f > 0.5 ? m + 1.0 : m;
+                        r[u] = badv[u] ? 0 : static_cast<long long>(rr);
+                    }
+                }
+                loc += r[u];
+            }
+            long long x = loc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long y = __shfl_up_sync(kFull, x, o);
+                if (lane >= static_cast<uint32_t>(o)) x += y;
+            }
+            if (lane == 31) wsum[warp] = x;
+            if (tid == 0) {
+                s_bad = 0xffffffffu;
+                s_hit = 0xffffffffu;
+            }
+            __syncthreads();
+            long long wpre = 0, tot = 0;
+            for (uint32_t w = 0; w < 8; ++w) {
+                if (w < warp) wpre += wsum[w];
+                tot += wsum[w];
+            }
+            long long run = wpre + (x - loc);  // exclusive prefix of this thread's first element
+            uint32_t first_bad = 0xffffffffu;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t i = tid * 8 + u;
+                if (i >= start && i < len && first_bad == 0xffffffffu) {
+                    const double before = S0 + static_cast<double>(run);  // exact while < 2^53
+                    if (badv[u] || (!tiny && static_cast<double>(r[u]) + before >= kTwo53) || (!tiny && before >= kTwo53))
+                        first_bad = i;
+                    run += r[u];
+                }
+            }
+            if (first_bad != 0xffffffffu) atomicMin(&s_bad, first_bad);
+            __syncthreads();
+            const uint32_t bad = s_bad;
+            run = wpre + (x - loc);
+            double prev_bad = s0;  // the exact running value just before `bad` (this thread's copy)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t i = tid * 8 + u;
+                if (i >= start && i < len) {
+                    if (i == bad) prev_bad = tiny ? s0 : __dmul_rn(S0 + static_cast<double>(run), U);
+                    run += r[u];
+                    if (i < bad && target >= 0.0) {
+                        const double val = tiny ? s0 : __dmul_rn(S0 + static_cast<double>(run), U);
+                        if (val > target) atomicMin(&s_hit, i);
+                    }
+                }
+            }
+            if (target >= 0.0 && tid == (bad >> 3) && bad < len) {  // the serial add may be the pick
+                const double nv = __dadd_rn(prev_bad, v[bad & 7u]);
+                if (nv > target) atomicMin(&s_hit, bad);
+            }
+            __syncthreads();
+            if (target >= 0.0 && s_hit != 0xffffffffu) {
+                if (tid == 0) *first = base + s_hit;
+                __syncthreads();
+                return s0;
+            }
+            if (bad == 0xffffffffu || bad >= len) {  // the whole rest of the tile was good
+                if (tid == 0) s_run = tiny ? s0 : __dmul_rn(S0 + static_cast<double>(tot), U);
+                __syncthreads();
+                break;
+            }
+            if (tid == (bad >> 3)) s_run = __dadd_rn(prev_bad, v[bad & 7u]);  // one serial add
+            __syncthreads();
+            start = bad + 1;
+        }
+    }
+    const double out = s_run;
+    __syncthreads();
+    return out;
+}
+
+// Plain (any-order) sum of each chunk: the approximate prefixes that choose the chunks' binades.
+__global__ void __launch_bounds__(256) kpp_chunk_sum_kernel(const double* __restrict__ min_dist, uint64_t n,
+                                                            uint32_t NC, double* __restrict__ csum) {
+    __shared__ double red[8];
+    const uint32_t j = blockIdx.y, c = blockIdx.x, tid = threadIdx.x;
+    const uint64_t lo = uint64_t(c) * kKppChunk, hi = min_u64(n, lo + kKppChunk);
+    const double* md = min_dist + uint64_t(j) * n;
+    double a = 0.0;
+    for (uint64_t i = lo + tid; i < hi; i += 256) a += md[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(kFull, a, o);
+    if ((tid & 31u) == 0) red[tid >> 5] = a;
+    __syncthreads();
+    if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += red[w];
+        csum[uint64_t(j) * NC + c] = t;
+    }
+}
+
+// The exact fold chunk by chunk (see above): sin / sout = exact running sums at each chunk's ends.
+__global__ void __launch_bounds__(256) kpp_chunk_fold_kernel(const double* __restrict__ min_dist, uint64_t n,
+                                                             uint32_t NC, uint32_t J, const uint8_t* exact,
+                                                             const double* __restrict__ csum, double* sin, double* sout,
+                                                             uint32_t* ready, uint32_t* ticket, uint32_t epoch) {
+    __shared__ uint32_t s_t;
+    __shared__ double red[8];
+    __shared__ long long redi[8];
+    __shared__ int redb[8];
+    __shared__ double s_in_sh;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    if (tid == 0) s_t = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint32_t c = s_t / J, j = s_t % J;  // chunk-major tickets: a predecessor always holds a smaller one
+    const uint64_t lo = uint64_t(c) * kKppChunk, hi = min_u64(n, lo + kKppChunk);
+    const double* md = min_dist + uint64_t(j) * n;
+    const double* cs = csum + uint64_t(j) * NC;
+    const bool ex = exact[j] != 0;
+    // approximate prefix of the chunk's start
+    double pa = 0.0;
+    for (uint32_t c2 = tid; c2 < c; c2 += 256) pa += cs[c2];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pa += __shfl_xor_sync(kFull, pa, o);
+    if (lane == 0) red[warp] = pa;
+    __syncthreads();
+    double P = 0.0;
+    for (int w = 0; w < 8; ++w) P += red[w];
+    bool slow = true;
+    int e = 0;
+    long long R = 0;
+    if (!ex && c > 0 && P >= 2.2250738585072014e-308) {
+        e = ilogb(P);
+        const double lo_b = ldexp(1.0, e), hi_b = ldexp(1.0, e + 1);
+        const double A = cs[c];
+        // away from the binade's edges by far more than the approximate prefix can be off
+        slow = !(P >= lo_b * (1.0 + 0x1p-24) && P + A <= hi_b * (1.0 - 0x1p-24));
+        if (!slow) {
+            const double U = ldexp(1.0, e - 52);
+            long long loc = 0;
+            bool bad = false;
+            for (uint64_t i = lo + tid; i < hi; i += 256) {
+                const double q = md[i] / U;
+                const double m = floor(q);
+                const double f = q - m;
+                bad |= f == 0.5 || q >= 4503599627370496.0;
+                loc += static_cast<long long>(f > 0.5 ? m + 1.0 : m);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) loc += __shfl_xor_sync(kFull, loc, o);
+            const int anyb = __any_sync(kFull, bad);
+            if (lane == 0) {
+                redi[warp] = loc;
+                redb[warp] = anyb;
+            }
+            __syncthreads();
+            for (int w = 0; w < 8; ++w) {
+                R += redi[w];
+                slow |= redb[w] != 0;
+            }
+        }
+    }
+    // look-back: the exact running sum at the chunk's start
+    if (tid == 0) {
+        double si = 0.0;
+        if (c > 0) {
+            const volatile uint32_t* rd = ready + uint64_t(j) * NC + c - 1;
+            while (*rd != epoch) __nanosleep(32);
+            __threadfence();
+            si = ld_volatile_f64(sout + uint64_t(j) * NC + c - 1);
+        }
+        s_in_sh = si;
+    }
+    __syncthreads();
+    const double s_in = s_in_sh;
+    double s_out;
+    if (ex) {
+        s_out = s_in + cs[c];  // integer-exact: every partial sum is exact, any order
+    } else if (!slow && s_in >= ldexp(1.0, e) && s_in < ldexp(1.0, e + 1) &&
+               s_in / ldexp(1.0, e - 52) + static_cast<double>(R) < 9007199254740992.0) {
+        const double U = ldexp(1.0, e - 52);
+        s_out = __dmul_rn(s_in / U + static_cast<double>(R), U);  // exact: an integer below 2^53 times U
+    } else {
+        s_out = fold_tiles(md, lo, hi, s_in, false, -1.0, nullptr);
+    }
+    if (tid == 0) {
+        sin[uint64_t(j) * NC + c] = s_in;
+        sout[uint64_t(j) * NC + c] = s_out;
+        __threadfence();
+        *reinterpret_cast<volatile uint32_t*>(ready + uint64_t(j) * NC + c) = epoch;
+    }
+}
+
+// The pick of each job (kmeans.cpp:75-111): the first index whose running sum exceeds u * total,
+// found in the one chunk that holds it; then the reference's fallbacks (kpp_select_kernel's tail).
+__global__ void __launch_bounds__(256) kpp_pick_kernel(const float* proj, const KJob* jobs, uint64_t n, uint32_t c,
+                                                       const double* __restrict__ min_dist, const uint8_t* chosen,
+                                                       const uint8_t* exact, const double* uniforms, uint32_t kmax,
+                                                       uint32_t* used, uint32_t* pick, const double* sin,
+                                                       const double* sout, uint32_t NC, float* cent) {
+    __shared__ uint32_t shu[8];
+    __shared__ uint32_t s_pick, s_chunk;
+    __shared__ double s_target;
+    __shared__ uint64_t s_first;
+    const uint32_t j = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const double* md = min_dist + uint64_t(j) * n;
+    const double total = sout[uint64_t(j) * NC + NC - 1];
+    uint32_t p = 0xffffffffu;  // "n" sentinel
+    if (total > 0.0) {
+        if (tid == 0) {
+            const double u = uniforms[uint64_t(j) * kmax + used[j]];
+            used[j] += 1;
+            const double target = __dmul_rn(u, total);
+            uint32_t l = 0, h = NC;  // first chunk whose end value exceeds the target
+            while (l < h) {
+                const uint32_t mid = (l + h) >> 1;
+                if (sout[uint64_t(j) * NC + mid] > target) h = mid;
+                else l = mid + 1;
+            }
+            s_chunk = l;
+            s_target = target;
+        }
+        __syncthreads();
+        const uint32_t cc = s_chunk;
+        if (cc < NC) {
+            const uint64_t lo = uint64_t(cc) * kKppChunk, hi = min_u64(n, lo + kKppChunk);
+            fold_tiles(md, lo, hi, sin[uint64_t(j) * NC + cc], exact[j] != 0, s_target, &s_first);
+            __syncthreads();
+            p = s_first != ~0ull ? static_cast<uint32_t>(s_first) : 0xffffffffu;
+        }
+        if (p == 0xffffffffu) {  // round-off overran the walk: last positive-weight point
+            uint32_t best = 0;
+            bool found = false;
+            for (uint64_t i = tid; i < n; i += blockDim.x) {
+                if (md[i] > 0.0) {
+                    best = static_cast<uint32_t>(i);
+                    found = true;
+                }
+            }
+            uint32_t key = found ? best + 1 : 0;
+            for (int o = 16; o > 0; o >>= 1) key = max(key, __shfl_xor_sync(kFull, key, o));
+            if (lane == 0) shu[warp] = key;
+            __syncthreads();
+            if (tid == 0) {
+                uint32_t k2 = 0;
+                for (int w = 0; w < 8; ++w) k2 = max(k2, shu[w]);
+                s_pick = k2 ? k2 - 1 : 0xffffffffu;
+            }
+            __syncthreads();
+            p = s_pick;
+        }
+    }
+    if (p == 0xffffffffu) {  // all remaining points coincide with chosen centroids: lowest unchosen id
+        const uint8_t* ch = chosen + uint64_t(j) * n;
+        uint32_t best = 0xffffffffu;
+        for (uint64_t i = tid; i < n; i += blockDim.x) {
+            if (!ch[i]) {
+                best = static_cast<uint32_t>(i);
+                break;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(kFull, best, o));
+        if (lane == 0) shu[warp] = best;
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t b2 = 0xffffffffu;
+            for (int w = 0; w < 8; ++w) b2 = min(b2, shu[w]);
+            s_pick = b2 == 0xffffffffu ? 0u : b2;
+        }
+        __syncthreads();
+        p = s_pick;
+    }
+    if (tid == 0) pick[j] = p;
+    const KJob jb = jobs[j];
+    for (uint32_t t = tid; t < jb.h; t += blockDim.x) cent[jb.coff + uint64_t(c) * jb.h + t] = proj[jb.off + uint64_t(p) * jb.h + t];
+}
+
 // ------------------------------------------------------------------- assign
 // nearest_centroid (kmeans.cpp:19-33) for every point of every job.
 template <int HB>
@@ -784,7 +1160,7 @@ void kmeans_jobs(const float* proj, const std::vector<KJob>& host_jobs, const KJ
         pick0[j] = static_cast<uint32_t>(g.uniform_below(n));
         for (uint32_t c = 0; c + 1 < k; ++c) unis[uint64_t(j) * k + c] = g.uniform_unit();
     }
-    Dev<double> min_dist(uint64_t(J) * n), prefix(uint64_t(J) * n), d_unis(unis.size());
+    Dev<double> min_dist(uint64_t(J) * n), prefix(kpp_serial ? uint64_t(J) * n : 1), d_unis(unis.size());
     Dev<uint8_t> chosen(uint64_t(J) * n), d_exact(J);
     Dev<uint32_t> pick(J), used(J);
     BCUDA(cudaMemcpyAsync(d_unis.p, unis.data(), unis.size() * 8, cudaMemcpyHostToDevice, st));
@@ -795,10 +1171,24 @@ void kmeans_jobs(const float* proj, const std::vector<KJob>& host_jobs, const KJ
     copy_centroid_kernel<<<J, 64, 0, st>>>(proj, jobs, pick.p, 0, cent);
     BCUDA(cudaGetLastError());
     const dim3 gu(grid_for(n, 256, 148 * 4), J);
+    // the chunked fold (kpp_chunk_*); SUCO_KPP_SERIAL keeps the one-CTA-per-job kernel for A/B
+    const uint32_t NC = static_cast<uint32_t>((n + kKppChunk - 1) / kKppChunk);
+    Dev<double> csum(uint64_t(J) * NC), csin(uint64_t(J) * NC), csout(uint64_t(J) * NC);
+    Dev<uint32_t> cready(uint64_t(J) * NC), ticket(k);
+    BCUDA(cudaMemsetAsync(cready.p, 0, uint64_t(J) * NC * 4, st));
+    BCUDA(cudaMemsetAsync(ticket.p, 0, uint64_t(k) * 4, st));
     for (uint32_t c = 1; c < k; ++c) {
         kpp_update_kernel<<<gu, 256, 0, st>>>(proj, jobs, n, pick.p, min_dist.p, chosen.p);
-        kpp_select_kernel<<<J, 256, 0, st>>>(proj, jobs, n, c, min_dist.p, chosen.p, d_exact.p, d_unis.p, k, used.p,
-                                             pick.p, prefix.p, cent, kpp_serial);
+        if (kpp_serial) {
+            kpp_select_kernel<<<J, 256, 0, st>>>(proj, jobs, n, c, min_dist.p, chosen.p, d_exact.p, d_unis.p, k,
+                                                 used.p, pick.p, prefix.p, cent, kpp_serial);
+        } else {
+            kpp_chunk_sum_kernel<<<dim3(NC, J), 256, 0, st>>>(min_dist.p, n, NC, csum.p);
+            kpp_chunk_fold_kernel<<<NC * J, 256, 0, st>>>(min_dist.p, n, NC, J, d_exact.p, csum.p, csin.p, csout.p,
+                                                          cready.p, ticket.p + c, c);
+            kpp_pick_kernel<<<J, 256, 0, st>>>(proj, jobs, n, c, min_dist.p, chosen.p, d_exact.p, d_unis.p, k, used.p,
+                                               pick.p, csin.p, csout.p, NC, cent);
+        }
         BCUDA(cudaGetLastError());
     }
     min_dist.release();

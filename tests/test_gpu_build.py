@@ -24,12 +24,16 @@ def test_kmeans_golden(gpu):
                                                 (600, 4, 3, 10, "float"), (12, 2, 12, 3, "float"),
                                                 (20000, 8, 100, 2, "int"), (800, 40, 10, 3, "int"),
                                                 (60000, 4, 20, 2, "dyadic"), (50000, 6, 16, 2, "float"),
-                                                (30000, 2, 9, 2, "huge")])
+                                                (30000, 2, 9, 2, "huge"), (300000, 4, 16, 2, "dyadic"),
+                                                (400000, 6, 24, 2, "float"), (300000, 2, 9, 2, "huge"),
+                                                (250000, 5, 12, 2, "unit"), (200000, 8, 20, 1, "int")])
 def test_kmeans_vs_oracle(gpu, oracle, n, dim, k, iters, kind):
     """Exact k-means against the restated reference. "dyadic" (quarter-integers plus halves: few
     mantissa bits, so the running k-means++ sum meets exact rounding ties) and "huge" (magnitudes
     spanning 1e-30..1e30: binade crossings and serial adds everywhere) stress the parallel exact
-    fold of the k-means++ sums; the larger float corpora cross many binades."""
+    fold of the k-means++ sums; the larger float corpora cross many binades. Corpora past 32,768
+    points span several fold chunks (build.cu kpp_chunk_fold_kernel: per-chunk integer sums under
+    the predicted binade, look-back of the exact running sum, tile scans for the crossing chunks)."""
     rng = np.random.default_rng(n + dim + k)
     if kind == "int":
         pts = np.clip(np.rint(rng.normal(100, 30, (n, dim))), 0, 255).astype(np.float32)
