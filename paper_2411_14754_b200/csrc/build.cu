@@ -51,6 +51,7 @@ namespace {
     } while (0)
 
 constexpr uint32_t kFull = 0xffffffffu;
+constexpr float kInfF = __builtin_huge_valf();
 
 template <typename T>
 struct Dev {
@@ -806,19 +807,55 @@ template <int HB>
 __global__ void __launch_bounds__(256) assign_kernel(const float* __restrict__ proj, const KJob* __restrict__ jobs,
                                                      uint64_t n, uint32_t k, const float* __restrict__ cent,
                                                      uint32_t* __restrict__ assign) {
-    extern __shared__ __align__(16) double cs[];  // k x h centroids as doubles
+    extern __shared__ __align__(16) double cs[];  // k x h centroids as doubles (then as floats: the screen)
     const uint32_t j = blockIdx.y;
     const KJob jb = jobs[j];
     const uint32_t h = jb.h;
-    for (uint32_t t = threadIdx.x; t < k * h; t += blockDim.x) cs[t] = static_cast<double>(cent[jb.coff + t]);
+    float* cf = reinterpret_cast<float*>(cs + size_t(k) * h);
+    for (uint32_t t = threadIdx.x; t < k * h; t += blockDim.x) {
+        cs[t] = static_cast<double>(cent[jb.coff + t]);
+        if constexpr (HB > 0) cf[t] = cent[jb.coff + t];
+    }
     __syncthreads();
     const float* x = proj + jb.off;
     uint32_t* as = assign + uint64_t(j) * n;
+    // fp32 screen (HB > 0): FFMA distances f_c; f is within G f + E of the reference's fp64 value
+    // (one rounding of x - c, h accumulation roundings), so when the runner-up's lower bound is above
+    // the best's upper bound the fp64 argmin is that best — strictly, so the lowest-id tie rule
+    // cannot apply. Otherwise (near-ties, overflow) the point takes the exact fp64 loop below.
+    const float G = static_cast<float>(2 * h + 8) * 5.9604645e-08f, E = 7.5231638e-37f;  // (2h+8) 2^-24, 2^-120
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
         double p[HB > 0 ? HB : 1];
         if constexpr (HB > 0) {
+            float pf[HB];
 #pragma unroll
-            for (int t = 0; t < HB; ++t) p[t] = t < (int)h ? static_cast<double>(x[i * h + t]) : 0.0;
+            for (int t = 0; t < HB; ++t) pf[t] = t < (int)h ? x[i * h + t] : 0.f;
+            float f1 = kInfF, f2 = kInfF;
+            uint32_t b1 = 0;
+            for (uint32_t c = 0; c < k; ++c) {
+                const float* cc = cf + c * h;
+                float acc = 0.f;
+#pragma unroll
+                for (int t = 0; t < HB; ++t) {
+                    if ((uint32_t)t < h) {
+                        const float e = pf[t] - cc[t];
+                        acc = __fmaf_rn(e, e, acc);
+                    }
+                }
+                if (acc < f1) {
+                    f2 = f1;
+                    f1 = acc;
+                    b1 = c;
+                } else if (acc < f2) {
+                    f2 = acc;
+                }
+            }
+            if (f1 <= 3.0e38f && f2 * (1.f - G) - E > f1 * (1.f + G) + E) {
+                as[i] = b1;
+                continue;
+            }
+#pragma unroll
+            for (int t = 0; t < HB; ++t) p[t] = static_cast<double>(pf[t]);
         }
         uint32_t best = 0;
         double bd = kInf;
@@ -999,6 +1036,135 @@ __global__ void update_kernel(const float* __restrict__ proj, const KJob* __rest
     cent[jb.coff + uint64_t(c) * h + dim] = __double2float_rn(__dmul_rn(sum, inv));
 }
 
+// The same sums folded exactly in parallel: one CTA per (job, cluster, dim). A signed running sum
+// s with |s| in [2^e, 2^(e+1)) moves in steps of U = ulp(s): while every partial sum keeps s's sign
+// and binade, fl(s + a) = s + U rint(a / U) (ties excepted), so a tile is an int64 block scan of
+// rint(a_i / U) up to its first element that leaves the binade (up or down), is a tie, or meets a
+// zero / subnormal s; that element gets one serial __dadd_rn and the scan resumes. Measured at cfg4
+// (16 jobs x 64 clusters x 6 dims, 10M points): 50 ms per Lloyd round with one thread per column.
+template <class F>
+__device__ double fold_signed(F load, uint32_t count) {
+    __shared__ long long wsum[8];
+    __shared__ uint32_t s_bad;
+    __shared__ double s_run;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    constexpr long long kTwo52 = 4503599627370496ll, kTwo53 = 9007199254740992ll;
+    if (tid == 0) s_run = 0.0;
+    __syncthreads();
+    for (uint32_t base = 0; base < count; base += 2048) {
+        const uint32_t len = min(2048u, count - base);
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint32_t i = tid * 8 + u;
+            v[u] = i < len ? load(base + i) : 0.0;
+        }
+        uint32_t start = 0;
+        while (start < len) {
+            const double s0 = s_run;  // exact running sum before element `start`
+            const bool tiny = !(fabs(s0) >= 2.2250738585072014e-308);  // 0 or subnormal
+            const double U = tiny ? 0.0 : ldexp(1.0, ilogb(s0) - 52);
+            const long long S0 = tiny ? 0 : static_cast<long long>(s0 / U);  // exact, |S0| in [2^52, 2^53)
+            long long r[8];
+            bool badv[8];
+            long long loc = 0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t i = tid * 8 + u;
+                const bool live = i >= start && i < len;
+                r[u] = 0;
+                badv[u] = false;
+                if (live) {
+                    if (tiny) {
+                        badv[u] = v[u] != 0.0;
+                    } else {
+                        const double q = v[u] / U;  // exact (power-of-two scaling) unless huge
+                        if (!(fabs(q) < 4503599627370496.0)) {
+                            badv[u] = true;
+                        } else {
+                            const double m = floor(q);
+                            const double f = q - m;  // exact
+                            badv[u] = f == 0.5;  // a rounding tie: the result depends on s's last bit
+                            r[u] = static_cast<long long>(f > 0.5 ? m + 1.0 : m);
+                        }
+                    }
+                }
+                if (badv[u]) r[u] = 0;
+                loc += r[u];
+            }
+            long long x = loc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long y = __shfl_up_sync(kFull, x, o);
+                if (lane >= static_cast<uint32_t>(o)) x += y;
+            }
+            if (lane == 31) wsum[warp] = x;
+            if (tid == 0) s_bad = 0xffffffffu;
+            __syncthreads();
+            long long wpre = 0, tot = 0;
+            for (uint32_t w = 0; w < 8; ++w) {
+                if (w < warp) wpre += wsum[w];
+                tot += wsum[w];
+            }
+            long long run = wpre + (x - loc);
+            uint32_t first_bad = 0xffffffffu;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t i = tid * 8 + u;
+                if (i >= start && i < len && first_bad == 0xffffffffu) {
+                    const long long t = S0 + run + r[u];  // the partial after this element, in units of U
+                    const long long at = t < 0 ? -t : t;
+                    if (badv[u] || (!tiny && ((t < 0) != (S0 < 0) || at < kTwo52 || at >= kTwo53))) first_bad = i;
+                    run += r[u];
+                }
+            }
+            if (first_bad != 0xffffffffu) atomicMin(&s_bad, first_bad);
+            __syncthreads();
+            const uint32_t bad = s_bad;
+            if (bad == 0xffffffffu || bad >= len) {  // the whole rest of the tile stayed in the binade
+                if (tid == 0) s_run = tiny ? s0 : __dmul_rn(static_cast<double>(S0 + tot), U);
+                __syncthreads();
+                break;
+            }
+            if (tid == (bad >> 3)) {  // its predecessor's exact value, then one serial add
+                long long rb = wpre + (x - loc);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    if (tid * 8 + u < bad && tid * 8 + u >= start) rb += r[u];
+                }
+                const double prev = tiny ? s0 : __dmul_rn(static_cast<double>(S0 + rb), U);
+                s_run = __dadd_rn(prev, v[bad & 7u]);
+            }
+            __syncthreads();
+            start = bad + 1;
+        }
+    }
+    const double out = s_run;
+    __syncthreads();
+    return out;
+}
+
+__global__ void __launch_bounds__(256) update_fold_kernel(const float* __restrict__ proj, const KJob* __restrict__ jobs,
+                                                          uint64_t n, uint32_t k, const uint32_t* __restrict__ offsets,
+                                                          const uint32_t* __restrict__ perm, float* cent) {
+    const uint32_t j = blockIdx.y;
+    const KJob jb = jobs[j];
+    const uint32_t h = jb.h;
+    const uint32_t c = blockIdx.x / h, dim = blockIdx.x % h;
+    if (c >= k) return;
+    const uint32_t* off = offsets + uint64_t(j) * (k + 1);
+    const uint32_t b = off[c], e = off[c + 1];
+    if (b == e) return;  // empty: repaired by the caller
+    const uint32_t* pp = perm + uint64_t(j) * n + b;
+    const float* x = proj + jb.off + dim;
+    const double sum = fold_signed([&](uint32_t i) { return static_cast<double>(__ldg(x + uint64_t(__ldg(pp + i)) * h)); },
+                                   e - b);
+    if (threadIdx.x == 0) {
+        const double inv = 1.0 / static_cast<double>(e - b);
+        cent[jb.coff + uint64_t(c) * h + dim] = __double2float_rn(__dmul_rn(sum, inv));
+    }
+}
+
 // ------------------------------------------------------------------- repair
 struct FarArgs {
     uint32_t job, cluster;
@@ -1111,7 +1277,7 @@ void bucket_sort(const uint32_t* keys, uint64_t n, uint32_t B, uint32_t J, uint3
 
 void launch_assign(const float* proj, const KJob* jobs, uint64_t n, uint32_t k, uint32_t hmax, const float* cent,
                    uint32_t* assign, uint32_t J, cudaStream_t st) {
-    const size_t smem = size_t(k) * hmax * 8;
+    const size_t smem = size_t(k) * hmax * (hmax <= 32 ? 8 + 4 : 8);  // doubles (+ the fp32 screen's floats)
     if (smem > 200 * 1024) raise(SUCO_ERR_INTERNAL, "k x h centroid table exceeds shared memory");
     const dim3 g(grid_for(n, 256, 148 * 4), J);
     auto go = [&](auto kern) {
@@ -1204,8 +1370,12 @@ void kmeans_jobs(const float* proj, const std::vector<KJob>& host_jobs, const KJ
     for (uint32_t it = 0; it < iterations; ++it) {
         launch_assign(proj, jobs, n, k, hmax, cent, assign, J, st);
         bucket_sort(assign, n, k, J, offsets.p, perm.p, st);
-        update_kernel<<<dim3(grid_for(uint64_t(k) * hmax, 128, 1u << 30), J), 128, 0, st>>>(proj, jobs, n, k, offsets.p,
-                                                                                           perm.p, cent);
+        if (kpp_serial) {  // (A/B and tests: the one-thread-per-column fold)
+            update_kernel<<<dim3(grid_for(uint64_t(k) * hmax, 128, 1u << 30), J), 128, 0, st>>>(proj, jobs, n, k,
+                                                                                               offsets.p, perm.p, cent);
+        } else {
+            update_fold_kernel<<<dim3(k * hmax, J), 256, 0, st>>>(proj, jobs, n, k, offsets.p, perm.p, cent);
+        }
         BCUDA(cudaGetLastError());
         BCUDA(cudaMemcpyAsync(hoff.data(), offsets.p, hoff.size() * 4, cudaMemcpyDeviceToHost, st));
         BCUDA(cudaStreamSynchronize(st));
