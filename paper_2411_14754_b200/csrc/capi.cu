@@ -293,7 +293,9 @@ void finalize_dense(suco_gpu_index* x, bool allow_half) {
                     dense_half_supported(ns, x->K);
     if (x->dense_half) {
         x->dense = true;
-        const uint64_t n_pad = (n + kDensePiece - 1) / kDensePiece * kDensePiece;  // whole last piece
+        // whole last piece of any single-pass piece size, plus two 64-point tiles (the fused pass
+        // loads the codes two tiles ahead of the one it scores)
+        const uint64_t n_pad = (n + kMaxPiece - 1) / kMaxPiece * kMaxPiece + 128;
         x->codes.reserve(n_pad * 8);
         CUDA_TRY(launch_dense_codes_half(x->ids.p, x->cell_off.p, n, n_pad, ns, x->K, x->codes.p, x->own));
     } else if (x->dense) {
@@ -490,11 +492,10 @@ struct FbLists {
 // pass about sixteen CTAs per SM (32 pieces per CTA row, 32 queries per CTA). Measured per step:
 // cfg4 (10M points, 10K queries) 2048 / 8192 / 16384 -> 38.2 / 32.9 / 31.4 ms; cfg2 (1M, 10K)
 // 2048 / 4096 / 8192 -> 4.19 / 4.09 / 4.29 ms; small corpora or batches keep 2048 (cfg1, cfg3).
-uint32_t fused_piece(uint64_t n, uint64_t nq, uint32_t nc) {
+uint32_t fused_piece(uint64_t n, uint64_t nq, uint32_t qper) {
     int sms = 148, dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const uint64_t qblocks = (nq + 31) / 32;
-    (void)nc;
+    const uint64_t qblocks = (nq + qper - 1) / qper;  // queries per CTA: 32, 16 in the half-width mode
     for (uint32_t wp = 16384; wp > kDensePiece; wp /= 2) {
         const uint64_t P = (n + wp - 1) / wp;
         if (qblocks * ((P + 31) / 32) >= 16ull * sms) return wp;
@@ -535,8 +536,8 @@ FbLists stage_select(const suco_gpu_index* x, suco_gpu_query_ctx* c, suco_gpu_qu
             // are padded to whole 2048-point pieces): a quarter of the per-(query, piece) counts,
             // quotas and buffers, and buffers four times fuller, so far fewer partly written sectors
             // (measured at cfg4: fused pass writes and compaction reads)
-            if (!da.half) {
-                da.WP = tn.dense_piece ? tn.dense_piece : fused_piece(h.n, nt, h.layout.ns > 8 ? 2u : 1u);
+            if (!(da.half && da.pair)) {  // (the cluster-pair pass walks 2048-point pieces)
+                da.WP = tn.dense_piece ? tn.dense_piece : fused_piece(h.n, nt, da.half ? 16u : 32u);
                 da.P = static_cast<uint32_t>((h.n + da.WP - 1) / da.WP);
             }
             // two output offsets per (query, piece): score > T entries fill the front of the query's

@@ -978,15 +978,16 @@ struct RegionOff {
     }
 };
 
-__device__ __forceinline__ void planes_h(const uint16_t* M16, const RegionOff& ro, uint4 ca, uint4 cb,
-                                         uint32_t (&b)[4]) {
+__device__ __forceinline__ void masks_h(const uint16_t* M16, const RegionOff& ro, uint4 ca, uint4 cb, uint32_t (&m)[8]) {
     const uint32_t xa[4] = {ca.x, ca.y, ca.z, ca.w}, xb[4] = {cb.x, cb.y, cb.z, cb.w};
-    uint32_t m[8];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         m[2 * i] = uint32_t(M16[ro.o[2 * i] + (xa[i] & 0xffffu)]) | (uint32_t(M16[ro.o[2 * i] + (xb[i] & 0xffffu)]) << 16);
         m[2 * i + 1] = uint32_t(M16[ro.o[2 * i + 1] + (xa[i] >> 16)]) | (uint32_t(M16[ro.o[2 * i + 1] + (xb[i] >> 16)]) << 16);
     }
+}
+
+__device__ __forceinline__ void csa_h(const uint32_t (&m)[8], uint32_t (&b)[4]) {
     uint32_t s1, c1, s2, c2, b0, c4, s5, c5;
     fadd(m[0], m[1], m[2], s1, c1);
     fadd(m[3], m[4], m[5], s2, c2);
@@ -998,6 +999,13 @@ __device__ __forceinline__ void planes_h(const uint16_t* M16, const RegionOff& r
     b[1] = s5 ^ c4;
     b[2] = c5 ^ c6;
     b[3] = c5 & c6;
+}
+
+__device__ __forceinline__ void planes_h(const uint16_t* M16, const RegionOff& ro, uint4 ca, uint4 cb,
+                                         uint32_t (&b)[4]) {
+    uint32_t m[8];
+    masks_h(M16, ro, ca, cb, m);
+    csa_h(m, b);
 }
 
 // K1 (half width): per (query, piece) #points with score >= t, t = 1..8.
@@ -1143,17 +1151,22 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_h_kernel(DenseArg
         const uint64_t hi = min_u64(a.n, lo + a.WP);
         uint32_t cnt = 0, nb = 0;
         uint16_t* buf = cb_base(a, mine ? q0 + qj : q0, piece);
-        // 32-bit tile loop (the padded code rows cover a whole last piece)
+        // 32-bit tile loop (the padded code rows cover a whole last piece and one tile past it);
+        // the next tile's mask lookups are in flight while this tile is compared and emitted
         const uint32_t len = static_cast<uint32_t>(hi - lo);
         const uint4* cptr = a.codes + lo + lane;
-        uint4 ca = __ldg(cptr), cb = __ldg(cptr + 32);
+        uint32_t mk[8];
+        masks_h(M16, ro, __ldg(cptr), __ldg(cptr + 32), mk);
+        uint4 ca = __ldg(cptr + 64), cb = __ldg(cptr + 96);
+        // past every lane's tie cut only score > L is kept: one transpose per tile (the piece's
+        // #(score >= L) is recorded as #(score > L), as in fused_pieces)
+        const bool need_ge = __any_sync(kFull, piece < cut);
         for (uint32_t tb0 = 0; tb0 < len; tb0 += 64) {
             cptr += 64;
-            const bool more = tb0 + 64 < len;  // one tile ahead
-            const uint4 na = more ? __ldg(cptr) : ca;
-            const uint4 nbv = more ? __ldg(cptr + 32) : cb;
+            const uint4 na = __ldg(cptr + 64), nbv = __ldg(cptr + 96);
             uint32_t b[4];
-            planes_h(M16, ro, ca, cb, b);
+            csa_h(mk, b);
+            masks_h(M16, ro, ca, cb, mk);
             ca = na;
             cb = nbv;
             uint32_t gt = b[3] & ~T3, eq = ~(b[3] ^ T3);
@@ -1164,10 +1177,16 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_h_kernel(DenseArg
             gt |= eq & b[0] & ~T0;
             eq &= ~(b[0] ^ T0);
             // queries past the block's last have no live bits: their lanes see empty words
-            const uint32_t ge0 = xp((gt | eq) & live);
             const uint32_t g1 = xp(gt & live);
-            cnt += __popc(ge0) | (__popc(g1) << 16);
-            const uint32_t kept = piece < cut ? ge0 : g1;  // past the tie cut: score > L only
+            uint32_t kept = g1;
+            if (need_ge) {
+                const uint32_t ge0 = xp((gt | eq) & live);
+                cnt += __popc(ge0) | (__popc(g1) << 16);
+                if (piece < cut) kept = ge0;  // before the tie cut: every score >= L
+            } else {
+                const uint32_t c1 = __popc(g1);
+                cnt += c1 | (c1 << 16);
+            }
             const uint32_t c0 = __popc(kept), o0 = __shfl_xor_sync(kFull, c0, 16);
             uint32_t at = nb + (half ? o0 : 0u);
             const uint32_t tb = tb0 + 32 * half;
@@ -1180,7 +1199,7 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_h_kernel(DenseArg
             }
             nb += c0 + o0;
         }
-        cnt += __shfl_xor_sync(kFull, cnt, 16);  // packed 16-bit halves, each <= 2048
+        cnt += __shfl_xor_sync(kFull, cnt, 16);  // packed 16-bit halves, each <= WP
         if (half == 0 && mine) {
             const uint64_t i = (q0 + qj) * a.P + piece;
             a.h2[i] = cnt;

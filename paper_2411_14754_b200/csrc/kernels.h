@@ -161,7 +161,8 @@ cudaError_t launch_dense_emit(const DenseArgs& a, cudaStream_t st);
 constexpr uint32_t kDensePiece = 2048;  // points per piece (one warp)
 constexpr uint32_t kDenseBuf = 96;      // single-pass candidate buffer entries per 2048 points of a (piece, query)
 constexpr uint32_t kDenseCodePad = 128;  // zero-slot code rows past n (the fused pass loads two tiles ahead)
-constexpr uint32_t kFusedPiece = 8192;  // points per piece of the single-pass select (half-width mode: kDensePiece)
+constexpr uint32_t kFusedPiece = 8192;
+constexpr uint32_t kMaxPiece = 32768;   // largest single-pass piece (SUCO_DENSE_PIECE): 15-bit in-piece offsets  // points per piece of the single-pass select (half-width mode: kDensePiece)
 
 // ------------------------------------------------------------------ rerank
 // Exact fp64 re-rank of the candidate rows (query.cpp:159-197) with a
