@@ -49,6 +49,16 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+_JSON_OUT = None
+
+
+def emit(obj) -> None:
+    """The ONE JSON line the driver parses, on the process's original stdout (see main())."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(obj) + "\n")
+    out.flush()
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -185,7 +195,7 @@ def run_reference_arm(args, cfg):
         return
     from oracle.oracle import ref, ref_available
     if not ref_available():
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libsuco_ref.so not built"}))
+        emit({"impl": "reference", "unavailable": "oracle/_ref/libsuco_ref.so not built"})
         return
     R = ref()
     base, queries = bench_data.generate(cfg)
@@ -213,12 +223,16 @@ def run_reference_arm(args, cfg):
                                    f"parallel_chunks over {threads} threads; index build {build_s:.1f} s"},
         "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def main():
-    # the driver parses ONE JSON line from stdout: NCCL's own messages go to stderr
-    os.environ.setdefault("NCCL_DEBUG", "WARN")
+    # the driver parses ONE JSON line from stdout: everything else written to file descriptor 1 (NCCL's
+    # version banner, native libraries) is sent to stderr, and the JSON line goes to the original stdout
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -266,9 +280,9 @@ def main():
 
     if args.impl == "reference":
         if sampled:
-            print(json.dumps({"impl": "reference", "unavailable": f"{cfg.name}'s sampled build has no reference "
-                              "API (bench.py --config {cfg.name} reports the reference knn_query on the GPU-built "
-                              "index as its cpu_baseline)"}))
+            emit({"impl": "reference", "unavailable": f"{cfg.name}'s sampled build has no reference "
+                              f"API (bench.py --config {cfg.name} reports the reference knn_query on the GPU-built "
+                              "index as its cpu_baseline)"})
             return
         run_reference_arm(args, cfg)
         return
@@ -541,7 +555,7 @@ def main():
         "gpu_launches": launches_per_step * args.steps, "clocks": clocks.summary(),
     }
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     if ws > 1:
         torch.distributed.destroy_process_group()
 
@@ -662,7 +676,7 @@ def run_sharded(args, cfg, ws, rank, local):
         "gpu_launches": launches * args.steps, "clocks": clocks.summary(),
     }
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     dist.destroy_process_group()
 
 
@@ -707,10 +721,9 @@ def run_emulated(args, cfg):
                                                          outs_d[r][0].data_ptr(), outs_d[r][1].data_ptr(),
                                                          scratch=ctxs[r]), ctxs[r].synchronize()), G)
     wall = time.time() - t0
-    print(json.dumps({"emulate": G, "workload": cfg.describe(), "block": block, "sharded_build_equals_cut": same_build,
+    emit({"emulate": G, "workload": cfg.describe(), "block": block, "sharded_build_equals_cut": same_build,
                       "build_s_emulated": build_s, "ranks_bit_identical_to_unsharded": ok,
-                      "exchange_bytes_per_rank": ctxs[0].exchange_bytes(), "wall_s_all_ranks_one_gpu": wall}),
-          flush=True)
+                      "exchange_bytes_per_rank": ctxs[0].exchange_bytes(), "wall_s_all_ranks_one_gpu": wall})
     for c in comms:
         c.close()
 
