@@ -74,6 +74,7 @@ suco_gpu_query_ctx::~suco_gpu_query_ctx() {
     }
     sh_tot.release(), sh_tot_all.release(), sh_ties.release(), sh_ties_all.release(), sh_qblk.release();
     sh_counts.release(), sh_ids.release(), sh_ids_all.release(), sh_need.release(), sh_sq.release(), sh_sq_all.release();
+    sh_s17.release(), sh_gt.release(), sh_gts.release(), sh_nflag.release();
     stat_cum.release();
     for (cudaStream_t t : pipe) {
         if (t) cudaStreamDestroy(t);
@@ -477,17 +478,6 @@ void rerank_args(const suco_gpu_index* x, RerankArgs& ra) {
     ra.pipe = x->tune.rerank_pipe == 2 ? 0 : x->tune.rerank_pipe == 1 ? 1 : 2;
 }
 
-}  // namespace suco_gpu
-
-namespace {
-
-// The dense select's fallback lists (qflag: nq flags; qmap[0 .. *nmap): the flagged queries).
-struct FbLists {
-    const uint32_t* qflag = nullptr;
-    const uint32_t* qmap = nullptr;
-    const uint32_t* nmap = nullptr;
-};
-
 // Points per piece of the single pass: the largest of 16384 .. 2048 that still gives the fused
 // pass about sixteen CTAs per SM (32 pieces per CTA row, 32 queries per CTA). Measured per step:
 // cfg4 (10M points, 10K queries) 2048 / 8192 / 16384 -> 38.2 / 32.9 / 31.4 ms; cfg2 (1M, 10K)
@@ -502,6 +492,18 @@ uint32_t fused_piece(uint64_t n, uint64_t nq, uint32_t qper) {
     }
     return kDensePiece;
 }
+
+}  // namespace suco_gpu
+
+namespace {
+
+// The dense select's fallback lists (qflag: nq flags; qmap[0 .. *nmap): the flagged queries).
+struct FbLists {
+    const uint32_t* qflag = nullptr;
+    const uint32_t* qmap = nullptr;
+    const uint32_t* nmap = nullptr;
+};
+
 
 // Bytes of single-pass candidate buffers beyond kDenseBuf entries (small batches): at most 1 GB.
 constexpr uint64_t kDenseBufExtra = 1ull << 30;

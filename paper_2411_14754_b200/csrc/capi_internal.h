@@ -140,6 +140,7 @@ struct suco_gpu_query_ctx {
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     // shard protocol scratch (capi_shard.cu)
     suco_gpu::DevBuf<uint32_t> sh_tot, sh_tot_all, sh_ties, sh_ties_all, sh_qblk, sh_counts, sh_ids, sh_ids_all;
+    suco_gpu::DevBuf<uint32_t> sh_s17, sh_gt, sh_gts, sh_nflag;  // shard single pass: sampled totals, #(> L), flags
     suco_gpu::DevBuf<uint64_t> sh_need;
     suco_gpu::DevBuf<double> sh_sq, sh_sq_all;
     uint64_t exchange_bytes = 0;  // bytes this rank sent through the communicator in the last call
@@ -210,6 +211,8 @@ void begin_call(suco_gpu_query_ctx* c, uint64_t nq, uint64_t m, cudaStream_t st)
 void stage_traverse(const suco_gpu_index* x, suco_gpu_query_ctx* c, suco_gpu_query_ctx::Slot& sl, const float* d_q,
                     uint64_t nt, uint64_t target, cudaStream_t st, double* dbg_sum, uint64_t* dbg_cum, bool profiled);
 DenseArgs dense_args(const suco_gpu_index* x, suco_gpu_query_ctx::Slot& sl, uint64_t nq);
+// points per piece of the dense single pass for n points and nq queries (qper queries per CTA)
+uint32_t fused_piece(uint64_t n, uint64_t nq, uint32_t qper);
 void rerank_args(const suco_gpu_index* x, RerankArgs& ra);
 
 // Device upload pieces shared by build / load / shard (capi.cu).

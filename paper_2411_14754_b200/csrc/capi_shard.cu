@@ -21,6 +21,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -56,6 +57,102 @@ void finalize_shard(suco_gpu_index* x) {
     set_l2_persisting(x);
 }
 
+// The protocol's select as ONE scoring pass (dense.cu, "the shard protocol's single pass"): the
+// sampled totals are summed over the shards so every shard takes the same speculative bound L and
+// tie cut, the fused pass scores the shard's pieces once, #(score > L) is summed and the per-block
+// ties gathered, and the plan cuts the reference's global top-m exactly. Returns false — after
+// every shard agreed on it — when any shard flagged a query (T != L, a quota past the cut, an
+// overflowing buffer); the caller then runs the two-pass protocol for the tile.
+bool shard_fused_select(const suco_gpu_index* x, suco_gpu_query_ctx* c, suco_gpu_query_ctx::Slot& sl, suco_comm* comm,
+                        uint64_t nt, uint64_t m, uint32_t G, uint32_t r, uint64_t nb, uint32_t nbl, uint32_t nbl_max,
+                        cudaStream_t s) {
+    const HostIndex& h = x->host;
+    const Tuning& tn = x->tune;
+    if (!x->dense || nt == 0) return false;
+    DenseArgs da = dense_args(x, sl, nt);
+    da.m = m;
+    // pieces: the unsharded path's choice over the shard's points, dividing the id block
+    uint32_t wp = tn.dense_piece ? tn.dense_piece : fused_piece(h.n, nt, da.half ? 16u : 32u);
+    while (wp > kDensePiece && x->block % wp) wp /= 2;
+    if (x->block % wp) return false;
+    da.WP = wp;
+    da.P = static_cast<uint32_t>((h.n + wp - 1) / wp);
+    const uint32_t ppbf = x->block / wp;
+    const uint32_t P_global = static_cast<uint32_t>((x->n_global + wp - 1) / wp);
+    da.shG = G;
+    da.shR = r;
+    da.shPPB = ppbf;
+    const uint32_t P2 = static_cast<uint32_t>((h.n + kDensePiece - 1) / kDensePiece);
+    da.sWP = kDensePiece;
+    da.pstride = P2 <= 64 ? 1u : std::min<uint32_t>(64, P2 / 16);
+    da.Ps = (P2 + da.pstride - 1) / da.pstride;
+    sl.dsample.reserve(nt * da.Ps * 8 * da.nc);
+    da.hsample = sl.dsample.p;
+    const uint64_t fit = (1ull << 30) / (2ull * nt * da.P) / 8 * 8;
+    const uint64_t minb = uint64_t(kDenseBuf) * (da.WP / kDensePiece);
+    da.B = static_cast<uint32_t>(std::min<uint64_t>(da.WP, std::max<uint64_t>(minb, fit)));
+    if (tn.dense_buf) da.B = tn.dense_buf;
+    sl.dcbuf.reserve(nt * da.P * da.B);
+    sl.dccnt.reserve(nt * da.P);
+    sl.dL.reserve(nt);
+    sl.dh2.reserve(nt * da.P);
+    sl.dT.reserve(nt);
+    sl.dquota.reserve(nt * da.P);
+    sl.dbase.reserve(2 * nt * da.P);
+    sl.dflag.reserve(5 * nt + 3);
+    da.cbuf = sl.dcbuf.p;
+    da.ccnt = sl.dccnt.p;
+    da.L = sl.dL.p;
+    da.h2 = sl.dh2.p;
+    da.T = sl.dT.p;
+    da.quota = sl.dquota.p;
+    da.base = sl.dbase.p;
+    da.base2 = sl.dbase.p + nt * da.P;
+    da.qflag = sl.dflag.p;
+    da.pcut = sl.dflag.p + 2 * nt + 1;
+    da.clist = sl.dflag.p + 3 * nt + 1;
+    da.nclist = sl.dflag.p + 5 * nt + 1;
+    da.stage_all = tn.dense_stage;
+    da.no_cut = tn.dense_nocut;
+    da.compact_mode = tn.dense_compact;
+    da.compact_rows = tn.dense_compact_rows;
+    da.cands = sl.cands.p;
+    c->sh_s17.reserve(nt * 17);
+    c->sh_gt.reserve(nt);
+    c->sh_gts.reserve(nt);
+    c->sh_nflag.reserve(1);
+    c->sh_ties.reserve(nt * nbl_max);
+    c->sh_ties_all.reserve(G * nt * nbl_max);
+    c->sh_qblk.reserve(nt * nbl_max);
+    // S0: the same L and tie cut on every shard
+    CUDA_TRY(launch_shard_sample(da, c->sh_s17.p, s));
+    comm->allreduce_sum_u32(c->sh_s17.p, nt * 17, s);
+    CUDA_TRY(launch_shard_bound(da, c->sh_s17.p, x->n_global, P_global, s));
+    // S1: one scoring pass over the shard's pieces
+    CUDA_TRY(launch_dense_fused_pass(da, s));
+    // S2: #(score > L) summed, the blocks' ties gathered
+    CUDA_TRY(launch_shard_fused_sums(da, ppbf, nbl, nbl_max, c->sh_gt.p, c->sh_ties.p, s));
+    CUDA_TRY(cudaMemcpyAsync(c->sh_gts.p, c->sh_gt.p, nt * 4, cudaMemcpyDeviceToDevice, s));
+    comm->allreduce_sum_u32(c->sh_gts.p, nt, s);
+    comm->allgather(c->sh_ties.p, c->sh_ties_all.p, nt * nbl_max * 4, s);
+    // S3: the plan; any flag on any shard sends the tile to the two-pass protocol
+    CUDA_TRY(cudaMemsetAsync(c->sh_nflag.p, 0, 4, s));
+    CUDA_TRY(launch_shard_fused_plan(da, c->sh_gts.p, c->sh_gt.p, c->sh_ties_all.p, G, r, nb, ppbf, nbl, nbl_max,
+                                     c->sh_qblk.p, c->sh_counts.p, c->sh_nflag.p, s));
+    comm->allreduce_sum_u32(c->sh_nflag.p, 1, s);
+    uint32_t nflag = 0;
+    CUDA_TRY(cudaMemcpyAsync(&nflag, c->sh_nflag.p, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    c->launches += 8;
+    if (tn.dense_stats)
+        std::fprintf(stderr, "[suco] shard %u/%u single pass: %u flagged queries of %llu (all shards)%s\n", r, G, nflag,
+                     static_cast<unsigned long long>(nt), nflag ? ": two-pass protocol for the tile" : "");
+    if (nflag) return false;
+    CUDA_TRY(launch_dense_compaction(da, s));
+    c->launches += 2;
+    return true;
+}
+
 // The protocol over one query batch (all ranks call it with the same queries and params).
 void shard_run(const suco_gpu_index* x, suco_gpu_query_ctx* c, suco_comm* comm, const float* h_q, const float* d_q,
                uint64_t nq, uint32_t qlen, const suco_collision_params* p, uint32_t* d_ids, double* d_dists,
@@ -75,7 +172,8 @@ void shard_run(const suco_gpu_index* x, suco_gpu_query_ctx* c, suco_comm* comm, 
     const uint64_t P = (x->host.n + kDensePiece - 1) / kDensePiece;
     const uint64_t nc = x->host.layout.ns > 8 ? 2 : 1;
     const uint64_t per = uint64_t(x->host.layout.ns) * x->K * 4 + 64 + m * 4 + (k > 32 ? m * 12 : 0) + qlen * 4 +
-                         uint64_t(G) * (64 + nbl_max * 4 + k * 12) + nbl_max * 8 + P * (16 * nc + 8) + k * 12;
+                         uint64_t(G) * (64 + nbl_max * 4 + k * 12) + nbl_max * 8 + P * (16 * nc + 8) + k * 12 +
+                         P * (14 + 2 * kDenseBuf) + 128 * 16 * nc + G * 68 + 32;  // + the single pass's buffers
     // the tile count is agreed once per (nq, m, k) and cached (the agreement is a host round trip)
     if (c->sh_key[0] != nq || c->sh_key[1] != m || c->sh_key[2] != k || !c->sh_tiles) {
         uint64_t budget = x->tune.scratch_bytes;
@@ -105,6 +203,11 @@ void shard_run(const suco_gpu_index* x, suco_gpu_query_ctx* c, suco_comm* comm, 
             tq = sl.q.p;
         }
         stage_traverse(x, c, sl, tq, nt, target, s, nullptr, nullptr, true);
+        c->sh_counts.reserve(nt);
+        sl.cands.reserve(nt * m);
+        const bool fused = x->tune.dense_fused && !(x->dense_half && x->tune.dense_pair) &&
+                           shard_fused_select(x, c, sl, comm, nt, m, G, r, nb, nbl, nbl_max, s);
+        if (!fused) {
         DenseArgs da = dense_args(x, sl, nt);
         da.m = m;
         sl.dhist.reserve(nt * da.P * 8 * da.nc);
@@ -134,6 +237,7 @@ void shard_run(const suco_gpu_index* x, suco_gpu_query_ctx* c, suco_comm* comm, 
                                     c->sh_counts.p, s));
         CUDA_TRY(launch_dense_emit(da, s));
         c->launches += 5;
+        }
         // local exact re-rank, global ids, exchange 3, merge
         c->sh_ids.reserve(nt * k);
         c->sh_sq.reserve(nt * k);

@@ -354,6 +354,11 @@ __device__ __forceinline__ uint32_t level_n(const uint4* row, uint32_t t) {
 
 __device__ __forceinline__ uint32_t nc_of(const DenseArgs& a) { return a.nc ? a.nc : 1u; }
 
+// The global piece index of local piece p (tie cuts are in global id order; block-cyclic shards).
+__device__ __forceinline__ uint32_t gpiece(const DenseArgs& a, uint32_t p) {
+    return a.shG ? ((p / a.shPPB) * a.shG + a.shR) * a.shPPB + p % a.shPPB : p;
+}
+
 // Which single-pass compaction kernel takes query q: the warp kernel for dense supersets (the L[q]
 // flag of the bound kernel), the thread kernel for sparse ones (Tuning::dense_compact forces either).
 __device__ __forceinline__ bool dense_compact_warp(const DenseArgs& a, uint64_t q) {
@@ -572,13 +577,60 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_emit_kernel(DenseArgs a
 }
 
 // K0 -> L: per query, the largest t whose sampled #(score >= t), scaled to n, reaches m (0 if none).
-__global__ void __launch_bounds__(256) dense_bound_kernel(DenseArgs a) {
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint64_t q = uint64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
-    if (q >= a.nq) return;
+// L (the speculative T), the dense-superset flag and the tie cut of one query from its sampled
+// totals tot[t - 1] = #(score >= t) over `sampled` points of a corpus of n points in P pieces.
+struct Bound {
+    uint32_t L, cut;
+    bool dense;
+};
+__device__ __forceinline__ Bound bound_core(const DenseArgs& a, const uint32_t (&tot)[16], uint64_t sampled,
+                                            uint64_t n, uint32_t P) {
+    const uint32_t LV = 8 * nc_of(a);
+    uint32_t L = 0;
+    uint32_t atL = 0;
+#pragma unroll
+    for (int t = 16; t >= 1; --t) {
+        if (L == 0 && static_cast<uint32_t>(t) <= min(a.ns, LV) && sampled &&
+            static_cast<double>(tot[t - 1]) * static_cast<double>(n) / static_cast<double>(sampled) >=
+                static_cast<double>(a.m)) {
+            L = t;
+            atL = tot[t - 1];
+        }
+    }
+    // The single pass writes one 8-byte record per tile holding a point with score >= L, at most
+    // 0.25 B per (point, query) even when every tile has one; a second scoring pass costs more.
+    // dense supersets (> 1% of the points at L) make the fused pass stage its stores
+    const bool dense = L && (a.stage_all || static_cast<double>(atL) > 0.01 * static_cast<double>(sampled));
+    // Tie cut: the quota takes the first `need` score == L points in id order, so the fused pass
+    // stores tie entries only in the pieces the quota is expected to reach (x1.25 + 8 pieces of
+    // margin); later pieces keep just their score > L entries. A quota that reaches past the cut
+    // flags the query for the exact fallback.
+    uint32_t cut = P;
+    if (L && sampled && a.pcut && !a.no_cut) {
+        uint32_t above = 0;  // sampled #(score >= L + 1)
+#pragma unroll
+        for (int t = 1; t <= 16; ++t) {
+            if (static_cast<uint32_t>(t) == L + 1 && static_cast<uint32_t>(t) <= LV) above = tot[t - 1];
+        }
+        const double scale = static_cast<double>(n) / static_cast<double>(sampled);
+        const double ties = (static_cast<double>(atL) - static_cast<double>(above)) * scale;
+        const double need = static_cast<double>(a.m) - static_cast<double>(above) * scale;
+        if (ties > 0.0 && need < ties) {
+            const double cs = a.cut_scale > 0.f ? static_cast<double>(a.cut_scale) : 1.25;
+            // (+8 pieces of 2048 points: the pad is in points, whatever the piece size)
+            const double cp = a.cut_scale > 0.f ? static_cast<double>(a.cut_pad) : 8.0 * kDensePiece / a.WP;
+            const double c = static_cast<double>(P) * (need > 0.0 ? need / ties : 0.0) * cs + cp;
+            cut = c < static_cast<double>(P) ? static_cast<uint32_t>(c) : P;
+        }
+    }
+    return {L, cut, dense};
+}
+
+// The sampled totals of one query (warp): tot[t - 1] = #(score >= t) over the sampled pieces, and
+// the number of points they scanned.
+__device__ __forceinline__ uint64_t sample_totals(const DenseArgs& a, uint64_t q, uint32_t lane, uint32_t (&tot)[16]) {
     const uint32_t nc = nc_of(a), LV = 8 * nc;
     const uint4* h = reinterpret_cast<const uint4*>(a.hsample) + q * a.Ps * nc;
-    uint32_t tot[16];
 #pragma unroll
     for (int t = 0; t < 16; ++t) tot[t] = 0;
     for (uint32_t p = lane; p < a.Ps; p += 32) {
@@ -598,46 +650,19 @@ __global__ void __launch_bounds__(256) dense_bound_kernel(DenseArgs a) {
         const uint64_t lo = uint64_t(p) * a.pstride * swp;
         if (lo < a.n) sampled += min_u64(swp, a.n - lo);
     }
-    uint32_t L = 0;
-    uint32_t atL = 0;
-#pragma unroll
-    for (int t = 16; t >= 1; --t) {
-        if (L == 0 && static_cast<uint32_t>(t) <= min(a.ns, LV) && sampled &&
-            static_cast<double>(tot[t - 1]) * static_cast<double>(a.n) / static_cast<double>(sampled) >=
-                static_cast<double>(a.m)) {
-            L = t;
-            atL = tot[t - 1];
-        }
-    }
-    // The single pass writes one 8-byte record per tile holding a point with score >= L, at most
-    // 0.25 B per (point, query) even when every tile has one; a second scoring pass costs more.
-    // dense supersets (> 1% of the points at L) make the fused pass stage its stores
-    const bool dense = L && (a.stage_all || static_cast<double>(atL) > 0.01 * static_cast<double>(sampled));
-    // Tie cut: the quota takes the first `need` score == L points in id order, so the fused pass
-    // stores tie entries only in the pieces the quota is expected to reach (x1.25 + 8 pieces of
-    // margin); later pieces keep just their score > L entries. A quota that reaches past the cut
-    // flags the query for the exact fallback.
-    uint32_t cut = a.P;
-    if (L && sampled && a.pcut && !a.no_cut) {
-        uint32_t above = 0;  // sampled #(score >= L + 1)
-#pragma unroll
-        for (int t = 1; t <= 16; ++t) {
-            if (static_cast<uint32_t>(t) == L + 1 && static_cast<uint32_t>(t) <= LV) above = tot[t - 1];
-        }
-        const double scale = static_cast<double>(a.n) / static_cast<double>(sampled);
-        const double ties = (static_cast<double>(atL) - static_cast<double>(above)) * scale;
-        const double need = static_cast<double>(a.m) - static_cast<double>(above) * scale;
-        if (ties > 0.0 && need < ties) {
-            const double cs = a.cut_scale > 0.f ? static_cast<double>(a.cut_scale) : 1.25;
-            // (+8 pieces of 2048 points: the pad is in points, whatever the piece size)
-            const double cp = a.cut_scale > 0.f ? static_cast<double>(a.cut_pad) : 8.0 * kDensePiece / a.WP;
-            const double c = static_cast<double>(a.P) * (need > 0.0 ? need / ties : 0.0) * cs + cp;
-            cut = c < static_cast<double>(a.P) ? static_cast<uint32_t>(c) : a.P;
-        }
-    }
+    return sampled;
+}
+
+__global__ void __launch_bounds__(256) dense_bound_kernel(DenseArgs a) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t q = uint64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (q >= a.nq) return;
+    uint32_t tot[16];
+    const uint64_t sampled = sample_totals(a, q, lane, tot);
+    const Bound b = bound_core(a, tot, sampled, a.n, a.P);
     if (lane == 0) {
-        a.L[q] = L | (dense ? kDenseStage : 0u);
-        if (a.pcut) a.pcut[q] = cut;
+        a.L[q] = b.L | (b.dense ? kDenseStage : 0u);
+        if (a.pcut) a.pcut[q] = b.cut;
     }
 }
 
@@ -681,8 +706,9 @@ __device__ __forceinline__ void fused_pieces(const DenseArgs& a, const uint32_t*
         // instead of two; their #(score >= L) is not needed by the plan (its ties are never taken:
         // a quota that reaches past the cut flags the query) and is recorded as #(score > L).
         bool need_ge = false;
+        const uint32_t gp = gpiece(a, piece);
 #pragma unroll
-        for (uint32_t w = 0; w < W; ++w) need_ge |= piece < cut[w];
+        for (uint32_t w = 0; w < W; ++w) need_ge |= gp < cut[w];
         need_ge = __any_sync(kFull, need_ge);
         for (uint32_t tb = 0; tb < len; tb += 32) {
             cptr += 32 * NC;
@@ -706,7 +732,7 @@ __device__ __forceinline__ void fused_pieces(const DenseArgs& a, const uint32_t*
                 if (need_ge) {
                     const uint32_t ge0 = xp((gt | eq) & live[w]);
                     cnt[w] += __popc(ge0) | (__popc(g1) << 16);
-                    if (piece < cut[w]) bits = ge0;  // before the tie cut: every score >= L
+                    if (gp < cut[w]) bits = ge0;  // before the tie cut: every score >= L
                 } else {
                     const uint32_t c1 = __popc(g1);
                     cnt[w] += c1 | (c1 << 16);
@@ -1160,7 +1186,8 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_h_kernel(DenseArg
         uint4 ca = __ldg(cptr + 64), cb = __ldg(cptr + 96);
         // past every lane's tie cut only score > L is kept: one transpose per tile (the piece's
         // #(score >= L) is recorded as #(score > L), as in fused_pieces)
-        const bool need_ge = __any_sync(kFull, piece < cut);
+        const uint32_t gp = gpiece(a, piece);
+        const bool need_ge = __any_sync(kFull, gp < cut);
         for (uint32_t tb0 = 0; tb0 < len; tb0 += 64) {
             cptr += 64;
             const uint4 na = __ldg(cptr + 64), nbv = __ldg(cptr + 96);
@@ -1182,7 +1209,7 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_h_kernel(DenseArg
             if (need_ge) {
                 const uint32_t ge0 = xp((gt | eq) & live);
                 cnt += __popc(ge0) | (__popc(g1) << 16);
-                if (piece < cut) kept = ge0;  // before the tie cut: every score >= L
+                if (gp < cut) kept = ge0;  // before the tie cut: every score >= L
             } else {
                 const uint32_t c1 = __popc(g1);
                 cnt += c1 | (c1 << 16);
@@ -1610,35 +1637,28 @@ static cudaError_t launch_fused_pair(const DenseArgs& a, cudaStream_t st) {
     return cudaLaunchKernelEx(&cfg, kern, b);
 }
 
-cudaError_t launch_dense_select_fused(const DenseArgs& args, cudaStream_t st, cudaEvent_t main_done,
-                                      cudaStream_t fb_st) {
-    if (args.nq == 0) return cudaSuccess;
-    DenseArgs a = args;  // every pass but the fallback emission sees the queries unmapped
-    a.qmap = nullptr;
-    // K0: histograms of every pstride-th piece, then the speculative bound L per query
+// K0 of the single pass: histograms of every pstride-th short piece.
+cudaError_t launch_dense_sample(const DenseArgs& a, cudaStream_t st) {
     DenseArgs s0 = a;
+    s0.qmap = nullptr;
     s0.P = a.Ps;
     s0.hist = a.hsample;
     if (a.sWP) s0.WP = a.sWP;  // short sampled pieces: many warps per CTA row, few tiles each
-    cudaError_t e = launch_dense_hist(s0, st);
-    if (e != cudaSuccess) return e;
-    dense_bound_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(a);
-    // K3': histograms + supersets in one pass
-    if (a.half && a.pair) {
-        e = launch_fused_pair(a, st);
-    } else if (a.half) {
-        e = launch_h<2>(a, st);
-    } else {
-        const Shape sh = dense_shape(a);
-        if (a.nc == 2) e = sh.threads == 512 ? launch_fused_t<512, 1, 2>(a, sh.smem, st) : launch_fused_t<1024, 1, 2>(a, sh.smem, st);
-        else if (sh.words == 2) e = launch_fused_t<1024, 2>(a, sh.smem, st);
-        else e = sh.threads == 512 ? launch_fused_t<512, 1>(a, sh.smem, st) : launch_fused_t<1024, 1>(a, sh.smem, st);
-    }
-    if (e != cudaSuccess) return e;
-    // plan (+ fallback flags and the compaction work lists) from the two levels, compaction
-    e = cudaMemsetAsync(a.nclist, 0, 2 * sizeof(uint32_t), st);
-    if (e != cudaSuccess) return e;
-    dense_plan_fused_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(a);
+    return launch_dense_hist(s0, st);
+}
+
+// K3' of the single pass: the fused histogram + superset pass (kernel by table shape).
+cudaError_t launch_dense_fused_pass(const DenseArgs& a, cudaStream_t st) {
+    if (a.half && a.pair) return launch_fused_pair(a, st);
+    if (a.half) return launch_h<2>(a, st);
+    const Shape sh = dense_shape(a);
+    if (a.nc == 2) return sh.threads == 512 ? launch_fused_t<512, 1, 2>(a, sh.smem, st) : launch_fused_t<1024, 1, 2>(a, sh.smem, st);
+    if (sh.words == 2) return launch_fused_t<1024, 2>(a, sh.smem, st);
+    return sh.threads == 512 ? launch_fused_t<512, 1>(a, sh.smem, st) : launch_fused_t<1024, 1>(a, sh.smem, st);
+}
+
+// K4 of the single pass: the compaction kernels over the plan's work lists.
+cudaError_t launch_dense_compaction(const DenseArgs& a, cudaStream_t st) {
     const unsigned qrows = static_cast<unsigned>(min_u64(a.nq, 1024));  // rows walk the work lists
     if (a.compact_mode != 2) dense_compact_thread_kernel<<<dim3((a.P + 255) / 256, qrows), 256, 0, st>>>(a);  // sparse
     if (a.compact_mode != 1) {  // dense supersets: a warp per (query, piece); rows walk the work list
@@ -1646,6 +1666,27 @@ cudaError_t launch_dense_select_fused(const DenseArgs& args, cudaStream_t st, cu
         const unsigned wrows = static_cast<unsigned>(min_u64(a.nq, a.compact_rows ? a.compact_rows : 1024));
         dense_compact_kernel<<<dim3((a.P + 7) / 8, wrows), 256, 0, st>>>(a);
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dense_select_fused(const DenseArgs& args, cudaStream_t st, cudaEvent_t main_done,
+                                      cudaStream_t fb_st) {
+    if (args.nq == 0) return cudaSuccess;
+    DenseArgs a = args;  // every pass but the fallback emission sees the queries unmapped
+    a.qmap = nullptr;
+    // K0: histograms of every pstride-th piece, then the speculative bound L per query
+    cudaError_t e = launch_dense_sample(a, st);
+    if (e != cudaSuccess) return e;
+    dense_bound_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(a);
+    // K3': histograms + supersets in one pass
+    e = launch_dense_fused_pass(a, st);
+    if (e != cudaSuccess) return e;
+    // plan (+ fallback flags and the compaction work lists) from the two levels, compaction
+    e = cudaMemsetAsync(a.nclist, 0, 2 * sizeof(uint32_t), st);
+    if (e != cudaSuccess) return e;
+    dense_plan_fused_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(a);
+    e = launch_dense_compaction(a, st);
+    if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(args.nmap, 0, 4, st);
     if (e != cudaSuccess) return e;
     dense_flag_list_kernel<<<static_cast<unsigned>((a.nq + 255) / 256), 256, 0, st>>>(args);
@@ -1826,6 +1867,191 @@ __global__ void __launch_bounds__(256) shard_quota_kernel(DenseArgs a, const uin
         out_run += __shfl_sync(kFull, x, 31);
     }
     if (lane == 0) counts[q] = static_cast<uint32_t>(out_run);
+}
+
+// ---- the shard protocol's single pass (the unsharded path's K0 / bound / fused pass / plan /
+// compaction, with the speculative bound and the tie quotas agreed across shards):
+//   S0 every shard's sampled totals (17 u32 per query) -> all-reduce (sum) -> shard_bound_kernel:
+//      the same L and the same tie cut (in GLOBAL pieces) on every shard;
+//   S1 the fused pass over the shard's pieces (tie cuts compared in global piece order, gpiece);
+//   S2 per query #(score > L) of the shard -> all-reduce; per local block the ties counted before
+//      the cut -> all-gather;
+//   S3 shard_fused_plan_kernel: need = m - #(score > L), the first `need` ties in GLOBAL id order
+//      give each block its quota (shard_quota_kernel's rule), split over the block's pieces in id
+//      order; offsets (score > L first, then the ties) and the shard's candidate count; a query
+//      whose quota reaches past the cut or whose contributing buffer overflowed is flagged, and a
+//      flag on any shard sends the whole tile through the two-pass protocol above.
+__global__ void __launch_bounds__(256) shard_sample_kernel(DenseArgs a, uint32_t* out) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t q = uint64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (q >= a.nq) return;
+    uint32_t tot[16];
+    const uint64_t sampled = sample_totals(a, q, lane, tot);
+    if (lane < 17) {
+        uint32_t v = static_cast<uint32_t>(sampled);
+#pragma unroll
+        for (int t = 0; t < 16; ++t) v = lane == static_cast<uint32_t>(t) ? tot[t] : v;
+        out[q * 17 + lane] = v;
+    }
+}
+
+__global__ void __launch_bounds__(256) shard_bound_kernel(DenseArgs a, const uint32_t* sum17, uint64_t n_global,
+                                                          uint32_t P_global) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t q = uint64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (q >= a.nq) return;
+    uint32_t tot[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) tot[t] = sum17[q * 17 + t];
+    const Bound b = bound_core(a, tot, sum17[q * 17 + 16], n_global, P_global);
+    if (lane == 0) {
+        a.L[q] = b.L | (b.dense ? kDenseStage : 0u);
+        a.pcut[q] = b.cut;
+    }
+}
+
+// gt[q] = the shard's #(score > L); ties[q][lb] = its block lb's ties at L counted by the fused pass
+// (pieces past every tie cut of their CTA recorded none).
+__global__ void __launch_bounds__(256) shard_fused_sums_kernel(DenseArgs a, uint32_t ppb, uint32_t nbl,
+                                                               uint32_t nbl_max, uint32_t* gt, uint32_t* ties) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t q = uint64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (q >= a.nq) return;
+    const uint32_t* h = a.h2 + q * a.P;
+    uint32_t g = 0;
+    for (uint32_t lb = lane; lb < nbl_max; lb += 32) {
+        uint32_t t = 0;
+        if (lb < nbl) {
+            for (uint32_t p = lb * ppb; p < min(a.P, (lb + 1) * ppb); ++p) {
+                const uint32_t v = h[p];
+                g += v >> 16;
+                t += (v & 0xffffu) - (v >> 16);
+            }
+        }
+        ties[q * nbl_max + lb] = t;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) g += __shfl_xor_sync(kFull, g, o);
+    if (lane == 0) gt[q] = g;
+}
+
+__global__ void __launch_bounds__(256) shard_fused_plan_kernel(DenseArgs a, const uint32_t* gt_sum, const uint32_t* gt_local,
+                                                               const uint32_t* ties_all, uint32_t G, uint32_t shard,
+                                                               uint64_t nb_global, uint32_t ppb, uint32_t nbl,
+                                                               uint32_t nbl_max, uint32_t* qblk, uint32_t* counts,
+                                                               uint32_t* nflag) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t q = uint64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (q >= a.nq) return;
+    const uint32_t L = a.L[q] & 0xffu;
+    const uint64_t geL1 = gt_sum[q];  // global #(score > L)
+    bool ok = L >= 1 && geL1 < a.m;
+    const uint64_t need = ok ? a.m - geL1 : 0;
+    // block quotas in global id order (block j on shard j % G, local block j / G)
+    uint64_t run = 0;
+    for (uint64_t j0 = 0; j0 < nb_global; j0 += 32) {
+        const uint64_t j = j0 + lane;
+        const uint32_t t = j < nb_global ? ties_all[(uint64_t(j % G) * a.nq + q) * nbl_max + j / G] : 0u;
+        uint32_t x = t;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, x, o);
+            if (lane >= static_cast<uint32_t>(o)) x += y;
+        }
+        const uint64_t before = run + x - t;
+        const uint32_t quota = before >= need ? 0u : static_cast<uint32_t>(min_u64(t, need - before));
+        if (j < nb_global && j % G == shard) qblk[q * nbl_max + j / G] = quota;
+        run += __shfl_sync(kFull, x, 31);
+    }
+    ok = ok && run >= need;  // the ties counted before the cuts cover the quota
+    __syncwarp();
+    // per local block (lane), its pieces in id order: quotas, the two offsets, the checks
+    const uint32_t* h = a.h2 + q * a.P;
+    const uint64_t gl = gt_local[q];
+    uint64_t gt_run = 0, tie_run = 0;
+    for (uint32_t lb0 = 0; lb0 < nbl; lb0 += 32) {
+        const uint32_t lb = lb0 + lane;
+        uint32_t bgt = 0, btie = 0;
+        if (lb < nbl) {
+            uint32_t left = qblk[q * nbl_max + lb];
+            for (uint32_t p = lb * ppb; p < min(a.P, (lb + 1) * ppb); ++p) {
+                const uint32_t v = h[p];
+                const uint32_t gt = v >> 16, ties = (v & 0xffffu) - gt;
+                const uint32_t pq = min(ties, left);
+                left -= pq;
+                a.quota[q * a.P + p] = pq;
+                if (pq && gpiece(a, p) >= a.pcut[q]) ok = false;           // ties needed past the tie cut
+                if ((gt + pq) && a.ccnt[q * a.P + p] > a.B) ok = false;   // a contributing buffer overflowed
+                bgt += gt;
+                btie += pq;
+            }
+        }
+        uint32_t xg = bgt, xt = btie;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, xg, o), z = __shfl_up_sync(kFull, xt, o);
+            if (lane >= static_cast<uint32_t>(o)) {
+                xg += y;
+                xt += z;
+            }
+        }
+        if (lb < nbl) {
+            uint32_t pg = static_cast<uint32_t>(gt_run + xg - bgt), pt = static_cast<uint32_t>(gl + tie_run + xt - btie);
+            for (uint32_t p = lb * ppb; p < min(a.P, (lb + 1) * ppb); ++p) {
+                a.base[q * a.P + p] = pg;
+                a.base2[q * a.P + p] = pt;
+                pg += h[p] >> 16;
+                pt += a.quota[q * a.P + p];
+            }
+        }
+        gt_run += __shfl_sync(kFull, xg, 31);
+        tie_run += __shfl_sync(kFull, xt, 31);
+    }
+    ok = __all_sync(kFull, ok);
+    if (lane == 0) {
+        a.qflag[q] = ok ? 0u : 1u;
+        a.T[q] = L;
+        counts[q] = static_cast<uint32_t>(gl + tie_run);
+        if (!ok) atomicAdd(nflag, 1u);
+        if (ok && a.clist) {  // the compaction kernels' work lists
+            const uint32_t wl = dense_compact_warp(a, q) ? 0u : 1u;
+            a.clist[wl * a.nq + atomicAdd(a.nclist + wl, 1u)] = static_cast<uint32_t>(q);
+        }
+    }
+}
+
+cudaError_t launch_shard_sample(const DenseArgs& a, uint32_t* sum17, cudaStream_t st) {
+    if (a.nq == 0) return cudaSuccess;
+    cudaError_t e = launch_dense_sample(a, st);
+    if (e != cudaSuccess) return e;
+    shard_sample_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(a, sum17);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_shard_bound(const DenseArgs& a, const uint32_t* sum17, uint64_t n_global, uint32_t P_global,
+                               cudaStream_t st) {
+    if (a.nq == 0) return cudaSuccess;
+    shard_bound_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(a, sum17, n_global, P_global);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_shard_fused_sums(const DenseArgs& a, uint32_t ppb, uint32_t nbl, uint32_t nbl_max, uint32_t* gt,
+                                    uint32_t* ties, cudaStream_t st) {
+    if (a.nq == 0) return cudaSuccess;
+    shard_fused_sums_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(a, ppb, nbl, nbl_max, gt, ties);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_shard_fused_plan(const DenseArgs& a, const uint32_t* gt_sum, const uint32_t* gt_local,
+                                    const uint32_t* ties_all, uint32_t G, uint32_t shard, uint64_t nb_global,
+                                    uint32_t ppb, uint32_t nbl, uint32_t nbl_max, uint32_t* qblk, uint32_t* counts,
+                                    uint32_t* nflag, cudaStream_t st) {
+    if (a.nq == 0) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(a.nclist, 0, 2 * sizeof(uint32_t), st);
+    if (e != cudaSuccess) return e;
+    shard_fused_plan_kernel<<<static_cast<unsigned>((a.nq + 7) / 8), 256, 0, st>>>(
+        a, gt_sum, gt_local, ties_all, G, shard, nb_global, ppb, nbl, nbl_max, qblk, counts, nflag);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_shard_totals(const DenseArgs& a, uint32_t* tot, cudaStream_t st) {

@@ -108,6 +108,8 @@ struct DenseArgs {
     uint32_t nc;                  // uint4 code vectors per point: 1 (N_s <= 8, default) or 2 (N_s <= 16)
     uint32_t* pcut;               // single pass: nq, tie entries are stored only in pieces < pcut[q]
     uint32_t no_cut;              // tests: store every tie (pcut = P)
+    uint32_t shG, shR, shPPB;     // shard single pass: G shards, this shard r, pieces per id block (0: unsharded);
+                                  // local piece p is global piece ((p / shPPB) * G + r) * shPPB + p % shPPB
     uint32_t* clist;              // single pass: nq x 2 — unflagged queries with dense supersets from the front,
                                   // sparse ones from nq on (compaction work lists, any order)
     uint32_t* nclist;             // their two counts
@@ -147,6 +149,10 @@ cudaError_t launch_dense_codes_half(const uint32_t* ids, const uint32_t* cell_of
 cudaError_t launch_dense_codes(const uint32_t* ids, const uint32_t* cell_off, uint64_t n, uint32_t ns, uint32_t K,
                                uint16_t* codes, cudaStream_t st);
 cudaError_t launch_dense_select(const DenseArgs& a, cudaStream_t st);  // hist + plan + emit
+// the single pass's stages (launch_dense_select_fused runs them; the shard protocol interleaves its exchanges)
+cudaError_t launch_dense_sample(const DenseArgs& a, cudaStream_t st);
+cudaError_t launch_dense_fused_pass(const DenseArgs& a, cudaStream_t st);
+cudaError_t launch_dense_compaction(const DenseArgs& a, cudaStream_t st);
 // single pass: K0 sample -> L estimate -> fused hist + superset -> plan + checks -> compaction ->
 // exact emission for the flagged query blocks (rare); needs hsample/L/cbuf/ccnt/qflag/B
 // main_done (optional) is recorded once every unflagged query's candidates are written; the
@@ -217,6 +223,19 @@ cudaError_t launch_shard_imi(const uint32_t* ids, const uint32_t* cell_off, uint
 // from every shard's ties [G][nq][nbl_max]: per-piece quota / base (into a.quota / a.base, a.T
 // read) and the local candidate count per query. ppb = pieces per block.
 cudaError_t launch_shard_totals(const DenseArgs& a, uint32_t* tot, cudaStream_t st);
+// the shard protocol's single pass (dense.cu): sampled totals (nq x 17 u32: #(score >= t), t = 1..16,
+// and the points sampled) -> all-reduce -> bound (same L and tie cut on every shard) -> fused pass ->
+// per-query #(score > L) and per-block ties -> all-reduce / all-gather -> plan (quotas, offsets, the
+// shard's candidate counts, flags; *nflag += flagged queries) -> compaction
+cudaError_t launch_shard_sample(const DenseArgs& a, uint32_t* sum17, cudaStream_t st);
+cudaError_t launch_shard_bound(const DenseArgs& a, const uint32_t* sum17, uint64_t n_global, uint32_t P_global,
+                               cudaStream_t st);
+cudaError_t launch_shard_fused_sums(const DenseArgs& a, uint32_t ppb, uint32_t nbl, uint32_t nbl_max, uint32_t* gt,
+                                    uint32_t* ties, cudaStream_t st);
+cudaError_t launch_shard_fused_plan(const DenseArgs& a, const uint32_t* gt_sum, const uint32_t* gt_local,
+                                    const uint32_t* ties_all, uint32_t G, uint32_t shard, uint64_t nb_global,
+                                    uint32_t ppb, uint32_t nbl, uint32_t nbl_max, uint32_t* qblk, uint32_t* counts,
+                                    uint32_t* nflag, cudaStream_t st);
 cudaError_t launch_shard_ties(const DenseArgs& a, const uint32_t* tot_all, uint32_t G, uint32_t ppb, uint32_t nbl,
                               uint32_t nbl_max, uint32_t* T, uint64_t* need, uint32_t* ties, cudaStream_t st);
 cudaError_t launch_shard_quota(const DenseArgs& a, const uint32_t* ties_all, uint32_t G, uint32_t shard,

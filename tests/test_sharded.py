@@ -210,21 +210,35 @@ def test_gpu_sharded_build_error_reaches_every_rank(gpu):
 
 
 @pytest.mark.gpu
-def test_gpu_shard_exchange_volume(gpu, oracle):
-    """Bytes each rank sends per query: 64 (totals) + 4 x ceil(#blocks / G) (tie counts) + 12 k
-    (local top-k) — the two-round exchange, not the per-piece histograms."""
+def test_gpu_shard_exchange_volume(gpu, oracle, monkeypatch):
+    """Bytes each rank sends per query. Two-pass protocol: 64 (totals) + 4 x ceil(#blocks / G)
+    (tie counts) + 12 k (local top-k). Single pass: 68 (sampled totals) + 4 (#(score > L)) +
+    4 x ceil(#blocks / G) + 12 k, plus 4 per tile (the flag count); a tile some shard flagged also
+    runs the two-pass exchange. Never the per-piece histograms."""
     from paper_2411_14754_b200.sharded import Comm, Shard, run_ranks
     base, qs = _gpu_corpus(oracle, 4)
-    idx = gpu.build_index(base, gpu.IndexParams(4, 16, 3, 42))
     G, block = 4, 2048
-    shards = [Shard.cut(idx, r, G, block) for r in range(G)]
-    ctxs = [s.context() for s in shards]
-    comms = Comm.local(G)
-    cp = gpu.CollisionParams(0.05, 0.005, 10)
-    run_ranks(lambda r: shards[r].knn_query_batch(comms[r], qs, cp, scratch=ctxs[r]), G)
     nb = -(-len(base) // block)
-    want = len(qs) * (64 + 4 * (-(-nb // G)) + 12 * cp.k)
-    assert all(c.exchange_bytes() == want for c in ctxs), [c.exchange_bytes() for c in ctxs]
+    nblm = -(-nb // G)
+    cp = gpu.CollisionParams(0.05, 0.005, 10)
+    nq = len(qs)
+    two = 64 + 4 * nblm
+    one = 68 + 4 + 4 * nblm
+    for fused in ("0", "1"):
+        monkeypatch.setenv("SUCO_DENSE_FUSED", fused)
+        idx = gpu.build_index(base, gpu.IndexParams(4, 16, 3, 42))
+        shards = [Shard.cut(idx, r, G, block) for r in range(G)]
+        ctxs = [s.context() for s in shards]
+        comms = Comm.local(G)
+        run_ranks(lambda r: shards[r].knn_query_batch(comms[r], qs, cp, scratch=ctxs[r]), G)
+        got = [c.exchange_bytes() for c in ctxs]
+        if fused == "0":
+            want = {nq * (two + 12 * cp.k)}
+        else:
+            want = {nq * (one + 12 * cp.k) + 4, nq * (one + two + 12 * cp.k) + 4}
+        assert all(v in want for v in got), (fused, got, want)
+        for c in comms:
+            c.close()
 
 
 @pytest.mark.gpu
