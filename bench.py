@@ -82,7 +82,7 @@ def ncu_traffic(workload: str) -> dict:
                 "ncu_ms": v.get("duration_ms")} for k, v in w["kernels"].items()}
 
 
-def rerank_row_bytes(base, queries):
+def rerank_row_bytes(base, queries, m=None):
     """Bytes the re-rank reads per candidate row: the u8 copy (d padded to 16) for u8-valued data,
     else the int8 screen record (d padded to 16, + 16 bytes of bound terms, padded to 64) when
     d % 4 == 0 and d <= 128 (capi.cu upload_data), else the f32 row."""
@@ -90,7 +90,7 @@ def rerank_row_bytes(base, queries):
     u8 = u8_row_bytes(base, queries)
     if u8:
         return u8, "u8 rows"
-    if d % 4 == 0 and d <= 128 and not os.environ.get("SUCO_Q8") == "0":
+    if d % 4 == 0 and d <= 128 and not os.environ.get("SUCO_Q8") == "0" and (m is None or m >= 8192):
         if d > 48:  # the prefix-bound layout: the first 64 bytes of every record, the rest for a few
             return 64, "int8 screen record prefixes (+ the rest of the rows past the prefix bound)"
         return ((d + 15) // 16 * 16 + 16 + 63) // 64 * 64, "int8 screen records (+ exact f32 rows of the survivors)"
@@ -441,7 +441,7 @@ def main():
     peak, peak_src = measured_peaks()
     cum, sq, m = stats
     stage_avg = stage_ms / args.steps
-    row_bytes, row_kind = rerank_row_bytes(base, queries)
+    row_bytes, row_kind = rerank_row_bytes(base, queries, m)
     traffic = ncu_traffic(cfg.name)
     names = ["traverse", "select", "rerank"]
     id_equiv = {"select": 4.0 * cum, "rerank": 4.0 * d * m * sq + 4.0 * d * sq}

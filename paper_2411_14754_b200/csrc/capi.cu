@@ -472,6 +472,7 @@ void rerank_args(const suco_gpu_index* x, RerankArgs& ra) {
     ra.qpad = x->qpad;
     ra.qrec = x->qrec;
     ra.qpre = x->qpre;
+    ra.q8_min = x->tune.q8 == 2 ? 0 : kQ8MinCands;
     ra.qsplit = x->qsplit;
     ra.u8_regs = x->tune.rerank_u8_regs;
     ra.no_tma = !x->tune.rerank_tma;

@@ -166,6 +166,7 @@ cudaError_t launch_dense_hist_rows(const DenseArgs& a, uint32_t* out, cudaStream
 cudaError_t launch_dense_emit(const DenseArgs& a, cudaStream_t st);
 constexpr uint32_t kDensePiece = 2048;  // points per piece (one warp)
 constexpr uint32_t kDenseBuf = 96;      // single-pass candidate buffer entries per 2048 points of a (piece, query)
+constexpr uint64_t kQ8MinCands = 8192;  // the int8 screen pays off from this many candidates per query
 constexpr uint32_t kDenseCodePad = 128;  // zero-slot code rows past n (the fused pass loads two tiles ahead)
 constexpr uint32_t kFusedPiece = 8192;
 constexpr uint32_t kMaxPiece = 32768;   // largest single-pass piece (SUCO_DENSE_PIECE): 15-bit in-piece offsets  // points per piece of the single-pass select (half-width mode: kDensePiece)
@@ -202,6 +203,7 @@ struct RerankArgs {
     uint32_t qpad;          // int8 bytes of a record (d rounded up to 16)
     uint32_t qrec;          // record stride (qpad + 16 rounded up to 64)
     uint32_t qpre;          // prefix-bound layout: prefix words (16 dims each; 0 = plain records)
+    uint64_t q8_min;        // candidates per query from which the int8 screen is used (kQ8MinCands; tests: 0)
     uint32_t qsplit;        // byte offset of the rest of the row (the second read of rerank_q8p_kernel)
     bool no_tma;            // !Tuning::rerank_tma: 16-byte cp.async row gathers instead of per-row TMA bulk copies
     unsigned long long* screen_stats;  // optional diagnostics: [0] += exact re-ranks, [1] += queries re-ranked in full

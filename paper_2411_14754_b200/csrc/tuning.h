@@ -14,7 +14,8 @@ namespace suco_gpu {
 struct Tuning {
     int cluster = 0;             // SUCO_CLUSTER: cluster-counting select cluster size (0 = by occupancy)
     bool no_u8 = false;          // SUCO_NO_U8: never keep a byte copy of u8-valued rows
-    bool q8 = true;              // SUCO_Q8=0: no int8 screen copy of float rows (the fp32 screen reads f32 rows)
+    int q8 = 1;                  // SUCO_Q8: int8 screen copy of float rows: 0 none (the fp32 screen reads f32 rows),
+                                 // 1 used from kQ8MinCands candidates per query, 2 always (tests)
     uint32_t q8_prefix = 3;      // SUCO_Q8_PREFIX: int8 screen prefix words (16 dims each: 3 = one 64-byte read,
                                  // 1 = one 32-byte sector, 0 = no prefix bound). Measured at cfg4: 3 -> 2,053 of
                                  // 50,000 rows per query past the bound, rerank 7.90 ms; 1 -> 12,600 rows, 8.37 ms

@@ -181,7 +181,8 @@ Tuning tuning_from_env() {
     const int c = env_int("SUCO_CLUSTER", 0);
     t.cluster = (c >= 1 && c <= 16) ? c : 0;
     t.no_u8 = std::getenv("SUCO_NO_U8") != nullptr;
-    t.q8 = env_int("SUCO_Q8", 1) != 0;
+    const int q8 = env_int("SUCO_Q8", 1);
+    t.q8 = q8 == 0 || q8 == 2 ? q8 : 1;
     const int qp = env_int("SUCO_Q8_PREFIX", 3);
     t.q8_prefix = (qp == 0 || qp == 1 || qp == 3) ? static_cast<uint32_t>(qp) : 3u;
     t.dense = env_int("SUCO_DENSE", 1) != 0;

@@ -443,6 +443,45 @@ def test_screened_rerank_extreme_magnitudes(gpu, oracle, scale):
         assert np.array_equal(ids, oi) and np.array_equal(dd, od), (scale, a, b, k)
 
 
+@pytest.mark.parametrize("prefix", ["0", "1", "3"])
+def test_int8_screen_forced(gpu, oracle, ref, prefix, monkeypatch):
+    """The int8-screened re-rank (SUCO_Q8=2: even for short candidate lists) with plain records
+    (prefix 0) and the prefix-bound layouts of 16 and 48 dims: masses of exact ties next to the
+    queries, squared distances that underflow / overflow fp32, and the float / 8 x 64^2-cell
+    corpora of test_knn_vs_oracle — answers identical to the reference."""
+    monkeypatch.setenv("SUCO_Q8", "2")
+    monkeypatch.setenv("SUCO_Q8_PREFIX", prefix)
+    full = oracle.clustered(8000 + 12, 64, 10, 99, 0, 1, 0.05, False)
+    base, qs = oracle.hold_out(full, 12, 100)
+    base = np.concatenate([base, np.repeat(base[17:18], 3000, axis=0)])
+    qs = np.concatenate([qs, base[17:18] + np.float32(1e-3), base[17:18]])
+    oidx = oracle.build_index(base, 4, 10, 3, 42, 0)
+    idx = gpu.load_index(oidx.serialize(), base)
+    for a, b, k in ((1.0, 1.0, 10), (0.3, 0.2, 32), (0.05, 0.01, 1), (0.3, 0.2, 64)):
+        ids, dd = idx.knn_query_batch(qs, gpu.CollisionParams(a, b, k))
+        oi, od, _ = oidx.knn_query_batch(base, qs, a, b, k)
+        assert np.array_equal(ids, oi) and np.array_equal(dd, od), (prefix, a, b, k)
+    for scale in (1e-22, 1e20):
+        full = oracle.clustered(3000 + 8, 96, 6, 7, 0, 1, 0.1, False) * np.float32(scale)
+        base2, qs2 = oracle.hold_out(full, 8, 8)
+        oidx2 = oracle.build_index(base2, 2, 6, 2, 42, 0)
+        idx2 = gpu.load_index(oidx2.serialize(), base2)
+        for a, b, k in ((1.0, 1.0, 10), (0.2, 0.05, 5)):
+            ids, dd = idx2.knn_query_batch(qs2, gpu.CollisionParams(a, b, k))
+            oi, od, _ = oidx2.knn_query_batch(base2, qs2, a, b, k)
+            assert np.array_equal(ids, oi) and np.array_equal(dd, od), (prefix, scale, a, b, k)
+    for case in ("float", "dense_1024"):
+        n, d, cl, lo, hi, sig, quant, ns, kh, it, mode, plist = CASES[case]
+        full = oracle.clustered(n + 40, d, cl, 1000 + n, lo, hi, sig, quant)
+        base3, qs3 = oracle.hold_out(full, 40, 1001 + n)
+        oidx3 = oracle.build_index(base3, ns, kh, it, 42, mode)
+        idx3 = gpu.load_index(oidx3.serialize(), base3)
+        for a, b, k in plist:
+            ids, dd = idx3.knn_query_batch(qs3, gpu.CollisionParams(a, b, k))
+            oi, od, _ = oidx3.knn_query_batch(base3, qs3, a, b, k)
+            assert np.array_equal(ids, oi) and np.array_equal(dd, od), (prefix, case, a, b, k)
+
+
 @pytest.mark.parametrize("fused", ["1", "0"])
 @pytest.mark.parametrize("ns,kh", [(16, 12), (12, 20), (9, 7)])
 def test_dense_select_16_subspaces(gpu, oracle, ns, kh, fused, monkeypatch):
