@@ -168,26 +168,33 @@ __device__ __forceinline__ Codes<NC> load_codes_at(const DenseArgs& a, const uin
 
 // One 32-bit mask per slot at the shared-window address mb + 4 slot: the shift and add are one LEA
 // per lookup (through a generic pointer ptxas adds the window base to every address separately).
+// MB >= 0: the table's shared-window address is the constant MB (checked by the caller), folded
+// into the load's immediate offset: the lookup's address is then one shift-and-mask of the code.
+template <int MB>
 __device__ __forceinline__ uint32_t lds_slot(uint32_t mb, uint32_t slot) {
     uint32_t v;
-    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(mb + (slot << 2)));
+    if constexpr (MB >= 0) {
+        asm volatile("ld.shared.b32 %0, [%1+%2];" : "=r"(v) : "r"(slot << 2), "n"(MB));
+    } else {
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(mb + (slot << 2)));
+    }
     return v;
 }
 
-template <uint32_t W, uint32_t NC>
+template <uint32_t W, uint32_t NC, int MB = -1>
 __device__ __forceinline__ void masks_of(const uint32_t* M, const Codes<NC>& c, uint32_t (&m)[8 * NC][W]) {
     if constexpr (W == 1) {
         const uint32_t mb = static_cast<uint32_t>(__cvta_generic_to_shared(M));
 #pragma unroll
         for (uint32_t i = 0; i < NC; ++i) {
-            m[8 * i + 0][0] = lds_slot(mb, c.v[i].x & 0xffffu);
-            m[8 * i + 1][0] = lds_slot(mb, c.v[i].x >> 16);
-            m[8 * i + 2][0] = lds_slot(mb, c.v[i].y & 0xffffu);
-            m[8 * i + 3][0] = lds_slot(mb, c.v[i].y >> 16);
-            m[8 * i + 4][0] = lds_slot(mb, c.v[i].z & 0xffffu);
-            m[8 * i + 5][0] = lds_slot(mb, c.v[i].z >> 16);
-            m[8 * i + 6][0] = lds_slot(mb, c.v[i].w & 0xffffu);
-            m[8 * i + 7][0] = lds_slot(mb, c.v[i].w >> 16);
+            m[8 * i + 0][0] = lds_slot<MB>(mb, c.v[i].x & 0xffffu);
+            m[8 * i + 1][0] = lds_slot<MB>(mb, c.v[i].x >> 16);
+            m[8 * i + 2][0] = lds_slot<MB>(mb, c.v[i].y & 0xffffu);
+            m[8 * i + 3][0] = lds_slot<MB>(mb, c.v[i].y >> 16);
+            m[8 * i + 4][0] = lds_slot<MB>(mb, c.v[i].z & 0xffffu);
+            m[8 * i + 5][0] = lds_slot<MB>(mb, c.v[i].z >> 16);
+            m[8 * i + 6][0] = lds_slot<MB>(mb, c.v[i].w & 0xffffu);
+            m[8 * i + 7][0] = lds_slot<MB>(mb, c.v[i].w >> 16);
         }
         return;
     }
@@ -669,7 +676,7 @@ __global__ void __launch_bounds__(256) dense_bound_kernel(DenseArgs a) {
 // The fused pass's walk over a warp's pieces (below). STAGE: entries go through a 64-bit register
 // (four per 8-byte store) — for dense supersets, where 2-byte stores multiply DRAM traffic; sparse
 // ones store each entry directly (fewer instructions per tile).
-template <uint32_t kDW, uint32_t W, bool STAGE, uint32_t NC>
+template <uint32_t kDW, uint32_t W, bool STAGE, uint32_t NC, int MB = -1>
 __device__ __forceinline__ void fused_pieces(const DenseArgs& a, const uint32_t* M, uint64_t q0, uint32_t nqb,
                                              const uint32_t (&TL)[W][Np<NC>::v], const uint32_t (&live)[W],
                                              const uint32_t (&cut)[W], uint32_t lane, uint32_t warp) {
@@ -682,15 +689,15 @@ __device__ __forceinline__ void fused_pieces(const DenseArgs& a, const uint32_t*
         const uint64_t lo = uint64_t(piece) * a.WP;
         const uint64_t hi = min_u64(a.n, lo + a.WP);
         uint32_t cnt[W], nb[W];
-        uint16_t* buf[W];  // [query][piece][B]: a lane appends to its own contiguous buffer
-        uint64_t sw[W];    // STAGE: four entries shifted in from the top
+        uint16_t* bp[W];  // [query][piece][B]: a lane appends to its own contiguous buffer (next store)
+        uint64_t sw[W];   // STAGE: four entries shifted in from the top
 #pragma unroll
         for (uint32_t w = 0; w < W; ++w) {
             cnt[w] = 0;
             nb[w] = 0;
             sw[w] = 0;
             const uint64_t q = 32 * w + lane < nqb ? q0 + 32 * w + lane : q0;  // idle lanes append nothing
-            buf[w] = cb_base(a, q, piece);
+            bp[w] = cb_base(a, q, piece);
         }
         // 32-bit tile loop over the piece: a running code pointer, the piece's point count
         const uint32_t len = static_cast<uint32_t>(hi - lo);
@@ -700,7 +707,7 @@ __device__ __forceinline__ void fused_pieces(const DenseArgs& a, const uint32_t*
         uint32_t mk[8 * NC][W];
         // (unconditional loads: the code rows are padded with zero-slot codes past n, and loads past
         // a piece's end read the next piece's codes, never scored)
-        masks_of<W, NC>(M, load_codes_at<NC>(a, cptr, true), mk);
+        masks_of<W, NC, MB>(M, load_codes_at<NC>(a, cptr, true), mk);
         Codes<NC> code1 = load_codes_at<NC>(a, cptr + 32 * NC, true);
         // Pieces past every lane's tie cut need only score > L (lane = query): one transpose per tile
         // instead of two; their #(score >= L) is not needed by the plan (its ties are never taken:
@@ -716,7 +723,7 @@ __device__ __forceinline__ void fused_pieces(const DenseArgs& a, const uint32_t*
             const Codes<NC> next = load_codes_at<NC>(a, cptr + 32 * NC, true);
             uint32_t b[W][NP];
             csa_planes<W, NC>(mk, b);
-            masks_of<W, NC>(M, code1, mk);  // (past the piece end: the zero slot)
+            masks_of<W, NC, MB>(M, code1, mk);  // (past the piece end: the zero slot)
             code1 = next;
 #pragma unroll
             for (uint32_t w = 0; w < W; ++w) {
@@ -737,19 +744,25 @@ __device__ __forceinline__ void fused_pieces(const DenseArgs& a, const uint32_t*
                     const uint32_t c1 = __popc(g1);
                     cnt[w] += c1 | (c1 << 16);
                 }
-                while (bits) {  // id order
-                    const uint32_t r = __ffs(bits) - 1;
-                    bits &= bits - 1;
-                    if (nb[w] < a.B) {
-                        const uint32_t v = (tb + r) | (((g1 >> r) & 1u) << 15);
-                        if constexpr (STAGE) {
-                            sw[w] = (sw[w] >> 16) | (static_cast<uint64_t>(v) << 48);
-                            if ((nb[w] & 3u) == 3u) *reinterpret_cast<uint64_t*>(buf[w] + cb_off(a, nb[w] & ~3u)) = sw[w];
-                        } else {
-                            buf[w][cb_off(a, nb[w])] = static_cast<uint16_t>(v);
+                if (bits) {  // id order; the capacity check once per tile while the buffer has room
+                    const bool room = nb[w] + __popc(bits) <= a.B;
+                    do {
+                        const uint32_t r = __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        if (room || nb[w] < a.B) {
+                            const uint32_t v = (tb + r) | (((g1 >> r) & 1u) << 15);
+                            if constexpr (STAGE) {
+                                sw[w] = (sw[w] >> 16) | (static_cast<uint64_t>(v) << 48);
+                                if ((nb[w] & 3u) == 3u) {
+                                    *reinterpret_cast<uint64_t*>(bp[w]) = sw[w];
+                                    bp[w] += 4;
+                                }
+                            } else {
+                                *bp[w]++ = static_cast<uint16_t>(v);
+                            }
                         }
-                    }
-                    ++nb[w];
+                        ++nb[w];
+                    } while (bits);
                 }
             }
         }
@@ -759,8 +772,8 @@ __device__ __forceinline__ void fused_pieces(const DenseArgs& a, const uint32_t*
                 const uint64_t i = (q0 + 32 * w + lane) * a.P + piece;
                 if constexpr (STAGE) {
                     const uint32_t kept = min(nb[w], a.B), part = kept & 3u;
-                    if (part)  // the last, partial chunk: its entries down to the low end
-                        *reinterpret_cast<uint64_t*>(buf[w] + cb_off(a, kept & ~3u)) = sw[w] >> (16 * (4 - part));
+                    if (part)  // the last, partial chunk (at the running pointer): its entries down to the low end
+                        *reinterpret_cast<uint64_t*>(bp[w]) = sw[w] >> (16 * (4 - part));
                 }
                 a.h2[i] = cnt[w];
                 a.ccnt[i] = static_cast<uint16_t>(nb[w]);  // <= WP <= 32768
@@ -797,8 +810,16 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs 
         live[w] = __ballot_sync(kFull, L != 0);
         cut[w] = a.pcut && 32 * w + lane < nqb ? a.pcut[q0 + 32 * w + lane] : a.P;
     }
-    if (stage) fused_pieces<kDW, W, true, NC>(a, M, q0, nqb, TL, live, cut, lane, warp);
-    else fused_pieces<kDW, W, false, NC>(a, M, q0, nqb, TL, live, cut, lane, warp);
+    // the table at shared address 1024 (dynamic shared memory after the 1 KB reserved for the
+    // system on sm_100): lookups with the base folded into the load's immediate
+    const bool at1k = static_cast<uint32_t>(__cvta_generic_to_shared(M)) == 1024u;
+    if (W == 1 && NC == 1 && at1k) {
+        if (stage) fused_pieces<kDW, W, true, NC, 1024>(a, M, q0, nqb, TL, live, cut, lane, warp);
+        else fused_pieces<kDW, W, false, NC, 1024>(a, M, q0, nqb, TL, live, cut, lane, warp);
+    } else {
+        if (stage) fused_pieces<kDW, W, true, NC>(a, M, q0, nqb, TL, live, cut, lane, warp);
+        else fused_pieces<kDW, W, false, NC>(a, M, q0, nqb, TL, live, cut, lane, warp);
+    }
 }
 
 // K4: thread per (query, piece), T == L: the piece's buffer holds its score >= T points in id
