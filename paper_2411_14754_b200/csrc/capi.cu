@@ -207,7 +207,8 @@ void upload_data(suco_gpu_index* x, const float* data, uint64_t n, uint32_t d) {
     // other rows: an int8 copy with per-row bound terms for the re-rank's certified screen (a
     // quarter of the f32 row bytes; rerank_q8_kernel)
     x->qpad = x->qrec = 0;
-    if (!x->dpad && x->tune.q8 && d % 4 == 0 && d <= 128) {
+    // (d <= 128: rerank_q8p / rerank_q8 kernels; 128 < d <= 1024: rerank_q8w, prefix records only)
+    if (!x->dpad && x->tune.q8 && d % 4 == 0 && (d <= 128 || (d <= 1024 && x->tune.q8_prefix == 3))) {
         x->qpad = (d + 15) / 16 * 16;
         // Past the prefix: the prefix-bound layout (meta0 and the prefix dims in the first qsplit
         // bytes, the rest and meta1 after them: pack_q8_kernel); whole 64-byte granules per record

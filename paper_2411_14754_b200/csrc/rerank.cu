@@ -1019,7 +1019,7 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_q8_kernel(RerankArgs a, ui
 // ------------------------------------------- int8 screen with a prefix bound (NW >= 4)
 // Record (qrec bytes, a multiple of 64): [meta0][dims 0 .. 16 kQ8P) in the first qsplit bytes (32
 // for one prefix word, 64 for three), then [dims 16 kQ8P .. 16 NW)[meta1]; meta0 = (s, |a_S|^2
-// (u32 bits), ||e_x,S|| up, 0), meta1 = (|x|^2, ||s a|| up, ||e_x|| up, s), S = the prefix dims.
+// (u32 bits), ||e_x,S|| up, 0), meta1 = (|a|^2 (u32 bits), ||e_x|| up, s, 0), S = the prefix dims.
 // Stage 1 reads the first qsplit bytes of every candidate. The prefix alone bounds the distance from below:
 //     D >= sum_{i in S} (x_i - q_i)^2 >= (||s a_S - t b_S|| - ||e_x,S|| - ||e_q,S||)^2,
 //     ||s a_S - t b_S||^2 = s^2 |a_S|^2 + t^2 |b_S|^2 - 2 s t (a_S . b_S),   a_S . b_S exact (IDP.4A)
@@ -1031,6 +1031,23 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_q8_kernel(RerankArgs a, ui
 // next prefix step and consumed one step later, so the copies never drain; tau is shared across
 // the CTA's warps (the minimum of their k-th upper bounds bounds the query's k-th distance).
 constexpr uint32_t kQ8QCap = 64;  // queued rows per warp (at most 63 by construction)
+
+// Certified bounds lo <= D <= up of the reference's fp64 squared distance from the int8 forms
+// x = s a + e_x, q = t b + e_q: ||x - q|| is within ||e_x|| + ||e_q|| of ||s a - t b||, whose square
+// s^2 |a|^2 + t^2 |b|^2 - 2 s t (a . b) is exact up to fp64 rounding (a . b exact from IDP.4A). The
+// error is relative to sqrt(D), not to |x| (the Cauchy-Schwarz form |x.q - s t a.b| <= ... is not:
+// at cfg3, rows of norm 17 at distance 2, it let a thousand candidates per query through).
+__device__ __forceinline__ void tri_bounds(double s, double a2, double tb2, double qt, int I, double ex, double eq,
+                                           double& lo, double& up) {
+    const double sa = s * s * a2;
+    const double cr = 2.0 * s * qt * static_cast<double>(I);
+    const double V = sa + tb2 - cr;
+    const double sl = 1.1368683772161603e-13 * (sa + tb2 + fabs(cr));  // 2^-43: every fp64 rounding above
+    const double rlo = sqrt(fmax(V - sl, 0.0)) * (1.0 - 1e-15) - ex - eq;
+    const double rhi = sqrt(fmax(V + sl, 0.0)) * (1.0 + 1e-15) + ex + eq;
+    lo = rlo > 0.0 ? rlo * rlo * (1.0 - 1e-9) : 0.0;  // (1e-9: the reference's 4-chain sum vs the real value)
+    up = rhi * rhi * (1.0 + 1e-9);
+}
 
 template <uint32_t kQ8P, uint32_t NR>  // prefix words (16 dims each), rest words: NW = kQ8P + NR
 __global__ void __launch_bounds__(kThreads, 2) rerank_q8p_kernel(RerankArgs a, uint32_t stride) {
@@ -1049,7 +1066,7 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_q8p_kernel(RerankArgs a, u
     __shared__ int qqI[kWarps][kQ8QCap];
     __shared__ double md[kWarps * 32];
     __shared__ uint32_t mi[kWarps * 32];
-    __shared__ double qpar[6];  // t, |q|^2, ||t b|| (up), ||e_q|| (up), t^2 |b_S|^2, ||e_q,S|| (up)
+    __shared__ double qpar[7];  // t, |q|^2, ||t b|| (up), ||e_q|| (up), t^2 |b_S|^2, ||e_q,S|| (up), t^2 |b|^2
     __shared__ double tau_cta;
     __shared__ unsigned long long tau_sh;  // CTA-wide min of the warps' k-th upper bounds (bits of a double >= 0)
     __shared__ int ovf, qok;
@@ -1098,6 +1115,7 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_q8p_kernel(RerankArgs a, u
             qpar[3] = sqrt(e2) * (1.0 + 1e-12);
             qpar[4] = static_cast<double>(t) * static_cast<double>(t) * b2s;  // b2s: an exact integer
             qpar[5] = sqrt(e2s) * (1.0 + 1e-12);
+            qpar[6] = static_cast<double>(t) * static_cast<double>(t) * b2;
             qok = isfinite(n2) && isfinite(e2) && isfinite(qpar[2]);
             ovf = 0;
             tau_sh = 0x7ff0000000000000ull;  // +inf
@@ -1110,7 +1128,7 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_q8p_kernel(RerankArgs a, u
 #pragma unroll
         for (uint32_t j = 0; j < 4; ++j) qv[w][j] = static_cast<int>(qpack[4 * w + j]);
     }
-    const double qt = qpar[0], n2q = qpar[1], Bq = qpar[2], rq = qpar[3], tb2S = qpar[4], eqS = qpar[5];
+    const double qt = qpar[0], rq = qpar[3], tb2S = qpar[4], eqS = qpar[5], tb2 = qpar[6];
     const bool qfin = qok != 0;
     uint4* ra = reinterpret_cast<uint4*>(wbase + warp * per_warp);
     uint4* rb = ra + ringA;
@@ -1204,21 +1222,13 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_q8p_kernel(RerankArgs a, u
                 c2 = __dp4a(static_cast<int>(x.z), qv[kQ8P + w][2], c2);
                 c3 = __dp4a(static_cast<int>(x.w), qv[kQ8P + w][3], c3);
             }
-            const uint4 mw = row[NR];
+            const uint4 mw = row[NR];  // meta1 = (|a|^2, ||e_x|| up, s, 0)
             const int I = (c0 + c1) + (c2 + c3);
-            const float rn2 = __uint_as_float(mw.x), rA = __uint_as_float(mw.y), rR = __uint_as_float(mw.z);
-            const float rs = __uint_as_float(mw.w);
+            const float rR = __uint_as_float(mw.y), rs = __uint_as_float(mw.z);
             const bool valid = lane < fcnt;
             double lo = 0.0, up = kInf;
-            if (qfin && rs >= 0.f) {
-                const double dot = static_cast<double>(rs) * qt * static_cast<double>(I);
-                const double approx = static_cast<double>(rn2) + n2q - 2.0 * dot;
-                const double err = 2.0 * (static_cast<double>(rA) * rq + Bq * static_cast<double>(rR) +
-                                          static_cast<double>(rR) * rq);
-                const double slack = 9.5367431640625e-07 * (static_cast<double>(rn2) + n2q + 2.0 * fabs(dot)) + 1e-300;
-                lo = approx - err - slack;
-                up = approx + err + slack;
-            }
+            if (qfin && rs >= 0.f)
+                tri_bounds(static_cast<double>(rs), static_cast<double>(mw.x), tb2, qt, I, static_cast<double>(rR), rq, lo, up);
             const double tau0 = __shfl_sync(kFull, sl, a.k - 1);
             uint32_t bal = __ballot_sync(kFull, valid && up < tau0);
             if (bal) {
@@ -1340,6 +1350,363 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_q8p_kernel(RerankArgs a, u
                    [&](uint64_t t) { return a.identity ? static_cast<uint32_t>(lo + t) : cands[lo + t]; }, ld, lid, lane);
     } else {
         uint32_t kept = 0;  // survivors: buffered rows whose lower bound is within the CTA's tau
+        for (uint32_t t0 = 0; t0 < nsurv; t0 += 32) {
+            const uint32_t t = t0 + lane;
+            const bool in = t < nsurv;
+            const uint32_t idv = in ? sid[warp][t] : 0u;
+            const bool keep = in && static_cast<double>(slo[warp][t]) <= tau;
+            const uint32_t kb = __ballot_sync(kFull, keep);
+            __syncwarp();
+            if (keep) sid[warp][kept + __popc(kb & ((1u << lane) - 1u))] = idv;
+            kept += __popc(kb);
+            __syncwarp();
+        }
+        if (a.screen_stats && lane == 0) atomicAdd(a.screen_stats, static_cast<unsigned long long>(kept));
+        exact_rows(a, st, stride, qd, kept, [&](uint64_t t) { return sid[warp][t]; }, ld, lid, lane);
+    }
+    __syncthreads();
+    md[warp * 32 + lane] = ld;
+    mi[warp * 32 + lane] = lid;
+    __syncthreads();
+    if (warp == 0) {
+        for (uint32_t w = 1; w < kWarps; ++w) {
+            for (uint32_t i = 0; i < a.k; ++i) {
+                const double dv = md[w * 32 + i];
+                if (dv == kInf) break;
+                warp_insert(dv, mi[w * 32 + i], ld, lid, a.k, lane);
+            }
+        }
+        if (lane < a.k) {
+            a.out_ids[q * a.k + lane] = lid;
+            a.out_dists[q * a.k + lane] = a.squared ? ld : __dsqrt_rn(ld);
+        }
+    }
+}
+
+// ---------------------------- int8 screen with a prefix bound, wide rows (128 < d <= 1024)
+// rerank_q8p_kernel's stage 1 unchanged (the first 48 dims in one 64-byte read, the query's prefix
+// words in registers). Stage 2 — the rest of a queued row (up to 61 words) — is a warp-cooperative
+// pass instead of a ring of whole rows: for each queued row, lane l loads words l and 32 + l of its
+// rest, folds them against the query words it holds in registers, and a warp reduction gives the
+// row's exact int8 dot product, four rows' loads in flight at a time. The full certified bounds,
+// the shared tau and the exact fp64 survivors are rerank_q8p_kernel's. At cfg3 (d = 960) the first
+// 48 dims rule out about 90 % of the candidates against the final tau (tools/partial_bound.py): a
+// candidate costs 64 bytes instead of the 3,840 of its f32 row.
+__global__ void __launch_bounds__(kThreads, 2) rerank_q8w_kernel(RerankArgs a, uint32_t stride) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr uint32_t kP = 3;               // prefix words
+    constexpr uint32_t suA = kP + 2;         // meta0 + prefix words + 1: odd 16-byte stride
+    double* qd = reinterpret_cast<double*>(smem);  // d
+    const uint32_t ringA = kQ8Stages * 32 * suA;   // uint4 units
+    const uint32_t per_warp = max(ringA * 16, kRows * stride * 4);
+    unsigned char* wbase = smem + ((a.d * 8 + 15) / 16) * 16;
+    __shared__ uint32_t qpack[256];          // the query's int8 words (d <= 1024)
+    __shared__ uint32_t sid[kWarps][kQ8Cap];
+    __shared__ float slo[kWarps][kQ8Cap];
+    __shared__ uint32_t qqid[kWarps][kQ8QCap];
+    __shared__ int qqI[kWarps][kQ8QCap];
+    __shared__ double md[kWarps * 32];
+    __shared__ uint32_t mi[kWarps * 32];
+    __shared__ double qred[8][5];            // per warp: e2, b2, n2, e2s, b2s
+    __shared__ double qpar[7];  // t, |q|^2, ||t b|| (up), ||e_q|| (up), t^2 |b_S|^2, ||e_q,S|| (up), t^2 |b|^2
+    __shared__ double tau_cta;
+    __shared__ unsigned long long tau_sh;
+    __shared__ float qmax_sh[kWarps];
+    __shared__ int ovf, qok;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    uint64_t q;
+    if (!rerank_query(a, q)) return;
+    const float* query = a.queries + q * a.d;
+    const uint32_t nwq = a.qpad / 16, nr = nwq - kP;  // rest words
+    for (uint32_t i = tid; i < a.d; i += kThreads) qd[i] = static_cast<double>(query[i]);
+    // quantise the query: t = max|q| / 127 over the whole CTA; thread owns dims 4 tid .. 4 tid + 3
+    float v[4], mx = 0.f;
+#pragma unroll
+    for (uint32_t j = 0; j < 4; ++j) {
+        const uint32_t i = 4 * tid + j;
+        v[j] = i < a.d ? query[i] : 0.f;
+        mx = fmaxf(mx, fabsf(v[j]));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
+    if (lane == 0) qmax_sh[warp] = mx;
+    __syncthreads();
+    mx = 0.f;
+    for (uint32_t w = 0; w < kWarps; ++w) mx = fmaxf(mx, qmax_sh[w]);
+    const float tq = mx / 127.f;
+    {
+        double e2 = 0.0, b2 = 0.0, n2 = 0.0;
+        uint32_t packed = 0;
+#pragma unroll
+        for (uint32_t j = 0; j < 4; ++j) {
+            const float bq = tq > 0.f ? fminf(127.f, fmaxf(-127.f, rintf(v[j] / tq))) : 0.f;
+            const double e = static_cast<double>(v[j]) - static_cast<double>(tq) * static_cast<double>(bq);
+            e2 += e * e;
+            b2 += static_cast<double>(bq) * static_cast<double>(bq);
+            n2 += static_cast<double>(v[j]) * static_cast<double>(v[j]);
+            packed |= (static_cast<uint32_t>(static_cast<int>(bq)) & 0xffu) << (8 * j);
+        }
+        const bool pre = tid < 4 * kP;  // this thread's dims are in the prefix
+        double e2s = pre ? e2 : 0.0, b2s = pre ? b2 : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            e2 += __shfl_xor_sync(kFull, e2, o);
+            b2 += __shfl_xor_sync(kFull, b2, o);
+            n2 += __shfl_xor_sync(kFull, n2, o);
+            e2s += __shfl_xor_sync(kFull, e2s, o);
+            b2s += __shfl_xor_sync(kFull, b2s, o);
+        }
+        qpack[tid] = packed;
+        if (lane == 0) {
+            qred[warp][0] = e2;
+            qred[warp][1] = b2;
+            qred[warp][2] = n2;
+            qred[warp][3] = e2s;
+            qred[warp][4] = b2s;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double e2 = 0.0, b2 = 0.0, n2 = 0.0, e2s = 0.0, b2s = 0.0;
+        for (uint32_t w = 0; w < kWarps; ++w) {
+            e2 += qred[w][0];
+            b2 += qred[w][1];
+            n2 += qred[w][2];
+            e2s += qred[w][3];
+            b2s += qred[w][4];
+        }
+        qpar[0] = static_cast<double>(tq);
+        qpar[1] = n2;
+        qpar[2] = static_cast<double>(tq) * sqrt(b2) * (1.0 + 1e-12);
+        qpar[3] = sqrt(e2) * (1.0 + 1e-12);
+        qpar[4] = static_cast<double>(tq) * static_cast<double>(tq) * b2s;
+        qpar[5] = sqrt(e2s) * (1.0 + 1e-12);
+        qpar[6] = static_cast<double>(tq) * static_cast<double>(tq) * b2;
+        qok = isfinite(n2) && isfinite(e2) && isfinite(qpar[2]);
+        ovf = 0;
+        tau_sh = 0x7ff0000000000000ull;
+    }
+    __syncthreads();
+    int qv[kP][4];
+#pragma unroll
+    for (uint32_t w = 0; w < kP; ++w) {
+#pragma unroll
+        for (uint32_t j = 0; j < 4; ++j) qv[w][j] = static_cast<int>(qpack[4 * w + j]);
+    }
+    // this lane's query rest words: kP + lane and kP + 32 + lane
+    int qr[2][4];
+#pragma unroll
+    for (uint32_t u = 0; u < 2; ++u) {
+        const uint32_t w = kP + 32 * u + lane;
+#pragma unroll
+        for (uint32_t j = 0; j < 4; ++j) qr[u][j] = w < nwq ? static_cast<int>(qpack[4 * w + j]) : 0;
+    }
+    const double qt = qpar[0], rq = qpar[3], tb2S = qpar[4], eqS = qpar[5], tb2 = qpar[6];
+    const bool qfin = qok != 0;
+    uint4* ra = reinterpret_cast<uint4*>(wbase + warp * per_warp);
+    uint32_t* qid = qqid[warp];
+    int* qI = qqI[warp];
+    const uint32_t* cands = a.cands + q * a.m;
+    const uint64_t mq = a.counts ? a.counts[q] : a.m;
+    const uint64_t first = uint64_t(warp) * 32;
+    const uint64_t steps = mq > first ? (mq - first + 32 * kWarps - 1) / (32 * kWarps) : 0;
+    auto sbase = [&](uint64_t g) { return first + g * 32 * kWarps; };
+    auto load_id = [&](uint64_t g) -> uint32_t {
+        const uint64_t i = sbase(g) + lane;
+        if (g >= steps || i >= mq) return 0u;
+        return a.identity ? static_cast<uint32_t>(i) : __ldcs(cands + i);
+    };
+    uint32_t id0 = load_id(0), id1 = load_id(1);
+    auto issue_a = [&](uint64_t g) {  // the first 64 bytes of the step's 32 rows
+        const uint32_t myid = (g & 1u) ? id1 : id0;
+        uint4* st = ra + static_cast<uint32_t>(g % kQ8Stages) * 32 * suA;
+        const uint64_t b = sbase(g);
+#pragma unroll
+        for (uint32_t t = lane; t < 32 * (kP + 1); t += 32) {
+            const uint32_t row = t / (kP + 1), col = t % (kP + 1);
+            const uint32_t id = __shfl_sync(kFull, myid, row);
+            if (b + row < mq) cp_async16(st + row * suA + col, a.q8 + uint64_t(id) * a.qrec + 16u * col);
+        }
+        if (g & 1u) id1 = load_id(g + 2);
+        else id0 = load_id(g + 2);
+        return myid;
+    };
+    uint32_t rowid0 = 0, rowid1 = 0;
+    if (steps) rowid0 = issue_a(0);
+    cp_async_commit();
+    double sl = kInf;  // this warp's k smallest upper bounds (lane i = entry i)
+    uint32_t nsurv = 0, qn = 0;
+    bool overflow = false;
+    auto tau_now = [&]() {
+        const double own = __shfl_sync(kFull, sl, a.k - 1);
+        const double shared = __longlong_as_double(static_cast<long long>(*reinterpret_cast<volatile unsigned long long*>(&tau_sh)));
+        return fmin(own, shared);
+    };
+    // stage 2 over the queued rows [0, cnt): warp-cooperative rest-of-row dot products, 4 rows at a time
+    auto drain = [&](uint32_t cnt) {
+        for (uint32_t r0 = 0; r0 < cnt; r0 += 4) {
+            uint4 x[4][2], mw[4];
+            uint32_t rid[4];
+            int rI[4];
+#pragma unroll
+            for (uint32_t u = 0; u < 4; ++u) {
+                const bool live = r0 + u < cnt;
+                rid[u] = live ? qid[r0 + u] : 0u;
+                rI[u] = live ? qI[r0 + u] : 0;
+                const int8_t* rec = a.q8 + uint64_t(rid[u]) * a.qrec + a.qsplit;
+                x[u][0] = live && lane < nr ? __ldcs(reinterpret_cast<const uint4*>(rec) + lane) : make_uint4(0, 0, 0, 0);
+                x[u][1] = live && 32 + lane < nr ? __ldcs(reinterpret_cast<const uint4*>(rec) + 32 + lane) : make_uint4(0, 0, 0, 0);
+                mw[u] = live ? __ldcs(reinterpret_cast<const uint4*>(rec) + nr) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (uint32_t u = 0; u < 4; ++u) {
+                if (r0 + u >= cnt) break;
+                int c = 0;
+#pragma unroll
+                for (uint32_t h = 0; h < 2; ++h) {
+                    c = __dp4a(static_cast<int>(x[u][h].x), qr[h][0], c);
+                    c = __dp4a(static_cast<int>(x[u][h].y), qr[h][1], c);
+                    c = __dp4a(static_cast<int>(x[u][h].z), qr[h][2], c);
+                    c = __dp4a(static_cast<int>(x[u][h].w), qr[h][3], c);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+                const int I = rI[u] + c;
+                const float rR = __uint_as_float(mw[u].y), rs = __uint_as_float(mw[u].z);  // (|a|^2, ||e_x||, s, 0)
+                double lo = 0.0, up = kInf;
+                if (qfin && rs >= 0.f)
+                    tri_bounds(static_cast<double>(rs), static_cast<double>(mw[u].x), tb2, qt, I, static_cast<double>(rR),
+                               rq, lo, up);
+                if (up < __shfl_sync(kFull, sl, a.k - 1)) {  // (uniform across the warp)
+                    list_insert_val(up, sl, a.k, lane);
+                    const double own = __shfl_sync(kFull, sl, a.k - 1);
+                    if (lane == 0 && own < kInf && own >= 0.0)
+                        atomicMin(&tau_sh, static_cast<unsigned long long>(__double_as_longlong(own)));
+                }
+                const double tau2 = tau_now();
+                if (lo <= tau2 && !overflow) {
+                    if (nsurv >= kQ8Cap) {  // drop buffered rows the tighter tau now excludes
+                        const double tau = tau_now();
+                        uint32_t kept = 0;
+                        for (uint32_t t0 = 0; t0 < nsurv; t0 += 32) {
+                            const uint32_t t = t0 + lane;
+                            const bool in = t < nsurv;
+                            const uint32_t idv = in ? sid[warp][t] : 0u;
+                            const float lv = in ? slo[warp][t] : 0.f;
+                            const bool keep = in && static_cast<double>(lv) <= tau;
+                            const uint32_t kb = __ballot_sync(kFull, keep);
+                            __syncwarp();
+                            if (keep) {
+                                const uint32_t p = kept + __popc(kb & ((1u << lane) - 1u));
+                                sid[warp][p] = idv;
+                                slo[warp][p] = lv;
+                            }
+                            kept += __popc(kb);
+                            __syncwarp();
+                        }
+                        nsurv = kept;
+                    }
+                    if (nsurv >= kQ8Cap) {
+                        overflow = true;
+                    } else {
+                        if (lane == 0) {
+                            sid[warp][nsurv] = rid[u];
+                            slo[warp][nsurv] = __double2float_rd(lo);
+                        }
+                        ++nsurv;
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+    };
+    for (uint64_t g = 0; g < steps; ++g) {
+        if (g + 1 < steps) {
+            const uint32_t v2 = issue_a(g + 1);
+            if (g & 1u) rowid0 = v2;
+            else rowid1 = v2;
+        }
+        cp_async_commit();
+        cp_async_wait<1>();  // the prefix step g has landed
+        __syncwarp();
+        // stage 1: the prefix bound of step g's rows
+        const uint32_t myid = (g & 1u) ? rowid1 : rowid0;
+        const uint4* row = ra + static_cast<uint32_t>(g % kQ8Stages) * 32 * suA + lane * suA;
+        const uint4 m0 = row[0];
+        int c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+#pragma unroll
+        for (uint32_t w = 0; w < kP; ++w) {
+            const uint4 x = row[1 + w];
+            c0 = __dp4a(static_cast<int>(x.x), qv[w][0], c0);
+            c1 = __dp4a(static_cast<int>(x.y), qv[w][1], c1);
+            c2 = __dp4a(static_cast<int>(x.z), qv[w][2], c2);
+            c3 = __dp4a(static_cast<int>(x.w), qv[w][3], c3);
+        }
+        __syncwarp();  // the slot is refilled by the next issue
+        const int IS = (c0 + c1) + (c2 + c3);
+        const float rs = __uint_as_float(m0.x), eS = __uint_as_float(m0.z);
+        const bool valid = sbase(g) + lane < mq;
+        double lb = 0.0;
+        if (qfin && rs >= 0.f) {
+            const double sv = static_cast<double>(rs);
+            const double sa = sv * sv * static_cast<double>(m0.y);
+            const double cr = 2.0 * sv * qt * static_cast<double>(IS);
+            const double V = sa + tb2S - cr - 1.1368683772161603e-13 * (sa + tb2S + fabs(cr));
+            const double r = sqrt(fmax(V, 0.0)) * (1.0 - 1e-15) - static_cast<double>(eS) - eqS;
+            lb = r > 0.0 ? r * r * (1.0 - 1e-9) : 0.0;
+        }
+        const double tau1 = tau_now();  // (every lane: the shuffle inside must not sit in an && chain)
+        const uint32_t keep = __ballot_sync(kFull, valid && lb <= tau1);
+        if (keep) {
+            if ((keep >> lane) & 1u) {
+                const uint32_t p = qn + __popc(keep & ((1u << lane) - 1u));
+                qid[p] = myid;
+                qI[p] = IS;
+            }
+            qn += __popc(keep);
+            __syncwarp();
+        }
+        if (qn >= 32) {  // stage 2 of 32 queued rows (the rest moves to the front)
+            drain(32);
+            const uint32_t r0v = 32 + lane < qn ? qid[32 + lane] : 0u;
+            const int r1v = 32 + lane < qn ? qI[32 + lane] : 0;
+            __syncwarp();
+            if (32 + lane < qn) {
+                qid[lane] = r0v;
+                qI[lane] = r1v;
+            }
+            __syncwarp();
+            qn -= 32;
+        }
+    }
+    if (qn) drain(qn);
+    cp_async_wait<0>();
+    if (overflow && lane == 0) atomicOr(&ovf, 1);
+    md[warp * 32 + lane] = sl;
+    __syncthreads();
+    if (warp == 0) {
+        for (uint32_t w = 1; w < kWarps; ++w) {
+            for (uint32_t i = 0; i < a.k; ++i) {
+                const double vv = md[w * 32 + i];
+                if (!(vv < __shfl_sync(kFull, sl, a.k - 1))) break;  // lists are sorted
+                list_insert_val(vv, sl, a.k, lane);
+            }
+        }
+        const double t = __shfl_sync(kFull, sl, a.k - 1);
+        if (lane == 0) tau_cta = t;
+    }
+    __syncthreads();
+    const double tau = tau_cta;
+    double ld = kInf;
+    uint32_t lid = 0xffffffffu;
+    float* st = reinterpret_cast<float*>(ra);  // the drained ring is staging now
+    if (ovf) {  // exact re-rank of the whole query, the warps splitting the candidates
+        const uint64_t per = (mq + kWarps - 1) / kWarps, lo = min_u64(mq, warp * per), hi = min_u64(mq, lo + per);
+        if (a.screen_stats && tid == 0) atomicAdd(a.screen_stats + 1, 1ull);
+        exact_rows(a, st, stride, qd, hi - lo,
+                   [&](uint64_t t) { return a.identity ? static_cast<uint32_t>(lo + t) : cands[lo + t]; }, ld, lid, lane);
+    } else {
+        uint32_t kept = 0;
         for (uint32_t t0 = 0; t0 < nsurv; t0 += 32) {
             const uint32_t t = t0 + lane;
             const bool in = t < nsurv;
@@ -1912,6 +2279,16 @@ cudaError_t launch_rerank(const RerankArgs& a, uint64_t nq, cudaStream_t st) {
     // screen is cheap and the int8 bounds prune little (measured, cfg1 m = 500: every candidate
     // survived the prefix bound, re-rank 0.27 ms vs 0.095 ms for the fp32 screen; cfg4 m = 50,000:
     // 7.9 ms vs 28.3 ms)
+    if (vec && !generic && pmode == 2 && a.q8 && a.qpre == 3 && a.qpad > 128 && a.qpad <= 1024 &&
+        a.m >= a.q8_min) {  // wide rows: the prefix screen with a warp-cooperative second stage
+        const uint32_t stride = 32 * ((min(a.d, kChunk) + 31) / 32) + 4;
+        const size_t rings = size_t(kQ8Stages) * 32 * 5 * 16;
+        const size_t wsmem = ((a.d * 8 + 15) / 16) * 16 + kWarps * std::max<size_t>(rings, size_t(kRows) * stride * 4);
+        e = cudaFuncSetAttribute(rerank_q8w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wsmem));
+        if (e != cudaSuccess) return e;
+        rerank_q8w_kernel<<<static_cast<unsigned>(nq), kThreads, wsmem, st>>>(a, stride);
+        return cudaGetLastError();
+    }
     if (vec && !generic && pmode == 2 && a.q8 && a.qpad >= 16 && a.qpad <= 128 && a.m >= a.q8_min) {
         const uint32_t stride = 32 * ((min(a.d, kChunk) + 31) / 32) + 4;
         const uint32_t nwq = a.qpad / 16, su = (nwq + 1) | 1u;

@@ -72,8 +72,8 @@ __global__ void pack_u8_kernel(const float* data, uint64_t n, uint32_t d, uint32
 // the screen.
 // The int8 screen's records (rerank.cu). Plain (qpre = 0): [int8 row][meta = (s, |x|^2, ||s a|| up,
 // ||e_x|| up)]. Prefix-bound layout (rerank_q8p_kernel): [meta0 = (s, |a_S|^2, ||e_x,S|| up, 0)]
-// [dims 0 .. 16 qpre), then from byte qsplit [the other dims][meta1 = (|x|^2, ||s a|| up, ||e_x|| up,
-// s)], S = the first 16 qpre dims. A row with a non-finite term gets s = -1 (always re-ranked exactly).
+// [dims 0 .. 16 qpre), then from byte qsplit [the other dims][meta1 = (|a|^2, ||e_x|| up, s, 0)],
+// S = the first 16 qpre dims. A row with a non-finite term gets s = -1 (always re-ranked exactly).
 __global__ void pack_q8_kernel(const float* __restrict__ data, uint64_t n, uint32_t d, uint32_t qpad, uint32_t qrec,
                                uint32_t qpre, uint32_t qsplit, int8_t* __restrict__ out) {
     const uint32_t kPre = 16 * qpre;  // prefix dims
@@ -127,7 +127,8 @@ __global__ void pack_q8_kernel(const float* __restrict__ data, uint64_t n, uint3
                 const uint32_t m1 = qsplit + (qpad - kPre);  // meta1 after the rest of the row
                 *reinterpret_cast<uint4*>(rec) =
                     make_uint4(__float_as_uint(fs), static_cast<uint32_t>(a2s), __float_as_uint(fRS), 0u);
-                *reinterpret_cast<float4*>(rec + m1) = make_float4(fn2, fA, fR, fs);
+                *reinterpret_cast<uint4*>(rec + m1) =
+                    make_uint4(static_cast<uint32_t>(a2), __float_as_uint(fR), __float_as_uint(fs), 0u);
                 for (uint32_t i = m1 + 16; i < qrec; ++i) rec[i] = 0;
             }
         }

@@ -470,6 +470,18 @@ def test_int8_screen_forced(gpu, oracle, ref, prefix, monkeypatch):
             ids, dd = idx2.knn_query_batch(qs2, gpu.CollisionParams(a, b, k))
             oi, od, _ = oidx2.knn_query_batch(base2, qs2, a, b, k)
             assert np.array_equal(ids, oi) and np.array_equal(dd, od), (prefix, scale, a, b, k)
+    if prefix == "3":  # wide rows (128 < d <= 1024): the prefix screen's warp-cooperative second stage
+        for d in (140, 384):
+            full = oracle.clustered(4000 + 10, d, 8, 5 + d, 0, 1, 0.05, False)
+            base4, qs4 = oracle.hold_out(full, 10, 77)
+            base4 = np.concatenate([base4, np.repeat(base4[3:4], 500, axis=0)])
+            qs4 = np.concatenate([qs4, base4[3:4]])
+            oidx4 = oracle.build_index(base4, 4, 8, 2, 42, 0)
+            idx4 = gpu.load_index(oidx4.serialize(), base4)
+            for a, b, k in ((1.0, 1.0, 10), (0.3, 0.2, 32), (0.2, 0.05, 5)):
+                ids, dd = idx4.knn_query_batch(qs4, gpu.CollisionParams(a, b, k))
+                oi, od, _ = oidx4.knn_query_batch(base4, qs4, a, b, k)
+                assert np.array_equal(ids, oi) and np.array_equal(dd, od), (prefix, d, a, b, k)
     for case in ("float", "dense_1024"):
         n, d, cl, lo, hi, sig, quant, ns, kh, it, mode, plist = CASES[case]
         full = oracle.clustered(n + 40, d, cl, 1000 + n, lo, hi, sig, quant)
