@@ -734,15 +734,41 @@ __device__ __forceinline__ void fused_pieces(const DenseArgs& a, const uint32_t*
                     gt |= eq & b[w][i] & ~TL[w][i];
                     eq &= ~(b[w][i] ^ TL[w][i]);
                 }
+                if (!need_ge) {
+                    // Past every tie cut only score > L entries are kept, and they are sparse; their order
+                    // is free (the plan and the compaction keep every one), so no transpose: each point
+                    // (lane) holding some, in turn, broadcasts its query mask and those queries' lanes
+                    // append it.
+                    const uint32_t gl = gt & live[w];  // lane = point, bit j = query 32w + j
+                    uint32_t pending = __ballot_sync(kFull, gl != 0);
+                    while (pending) {
+                        const uint32_t p = __ffs(pending) - 1;
+                        pending &= pending - 1;
+                        if ((__shfl_sync(kFull, gl, p) >> lane) & 1u) {
+                            cnt[w] += 0x10001u;  // #(score >= L) and #(score > L), recorded alike
+                            if (nb[w] < a.B) {
+                                const uint32_t v = (tb + p) | 0x8000u;
+                                if constexpr (STAGE) {
+                                    sw[w] = (sw[w] >> 16) | (static_cast<uint64_t>(v) << 48);
+                                    if ((nb[w] & 3u) == 3u) {
+                                        *reinterpret_cast<uint64_t*>(bp[w]) = sw[w];
+                                        bp[w] += 4;
+                                    }
+                                } else {
+                                    *bp[w]++ = static_cast<uint16_t>(v);
+                                }
+                            }
+                            ++nb[w];
+                        }
+                    }
+                    continue;
+                }
                 const uint32_t g1 = xp(gt & live[w]);  // lane = query, bit r = point t0 + r
                 uint32_t bits = g1;
-                if (need_ge) {
+                {
                     const uint32_t ge0 = xp((gt | eq) & live[w]);
                     cnt[w] += __popc(ge0) | (__popc(g1) << 16);
                     if (gp < cut[w]) bits = ge0;  // before the tie cut: every score >= L
-                } else {
-                    const uint32_t c1 = __popc(g1);
-                    cnt[w] += c1 | (c1 << 16);
                 }
                 if (bits) {  // id order; the capacity check once per tile while the buffer has room
                     const bool room = nb[w] + __popc(bits) <= a.B;
