@@ -1251,15 +1251,37 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_h_kernel(DenseArg
             gt |= eq & b[0] & ~T0;
             eq &= ~(b[0] ^ T0);
             // queries past the block's last have no live bits: their lanes see empty words
+            if (!need_ge) {
+                // past every tie cut: no transpose (fused_pieces); lane p's word holds point t0 + p's
+                // queries in bits 0-15 and point t0 + 32 + p's in bits 16-31, so the A points go
+                // first (id order), each appended by its query's lane of half 0, then the B points by
+                // half 1; both lanes of a query keep its count
+                const uint32_t gl = gt & live;
+                uint32_t pend = __ballot_sync(kFull, gl != 0);
+#pragma unroll
+                for (uint32_t hh = 0; hh < 2; ++hh) {
+                    uint32_t pp = pend;
+                    while (pp) {
+                        const uint32_t p = __ffs(pp) - 1;
+                        pp &= pp - 1;
+                        const uint32_t m = __shfl_sync(kFull, gl, p);
+                        if ((m >> (16 * hh + qj)) & 1u) {
+                            if (half == hh) {
+                                cnt += 0x10001u;
+                                if (nb < a.B) buf[cb_off(a, nb)] = static_cast<uint16_t>((tb0 + 32 * hh + p) | 0x8000u);
+                            }
+                            ++nb;
+                        }
+                    }
+                }
+                continue;
+            }
             const uint32_t g1 = xp(gt & live);
             uint32_t kept = g1;
-            if (need_ge) {
+            {
                 const uint32_t ge0 = xp((gt | eq) & live);
                 cnt += __popc(ge0) | (__popc(g1) << 16);
                 if (gp < cut) kept = ge0;  // before the tie cut: every score >= L
-            } else {
-                const uint32_t c1 = __popc(g1);
-                cnt += c1 | (c1 << 16);
             }
             const uint32_t c0 = __popc(kept), o0 = __shfl_xor_sync(kFull, c0, 16);
             uint32_t at = nb + (half ? o0 : 0u);
