@@ -299,7 +299,9 @@ void finalize_dense(suco_gpu_index* x, bool allow_half) {
         // loads the codes two tiles ahead of the one it scores)
         const uint64_t n_pad = (n + kMaxPiece - 1) / kMaxPiece * kMaxPiece + 128;
         x->codes.reserve(n_pad * 8);
-        CUDA_TRY(launch_dense_codes_half(x->ids.p, x->cell_off.p, n, n_pad, ns, x->K, x->codes.p, x->own));
+        x->dense_hgroup = ns == 8 && !t.dense_pair;
+        CUDA_TRY(launch_dense_codes_half(x->ids.p, x->cell_off.p, n, n_pad, ns, x->K, x->codes.p,
+                                         x->dense_hgroup ? 1u : 0u, x->own));
     } else if (x->dense) {
         x->codes.reserve((n + kDenseCodePad) * (ns > 8 ? 16 : 8));
         CUDA_TRY(launch_dense_codes(x->ids.p, x->cell_off.p, n, ns, x->K, x->codes.p, x->own));
@@ -456,6 +458,7 @@ DenseArgs dense_args(const suco_gpu_index* x, suco_gpu_query_ctx::Slot& sl, uint
     da.WP = kDensePiece;
     da.P = static_cast<uint32_t>((h.n + da.WP - 1) / da.WP);
     da.half = x->dense_half ? 1u : 0u;
+    da.hgroup = x->dense_half && x->dense_hgroup ? 1u : 0u;
     da.nc = h.layout.ns > 8 ? 2u : 1u;  // 9..16 subspaces: two code vectors, 16 histogram levels
     da.words = x->tune.dense_words;
     da.pair = x->dense_half && x->tune.dense_pair != 0 && dense_pair_supported(h.layout.ns, x->K) ? 1u : 0u;

@@ -180,6 +180,7 @@ struct suco_gpu_index {
     uint32_t qpre = 0, qsplit = 0;     // prefix-bound record layout (pack_q8_kernel)
     suco_gpu::DevBuf<uint16_t> codes;  // n x 8: s*K + cell of every point (dense select, N_s <= 8)
     bool dense = false;         // select stage = dense bit-sliced 32-query blocks (dense.cu)
+    bool dense_hgroup = false;  // ... with the interleaved table (eight subspaces, not the cluster-pair pass)
     bool dense_half = false;    // ... in the half-width mode (16-query blocks, u16 masks; large N_s*K)
     uint32_t dpad = 0;          // row bytes of data8 (0: no u8 copy)
     // block-cyclic shard: global blocks j with j % num_shards == shard

@@ -1034,7 +1034,7 @@ __device__ void build_masks_h(const DenseArgs& a, uint32_t* M, uint64_t q0, uint
             const uint32_t cnt = a.cells_off ? static_cast<uint32_t>(a.cells_off[t + 1] - a.cells_off[t]) : a.ncells[t];
             const uint32_t* cp = a.cells + (a.cells_off ? a.cells_off[t] : t * a.cells_cap);
             for (uint32_t i = lane; i < cnt; i += 32) {
-                const uint32_t slot = s * R + cp[i] + 1;
+                const uint32_t slot = a.hgroup ? ((cp[i] + 1) << 3) | s : s * R + cp[i] + 1;
                 atomicOr(M + (slot >> 1), 1u << (j + ((slot & 1u) << 4)));
             }
         }
@@ -1042,12 +1042,18 @@ __device__ void build_masks_h(const DenseArgs& a, uint32_t* M, uint64_t q0, uint
     __syncthreads();
 }
 
-// Region offsets of the 8 code positions (positions >= N_s read region 0's zero slot).
+// Slot of code c' (cell + 1) at code position j. Region layout: s * (K + 1) + c' (positions >= N_s
+// read region 0's zero slot). Interleaved layout (eight subspaces, a.hgroup): c' * 8 + s, with
+// position j holding subspace (j + p) % 8 for point p — in lookup j, lane l reads subspace
+// (j + l) % 8: subspaces 2g and 2g + 1 share 32-bit words, and each pair of subspaces owns the eight
+// banks g, g + 4, .., g + 28, eight lanes per 8-bank group instead of 32 lanes over 32 banks; the
+// slot is one shift-add of the code.
 struct RegionOff {
-    uint32_t o[8];
-    __device__ RegionOff(uint32_t ns, uint32_t K) {
+    uint32_t o[8], sh;
+    __device__ RegionOff(const DenseArgs& a, uint32_t lane) {
+        sh = a.hgroup ? 3u : 0u;
 #pragma unroll
-        for (uint32_t s = 0; s < 8; ++s) o[s] = s < ns ? s * (K + 1) : 0u;
+        for (uint32_t j = 0; j < 8; ++j) o[j] = a.hgroup ? (lane + j) & 7u : j < a.ns ? j * (a.K + 1) : 0u;
     }
 };
 
@@ -1055,8 +1061,10 @@ __device__ __forceinline__ void masks_h(const uint16_t* M16, const RegionOff& ro
     const uint32_t xa[4] = {ca.x, ca.y, ca.z, ca.w}, xb[4] = {cb.x, cb.y, cb.z, cb.w};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        m[2 * i] = uint32_t(M16[ro.o[2 * i] + (xa[i] & 0xffffu)]) | (uint32_t(M16[ro.o[2 * i] + (xb[i] & 0xffffu)]) << 16);
-        m[2 * i + 1] = uint32_t(M16[ro.o[2 * i + 1] + (xa[i] >> 16)]) | (uint32_t(M16[ro.o[2 * i + 1] + (xb[i] >> 16)]) << 16);
+        m[2 * i] = uint32_t(M16[ro.o[2 * i] + ((xa[i] & 0xffffu) << ro.sh)]) |
+                   (uint32_t(M16[ro.o[2 * i] + ((xb[i] & 0xffffu) << ro.sh)]) << 16);
+        m[2 * i + 1] = uint32_t(M16[ro.o[2 * i + 1] + ((xa[i] >> 16) << ro.sh)]) |
+                       (uint32_t(M16[ro.o[2 * i + 1] + ((xb[i] >> 16) << ro.sh)]) << 16);
     }
 }
 
@@ -1098,7 +1106,7 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_hist_h_kernel(DenseArgs
     if (lo >= a.n) return;
     const uint64_t hi = min_u64(a.n, lo + a.WP);  // rows past n are zero-code padding: score 0
     const uint16_t* M16 = reinterpret_cast<const uint16_t*>(M);
-    const RegionOff ro(a.ns, a.K);
+    const RegionOff ro(a, lane);
     const Xpose xp(lane);
     uint32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (uint64_t t0 = lo; t0 < hi; t0 += 64) {
@@ -1154,7 +1162,7 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_emit_h_kernel(DenseArgs
     uint32_t pos = mine ? a.base[q * a.P + piece] : 0u, tseen = 0;
     uint32_t* out = a.cands + q * a.m;
     const uint16_t* M16 = reinterpret_cast<const uint16_t*>(M);
-    const RegionOff ro(a.ns, a.K);
+    const RegionOff ro(a, lane);
     const Xpose xp(lane);
     for (uint64_t t0 = lo; t0 < hi; t0 += 64) {
         uint32_t b[4];
@@ -1215,7 +1223,7 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_h_kernel(DenseArg
     const uint32_t live = __ballot_sync(kFull, L != 0);
     const uint32_t cut = a.pcut && mine ? a.pcut[q0 + qj] : a.P;
     const uint16_t* M16 = reinterpret_cast<const uint16_t*>(M);
-    const RegionOff ro(a.ns, a.K);
+    const RegionOff ro(a, lane);
     const Xpose xp(lane);
     for (uint32_t k = 0; k < a.ppw; ++k) {
         const uint32_t piece = (blockIdx.y * kDW + warp) * a.ppw + k;
@@ -1511,13 +1519,16 @@ __global__ void __launch_bounds__(kDT, 1) dense_fused_pair_kernel(DenseArgs a) {
 }
 
 __global__ void dense_codes_half_kernel(const uint32_t* ids, const uint32_t* cell_off, uint64_t n, uint32_t ns,
-                                        uint32_t K, uint16_t* codes) {
+                                        uint32_t K, uint16_t* codes, uint32_t group) {
     const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
     if (t >= uint64_t(ns) * K) return;
     const uint32_t s = static_cast<uint32_t>(t / K), cell = static_cast<uint32_t>(t % K);
     const uint32_t* off = cell_off + uint64_t(s) * (K + 1);
     const uint32_t* sid = ids + uint64_t(s) * n;
-    for (uint32_t i = off[cell]; i < off[cell + 1]; ++i) codes[uint64_t(sid[i]) * 8 + s] = static_cast<uint16_t>(cell + 1);
+    for (uint32_t i = off[cell]; i < off[cell + 1]; ++i) {
+        const uint32_t pos = group ? (s - sid[i]) & 7u : s;  // interleaved layout: lane-rotated positions
+        codes[uint64_t(sid[i]) * 8 + pos] = static_cast<uint16_t>(cell + 1);
+    }
 }
 
 }  // namespace
@@ -1529,11 +1540,12 @@ bool dense_half_supported(uint32_t ns, uint32_t K) {
 static size_t dense_half_smem(uint32_t ns, uint32_t K) { return ((size_t(ns) * (K + 1) + 1) / 2) * 4; }
 
 cudaError_t launch_dense_codes_half(const uint32_t* ids, const uint32_t* cell_off, uint64_t n, uint64_t n_pad,
-                                    uint32_t ns, uint32_t K, uint16_t* codes, cudaStream_t st) {
+                                    uint32_t ns, uint32_t K, uint16_t* codes, uint32_t group, cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(codes, 0, n_pad * 8 * sizeof(uint16_t), st);
     if (e != cudaSuccess) return e;
     const uint64_t total = uint64_t(ns) * K;
-    dense_codes_half_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(ids, cell_off, n, ns, K, codes);
+    dense_codes_half_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(ids, cell_off, n, ns, K, codes,
+                                                                                       group);
     return cudaGetLastError();
 }
 

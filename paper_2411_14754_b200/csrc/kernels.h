@@ -105,6 +105,7 @@ struct DenseArgs {
     uint32_t ppw;                 // fused pass: pieces per warp (set by the launcher)
     uint32_t stage_all;           // fused pass: stage every block's stores (tests; else by density)
     uint32_t half;                // 16-query blocks, u16 masks, codes = cell + 1 per subspace (large N_s*K)
+    uint32_t hgroup;              // half-width mode, eight subspaces: interleaved table (slot c' * 8 + s, rotated codes)
     uint32_t nc;                  // uint4 code vectors per point: 1 (N_s <= 8, default) or 2 (N_s <= 16)
     uint32_t* pcut;               // single pass: nq, tie entries are stored only in pieces < pcut[q]
     uint32_t no_cut;              // tests: store every tie (pcut = P)
@@ -145,7 +146,7 @@ bool dense_half_supported(uint32_t ns, uint32_t K);
 // the cluster-pair fused pass for half-mode tables: 5..8 subspaces, 4 x (K + 1) 32-bit slots per CTA
 bool dense_pair_supported(uint32_t ns, uint32_t K);
 cudaError_t launch_dense_codes_half(const uint32_t* ids, const uint32_t* cell_off, uint64_t n, uint64_t n_pad,
-                                    uint32_t ns, uint32_t K, uint16_t* codes, cudaStream_t st);
+                                    uint32_t ns, uint32_t K, uint16_t* codes, uint32_t group, cudaStream_t st);
 cudaError_t launch_dense_codes(const uint32_t* ids, const uint32_t* cell_off, uint64_t n, uint32_t ns, uint32_t K,
                                uint16_t* codes, cudaStream_t st);
 cudaError_t launch_dense_select(const DenseArgs& a, cudaStream_t st);  // hist + plan + emit
