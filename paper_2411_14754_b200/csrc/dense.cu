@@ -855,21 +855,28 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_kernel(DenseArgs 
 // loads), places its kept ids in shared staging copies of the two runs, and the block writes the
 // runs with coalesced stores. Runs longer than a staging half write their tail directly.
 constexpr uint32_t kCompactStage = 4096;  // staged candidate ids per run (2 x 16 KB)
+// DENSE: the dense-superset queries' pieces past their tie cut (score > T entries only, a few per
+// piece: a thread each instead of a warp); else the sparse-superset queries' pieces.
+template <bool DENSE>
 __global__ void __launch_bounds__(256) dense_compact_thread_kernel(DenseArgs a) {
     __shared__ uint32_t stage[2][kCompactStage];
     __shared__ uint32_t run_lo[2], run_hi[2];
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t pbase = p * a.WP;
-    const uint32_t nlist = a.nclist[1];
+    const uint32_t nlist = a.nclist[DENSE ? 0 : 1];
     for (uint32_t j = blockIdx.y; j < nlist; j += gridDim.y) {
-        const uint64_t q = a.clist[a.nq + j];  // an unflagged query with a sparse superset
+        const uint64_t q = DENSE ? a.clist[j] : a.clist[a.nq + j];  // an unflagged query of the list
+        if constexpr (DENSE) {  // the whole block before the cut: the warp kernel has it
+            if ((blockIdx.x + 1) * blockDim.x <= a.P && gpiece(a, (blockIdx.x + 1) * blockDim.x - 1) < a.pcut[q]) continue;
+        }
         if (threadIdx.x < 2) {
             run_lo[threadIdx.x] = 0xffffffffu;
             run_hi[threadIdx.x] = 0;
         }
         __syncthreads();
         const uint64_t i = q * a.P + p;
-        const uint32_t n = p < a.P ? min(static_cast<uint32_t>(a.ccnt[i]), a.B) : 0u;
+        const bool mine = p < a.P && (!DENSE || gpiece(a, p) >= a.pcut[q]);
+        const uint32_t n = mine ? min(static_cast<uint32_t>(a.ccnt[i]), a.B) : 0u;
         uint32_t quota = 0, pos = 0, pos2 = 0;
         if (n) {
             quota = a.quota[i];
@@ -938,16 +945,24 @@ __global__ void __launch_bounds__(256) dense_compact_kernel(DenseArgs a) {
         uint64_t q;
         uint32_t n, quota, pos, pos2, x0, x1;
     };
+    const uint32_t gp = gpiece(a, p);
     auto fetch = [&](uint32_t j, Item& it) {
         it.q = a.clist[j];  // an unflagged query with a dense superset
         const uint64_t i = it.q * a.P + p;
         const uint16_t* buf = cb_base(a, it.q, p);
-        it.n = min(static_cast<uint32_t>(a.ccnt[i]), a.B);
-        it.quota = a.quota[i];
-        it.pos = a.base[i];  // score > T entries
-        it.pos2 = a.base2[i];  // ties
-        it.x0 = __ldcs(buf + cb_off(a, lane));
-        it.x1 = 32 + lane < a.B ? __ldcs(buf + cb_off(a, 32 + lane)) : 0u;
+        // pieces past the query's tie cut hold a few score > T entries: the thread kernel's (by
+        // superset density); everything else loads at once: counts, quota, offsets, two rows
+        const bool mine = a.compact_mode != 0 || !a.pcut || gp < a.pcut[it.q];
+        it.n = 0;
+        it.quota = it.pos = it.pos2 = it.x0 = it.x1 = 0;
+        if (mine) {
+            it.n = min(static_cast<uint32_t>(a.ccnt[i]), a.B);
+            it.quota = a.quota[i];
+            it.pos = a.base[i];    // score > T entries
+            it.pos2 = a.base2[i];  // ties
+            it.x0 = __ldcs(buf + cb_off(a, lane));
+            it.x1 = 32 + lane < a.B ? __ldcs(buf + cb_off(a, 32 + lane)) : 0u;
+        }
     };
     Item cur;
     if (blockIdx.y < nlist) fetch(blockIdx.y, cur);
@@ -1741,7 +1756,9 @@ cudaError_t launch_dense_fused_pass(const DenseArgs& a, cudaStream_t st) {
 // K4 of the single pass: the compaction kernels over the plan's work lists.
 cudaError_t launch_dense_compaction(const DenseArgs& a, cudaStream_t st) {
     const unsigned qrows = static_cast<unsigned>(min_u64(a.nq, 1024));  // rows walk the work lists
-    if (a.compact_mode != 2) dense_compact_thread_kernel<<<dim3((a.P + 255) / 256, qrows), 256, 0, st>>>(a);  // sparse
+    if (a.compact_mode != 2) dense_compact_thread_kernel<false><<<dim3((a.P + 255) / 256, qrows), 256, 0, st>>>(a);  // sparse
+    if (a.compact_mode == 0 && a.pcut)  // dense supersets past their tie cuts
+        dense_compact_thread_kernel<true><<<dim3((a.P + 255) / 256, qrows), 256, 0, st>>>(a);
     if (a.compact_mode != 1) {  // dense supersets: a warp per (query, piece); rows walk the work list
         // (measured at cfg4: 1024 / 4096 / 65535 grid rows -> 29.73 / 29.86 / 30.06 ms per step)
         const unsigned wrows = static_cast<unsigned>(min_u64(a.nq, a.compact_rows ? a.compact_rows : 1024));
