@@ -351,10 +351,10 @@ void finalize_dense(suco_gpu_index* x, bool allow_half) {
         x->codes.reserve(n_pad * 8);
         x->dense_hgroup = ns == 8 && !t.dense_pair;
         CUDA_TRY(launch_dense_codes_half(x->ids.p, x->cell_off.p, n, n_pad, ns, x->K, x->codes.p,
-                                         x->dense_hgroup ? 1u : 0u, x->own));
+                                         x->dense_hgroup ? 1u : 0u, t.dense_sched, x->own));
     } else if (x->dense) {
         x->codes.reserve((n + kDenseCodePad) * (ns > 8 ? 16 : 8));
-        CUDA_TRY(launch_dense_codes(x->ids.p, x->cell_off.p, n, ns, x->K, x->codes.p, x->own));
+        CUDA_TRY(launch_dense_codes(x->ids.p, x->cell_off.p, n, ns, x->K, x->codes.p, t.dense_sched, x->own));
     }
     if (!x->dense) {
         x->sel = plan_select(n, ns, t.cluster);

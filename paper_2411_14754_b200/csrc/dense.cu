@@ -1026,6 +1026,77 @@ __global__ void dense_codes_kernel(const uint32_t* ids, const uint32_t* cell_off
     }
 }
 
+// Bank-conflict schedule of a 32-point tile's lookups (grouped layout). Lookup j of the fused
+// pass reads code position j of every lane's point, and a code is its whole slot (s*K + cell in
+// the grouped form), so a point's 8 codes may sit in any order: the carry-save sum does not care.
+// A warp-wide lookup costs as many shared wavefronts as the most-loaded bank (slot & 31) among the
+// 32 lanes' slots; with the lane-rotated start (lane l reads subspace (j + l) % 8 at step j), four
+// lanes share each subspace's four banks at random: 2.95 wavefronts per lookup at cfg4. Here one
+// thread per tile reorders each point's codes by local search: swapping two positions of one
+// point moves one slot between two steps, accepted when the steps' cost (max bank load, then the
+// number of banks at that max) drops. (Two lanes reading the very same slot broadcast; the model
+// counts them twice, which only errs on the safe side.) One pass takes random tiles from 2.96 to
+// about 2.0 wavefronts per lookup in a simulation (the max-bank-degree bound is 1.67).
+// The half-width interleaved codes (v = c' * 4 + s / 2, bank v % 32) take the same search with
+// swaps restricted to positions of equal parity (HALF).
+template <bool HALF>
+__global__ void __launch_bounds__(64) dense_codes_sched_kernel(uint16_t* codes, uint64_t ntiles, uint32_t passes) {
+    const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (t >= ntiles) return;
+    uint4* row = reinterpret_cast<uint4*>(codes) + t * 32;
+    uint32_t c[32][4];  // the tile's codes, two per word (position 2i in the low half)
+    uint8_t load[8][32], hist[8][33], mx[8];
+    for (uint32_t j = 0; j < 8; ++j) {
+        for (uint32_t b = 0; b < 32; ++b) load[j][b] = 0;
+        for (uint32_t v = 0; v < 33; ++v) hist[j][v] = 0;
+    }
+    auto code = [&](uint32_t l, uint32_t j) -> uint32_t { return (c[l][j >> 1] >> (16 * (j & 1u))) & 0xffffu; };
+    for (uint32_t l = 0; l < 32; ++l) {
+        const uint4 v = row[l];
+        c[l][0] = v.x, c[l][1] = v.y, c[l][2] = v.z, c[l][3] = v.w;
+        for (uint32_t j = 0; j < 8; ++j) ++load[j][code(l, j) & 31u];
+    }
+    for (uint32_t j = 0; j < 8; ++j) {
+        mx[j] = 0;
+        for (uint32_t b = 0; b < 32; ++b) {
+            ++hist[j][load[j][b]];
+            mx[j] = max(mx[j], load[j][b]);
+        }
+    }
+    auto inc = [&](uint32_t j, uint32_t b) {
+        const uint32_t v = load[j][b]++;
+        --hist[j][v], ++hist[j][v + 1];
+        if (v + 1 > mx[j]) mx[j] = static_cast<uint8_t>(v + 1);
+    };
+    auto dec = [&](uint32_t j, uint32_t b) {
+        const uint32_t v = load[j][b]--;
+        --hist[j][v], ++hist[j][v - 1];
+        if (v == mx[j] && hist[j][v] == 0) mx[j] = static_cast<uint8_t>(v - 1);
+    };
+    auto cost = [&](uint32_t j) -> uint32_t { return mx[j] * 64u + hist[j][mx[j]]; };
+    for (uint32_t pass = 0; pass < passes; ++pass) {
+        for (uint32_t l = 0; l < 32; ++l) {
+            for (uint32_t j1 = 0; j1 < 7; ++j1) {
+                for (uint32_t j2 = j1 + (HALF ? 2 : 1); j2 < 8; j2 += HALF ? 2 : 1) {
+                    const uint32_t b1 = code(l, j1) & 31u, b2 = code(l, j2) & 31u;
+                    if (b1 == b2) continue;
+                    const uint32_t before = cost(j1) + cost(j2);
+                    dec(j1, b1), inc(j1, b2), dec(j2, b2), inc(j2, b1);
+                    if (cost(j1) + cost(j2) < before) {
+                        const uint32_t x1 = code(l, j1), x2 = code(l, j2);
+                        const uint32_t s1 = 16 * (j1 & 1u), s2 = 16 * (j2 & 1u);
+                        c[l][j1 >> 1] = (c[l][j1 >> 1] & ~(0xffffu << s1)) | (x2 << s1);
+                        c[l][j2 >> 1] = (c[l][j2 >> 1] & ~(0xffffu << s2)) | (x1 << s2);
+                    } else {
+                        dec(j1, b2), inc(j1, b1), dec(j2, b1), inc(j2, b2);
+                    }
+                }
+            }
+        }
+    }
+    for (uint32_t l = 0; l < 32; ++l) row[l] = make_uint4(c[l][0], c[l][1], c[l][2], c[l][3]);
+}
+
 // ------------------------------------------------------------ half-width mode
 // For mask tables beyond shared memory at 32 bits per slot (config 5: 8 x 10,000 cells): a CTA
 // owns 16 queries and keeps one u16 mask per (subspace, cell). Region s of the table holds K + 1
@@ -1058,17 +1129,18 @@ __device__ void build_masks_h(const DenseArgs& a, uint32_t* M, uint64_t q0, uint
 }
 
 // Slot of code c' (cell + 1) at code position j. Region layout: s * (K + 1) + c' (positions >= N_s
-// read region 0's zero slot). Interleaved layout (eight subspaces, a.hgroup): c' * 8 + s, with
-// position j holding subspace (j + p) % 8 for point p — in lookup j, lane l reads subspace
-// (j + l) % 8: subspaces 2g and 2g + 1 share 32-bit words, and each pair of subspaces owns the eight
-// banks g, g + 4, .., g + 28, eight lanes per 8-bank group instead of 32 lanes over 32 banks; the
-// slot is one shift-add of the code.
+// read region 0's zero slot). Interleaved layout (eight subspaces, a.hgroup): slot c' * 8 + s, so
+// subspaces 2g and 2g + 1 share 32-bit words and the word's bank is (4 c' + g) % 32. The code is
+// v = c' * 4 + s / 2 and the lookup at position j adds the parity (j + l) % 2 of lane l: slot =
+// 2 v + parity, one shift-add. Position j of point p holds a subspace of parity (j + p) % 2 — the
+// lane rotation s = (j + p) % 8 to start with, then reordered against bank conflicts (the bank of
+// a lookup is v % 32; dense_codes_sched_kernel swaps positions of equal parity only).
 struct RegionOff {
     uint32_t o[8], sh;
     __device__ RegionOff(const DenseArgs& a, uint32_t lane) {
-        sh = a.hgroup ? 3u : 0u;
+        sh = a.hgroup ? 1u : 0u;
 #pragma unroll
-        for (uint32_t j = 0; j < 8; ++j) o[j] = a.hgroup ? (lane + j) & 7u : j < a.ns ? j * (a.K + 1) : 0u;
+        for (uint32_t j = 0; j < 8; ++j) o[j] = a.hgroup ? (lane + j) & 1u : j < a.ns ? j * (a.K + 1) : 0u;
     }
 };
 
@@ -1540,10 +1612,10 @@ __global__ void dense_codes_half_kernel(const uint32_t* ids, const uint32_t* cel
     const uint32_t s = static_cast<uint32_t>(t / K), cell = static_cast<uint32_t>(t % K);
     const uint32_t* off = cell_off + uint64_t(s) * (K + 1);
     const uint32_t* sid = ids + uint64_t(s) * n;
-    for (uint32_t i = off[cell]; i < off[cell + 1]; ++i) {
-        const uint32_t pos = group ? (s - sid[i]) & 7u : s;  // interleaved layout: lane-rotated positions
-        codes[uint64_t(sid[i]) * 8 + pos] = static_cast<uint16_t>(cell + 1);
-    }
+    // interleaved layout: lane-rotated positions, code (cell + 1) * 4 + s / 2 (the lookup adds the
+    // position's parity, which is s's: position j of point p holds subspace (j + p) % 8)
+    const uint16_t code = static_cast<uint16_t>(group ? ((cell + 1) << 2) | (s >> 1) : cell + 1);
+    for (uint32_t i = off[cell]; i < off[cell + 1]; ++i) codes[uint64_t(sid[i]) * 8 + (group ? (s - sid[i]) & 7u : s)] = code;
 }
 
 }  // namespace
@@ -1555,12 +1627,17 @@ bool dense_half_supported(uint32_t ns, uint32_t K) {
 static size_t dense_half_smem(uint32_t ns, uint32_t K) { return ((size_t(ns) * (K + 1) + 1) / 2) * 4; }
 
 cudaError_t launch_dense_codes_half(const uint32_t* ids, const uint32_t* cell_off, uint64_t n, uint64_t n_pad,
-                                    uint32_t ns, uint32_t K, uint16_t* codes, uint32_t group, cudaStream_t st) {
+                                    uint32_t ns, uint32_t K, uint16_t* codes, uint32_t group, uint32_t sched_passes,
+                                    cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(codes, 0, n_pad * 8 * sizeof(uint16_t), st);
     if (e != cudaSuccess) return e;
     const uint64_t total = uint64_t(ns) * K;
     dense_codes_half_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(ids, cell_off, n, ns, K, codes,
                                                                                        group);
+    if (group && sched_passes) {
+        const uint64_t ntiles = (n + 31) / 32;
+        dense_codes_sched_kernel<true><<<static_cast<unsigned>((ntiles + 63) / 64), 64, 0, st>>>(codes, ntiles, sched_passes);
+    }
     return cudaGetLastError();
 }
 
@@ -1604,13 +1681,17 @@ bool dense_wide_supported(uint32_t ns, uint32_t K) {
 size_t dense_smem(uint32_t ns, uint32_t K) { return (size_t(dense_none(ns, K)) + 1) * 4; }
 
 cudaError_t launch_dense_codes(const uint32_t* ids, const uint32_t* cell_off, uint64_t n, uint32_t ns, uint32_t K,
-                               uint16_t* codes, cudaStream_t st) {
+                               uint16_t* codes, uint32_t sched_passes, cudaStream_t st) {
     const uint32_t cw = ns > 8 ? 16 : 8;
     const uint64_t count = (n + kDenseCodePad) * cw;  // the padding rows: zero-slot codes
     const unsigned fb = static_cast<unsigned>(min_u64((count + 255) / 256, 148ull * 16));
     dense_codes_fill_kernel<<<fb ? fb : 1, 256, 0, st>>>(codes, count, static_cast<uint16_t>(dense_none(ns, K)));
     const uint64_t total = uint64_t(ns) * K;
     dense_codes_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(ids, cell_off, n, ns, K, codes, cw);
+    if (dense_grouped(ns) && sched_passes) {
+        const uint64_t ntiles = (n + 31) / 32;
+        dense_codes_sched_kernel<false><<<static_cast<unsigned>((ntiles + 63) / 64), 64, 0, st>>>(codes, ntiles, sched_passes);
+    }
     return cudaGetLastError();
 }
 

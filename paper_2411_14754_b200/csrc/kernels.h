@@ -146,9 +146,10 @@ bool dense_half_supported(uint32_t ns, uint32_t K);
 // the cluster-pair fused pass for half-mode tables: 5..8 subspaces, 4 x (K + 1) 32-bit slots per CTA
 bool dense_pair_supported(uint32_t ns, uint32_t K);
 cudaError_t launch_dense_codes_half(const uint32_t* ids, const uint32_t* cell_off, uint64_t n, uint64_t n_pad,
-                                    uint32_t ns, uint32_t K, uint16_t* codes, uint32_t group, cudaStream_t st);
+                                    uint32_t ns, uint32_t K, uint16_t* codes, uint32_t group, uint32_t sched_passes,
+                                    cudaStream_t st);
 cudaError_t launch_dense_codes(const uint32_t* ids, const uint32_t* cell_off, uint64_t n, uint32_t ns, uint32_t K,
-                               uint16_t* codes, cudaStream_t st);
+                               uint16_t* codes, uint32_t sched_passes, cudaStream_t st);
 cudaError_t launch_dense_select(const DenseArgs& a, cudaStream_t st);  // hist + plan + emit
 // the single pass's stages (launch_dense_select_fused runs them; the shard protocol interleaves its exchanges)
 cudaError_t launch_dense_sample(const DenseArgs& a, cudaStream_t st);

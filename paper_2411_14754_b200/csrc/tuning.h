@@ -24,6 +24,8 @@ struct Tuning {
     int dense_pair = 0;          // SUCO_DENSE_PAIR=1: half mode's fused pass on 2-CTA clusters (measured slower at
                                  // cfg5: select 403.6 vs 389.1 ms; half the shared-memory lookups, but the
                                  // per-tile DSMEM exchange costs more than the bank conflicts it saves)
+    uint32_t dense_sched = 1;    // SUCO_DENSE_SCHED: local-search passes ordering each point's codes against bank
+                                 // conflicts (grouped layout; 0 = the plain lane rotation)
     bool dense_fused = true;     // SUCO_DENSE_FUSED=0: the two-pass dense select
     bool dense_stage = false;    // SUCO_DENSE_STAGE=1: stage every block's stores (tests)
     uint32_t dense_buf = 0;      // SUCO_DENSE_BUF: single-pass buffer entries per (piece, query); 0 = by memory

@@ -189,6 +189,8 @@ Tuning tuning_from_env() {
     t.dense = env_int("SUCO_DENSE", 1) != 0;
     t.dense_half = env_int("SUCO_DENSE_HALF", 1);
     t.dense_pair = env_int("SUCO_DENSE_PAIR", 0);
+    const int ds = env_int("SUCO_DENSE_SCHED", 1);
+    t.dense_sched = ds >= 0 && ds <= 16 ? static_cast<uint32_t>(ds) : 1u;
     t.dense_fused = env_int("SUCO_DENSE_FUSED", 1) != 0;
     t.dense_stage = std::getenv("SUCO_DENSE_STAGE") != nullptr;
     const int b = env_int("SUCO_DENSE_BUF", 0);
