@@ -739,27 +739,17 @@ __device__ __forceinline__ void fused_pieces(const DenseArgs& a, const uint32_t*
                     // is free (the plan and the compaction keep every one), so no transpose: each point
                     // (lane) holding some, in turn, broadcasts its query mask and those queries' lanes
                     // append it.
+                    // Branch-free: every lane runs the warp-uniform loop, the hit lane stores (one
+                    // predicated 2-byte store at its entry count; such pieces never stage).
                     const uint32_t gl = gt & live[w];  // lane = point, bit j = query 32w + j
                     uint32_t pending = __ballot_sync(kFull, gl != 0);
                     while (pending) {
                         const uint32_t p = __ffs(pending) - 1;
                         pending &= pending - 1;
-                        if ((__shfl_sync(kFull, gl, p) >> lane) & 1u) {
-                            cnt[w] += 0x10001u;  // #(score >= L) and #(score > L), recorded alike
-                            if (nb[w] < a.B) {
-                                const uint32_t v = (tb + p) | 0x8000u;
-                                if constexpr (STAGE) {
-                                    sw[w] = (sw[w] >> 16) | (static_cast<uint64_t>(v) << 48);
-                                    if ((nb[w] & 3u) == 3u) {
-                                        *reinterpret_cast<uint64_t*>(bp[w]) = sw[w];
-                                        bp[w] += 4;
-                                    }
-                                } else {
-                                    *bp[w]++ = static_cast<uint16_t>(v);
-                                }
-                            }
-                            ++nb[w];
-                        }
+                        const uint32_t hit = (__shfl_sync(kFull, gl, p) >> lane) & 1u;
+                        if (hit && nb[w] < a.B) bp[w][nb[w]] = static_cast<uint16_t>((tb + p) | 0x8000u);
+                        nb[w] += hit;
+                        cnt[w] += hit * 0x10001u;  // #(score >= L) and #(score > L), recorded alike
                     }
                     continue;
                 }
@@ -796,7 +786,7 @@ __device__ __forceinline__ void fused_pieces(const DenseArgs& a, const uint32_t*
         for (uint32_t w = 0; w < W; ++w) {
             if (32 * w + lane < nqb) {
                 const uint64_t i = (q0 + 32 * w + lane) * a.P + piece;
-                if constexpr (STAGE) {
+                if (STAGE && need_ge) {  // (pieces past every tie cut store each entry directly)
                     const uint32_t kept = min(nb[w], a.B), part = kept & 3u;
                     if (part)  // the last, partial chunk (at the running pointer): its entries down to the low end
                         *reinterpret_cast<uint64_t*>(bp[w]) = sw[w] >> (16 * (4 - part));
@@ -1129,29 +1119,45 @@ __device__ void build_masks_h(const DenseArgs& a, uint32_t* M, uint64_t q0, uint
 }
 
 // Slot of code c' (cell + 1) at code position j. Region layout: s * (K + 1) + c' (positions >= N_s
-// read region 0's zero slot). Interleaved layout (eight subspaces, a.hgroup): slot c' * 8 + s, so
-// subspaces 2g and 2g + 1 share 32-bit words and the word's bank is (4 c' + g) % 32. The code is
-// v = c' * 4 + s / 2 and the lookup at position j adds the parity (j + l) % 2 of lane l: slot =
-// 2 v + parity, one shift-add. Position j of point p holds a subspace of parity (j + p) % 2 — the
-// lane rotation s = (j + p) % 8 to start with, then reordered against bank conflicts (the bank of
-// a lookup is v % 32; dense_codes_sched_kernel swaps positions of equal parity only).
+// read region 0's zero slot). Interleaved layout (eight subspaces, a.hgroup; HG): slot c' * 8 + s,
+// so subspaces 2g and 2g + 1 share 32-bit words and the word's bank is (4 c' + g) % 32. The code is
+// v = c' * 4 + s / 2 and position j holds a subspace of parity j % 2, so the lookup's byte address
+// is 4 v + 2 (j % 2): the odd positions' +2 sits in the load's immediate, and the address is one
+// extraction plus one shift-add of the code. Position j of point p holds subspace (j + 2p) % 8 to
+// start with, then the codes are reordered against bank conflicts (the bank of a lookup is v % 32;
+// dense_codes_sched_kernel swaps positions of equal parity only).
 struct RegionOff {
-    uint32_t o[8], sh;
-    __device__ RegionOff(const DenseArgs& a, uint32_t lane) {
-        sh = a.hgroup ? 1u : 0u;
+    uint32_t o[8], mb;
+    __device__ RegionOff(const DenseArgs& a, const uint32_t* M) {
+        mb = static_cast<uint32_t>(__cvta_generic_to_shared(M));
 #pragma unroll
-        for (uint32_t j = 0; j < 8; ++j) o[j] = a.hgroup ? (lane + j) & 1u : j < a.ns ? j * (a.K + 1) : 0u;
+        for (uint32_t j = 0; j < 8; ++j) o[j] = j < a.ns ? j * (a.K + 1) : 0u;
     }
 };
 
+template <uint32_t IMM>
+__device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u16 %0, [%1+%2];" : "=r"(v) : "r"(addr), "n"(IMM));
+    return v;
+}
+
+template <bool HG>
 __device__ __forceinline__ void masks_h(const uint16_t* M16, const RegionOff& ro, uint4 ca, uint4 cb, uint32_t (&m)[8]) {
     const uint32_t xa[4] = {ca.x, ca.y, ca.z, ca.w}, xb[4] = {cb.x, cb.y, cb.z, cb.w};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        m[2 * i] = uint32_t(M16[ro.o[2 * i] + ((xa[i] & 0xffffu) << ro.sh)]) |
-                   (uint32_t(M16[ro.o[2 * i] + ((xb[i] & 0xffffu) << ro.sh)]) << 16);
-        m[2 * i + 1] = uint32_t(M16[ro.o[2 * i + 1] + ((xa[i] >> 16) << ro.sh)]) |
-                       (uint32_t(M16[ro.o[2 * i + 1] + ((xb[i] >> 16) << ro.sh)]) << 16);
+        if constexpr (HG) {
+            m[2 * i] = __byte_perm(lds_u16<0>(ro.mb + ((xa[i] & 0xffffu) << 2)),
+                                   lds_u16<0>(ro.mb + ((xb[i] & 0xffffu) << 2)), 0x5410);
+            m[2 * i + 1] = __byte_perm(lds_u16<2>(ro.mb + ((xa[i] >> 16) << 2)),
+                                       lds_u16<2>(ro.mb + ((xb[i] >> 16) << 2)), 0x5410);
+        } else {
+            m[2 * i] = uint32_t(M16[ro.o[2 * i] + (xa[i] & 0xffffu)]) |
+                       (uint32_t(M16[ro.o[2 * i] + (xb[i] & 0xffffu)]) << 16);
+            m[2 * i + 1] = uint32_t(M16[ro.o[2 * i + 1] + (xa[i] >> 16)]) |
+                           (uint32_t(M16[ro.o[2 * i + 1] + (xb[i] >> 16)]) << 16);
+        }
     }
 }
 
@@ -1169,15 +1175,16 @@ __device__ __forceinline__ void csa_h(const uint32_t (&m)[8], uint32_t (&b)[4]) 
     b[3] = c5 & c6;
 }
 
+template <bool HG>
 __device__ __forceinline__ void planes_h(const uint16_t* M16, const RegionOff& ro, uint4 ca, uint4 cb,
                                          uint32_t (&b)[4]) {
     uint32_t m[8];
-    masks_h(M16, ro, ca, cb, m);
+    masks_h<HG>(M16, ro, ca, cb, m);
     csa_h(m, b);
 }
 
 // K1 (half width): per (query, piece) #points with score >= t, t = 1..8.
-template <uint32_t kDT>
+template <uint32_t kDT, bool HG>
 __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_hist_h_kernel(DenseArgs a) {
     constexpr uint32_t kDW = kDT / 32;
     extern __shared__ uint32_t M[];
@@ -1193,12 +1200,12 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_hist_h_kernel(DenseArgs
     if (lo >= a.n) return;
     const uint64_t hi = min_u64(a.n, lo + a.WP);  // rows past n are zero-code padding: score 0
     const uint16_t* M16 = reinterpret_cast<const uint16_t*>(M);
-    const RegionOff ro(a, lane);
+    const RegionOff ro(a, M);
     const Xpose xp(lane);
     uint32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (uint64_t t0 = lo; t0 < hi; t0 += 64) {
         uint32_t b[4];
-        planes_h(M16, ro, __ldg(a.codes + t0 + lane), __ldg(a.codes + t0 + 32 + lane), b);
+        planes_h<HG>(M16, ro, __ldg(a.codes + t0 + lane), __ldg(a.codes + t0 + 32 + lane), b);
         const uint32_t B0 = xp(b[0]), B1 = xp(b[1]), B2 = xp(b[2]), B3 = xp(b[3]);
         const uint32_t g8 = B3, g4 = B3 | B2, g2 = g4 | B1, g1 = g2 | B0;
         const uint32_t g6 = B3 | (B2 & B1), g5 = B3 | (B2 & (B1 | B0)), g7 = B3 | (B2 & B1 & B0);
@@ -1227,7 +1234,7 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_hist_h_kernel(DenseArgs
 
 // K3 (half width): lanes c and c + 16 share query c; ties and output slots are taken in id order
 // (the first half of a tile before the second).
-template <uint32_t kDT>
+template <uint32_t kDT, bool HG>
 __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_emit_h_kernel(DenseArgs a) {
     constexpr uint32_t kDW = kDT / 32;
     extern __shared__ uint32_t M[];
@@ -1249,11 +1256,11 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_emit_h_kernel(DenseArgs
     uint32_t pos = mine ? a.base[q * a.P + piece] : 0u, tseen = 0;
     uint32_t* out = a.cands + q * a.m;
     const uint16_t* M16 = reinterpret_cast<const uint16_t*>(M);
-    const RegionOff ro(a, lane);
+    const RegionOff ro(a, M);
     const Xpose xp(lane);
     for (uint64_t t0 = lo; t0 < hi; t0 += 64) {
         uint32_t b[4];
-        planes_h(M16, ro, __ldg(a.codes + t0 + lane), __ldg(a.codes + t0 + 32 + lane), b);
+        planes_h<HG>(M16, ro, __ldg(a.codes + t0 + lane), __ldg(a.codes + t0 + 32 + lane), b);
         const uint32_t B0 = xp(b[0]), B1 = xp(b[1]), B2 = xp(b[2]), B3 = xp(b[3]);
         const uint64_t pb = t0 + 32 * half;  // this lane's first point
         const uint32_t vmask = !mine || pb >= hi ? 0u : hi - pb >= 32 ? kFull : ((1u << (hi - pb)) - 1u);
@@ -1291,7 +1298,7 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_emit_h_kernel(DenseArgs
 
 // K3' (half width): histograms + per-(query, piece) supersets in one pass (as fused_pieces, 2-byte
 // stores; lanes c and c + 16 append to query c's buffer in id order).
-template <uint32_t kDT>
+template <uint32_t kDT, bool HG>
 __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_h_kernel(DenseArgs a) {
     constexpr uint32_t kDW = kDT / 32;
     extern __shared__ uint32_t M[];
@@ -1310,7 +1317,7 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_h_kernel(DenseArg
     const uint32_t live = __ballot_sync(kFull, L != 0);
     const uint32_t cut = a.pcut && mine ? a.pcut[q0 + qj] : a.P;
     const uint16_t* M16 = reinterpret_cast<const uint16_t*>(M);
-    const RegionOff ro(a, lane);
+    const RegionOff ro(a, M);
     const Xpose xp(lane);
     for (uint32_t k = 0; k < a.ppw; ++k) {
         const uint32_t piece = (blockIdx.y * kDW + warp) * a.ppw + k;
@@ -1324,7 +1331,7 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_h_kernel(DenseArg
         const uint32_t len = static_cast<uint32_t>(hi - lo);
         const uint4* cptr = a.codes + lo + lane;
         uint32_t mk[8];
-        masks_h(M16, ro, __ldg(cptr), __ldg(cptr + 32), mk);
+        masks_h<HG>(M16, ro, __ldg(cptr), __ldg(cptr + 32), mk);
         uint4 ca = __ldg(cptr + 64), cb = __ldg(cptr + 96);
         // past every lane's tie cut only score > L is kept: one transpose per tile (the piece's
         // #(score >= L) is recorded as #(score > L), as in fused_pieces)
@@ -1335,7 +1342,7 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_h_kernel(DenseArg
             const uint4 na = __ldg(cptr + 64), nbv = __ldg(cptr + 96);
             uint32_t b[4];
             csa_h(mk, b);
-            masks_h(M16, ro, ca, cb, mk);
+            masks_h<HG>(M16, ro, ca, cb, mk);
             ca = na;
             cb = nbv;
             uint32_t gt = b[3] & ~T3, eq = ~(b[3] ^ T3);
@@ -1359,14 +1366,11 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_h_kernel(DenseArg
                     while (pp) {
                         const uint32_t p = __ffs(pp) - 1;
                         pp &= pp - 1;
-                        const uint32_t m = __shfl_sync(kFull, gl, p);
-                        if ((m >> (16 * hh + qj)) & 1u) {
-                            if (half == hh) {
-                                cnt += 0x10001u;
-                                if (nb < a.B) buf[cb_off(a, nb)] = static_cast<uint16_t>((tb0 + 32 * hh + p) | 0x8000u);
-                            }
-                            ++nb;
-                        }
+                        const uint32_t hit = (__shfl_sync(kFull, gl, p) >> (16 * hh + qj)) & 1u;  // branch-free
+                        const uint32_t own = half == hh ? hit : 0u;
+                        if (own && nb < a.B) buf[cb_off(a, nb)] = static_cast<uint16_t>((tb0 + 32 * hh + p) | 0x8000u);
+                        cnt += own * 0x10001u;
+                        nb += hit;
                     }
                 }
                 continue;
@@ -1612,10 +1616,11 @@ __global__ void dense_codes_half_kernel(const uint32_t* ids, const uint32_t* cel
     const uint32_t s = static_cast<uint32_t>(t / K), cell = static_cast<uint32_t>(t % K);
     const uint32_t* off = cell_off + uint64_t(s) * (K + 1);
     const uint32_t* sid = ids + uint64_t(s) * n;
-    // interleaved layout: lane-rotated positions, code (cell + 1) * 4 + s / 2 (the lookup adds the
-    // position's parity, which is s's: position j of point p holds subspace (j + p) % 8)
+    // interleaved layout: code (cell + 1) * 4 + s / 2 at a position of s's parity (the lookup adds
+    // the position's parity), lane-rotated: position j of point p holds subspace (j + 2p) % 8
     const uint16_t code = static_cast<uint16_t>(group ? ((cell + 1) << 2) | (s >> 1) : cell + 1);
-    for (uint32_t i = off[cell]; i < off[cell + 1]; ++i) codes[uint64_t(sid[i]) * 8 + (group ? (s - sid[i]) & 7u : s)] = code;
+    for (uint32_t i = off[cell]; i < off[cell + 1]; ++i)
+        codes[uint64_t(sid[i]) * 8 + (group ? (s - 2 * sid[i]) & 7u : s)] = code;
 }
 
 }  // namespace
@@ -1643,7 +1648,10 @@ cudaError_t launch_dense_codes_half(const uint32_t* ids, const uint32_t* cell_of
 
 template <uint32_t kDT, int KIND>  // 0 hist, 1 emit, 2 fused
 static cudaError_t launch_h_t(const DenseArgs& a, size_t smem, cudaStream_t st) {
-    auto kern = KIND == 0 ? dense_hist_h_kernel<kDT> : KIND == 1 ? dense_emit_h_kernel<kDT> : dense_fused_h_kernel<kDT>;
+    auto kern = a.hgroup ? (KIND == 0 ? dense_hist_h_kernel<kDT, true>
+                            : KIND == 1 ? dense_emit_h_kernel<kDT, true> : dense_fused_h_kernel<kDT, true>)
+                         : (KIND == 0 ? dense_hist_h_kernel<kDT, false>
+                            : KIND == 1 ? dense_emit_h_kernel<kDT, false> : dense_fused_h_kernel<kDT, false>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     constexpr uint32_t kDW = kDT / 32;
