@@ -490,7 +490,7 @@ void stage_traverse(const suco_gpu_index* x, suco_gpu_query_ctx* c, suco_gpu_que
     ta.mode = x->tune.traverse;
     if (ev) CUDA_TRY(cudaEventRecord(ev[0], st));
     CUDA_TRY(launch_traverse(ta, st));
-    c->launches += 1;
+    c->launches += traverse_launch_count(ta);
     if (ev) CUDA_TRY(cudaEventRecord(ev[1], st));
 }
 

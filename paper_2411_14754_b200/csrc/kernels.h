@@ -32,6 +32,7 @@ struct TraverseArgs {
     char mode;         // Tuning::traverse (0 = by shape)
 };
 cudaError_t launch_traverse(const TraverseArgs& a, cudaStream_t st);
+uint32_t traverse_launch_count(const TraverseArgs& a);  // kernels launch_traverse issues (1, or 2: rank + merge)
 
 // Stand-alone stages for parity tests.
 cudaError_t launch_centroid_distances(const float* d_q, uint32_t dim, const float* d_cent, uint32_t k_half,

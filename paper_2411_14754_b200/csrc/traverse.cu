@@ -367,6 +367,121 @@ __global__ void __launch_bounds__(256, 5) traverse_kernel(TraverseArgs a, uint32
 }
 
 // ---------------------------------------------------------------------------
+// Two-phase traversal (default for 6 <= k_half <= 128). The centroid distances and the O(k^2)
+// (dist, id) ranking are most of a task's instructions, and in the thread-per-task kernel they run
+// at the merge's occupancy (a few warps per SM: ~1.8 KB of merge state per task). Phase 1 ranks
+// every (query, subspace, half) with one WARP each — no per-thread state, full occupancy — and
+// leaves the ranked distances and rank -> centroid maps in a record at the tail of the task's own
+// row of the cell-list output (K words per task, of which Dynamic Activation fills ~alpha * K from
+// the front, and only after phase 2 has copied the record into shared memory). Phase 2 is the
+// thread-per-task merge alone.
+//
+// Record of task t (16-byte aligned, inside cells[t*K .. (t+1)*K)): d1r[k], d2r[k] (f64), o1[k],
+// o2[k] (u8).
+__host__ __device__ inline bool rank_rec_fits(uint32_t k, uint32_t K) { return 4ull * K >= 18ull * k + 16ull && k >= 2; }
+
+__device__ __forceinline__ unsigned char* rank_rec(uint32_t* cells, uint64_t task, uint32_t K, uint32_t k) {
+    const uintptr_t end = reinterpret_cast<uintptr_t>(cells + (task + 1) * K);
+    return reinterpret_cast<unsigned char*>((end - 18u * k) & ~static_cast<uintptr_t>(15));
+}
+
+// rank of c = #{o : (d_o, o) < (d_c, c)} for the U elements c = lane + 32u of one lane, in one pass
+// over o: every loaded value serves U independent counters. Without ties the rank is #{o : d_o <
+// d_c} — one comparison per pair. Tied elements count the same number of strictly smaller values and
+// collide in a shared-memory scatter of their ids, which the owners see when they read it back; only then the warp
+// ranks again with the id tie-break (query.cpp:56-62).
+template <uint32_t U>
+__device__ __forceinline__ void rank_warp(const double* scr, uint8_t* slot, uint32_t k, double* dr, uint8_t* ord,
+                                          uint32_t lane) {
+    double dc[U];
+    uint32_t r[U];
+#pragma unroll
+    for (uint32_t u = 0; u < U; ++u) {
+        const uint32_t c = lane + 32u * u;
+        dc[u] = c < k ? scr[c] : kInf;
+        r[u] = 0;
+    }
+#pragma unroll 8
+    for (uint32_t o = 0; o < k; ++o) {
+        const double v = scr[o];
+#pragma unroll
+        for (uint32_t u = 0; u < U; ++u) r[u] += v < dc[u];
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < U; ++u) {
+        const uint32_t c = lane + 32u * u;
+        if (c < k) slot[r[u]] = static_cast<uint8_t>(c);
+    }
+    __syncwarp();
+    bool lost = false;
+#pragma unroll
+    for (uint32_t u = 0; u < U; ++u) {
+        const uint32_t c = lane + 32u * u;
+        if (c < k) {
+            lost |= slot[r[u]] != static_cast<uint8_t>(c);
+            dr[r[u]] = dc[u];
+            ord[r[u]] = static_cast<uint8_t>(c);
+        }
+    }
+    if (__any_sync(kFull, lost)) {  // ties: exact (dist, id) ranks
+        __syncwarp();
+#pragma unroll 1
+        for (uint32_t u = 0; u < U; ++u) {
+            const uint32_t c = lane + 32u * u;
+            if (c >= k) continue;
+            const double d = scr[c];
+            uint32_t rr = 0;
+            for (uint32_t o = 0; o < k; ++o) {
+                const double v = scr[o];
+                rr += v < d || (v == d && o < c);
+            }
+            dr[rr] = d;
+            ord[rr] = static_cast<uint8_t>(c);
+        }
+    }
+}
+
+constexpr uint32_t kRankWarps = 8;
+
+// grid (ceil(nq / kRankWarps), 2 * ns): one warp per (query, subspace, half).
+template <uint32_t U>
+__global__ void __launch_bounds__(32 * kRankWarps) rank_halves_kernel(TraverseArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const uint32_t s = blockIdx.y >> 1, half = blockIdx.y & 1u, k = a.k_half;
+    const uint64_t q = static_cast<uint64_t>(blockIdx.x) * kRankWarps + warp;
+    if (q >= a.nq) return;
+    double* scr = reinterpret_cast<double*>(smem) + static_cast<size_t>(warp) * k;
+    float* qh = reinterpret_cast<float*>(reinterpret_cast<double*>(smem) + static_cast<size_t>(kRankWarps) * k) +
+                static_cast<size_t>(warp) * a.hmax;
+    uint8_t* slot = reinterpret_cast<uint8_t*>(reinterpret_cast<double*>(smem) + static_cast<size_t>(kRankWarps) * k) +
+                    static_cast<size_t>(kRankWarps) * a.hmax * 4 + static_cast<size_t>(warp) * 128;
+    const SubDesc sd = a.sub[s];
+    const uint32_t h = half ? sd.h2 : sd.h1;
+    const uint32_t* dims = a.dims + (half ? sd.dims2 : sd.dims1);
+    const float* query = a.queries + q * a.d;
+    for (uint32_t i = lane; i < h; i += 32) qh[i] = query[__ldg(dims + i)];  // project_into (subspace.cpp:83-92)
+    __syncwarp();
+    half_distances(a.cent + (half ? sd.cent2 : sd.cent1), qh, h, k, scr, lane);  // query.cpp:42-55
+    __syncwarp();
+    unsigned char* rec = rank_rec(a.cells, q * a.ns + s, a.K, k);
+    rank_warp<U>(scr, slot, k, reinterpret_cast<double*>(rec) + (half ? k : 0u), rec + 16u * k + (half ? k : 0u), lane);
+}
+
+// (ka, ra) < (kb, rb) lexicographically on the BIT PATTERNS of non-negative doubles (their integer
+// order is their numeric order, +inf above every finite value): the borrow of one 96-bit
+// subtraction — four dependent integer adds instead of two dependent FP64 compares, whose latency
+// is what a pop of the merge waits on (one warp per scheduler, nothing to hide it).
+__device__ __forceinline__ bool key_row_less(uint64_t ka, uint32_t ra, uint64_t kb, uint32_t rb) {
+    uint32_t borrow;
+    asm("{\n\t.reg .u32 t;\n\tsub.cc.u32 t, %1, %2;\n\tsubc.cc.u32 t, %3, %4;\n\tsubc.cc.u32 t, %5, %6;\n\tsubc.u32 %0, 0, 0;\n\t}"
+        : "=r"(borrow)
+        : "r"(ra), "r"(rb), "r"(static_cast<uint32_t>(ka)), "r"(static_cast<uint32_t>(kb)),
+          "r"(static_cast<uint32_t>(ka >> 32)), "r"(static_cast<uint32_t>(kb >> 32)));
+    return borrow != 0;
+}
+
+// ---------------------------------------------------------------------------
 // Thread-per-task traversal (k_half <= 128): one thread owns one (query,
 // subspace) task end to end; a CTA holds tasks of ONE subspace, so that
 // subspace's cell sizes sit in shared memory and the cumulative check never
@@ -388,8 +503,10 @@ __global__ void __launch_bounds__(256, 5) traverse_kernel(TraverseArgs a, uint32
 // SPLIT: two threads per task (adjacent lanes) compute and rank one half each — the centroid
 // distances and the O(k^2) ranking are most of a task's latency — then the even thread runs
 // Dynamic Activation alone; each half has its own ranking scratch and projected query.
-template <uint32_t L, uint32_t SP>  // SP threads per task: 1, 2 (one half each) or 4 (half a half each)
+// PRE: the halves arrive ranked (rank_halves_kernel's records); the thread only merges.
+template <uint32_t L, uint32_t SP, bool PRE = false>  // SP threads per task: 1, 2 (one half each) or 4 (half a half each)
 __global__ void traverse_thread_kernel(TraverseArgs a) {
+    static_assert(!PRE || SP == 1, "pre-ranked halves: one thread per task");
     constexpr bool SPLIT = SP > 1;
     constexpr uint32_t LOG = L == 64 ? 6 : 7;
     static_assert(L == 64 || L == 128, "leaves");
@@ -401,14 +518,15 @@ __global__ void traverse_thread_kernel(TraverseArgs a) {
     double* d2r = d1r + k * T;                        // [k][T]
     double* scr2 = d2r + k * T;                       // SPLIT: [k][T] the second half's ranking scratch
     uint32_t* cs = reinterpret_cast<uint32_t*>(scr2 + (SPLIT ? k * T : 0));  // [K] this subspace's cell sizes
-    float* qh = reinterpret_cast<float*>(cs + K);              // [hmax][T] (x2 with SPLIT)
-    uint8_t* trow = reinterpret_cast<uint8_t*>(qh + a.hmax * T * (SPLIT ? 2 : 1));  // [L][T]
+    float* qh = reinterpret_cast<float*>(cs + K);              // [hmax][T] (x2 with SPLIT; none with PRE)
+    uint8_t* trow = reinterpret_cast<uint8_t*>(qh + (PRE ? 0u : a.hmax * T * (SPLIT ? 2 : 1)));  // [L][T]
     uint8_t* o1 = trow + L * T;  // [k][T]
     uint8_t* o2 = o1 + k * T;
     uint8_t* cur = o2 + k * T;
+    const uint64_t q = static_cast<uint64_t>(blockIdx.x) * T + t;
+#pragma unroll 8
     for (uint32_t i = threadIdx.x; i < K; i += blockDim.x) cs[i] = __ldg(a.cell_size + static_cast<size_t>(s) * K + i);
     __syncthreads();
-    const uint64_t q = static_cast<uint64_t>(blockIdx.x) * T + t;
     if (q >= a.nq) return;
     const SubDesc sd = a.sub[s];
     const float* query = a.queries + q * a.d;
@@ -420,8 +538,38 @@ __global__ void traverse_thread_kernel(TraverseArgs a) {
     const uint32_t kpart = (a.k_half + 1) / 2;
     const uint32_t c_lo = SP == 4 ? (sub & 1u) * kpart : 0u, c_hi = SP == 4 ? min(a.k_half, c_lo + kpart) : a.k_half;
     const uint32_t lane = threadIdx.x & 31u;
+    if constexpr (PRE) {
+        // the task's record: 16-byte loads of the ranked distances, then the rank -> centroid bytes
+        const unsigned char* rec = rank_rec(a.cells, q * a.ns + s, K, k);
+        const double2* rd = reinterpret_cast<const double2*>(rec);
+#pragma unroll 8
+        for (uint32_t e = 0; e < k; ++e) {  // 2k doubles = k double2: d1r[0..k) then d2r[0..k)
+            const double2 v = rd[e];
+            const uint32_t e0 = 2 * e, e1 = 2 * e + 1;
+            (e0 < k ? d1r[e0 * T + t] : d2r[(e0 - k) * T + t]) = v.x;
+            (e1 < k ? d1r[e1 * T + t] : d2r[(e1 - k) * T + t]) = v.y;
+        }
+        const unsigned char* ro = rec + 16u * k;
+        if ((k & 1u) == 0) {
+            const uint16_t* r2 = reinterpret_cast<const uint16_t*>(ro);
+            for (uint32_t e = 0; e < k; e += 2) {
+                const uint32_t v1 = r2[e >> 1], v2 = r2[(k + e) >> 1];
+                o1[e * T + t] = static_cast<uint8_t>(v1);
+                o1[(e + 1) * T + t] = static_cast<uint8_t>(v1 >> 8);
+                o2[e * T + t] = static_cast<uint8_t>(v2);
+                o2[(e + 1) * T + t] = static_cast<uint8_t>(v2 >> 8);
+            }
+        } else {
+            for (uint32_t e = 0; e < k; ++e) {
+                o1[e * T + t] = ro[e];
+                o2[e * T + t] = ro[k + e];
+            }
+        }
+        // (the record sits in the tail of this task's own cell row: it is in shared memory before
+        // the merge below writes the row's first cell)
+    }
 #pragma unroll 1
-    for (uint32_t half = h_lo; half < h_hi; ++half) {
+    for (uint32_t half = PRE ? 2u : h_lo; half < h_hi; ++half) {
         const uint32_t h = half ? sd.h2 : sd.h1;
         const uint32_t* dims = a.dims + (half ? sd.dims2 : sd.dims1);
         const float* cent = a.cent + (half ? sd.cent2 : sd.cent1);
@@ -499,7 +647,9 @@ __global__ void traverse_thread_kernel(TraverseArgs a) {
         }
     }
     for (uint32_t r = 0; r < k; ++r) cur[r * T + t] = 0;
-    double wkey = __dadd_rn(d1r[t], d20);
+    constexpr uint64_t kInfBits = 0x7ff0000000000000ull;
+    uint64_t* tbits = reinterpret_cast<uint64_t*>(tkey);  // the tree's keys, compared as integers
+    uint64_t wkey = static_cast<uint64_t>(__double_as_longlong(__dadd_rn(d1r[t], d20)));
     uint32_t wrow = 0;
 
     const uint64_t task = q * a.ns + s;
@@ -509,34 +659,35 @@ __global__ void traverse_thread_kernel(TraverseArgs a) {
     uint32_t ncell = 0;
     uint64_t cum = 0;
     while (cum < a.target) {
-        if (wkey == kInf) break;  // unreachable while the IMI partitions all n points
+        if (wkey == kInfBits) break;  // unreachable while the IMI partitions all n points
         const uint32_t row = wrow, j = cur[row * T + t];
         const uint32_t cell = static_cast<uint32_t>(o1[row * T + t]) * k + o2[j * T + t];
         cum += cs[cell];
         out[ncell] = cell;
         if (dbg_sum) {
-            dbg_sum[ncell] = wkey;
+            dbg_sum[ncell] = __longlong_as_double(static_cast<long long>(wkey));
             dbg_cum[ncell] = cum;
         }
         ++ncell;
         // the row's next cell (query.cpp:113-118), then replay its leaf-to-root path
         const uint32_t j1 = j + 1;
         cur[row * T + t] = static_cast<uint8_t>(j1);
-        double ck = j1 < k ? __dadd_rn(d1r[row * T + t], d2r[j1 * T + t]) : kInf;
+        uint64_t ck = j1 < k ? static_cast<uint64_t>(__double_as_longlong(__dadd_rn(d1r[row * T + t], d2r[j1 * T + t])))
+                             : kInfBits;
         uint32_t cr = row;
         const uint32_t n0 = (row + L) >> 1;
-        double pk[LOG];
+        uint64_t pk[LOG];
         uint32_t pr[LOG];
 #pragma unroll
         for (uint32_t lv = 0; lv < LOG; ++lv) {
-            pk[lv] = tkey[(n0 >> lv) * T + t];
+            pk[lv] = tbits[(n0 >> lv) * T + t];
             pr[lv] = trow[(n0 >> lv) * T + t];
         }
 #pragma unroll
         for (uint32_t lv = 0; lv < LOG; ++lv) {
-            if (pk[lv] < ck || (pk[lv] == ck && pr[lv] < cr)) {  // the stored loser wins: swap
+            if (key_row_less(pk[lv], pr[lv], ck, cr)) {  // the stored loser wins: swap
                 const uint32_t n = n0 >> lv;
-                tkey[n * T + t] = ck;
+                tbits[n * T + t] = ck;
                 trow[n * T + t] = static_cast<uint8_t>(cr);
                 ck = pk[lv];
                 cr = pr[lv];
@@ -581,12 +732,55 @@ __global__ void da_only_kernel(const double* d1, const uint32_t* o1, const doubl
 
 static size_t da_extra_bytes(uint32_t k) { return k > 256 ? static_cast<size_t>(k) * 4 + 16 : 0; }
 
+uint32_t traverse_launch_count(const TraverseArgs& a) {
+    const char tv = a.mode;
+    return a.nq != 0 && a.k_half <= 128 && rank_rec_fits(a.k_half, a.K) && (tv == 0 || tv == 'r') ? 2u : 1u;
+}
+
 cudaError_t launch_traverse(const TraverseArgs& a, cudaStream_t st) {
     if (a.nq == 0) return cudaSuccess;
     const char tv = a.mode;  // Tuning::traverse (tests): 'w' forces the warp-per-task kernel
     const bool warp_path = tv == 'w';
     if (a.k_half <= 128 && !warp_path) {
         const uint32_t L = a.k_half <= 64 ? 64 : 128;
+        // two-phase (default): warp-per-half ranking at full occupancy, then the thread-per-task merge
+        // ('r' forces it, 't' / 's' / 'n' force the one-kernel thread path)
+        const bool two_phase = rank_rec_fits(a.k_half, a.K) && (tv == 0 || tv == 'r');
+        if (two_phase) {
+            const size_t per_t = size_t(L) * 9 + size_t(a.k_half) * 19;
+            const size_t fixed = size_t(a.K) * 4 + 16;
+            uint32_t best_T = 0, best_res = 0;
+            for (uint32_t T = 32; T <= 256; T += 32) {
+                const size_t smem = fixed + per_t * T;
+                if (smem > 227 * 1024) break;
+                const uint32_t res = static_cast<uint32_t>((228 * 1024) / (smem + 1024)) * T;
+                if (res > best_res) {
+                    best_res = res;
+                    best_T = T;
+                }
+            }
+            if (best_T) {
+                const uint32_t U = (a.k_half + 31) / 32;
+                auto rk = U == 1 ? rank_halves_kernel<1> : U == 2 ? rank_halves_kernel<2> : U == 3 ? rank_halves_kernel<3>
+                                                                                                   : rank_halves_kernel<4>;
+                const size_t rsmem = kRankWarps * (size_t(a.k_half) * 8 + size_t(a.hmax) * 4 + 128);
+                cudaError_t e = cudaSuccess;
+                if (rsmem > 48 * 1024) {
+                    e = cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rsmem));
+                    if (e != cudaSuccess) return e;
+                }
+                rk<<<dim3(static_cast<unsigned>((a.nq + kRankWarps - 1) / kRankWarps), 2 * a.ns), 32 * kRankWarps, rsmem,
+                     st>>>(a);
+                e = cudaGetLastError();
+                if (e != cudaSuccess) return e;
+                const size_t smem = fixed + per_t * best_T;
+                auto kern = L == 64 ? traverse_thread_kernel<64, 1, true> : traverse_thread_kernel<128, 1, true>;
+                e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+                if (e != cudaSuccess) return e;
+                kern<<<dim3(static_cast<unsigned>((a.nq + best_T - 1) / best_T), a.ns), best_T, smem, st>>>(a);
+                return cudaGetLastError();
+            }
+        }
         // two threads per task measured faster with short halves and small tables (cfg1/cfg2:
         // 0.64 -> 0.60 ms) and slower otherwise (cfg3, h = 30: 0.25 -> 0.34 ms; cfg4, K = 4096:
         // 1.13 -> 1.17 ms); Tuning::traverse 's' / 'n' force it

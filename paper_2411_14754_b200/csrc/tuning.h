@@ -41,7 +41,7 @@ struct Tuning {
     uint32_t tiles = 1;          // SUCO_TILES: minimum pipeline tiles per batch (tests: slot reuse)
     uint64_t scratch_bytes = 0;  // SUCO_SCRATCH_MB: query scratch budget per context (0 = from free memory)
     int fb_overlap = -1;         // SUCO_FB_OVERLAP: overlapped dense fallback (-1 auto, 0, 1)
-    char traverse = 0;           // SUCO_TRAVERSE: 0 auto, 'w' warp kernel, 's' / 'n' force / forbid split tasks
+    char traverse = 0;           // SUCO_TRAVERSE: 0 auto, 'r' rank + merge kernels, 't' one thread kernel, 'w' warp kernel, 's' / 'n' thread kernel with / without split tasks
     bool rerank_u8_regs = false; // SUCO_RERANK_U8_PIPE=0: the register byte re-rank instead of the ring
     bool rerank_tma = false;     // SUCO_RERANK_TMA=1: int8-screen rows by per-row TMA bulk copies (measured slower:
                                  // cfg4 re-rank 12.96 vs 8.58 ms with the warp's coalesced 16-byte cp.async)

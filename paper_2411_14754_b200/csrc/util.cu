@@ -212,7 +212,7 @@ Tuning tuning_from_env() {
     t.scratch_bytes = mb && std::atoll(mb) > 0 ? static_cast<uint64_t>(std::atoll(mb)) << 20 : 0;
     t.fb_overlap = std::getenv("SUCO_FB_OVERLAP") ? (env_int("SUCO_FB_OVERLAP", 0) != 0) : -1;
     const char* tv = std::getenv("SUCO_TRAVERSE");
-    t.traverse = tv && (tv[0] == 'w' || tv[0] == 's' || tv[0] == 'n') ? tv[0] : 0;
+    t.traverse = tv && (tv[0] == 'w' || tv[0] == 's' || tv[0] == 'n' || tv[0] == 't' || tv[0] == 'r') ? tv[0] : 0;
     t.rerank_u8_regs = env_int("SUCO_RERANK_U8_PIPE", 1) == 0;
     t.rerank_tma = env_int("SUCO_RERANK_TMA", 0) != 0;
     const int rp = env_int("SUCO_RERANK_PIPE", 2);

@@ -180,7 +180,7 @@ CASES = {
 }
 
 
-@pytest.mark.parametrize("trav", ["warp", "thread", "split", "nosplit"])
+@pytest.mark.parametrize("trav", ["warp", "thread", "split", "nosplit", "ranked"])
 @pytest.mark.parametrize("case", list(CASES))
 def test_knn_vs_oracle(gpu, oracle, case, trav, monkeypatch):
     """Both traversal kernels (warp per task; thread per task with the merge tree, which large batches
