@@ -919,21 +919,36 @@ __global__ void __launch_bounds__(256) dense_compact_thread_kernel(DenseArgs a) 
     }
 }
 
-// K4 (default): a warp per (query, piece). The lanes read the buffer in 32-entry rows (64
-// contiguous bytes; four rows in flight), keep every score > T entry and the first `quota` ties
-// (id order: the buffer order), and write consecutive output positions.
-__global__ void __launch_bounds__(256) dense_compact_kernel(DenseArgs a) {
+// K4 (default): a warp per (query, piece). A lane reads four consecutive entries (8 bytes; the warp
+// 128 entries = 256 contiguous bytes per load), keeps every score > T entry and the first `quota`
+// ties (id order = buffer order = (lane, h) order), and writes consecutive output positions.
+__device__ __forceinline__ uint2 cb_load4(const DenseArgs& a, const uint16_t* buf, uint32_t e, uint32_t n) {
+    uint2 v = make_uint2(0u, 0u);
+    if (e < n) {
+        if ((a.B & 3u) == 0) {  // buffers start 8-byte aligned and e + 3 < B
+            v = __ldcs(reinterpret_cast<const uint2*>(buf + e));
+        } else {
+            const uint32_t x0 = __ldcs(buf + e), x1 = e + 1 < n ? __ldcs(buf + e + 1) : 0u;
+            const uint32_t x2 = e + 2 < n ? __ldcs(buf + e + 2) : 0u, x3 = e + 3 < n ? __ldcs(buf + e + 3) : 0u;
+            v = make_uint2(x0 | (x1 << 16), x2 | (x3 << 16));
+        }
+    }
+    return v;
+}
+
+__global__ void __launch_bounds__(256, 5) dense_compact_kernel(DenseArgs a) {
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const uint32_t p = blockIdx.x * 8 + warp;
     if (p >= a.P) return;
     const uint32_t lt = (1u << lane) - 1u;
     const uint32_t pbase = p * a.WP;
     const uint32_t nlist = a.nclist[0];
-    // The next work item's counts, quota, offsets and first two rows are loaded while this one is
-    // processed (the loop is latency-bound otherwise: one dependent round trip per item).
+    // The next work item's counts, quota, offsets and first 128 entries are loaded while this one
+    // is processed (the loop is latency-bound otherwise: one dependent round trip per item).
     struct Item {
         uint64_t q;
-        uint32_t n, quota, pos, pos2, x0, x1;
+        uint32_t n, quota, pos, pos2;
+        uint2 x;
     };
     const uint32_t gp = gpiece(a, p);
     auto fetch = [&](uint32_t j, Item& it) {
@@ -941,17 +956,18 @@ __global__ void __launch_bounds__(256) dense_compact_kernel(DenseArgs a) {
         const uint64_t i = it.q * a.P + p;
         const uint16_t* buf = cb_base(a, it.q, p);
         // pieces past the query's tie cut hold a few score > T entries: the thread kernel's (by
-        // superset density); everything else loads at once: counts, quota, offsets, two rows
+        // superset density); everything else loads at once: counts, quota, offsets, 128 entries
         const bool mine = a.compact_mode != 0 || !a.pcut || gp < a.pcut[it.q];
         it.n = 0;
-        it.quota = it.pos = it.pos2 = it.x0 = it.x1 = 0;
+        it.quota = it.pos = it.pos2 = 0;
+        it.x = make_uint2(0u, 0u);
         if (mine) {
+            // the entries first, under the buffer's capacity (their count arrives with them)
+            it.x = cb_load4(a, buf, 4 * lane, a.B);
             it.n = min(static_cast<uint32_t>(a.ccnt[i]), a.B);
             it.quota = a.quota[i];
             it.pos = a.base[i];    // score > T entries
             it.pos2 = a.base2[i];  // ties
-            it.x0 = __ldcs(buf + cb_off(a, lane));
-            it.x1 = 32 + lane < a.B ? __ldcs(buf + cb_off(a, 32 + lane)) : 0u;
         }
     };
     Item cur;
@@ -963,28 +979,39 @@ __global__ void __launch_bounds__(256) dense_compact_kernel(DenseArgs a) {
         uint32_t pos = cur.pos, pos2 = cur.pos2, ties = 0;
         uint32_t* out = a.cands + cur.q * a.m;
         const uint16_t* buf = cb_base(a, cur.q, p);
-        for (uint32_t e0 = 0; e0 < n; e0 += 256) {
-            uint32_t x[8];
+        for (uint32_t e0 = 0; e0 < n; e0 += 128) {
+            const uint32_t e = e0 + 4 * lane;
+            const uint2 v = e0 == 0 ? cur.x : cb_load4(a, buf, e, n);
+            // this lane's four entries as 4-bit masks: score > T, ties (valid entries only)
+            const uint32_t nv = e < n ? min(n - e, 4u) : 0u;
+            const uint32_t vmask = (1u << nv) - 1u;
+            const uint32_t gbits = ((v.x >> 15) & 1u) | ((v.x >> 30) & 2u) | ((v.y >> 13) & 4u) | ((v.y >> 28) & 8u);
+            const uint32_t gm = gbits & vmask, tm = ~gbits & vmask;
+            // entries before this lane's in id order: one inclusive warp scan of both counts
+            const uint32_t own = __popc(gm) | (__popc(tm) << 16);
+            uint32_t inc = own;
 #pragma unroll
-            for (uint32_t u = 0; u < 8; ++u) {
-                const uint32_t e = e0 + 32 * u + lane;
-                x[u] = e0 == 0 && u == 0 ? cur.x0 : e0 == 0 && u == 1 ? cur.x1 : e < n ? __ldcs(buf + cb_off(a, e)) : 0u;
+            for (uint32_t d = 1; d < 32; d <<= 1) {
+                const uint32_t up = __shfl_up_sync(kFull, inc, d);
+                if (lane >= d) inc += up;
             }
+            const uint32_t tot = __shfl_sync(kFull, inc, 31);
+            const uint32_t before = inc - own;
+            uint32_t gpos = pos + (before & 0xffffu);
+            uint32_t tbefore = before >> 16;
+            const uint32_t room = quota > ties ? quota - ties : 0u;  // ties of this step still kept
+            const uint32_t xs[4] = {v.x & 0x7fffu, (v.x >> 16) & 0x7fffu, v.y & 0x7fffu, (v.y >> 16) & 0x7fffu};
 #pragma unroll
-            for (uint32_t u = 0; u < 8; ++u) {
-                if (e0 + 32 * u >= n) break;
-                const bool valid = e0 + 32 * u + lane < n;
-                const bool gt = valid && (x[u] & 0x8000u);
-                const bool tie = valid && !(x[u] & 0x8000u);
-                const uint32_t tb = __ballot_sync(kFull, tie);
-                const bool keep = tie && ties + __popc(tb & lt) < quota;
-                const uint32_t gb = __ballot_sync(kFull, gt), kb = __ballot_sync(kFull, keep);
-                if (gt) __stcs(out + pos + __popc(gb & lt), pbase + (x[u] & 0x7fffu));
-                if (keep) __stcs(out + pos2 + __popc(kb & lt), pbase + (x[u] & 0x7fffu));
-                pos += __popc(gb);
-                pos2 += __popc(kb);
-                ties += __popc(tb);
+            for (uint32_t h = 0; h < 4; ++h) {
+                const bool g = (gm >> h) & 1u, t = (tm >> h) & 1u;
+                if (g) __stcs(out + gpos, pbase + xs[h]);
+                if (t && tbefore < room) __stcs(out + pos2 + tbefore, pbase + xs[h]);
+                gpos += g ? 1u : 0u;
+                tbefore += t ? 1u : 0u;
             }
+            pos += tot & 0xffffu;
+            pos2 += min(tot >> 16, room);
+            ties += tot >> 16;
         }
         cur = nxt;
     }
