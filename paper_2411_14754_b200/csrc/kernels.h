@@ -30,6 +30,7 @@ struct TraverseArgs {
     uint64_t* dbg_cum; // optional, nq x ns x K
     unsigned long long* stat_cum;  // optional: += final cumulative of every traversal
     char mode;         // Tuning::traverse (0 = by shape)
+    uint32_t cs_global;  // set by launch_traverse: the merge kernel reads cell sizes from global memory
 };
 cudaError_t launch_traverse(const TraverseArgs& a, cudaStream_t st);
 uint32_t traverse_launch_count(const TraverseArgs& a);  // kernels launch_traverse issues (1, or 2: rank + merge)

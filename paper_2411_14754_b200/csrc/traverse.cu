@@ -518,14 +518,20 @@ __global__ void traverse_thread_kernel(TraverseArgs a) {
     double* d2r = d1r + k * T;                        // [k][T]
     double* scr2 = d2r + k * T;                       // SPLIT: [k][T] the second half's ranking scratch
     uint32_t* cs = reinterpret_cast<uint32_t*>(scr2 + (SPLIT ? k * T : 0));  // [K] this subspace's cell sizes
-    float* qh = reinterpret_cast<float*>(cs + K);              // [hmax][T] (x2 with SPLIT; none with PRE)
+    // PRE with cs_global: the cell sizes stay in global memory (L2; the cumulative check is off the
+    // merge's critical path) and their K words of shared memory go to more resident tasks
+    const bool csg = PRE && a.cs_global != 0;
+    const uint32_t* csz = a.cell_size + static_cast<size_t>(s) * K;
+    float* qh = reinterpret_cast<float*>(cs + (csg ? 0u : K));  // [hmax][T] (x2 with SPLIT; none with PRE)
     uint8_t* trow = reinterpret_cast<uint8_t*>(qh + (PRE ? 0u : a.hmax * T * (SPLIT ? 2 : 1)));  // [L][T]
     uint8_t* o1 = trow + L * T;  // [k][T]
     uint8_t* o2 = o1 + k * T;
     uint8_t* cur = o2 + k * T;
     const uint64_t q = static_cast<uint64_t>(blockIdx.x) * T + t;
+    if (!csg) {
 #pragma unroll 8
-    for (uint32_t i = threadIdx.x; i < K; i += blockDim.x) cs[i] = __ldg(a.cell_size + static_cast<size_t>(s) * K + i);
+        for (uint32_t i = threadIdx.x; i < K; i += blockDim.x) cs[i] = __ldg(csz + i);
+    }
     __syncthreads();
     if (q >= a.nq) return;
     const SubDesc sd = a.sub[s];
@@ -662,7 +668,7 @@ __global__ void traverse_thread_kernel(TraverseArgs a) {
         if (wkey == kInfBits) break;  // unreachable while the IMI partitions all n points
         const uint32_t row = wrow, j = cur[row * T + t];
         const uint32_t cell = static_cast<uint32_t>(o1[row * T + t]) * k + o2[j * T + t];
-        cum += cs[cell];
+        cum += csg ? __ldg(csz + cell) : cs[cell];
         out[ncell] = cell;
         if (dbg_sum) {
             dbg_sum[ncell] = __longlong_as_double(static_cast<long long>(wkey));
@@ -748,15 +754,22 @@ cudaError_t launch_traverse(const TraverseArgs& a, cudaStream_t st) {
         const bool two_phase = rank_rec_fits(a.k_half, a.K) && (tv == 0 || tv == 'r');
         if (two_phase) {
             const size_t per_t = size_t(L) * 9 + size_t(a.k_half) * 19;
-            const size_t fixed = size_t(a.K) * 4 + 16;
+            // most resident tasks per SM, the cell sizes staged in shared memory or left in global
+            size_t fixed = 16;
             uint32_t best_T = 0, best_res = 0;
-            for (uint32_t T = 32; T <= 256; T += 32) {
-                const size_t smem = fixed + per_t * T;
-                if (smem > 227 * 1024) break;
-                const uint32_t res = static_cast<uint32_t>((228 * 1024) / (smem + 1024)) * T;
-                if (res > best_res) {
-                    best_res = res;
-                    best_T = T;
+            bool cs_global = false;
+            for (int g = 0; g < 2; ++g) {
+                const size_t fx = g ? 16 : size_t(a.K) * 4 + 16;
+                for (uint32_t T = 32; T <= 256; T += 32) {
+                    const size_t smem = fx + per_t * T;
+                    if (smem > 227 * 1024) break;
+                    const uint32_t res = static_cast<uint32_t>((228 * 1024) / (smem + 1024)) * T;
+                    if (res > best_res) {
+                        best_res = res;
+                        best_T = T;
+                        fixed = fx;
+                        cs_global = g != 0;
+                    }
                 }
             }
             if (best_T) {
@@ -777,7 +790,9 @@ cudaError_t launch_traverse(const TraverseArgs& a, cudaStream_t st) {
                 auto kern = L == 64 ? traverse_thread_kernel<64, 1, true> : traverse_thread_kernel<128, 1, true>;
                 e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
                 if (e != cudaSuccess) return e;
-                kern<<<dim3(static_cast<unsigned>((a.nq + best_T - 1) / best_T), a.ns), best_T, smem, st>>>(a);
+                TraverseArgs b = a;
+                b.cs_global = cs_global ? 1u : 0u;
+                kern<<<dim3(static_cast<unsigned>((a.nq + best_T - 1) / best_T), a.ns), best_T, smem, st>>>(b);
                 return cudaGetLastError();
             }
         }
