@@ -38,7 +38,7 @@ PIPE_METRICS = {
 def stage_of(name: str):
     if name.startswith("dense_codes") or name.startswith("pack_"):
         return None  # index build
-    if name.startswith("traverse"):
+    if name.startswith(("traverse", "rank_halves")):
         return "traverse"
     if name.startswith(("dense_", "select_", "shard_")):
         return "select"
