@@ -886,6 +886,7 @@ __global__ void __launch_bounds__(256) dense_compact_thread_kernel(DenseArgs a) 
             for (uint32_t u = 0; u < 8; ++u) v[u] = e0 + 8 * u < n ? __ldcs(buf + (e0 >> 3) + u) : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
             for (uint32_t u = 0; u < 8; ++u) {
+                if (e0 + 8 * u >= n) break;  // (pieces past the tie cut hold a few entries: one or two words)
                 const uint32_t w4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
                 for (uint32_t h = 0; h < 8; ++h) {
@@ -922,6 +923,13 @@ __global__ void __launch_bounds__(256) dense_compact_thread_kernel(DenseArgs a) 
 // K4 (default): a warp per (query, piece). A lane reads four consecutive entries (8 bytes; the warp
 // 128 entries = 256 contiguous bytes per load), keeps every score > T entry and the first `quota`
 // ties (id order = buffer order = (lane, h) order), and writes consecutive output positions.
+__device__ __forceinline__ void st_cs_if(bool p, uint32_t* addr, uint32_t v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q st.global.cs.u32 [%1], %2;\n\t}"
+                 :
+                 : "r"(static_cast<uint32_t>(p)), "l"(addr), "r"(v)
+                 : "memory");
+}
+
 __device__ __forceinline__ uint2 cb_load4(const DenseArgs& a, const uint16_t* buf, uint32_t e, uint32_t n) {
     uint2 v = make_uint2(0u, 0u);
     if (e < n) {
@@ -1004,8 +1012,8 @@ __global__ void __launch_bounds__(256, 5) dense_compact_kernel(DenseArgs a) {
 #pragma unroll
             for (uint32_t h = 0; h < 4; ++h) {
                 const bool g = (gm >> h) & 1u, t = (tm >> h) & 1u;
-                if (g) __stcs(out + gpos, pbase + xs[h]);
-                if (t && tbefore < room) __stcs(out + pos2 + tbefore, pbase + xs[h]);
+                st_cs_if(g, out + gpos, pbase + xs[h]);  // predicated stores: no branch per entry
+                st_cs_if(t && tbefore < room, out + pos2 + tbefore, pbase + xs[h]);
                 gpos += g ? 1u : 0u;
                 tbefore += t ? 1u : 0u;
             }

@@ -179,7 +179,7 @@ def test_sampled_build_errors(gpu):
 
 def test_sampled_cfg5_shape_query_vs_reference(gpu, ref):
     """Config 5's shape scaled down (u8 descriptors, N_s = 8, 100 x 100 centroids on a 1 % sample,
-    alpha = 0.02, beta = 0.002): K = 10,000 cells per subspace takes the cluster-counting select.
+    alpha = 0.02, beta = 0.002): K = 10,000 cells per subspace takes the half-width dense select (u16 masks, two points per lane).
     The reference's own load_index + knn_query on the GPU-built bytes give the same answers."""
     import bench_data
 
