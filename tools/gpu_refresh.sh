@@ -9,6 +9,6 @@ timeout 1200 python bench.py > $O/${TAG}_bench_cfg4.json 2> $O/${TAG}_bench_cfg4
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $O/${TAG}_bench_cfg4_reference_arm.json 2> $O/${TAG}_ref.err
 for c in cfg1 cfg2 cfg3; do timeout 1500 python bench.py --config $c > $O/${TAG}_bench_$c.json 2> $O/${TAG}_bench_$c.err; done
 bash tools/profile_cfg.sh cfg4 $TAG
-timeout 3000 python bench.py --config cfg5 --steps 3 --warmup 3 > $O/${TAG}_bench_cfg5.json 2> $O/${TAG}_bench_cfg5.err
+timeout 4000 python bench.py --config cfg5 --steps 3 --warmup 3 ${CFG5_ARGS:-} > $O/${TAG}_bench_cfg5.json 2> $O/${TAG}_bench_cfg5.err
 python tools/ab_summary.py $O/${TAG}_bench_cfg*.json
 echo done
