@@ -84,14 +84,16 @@ def ncu_traffic(workload: str) -> dict:
 
 def rerank_row_bytes(base, queries, m=None):
     """Bytes the re-rank reads per candidate row: the u8 copy (d padded to 16) for u8-valued data,
-    else the int8 screen record (d padded to 16, + 16 bytes of bound terms, padded to 64) when
-    d % 4 == 0 and d <= 128 (capi.cu upload_data), else the f32 row."""
+    else the int8 screen record (d padded to 16, + 16 bytes of bound terms, padded to 64; from d = 49
+    up only its first 64 bytes for most rows) when d % 4 == 0 and d <= 1024 and the candidate lists
+    are long enough for the int8 screen (capi.cu upload_data, launch_rerank), else the f32 row."""
     d = base.shape[1]
     u8 = u8_row_bytes(base, queries)
     if u8:
         return u8, "u8 rows"
-    if d % 4 == 0 and d <= 128 and not os.environ.get("SUCO_Q8") == "0" and (m is None or m >= 8192):
-        if d > 48:  # the prefix-bound layout: the first 64 bytes of every record, the rest for a few
+    if d % 4 == 0 and d <= 1024 and not os.environ.get("SUCO_Q8") == "0" and (m is None or m >= 8192):
+        if d > 48:  # the prefix-bound layout (rerank_q8p_kernel, rerank_q8w_kernel for d > 128): the first
+            # 64 bytes of every record, the rest for the few rows past the prefix bound
             return 64, "int8 screen record prefixes (+ the rest of the rows past the prefix bound)"
         return ((d + 15) // 16 * 16 + 16 + 63) // 64 * 64, "int8 screen records (+ exact f32 rows of the survivors)"
     return 4 * d, "f32 rows"

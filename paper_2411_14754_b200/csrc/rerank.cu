@@ -1049,6 +1049,26 @@ __device__ __forceinline__ void tri_bounds(double s, double a2, double tb2, doub
     up = rhi * rhi * (1.0 + 1e-9);
 }
 
+// Stage 1 of the prefix screens without a square root per row. The prefix bound is lb = r^2 (1 - 1e-9)
+// with r = sqrt(max(V, 0)) (1 - 1e-15) - e_S - e_qS (0 when r <= 0), and a row is queued when
+// lb <= tau. Every such row satisfies sqrt(V) (1 - 2e-15) <= rt + e_S + e_qS with
+// rt = sqrt(tau (1 + 3e-9)) (1 + 1e-15), i.e. V (1 - 4e-14) <= (rt + e_S + e_qS)^2 with room for the
+// roundings on both sides: the test below keeps a superset of the rows the bound keeps, so it is as
+// certified as the bound, and the square root is taken once per change of tau instead of per row.
+struct PrefixGate {
+    double tau = -1.0, rtq = kInf;  // the tau the gate was built for; rt + e_qS
+    __device__ __forceinline__ void update(double tau_new, double eqS) {
+        if (tau_new != tau) {
+            tau = tau_new;
+            rtq = tau_new < kInf ? sqrt(tau_new * (1.0 + 3e-9)) * (1.0 + 1e-15) + eqS : kInf;
+        }
+    }
+    __device__ __forceinline__ bool keeps(double V, float eS) const {
+        const double c = rtq + static_cast<double>(eS);
+        return !(fmax(V, 0.0) * (1.0 - 4e-14) > c * c);  // (NaN: kept, as the bound's lb = 0 is)
+    }
+};
+
 template <uint32_t kQ8P, uint32_t NR>  // prefix words (16 dims each), rest words: NW = kQ8P + NR
 __global__ void __launch_bounds__(kThreads, 2) rerank_q8p_kernel(RerankArgs a, uint32_t stride) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -1181,6 +1201,7 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_q8p_kernel(RerankArgs a, u
         const double shared = __longlong_as_double(static_cast<long long>(*reinterpret_cast<volatile unsigned long long*>(&tau_sh)));
         return fmin(own, shared);
     };
+    PrefixGate gate;
     for (uint64_t g = 0; g < steps || fcnt || qn; ++g) {
         if (g + 1 < steps) {
             const uint32_t v = issue_a(g + 1);
@@ -1301,17 +1322,16 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_q8p_kernel(RerankArgs a, u
             const int IS = (c0 + c1) + (c2 + c3);
             const float rs = __uint_as_float(m0.x), eS = __uint_as_float(m0.z);
             const bool valid = sbase(g) + lane < mq;
-            double lb = 0.0;
+            gate.update(tau_now(), eqS);
+            bool under = true;  // the prefix bound is within tau (PrefixGate: no square root per row)
             if (qfin && rs >= 0.f) {
                 const double s = static_cast<double>(rs);
                 const double sa = s * s * static_cast<double>(m0.y);  // |a_S|^2: an exact integer
                 const double cr = 2.0 * s * qt * static_cast<double>(IS);
                 const double V = sa + tb2S - cr - 1.1368683772161603e-13 * (sa + tb2S + fabs(cr));  // 2^-43 slack
-                const double r = sqrt(fmax(V, 0.0)) * (1.0 - 1e-15) - static_cast<double>(eS) - eqS;
-                lb = r > 0.0 ? r * r * (1.0 - 1e-9) : 0.0;
+                under = gate.keeps(V, eS);
             }
-            const double tau = tau_now();
-            const uint32_t keep = __ballot_sync(kFull, valid && lb <= tau);
+            const uint32_t keep = __ballot_sync(kFull, valid && under);
             if (keep) {
                 if ((keep >> lane) & 1u) {
                     const uint32_t p = qn + __popc(keep & ((1u << lane) - 1u));
@@ -1620,6 +1640,7 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_q8w_kernel(RerankArgs a, u
             }
         }
     };
+    PrefixGate gate;
     for (uint64_t g = 0; g < steps; ++g) {
         if (g + 1 < steps) {
             const uint32_t v2 = issue_a(g + 1);
@@ -1646,17 +1667,16 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_q8w_kernel(RerankArgs a, u
         const int IS = (c0 + c1) + (c2 + c3);
         const float rs = __uint_as_float(m0.x), eS = __uint_as_float(m0.z);
         const bool valid = sbase(g) + lane < mq;
-        double lb = 0.0;
+        gate.update(tau_now(), eqS);  // (every lane: the shuffle inside must not sit in an && chain)
+        bool under = true;  // the prefix bound is within tau (PrefixGate: no square root per row)
         if (qfin && rs >= 0.f) {
             const double sv = static_cast<double>(rs);
             const double sa = sv * sv * static_cast<double>(m0.y);
             const double cr = 2.0 * sv * qt * static_cast<double>(IS);
             const double V = sa + tb2S - cr - 1.1368683772161603e-13 * (sa + tb2S + fabs(cr));
-            const double r = sqrt(fmax(V, 0.0)) * (1.0 - 1e-15) - static_cast<double>(eS) - eqS;
-            lb = r > 0.0 ? r * r * (1.0 - 1e-9) : 0.0;
+            under = gate.keeps(V, eS);
         }
-        const double tau1 = tau_now();  // (every lane: the shuffle inside must not sit in an && chain)
-        const uint32_t keep = __ballot_sync(kFull, valid && lb <= tau1);
+        const uint32_t keep = __ballot_sync(kFull, valid && under);
         if (keep) {
             if ((keep >> lane) & 1u) {
                 const uint32_t p = qn + __popc(keep & ((1u << lane) - 1u));
