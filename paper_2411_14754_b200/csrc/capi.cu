@@ -267,6 +267,7 @@ void upload_data(suco_gpu_index* x, const float* data, uint64_t n, uint32_t d) {
         x->qsplit = x->qpre ? (16 + 16 * x->qpre + 31) / 32 * 32 : 0u;
         x->qrec = x->qpre ? (x->qsplit + (nw - x->qpre + 1) * 16 + 63) / 64 * 64 : (x->qpad + 16 + 63) / 64 * 64;
         x->q8.reserve(n * x->qrec);
+        x->q8_rows = n;
         CUDA_TRY(launch_pack_q8(x->data.p, n, d, x->qpad, x->qrec, x->qpre, x->qsplit, x->q8.p, x->own));
         CUDA_TRY(cudaStreamSynchronize(x->own));
     }
@@ -528,6 +529,7 @@ void rerank_args(const suco_gpu_index* x, RerankArgs& ra) {
     ra.qpre = x->qpre;
     ra.q8_min = x->tune.q8 == 2 ? 0 : kQ8MinCands;
     ra.qsplit = x->qsplit;
+    ra.q8b = x->qpad ? x->q8.p + x->q8_rows * x->qsplit : nullptr;
     ra.u8_regs = x->tune.rerank_u8_regs;
     ra.no_tma = !x->tune.rerank_tma;
     ra.pipe = x->tune.rerank_pipe == 2 ? 0 : x->tune.rerank_pipe == 1 ? 1 : 2;

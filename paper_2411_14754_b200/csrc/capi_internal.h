@@ -178,6 +178,7 @@ struct suco_gpu_index {
     suco_gpu::DevBuf<int8_t> q8;       // int8 screen records of float rows (n x qrec; rerank_q8_kernel)
     uint32_t qpad = 0, qrec = 0;       // int8 bytes / record stride (0: no int8 copy)
     uint32_t qpre = 0, qsplit = 0;     // prefix-bound record layout (pack_q8_kernel)
+    uint64_t q8_rows = 0;              // rows in q8 (the rests of prefix-bound records start at q8_rows * qsplit)
     suco_gpu::DevBuf<uint16_t> codes;  // n x 8: s*K + cell of every point (dense select, N_s <= 8)
     bool dense = false;         // select stage = dense bit-sliced 32-query blocks (dense.cu)
     bool dense_hgroup = false;  // ... with the interleaved table (eight subspaces, not the cluster-pair pass)

@@ -360,11 +360,11 @@ int suco_gpu_make_shard(const suco_gpu_index* full, uint32_t shard, uint32_t num
                     CUDA_TRY(cudaMemcpyAsync(x->data8.p + lo * x->dpad, full->data8.p + j * block * x->dpad,
                                              len * x->dpad, cudaMemcpyDeviceToDevice, x->own));
                 }
-                if (x->qpad) {
-                    CUDA_TRY(cudaMemcpyAsync(x->q8.p + lo * x->qrec, full->q8.p + j * block * x->qrec, len * x->qrec,
-                                             cudaMemcpyDeviceToDevice, x->own));
-                }
                 lo += len;
+            }
+            if (x->qpad) {  // the int8 records of the owned rows, packed from them (a row's record depends on the row alone)
+                x->q8_rows = n_local;
+                CUDA_TRY(launch_pack_q8(x->data.p, n_local, d, x->qpad, x->qrec, x->qpre, x->qsplit, x->q8.p, x->own));
             }
             upload_codebooks(x);
             x->K = full->K;

@@ -208,7 +208,8 @@ struct RerankArgs {
     uint32_t qrec;          // record stride (qpad + 16 rounded up to 64)
     uint32_t qpre;          // prefix-bound layout: prefix words (16 dims each; 0 = plain records)
     uint64_t q8_min;        // candidates per query from which the int8 screen is used (kQ8MinCands; tests: 0)
-    uint32_t qsplit;        // byte offset of the rest of the row (the second read of rerank_q8p_kernel)
+    uint32_t qsplit;        // prefix-bound layout: bytes of a record's prefix part (stride of the prefix array)
+    const int8_t* q8b;      // prefix-bound layout: the rests of the records (q8 + rows * qsplit), stride qrec - qsplit
     bool no_tma;            // !Tuning::rerank_tma: 16-byte cp.async row gathers instead of per-row TMA bulk copies
     unsigned long long* screen_stats;  // optional diagnostics: [0] += exact re-ranks, [1] += queries re-ranked in full
     bool u8_regs;           // Tuning::rerank_u8_regs: the register byte kernel instead of the smem ring

@@ -1017,10 +1017,11 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_q8_kernel(RerankArgs a, ui
 }
 
 // ------------------------------------------- int8 screen with a prefix bound (NW >= 4)
-// Record (qrec bytes, a multiple of 64): [meta0][dims 0 .. 16 kQ8P) in the first qsplit bytes (32
-// for one prefix word, 64 for three), then [dims 16 kQ8P .. 16 NW)[meta1]; meta0 = (s, |a_S|^2
+// Record (qrec bytes, a multiple of 64) in two arrays: [meta0][dims 0 .. 16 kQ8P) — qsplit bytes (32
+// for one prefix word, 64 for three), the n prefix parts back to back at q8 — and
+// [dims 16 kQ8P .. 16 NW)[meta1] at q8b, stride qrec - qsplit; meta0 = (s, |a_S|^2
 // (u32 bits), ||e_x,S|| up, 0), meta1 = (|a|^2 (u32 bits), ||e_x|| up, s, 0), S = the prefix dims.
-// Stage 1 reads the first qsplit bytes of every candidate. The prefix alone bounds the distance from below:
+// Stage 1 reads the prefix part of every candidate. The prefix alone bounds the distance from below:
 //     D >= sum_{i in S} (x_i - q_i)^2 >= (||s a_S - t b_S|| - ||e_x,S|| - ||e_q,S||)^2,
 //     ||s a_S - t b_S||^2 = s^2 |a_S|^2 + t^2 |b_S|^2 - 2 s t (a_S . b_S),   a_S . b_S exact (IDP.4A)
 // (at cfg4 the first 24 of 96 dims rule out about 98 % of the candidates against the final k-th
@@ -1173,7 +1174,7 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_q8p_kernel(RerankArgs a, u
         for (uint32_t t = lane; t < 32 * (kQ8P + 1); t += 32) {
             const uint32_t row = t / (kQ8P + 1), col = t % (kQ8P + 1);
             const uint32_t id = __shfl_sync(kFull, myid, row);
-            if (b + row < mq) cp_async16(st + row * suA + col, a.q8 + uint64_t(id) * a.qrec + 16u * col);
+            if (b + row < mq) cp_async16(st + row * suA + col, a.q8 + uint64_t(id) * a.qsplit + 16u * col);
         }
         if (g & 1u) id1 = load_id(g + 2);
         else id0 = load_id(g + 2);
@@ -1185,7 +1186,7 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_q8p_kernel(RerankArgs a, u
         for (uint32_t t = lane; t < 32 * (NR + 1); t += 32) {
             const uint32_t row = t / (NR + 1), col = t % (NR + 1);
             const uint32_t id = __shfl_sync(kFull, bid, row);
-            if (row < cnt) cp_async16(st + row * suB + col, a.q8 + uint64_t(id) * a.qrec + a.qsplit + 16u * col);
+            if (row < cnt) cp_async16(st + row * suB + col, a.q8b + uint64_t(id) * (a.qrec - a.qsplit) + 16u * col);
         }
     };
     uint32_t rowid0 = 0, rowid1 = 0;
@@ -1545,7 +1546,7 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_q8w_kernel(RerankArgs a, u
         for (uint32_t t = lane; t < 32 * (kP + 1); t += 32) {
             const uint32_t row = t / (kP + 1), col = t % (kP + 1);
             const uint32_t id = __shfl_sync(kFull, myid, row);
-            if (b + row < mq) cp_async16(st + row * suA + col, a.q8 + uint64_t(id) * a.qrec + 16u * col);
+            if (b + row < mq) cp_async16(st + row * suA + col, a.q8 + uint64_t(id) * a.qsplit + 16u * col);
         }
         if (g & 1u) id1 = load_id(g + 2);
         else id0 = load_id(g + 2);
@@ -1573,7 +1574,7 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_q8w_kernel(RerankArgs a, u
                 const bool live = r0 + u < cnt;
                 rid[u] = live ? qid[r0 + u] : 0u;
                 rI[u] = live ? qI[r0 + u] : 0;
-                const int8_t* rec = a.q8 + uint64_t(rid[u]) * a.qrec + a.qsplit;
+                const int8_t* rec = a.q8b + uint64_t(rid[u]) * (a.qrec - a.qsplit);
                 x[u][0] = live && lane < nr ? __ldcs(reinterpret_cast<const uint4*>(rec) + lane) : make_uint4(0, 0, 0, 0);
                 x[u][1] = live && 32 + lane < nr ? __ldcs(reinterpret_cast<const uint4*>(rec) + 32 + lane) : make_uint4(0, 0, 0, 0);
                 mw[u] = live ? __ldcs(reinterpret_cast<const uint4*>(rec) + nr) : make_uint4(0, 0, 0, 0);

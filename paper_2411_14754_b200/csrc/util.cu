@@ -72,8 +72,12 @@ __global__ void pack_u8_kernel(const float* data, uint64_t n, uint32_t d, uint32
 // the screen.
 // The int8 screen's records (rerank.cu). Plain (qpre = 0): [int8 row][meta = (s, |x|^2, ||s a|| up,
 // ||e_x|| up)]. Prefix-bound layout (rerank_q8p_kernel): [meta0 = (s, |a_S|^2, ||e_x,S|| up, 0)]
-// [dims 0 .. 16 qpre), then from byte qsplit [the other dims][meta1 = (|a|^2, ||e_x|| up, s, 0)],
-// S = the first 16 qpre dims. A row with a non-finite term gets s = -1 (always re-ranked exactly).
+// [dims 0 .. 16 qpre) in qsplit bytes, and [the other dims][meta1 = (|a|^2, ||e_x|| up, s, 0)] in
+// qrec - qsplit bytes, S = the first 16 qpre dims. The two parts are two arrays: the n prefix parts
+// back to back (stride qsplit: every candidate's first read — random accesses cost DRAM per access,
+// not per byte (profiles/r02_gather_peak.json), so the dense array is what L2 and the DRAM pages
+// see), then the n rests (stride qrec - qsplit, from byte n * qsplit). A row with a non-finite
+// term gets s = -1 (always re-ranked exactly).
 __global__ void pack_q8_kernel(const float* __restrict__ data, uint64_t n, uint32_t d, uint32_t qpad, uint32_t qrec,
                                uint32_t qpre, uint32_t qsplit, int8_t* __restrict__ out) {
     const uint32_t kPre = 16 * qpre;  // prefix dims
@@ -82,7 +86,9 @@ __global__ void pack_q8_kernel(const float* __restrict__ data, uint64_t n, uint3
     const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x / 32);
     for (uint64_t r = blockIdx.x * uint64_t(blockDim.x / 32) + (threadIdx.x >> 5); r < n; r += warps) {
         const float* x = data + r * d;
-        int8_t* rec = out + r * qrec;
+        int8_t* rec = out + r * qrec;                                  // plain records
+        int8_t* recA = out + r * qsplit;                               // prefix part
+        int8_t* recB = out + n * uint64_t(qsplit) + r * (qrec - qsplit);  // the rest
         float mx = 0.f;
         for (uint32_t i = lane; i < d; i += 32) mx = fmaxf(mx, fabsf(x[i]));
         for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -102,7 +108,9 @@ __global__ void pack_q8_kernel(const float* __restrict__ data, uint64_t n, uint3
                     a2s += static_cast<double>(av) * static_cast<double>(av);
                 }
             }
-            rec[!split ? i : i < kPre ? 16 + i : qsplit + (i - kPre)] = static_cast<int8_t>(av);
+            if (!split) rec[i] = static_cast<int8_t>(av);
+            else if (i < kPre) recA[16 + i] = static_cast<int8_t>(av);
+            else recB[i - kPre] = static_cast<int8_t>(av);
         }
         for (int o = 16; o > 0; o >>= 1) {
             e2 += __shfl_xor_sync(0xffffffffu, e2, o);
@@ -123,13 +131,13 @@ __global__ void pack_q8_kernel(const float* __restrict__ data, uint64_t n, uint3
                 *reinterpret_cast<float4*>(rec + qpad) = ok ? make_float4(s, fn2, fA, fR) : make_float4(-1.f, 0.f, 0.f, 0.f);
                 for (uint32_t i = qpad + 16; i < qrec; ++i) rec[i] = 0;
             } else {
-                for (uint32_t i = 16 + kPre; i < qsplit; ++i) rec[i] = 0;
-                const uint32_t m1 = qsplit + (qpad - kPre);  // meta1 after the rest of the row
-                *reinterpret_cast<uint4*>(rec) =
+                for (uint32_t i = 16 + kPre; i < qsplit; ++i) recA[i] = 0;
+                const uint32_t m1 = qpad - kPre;  // meta1 after the rest of the row
+                *reinterpret_cast<uint4*>(recA) =
                     make_uint4(__float_as_uint(fs), static_cast<uint32_t>(a2s), __float_as_uint(fRS), 0u);
-                *reinterpret_cast<uint4*>(rec + m1) =
+                *reinterpret_cast<uint4*>(recB + m1) =
                     make_uint4(static_cast<uint32_t>(a2), __float_as_uint(fR), __float_as_uint(fs), 0u);
-                for (uint32_t i = m1 + 16; i < qrec; ++i) rec[i] = 0;
+                for (uint32_t i = m1 + 16; i < qrec - qsplit; ++i) recB[i] = 0;
             }
         }
     }
