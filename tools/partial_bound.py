@@ -12,7 +12,7 @@ cfg = bench_data.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "cfg4"]
 base, qs = bench_data.generate(cfg)
 idx = suco.build_index(base, suco.IndexParams(cfg.num_subspaces, cfg.k_half, cfg.iterations, 42), device=0)
 cp = suco.CollisionParams(cfg.alpha, cfg.beta, cfg.k)
-hs = sorted({16, 48, 96, cfg.d // 4, cfg.d // 2} - {0})
+hs = sorted({4, 8, 12, 16, 48, 96, cfg.d // 4, cfg.d // 2} - {0})
 fr = {h: [] for h in hs}
 for i in range(0, len(qs), len(qs) // 20):
     _, cands, _, _ = idx.query_intermediates(qs[i], cp)
