@@ -82,6 +82,21 @@ def ncu_traffic(workload: str) -> dict:
                 "ncu_ms": v.get("duration_ms")} for k, v in w["kernels"].items()}
 
 
+def gather_ceiling(row_bytes: int):
+    """GB/s of uniformly random gathers of row_bytes-byte rows on this B200 (profiles/r02_gather_peak.json,
+    tools/micro/gather_peak.cu): random row reads cost DRAM per access, so this, not the copy bandwidth,
+    is what a re-rank's gathers can reach without locality. None if no matching measurement."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_gather_peak.json")) as f:
+            runs = json.load(f)["runs"]
+    except (OSError, ValueError, KeyError):
+        return None
+    for r in runs:
+        if r.get("record_bytes") == row_bytes and r.get("read_bytes") == row_bytes:
+            return float(r["GBps"])
+    return None
+
+
 def rerank_row_bytes(base, queries, m=None):
     """Bytes the re-rank reads per candidate row: the u8 copy (d padded to 16) for u8-valued data,
     else the int8 screen record (d padded to 16, + 16 bytes of bound terms, padded to 64; from d = 49
@@ -460,6 +475,12 @@ def main():
                           "achieved_gbs": b / t / 1e9 if b else None, "frac": b / t / 1e9 / peak if b else None,
                           "dram_bytes_ncu": (traffic.get(nm) or {}).get("dram_bytes"),
                           "binding_pipes_ncu": (traffic.get(nm) or {}).get("pipes")}
+        if nm == "rerank" and b:
+            g = gather_ceiling(int(row_bytes))
+            if g:  # the re-rank's own ceiling: random row gathers (cost per DRAM access, not per byte)
+                per_kernel[nm]["random_gather_ceiling"] = {
+                    "gbs": g, "frac": float(row_bytes) * m * sq / t / 1e9 / g,
+                    "source": f"profiles/r02_gather_peak.json: uniformly random {int(row_bytes)}-byte rows"}
         if nm in id_equiv:
             per_kernel[nm]["id_equivalent"] = {"bytes": id_equiv[nm], "gbs": id_equiv[nm] / t / 1e9,
                                                "note": "SURVEY 8(d) bytes (u32 ids / f32 rows), not what moves"}
