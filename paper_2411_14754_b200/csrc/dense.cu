@@ -27,6 +27,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -717,71 +718,78 @@ __device__ __forceinline__ void fused_pieces(const DenseArgs& a, const uint32_t*
 #pragma unroll
         for (uint32_t w = 0; w < W; ++w) need_ge |= gp < cut[w];
         need_ge = __any_sync(kFull, need_ge);
-        for (uint32_t tb = 0; tb < len; tb += 32) {
-            cptr += 32 * NC;
-            // two tiles ahead: the code loads miss L2 often enough that one tile did not cover them
-            const Codes<NC> next = load_codes_at<NC>(a, cptr + 32 * NC, true);
-            uint32_t b[W][NP];
-            csa_planes<W, NC>(mk, b);
-            masks_of<W, NC, MB>(M, code1, mk);  // (past the piece end: the zero slot)
-            code1 = next;
-#pragma unroll
-            for (uint32_t w = 0; w < W; ++w) {
-                // most significant plane first; points past the piece end score 0 < L
-                uint32_t gt = b[w][NP - 1] & ~TL[w][NP - 1], eq = ~(b[w][NP - 1] ^ TL[w][NP - 1]);
-#pragma unroll
-                for (int i = NP - 2; i >= 0; --i) {
-                    gt |= eq & b[w][i] & ~TL[w][i];
-                    eq &= ~(b[w][i] ^ TL[w][i]);
-                }
-                if (!need_ge) {
-                    // Past every tie cut only score > L entries are kept, and they are sparse; their order
-                    // is free (the plan and the compaction keep every one), so no transpose: each point
-                    // (lane) holding some, in turn, broadcasts its query mask and those queries' lanes
-                    // append it.
-                    // Branch-free: every lane runs the warp-uniform loop, the hit lane stores (one
-                    // predicated 2-byte store at its entry count; such pieces never stage).
-                    const uint32_t gl = gt & live[w];  // lane = point, bit j = query 32w + j
-                    uint32_t pending = __ballot_sync(kFull, gl != 0);
-                    while (pending) {
-                        const uint32_t p = __ffs(pending) - 1;
-                        pending &= pending - 1;
-                        const uint32_t hit = (__shfl_sync(kFull, gl, p) >> lane) & 1u;
-                        if (hit && nb[w] < a.B) bp[w][nb[w]] = static_cast<uint16_t>((tb + p) | 0x8000u);
-                        nb[w] += hit;
-                        cnt[w] += hit * 0x10001u;  // #(score >= L) and #(score > L), recorded alike
+        // the tile loop, compiled once for pieces some query of the block still needs ties from
+        // (NEED_GE) and once for pieces past every tie cut
+        auto tile_loop = [&](auto need_ge_c) {
+            constexpr bool NEED_GE = decltype(need_ge_c)::value;
+            for (uint32_t tb = 0; tb < len; tb += 32) {
+                cptr += 32 * NC;
+                // two tiles ahead: the code loads miss L2 often enough that one tile did not cover them
+                const Codes<NC> next = load_codes_at<NC>(a, cptr + 32 * NC, true);
+                uint32_t b[W][NP];
+                csa_planes<W, NC>(mk, b);
+                masks_of<W, NC, MB>(M, code1, mk);  // (past the piece end: the zero slot)
+                code1 = next;
+    #pragma unroll
+                for (uint32_t w = 0; w < W; ++w) {
+                    // most significant plane first; points past the piece end score 0 < L
+                    uint32_t gt = b[w][NP - 1] & ~TL[w][NP - 1], eq = ~(b[w][NP - 1] ^ TL[w][NP - 1]);
+    #pragma unroll
+                    for (int i = NP - 2; i >= 0; --i) {
+                        gt |= eq & b[w][i] & ~TL[w][i];
+                        eq &= ~(b[w][i] ^ TL[w][i]);
                     }
-                    continue;
-                }
-                const uint32_t g1 = xp(gt & live[w]);  // lane = query, bit r = point t0 + r
-                uint32_t bits = g1;
-                {
-                    const uint32_t ge0 = xp((gt | eq) & live[w]);
-                    cnt[w] += __popc(ge0) | (__popc(g1) << 16);
-                    if (gp < cut[w]) bits = ge0;  // before the tie cut: every score >= L
-                }
-                if (bits) {  // id order; the capacity check once per tile while the buffer has room
-                    const bool room = nb[w] + __popc(bits) <= a.B;
-                    do {
-                        const uint32_t r = __ffs(bits) - 1;
-                        bits &= bits - 1;
-                        if (room || nb[w] < a.B) {
-                            const uint32_t v = (tb + r) | (((g1 >> r) & 1u) << 15);
-                            if constexpr (STAGE) {
-                                sw[w] = (sw[w] >> 16) | (static_cast<uint64_t>(v) << 48);
-                                if ((nb[w] & 3u) == 3u) {
-                                    *reinterpret_cast<uint64_t*>(bp[w]) = sw[w];
-                                    bp[w] += 4;
-                                }
-                            } else {
-                                *bp[w]++ = static_cast<uint16_t>(v);
-                            }
+                    if constexpr (!NEED_GE) {
+                        // Past every tie cut only score > L entries are kept, and they are sparse; their order
+                        // is free (the plan and the compaction keep every one), so no transpose: each point
+                        // (lane) holding some, in turn, broadcasts its query mask and those queries' lanes
+                        // append it.
+                        // Branch-free: every lane runs the warp-uniform loop, the hit lane stores (one
+                        // predicated 2-byte store at its entry count; such pieces never stage).
+                        const uint32_t gl = gt & live[w];  // lane = point, bit j = query 32w + j
+                        uint32_t pending = __ballot_sync(kFull, gl != 0);
+                        while (pending) {
+                            const uint32_t p = __ffs(pending) - 1;
+                            pending &= pending - 1;
+                            const uint32_t hit = (__shfl_sync(kFull, gl, p) >> lane) & 1u;
+                            if (hit && nb[w] < a.B) bp[w][nb[w]] = static_cast<uint16_t>((tb + p) | 0x8000u);
+                            nb[w] += hit;
+                            cnt[w] += hit * 0x10001u;  // #(score >= L) and #(score > L), recorded alike
                         }
-                        ++nb[w];
-                    } while (bits);
+                        continue;
+                    }
+                    const uint32_t g1 = xp(gt & live[w]);  // lane = query, bit r = point t0 + r
+                    uint32_t bits = g1;
+                    {
+                        const uint32_t ge0 = xp((gt | eq) & live[w]);
+                        cnt[w] += __popc(ge0) | (__popc(g1) << 16);
+                        if (gp < cut[w]) bits = ge0;  // before the tie cut: every score >= L
+                    }
+                    if (bits) {  // id order; the capacity check once per tile while the buffer has room
+                        const bool room = nb[w] + __popc(bits) <= a.B;
+                        do {
+                            const uint32_t r = __ffs(bits) - 1;
+                            bits &= bits - 1;
+                            if (room || nb[w] < a.B) {
+                                const uint32_t v = (tb + r) | (((g1 >> r) & 1u) << 15);
+                                if constexpr (STAGE) {
+                                    sw[w] = (sw[w] >> 16) | (static_cast<uint64_t>(v) << 48);
+                                    if ((nb[w] & 3u) == 3u) {
+                                        *reinterpret_cast<uint64_t*>(bp[w]) = sw[w];
+                                        bp[w] += 4;
+                                    }
+                                } else {
+                                    *bp[w]++ = static_cast<uint16_t>(v);
+                                }
+                            }
+                            ++nb[w];
+                        } while (bits);
+                    }
                 }
             }
-        }
+        };
+        if (need_ge) tile_loop(std::true_type{});
+        else tile_loop(std::false_type{});
 #pragma unroll
         for (uint32_t w = 0; w < W; ++w) {
             if (32 * w + lane < nqb) {
