@@ -1380,63 +1380,69 @@ __global__ void __launch_bounds__(kDT, 1024 / kDT) dense_fused_h_kernel(DenseArg
         // #(score >= L) is recorded as #(score > L), as in fused_pieces)
         const uint32_t gp = gpiece(a, piece);
         const bool need_ge = __any_sync(kFull, gp < cut);
-        for (uint32_t tb0 = 0; tb0 < len; tb0 += 64) {
-            cptr += 64;
-            const uint4 na = __ldg(cptr + 64), nbv = __ldg(cptr + 96);
-            uint32_t b[4];
-            csa_h(mk, b);
-            masks_h<HG>(M16, ro, ca, cb, mk);
-            ca = na;
-            cb = nbv;
-            uint32_t gt = b[3] & ~T3, eq = ~(b[3] ^ T3);
-            gt |= eq & b[2] & ~T2;
-            eq &= ~(b[2] ^ T2);
-            gt |= eq & b[1] & ~T1;
-            eq &= ~(b[1] ^ T1);
-            gt |= eq & b[0] & ~T0;
-            eq &= ~(b[0] ^ T0);
-            // queries past the block's last have no live bits: their lanes see empty words
-            if (!need_ge) {
-                // past every tie cut: no transpose (fused_pieces); lane p's word holds point t0 + p's
-                // queries in bits 0-15 and point t0 + 32 + p's in bits 16-31, so the A points go
-                // first (id order), each appended by its query's lane of half 0, then the B points by
-                // half 1; both lanes of a query keep its count
-                const uint32_t gl = gt & live;
-                uint32_t pend = __ballot_sync(kFull, gl != 0);
-#pragma unroll
-                for (uint32_t hh = 0; hh < 2; ++hh) {
-                    uint32_t pp = pend;
-                    while (pp) {
-                        const uint32_t p = __ffs(pp) - 1;
-                        pp &= pp - 1;
-                        const uint32_t hit = (__shfl_sync(kFull, gl, p) >> (16 * hh + qj)) & 1u;  // branch-free
-                        const uint32_t own = half == hh ? hit : 0u;
-                        if (own && nb < a.B) buf[cb_off(a, nb)] = static_cast<uint16_t>((tb0 + 32 * hh + p) | 0x8000u);
-                        cnt += own * 0x10001u;
-                        nb += hit;
+        // the tile loop, compiled once per piece kind (some query still needs ties / past every tie cut)
+        auto tile_loop = [&](auto need_ge_c) {
+            constexpr bool NEED_GE = decltype(need_ge_c)::value;
+            for (uint32_t tb0 = 0; tb0 < len; tb0 += 64) {
+                cptr += 64;
+                const uint4 na = __ldg(cptr + 64), nbv = __ldg(cptr + 96);
+                uint32_t b[4];
+                csa_h(mk, b);
+                masks_h<HG>(M16, ro, ca, cb, mk);
+                ca = na;
+                cb = nbv;
+                uint32_t gt = b[3] & ~T3, eq = ~(b[3] ^ T3);
+                gt |= eq & b[2] & ~T2;
+                eq &= ~(b[2] ^ T2);
+                gt |= eq & b[1] & ~T1;
+                eq &= ~(b[1] ^ T1);
+                gt |= eq & b[0] & ~T0;
+                eq &= ~(b[0] ^ T0);
+                // queries past the block's last have no live bits: their lanes see empty words
+                if constexpr (!NEED_GE) {
+                    // past every tie cut: no transpose (fused_pieces); lane p's word holds point t0 + p's
+                    // queries in bits 0-15 and point t0 + 32 + p's in bits 16-31, so the A points go
+                    // first (id order), each appended by its query's lane of half 0, then the B points by
+                    // half 1; both lanes of a query keep its count
+                    const uint32_t gl = gt & live;
+                    uint32_t pend = __ballot_sync(kFull, gl != 0);
+    #pragma unroll
+                    for (uint32_t hh = 0; hh < 2; ++hh) {
+                        uint32_t pp = pend;
+                        while (pp) {
+                            const uint32_t p = __ffs(pp) - 1;
+                            pp &= pp - 1;
+                            const uint32_t hit = (__shfl_sync(kFull, gl, p) >> (16 * hh + qj)) & 1u;  // branch-free
+                            const uint32_t own = half == hh ? hit : 0u;
+                            if (own && nb < a.B) buf[cb_off(a, nb)] = static_cast<uint16_t>((tb0 + 32 * hh + p) | 0x8000u);
+                            cnt += own * 0x10001u;
+                            nb += hit;
+                        }
                     }
+                    continue;
                 }
-                continue;
+                const uint32_t g1 = xp(gt & live);
+                uint32_t kept = g1;
+                {
+                    const uint32_t ge0 = xp((gt | eq) & live);
+                    cnt += __popc(ge0) | (__popc(g1) << 16);
+                    if (gp < cut) kept = ge0;  // before the tie cut: every score >= L
+                }
+                const uint32_t c0 = __popc(kept), o0 = __shfl_xor_sync(kFull, c0, 16);
+                uint32_t at = nb + (half ? o0 : 0u);
+                const uint32_t tb = tb0 + 32 * half;
+                uint32_t bits = kept;
+                while (bits) {  // id order
+                    const uint32_t r = __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    if (at < a.B) buf[cb_off(a, at)] = static_cast<uint16_t>((tb + r) | (((g1 >> r) & 1u) << 15));
+                    ++at;
+                }
+                nb += c0 + o0;
             }
-            const uint32_t g1 = xp(gt & live);
-            uint32_t kept = g1;
-            {
-                const uint32_t ge0 = xp((gt | eq) & live);
-                cnt += __popc(ge0) | (__popc(g1) << 16);
-                if (gp < cut) kept = ge0;  // before the tie cut: every score >= L
-            }
-            const uint32_t c0 = __popc(kept), o0 = __shfl_xor_sync(kFull, c0, 16);
-            uint32_t at = nb + (half ? o0 : 0u);
-            const uint32_t tb = tb0 + 32 * half;
-            uint32_t bits = kept;
-            while (bits) {  // id order
-                const uint32_t r = __ffs(bits) - 1;
-                bits &= bits - 1;
-                if (at < a.B) buf[cb_off(a, at)] = static_cast<uint16_t>((tb + r) | (((g1 >> r) & 1u) << 15));
-                ++at;
-            }
-            nb += c0 + o0;
-        }
+        };
+        if (need_ge) tile_loop(std::true_type{});
+        else tile_loop(std::false_type{});
         cnt += __shfl_xor_sync(kFull, cnt, 16);  // packed 16-bit halves, each <= WP
         if (half == 0 && mine) {
             const uint64_t i = (q0 + qj) * a.P + piece;
