@@ -636,6 +636,8 @@ FbLists stage_select(const suco_gpu_index* x, suco_gpu_query_ctx* c, suco_gpu_qu
             da.clist = sl.dflag.p + 3 * nt + 1;
             da.nclist = sl.dflag.p + 5 * nt + 1;
             da.no_cut = tn.dense_nocut;
+            da.cut_scale = tn.tie_cut_scale;
+            da.cut_pad = tn.tie_cut_pad;
             da.compact_mode = tn.dense_compact;
             da.compact_rows = tn.dense_compact_rows;
             da.hsample = sl.dsample.p;
@@ -672,6 +674,17 @@ FbLists stage_select(const suco_gpu_index* x, suco_gpu_query_ctx* c, suco_gpu_qu
                     if (p < cut[q]) before += v;
                 }
             }
+            double bmax = 0, bsorted = 0;  // mean over 32-query blocks of the block's largest cut: in query order, sorted by cut
+            std::vector<uint32_t> sc(cut);
+            std::sort(sc.begin(), sc.end());
+            for (uint64_t q0 = 0; q0 < nt; q0 += 32) {
+                uint32_t mx = 0;
+                for (uint64_t q = q0; q < std::min<uint64_t>(nt, q0 + 32); ++q) mx = std::max(mx, cut[q]);
+                bmax += mx;
+                bsorted += sc[std::min<uint64_t>(nt, q0 + 32) - 1];
+            }
+            std::fprintf(stderr, "[suco] dense select: mean block-max cut %.1f (query order) vs %.1f (queries sorted by cut)\n",
+                         bmax / ((nt + 31) / 32), bsorted / ((nt + 31) / 32));
             std::fprintf(stderr,
                          "[suco] dense select: %u of %llu queries took the two-pass fallback (pstride %u); superset "
                          "%.0f entries/query (%.0f before the tie cut), %.1f%% of (query, piece) buffers used, mean "

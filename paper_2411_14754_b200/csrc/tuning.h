@@ -29,6 +29,8 @@ struct Tuning {
     bool dense_fused = true;     // SUCO_DENSE_FUSED=0: the two-pass dense select
     bool dense_stage = false;    // SUCO_DENSE_STAGE=1: stage every block's stores (tests)
     uint32_t dense_buf = 0;      // SUCO_DENSE_BUF: single-pass buffer entries per (piece, query); 0 = by memory
+    float tie_cut_scale = 0.f;   // SUCO_TIE_CUT=scale,pad: tie cut = P * need / ties * scale + pad pieces (A/B; 0: 1.25, 8 x 2048 points)
+    uint32_t tie_cut_pad = 0;
     bool dense_nocut = false;    // SUCO_DENSE_NOCUT=1: store every tie (tests)
     uint32_t dense_words = 0;    // SUCO_DENSE_WORDS: mask words per slot (0 auto, 1, 2)
     uint32_t dense_compact = 0;  // SUCO_DENSE_COMPACT: 0 by superset density (default), 1 thread per piece with a

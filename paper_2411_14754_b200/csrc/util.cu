@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -204,6 +205,14 @@ Tuning tuning_from_env() {
     const int b = env_int("SUCO_DENSE_BUF", 0);
     t.dense_buf = b > 0 ? static_cast<uint32_t>(b < 8 ? 8 : b / 8 * 8) : 0u;
     t.dense_nocut = std::getenv("SUCO_DENSE_NOCUT") != nullptr;
+    if (const char* tc = std::getenv("SUCO_TIE_CUT")) {
+        float sc = 0.f;
+        unsigned pad = 0;
+        if (std::sscanf(tc, "%f,%u", &sc, &pad) == 2 && sc >= 1.f && sc <= 4.f) {
+            t.tie_cut_scale = sc;
+            t.tie_cut_pad = pad;
+        }
+    }
     const int w = env_int("SUCO_DENSE_WORDS", 0);
     t.dense_words = (w == 1 || w == 2) ? static_cast<uint32_t>(w) : 0u;
     t.dense_stats = std::getenv("SUCO_DENSE_STATS") != nullptr;
