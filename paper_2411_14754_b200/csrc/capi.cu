@@ -683,7 +683,7 @@ FbLists stage_select(const suco_gpu_index* x, suco_gpu_query_ctx* c, suco_gpu_qu
                 bmax += mx;
                 bsorted += sc[std::min<uint64_t>(nt, q0 + 32) - 1];
             }
-            std::fprintf(stderr, "[suco] dense select: mean block-max cut %.1f (query order) vs %.1f (queries sorted by cut)\n",
+            std::fprintf(stderr, "[suco] dense cuts: mean block-max cut %.1f (query order) vs %.1f (queries sorted by cut)\n",
                          bmax / ((nt + 31) / 32), bsorted / ((nt + 31) / 32));
             std::fprintf(stderr,
                          "[suco] dense select: %u of %llu queries took the two-pass fallback (pstride %u); superset "
