@@ -753,8 +753,7 @@ __device__ __forceinline__ void fused_pieces(const DenseArgs& a, const uint32_t*
                             pending &= pending - 1;
                             const uint32_t hit = (__shfl_sync(kFull, gl, p) >> lane) & 1u;
                             if (hit && nb[w] < a.B) bp[w][nb[w]] = static_cast<uint16_t>((tb + p) | 0x8000u);
-                            nb[w] += hit;
-                            cnt[w] += hit * 0x10001u;  // #(score >= L) and #(score > L), recorded alike
+                            nb[w] += hit;  // (#(score >= L) and #(score > L) are recorded alike: nb, after the loop)
                         }
                         continue;
                     }
@@ -788,8 +787,13 @@ __device__ __forceinline__ void fused_pieces(const DenseArgs& a, const uint32_t*
                 }
             }
         };
-        if (need_ge) tile_loop(std::true_type{});
-        else tile_loop(std::false_type{});
+        if (need_ge) {
+            tile_loop(std::true_type{});
+        } else {
+            tile_loop(std::false_type{});
+#pragma unroll
+            for (uint32_t w = 0; w < W; ++w) cnt[w] = nb[w] * 0x10001u;  // every entry is a score > L point
+        }
 #pragma unroll
         for (uint32_t w = 0; w < W; ++w) {
             if (32 * w + lane < nqb) {
