@@ -764,7 +764,7 @@ cudaError_t launch_traverse(const TraverseArgs& a, cudaStream_t st) {
                     const size_t smem = fx + per_t * T;
                     if (smem > 227 * 1024) break;
                     const uint32_t res = static_cast<uint32_t>((228 * 1024) / (smem + 1024)) * T;
-                    if (res > best_res) {
+                    if (res > best_res || (g && res == best_res && T == best_T)) {
                         best_res = res;
                         best_T = T;
                         fixed = fx;
